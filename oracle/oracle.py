@@ -1,0 +1,421 @@
+"""fp64 CPU ORACLE for the hot path of arXiv 2206.07630 (Thornton & Cuturi).
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and
+``bench.py``'s ``cpu_baseline`` / ``--impl reference`` legs may import this
+module.  It shares no code with the CUDA path (``paper_2206_07630_b200``), and
+the CUDA path never imports it.
+
+Two layers:
+  * ``sk_oracle.c`` (plain C, fp64, OpenMP over independent rows/columns only):
+    cost by direct differences, soft-min, Sinkhorn (Alg. 1), the explicit
+    marginal error (threshold appendix) and Eq. (2), sorting, DualSort (Alg. 2)
+    and the Subsample extrapolation (Eq. 8).
+  * this file (numpy fp64): the d x d linear algebra of the Gaussian (Sec. 3.2,
+    Gaussian-Potential appendix) and GMM (Sec. 3.3) initializers, with matrix
+    square roots by symmetric eigendecomposition (``numpy.linalg.eigh``), a
+    library primitive used as one step.
+
+Inputs are the fp32 arrays of ``workloads.gen`` promoted exactly to fp64.
+Readings of the paper used here are DESIGN.md R-1..R-20.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from typing import Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "sk_oracle.c")
+_LIB_PATH = os.path.join(_HERE, "libsk_oracle.so")
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile sk_oracle.c with gcc (-O2 -fopenmp).  Building the checker is not using it."""
+    if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(_SRC):
+        tmp = _LIB_PATH + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-fPIC", "-shared", "-std=c11",
+                               "-fno-fast-math", _SRC, "-o", tmp, "-lm"])
+        os.replace(tmp, _LIB_PATH)
+    return _LIB_PATH
+
+
+def _L():
+    global _lib
+    if _lib is None:
+        build()
+        lib = ctypes.CDLL(_LIB_PATH)
+        D, I64, I = ctypes.c_double, ctypes.c_int64, ctypes.c_int
+        P = ctypes.c_void_p
+        lib.ora_softmin.restype = D
+        lib.ora_softmin.argtypes = [I64, P, D]
+        lib.ora_sinkhorn_points.restype = I
+        lib.ora_sinkhorn_points.argtypes = [I64, I64, I, P, P, P, P, D, D, I, I, P, P, P, P, P, P, P]
+        lib.ora_sinkhorn_matrix.restype = I
+        lib.ora_sinkhorn_matrix.argtypes = [I64, I64, P, P, P, D, D, I, I, P, P, P, P, P, P, P]
+        lib.ora_f_update_points.argtypes = [I64, I64, I, P, P, P, P, D, P, P, I64]
+        lib.ora_g_update_points.argtypes = [I64, I64, I, P, P, P, P, D, P, P, I64]
+        for nm in ("ora_marginal_error_points", "ora_dual_objective_points"):
+            getattr(lib, nm).restype = D
+            getattr(lib, nm).argtypes = [I64, I64, I, P, P, P, P, P, P, D]
+        for nm in ("ora_marginal_error_matrix", "ora_dual_objective_matrix"):
+            getattr(lib, nm).restype = D
+            getattr(lib, nm).argtypes = [I64, I64, P, P, P, P, P, D]
+        lib.ora_plan_row_sums.argtypes = [I64, I64, I, P, P, P, P, D, P, I64, P]
+        lib.ora_plan_col_sums.argtypes = [I64, I64, I, P, P, P, P, D, P, I64, P]
+        lib.ora_subsample_extrapolate.argtypes = [I64, I64, I, P, P, P, D, P, P, I64]
+        lib.ora_sort_rank.restype = I
+        lib.ora_sort_rank.argtypes = [I64, I64, P, P, P]
+        lib.ora_dualsort.restype = I
+        lib.ora_dualsort.argtypes = [I64, P, P, I, P]
+        lib.ora_cost_matrix.argtypes = [I64, I64, I, P, P, P]
+        lib.ora_num_threads.restype = I
+        lib.ora_set_num_threads.argtypes = [I]
+        _lib = lib
+    return _lib
+
+
+def _d(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+
+
+def _p(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _pts(x) -> np.ndarray:
+    x = _d(x)
+    return x.reshape(x.shape[0], -1) if x.ndim != 1 else x.reshape(-1, 1)
+
+
+def _weights(w, n) -> np.ndarray:
+    return np.full(n, 1.0 / n) if w is None else _d(w)
+
+
+def num_threads() -> int:
+    return _L().ora_num_threads()
+
+
+def set_num_threads(t: int) -> None:
+    _L().ora_set_num_threads(int(t))
+
+
+# ---------------------------------------------------------------- basics ---
+def cost_matrix(x, y) -> np.ndarray:
+    """C_ij = sum_k (x_ik - y_jk)^2 by direct differences."""
+    x, y = _pts(x), _pts(y)
+    C = np.empty((x.shape[0], y.shape[0]))
+    _L().ora_cost_matrix(x.shape[0], y.shape[0], x.shape[1], _p(x), _p(y), _p(C))
+    return C
+
+
+def softmin(S_row, eps: float) -> float:
+    """min_eps of one row."""
+    S = _d(S_row).ravel()
+    return _L().ora_softmin(S.size, _p(S), float(eps))
+
+
+class Result(dict):
+    __getattr__ = dict.__getitem__
+
+
+def sinkhorn(x, y, eps, a=None, b=None, tol=1e-3, max_iter=10000, check_every=1,
+             f0=None, trace=False) -> Result:
+    """Alg. 1 (omega=1), g-then-f, explicit stopping rule; tol<=0 = exactly max_iter sweeps."""
+    x, y = _pts(x), _pts(y)
+    n, m, d = x.shape[0], y.shape[0], x.shape[1]
+    a, b = _weights(a, n), _weights(b, m)
+    f, g = np.empty(n), np.empty(m)
+    it, err, E = ctypes.c_int(), ctypes.c_double(), ctypes.c_double()
+    f0a = None if f0 is None else _d(f0)
+    tr = np.empty(max_iter) if trace else None
+    conv = _L().ora_sinkhorn_points(n, m, d, _p(x), _p(y), _p(a), _p(b), float(eps), float(tol),
+                                    int(max_iter), int(check_every), _p(f0a), _p(f), _p(g),
+                                    ctypes.byref(it), ctypes.byref(err), ctypes.byref(E), _p(tr))
+    r = Result(f=f, g=g, iterations=it.value, converged=bool(conv), err=err.value, E=E.value)
+    if trace:
+        r["trace"] = tr[: it.value]
+    return r
+
+
+def sinkhorn_matrix(C, eps, a=None, b=None, tol=1e-3, max_iter=10000, check_every=1,
+                    f0=None, trace=False) -> Result:
+    C = _d(C)
+    n, m = C.shape
+    a, b = _weights(a, n), _weights(b, m)
+    f, g = np.empty(n), np.empty(m)
+    it, err, E = ctypes.c_int(), ctypes.c_double(), ctypes.c_double()
+    f0a = None if f0 is None else _d(f0)
+    tr = np.empty(max_iter) if trace else None
+    conv = _L().ora_sinkhorn_matrix(n, m, _p(C), _p(a), _p(b), float(eps), float(tol),
+                                    int(max_iter), int(check_every), _p(f0a), _p(f), _p(g),
+                                    ctypes.byref(it), ctypes.byref(err), ctypes.byref(E), _p(tr))
+    r = Result(f=f, g=g, iterations=it.value, converged=bool(conv), err=err.value, E=E.value)
+    if trace:
+        r["trace"] = tr[: it.value]
+    return r
+
+
+def f_update(x, y, g, eps, a=None, rows=None) -> np.ndarray:
+    """f_i = eps log a_i - eps LSE_j((g_j - C_ij)/eps) for the given rows (all if None)."""
+    x, y, g = _pts(x), _pts(y), _d(g)
+    n, m, d = x.shape[0], y.shape[0], x.shape[1]
+    a = _weights(a, n)
+    r = None if rows is None else np.ascontiguousarray(rows, dtype=np.int64)
+    out = np.empty(n if r is None else r.size)
+    _L().ora_f_update_points(n, m, d, _p(x), _p(y), _p(a), _p(g), float(eps), _p(out), _p(r),
+                             0 if r is None else r.size)
+    return out
+
+
+def g_update(x, y, f, eps, b=None, cols=None) -> np.ndarray:
+    """g_j = eps log b_j - eps LSE_i((f_i - C_ij)/eps) for the given columns (all if None)."""
+    x, y, f = _pts(x), _pts(y), _d(f)
+    n, m, d = x.shape[0], y.shape[0], x.shape[1]
+    b = _weights(b, m)
+    c = None if cols is None else np.ascontiguousarray(cols, dtype=np.int64)
+    out = np.empty(m if c is None else c.size)
+    _L().ora_g_update_points(n, m, d, _p(x), _p(y), _p(b), _p(f), float(eps), _p(out), _p(c),
+                             0 if c is None else c.size)
+    return out
+
+
+def marginal_error(x, y, f, g, eps, a=None, b=None) -> float:
+    x, y = _pts(x), _pts(y)
+    n, m, d = x.shape[0], y.shape[0], x.shape[1]
+    return _L().ora_marginal_error_points(n, m, d, _p(x), _p(y), _p(_weights(a, n)),
+                                          _p(_weights(b, m)), _p(_d(f)), _p(_d(g)), float(eps))
+
+
+def dual_objective(x, y, f, g, eps, a=None, b=None) -> float:
+    x, y = _pts(x), _pts(y)
+    n, m, d = x.shape[0], y.shape[0], x.shape[1]
+    return _L().ora_dual_objective_points(n, m, d, _p(x), _p(y), _p(_weights(a, n)),
+                                          _p(_weights(b, m)), _p(_d(f)), _p(_d(g)), float(eps))
+
+
+def marginal_error_matrix(C, f, g, eps, a=None, b=None) -> float:
+    C = _d(C)
+    n, m = C.shape
+    return _L().ora_marginal_error_matrix(n, m, _p(C), _p(_weights(a, n)), _p(_weights(b, m)),
+                                          _p(_d(f)), _p(_d(g)), float(eps))
+
+
+def dual_objective_matrix(C, f, g, eps, a=None, b=None) -> float:
+    C = _d(C)
+    n, m = C.shape
+    return _L().ora_dual_objective_matrix(n, m, _p(C), _p(_weights(a, n)), _p(_weights(b, m)),
+                                          _p(_d(f)), _p(_d(g)), float(eps))
+
+
+def plan_row_sums(x, y, f, g, eps, rows) -> np.ndarray:
+    x, y = _pts(x), _pts(y)
+    r = np.ascontiguousarray(rows, dtype=np.int64)
+    out = np.empty(r.size)
+    _L().ora_plan_row_sums(x.shape[0], y.shape[0], x.shape[1], _p(x), _p(y), _p(_d(f)),
+                           _p(_d(g)), float(eps), _p(r), r.size, _p(out))
+    return out
+
+
+def plan_col_sums(x, y, f, g, eps, cols) -> np.ndarray:
+    x, y = _pts(x), _pts(y)
+    c = np.ascontiguousarray(cols, dtype=np.int64)
+    out = np.empty(c.size)
+    _L().ora_plan_col_sums(x.shape[0], y.shape[0], x.shape[1], _p(x), _p(y), _p(_d(f)),
+                           _p(_d(g)), float(eps), _p(c), c.size, _p(out))
+    return out
+
+
+def center(f, g=None):
+    """Appendix A: potentials are unique up to (f - s, g + s); compare after centering."""
+    s = float(np.mean(f))
+    return (np.asarray(f) - s) if g is None else (np.asarray(f) - s, np.asarray(g) + s)
+
+
+# ------------------------------------------------------------- 1D / sort ---
+def sort_rank(x):
+    """Stable ascending sort of each row of x (B, n) (ties by index): perm, rank (int32)."""
+    x = np.ascontiguousarray(np.asarray(x, dtype=np.float32))
+    x2 = x.reshape(-1, x.shape[-1]) if x.ndim > 1 else x.reshape(1, -1)
+    B, n = x2.shape
+    perm = np.empty((B, n), np.int32)
+    rank = np.empty((B, n), np.int32)
+    if _L().ora_sort_rank(B, n, _p(x2), _p(perm), _p(rank)) != 0:
+        raise ValueError("NaN in sort input")
+    return perm.reshape(x.shape), rank.reshape(x.shape)
+
+
+def dualsort(xs_sorted, ys_sorted, sweeps: int = 0):
+    """Alg. 2 (Jacobi) on sorted supports; sweeps=0 -> fixed point.  Returns (f, sweeps_done)."""
+    xs, ys = _d(xs_sorted).ravel(), _d(ys_sorted).ravel()
+    f = np.empty(xs.size)
+    s = _L().ora_dualsort(xs.size, _p(xs), _p(ys), int(sweeps), _p(f))
+    return f, s
+
+
+def init_sort1d(x, y, sweeps: int = 0) -> np.ndarray:
+    """Sec. 3.1 DualSort initializer for n = m, uniform weights, cost (x - y)^2:
+    sort x (sigma) and y (rho), DualSort on the sorted cost, f0_{sigma(k)} = f_k."""
+    x = np.asarray(x, np.float32).ravel()
+    y = np.asarray(y, np.float32).ravel()
+    if x.size != y.size:
+        raise ValueError("sort1d initializer needs n == m (identity matching)")
+    px, _ = sort_rank(x)
+    py, _ = sort_rank(y)
+    fs, _ = dualsort(x[px].astype(np.float64), y[py].astype(np.float64), sweeps)
+    f0 = np.empty(x.size)
+    f0[px] = fs
+    return f0
+
+
+# ------------------------------------------------------------- Gaussian ---
+def _sym_fn(M, fn):
+    """Symmetric matrix function by eigendecomposition (library eigh as one step)."""
+    M = 0.5 * (M + M.T)
+    w, V = np.linalg.eigh(M)
+    return (V * fn(w)) @ V.T
+
+
+def sqrtm(M):
+    return _sym_fn(M, np.sqrt)
+
+
+def inv_sqrtm(M):
+    return _sym_fn(M, lambda w: 1.0 / np.sqrt(w))
+
+
+def moments(x, w=None, ridge_rel: float = 1e-6):
+    """Weighted mean m = sum_i w_i x_i and biased covariance
+    sum_i w_i (x_i - m)(x_i - m)^T + ridge_rel * tr/d * I   (reading R-11)."""
+    x = _pts(x)
+    n, d = x.shape
+    w = _weights(w, n)
+    m = (w[:, None] * x).sum(0)
+    xc = x - m
+    S = (w[:, None] * xc).T @ xc
+    S = S + ridge_rel * np.trace(S) / d * np.eye(d)
+    return m, S
+
+
+def monge_A(S1, S2):
+    """A = S1^{-1/2} (S1^{1/2} S2 S1^{1/2})^{1/2} S1^{-1/2}, symmetrised."""
+    r = sqrtm(S1)
+    ri = inv_sqrtm(S1)
+    A = ri @ sqrtm(r @ S2 @ r) @ ri
+    return 0.5 * (A + A.T)
+
+
+def gaussian_potential(xe, m_mu, m_nu, A):
+    """f*(x) = ||x||^2 - (x - m_mu)^T A (x - m_mu) - 2 m_nu^T x  (Gaussian-Potential appendix,
+    P:613-615, cost ||x-y||^2; reading R-4)."""
+    xe = _pts(xe)
+    xc = xe - m_mu
+    return (xe * xe).sum(1) - np.einsum("ij,jk,ik->i", xc, A, xc) - 2.0 * xe @ m_nu
+
+
+def bures2(S1, S2):
+    """B^2(S1,S2) = tr(S1 + S2 - 2 (S1^{1/2} S2 S1^{1/2})^{1/2})  (Eq. 6)."""
+    r = sqrtm(S1)
+    return float(np.trace(S1) + np.trace(S2) - 2.0 * np.trace(sqrtm(r @ S2 @ r)))
+
+
+def w2_gaussians(m1, S1, m2, S2):
+    """W_2^2 between Gaussians, Eq. (6)."""
+    return float(np.sum((np.asarray(m1) - np.asarray(m2)) ** 2)) + bures2(S1, S2)
+
+
+def init_gaussian(x, y, a=None, b=None, ridge_rel: float = 1e-6):
+    """Gaus initializer (Sec. 3.2): moments, A, evaluate the quadratic potential on
+    the smaller side (n <= m -> on x, side 0; else on y, side 1, reading R-15)."""
+    x, y = _pts(x), _pts(y)
+    m_mu, S_mu = moments(x, a, ridge_rel)
+    m_nu, S_nu = moments(y, b, ridge_rel)
+    if x.shape[0] <= y.shape[0]:
+        return gaussian_potential(x, m_mu, m_nu, monge_A(S_mu, S_nu)), 0
+    return gaussian_potential(y, m_nu, m_mu, monge_A(S_nu, S_mu)), 1
+
+
+# ------------------------------------------------------------------ GMM ---
+def gmm_log_resp(x, weights, means, covs):
+    """log p_k(x) of Eq. (7): log alpha_k + log N(x; m_k, S_k), normalised by LSE over k
+    (the (2 pi)^{-d/2} factor cancels).  Cholesky S_k = L L^T (library step)."""
+    x = _pts(x)
+    K = len(weights)
+    lp = np.empty((x.shape[0], K))
+    for k in range(K):
+        L = np.linalg.cholesky(_d(covs[k]))
+        z = np.linalg.solve(L, (x - _d(means[k])).T)
+        lp[:, k] = np.log(float(weights[k])) - 0.5 * (z * z).sum(0) - np.log(np.diag(L)).sum()
+    mx = lp.max(1, keepdims=True)
+    return lp - (mx + np.log(np.exp(lp - mx).sum(1, keepdims=True)))
+
+
+def gmm_cost(mx, cx, my, cy):
+    """C~_kl = ||m_k - m'_l||^2 + B^2(S_k, S'_l)  (Eq. 6)."""
+    K, L = len(mx), len(my)
+    C = np.empty((K, L))
+    for k in range(K):
+        for l in range(L):
+            C[k, l] = w2_gaussians(_d(mx[k]), _d(cx[k]), _d(my[l]), _d(cy[l]))
+    return C
+
+
+def init_gmm(x, y, gx: dict, gy: dict, eps, inner_tol=1e-9, inner_max_iter=100000):
+    """GMM initializer (Sec. 3.3): K x K Bures-cost Sinkhorn at the same eps
+    (reading R-13) -> f~; f0_i = sum_k f~_k p_k(x_i) on the smaller side."""
+    x, y = _pts(x), _pts(y)
+    if x.shape[0] > y.shape[0]:
+        f, _ = init_gmm(y, x, gy, gx, eps, inner_tol, inner_max_iter)
+        return f, 1
+    C = gmm_cost(gx["means"], gx["covs"], gy["means"], gy["covs"])
+    r = sinkhorn_matrix(C, eps, a=_d(gx["weights"]), b=_d(gy["weights"]), tol=inner_tol,
+                        max_iter=inner_max_iter)
+    P = np.exp(gmm_log_resp(x, gx["weights"], gx["means"], gx["covs"]))
+    return P @ r.f, 0
+
+
+# ------------------------------------------------------------- Subsample ---
+def subsample_extrapolate(x, z, gb, eps, rows=None) -> np.ndarray:
+    """Eq. (8): f0_i = -eps log (1/ms) sum_j exp((gb_j - c(x_i, z_j))/eps)."""
+    x, z, gb = _pts(x), _pts(z), _d(gb)
+    r = None if rows is None else np.ascontiguousarray(rows, dtype=np.int64)
+    out = np.empty(x.shape[0] if r is None else r.size)
+    _L().ora_subsample_extrapolate(x.shape[0], z.shape[0], x.shape[1], _p(x), _p(z), _p(gb),
+                                   float(eps), _p(out), _p(r), 0 if r is None else r.size)
+    return out
+
+
+def init_subsample(x, y, idx_x, idx_y, eps, inner_tol, inner_max_iter=10000, rows=None):
+    """Subsample initializer (Sec. 3.4): inner Sinkhorn on the uniform subsamples
+    w = x[idx_x], z = y[idx_y] at the same eps (reading R-14), then Eq. (8) from g-breve.
+    Side 0 (f on x) when n <= m."""
+    x, y = _pts(x), _pts(y)
+    if x.shape[0] > y.shape[0]:
+        f, _, inner = init_subsample(y, x, idx_y, idx_x, eps, inner_tol, inner_max_iter, rows)
+        return f, 1, inner
+    w, z = x[np.asarray(idx_x)], y[np.asarray(idx_y)]
+    inner = sinkhorn(w, z, eps, tol=inner_tol, max_iter=inner_max_iter)
+    return subsample_extrapolate(x, z, inner.g, eps, rows), 0, inner
+
+
+# ----------------------------------------------------------- sharded (O9) ---
+def column_partials(x_rows, y, f_rows, eps):
+    """Per-shard column partials of the g-pass:
+    (M_j, S_j) with M_j = max_i (f_i - C_ij)/eps and S_j = sum_i exp((f_i - C_ij)/eps - M_j)
+    over the shard's rows.  Plain fp64 loops over the cost matrix of the shard."""
+    C = cost_matrix(x_rows, y)
+    V = (_d(f_rows)[:, None] - C) / eps
+    M = V.max(0)
+    return M, np.exp(V - M).sum(0)
+
+
+def merge_partials(parts, b, eps):
+    """Stable LSE merge of shard partials in rank order -> g_j = eps log b_j - eps LSE."""
+    M = np.max([p[0] for p in parts], axis=0)
+    S = np.zeros_like(M)
+    for Mp, Sp in parts:
+        S = S + Sp * np.exp(Mp - M)
+    return eps * np.log(_d(b)) - eps * (M + np.log(S))

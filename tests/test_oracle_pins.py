@@ -1,0 +1,397 @@
+"""Pins for the fp64 oracle (-m "not gpu"): closed forms, invariants, brute force and
+independent library routines — never a retyped copy of the oracle's own formula.
+
+Each test names the passage (PAPER.md line, "P:n") or DESIGN.md reading it checks.
+"""
+import itertools
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "analytic_cases.json")))
+
+
+def rand_cloud(rng, n, d, shift=0.0):
+    return (rng.standard_normal((n, d)) + shift).astype(np.float32)
+
+
+# ------------------------------------------------------------------ cost / soft-min
+def test_cost_analytic_and_invariants(O):
+    assert O.cost_matrix([[0.0]], [[3.0]])[0, 0] == 9.0
+    rng = np.random.default_rng(1)
+    x = rand_cloud(rng, 7, 3)
+    C = O.cost_matrix(x, x)
+    assert np.all(np.diag(C) == 0) and np.array_equal(C, C.T)
+    t = np.array([0.5, -2.0, 1.25], np.float32)
+    y = rand_cloud(rng, 5, 3)
+    assert np.allclose(O.cost_matrix(x + t, y + t), O.cost_matrix(x, y), atol=1e-9)
+
+
+def test_softmin_closed_form_and_limits(O):
+    g = GOLD["softmin_two_zeros"]
+    assert abs(O.softmin(g["S"], g["eps"]) - g["value"]) < 1e-15
+    rng = np.random.default_rng(2)
+    S = rng.uniform(0, 3, 9)
+    # eps -> 0 gives the hard minimum (P:49 limit)
+    assert abs(O.softmin(S, 1e-9) - S.min()) < 1e-6
+    # brute-force exactly-rounded summation (math.fsum) without max shift
+    eps = 0.7
+    ref = -eps * math.log(math.fsum(math.exp(-s / eps) for s in S))
+    assert abs(O.softmin(S, eps) - ref) < 1e-12
+    # max shift: no overflow for huge costs
+    assert np.isfinite(O.softmin(S + 1e5, 1e-3))
+
+
+# ------------------------------------------------------------------ Sinkhorn + Eq. (2)
+def test_single_atom_forced_coupling(O):
+    g = GOLD["single_atom"]
+    r = O.sinkhorn(g["x"], g["y"], g["eps"], tol=1e-12, max_iter=5)
+    assert r.iterations == 1 and r.converged
+    assert abs(r.f[0] + r.g[0] - g["f_plus_g"]) < 1e-12
+    assert abs(r.E - g["E"]) < 1e-12
+
+
+def test_zero_potentials_objective(O):
+    E = O.dual_objective([[0.0]], [[0.0]], [0.0], [0.0], 1.0)
+    assert E == GOLD["zero_potentials_zero_cost"]["E"]
+
+
+def test_symmetric_two_point_problem(O):
+    # C = [[0,1],[1,0]], eps=1 (SPEC-style symmetry case): marginals (1/2,1/2), f ~ g
+    x = y = np.array([[0.0], [1.0]], np.float32)
+    r = O.sinkhorn(x, y, 1.0, tol=1e-13, max_iter=1000)
+    C = O.cost_matrix(x, y)
+    P = np.exp((r.f[:, None] + r.g[None, :] - C) / 1.0)
+    assert np.allclose(P.sum(1), 0.5, atol=1e-12) and np.allclose(P.sum(0), 0.5, atol=1e-12)
+    fc, gc = r.f - r.f.mean(), r.g - r.g.mean()
+    assert np.allclose(fc, gc, atol=1e-12)
+
+
+def test_dual_ascent_monotone_and_identity(O):
+    # Each half-update is an exact block maximisation of Eq. (2): E nondecreasing.
+    rng = np.random.default_rng(3)
+    x, y = rand_cloud(rng, 16, 2), rand_cloud(rng, 19, 2, 0.5)
+    a = rng.uniform(0.5, 1.5, 16); a /= a.sum()
+    b = rng.uniform(0.5, 1.5, 19); b /= b.sum()
+    r = O.sinkhorn(x, y, 0.1, a=a, b=b, tol=0, max_iter=60, trace=True)
+    assert np.all(np.diff(r.trace) >= -1e-12)
+    # After an f-update the row sums of P equal a exactly, so E = <f,a> + <g,b> - eps sum(a)
+    assert abs(r.E - (r.f @ a + r.g @ b - 0.1 * a.sum())) < 1e-12
+
+
+def test_shift_invariance_and_weak_strong_duality(O):
+    rng = np.random.default_rng(4)
+    n, m, eps = 8, 8, 0.1
+    x, y = rand_cloud(rng, n, 2), rand_cloud(rng, m, 2, 0.3)
+    a, b = np.full(n, 1 / n), np.full(m, 1 / m)
+    C = O.cost_matrix(x, y)
+    f, g = rng.standard_normal(n), rng.standard_normal(m)
+    # shift invariance (BJ.ns)
+    E0 = O.dual_objective(x, y, f, g, eps)
+    assert abs(O.dual_objective(x, y, f + 0.37, g - 0.37, eps) - E0) < 1e-14 * abs(E0)
+
+    def primal(P):  # Eq. (1) with the + entropy sign (reading R-3)
+        return float((P * C).sum() + eps * (P * (np.log(P) - 1)).sum())
+
+    # weak duality: any (f,g) is below the primal value of any feasible P (here a b^T)
+    for _ in range(20):
+        f, g = rng.standard_normal(n), rng.standard_normal(m)
+        assert O.dual_objective(x, y, f, g, eps) <= primal(np.outer(a, b)) + 1e-12
+    # strong duality at convergence: E* = primal(P*)
+    eps = 1.0
+    r = O.sinkhorn(x, y, eps, tol=1e-13, max_iter=100000)
+    assert r.converged
+    P = np.exp((r.f[:, None] + r.g[None, :] - C) / eps)
+    assert abs(r.E - primal(P)) < 1e-9
+    # the printed "-eps" sign of Eq. (1) does NOT give strong duality (why R-3 is needed)
+    assert abs(r.E - float((P * C).sum() - eps * (P * (np.log(P) - 1)).sum())) > 1e-3
+
+
+def test_converged_plan_meets_both_marginals_independently(O):
+    rng = np.random.default_rng(5)
+    x, y = rand_cloud(rng, 30, 3), rand_cloud(rng, 25, 3, 1.0)
+    eps = 0.05 * float(O.cost_matrix(x, y).mean())
+    r = O.sinkhorn(x, y, eps, tol=1e-3)
+    assert r.converged
+    C = ((x[:, None, :].astype(np.float64) - y[None, :, :]) ** 2).sum(-1)
+    P = np.exp((r.f[:, None] + r.g[None, :] - C) / eps)
+    err = np.abs(P.sum(1) - 1 / 30).sum() + np.abs(P.sum(0) - 1 / 25).sum()
+    assert err < 1e-3 and abs(err - r.err) < 1e-12
+
+
+def test_warm_start_from_solution(O):
+    rng = np.random.default_rng(6)
+    x, y = rand_cloud(rng, 20, 2), rand_cloud(rng, 20, 2, 0.5)
+    r = O.sinkhorn(x, y, 0.2, tol=1e-10, max_iter=100000)
+    r2 = O.sinkhorn(x, y, 0.2, tol=1e-9, f0=r.f)
+    assert r2.iterations == 1
+
+
+def test_fused_error_identity(O):
+    # err_l from the next g-update: sum_j b_j |expm1((g^l - g^{l+1})/eps)| (H5)
+    rng = np.random.default_rng(7)
+    x, y = rand_cloud(rng, 24, 2), rand_cloud(rng, 17, 2, 0.4)
+    eps = 0.3
+    r = O.sinkhorn(x, y, eps, tol=0, max_iter=7)
+    g_next = O.g_update(x, y, r.f, eps)
+    fused = float((np.full(17, 1 / 17) * np.abs(np.expm1((r.g - g_next) / eps))).sum())
+    assert abs(fused - r.err) < 1e-13
+
+
+def test_sampled_updates_match_full(O):
+    rng = np.random.default_rng(8)
+    x, y = rand_cloud(rng, 40, 3), rand_cloud(rng, 33, 3)
+    g = rng.standard_normal(33)
+    full = O.f_update(x, y, g, 0.4)
+    rows = np.array([0, 5, 39, 17])
+    assert np.array_equal(O.f_update(x, y, g, 0.4, rows=rows), full[rows])
+    # one f-update makes the row marginals exact
+    rs = O.plan_row_sums(x, y, full, g, 0.4, np.arange(40))
+    assert np.allclose(rs, 1 / 40, rtol=1e-12)
+
+
+# ------------------------------------------------------------------ 1D: sort, eps->0
+def test_sort_rank_stable_ties(O):
+    x = np.array([[0.5, -0.0, 0.1, 0.0, 0.5, -1.0]], np.float32)
+    perm, rank = O.sort_rank(x)
+    assert perm.tolist() == [[5, 1, 3, 2, 0, 4]]   # -0.0 == +0.0 -> index order
+    assert np.array_equal(rank[0][perm[0]], np.arange(6))
+    rng = np.random.default_rng(9)
+    xb = rng.integers(0, 50, (64, 200)).astype(np.float32)  # heavy ties
+    perm, rank = O.sort_rank(xb)
+    assert np.array_equal(perm, np.argsort(xb, axis=1, kind="stable"))
+    with pytest.raises(ValueError):
+        O.sort_rank(np.array([1.0, np.nan], np.float32))
+
+
+def brute_assignment(C):
+    n = C.shape[0]
+    return min(sum(C[i, p[i]] for i in range(n)) for p in itertools.permutations(range(n))) / n
+
+
+@pytest.mark.parametrize("n", [2, 3, 4, 5, 6])
+def test_1d_eps0_limit_sorted_matching_is_lp_optimum(O, n):
+    rng = np.random.default_rng(10 + n)
+    for _ in range(5):
+        x, y = rng.normal(size=n).astype(np.float32), rng.normal(size=n).astype(np.float32)
+        C = O.cost_matrix(x.reshape(-1, 1), y.reshape(-1, 1))
+        W_lp = brute_assignment(C)
+        xs, ys = np.sort(x).astype(np.float64), np.sort(y).astype(np.float64)
+        W_sorted = float(np.mean((xs - ys) ** 2))              # P:110 NW solution, n=m uniform
+        assert abs(W_lp - W_sorted) < 1e-12
+        # DualSort fixed point certifies optimality: feasible and tight on the diagonal (A.1-A.2)
+        f, _ = O.dualsort(xs, ys)
+        Cs = (xs[:, None] - ys[None, :]) ** 2
+        g = np.diag(Cs) - f
+        assert np.all(f[:, None] + g[None, :] <= Cs + 1e-12)
+        assert abs((f.mean() + g.mean()) - W_lp) < 1e-12
+        # entropic brackets: W - eps(1+log nm) <= E* <= W - eps(1+log n) (DESIGN.md pin)
+        for eps in (1.0, 0.1, 0.01):
+            r = O.sinkhorn(x.reshape(-1, 1), y.reshape(-1, 1), eps, tol=1e-12, max_iter=200000)
+            assert W_lp - eps * (1 + math.log(n * n)) - 1e-9 <= r.E <= W_lp - eps * (1 + math.log(n)) + 1e-9
+
+
+def test_dualsort_golden_and_paper_mode(O):
+    gd = GOLD["dualsort_swap"]
+    f, s = O.dualsort(gd["xs"], gd["ys"])
+    assert f.tolist() == gd["f"]
+    rng = np.random.default_rng(11)
+    xs, ys = np.sort(rng.random(50)), np.sort(rng.random(50))
+    Cs = (xs[:, None] - ys[None, :]) ** 2
+    f1, s1 = O.dualsort(xs, ys, sweeps=1)
+    assert s1 == 1 and np.allclose(f1, np.min(Cs - np.diag(Cs)[None, :], axis=1), atol=0)
+    f, s = O.dualsort(xs, ys)
+    assert s <= 51
+    # the fixed point is the largest f <= 0 satisfying feasibility (reading R-7):
+    # perturbing any entry upward breaks feasibility or the f <= 0 cap.
+    g = np.diag(Cs) - f
+    slack = Cs - f[:, None] - g[None, :]
+    assert slack.min() > -1e-12
+
+
+def test_init_sort1d_equivariance(O):
+    rng = np.random.default_rng(12)
+    x = rng.random(64).astype(np.float32)
+    y = (np.arange(64) / 63).astype(np.float32)
+    f0 = O.init_sort1d(x, y)
+    p = rng.permutation(64)
+    assert np.allclose(O.init_sort1d(x[p], y)[np.argsort(p)], f0, atol=0)
+
+
+def test_sort1d_init_helps_on_1d(O):
+    # Sec. 3.1 claim on a small instance: the ε=0 dual is a much better start than 0
+    rng = np.random.default_rng(13)
+    x = rng.random(128).astype(np.float32).reshape(-1, 1)
+    y = (np.arange(128) / 127).astype(np.float32).reshape(-1, 1)
+    eps = 1e-3
+    r0 = O.sinkhorn(x, y, eps)
+    r1 = O.sinkhorn(x, y, eps, f0=O.init_sort1d(x, y))
+    assert r1.converged and r1.iterations < r0.iterations / 2
+
+
+# ------------------------------------------------------------------ Gaussian
+def test_bures_and_monge_closed_forms(O):
+    gb = GOLD["bures_4I_I"]
+    assert abs(O.bures2(4 * np.eye(2), np.eye(2)) - gb["value"]) < 1e-12
+    assert np.allclose(O.monge_A(np.eye(3), 4 * np.eye(3)), GOLD["monge_I_4I"]["A_diag"] * np.eye(3))
+    rng = np.random.default_rng(14)
+    G = rng.standard_normal((4, 4)); S = G @ G.T + 0.1 * np.eye(4)
+    assert np.allclose(O.monge_A(S, S), np.eye(4), atol=1e-10)
+    assert abs(O.bures2(S, S)) < 1e-10
+    H = rng.standard_normal((4, 4)); T = H @ H.T + 0.2 * np.eye(4)
+    assert abs(O.bures2(S, T) - O.bures2(T, S)) < 1e-10
+    A = O.monge_A(S, T)
+    assert np.allclose(A, A.T) and np.allclose(A @ S @ A, T, atol=1e-9)       # push-forward
+    # W2^2 via the map, E||x - T(x)||^2 = tr((I-A) S (I-A)) + |dm|^2, equals Eq. (6)
+    m1, m2 = rng.standard_normal(4), rng.standard_normal(4)
+    I = np.eye(4)
+    assert abs(np.trace((I - A) @ S @ (I - A)) + np.sum((m1 - m2) ** 2) - O.w2_gaussians(m1, S, m2, T)) < 1e-9
+
+
+def _sigma_point_mean(q, m, S):
+    """Exact E[q(y)] for quadratic q, y ~ N(m, S): q(m) + 1/2 sum_k [q(m+Le_k)+q(m-Le_k)-2q(m)]."""
+    L = np.linalg.cholesky(S)
+    q0 = q(m)
+    return q0 + 0.5 * sum(q(m + L[:, k]) + q(m - L[:, k]) - 2 * q0 for k in range(len(m)))
+
+
+def test_gaussian_potential_is_optimal_dual(O):
+    """Gaussian-Potential appendix, cost ||x-y||^2: E_mu[f] + E_nu[f^c] = W2^2 (Eq. 6)
+    and T = Id - 1/2 grad f.  This pins the sign of the linear term (reading R-4)."""
+    rng = np.random.default_rng(15)
+    d = 3
+    G = rng.standard_normal((d, d)); S1 = G @ G.T + 0.3 * np.eye(d)
+    H = rng.standard_normal((d, d)); S2 = H @ H.T + 0.3 * np.eye(d)
+    m1, m2 = rng.standard_normal(d), rng.standard_normal(d)
+    A = O.monge_A(S1, S2)
+    f = lambda x: float(O.gaussian_potential(np.asarray(x)[None, :], m1, m2, A)[0])
+    Ai = np.linalg.inv(A)
+
+    def fc(y):  # c-transform, minimiser x* = m1 + A^{-1}(y - m2) (grad of |x-y|^2 - f vanishes)
+        xs = m1 + Ai @ (y - m2)
+        return float(np.sum((xs - y) ** 2)) - f(xs)
+
+    # x* really is the minimiser (finite differences of |x-y|^2 - f(x))
+    yv = rng.standard_normal(d)
+    xs = m1 + Ai @ (yv - m2)
+    obj = lambda x: float(np.sum((x - yv) ** 2)) - f(x)
+    for k in range(d):
+        e = np.zeros(d); e[k] = 1e-5
+        assert abs((obj(xs + e) - obj(xs - e)) / 2e-5) < 1e-6
+    dual = _sigma_point_mean(f, m1, S1) + _sigma_point_mean(fc, m2, S2)
+    assert abs(dual - O.w2_gaussians(m1, S1, m2, S2)) < 1e-9
+    # T(x) = A(x - m1) + m2 = x - 1/2 grad f(x)
+    x0 = rng.standard_normal(d)
+    grad = np.array([(f(x0 + h) - f(x0 - h)) / 2e-6 for h in np.eye(d) * 1e-6])
+    assert np.allclose(x0 - 0.5 * grad, A @ (x0 - m1) + m2, atol=1e-6)
+    # Eq. (5)'s printed linear term (m2 - A m1) with the 1/2-cost convention fails this test
+    f5 = lambda x: 0.5 * x @ (np.eye(d) - A) @ x + (m2 - A @ m1) @ x
+    grad5 = np.array([(f5(x0 + h) - f5(x0 - h)) / 2e-6 for h in np.eye(d) * 1e-6])
+    assert not np.allclose(x0 - grad5, A @ (x0 - m1) + m2, atol=1e-3)
+
+
+def test_gaussian_special_cases(O):
+    rng = np.random.default_rng(16)
+    x = rng.standard_normal((500, 2)).astype(np.float32)
+    # equal moments -> A = I -> f constant (= -|m|^2)
+    f0, side = O.init_gaussian(x, x)
+    assert side == 0 and np.ptp(f0) < 1e-9
+    # m_mu = 0, m_nu = t, S = I -> f = -2 t^T x
+    t = np.array([0.7, -0.2])
+    A = O.monge_A(np.eye(2), np.eye(2))
+    f = O.gaussian_potential(x, np.zeros(2), t, A)
+    assert np.allclose(f, -2 * x.astype(np.float64) @ t, atol=1e-12)
+    # moments: independent numpy weighted covariance
+    w = rng.uniform(0.5, 1.5, 500); w /= w.sum()
+    m, S = O.moments(x, w, ridge_rel=0.0)
+    assert np.allclose(m, np.average(x, axis=0, weights=w))
+    assert np.allclose(S, np.cov(x.T.astype(np.float64), aweights=w, bias=True), atol=1e-12)
+    # side selection: n > m -> potential on y
+    _, side = O.init_gaussian(x, x[:100])
+    assert side == 1
+
+
+# ------------------------------------------------------------------ GMM
+def _mix(rng, K, d):
+    means = rng.normal(0, 2, (K, d))
+    covs = []
+    for _ in range(K):
+        G = rng.standard_normal((d, d)) / np.sqrt(d)
+        covs.append(G.T @ G + 0.05 * np.eye(d))
+    w = rng.uniform(0.5, 1.5, K); w /= w.sum()
+    return {"weights": w, "means": means, "covs": np.array(covs)}
+
+
+def test_gmm_responsibilities_independent(O):
+    from scipy.stats import multivariate_normal
+    rng = np.random.default_rng(17)
+    g = _mix(rng, 4, 3)
+    x = rng.standard_normal((50, 3)) * 2
+    lr = O.gmm_log_resp(x, g["weights"], g["means"], g["covs"])
+    dens = np.stack([g["weights"][k] * multivariate_normal(g["means"][k], g["covs"][k]).pdf(x)
+                     for k in range(4)], 1)
+    assert np.allclose(np.exp(lr), dens / dens.sum(1, keepdims=True), atol=1e-12)
+    assert np.allclose(np.exp(lr).sum(1), 1.0)
+
+
+def test_gmm_cost_and_init_properties(O):
+    rng = np.random.default_rng(18)
+    gx, gy = _mix(rng, 3, 2), _mix(rng, 3, 2)
+    C = O.gmm_cost(gx["means"], gx["covs"], gx["means"], gx["covs"])
+    assert np.allclose(np.diag(C), 0, atol=1e-10)
+    I = np.array([np.eye(2)] * 3)
+    Ci = O.gmm_cost(gx["means"], I, gy["means"], I)
+    assert np.allclose(Ci, ((gx["means"][:, None] - gy["means"][None]) ** 2).sum(-1), atol=1e-12)
+    x = rng.standard_normal((40, 2)).astype(np.float32)
+    y = rng.standard_normal((60, 2)).astype(np.float32)
+    # K = 1 -> responsibilities are 1 -> constant potential
+    g1 = {k: v[:1] for k, v in gx.items()}; g1["weights"] = np.ones(1)
+    h1 = {k: v[:1] for k, v in gy.items()}; h1["weights"] = np.ones(1)
+    f, side = O.init_gmm(x, y, g1, h1, 0.5)
+    assert side == 0 and np.ptp(f) < 1e-12
+    # relabelling invariance
+    f, _ = O.init_gmm(x, y, gx, gy, 0.5)
+    p = [2, 0, 1]
+    gp = {k: v[p] for k, v in gx.items()}
+    fp, _ = O.init_gmm(x, y, gp, gy, 0.5)
+    assert np.allclose(f, fp, atol=1e-9)
+
+
+# ------------------------------------------------------------------ Subsample
+def test_subsample_full_equals_solution(O):
+    rng = np.random.default_rng(19)
+    n = 48
+    x, y = rand_cloud(rng, n, 2), rand_cloud(rng, n, 2, 0.5)
+    eps = 0.2
+    idx = np.arange(n)
+    f0, side, inner = O.init_subsample(x, y, idx, idx, eps, inner_tol=1e-11, inner_max_iter=100000)
+    full = O.sinkhorn(x, y, eps, tol=1e-11, max_iter=100000)
+    assert side == 0 and inner.converged
+    assert np.allclose(O.center(f0), O.center(full.f), atol=1e-9)
+
+
+def test_subsample_degenerate_and_shift(O):
+    rng = np.random.default_rng(20)
+    x, z = rand_cloud(rng, 30, 3), rand_cloud(rng, 1, 3)
+    gb = np.array([0.3])
+    f0 = O.subsample_extrapolate(x, z, gb, 0.05)
+    c = ((x.astype(np.float64) - z.astype(np.float64)) ** 2).sum(1)
+    assert np.allclose(f0, c - 0.3, atol=1e-12)
+    z = rand_cloud(rng, 12, 3)
+    gb = rng.standard_normal(12)
+    assert np.allclose(O.subsample_extrapolate(x, z, gb + 0.9, 0.3),
+                       O.subsample_extrapolate(x, z, gb, 0.3) - 0.9, atol=1e-12)
+
+
+# ------------------------------------------------------------------ sharded decomposition (O9)
+def test_shard_merge_equals_unsharded_g_update(O):
+    rng = np.random.default_rng(21)
+    x, y = rand_cloud(rng, 64, 3), rand_cloud(rng, 40, 3)
+    f = rng.standard_normal(64)
+    eps = 0.25
+    b = np.full(40, 1 / 40)
+    parts = [O.column_partials(x[s], y, f[s], eps) for s in (slice(0, 16), slice(16, 48), slice(48, 64))]
+    assert np.allclose(O.merge_partials(parts, b, eps), O.g_update(x, y, f, eps), atol=1e-12)
