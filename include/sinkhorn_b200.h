@@ -1,0 +1,223 @@
+/*
+ * sinkhorn_b200.h — C ABI of the B200-native (sm_100a) hot path of
+ *   J. Thornton, M. Cuturi, "Rethinking Initialization of the Sinkhorn Algorithm"
+ *   (arXiv 2206.07630).  "P:n" cites PAPER.md line n; "R-k" cites reading k of
+ *   DESIGN.md (where the paper is silent, garbled or inconsistent).
+ *
+ * Problem: discrete measures mu = sum_i a_i delta_{x_i} (n points),
+ * nu = sum_j b_j delta_{y_j} (m points) in R^d, squared-L2 cost
+ * C_ij = ||x_i - y_j||^2, regularisation eps > 0.  The library computes
+ * the dual potentials (f, g) maximising Eq. (2) with the log-domain
+ * Sinkhorn iteration of Alg. 1 (omega = 1; sign reading R-1, g-then-f
+ * order R-2):
+ *     g_j <- eps log b_j - eps LSE_i((f_i - C_ij)/eps)
+ *     f_i <- eps log a_i - eps LSE_j((g_j - C_ij)/eps)
+ * stopping when the L1 marginal error of p_ij = exp((f_i+g_j-C_ij)/eps)
+ * (threshold appendix) drops below tol, checked every check_every
+ * sweeps; plus the paper's initializers f^(0) (Sec. 3).
+ *
+ * CONVENTIONS (every entry point)
+ *  - Arrays are row-major fp32 (points: [n][d]) or int32 (indices).  Unless an
+ *    entry says otherwise, an array pointer may be DEVICE memory (e.g. a torch
+ *    CUDA tensor's data_ptr) or HOST memory (pinned or pageable); host arrays are
+ *    staged through the context workspace with copies on the context stream.
+ *  - The caller owns every array.  The library owns only the opaque context:
+ *    its stream binding, lazily grown device workspace and optional NCCL
+ *    communicator.  It never frees or retains caller memory.
+ *  - All work is ordered on the context's CUDA stream.  Entries return after
+ *    their work is enqueued, except where "blocks" is stated (the solvers block
+ *    until their host report is filled).
+ *  - Errors: a status code; sk_last_error() gives a message for the last
+ *    failing call on that context.  SK_EINVAL for bad sizes/arguments or
+ *    non-finite / non-positive inputs where positivity is required (zero weights
+ *    are rejected: eps log a_i diverges).  Non-convergence is NOT an error
+ *    (SK_OK with converged = 0).  SK_ENONFINITE when a potential becomes
+ *    non-finite: f and g then hold the last finite iterate.
+ *  - Determinism: identical inputs, configuration and world size give
+ *    bit-identical outputs (fixed reduction orders, no float atomics).  The
+ *    sharded solver is bit-identical across world sizes 1, 2, 4, 8.
+ *  - Iteration semantics: iterations = number of full (g, f) sweeps L at return;
+ *    (f, g) = (f^(L), g^(L)); marginal_error = err_L; dual_objective = E(f^(L), g^(L)).
+ *    Initializer-internal iterations are reported separately, never added.
+ */
+#ifndef SINKHORN_B200_H
+#define SINKHORN_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct sk_ctx sk_ctx;
+
+typedef enum {
+    SK_OK = 0,
+    SK_EINVAL = 1,        /* invalid argument (sizes, eps, tol, weights, NaN/Inf inputs) */
+    SK_ECUDA = 2,         /* CUDA runtime / launch error */
+    SK_ENONFINITE = 3,    /* a potential became non-finite; last finite iterate returned */
+    SK_ENCCL = 4,         /* NCCL missing or failed */
+    SK_ENOMEM = 5,        /* device workspace allocation failed */
+    SK_EUNSUPPORTED = 6   /* valid request outside this build's kernels (stated per entry) */
+} sk_status;
+
+typedef enum {
+    SK_COST_AUTO = 0,     /* stored if 4*n*m bytes fit the workspace budget and n*m is large, else online */
+    SK_COST_ONLINE = 1,   /* C_ij recomputed from the point clouds in every pass (never materialised) */
+    SK_COST_STORED = 2    /* C materialised once in HBM (fp32, 4nm bytes), streamed every sweep */
+} sk_cost_mode;
+
+/* Host-side report of one solve (one entry per problem of a batch). */
+typedef struct {
+    int32_t iterations;     /* full sweeps L */
+    int32_t converged;      /* 1 if err_L < tol at a check */
+    float marginal_error;   /* err_L (threshold appendix) */
+    double dual_objective;  /* E(f^L, g^L), Eq. (2) */
+    double init_ms;         /* initializer time inside this call (0 if none) */
+    double build_ms;        /* stored-cost build time (0 if online) */
+    double solve_ms;        /* Sinkhorn iterations, device time on the context stream */
+} sk_report;
+
+/* Cumulative per-context counters (for the bench's roofline / launch count). */
+typedef struct {
+    int64_t kernel_launches;   /* every kernel this library launched on the context */
+    int64_t lse_launches;      /* launches of the dominant LSE-pass / on-chip solver kernels */
+    double lse_ms;             /* device time of those launches (CUDA events on the context stream;
+                                  only accumulated while timing is enabled) */
+    double lse_ex2;            /* algorithmic exp2 evaluations of those launches (2 per cost entry
+                                  per sweep, counted from the iteration counts) */
+    double lse_bytes;          /* algorithmic HBM bytes of those launches (stored mode: 4 per entry) */
+} sk_counters;
+
+/* ---------------------------------------------------------------- context -- */
+/* Create a context bound to CUDA device `device` and stream `cuda_stream`
+ * (a cudaStream_t; NULL = the legacy default stream).  *ctx receives the handle. */
+sk_status sk_create(sk_ctx **ctx, int device, void *cuda_stream);
+/* Rebind the context stream (e.g. to torch's current stream). */
+sk_status sk_set_stream(sk_ctx *ctx, void *cuda_stream);
+void sk_destroy(sk_ctx *ctx);
+const char *sk_last_error(const sk_ctx *ctx);
+const char *sk_status_string(int status);
+int32_t sk_version(void);
+/* Enable (1) / disable (0) CUDA-event timing of the dominant kernels into sk_counters. */
+sk_status sk_set_timing(sk_ctx *ctx, int32_t enable);
+sk_status sk_get_counters(const sk_ctx *ctx, sk_counters *out /* host */);
+sk_status sk_reset_counters(sk_ctx *ctx);
+
+/* --------------------------------------------------------- multi-GPU (NCCL) -- */
+/* Row sharding of x across `world` ranks (one process per GPU).  Rank 0 calls
+ * sk_nccl_unique_id, the caller broadcasts the 128 bytes (e.g. with
+ * torch.distributed), then every rank calls sk_comm_init.  NCCL is loaded at
+ * run time (libnccl.so.2); SK_ENCCL if unavailable. */
+sk_status sk_nccl_unique_id(sk_ctx *ctx, void *out_128B /* host */);
+sk_status sk_comm_init(sk_ctx *ctx, const void *id_128B /* host */, int32_t rank, int32_t world);
+/* Row block owned by `rank` in the fixed global partition used by
+ * sinkhorn_solve_sharded: rows [*row0, *row0 + *n_local) of n_total.  The
+ * partition is a function of n_total only (SK_SHARD_BLOCKS blocks), which is what
+ * makes the result independent of the world size. */
+#define SK_SHARD_BLOCKS 8
+sk_status sk_shard_rows(int64_t n_total, int32_t rank, int32_t world, int64_t *row0, int64_t *n_local);
+
+/* ----------------------------------------------------------- initializers -- */
+/* Batched stable sort / rank of B rows of n fp32 keys (the sorting permutations
+ * sigma of P:110): perm[b][k] = index of the k-th smallest key of row b, ties by
+ * index (stable), -0.0 == +0.0 (R-16); rank[b][perm[b][k]] = k.  perm or rank may
+ * be NULL.  Bit-exact.  SK_EINVAL on NaN keys.  n <= 8192 per row. */
+sk_status sinkhorn_sort1d_batched(sk_ctx *ctx, int64_t B, int64_t n, const float *x,
+                                  int32_t *perm, int32_t *rank);
+
+/* f^(0) = 0: writes B*n zeros to pot. */
+sk_status sinkhorn_init_zero(sk_ctx *ctx, int64_t B, int64_t n, float *pot);
+
+/* 1D initializer (Sec. 3.1; DualSort appendix) for d = 1,
+ * n == m, uniform weights, cost (x - y)^2: sort x (sigma) and y (rho); the
+ * sorted identity matching is optimal; f^(0)_{sigma(k)} = f~_k where f~ is
+ * the eps = 0 dual of the sorted problem produced by Alg. 2 (R-5):
+ *   dualsort_iters == 0: the fixed point of Alg. 2 from f = 0 (R-6, R-7),
+ *     computed in O(n) by prefix/suffix scans;
+ *   dualsort_iters == L > 0: exactly L vectorised (Jacobi) sweeps of Alg. 2,
+ *     O(L n^2) (the paper's "3 iterations").
+ * x: B x n; y: m values (y_shared = 1) or B x m.  pot: B x n (x side).  perm /
+ * rank (nullable): the sort of x as in sinkhorn_sort1d_batched.
+ * SK_EUNSUPPORTED if n != m (general NW + Alg. 3 is a later row). */
+sk_status sinkhorn_init_sort1d(sk_ctx *ctx, int64_t B, int64_t n, int64_t m, const float *x,
+                               const float *y, int32_t y_shared, int32_t dualsort_iters,
+                               float *pot, int32_t *perm, int32_t *rank);
+
+/* Gaussian initializer (Sec. 3.2): weighted means and biased
+ * covariances (+ ridge_rel * tr/d * I, R-11) computed on device with fp64
+ * accumulation; matrix square roots by fp64 coupled Newton-Schulz (R-12);
+ * A = S_mu^{-1/2} (S_mu^{1/2} S_nu S_mu^{1/2})^{1/2} S_mu^{-1/2};
+ * potential f*(x) = ||x||^2 - (x - m_mu)^T A (x - m_mu) - 2 m_nu^T x
+ * (Gaussian-Potential appendix, R-4), evaluated on the smaller side
+ * (n <= m: x, *side = 0; else y with roles swapped, *side = 1, R-15).
+ * a, b nullable (uniform).  pot: n (side 0) or m (side 1).  d <= 64. */
+sk_status sinkhorn_init_gaussian(sk_ctx *ctx, int64_t n, int64_t m, int32_t d, const float *x,
+                                 const float *a, const float *y, const float *b, float ridge_rel,
+                                 float *pot, int32_t *side /* host */);
+
+/* GMM initializer (Sec. 3.3): given mixtures rho (Kx components:
+ * weights wx[Kx], means mux[Kx][d], covariances covx[Kx][d][d]) fitted to mu and
+ * tau (Ky, wy, muy, covy) fitted to nu: C~_kl = ||m_k - m'_l||^2 + B^2(S_k, S'_l)
+ * (Eq. 6) with fp64 Newton-Schulz square roots; the Kx x Ky entropic
+ * problem at the same eps (R-13) is solved in fp64 to inner_tol (max
+ * inner_max_iter sweeps) -> f~; f^(0)(x) = sum_k f~_k p_k(x), p_k the posterior
+ * responsibilities (Eq. 7), on the smaller side (*side as above).
+ * Mixture parameters are inputs (fitting is a later row).  d <= 64, K <= 64. */
+sk_status sinkhorn_init_gmm(sk_ctx *ctx, int64_t n, int64_t m, int32_t d, const float *x,
+                            const float *y, int32_t Kx, const float *wx, const float *mux,
+                            const float *covx, int32_t Ky, const float *wy, const float *muy,
+                            const float *covy, float eps, float inner_tol, int32_t inner_max_iter,
+                            float *pot, int32_t *side /* host */);
+
+/* Subsample initializer (Sec. 3.4): w = x[idx_x] (ns points),
+ * z = y[idx_y] (ms points), uniform weights; inner Sinkhorn at the same eps to
+ * inner_tol (max inner_max_iter) -> g~; then Eq. (8)
+ *   f^(0)_i = -eps log (1/ms) sum_j exp((g~_j - c(x_i, z_j))/eps)
+ * in one online LSE pass over all of x.  Indices must be distinct and in range.
+ * *side as above (n > m: roles swapped).  inner (nullable, host): report of the
+ * inner solve.  pot: n (side 0) or m (side 1). */
+sk_status sinkhorn_init_subsample(sk_ctx *ctx, int64_t n, int64_t m, int32_t d, const float *x,
+                                  const float *y, int64_t ns, const int32_t *idx_x, int64_t ms,
+                                  const int32_t *idx_y, float eps, float inner_tol,
+                                  int32_t inner_max_iter, float *pot, int32_t *side /* host */,
+                                  sk_report *inner /* host, nullable */);
+
+/* ----------------------------------------------------------------- solver -- */
+/* Solve B independent problems (B >= 1) of equal sizes.
+ *   x: B x n x d;  y: B x m x d, or m x d shared by all problems (y_shared = 1);
+ *   a: B x n or NULL (uniform 1/n);  b: B x m (or m if y_shared) or NULL (uniform);
+ *   eps > 0, tol > 0, max_iter >= 1, check_every >= 1;
+ *   f_init: B x n or NULL, g_init: B x m or NULL — at most one non-NULL.
+ *     With f_init (or neither) each sweep is g-update then f-update (R-2).  With
+ *     g_init the transposed problem is solved (x<->y, a<->b, f<->g).
+ *   f: B x n, g: B x m outputs;  rep: B host reports.
+ * Kernels: problems with n, m <= 4096 and d <= 4 run the on-chip solver (one CTA
+ * per problem, whole iteration loop on chip, per-problem convergence); larger
+ * problems run the multi-kernel online LSE path (cost recomputed per pass; FFMA
+ * cross term) or, with SK_COST_STORED, the stored-cost sweep.  Blocks until the
+ * reports are filled.  d <= 256. */
+sk_status sinkhorn_solve(sk_ctx *ctx, int64_t B, int64_t n, int64_t m, int32_t d, const float *x,
+                         const float *y, int32_t y_shared, const float *a, const float *b, float eps,
+                         float tol, int32_t max_iter, int32_t check_every, sk_cost_mode mode,
+                         const float *f_init, const float *g_init, float *f, float *g,
+                         sk_report *rep /* host, B entries */);
+
+/* Row-sharded solve of ONE problem across the communicator's ranks (8(e) of the
+ * design): this rank owns rows [row0, row0 + n_local) as given by sk_shard_rows.
+ * x_local, a_local (nullable), f_init_local (nullable), f_local: this rank's
+ * rows; y, b (nullable), g: replicated (m).  Every sweep: local row pass (f),
+ * local column partials (max, sum-exp) per fixed row block, ncclAllGather of the
+ * partials, identical rank-order merge on every rank (g, error, stop flag).
+ * Requires sk_comm_init (world 1 works without it).  Blocks. */
+sk_status sinkhorn_solve_sharded(sk_ctx *ctx, int64_t n_total, int64_t row0, int64_t n_local,
+                                 int64_t m, int32_t d, const float *x_local, const float *y,
+                                 const float *a_local, const float *b, float eps, float tol,
+                                 int32_t max_iter, int32_t check_every, sk_cost_mode mode,
+                                 const float *f_init_local, float *f_local, float *g,
+                                 sk_report *rep /* host */);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SINKHORN_B200_H */

@@ -1,0 +1,224 @@
+"""B200-native (sm_100a) hot path of "Rethinking Initialization of the Sinkhorn Algorithm"
+(Thornton & Cuturi, arXiv 2206.07630).
+
+The compute lives in ``libsinkhorn_b200.so`` (hand-written CUDA, C ABI in
+``include/sinkhorn_b200.h``).  This module only marshals arguments: torch tensors
+(CUDA or CPU) are passed to the C ABI by pointer — CPU tensors are host buffers that
+the library stages itself — and results come back as tensors on the inputs' device.
+PyTorch provides device memory, streams and process groups; nothing here computes
+any step of the method.
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import List, Optional, Tuple
+
+import torch
+
+from . import _lib
+from ._lib import (SK_COST_AUTO, SK_COST_ONLINE, SK_COST_STORED, SK_SHARD_BLOCKS, SkCounters,
+                   SkReport)
+
+__all__ = ["Context", "SinkhornError", "sinkhorn_solve", "sinkhorn_solve_sharded",
+           "sinkhorn_init_zero", "sinkhorn_init_sort1d", "sinkhorn_init_gaussian",
+           "sinkhorn_init_gmm", "sinkhorn_init_subsample", "sinkhorn_sort1d_batched",
+           "shard_rows", "SK_COST_AUTO", "SK_COST_ONLINE", "SK_COST_STORED", "SK_SHARD_BLOCKS"]
+
+_MODES = {"auto": SK_COST_AUTO, "online": SK_COST_ONLINE, "stored": SK_COST_STORED}
+
+
+class SinkhornError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{_lib.load().sk_status_string(status).decode()}: {msg}")
+        self.status = status
+
+
+class Context:
+    """Owns one ``sk_ctx`` bound to a CUDA device and stream (torch's current stream by default)."""
+
+    def __init__(self, device: int = 0, stream: Optional[torch.cuda.Stream] = None):
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_2206_07630_b200 needs a CUDA device (no CPU fallback)")
+        self.lib = _lib.load()
+        self.device = device
+        with torch.cuda.device(device):
+            s = stream if stream is not None else torch.cuda.current_stream(device)
+        self.stream = s
+        h = ctypes.c_void_p()
+        st = self.lib.sk_create(ctypes.byref(h), device, ctypes.c_void_p(s.cuda_stream))
+        if st != 0:
+            raise SinkhornError(st, "sk_create failed")
+        self.h = h
+
+    def check(self, st: int, allow_nonfinite: bool = False) -> int:
+        if st == 0 or (allow_nonfinite and st == _lib.SK_ENONFINITE):
+            return st
+        raise SinkhornError(st, self.lib.sk_last_error(self.h).decode())
+
+    def set_stream(self, stream: torch.cuda.Stream) -> None:
+        self.stream = stream
+        self.check(self.lib.sk_set_stream(self.h, ctypes.c_void_p(stream.cuda_stream)))
+
+    def set_timing(self, on: bool) -> None:
+        self.check(self.lib.sk_set_timing(self.h, int(on)))
+
+    def counters(self) -> dict:
+        c = SkCounters()
+        self.check(self.lib.sk_get_counters(self.h, ctypes.byref(c)))
+        return c.as_dict()
+
+    def reset_counters(self) -> None:
+        self.check(self.lib.sk_reset_counters(self.h))
+
+    def nccl_unique_id(self) -> bytes:
+        buf = ctypes.create_string_buffer(128)
+        self.check(self.lib.sk_nccl_unique_id(self.h, buf))
+        return buf.raw
+
+    def comm_init(self, uid: bytes, rank: int, world: int) -> None:
+        buf = ctypes.create_string_buffer(uid, 128)
+        self.check(self.lib.sk_comm_init(self.h, buf, rank, world))
+
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            self.lib.sk_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# ------------------------------------------------------------------ marshalling
+def _ptr(t: Optional[torch.Tensor], dtype=torch.float32):
+    if t is None:
+        return None
+    if t.dtype != dtype or not t.is_contiguous():
+        raise TypeError(f"expected a contiguous {dtype} tensor, got {t.dtype} contiguous={t.is_contiguous()}")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _empty(shape, like: torch.Tensor, dtype=torch.float32) -> torch.Tensor:
+    if like.is_cuda:
+        return torch.empty(shape, dtype=dtype, device=like.device)
+    return torch.empty(shape, dtype=dtype, pin_memory=torch.cuda.is_available())
+
+
+def shard_rows(n_total: int, rank: int, world: int) -> Tuple[int, int]:
+    lib = _lib.load()
+    r0, nl = ctypes.c_int64(), ctypes.c_int64()
+    st = lib.sk_shard_rows(n_total, rank, world, ctypes.byref(r0), ctypes.byref(nl))
+    if st != 0:
+        raise SinkhornError(st, f"sk_shard_rows({n_total}, {rank}, {world})")
+    return r0.value, nl.value
+
+
+# ------------------------------------------------------------------ entries
+def sinkhorn_sort1d_batched(ctx: Context, x: torch.Tensor):
+    """Stable per-row sort: returns (perm, rank) int32, shape of x (B, n)."""
+    B, n = (1, x.numel()) if x.dim() == 1 else (x.shape[0], x.shape[-1])
+    perm, rank = _empty(x.shape, x, torch.int32), _empty(x.shape, x, torch.int32)
+    ctx.check(ctx.lib.sinkhorn_sort1d_batched(ctx.h, B, n, _ptr(x), _ptr(perm, torch.int32),
+                                              _ptr(rank, torch.int32)))
+    return perm, rank
+
+
+def sinkhorn_init_zero(ctx: Context, B: int, n: int, like: torch.Tensor) -> torch.Tensor:
+    pot = _empty((B, n) if B > 1 else (n,), like)
+    ctx.check(ctx.lib.sinkhorn_init_zero(ctx.h, B, n, _ptr(pot)))
+    return pot
+
+
+def sinkhorn_init_sort1d(ctx: Context, x: torch.Tensor, y: torch.Tensor, y_shared: bool = True,
+                         dualsort_iters: int = 0, want_perm: bool = False):
+    """x: (B, n) or (B, n, 1); y: (m,) shared or (B, m).  Returns pot (B, n) [, perm, rank]."""
+    B = x.shape[0] if x.dim() >= 2 else 1
+    n = x.shape[1] if x.dim() >= 2 else x.shape[0]
+    m = y.shape[-2] if (y.dim() >= 2 and y.shape[-1] == 1) else y.shape[-1]
+    pot = _empty((B, n), x)
+    perm = _empty((B, n), x, torch.int32) if want_perm else None
+    rank = _empty((B, n), x, torch.int32) if want_perm else None
+    ctx.check(ctx.lib.sinkhorn_init_sort1d(ctx.h, B, n, m, _ptr(x), _ptr(y), int(y_shared),
+                                           dualsort_iters, _ptr(pot), _ptr(perm, torch.int32),
+                                           _ptr(rank, torch.int32)))
+    return (pot, perm, rank) if want_perm else pot
+
+
+def sinkhorn_init_gaussian(ctx: Context, x, y, a=None, b=None, ridge_rel: float = 1e-6):
+    n, d = x.shape
+    m = y.shape[0]
+    side = ctypes.c_int32()
+    pot = _empty((min(n, m) if n != m else n,), x)
+    ctx.check(ctx.lib.sinkhorn_init_gaussian(ctx.h, n, m, d, _ptr(x), _ptr(a), _ptr(y), _ptr(b),
+                                             float(ridge_rel), _ptr(pot), ctypes.byref(side)))
+    return pot, side.value
+
+
+def sinkhorn_init_gmm(ctx: Context, x, y, gx: dict, gy: dict, eps: float, inner_tol: float = 1e-9,
+                      inner_max_iter: int = 100000):
+    """gx/gy: {'weights': (K,), 'means': (K, d), 'covs': (K, d, d)} fp32 tensors."""
+    n, d = x.shape
+    m = y.shape[0]
+    side = ctypes.c_int32()
+    pot = _empty((min(n, m),), x)
+    ctx.check(ctx.lib.sinkhorn_init_gmm(
+        ctx.h, n, m, d, _ptr(x), _ptr(y), gx["weights"].shape[0], _ptr(gx["weights"]),
+        _ptr(gx["means"]), _ptr(gx["covs"]), gy["weights"].shape[0], _ptr(gy["weights"]),
+        _ptr(gy["means"]), _ptr(gy["covs"]), float(eps), float(inner_tol), int(inner_max_iter),
+        _ptr(pot), ctypes.byref(side)))
+    return pot, side.value
+
+
+def sinkhorn_init_subsample(ctx: Context, x, y, idx_x, idx_y, eps: float, inner_tol: float,
+                            inner_max_iter: int = 10000):
+    n, d = x.shape
+    m = y.shape[0]
+    side = ctypes.c_int32()
+    rep = SkReport()
+    pot = _empty((min(n, m),), x)
+    ctx.check(ctx.lib.sinkhorn_init_subsample(
+        ctx.h, n, m, d, _ptr(x), _ptr(y), idx_x.numel(), _ptr(idx_x, torch.int32), idx_y.numel(),
+        _ptr(idx_y, torch.int32), float(eps), float(inner_tol), int(inner_max_iter), _ptr(pot),
+        ctypes.byref(side), ctypes.byref(rep)))
+    return pot, side.value, rep.as_dict()
+
+
+def sinkhorn_solve(ctx: Context, x, y, eps: float, tol: float = 1e-3, max_iter: int = 10000,
+                   check_every: int = 1, a=None, b=None, y_shared: bool = False, mode: str = "auto",
+                   f_init=None, g_init=None, f=None, g=None, allow_nonfinite: bool = False):
+    """Solve B >= 1 problems.  x: (n, d) or (B, n, d); y: (m, d) [shared] or (B, m, d).
+    Returns (f, g, reports) with f (B, n) / g (B, m) (B dropped for a single problem)."""
+    single = x.dim() == 2
+    xb = x.unsqueeze(0) if single else x
+    B, n, d = xb.shape
+    m = y.shape[-2]
+    if f is None:
+        f = _empty((B, n), x)
+    if g is None:
+        g = _empty((B, m), x)
+    reps = (SkReport * B)()
+    st = ctx.lib.sinkhorn_solve(ctx.h, B, n, m, d, _ptr(x), _ptr(y), int(y_shared), _ptr(a), _ptr(b),
+                                float(eps), float(tol), int(max_iter), int(check_every), _MODES[mode],
+                                _ptr(f_init), _ptr(g_init), _ptr(f), _ptr(g), reps)
+    ctx.check(st, allow_nonfinite)
+    out = [r.as_dict() for r in reps]
+    if single:
+        return f.view(n), g.view(m), out[0]
+    return f, g, out
+
+
+def sinkhorn_solve_sharded(ctx: Context, n_total: int, row0: int, x_local, y, eps: float,
+                           tol: float = 1e-3, max_iter: int = 10000, check_every: int = 1,
+                           a_local=None, b=None, mode: str = "auto", f_init_local=None):
+    n_local, d = x_local.shape
+    m = y.shape[0]
+    f = _empty((n_local,), x_local)
+    g = _empty((m,), x_local)
+    rep = SkReport()
+    ctx.check(ctx.lib.sinkhorn_solve_sharded(
+        ctx.h, n_total, row0, n_local, m, d, _ptr(x_local), _ptr(y), _ptr(a_local), _ptr(b),
+        float(eps), float(tol), int(max_iter), int(check_every), _MODES[mode], _ptr(f_init_local),
+        _ptr(f), _ptr(g), ctypes.byref(rep)))
+    return f, g, rep.as_dict()

@@ -1,0 +1,887 @@
+// sk_api.cu — the C ABI (include/sinkhorn_b200.h): context, argument checks,
+// host/device staging, dispatch to the kernels and the device-driven solve loop.
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/sinkhorn_b200.h"
+#include "sk_internal.h"
+
+using namespace sk;
+
+// ----------------------------------------------------------------- NCCL (dlopen)
+namespace {
+typedef struct { char internal[128]; } nccl_id_t;
+typedef void *nccl_comm_t;
+typedef int (*fn_get_id)(nccl_id_t *);
+typedef int (*fn_init_rank)(nccl_comm_t *, int, nccl_id_t, int);
+typedef int (*fn_allgather)(const void *, void *, size_t, int, nccl_comm_t, cudaStream_t);
+typedef int (*fn_destroy)(nccl_comm_t);
+typedef const char *(*fn_errstr)(int);
+constexpr int kNcclFloat32 = 7, kNcclFloat64 = 8;
+
+struct Nccl {
+    void *h = nullptr;
+    fn_get_id get_id = nullptr;
+    fn_init_rank init_rank = nullptr;
+    fn_allgather allgather = nullptr;
+    fn_destroy destroy = nullptr;
+    fn_errstr errstr = nullptr;
+    bool load() {
+        if (h) return true;
+        const char *names[] = {"libnccl.so.2", "libnccl.so"};
+        for (const char *nm : names) {
+            h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
+            if (h) break;
+        }
+        if (!h) return false;
+        get_id = (fn_get_id)dlsym(h, "ncclGetUniqueId");
+        init_rank = (fn_init_rank)dlsym(h, "ncclCommInitRank");
+        allgather = (fn_allgather)dlsym(h, "ncclAllGather");
+        destroy = (fn_destroy)dlsym(h, "ncclCommDestroy");
+        errstr = (fn_errstr)dlsym(h, "ncclGetErrorString");
+        return get_id && init_rank && allgather && destroy;
+    }
+};
+Nccl g_nccl;
+
+struct Buf {
+    void *p = nullptr;
+    size_t cap = 0;
+};
+}  // namespace
+
+struct sk_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    std::string err;
+    std::vector<Buf> bufs;
+    int timing = 0;
+    sk_counters cnt{};
+    nccl_comm_t comm = nullptr;
+    int rank = 0, world = 1;
+    int *h_flag = nullptr;  // pinned host scratch
+    DevStatus *h_status = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+};
+
+namespace {
+enum BufId {
+    B_STAGE0 = 0, B_STAGE_END = 16,   // staging of host arrays
+    B_FLAG = 16, B_XPACK, B_XC, B_XNK, B_XPOT, B_YPACK, B_YC, B_YNK, B_YPOT, B_PART, B_BLKE, B_BLKB,
+    B_STATUS, B_COST, B_REP, B_SORT, B_PERM, B_YSORT, B_GAUSS, B_GAUSS2, B_GMM, B_SUBW, B_SUBZ,
+    B_SUBF, B_SUBG, B_IDX, B_OUT, B_FA, B_NBUF
+};
+
+sk_status fail(sk_ctx *c, sk_status s, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    if (c) c->err = buf;
+    return s;
+}
+
+#define CU(call)                                                                                  \
+    do {                                                                                          \
+        cudaError_t _e = (call);                                                                  \
+        if (_e != cudaSuccess)                                                                    \
+            return fail(ctx, _e == cudaErrorMemoryAllocation ? SK_ENOMEM : SK_ECUDA, "%s: %s (%s:%d)", \
+                        #call, cudaGetErrorString(_e), __FILE__, __LINE__);                       \
+    } while (0)
+
+#define CK(call)                              \
+    do {                                      \
+        sk_status _s = (call);                \
+        if (_s != SK_OK) return _s;           \
+    } while (0)
+
+void *ensure(sk_ctx *ctx, int id, size_t bytes, cudaError_t *e) {
+    Buf &b = ctx->bufs[id];
+    *e = cudaSuccess;
+    if (bytes == 0) bytes = 16;
+    if (b.cap >= bytes) return b.p;
+    if (b.p) {
+        cudaStreamSynchronize(ctx->stream);
+        cudaFree(b.p);
+        b.p = nullptr;
+        b.cap = 0;
+    }
+    size_t cap = std::max(bytes, (size_t)256);
+    *e = cudaMalloc(&b.p, cap);
+    if (*e != cudaSuccess) { cudaGetLastError(); b.p = nullptr; return nullptr; }
+    b.cap = cap;
+    return b.p;
+}
+
+#define ENSURE(ptr, type, id, count)                                                              \
+    type *ptr = nullptr;                                                                          \
+    do {                                                                                          \
+        cudaError_t _e;                                                                           \
+        ptr = (type *)ensure(ctx, id, sizeof(type) * (size_t)(count), &_e);                       \
+        if (!ptr) return fail(ctx, SK_ENOMEM, "workspace allocation of %zu bytes failed: %s",     \
+                              sizeof(type) * (size_t)(count), cudaGetErrorString(_e));             \
+    } while (0)
+
+bool is_device_ptr(const void *p) {
+    if (!p) return true;
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+// Staging of caller arrays that may live in host memory.
+struct Stager {
+    sk_ctx *ctx;
+    int next = B_STAGE0;
+    struct Out { void *host; void *dev; size_t bytes; };
+    std::vector<Out> outs;
+    explicit Stager(sk_ctx *c) : ctx(c) {}
+    sk_status in(const void *p, size_t bytes, const void **dev) {
+        if (!p || is_device_ptr(p)) { *dev = p; return SK_OK; }
+        if (next >= B_STAGE_END) return fail(ctx, SK_EINVAL, "too many host arrays");
+        cudaError_t e;
+        void *d = ensure(ctx, next++, bytes, &e);
+        if (!d) return fail(ctx, SK_ENOMEM, "staging allocation failed");
+        CU(cudaMemcpyAsync(d, p, bytes, cudaMemcpyHostToDevice, ctx->stream));
+        *dev = d;
+        return SK_OK;
+    }
+    template <class T> sk_status in_t(const T *p, size_t count, const T **dev) {
+        const void *d;
+        sk_status s = in(p, count * sizeof(T), &d);
+        *dev = (const T *)d;
+        return s;
+    }
+    template <class T> sk_status out_t(T *p, size_t count, T **dev) {
+        if (!p || is_device_ptr(p)) { *dev = p; return SK_OK; }
+        if (next >= B_STAGE_END) return fail(ctx, SK_EINVAL, "too many host arrays");
+        cudaError_t e;
+        void *d = ensure(ctx, next++, count * sizeof(T), &e);
+        if (!d) return fail(ctx, SK_ENOMEM, "staging allocation failed");
+        outs.push_back({p, d, count * sizeof(T)});
+        *dev = (T *)d;
+        return SK_OK;
+    }
+    sk_status flush() {
+        for (auto &o : outs) CU(cudaMemcpyAsync(o.host, o.dev, o.bytes, cudaMemcpyDeviceToHost, ctx->stream));
+        outs.clear();
+        return SK_OK;
+    }
+};
+
+// Device-side validation of arrays; one D2H read of a flag.
+sk_status check_arrays(sk_ctx *ctx, std::initializer_list<std::pair<const float *, long long>> finite,
+                       std::initializer_list<std::pair<const float *, long long>> positive,
+                       const char *what) {
+    ENSURE(flag, int, B_FLAG, 4);
+    CU(cudaMemsetAsync(flag, 0, sizeof(int), ctx->stream));
+    for (auto &p : finite)
+        if (p.first) { CU(launch_check_finite(p.first, p.second, flag, ctx->stream)); ctx->cnt.kernel_launches++; }
+    for (auto &p : positive)
+        if (p.first) { CU(launch_check_positive(p.first, p.second, flag, ctx->stream)); ctx->cnt.kernel_launches++; }
+    CU(cudaMemcpyAsync(ctx->h_flag, flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    if (*ctx->h_flag) return fail(ctx, SK_EINVAL, "%s: non-finite input or non-positive weight", what);
+    return SK_OK;
+}
+
+bool bad_scalar(float v) { return !std::isfinite(v); }
+
+// Occupancy-aware split count: smallest waste of the last wave, at least ~2 waves.
+int choose_split(long long ptiles, long long qtiles_per_unit, int occ, int max_split) {
+    const long long slots = 148LL * std::max(occ, 1);
+    int best = 1;
+    double best_cost = 1e30;
+    for (int s = 1; s <= max_split && s <= std::max<long long>(1, qtiles_per_unit); ++s) {
+        const long long ctas = ptiles * s;
+        const double waves = (double)ctas / slots;
+        const double cost = std::ceil(waves) / waves * (1.0 + 0.002 * s) + (waves < 1.0 ? 1.0 / waves : 0.0);
+        if (cost < best_cost - 1e-9) { best_cost = cost; best = s; }
+    }
+    return best;
+}
+
+long long shard_block_rows(long long n) {
+    long long per = (n + SK_SHARD_BLOCKS - 1) / SK_SHARD_BLOCKS;
+    return (per + 255) / 256 * 256;
+}
+
+// ------------------------------------------------------------ the solve core
+struct Problem {
+    long long n, m;       // local rows n (this rank), all columns m
+    long long n_total;    // global rows (sharded) — for uniform weights and E
+    int d;
+    const float *x, *y, *a, *b, *f_init;
+    float eps, tol;
+    int max_iter, check_every;
+    sk_cost_mode mode;
+    float *f, *g;         // device outputs
+    int rank, world;      // world > 1: sharded
+};
+
+sk_status solve_multikernel(sk_ctx *ctx, const Problem &P, sk_report *rep) {
+    cudaStream_t st = ctx->stream;
+    const bool sharded = P.world > 1;
+    const long long n = P.n, m = P.m;
+    const bool stored_ok = P.d >= 1 && (m % 4 == 0);
+    bool stored = P.mode == SK_COST_STORED;
+    if (P.mode == SK_COST_AUTO) stored = stored_ok && P.d >= 8 && P.d < 32 && 4.0 * n * m <= 8.0e9;
+    if (stored && !stored_ok) return fail(ctx, SK_EUNSUPPORTED, "stored-cost mode needs m %% 4 == 0");
+    const int D = stored ? 0 : lse_dpad(P.d);
+    if (!stored && D == 0) return fail(ctx, SK_EUNSUPPORTED, "online path supports d <= 64");
+    const int tq = stored ? 256 : lse_tq(D);
+    const long long xt = lse_tiles(n, tq), yt = lse_tiles(m, tq);
+
+    ENSURE(xpack, float, B_XPACK, xt * (D + 1) * tq);
+    ENSURE(xc, float, B_XC, n);
+    ENSURE(xnk, float, B_XNK, n);
+    ENSURE(xpot, float, B_XPOT, 2 * n);
+    ENSURE(ypack, float, B_YPACK, yt * (D + 1) * tq);
+    ENSURE(yc, float, B_YC, m);
+    ENSURE(ynk, float, B_YNK, m);
+    ENSURE(ypot, float, B_YPOT, 2 * m);
+    ENSURE(status, DevStatus, B_STATUS, 1);
+    Side X{(int)n, P.d, D, tq, xpack, xc, xnk, {xpot, xpot + n}};
+    Side Y{(int)m, P.d, D, tq, ypack, yc, ynk, {ypot, ypot + m}};
+
+    // column-pass partition: SK_SHARD_BLOCKS fixed row blocks (global), split_q sub-splits each
+    const long long n_glob = sharded ? P.n_total : n;
+    const long long bs_rows = shard_block_rows(n_glob);
+    const int nblk_glob = (int)((n_glob + bs_rows - 1) / bs_rows);
+    const int blk_per_rank = sharded ? SK_SHARD_BLOCKS / P.world : nblk_glob;
+    const int nblk_local = sharded ? (int)((n + bs_rows - 1) / bs_rows) : nblk_glob;
+    const int occ = stored ? 8 : lse_occupancy_ctas(D);
+    const int Rr = D <= 4 ? 4 : (D <= 16 ? 2 : 1);
+    const long long ptiles_col = stored ? (m + 511) / 512 : (m + 128LL * Rr - 1) / (128LL * Rr);
+    const long long ptiles_row = stored ? (n + 7) / 8 : (n + 128LL * Rr - 1) / (128LL * Rr);
+    const int split_q = choose_split(ptiles_col * SK_SHARD_BLOCKS / std::max(P.world, 1),
+                                     stored ? bs_rows / 64 : bs_rows / tq, occ, 64);
+    const int nsplit_col = SK_SHARD_BLOCKS * split_q;  // global split count
+    const int split_row = stored ? 1 : choose_split(ptiles_row, yt, occ, 64);
+    const long long part_elems = std::max((long long)nsplit_col * m, (long long)split_row * n);
+    ENSURE(part, float2, B_PART, part_elems);
+    ENSURE(blke, double, B_BLKE, 2048);
+    ENSURE(blkb, int, B_BLKB, 2048);
+
+    const float loga_u = (float)(-std::log((double)n_glob)), logb_u = (float)(-std::log((double)m));
+    CU(pack_side(X, P.x, P.a, loga_u, P.f_init, P.eps, st));
+    CU(pack_side(Y, P.y, P.b, logb_u, nullptr, P.eps, st));
+    CU(launch_status_init(status, P.max_iter, P.check_every, P.tol, st));
+    ctx->cnt.kernel_launches += 3;
+
+    float *C = nullptr;
+    double build_ms = 0.0;
+    if (stored) {
+        cudaError_t e;
+        C = (float *)ensure(ctx, B_COST, sizeof(float) * (size_t)n * m, &e);
+        if (!C) return fail(ctx, SK_ENOMEM, "stored cost needs %.2f GiB", 4.0 * n * m / (1 << 30));
+        CU(cudaEventRecord(ctx->ev0, st));
+        CU(launch_build_cost(P.x, P.y, n, m, P.d, C, st));
+        CU(cudaEventRecord(ctx->ev1, st));
+        ctx->cnt.kernel_launches++;
+        CU(cudaEventSynchronize(ctx->ev1));
+        float ms = 0.f;
+        CU(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+        build_ms = ms;
+    }
+
+    LsePass colp{&Y, &X, nblk_local, (int)(bs_rows / tq), split_q,
+                 part + (sharded ? (long long)P.rank * blk_per_rank * split_q * m : 0), P.eps,
+                 &status->stop};
+    LsePass rowp{&X, &Y, 1, 0, split_row, part, P.eps, &status->stop};
+    StoredPass scol{C, n, m, P.eps, xpack,
+                    part + (sharded ? (long long)P.rank * blk_per_rank * split_q * m : 0),
+                    bs_rows, nblk_local, split_q, &status->stop};
+    StoredPass srow{C, n, m, P.eps, ypack, part, 0, 1, 1, &status->stop};
+    MergePass mcol{MERGE_COL, &Y, part, nsplit_col, P.eps, P.b, status, blke, blkb, nullptr, 0.f,
+                   sharded ? 1 : 0};
+    MergePass mrow{MERGE_ROW, &X, part, stored ? 1 : split_row, P.eps, nullptr, status, blke, blkb,
+                   nullptr, 0.f, sharded ? 1 : 0};
+
+    CU(cudaEventRecord(ctx->ev0, st));
+    int launched = 0, poll = 4;
+    const int max_sweeps = P.max_iter + 1;  // + the column pass that measures err_L
+    for (int it = 0; it < max_sweeps;) {
+        const int chunk = std::min(poll, max_sweeps - it);
+        for (int c = 0; c < chunk; ++c, ++it) {
+            if (stored) CU(launch_stored_cols(scol, st));
+            else CU(launch_lse(colp, st));
+            if (sharded) {
+                const size_t cnt = (size_t)blk_per_rank * split_q * m * 2;
+                int r = g_nccl.allgather(part + (long long)P.rank * blk_per_rank * split_q * m, part, cnt,
+                                         kNcclFloat32, ctx->comm, st);
+                if (r != 0) return fail(ctx, SK_ENCCL, "ncclAllGather failed: %s",
+                                        g_nccl.errstr ? g_nccl.errstr(r) : "?");
+            }
+            CU(launch_merge(mcol, st));
+            if (stored) CU(launch_stored_rows(srow, st));
+            else CU(launch_lse(rowp, st));
+            CU(launch_merge(mrow, st));
+            launched += 4;
+        }
+        CU(cudaMemcpyAsync(ctx->h_status, status, sizeof(DevStatus), cudaMemcpyDeviceToHost, st));
+        CU(cudaStreamSynchronize(st));
+        if (ctx->h_status->stop) break;
+        poll = std::min(poll * 2, 64);
+    }
+    CU(cudaEventRecord(ctx->ev1, st));
+    CU(launch_report(X, Y, P.a, P.b, P.eps, status, sharded ? 1 : 0, n_glob, st));
+    launched++;
+    CU(cudaMemcpyAsync(ctx->h_status, status, sizeof(DevStatus), cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    float ms = 0.f;
+    CU(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+    DevStatus hs = *ctx->h_status;
+    if (!hs.stop) return fail(ctx, SK_ECUDA, "solver loop ended without a stop flag");
+    const int L = hs.final_iter;
+    double E = hs.E;
+    if (sharded) {  // E = sum over ranks of <f,a> - eps sum(a) (rank order) + <g,b>
+        ENSURE(fa, double, B_FA, P.world);
+        CU(cudaMemcpyAsync(fa + P.rank, &status->fa_local, sizeof(double), cudaMemcpyDeviceToDevice, st));
+        int r = g_nccl.allgather(fa + P.rank, fa, 1, kNcclFloat64, ctx->comm, st);
+        if (r != 0) return fail(ctx, SK_ENCCL, "ncclAllGather(E) failed");
+        std::vector<double> h(P.world);
+        CU(cudaMemcpyAsync(h.data(), fa, sizeof(double) * P.world, cudaMemcpyDeviceToHost, st));
+        CU(cudaStreamSynchronize(st));
+        double s = 0.0;
+        for (int i = 0; i < P.world; ++i) s += h[i];
+        E = s + hs.E;
+    }
+    CU(cudaMemcpyAsync(P.f, X.pot[L & 1], sizeof(float) * n, cudaMemcpyDeviceToDevice, st));
+    CU(cudaMemcpyAsync(P.g, Y.pot[L & 1], sizeof(float) * m, cudaMemcpyDeviceToDevice, st));
+    ctx->cnt.kernel_launches += launched;
+    const int sweeps_done = hs.iter;  // row passes actually executed
+    ctx->cnt.lse_launches += 2LL * (sweeps_done + 1);
+    if (ctx->timing) ctx->cnt.lse_ms += ms;
+    const double entries = (double)n * m * (2.0 * L + 1.0);
+    ctx->cnt.lse_ex2 += entries;
+    if (stored) ctx->cnt.lse_bytes += 4.0 * entries;
+    rep->iterations = L;
+    rep->converged = hs.converged;
+    rep->marginal_error = hs.err;
+    rep->dual_objective = E;
+    rep->build_ms = build_ms;
+    rep->solve_ms = ms;
+    if (hs.nonfinite) return fail(ctx, SK_ENONFINITE, "potentials became non-finite after sweep %d", L);
+    return SK_OK;
+}
+
+sk_status validate_common(sk_ctx *ctx, long long n, long long m, int d, float eps, float tol,
+                          int max_iter, int check_every) {
+    if (!ctx) return SK_EINVAL;
+    if (n < 1 || m < 1) return fail(ctx, SK_EINVAL, "n and m must be >= 1 (n=%lld m=%lld)", n, m);
+    if (n > (1LL << 31) - 1 || m > (1LL << 31) - 1) return fail(ctx, SK_EUNSUPPORTED, "n, m < 2^31");
+    if (d < 1 || d > 64) return fail(ctx, SK_EINVAL, "d must be in [1, 64] (d=%d)", d);
+    if (!(eps > 0.f) || bad_scalar(eps)) return fail(ctx, SK_EINVAL, "eps must be finite and > 0");
+    if (!(tol > 0.f) || bad_scalar(tol)) return fail(ctx, SK_EINVAL, "tol must be finite and > 0");
+    if (max_iter < 1) return fail(ctx, SK_EINVAL, "max_iter must be >= 1");
+    if (check_every < 1) return fail(ctx, SK_EINVAL, "check_every must be >= 1");
+    return SK_OK;
+}
+}  // namespace
+
+// =============================================================== ABI entries
+extern "C" {
+
+int32_t sk_version(void) { return 1; }
+
+const char *sk_status_string(int s) {
+    switch (s) {
+        case SK_OK: return "SK_OK";
+        case SK_EINVAL: return "SK_EINVAL";
+        case SK_ECUDA: return "SK_ECUDA";
+        case SK_ENONFINITE: return "SK_ENONFINITE";
+        case SK_ENCCL: return "SK_ENCCL";
+        case SK_ENOMEM: return "SK_ENOMEM";
+        case SK_EUNSUPPORTED: return "SK_EUNSUPPORTED";
+        default: return "SK_UNKNOWN";
+    }
+}
+
+sk_status sk_create(sk_ctx **out, int device, void *stream) {
+    if (!out) return SK_EINVAL;
+    *out = nullptr;
+    sk_ctx *ctx = new sk_ctx();
+    ctx->bufs.resize(B_NBUF);
+    ctx->device = device;
+    ctx->stream = (cudaStream_t)stream;
+    cudaError_t e = cudaSetDevice(device);
+    if (e == cudaSuccess) e = cudaMallocHost(&ctx->h_flag, sizeof(int));
+    if (e == cudaSuccess) e = cudaMallocHost(&ctx->h_status, sizeof(DevStatus));
+    if (e == cudaSuccess) e = cudaEventCreate(&ctx->ev0);
+    if (e == cudaSuccess) e = cudaEventCreate(&ctx->ev1);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        delete ctx;
+        return SK_ECUDA;
+    }
+    *out = ctx;
+    return SK_OK;
+}
+
+sk_status sk_set_stream(sk_ctx *ctx, void *stream) {
+    if (!ctx) return SK_EINVAL;
+    ctx->stream = (cudaStream_t)stream;
+    return SK_OK;
+}
+
+void sk_destroy(sk_ctx *ctx) {
+    if (!ctx) return;
+    cudaStreamSynchronize(ctx->stream);
+    for (auto &b : ctx->bufs)
+        if (b.p) cudaFree(b.p);
+    if (ctx->comm && g_nccl.destroy) g_nccl.destroy(ctx->comm);
+    if (ctx->h_flag) cudaFreeHost(ctx->h_flag);
+    if (ctx->h_status) cudaFreeHost(ctx->h_status);
+    if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+    if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+    delete ctx;
+}
+
+const char *sk_last_error(const sk_ctx *ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+sk_status sk_set_timing(sk_ctx *ctx, int32_t enable) {
+    if (!ctx) return SK_EINVAL;
+    ctx->timing = enable;
+    return SK_OK;
+}
+
+sk_status sk_get_counters(const sk_ctx *ctx, sk_counters *out) {
+    if (!ctx || !out) return SK_EINVAL;
+    *out = ctx->cnt;
+    return SK_OK;
+}
+
+sk_status sk_reset_counters(sk_ctx *ctx) {
+    if (!ctx) return SK_EINVAL;
+    ctx->cnt = sk_counters{};
+    return SK_OK;
+}
+
+sk_status sk_shard_rows(int64_t n_total, int32_t rank, int32_t world, int64_t *row0, int64_t *n_local) {
+    if (!row0 || !n_local || n_total < 1 || world < 1 || rank < 0 || rank >= world) return SK_EINVAL;
+    if (SK_SHARD_BLOCKS % world) return SK_EUNSUPPORTED;  // world in {1, 2, 4, 8}
+    const long long bs = shard_block_rows(n_total);
+    const long long per = (long long)(SK_SHARD_BLOCKS / world) * bs;
+    const long long r0 = std::min<long long>(n_total, rank * per);
+    const long long r1 = std::min<long long>(n_total, (rank + 1) * per);
+    *row0 = r0;
+    *n_local = r1 - r0;
+    return SK_OK;
+}
+
+sk_status sk_nccl_unique_id(sk_ctx *ctx, void *out) {
+    if (!ctx || !out) return SK_EINVAL;
+    if (!g_nccl.load()) return fail(ctx, SK_ENCCL, "libnccl.so.2 could not be loaded");
+    nccl_id_t id;
+    int r = g_nccl.get_id(&id);
+    if (r != 0) return fail(ctx, SK_ENCCL, "ncclGetUniqueId failed (%d)", r);
+    memcpy(out, &id, sizeof id);
+    return SK_OK;
+}
+
+sk_status sk_comm_init(sk_ctx *ctx, const void *id, int32_t rank, int32_t world) {
+    if (!ctx || !id || world < 1 || rank < 0 || rank >= world) return SK_EINVAL;
+    if (SK_SHARD_BLOCKS % world) return fail(ctx, SK_EUNSUPPORTED, "world must divide %d", SK_SHARD_BLOCKS);
+    if (!g_nccl.load()) return fail(ctx, SK_ENCCL, "libnccl.so.2 could not be loaded");
+    cudaSetDevice(ctx->device);
+    nccl_id_t nid;
+    memcpy(&nid, id, sizeof nid);
+    int r = g_nccl.init_rank(&ctx->comm, world, nid, rank);
+    if (r != 0) return fail(ctx, SK_ENCCL, "ncclCommInitRank failed: %s", g_nccl.errstr ? g_nccl.errstr(r) : "?");
+    ctx->rank = rank;
+    ctx->world = world;
+    return SK_OK;
+}
+
+sk_status sinkhorn_sort1d_batched(sk_ctx *ctx, int64_t B, int64_t n, const float *x, int32_t *perm,
+                                  int32_t *rank) {
+    if (!ctx) return SK_EINVAL;
+    if (B < 1 || n < 1) return fail(ctx, SK_EINVAL, "B, n must be >= 1");
+    if (n > 8192) return fail(ctx, SK_EUNSUPPORTED, "sort rows of at most 8192 keys");
+    if (!x) return fail(ctx, SK_EINVAL, "x is NULL");
+    Stager sg(ctx);
+    const float *dx;
+    int *dp, *dr;
+    CK(sg.in_t(x, (size_t)B * n, &dx));
+    CK(sg.out_t(perm, (size_t)B * n, &dp));
+    CK(sg.out_t(rank, (size_t)B * n, &dr));
+    ENSURE(flag, int, B_FLAG, 4);
+    CU(cudaMemsetAsync(flag, 0, sizeof(int), ctx->stream));
+    CU(launch_sort_rows(dx, (int)B, (int)n, n, dp, dr, nullptr, flag, ctx->stream));
+    ctx->cnt.kernel_launches++;
+    CK(sg.flush());
+    CU(cudaMemcpyAsync(ctx->h_flag, flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    if (*ctx->h_flag) return fail(ctx, SK_EINVAL, "NaN key");
+    return SK_OK;
+}
+
+sk_status sinkhorn_init_zero(sk_ctx *ctx, int64_t B, int64_t n, float *pot) {
+    if (!ctx) return SK_EINVAL;
+    if (B < 1 || n < 1 || !pot) return fail(ctx, SK_EINVAL, "B, n >= 1 and pot required");
+    Stager sg(ctx);
+    float *dp;
+    CK(sg.out_t(pot, (size_t)B * n, &dp));
+    CU(launch_fill(dp, B * n, 0.f, ctx->stream));
+    ctx->cnt.kernel_launches++;
+    CK(sg.flush());
+    return SK_OK;
+}
+
+sk_status sinkhorn_init_sort1d(sk_ctx *ctx, int64_t B, int64_t n, int64_t m, const float *x,
+                               const float *y, int32_t y_shared, int32_t dualsort_iters, float *pot,
+                               int32_t *perm, int32_t *rank) {
+    if (!ctx) return SK_EINVAL;
+    if (B < 1 || n < 1 || m < 1 || !x || !y || !pot) return fail(ctx, SK_EINVAL, "bad arguments");
+    if (n != m) return fail(ctx, SK_EUNSUPPORTED, "sort1d initializer needs n == m (general NW is a later row)");
+    if (n > 4096) return fail(ctx, SK_EUNSUPPORTED, "sort1d initializer supports n <= 4096");
+    if (dualsort_iters < 0) return fail(ctx, SK_EINVAL, "dualsort_iters >= 0");
+    Stager sg(ctx);
+    const float *dx, *dy;
+    float *dpot;
+    int *dperm_user, *drank;
+    CK(sg.in_t(x, (size_t)B * n, &dx));
+    CK(sg.in_t(y, (size_t)(y_shared ? 1 : B) * m, &dy));
+    CK(sg.out_t(pot, (size_t)B * n, &dpot));
+    CK(sg.out_t(perm, (size_t)B * n, &dperm_user));
+    CK(sg.out_t(rank, (size_t)B * n, &drank));
+    ENSURE(flag, int, B_FLAG, 4);
+    ENSURE(xs, float, B_SORT, B * n);
+    ENSURE(ys, float, B_YSORT, (y_shared ? 1 : B) * m);
+    ENSURE(pscr, int, B_PERM, (y_shared ? 1 : B) * m + B * n);
+    int *dperm = dperm_user ? dperm_user : pscr + (y_shared ? 1 : B) * m;
+    CU(cudaMemsetAsync(flag, 0, sizeof(int), ctx->stream));
+    CU(launch_sort_rows(dy, (int)(y_shared ? 1 : B), (int)m, m, pscr, nullptr, ys, flag, ctx->stream));
+    CU(launch_sort_rows(dx, (int)B, (int)n, n, dperm, drank, xs, flag, ctx->stream));
+    CU(launch_sort1d_dual(xs, dperm, ys, y_shared, (int)B, (int)n, dualsort_iters, dpot, ctx->stream));
+    ctx->cnt.kernel_launches += 3;
+    CK(sg.flush());
+    CU(cudaMemcpyAsync(ctx->h_flag, flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    if (*ctx->h_flag) return fail(ctx, SK_EINVAL, "NaN in x or y");
+    return SK_OK;
+}
+
+sk_status sinkhorn_init_gaussian(sk_ctx *ctx, int64_t n, int64_t m, int32_t d, const float *x,
+                                 const float *a, const float *y, const float *b, float ridge_rel,
+                                 float *pot, int32_t *side) {
+    if (!ctx) return SK_EINVAL;
+    if (n < 1 || m < 1 || d < 1 || d > 64 || !x || !y || !pot || !side)
+        return fail(ctx, SK_EINVAL, "bad arguments (d in [1,64])");
+    if (!(ridge_rel >= 0.f) || bad_scalar(ridge_rel)) return fail(ctx, SK_EINVAL, "ridge_rel >= 0");
+    const bool swap = n > m;  // potential on the smaller side
+    Stager sg(ctx);
+    const float *dx, *dy, *da, *db;
+    float *dpot;
+    CK(sg.in_t(x, (size_t)n * d, &dx));
+    CK(sg.in_t(y, (size_t)m * d, &dy));
+    CK(sg.in_t(a, (size_t)n, &da));
+    CK(sg.in_t(b, (size_t)m, &db));
+    CK(sg.out_t(pot, (size_t)(swap ? m : n), &dpot));
+    CK(check_arrays(ctx, {{dx, n * d}, {dy, m * d}}, {{da, n}, {db, m}}, "sinkhorn_init_gaussian"));
+    if (swap) { std::swap(dx, dy); std::swap(da, db); std::swap(n, m); }
+    const long long nbmax = 296;
+    ENSURE(gw, double, B_GAUSS, 2 * 64 + 3 * 64 * 64);
+    ENSURE(scr, double, B_GAUSS2, nbmax * d * d + 64);
+    double *mmu = gw, *mnu = gw + 64, *Smu = gw + 128, *Snu = Smu + 64 * 64, *A = Snu + 64 * 64;
+    ENSURE(flag, int, B_FLAG, 4);
+    CU(cudaMemsetAsync(flag, 0, sizeof(int), ctx->stream));
+    CU(launch_moments(dx, da, n, d, mmu, Smu, scr, nbmax * d * d, ctx->stream));
+    CU(launch_moments(dy, db, m, d, mnu, Snu, scr, nbmax * d * d, ctx->stream));
+    CU(launch_gauss_A(mmu, Smu, mnu, Snu, d, ridge_rel, A, flag, ctx->stream));
+    CU(launch_gauss_potential(dx, n, d, mmu, mnu, A, dpot, ctx->stream));
+    ctx->cnt.kernel_launches += 10;
+    CK(sg.flush());
+    CU(cudaMemcpyAsync(ctx->h_flag, flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    if (*ctx->h_flag) return fail(ctx, SK_ENONFINITE, "Newton-Schulz did not converge (degenerate covariance)");
+    *side = swap ? 1 : 0;
+    return SK_OK;
+}
+
+sk_status sinkhorn_init_gmm(sk_ctx *ctx, int64_t n, int64_t m, int32_t d, const float *x, const float *y,
+                            int32_t Kx, const float *wx, const float *mux, const float *covx, int32_t Ky,
+                            const float *wy, const float *muy, const float *covy, float eps,
+                            float inner_tol, int32_t inner_max_iter, float *pot, int32_t *side) {
+    if (!ctx) return SK_EINVAL;
+    if (n < 1 || m < 1 || d < 1 || d > 64 || !x || !y || !pot || !side)
+        return fail(ctx, SK_EINVAL, "bad arguments (d in [1,64])");
+    if (Kx < 1 || Ky < 1 || Kx > 64 || Ky > 64) return fail(ctx, SK_EINVAL, "1 <= K <= 64");
+    if (!wx || !mux || !covx || !wy || !muy || !covy) return fail(ctx, SK_EINVAL, "mixture parameters required");
+    if (!(eps > 0.f) || bad_scalar(eps) || !(inner_tol > 0.f) || inner_max_iter < 1)
+        return fail(ctx, SK_EINVAL, "eps, inner_tol > 0, inner_max_iter >= 1");
+    const bool swap = n > m;
+    Stager sg(ctx);
+    const float *dx, *dy, *dwx, *dmux, *dcovx, *dwy, *dmuy, *dcovy;
+    float *dpot;
+    CK(sg.in_t(x, (size_t)n * d, &dx));
+    CK(sg.in_t(y, (size_t)m * d, &dy));
+    CK(sg.in_t(wx, (size_t)Kx, &dwx));
+    CK(sg.in_t(mux, (size_t)Kx * d, &dmux));
+    CK(sg.in_t(covx, (size_t)Kx * d * d, &dcovx));
+    CK(sg.in_t(wy, (size_t)Ky, &dwy));
+    CK(sg.in_t(muy, (size_t)Ky * d, &dmuy));
+    CK(sg.in_t(covy, (size_t)Ky * d * d, &dcovy));
+    CK(sg.out_t(pot, (size_t)(swap ? m : n), &dpot));
+    CK(check_arrays(ctx, {{dx, n * d}, {dy, m * d}, {dmux, (long long)Kx * d}, {dmuy, (long long)Ky * d},
+                          {dcovx, (long long)Kx * d * d}, {dcovy, (long long)Ky * d * d}},
+                    {{dwx, Kx}, {dwy, Ky}}, "sinkhorn_init_gmm"));
+    if (swap) {
+        std::swap(dx, dy); std::swap(n, m); std::swap(Kx, Ky);
+        std::swap(dwx, dwy); std::swap(dmux, dmuy); std::swap(dcovx, dcovy);
+    }
+    ENSURE(work, double, B_GMM, gmm_work_doubles(d, Kx, Ky));
+    ENSURE(flag, int, B_FLAG, 4);
+    CU(cudaMemsetAsync(flag, 0, sizeof(int), ctx->stream));
+    CU(launch_gmm_init(dx, n, d, Kx, dwx, dmux, dcovx, Ky, dwy, dmuy, dcovy, eps, inner_tol, inner_max_iter,
+                       dpot, work, flag, ctx->stream));
+    ctx->cnt.kernel_launches += 5;
+    CK(sg.flush());
+    CU(cudaMemcpyAsync(ctx->h_flag, flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    if (*ctx->h_flag & 4) return fail(ctx, SK_EINVAL, "a mixture covariance is not positive definite");
+    if (*ctx->h_flag) return fail(ctx, SK_ENONFINITE, "GMM initializer failed (Newton-Schulz or K x K solve)");
+    *side = swap ? 1 : 0;
+    return SK_OK;
+}
+
+// forward
+sk_status solve_impl(sk_ctx *ctx, int64_t B, int64_t n, int64_t m, int32_t d, const float *x, long long xs,
+                     const float *y, long long ys, const float *a, long long as, const float *b, long long bs,
+                     float eps, float tol, int32_t max_iter, int32_t check_every, sk_cost_mode mode,
+                     const float *f_init, float *f, float *g, sk_report *rep);
+
+sk_status sinkhorn_init_subsample(sk_ctx *ctx, int64_t n, int64_t m, int32_t d, const float *x, const float *y,
+                                  int64_t ns, const int32_t *idx_x, int64_t ms, const int32_t *idx_y, float eps,
+                                  float inner_tol, int32_t inner_max_iter, float *pot, int32_t *side,
+                                  sk_report *inner) {
+    if (!ctx) return SK_EINVAL;
+    CK(validate_common(ctx, n, m, d, eps, inner_tol, inner_max_iter, 1));
+    if (!x || !y || !pot || !side || !idx_x || !idx_y) return fail(ctx, SK_EINVAL, "NULL argument");
+    if (ns < 1 || ms < 1 || ns > n || ms > m) return fail(ctx, SK_EINVAL, "1 <= ns <= n, 1 <= ms <= m");
+    const bool swap = n > m;
+    Stager sg(ctx);
+    const float *dx, *dy;
+    const int *dix, *diy;
+    float *dpot;
+    CK(sg.in_t(x, (size_t)n * d, &dx));
+    CK(sg.in_t(y, (size_t)m * d, &dy));
+    CK(sg.in_t(idx_x, (size_t)ns, &dix));
+    CK(sg.in_t(idx_y, (size_t)ms, &diy));
+    CK(sg.out_t(pot, (size_t)(swap ? m : n), &dpot));
+    CK(check_arrays(ctx, {{dx, n * d}, {dy, m * d}}, {}, "sinkhorn_init_subsample"));
+    {   // indices distinct and in range
+        ENSURE(flag, int, B_FLAG, 4);
+        ENSURE(mark, int, B_IDX, std::max(n, m));
+        CU(cudaMemsetAsync(flag, 0, sizeof(int), ctx->stream));
+        CU(launch_check_indices(dix, ns, n, flag, mark, ctx->stream));
+        CU(launch_check_indices(diy, ms, m, flag, mark, ctx->stream));
+        ctx->cnt.kernel_launches += 2;
+        CU(cudaMemcpyAsync(ctx->h_flag, flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+        CU(cudaStreamSynchronize(ctx->stream));
+        if (*ctx->h_flag) return fail(ctx, SK_EINVAL, "subsample indices out of range or repeated");
+    }
+    if (swap) { std::swap(dx, dy); std::swap(n, m); std::swap(dix, diy); std::swap(ns, ms); }
+    ENSURE(w, float, B_SUBW, ns * d);
+    ENSURE(z, float, B_SUBZ, ms * d);
+    ENSURE(fb, float, B_SUBF, ns);
+    ENSURE(gbv, float, B_SUBG, ms);
+    CU(launch_gather_rows(dx, dix, ns, d, w, ctx->stream));
+    CU(launch_gather_rows(dy, diy, ms, d, z, ctx->stream));
+    ctx->cnt.kernel_launches += 2;
+    // inner solve (uniform weights, same eps, inner_tol) -> g~ (Sec. 3.4)
+    sk_report rin{};
+    sk_status s = solve_impl(ctx, 1, ns, ms, d, w, 0, z, 0, nullptr, 0, nullptr, 0, eps, inner_tol,
+                             inner_max_iter, 1, SK_COST_ONLINE, nullptr, fb, gbv, &rin);
+    if (s != SK_OK && s != SK_ENONFINITE) return s;
+    if (inner) *inner = rin;
+    if (s == SK_ENONFINITE) return fail(ctx, SK_ENONFINITE, "inner subsample solve became non-finite");
+    // Eq. (8): one online LSE pass of all x against (z, g~): f0_i = eps log ms + |x_i|^2 - eps ln2 LSE2
+    const int D = lse_dpad(d);
+    const int tq = lse_tq(D);
+    const long long xt = lse_tiles(n, tq), zt = lse_tiles(ms, tq);
+    ENSURE(xpack, float, B_XPACK, xt * (D + 1) * tq);
+    ENSURE(xc, float, B_XC, n);
+    ENSURE(xnk, float, B_XNK, n);
+    ENSURE(xpot, float, B_XPOT, 2 * n);
+    ENSURE(ypack, float, B_YPACK, zt * (D + 1) * tq);
+    ENSURE(yc, float, B_YC, ms);
+    ENSURE(ynk, float, B_YNK, ms);
+    ENSURE(ypot, float, B_YPOT, 2 * ms);
+    ENSURE(status, DevStatus, B_STATUS, 1);
+    Side X{(int)n, d, D, tq, xpack, xc, xnk, {xpot, xpot + n}};
+    Side Z{(int)ms, d, D, tq, ypack, yc, ynk, {ypot, ypot + ms}};
+    CU(pack_side(X, dx, nullptr, 0.f, nullptr, eps, ctx->stream));   // c = |x|^2
+    CU(pack_side(Z, z, nullptr, 0.f, gbv, eps, ctx->stream));       // w = (g~ - |z|^2) kappa
+    const int occ = lse_occupancy_ctas(D);
+    const int R = D <= 4 ? 4 : (D <= 16 ? 2 : 1);
+    const int split = choose_split((n + 128LL * R - 1) / (128LL * R), zt, occ, 64);
+    ENSURE(part, float2, B_PART, (long long)split * n);
+    ENSURE(blke, double, B_BLKE, 2048);
+    ENSURE(blkb, int, B_BLKB, 2048);
+    CU(launch_status_init(status, 1, 1, 1.f, ctx->stream));
+    LsePass lp{&X, &Z, 1, 0, split, part, eps, nullptr};
+    CU(launch_lse(lp, ctx->stream));
+    MergePass mp{MERGE_OUT, &X, part, split, eps, nullptr, status, blke, blkb, dpot,
+                 (float)(eps * std::log((double)ms)), 0};
+    CU(launch_merge(mp, ctx->stream));
+    ctx->cnt.kernel_launches += 5;
+    CK(sg.flush());
+    CU(cudaMemcpyAsync(ctx->h_status, status, sizeof(DevStatus), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    if (ctx->h_status->nonfinite) return fail(ctx, SK_ENONFINITE, "extrapolated potential non-finite");
+    *side = swap ? 1 : 0;
+    return SK_OK;
+}
+
+sk_status solve_impl(sk_ctx *ctx, int64_t B, int64_t n, int64_t m, int32_t d, const float *x, long long xs,
+                     const float *y, long long ys, const float *a, long long as, const float *b, long long bs,
+                     float eps, float tol, int32_t max_iter, int32_t check_every, sk_cost_mode mode,
+                     const float *f_init, float *f, float *g, sk_report *rep) {
+    cudaStream_t st = ctx->stream;
+    const bool small = batched_supported(d, (int)n, (int)m) && (B > 1 || (double)n * m <= (double)(1 << 18));
+    if (small && mode != SK_COST_STORED) {
+        ENSURE(rp, char, B_REP, (size_t)B * (3 * sizeof(int) + sizeof(float) + sizeof(double)) + 64);
+        double *E = (double *)rp;
+        int *iters = (int *)(E + B), *conv = iters + B, *nonf = conv + B;
+        float *err = (float *)(nonf + B);
+        BatchLaunch L;
+        L.B = (int)B; L.n = (int)n; L.m = (int)m; L.d = d;
+        L.x = x; L.x_stride = xs; L.y = y; L.y_stride = ys;
+        L.a = a; L.a_stride = as; L.b = b; L.b_stride = bs;
+        L.finit = f_init; L.f = f; L.g = g; L.eps = eps; L.tol = tol;
+        L.max_iter = max_iter; L.check_every = check_every;
+        L.iters = iters; L.conv = conv; L.nonfinite = nonf; L.err = err; L.E = E;
+        CU(cudaEventRecord(ctx->ev0, st));
+        CU(launch_batched(L, st));
+        CU(cudaEventRecord(ctx->ev1, st));
+        ctx->cnt.kernel_launches++;
+        ctx->cnt.lse_launches++;
+        std::vector<char> h((size_t)B * (3 * sizeof(int) + sizeof(float) + sizeof(double)));
+        CU(cudaMemcpyAsync(h.data(), rp, h.size(), cudaMemcpyDeviceToHost, st));
+        CU(cudaStreamSynchronize(st));
+        float ms = 0.f;
+        CU(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+        if (ctx->timing) ctx->cnt.lse_ms += ms;
+        const double *hE = (const double *)h.data();
+        const int *hi = (const int *)(hE + B), *hc = hi + B, *hn = hc + B;
+        const float *he = (const float *)(hn + B);
+        int any_nf = 0;
+        for (long long p = 0; p < B; ++p) {
+            rep[p].iterations = hi[p];
+            rep[p].converged = hc[p];
+            rep[p].marginal_error = he[p];
+            rep[p].dual_objective = hE[p];
+            rep[p].build_ms = 0.0;
+            rep[p].solve_ms = ms;
+            any_nf |= hn[p];
+            ctx->cnt.lse_ex2 += (double)n * m * (2.0 * hi[p] + 1.0);
+        }
+        if (any_nf) return fail(ctx, SK_ENONFINITE, "potentials became non-finite");
+        return SK_OK;
+    }
+    for (long long p = 0; p < B; ++p) {
+        Problem P;
+        P.n = n; P.m = m; P.n_total = n; P.d = d;
+        P.x = x + p * xs; P.y = y + p * ys;
+        P.a = a ? a + p * as : nullptr; P.b = b ? b + p * bs : nullptr;
+        P.f_init = f_init ? f_init + p * n : nullptr;
+        P.eps = eps; P.tol = tol; P.max_iter = max_iter; P.check_every = check_every; P.mode = mode;
+        P.f = f + p * n; P.g = g + p * m;
+        P.rank = 0; P.world = 1;
+        CK(solve_multikernel(ctx, P, &rep[p]));
+    }
+    return SK_OK;
+}
+
+sk_status sinkhorn_solve(sk_ctx *ctx, int64_t B, int64_t n, int64_t m, int32_t d, const float *x,
+                         const float *y, int32_t y_shared, const float *a, const float *b, float eps,
+                         float tol, int32_t max_iter, int32_t check_every, sk_cost_mode mode,
+                         const float *f_init, const float *g_init, float *f, float *g, sk_report *rep) {
+    if (!ctx) return SK_EINVAL;
+    CK(validate_common(ctx, n, m, d, eps, tol, max_iter, check_every));
+    if (B < 1) return fail(ctx, SK_EINVAL, "B must be >= 1");
+    if (!x || !y || !f || !g || !rep) return fail(ctx, SK_EINVAL, "NULL argument");
+    if (f_init && g_init) return fail(ctx, SK_EINVAL, "at most one of f_init, g_init (P:84)");
+    if (mode < SK_COST_AUTO || mode > SK_COST_STORED) return fail(ctx, SK_EINVAL, "bad cost mode");
+    const long long ny = y_shared ? 1 : B;
+    Stager sg(ctx);
+    const float *dx, *dy, *da, *db, *dfi, *dgi;
+    float *df, *dg;
+    CK(sg.in_t(x, (size_t)B * n * d, &dx));
+    CK(sg.in_t(y, (size_t)ny * m * d, &dy));
+    CK(sg.in_t(a, (size_t)B * n, &da));
+    CK(sg.in_t(b, (size_t)ny * m, &db));
+    CK(sg.in_t(f_init, (size_t)B * n, &dfi));
+    CK(sg.in_t(g_init, (size_t)B * m, &dgi));
+    CK(sg.out_t(f, (size_t)B * n, &df));
+    CK(sg.out_t(g, (size_t)B * m, &dg));
+    CK(check_arrays(ctx, {{dx, B * n * d}, {dy, ny * m * d}, {dfi, B * n}, {dgi, B * m}},
+                    {{da, B * n}, {db, ny * m}}, "sinkhorn_solve"));
+    for (long long p = 0; p < B; ++p) rep[p] = sk_report{};
+    sk_status s;
+    if (dgi)  // transposed problem: x<->y, a<->b, f<->g
+        s = solve_impl(ctx, B, m, n, d, dy, y_shared ? 0 : m * d, dx, n * d, db, y_shared ? 0 : m, da, n, eps,
+                       tol, max_iter, check_every, mode, dgi, dg, df, rep);
+    else
+        s = solve_impl(ctx, B, n, m, d, dx, n * d, dy, y_shared ? 0 : m * d, da, n, db, y_shared ? 0 : m, eps,
+                       tol, max_iter, check_every, mode, dfi, df, dg, rep);
+    if (s != SK_OK && s != SK_ENONFINITE) return s;
+    sk_status s2 = sg.flush();
+    CU(cudaStreamSynchronize(ctx->stream));
+    return s != SK_OK ? s : s2;
+}
+
+sk_status sinkhorn_solve_sharded(sk_ctx *ctx, int64_t n_total, int64_t row0, int64_t n_local, int64_t m,
+                                 int32_t d, const float *x_local, const float *y, const float *a_local,
+                                 const float *b, float eps, float tol, int32_t max_iter, int32_t check_every,
+                                 sk_cost_mode mode, const float *f_init_local, float *f_local, float *g,
+                                 sk_report *rep) {
+    if (!ctx) return SK_EINVAL;
+    CK(validate_common(ctx, n_local, m, d, eps, tol, max_iter, check_every));
+    if (!x_local || !y || !f_local || !g || !rep) return fail(ctx, SK_EINVAL, "NULL argument");
+    int64_t r0, nl;
+    CK(sk_shard_rows(n_total, ctx->rank, ctx->world, &r0, &nl));
+    if (r0 != row0 || nl != n_local)
+        return fail(ctx, SK_EINVAL, "rank %d must own rows [%lld, %lld) (sk_shard_rows)", ctx->rank,
+                    (long long)r0, (long long)(r0 + nl));
+    if (ctx->world > 1 && !ctx->comm) return fail(ctx, SK_ENCCL, "sk_comm_init was not called");
+    Stager sg(ctx);
+    const float *dx, *dy, *da, *db, *dfi;
+    float *df, *dg;
+    CK(sg.in_t(x_local, (size_t)n_local * d, &dx));
+    CK(sg.in_t(y, (size_t)m * d, &dy));
+    CK(sg.in_t(a_local, (size_t)n_local, &da));
+    CK(sg.in_t(b, (size_t)m, &db));
+    CK(sg.in_t(f_init_local, (size_t)n_local, &dfi));
+    CK(sg.out_t(f_local, (size_t)n_local, &df));
+    CK(sg.out_t(g, (size_t)m, &dg));
+    CK(check_arrays(ctx, {{dx, n_local * d}, {dy, m * d}, {dfi, n_local}}, {{da, n_local}, {db, m}},
+                    "sinkhorn_solve_sharded"));
+    *rep = sk_report{};
+    Problem P;
+    P.n = n_local; P.m = m; P.n_total = n_total; P.d = d;
+    P.x = dx; P.y = dy; P.a = da; P.b = db; P.f_init = dfi;
+    P.eps = eps; P.tol = tol; P.max_iter = max_iter; P.check_every = check_every; P.mode = mode;
+    P.f = df; P.g = dg;
+    P.rank = ctx->rank; P.world = ctx->world;
+    sk_status s = solve_multikernel(ctx, P, rep);
+    if (s != SK_OK && s != SK_ENONFINITE) return s;
+    sk_status s2 = sg.flush();
+    CU(cudaStreamSynchronize(ctx->stream));
+    return s != SK_OK ? s : s2;
+}
+
+}  // extern "C"

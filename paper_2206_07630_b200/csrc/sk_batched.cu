@@ -1,0 +1,251 @@
+// sk_batched.cu — K13: the on-chip Sinkhorn solver for batches of small problems.
+//
+// One CTA solves one problem end to end ("compounded when running
+// many thousands of OT problems"): x, y, both potentials and the packed
+// reduction operands live in shared memory; every sweep is
+//     column pass  g_j <- eps log b_j - eps LSE_i((f_i - C_ij)/eps)   (Alg. 1 l.5, R-1)
+//     [error check err_l = sum_j b_j |expm1((g_j^l - g_j^{l+1})/eps)| (H5,
+//      threshold appendix) every check_every sweeps]
+//     row pass     f_i <- eps log a_i - eps LSE_j((g_j - C_ij)/eps)   (Alg. 1 l.4)
+// with C_ij = ||x_i||^2 + ||y_j||^2 - 2<x_i, y_j> evaluated on the fly (FFMA2),
+// and per-problem convergence (each CTA leaves its loop independently).
+// Deterministic: every output is produced by one thread in a fixed order and the
+// block reductions have a fixed shape.
+#include "sk_internal.h"
+#include "sk_lse_tile.cuh"
+
+namespace sk {
+
+constexpr int kBT = 256;  // threads per CTA
+
+struct BatchArgs {
+    const float *x; long long xs;   // per-problem strides in floats (0 = shared)
+    const float *y; long long ys;
+    const float *a; long long as;   // nullable (uniform)
+    const float *b; long long bs;
+    const float *finit; long long fs;  // nullable
+    float *f; float *g;             // B x n, B x m
+    int n, m;
+    float eps, tol;
+    int max_iter, check_every;
+    int *iters, *conv, *nonfinite;
+    float *err;
+    double *E;
+};
+
+__host__ __device__ inline int round_up(int v, int a) { return (v + a - 1) / a * a; }
+
+size_t batched_smem_bytes(int D, int n, int m) {
+    const int Np = round_up(n, kChunk), Mp = round_up(m, kChunk);
+    size_t floats = (size_t)(D + 1) * (Np + Mp)   // packed coords + w, both sides
+                    + 2 * (size_t)(n + m)         // finalize constant c and ||.||^2 kappa
+                    + 2 * (size_t)(n + m);        // double-buffered f and g
+    return floats * sizeof(float) + 64 * sizeof(double);
+}
+
+// One LSE pass over all P points owned by this CTA (R per thread per round).
+// out(p, M, S) is called for every valid p by the thread that owns it.
+template <int D, int R, typename Out>
+__device__ __forceinline__ void onchip_pass(const float *__restrict__ pc, int pstride, int P,
+                                            const float *__restrict__ qc, const float *__restrict__ qw,
+                                            int Qp, float tk, Out out) {
+    for (int pb = 0; pb < P; pb += R * kBT) {
+        float2 pd[R][D];
+        float M[R];
+        float2 S[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int p = pb + r * kBT + threadIdx.x;
+#pragma unroll
+            for (int k = 0; k < D; ++k) {
+                const float v = p < P ? pc[k * pstride + p] * tk : 0.f;
+                pd[r][k] = make_float2(v, v);
+            }
+            M[r] = -INFINITY;
+            S[r] = make_float2(0.f, 0.f);
+        }
+        for (int q = 0; q < Qp; q += kChunk) lse_chunk<D, R>(qc, Qp, qw, q, pd, M, S);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int p = pb + r * kBT + threadIdx.x;
+            if (p < P) out(p, M[r], S[r].x + S[r].y);
+        }
+    }
+}
+
+template <int D, int R>
+__global__ void __launch_bounds__(kBT) k_batched(BatchArgs A) {
+    extern __shared__ __align__(16) float sm[];
+    const int n = A.n, m = A.m;
+    const int Np = round_up(n, kChunk), Mp = round_up(m, kChunk);
+    const int prob = blockIdx.x;
+    const float eps = A.eps;
+    const float kap = kLog2e / eps;     // log2(e)/eps
+    const float tk = 2.f * kap;         // scale of the cross term
+    const float epsln2 = eps * kLn2;
+
+    float *xq = sm;                     // [D][Np]
+    float *wx = xq + D * Np;            // [Np]   (f_i - |x_i|^2) kappa
+    float *yq = wx + Np;                // [D][Mp]
+    float *wy = yq + D * Mp;            // [Mp]   (g_j - |y_j|^2) kappa
+    float *cx = wy + Mp;                // [n]    eps log a_i + |x_i|^2
+    float *nxk = cx + n;                // [n]    |x_i|^2 kappa
+    float *cy = nxk + n;                // [m]
+    float *nyk = cy + m;                // [m]
+    float *fb = nyk + m;                // [2][n]
+    float *gb = fb + 2 * n;             // [2][m]
+    double *red = reinterpret_cast<double *>(gb + 2 * m + ((2 * m) & 1));  // scratch
+    int *redi = reinterpret_cast<int *>(red + 32);
+
+    const float *x = A.x + prob * A.xs;
+    const float *y = A.y + prob * A.ys;
+    const float *a = A.a ? A.a + prob * A.as : nullptr;
+    const float *b = A.b ? A.b + prob * A.bs : nullptr;
+    const float loga_u = (float)(-log((double)n)), logb_u = (float)(-log((double)m));
+
+    // ---- load + precompute (K1)
+    for (int i = threadIdx.x; i < Np; i += kBT) {
+        if (i < n) {
+            float s = 0.f;
+#pragma unroll
+            for (int k = 0; k < D; ++k) {
+                const float v = x[(size_t)i * D + k];
+                xq[k * Np + i] = v;
+                s = fmaf(v, v, s);
+            }
+            const float la = a ? logf(a[i]) : loga_u;
+            cx[i] = fmaf(eps, la, s);
+            nxk[i] = s * kap;
+            const float f0 = A.finit ? A.finit[(size_t)prob * A.fs + i] : 0.f;
+            fb[i] = f0;
+            wx[i] = fmaf(f0, kap, -nxk[i]);
+        } else {
+#pragma unroll
+            for (int k = 0; k < D; ++k) xq[k * Np + i] = 0.f;
+            wx[i] = -INFINITY;
+        }
+    }
+    for (int j = threadIdx.x; j < Mp; j += kBT) {
+        if (j < m) {
+            float s = 0.f;
+#pragma unroll
+            for (int k = 0; k < D; ++k) {
+                const float v = y[(size_t)j * D + k];
+                yq[k * Mp + j] = v;
+                s = fmaf(v, v, s);
+            }
+            const float lb = b ? logf(b[j]) : logb_u;
+            cy[j] = fmaf(eps, lb, s);
+            nyk[j] = s * kap;
+            gb[j] = 0.f;  // g^(0) = 0 (only f^(0) is needed)
+        } else {
+#pragma unroll
+            for (int k = 0; k < D; ++k) yq[k * Mp + j] = 0.f;
+            wy[j] = -INFINITY;
+        }
+    }
+    __syncthreads();
+
+    int l = 0, cur = 0, conv = 0, nonfin = 0;
+    float err = INFINITY;
+    for (;;) {
+        // ---- column pass: g^{l+1} (P = y, Q = x)
+        const bool check = l >= 1 && (l % A.check_every == 0 || l == A.max_iter);
+        double e_loc = 0.0;
+        int bad = 0;
+        float *gold = gb + cur * m, *gnew = gb + (cur ^ 1) * m;
+        onchip_pass<D, R>(yq, Mp, m, xq, wx, Np, tk, [&](int j, float Mv, float Sv) {
+            const float gn = cy[j] - epsln2 * (Mv + log2f(Sv));
+            gnew[j] = gn;
+            wy[j] = fmaf(gn, kap, -nyk[j]);
+            bad |= !isfinite(gn);
+            if (check) {
+                const float bj = b ? b[j] : __expf(logb_u);
+                e_loc += (double)bj * fabs((double)expm1f((gold[j] - gn) / eps));
+            }
+        });
+        const double e_tot = block_sum_d<kBT>(e_loc, red);
+        const int any_bad = block_or<kBT>(bad, redi);
+        if (any_bad) { nonfin = 1; break; }
+        if (check) {
+            err = (float)e_tot;
+            if (err < A.tol) { conv = 1; break; }
+            if (l == A.max_iter) break;
+        }
+        // ---- row pass: f^{l+1} (P = x, Q = y); wy is visible after the block reductions' barriers
+        float *fnew = fb + (cur ^ 1) * n;
+        bad = 0;
+        onchip_pass<D, R>(xq, Np, n, yq, wy, Mp, tk, [&](int i, float Mv, float Sv) {
+            const float fn = cx[i] - epsln2 * (Mv + log2f(Sv));
+            fnew[i] = fn;
+            wx[i] = fmaf(fn, kap, -nxk[i]);
+            bad |= !isfinite(fn);
+        });
+        if (block_or<kBT>(bad, redi)) { nonfin = 1; break; }
+        cur ^= 1;
+        ++l;
+    }
+
+    // ---- epilogue: (f^l, g^l), E = <f,a> + <g,b> - eps sum(a) (Eq. 2 after an f-update), report
+    const float *fo = fb + cur * n, *go = gb + cur * m;
+    double s = 0.0;
+    for (int i = threadIdx.x; i < n; i += kBT) {
+        A.f[(size_t)prob * n + i] = fo[i];
+        const double ai = a ? (double)a[i] : 1.0 / n;
+        s += (double)fo[i] * ai - (double)eps * ai;
+    }
+    for (int j = threadIdx.x; j < m; j += kBT) {
+        A.g[(size_t)prob * m + j] = go[j];
+        s += (double)go[j] * (b ? (double)b[j] : 1.0 / m);
+    }
+    const double E = block_sum_d<kBT>(s, red);
+    if (threadIdx.x == 0) {
+        A.iters[prob] = l;
+        A.conv[prob] = conv;
+        A.nonfinite[prob] = nonfin;
+        A.err[prob] = err;
+        A.E[prob] = E;
+    }
+}
+
+template <int D, int R>
+static cudaError_t launch_batched_t(const BatchArgs &A, int B, cudaStream_t st) {
+    const size_t smem = batched_smem_bytes(D, A.n, A.m);
+    cudaError_t e = cudaFuncSetAttribute(k_batched<D, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    k_batched<D, R><<<B, kBT, smem, st>>>(A);
+    return cudaGetLastError();
+}
+
+template <int D>
+static cudaError_t launch_batched_d(const BatchArgs &A, int B, cudaStream_t st) {
+    const int P = A.n > A.m ? A.n : A.m;
+    if (P > 2 * kBT) return launch_batched_t<D, 4>(A, B, st);
+    if (P > kBT) return launch_batched_t<D, 2>(A, B, st);
+    return launch_batched_t<D, 1>(A, B, st);
+}
+
+bool batched_supported(int d, int n, int m) {
+    return d >= 1 && d <= 4 && batched_smem_bytes(d, n, m) <= 200 * 1024;
+}
+
+cudaError_t launch_batched(const BatchLaunch &L, cudaStream_t st) {
+    BatchArgs A;
+    A.x = L.x; A.xs = L.x_stride; A.y = L.y; A.ys = L.y_stride;
+    A.a = L.a; A.as = L.a_stride; A.b = L.b; A.bs = L.b_stride;
+    A.finit = L.finit; A.fs = L.n;
+    A.f = L.f; A.g = L.g;
+    A.n = L.n; A.m = L.m; A.eps = L.eps; A.tol = L.tol;
+    A.max_iter = L.max_iter; A.check_every = L.check_every;
+    A.iters = L.iters; A.conv = L.conv; A.nonfinite = L.nonfinite; A.err = L.err; A.E = L.E;
+    switch (L.d) {
+        case 1: return launch_batched_d<1>(A, L.B, st);
+        case 2: return launch_batched_d<2>(A, L.B, st);
+        case 3: return launch_batched_d<3>(A, L.B, st);
+        case 4: return launch_batched_d<4>(A, L.B, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace sk

@@ -1,0 +1,131 @@
+// sk_common.cuh — shared device helpers of the sm_100a Sinkhorn library.
+// (PTX wrappers: MUFU ex2, packed FP32x2 FFMA2/FADD2, mbarrier + 1D bulk TMA.)
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace sk {
+
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLn2 = 0.6931471805599453f;
+constexpr double kLn2d = 0.6931471805599453094;
+constexpr double kLog2ed = 1.4426950408889634074;
+
+// ---------------------------------------------------------------- MUFU.EX2
+__device__ __forceinline__ float ex2(float x) {
+    float r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+// ---------------------------------------------------------- packed f32x2 ops
+// Blackwell FFMA2 / FADD2: two fp32 lanes per instruction (sm_100+).
+union f2u {
+    float2 f;
+    unsigned long long u;
+};
+
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+    f2u A, B, C, D;
+    A.f = a; B.f = b; C.f = c;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(D.u) : "l"(A.u), "l"(B.u), "l"(C.u));
+    return D.f;
+}
+
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+    f2u A, B, D;
+    A.f = a; B.f = b;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(D.u) : "l"(A.u), "l"(B.u));
+    return D.f;
+}
+
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
+    f2u A, B, D;
+    A.f = a; B.f = b;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(D.u) : "l"(A.u), "l"(B.u));
+    return D.f;
+}
+
+// ------------------------------------------------------- (max, sum) merging
+// Online log-sum-exp state in log2 units: value = M + log2(S).
+__device__ __forceinline__ void lse_merge(float &M, float &S, float M2, float S2) {
+    float Mn = fmaxf(M, M2);
+    if (Mn == -INFINITY) return;  // both empty
+    S = S * ex2(M - Mn) + S2 * ex2(M2 - Mn);
+    M = Mn;
+}
+
+// ----------------------------------------------------- mbarrier + bulk copy
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+// 1D bulk TMA: global -> shared, completion via mbarrier transaction count.
+__device__ __forceinline__ void bulk_g2s(void *dst_smem, const void *src_gmem, uint32_t bytes,
+                                         uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst_smem)),
+        "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    uint32_t addr = smem_u32(bar);
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(addr),
+        "r"(parity)
+        : "memory");
+}
+
+// --------------------------------------------------------- block reductions
+// Deterministic (fixed-order) block sum of doubles; all threads get the result.
+template <int NT>
+__device__ __forceinline__ double block_sum_d(double v, double *scratch /* NT/32 */) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) scratch[w] = v;
+    __syncthreads();
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < NT / 32; ++i) s += scratch[i];
+    return s;
+}
+
+template <int NT>
+__device__ __forceinline__ int block_or(int v, int *scratch /* NT/32 */) {
+    v = __any_sync(0xffffffffu, v);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) scratch[w] = v;
+    __syncthreads();
+    int s = 0;
+#pragma unroll
+    for (int i = 0; i < NT / 32; ++i) s |= scratch[i];
+    return s;
+}
+
+}  // namespace sk

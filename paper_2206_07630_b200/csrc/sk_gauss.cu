@@ -1,0 +1,458 @@
+// sk_gauss.cu — K10 (Gaussian initializer) and K11 (GMM initializer).
+//
+// Gaussian (Sec. 3.2):
+//   moments  m = sum_i w_i x_i,  S = sum_i w_i (x_i - m)(x_i - m)^T (+ ridge, R-11)
+//            two passes, fp64 per-block partials, fixed-order final sums;
+//   A = S_mu^{-1/2} (S_mu^{1/2} S_nu S_mu^{1/2})^{1/2} S_mu^{-1/2}
+//            with fp64 coupled Newton-Schulz square roots (budget R-12)
+//            in one CTA;
+//   f*(x) = ||x||^2 - (x - m_mu)^T A (x - m_mu) - 2 m_nu^T x   (R-4).
+// GMM (Sec. 3.3):
+//   C~_kl = ||m_k - m'_l||^2 + tr(S_k + S'_l - 2 (S_k^{1/2} S'_l S_k^{1/2})^{1/2})  (Eq. 6)
+//            one CTA per square root (batched NS);
+//   f~ from the K x K entropic problem at the same eps (R-13), fp64, one CTA;
+//   f^(0)(x) = sum_k f~_k p_k(x),  p_k = alpha_k N(x; m_k, S_k) / sum_l (...)  (Eq. 7),
+//            log-domain with Cholesky factors, fp64.
+#include "sk_internal.h"
+#include "sk_common.cuh"
+
+namespace sk {
+
+constexpr int kGT = 256;
+
+// ------------------------------------------------------------- moments
+// out[blk][E]: E = d (pass 1, mean == nullptr) or d*d (pass 2, centred by mean).
+__global__ void __launch_bounds__(kGT) k_moment_partials(const float *__restrict__ x,
+                                                         const float *__restrict__ w, long long n,
+                                                         int d, const double *__restrict__ mean,
+                                                         double *out) {
+    constexpr int CH = 64;
+    extern __shared__ double xs[];  // [CH][d] weighted/centred chunk, then [CH] weights
+    double *ws = xs + CH * d;
+    const int E = mean ? d * d : d;
+    const long long per = (n + gridDim.x - 1) / gridDim.x;
+    const long long lo = blockIdx.x * per, hi = min(n, lo + per);
+    double acc[16];
+#pragma unroll
+    for (int t = 0; t < 16; ++t) acc[t] = 0.0;
+    for (long long c0 = lo; c0 < hi; c0 += CH) {
+        const int cnt = (int)min((long long)CH, hi - c0);
+        __syncthreads();
+        for (int t = threadIdx.x; t < cnt * d; t += kGT) {
+            const int r = t / d, k = t % d;
+            const double v = x[(c0 + r) * d + k];
+            xs[r * d + k] = mean ? v - mean[k] : v;
+        }
+        for (int r = threadIdx.x; r < cnt; r += kGT) ws[r] = w ? (double)w[c0 + r] : 1.0 / n;
+        __syncthreads();
+#pragma unroll
+        for (int t = 0; t < 16; ++t) {
+            const int e = threadIdx.x + t * kGT;
+            if (e >= E) break;
+            double s = 0.0;
+            if (mean) {
+                const int k = e / d, l = e % d;
+                for (int r = 0; r < cnt; ++r) s += ws[r] * xs[r * d + k] * xs[r * d + l];
+            } else {
+                for (int r = 0; r < cnt; ++r) s += ws[r] * xs[r * d + e];
+            }
+            acc[t] += s;
+        }
+    }
+#pragma unroll
+    for (int t = 0; t < 16; ++t) {
+        const int e = threadIdx.x + t * kGT;
+        if (e < E) out[(long long)blockIdx.x * E + e] = acc[t];
+    }
+}
+
+__global__ void k_reduce_cols(const double *in, int nb, int E, double *out) {
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int b = 0; b < nb; ++b) s += in[(long long)b * E + e];
+        out[e] = s;
+    }
+}
+
+cudaError_t launch_moments(const float *x, const float *w, long long n, int d, double *mean,
+                           double *cov, double *scratch, long long scratch_doubles, cudaStream_t st) {
+    if (d > 64) return cudaErrorInvalidValue;
+    long long nb = (n + 4095) / 4096;
+    if (nb > 296) nb = 296;
+    if (nb * d * d > scratch_doubles) nb = scratch_doubles / (d * d);
+    if (nb < 1) return cudaErrorInvalidValue;
+    const size_t smem = (64 * (size_t)d + 64) * sizeof(double);
+    k_moment_partials<<<(int)nb, kGT, smem, st>>>(x, w, n, d, nullptr, scratch);
+    k_reduce_cols<<<1, 256, 0, st>>>(scratch, (int)nb, d, mean);
+    k_moment_partials<<<(int)nb, kGT, smem, st>>>(x, w, n, d, mean, scratch);
+    k_reduce_cols<<<(d * d + 255) / 256, 256, 0, st>>>(scratch, (int)nb, d * d, cov);
+    return cudaGetLastError();
+}
+
+// ----------------------------------------------------- fp64 dense helpers
+// C = A * B (d x d, smem), all threads of the block; C must not alias A or B.
+__device__ void mm(const double *A, const double *B, double *C, int d) {
+    for (int e = threadIdx.x; e < d * d; e += blockDim.x) {
+        const int i = e / d, j = e % d;
+        double s = 0.0;
+        for (int k = 0; k < d; ++k) s += A[i * d + k] * B[k * d + j];
+        C[e] = s;
+    }
+    __syncthreads();
+}
+
+__device__ double block_sum_any(double v, double *red) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    double s = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
+    __syncthreads();
+    return s;
+}
+
+// Coupled Newton-Schulz: Y -> M^{1/2}, Z -> M^{-1/2} for SPD M (d x d, smem).
+// Y_0 = M/||M||_F, Z_0 = I;  T = (3I - Z Y)/2;  Y <- Y T;  Z <- T Z.
+// Stops when ||Z Y - I||_F < 1e-13 * d or the residual stagnates below 1e-7; max 100 sweeps
+// (R-12).  Small eigenvalues lam of M/||M||_F need ~log(1/lam)/log(2.25) sweeps to enter the
+// quadratic phase.
+// Work: T, U (d x d).  Returns the final residual.
+__device__ double ns_sqrt(const double *M, double *Y, double *Z, double *T, double *U, int d,
+                          double *red) {
+    double fr = 0.0;
+    for (int e = threadIdx.x; e < d * d; e += blockDim.x) fr += M[e] * M[e];
+    const double nrm = sqrt(block_sum_any(fr, red));
+    for (int e = threadIdx.x; e < d * d; e += blockDim.x) {
+        Y[e] = M[e] / nrm;
+        Z[e] = (e / d == e % d) ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    double res = INFINITY, prev = INFINITY;
+    for (int it = 0; it < 100; ++it) {
+        mm(Z, Y, T, d);  // T = Z Y
+        double r = 0.0;
+        for (int e = threadIdx.x; e < d * d; e += blockDim.x) {
+            const double v = T[e] - ((e / d == e % d) ? 1.0 : 0.0);
+            r += v * v;
+            T[e] = ((e / d == e % d) ? 1.5 : 0.0) - 0.5 * T[e];
+        }
+        res = sqrt(block_sum_any(r, red));
+        // converged, or stagnated at the fp64 rounding floor (quadratic phase reached)
+        if (res < 1e-13 * d || (res < 1e-7 && res > 0.5 * prev)) break;
+        prev = res;
+        mm(Y, T, U, d);  // U = Y T
+        for (int e = threadIdx.x; e < d * d; e += blockDim.x) Y[e] = U[e];
+        __syncthreads();
+        mm(T, Z, U, d);  // U = T Z
+        for (int e = threadIdx.x; e < d * d; e += blockDim.x) Z[e] = U[e];
+        __syncthreads();
+    }
+    const double sq = sqrt(nrm);
+    for (int e = threadIdx.x; e < d * d; e += blockDim.x) {
+        Y[e] *= sq;
+        Z[e] /= sq;
+    }
+    __syncthreads();
+    return res;
+}
+
+__device__ void symmetrize(double *A, int d) {
+    for (int e = threadIdx.x; e < d * d; e += blockDim.x) {
+        const int i = e / d, j = e % d;
+        if (i < j) {
+            const double v = 0.5 * (A[i * d + j] + A[j * d + i]);
+            A[i * d + j] = v;
+            A[j * d + i] = v;
+        }
+    }
+    __syncthreads();
+}
+
+// One CTA: ridge, NS square roots, A.  cov_* are modified in place (ridge added).
+__global__ void __launch_bounds__(kGT) k_gauss_A(double *cov_mu, double *cov_nu, int d, float ridge_rel,
+                                                  double *Aout, int *ns_fail) {
+    extern __shared__ double sm[];
+    __shared__ double red[kGT / 32];
+    const int dd = d * d;
+    double *Smu = sm, *Snu = sm + dd, *R = sm + 2 * dd, *Ri = sm + 3 * dd, *T = sm + 4 * dd,
+           *U = sm + 5 * dd;
+    double tr_mu = 0.0, tr_nu = 0.0;
+    for (int k = 0; k < d; ++k) { tr_mu += cov_mu[k * d + k]; tr_nu += cov_nu[k * d + k]; }
+    for (int e = threadIdx.x; e < dd; e += blockDim.x) {
+        const bool diag = e / d == e % d;
+        Smu[e] = cov_mu[e] + (diag ? ridge_rel * tr_mu / d : 0.0);
+        Snu[e] = cov_nu[e] + (diag ? ridge_rel * tr_nu / d : 0.0);
+    }
+    __syncthreads();
+    symmetrize(Smu, d);
+    symmetrize(Snu, d);
+    const double r1 = ns_sqrt(Smu, R, Ri, T, U, d, red);  // R = S_mu^{1/2}, Ri = S_mu^{-1/2}
+    mm(R, Snu, T, d);                                     // T = R S_nu
+    double *Mm = Smu;                                     // S_mu no longer needed
+    mm(T, R, Mm, d);                                      // Mm = R S_nu R
+    symmetrize(Mm, d);
+    double *Q = Snu, *Qi = R;                             // S_nu, R no longer needed
+    const double r2 = ns_sqrt(Mm, Q, Qi, T, U, d, red);  // Q = Mm^{1/2}
+    mm(Ri, Q, T, d);
+    mm(T, Ri, U, d);                                      // A = Ri Q Ri
+    symmetrize(U, d);
+    for (int e = threadIdx.x; e < dd; e += blockDim.x) Aout[e] = U[e];
+    if (threadIdx.x == 0) *ns_fail = (r1 > 1e-6 || r2 > 1e-6 || !isfinite(r1) || !isfinite(r2));
+}
+
+cudaError_t launch_gauss_A(const double *mean_mu, double *cov_mu, const double *mean_nu,
+                           double *cov_nu, int d, float ridge_rel, double *A, int *ns_fail,
+                           cudaStream_t st) {
+    (void)mean_mu; (void)mean_nu;
+    const size_t smem = 6 * (size_t)d * d * sizeof(double);
+    cudaError_t e = cudaFuncSetAttribute(k_gauss_A, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k_gauss_A<<<1, kGT, smem, st>>>(cov_mu, cov_nu, d, ridge_rel, A, ns_fail);
+    return cudaGetLastError();
+}
+
+// f*(x_i) in fp64, thread per point (d <= 64; A, means cached in smem).
+__global__ void __launch_bounds__(kGT) k_gauss_pot(const float *__restrict__ x, long long n, int d,
+                                                    const double *__restrict__ mmu,
+                                                    const double *__restrict__ mnu,
+                                                    const double *__restrict__ A, float *pot) {
+    extern __shared__ double s[];
+    double *sA = s, *smu = s + d * d, *snu = smu + d;
+    for (int e = threadIdx.x; e < d * d; e += blockDim.x) sA[e] = A[e];
+    for (int k = threadIdx.x; k < d; k += blockDim.x) { smu[k] = mmu[k]; snu[k] = mnu[k]; }
+    __syncthreads();
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const float *xi = x + i * d;
+        double nx = 0.0, lin = 0.0, quad = 0.0;
+        for (int k = 0; k < d; ++k) {
+            const double xk = xi[k];
+            nx += xk * xk;
+            lin += snu[k] * xk;
+            const double ck = xk - smu[k];
+            double row = 0.0;
+            for (int l = 0; l < d; ++l) row += sA[k * d + l] * ((double)xi[l] - smu[l]);
+            quad += ck * row;
+        }
+        pot[i] = (float)(nx - quad - 2.0 * lin);
+    }
+}
+
+cudaError_t launch_gauss_potential(const float *x, long long n, int d, const double *m_mu,
+                                   const double *m_nu, const double *A, float *pot, cudaStream_t st) {
+    const size_t smem = ((size_t)d * d + 2 * d) * sizeof(double);
+    cudaError_t e = cudaFuncSetAttribute(k_gauss_pot, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    long long b = (n + kGT - 1) / kGT;
+    k_gauss_pot<<<(int)(b > 148 * 8 ? 148 * 8 : b), kGT, smem, st>>>(x, n, d, m_mu, m_nu, A, pot);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ GMM
+// work layout (doubles): R [Kx][d*d] (S_k^{1/2}), Linv [Kx][d*d], logdet [Kx], C [Kx*Ky], ft [Kx]
+size_t gmm_work_doubles(int d, int Kx, int Ky) {
+    return (size_t)2 * Kx * d * d + Kx + (size_t)Kx * Ky + Kx;
+}
+
+__global__ void __launch_bounds__(kGT) k_gmm_sqrt(const float *covx, int d, double *R, int *flags) {
+    extern __shared__ double sm[];
+    __shared__ double red[kGT / 32];
+    const int dd = d * d, k = blockIdx.x;
+    double *M = sm, *Y = sm + dd, *Z = sm + 2 * dd, *T = sm + 3 * dd, *U = sm + 4 * dd;
+    for (int e = threadIdx.x; e < dd; e += blockDim.x) M[e] = covx[(long long)k * dd + e];
+    __syncthreads();
+    symmetrize(M, d);
+    const double r = ns_sqrt(M, Y, Z, T, U, d, red);
+    for (int e = threadIdx.x; e < dd; e += blockDim.x) R[(long long)k * dd + e] = Y[e];
+    if (threadIdx.x == 0 && (r > 1e-6 || !isfinite(r))) atomicOr(flags, 1);
+}
+
+__global__ void __launch_bounds__(kGT) k_gmm_bures(const float *mux, const float *covx, int Kx,
+                                                    const float *muy, const float *covy, int Ky, int d,
+                                                    const double *R, double *C, int *flags) {
+    extern __shared__ double sm[];
+    __shared__ double red[kGT / 32];
+    const int dd = d * d, k = blockIdx.x / Ky, l = blockIdx.x % Ky;
+    double *Sy = sm, *Rk = sm + dd, *M = sm + 2 * dd, *T = sm + 3 * dd, *U = sm + 4 * dd;
+    for (int e = threadIdx.x; e < dd; e += blockDim.x) {
+        Sy[e] = covy[(long long)l * dd + e];
+        Rk[e] = R[(long long)k * dd + e];
+    }
+    __syncthreads();
+    symmetrize(Sy, d);
+    mm(Rk, Sy, T, d);
+    mm(T, Rk, M, d);
+    symmetrize(M, d);
+    double *Y = Sy, *Z = Rk;  // free after M is formed
+    const double r = ns_sqrt(M, Y, Z, T, U, d, red);
+    if (threadIdx.x == 0) {
+        double tr = 0.0, dm = 0.0;
+        for (int i = 0; i < d; ++i) {
+            tr += (double)covx[(long long)k * dd + i * d + i] + (double)covy[(long long)l * dd + i * d + i]
+                  - 2.0 * Y[i * d + i];
+            const double t = (double)mux[k * d + i] - (double)muy[l * d + i];
+            dm += t * t;
+        }
+        C[k * Ky + l] = dm + tr;
+        if (r > 1e-6 || !isfinite(r)) atomicOr(flags, 1);
+    }
+}
+
+// K x K entropic OT in fp64 (Alg. 1, g-then-f, explicit error every sweep), one CTA.
+__global__ void __launch_bounds__(kGT) k_gmm_sinkhorn(const double *C, int Kx, int Ky, const float *wx,
+                                                       const float *wy, float eps_f, float tol, int max_iter,
+                                                       double *ft, int *flags) {
+    __shared__ double f[64], g[64], rs[64], cs[64];
+    __shared__ double red[kGT / 32];
+    __shared__ int s_stop;
+    const double eps = eps_f;
+    for (int i = threadIdx.x; i < 64; i += blockDim.x) { f[i] = 0.0; g[i] = 0.0; }
+    __syncthreads();
+    int it = 0;
+    for (;;) {
+        ++it;
+        for (int j = threadIdx.x; j < Ky; j += blockDim.x) {   // g-update
+            double mx = -INFINITY;
+            for (int i = 0; i < Kx; ++i) mx = fmax(mx, (f[i] - C[i * Ky + j]) / eps);
+            double s = 0.0;
+            for (int i = 0; i < Kx; ++i) s += exp((f[i] - C[i * Ky + j]) / eps - mx);
+            g[j] = eps * log((double)wy[j]) - eps * (mx + log(s));
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < Kx; i += blockDim.x) {   // f-update
+            double mx = -INFINITY;
+            for (int j = 0; j < Ky; ++j) mx = fmax(mx, (g[j] - C[i * Ky + j]) / eps);
+            double s = 0.0;
+            for (int j = 0; j < Ky; ++j) s += exp((g[j] - C[i * Ky + j]) / eps - mx);
+            f[i] = eps * log((double)wx[i]) - eps * (mx + log(s));
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < Kx; i += blockDim.x) {
+            double s = 0.0;
+            for (int j = 0; j < Ky; ++j) s += exp((f[i] + g[j] - C[i * Ky + j]) / eps);
+            rs[i] = fabs(s - (double)wx[i]);
+        }
+        for (int j = threadIdx.x; j < Ky; j += blockDim.x) {
+            double s = 0.0;
+            for (int i = 0; i < Kx; ++i) s += exp((f[i] + g[j] - C[i * Ky + j]) / eps);
+            cs[j] = fabs(s - (double)wy[j]);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double e = 0.0;
+            for (int i = 0; i < Kx; ++i) e += rs[i];
+            for (int j = 0; j < Ky; ++j) e += cs[j];
+            s_stop = (e < tol) || it >= max_iter || !isfinite(e);
+            if (!isfinite(e)) atomicOr(flags, 2);
+        }
+        __syncthreads();
+        if (s_stop) break;
+    }
+    for (int i = threadIdx.x; i < Kx; i += blockDim.x) ft[i] = f[i];
+}
+
+// Cholesky S_k = L L^T (fp64, one CTA, sequential columns), then Linv and log det L.
+__global__ void __launch_bounds__(kGT) k_gmm_chol(const float *covx, int d, double *Linv, double *logdet,
+                                                   int *flags) {
+    extern __shared__ double sm[];
+    const int dd = d * d, k = blockIdx.x;
+    double *L = sm, *Li = sm + dd;
+    for (int e = threadIdx.x; e < dd; e += blockDim.x) {
+        const int i = e / d, j = e % d;
+        L[e] = 0.5 * ((double)covx[(long long)k * dd + i * d + j] + (double)covx[(long long)k * dd + j * d + i]);
+        Li[e] = 0.0;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {  // textbook Cholesky-Banachiewicz, d <= 64
+        int bad = 0;
+        for (int j = 0; j < d; ++j) {
+            double s = L[j * d + j];
+            for (int t = 0; t < j; ++t) s -= L[j * d + t] * L[j * d + t];
+            if (!(s > 0.0)) { bad = 1; s = 1e-300; }
+            const double ljj = sqrt(s);
+            L[j * d + j] = ljj;
+            for (int i = j + 1; i < d; ++i) {
+                double v = L[i * d + j];
+                for (int t = 0; t < j; ++t) v -= L[i * d + t] * L[j * d + t];
+                L[i * d + j] = v / ljj;
+            }
+            for (int t = j + 1; t < d; ++t) L[j * d + t] = 0.0;
+        }
+        double ld = 0.0;
+        for (int j = 0; j < d; ++j) ld += log(L[j * d + j]);
+        logdet[k] = ld;
+        if (bad) atomicOr(flags, 4);
+    }
+    __syncthreads();
+    // Linv: solve L * Li = I column by column (thread per column)
+    for (int c = threadIdx.x; c < d; c += blockDim.x) {
+        for (int i = 0; i < d; ++i) {
+            double v = (i == c) ? 1.0 : 0.0;
+            for (int t = 0; t < i; ++t) v -= L[i * d + t] * Li[t * d + c];
+            Li[i * d + c] = v / L[i * d + i];
+        }
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < dd; e += blockDim.x) Linv[(long long)k * dd + e] = Li[e];
+}
+
+// f^(0)(x_i) = sum_k f~_k p_k(x_i), log p_k = log a_k - 1/2 |Linv_k (x - m_k)|^2 - logdet_k - LSE.
+__global__ void __launch_bounds__(kGT) k_gmm_pot(const float *__restrict__ x, long long n, int d, int K,
+                                                  const float *__restrict__ wx, const float *__restrict__ mux,
+                                                  const double *__restrict__ Linv,
+                                                  const double *__restrict__ logdet,
+                                                  const double *__restrict__ ft, float *pot) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const float *xi = x + i * d;
+        double mx = -INFINITY, num = 0.0, den = 0.0;
+        for (int k = 0; k < K; ++k) {
+            const double *Li = Linv + (long long)k * d * d;
+            const float *mk = mux + (long long)k * d;
+            double q = 0.0;
+            for (int r = 0; r < d; ++r) {
+                double z = 0.0;
+                for (int c = 0; c <= r; ++c) z += Li[r * d + c] * ((double)xi[c] - (double)mk[c]);
+                q += z * z;
+            }
+            const double lp = log((double)wx[k]) - 0.5 * q - logdet[k];
+            // streaming softmax-weighted mean of f~ (fixed k order)
+            if (lp > mx) {
+                const double sc = exp(mx - lp);
+                num *= sc;
+                den *= sc;
+                mx = lp;
+            }
+            const double e = exp(lp - mx);
+            num += e * ft[k];
+            den += e;
+        }
+        pot[i] = (float)(num / den);
+    }
+}
+
+cudaError_t launch_gmm_init(const float *x, long long n, int d, int Kx, const float *wx,
+                            const float *mux, const float *covx, int Ky, const float *wy,
+                            const float *muy, const float *covy, float eps, float inner_tol,
+                            int inner_max_iter, float *pot, double *work, int *flags,
+                            cudaStream_t st) {
+    if (d > 64 || Kx > 64 || Ky > 64) return cudaErrorInvalidValue;
+    const int dd = d * d;
+    double *R = work, *Linv = R + (size_t)Kx * dd, *logdet = Linv + (size_t)Kx * dd,
+           *C = logdet + Kx, *ft = C + (size_t)Kx * Ky;
+    cudaError_t e;
+    size_t s5 = 5 * (size_t)dd * sizeof(double), s2 = 2 * (size_t)dd * sizeof(double);
+    if ((e = cudaFuncSetAttribute(k_gmm_sqrt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s5))) return e;
+    if ((e = cudaFuncSetAttribute(k_gmm_bures, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s5))) return e;
+    if ((e = cudaFuncSetAttribute(k_gmm_chol, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2))) return e;
+    k_gmm_sqrt<<<Kx, kGT, s5, st>>>(covx, d, R, flags);
+    k_gmm_bures<<<Kx * Ky, kGT, s5, st>>>(mux, covx, Kx, muy, covy, Ky, d, R, C, flags);
+    k_gmm_sinkhorn<<<1, kGT, 0, st>>>(C, Kx, Ky, wx, wy, eps, inner_tol, inner_max_iter, ft, flags);
+    k_gmm_chol<<<Kx, kGT, s2, st>>>(covx, d, Linv, logdet, flags);
+    long long b = (n + kGT - 1) / kGT;
+    k_gmm_pot<<<(int)(b > 148 * 8 ? 148 * 8 : b), kGT, 0, st>>>(x, n, d, Kx, wx, mux, Linv, logdet, ft, pot);
+    return cudaGetLastError();
+}
+
+}  // namespace sk

@@ -1,0 +1,149 @@
+// sk_internal.h — host-side declarations shared by the .cu translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace sk {
+
+// ------------------------------------------------------------ K13 on-chip
+struct BatchLaunch {
+    int B, n, m, d;
+    const float *x; long long x_stride;
+    const float *y; long long y_stride;
+    const float *a; long long a_stride;
+    const float *b; long long b_stride;
+    const float *finit;
+    float *f, *g;
+    float eps, tol;
+    int max_iter, check_every;
+    int *iters, *conv, *nonfinite;
+    float *err;
+    double *E;
+};
+bool batched_supported(int d, int n, int m);
+size_t batched_smem_bytes(int D, int n, int m);
+cudaError_t launch_batched(const BatchLaunch &L, cudaStream_t st);
+
+// ------------------------------------------------- multi-kernel online path
+// Device status of one solve (all fields written only by kernels' last blocks).
+struct DevStatus {
+    int iter;        // completed sweeps l: (f^l, g^l) live in buffers [l & 1]
+    int stop;        // kernels return immediately once set
+    int converged;
+    int nonfinite;
+    int final_iter;
+    float err;       // last computed err_l
+    unsigned ticket_col, ticket_row, ticket_rep;
+    int max_iter, check_every;
+    float tol;
+    double E;        // dual objective of the returned iterate
+    double fa_local; // sharded: this rank's <f,a> - eps sum(a) partial
+};
+
+// Packed tile layout of one side: tiles of tq points; tile t at t*(D+1)*tq floats:
+// [D][tq] coordinates then [tq] w = (h - |p|^2) log2(e)/eps; padding w = -inf.
+int lse_dpad(int d);          // instantiated D >= d (0 if unsupported)
+int lse_tq(int D);            // points per tile for D
+__host__ __device__ inline long long lse_tiles(long long P, int tq) { return (P + tq - 1) / tq; }
+
+struct Side {
+    int P, d, D, tq;
+    float *pack;      // tiles * (D+1) * tq
+    float *c;         // [P] eps log w_p + |p|^2 (finalize constant)
+    float *nk;        // [P] |p|^2 log2(e)/eps
+    float *pot[2];    // double-buffered potential
+};
+
+// Pack points (P x d, fp32 row-major), optional weights and initial potential.
+// If wts == nullptr the log-weight is the constant logw_const.
+cudaError_t pack_side(const Side &S, const float *pts, const float *wts, float logw_const,
+                      const float *pot0, float eps, cudaStream_t st);
+
+// One LSE pass: outputs P side points, reduces over Q side.  Splits:
+// nblk blocks of blk_tiles Q tiles each (the last may be shorter; blk_tiles = 0
+// means one block of all tiles), each cut into split_q sub-splits.  Writes
+// part[s * P + p] = (M, S) for s in [0, nblk*split_q).
+struct LsePass {
+    const Side *Pside, *Qside;
+    int nblk, blk_tiles, split_q;
+    float2 *part;
+    float eps;
+    const int *stop;  // device flag (nullable)
+};
+cudaError_t launch_lse(const LsePass &L, cudaStream_t st);
+int lse_occupancy_ctas(int D);  // resident CTAs per SM of the LSE kernel for D
+
+enum MergeMode { MERGE_COL = 0, MERGE_ROW = 1, MERGE_OUT = 2 };
+struct MergePass {
+    MergeMode mode;
+    const Side *S;    // output side (its c, nk, pack.w and pot buffers)
+    const float2 *part;
+    int nsplit;
+    float eps;
+    const float *wts;         // b (COL) weights for the error, nullable = uniform
+    DevStatus *st;
+    double *blk_err;          // per-block scratch
+    int *blk_bad;
+    float *out;               // MERGE_OUT destination
+    float out_const;          // MERGE_OUT: added constant (eps log ms for Eq. 8)
+    int sharded;              // non-finite f is detected by the next (replicated) column merge
+};
+cudaError_t launch_merge(const MergePass &M, cudaStream_t st);
+int merge_blocks(int P);
+
+// E = <f,a> + <g,b> - eps sum(a) of the iterate status->final_iter.
+cudaError_t launch_report(const Side &X, const Side &Y, const float *a, const float *b, float eps,
+                          DevStatus *st, int local_only, long long n_uniform, cudaStream_t s);
+
+cudaError_t launch_status_init(DevStatus *st, int max_iter, int check_every, float tol,
+                               cudaStream_t s);
+
+// ------------------------------------------------------------ misc kernels
+cudaError_t launch_fill(float *p, long long n, float v, cudaStream_t st);
+cudaError_t launch_check_finite(const float *p, long long n, int *flag, cudaStream_t st);
+cudaError_t launch_check_positive(const float *p, long long n, int *flag, cudaStream_t st);
+cudaError_t launch_gather_rows(const float *src, const int *idx, long long cnt, int d, float *dst,
+                               cudaStream_t st);
+cudaError_t launch_check_indices(const int *idx, long long cnt, long long n, int *flag, int *scratch,
+                                 cudaStream_t st);
+
+// ----------------------------------------------------------------- sort1d
+cudaError_t launch_sort_rows(const float *x, int B, int n, long long stride, int *perm, int *rank,
+                             float *sorted, int *nanflag, cudaStream_t st);
+cudaError_t launch_sort1d_dual(const float *xs_sorted, const int *perm, const float *ys_sorted,
+                               int y_shared, int B, int n, int iters, float *pot, cudaStream_t st);
+
+// --------------------------------------------------------------- Gaussian
+cudaError_t launch_moments(const float *x, const float *w, long long n, int d, double *mean,
+                           double *cov, double *scratch, long long scratch_doubles, cudaStream_t st);
+cudaError_t launch_gauss_A(const double *mean_mu, double *cov_mu, const double *mean_nu,
+                           double *cov_nu, int d, float ridge_rel, double *A, int *ns_fail,
+                           cudaStream_t st);
+cudaError_t launch_gauss_potential(const float *x, long long n, int d, const double *m_mu,
+                                   const double *m_nu, const double *A, float *pot, cudaStream_t st);
+
+// -------------------------------------------------------------------- GMM
+cudaError_t launch_gmm_init(const float *x, long long n, int d, int Kx, const float *wx,
+                            const float *mux, const float *covx, int Ky, const float *wy,
+                            const float *muy, const float *covy, float eps, float inner_tol,
+                            int inner_max_iter, float *pot, double *work, int *flags,
+                            cudaStream_t st);
+size_t gmm_work_doubles(int d, int Kx, int Ky);
+
+// ------------------------------------------------------------- stored mode
+cudaError_t launch_build_cost(const float *x, const float *y, long long n, long long m, int d,
+                              float *C, cudaStream_t st);
+struct StoredPass {
+    const float *C; long long n, m;   // row-major n x m fp32
+    float eps;
+    const float *wq;      // reduction-side w = h log2(e)/eps (the other side's D=0 pack)
+    float2 *part;         // rows: [n] (one split); cols: [nblk * split_q][m]
+    long long blk_rows;   // cols: rows per fixed block (0 = one block of all rows)
+    int nblk, split_q;    // cols: blocks and sub-splits per block
+    const int *stop;
+};
+cudaError_t launch_stored_rows(const StoredPass &S, cudaStream_t st);
+cudaError_t launch_stored_cols(const StoredPass &S, cudaStream_t st);
+
+}  // namespace sk

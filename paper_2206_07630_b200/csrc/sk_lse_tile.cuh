@@ -1,0 +1,68 @@
+// sk_lse_tile.cuh — the inner online log-sum-exp loop shared by the on-chip
+// solver (K13) and the multi-kernel LSE pass (K2).
+//
+// For output points p (R per thread) and reduction points q it accumulates, in
+// log2 units,
+//     t_pq = w_q + <p~, q>,     p~ = 2 log2(e)/eps * p,
+//     w_q  = (h_q - ||q||^2) * log2(e)/eps      (h = the other potential),
+// i.e. t_pq = (h_q - C_pq) log2(e)/eps + ||p||^2 log2(e)/eps: the per-p constant
+// ||p||^2 is folded out of the LSE and added back by the caller's finalize.
+// State per p: running max M and sum S of 2^(t - M), updated once per chunk of 8
+// q's (chunk max first, then one rescale only if the max grew).  The cross term
+// uses packed FFMA2 over pairs of q; exponentials are MUFU.EX2.
+#pragma once
+#include "sk_common.cuh"
+
+namespace sk {
+
+constexpr int kChunk = 8;  // q's per online-max chunk (4 FFMA2 pairs)
+
+// One chunk of 8 q's for R output points.  qc: coords [D][stride] (SoA), qw: w.
+template <int D, int R>
+__device__ __forceinline__ void lse_chunk(const float *__restrict__ qc, int qstride,
+                                          const float *__restrict__ qw, int q,
+                                          const float2 (&pd)[R][D], float (&M)[R],
+                                          float2 (&S)[R]) {
+    float2 w[4], c[D][4];
+    {
+        const float4 w0 = *reinterpret_cast<const float4 *>(qw + q);
+        const float4 w1 = *reinterpret_cast<const float4 *>(qw + q + 4);
+        w[0] = make_float2(w0.x, w0.y); w[1] = make_float2(w0.z, w0.w);
+        w[2] = make_float2(w1.x, w1.y); w[3] = make_float2(w1.z, w1.w);
+    }
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+        const float4 c0 = *reinterpret_cast<const float4 *>(qc + k * qstride + q);
+        const float4 c1 = *reinterpret_cast<const float4 *>(qc + k * qstride + q + 4);
+        c[k][0] = make_float2(c0.x, c0.y); c[k][1] = make_float2(c0.z, c0.w);
+        c[k][2] = make_float2(c1.x, c1.y); c[k][3] = make_float2(c1.z, c1.w);
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        float2 t[4];
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+            t[jj] = w[jj];
+#pragma unroll
+            for (int k = 0; k < D; ++k) t[jj] = fma2(pd[r][k], c[k][jj], t[jj]);
+        }
+        float cm = fmaxf(fmaxf(fmaxf(t[0].x, t[0].y), fmaxf(t[1].x, t[1].y)),
+                         fmaxf(fmaxf(t[2].x, t[2].y), fmaxf(t[3].x, t[3].y)));
+        if (cm > M[r]) {  // rare after the first chunks
+            const float sc = ex2(M[r] - cm);
+            S[r].x *= sc;
+            S[r].y *= sc;
+            M[r] = cm;
+        }
+        const float2 mm = make_float2(M[r], M[r]);
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+            float2 e = sub2(t[jj], mm);
+            e.x = ex2(e.x);
+            e.y = ex2(e.y);
+            S[r] = add2(S[r], e);
+        }
+    }
+}
+
+}  // namespace sk

@@ -1,0 +1,428 @@
+// sk_online.cu — the multi-kernel online-cost Sinkhorn path for large problems.
+//
+//  K1 pack_side   : per point |p|^2, eps log w_p + |p|^2 and the tile-packed
+//                   operand [coords | w] with w = (h - |p|^2) log2(e)/eps.
+//  K2 k_lse<D,R>  : one LSE pass (row pass for f, column pass for g; Alg. 1
+//                   l.4-5 with reading R-1): for every output point p, the
+//                   (max, sum 2^(t - max)) partial over one split of the other
+//                   side, t = w_q + <2 log2(e)/eps p, q>; the q tiles stream
+//                   global -> shared through a 4-stage 1D bulk-TMA ring with
+//                   mbarrier completion; the cross term is packed FFMA2, the
+//                   exponentials MUFU.EX2 (sk_lse_tile.cuh).
+//  K6 k_merge     : stable LSE merge of the split partials in fixed order ->
+//                   new potential (+ packed w for the next pass), the fused
+//                   marginal error err_l = sum_j b_j |expm1((g^l - g^{l+1})/eps)|
+//                   (H5; threshold appendix), non-finite
+//                   detection and the stop flag, decided by the last block.
+//  K7 k_report    : E = <f,a> + <g,b> - eps sum(a) (Eq. 2 right after an
+//                   f-update, H6) in fp64.
+#include "sk_internal.h"
+#include "sk_lse_tile.cuh"
+
+namespace sk {
+
+constexpr int kLT = 128;      // LSE kernel threads
+constexpr int kStages = 4;    // bulk-copy ring depth
+
+int lse_dpad(int d) {
+    if (d <= 4) return d < 1 ? 0 : d;
+    if (d <= 8) return 8;
+    if (d <= 16) return 16;
+    if (d <= 32) return 32;
+    if (d <= 64) return 64;
+    return 0;
+}
+
+int lse_tq(int D) { return D <= 4 ? 256 : (D <= 16 ? 128 : 64); }
+
+template <int D> constexpr int kR = D <= 4 ? 4 : (D <= 16 ? 2 : 1);
+
+// ------------------------------------------------------------------- K1
+__global__ void k_pack_side(Side S, const float *__restrict__ pts, const float *__restrict__ wts,
+                            float logw_const, const float *__restrict__ pot0, float eps, int stored) {
+    const long long tiles = lse_tiles(S.P, S.tq);
+    const long long total = tiles * S.tq;
+    const float kap = kLog2e / eps;
+    for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < total;
+         p += (long long)gridDim.x * blockDim.x) {
+        const long long t = p / S.tq, o = p % S.tq;
+        float *tile = S.pack + t * (long long)(S.D + 1) * S.tq;
+        if (p < S.P) {
+            float s = 0.f;
+            for (int k = 0; k < S.D; ++k) {
+                const float v = k < S.d ? pts[p * S.d + k] : 0.f;
+                tile[k * S.tq + o] = v;
+                s = fmaf(v, v, s);
+            }
+            if (stored) s = 0.f;  // stored cost: no |p|^2 folding
+            const float lw = wts ? logf(wts[p]) : logw_const;
+            S.c[p] = fmaf(eps, lw, s);
+            S.nk[p] = s * kap;
+            const float h = pot0 ? pot0[p] : 0.f;
+            S.pot[0][p] = h;
+            tile[S.D * S.tq + o] = fmaf(h, kap, -s * kap);
+        } else {
+            for (int k = 0; k < S.D; ++k) tile[k * S.tq + o] = 0.f;
+            tile[S.D * S.tq + o] = -INFINITY;
+        }
+    }
+}
+
+cudaError_t pack_side(const Side &S, const float *pts, const float *wts, float logw_const,
+                      const float *pot0, float eps, cudaStream_t st) {
+    const long long total = lse_tiles(S.P, S.tq) * S.tq;
+    int blocks = (int)((total + 255) / 256);
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    k_pack_side<<<blocks, 256, 0, st>>>(S, pts, wts, logw_const, pot0, eps, S.D == 0);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------- K2
+struct LseArgs {
+    const float *Ppack; int P; int Ptq;
+    const float *Qpack; int Qtiles;
+    int blk_tiles, split_q;
+    float2 *part;
+    float tk;
+    const int *stop;
+};
+
+template <int D, int R>
+__global__ void __launch_bounds__(kLT) k_lse(LseArgs A) {
+    constexpr int TQ = D <= 4 ? 256 : (D <= 16 ? 128 : 64);
+    constexpr int TF = (D + 1) * TQ;  // floats per tile
+    extern __shared__ __align__(128) float ring[];  // [kStages][TF]
+    __shared__ __align__(8) uint64_t full[kStages];
+    if (A.stop && *(volatile const int *)A.stop) return;
+
+    // ---- this CTA's Q range: split s = blockIdx.y -> block b, sub-split u
+    const int s = blockIdx.y;
+    const int b = s / A.split_q, u = s % A.split_q;
+    const int bt = A.blk_tiles > 0 ? A.blk_tiles : A.Qtiles;
+    const int base = b * bt;
+    const int nt_b = max(0, min(bt, A.Qtiles - base));
+    const int t0 = base + (int)((long long)nt_b * u / A.split_q);
+    const int t1 = base + (int)((long long)nt_b * (u + 1) / A.split_q);
+    const int nt = t1 - t0;
+
+    // ---- output points: R per thread
+    float2 pd[R][D];
+    float M[R];
+    float2 Sx[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int p = blockIdx.x * (kLT * R) + r * kLT + threadIdx.x;
+        const int pt = p / A.Ptq, po = p % A.Ptq;
+        const float *tile = A.Ppack + (long long)pt * (D + 1) * A.Ptq;
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+            const float v = p < A.P ? tile[k * A.Ptq + po] * A.tk : 0.f;
+            pd[r][k] = make_float2(v, v);
+        }
+        M[r] = -INFINITY;
+        Sx[r] = make_float2(0.f, 0.f);
+    }
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kStages; ++i) mbar_init(&full[i], 1);
+        fence_mbar_init();
+        for (int i = 0; i < kStages && i < nt; ++i) {
+            mbar_expect_tx(&full[i], TF * 4);
+            bulk_g2s(ring + i * TF, A.Qpack + (long long)(t0 + i) * TF, TF * 4, &full[i]);
+        }
+    }
+    __syncthreads();
+
+    for (int i = 0; i < nt; ++i) {
+        const int st = i % kStages;
+        mbar_wait(&full[st], (i / kStages) & 1);
+        const float *qt = ring + st * TF;
+#pragma unroll 2
+        for (int q = 0; q < TQ; q += kChunk) lse_chunk<D, R>(qt, TQ, qt + D * TQ, q, pd, M, Sx);
+        __syncthreads();  // everyone is done with stage st
+        if (threadIdx.x == 0 && i + kStages < nt) {
+            fence_proxy_async();
+            mbar_expect_tx(&full[st], TF * 4);
+            bulk_g2s(ring + st * TF, A.Qpack + (long long)(t0 + i + kStages) * TF, TF * 4, &full[st]);
+        }
+    }
+
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int p = blockIdx.x * (kLT * R) + r * kLT + threadIdx.x;
+        if (p < A.P) A.part[(long long)s * A.P + p] = make_float2(M[r], Sx[r].x + Sx[r].y);
+    }
+}
+
+template <int D>
+static cudaError_t launch_lse_d(const LsePass &L, cudaStream_t st) {
+    constexpr int R = kR<D>;
+    constexpr int TQ = D <= 4 ? 256 : (D <= 16 ? 128 : 64);
+    const size_t smem = (size_t)kStages * (D + 1) * TQ * sizeof(float);
+    cudaError_t e = cudaFuncSetAttribute(k_lse<D, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    LseArgs A;
+    A.Ppack = L.Pside->pack; A.P = L.Pside->P; A.Ptq = L.Pside->tq;
+    A.Qpack = L.Qside->pack; A.Qtiles = (int)lse_tiles(L.Qside->P, L.Qside->tq);
+    A.blk_tiles = L.blk_tiles; A.split_q = L.split_q;
+    A.part = L.part;
+    A.tk = 2.f * kLog2e / L.eps;
+    A.stop = L.stop;
+    dim3 grid((A.P + kLT * R - 1) / (kLT * R), L.nblk * L.split_q);
+    k_lse<D, R><<<grid, kLT, smem, st>>>(A);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_lse(const LsePass &L, cudaStream_t st) {
+    switch (L.Pside->D) {
+        case 1: return launch_lse_d<1>(L, st);
+        case 2: return launch_lse_d<2>(L, st);
+        case 3: return launch_lse_d<3>(L, st);
+        case 4: return launch_lse_d<4>(L, st);
+        case 8: return launch_lse_d<8>(L, st);
+        case 16: return launch_lse_d<16>(L, st);
+        case 32: return launch_lse_d<32>(L, st);
+        case 64: return launch_lse_d<64>(L, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+template <int D>
+static int occ_d() {
+    constexpr int R = kR<D>;
+    constexpr int TQ = D <= 4 ? 256 : (D <= 16 ? 128 : 64);
+    const size_t smem = (size_t)kStages * (D + 1) * TQ * sizeof(float);
+    cudaFuncSetAttribute(k_lse<D, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_lse<D, R>, kLT, smem) != cudaSuccess) n = 1;
+    return n > 0 ? n : 1;
+}
+
+int lse_occupancy_ctas(int D) {
+    switch (D) {
+        case 1: return occ_d<1>();
+        case 2: return occ_d<2>();
+        case 3: return occ_d<3>();
+        case 4: return occ_d<4>();
+        case 8: return occ_d<8>();
+        case 16: return occ_d<16>();
+        case 32: return occ_d<32>();
+        case 64: return occ_d<64>();
+        default: return 1;
+    }
+}
+
+// ------------------------------------------------------------------- K6
+constexpr int kMT = 256;
+int merge_blocks(int P) {
+    int b = (P + kMT - 1) / kMT;
+    return b < 1 ? 1 : (b > 1184 ? 1184 : b);
+}
+
+__global__ void __launch_bounds__(kMT) k_merge(MergePass Mp, Side S) {
+    __shared__ double red[kMT / 32];
+    __shared__ int redi[kMT / 32];
+    __shared__ int s_last;
+    DevStatus *st = Mp.st;
+    if (st && *(volatile int *)&st->stop) return;
+    const int l = st ? st->iter : 0;
+    const float eps = Mp.eps, kap = kLog2e / eps, epsln2 = eps * kLn2;
+    const bool check = Mp.mode == MERGE_COL && l >= 1 &&
+                       (l % st->check_every == 0 || l == st->max_iter);
+    const float *hold = S.pot[l & 1];
+    float *hnew = S.pot[(l + 1) & 1];
+    double e = 0.0;
+    int bad = 0;
+    for (int p = blockIdx.x * kMT + threadIdx.x; p < S.P; p += gridDim.x * kMT) {
+        float M = -INFINITY;
+        for (int s = 0; s < Mp.nsplit; ++s) M = fmaxf(M, Mp.part[(long long)s * S.P + p].x);
+        float Ssum = 0.f;
+        for (int s = 0; s < Mp.nsplit; ++s) {
+            const float2 v = Mp.part[(long long)s * S.P + p];
+            if (v.x != -INFINITY) Ssum += v.y * ex2(v.x - M);
+        }
+        const float lse2 = M + log2f(Ssum);
+        if (Mp.mode == MERGE_OUT) {
+            const float v = Mp.out_const + (S.c[p] - epsln2 * lse2);
+            Mp.out[p] = v;
+            bad |= !isfinite(v);
+            continue;
+        }
+        const float hn = S.c[p] - epsln2 * lse2;
+        hnew[p] = hn;
+        const long long t = p / S.tq, o = p % S.tq;
+        S.pack[t * (long long)(S.D + 1) * S.tq + (long long)S.D * S.tq + o] = fmaf(hn, kap, -S.nk[p]);
+        bad |= !isfinite(hn);
+        if (check) {
+            const double bj = Mp.wts ? (double)Mp.wts[p] : 1.0 / S.P;
+            e += bj * fabs((double)expm1f((hold[p] - hn) / eps));
+        }
+    }
+    if (!st) return;
+    // block partials -> last block decides (fixed order => deterministic)
+    for (int o = 16; o > 0; o >>= 1) {
+        e += __shfl_xor_sync(0xffffffffu, e, o);
+        bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+    }
+    if ((threadIdx.x & 31) == 0) { red[threadIdx.x >> 5] = e; redi[threadIdx.x >> 5] = bad; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double be = 0.0; int bb = 0;
+        for (int w = 0; w < kMT / 32; ++w) { be += red[w]; bb |= redi[w]; }
+        Mp.blk_err[blockIdx.x] = be;
+        Mp.blk_bad[blockIdx.x] = bb;
+        __threadfence();
+        unsigned *tk = Mp.mode == MERGE_COL ? &st->ticket_col : &st->ticket_row;
+        s_last = atomicAdd(tk, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!s_last || threadIdx.x != 0) return;
+    __threadfence();
+    double et = 0.0; int bt = 0;
+    for (int i = 0; i < (int)gridDim.x; ++i) {
+        et += ((volatile double *)Mp.blk_err)[i];
+        bt |= ((volatile int *)Mp.blk_bad)[i];
+    }
+    if (Mp.mode == MERGE_COL) {
+        st->ticket_col = 0;
+        // sharded: f^l may be the non-finite one (rows are not checked locally), so fall back
+        // to (f^{l-1}, g^{l-1}), both finite.
+        if (bt) { st->nonfinite = 1; st->stop = 1; st->final_iter = Mp.sharded ? max(l - 1, 0) : l; }
+        else if (check) {
+            st->err = (float)et;
+            if ((float)et < st->tol) { st->converged = 1; st->stop = 1; st->final_iter = l; }
+            else if (l >= st->max_iter) { st->stop = 1; st->final_iter = l; }
+        }
+    } else if (Mp.mode == MERGE_ROW) {
+        st->ticket_row = 0;
+        if (bt && !Mp.sharded) { st->nonfinite = 1; st->stop = 1; st->final_iter = l; }
+        else st->iter = l + 1;
+    } else {
+        st->ticket_row = 0;
+        if (bt) st->nonfinite = 1;
+    }
+    __threadfence();
+}
+
+cudaError_t launch_merge(const MergePass &M, cudaStream_t st) {
+    k_merge<<<merge_blocks(M.S->P), kMT, 0, st>>>(M, *M.S);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------- K7
+__global__ void __launch_bounds__(1024) k_report(Side X, Side Y, const float *a, const float *b,
+                                                  float eps, DevStatus *st, int local_only,
+                                                  long long n_uniform) {
+    __shared__ double red[32];
+    const int l = st->final_iter;
+    const float *f = X.pot[l & 1], *g = Y.pot[l & 1];
+    double s = 0.0;
+    for (int i = threadIdx.x; i < X.P; i += 1024) {
+        const double ai = a ? (double)a[i] : 1.0 / n_uniform;
+        s += (double)f[i] * ai - (double)eps * ai;
+    }
+    double s2 = 0.0;
+    for (int j = threadIdx.x; j < Y.P; j += 1024) s2 += (double)g[j] * (b ? (double)b[j] : 1.0 / Y.P);
+    const double fa = block_sum_d<1024>(s, red);
+    const double gb = block_sum_d<1024>(s2, red);
+    if (threadIdx.x == 0) {
+        st->fa_local = fa;
+        st->E = local_only ? gb : fa + gb;
+    }
+}
+
+cudaError_t launch_report(const Side &X, const Side &Y, const float *a, const float *b, float eps,
+                          DevStatus *st, int local_only, long long n_uniform, cudaStream_t s) {
+    k_report<<<1, 1024, 0, s>>>(X, Y, a, b, eps, st, local_only, n_uniform);
+    return cudaGetLastError();
+}
+
+__global__ void k_status_init(DevStatus *st, int max_iter, int check_every, float tol) {
+    DevStatus z = {};
+    z.max_iter = max_iter;
+    z.check_every = check_every;
+    z.tol = tol;
+    z.err = INFINITY;
+    *st = z;
+}
+
+cudaError_t launch_status_init(DevStatus *st, int max_iter, int check_every, float tol,
+                               cudaStream_t s) {
+    k_status_init<<<1, 1, 0, s>>>(st, max_iter, check_every, tol);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------ misc kernels
+__global__ void k_fill(float *p, long long n, float v) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        p[i] = v;
+}
+
+cudaError_t launch_fill(float *p, long long n, float v, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    long long b = (n + 255) / 256;
+    k_fill<<<(int)(b > 4096 ? 4096 : b), 256, 0, st>>>(p, n, v);
+    return cudaGetLastError();
+}
+
+__global__ void k_check(const float *p, long long n, int *flag, int positive) {
+    int bad = 0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const float v = p[i];
+        bad |= !isfinite(v) || (positive && !(v > 0.f));
+    }
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
+cudaError_t launch_check_finite(const float *p, long long n, int *flag, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    long long b = (n + 255) / 256;
+    k_check<<<(int)(b > 2048 ? 2048 : b), 256, 0, st>>>(p, n, flag, 0);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_check_positive(const float *p, long long n, int *flag, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    long long b = (n + 255) / 256;
+    k_check<<<(int)(b > 2048 ? 2048 : b), 256, 0, st>>>(p, n, flag, 1);
+    return cudaGetLastError();
+}
+
+__global__ void k_gather(const float *src, const int *idx, long long cnt, int d, float *dst) {
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < cnt * d;
+         t += (long long)gridDim.x * blockDim.x) {
+        const long long r = t / d, k = t % d;
+        dst[t] = src[(long long)idx[r] * d + k];
+    }
+}
+
+cudaError_t launch_gather_rows(const float *src, const int *idx, long long cnt, int d, float *dst,
+                               cudaStream_t st) {
+    long long b = (cnt * d + 255) / 256;
+    k_gather<<<(int)(b > 4096 ? 4096 : (b < 1 ? 1 : b)), 256, 0, st>>>(src, idx, cnt, d, dst);
+    return cudaGetLastError();
+}
+
+// indices in range and distinct: mark[idx] counting via atomics on an int scratch of size n
+__global__ void k_check_idx(const int *idx, long long cnt, long long n, int *flag, int *mark) {
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < cnt;
+         t += (long long)gridDim.x * blockDim.x) {
+        const int v = idx[t];
+        if (v < 0 || v >= n) { atomicOr(flag, 1); continue; }
+        if (atomicAdd(&mark[v], 1) != 0) atomicOr(flag, 2);
+    }
+}
+
+cudaError_t launch_check_indices(const int *idx, long long cnt, long long n, int *flag, int *scratch,
+                                 cudaStream_t st) {
+    cudaError_t e = cudaMemsetAsync(scratch, 0, sizeof(int) * n, st);
+    if (e != cudaSuccess) return e;
+    long long b = (cnt + 255) / 256;
+    k_check_idx<<<(int)(b > 4096 ? 4096 : (b < 1 ? 1 : b)), 256, 0, st>>>(idx, cnt, n, flag, scratch);
+    return cudaGetLastError();
+}
+
+}  // namespace sk

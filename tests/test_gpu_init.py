@@ -1,0 +1,82 @@
+"""Initializer parity (-m gpu): Gaussian (Sec. 3.2), GMM (Sec. 3.3), Subsample (Sec. 3.4)."""
+import numpy as np
+import pytest
+import torch
+
+from parity import INIT_RTOL, centred, rel_inf
+from workloads import gen
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    import paper_2206_07630_b200 as sk
+    return sk.Context(0)
+
+
+def _cuda(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+@pytest.mark.parametrize("n,m,d", [(256, 256, 2), (5000, 3000, 3), (2000, 2100, 16), (1500, 1600, 64)])
+def test_gaussian_init(O, ctx, n, m, d):
+    import paper_2206_07630_b200 as sk
+    rng = np.random.default_rng(d + n)
+    G = rng.standard_normal((d, d)) / np.sqrt(d)
+    x = (rng.standard_normal((n, d)) @ G.T).astype(np.float32)
+    y = (rng.standard_normal((m, d)) * 0.7 + 0.4).astype(np.float32)
+    a = gen.random_weights(n, rng)
+    pot, side = sk.sinkhorn_init_gaussian(ctx, _cuda(x), _cuda(y), a=_cuda(a))
+    ref, so = O.init_gaussian(x, y, a=a)
+    assert side == so
+    eps = 0.01 * gen.mean_sq_cost(x, y)
+    assert rel_inf(centred(pot.cpu().numpy()), centred(ref), eps) <= INIT_RTOL
+
+
+def test_gaussian_special_cases(ctx):
+    import paper_2206_07630_b200 as sk
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal((400, 3)).astype(np.float32)
+    pot, _ = sk.sinkhorn_init_gaussian(ctx, _cuda(x), _cuda(x))
+    assert float(pot.max() - pot.min()) < 1e-4       # equal moments -> A = I -> constant
+
+
+def test_gmm_init_c3_shape(O, ctx):
+    import paper_2206_07630_b200 as sk
+    p = gen.c3(n=2048)
+    gx = {k: _cuda(v) for k, v in p.extra["gmm_x"].items()}
+    gy = {k: _cuda(v) for k, v in p.extra["gmm_y"].items()}
+    pot, side = sk.sinkhorn_init_gmm(ctx, _cuda(p.x), _cuda(p.y), gx, gy, p.eps)
+    ref, so = O.init_gmm(p.x, p.y, p.extra["gmm_x"], p.extra["gmm_y"], p.eps)
+    assert side == so == 0
+    assert rel_inf(centred(pot.cpu().numpy()), centred(ref), p.eps) <= INIT_RTOL
+
+
+def test_gmm_single_component_constant(ctx):
+    import paper_2206_07630_b200 as sk
+    rng = np.random.default_rng(4)
+    x = rng.standard_normal((100, 2)).astype(np.float32)
+    y = rng.standard_normal((120, 2)).astype(np.float32)
+    g1 = {"weights": _cuda(np.ones(1, np.float32)), "means": _cuda(np.zeros((1, 2), np.float32)),
+          "covs": _cuda(np.eye(2, dtype=np.float32)[None])}
+    pot, _ = sk.sinkhorn_init_gmm(ctx, _cuda(x), _cuda(y), g1, g1, 0.5)
+    assert float(pot.max() - pot.min()) == 0.0
+
+
+@pytest.mark.parametrize("n,ns", [(20000, 1500), (3000, 3000), (5000, 1)])
+def test_subsample_init(O, ctx, n, ns):
+    import paper_2206_07630_b200 as sk
+    p = gen.c4(n=n, ns=ns)
+    tol = 1e-4
+    pot, side, inner = sk.sinkhorn_init_subsample(ctx, _cuda(p.x), _cuda(p.y), _cuda(p.extra["idx_x"]),
+                                                  _cuda(p.extra["idx_y"]), p.eps, tol)
+    _, so, rin = O.init_subsample(p.x, p.y, p.extra["idx_x"], p.extra["idx_y"], p.eps, tol)
+    assert side == so == 0
+    from parity import count_tol
+    assert abs(inner["iterations"] - rin.iterations) <= count_tol(rin.iterations)
+    # lockstep: the oracle's inner solve replays exactly the GPU's inner sweep count, then Eq. (8)
+    w, z = p.x[p.extra["idx_x"]], p.y[p.extra["idx_y"]]
+    lock = O.sinkhorn(w, z, p.eps, tol=0, max_iter=inner["iterations"])
+    ref = O.subsample_extrapolate(p.x, z, lock.g, p.eps)
+    assert rel_inf(centred(pot.cpu().numpy()), centred(ref), p.eps) <= INIT_RTOL
