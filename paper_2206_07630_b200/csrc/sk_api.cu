@@ -260,14 +260,16 @@ sk_status solve_multikernel(sk_ctx *ctx, const Problem &P, sk_report *rep) {
     const long long bs_rows = shard_block_rows(n_glob);
     const int nblk_glob = (int)((n_glob + bs_rows - 1) / bs_rows);
     const int blk_per_rank = sharded ? SK_SHARD_BLOCKS / P.world : nblk_glob;
-    const int nblk_local = sharded ? (int)((n + bs_rows - 1) / bs_rows) : nblk_glob;
     const int occ = stored ? 8 : lse_occupancy_ctas(D);
     const int Rr = D <= 4 ? 4 : (D <= 16 ? 2 : 1);
     const long long ptiles_col = stored ? (m + 511) / 512 : (m + 128LL * Rr - 1) / (128LL * Rr);
     const long long ptiles_row = stored ? (n + 7) / 8 : (n + 128LL * Rr - 1) / (128LL * Rr);
     const int split_q = choose_split(ptiles_col * SK_SHARD_BLOCKS / std::max(P.world, 1),
                                      stored ? bs_rows / 64 : bs_rows / tq, occ, 64);
-    const int nsplit_col = SK_SHARD_BLOCKS * split_q;  // global split count
+    // merged split count: sharded ranks always contribute blk_per_rank blocks (empty blocks
+    // write (-inf, 0) partials), so the merge sees SK_SHARD_BLOCKS * split_q slots.
+    const int nblk_launch = sharded ? blk_per_rank : nblk_glob;
+    const int nsplit_col = (sharded ? SK_SHARD_BLOCKS : nblk_glob) * split_q;
     const int split_row = stored ? 1 : choose_split(ptiles_row, yt, occ, 64);
     const long long part_elems = std::max((long long)nsplit_col * m, (long long)split_row * n);
     ENSURE(part, float2, B_PART, part_elems);
@@ -296,13 +298,13 @@ sk_status solve_multikernel(sk_ctx *ctx, const Problem &P, sk_report *rep) {
         build_ms = ms;
     }
 
-    LsePass colp{&Y, &X, nblk_local, (int)(bs_rows / tq), split_q,
+    LsePass colp{&Y, &X, nblk_launch, (int)(bs_rows / tq), split_q,
                  part + (sharded ? (long long)P.rank * blk_per_rank * split_q * m : 0), P.eps,
                  &status->stop};
     LsePass rowp{&X, &Y, 1, 0, split_row, part, P.eps, &status->stop};
     StoredPass scol{C, n, m, P.eps, xpack,
                     part + (sharded ? (long long)P.rank * blk_per_rank * split_q * m : 0),
-                    bs_rows, nblk_local, split_q, &status->stop};
+                    bs_rows, nblk_launch, split_q, &status->stop};
     StoredPass srow{C, n, m, P.eps, ypack, part, 0, 1, 1, &status->stop};
     MergePass mcol{MERGE_COL, &Y, part, nsplit_col, P.eps, P.b, status, blke, blkb, nullptr, 0.f,
                    sharded ? 1 : 0};
