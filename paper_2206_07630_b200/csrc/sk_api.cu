@@ -76,7 +76,7 @@ enum BufId {
     B_STAGE0 = 0, B_STAGE_END = 16,   // staging of host arrays
     B_FLAG = 16, B_XPACK, B_XC, B_XNK, B_XPOT, B_YPACK, B_YC, B_YNK, B_YPOT, B_PART, B_BLKE, B_BLKB,
     B_STATUS, B_COST, B_REP, B_SORT, B_PERM, B_YSORT, B_GAUSS, B_GAUSS2, B_GMM, B_SUBW, B_SUBZ,
-    B_SUBF, B_SUBG, B_IDX, B_OUT, B_FA, B_NBUF
+    B_SUBF, B_SUBG, B_IDX, B_OUT, B_FA, B_QUEUE, B_NBUF
 };
 
 sk_status fail(sk_ctx *c, sk_status s, const char *fmt, ...) {
@@ -756,11 +756,12 @@ sk_status solve_impl(sk_ctx *ctx, int64_t B, int64_t n, int64_t m, int32_t d, co
     const bool small = batched_supported(d, (int)n, (int)m) && (B > 1 || (double)n * m <= (double)(1 << 18));
     if (small && mode != SK_COST_STORED) {
         ENSURE(rp, char, B_REP, (size_t)B * (3 * sizeof(int) + sizeof(float) + sizeof(double)) + 64);
+        ENSURE(queue, int, B_QUEUE, 4);
         double *E = (double *)rp;
         int *iters = (int *)(E + B), *conv = iters + B, *nonf = conv + B;
         float *err = (float *)(nonf + B);
         BatchLaunch L;
-        L.B = (int)B; L.n = (int)n; L.m = (int)m; L.d = d;
+        L.B = (int)B; L.n = (int)n; L.m = (int)m; L.d = d; L.queue = queue;
         L.x = x; L.x_stride = xs; L.y = y; L.y_stride = ys;
         L.a = a; L.a_stride = as; L.b = b; L.b_stride = bs;
         L.finit = f_init; L.f = f; L.g = g; L.eps = eps; L.tol = tol;

@@ -14,11 +14,14 @@
 #include "sk_internal.h"
 #include "sk_lse_tile.cuh"
 
+#include <algorithm>
+
 namespace sk {
 
-constexpr int kBT = 256;  // threads per CTA
 
 struct BatchArgs {
+    int B;
+    int *queue;                     // dynamic problem queue (zeroed before launch)
     const float *x; long long xs;   // per-problem strides in floats (0 = shared)
     const float *y; long long ys;
     const float *a; long long as;   // nullable (uniform)
@@ -45,17 +48,17 @@ size_t batched_smem_bytes(int D, int n, int m) {
 
 // One LSE pass over all P points owned by this CTA (R per thread per round).
 // out(p, M, S) is called for every valid p by the thread that owns it.
-template <int D, int R, typename Out>
+template <int D, int R, int NT, typename Out>
 __device__ __forceinline__ void onchip_pass(const float *__restrict__ pc, int pstride, int P,
                                             const float *__restrict__ qc, const float *__restrict__ qw,
                                             int Qp, float tk, Out out) {
-    for (int pb = 0; pb < P; pb += R * kBT) {
+    for (int pb = 0; pb < P; pb += R * NT) {
         float2 pd[R][D];
         float M[R];
         float2 S[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-            const int p = pb + r * kBT + threadIdx.x;
+            const int p = pb + r * NT + threadIdx.x;
 #pragma unroll
             for (int k = 0; k < D; ++k) {
                 const float v = p < P ? pc[k * pstride + p] * tk : 0.f;
@@ -67,18 +70,17 @@ __device__ __forceinline__ void onchip_pass(const float *__restrict__ pc, int ps
         for (int q = 0; q < Qp; q += kChunk) lse_chunk<D, R>(qc, Qp, qw, q, pd, M, S);
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-            const int p = pb + r * kBT + threadIdx.x;
+            const int p = pb + r * NT + threadIdx.x;
             if (p < P) out(p, M[r], S[r].x + S[r].y);
         }
     }
 }
 
-template <int D, int R>
-__global__ void __launch_bounds__(kBT) k_batched(BatchArgs A) {
-    extern __shared__ __align__(16) float sm[];
+// Solve problem `prob` with the whole CTA.
+template <int D, int R, int NT>
+__device__ __forceinline__ void solve_one(const BatchArgs &A, int prob, float *sm) {
     const int n = A.n, m = A.m;
     const int Np = round_up(n, kChunk), Mp = round_up(m, kChunk);
-    const int prob = blockIdx.x;
     const float eps = A.eps;
     const float kap = kLog2e / eps;     // log2(e)/eps
     const float tk = 2.f * kap;         // scale of the cross term
@@ -104,7 +106,7 @@ __global__ void __launch_bounds__(kBT) k_batched(BatchArgs A) {
     const float loga_u = (float)(-log((double)n)), logb_u = (float)(-log((double)m));
 
     // ---- load + precompute (K1)
-    for (int i = threadIdx.x; i < Np; i += kBT) {
+    for (int i = threadIdx.x; i < Np; i += NT) {
         if (i < n) {
             float s = 0.f;
 #pragma unroll
@@ -125,7 +127,7 @@ __global__ void __launch_bounds__(kBT) k_batched(BatchArgs A) {
             wx[i] = -INFINITY;
         }
     }
-    for (int j = threadIdx.x; j < Mp; j += kBT) {
+    for (int j = threadIdx.x; j < Mp; j += NT) {
         if (j < m) {
             float s = 0.f;
 #pragma unroll
@@ -154,18 +156,18 @@ __global__ void __launch_bounds__(kBT) k_batched(BatchArgs A) {
         double e_loc = 0.0;
         int bad = 0;
         float *gold = gb + cur * m, *gnew = gb + (cur ^ 1) * m;
-        onchip_pass<D, R>(yq, Mp, m, xq, wx, Np, tk, [&](int j, float Mv, float Sv) {
+        onchip_pass<D, R, NT>(yq, Mp, m, xq, wx, Np, tk, [&](int j, float Mv, float Sv) {
             const float gn = cy[j] - epsln2 * (Mv + log2f(Sv));
             gnew[j] = gn;
             wy[j] = fmaf(gn, kap, -nyk[j]);
             bad |= !isfinite(gn);
             if (check) {
-                const float bj = b ? b[j] : __expf(logb_u);
-                e_loc += (double)bj * fabs((double)expm1f((gold[j] - gn) / eps));
+                const double bj = b ? (double)b[j] : 1.0 / m;
+                e_loc += bj * fabs((double)expm1f((gold[j] - gn) / eps));
             }
         });
-        const double e_tot = block_sum_d<kBT>(e_loc, red);
-        const int any_bad = block_or<kBT>(bad, redi);
+        const double e_tot = block_sum_d<NT>(e_loc, red);
+        const int any_bad = block_or<NT>(bad, redi);
         if (any_bad) { nonfin = 1; break; }
         if (check) {
             err = (float)e_tot;
@@ -175,13 +177,13 @@ __global__ void __launch_bounds__(kBT) k_batched(BatchArgs A) {
         // ---- row pass: f^{l+1} (P = x, Q = y); wy is visible after the block reductions' barriers
         float *fnew = fb + (cur ^ 1) * n;
         bad = 0;
-        onchip_pass<D, R>(xq, Np, n, yq, wy, Mp, tk, [&](int i, float Mv, float Sv) {
+        onchip_pass<D, R, NT>(xq, Np, n, yq, wy, Mp, tk, [&](int i, float Mv, float Sv) {
             const float fn = cx[i] - epsln2 * (Mv + log2f(Sv));
             fnew[i] = fn;
             wx[i] = fmaf(fn, kap, -nxk[i]);
             bad |= !isfinite(fn);
         });
-        if (block_or<kBT>(bad, redi)) { nonfin = 1; break; }
+        if (block_or<NT>(bad, redi)) { nonfin = 1; break; }
         cur ^= 1;
         ++l;
     }
@@ -189,16 +191,16 @@ __global__ void __launch_bounds__(kBT) k_batched(BatchArgs A) {
     // ---- epilogue: (f^l, g^l), E = <f,a> + <g,b> - eps sum(a) (Eq. 2 after an f-update), report
     const float *fo = fb + cur * n, *go = gb + cur * m;
     double s = 0.0;
-    for (int i = threadIdx.x; i < n; i += kBT) {
+    for (int i = threadIdx.x; i < n; i += NT) {
         A.f[(size_t)prob * n + i] = fo[i];
         const double ai = a ? (double)a[i] : 1.0 / n;
         s += (double)fo[i] * ai - (double)eps * ai;
     }
-    for (int j = threadIdx.x; j < m; j += kBT) {
+    for (int j = threadIdx.x; j < m; j += NT) {
         A.g[(size_t)prob * m + j] = go[j];
         s += (double)go[j] * (b ? (double)b[j] : 1.0 / m);
     }
-    const double E = block_sum_d<kBT>(s, red);
+    const double E = block_sum_d<NT>(s, red);
     if (threadIdx.x == 0) {
         A.iters[prob] = l;
         A.conv[prob] = conv;
@@ -206,24 +208,49 @@ __global__ void __launch_bounds__(kBT) k_batched(BatchArgs A) {
         A.err[prob] = err;
         A.E[prob] = E;
     }
+    __syncthreads();  // smem is reused by the next problem
 }
 
-template <int D, int R>
+// Persistent CTAs (one or two per SM) pull problems from a global queue: iteration
+// counts differ per problem, so dynamic assignment balances the SMs.
+template <int D, int R, int NT>
+__global__ void __launch_bounds__(NT) k_batched(BatchArgs A) {
+    extern __shared__ __align__(16) float sm[];
+    __shared__ int s_prob;
+    for (;;) {
+        if (threadIdx.x == 0) s_prob = atomicAdd(A.queue, 1);
+        __syncthreads();
+        const int prob = s_prob;
+        __syncthreads();
+        if (prob >= A.B) break;
+        solve_one<D, R, NT>(A, prob, sm);
+    }
+}
+
+template <int D, int R, int NT>
 static cudaError_t launch_batched_t(const BatchArgs &A, int B, cudaStream_t st) {
     const size_t smem = batched_smem_bytes(D, A.n, A.m);
-    cudaError_t e = cudaFuncSetAttribute(k_batched<D, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(k_batched<D, R, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
-    k_batched<D, R><<<B, kBT, smem, st>>>(A);
+    int occ = 0, dev = 0, nsm = 148;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_batched<D, R, NT>, NT, smem);
+    if (e != cudaSuccess) return e;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const int grid = std::max(1, std::min(B, nsm * std::max(occ, 1)));
+    k_batched<D, R, NT><<<grid, NT, smem, st>>>(A);
     return cudaGetLastError();
 }
 
+// One wide CTA per problem: NT threads x R output points per thread per round.
 template <int D>
 static cudaError_t launch_batched_d(const BatchArgs &A, int B, cudaStream_t st) {
     const int P = A.n > A.m ? A.n : A.m;
-    if (P > 2 * kBT) return launch_batched_t<D, 4>(A, B, st);
-    if (P > kBT) return launch_batched_t<D, 2>(A, B, st);
-    return launch_batched_t<D, 1>(A, B, st);
+    if (P <= 256) return launch_batched_t<D, 1, 256>(A, B, st);
+    if (P <= 512) return launch_batched_t<D, 1, 512>(A, B, st);
+    if (P <= 1024) return launch_batched_t<D, 1, 1024>(A, B, st);
+    return launch_batched_t<D, 2, 1024>(A, B, st);  // more rounds of 2048 points for larger P
 }
 
 bool batched_supported(int d, int n, int m) {
@@ -232,6 +259,10 @@ bool batched_supported(int d, int n, int m) {
 
 cudaError_t launch_batched(const BatchLaunch &L, cudaStream_t st) {
     BatchArgs A;
+    A.B = L.B;
+    A.queue = L.queue;
+    cudaError_t e = cudaMemsetAsync(L.queue, 0, sizeof(int), st);
+    if (e != cudaSuccess) return e;
     A.x = L.x; A.xs = L.x_stride; A.y = L.y; A.ys = L.y_stride;
     A.a = L.a; A.as = L.a_stride; A.b = L.b; A.bs = L.b_stride;
     A.finit = L.finit; A.fs = L.n;

@@ -9,6 +9,7 @@ namespace sk {
 // ------------------------------------------------------------ K13 on-chip
 struct BatchLaunch {
     int B, n, m, d;
+    int *queue;       // device int (dynamic problem queue)
     const float *x; long long x_stride;
     const float *y; long long y_stride;
     const float *a; long long a_stride;
