@@ -15,6 +15,7 @@
 #include "sk_lse_tile.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace sk {
 
@@ -42,16 +43,22 @@ size_t batched_smem_bytes(int D, int n, int m) {
     const int Np = round_up(n, kChunk), Mp = round_up(m, kChunk);
     size_t floats = (size_t)(D + 1) * (Np + Mp)   // packed coords + w, both sides
                     + 2 * (size_t)(n + m)         // finalize constant c and ||.||^2 kappa
-                    + 2 * (size_t)(n + m);        // double-buffered f and g
+                    + 2 * (size_t)(n + m)         // double-buffered f and g
+                    + (size_t)(n + m);            // last running max per point (seed)
     return floats * sizeof(float) + 64 * sizeof(double);
 }
 
+constexpr float kSeedMargin = 4.f;   // log2 units added to the previous sweep's max
+
 // One LSE pass over all P points owned by this CTA (R per thread per round).
+// First sweep: exact online max per chunk (lse_chunk).  Later sweeps: the shift is
+// fixed at the point's previous LSE + kSeedMargin (lse_chunk_seeded: no max, no
+// rescale); if the sum leaves [2^-100, 2^100] the point is recomputed exactly.
 // out(p, M, S) is called for every valid p by the thread that owns it.
-template <int D, int R, int NT, typename Out>
+template <int D, int R, int NT, int EMU, typename Out>
 __device__ __forceinline__ void onchip_pass(const float *__restrict__ pc, int pstride, int P,
                                             const float *__restrict__ qc, const float *__restrict__ qw,
-                                            int Qp, float tk, Out out) {
+                                            int Qp, float tk, float *pm, bool seeded, Out out) {
     for (int pb = 0; pb < P; pb += R * NT) {
         float2 pd[R][D];
         float M[R];
@@ -64,20 +71,37 @@ __device__ __forceinline__ void onchip_pass(const float *__restrict__ pc, int ps
                 const float v = p < P ? pc[k * pstride + p] * tk : 0.f;
                 pd[r][k] = make_float2(v, v);
             }
-            M[r] = -INFINITY;
+            M[r] = seeded && p < P ? pm[p] + kSeedMargin : -INFINITY;
             S[r] = make_float2(0.f, 0.f);
         }
-        for (int q = 0; q < Qp; q += kChunk) lse_chunk<D, R>(qc, Qp, qw, q, pd, M, S);
+        if (seeded) {
+            for (int q = 0; q < Qp; q += kChunk) lse_chunk_seeded<D, R, EMU>(qc, Qp, qw, q, pd, M, S);
+        } else {
+            for (int q = 0; q < Qp; q += kChunk) lse_chunk<D, R, EMU>(qc, Qp, qw, q, pd, M, S);
+        }
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             const int p = pb + r * NT + threadIdx.x;
-            if (p < P) out(p, M[r], S[r].x + S[r].y);
+            if (p >= P) continue;
+            float Sv = S[r].x + S[r].y;
+            if (!(Sv >= 0x1p-100f && Sv <= 0x1p100f)) {  // seed far off the true max: exact recompute
+                float2 Sr[1] = {make_float2(0.f, 0.f)};
+                float Mr[1] = {-INFINITY};
+                float2 pr[1][D];
+#pragma unroll
+                for (int k = 0; k < D; ++k) pr[0][k] = pd[r][k];
+                for (int q = 0; q < Qp; q += kChunk) lse_chunk<D, 1, 0>(qc, Qp, qw, q, pr, Mr, Sr);
+                M[r] = Mr[0];
+                Sv = Sr[0].x + Sr[0].y;
+            }
+            pm[p] = M[r] + log2f(Sv);  // this sweep's LSE: the next sweep's seed
+            out(p, M[r], Sv);
         }
     }
 }
 
 // Solve problem `prob` with the whole CTA.
-template <int D, int R, int NT>
+template <int D, int R, int NT, int EMU>
 __device__ __forceinline__ void solve_one(const BatchArgs &A, int prob, float *sm) {
     const int n = A.n, m = A.m;
     const int Np = round_up(n, kChunk), Mp = round_up(m, kChunk);
@@ -96,7 +120,9 @@ __device__ __forceinline__ void solve_one(const BatchArgs &A, int prob, float *s
     float *nyk = cy + m;                // [m]
     float *fb = nyk + m;                // [2][n]
     float *gb = fb + 2 * n;             // [2][m]
-    double *red = reinterpret_cast<double *>(gb + 2 * m + ((2 * m) & 1));  // scratch
+    float *mxs = gb + 2 * m;            // [n]    last running max (x side, row pass)
+    float *mys = mxs + n;               // [m]    (y side, column pass)
+    double *red = reinterpret_cast<double *>(mys + m + ((n + m) & 1));  // scratch
     int *redi = reinterpret_cast<int *>(red + 32);
 
     const float *x = A.x + prob * A.xs;
@@ -121,6 +147,7 @@ __device__ __forceinline__ void solve_one(const BatchArgs &A, int prob, float *s
             const float f0 = A.finit ? A.finit[(size_t)prob * A.fs + i] : 0.f;
             fb[i] = f0;
             wx[i] = fmaf(f0, kap, -nxk[i]);
+            mxs[i] = -INFINITY;
         } else {
 #pragma unroll
             for (int k = 0; k < D; ++k) xq[k * Np + i] = 0.f;
@@ -140,6 +167,7 @@ __device__ __forceinline__ void solve_one(const BatchArgs &A, int prob, float *s
             cy[j] = fmaf(eps, lb, s);
             nyk[j] = s * kap;
             gb[j] = 0.f;  // g^(0) = 0 (only f^(0) is needed)
+            mys[j] = -INFINITY;
         } else {
 #pragma unroll
             for (int k = 0; k < D; ++k) yq[k * Mp + j] = 0.f;
@@ -156,7 +184,7 @@ __device__ __forceinline__ void solve_one(const BatchArgs &A, int prob, float *s
         double e_loc = 0.0;
         int bad = 0;
         float *gold = gb + cur * m, *gnew = gb + (cur ^ 1) * m;
-        onchip_pass<D, R, NT>(yq, Mp, m, xq, wx, Np, tk, [&](int j, float Mv, float Sv) {
+        onchip_pass<D, R, NT, EMU>(yq, Mp, m, xq, wx, Np, tk, mys, l >= 1, [&](int j, float Mv, float Sv) {
             const float gn = cy[j] - epsln2 * (Mv + log2f(Sv));
             gnew[j] = gn;
             wy[j] = fmaf(gn, kap, -nyk[j]);
@@ -177,7 +205,7 @@ __device__ __forceinline__ void solve_one(const BatchArgs &A, int prob, float *s
         // ---- row pass: f^{l+1} (P = x, Q = y); wy is visible after the block reductions' barriers
         float *fnew = fb + (cur ^ 1) * n;
         bad = 0;
-        onchip_pass<D, R, NT>(xq, Np, n, yq, wy, Mp, tk, [&](int i, float Mv, float Sv) {
+        onchip_pass<D, R, NT, EMU>(xq, Np, n, yq, wy, Mp, tk, mxs, l >= 1, [&](int i, float Mv, float Sv) {
             const float fn = cx[i] - epsln2 * (Mv + log2f(Sv));
             fnew[i] = fn;
             wx[i] = fmaf(fn, kap, -nxk[i]);
@@ -213,7 +241,7 @@ __device__ __forceinline__ void solve_one(const BatchArgs &A, int prob, float *s
 
 // Persistent CTAs (one or two per SM) pull problems from a global queue: iteration
 // counts differ per problem, so dynamic assignment balances the SMs.
-template <int D, int R, int NT>
+template <int D, int R, int NT, int EMU>
 __global__ void __launch_bounds__(NT) k_batched(BatchArgs A) {
     extern __shared__ __align__(16) float sm[];
     __shared__ int s_prob;
@@ -223,34 +251,56 @@ __global__ void __launch_bounds__(NT) k_batched(BatchArgs A) {
         const int prob = s_prob;
         __syncthreads();
         if (prob >= A.B) break;
-        solve_one<D, R, NT>(A, prob, sm);
+        solve_one<D, R, NT, EMU>(A, prob, sm);
     }
 }
 
-template <int D, int R, int NT>
+// EMU: exponential pairs (of 4 per chunk) evaluated on the FMA pipe instead of MUFU.
+// Default 1 (25%); SK_BATCHED_EMU=0..2 overrides it (tuning knob).
+static int batched_emu() {
+    static int v = [] {
+        const char *e = getenv("SK_BATCHED_EMU");
+        int x = e ? atoi(e) : 1;
+        return x < 0 ? 0 : (x > 2 ? 2 : x);
+    }();
+    return v;
+}
+
+template <int D, int R, int NT, int EMU>
 static cudaError_t launch_batched_t(const BatchArgs &A, int B, cudaStream_t st) {
     const size_t smem = batched_smem_bytes(D, A.n, A.m);
-    cudaError_t e = cudaFuncSetAttribute(k_batched<D, R, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(k_batched<D, R, NT, EMU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
     int occ = 0, dev = 0, nsm = 148;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_batched<D, R, NT>, NT, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_batched<D, R, NT, EMU>, NT, smem);
     if (e != cudaSuccess) return e;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     const int grid = std::max(1, std::min(B, nsm * std::max(occ, 1)));
-    k_batched<D, R, NT><<<grid, NT, smem, st>>>(A);
+    k_batched<D, R, NT, EMU><<<grid, NT, smem, st>>>(A);
     return cudaGetLastError();
 }
 
+template <int D, int R, int NT>
+static cudaError_t launch_batched_e(const BatchArgs &A, int B, cudaStream_t st) {
+    switch (batched_emu()) {
+        case 0: return launch_batched_t<D, R, NT, 0>(A, B, st);
+        case 2: return launch_batched_t<D, R, NT, 2>(A, B, st);
+        default: return launch_batched_t<D, R, NT, 1>(A, B, st);
+    }
+}
+
 // One wide CTA per problem: NT threads x R output points per thread per round.
+// SK_BATCHED_SHAPE=1 selects 512 threads x 2 points for 512 < P <= 1024 (tuning knob).
 template <int D>
 static cudaError_t launch_batched_d(const BatchArgs &A, int B, cudaStream_t st) {
+    static int shape = [] { const char *e = getenv("SK_BATCHED_SHAPE"); return e ? atoi(e) : 1; }();
     const int P = A.n > A.m ? A.n : A.m;
-    if (P <= 256) return launch_batched_t<D, 1, 256>(A, B, st);
-    if (P <= 512) return launch_batched_t<D, 1, 512>(A, B, st);
-    if (P <= 1024) return launch_batched_t<D, 1, 1024>(A, B, st);
-    return launch_batched_t<D, 2, 1024>(A, B, st);  // more rounds of 2048 points for larger P
+    if (P <= 256) return launch_batched_e<D, 1, 256>(A, B, st);
+    if (P <= 512) return launch_batched_e<D, 1, 512>(A, B, st);
+    if (P <= 1024) return shape == 1 ? launch_batched_e<D, 2, 512>(A, B, st) : launch_batched_e<D, 1, 1024>(A, B, st);
+    return launch_batched_e<D, 2, 1024>(A, B, st);  // more rounds of 2048 points for larger P
 }
 
 bool batched_supported(int d, int n, int m) {
