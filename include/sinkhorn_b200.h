@@ -217,6 +217,19 @@ sk_status sinkhorn_solve_sharded(sk_ctx *ctx, int64_t n_total, int64_t row0, int
                                  const float *f_init_local, float *f_local, float *g,
                                  sk_report *rep /* host */);
 
+/* Test / diagnostic entry: the sharded algorithm of sinkhorn_solve_sharded for
+ * `world` virtual ranks inside one process on one GPU.  Every sweep each virtual
+ * rank computes the column partials of its sk_shard_rows row block into its own
+ * slots (what ncclAllGather delivers on a real box), then the same rank-order merge
+ * runs once.  Same partition, kernels and merge order, hence bit-identical to a
+ * world-GPU run and to world = 1; it exercises the partial/merge math without
+ * NCCL.  x, a, f_init, f: all n rows (global order).  Blocks. */
+sk_status sinkhorn_solve_sharded_emulated(sk_ctx *ctx, int32_t world, int64_t n, int64_t m, int32_t d,
+                                          const float *x, const float *y, const float *a,
+                                          const float *b, float eps, float tol, int32_t max_iter,
+                                          int32_t check_every, sk_cost_mode mode, const float *f_init,
+                                          float *f, float *g, sk_report *rep /* host */);
+
 #ifdef __cplusplus
 }
 #endif

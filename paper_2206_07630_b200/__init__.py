@@ -20,6 +20,7 @@ from ._lib import (SK_COST_AUTO, SK_COST_ONLINE, SK_COST_STORED, SK_SHARD_BLOCKS
                    SkReport)
 
 __all__ = ["Context", "SinkhornError", "sinkhorn_solve", "sinkhorn_solve_sharded",
+           "sinkhorn_solve_sharded_emulated",
            "sinkhorn_init_zero", "sinkhorn_init_sort1d", "sinkhorn_init_gaussian",
            "sinkhorn_init_gmm", "sinkhorn_init_subsample", "sinkhorn_sort1d_batched",
            "shard_rows", "SK_COST_AUTO", "SK_COST_ONLINE", "SK_COST_STORED", "SK_SHARD_BLOCKS"]
@@ -207,6 +208,21 @@ def sinkhorn_solve(ctx: Context, x, y, eps: float, tol: float = 1e-3, max_iter: 
     if single:
         return f.view(n), g.view(m), out[0]
     return f, g, out
+
+
+def sinkhorn_solve_sharded_emulated(ctx: Context, world: int, x, y, eps: float, tol: float = 1e-3,
+                                    max_iter: int = 10000, check_every: int = 1, a=None, b=None,
+                                    mode: str = "auto", f_init=None):
+    """The row-sharded algorithm for `world` virtual ranks on one GPU (test entry)."""
+    n, d = x.shape
+    m = y.shape[0]
+    f = _empty((n,), x)
+    g = _empty((m,), x)
+    rep = SkReport()
+    ctx.check(ctx.lib.sinkhorn_solve_sharded_emulated(
+        ctx.h, world, n, m, d, _ptr(x), _ptr(y), _ptr(a), _ptr(b), float(eps), float(tol),
+        int(max_iter), int(check_every), _MODES[mode], _ptr(f_init), _ptr(f), _ptr(g), ctypes.byref(rep)))
+    return f, g, rep.as_dict()
 
 
 def sinkhorn_solve_sharded(ctx: Context, n_total: int, row0: int, x_local, y, eps: float,

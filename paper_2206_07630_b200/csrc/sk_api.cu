@@ -218,98 +218,122 @@ long long shard_block_rows(long long n) {
 }
 
 // ------------------------------------------------------------ the solve core
+// One problem: all m columns, and the rows of one or more "rank slices".  The
+// real sharded path has one slice per process and an ncclAllGather of the column
+// partials; the unsharded path has one slice covering all rows; the emulated
+// path (testing) has `world` slices in one process whose column partials land in
+// their slots directly.  The partition of rows into SK_SHARD_BLOCKS fixed blocks
+// and of each block into split_q sub-splits depends on (n_total, m, d) only, so all
+// three produce bit-identical results.
+struct Slice {
+    long long row0, n;
+    const float *x, *a, *f_init;
+    float *f;               // device output (n)
+    int rank;
+};
+
 struct Problem {
-    long long n, m;       // local rows n (this rank), all columns m
-    long long n_total;    // global rows (sharded) — for uniform weights and E
+    long long n_total, m;
     int d;
-    const float *x, *y, *a, *b, *f_init;
+    const float *y, *b;
     float eps, tol;
     int max_iter, check_every;
     sk_cost_mode mode;
-    float *f, *g;         // device outputs
-    int rank, world;      // world > 1: sharded
+    float *g;               // device output (m)
+    int world;              // ranks of the partition (1 = unsharded)
+    bool nccl;              // partials exchanged with ncclAllGather (one local slice)
 };
 
-sk_status solve_multikernel(sk_ctx *ctx, const Problem &P, sk_report *rep) {
+sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, sk_report *rep) {
     cudaStream_t st = ctx->stream;
     const bool sharded = P.world > 1;
-    const long long n = P.n, m = P.m;
+    const long long m = P.m, n_glob = P.n_total;
+    const int ns = (int)slices.size();
+    long long n_max = 0, n_sum = 0;
+    for (auto &sl : slices) { n_max = std::max(n_max, sl.n); n_sum += sl.n; }
     const bool stored_ok = P.d >= 1 && (m % 4 == 0);
     bool stored = P.mode == SK_COST_STORED;
-    if (P.mode == SK_COST_AUTO) stored = stored_ok && P.d >= 8 && P.d < 32 && 4.0 * n * m <= 8.0e9;
+    if (P.mode == SK_COST_AUTO) stored = stored_ok && P.d >= 8 && P.d < 32 && 4.0 * n_sum * m <= 8.0e9;
     if (stored && !stored_ok) return fail(ctx, SK_EUNSUPPORTED, "stored-cost mode needs m %% 4 == 0");
     const int D = stored ? 0 : lse_dpad(P.d);
     if (!stored && D == 0) return fail(ctx, SK_EUNSUPPORTED, "online path supports d <= 64");
     const int tq = stored ? 256 : lse_tq(D);
-    const long long xt = lse_tiles(n, tq), yt = lse_tiles(m, tq);
+    const long long yt = lse_tiles(m, tq);
 
-    ENSURE(xpack, float, B_XPACK, xt * (D + 1) * tq);
-    ENSURE(xc, float, B_XC, n);
-    ENSURE(xnk, float, B_XNK, n);
-    ENSURE(xpot, float, B_XPOT, 2 * n);
+    // per-slice X sides, carved from one allocation per array
+    std::vector<long long> off(ns + 1, 0), offp(ns + 1, 0);
+    for (int i = 0; i < ns; ++i) {
+        off[i + 1] = off[i] + slices[i].n;
+        offp[i + 1] = offp[i] + lse_tiles(slices[i].n, tq) * (D + 1) * tq;
+    }
+    ENSURE(xpack, float, B_XPACK, offp[ns]);
+    ENSURE(xc, float, B_XC, off[ns]);
+    ENSURE(xnk, float, B_XNK, off[ns]);
+    ENSURE(xpot, float, B_XPOT, 2 * off[ns]);
     ENSURE(ypack, float, B_YPACK, yt * (D + 1) * tq);
     ENSURE(yc, float, B_YC, m);
     ENSURE(ynk, float, B_YNK, m);
     ENSURE(ypot, float, B_YPOT, 2 * m);
     ENSURE(status, DevStatus, B_STATUS, 1);
-    Side X{(int)n, P.d, D, tq, xpack, xc, xnk, {xpot, xpot + n}};
+    std::vector<Side> X(ns);
+    for (int i = 0; i < ns; ++i) {
+        const long long n = slices[i].n;
+        X[i] = Side{(int)n, P.d, D, tq, xpack + offp[i], xc + off[i], xnk + off[i],
+                    {xpot + 2 * off[i], xpot + 2 * off[i] + n}};
+    }
     Side Y{(int)m, P.d, D, tq, ypack, yc, ynk, {ypot, ypot + m}};
 
-    // column-pass partition: SK_SHARD_BLOCKS fixed row blocks (global), split_q sub-splits each
-    const long long n_glob = sharded ? P.n_total : n;
+    // column-pass partition (a function of n_total, m, d only): SK_SHARD_BLOCKS fixed row
+    // blocks, each cut into split_q sub-splits sized for the 8-rank launch; empty blocks
+    // write (-inf, 0) partials.
     const long long bs_rows = shard_block_rows(n_glob);
     const int nblk_glob = (int)((n_glob + bs_rows - 1) / bs_rows);
     const int blk_per_rank = sharded ? SK_SHARD_BLOCKS / P.world : nblk_glob;
     const int occ = stored ? 8 : lse_occupancy_ctas(D);
     const int Rr = D <= 4 ? 4 : (D <= 16 ? 2 : 1);
     const long long ptiles_col = stored ? (m + 511) / 512 : (m + 128LL * Rr - 1) / (128LL * Rr);
-    const long long ptiles_row = stored ? (n + 7) / 8 : (n + 128LL * Rr - 1) / (128LL * Rr);
-    const int split_q = choose_split(ptiles_col * SK_SHARD_BLOCKS / std::max(P.world, 1),
-                                     stored ? bs_rows / 64 : bs_rows / tq, occ, 64);
-    // merged split count: sharded ranks always contribute blk_per_rank blocks (empty blocks
-    // write (-inf, 0) partials), so the merge sees SK_SHARD_BLOCKS * split_q slots.
-    const int nblk_launch = sharded ? blk_per_rank : nblk_glob;
+    const int split_q = choose_split(ptiles_col, stored ? bs_rows / 64 : bs_rows / tq, occ, 64);
     const int nsplit_col = (sharded ? SK_SHARD_BLOCKS : nblk_glob) * split_q;
-    const int split_row = stored ? 1 : choose_split(ptiles_row, yt, occ, 64);
-    const long long part_elems = std::max((long long)nsplit_col * m, (long long)split_row * n);
+    int split_row = 1;
+    if (!stored) {
+        const long long ptiles_row = (n_max + 128LL * Rr - 1) / (128LL * Rr);
+        split_row = choose_split(ptiles_row, yt, occ, 64);
+    }
+    const long long part_elems = std::max((long long)nsplit_col * m, (long long)split_row * n_max);
     ENSURE(part, float2, B_PART, part_elems);
     ENSURE(blke, double, B_BLKE, 2048);
     ENSURE(blkb, int, B_BLKB, 2048);
 
     const float loga_u = (float)(-std::log((double)n_glob)), logb_u = (float)(-std::log((double)m));
-    CU(pack_side(X, P.x, P.a, loga_u, P.f_init, P.eps, st));
+    for (int i = 0; i < ns; ++i)
+        CU(pack_side(X[i], slices[i].x, slices[i].a, loga_u, slices[i].f_init, P.eps, st));
     CU(pack_side(Y, P.y, P.b, logb_u, nullptr, P.eps, st));
     CU(launch_status_init(status, P.max_iter, P.check_every, P.tol, st));
-    ctx->cnt.kernel_launches += 3;
+    ctx->cnt.kernel_launches += ns + 2;
 
-    float *C = nullptr;
+    std::vector<float *> C(ns, nullptr);
     double build_ms = 0.0;
     if (stored) {
         cudaError_t e;
-        C = (float *)ensure(ctx, B_COST, sizeof(float) * (size_t)n * m, &e);
-        if (!C) return fail(ctx, SK_ENOMEM, "stored cost needs %.2f GiB", 4.0 * n * m / (1 << 30));
+        float *Call = (float *)ensure(ctx, B_COST, sizeof(float) * (size_t)n_sum * m, &e);
+        if (!Call) return fail(ctx, SK_ENOMEM, "stored cost needs %.2f GiB", 4.0 * n_sum * m / (1 << 30));
         CU(cudaEventRecord(ctx->ev0, st));
-        CU(launch_build_cost(P.x, P.y, n, m, P.d, C, st));
+        for (int i = 0; i < ns; ++i) {
+            C[i] = Call + off[i] * m;
+            CU(launch_build_cost(slices[i].x, P.y, slices[i].n, m, P.d, C[i], st));
+            ctx->cnt.kernel_launches++;
+        }
         CU(cudaEventRecord(ctx->ev1, st));
-        ctx->cnt.kernel_launches++;
         CU(cudaEventSynchronize(ctx->ev1));
         float ms = 0.f;
         CU(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
         build_ms = ms;
     }
 
-    LsePass colp{&Y, &X, nblk_launch, (int)(bs_rows / tq), split_q,
-                 part + (sharded ? (long long)P.rank * blk_per_rank * split_q * m : 0), P.eps,
-                 &status->stop};
-    LsePass rowp{&X, &Y, 1, 0, split_row, part, P.eps, &status->stop};
-    StoredPass scol{C, n, m, P.eps, xpack,
-                    part + (sharded ? (long long)P.rank * blk_per_rank * split_q * m : 0),
-                    bs_rows, nblk_launch, split_q, &status->stop};
-    StoredPass srow{C, n, m, P.eps, ypack, part, 0, 1, 1, &status->stop};
+    const long long slot = (long long)blk_per_rank * split_q * m;   // one rank's partial slots
+    auto col_part = [&](int i) { return part + (sharded ? (long long)slices[i].rank * slot : 0); };
     MergePass mcol{MERGE_COL, &Y, part, nsplit_col, P.eps, P.b, status, blke, blkb, nullptr, 0.f,
-                   sharded ? 1 : 0};
-    MergePass mrow{MERGE_ROW, &X, part, stored ? 1 : split_row, P.eps, nullptr, status, blke, blkb,
-                   nullptr, 0.f, sharded ? 1 : 0};
+                   sharded ? 1 : 0, 0};
 
     CU(cudaEventRecord(ctx->ev0, st));
     int launched = 0, poll = 4;
@@ -317,20 +341,39 @@ sk_status solve_multikernel(sk_ctx *ctx, const Problem &P, sk_report *rep) {
     for (int it = 0; it < max_sweeps;) {
         const int chunk = std::min(poll, max_sweeps - it);
         for (int c = 0; c < chunk; ++c, ++it) {
-            if (stored) CU(launch_stored_cols(scol, st));
-            else CU(launch_lse(colp, st));
-            if (sharded) {
-                const size_t cnt = (size_t)blk_per_rank * split_q * m * 2;
-                int r = g_nccl.allgather(part + (long long)P.rank * blk_per_rank * split_q * m, part, cnt,
-                                         kNcclFloat32, ctx->comm, st);
+            for (int i = 0; i < ns; ++i) {
+                if (stored) {
+                    StoredPass scol{C[i], slices[i].n, m, P.eps, X[i].pack, col_part(i), bs_rows,
+                                    sharded ? blk_per_rank : nblk_glob, split_q, &status->stop};
+                    CU(launch_stored_cols(scol, st));
+                } else {
+                    LsePass colp{&Y, &X[i], sharded ? blk_per_rank : nblk_glob, (int)(bs_rows / tq), split_q,
+                                 col_part(i), P.eps, &status->stop};
+                    CU(launch_lse(colp, st));
+                }
+                ++launched;
+            }
+            if (P.nccl && sharded) {
+                int r = g_nccl.allgather(col_part(0), part, (size_t)slot * 2, kNcclFloat32, ctx->comm, st);
                 if (r != 0) return fail(ctx, SK_ENCCL, "ncclAllGather failed: %s",
                                         g_nccl.errstr ? g_nccl.errstr(r) : "?");
             }
             CU(launch_merge(mcol, st));
-            if (stored) CU(launch_stored_rows(srow, st));
-            else CU(launch_lse(rowp, st));
-            CU(launch_merge(mrow, st));
-            launched += 4;
+            ++launched;
+            for (int i = 0; i < ns; ++i) {
+                if (stored) {
+                    StoredPass srow{C[i], slices[i].n, m, P.eps, Y.pack, part, 0, 1, 1, &status->stop};
+                    CU(launch_stored_rows(srow, st));
+                } else {
+                    LsePass rowp{&X[i], &Y, 1, 0, split_row, part, P.eps, &status->stop};
+                    CU(launch_lse(rowp, st));
+                }
+                // only the last slice's merge advances the sweep counter
+                MergePass mrow{MERGE_ROW, &X[i], part, stored ? 1 : split_row, P.eps, nullptr, status, blke,
+                               blkb, nullptr, 0.f, sharded ? 1 : 0, i + 1 < ns ? 1 : 0};
+                CU(launch_merge(mrow, st));
+                launched += 2;
+            }
         }
         CU(cudaMemcpyAsync(ctx->h_status, status, sizeof(DevStatus), cudaMemcpyDeviceToHost, st));
         CU(cudaStreamSynchronize(st));
@@ -338,35 +381,41 @@ sk_status solve_multikernel(sk_ctx *ctx, const Problem &P, sk_report *rep) {
         poll = std::min(poll * 2, 64);
     }
     CU(cudaEventRecord(ctx->ev1, st));
-    CU(launch_report(X, Y, P.a, P.b, P.eps, status, sharded ? 1 : 0, n_glob, st));
-    launched++;
-    CU(cudaMemcpyAsync(ctx->h_status, status, sizeof(DevStatus), cudaMemcpyDeviceToHost, st));
-    CU(cudaStreamSynchronize(st));
+    // E = sum over slices (rank order) of <f,a> - eps sum(a), plus <g,b> (replicated)
+    std::vector<double> fa_parts;
+    double gb_part = 0.0;
+    for (int i = 0; i < ns; ++i) {
+        CU(launch_report(X[i], Y, slices[i].a, P.b, P.eps, status, 1, n_glob, st));
+        CU(cudaMemcpyAsync(ctx->h_status, status, sizeof(DevStatus), cudaMemcpyDeviceToHost, st));
+        CU(cudaStreamSynchronize(st));
+        fa_parts.push_back(ctx->h_status->fa_local);
+        gb_part = ctx->h_status->E;
+        launched++;
+    }
     float ms = 0.f;
     CU(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
     DevStatus hs = *ctx->h_status;
     if (!hs.stop) return fail(ctx, SK_ECUDA, "solver loop ended without a stop flag");
     const int L = hs.final_iter;
-    double E = hs.E;
-    if (sharded) {  // E = sum over ranks of <f,a> - eps sum(a) (rank order) + <g,b>
+    if (P.nccl && sharded) {  // gather every rank's <f,a> partial, sum in rank order
         ENSURE(fa, double, B_FA, P.world);
-        CU(cudaMemcpyAsync(fa + P.rank, &status->fa_local, sizeof(double), cudaMemcpyDeviceToDevice, st));
-        int r = g_nccl.allgather(fa + P.rank, fa, 1, kNcclFloat64, ctx->comm, st);
+        CU(cudaMemcpyAsync(fa + slices[0].rank, &status->fa_local, sizeof(double), cudaMemcpyDeviceToDevice, st));
+        int r = g_nccl.allgather(fa + slices[0].rank, fa, 1, kNcclFloat64, ctx->comm, st);
         if (r != 0) return fail(ctx, SK_ENCCL, "ncclAllGather(E) failed");
-        std::vector<double> h(P.world);
-        CU(cudaMemcpyAsync(h.data(), fa, sizeof(double) * P.world, cudaMemcpyDeviceToHost, st));
+        fa_parts.assign(P.world, 0.0);
+        CU(cudaMemcpyAsync(fa_parts.data(), fa, sizeof(double) * P.world, cudaMemcpyDeviceToHost, st));
         CU(cudaStreamSynchronize(st));
-        double s = 0.0;
-        for (int i = 0; i < P.world; ++i) s += h[i];
-        E = s + hs.E;
     }
-    CU(cudaMemcpyAsync(P.f, X.pot[L & 1], sizeof(float) * n, cudaMemcpyDeviceToDevice, st));
+    double E = 0.0;
+    for (double v : fa_parts) E += v;
+    E += gb_part;
+    for (int i = 0; i < ns; ++i)
+        CU(cudaMemcpyAsync(slices[i].f, X[i].pot[L & 1], sizeof(float) * slices[i].n, cudaMemcpyDeviceToDevice, st));
     CU(cudaMemcpyAsync(P.g, Y.pot[L & 1], sizeof(float) * m, cudaMemcpyDeviceToDevice, st));
     ctx->cnt.kernel_launches += launched;
-    const int sweeps_done = hs.iter;  // row passes actually executed
-    ctx->cnt.lse_launches += 2LL * (sweeps_done + 1);
+    ctx->cnt.lse_launches += (long long)(ns + 1) * (hs.iter + 1);
     if (ctx->timing) ctx->cnt.lse_ms += ms;
-    const double entries = (double)n * m * (2.0 * L + 1.0);
+    const double entries = (double)n_sum * m * (2.0 * L + 1.0);
     ctx->cnt.lse_ex2 += entries;
     if (stored) ctx->cnt.lse_bytes += 4.0 * entries;
     rep->iterations = L;
@@ -737,7 +786,7 @@ sk_status sinkhorn_init_subsample(sk_ctx *ctx, int64_t n, int64_t m, int32_t d, 
     LsePass lp{&X, &Z, 1, 0, split, part, eps, nullptr};
     CU(launch_lse(lp, ctx->stream));
     MergePass mp{MERGE_OUT, &X, part, split, eps, nullptr, status, blke, blkb, dpot,
-                 (float)(eps * std::log((double)ms)), 0};
+                 (float)(eps * std::log((double)ms)), 0, 0};
     CU(launch_merge(mp, ctx->stream));
     ctx->cnt.kernel_launches += 5;
     CK(sg.flush());
@@ -797,14 +846,14 @@ sk_status solve_impl(sk_ctx *ctx, int64_t B, int64_t n, int64_t m, int32_t d, co
     }
     for (long long p = 0; p < B; ++p) {
         Problem P;
-        P.n = n; P.m = m; P.n_total = n; P.d = d;
-        P.x = x + p * xs; P.y = y + p * ys;
-        P.a = a ? a + p * as : nullptr; P.b = b ? b + p * bs : nullptr;
-        P.f_init = f_init ? f_init + p * n : nullptr;
+        P.n_total = n; P.m = m; P.d = d;
+        P.y = y + p * ys; P.b = b ? b + p * bs : nullptr;
         P.eps = eps; P.tol = tol; P.max_iter = max_iter; P.check_every = check_every; P.mode = mode;
-        P.f = f + p * n; P.g = g + p * m;
-        P.rank = 0; P.world = 1;
-        CK(solve_multikernel(ctx, P, &rep[p]));
+        P.g = g + p * m;
+        P.world = 1; P.nccl = false;
+        std::vector<Slice> sl{Slice{0, n, x + p * xs, a ? a + p * as : nullptr,
+                                    f_init ? f_init + p * n : nullptr, f + p * n, 0}};
+        CK(solve_core(ctx, P, sl, &rep[p]));
     }
     return SK_OK;
 }
@@ -875,12 +924,55 @@ sk_status sinkhorn_solve_sharded(sk_ctx *ctx, int64_t n_total, int64_t row0, int
                     "sinkhorn_solve_sharded"));
     *rep = sk_report{};
     Problem P;
-    P.n = n_local; P.m = m; P.n_total = n_total; P.d = d;
-    P.x = dx; P.y = dy; P.a = da; P.b = db; P.f_init = dfi;
+    P.n_total = n_total; P.m = m; P.d = d;
+    P.y = dy; P.b = db;
     P.eps = eps; P.tol = tol; P.max_iter = max_iter; P.check_every = check_every; P.mode = mode;
-    P.f = df; P.g = dg;
-    P.rank = ctx->rank; P.world = ctx->world;
-    sk_status s = solve_multikernel(ctx, P, rep);
+    P.g = dg;
+    P.world = ctx->world; P.nccl = ctx->world > 1;
+    std::vector<Slice> sl{Slice{row0, n_local, dx, da, dfi, df, ctx->rank}};
+    sk_status s = solve_core(ctx, P, sl, rep);
+    if (s != SK_OK && s != SK_ENONFINITE) return s;
+    sk_status s2 = sg.flush();
+    CU(cudaStreamSynchronize(ctx->stream));
+    return s != SK_OK ? s : s2;
+}
+
+sk_status sinkhorn_solve_sharded_emulated(sk_ctx *ctx, int32_t world, int64_t n, int64_t m, int32_t d,
+                                          const float *x, const float *y, const float *a, const float *b,
+                                          float eps, float tol, int32_t max_iter, int32_t check_every,
+                                          sk_cost_mode mode, const float *f_init, float *f, float *g,
+                                          sk_report *rep) {
+    if (!ctx) return SK_EINVAL;
+    CK(validate_common(ctx, n, m, d, eps, tol, max_iter, check_every));
+    if (!x || !y || !f || !g || !rep) return fail(ctx, SK_EINVAL, "NULL argument");
+    if (world < 1 || SK_SHARD_BLOCKS % world) return fail(ctx, SK_EINVAL, "world must divide %d", SK_SHARD_BLOCKS);
+    Stager sg(ctx);
+    const float *dx, *dy, *da, *db, *dfi;
+    float *df, *dg;
+    CK(sg.in_t(x, (size_t)n * d, &dx));
+    CK(sg.in_t(y, (size_t)m * d, &dy));
+    CK(sg.in_t(a, (size_t)n, &da));
+    CK(sg.in_t(b, (size_t)m, &db));
+    CK(sg.in_t(f_init, (size_t)n, &dfi));
+    CK(sg.out_t(f, (size_t)n, &df));
+    CK(sg.out_t(g, (size_t)m, &dg));
+    CK(check_arrays(ctx, {{dx, n * d}, {dy, m * d}, {dfi, n}}, {{da, n}, {db, m}},
+                    "sinkhorn_solve_sharded_emulated"));
+    *rep = sk_report{};
+    Problem P;
+    P.n_total = n; P.m = m; P.d = d;
+    P.y = dy; P.b = db;
+    P.eps = eps; P.tol = tol; P.max_iter = max_iter; P.check_every = check_every; P.mode = mode;
+    P.g = dg;
+    P.world = world; P.nccl = false;
+    std::vector<Slice> sl;
+    for (int r = 0; r < world; ++r) {
+        int64_t r0, nl;
+        CK(sk_shard_rows(n, r, world, &r0, &nl));
+        if (nl < 1) return fail(ctx, SK_EUNSUPPORTED, "rank %d would own no rows (n too small for %d ranks)", r, world);
+        sl.push_back(Slice{r0, nl, dx + r0 * d, da ? da + r0 : nullptr, dfi ? dfi + r0 : nullptr, df + r0, r});
+    }
+    sk_status s = solve_core(ctx, P, sl, rep);
     if (s != SK_OK && s != SK_ENONFINITE) return s;
     sk_status s2 = sg.flush();
     CU(cudaStreamSynchronize(ctx->stream));

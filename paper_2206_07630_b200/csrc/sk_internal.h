@@ -89,6 +89,7 @@ struct MergePass {
     float *out;               // MERGE_OUT destination
     float out_const;          // MERGE_OUT: added constant (eps log ms for Eq. 8)
     int sharded;              // non-finite f is detected by the next (replicated) column merge
+    int no_iter_inc;          // MERGE_ROW of a non-final slice (emulated ranks): keep the counter
 };
 cudaError_t launch_merge(const MergePass &M, cudaStream_t st);
 int merge_blocks(int P);

@@ -297,7 +297,7 @@ __global__ void __launch_bounds__(kMT) k_merge(MergePass Mp, Side S) {
     } else if (Mp.mode == MERGE_ROW) {
         st->ticket_row = 0;
         if (bt && !Mp.sharded) { st->nonfinite = 1; st->stop = 1; st->final_iter = l; }
-        else st->iter = l + 1;
+        else if (!Mp.no_iter_inc) st->iter = l + 1;
     } else {
         st->ticket_row = 0;
         if (bt) st->nonfinite = 1;

@@ -1,0 +1,214 @@
+"""Row sharding and the full-size configs C3/C4/C5 (-m gpu).
+
+Sharding: the sharded algorithm for W virtual ranks on one GPU
+(sinkhorn_solve_sharded_emulated: same fixed row-block partition, kernels and
+rank-order merge as W processes with ncclAllGather) must be bit-identical for
+W = 1, 2, 4, 8, to the unsharded solve and to sinkhorn_solve_sharded(world=1), and
+match the unsharded fp64 oracle.
+
+Full size (BASELINE.json shapes, the bench's launch configuration): lockstep for a few
+sweeps against the oracle where a full fp64 pass finishes in seconds (C3), sampled
+outputs the oracle computes one by one (C4, C5: columns of g^1 from f^0) plus the exact
+row-marginal property of the returned pair, and full convergence parity at reduced n
+from the same generators.
+"""
+import numpy as np
+import pytest
+import torch
+
+from parity import (INIT_RTOL, assert_obj_close, assert_pair_close, centred, count_tol, rel_inf)
+from workloads import gen
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    import paper_2206_07630_b200 as sk
+    return sk.Context(0)
+
+
+def _cuda(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def _row_marginals(x, y, f, g, eps, rows, chunk=64):
+    """fp64 row sums of the plan of (f, g) on sampled rows (property check of CUDA outputs)."""
+    y64 = np.asarray(y, np.float64)
+    out = []
+    for i0 in range(0, len(rows), chunk):
+        r = rows[i0:i0 + chunk]
+        xi = np.asarray(x[r], np.float64)
+        C = ((xi[:, None, :] - y64[None, :, :]) ** 2).sum(-1)
+        out.append(np.exp((np.asarray(f, np.float64)[r, None] + np.asarray(g, np.float64)[None, :] - C) / eps).sum(1))
+    return np.concatenate(out)
+
+
+# ------------------------------------------------------------------ sharding
+@pytest.mark.parametrize("mode,n,m,d", [("online", 5000, 3000, 3), ("stored", 4100, 2048, 16)])
+def test_sharded_bit_identical_across_world_sizes(O, ctx, mode, n, m, d):
+    import paper_2206_07630_b200 as sk
+    rng = np.random.default_rng(n + d)
+    x = rng.random((n, d)).astype(np.float32)
+    y = rng.random((m, d)).astype(np.float32)
+    a = gen.random_weights(n, rng)
+    eps = float(np.float32(0.04 * gen.mean_sq_cost(x, y)))
+    xd, yd, ad = _cuda(x), _cuda(y), _cuda(a)
+    outs = {}
+    for W in (1, 2, 4, 8):
+        outs[W] = sk.sinkhorn_solve_sharded_emulated(ctx, W, xd, yd, eps, a=ad, mode=mode)
+    f1, g1, r1 = outs[1]
+    for W in (2, 4, 8):
+        f, g, r = outs[W]
+        assert torch.equal(f, f1) and torch.equal(g, g1), W
+        assert r["iterations"] == r1["iterations"] and r["dual_objective"] == r1["dual_objective"]
+    # the unsharded path and the real sharded entry at world = 1 use the same partition
+    fu, gu, ru = sk.sinkhorn_solve(ctx, xd, yd, eps, a=ad, mode=mode)
+    assert torch.equal(fu, f1) and torch.equal(gu, g1)
+    fs, gs, rs = sk.sinkhorn_solve_sharded(ctx, n, 0, xd, yd, eps, a_local=ad, mode=mode)
+    assert torch.equal(fs, f1) and torch.equal(gs, g1)
+    # and the oracle (unsharded, fp64)
+    L = r1["iterations"]
+    ref = O.sinkhorn(x, y, eps, a=a)
+    assert abs(L - ref.iterations) <= count_tol(ref.iterations)
+    lock = O.sinkhorn(x, y, eps, a=a, tol=0, max_iter=L)
+    assert_pair_close(f1.cpu().numpy(), g1.cpu().numpy(), lock.f, lock.g, eps)
+    assert_obj_close(r1["dual_objective"], lock.E, eps)
+
+
+def test_shard_partition_small_n_rejected_for_empty_ranks(ctx):
+    import paper_2206_07630_b200 as sk
+    x = _cuda(np.random.default_rng(0).random((300, 2)).astype(np.float32))
+    with pytest.raises(sk.SinkhornError):
+        sk.sinkhorn_solve_sharded_emulated(ctx, 8, x, x, 0.1)
+
+
+# ------------------------------------------------------------------ C3 (stored, d=16)
+@pytest.fixture(scope="module")
+def c3():
+    return gen.c3(eps_factor=0.05)
+
+
+@pytest.mark.parametrize("init", ["zero", "gaussian", "gmm"])
+def test_c3_full_size_lockstep(O, ctx, c3, init):
+    """BJ.cfg3 at full size (16384^2, stored 1 GiB C): 2 sweeps in lockstep with the oracle."""
+    import paper_2206_07630_b200 as sk
+    p = c3
+    x, y = _cuda(p.x), _cuda(p.y)
+    f0 = None
+    if init == "gaussian":
+        f0, _ = sk.sinkhorn_init_gaussian(ctx, x, y)
+        ref0, _ = O.init_gaussian(p.x, p.y)
+        assert rel_inf(centred(f0.cpu().numpy()), centred(ref0), p.eps) <= INIT_RTOL
+    elif init == "gmm":
+        gx = {k: _cuda(v) for k, v in p.extra["gmm_x"].items()}
+        gy = {k: _cuda(v) for k, v in p.extra["gmm_y"].items()}
+        f0, _ = sk.sinkhorn_init_gmm(ctx, x, y, gx, gy, p.eps)
+        ref0, _ = O.init_gmm(p.x, p.y, p.extra["gmm_x"], p.extra["gmm_y"], p.eps)
+        assert rel_inf(centred(f0.cpu().numpy()), centred(ref0), p.eps) <= INIT_RTOL
+    f, g, rep = sk.sinkhorn_solve(ctx, x, y, p.eps, tol=1e-9, max_iter=2, mode="stored", f_init=f0)
+    assert rep["iterations"] == 2
+    f0n = None if f0 is None else f0.cpu().numpy()
+    lock = O.sinkhorn(p.x, p.y, p.eps, tol=0, max_iter=2, f0=f0n)
+    assert_pair_close(f.cpu().numpy(), g.cpu().numpy(), lock.f, lock.g, p.eps, what=f"c3-{init}")
+    assert_obj_close(rep["dual_objective"], lock.E, p.eps, what=f"c3-{init}")
+
+
+def test_c3_reduced_full_convergence(O, ctx):
+    import paper_2206_07630_b200 as sk
+    p = gen.c3(n=3072, eps_factor=0.05)
+    f, g, rep = sk.sinkhorn_solve(ctx, _cuda(p.x), _cuda(p.y), p.eps, mode="stored")
+    ref = O.sinkhorn(p.x, p.y, p.eps)
+    assert rep["converged"] and abs(rep["iterations"] - ref.iterations) <= count_tol(ref.iterations)
+    lock = O.sinkhorn(p.x, p.y, p.eps, tol=0, max_iter=rep["iterations"])
+    assert_pair_close(f.cpu().numpy(), g.cpu().numpy(), lock.f, lock.g, p.eps)
+    assert_obj_close(rep["dual_objective"], lock.E, p.eps)
+
+
+# ------------------------------------------------------------------ C4 (online, d=3)
+@pytest.fixture(scope="module")
+def c4():
+    return gen.c4()
+
+
+def test_c4_full_size_first_sweep_sampled(O, ctx, c4):
+    """BJ.cfg4 at full size (262144^2 online): g^1 from f^0 = 0 on sampled columns (oracle,
+    O(n d) each) and the exact row marginals of (f^1, g^1) on sampled rows."""
+    import paper_2206_07630_b200 as sk
+    p = c4
+    f, g, rep = sk.sinkhorn_solve(ctx, _cuda(p.x), _cuda(p.y), p.eps, tol=1e-9, max_iter=1, mode="online")
+    f, g = f.cpu().numpy(), g.cpu().numpy()
+    rng = np.random.default_rng(0)
+    cols = np.sort(rng.choice(p.m, 64, replace=False))
+    rows = np.sort(rng.choice(p.n, 64, replace=False))
+    g_ref = O.g_update(p.x, p.y, np.zeros(p.n), p.eps, cols=cols)
+    assert np.abs(g[cols] - g_ref).max() <= 1e-4 * max(np.abs(g_ref).max(), p.eps)
+    rm = _row_marginals(p.x, p.y, f, g, p.eps, rows)
+    assert np.abs(rm * p.n - 1.0).max() < 1e-3
+
+
+def test_c4_subsample_init_full_size(O, ctx, c4):
+    """Subsample initializer (4096 of 262144 per side) at full size: inner solve in lockstep,
+    Eq. (8) extrapolation on sampled rows."""
+    import paper_2206_07630_b200 as sk
+    p = c4
+    tol = 1e-4
+    pot, side, inner = sk.sinkhorn_init_subsample(ctx, _cuda(p.x), _cuda(p.y), _cuda(p.extra["idx_x"]),
+                                                  _cuda(p.extra["idx_y"]), p.eps, tol)
+    w, z = p.x[p.extra["idx_x"]], p.y[p.extra["idx_y"]]
+    ref_in = O.sinkhorn(w, z, p.eps, tol=tol)
+    assert abs(inner["iterations"] - ref_in.iterations) <= count_tol(ref_in.iterations)
+    lock = O.sinkhorn(w, z, p.eps, tol=0, max_iter=inner["iterations"])
+    rows = np.sort(np.random.default_rng(1).choice(p.n, 2048, replace=False))
+    ref = O.subsample_extrapolate(p.x, z, lock.g, p.eps, rows=rows)
+    got = pot.cpu().numpy()[rows]
+    assert rel_inf(got - got.mean(), ref - ref.mean(), p.eps) <= INIT_RTOL
+
+
+@pytest.mark.parametrize("init", ["zero", "subsample"])
+def test_c4_reduced_full_convergence(O, ctx, init):
+    import paper_2206_07630_b200 as sk
+    p = gen.c4(n=6000, ns=600)
+    f0 = None
+    if init == "subsample":
+        f0, _, _ = sk.sinkhorn_init_subsample(ctx, _cuda(p.x), _cuda(p.y), _cuda(p.extra["idx_x"]),
+                                              _cuda(p.extra["idx_y"]), p.eps, 1e-4)
+    f, g, rep = sk.sinkhorn_solve(ctx, _cuda(p.x), _cuda(p.y), p.eps, mode="online", f_init=f0)
+    f0n = None if f0 is None else f0.cpu().numpy()
+    ref = O.sinkhorn(p.x, p.y, p.eps, f0=f0n)
+    assert rep["converged"] and abs(rep["iterations"] - ref.iterations) <= count_tol(ref.iterations)
+    lock = O.sinkhorn(p.x, p.y, p.eps, tol=0, max_iter=rep["iterations"], f0=f0n)
+    assert_pair_close(f.cpu().numpy(), g.cpu().numpy(), lock.f, lock.g, p.eps)
+    assert_obj_close(rep["dual_objective"], lock.E, p.eps)
+
+
+# ------------------------------------------------------------------ C5 (d=64)
+def test_c5_full_size_first_sweep_sampled(O, ctx):
+    import paper_2206_07630_b200 as sk
+    p = gen.c5(eps_factor=0.1)
+    f0, _ = sk.sinkhorn_init_gaussian(ctx, _cuda(p.x), _cuda(p.y))
+    f0n = f0.cpu().numpy()
+    ref0, _ = O.init_gaussian(p.x, p.y)
+    assert rel_inf(centred(f0n), centred(ref0), p.eps) <= INIT_RTOL
+    f, g, rep = sk.sinkhorn_solve(ctx, _cuda(p.x), _cuda(p.y), p.eps, tol=1e-9, max_iter=1,
+                                  mode="online", f_init=f0)
+    f, g = f.cpu().numpy(), g.cpu().numpy()
+    rng = np.random.default_rng(2)
+    cols = np.sort(rng.choice(p.m, 32, replace=False))
+    g_ref = O.g_update(p.x, p.y, f0n, p.eps, cols=cols)
+    assert np.abs(g[cols] - g_ref).max() <= 1e-4 * max(np.abs(g_ref).max(), p.eps)
+    rows = np.sort(rng.choice(p.n, 32, replace=False))
+    rm = _row_marginals(p.x, p.y, f, g, p.eps, rows)
+    assert np.abs(rm * p.n - 1.0).max() < 1e-3
+
+
+@pytest.mark.parametrize("eps_factor", [1e-2, 1e-1])
+def test_c5_reduced_full_convergence(O, ctx, eps_factor):
+    import paper_2206_07630_b200 as sk
+    p = gen.c5(n=2048, eps_factor=eps_factor)
+    f, g, rep = sk.sinkhorn_solve(ctx, _cuda(p.x), _cuda(p.y), p.eps, mode="online")
+    ref = O.sinkhorn(p.x, p.y, p.eps)
+    assert rep["converged"] and abs(rep["iterations"] - ref.iterations) <= count_tol(ref.iterations)
+    lock = O.sinkhorn(p.x, p.y, p.eps, tol=0, max_iter=rep["iterations"])
+    assert_pair_close(f.cpu().numpy(), g.cpu().numpy(), lock.f, lock.g, p.eps)
+    assert_obj_close(rep["dual_objective"], lock.E, p.eps)
