@@ -1,15 +1,18 @@
 #!/usr/bin/env python
-"""Benchmark of the hot path (BASELINE.json metric: Sinkhorn cost-entries/s and time-to-tol
-per init, with the roofline fraction of the dominant kernel).
+"""Benchmark of the hot path (BASELINE.json metric: Sinkhorn cost-entries/s — n*m per
+iteration — and time-to-tol per init, with the roofline fraction of the dominant kernel).
 
 Default workload (N=1): BASELINE.json configs[1] (C2) — B=1024 independent 1D problems,
-n=m=1024, eps=1e-3, tol=1e-3; one step = the paper's method on the whole batch: the
+n=m=1024, eps=1e-3, tol=1e-3.  One step = the paper's method on the whole batch: the
 sorted closed-form dual initializer (Sec. 3.1) followed by the on-chip batched Sinkhorn
-solve to tolerance.  value = sum_b n*m*L_b / step time (cost-entries per second).
-With N>1 (torchrun) every rank solves its own batch of 1024 problems (weak scaling,
-no data-path collective).  --workload c4 runs the row-sharded online path (NCCL).
+solve to tolerance.  value = sum_b n*m*L_b / step time.  With N>1 (torchrun) every rank
+solves its own batch of 1024 problems (weak scaling, no data-path collective).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload c2|c4|c1|c3|c5]
+Other workloads (parity configs, also measurable): --workload c1 | c3 | c4 | c5.
+  c4 is row-sharded over N GPUs (NCCL allgather of column partials every sweep; strong
+  scaling: the total problem is fixed).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload ...]
 """
 from __future__ import annotations
 
@@ -18,7 +21,6 @@ import json
 import os
 import subprocess
 import sys
-import threading
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
@@ -26,15 +28,15 @@ sys.path.insert(0, ROOT)
 
 import numpy as np  # noqa: E402
 
-MUFU_EX2_PER_CLK_SM = 16     # B200 (sm_100) SFU ex2 rate, CUDA programming guide arithmetic table
+MUFU_EX2_PER_CLK_SM = 16     # B200 (sm_100) SFU ex2 throughput per SM per clock
+FFMA_PER_CLK_SM = 128        # FP32 lanes per SM
 N_SM = 148
 
 
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
-        d = json.load(open(p))
-        return d, "measured"
+        return json.load(open(p)), "measured"
     return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
 
 
@@ -80,76 +82,278 @@ class ClockSampler:
 
 
 def dist_env():
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return world, rank, local
+    return (int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")),
+            int(os.environ.get("LOCAL_RANK", "0")))
 
 
-# =============================================================== reference arm (oracle)
-def oracle_c2_sample(n_problems: int, seed: int = 0):
-    """The fp64 oracle, as it stands, on a bounded sample of the C2 workload (sort1d init +
-    Sinkhorn to tol for the first n_problems problems).  Returns (entries, seconds, threads)."""
-    from oracle import oracle as O
-    from workloads import gen
-    p = gen.c2(B=max(n_problems, 1), seed=seed)
-    t0 = time.perf_counter()
-    entries = 0.0
-    for b in range(n_problems):
-        f0 = O.init_sort1d(p.x[b].ravel(), p.y.ravel())
-        r = O.sinkhorn(p.x[b], p.y, p.eps, tol=p.tol, f0=f0)
-        entries += float(p.n) * p.m * r.iterations
-    return entries, time.perf_counter() - t0, O.num_threads()
+# ==================================================================== workloads
+class Workload:
+    """One BASELINE.json config.  step() runs the hot path once on this rank's inputs (already
+    in HBM) and returns the cost entries n*m*L it processed; e2e_step() runs the same through
+    the C ABI with pinned host buffers."""
+    scaling = "weak"
+    roof = "mufu"           # mufu | hbm | ffma
+
+    def cpu_sample(self):  # -> (entries, seconds, threads, description)
+        raise NotImplementedError
 
 
+class C2(Workload):
+    name = "c2"
+
+    def __init__(self, sk, ctx, dev, rank, world, args):
+        from workloads import gen
+        self.sk, self.ctx, self.world = sk, ctx, world
+        self.p = p = gen.c2(seed=rank)
+        self.B, self.n, self.m = p.batch, p.n, p.m
+        import torch
+        self.x = torch.from_numpy(p.x).to(dev)
+        self.y = torch.from_numpy(p.y).to(dev)
+        self.xh = torch.from_numpy(p.x).pin_memory()
+        self.yh = torch.from_numpy(p.y).pin_memory()
+
+    def config(self):
+        return {"workload": "BJ.cfg2 (C2): batched 1D sorting/ranking, B=1024 per GPU x n=m=1024, d=1, "
+                            "x~U[0,1), y_j=j/(m-1), eps=1e-3, tol=1e-3 (L1 marginal), max_iter=10000",
+                "init": "sort1d (closed-form eps=0 dual, Sec. 3.1)", "global_batch": 1024 * self.world,
+                "parallelism": f"dp{self.world} (independent problems per rank)",
+                "l2": "flushed (256 MiB write) before every timed step"}
+
+    def _run(self, x, y, init=True):
+        sk, p = self.sk, self.p
+        f0 = sk.sinkhorn_init_sort1d(self.ctx, x.view(self.B, self.n), y.view(self.m), y_shared=True) if init else None
+        _, _, reps = sk.sinkhorn_solve(self.ctx, x, y, p.eps, tol=p.tol, max_iter=p.max_iter, y_shared=True,
+                                       f_init=f0)
+        self.its = np.array([r["iterations"] for r in reps])
+        return float(self.n) * self.m * float(self.its.sum())
+
+    def step(self):
+        return self._run(self.x, self.y)
+
+    def e2e_step(self):
+        e = self._run(self.xh, self.yh)
+        B, n, m = self.B, self.n, self.m
+        h2d = 2 * (self.xh.numel() + self.yh.numel()) * 4 + B * n * 4   # x,y twice + f0 back in
+        d2h = B * n * 4 + B * n * 4 + B * m * 4                          # f0, f, g
+        return e, h2d, d2h
+
+    def baseline(self):
+        e = self._run(self.x, self.y, init=False)
+        return {"init": "zero", "iterations_mean": float(self.its.mean()), "iterations_max": int(self.its.max())}
+
+    def extra(self):
+        return {"iterations_mean": float(self.its.mean()), "iterations_max": int(self.its.max())}
+
+    kernel = "k_batched<1,2,512> (on-chip persistent solver, K13)"
+
+    def cpu_sample(self, nprob=4):
+        from oracle import oracle as O
+        from workloads import gen
+        p = gen.c2(B=nprob)
+        t0 = time.perf_counter()
+        e = 0.0
+        for b in range(nprob):
+            f0 = O.init_sort1d(p.x[b].ravel(), p.y.ravel())
+            r = O.sinkhorn(p.x[b], p.y, p.eps, tol=p.tol, f0=f0)
+            e += float(p.n) * p.m * r.iterations
+        return e, time.perf_counter() - t0, O.num_threads(), f"{nprob} of the 1024 C2 problems (sort1d init + fp64 solve to tol)"
+
+
+class Single(Workload):
+    """One problem (C1, C3, C4, C5); C4 is row-sharded over the ranks."""
+
+    def __init__(self, sk, ctx, dev, rank, world, args):
+        from workloads import gen
+        import torch
+        self.sk, self.ctx, self.world, self.rank, self.args = sk, ctx, world, rank, args
+        self.name = args.workload
+        if self.name == "c1":
+            self.p = gen.c1(); self.init = "gaussian"; self.mode = "auto"; self.roof = "mufu"
+            self.kernel = "k_batched (on-chip solver, one CTA)"
+        elif self.name == "c3":
+            self.p = gen.c3(eps_factor=args.eps_factor or 0.01); self.init = args.init or "gmm"
+            self.mode = "stored"; self.roof = "hbm"; self.kernel = "k_rows + k_cols (stored-cost sweep, K5)"
+        elif self.name == "c4":
+            self.p = gen.c4(); self.init = args.init or "subsample"; self.mode = "online"; self.roof = "mufu"
+            self.kernel = "k_lse<3,4> (online LSE pass, K2)"
+            self.scaling = "strong"
+        else:
+            self.p = gen.c5(eps_factor=args.eps_factor or 1e-2); self.init = args.init or "gaussian"
+            self.mode = "online"; self.roof = "ffma"; self.kernel = "k_lse<64,1> (online LSE pass, FFMA cross term)"
+        p = self.p
+        self.n, self.m, self.d = p.n, p.m, p.d
+        self.sharded = self.name == "c4" and world > 1
+        if self.sharded:
+            from paper_2206_07630_b200 import dist as skd
+            skd.init_comm(ctx)
+        self.row0, self.nl = sk.shard_rows(p.n, rank, world) if self.name == "c4" else (0, p.n)
+        self.x = torch.from_numpy(p.x).to(dev)
+        self.y = torch.from_numpy(p.y).to(dev)
+        self.xh = torch.from_numpy(p.x).pin_memory()
+        self.yh = torch.from_numpy(p.y).pin_memory()
+        self.dev = dev
+        if self.init == "gmm":
+            self.gx = {k: torch.from_numpy(v).to(dev) for k, v in p.extra["gmm_x"].items()}
+            self.gy = {k: torch.from_numpy(v).to(dev) for k, v in p.extra["gmm_y"].items()}
+        if self.init == "subsample":
+            self.ix = torch.from_numpy(p.extra["idx_x"]).to(dev)
+            self.iy = torch.from_numpy(p.extra["idx_y"]).to(dev)
+
+    def config(self):
+        p = self.p
+        c = {"workload": {"c1": "BJ.cfg1 (C1): n=m=256, d=2, Gaussian clouds, eps=0.01*mean(C)",
+                          "c3": f"BJ.cfg3 (C3): n=m=16384, d=16 GMM clouds, stored-cost mode (1 GiB C), eps={p.eps:.4g}",
+                          "c4": "BJ.cfg4 (C4): n=m=262144, d=3 RGB-pixel mixtures, eps=1e-2, online cost",
+                          "c5": f"BJ.cfg5 (C5): n=m=65536, d=64 embeddings, eps={p.eps:.4g}, online cost"}[self.name],
+             "init": self.init, "tol": p.tol, "mode": self.mode,
+             "parallelism": f"row-sharded x{self.world}" if self.sharded else "1 GPU",
+             "l2": "flushed (256 MiB write) before every timed step" if self.name in ("c1",) else
+                   "inputs + cost larger than L2 / flushed before each step"}
+        return c
+
+    def _init(self, x, y):
+        sk, p = self.sk, self.p
+        if self.init == "gaussian":
+            f0, _ = sk.sinkhorn_init_gaussian(self.ctx, x, y)
+        elif self.init == "gmm":
+            import torch
+            gx, gy = self.gx, self.gy
+            if not x.is_cuda:
+                gx = {k: v.cpu() for k, v in gx.items()}
+                gy = {k: v.cpu() for k, v in gy.items()}
+            f0, _ = sk.sinkhorn_init_gmm(self.ctx, x, y, gx, gy, p.eps)
+        elif self.init == "subsample":
+            ix, iy = (self.ix, self.iy) if x.is_cuda else (self.ix.cpu(), self.iy.cpu())
+            f0, _, self.inner = sk.sinkhorn_init_subsample(self.ctx, x, y, ix, iy, p.eps, p.tol / 10)
+        else:
+            f0 = None
+        return f0
+
+    def _run(self, x, y, init=True):
+        sk, p = self.sk, self.p
+        f0 = self._init(x, y) if init else None
+        if self.sharded:
+            xl = x[self.row0:self.row0 + self.nl]
+            f0l = None if f0 is None else f0[self.row0:self.row0 + self.nl].contiguous()
+            _, _, rep = sk.sinkhorn_solve_sharded(self.ctx, self.n, self.row0, xl, y, p.eps, tol=p.tol,
+                                                  max_iter=p.max_iter, mode=self.mode, f_init_local=f0l)
+        else:
+            _, _, rep = sk.sinkhorn_solve(self.ctx, x, y, p.eps, tol=p.tol, max_iter=p.max_iter, mode=self.mode,
+                                          f_init=f0)
+        self.rep = rep
+        return float(self.n) * self.m * rep["iterations"] / self.world   # each rank's share
+
+    def step(self):
+        return self._run(self.x, self.y)
+
+    def e2e_step(self):
+        e = self._run(self.xh, self.yh)
+        n, m, d = self.n, self.m, self.d
+        h2d = 2 * (n * d + m * d) * 4 + n * 4
+        d2h = n * 4 + n * 4 + m * 4
+        return e, h2d, d2h
+
+    def baseline(self):
+        self._run(self.x, self.y, init=False)
+        return {"init": "zero", "iterations": self.rep["iterations"]}
+
+    def extra(self):
+        out = {"iterations": self.rep["iterations"], "converged": self.rep["converged"],
+               "dual_objective": self.rep["dual_objective"], "build_ms": self.rep["build_ms"]}
+        if hasattr(self, "inner"):
+            out["subsample_inner_iterations"] = self.inner["iterations"]
+        return out
+
+    def cpu_sample(self):
+        """The fp64 oracle timed on a bounded sample: one f-update (row LSE) on sampled rows."""
+        from oracle import oracle as O
+        p = self.p
+        rows = np.arange(0, p.n, max(1, p.n // {"c1": 256, "c3": 2048, "c4": 256, "c5": 512}[self.name]))
+        g = np.zeros(p.m)
+        t0 = time.perf_counter()
+        O.f_update(p.x, p.y, g, p.eps, rows=rows)
+        t = time.perf_counter() - t0
+        return float(len(rows)) * p.m / 2, t, O.num_threads(), \
+            f"oracle row pass (f-update) over {len(rows)} sampled rows x {p.m} columns; one cost entry = 2 passes"
+
+
+def make_workload(args, sk, ctx, dev, rank, world):
+    return C2(sk, ctx, dev, rank, world, args) if args.workload == "c2" else Single(sk, ctx, dev, rank, world, args)
+
+
+def roofline(w, cnt, steps, pk, src):
+    sm_max = float(pk.get("sm_max_mhz", 1965.0))
+    ms = cnt["lse_ms"] / max(steps, 1)
+    if w.roof == "hbm":
+        achieved = cnt["lse_bytes"] / (cnt["lse_ms"] / 1e3) / 1e9 if cnt["lse_ms"] > 0 else 0.0
+        peak = float(pk["hbm_gbs"])
+        return {"bound": "hbm", "kernel": w.kernel, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": None,
+                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({src})",
+                "algorithmic": "4 bytes (one fp32 C_ij read) per cost entry per pass",
+                "kernel_ms_per_step": ms}
+    if w.roof == "ffma":
+        flops = cnt["lse_ex2"] * 2 * w.d     # cross term: d FMA per entry per pass
+        achieved = flops / (cnt["lse_ms"] / 1e3) / 1e12 if cnt["lse_ms"] > 0 else 0.0
+        peak = N_SM * FFMA_PER_CLK_SM * 2 * sm_max * 1e6 / 1e12
+        return {"bound": "alu", "pipe": "FFMA (cross term 2d flops/entry)", "kernel": w.kernel,
+                "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
+                "peak_source": f"derived: {N_SM} SM x {FFMA_PER_CLK_SM} FP32 lanes x 2 x {sm_max:.0f} MHz ({src})",
+                "kernel_ms_per_step": ms}
+    achieved = cnt["lse_ex2"] / (cnt["lse_ms"] / 1e3) if cnt["lse_ms"] > 0 else 0.0
+    peak = N_SM * MUFU_EX2_PER_CLK_SM * sm_max * 1e6
+    return {"bound": "alu", "pipe": "MUFU.EX2 (SFU)", "kernel": w.kernel, "achieved": achieved / 1e9,
+            "peak": peak / 1e9, "unit": "Gex2/s", "frac": achieved / peak, "traffic": None,
+            "peak_source": f"derived: {N_SM} SM x {MUFU_EX2_PER_CLK_SM} ex2/clk x {sm_max:.0f} MHz "
+                           f"(sm_max_mhz from MEASURED_PEAKS.json, {src})",
+            "algorithmic": "one exp2 per cost entry per pass; 2 passes per sweep (+1 column pass for err_L)",
+            "kernel_ms_per_step": ms}
+
+
+# ==================================================================== reference arm
 def run_reference(args):
     world, rank, _ = dist_env()
     if rank != 0:
         return 0
     from oracle import oracle as O
     O.build()
+
+    class _Stub:
+        pass
+    w = C2.__new__(C2) if args.workload == "c2" else Single.__new__(Single)
     if args.workload != "c2":
-        print(json.dumps({"impl": "reference", "unavailable": f"reference arm implemented for c2 only"}))
-        return 0
-    per_step = 2
+        from workloads import gen
+        w.name = args.workload
+        w.p = {"c1": gen.c1, "c3": lambda: gen.c3(eps_factor=args.eps_factor or 0.01), "c4": gen.c4,
+               "c5": lambda: gen.c5(eps_factor=args.eps_factor or 1e-2)}[w.name]()
+    w.world = world
     for _ in range(args.warmup):
-        oracle_c2_sample(1)
-    tot_e, tot_t = 0.0, 0.0
-    for s in range(args.steps):
-        e, t, thr = oracle_c2_sample(per_step, seed=0)
+        (w.cpu_sample(1) if args.workload == "c2" else w.cpu_sample())
+    tot_e, tot_t, thr, desc = 0.0, 0.0, 1, ""
+    for _ in range(args.steps):
+        e, t, thr, desc = w.cpu_sample(2) if args.workload == "c2" else w.cpu_sample()
         tot_e += e
         tot_t += t
     v = tot_e / tot_t
-    line = {"impl": "reference", "metric": "sinkhorn_cost_entries_per_s", "value": v,
-            "unit": "cost-entries/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * tot_t / args.steps, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": c2_config(args),
-            "cpu_baseline": {"value": v, "unit": "cost-entries/s", "cores": thr, "kind": "oracle",
-                             "sample": f"{per_step} of the 1024 C2 problems per step (sort1d init + solve to tol)"},
+    cfg = w.config() if args.workload == "c2" else {"workload": args.workload}
+    line = {"impl": "reference", "metric": "sinkhorn_cost_entries_per_s", "value": v, "unit": "cost-entries/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": cfg,
+            "cpu_baseline": {"value": v, "unit": "cost-entries/s", "cores": thr, "kind": "oracle", "sample": desc},
             "e2e": {"value": v, "unit": "cost-entries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line))
+    print(json.dumps(line), flush=True)
     return 0
 
 
-def c2_config(args):
-    return {"workload": "BJ.cfg2 (C2): batched 1D sorting/ranking, B=1024 per GPU x n=m=1024, d=1, "
-                        "x~U[0,1), y_j=j/(m-1), eps=1e-3, tol=1e-3 (L1 marginal), max_iter=10000",
-            "init": "sort1d (closed-form eps=0 dual, Sec. 3.1)", "global_batch": 1024 * args.world,
-            "parallelism": f"dp{args.world} (independent problems per rank)",
-            "l2": "flushed (256 MiB write) before every timed step"}
-
-
-# =============================================================== our arm
+# ==================================================================== our arm
 def run_ours(args):
     import torch
     import torch.distributed as dist
 
     import paper_2206_07630_b200 as sk
-    from workloads import gen
 
     world, rank, local = dist_env()
-    args.world = world
     if world > 1:
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -161,28 +365,13 @@ def run_ours(args):
 
     def barrier():
         if world > 1:
-            dist.barrier()
+            dist.barrier(device_ids=[dev.index])
         torch.cuda.synchronize(dev)
 
-    if args.workload != "c2":
-        raise SystemExit("only --workload c2 is wired in this bench version")
-
-    p = gen.c2(seed=rank)
-    B, n, m = p.batch, p.n, p.m
-    x = torch.from_numpy(p.x).to(dev)
-    y = torch.from_numpy(p.y).to(dev)
-    x2 = x.view(B, n)
-    y1 = y.view(m)
-
-    def step():
-        with torch.cuda.stream(stream):
-            f0 = sk.sinkhorn_init_sort1d(ctx, x2, y1, y_shared=True)
-            f, g, reps = sk.sinkhorn_solve(ctx, x, y, p.eps, tol=p.tol, max_iter=p.max_iter,
-                                           y_shared=True, f_init=f0)
-        return reps
-
-    for _ in range(max(args.warmup, 0)):
-        reps = step()
+    with torch.cuda.stream(stream):
+        w = make_workload(args, sk, ctx, dev, rank, world)
+        for _ in range(max(args.warmup, 0)):
+            w.step()
     barrier()
     ctx.reset_counters()
     ctx.set_timing(True)
@@ -194,93 +383,73 @@ def run_ours(args):
             with torch.cuda.stream(stream):
                 flush.fill_(float(s))                     # L2 flush, outside the timed events
                 ev[s][0].record(stream)
-            reps = step()
-            with torch.cuda.stream(stream):
+                entries += w.step()
                 ev[s][1].record(stream)
-            entries += sum(float(n) * m * r["iterations"] for r in reps)
         barrier()
     ctx.set_timing(False)
     cnt = ctx.counters()
     ms = sum(a.elapsed_time(b) for a, b in ev)
-    t_local = torch.tensor([ms, entries], dtype=torch.float64, device=dev)
-    if world > 1:
-        tmax = t_local.clone()
-        dist.all_reduce(tmax[:1], op=dist.ReduceOp.MAX)
-        tsum = t_local.clone()
-        dist.all_reduce(tsum[1:], op=dist.ReduceOp.SUM)
-        ms_all, entries_all = float(tmax[0]), float(tsum[1])
-    else:
-        ms_all, entries_all = ms, entries
+    from paper_2206_07630_b200 import dist as skd
+    ms_all = skd.max_over_ranks([ms], device=dev)[0] if world > 1 else ms
+    entries_all = skd.sum_over_ranks([entries], device=dev)[0] if world > 1 else entries
     value = entries_all / (ms_all / 1e3)
-    its = np.array([r["iterations"] for r in reps])
+    extra = w.extra()
 
-    # ---- e2e: the same step through the C ABI with HOST buffers (pinned), copies inside the timing
-    xh = torch.from_numpy(p.x).pin_memory()
-    yh = torch.from_numpy(p.y).pin_memory()
-    e2e_ms, e2e_entries = 0.0, 0.0
-    for s in range(args.steps):
-        flush.fill_(float(s))
-        torch.cuda.synchronize(dev)
+    # ---- e2e: the same step through the C ABI with pinned HOST buffers, copies inside the timing
+    e2e_ms, e2e_entries, h2d, d2h = 0.0, 0.0, 0, 0
+    e2e_steps = max(1, min(args.steps, 5))
+    for s in range(e2e_steps):
+        with torch.cuda.stream(stream):
+            flush.fill_(float(s))
+        barrier()
         t0 = time.perf_counter()
         with torch.cuda.stream(stream):
-            f0h = sk.sinkhorn_init_sort1d(ctx, xh.view(B, n), yh.view(m), y_shared=True)
-            fh, gh, repsh = sk.sinkhorn_solve(ctx, xh, yh, p.eps, tol=p.tol, y_shared=True, f_init=f0h)
+            e, h2d, d2h = w.e2e_step()
         torch.cuda.synchronize(dev)
         e2e_ms += 1e3 * (time.perf_counter() - t0)
-        e2e_entries += sum(float(n) * m * r["iterations"] for r in repsh)
-    h2d = 2 * (xh.numel() * 4 + yh.numel() * 4) + B * n * 4
-    d2h = B * n * 4 + B * n * 4 + B * m * 4
+        e2e_entries += e
+    if world > 1:
+        e2e_ms = skd.max_over_ranks([e2e_ms], device=dev)[0]
+        e2e_entries = skd.sum_over_ranks([e2e_entries], device=dev)[0]
 
-    # ---- time-to-tol of the zero initializer on the same batch (context for the init's effect)
-    flush.fill_(0.0)
-    torch.cuda.synchronize(dev)
+    # ---- time-to-tol of the zero initializer (context for the initializer's effect)
+    with torch.cuda.stream(stream):
+        flush.fill_(0.0)
+    barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with torch.cuda.stream(stream):
         e0.record(stream)
-        _, _, reps0 = sk.sinkhorn_solve(ctx, x, y, p.eps, tol=p.tol, y_shared=True)
+        zero = w.baseline()
         e1.record(stream)
     torch.cuda.synchronize(dev)
-    zero_ms = e0.elapsed_time(e1)
-    its0 = np.array([r["iterations"] for r in reps0])
+    zero["time_to_tol_ms"] = e0.elapsed_time(e1)
 
     if rank == 0:
         pk, src = peaks()
-        clocks = clk.summary()
-        sm_max = float(pk.get("sm_max_mhz", 1965.0))
-        peak_ex2 = N_SM * MUFU_EX2_PER_CLK_SM * sm_max * 1e6
-        achieved = cnt["lse_ex2"] / (cnt["lse_ms"] / 1e3) if cnt["lse_ms"] > 0 else 0.0
         line = {
             "metric": "sinkhorn_cost_entries_per_s", "value": value, "unit": "cost-entries/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms_all / args.steps, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": ms_all / args.steps, "higher_is_better": True, "scaling": w.scaling,
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": c2_config(args),
-            "time_to_tol_ms": {"sort1d": ms / args.steps, "zero": zero_ms},
-            "iterations": {"sort1d": {"mean": float(its.mean()), "max": int(its.max())},
-                           "zero": {"mean": float(its0.mean()), "max": int(its0.max())}},
-            "roofline": {"bound": "alu", "pipe": "MUFU.EX2 (SFU)", "kernel": "k_batched<1,4> (on-chip solver)",
-                         "achieved": achieved / 1e9, "peak": peak_ex2 / 1e9, "unit": "Gex2/s",
-                         "frac": achieved / peak_ex2, "traffic": None,
-                         "peak_source": f"derived: {N_SM} SM x {MUFU_EX2_PER_CLK_SM} ex2/clk x {sm_max:.0f} MHz "
-                                        f"(sm_max_mhz from MEASURED_PEAKS.json, {src})",
-                         "algorithmic": "2 ex2 per cost entry per sweep (+1 column pass for the final error)",
-                         "kernel_ms_per_step": cnt["lse_ms"] / args.steps},
+            "config": w.config(),
+            "time_to_tol_ms": {"init": ms / args.steps, "zero_init": zero["time_to_tol_ms"]},
+            "solve": extra, "zero_init": zero,
+            "roofline": roofline(w, cnt, args.steps, pk, src),
             "gpu_launches": int(cnt["kernel_launches"]),
-            "clocks": clocks,
+            "clocks": clk.summary(),
             "e2e": {"value": e2e_entries / (e2e_ms / 1e3), "unit": "cost-entries/s",
                     "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
         }
         if not args.no_cpu_baseline:
             try:
-                e, t, thr = oracle_c2_sample(args.cpu_problems)
+                e, t, thr, desc = w.cpu_sample()
                 line["cpu_baseline"] = {"value": e / t, "unit": "cost-entries/s", "cores": thr, "kind": "oracle",
-                                        "sample": f"{args.cpu_problems} of the 1024 C2 problems "
-                                                  f"(sort1d init + fp64 solve to tol), {t:.1f} s"}
+                                        "sample": f"{desc}, {t:.1f} s"}
             except Exception as ex:  # pragma: no cover
-                line["cpu_baseline"] = {"value": None, "error": str(ex)}
+                line["cpu_baseline"] = {"value": None, "error": repr(ex)}
         print(json.dumps(line), flush=True)
     if world > 1:
-        dist.barrier()
+        dist.barrier(device_ids=[dev.index])
         dist.destroy_process_group()
     ctx.close()
     return 0
@@ -293,10 +462,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
-    ap.add_argument("--cpu-problems", type=int, default=4)
+    ap.add_argument("--init", default=None, help="c3/c4/c5 initializer: zero|gaussian|gmm|subsample")
+    ap.add_argument("--eps-factor", type=float, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
-    args.world = int(os.environ.get("WORLD_SIZE", "1"))
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)
