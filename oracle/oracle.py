@@ -363,7 +363,7 @@ def gmm_cost(mx, cx, my, cy):
     return C
 
 
-def init_gmm(x, y, gx: dict, gy: dict, eps, inner_tol=1e-9, inner_max_iter=100000):
+def init_gmm(x, y, gx: dict, gy: dict, eps, inner_tol=1e-4, inner_max_iter=100000):
     """GMM initializer (Sec. 3.3): K x K Bures-cost Sinkhorn at the same eps
     (reading R-13) -> f~; f0_i = sum_k f~_k p_k(x_i) on the smaller side."""
     x, y = _pts(x), _pts(y)

@@ -157,7 +157,7 @@ def sinkhorn_init_gaussian(ctx: Context, x, y, a=None, b=None, ridge_rel: float 
     return pot, side.value
 
 
-def sinkhorn_init_gmm(ctx: Context, x, y, gx: dict, gy: dict, eps: float, inner_tol: float = 1e-9,
+def sinkhorn_init_gmm(ctx: Context, x, y, gx: dict, gy: dict, eps: float, inner_tol: float = 1e-4,
                       inner_max_iter: int = 100000):
     """gx/gy: {'weights': (K,), 'means': (K, d), 'covs': (K, d, d)} fp32 tensors."""
     n, d = x.shape

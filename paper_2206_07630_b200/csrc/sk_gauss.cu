@@ -299,57 +299,52 @@ __global__ void __launch_bounds__(kGT) k_gmm_bures(const float *mux, const float
     }
 }
 
-// K x K entropic OT in fp64 (Alg. 1, g-then-f, explicit error every sweep), one CTA.
-__global__ void __launch_bounds__(kGT) k_gmm_sinkhorn(const double *C, int Kx, int Ky, const float *wx,
-                                                       const float *wy, float eps_f, float tol, int max_iter,
-                                                       double *ft, int *flags) {
-    __shared__ double f[64], g[64], rs[64], cs[64];
-    __shared__ double red[kGT / 32];
-    __shared__ int s_stop;
+// K x K entropic OT in fp64 (Alg. 1, g-then-f; R-13), one warp: lane t owns indices t and
+// t + 32.  Each sweep is a g-update then an f-update; err_l is evaluated with the fused
+// identity of the main solver (H5): after an f-update the row marginals are
+// exact, so err_l = sum_j b_j |expm1((g_j^l - g_j^{l+1})/eps)|, known at the next
+// g-update; the returned f~ is f^l of the first l with err_l < tol (or max_iter).
+__global__ void __launch_bounds__(32) k_gmm_sinkhorn(const double *C, int Kx, int Ky, const float *wx,
+                                                      const float *wy, float eps_f, float tol, int max_iter,
+                                                      double *ft, int *flags) {
+    __shared__ double f[64], g[64], fprev[64];
     const double eps = eps_f;
-    for (int i = threadIdx.x; i < 64; i += blockDim.x) { f[i] = 0.0; g[i] = 0.0; }
-    __syncthreads();
-    int it = 0;
+    const int t = threadIdx.x;
+    for (int i = t; i < 64; i += 32) { f[i] = 0.0; g[i] = 0.0; fprev[i] = 0.0; }
+    __syncwarp();
+    int l = 0;
     for (;;) {
-        ++it;
-        for (int j = threadIdx.x; j < Ky; j += blockDim.x) {   // g-update
+        // g-update g^{l+1} from f^l, with err_l from (g^l, g^{l+1})
+        double e = 0.0;
+        for (int j = t; j < Ky; j += 32) {
             double mx = -INFINITY;
             for (int i = 0; i < Kx; ++i) mx = fmax(mx, (f[i] - C[i * Ky + j]) / eps);
             double s = 0.0;
             for (int i = 0; i < Kx; ++i) s += exp((f[i] - C[i * Ky + j]) / eps - mx);
-            g[j] = eps * log((double)wy[j]) - eps * (mx + log(s));
+            const double gn = eps * log((double)wy[j]) - eps * (mx + log(s));
+            e += (double)wy[j] * fabs(expm1((g[j] - gn) / eps));
+            g[j] = gn;
         }
-        __syncthreads();
-        for (int i = threadIdx.x; i < Kx; i += blockDim.x) {   // f-update
+        for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
+        __syncwarp();
+        if (l >= 1 && (e < tol || !isfinite(e))) {
+            if (!isfinite(e) && t == 0) atomicOr(flags, 2);
+            break;
+        }
+        if (l >= max_iter) break;
+        // f-update f^{l+1} from g^{l+1}
+        for (int i = t; i < Kx; i += 32) {
             double mx = -INFINITY;
             for (int j = 0; j < Ky; ++j) mx = fmax(mx, (g[j] - C[i * Ky + j]) / eps);
             double s = 0.0;
             for (int j = 0; j < Ky; ++j) s += exp((g[j] - C[i * Ky + j]) / eps - mx);
+            fprev[i] = f[i];
             f[i] = eps * log((double)wx[i]) - eps * (mx + log(s));
         }
-        __syncthreads();
-        for (int i = threadIdx.x; i < Kx; i += blockDim.x) {
-            double s = 0.0;
-            for (int j = 0; j < Ky; ++j) s += exp((f[i] + g[j] - C[i * Ky + j]) / eps);
-            rs[i] = fabs(s - (double)wx[i]);
-        }
-        for (int j = threadIdx.x; j < Ky; j += blockDim.x) {
-            double s = 0.0;
-            for (int i = 0; i < Kx; ++i) s += exp((f[i] + g[j] - C[i * Ky + j]) / eps);
-            cs[j] = fabs(s - (double)wy[j]);
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            double e = 0.0;
-            for (int i = 0; i < Kx; ++i) e += rs[i];
-            for (int j = 0; j < Ky; ++j) e += cs[j];
-            s_stop = (e < tol) || it >= max_iter || !isfinite(e);
-            if (!isfinite(e)) atomicOr(flags, 2);
-        }
-        __syncthreads();
-        if (s_stop) break;
+        __syncwarp();
+        ++l;
     }
-    for (int i = threadIdx.x; i < Kx; i += blockDim.x) ft[i] = f[i];
+    for (int i = t; i < Kx; i += 32) ft[i] = f[i];
 }
 
 // Cholesky S_k = L L^T (fp64, one CTA, sequential columns), then Linv and log det L.
@@ -448,7 +443,7 @@ cudaError_t launch_gmm_init(const float *x, long long n, int d, int Kx, const fl
     if ((e = cudaFuncSetAttribute(k_gmm_chol, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2))) return e;
     k_gmm_sqrt<<<Kx, kGT, s5, st>>>(covx, d, R, flags);
     k_gmm_bures<<<Kx * Ky, kGT, s5, st>>>(mux, covx, Kx, muy, covy, Ky, d, R, C, flags);
-    k_gmm_sinkhorn<<<1, kGT, 0, st>>>(C, Kx, Ky, wx, wy, eps, inner_tol, inner_max_iter, ft, flags);
+    k_gmm_sinkhorn<<<1, 32, 0, st>>>(C, Kx, Ky, wx, wy, eps, inner_tol, inner_max_iter, ft, flags);
     k_gmm_chol<<<Kx, kGT, s2, st>>>(covx, d, Linv, logdet, flags);
     long long b = (n + kGT - 1) / kGT;
     k_gmm_pot<<<(int)(b > 148 * 8 ? 148 * 8 : b), kGT, 0, st>>>(x, n, d, Kx, wx, mux, Linv, logdet, ft, pot);

@@ -23,6 +23,7 @@ namespace sk {
 
 constexpr int kLT = 128;      // LSE kernel threads
 constexpr int kStages = 4;    // bulk-copy ring depth
+constexpr int kLseEmu = 1;    // exp2 pairs (of 4 per chunk) on the FMA pipe when D <= 4
 
 int lse_dpad(int d) {
     if (d <= 4) return d < 1 ? 0 : d;
@@ -138,7 +139,7 @@ __global__ void __launch_bounds__(kLT) k_lse(LseArgs A) {
         mbar_wait(&full[st], (i / kStages) & 1);
         const float *qt = ring + st * TF;
 #pragma unroll 2
-        for (int q = 0; q < TQ; q += kChunk) lse_chunk<D, R>(qt, TQ, qt + D * TQ, q, pd, M, Sx);
+        for (int q = 0; q < TQ; q += kChunk) lse_chunk<D, R, (D <= 4 ? kLseEmu : 0)>(qt, TQ, qt + D * TQ, q, pd, M, Sx);
         __syncthreads();  // everyone is done with stage st
         if (threadIdx.x == 0 && i + kStages < nt) {
             fence_proxy_async();
