@@ -146,17 +146,26 @@ class C2(Workload):
 
     kernel = "k_batched<1,2,512> (on-chip persistent solver, K13)"
 
-    def cpu_sample(self, nprob=4):
+    def cpu_sample(self, nprob=None, target_s=10.0):
+        """The fp64 oracle, as it stands, on whole C2 problems (sort1d init + solve to tol);
+        the number of problems is scaled so the sample takes about target_s seconds."""
         from oracle import oracle as O
         from workloads import gen
-        p = gen.c2(B=nprob)
-        t0 = time.perf_counter()
-        e = 0.0
-        for b in range(nprob):
-            f0 = O.init_sort1d(p.x[b].ravel(), p.y.ravel())
-            r = O.sinkhorn(p.x[b], p.y, p.eps, tol=p.tol, f0=f0)
-            e += float(p.n) * p.m * r.iterations
-        return e, time.perf_counter() - t0, O.num_threads(), f"{nprob} of the 1024 C2 problems (sort1d init + fp64 solve to tol)"
+        p = gen.c2(B=256)
+
+        def run(k):
+            t0 = time.perf_counter()
+            e = 0.0
+            for b in range(k):
+                f0 = O.init_sort1d(p.x[b].ravel(), p.y.ravel())
+                r = O.sinkhorn(p.x[b], p.y, p.eps, tol=p.tol, f0=f0)
+                e += float(p.n) * p.m * r.iterations
+            return e, time.perf_counter() - t0
+        if nprob is None:
+            e, t = run(2)
+            nprob = int(min(256, max(2, 2 * target_s / max(t, 1e-3))))
+        e, t = run(nprob)
+        return e, t, O.num_threads(), f"{nprob} of the 1024 C2 problems (sort1d init + fp64 solve to tol)"
 
 
 class Single(Workload):
@@ -264,17 +273,24 @@ class Single(Workload):
             out["subsample_inner_iterations"] = self.inner["iterations"]
         return out
 
-    def cpu_sample(self):
-        """The fp64 oracle timed on a bounded sample: one f-update (row LSE) on sampled rows."""
+    def cpu_sample(self, target_s=10.0):
+        """The fp64 oracle timed on a bounded sample: one f-update (row LSE pass) on sampled
+        rows, sized to take about target_s seconds."""
         from oracle import oracle as O
         p = self.p
-        rows = np.arange(0, p.n, max(1, p.n // {"c1": 256, "c3": 2048, "c4": 256, "c5": 512}[self.name]))
         g = np.zeros(p.m)
-        t0 = time.perf_counter()
-        O.f_update(p.x, p.y, g, p.eps, rows=rows)
-        t = time.perf_counter() - t0
-        return float(len(rows)) * p.m / 2, t, O.num_threads(), \
-            f"oracle row pass (f-update) over {len(rows)} sampled rows x {p.m} columns; one cost entry = 2 passes"
+
+        def run(k):
+            rows = np.linspace(0, p.n - 1, k).astype(np.int64)
+            t0 = time.perf_counter()
+            O.f_update(p.x, p.y, g, p.eps, rows=rows)
+            return time.perf_counter() - t0
+        k = min(p.n, 32)
+        t = run(k)
+        k = int(min(p.n, max(k, k * target_s / max(t, 1e-4))))
+        t = run(k)
+        return float(k) * p.m / 2, t, O.num_threads(), \
+            f"oracle row pass (f-update) over {k} sampled rows x {p.m} columns; one cost entry = 2 passes"
 
 
 def make_workload(args, sk, ctx, dev, rank, world):
@@ -328,10 +344,10 @@ def run_reference(args):
                "c5": lambda: gen.c5(eps_factor=args.eps_factor or 1e-2)}[w.name]()
     w.world = world
     for _ in range(args.warmup):
-        (w.cpu_sample(1) if args.workload == "c2" else w.cpu_sample())
+        (w.cpu_sample(1) if args.workload == "c2" else w.cpu_sample(target_s=1.0))
     tot_e, tot_t, thr, desc = 0.0, 0.0, 1, ""
     for _ in range(args.steps):
-        e, t, thr, desc = w.cpu_sample(2) if args.workload == "c2" else w.cpu_sample()
+        e, t, thr, desc = w.cpu_sample(2) if args.workload == "c2" else w.cpu_sample(target_s=5.0)
         tot_e += e
         tot_t += t
     v = tot_e / tot_t
