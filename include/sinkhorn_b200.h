@@ -230,6 +230,12 @@ sk_status sinkhorn_solve_sharded_emulated(sk_ctx *ctx, int32_t world, int64_t n,
                                           int32_t check_every, sk_cost_mode mode, const float *f_init,
                                           float *f, float *g, sk_report *rep /* host */);
 
+/* Diagnostic: out[i][j] = <x_i, y_j> for 128 x d and 128 x d fp32 inputs (row-major;
+ * out 128 x 128), computed by the tensor-core path of the LSE pass (K3: 3xTF32 split,
+ * tcgen05.mma kind::tf32, fp32 accumulators read back from TMEM).  d in [1, 64].  For
+ * testing the operand layout and the error compensation.  Blocks. */
+sk_status sk_selftest_tc_dot(sk_ctx *ctx, int32_t d, const float *x, const float *y, float *out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -40,7 +40,7 @@ EXPORTS = [
     "sk_set_timing", "sk_get_counters", "sk_reset_counters", "sk_nccl_unique_id", "sk_comm_init",
     "sk_shard_rows", "sinkhorn_sort1d_batched", "sinkhorn_init_zero", "sinkhorn_init_sort1d",
     "sinkhorn_init_gaussian", "sinkhorn_init_gmm", "sinkhorn_init_subsample", "sinkhorn_solve",
-    "sinkhorn_solve_sharded", "sinkhorn_solve_sharded_emulated",
+    "sinkhorn_solve_sharded", "sinkhorn_solve_sharded_emulated", "sk_selftest_tc_dot",
 ]
 
 _lib = None
@@ -83,6 +83,7 @@ def load() -> ctypes.CDLL:
                                        ctypes.c_int, P, P, P, ctypes.POINTER(SkReport)]),
         "sinkhorn_solve_sharded_emulated": (S, [P, I32, I64, I64, I32, P, P, P, P, F, F, I32, I32,
                                                 ctypes.c_int, P, P, P, ctypes.POINTER(SkReport)]),
+        "sk_selftest_tc_dot": (S, [P, I32, P, P, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -76,7 +76,7 @@ enum BufId {
     B_STAGE0 = 0, B_STAGE_END = 16,   // staging of host arrays
     B_FLAG = 16, B_XPACK, B_XC, B_XNK, B_XPOT, B_YPACK, B_YC, B_YNK, B_YPOT, B_PART, B_BLKE, B_BLKB,
     B_STATUS, B_COST, B_REP, B_SORT, B_PERM, B_YSORT, B_GAUSS, B_GAUSS2, B_GMM, B_SUBW, B_SUBZ,
-    B_SUBF, B_SUBG, B_IDX, B_OUT, B_FA, B_QUEUE, B_NBUF
+    B_SUBF, B_SUBG, B_IDX, B_OUT, B_FA, B_QUEUE, B_XIMG, B_YIMG, B_NBUF
 };
 
 sk_status fail(sk_ctx *c, sk_status s, const char *fmt, ...) {
@@ -255,10 +255,16 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
     bool stored = P.mode == SK_COST_STORED;
     if (P.mode == SK_COST_AUTO) stored = stored_ok && P.d >= 8 && P.d < 32 && 4.0 * n_sum * m <= 8.0e9;
     if (stored && !stored_ok) return fail(ctx, SK_EUNSUPPORTED, "stored-cost mode needs m %% 4 == 0");
-    const int D = stored ? 0 : lse_dpad(P.d);
-    if (!stored && D == 0) return fail(ctx, SK_EUNSUPPORTED, "online path supports d <= 64");
-    const int tq = stored ? 256 : lse_tq(D);
+    // tensor-core cross term for d in (16, 64] (BJ.ns "only when d >= 32"; d in (16, 32] pads to
+    // K = 32); SK_TC=0 forces the FFMA kernel (tuning / comparison knob)
+    static const int tc_env = [] { const char *e = getenv("SK_TC"); return e ? atoi(e) : 1; }();
+    const bool tc = !stored && P.d > 16 && P.d <= 64 && tc_env != 0;
+    const int katoms = P.d > 32 ? 2 : 1;
+    const int D = (stored || tc) ? 0 : lse_dpad(P.d);
+    if (!stored && !tc && D == 0) return fail(ctx, SK_EUNSUPPORTED, "online path supports d <= 64");
+    const int tq = stored ? 256 : (tc ? 128 : lse_tq(D));
     const long long yt = lse_tiles(m, tq);
+    const int pmode = stored ? PACK_STORED : (tc ? PACK_TC : PACK_ONLINE);
 
     // per-slice X sides, carved from one allocation per array
     std::vector<long long> off(ns + 1, 0), offp(ns + 1, 0);
@@ -275,6 +281,18 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
     ENSURE(ynk, float, B_YNK, m);
     ENSURE(ypot, float, B_YPOT, 2 * m);
     ENSURE(status, DevStatus, B_STATUS, 1);
+    float *ximg = nullptr, *yimg = nullptr;
+    std::vector<long long> offi(ns + 1, 0);
+    if (tc) {
+        for (int i = 0; i < ns; ++i) offi[i + 1] = offi[i] + (long long)tc_image_floats(slices[i].n, katoms);
+        cudaError_t e1, e2;
+        ximg = (float *)ensure(ctx, B_XIMG, sizeof(float) * (size_t)offi[ns], &e1);
+        yimg = (float *)ensure(ctx, B_YIMG, sizeof(float) * tc_image_floats(m, katoms), &e2);
+        if (!ximg || !yimg) return fail(ctx, SK_ENOMEM, "tensor-core operand images");
+        for (int i = 0; i < ns; ++i) CU(launch_pack_tc(slices[i].x, slices[i].n, P.d, katoms, ximg + offi[i], st));
+        CU(launch_pack_tc(P.y, m, P.d, katoms, yimg, st));
+        ctx->cnt.kernel_launches += ns + 1;
+    }
     std::vector<Side> X(ns);
     for (int i = 0; i < ns; ++i) {
         const long long n = slices[i].n;
@@ -289,8 +307,8 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
     const long long bs_rows = shard_block_rows(n_glob);
     const int nblk_glob = (int)((n_glob + bs_rows - 1) / bs_rows);
     const int blk_per_rank = sharded ? SK_SHARD_BLOCKS / P.world : nblk_glob;
-    const int occ = stored ? 8 : lse_occupancy_ctas(D);
-    const int Rr = D <= 4 ? 4 : (D <= 16 ? 2 : 1);
+    const int occ = stored ? 8 : (tc ? 1 : lse_occupancy_ctas(D));
+    const int Rr = tc ? 1 : (D <= 4 ? 4 : (D <= 16 ? 2 : 1));
     const long long ptiles_col = stored ? (m + 511) / 512 : (m + 128LL * Rr - 1) / (128LL * Rr);
     const int split_q = choose_split(ptiles_col, stored ? bs_rows / 64 : bs_rows / tq, occ, 64);
     const int nsplit_col = (sharded ? SK_SHARD_BLOCKS : nblk_glob) * split_q;
@@ -306,8 +324,8 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
 
     const float loga_u = (float)(-std::log((double)n_glob)), logb_u = (float)(-std::log((double)m));
     for (int i = 0; i < ns; ++i)
-        CU(pack_side(X[i], slices[i].x, slices[i].a, loga_u, slices[i].f_init, P.eps, st));
-    CU(pack_side(Y, P.y, P.b, logb_u, nullptr, P.eps, st));
+        CU(pack_side(X[i], slices[i].x, slices[i].a, loga_u, slices[i].f_init, P.eps, st, pmode));
+    CU(pack_side(Y, P.y, P.b, logb_u, nullptr, P.eps, st, pmode));
     CU(launch_status_init(status, P.max_iter, P.check_every, P.tol, st));
     ctx->cnt.kernel_launches += ns + 2;
 
@@ -346,6 +364,11 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
                     StoredPass scol{C[i], slices[i].n, m, P.eps, X[i].pack, col_part(i), bs_rows,
                                     sharded ? blk_per_rank : nblk_glob, split_q, &status->stop};
                     CU(launch_stored_cols(scol, st));
+                } else if (tc) {
+                    TcPass colp{yimg, ximg + offi[i], X[i].pack, (int)m, slices[i].n, katoms,
+                                sharded ? blk_per_rank : nblk_glob, (int)(bs_rows / tq), split_q, col_part(i),
+                                P.eps, &status->stop, nullptr};
+                    CU(launch_lse_tc(colp, st));
                 } else {
                     LsePass colp{&Y, &X[i], sharded ? blk_per_rank : nblk_glob, (int)(bs_rows / tq), split_q,
                                  col_part(i), P.eps, &status->stop};
@@ -364,6 +387,10 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
                 if (stored) {
                     StoredPass srow{C[i], slices[i].n, m, P.eps, Y.pack, part, 0, 1, 1, &status->stop};
                     CU(launch_stored_rows(srow, st));
+                } else if (tc) {
+                    TcPass rowp{ximg + offi[i], yimg, Y.pack, (int)slices[i].n, m, katoms, 1, 0, split_row, part,
+                                P.eps, &status->stop, nullptr};
+                    CU(launch_lse_tc(rowp, st));
                 } else {
                     LsePass rowp{&X[i], &Y, 1, 0, split_row, part, P.eps, &status->stop};
                     CU(launch_lse(rowp, st));
@@ -977,6 +1004,31 @@ sk_status sinkhorn_solve_sharded_emulated(sk_ctx *ctx, int32_t world, int64_t n,
     sk_status s2 = sg.flush();
     CU(cudaStreamSynchronize(ctx->stream));
     return s != SK_OK ? s : s2;
+}
+
+sk_status sk_selftest_tc_dot(sk_ctx *ctx, int32_t d, const float *x, const float *y, float *out) {
+    if (!ctx) return SK_EINVAL;
+    if (d < 1 || d > 64 || !x || !y || !out) return fail(ctx, SK_EINVAL, "d in [1, 64], non-NULL arrays");
+    const int katoms = d > 32 ? 2 : 1;
+    Stager sg(ctx);
+    const float *dx, *dy;
+    float *dout;
+    CK(sg.in_t(x, (size_t)128 * d, &dx));
+    CK(sg.in_t(y, (size_t)128 * d, &dy));
+    CK(sg.out_t(out, (size_t)128 * 128, &dout));
+    ENSURE(ximg, float, B_XIMG, tc_image_floats(128, katoms));
+    ENSURE(yimg, float, B_YIMG, tc_image_floats(128, katoms));
+    ENSURE(w, float, B_SUBG, 128);
+    ENSURE(part, float2, B_PART, 128);
+    CU(launch_pack_tc(dx, 128, d, katoms, ximg, ctx->stream));
+    CU(launch_pack_tc(dy, 128, d, katoms, yimg, ctx->stream));
+    CU(launch_fill(w, 128, 0.f, ctx->stream));
+    TcPass tp{ximg, yimg, w, 128, 128, katoms, 1, 0, 1, part, 1.f, nullptr, dout};
+    CU(launch_lse_tc(tp, ctx->stream));
+    ctx->cnt.kernel_launches += 4;
+    CK(sg.flush());
+    CU(cudaStreamSynchronize(ctx->stream));
+    return SK_OK;
 }
 
 }  // extern "C"

@@ -57,9 +57,28 @@ struct Side {
 };
 
 // Pack points (P x d, fp32 row-major), optional weights and initial potential.
-// If wts == nullptr the log-weight is the constant logw_const.
+// If wts == nullptr the log-weight is the constant logw_const.  mode: PACK_ONLINE (coords
+// in the tiles, |p|^2 folded), PACK_STORED (D = 0, no |p|^2: the cost is stored), PACK_TC
+// (D = 0, |p|^2 folded, coordinates live in the tensor-core images).
+enum PackMode { PACK_ONLINE = 0, PACK_STORED = 1, PACK_TC = 2 };
 cudaError_t pack_side(const Side &S, const float *pts, const float *wts, float logw_const,
-                      const float *pot0, float eps, cudaStream_t st);
+                      const float *pot0, float eps, cudaStream_t st, int mode = -1);
+
+// ------------------------------------------------------- K3 tensor-core pass
+struct TcPass {
+    const float *Aimg, *Bimg;   // images of the output side (A) and the reduced side (B)
+    const float *Bw;            // reduced side w (D = 0 pack, tq = 128)
+    int P;  long long Q;
+    int katoms;                 // 1 (K = 32) or 2 (K = 64)
+    int nblk, blk_tiles, split_q;
+    float2 *part;
+    float eps;
+    const int *stop;
+    float *debug_acc;
+};
+size_t tc_image_floats(long long P, int katoms);
+cudaError_t launch_pack_tc(const float *pts, long long P, int d, int katoms, float *img, cudaStream_t st);
+cudaError_t launch_lse_tc(const TcPass &L, cudaStream_t st);
 
 // One LSE pass: outputs P side points, reduces over Q side.  Splits:
 // nblk blocks of blk_tiles Q tiles each (the last may be shorter; blk_tiles = 0

@@ -40,7 +40,7 @@ template <int D> constexpr int kR = D <= 4 ? 4 : (D <= 16 ? 2 : 1);
 
 // ------------------------------------------------------------------- K1
 __global__ void k_pack_side(Side S, const float *__restrict__ pts, const float *__restrict__ wts,
-                            float logw_const, const float *__restrict__ pot0, float eps, int stored) {
+                            float logw_const, const float *__restrict__ pot0, float eps, int mode) {
     const long long tiles = lse_tiles(S.P, S.tq);
     const long long total = tiles * S.tq;
     const float kap = kLog2e / eps;
@@ -55,7 +55,9 @@ __global__ void k_pack_side(Side S, const float *__restrict__ pts, const float *
                 tile[k * S.tq + o] = v;
                 s = fmaf(v, v, s);
             }
-            if (stored) s = 0.f;  // stored cost: no |p|^2 folding
+            if (mode == PACK_TC)
+                for (int k = 0; k < S.d; ++k) s = fmaf(pts[p * S.d + k], pts[p * S.d + k], s);
+            if (mode == PACK_STORED) s = 0.f;  // stored cost: no |p|^2 folding
             const float lw = wts ? logf(wts[p]) : logw_const;
             S.c[p] = fmaf(eps, lw, s);
             S.nk[p] = s * kap;
@@ -70,11 +72,12 @@ __global__ void k_pack_side(Side S, const float *__restrict__ pts, const float *
 }
 
 cudaError_t pack_side(const Side &S, const float *pts, const float *wts, float logw_const,
-                      const float *pot0, float eps, cudaStream_t st) {
+                      const float *pot0, float eps, cudaStream_t st, int mode) {
     const long long total = lse_tiles(S.P, S.tq) * S.tq;
     int blocks = (int)((total + 255) / 256);
     if (blocks > 148 * 16) blocks = 148 * 16;
-    k_pack_side<<<blocks, 256, 0, st>>>(S, pts, wts, logw_const, pot0, eps, S.D == 0);
+    if (mode < 0) mode = S.D == 0 ? PACK_STORED : PACK_ONLINE;
+    k_pack_side<<<blocks, 256, 0, st>>>(S, pts, wts, logw_const, pot0, eps, mode);
     return cudaGetLastError();
 }
 

@@ -1,0 +1,77 @@
+"""Tensor-core (tcgen05 3xTF32) cross term, -m gpu: the raw 128x128 tile product against fp64,
+and the d > 16 solve through the tensor-core pass against the oracle and the FFMA kernel."""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+import torch
+
+from parity import assert_obj_close, assert_pair_close, count_tol
+from workloads import gen
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    import paper_2206_07630_b200 as sk
+    return sk.Context(0)
+
+
+@pytest.mark.parametrize("d", [64, 48, 33, 32, 20, 3])
+def test_tc_tile_product_is_fp32_accurate(ctx, d):
+    import ctypes
+    import paper_2206_07630_b200 as sk
+    rng = np.random.default_rng(d)
+    x = rng.standard_normal((128, d)).astype(np.float32)
+    y = rng.standard_normal((128, d)).astype(np.float32)
+    out = torch.empty((128, 128), dtype=torch.float32, device="cuda")
+    xd, yd = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+    ctx.check(ctx.lib.sk_selftest_tc_dot(ctx.h, d, ctypes.c_void_p(xd.data_ptr()), ctypes.c_void_p(yd.data_ptr()),
+                                         ctypes.c_void_p(out.data_ptr())))
+    ref = x.astype(np.float64) @ y.astype(np.float64).T
+    scale = np.abs(x).astype(np.float64) @ np.abs(y).astype(np.float64).T
+    err = np.abs(out.cpu().numpy() - ref) / scale
+    # 3xTF32: ~2^-22 relative to sum |x_k y_k| (1xTF32 would be ~2^-11)
+    assert err.max() < 4e-6, err.max()
+
+
+@pytest.mark.parametrize("n,m,d,eps_factor", [(1000, 1300, 64, 1e-2), (700, 515, 40, 5e-2), (2048, 2048, 64, 1e-1)])
+def test_tc_solve_parity(O, ctx, n, m, d, eps_factor):
+    import paper_2206_07630_b200 as sk
+    p = gen.c5(n=max(n, m), d=d, eps_factor=eps_factor)
+    x, y = p.x[:n].copy(), p.y[:m].copy()
+    eps = p.eps
+    f, g, rep = sk.sinkhorn_solve(ctx, torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda(), eps, mode="online")
+    ref = O.sinkhorn(x, y, eps)
+    assert rep["converged"] and abs(rep["iterations"] - ref.iterations) <= count_tol(ref.iterations)
+    lock = O.sinkhorn(x, y, eps, tol=0, max_iter=rep["iterations"])
+    assert_pair_close(f.cpu().numpy(), g.cpu().numpy(), lock.f, lock.g, eps)
+    assert_obj_close(rep["dual_objective"], lock.E, eps)
+
+
+def test_tc_matches_ffma_kernel():
+    """Same problem through the tcgen05 pass and (SK_TC=0) the FFMA pass: same iteration count,
+    potentials within fp32 noise of each other."""
+    code = r'''
+import sys, numpy as np, torch
+sys.path.insert(0, %r)
+import paper_2206_07630_b200 as sk
+from workloads import gen
+p = gen.c5(n=1536, eps_factor=1e-2)
+ctx = sk.Context(0)
+f, g, r = sk.sinkhorn_solve(ctx, torch.from_numpy(p.x).cuda(), torch.from_numpy(p.y).cuda(), p.eps, mode="online")
+np.savez(sys.argv[1], f=f.cpu().numpy(), g=g.cpu().numpy(), it=r["iterations"])
+''' % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for tc in ("1", "0"):
+        fn = f"/tmp/tc_cmp_{tc}_{os.getpid()}.npz"
+        env = dict(os.environ, SK_TC=tc)
+        subprocess.check_call([sys.executable, "-c", code, fn], env=env)
+        outs.append(np.load(fn))
+    a, b = outs
+    assert abs(int(a["it"]) - int(b["it"])) <= 1
+    fa, fb = a["f"] - a["f"].mean(), b["f"] - b["f"].mean()
+    assert np.abs(fa - fb).max() <= 1e-4 * max(np.abs(fb).max(), 1e-3)
