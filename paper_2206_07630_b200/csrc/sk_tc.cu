@@ -23,7 +23,8 @@
 namespace sk {
 
 constexpr int kTcM = 128;       // points per tile (MMA M and N)
-constexpr int kTcThreads = 192; // 6 warps
+constexpr int kTcEpiWarps = 8;  // two per TMEM lane quadrant, each half of the columns
+constexpr int kTcThreads = 64 + 32 * kTcEpiWarps;
 constexpr int kTcStages = 2;
 
 __host__ __device__ constexpr int tc_img_bytes(int katoms) { return 16 * katoms * 1024; }  // one of hi/lo
@@ -149,8 +150,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lse_tc(TcArgs A) {
 
     if (threadIdx.x == 0) {
         mbar_init(&bar_a, 1);
-        for (int i = 0; i < kTcStages; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1 + 4); }
-        for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4); }
+        for (int i = 0; i < kTcStages; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1 + kTcEpiWarps); }
+        for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], kTcEpiWarps); }
         fence_mbar_init();
     }
     if (warp == 1) {  // 256 TMEM columns: two 128x128 fp32 accumulators
@@ -204,8 +205,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lse_tc(TcArgs A) {
             }
         }
     } else {
-        // epilogue: warp w reads TMEM lanes 32*(w%4) .. +31; thread = one output point
-        const int q4 = warp & 3;
+        // epilogue: warp w reads TMEM lanes 32*(w%4) .. +31 (its quadrant) and the column half
+        // h = (w-2)/4 of every accumulator; thread = one output point, (M, S) over its half.
+        const int q4 = warp & 3, h = (warp - 2) >> 2;
         const int row = q4 * 32 + lane;
         const int p = blockIdx.x * kTcM + row;
         float M = -INFINITY, S = 0.f;
@@ -213,34 +215,41 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lse_tc(TcArgs A) {
             const int st = i % kTcStages, b = i & 1;
             mbar_wait(&tfull[b], (i >> 1) & 1);
             tc_fence_after();
-            const float *w = sW + st * kTcM;
-#pragma unroll 1
-            for (int c = 0; c < kTcM; c += 32) {
-                uint32_t r[32];
-                const uint32_t taddr = tbase + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(b * kTcM + c);
-                TMEM_LD32(taddr, r);
-                tmem_ld_wait();
-                float t[32];
-                if (A.debug_acc && i == 0 && blockIdx.x == 0 && blockIdx.y == 0) {
+            const float *w = sW + st * kTcM + h * 64;
+            uint32_t r[64];
+            const uint32_t taddr = tbase + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(b * kTcM + h * 64);
+            TMEM_LD32(taddr, r);
+            TMEM_LD32(taddr + 32, (r + 32));
+            tmem_ld_wait();
+            if (A.debug_acc && i == 0 && blockIdx.x == 0 && blockIdx.y == 0) {
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) A.debug_acc[row * kTcM + c + j] = __uint_as_float(r[j]);
-                }
-#pragma unroll
-                for (int j = 0; j < 32; ++j) t[j] = fmaf(__uint_as_float(r[j]), A.tk, w[c + j]);
-                float cm = t[0];
-#pragma unroll
-                for (int j = 1; j < 32; ++j) cm = fmaxf(cm, t[j]);
-                if (cm > M) { S *= ex2(M - cm); M = cm; }
-                float s0 = 0.f, s1 = 0.f;
-#pragma unroll
-                for (int j = 0; j < 32; j += 2) { s0 += ex2(t[j] - M); s1 += ex2(t[j + 1] - M); }
-                S += s0 + s1;
+                for (int j = 0; j < 64; ++j) A.debug_acc[row * kTcM + h * 64 + j] = __uint_as_float(r[j]);
             }
+            float t[64];
+#pragma unroll
+            for (int j = 0; j < 64; ++j) t[j] = fmaf(__uint_as_float(r[j]), A.tk, w[j]);
+            // accumulator b and the w slot are no longer needed: release them early
             tc_fence_before();
             __syncwarp();
             if (lane == 0) { mbar_arrive(&tempty[b]); mbar_arrive(&empty[st]); }
+            float cm = t[0];
+#pragma unroll
+            for (int j = 1; j < 64; ++j) cm = fmaxf(cm, t[j]);
+            if (cm > M) { S *= ex2(M - cm); M = cm; }
+            float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+            for (int j = 0; j < 64; j += 2) { s0 += ex2(t[j] - M); s1 += ex2(t[j + 1] - M); }
+            S += s0 + s1;
         }
-        if (p < A.P) A.part[(long long)s * A.P + p] = make_float2(M, S);
+        // combine the two column halves of each row (fixed order: half 0 then half 1)
+        float2 *xch = reinterpret_cast<float2 *>(sW + kTcStages * kTcM);  // 128 x float2
+        if (h == 1) xch[row] = make_float2(M, S);
+        asm volatile("bar.sync 1, %0;" ::"r"(32 * kTcEpiWarps));
+        if (h == 0) {
+            const float2 o = xch[row];
+            lse_merge(M, S, o.x, o.y);
+            if (p < A.P) A.part[(long long)s * A.P + p] = make_float2(M, S);
+        }
     }
     tc_fence_before();
     __syncthreads();
@@ -264,8 +273,8 @@ cudaError_t launch_pack_tc(const float *pts, long long P, int d, int katoms, flo
 
 template <int KATOMS>
 static cudaError_t launch_tc_k(const TcArgs &A, int ptiles, int nsplit, cudaStream_t st) {
-    const size_t smem = 1024 + 2 * (size_t)tc_img_bytes(KATOMS) + kTcStages * (2 * (size_t)tc_img_bytes(KATOMS) + kTcM * 4);
-    static_assert(kTcStages * kTcM * 4 <= 1024, "w ring fits the slack");
+    const size_t smem = 1024 + 2 * (size_t)tc_img_bytes(KATOMS) + kTcStages * (2 * (size_t)tc_img_bytes(KATOMS) + kTcM * 4)
+                        + kTcM * 8;   // half-combination exchange
     cudaError_t e = cudaFuncSetAttribute(k_lse_tc<KATOMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     dim3 grid(ptiles, nsplit);
