@@ -236,6 +236,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lse_tc(TcArgs A) {
 #pragma unroll
             for (int j = 1; j < 64; ++j) cm = fmaxf(cm, t[j]);
             if (cm > M) { S *= ex2(M - cm); M = cm; }
+            if (M == -INFINITY) continue;  // only padding seen so far (ragged last tile's upper half)
             float s0 = 0.f, s1 = 0.f;
 #pragma unroll
             for (int j = 0; j < 64; j += 2) { s0 += ex2(t[j] - M); s1 += ex2(t[j + 1] - M); }
