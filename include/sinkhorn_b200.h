@@ -236,6 +236,13 @@ sk_status sinkhorn_solve_sharded_emulated(sk_ctx *ctx, int32_t world, int64_t n,
  * testing the operand layout and the error compensation.  Blocks. */
 sk_status sk_selftest_tc_dot(sk_ctx *ctx, int32_t d, const float *x, const float *y, float *out);
 
+/* K14 microbenchmarks (roofline denominators measured on this device, CUDA events on the
+ * context stream): kind 0 = MUFU.EX2 throughput (ex2/s); 1 = FP32 FMA throughput (FMA
+ * lane-operations/s, packed FFMA2); 2 = streaming HBM read bandwidth (bytes/s, 4 GiB,
+ * 128-bit non-allocating loads); 3 = tcgen05 kind::tf32 MMA throughput (flop/s, the K3
+ * kernel with its epilogue skipped).  *value (host) receives the rate.  Blocks. */
+sk_status sk_microbench(sk_ctx *ctx, int32_t kind, double *value);
+
 #ifdef __cplusplus
 }
 #endif

@@ -71,6 +71,13 @@ class Context:
     def reset_counters(self) -> None:
         self.check(self.lib.sk_reset_counters(self.h))
 
+    def microbench(self, kind: str) -> float:
+        """K14 roofline denominators: 'ex2' (ex2/s), 'ffma' (FMA/s), 'hbm' (read B/s), 'tf32' (flop/s)."""
+        k = {"ex2": 0, "ffma": 1, "hbm": 2, "tf32": 3}[kind]
+        v = ctypes.c_double()
+        self.check(self.lib.sk_microbench(self.h, k, ctypes.byref(v)))
+        return v.value
+
     def nccl_unique_id(self) -> bytes:
         buf = ctypes.create_string_buffer(128)
         self.check(self.lib.sk_nccl_unique_id(self.h, buf))

@@ -41,6 +41,7 @@ EXPORTS = [
     "sk_shard_rows", "sinkhorn_sort1d_batched", "sinkhorn_init_zero", "sinkhorn_init_sort1d",
     "sinkhorn_init_gaussian", "sinkhorn_init_gmm", "sinkhorn_init_subsample", "sinkhorn_solve",
     "sinkhorn_solve_sharded", "sinkhorn_solve_sharded_emulated", "sk_selftest_tc_dot",
+    "sk_microbench",
 ]
 
 _lib = None
@@ -84,6 +85,7 @@ def load() -> ctypes.CDLL:
         "sinkhorn_solve_sharded_emulated": (S, [P, I32, I64, I64, I32, P, P, P, P, F, F, I32, I32,
                                                 ctypes.c_int, P, P, P, ctypes.POINTER(SkReport)]),
         "sk_selftest_tc_dot": (S, [P, I32, P, P, P]),
+        "sk_microbench": (S, [P, I32, ctypes.POINTER(D)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

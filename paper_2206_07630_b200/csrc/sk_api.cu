@@ -367,7 +367,7 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
                 } else if (tc) {
                     TcPass colp{yimg, ximg + offi[i], X[i].pack, (int)m, slices[i].n, katoms,
                                 sharded ? blk_per_rank : nblk_glob, (int)(bs_rows / tq), split_q, col_part(i),
-                                P.eps, &status->stop, nullptr};
+                                P.eps, &status->stop, nullptr, 0};
                     CU(launch_lse_tc(colp, st));
                 } else {
                     LsePass colp{&Y, &X[i], sharded ? blk_per_rank : nblk_glob, (int)(bs_rows / tq), split_q,
@@ -389,7 +389,7 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
                     CU(launch_stored_rows(srow, st));
                 } else if (tc) {
                     TcPass rowp{ximg + offi[i], yimg, Y.pack, (int)slices[i].n, m, katoms, 1, 0, split_row, part,
-                                P.eps, &status->stop, nullptr};
+                                P.eps, &status->stop, nullptr, 0};
                     CU(launch_lse_tc(rowp, st));
                 } else {
                     LsePass rowp{&X[i], &Y, 1, 0, split_row, part, P.eps, &status->stop};
@@ -1023,11 +1023,56 @@ sk_status sk_selftest_tc_dot(sk_ctx *ctx, int32_t d, const float *x, const float
     CU(launch_pack_tc(dx, 128, d, katoms, ximg, ctx->stream));
     CU(launch_pack_tc(dy, 128, d, katoms, yimg, ctx->stream));
     CU(launch_fill(w, 128, 0.f, ctx->stream));
-    TcPass tp{ximg, yimg, w, 128, 128, katoms, 1, 0, 1, part, 1.f, nullptr, dout};
+    TcPass tp{ximg, yimg, w, 128, 128, katoms, 1, 0, 1, part, 1.f, nullptr, dout, 0};
     CU(launch_lse_tc(tp, ctx->stream));
     ctx->cnt.kernel_launches += 4;
     CK(sg.flush());
     CU(cudaStreamSynchronize(ctx->stream));
+    return SK_OK;
+}
+
+sk_status sk_microbench(sk_ctx *ctx, int32_t kind, double *value) {
+    if (!ctx || !value || kind < 0 || kind > 3) return fail(ctx, SK_EINVAL, "kind in [0, 3]");
+    cudaStream_t st = ctx->stream;
+    ENSURE(sink, float, B_OUT, 1024);
+    float ms = 0.f;
+    if (kind <= 1) {
+        double ops = 0.0;
+        CU(microbench_alu(kind, st, ctx->ev0, ctx->ev1, sink, &ops));
+        CU(cudaEventSynchronize(ctx->ev1));
+        CU(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+        *value = ops / (ms * 1e-3);
+    } else if (kind == 2) {
+        const long long bytes = 4LL << 30;
+        cudaError_t e;
+        float *buf = (float *)ensure(ctx, B_COST, bytes, &e);
+        if (!buf) return fail(ctx, SK_ENOMEM, "4 GiB probe buffer");
+        CU(cudaMemsetAsync(buf, 0, bytes, st));
+        CU(microbench_hbm(buf, bytes, st, ctx->ev0, ctx->ev1, sink));
+        CU(cudaEventSynchronize(ctx->ev1));
+        CU(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+        *value = (double)bytes / (ms * 1e-3);
+    } else {
+        const long long P = 32768, Q = 32768;   // 256 x 256 tiles of 128 x 128 x 64, 3 MMAs each
+        const int katoms = 2;
+        cudaError_t e1, e2;
+        float *img = (float *)ensure(ctx, B_XIMG, sizeof(float) * tc_image_floats(P, katoms), &e1);
+        ENSURE(w, float, B_SUBG, Q);
+        ENSURE(part, float2, B_PART, P * 8);
+        (void)e2;
+        if (!img) return fail(ctx, SK_ENOMEM, "tc probe images");
+        CU(cudaMemsetAsync(img, 0, sizeof(float) * tc_image_floats(P, katoms), st));
+        CU(launch_fill(w, Q, 0.f, st));
+        TcPass tp{img, img, w, (int)P, Q, katoms, 1, 0, 4, part, 1.f, nullptr, nullptr, 1};
+        CU(launch_lse_tc(tp, st));  // warm-up
+        CU(cudaEventRecord(ctx->ev0, st));
+        CU(launch_lse_tc(tp, st));
+        CU(cudaEventRecord(ctx->ev1, st));
+        CU(cudaEventSynchronize(ctx->ev1));
+        CU(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+        *value = 3.0 * 2.0 * 64.0 * (double)P * (double)Q / (ms * 1e-3);
+    }
+    ctx->cnt.kernel_launches += 2;
     return SK_OK;
 }
 

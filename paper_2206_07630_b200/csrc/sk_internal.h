@@ -75,6 +75,7 @@ struct TcPass {
     float eps;
     const int *stop;
     float *debug_acc;
+    int mma_only = 0;
 };
 size_t tc_image_floats(long long P, int katoms);
 cudaError_t launch_pack_tc(const float *pts, long long P, int d, int katoms, float *img, cudaStream_t st);
@@ -166,5 +167,10 @@ struct StoredPass {
 };
 cudaError_t launch_stored_rows(const StoredPass &S, cudaStream_t st);
 cudaError_t launch_stored_cols(const StoredPass &S, cudaStream_t st);
+
+// ------------------------------------------------------------ K14 microbenchmarks
+cudaError_t microbench_alu(int kind, cudaStream_t st, cudaEvent_t e0, cudaEvent_t e1, float *sink, double *ops);
+cudaError_t microbench_hbm(const float *buf, long long bytes, cudaStream_t st, cudaEvent_t e0, cudaEvent_t e1,
+                           float *sink);
 
 }  // namespace sk

@@ -121,6 +121,7 @@ struct TcArgs {
     float tk;               // 2 log2(e)/eps
     const int *stop;
     float *debug_acc;       // if non-null: write raw acc of the first Q tile, [128][128]
+    int mma_only;           // K14 microbenchmark: epilogue only releases the buffers
 };
 
 template <int KATOMS>
@@ -215,6 +216,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lse_tc(TcArgs A) {
             const int st = i % kTcStages, b = i & 1;
             mbar_wait(&tfull[b], (i >> 1) & 1);
             tc_fence_after();
+            if (A.mma_only) {
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) { mbar_arrive(&tempty[b]); mbar_arrive(&empty[st]); }
+                continue;
+            }
             const float *w = sW + st * kTcM + h * 64;
             uint32_t r[64];
             const uint32_t taddr = tbase + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(b * kTcM + h * 64);
@@ -289,6 +296,7 @@ cudaError_t launch_lse_tc(const TcPass &L, cudaStream_t st) {
     A.P = L.P; A.Qtiles = (int)((L.Q + kTcM - 1) / kTcM);
     A.blk_tiles = L.blk_tiles; A.split_q = L.split_q;
     A.part = L.part; A.tk = 2.f * kLog2e / L.eps; A.stop = L.stop; A.debug_acc = L.debug_acc;
+    A.mma_only = L.mma_only;
     const int ptiles = (L.P + kTcM - 1) / kTcM;
     const int nsplit = L.nblk * L.split_q;
     return L.katoms == 1 ? launch_tc_k<1>(A, ptiles, nsplit, st) : launch_tc_k<2>(A, ptiles, nsplit, st);

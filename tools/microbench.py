@@ -1,0 +1,13 @@
+"""K14: print the measured roofline denominators of this device (JSON)."""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2206_07630_b200 as sk  # noqa: E402
+
+ctx = sk.Context(0)
+out = {k: ctx.microbench(k) for k in ("ex2", "ffma", "hbm", "tf32")}
+out = {"ex2_per_s": out["ex2"], "ffma_per_s": out["ffma"], "hbm_read_GBps": out["hbm"] / 1e9,
+       "tf32_TFLOPs": out["tf32"] / 1e12}
+print(json.dumps(out))
