@@ -188,7 +188,8 @@ class Single(Workload):
             self.scaling = "strong"
         else:
             self.p = gen.c5(eps_factor=args.eps_factor or 1e-2); self.init = args.init or "gaussian"
-            self.mode = "online"; self.roof = "ffma"; self.kernel = "k_lse<64,1> (online LSE pass, FFMA cross term)"
+            self.mode = "online"; self.roof = "tensor"
+            self.kernel = "k_lse_tc<2> (online LSE pass, tcgen05 3xTF32 cross term, K3)"
         p = self.p
         self.n, self.m, self.d = p.n, p.m, p.d
         self.sharded = self.name == "c4" and world > 1
@@ -308,13 +309,14 @@ def roofline(w, cnt, steps, pk, src):
                 "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({src})",
                 "algorithmic": "4 bytes (one fp32 C_ij read) per cost entry per pass",
                 "kernel_ms_per_step": ms}
-    if w.roof == "ffma":
-        flops = cnt["lse_ex2"] * 2 * w.d     # cross term: d FMA per entry per pass
+    if w.roof == "tensor":
+        flops = cnt["lse_ex2"] * 3 * 2 * 64          # 3 TF32 MMAs (hi.hi, hi.lo, lo.hi), K = 64
         achieved = flops / (cnt["lse_ms"] / 1e3) / 1e12 if cnt["lse_ms"] > 0 else 0.0
-        peak = N_SM * FFMA_PER_CLK_SM * 2 * sm_max * 1e6 / 1e12
-        return {"bound": "alu", "pipe": "FFMA (cross term 2d flops/entry)", "kernel": w.kernel,
-                "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
-                "peak_source": f"derived: {N_SM} SM x {FFMA_PER_CLK_SM} FP32 lanes x 2 x {sm_max:.0f} MHz ({src})",
+        peak = float(pk["bf16_tflops"]) * 1.1 / 2.25   # TF32 = measured BF16 x nominal TF32/BF16 ratio
+        return {"bound": "tensor", "kernel": w.kernel, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak, "traffic": None,
+                "peak_source": f"MEASURED_PEAKS.json bf16_tflops x 1.1/2.25 (nominal TF32/BF16), {src}",
+                "algorithmic": "3 x 2 x 64 TF32 flops per cost entry per pass (3xTF32 split)",
                 "kernel_ms_per_step": ms}
     achieved = cnt["lse_ex2"] / (cnt["lse_ms"] / 1e3) if cnt["lse_ms"] > 0 else 0.0
     peak = N_SM * MUFU_EX2_PER_CLK_SM * sm_max * 1e6
@@ -384,6 +386,14 @@ def run_ours(args):
             dist.barrier(device_ids=[dev.index])
         torch.cuda.synchronize(dev)
 
+    k14 = {}
+    if rank == 0 and not args.no_k14:
+        # K14 microbenchmarks: this device's MUFU / FP32 / HBM / TF32 rates (roofline context)
+        try:
+            k14 = {"ex2_per_s": ctx.microbench("ex2"), "ffma_per_s": ctx.microbench("ffma"),
+                   "hbm_read_GBps": ctx.microbench("hbm") / 1e9, "tf32_TFLOPs": ctx.microbench("tf32") / 1e12}
+        except Exception as ex:  # pragma: no cover
+            k14 = {"error": repr(ex)}
     with torch.cuda.stream(stream):
         w = make_workload(args, sk, ctx, dev, rank, world)
         for _ in range(max(args.warmup, 0)):
@@ -453,6 +463,7 @@ def run_ours(args):
             "roofline": roofline(w, cnt, args.steps, pk, src),
             "gpu_launches": int(cnt["kernel_launches"]),
             "clocks": clk.summary(),
+            "k14_measured_peaks": k14,
             "e2e": {"value": e2e_entries / (e2e_ms / 1e3), "unit": "cost-entries/s",
                     "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
         }
@@ -481,6 +492,7 @@ def main():
     ap.add_argument("--init", default=None, help="c3/c4/c5 initializer: zero|gaussian|gmm|subsample")
     ap.add_argument("--eps-factor", type=float, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-k14", action="store_true", help="skip the K14 microbenchmarks")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -353,36 +353,69 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
     MergePass mcol{MERGE_COL, &Y, part, nsplit_col, P.eps, P.b, status, blke, blkb, nullptr, 0.f,
                    sharded ? 1 : 0, 0};
 
+    // stored mode: one HBM read of C per sweep (fused row + column passes, H4s) when m fits
+    static const int fused_env = [] { const char *e = getenv("SK_FUSED"); return e ? atoi(e) : 1; }();
+    const bool fused = stored && fused_env != 0 && stored_fused_supported(m);
+    bool first = true;
+
+    auto col_stage = [&]() -> sk_status {
+        for (int i = 0; i < ns; ++i) {
+            if (stored) {
+                StoredPass scol{C[i], slices[i].n, m, P.eps, X[i].pack, col_part(i), bs_rows,
+                                sharded ? blk_per_rank : nblk_glob, split_q, &status->stop};
+                CU(launch_stored_cols(scol, st));
+            } else if (tc) {
+                TcPass colp{yimg, ximg + offi[i], X[i].pack, (int)m, slices[i].n, katoms,
+                            sharded ? blk_per_rank : nblk_glob, (int)(bs_rows / tq), split_q, col_part(i),
+                            P.eps, &status->stop, nullptr, 0};
+                CU(launch_lse_tc(colp, st));
+            } else {
+                LsePass colp{&Y, &X[i], sharded ? blk_per_rank : nblk_glob, (int)(bs_rows / tq), split_q,
+                             col_part(i), P.eps, &status->stop};
+                CU(launch_lse(colp, st));
+            }
+        }
+        return SK_OK;
+    };
+    auto exchange_and_merge_col = [&]() -> sk_status {
+        if (P.nccl && sharded) {
+            int r = g_nccl.allgather(col_part(0), part, (size_t)slot * 2, kNcclFloat32, ctx->comm, st);
+            if (r != 0) return fail(ctx, SK_ENCCL, "ncclAllGather failed: %s", g_nccl.errstr ? g_nccl.errstr(r) : "?");
+        }
+        CU(launch_merge(mcol, st));
+        return SK_OK;
+    };
+
     CU(cudaEventRecord(ctx->ev0, st));
     int launched = 0, poll = 4;
     const int max_sweeps = P.max_iter + 1;  // + the column pass that measures err_L
     for (int it = 0; it < max_sweeps;) {
         const int chunk = std::min(poll, max_sweeps - it);
         for (int c = 0; c < chunk; ++c, ++it) {
-            for (int i = 0; i < ns; ++i) {
-                if (stored) {
-                    StoredPass scol{C[i], slices[i].n, m, P.eps, X[i].pack, col_part(i), bs_rows,
-                                    sharded ? blk_per_rank : nblk_glob, split_q, &status->stop};
-                    CU(launch_stored_cols(scol, st));
-                } else if (tc) {
-                    TcPass colp{yimg, ximg + offi[i], X[i].pack, (int)m, slices[i].n, katoms,
-                                sharded ? blk_per_rank : nblk_glob, (int)(bs_rows / tq), split_q, col_part(i),
-                                P.eps, &status->stop, nullptr, 0};
-                    CU(launch_lse_tc(colp, st));
-                } else {
-                    LsePass colp{&Y, &X[i], sharded ? blk_per_rank : nblk_glob, (int)(bs_rows / tq), split_q,
-                                 col_part(i), P.eps, &status->stop};
-                    CU(launch_lse(colp, st));
+            if (fused) {
+                if (first) {  // g^1 from f^0 with a plain column pass
+                    CK(col_stage());
+                    CK(exchange_and_merge_col());
+                    launched += ns + 1;
+                    first = false;
                 }
-                ++launched;
+                for (int i = 0; i < ns; ++i) {
+                    FusedLaunch fl{C[i], slices[i].n, m, P.eps, Y.pack, X[i].c, {X[i].pot[0], X[i].pot[1]},
+                                   X[i].pack, col_part(i), bs_rows, sharded ? blk_per_rank : nblk_glob, split_q,
+                                   status};
+                    CU(launch_stored_fused(fl, st));
+                    MergePass mrow{MERGE_ROW, &X[i], part, 1, P.eps, nullptr, status, blke, blkb, nullptr, 0.f,
+                                   sharded ? 1 : 0, i + 1 < ns ? 1 : 0, 1};
+                    CU(launch_merge(mrow, st));
+                    launched += 2;
+                }
+                CK(exchange_and_merge_col());
+                launched += 1;
+                continue;
             }
-            if (P.nccl && sharded) {
-                int r = g_nccl.allgather(col_part(0), part, (size_t)slot * 2, kNcclFloat32, ctx->comm, st);
-                if (r != 0) return fail(ctx, SK_ENCCL, "ncclAllGather failed: %s",
-                                        g_nccl.errstr ? g_nccl.errstr(r) : "?");
-            }
-            CU(launch_merge(mcol, st));
-            ++launched;
+            CK(col_stage());
+            CK(exchange_and_merge_col());
+            launched += ns + 1;
             for (int i = 0; i < ns; ++i) {
                 if (stored) {
                     StoredPass srow{C[i], slices[i].n, m, P.eps, Y.pack, part, 0, 1, 1, &status->stop};
@@ -444,7 +477,7 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
     if (ctx->timing) ctx->cnt.lse_ms += ms;
     const double entries = (double)n_sum * m * (2.0 * L + 1.0);
     ctx->cnt.lse_ex2 += entries;
-    if (stored) ctx->cnt.lse_bytes += 4.0 * entries;
+    if (stored) ctx->cnt.lse_bytes += 4.0 * (double)n_sum * m * (fused ? (1.0 + hs.iter) : (2.0 * L + 1.0));
     rep->iterations = L;
     rep->converged = hs.converged;
     rep->marginal_error = hs.err;

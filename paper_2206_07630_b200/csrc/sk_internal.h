@@ -110,6 +110,7 @@ struct MergePass {
     float out_const;          // MERGE_OUT: added constant (eps log ms for Eq. 8)
     int sharded;              // non-finite f is detected by the next (replicated) column merge
     int no_iter_inc;          // MERGE_ROW of a non-final slice (emulated ranks): keep the counter
+    int precomputed = 0;      // MERGE_ROW: potential and w already written (fused stored sweep)
 };
 cudaError_t launch_merge(const MergePass &M, cudaStream_t st);
 int merge_blocks(int P);
@@ -166,6 +167,21 @@ struct StoredPass {
     const int *stop;
 };
 cudaError_t launch_stored_rows(const StoredPass &S, cudaStream_t st);
+// Fused single-read sweep (H4s): f^{l+1} rows (written with their w) and the column partials
+// of g^{l+2} from one read of each row block of C.
+struct FusedLaunch {
+    const float *C; long long n, m;
+    float eps;
+    const float *gw, *xc;
+    float *xpot[2];
+    float *xw;
+    float2 *part;
+    long long blk_rows;
+    int nblk, split_q;
+    DevStatus *st;
+};
+bool stored_fused_supported(long long m);
+cudaError_t launch_stored_fused(const FusedLaunch &L, cudaStream_t st);
 cudaError_t launch_stored_cols(const StoredPass &S, cudaStream_t st);
 
 // ------------------------------------------------------------ K14 microbenchmarks

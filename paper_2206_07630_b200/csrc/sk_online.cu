@@ -234,11 +234,15 @@ __global__ void __launch_bounds__(kMT) k_merge(MergePass Mp, Side S) {
     const float eps = Mp.eps, kap = kLog2e / eps, epsln2 = eps * kLn2;
     const bool check = Mp.mode == MERGE_COL && l >= 1 &&
                        (l % st->check_every == 0 || l == st->max_iter);
-    const float *hold = S.pot[l & 1];
-    float *hnew = S.pot[(l + 1) & 1];
+    const float *hold = (l & 1) ? S.pot[1] : S.pot[0];      // no dynamic param indexing
+    float *hnew = (l & 1) ? S.pot[0] : S.pot[1];
     double e = 0.0;
     int bad = 0;
     for (int p = blockIdx.x * kMT + threadIdx.x; p < S.P; p += gridDim.x * kMT) {
+        if (Mp.precomputed) {  // fused stored sweep wrote f and w; only check finiteness
+            bad |= !isfinite(hnew[p]);
+            continue;
+        }
         float M = -INFINITY;
         for (int s = 0; s < Mp.nsplit; ++s) M = fmaxf(M, Mp.part[(long long)s * S.P + p].x);
         float Ssum = 0.f;
@@ -320,7 +324,7 @@ __global__ void __launch_bounds__(1024) k_report(Side X, Side Y, const float *a,
                                                   long long n_uniform) {
     __shared__ double red[32];
     const int l = st->final_iter;
-    const float *f = X.pot[l & 1], *g = Y.pot[l & 1];
+    const float *f = (l & 1) ? X.pot[1] : X.pot[0], *g = (l & 1) ? Y.pot[1] : Y.pot[0];
     double s = 0.0;
     for (int i = threadIdx.x; i < X.P; i += 1024) {
         const double ai = a ? (double)a[i] : 1.0 / n_uniform;

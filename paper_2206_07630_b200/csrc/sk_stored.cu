@@ -199,3 +199,159 @@ cudaError_t launch_stored_cols(const StoredPass &S, cudaStream_t st) {
 }
 
 }  // namespace sk
+
+namespace sk {
+
+// ------------------------------------------------------------------ K5 fused
+// One HBM read of C per sweep.  CTA s owns the rows of split s (same
+// fixed block structure as k_cols) and, in registers, the (max, sum) state of every column:
+// thread t owns the float4 groups t, t + 512, ... (CPT columns).  Per group of 4 rows:
+//   phase A  warps 4r..4r+3 stream row r (a quarter each) from HBM: exact online
+//            (max, sum) of t = g_j log2(e)/eps - C_ij log2(e)/eps, combined in fixed order
+//            -> f_i = eps log a_i - eps ln2 (M + log2 S) (Alg. 1 l.4), written with its w;
+//   phase B  every thread re-reads its columns of the 4 rows (L2 hits: the group was
+//            bulk-prefetched into L2 one group ahead) and updates the column state with
+//            t = f_i log2(e)/eps - C_ij log2(e)/eps (the partials of g^{l+2}, Alg. 1 l.5).
+// Deterministic: fixed per-row quarter order, per-column sequential row order.
+constexpr int kFT = 512;
+
+struct FusedArgs {
+    const float *C; long long n, m;
+    float eps;
+    const float *gw;        // g log2(e)/eps (Y side D = 0 pack), m
+    const float *xc;        // eps log a_i (X side c), n
+    float *xpot[2];         // X potential buffers (parity = iteration)
+    float *xw;              // X side w pack (f log2(e)/eps), n
+    float2 *part;           // column partials [nblk * split_q][m]
+    long long blk_rows;
+    int split_q;
+    DevStatus *st;
+};
+
+__device__ __forceinline__ void prefetch_l2(const void *p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+template <int CPT>
+__global__ void __launch_bounds__(kFT, 1) k_stored_fused(FusedArgs A) {
+    __shared__ float2 red[16];
+    __shared__ float wrow[4];
+    if (*(volatile const int *)&A.st->stop) return;
+    const int l = A.st->iter;                      // producing f^{l+1}
+    float *fnew = ((l + 1) & 1) ? A.xpot[1] : A.xpot[0];   // no dynamic param indexing
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const float kap = kLog2e / A.eps, epsln2 = A.eps * kLn2;
+    const int s = blockIdx.x;
+    const int bq = s / A.split_q, u = s % A.split_q;
+    const long long bs = A.blk_rows > 0 ? A.blk_rows : A.n;
+    const long long b0 = bq * bs, nb = max(0LL, min(bs, A.n - b0));
+    const long long r0 = b0 + nb * u / A.split_q, r1 = b0 + nb * (u + 1) / A.split_q;
+    const long long m4 = A.m >> 2;
+    const float4 *Gw = reinterpret_cast<const float4 *>(A.gw);
+
+    float cM[CPT], cS[CPT];
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) { cM[c] = -INFINITY; cS[c] = 0.f; }
+
+    if (threadIdx.x == 0)
+        for (long long i = r0; i < min(r1, r0 + 4); ++i) prefetch_l2(A.C + i * A.m, (uint32_t)(A.m * 4));
+
+    for (long long i0 = r0; i0 < r1; i0 += 4) {
+        const int rows = (int)min(4LL, r1 - i0);
+        if (threadIdx.x == 0)
+            for (long long i = i0 + 4; i < min(r1, i0 + 8); ++i) prefetch_l2(A.C + i * A.m, (uint32_t)(A.m * 4));
+        // ---- phase A: row r = warp / 4, quarter q = warp % 4
+        {
+            const int r = warp >> 2, q = warp & 3;
+            float M = -INFINITY, S0 = 0.f, S1 = 0.f;
+            if (r < rows) {
+                const float4 *Cr = reinterpret_cast<const float4 *>(A.C + (i0 + r) * A.m);
+                const long long g0 = m4 * q / 4, g1 = m4 * (q + 1) / 4;
+                for (long long g = g0 + lane; g < g1; g += 32) {
+                    float4 c;
+                    asm volatile("ld.global.L2::256B.v4.f32 {%0,%1,%2,%3}, [%4];"
+                                 : "=f"(c.x), "=f"(c.y), "=f"(c.z), "=f"(c.w) : "l"(Cr + g));
+                    const float4 w = __ldg(Gw + g);
+                    const float t0 = fmaf(c.x, -kap, w.x), t1 = fmaf(c.y, -kap, w.y),
+                                t2 = fmaf(c.z, -kap, w.z), t3 = fmaf(c.w, -kap, w.w);
+                    const float cm = fmaxf(fmaxf(t0, t1), fmaxf(t2, t3));
+                    if (cm > M) { const float sc = ex2(M - cm); S0 *= sc; S1 *= sc; M = cm; }
+                    S0 += ex2(t0 - M) + ex2(t2 - M);
+                    S1 += ex2(t1 - M) + ex2(t3 - M);
+                }
+            }
+            float Sv = S0 + S1;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const float M2 = __shfl_xor_sync(0xffffffffu, M, o);
+                const float S2 = __shfl_xor_sync(0xffffffffu, Sv, o);
+                lse_merge(M, Sv, M2, S2);
+            }
+            if (lane == 0) red[warp] = make_float2(M, Sv);
+        }
+        __syncthreads();
+        if (threadIdx.x < rows) {
+            const int r = threadIdx.x;
+            float M = red[4 * r].x, Sv = red[4 * r].y;
+            for (int q = 1; q < 4; ++q) lse_merge(M, Sv, red[4 * r + q].x, red[4 * r + q].y);
+            const long long i = i0 + r;
+            const float fn = A.xc[i] - epsln2 * (M + log2f(Sv));
+            fnew[i] = fn;
+            const float wv = fn * kap;
+            A.xw[i] = wv;
+            wrow[r] = wv;
+        }
+        __syncthreads();
+        // ---- phase B: column state over the rows of this group (L2 re-read)
+#pragma unroll
+        for (int k = 0; k < CPT / 4; ++k) {
+            const long long g = threadIdx.x + (long long)k * kFT;
+            if (g < m4) {
+                float t[4][4];
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    const long long rr = r < rows ? r : 0;   // duplicate row 0 as padding, masked below
+                    const float4 c = *reinterpret_cast<const float4 *>(A.C + (i0 + rr) * A.m + 4 * g);
+                    const float w = r < rows ? wrow[r] : -INFINITY;
+                    t[0][r] = fmaf(c.x, -kap, w); t[1][r] = fmaf(c.y, -kap, w);
+                    t[2][r] = fmaf(c.z, -kap, w); t[3][r] = fmaf(c.w, -kap, w);
+                }
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const float cm = fmaxf(fmaxf(t[c][0], t[c][1]), fmaxf(t[c][2], t[c][3]));
+                    if (cm > cM[4 * k + c]) { cS[4 * k + c] *= ex2(cM[4 * k + c] - cm); cM[4 * k + c] = cm; }
+                    const float mm = cM[4 * k + c];
+                    cS[4 * k + c] += (ex2(t[c][0] - mm) + ex2(t[c][1] - mm)) + (ex2(t[c][2] - mm) + ex2(t[c][3] - mm));
+                }
+            }
+        }
+        __syncthreads();   // red / wrow reuse
+    }
+#pragma unroll
+    for (int k = 0; k < CPT / 4; ++k) {
+        const long long g = threadIdx.x + (long long)k * kFT;
+        if (g < m4) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+                A.part[(long long)s * A.m + 4 * g + c] = make_float2(cM[4 * k + c], cS[4 * k + c]);
+        }
+    }
+}
+
+bool stored_fused_supported(long long m) { return m % 4 == 0 && m <= (long long)kFT * 32; }
+
+cudaError_t launch_stored_fused(const FusedLaunch &L, cudaStream_t st) {
+    FusedArgs A;
+    A.C = L.C; A.n = L.n; A.m = L.m; A.eps = L.eps; A.gw = L.gw; A.xc = L.xc;
+    A.xpot[0] = L.xpot[0]; A.xpot[1] = L.xpot[1]; A.xw = L.xw; A.part = L.part;
+    A.blk_rows = L.blk_rows; A.split_q = L.split_q; A.st = L.st;
+    const int grid = L.nblk * L.split_q;
+    const long long cpt = (L.m / 4 + kFT - 1) / kFT * 4;
+    if (cpt <= 8) k_stored_fused<8><<<grid, kFT, 0, st>>>(A);
+    else if (cpt <= 16) k_stored_fused<16><<<grid, kFT, 0, st>>>(A);
+    else if (cpt <= 32) k_stored_fused<32><<<grid, kFT, 0, st>>>(A);
+    else return cudaErrorInvalidValue;
+    return cudaGetLastError();
+}
+
+}  // namespace sk
