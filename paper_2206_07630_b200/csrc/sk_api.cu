@@ -310,7 +310,13 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
     const int occ = stored ? 8 : (tc ? 1 : lse_occupancy_ctas(D));
     const int Rr = tc ? 1 : (D <= 4 ? 4 : (D <= 16 ? 2 : 1));
     const long long ptiles_col = stored ? (m + 511) / 512 : (m + 128LL * Rr - 1) / (128LL * Rr);
-    const int split_q = choose_split(ptiles_col, stored ? bs_rows / 64 : bs_rows / tq, occ, 64);
+    // stored mode with the fused sweep (one persistent CTA per SM): 8 blocks x split_q = one wave
+    static const int fused_env = [] { const char *e = getenv("SK_FUSED"); return e ? atoi(e) : 1; }();
+    const bool fused = stored && fused_env != 0 && stored_fused_supported(m);
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device);
+    const int split_q = fused ? std::max(1, nsm / SK_SHARD_BLOCKS)
+                              : choose_split(ptiles_col, stored ? bs_rows / 64 : bs_rows / tq, occ, 64);
     const int nsplit_col = (sharded ? SK_SHARD_BLOCKS : nblk_glob) * split_q;
     int split_row = 1;
     if (!stored) {
@@ -354,8 +360,6 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
                    sharded ? 1 : 0, 0};
 
     // stored mode: one HBM read of C per sweep (fused row + column passes, H4s) when m fits
-    static const int fused_env = [] { const char *e = getenv("SK_FUSED"); return e ? atoi(e) : 1; }();
-    const bool fused = stored && fused_env != 0 && stored_fused_supported(m);
     bool first = true;
 
     auto col_stage = [&]() -> sk_status {

@@ -232,10 +232,13 @@ __device__ __forceinline__ void prefetch_l2(const void *p, uint32_t bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
+constexpr int kFR = 2;                  // rows per group
+constexpr int kFWR = (kFT / 32) / kFR;  // warps per row in phase A (8)
+
 template <int CPT>
 __global__ void __launch_bounds__(kFT, 1) k_stored_fused(FusedArgs A) {
-    __shared__ float2 red[16];
-    __shared__ float wrow[4];
+    __shared__ float2 red[kFT / 32];
+    __shared__ float wrow[kFR];
     if (*(volatile const int *)&A.st->stop) return;
     const int l = A.st->iter;                      // producing f^{l+1}
     float *fnew = ((l + 1) & 1) ? A.xpot[1] : A.xpot[0];   // no dynamic param indexing
@@ -253,25 +256,44 @@ __global__ void __launch_bounds__(kFT, 1) k_stored_fused(FusedArgs A) {
 #pragma unroll
     for (int c = 0; c < CPT; ++c) { cM[c] = -INFINITY; cS[c] = 0.f; }
 
+    // L2 prefetch two groups ahead (the TMA engine streams HBM while the warps compute)
     if (threadIdx.x == 0)
-        for (long long i = r0; i < min(r1, r0 + 4); ++i) prefetch_l2(A.C + i * A.m, (uint32_t)(A.m * 4));
+        for (long long i = r0; i < min(r1, r0 + 2 * kFR); ++i) prefetch_l2(A.C + i * A.m, (uint32_t)(A.m * 4));
 
-    for (long long i0 = r0; i0 < r1; i0 += 4) {
-        const int rows = (int)min(4LL, r1 - i0);
+    for (long long i0 = r0; i0 < r1; i0 += kFR) {
+        const int rows = (int)min((long long)kFR, r1 - i0);
         if (threadIdx.x == 0)
-            for (long long i = i0 + 4; i < min(r1, i0 + 8); ++i) prefetch_l2(A.C + i * A.m, (uint32_t)(A.m * 4));
-        // ---- phase A: row r = warp / 4, quarter q = warp % 4
+            for (long long i = i0 + 2 * kFR; i < min(r1, i0 + 3 * kFR); ++i)
+                prefetch_l2(A.C + i * A.m, (uint32_t)(A.m * 4));
+        // ---- phase A: row r = warp / kFWR, segment q = warp % kFWR (exact online LSE)
         {
-            const int r = warp >> 2, q = warp & 3;
+            const int r = warp / kFWR, q = warp % kFWR;
             float M = -INFINITY, S0 = 0.f, S1 = 0.f;
             if (r < rows) {
                 const float4 *Cr = reinterpret_cast<const float4 *>(A.C + (i0 + r) * A.m);
-                const long long g0 = m4 * q / 4, g1 = m4 * (q + 1) / 4;
-                for (long long g = g0 + lane; g < g1; g += 32) {
-                    float4 c;
-                    asm volatile("ld.global.L2::256B.v4.f32 {%0,%1,%2,%3}, [%4];"
-                                 : "=f"(c.x), "=f"(c.y), "=f"(c.z), "=f"(c.w) : "l"(Cr + g));
-                    const float4 w = __ldg(Gw + g);
+                const long long g0 = m4 * q / kFWR, g1 = m4 * (q + 1) / kFWR;
+                long long g = g0 + lane;
+                for (; g + 96 < g1; g += 128) {
+                    float4 c[4], w[4];
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) c[v] = Cr[g + 32 * v];
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) w[v] = __ldg(Gw + g + 32 * v);
+                    float t[16];
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) {
+                        t[4 * v + 0] = fmaf(c[v].x, -kap, w[v].x); t[4 * v + 1] = fmaf(c[v].y, -kap, w[v].y);
+                        t[4 * v + 2] = fmaf(c[v].z, -kap, w[v].z); t[4 * v + 3] = fmaf(c[v].w, -kap, w[v].w);
+                    }
+                    float cm = t[0];
+#pragma unroll
+                    for (int v = 1; v < 16; ++v) cm = fmaxf(cm, t[v]);
+                    if (cm > M) { const float sc = ex2(M - cm); S0 *= sc; S1 *= sc; M = cm; }
+#pragma unroll
+                    for (int v = 0; v < 16; v += 2) { S0 += ex2(t[v] - M); S1 += ex2(t[v + 1] - M); }
+                }
+                for (; g < g1; g += 32) {
+                    const float4 c = Cr[g], w = __ldg(Gw + g);
                     const float t0 = fmaf(c.x, -kap, w.x), t1 = fmaf(c.y, -kap, w.y),
                                 t2 = fmaf(c.z, -kap, w.z), t3 = fmaf(c.w, -kap, w.w);
                     const float cm = fmaxf(fmaxf(t0, t1), fmaxf(t2, t3));
@@ -292,8 +314,8 @@ __global__ void __launch_bounds__(kFT, 1) k_stored_fused(FusedArgs A) {
         __syncthreads();
         if (threadIdx.x < rows) {
             const int r = threadIdx.x;
-            float M = red[4 * r].x, Sv = red[4 * r].y;
-            for (int q = 1; q < 4; ++q) lse_merge(M, Sv, red[4 * r + q].x, red[4 * r + q].y);
+            float M = red[kFWR * r].x, Sv = red[kFWR * r].y;
+            for (int q = 1; q < kFWR; ++q) lse_merge(M, Sv, red[kFWR * r + q].x, red[kFWR * r + q].y);
             const long long i = i0 + r;
             const float fn = A.xc[i] - epsln2 * (M + log2f(Sv));
             fnew[i] = fn;
@@ -302,26 +324,28 @@ __global__ void __launch_bounds__(kFT, 1) k_stored_fused(FusedArgs A) {
             wrow[r] = wv;
         }
         __syncthreads();
-        // ---- phase B: column state over the rows of this group (L2 re-read)
+        // ---- phase B: column state over the rows of this group (L2 / L1 re-read)
+        float wr[kFR];
+#pragma unroll
+        for (int r = 0; r < kFR; ++r) wr[r] = r < rows ? wrow[r] : -INFINITY;
 #pragma unroll
         for (int k = 0; k < CPT / 4; ++k) {
             const long long g = threadIdx.x + (long long)k * kFT;
             if (g < m4) {
-                float t[4][4];
+                float t[4][kFR];
 #pragma unroll
-                for (int r = 0; r < 4; ++r) {
-                    const long long rr = r < rows ? r : 0;   // duplicate row 0 as padding, masked below
+                for (int r = 0; r < kFR; ++r) {
+                    const long long rr = r < rows ? r : 0;   // duplicate row 0 as padding, masked by wr
                     const float4 c = *reinterpret_cast<const float4 *>(A.C + (i0 + rr) * A.m + 4 * g);
-                    const float w = r < rows ? wrow[r] : -INFINITY;
-                    t[0][r] = fmaf(c.x, -kap, w); t[1][r] = fmaf(c.y, -kap, w);
-                    t[2][r] = fmaf(c.z, -kap, w); t[3][r] = fmaf(c.w, -kap, w);
+                    t[0][r] = fmaf(c.x, -kap, wr[r]); t[1][r] = fmaf(c.y, -kap, wr[r]);
+                    t[2][r] = fmaf(c.z, -kap, wr[r]); t[3][r] = fmaf(c.w, -kap, wr[r]);
                 }
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
-                    const float cm = fmaxf(fmaxf(t[c][0], t[c][1]), fmaxf(t[c][2], t[c][3]));
+                    const float cm = fmaxf(t[c][0], t[c][1]);
                     if (cm > cM[4 * k + c]) { cS[4 * k + c] *= ex2(cM[4 * k + c] - cm); cM[4 * k + c] = cm; }
                     const float mm = cM[4 * k + c];
-                    cS[4 * k + c] += (ex2(t[c][0] - mm) + ex2(t[c][1] - mm)) + (ex2(t[c][2] - mm) + ex2(t[c][3] - mm));
+                    cS[4 * k + c] += ex2(t[c][0] - mm) + ex2(t[c][1] - mm);
                 }
             }
         }

@@ -80,3 +80,50 @@ def test_subsample_init(O, ctx, n, ns):
     lock = O.sinkhorn(w, z, p.eps, tol=0, max_iter=inner["iterations"])
     ref = O.subsample_extrapolate(p.x, z, lock.g, p.eps)
     assert rel_inf(centred(pot.cpu().numpy()), centred(ref), p.eps) <= INIT_RTOL
+
+
+def test_initializer_argument_errors(ctx):
+    import paper_2206_07630_b200 as sk
+    x = _cuda(np.random.default_rng(0).random((10, 2)).astype(np.float32))
+    y = _cuda(np.random.default_rng(1).random((12, 2)).astype(np.float32))
+    # sort1d needs n == m (general NW + Alg. 3 is a later row) -> SK_EUNSUPPORTED
+    with pytest.raises(sk.SinkhornError) as e:
+        sk.sinkhorn_init_sort1d(ctx, x[:, :1].contiguous().view(1, 10), y[:, 0].contiguous(), y_shared=True)
+    assert e.value.status == 6
+    # subsample: repeated / out-of-range indices -> SK_EINVAL
+    ix = _cuda(np.array([0, 1, 1], np.int32))
+    iy = _cuda(np.array([0, 2, 3], np.int32))
+    with pytest.raises(sk.SinkhornError) as e:
+        sk.sinkhorn_init_subsample(ctx, x, y, ix, iy, 0.1, 1e-3)
+    assert e.value.status == 1
+    with pytest.raises(sk.SinkhornError):
+        sk.sinkhorn_init_subsample(ctx, x, y, _cuda(np.array([0, 10], np.int32)), iy, 0.1, 1e-3)
+    # GMM: a non-SPD covariance -> SK_EINVAL; zero mixture weight -> SK_EINVAL
+    g_bad = {"weights": _cuda(np.ones(1, np.float32)), "means": _cuda(np.zeros((1, 2), np.float32)),
+             "covs": _cuda(np.array([[[1.0, 2.0], [2.0, 1.0]]], np.float32))}
+    g_ok = {"weights": _cuda(np.ones(1, np.float32)), "means": _cuda(np.zeros((1, 2), np.float32)),
+            "covs": _cuda(np.eye(2, dtype=np.float32)[None])}
+    with pytest.raises(sk.SinkhornError):
+        sk.sinkhorn_init_gmm(ctx, x, y, g_bad, g_ok, 0.5)
+    g_zero = dict(g_ok, weights=_cuda(np.zeros(1, np.float32)))
+    with pytest.raises(sk.SinkhornError) as e:
+        sk.sinkhorn_init_gmm(ctx, x, y, g_zero, g_ok, 0.5)
+    assert e.value.status == 1
+    # Gaussian: NaN input -> SK_EINVAL
+    xn = x.clone()
+    xn[3, 0] = float("nan")
+    with pytest.raises(sk.SinkhornError) as e:
+        sk.sinkhorn_init_gaussian(ctx, xn, y)
+    assert e.value.status == 1
+
+
+def test_gaussian_side_swap_matches_oracle(O, ctx):
+    """n > m: the potential lives on y and equals the oracle's swapped evaluation."""
+    import paper_2206_07630_b200 as sk
+    rng = np.random.default_rng(9)
+    x = rng.standard_normal((900, 3)).astype(np.float32)
+    y = (rng.standard_normal((400, 3)) * 1.3 + 0.2).astype(np.float32)
+    pot, side = sk.sinkhorn_init_gaussian(ctx, _cuda(x), _cuda(y))
+    ref, so = O.init_gaussian(x, y)
+    assert side == so == 1 and pot.numel() == 400
+    assert rel_inf(centred(pot.cpu().numpy()), centred(ref), 0.01) <= INIT_RTOL
