@@ -76,7 +76,7 @@ enum BufId {
     B_STAGE0 = 0, B_STAGE_END = 16,   // staging of host arrays
     B_FLAG = 16, B_XPACK, B_XC, B_XNK, B_XPOT, B_YPACK, B_YC, B_YNK, B_YPOT, B_PART, B_BLKE, B_BLKB,
     B_STATUS, B_COST, B_REP, B_SORT, B_PERM, B_YSORT, B_GAUSS, B_GAUSS2, B_GMM, B_SUBW, B_SUBZ,
-    B_SUBF, B_SUBG, B_IDX, B_OUT, B_FA, B_QUEUE, B_XIMG, B_YIMG, B_NBUF
+    B_SUBF, B_SUBG, B_IDX, B_OUT, B_FA, B_QUEUE, B_XIMG, B_YIMG, B_XLSE, B_YLSE, B_NBUF
 };
 
 sk_status fail(sk_ctx *c, sk_status s, const char *fmt, ...) {
@@ -300,6 +300,17 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
                     {xpot + 2 * off[i], xpot + 2 * off[i] + n}};
     }
     Side Y{(int)m, P.d, D, tq, ypack, yc, ynk, {ypot, ypot + m}};
+    // online FFMA path: per-point LSE seeds for the max-free (seeded) passes from sweep 3 on
+    const bool seedable = !stored && !tc;
+    if (seedable) {
+        ENSURE(xlse, float, B_XLSE, off[ns]);
+        ENSURE(ylse, float, B_YLSE, m);
+        for (int i = 0; i < ns; ++i) X[i].lse = xlse + off[i];
+        Y.lse = ylse;
+    }
+    static const int seed_env = [] { const char *e = getenv("SK_SEEDED"); return e ? atoi(e) : 1; }();
+    const bool col_seed = seedable && seed_env && !sharded && ns == 1;   // exact fallback needs all rows
+    const bool row_seed = seedable && seed_env;
 
     // column-pass partition (a function of n_total, m, d only): SK_SHARD_BLOCKS fixed row
     // blocks, each cut into split_q sub-splits sized for the 8-rank launch; empty blocks
@@ -358,6 +369,8 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
     auto col_part = [&](int i) { return part + (sharded ? (long long)slices[i].rank * slot : 0); };
     MergePass mcol{MERGE_COL, &Y, part, nsplit_col, P.eps, P.b, status, blke, blkb, nullptr, 0.f,
                    sharded ? 1 : 0, 0};
+    if (col_seed) mcol.Q = &X[0];
+    int sweep = 0;   // sweeps enqueued so far (seeded passes from the third on)
 
     // stored mode: one HBM read of C per sweep (fused row + column passes, H4s) when m fits
     bool first = true;
@@ -376,6 +389,7 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
             } else {
                 LsePass colp{&Y, &X[i], sharded ? blk_per_rank : nblk_glob, (int)(bs_rows / tq), split_q,
                              col_part(i), P.eps, &status->stop};
+                colp.seeded = col_seed && sweep >= 2;
                 CU(launch_lse(colp, st));
             }
         }
@@ -430,14 +444,17 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
                     CU(launch_lse_tc(rowp, st));
                 } else {
                     LsePass rowp{&X[i], &Y, 1, 0, split_row, part, P.eps, &status->stop};
+                    rowp.seeded = row_seed && sweep >= 2;
                     CU(launch_lse(rowp, st));
                 }
                 // only the last slice's merge advances the sweep counter
                 MergePass mrow{MERGE_ROW, &X[i], part, stored ? 1 : split_row, P.eps, nullptr, status, blke,
                                blkb, nullptr, 0.f, sharded ? 1 : 0, i + 1 < ns ? 1 : 0};
+                if (row_seed) mrow.Q = &Y;
                 CU(launch_merge(mrow, st));
                 launched += 2;
             }
+            ++sweep;
         }
         CU(cudaMemcpyAsync(ctx->h_status, status, sizeof(DevStatus), cudaMemcpyDeviceToHost, st));
         CU(cudaStreamSynchronize(st));

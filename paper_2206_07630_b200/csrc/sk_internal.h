@@ -54,6 +54,7 @@ struct Side {
     float *c;         // [P] eps log w_p + |p|^2 (finalize constant)
     float *nk;        // [P] |p|^2 log2(e)/eps
     float *pot[2];    // double-buffered potential
+    float *lse;       // [P] last merged LSE (log2 units): the seed of the next pass (nullable)
 };
 
 // Pack points (P x d, fp32 row-major), optional weights and initial potential.
@@ -91,6 +92,7 @@ struct LsePass {
     float2 *part;
     float eps;
     const int *stop;  // device flag (nullable)
+    int seeded = 0;   // fixed shift = Pside->lse[p] + margin (no running max); see k_merge
 };
 cudaError_t launch_lse(const LsePass &L, cudaStream_t st);
 int lse_occupancy_ctas(int D);  // resident CTAs per SM of the LSE kernel for D
@@ -111,6 +113,7 @@ struct MergePass {
     int sharded;              // non-finite f is detected by the next (replicated) column merge
     int no_iter_inc;          // MERGE_ROW of a non-final slice (emulated ranks): keep the counter
     int precomputed = 0;      // MERGE_ROW: potential and w already written (fused stored sweep)
+    const Side *Q = nullptr;  // seeded passes: the reduced side, for the exact fallback
 };
 cudaError_t launch_merge(const MergePass &M, cudaStream_t st);
 int merge_blocks(int P);

@@ -24,6 +24,7 @@ namespace sk {
 constexpr int kLT = 128;      // LSE kernel threads
 constexpr int kStages = 4;    // bulk-copy ring depth
 constexpr int kLseEmu = 1;    // exp2 pairs (of 4 per chunk) on the FMA pipe when D <= 4
+constexpr int kLseEmuSeeded = 1;
 
 int lse_dpad(int d) {
     if (d <= 4) return d < 1 ? 0 : d;
@@ -63,6 +64,7 @@ __global__ void k_pack_side(Side S, const float *__restrict__ pts, const float *
             S.nk[p] = s * kap;
             const float h = pot0 ? pot0[p] : 0.f;
             S.pot[0][p] = h;
+            if (S.lse) S.lse[p] = -INFINITY;
             tile[S.D * S.tq + o] = fmaf(h, kap, -s * kap);
         } else {
             for (int k = 0; k < S.D; ++k) tile[k * S.tq + o] = 0.f;
@@ -89,9 +91,12 @@ struct LseArgs {
     float2 *part;
     float tk;
     const int *stop;
+    const float *seed;      // SEEDED: P side last LSE
 };
 
-template <int D, int R>
+constexpr float kSeedMarginMK = 4.f;  // log2 units above the previous LSE
+
+template <int D, int R, bool SEEDED>
 __global__ void __launch_bounds__(kLT) k_lse(LseArgs A) {
     constexpr int TQ = D <= 4 ? 256 : (D <= 16 ? 128 : 64);
     constexpr int TF = (D + 1) * TQ;  // floats per tile
@@ -123,7 +128,7 @@ __global__ void __launch_bounds__(kLT) k_lse(LseArgs A) {
             const float v = p < A.P ? tile[k * A.Ptq + po] * A.tk : 0.f;
             pd[r][k] = make_float2(v, v);
         }
-        M[r] = -INFINITY;
+        M[r] = (SEEDED && p < A.P) ? A.seed[p] + kSeedMarginMK : -INFINITY;
         Sx[r] = make_float2(0.f, 0.f);
     }
 
@@ -142,7 +147,11 @@ __global__ void __launch_bounds__(kLT) k_lse(LseArgs A) {
         mbar_wait(&full[st], (i / kStages) & 1);
         const float *qt = ring + st * TF;
 #pragma unroll 2
-        for (int q = 0; q < TQ; q += kChunk) lse_chunk<D, R, (D <= 4 ? kLseEmu : 0)>(qt, TQ, qt + D * TQ, q, pd, M, Sx);
+        if (SEEDED) {
+            for (int q = 0; q < TQ; q += kChunk) lse_chunk_seeded<D, R, (D <= 4 ? kLseEmuSeeded : 0)>(qt, TQ, qt + D * TQ, q, pd, M, Sx);
+        } else {
+            for (int q = 0; q < TQ; q += kChunk) lse_chunk<D, R, (D <= 4 ? kLseEmu : 0)>(qt, TQ, qt + D * TQ, q, pd, M, Sx);
+        }
         __syncthreads();  // everyone is done with stage st
         if (threadIdx.x == 0 && i + kStages < nt) {
             fence_proxy_async();
@@ -163,8 +172,10 @@ static cudaError_t launch_lse_d(const LsePass &L, cudaStream_t st) {
     constexpr int R = kR<D>;
     constexpr int TQ = D <= 4 ? 256 : (D <= 16 ? 128 : 64);
     const size_t smem = (size_t)kStages * (D + 1) * TQ * sizeof(float);
-    cudaError_t e = cudaFuncSetAttribute(k_lse<D, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(k_lse<D, R, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k_lse<D, R, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     LseArgs A;
     A.Ppack = L.Pside->pack; A.P = L.Pside->P; A.Ptq = L.Pside->tq;
@@ -173,8 +184,10 @@ static cudaError_t launch_lse_d(const LsePass &L, cudaStream_t st) {
     A.part = L.part;
     A.tk = 2.f * kLog2e / L.eps;
     A.stop = L.stop;
+    A.seed = L.Pside->lse;
     dim3 grid((A.P + kLT * R - 1) / (kLT * R), L.nblk * L.split_q);
-    k_lse<D, R><<<grid, kLT, smem, st>>>(A);
+    if (L.seeded && A.seed) k_lse<D, R, true><<<grid, kLT, smem, st>>>(A);
+    else k_lse<D, R, false><<<grid, kLT, smem, st>>>(A);
     return cudaGetLastError();
 }
 
@@ -197,9 +210,9 @@ static int occ_d() {
     constexpr int R = kR<D>;
     constexpr int TQ = D <= 4 ? 256 : (D <= 16 ? 128 : 64);
     const size_t smem = (size_t)kStages * (D + 1) * TQ * sizeof(float);
-    cudaFuncSetAttribute(k_lse<D, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_lse<D, R, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int n = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_lse<D, R>, kLT, smem) != cudaSuccess) n = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_lse<D, R, false>, kLT, smem) != cudaSuccess) n = 1;
     return n > 0 ? n : 1;
 }
 
@@ -222,6 +235,29 @@ constexpr int kMT = 256;
 int merge_blocks(int P) {
     int b = (P + kMT - 1) / kMT;
     return b < 1 ? 1 : (b > 1184 ? 1184 : b);
+}
+
+// Exact (online max) LSE of output point p of side S over every point of side Q, from the
+// packed tiles (coordinates + w): the fallback of a seeded pass.
+__device__ void exact_lse_point(const Side &S, const Side &Q, int p, float eps, float &M, float &Ssum) {
+    const float tk = 2.f * kLog2e / eps;
+    const long long pt = p / S.tq, po = p % S.tq;
+    const float *ptile = S.pack + pt * (long long)(S.D + 1) * S.tq;
+    float pc[64];
+    for (int k = 0; k < S.D; ++k) pc[k] = ptile[k * S.tq + po] * tk;
+    M = -INFINITY;
+    Ssum = 0.f;
+    const long long qt = lse_tiles(Q.P, Q.tq);
+    for (long long t = 0; t < qt; ++t) {
+        const float *tile = Q.pack + t * (long long)(Q.D + 1) * Q.tq;
+        for (int o = 0; o < Q.tq; ++o) {
+            float v = tile[Q.D * Q.tq + o];
+            if (v == -INFINITY) continue;
+            for (int k = 0; k < Q.D; ++k) v = fmaf(pc[k], tile[k * Q.tq + o], v);
+            if (v > M) { Ssum = Ssum * ex2(M - v); M = v; }
+            Ssum += ex2(v - M);
+        }
+    }
 }
 
 __global__ void __launch_bounds__(kMT) k_merge(MergePass Mp, Side S) {
@@ -250,7 +286,13 @@ __global__ void __launch_bounds__(kMT) k_merge(MergePass Mp, Side S) {
             const float2 v = Mp.part[(long long)s * S.P + p];
             if (v.x != -INFINITY) Ssum += v.y * ex2(v.x - M);
         }
+        if (Mp.Q && !(Ssum >= 0x1p-100f && Ssum <= 0x1p100f)) {
+            // seeded pass: the fixed shift was far from the true maximum -> exact recompute of
+            // this point over the whole reduced side (rare; one thread, online max)
+            exact_lse_point(S, *Mp.Q, p, eps, M, Ssum);
+        }
         const float lse2 = M + log2f(Ssum);
+        if (S.lse) S.lse[p] = lse2;
         if (Mp.mode == MERGE_OUT) {
             const float v = Mp.out_const + (S.c[p] - epsln2 * lse2);
             Mp.out[p] = v;
