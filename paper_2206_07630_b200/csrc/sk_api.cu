@@ -242,6 +242,7 @@ struct Problem {
     float *g;               // device output (m)
     int world;              // ranks of the partition (1 = unsharded)
     bool nccl;              // partials exchanged with ncclAllGather (one local slice)
+    bool partitioned = false;  // sharded entries: results must not depend on the world size
 };
 
 sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, sk_report *rep) {
@@ -309,7 +310,8 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
         Y.lse = ylse;
     }
     static const int seed_env = [] { const char *e = getenv("SK_SEEDED"); return e ? atoi(e) : 1; }();
-    const bool col_seed = seedable && seed_env && !sharded && ns == 1;   // exact fallback needs all rows
+    // the column pass's exact fallback needs all rows: seeded only in the unsharded entry
+    const bool col_seed = seedable && seed_env && !P.partitioned && !sharded && ns == 1;
     const bool row_seed = seedable && seed_env;
 
     // column-pass partition (a function of n_total, m, d only): SK_SHARD_BLOCKS fixed row
@@ -462,33 +464,33 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
         poll = std::min(poll * 2, 64);
     }
     CU(cudaEventRecord(ctx->ev1, st));
-    // E = sum over slices (rank order) of <f,a> - eps sum(a), plus <g,b> (replicated)
-    std::vector<double> fa_parts;
-    double gb_part = 0.0;
+    // E = <f,a> - eps sum(a) summed per fixed row block (bit-identical for every partition of the
+    // rows), plus <g,b> (replicated)
+    ENSURE(fa, double, B_FA, SK_SHARD_BLOCKS + 1);
+    CU(cudaMemsetAsync(fa, 0, sizeof(double) * (SK_SHARD_BLOCKS + 1), st));
     for (int i = 0; i < ns; ++i) {
-        CU(launch_report(X[i], Y, slices[i].a, P.b, P.eps, status, 1, n_glob, st));
-        CU(cudaMemcpyAsync(ctx->h_status, status, sizeof(DevStatus), cudaMemcpyDeviceToHost, st));
-        CU(cudaStreamSynchronize(st));
-        fa_parts.push_back(ctx->h_status->fa_local);
-        gb_part = ctx->h_status->E;
+        CU(launch_report_blocks(X[i], slices[i].a, P.eps, status, n_glob, slices[i].row0, bs_rows, fa, st));
         launched++;
     }
+    CU(launch_report(X[0], Y, slices[0].a, P.b, P.eps, status, 1, n_glob, st));   // <g,b> into status->E
+    launched++;
+    if (P.nccl && sharded) {  // every rank's blocks: allgather its slots of the 8-block array
+        int r = g_nccl.allgather(fa + (long long)slices[0].rank * blk_per_rank, fa, (size_t)blk_per_rank,
+                                 kNcclFloat64, ctx->comm, st);
+        if (r != 0) return fail(ctx, SK_ENCCL, "ncclAllGather(E) failed");
+    }
+    std::vector<double> fa_h(SK_SHARD_BLOCKS + 1, 0.0);
+    CU(cudaMemcpyAsync(fa_h.data(), fa, sizeof(double) * (SK_SHARD_BLOCKS + 1), cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(ctx->h_status, status, sizeof(DevStatus), cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    const double gb_part = ctx->h_status->E;
     float ms = 0.f;
     CU(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
     DevStatus hs = *ctx->h_status;
     if (!hs.stop) return fail(ctx, SK_ECUDA, "solver loop ended without a stop flag");
     const int L = hs.final_iter;
-    if (P.nccl && sharded) {  // gather every rank's <f,a> partial, sum in rank order
-        ENSURE(fa, double, B_FA, P.world);
-        CU(cudaMemcpyAsync(fa + slices[0].rank, &status->fa_local, sizeof(double), cudaMemcpyDeviceToDevice, st));
-        int r = g_nccl.allgather(fa + slices[0].rank, fa, 1, kNcclFloat64, ctx->comm, st);
-        if (r != 0) return fail(ctx, SK_ENCCL, "ncclAllGather(E) failed");
-        fa_parts.assign(P.world, 0.0);
-        CU(cudaMemcpyAsync(fa_parts.data(), fa, sizeof(double) * P.world, cudaMemcpyDeviceToHost, st));
-        CU(cudaStreamSynchronize(st));
-    }
     double E = 0.0;
-    for (double v : fa_parts) E += v;
+    for (int b = 0; b < SK_SHARD_BLOCKS; ++b) E += fa_h[b];
     E += gb_part;
     for (int i = 0; i < ns; ++i)
         CU(cudaMemcpyAsync(slices[i].f, X[i].pot[L & 1], sizeof(float) * slices[i].n, cudaMemcpyDeviceToDevice, st));
@@ -1009,7 +1011,7 @@ sk_status sinkhorn_solve_sharded(sk_ctx *ctx, int64_t n_total, int64_t row0, int
     P.y = dy; P.b = db;
     P.eps = eps; P.tol = tol; P.max_iter = max_iter; P.check_every = check_every; P.mode = mode;
     P.g = dg;
-    P.world = ctx->world; P.nccl = ctx->world > 1;
+    P.world = ctx->world; P.nccl = ctx->world > 1; P.partitioned = true;
     std::vector<Slice> sl{Slice{row0, n_local, dx, da, dfi, df, ctx->rank}};
     sk_status s = solve_core(ctx, P, sl, rep);
     if (s != SK_OK && s != SK_ENONFINITE) return s;
@@ -1045,7 +1047,7 @@ sk_status sinkhorn_solve_sharded_emulated(sk_ctx *ctx, int32_t world, int64_t n,
     P.y = dy; P.b = db;
     P.eps = eps; P.tol = tol; P.max_iter = max_iter; P.check_every = check_every; P.mode = mode;
     P.g = dg;
-    P.world = world; P.nccl = false;
+    P.world = world; P.nccl = false; P.partitioned = true;
     std::vector<Slice> sl;
     for (int r = 0; r < world; ++r) {
         int64_t r0, nl;

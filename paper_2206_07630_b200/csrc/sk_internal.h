@@ -124,6 +124,8 @@ cudaError_t launch_report(const Side &X, const Side &Y, const float *a, const fl
 
 cudaError_t launch_status_init(DevStatus *st, int max_iter, int check_every, float tol,
                                cudaStream_t s);
+cudaError_t launch_report_blocks(const Side &X, const float *a, float eps, DevStatus *st, long long n_uniform,
+                                 long long row0, long long bs, double *out, cudaStream_t s);
 
 // ------------------------------------------------------------ misc kernels
 cudaError_t launch_fill(float *p, long long n, float v, cudaStream_t st);

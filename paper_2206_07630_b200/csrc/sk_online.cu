@@ -397,6 +397,33 @@ __global__ void k_status_init(DevStatus *st, int max_iter, int check_every, floa
     *st = z;
 }
 
+// <f,a> - eps sum(a) per fixed row block (partition-invariant): block b of the global
+// partition covers rows [b*bs, (b+1)*bs); this slice holds rows [row0, row0 + X.P).  CTA k
+// reduces global block (row0 / bs + k) in a fixed order and writes out[block].
+__global__ void __launch_bounds__(1024) k_report_blocks(Side X, const float *a, float eps, DevStatus *st,
+                                                         long long n_uniform, long long row0, long long bs,
+                                                         double *out) {
+    __shared__ double red[32];
+    const int l = st->final_iter;
+    const float *f = (l & 1) ? X.pot[1] : X.pot[0];
+    const long long b = row0 / bs + blockIdx.x;
+    const long long lo = max(b * bs, row0) - row0, hi = min((b + 1) * bs, row0 + (long long)X.P) - row0;
+    double s = 0.0;
+    for (long long i = lo + threadIdx.x; i < hi; i += 1024) {
+        const double ai = a ? (double)a[i] : 1.0 / n_uniform;
+        s += (double)f[i] * ai - (double)eps * ai;
+    }
+    const double tot = block_sum_d<1024>(s, red);
+    if (threadIdx.x == 0) out[b] = tot;
+}
+
+cudaError_t launch_report_blocks(const Side &X, const float *a, float eps, DevStatus *st, long long n_uniform,
+                                 long long row0, long long bs, double *out, cudaStream_t s) {
+    const long long b0 = row0 / bs, b1 = (row0 + X.P - 1) / bs;
+    k_report_blocks<<<(unsigned)(b1 - b0 + 1), 1024, 0, s>>>(X, a, eps, st, n_uniform, row0, bs, out);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_status_init(DevStatus *st, int max_iter, int check_every, float tol,
                                cudaStream_t s) {
     k_status_init<<<1, 1, 0, s>>>(st, max_iter, check_every, tol);

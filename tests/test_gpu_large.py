@@ -62,11 +62,15 @@ def test_sharded_bit_identical_across_world_sizes(O, ctx, mode, n, m, d):
         f, g, r = outs[W]
         assert torch.equal(f, f1) and torch.equal(g, g1), W
         assert r["iterations"] == r1["iterations"] and r["dual_objective"] == r1["dual_objective"]
-    # the unsharded path and the real sharded entry at world = 1 use the same partition
-    fu, gu, ru = sk.sinkhorn_solve(ctx, xd, yd, eps, a=ad, mode=mode)
-    assert torch.equal(fu, f1) and torch.equal(gu, g1)
+    # the real sharded entry at world = 1 runs the same partition: bit-identical
     fs, gs, rs = sk.sinkhorn_solve_sharded(ctx, n, 0, xd, yd, eps, a_local=ad, mode=mode)
-    assert torch.equal(fs, f1) and torch.equal(gs, g1)
+    assert torch.equal(fs, f1) and torch.equal(gs, g1) and rs["dual_objective"] == r1["dual_objective"]
+    # the unsharded entry may also seed its column pass (needs all rows for the exact fallback):
+    # same iterate up to fp32 rounding
+    fu, gu, ru = sk.sinkhorn_solve(ctx, xd, yd, eps, a=ad, mode=mode)
+    assert abs(ru["iterations"] - r1["iterations"]) <= 1
+    if ru["iterations"] == r1["iterations"]:
+        assert_pair_close(fu.cpu().numpy(), gu.cpu().numpy(), f1.cpu().numpy(), g1.cpu().numpy(), eps, rtol=1e-5)
     # and the oracle (unsharded, fp64)
     L = r1["iterations"]
     ref = O.sinkhorn(x, y, eps, a=a)
