@@ -298,34 +298,54 @@ def make_workload(args, sk, ctx, dev, rank, world):
     return C2(sk, ctx, dev, rank, world, args) if args.workload == "c2" else Single(sk, ctx, dev, rank, world, args)
 
 
-def roofline(w, cnt, steps, pk, src):
+def roofline(w, cnt, steps, pk, src, step_ms):
+    """Roofline of the dominant kernel: ALGORITHMIC units per launch / its average launch
+    duration, both from the library's per-launch CUDA events on the launching stream
+    (sk_counters.dom_*: launches that returned at entry after the stop flag are excluded)."""
     sm_max = float(pk.get("sm_max_mhz", 1965.0))
-    ms = cnt["lse_ms"] / max(steps, 1)
+    nl = max(int(cnt["dom_launches"]), 1)
+    dom_s = cnt["dom_ms"] / 1e3
+    common = {"kernel": w.kernel, "launches": int(cnt["dom_launches"]),
+              "avg_launch_ms": cnt["dom_ms"] / nl,
+              "share_of_step": (cnt["dom_ms"] / max(steps, 1)) / step_ms if step_ms > 0 else None,
+              "traffic": traffic_from_profile(w)}
     if w.roof == "hbm":
-        achieved = cnt["lse_bytes"] / (cnt["lse_ms"] / 1e3) / 1e9 if cnt["lse_ms"] > 0 else 0.0
+        achieved = cnt["dom_bytes"] / dom_s / 1e9 if dom_s > 0 else 0.0
         peak = float(pk["hbm_gbs"])
-        return {"bound": "hbm", "kernel": w.kernel, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": None,
+        return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({src})",
-                "algorithmic": "4 bytes (one fp32 C_ij read) per cost entry per pass",
-                "kernel_ms_per_step": ms}
+                "algorithmic": "4 bytes (one fp32 C_ij read) per cost entry per launch; the fused sweep reads C "
+                               "once for a row pass and the next column pass",
+                "bytes_per_launch": cnt["dom_bytes"] / nl, **common}
     if w.roof == "tensor":
-        flops = cnt["lse_ex2"] * 3 * 2 * 64          # 3 TF32 MMAs (hi.hi, hi.lo, lo.hi), K = 64
-        achieved = flops / (cnt["lse_ms"] / 1e3) / 1e12 if cnt["lse_ms"] > 0 else 0.0
+        flops = cnt["dom_entries"] * 3 * 2 * 64          # 3 TF32 MMAs (hi.hi, hi.lo, lo.hi), K = 64
+        achieved = flops / dom_s / 1e12 if dom_s > 0 else 0.0
         peak = float(pk["bf16_tflops"]) * 1.1 / 2.25   # TF32 = measured BF16 x nominal TF32/BF16 ratio
-        return {"bound": "tensor", "kernel": w.kernel, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                "frac": achieved / peak, "traffic": None,
+        ex2_peak = N_SM * MUFU_EX2_PER_CLK_SM * sm_max * 1e6
+        return {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                 "peak_source": f"MEASURED_PEAKS.json bf16_tflops x 1.1/2.25 (nominal TF32/BF16), {src}",
                 "algorithmic": "3 x 2 x 64 TF32 flops per cost entry per pass (3xTF32 split)",
-                "kernel_ms_per_step": ms}
-    achieved = cnt["lse_ex2"] / (cnt["lse_ms"] / 1e3) if cnt["lse_ms"] > 0 else 0.0
+                "flops_per_launch": flops / nl,
+                "mufu_frac": (cnt["dom_entries"] / dom_s) / ex2_peak if dom_s > 0 else 0.0, **common}
+    achieved = cnt["dom_entries"] / dom_s if dom_s > 0 else 0.0
     peak = N_SM * MUFU_EX2_PER_CLK_SM * sm_max * 1e6
-    return {"bound": "alu", "pipe": "MUFU.EX2 (SFU)", "kernel": w.kernel, "achieved": achieved / 1e9,
-            "peak": peak / 1e9, "unit": "Gex2/s", "frac": achieved / peak, "traffic": None,
+    return {"bound": "alu", "pipe": "MUFU.EX2 (SFU)", "achieved": achieved / 1e9,
+            "peak": peak / 1e9, "unit": "Gex2/s", "frac": achieved / peak,
             "peak_source": f"derived: {N_SM} SM x {MUFU_EX2_PER_CLK_SM} ex2/clk x {sm_max:.0f} MHz "
                            f"(sm_max_mhz from MEASURED_PEAKS.json, {src})",
             "algorithmic": "one exp2 per cost entry per pass; 2 passes per sweep (+1 column pass for err_L)",
-            "kernel_ms_per_step": ms}
+            "ex2_per_launch": cnt["dom_entries"] / nl, **common}
+
+
+def traffic_from_profile(w):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant kernel from the
+    committed `ncu --set full` capture (profiles/traffic.json, written by tools/ncu_summary.py)."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        t = json.load(open(p)).get(w.name)
+        return t
+    except Exception:
+        return None
 
 
 # ==================================================================== reference arm
@@ -460,7 +480,7 @@ def run_ours(args):
             "config": w.config(),
             "time_to_tol_ms": {"init": ms / args.steps, "zero_init": zero["time_to_tol_ms"]},
             "solve": extra, "zero_init": zero,
-            "roofline": roofline(w, cnt, args.steps, pk, src),
+            "roofline": roofline(w, cnt, args.steps, pk, src, ms_all / args.steps),
             "gpu_launches": int(cnt["kernel_launches"]),
             "clocks": clk.summary(),
             "k14_measured_peaks": k14,

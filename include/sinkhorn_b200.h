@@ -87,6 +87,14 @@ typedef struct {
     double lse_ex2;            /* algorithmic exp2 evaluations of those launches (2 per cost entry
                                   per sweep, counted from the iteration counts) */
     double lse_bytes;          /* algorithmic HBM bytes of those launches (stored mode: 4 per entry) */
+    /* Per-launch timing of the dominant kernel alone (CUDA events recorded around each launch
+       on the context stream while timing is enabled; launches that returned at entry because
+       the solve had already stopped are excluded): */
+    int64_t dom_launches;      /* launches of the dominant kernel that did work */
+    double dom_ms;             /* sum of their durations */
+    double dom_entries;        /* cost entries they processed (n*m per pass; the fused stored sweep
+                                  processes 2 passes per launch) */
+    double dom_bytes;          /* algorithmic HBM bytes they read (stored mode: 4 per entry read) */
 } sk_counters;
 
 /* ---------------------------------------------------------------- context -- */

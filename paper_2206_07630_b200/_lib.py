@@ -29,7 +29,9 @@ class SkReport(ctypes.Structure):
 class SkCounters(ctypes.Structure):
     _fields_ = [("kernel_launches", ctypes.c_int64), ("lse_launches", ctypes.c_int64),
                 ("lse_ms", ctypes.c_double), ("lse_ex2", ctypes.c_double),
-                ("lse_bytes", ctypes.c_double)]
+                ("lse_bytes", ctypes.c_double), ("dom_launches", ctypes.c_int64),
+                ("dom_ms", ctypes.c_double), ("dom_entries", ctypes.c_double),
+                ("dom_bytes", ctypes.c_double)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -69,6 +69,7 @@ struct sk_ctx {
     int *h_flag = nullptr;  // pinned host scratch
     DevStatus *h_status = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    std::vector<cudaEvent_t> tev;   // per-launch timing events of the dominant kernel (pool)
 };
 
 namespace {
@@ -245,8 +246,58 @@ struct Problem {
     bool partitioned = false;  // sharded entries: results must not depend on the world size
 };
 
+// Per-launch CUDA-event timing of the dominant kernel (only while ctx->timing is set).  Each
+// launch is tagged with its sweep and kind so that launches that returned at entry (enqueued
+// ahead of the host poll, after the stop flag was set) are excluded once L is known.
+struct LaunchTimer {
+    enum Kind { COL = 0, ROW = 1, FUSED = 2 };
+    struct Rec { int a, b, sweep, kind; double entries, bytes; };
+    sk_ctx *ctx;
+    bool on;
+    std::vector<Rec> recs;
+    int next = 0;
+    LaunchTimer(sk_ctx *c) : ctx(c), on(c->timing != 0) {}
+    int ev() {
+        if (next >= (int)ctx->tev.size()) {
+            cudaEvent_t e;
+            if (cudaEventCreate(&e) != cudaSuccess) { cudaGetLastError(); return -1; }
+            ctx->tev.push_back(e);
+        }
+        return next++;
+    }
+    int start() {
+        if (!on) return -1;
+        const int a = ev();
+        if (a >= 0) cudaEventRecord(ctx->tev[a], ctx->stream);
+        return a;
+    }
+    void stop(int a, int sweep, int kind, double entries, double bytes) {
+        if (!on || a < 0) return;
+        const int b = ev();
+        if (b < 0) return;
+        cudaEventRecord(ctx->tev[b], ctx->stream);
+        recs.push_back({a, b, sweep, kind, entries, bytes});
+    }
+    // after the stream has been synchronised; L = sweeps of the solve
+    void collect(int L) {
+        for (const Rec &r : recs) {
+            const bool ran = r.kind == COL ? r.sweep <= L : r.sweep < L;
+            if (!ran) continue;
+            float ms = 0.f;
+            if (cudaEventElapsedTime(&ms, ctx->tev[r.a], ctx->tev[r.b]) != cudaSuccess) { cudaGetLastError(); continue; }
+            ctx->cnt.dom_launches++;
+            ctx->cnt.dom_ms += ms;
+            ctx->cnt.dom_entries += r.entries;
+            ctx->cnt.dom_bytes += r.bytes;
+        }
+        recs.clear();
+        next = 0;
+    }
+};
+
 sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, sk_report *rep) {
     cudaStream_t st = ctx->stream;
+    LaunchTimer tm(ctx);
     const bool sharded = P.world > 1;
     const long long m = P.m, n_glob = P.n_total;
     const int ns = (int)slices.size();
@@ -379,6 +430,8 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
 
     auto col_stage = [&]() -> sk_status {
         for (int i = 0; i < ns; ++i) {
+            const double ent = (double)slices[i].n * m;
+            const int t0 = fused ? -1 : tm.start();   // fused: the dominant kernel is the sweep
             if (stored) {
                 StoredPass scol{C[i], slices[i].n, m, P.eps, X[i].pack, col_part(i), bs_rows,
                                 sharded ? blk_per_rank : nblk_glob, split_q, &status->stop};
@@ -394,6 +447,7 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
                 colp.seeded = col_seed && sweep >= 2;
                 CU(launch_lse(colp, st));
             }
+            tm.stop(t0, sweep, LaunchTimer::COL, ent, stored ? 4.0 * ent : 0.0);
         }
         return SK_OK;
     };
@@ -423,7 +477,9 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
                     FusedLaunch fl{C[i], slices[i].n, m, P.eps, Y.pack, X[i].c, {X[i].pot[0], X[i].pot[1]},
                                    X[i].pack, col_part(i), bs_rows, sharded ? blk_per_rank : nblk_glob, split_q,
                                    status};
+                    const int t0 = tm.start();
                     CU(launch_stored_fused(fl, st));
+                    tm.stop(t0, sweep, LaunchTimer::FUSED, 2.0 * slices[i].n * m, 4.0 * slices[i].n * m);
                     MergePass mrow{MERGE_ROW, &X[i], part, 1, P.eps, nullptr, status, blke, blkb, nullptr, 0.f,
                                    sharded ? 1 : 0, i + 1 < ns ? 1 : 0, 1};
                     CU(launch_merge(mrow, st));
@@ -431,12 +487,14 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
                 }
                 CK(exchange_and_merge_col());
                 launched += 1;
+                ++sweep;
                 continue;
             }
             CK(col_stage());
             CK(exchange_and_merge_col());
             launched += ns + 1;
             for (int i = 0; i < ns; ++i) {
+                const int t0 = tm.start();
                 if (stored) {
                     StoredPass srow{C[i], slices[i].n, m, P.eps, Y.pack, part, 0, 1, 1, &status->stop};
                     CU(launch_stored_rows(srow, st));
@@ -449,6 +507,7 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
                     rowp.seeded = row_seed && sweep >= 2;
                     CU(launch_lse(rowp, st));
                 }
+                tm.stop(t0, sweep, LaunchTimer::ROW, (double)slices[i].n * m, stored ? 4.0 * slices[i].n * m : 0.0);
                 // only the last slice's merge advances the sweep counter
                 MergePass mrow{MERGE_ROW, &X[i], part, stored ? 1 : split_row, P.eps, nullptr, status, blke,
                                blkb, nullptr, 0.f, sharded ? 1 : 0, i + 1 < ns ? 1 : 0};
@@ -489,6 +548,7 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
     DevStatus hs = *ctx->h_status;
     if (!hs.stop) return fail(ctx, SK_ECUDA, "solver loop ended without a stop flag");
     const int L = hs.final_iter;
+    tm.collect(hs.iter);
     double E = 0.0;
     for (int b = 0; b < SK_SHARD_BLOCKS; ++b) E += fa_h[b];
     E += gb_part;
@@ -580,6 +640,7 @@ void sk_destroy(sk_ctx *ctx) {
     if (ctx->h_status) cudaFreeHost(ctx->h_status);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+    for (cudaEvent_t e : ctx->tev) cudaEventDestroy(e);
     delete ctx;
 }
 
@@ -909,7 +970,7 @@ sk_status solve_impl(sk_ctx *ctx, int64_t B, int64_t n, int64_t m, int32_t d, co
         CU(cudaStreamSynchronize(st));
         float ms = 0.f;
         CU(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
-        if (ctx->timing) ctx->cnt.lse_ms += ms;
+        if (ctx->timing) { ctx->cnt.lse_ms += ms; ctx->cnt.dom_ms += ms; ctx->cnt.dom_launches++; }
         const double *hE = (const double *)h.data();
         const int *hi = (const int *)(hE + B), *hc = hi + B, *hn = hc + B;
         const float *he = (const float *)(hn + B);
@@ -923,6 +984,7 @@ sk_status solve_impl(sk_ctx *ctx, int64_t B, int64_t n, int64_t m, int32_t d, co
             rep[p].solve_ms = ms;
             any_nf |= hn[p];
             ctx->cnt.lse_ex2 += (double)n * m * (2.0 * hi[p] + 1.0);
+            if (ctx->timing) ctx->cnt.dom_entries += (double)n * m * (2.0 * hi[p] + 1.0);
         }
         if (any_nf) return fail(ctx, SK_ENONFINITE, "potentials became non-finite");
         return SK_OK;

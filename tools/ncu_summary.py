@@ -62,6 +62,31 @@ def launches(path):
     return "\n".join(lines)
 
 
+def traffic(path):
+    """dram__bytes_read.sum + dram__bytes_write.sum (bytes) of the first kernel in a --set full report."""
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    r = list(csv.reader(io.StringIO(raw)))
+    h, u = r[0], r[1]
+    d, du = dict(zip(h, r[2])), dict(zip(h, u))
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+    tot = 0.0
+    for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+        tot += float(d[k].replace(",", "")) * scale.get(du[k], 1)
+    return tot
+
+
 if __name__ == "__main__":
-    kind, path = sys.argv[1], sys.argv[2]
-    print(report(path) if kind == "report" else launches(path))
+    # ncu_summary.py report|launches <file>
+    # ncu_summary.py traffic <out.json> name=<report> ...   (per-launch DRAM bytes for bench.py)
+    kind = sys.argv[1]
+    if kind == "traffic":
+        import json
+        out = {}
+        for a in sys.argv[3:]:
+            name, path = a.split("=", 1)
+            out[name] = traffic(path)
+        json.dump(out, open(sys.argv[2], "w"), indent=1)
+        print(out)
+    else:
+        path = sys.argv[2]
+        print(report(path) if kind == "report" else launches(path))
