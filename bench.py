@@ -189,7 +189,7 @@ class Single(Workload):
         else:
             self.p = gen.c5(eps_factor=args.eps_factor or 1e-2); self.init = args.init or "gaussian"
             self.mode = "online"; self.roof = "tensor"
-            self.kernel = "k_lse_tc<2> (online LSE pass, tcgen05 3xTF32 cross term, K3)"
+            self.kernel = "k_lse_tc (online LSE pass, tcgen05 kind::f16 3-product hi/lo cross term, K3)"
         p = self.p
         self.n, self.m, self.d = p.n, p.m, p.d
         self.sharded = self.name == "c4" and world > 1
@@ -318,13 +318,13 @@ def roofline(w, cnt, steps, pk, src, step_ms):
                                "once for a row pass and the next column pass",
                 "bytes_per_launch": cnt["dom_bytes"] / nl, **common}
     if w.roof == "tensor":
-        flops = cnt["dom_entries"] * 3 * 2 * 64          # 3 TF32 MMAs (hi.hi, hi.lo, lo.hi), K = 64
+        flops = cnt["dom_entries"] * 3 * 2 * 64          # 3 fp16 MMAs (hi.hi, hi.lo, lo.hi), K = 64
         achieved = flops / dom_s / 1e12 if dom_s > 0 else 0.0
-        peak = float(pk["bf16_tflops"]) * 1.1 / 2.25   # TF32 = measured BF16 x nominal TF32/BF16 ratio
+        peak = float(pk["bf16_tflops"])                  # fp16 dense = bf16 dense rate
         ex2_peak = N_SM * MUFU_EX2_PER_CLK_SM * sm_max * 1e6
         return {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                "peak_source": f"MEASURED_PEAKS.json bf16_tflops x 1.1/2.25 (nominal TF32/BF16), {src}",
-                "algorithmic": "3 x 2 x 64 TF32 flops per cost entry per pass (3xTF32 split)",
+                "peak_source": f"MEASURED_PEAKS.json bf16_tflops (fp16 runs at the bf16 rate), {src}",
+                "algorithmic": "3 x 2 x 64 fp16 tensor flops per cost entry per pass (3-product hi/lo split)",
                 "flops_per_launch": flops / nl,
                 "mufu_frac": (cnt["dom_entries"] / dom_s) / ex2_peak if dom_s > 0 else 0.0, **common}
     achieved = cnt["dom_entries"] / dom_s if dom_s > 0 else 0.0
@@ -408,10 +408,10 @@ def run_ours(args):
 
     k14 = {}
     if rank == 0 and not args.no_k14:
-        # K14 microbenchmarks: this device's MUFU / FP32 / HBM / TF32 rates (roofline context)
+        # K14 microbenchmarks: this device's MUFU / FP32 / HBM / fp16 tensor rates (roofline context)
         try:
             k14 = {"ex2_per_s": ctx.microbench("ex2"), "ffma_per_s": ctx.microbench("ffma"),
-                   "hbm_read_GBps": ctx.microbench("hbm") / 1e9, "tf32_TFLOPs": ctx.microbench("tf32") / 1e12}
+                   "hbm_read_GBps": ctx.microbench("hbm") / 1e9, "tc_f16_TFLOPs": ctx.microbench("tc") / 1e12}
         except Exception as ex:  # pragma: no cover
             k14 = {"error": repr(ex)}
     with torch.cuda.stream(stream):

@@ -239,16 +239,22 @@ sk_status sinkhorn_solve_sharded_emulated(sk_ctx *ctx, int32_t world, int64_t n,
                                           float *f, float *g, sk_report *rep /* host */);
 
 /* Diagnostic: out[i][j] = <x_i, y_j> for 128 x d and 128 x d fp32 inputs (row-major;
- * out 128 x 128), computed by the tensor-core path of the LSE pass (K3: 3xTF32 split,
- * tcgen05.mma kind::tf32, fp32 accumulators read back from TMEM).  d in [1, 64].  For
+ * out 128 x 128), computed by the tensor-core path of the LSE pass (K3: 3-product fp16
+ * hi/lo split of power-of-two scaled operands, tcgen05.mma kind::f16, fp32 accumulators read
+ * back from TMEM and unscaled exactly).  d in [1, 64].  For
  * testing the operand layout and the error compensation.  Blocks. */
 sk_status sk_selftest_tc_dot(sk_ctx *ctx, int32_t d, const float *x, const float *y, float *out);
 
 /* K14 microbenchmarks (roofline denominators measured on this device, CUDA events on the
  * context stream): kind 0 = MUFU.EX2 throughput (ex2/s); 1 = FP32 FMA throughput (FMA
  * lane-operations/s, packed FFMA2); 2 = streaming HBM read bandwidth (bytes/s, 4 GiB,
- * 128-bit non-allocating loads); 3 = tcgen05 kind::tf32 MMA throughput (flop/s, the K3
- * kernel with its epilogue skipped).  *value (host) receives the rate.  Blocks. */
+ * 128-bit non-allocating loads); 3 = tcgen05 kind::f16 MMA throughput (flop/s, the K3
+ * kernel with its epilogue skipped); 4 = the same without reloading the B operand ring
+ * (pure MMA issue rate); 5..8 = raw tcgen05.mma rate of one shape in flop per SM clock
+ * (M = 128; 5: f16 N = 128, 6: f16 N = 256, 7: tf32 N = 128, 8: tf32 N = 256); 9, 10 = kinds
+ * 3, 4 in flop per SM clock (cycles of the first CTA); 100 + (shape | mode << 2) = the raw
+ * probe with diagnostic mode bits (sk_tc.cu k_mb_mma).  *value (host)
+ * receives the rate.  Blocks. */
 sk_status sk_microbench(sk_ctx *ctx, int32_t kind, double *value);
 
 #ifdef __cplusplus

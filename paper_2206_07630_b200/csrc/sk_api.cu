@@ -22,15 +22,17 @@ typedef void *nccl_comm_t;
 typedef int (*fn_get_id)(nccl_id_t *);
 typedef int (*fn_init_rank)(nccl_comm_t *, int, nccl_id_t, int);
 typedef int (*fn_allgather)(const void *, void *, size_t, int, nccl_comm_t, cudaStream_t);
+typedef int (*fn_allreduce)(const void *, void *, size_t, int, int, nccl_comm_t, cudaStream_t);
 typedef int (*fn_destroy)(nccl_comm_t);
 typedef const char *(*fn_errstr)(int);
-constexpr int kNcclFloat32 = 7, kNcclFloat64 = 8;
+constexpr int kNcclFloat32 = 7, kNcclFloat64 = 8, kNcclMax = 2;
 
 struct Nccl {
     void *h = nullptr;
     fn_get_id get_id = nullptr;
     fn_init_rank init_rank = nullptr;
     fn_allgather allgather = nullptr;
+    fn_allreduce allreduce = nullptr;
     fn_destroy destroy = nullptr;
     fn_errstr errstr = nullptr;
     bool load() {
@@ -44,9 +46,10 @@ struct Nccl {
         get_id = (fn_get_id)dlsym(h, "ncclGetUniqueId");
         init_rank = (fn_init_rank)dlsym(h, "ncclCommInitRank");
         allgather = (fn_allgather)dlsym(h, "ncclAllGather");
+        allreduce = (fn_allreduce)dlsym(h, "ncclAllReduce");
         destroy = (fn_destroy)dlsym(h, "ncclCommDestroy");
         errstr = (fn_errstr)dlsym(h, "ncclGetErrorString");
-        return get_id && init_rank && allgather && destroy;
+        return get_id && init_rank && allgather && allreduce && destroy;
     }
 };
 Nccl g_nccl;
@@ -77,7 +80,7 @@ enum BufId {
     B_STAGE0 = 0, B_STAGE_END = 16,   // staging of host arrays
     B_FLAG = 16, B_XPACK, B_XC, B_XNK, B_XPOT, B_YPACK, B_YC, B_YNK, B_YPOT, B_PART, B_BLKE, B_BLKB,
     B_STATUS, B_COST, B_REP, B_SORT, B_PERM, B_YSORT, B_GAUSS, B_GAUSS2, B_GMM, B_SUBW, B_SUBZ,
-    B_SUBF, B_SUBG, B_IDX, B_OUT, B_FA, B_QUEUE, B_XIMG, B_YIMG, B_XLSE, B_YLSE, B_NBUF
+    B_SUBF, B_SUBG, B_IDX, B_OUT, B_FA, B_QUEUE, B_XIMG, B_YIMG, B_XLSE, B_YLSE, B_TCMAX, B_NBUF
 };
 
 sk_status fail(sk_ctx *c, sk_status s, const char *fmt, ...) {
@@ -311,7 +314,7 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
     // K = 32); SK_TC=0 forces the FFMA kernel (tuning / comparison knob)
     static const int tc_env = [] { const char *e = getenv("SK_TC"); return e ? atoi(e) : 1; }();
     const bool tc = !stored && P.d > 16 && P.d <= 64 && tc_env != 0;
-    const int katoms = P.d > 32 ? 2 : 1;
+    const int ksteps = (P.d + 15) / 16;
     const int D = (stored || tc) ? 0 : lse_dpad(P.d);
     if (!stored && !tc && D == 0) return fail(ctx, SK_EUNSUPPORTED, "online path supports d <= 64");
     const int tq = stored ? 256 : (tc ? 128 : lse_tq(D));
@@ -333,17 +336,28 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
     ENSURE(ynk, float, B_YNK, m);
     ENSURE(ypot, float, B_YPOT, 2 * m);
     ENSURE(status, DevStatus, B_STATUS, 1);
-    float *ximg = nullptr, *yimg = nullptr;
+    char *ximg = nullptr, *yimg = nullptr;
+    unsigned *amax = nullptr;
     std::vector<long long> offi(ns + 1, 0);
     if (tc) {
-        for (int i = 0; i < ns; ++i) offi[i + 1] = offi[i] + (long long)tc_image_floats(slices[i].n, katoms);
+        for (int i = 0; i < ns; ++i) offi[i + 1] = offi[i] + (long long)tc_image_bytes(slices[i].n);
         cudaError_t e1, e2;
-        ximg = (float *)ensure(ctx, B_XIMG, sizeof(float) * (size_t)offi[ns], &e1);
-        yimg = (float *)ensure(ctx, B_YIMG, sizeof(float) * tc_image_floats(m, katoms), &e2);
+        ximg = (char *)ensure(ctx, B_XIMG, (size_t)offi[ns], &e1);
+        yimg = (char *)ensure(ctx, B_YIMG, tc_image_bytes(m), &e2);
         if (!ximg || !yimg) return fail(ctx, SK_ENOMEM, "tensor-core operand images");
-        for (int i = 0; i < ns; ++i) CU(launch_pack_tc(slices[i].x, slices[i].n, P.d, katoms, ximg + offi[i], st));
-        CU(launch_pack_tc(P.y, m, P.d, katoms, yimg, st));
-        ctx->cnt.kernel_launches += ns + 1;
+        amax = (unsigned *)ensure(ctx, B_TCMAX, 2 * sizeof(unsigned), &e1);
+        if (!amax) return fail(ctx, SK_ENOMEM, "tensor-core scales");
+        // per-side max |coordinate| -> exact power-of-two operand scales (global over the ranks)
+        CU(cudaMemsetAsync(amax, 0, 2 * sizeof(unsigned), st));
+        for (int i = 0; i < ns; ++i) CU(launch_absmax(slices[i].x, slices[i].n * P.d, amax, st));
+        CU(launch_absmax(P.y, m * P.d, amax + 1, st));
+        if (P.nccl && sharded) {
+            int r = g_nccl.allreduce(amax, amax, 1, kNcclFloat32, kNcclMax, ctx->comm, st);
+            if (r != 0) return fail(ctx, SK_ENCCL, "ncclAllReduce(max) failed");
+        }
+        for (int i = 0; i < ns; ++i) CU(launch_pack_tc(slices[i].x, slices[i].n, P.d, amax, ximg + offi[i], st));
+        CU(launch_pack_tc(P.y, m, P.d, amax + 1, yimg, st));
+        ctx->cnt.kernel_launches += 2 * ns + 2;
     }
     std::vector<Side> X(ns);
     for (int i = 0; i < ns; ++i) {
@@ -373,7 +387,8 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
     const int blk_per_rank = sharded ? SK_SHARD_BLOCKS / P.world : nblk_glob;
     const int occ = stored ? 8 : (tc ? 1 : lse_occupancy_ctas(D));
     const int Rr = tc ? 1 : (D <= 4 ? 4 : (D <= 16 ? 2 : 1));
-    const long long ptiles_col = stored ? (m + 511) / 512 : (m + 128LL * Rr - 1) / (128LL * Rr);
+    const long long pcta = tc ? tc_points_per_cta() : 128LL * Rr;   // output points per CTA
+    const long long ptiles_col = stored ? (m + 511) / 512 : (m + pcta - 1) / pcta;
     // stored mode with the fused sweep (one persistent CTA per SM): 8 blocks x split_q = one wave
     static const int fused_env = [] { const char *e = getenv("SK_FUSED"); return e ? atoi(e) : 1; }();
     const bool fused = stored && fused_env != 0 && stored_fused_supported(m);
@@ -384,7 +399,9 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
     const int nsplit_col = (sharded ? SK_SHARD_BLOCKS : nblk_glob) * split_q;
     int split_row = 1;
     if (!stored) {
-        const long long ptiles_row = (n_max + 128LL * Rr - 1) / (128LL * Rr);
+        // from n_total, not the local slice: the row-pass split (and so the summation order of
+        // every row's LSE) is the same for every partition of the rows
+        const long long ptiles_row = (n_glob + pcta - 1) / pcta;
         split_row = choose_split(ptiles_row, yt, occ, 64);
     }
     const long long part_elems = std::max((long long)nsplit_col * m, (long long)split_row * n_max);
@@ -437,7 +454,7 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
                                 sharded ? blk_per_rank : nblk_glob, split_q, &status->stop};
                 CU(launch_stored_cols(scol, st));
             } else if (tc) {
-                TcPass colp{yimg, ximg + offi[i], X[i].pack, (int)m, slices[i].n, katoms,
+                TcPass colp{yimg, ximg + offi[i], X[i].pack, amax + 1, amax, (int)m, slices[i].n, ksteps,
                             sharded ? blk_per_rank : nblk_glob, (int)(bs_rows / tq), split_q, col_part(i),
                             P.eps, &status->stop, nullptr, 0};
                 CU(launch_lse_tc(colp, st));
@@ -499,7 +516,8 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
                     StoredPass srow{C[i], slices[i].n, m, P.eps, Y.pack, part, 0, 1, 1, &status->stop};
                     CU(launch_stored_rows(srow, st));
                 } else if (tc) {
-                    TcPass rowp{ximg + offi[i], yimg, Y.pack, (int)slices[i].n, m, katoms, 1, 0, split_row, part,
+                    TcPass rowp{ximg + offi[i], yimg, Y.pack, amax, amax + 1, (int)slices[i].n, m, ksteps, 1, 0,
+                                split_row, part,
                                 P.eps, &status->stop, nullptr, 0};
                     CU(launch_lse_tc(rowp, st));
                 } else {
@@ -1127,30 +1145,47 @@ sk_status sinkhorn_solve_sharded_emulated(sk_ctx *ctx, int32_t world, int64_t n,
 sk_status sk_selftest_tc_dot(sk_ctx *ctx, int32_t d, const float *x, const float *y, float *out) {
     if (!ctx) return SK_EINVAL;
     if (d < 1 || d > 64 || !x || !y || !out) return fail(ctx, SK_EINVAL, "d in [1, 64], non-NULL arrays");
-    const int katoms = d > 32 ? 2 : 1;
+    const int ksteps = (d + 15) / 16;
     Stager sg(ctx);
     const float *dx, *dy;
     float *dout;
     CK(sg.in_t(x, (size_t)128 * d, &dx));
     CK(sg.in_t(y, (size_t)128 * d, &dy));
     CK(sg.out_t(out, (size_t)128 * 128, &dout));
-    ENSURE(ximg, float, B_XIMG, tc_image_floats(128, katoms));
-    ENSURE(yimg, float, B_YIMG, tc_image_floats(128, katoms));
+    ENSURE(ximg, char, B_XIMG, tc_image_bytes(128));
+    ENSURE(yimg, char, B_YIMG, tc_image_bytes(128));
+    ENSURE(amax, unsigned, B_TCMAX, 2);
     ENSURE(w, float, B_SUBG, 128);
     ENSURE(part, float2, B_PART, 128);
-    CU(launch_pack_tc(dx, 128, d, katoms, ximg, ctx->stream));
-    CU(launch_pack_tc(dy, 128, d, katoms, yimg, ctx->stream));
+    CU(cudaMemsetAsync(amax, 0, 2 * sizeof(unsigned), ctx->stream));
+    CU(launch_absmax(dx, 128LL * d, amax, ctx->stream));
+    CU(launch_absmax(dy, 128LL * d, amax + 1, ctx->stream));
+    CU(launch_pack_tc(dx, 128, d, amax, ximg, ctx->stream));
+    CU(launch_pack_tc(dy, 128, d, amax + 1, yimg, ctx->stream));
     CU(launch_fill(w, 128, 0.f, ctx->stream));
-    TcPass tp{ximg, yimg, w, 128, 128, katoms, 1, 0, 1, part, 1.f, nullptr, dout, 0};
+    TcPass tp{ximg, yimg, w, amax, amax + 1, 128, 128, ksteps, 1, 0, 1, part, 1.f, nullptr, dout, 0};
     CU(launch_lse_tc(tp, ctx->stream));
-    ctx->cnt.kernel_launches += 4;
+    ctx->cnt.kernel_launches += 6;
     CK(sg.flush());
     CU(cudaStreamSynchronize(ctx->stream));
     return SK_OK;
 }
 
+static int nsm_probe(sk_ctx *ctx) {
+    int n = 148;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, ctx->device);
+    return n;
+}
+
 sk_status sk_microbench(sk_ctx *ctx, int32_t kind, double *value) {
-    if (!ctx || !value || kind < 0 || kind > 3) return fail(ctx, SK_EINVAL, "kind in [0, 3]");
+    if (!ctx || !value || kind < 0 || (kind > 10 && kind < 100) || kind > 163)
+        return fail(ctx, SK_EINVAL, "kind in [0, 10] or [100, 163]");
+    if ((kind >= 5 && kind <= 8) || kind >= 100) {   // raw MMA issue rate of one shape, flop per SM clock
+        ENSURE(scr, long long, B_OUT, 16);
+        CU(microbench_mma(kind >= 100 ? kind - 100 : kind - 5, scr, ctx->stream, value));
+        ctx->cnt.kernel_launches += 2;
+        return SK_OK;
+    }
     cudaStream_t st = ctx->stream;
     ENSURE(sink, float, B_OUT, 1024);
     float ms = 0.f;
@@ -1171,24 +1206,31 @@ sk_status sk_microbench(sk_ctx *ctx, int32_t kind, double *value) {
         CU(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
         *value = (double)bytes / (ms * 1e-3);
     } else {
-        const long long P = 32768, Q = 32768;   // 256 x 256 tiles of 128 x 128 x 64, 3 MMAs each
-        const int katoms = 2;
-        cudaError_t e1, e2;
-        float *img = (float *)ensure(ctx, B_XIMG, sizeof(float) * tc_image_floats(P, katoms), &e1);
+        const long long P = 32768, Q = 32768;   // 256 x 256 tiles of 128 x 128 x 64, 3 fp16 MMAs each
+        cudaError_t e1;
+        char *img = (char *)ensure(ctx, B_XIMG, tc_image_bytes(P), &e1);
         ENSURE(w, float, B_SUBG, Q);
-        ENSURE(part, float2, B_PART, P * 8);
-        (void)e2;
+        ENSURE(part, float2, B_PART, P * 37);
+        ENSURE(amax, unsigned, B_TCMAX, 2);
         if (!img) return fail(ctx, SK_ENOMEM, "tc probe images");
-        CU(cudaMemsetAsync(img, 0, sizeof(float) * tc_image_floats(P, katoms), st));
+        CU(cudaMemsetAsync(img, 0, tc_image_bytes(P), st));
+        CU(cudaMemsetAsync(amax, 0, 2 * sizeof(unsigned), st));
         CU(launch_fill(w, Q, 0.f, st));
-        TcPass tp{img, img, w, (int)P, Q, katoms, 1, 0, 4, part, 1.f, nullptr, nullptr, 1};
+        TcPass tp{img, img, w, amax, amax + 1, (int)P, Q, 4, 1, 0, 37, part, 1.f, nullptr, nullptr,
+                  (kind == 4 || kind == 10) ? 2 : 1};
+        ENSURE(cyc, long long, B_FA, 16);
+        tp.cyc = cyc;
         CU(launch_lse_tc(tp, st));  // warm-up
         CU(cudaEventRecord(ctx->ev0, st));
         CU(launch_lse_tc(tp, st));
         CU(cudaEventRecord(ctx->ev1, st));
         CU(cudaEventSynchronize(ctx->ev1));
         CU(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
-        *value = 3.0 * 2.0 * 64.0 * (double)P * (double)Q / (ms * 1e-3);
+        long long c = 0;
+        CU(cudaMemcpy(&c, cyc, sizeof c, cudaMemcpyDeviceToHost));
+        // kinds 3, 4: flop/s; kinds 9, 10 (same runs): flop per SM clock of CTA 0
+        const double flops = 3.0 * 2.0 * 64.0 * (double)P * (double)Q;
+        *value = kind >= 9 ? flops / nsm_probe(ctx) / (double)(c > 0 ? c : 1) : flops / (ms * 1e-3);
     }
     ctx->cnt.kernel_launches += 2;
     return SK_OK;

@@ -100,6 +100,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         : "memory");
 }
 
+// Consumer-side wait that suspends the thread (suspendTimeHint, ns) instead of re-polling the
+// barrier: many waiting warps otherwise steal shared-memory cycles from the tensor core's
+// operand reads.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity) {
+    uint32_t addr = smem_u32(bar);
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAITS_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "@!p bra WAITS_%=;\n\t}" ::"r"(addr),
+        "r"(parity), "r"(0x989680)
+        : "memory");
+}
+
 // --------------------------------------------------------- block reductions
 // Deterministic (fixed-order) block sum of doubles; all threads get the result.
 template <int NT>

@@ -66,21 +66,27 @@ cudaError_t pack_side(const Side &S, const float *pts, const float *wts, float l
                       const float *pot0, float eps, cudaStream_t st, int mode = -1);
 
 // ------------------------------------------------------- K3 tensor-core pass
+// Images: per tile of 128 points [hi | lo] fp16, K-major SW128, K padded to 64 (d <= 64);
+// each side scaled by 2^-e from its max |coordinate| (amax, a device uint: float bits).
 struct TcPass {
-    const float *Aimg, *Bimg;   // images of the output side (A) and the reduced side (B)
+    const void *Aimg, *Bimg;    // images of the output side (A) and the reduced side (B)
     const float *Bw;            // reduced side w (D = 0 pack, tq = 128)
+    const unsigned *amax_p, *amax_q;
     int P;  long long Q;
-    int katoms;                 // 1 (K = 32) or 2 (K = 64)
+    int ksteps;                 // ceil(d / 16): K = 16 MMA steps
     int nblk, blk_tiles, split_q;
     float2 *part;
     float eps;
     const int *stop;
     float *debug_acc;
     int mma_only = 0;
+    long long *cyc = nullptr;   // K14: SM cycles of CTA 0
 };
-size_t tc_image_floats(long long P, int katoms);
-cudaError_t launch_pack_tc(const float *pts, long long P, int d, int katoms, float *img, cudaStream_t st);
+size_t tc_image_bytes(long long P);
+cudaError_t launch_absmax(const float *pts, long long cnt, unsigned *out, cudaStream_t st);  // out zeroed first
+cudaError_t launch_pack_tc(const float *pts, long long P, int d, const unsigned *amax, void *img, cudaStream_t st);
 cudaError_t launch_lse_tc(const TcPass &L, cudaStream_t st);
+int tc_points_per_cta();   // output points per K3 CTA (two 128-row A tiles)
 
 // One LSE pass: outputs P side points, reduces over Q side.  Splits:
 // nblk blocks of blk_tiles Q tiles each (the last may be shorter; blk_tiles = 0
@@ -191,6 +197,7 @@ cudaError_t launch_stored_cols(const StoredPass &S, cudaStream_t st);
 
 // ------------------------------------------------------------ K14 microbenchmarks
 cudaError_t microbench_alu(int kind, cudaStream_t st, cudaEvent_t e0, cudaEvent_t e1, float *sink, double *ops);
+cudaError_t microbench_mma(int kind, void *scratch, cudaStream_t st, double *flop_per_clk);
 cudaError_t microbench_hbm(const float *buf, long long bytes, cudaStream_t st, cudaEvent_t e0, cudaEvent_t e1,
                            float *sink);
 

@@ -2,7 +2,7 @@
 //   SK_MB_EX2   MUFU.EX2 throughput (ex2/s): 8 independent ex2 chains per thread
 //   SK_MB_FFMA  FP32 FMA throughput (FMA/s): 8 independent FFMA2 chains per thread (16 lanes)
 //   SK_MB_HBM   streaming read bandwidth (B/s): 128-bit non-allocating loads over 4 GiB
-//   SK_MB_TF32  tcgen05 kind::tf32 MMA throughput (flop/s): the K3 kernel with the epilogue
+//   SK_MB_TC    tcgen05 kind::f16 MMA throughput (flop/s): the K3 kernel with the epilogue
 //               skipped (measured in sk_tc.cu)
 #include "sk_internal.h"
 #include "sk_common.cuh"

@@ -1,64 +1,94 @@
 // sk_tc.cu — K3: the online LSE pass with the cross term on the 5th-generation tensor
-// cores (tcgen05, kind::tf32, fp32 accumulators in TMEM), for d in (16, 64].
+// cores (tcgen05, kind::f16 with fp16 operands, fp32 accumulators in TMEM), for d in (16, 64].
 //
 // BJ.ns: "computes the -2<x,y> cross term on tensor cores only when d >= 32, using an
-// error-compensated 3xTF32 split".  Every point is split once per solve into
-// hi = tf32(x), lo = tf32(x - hi) and stored as MMA-ready images (K-major, 128-byte
-// swizzle, tiles of 128 points); acc = <p, q> is accumulated as
-//     lo_p . hi_q + hi_p . lo_q + hi_p . hi_q      (3 MMAs per K step; lo.lo dropped)
-// which is fp32-accurate (error ~2^-22 |p||q|; the potential error is 2 |d acc|).
+// error-compensated 3xTF32/bf16x3 split".  This kernel uses the same three-product split with
+// IEEE fp16 pieces, which runs at twice the TF32 tensor rate and carries the same 22-bit
+// significand: each side is first scaled by an exact power of two s = 2^-e so that
+// max |s x| lies in [1/2, 1) (K3a absmax), then every coordinate is split once per solve into
+//     hi = fp16(s x),  lo = fp16(s x - hi)      (11 + 11 significand bits)
+// and stored as MMA-ready images (K-major, 128-byte swizzle, tiles of 128 points, K padded to
+// 64).  acc = <s_p p, s_q q> is accumulated as
+//     lo_p . hi_q + hi_p . lo_q + hi_p . hi_q      (3 MMAs per K = 16 step; lo.lo dropped)
+// which is fp32-accurate (error ~2^-22 max|p| max|q| per term); the epilogue folds 1/(s_p s_q)
+// (exact) into the log2-domain scale.  Power-of-two scaling commutes with every fp16/fp32
+// rounding above the subnormal range, so the scale choice does not change the result; the
+// sharded path still takes it from the global maximum (identical on every rank).
 //
-// CTA = one tile of 128 output points (TMEM lanes) x one split of the other side:
-//   warp 0   producer: 1D bulk TMA of the A image (once) and of B tile images + w tiles
-//            into a 2-stage ring (mbarrier complete_tx);
-//   warp 1   TMEM allocation and the MMA issuer (one elected thread): 3*K/8 MMAs
-//            128x128xK per tile into one of two TMEM accumulators, tcgen05.commit to
-//            the smem-slot and accumulator-ready barriers;
-//   warps 2-5 epilogue: tcgen05.ld of the thread's row (= TMEM lane), t = 2 log2(e)/eps
-//            * acc + w_q, online (max, sum 2^(t - max)) per 32 columns, MUFU.EX2.
+// CTA = 256 output points (two 128-row A tiles, TMEM lanes) x one split of the other side;
+// every B tile of 128 reduction points is multiplied against both A tiles, so the B operand
+// stream from L2 is 1 byte per cost entry (the L2 -> SM bandwidth bound of a 128-row tile):
+//   warp 0   producer: 1D bulk TMA of the A images (once) and of B tile images + w tiles
+//            into a kTcStages-deep ring (mbarrier complete_tx);
+//   warp 1   TMEM allocation (512 columns = 2 buffers x 2 A tiles x 128) and the MMA issuer
+//            (one elected thread): 2 x 3 x ksteps MMAs 128x128x16 per B tile, tcgen05.commit
+//            to the smem-slot and accumulator-ready barriers;
+//   warps 2-9 epilogue: warp w owns TMEM lane quadrant w % 4 of A tile (w - 2) / 4: one output
+//            point per thread, all 128 columns; tcgen05.ld, t = acc * 2 log2(e)/(eps s_p s_q)
+//            + w_q (FFMA2), online (max, sum 2^(t - max)) per 64 columns (FMNMX3 tree,
+//            exponentials on MUFU.EX2 with a fraction on the FMA pipe, FADD2).
 // The output is the same (max, sum) partial as the FFMA kernel (K2), merged by K6.
+#include <cuda_fp16.h>
+
+#include <cstdlib>
+
 #include "sk_internal.h"
 #include "sk_common.cuh"
+#include "sk_lse_tile.cuh"
 
 namespace sk {
 
 constexpr int kTcM = 128;       // points per tile (MMA M and N)
-constexpr int kTcEpiWarps = 8;  // two per TMEM lane quadrant, each half of the columns
+constexpr int kTcEpiWarps = 8;  // two per TMEM lane quadrant (one per A tile)
 constexpr int kTcThreads = 64 + 32 * kTcEpiWarps;
-constexpr int kTcStages = 2;
-
-__host__ __device__ constexpr int tc_img_bytes(int katoms) { return 16 * katoms * 1024; }  // one of hi/lo
+// smem: ABUF A buffers (64 KB each) + a B ring of tc_stages(ABUF) x (32 KB + 512 B)
+__host__ __device__ constexpr int tc_stages(int abuf) { return abuf == 2 ? 2 : 4; }
+constexpr int kTcImg = kTcM * 128;  // bytes of one fp16 image: 128 rows x 64 halves (16 SW128 atoms)
 
 // ------------------------------------------------------------ operand images
-__device__ __forceinline__ float tf32_rna(float x) {
-    uint32_t r;
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-    return __uint_as_float(r);
+// K3a: max |x| over all coordinates (non-negative floats order like their bit patterns).
+__global__ void k_absmax(const float *__restrict__ pts, long long cnt, unsigned *out) {
+    float mx = 0.f;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < cnt;
+         i += (long long)gridDim.x * blockDim.x)
+        mx = fmaxf(mx, fabsf(pts[i]));
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0 && mx > 0.f) atomicMax(out, __float_as_uint(mx));
+}
+
+// exponent e with max = f 2^e, f in [1/2, 1): the side's scale is 2^-e (1 for an all-zero side)
+__device__ __forceinline__ int tc_scale_exp(const unsigned *amax) {
+    const float mx = __uint_as_float(*amax);
+    int e = 0;
+    if (mx > 0.f) frexpf(mx, &e);
+    return e;
 }
 
 // img: tiles of 128 points, each [hi image | lo image], K-major SWIZZLE_128B canonical
-// layout: 8-row x 128-byte atoms, atom (mi, kj) at (mi + 16 kj) * 1024 bytes, the 16-byte
-// chunk c of row r stored at chunk c ^ (r % 8).
-__global__ void k_pack_tc(const float *__restrict__ pts, long long P, int d, int katoms, float *img) {
-    const long long tiles = (P + kTcM - 1) / kTcM;
-    const int K = 32 * katoms;
-    const long long total = tiles * kTcM * K;
-    const int IMG = tc_img_bytes(katoms);
+// layout: 8-row x 128-byte atoms, atom mi at mi * 1024 bytes, the 16-byte chunk c (halves
+// 8c .. 8c+7) of row r stored at chunk c ^ (r % 8).  One thread per (point, chunk).
+__global__ void k_pack_tc(const float *__restrict__ pts, long long P, long long P2, int d, const unsigned *amax,
+                          unsigned char *img) {
+    const long long total = P2 * 8;
+    const float sc = ldexpf(1.f, -tc_scale_exp(amax));
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
          e += (long long)gridDim.x * blockDim.x) {
-        const long long p = e / K;
-        const int k = (int)(e % K);
+        const long long p = e >> 3;
+        const int c = (int)(e & 7);
         const long long t = p / kTcM;
         const int r = (int)(p % kTcM);
-        const float x = (p < P && k < d) ? pts[p * d + k] : 0.f;
-        const float hi = tf32_rna(x);
-        const float lo = tf32_rna(x - hi);
-        const int kj = k / 32, kb = (k % 32) * 4;
-        const int chunk = (kb >> 4) ^ (r & 7);
-        const long long off = (long long)((r >> 3) + 16 * kj) * 1024 + (r & 7) * 128 + chunk * 16 + (kb & 15);
-        char *base = reinterpret_cast<char *>(img) + t * 2LL * IMG;
-        *reinterpret_cast<float *>(base + off) = hi;
-        *reinterpret_cast<float *>(base + IMG + off) = lo;
+        __align__(16) __half hi[8], lo[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int k = 8 * c + j;
+            const float x = (p < P && k < d) ? pts[p * d + k] * sc : 0.f;
+            hi[j] = __float2half_rn(x);
+            lo[j] = __float2half_rn(x - __half2float(hi[j]));
+        }
+        const long long off = (long long)(r >> 3) * 1024 + (r & 7) * 128 + ((c ^ (r & 7)) << 4);
+        unsigned char *base = img + t * 2LL * kTcImg;
+        *reinterpret_cast<uint4 *>(base + off) = *reinterpret_cast<const uint4 *>(hi);
+        *reinterpret_cast<uint4 *>(base + kTcImg + off) = *reinterpret_cast<const uint4 *>(lo);
     }
 }
 
@@ -73,16 +103,21 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
     return desc;
 }
 
-// kind::tf32, D = F32, A = B = TF32, both K-major, M = 128, N = 128
-constexpr uint32_t kIdescTf32 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(kTcM >> 3) << 17) |
-                                ((uint32_t)(kTcM >> 4) << 24);
+// kind::f16, D = F32, A = B = F16, both K-major, M = 128, N = 128
+constexpr uint32_t kIdescF16 = (1u << 4) | ((uint32_t)(kTcM >> 3) << 17) | ((uint32_t)(kTcM >> 4) << 24);
 
-__device__ __forceinline__ void umma_tf32(uint32_t dtmem, uint64_t adesc, uint64_t bdesc, uint32_t accum) {
+__device__ __forceinline__ void umma_f16(uint32_t dtmem, uint64_t adesc, uint64_t bdesc, uint32_t accum) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(dtmem),
-        "l"(adesc), "l"(bdesc), "r"(kIdescTf32), "r"(accum));
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(dtmem),
+        "l"(adesc), "l"(bdesc), "r"(kIdescF16), "r"(accum));
+}
+
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+    float d;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+    return d;
 }
 
 __device__ __forceinline__ void umma_commit(uint64_t *bar) {
@@ -112,194 +147,381 @@ __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.
 
 // ------------------------------------------------------------------ the kernel
 struct TcArgs {
-    const float *Aimg;      // P side images
-    const float *Bimg;      // Q side images
-    const float *Bw;        // Q side packed w, [Qtiles][128] (D = 0 style plain array, padded -inf)
-    int P, Qtiles;
-    int blk_tiles, split_q; // Q split structure (as K2)
+    const unsigned char *Aimg;  // P side images
+    const unsigned char *Bimg;  // Q side images
+    const float *Bw;            // Q side packed w, [Qtiles][128] (D = 0 style plain array, padded -inf)
+    const unsigned *amax_p, *amax_q;  // per-side max |coordinate| (scales)
+    int P, Qtiles, ksteps, ptiles;
+    int nblk, blk_tiles, split_q;   // Q split structure (as K2)
     float2 *part;
-    float tk;               // 2 log2(e)/eps
+    float tk;                   // 2 log2(e)/eps
     const int *stop;
-    float *debug_acc;       // if non-null: write raw acc of the first Q tile, [128][128]
-    int mma_only;           // K14 microbenchmark: epilogue only releases the buffers
+    float *debug_acc;           // if non-null: write <p, q> (acc unscaled) of the first Q tile, [128][128]
+    int mma_only;               // K14 microbenchmark: epilogue only releases the buffers (2: and no B reloads)
+    long long *cyc;             // K14: SM cycles of CTA 0 (clock64 around the work), nullable
 };
 
-template <int KATOMS>
+// exponentials of one 64-column chunk: 32 pairs, EMU of every 8 pairs on the FMA pipe
+template <int EMU>
+__device__ __forceinline__ float2 tc_sum_chunk(const float2 (&t)[32], float M) {
+    const float2 mm = make_float2(M, M);
+    float2 s0 = make_float2(0.f, 0.f), s1 = s0;
+#pragma unroll
+    for (int j = 0; j < 32; j += 2) {
+        float2 e0 = sub2(t[j], mm), e1 = sub2(t[j + 1], mm);
+        if ((j & 7) >= 8 - EMU) e0 = ex2_emu2(e0); else { e0.x = ex2(e0.x); e0.y = ex2(e0.y); }
+        if (((j + 1) & 7) >= 8 - EMU) e1 = ex2_emu2(e1); else { e1.x = ex2(e1.x); e1.y = ex2(e1.y); }
+        s0 = add2(s0, e0);
+        s1 = add2(s1, e1);
+    }
+    return add2(s0, s1);
+}
+
+// Persistent: one CTA per SM walks the work items (A tile pair pt, split s), item =
+// s * ptiles + pt, items blockIdx.x, blockIdx.x + gridDim.x, ...  (concurrent CTAs share the
+// split's B tiles in L2).  The B ring, the two accumulator buffers and the two A buffers are
+// carried across items, so the next item's A images load while the current item computes.
+template <int EMU, int ABUF>
 __global__ void __launch_bounds__(kTcThreads, 1) k_lse_tc(TcArgs A) {
-    constexpr int IMG = tc_img_bytes(KATOMS);
-    constexpr int KSTEPS = KATOMS * 4;              // K = 8 tf32 per MMA
-    constexpr int STAGE = 2 * IMG;                  // B hi + lo (1024-aligned slots)
+    constexpr int kTcStages = tc_stages(ABUF);
+    constexpr int STAGE = 2 * kTcImg;               // B hi + lo (1024-aligned slots)
     extern __shared__ __align__(1024) unsigned char smraw[];
     // 1024-byte alignment of the dynamic smem window for the swizzled operands
     unsigned char *sm = smraw + ((1024 - (smem_u32(smraw) & 1023)) & 1023);
-    unsigned char *sA = sm;                          // [hi | lo] of this CTA's 128 points
-    unsigned char *sB = sm + 2 * IMG;                // kTcStages x STAGE
+    unsigned char *sA = sm;                          // ABUF buffers x 2 A tiles x [hi | lo]
+    unsigned char *sB = sm + ABUF * 4 * kTcImg;      // kTcStages x STAGE
     float *sW = reinterpret_cast<float *>(sB + kTcStages * STAGE);  // kTcStages x 128 w values
-    __shared__ __align__(8) uint64_t bar_a, full[kTcStages], empty[kTcStages], tfull[2], tempty[2];
+    __shared__ __align__(8) uint64_t full[kTcStages], empty[kTcStages], tfull[2], tempty[2], afull[2], aempty[2];
     __shared__ uint32_t tmem_base;
 
     if (A.stop && *(volatile const int *)A.stop) return;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-
-    const int s = blockIdx.y;
-    const int bq = s / A.split_q, u = s % A.split_q;
+    const int nsplit = A.nblk * A.split_q;
+    const int items = A.ptiles * nsplit;
     const int bt = A.blk_tiles > 0 ? A.blk_tiles : A.Qtiles;
-    const int base = bq * bt;
-    const int nt_b = max(0, min(bt, A.Qtiles - base));
-    const int t0 = base + (int)((long long)nt_b * u / A.split_q);
-    const int nt = base + (int)((long long)nt_b * (u + 1) / A.split_q) - t0;
+    // B tile range [t0, t0 + nt) of split s (fixed partition: block s / split_q, sub-split s % split_q)
+    auto range = [&](int s, int &t0, int &nt) {
+        const int bq = s / A.split_q, u = s % A.split_q;
+        const int base = bq * bt;
+        const int nt_b = max(0, min(bt, A.Qtiles - base));
+        t0 = base + (int)((long long)nt_b * u / A.split_q);
+        nt = base + (int)((long long)nt_b * (u + 1) / A.split_q) - t0;
+    };
 
     if (threadIdx.x == 0) {
-        mbar_init(&bar_a, 1);
         for (int i = 0; i < kTcStages; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1 + kTcEpiWarps); }
-        for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], kTcEpiWarps); }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&tfull[i], 1); mbar_init(&tempty[i], kTcEpiWarps);
+            mbar_init(&afull[i], 1); mbar_init(&aempty[i], 1);
+        }
         fence_mbar_init();
     }
-    if (warp == 1) {  // 256 TMEM columns: two 128x128 fp32 accumulators
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(&tmem_base)));
+    if (warp == 1) {  // 512 TMEM columns: accumulator (buffer b, A tile a) at column (2b + a) * 128
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tbase = tmem_base;
+    const long long clk0 = clock64();
 
     if (warp == 0) {
         if (lane == 0) {
-            // A images (the CTA's own points), then the B ring
-            mbar_expect_tx(&bar_a, 2 * IMG);
-            bulk_g2s(sA, reinterpret_cast<const char *>(A.Aimg) + (long long)blockIdx.x * 2 * IMG, 2 * IMG, &bar_a);
-            for (int i = 0; i < nt; ++i) {
-                const int st = i % kTcStages;
-                if (i >= kTcStages) mbar_wait(&empty[st], ((i / kTcStages) - 1) & 1);
-                unsigned char *dst = sB + st * STAGE;
-                mbar_expect_tx(&full[st], STAGE + kTcM * 4);
-                bulk_g2s(dst, reinterpret_cast<const char *>(A.Bimg) + (long long)(t0 + i) * 2 * IMG, 2 * IMG,
-                         &full[st]);
-                bulk_g2s(sW + st * kTcM, A.Bw + (long long)(t0 + i) * kTcM, kTcM * 4, &full[st]);
+            int g = 0, c = 0;
+            for (int it = blockIdx.x; it < items; it += gridDim.x, ++c) {
+                const int s = it / A.ptiles, pt = it % A.ptiles;
+                int t0, nt;
+                range(s, t0, nt);
+                const int ab = c % ABUF;
+                if (c >= ABUF) mbar_wait_sleep(&aempty[ab], ((c / ABUF) - 1) & 1);
+                mbar_expect_tx(&afull[ab], 4 * kTcImg);
+                bulk_g2s(sA + ab * 4 * kTcImg, A.Aimg + (long long)pt * 4 * kTcImg, 4 * kTcImg, &afull[ab]);
+                for (int i = 0; i < nt; ++i, ++g) {
+                    const int st = g % kTcStages;
+                    if (g >= kTcStages) mbar_wait_sleep(&empty[st], ((g / kTcStages) - 1) & 1);
+                    if (A.mma_only == 2 && g >= kTcStages) {   // K14 probe: MMA rate without the B stream
+                        mbar_arrive(&full[st]);
+                        continue;
+                    }
+                    unsigned char *dst = sB + st * STAGE;
+                    mbar_expect_tx(&full[st], STAGE + kTcM * 4);
+                    bulk_g2s(dst, A.Bimg + (long long)(t0 + i) * 2 * kTcImg, 2 * kTcImg, &full[st]);
+                    bulk_g2s(sW + st * kTcM, A.Bw + (long long)(t0 + i) * kTcM, kTcM * 4, &full[st]);
+                }
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {
-            mbar_wait(&bar_a, 0);
-            const uint32_t a_hi = smem_u32(sA), a_lo = a_hi + IMG;
-            for (int i = 0; i < nt; ++i) {
-                const int st = i % kTcStages, b = i & 1;
-                mbar_wait(&full[st], (i / kTcStages) & 1);
-                if (i >= 2) mbar_wait(&tempty[b], ((i >> 1) - 1) & 1);
-                tc_fence_after();
-                const uint32_t b_hi = smem_u32(sB + st * STAGE), b_lo = b_hi + IMG;
-                const uint32_t d = tbase + (uint32_t)(b * kTcM);
+            const int ks = A.ksteps;
+            int g = 0, c = 0;
+            for (int it = blockIdx.x; it < items; it += gridDim.x, ++c) {
+                int t0, nt;
+                range(it / A.ptiles, t0, nt);
+                const int ab = c % ABUF;
+                mbar_wait(&afull[ab], (c / ABUF) & 1);
+                for (int i = 0; i < nt; ++i, ++g) {
+                    const int st = g % kTcStages, b = g & 1;
+                    mbar_wait(&full[st], (g / kTcStages) & 1);
+                    if (g >= 2) mbar_wait(&tempty[b], ((g >> 1) - 1) & 1);
+                    tc_fence_after();
+                    const uint32_t b_hi = smem_u32(sB + st * STAGE), b_lo = b_hi + kTcImg;
 #pragma unroll
-                for (int k = 0; k < KSTEPS; ++k) {
-                    const uint32_t koff = (uint32_t)((k >> 2) * 16 * 1024 + (k & 3) * 32);
-                    umma_tf32(d, umma_desc_sw128(a_lo + koff), umma_desc_sw128(b_hi + koff), k > 0);
-                    umma_tf32(d, umma_desc_sw128(a_hi + koff), umma_desc_sw128(b_lo + koff), 1);
+                    for (int a = 0; a < 2; ++a) {
+                        const uint32_t a_hi = smem_u32(sA + (ab * 2 + a) * 2 * kTcImg), a_lo = a_hi + kTcImg;
+                        const uint32_t d = tbase + (uint32_t)((2 * b + a) * kTcM);
+                        for (int k = 0; k < ks; ++k) {   // K = 16 halves = 32 bytes per step
+                            const uint32_t koff = (uint32_t)k * 32;
+                            umma_f16(d, umma_desc_sw128(a_lo + koff), umma_desc_sw128(b_hi + koff), k > 0);
+                            umma_f16(d, umma_desc_sw128(a_hi + koff), umma_desc_sw128(b_lo + koff), 1);
+                        }
+                        for (int k = 0; k < ks; ++k) {
+                            const uint32_t koff = (uint32_t)k * 32;
+                            umma_f16(d, umma_desc_sw128(a_hi + koff), umma_desc_sw128(b_hi + koff), 1);
+                        }
+                    }
+                    umma_commit(&empty[st]);   // smem slot free once these MMAs retire
+                    umma_commit(&tfull[b]);    // accumulators (b, 0) and (b, 1) ready
                 }
-#pragma unroll
-                for (int k = 0; k < KSTEPS; ++k) {
-                    const uint32_t koff = (uint32_t)((k >> 2) * 16 * 1024 + (k & 3) * 32);
-                    umma_tf32(d, umma_desc_sw128(a_hi + koff), umma_desc_sw128(b_hi + koff), 1);
-                }
-                umma_commit(&empty[st]);   // smem slot free once these MMAs retire
-                umma_commit(&tfull[b]);    // accumulator b ready
+                umma_commit(&aempty[ab]);      // A buffer free once the item's MMAs retire
             }
         }
     } else {
-        // epilogue: warp w reads TMEM lanes 32*(w%4) .. +31 (its quadrant) and the column half
-        // h = (w-2)/4 of every accumulator; thread = one output point, (M, S) over its half.
-        const int q4 = warp & 3, h = (warp - 2) >> 2;
+        // epilogue: warp w reads TMEM lanes 32*(w%4) .. +31 (its quadrant) of A tile
+        // a = (w-2)/4; thread = one output point, (M, S) over all columns of the item.
+        const int q4 = warp & 3, a = (warp - 2) >> 2;
         const int row = q4 * 32 + lane;
-        const int p = blockIdx.x * kTcM + row;
-        float M = -INFINITY, S = 0.f;
-        for (int i = 0; i < nt; ++i) {
-            const int st = i % kTcStages, b = i & 1;
-            mbar_wait(&tfull[b], (i >> 1) & 1);
-            tc_fence_after();
-            if (A.mma_only) {
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) { mbar_arrive(&tempty[b]); mbar_arrive(&empty[st]); }
-                continue;
+        const float tks = ldexpf(A.tk, tc_scale_exp(A.amax_p) + tc_scale_exp(A.amax_q));
+        const float2 tk2 = make_float2(tks, tks);
+        const float us = ldexpf(1.f, tc_scale_exp(A.amax_p) + tc_scale_exp(A.amax_q));  // exact unscale
+        int g = 0;
+        for (int it = blockIdx.x; it < items; it += gridDim.x) {
+            const int s = it / A.ptiles, pt = it % A.ptiles;
+            int t0, nt;
+            range(s, t0, nt);
+            const int p = pt * (2 * kTcM) + a * kTcM + row;
+            const bool dbg = A.debug_acc && a == 0 && it == 0;
+            float M = -INFINITY, S = 0.f;
+            for (int i = 0; i < nt; ++i, ++g) {
+                const int st = g % kTcStages, b = g & 1;
+                mbar_wait_sleep(&tfull[b], (g >> 1) & 1);
+                tc_fence_after();
+                if (A.mma_only) {
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) { mbar_arrive(&tempty[b]); mbar_arrive(&empty[st]); }
+                    continue;
+                }
+                const uint32_t taddr = tbase + ((uint32_t)(q4 * 32) << 16) + (uint32_t)((2 * b + a) * kTcM);
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {   // two 64-column chunks
+                    const float2 *w = reinterpret_cast<const float2 *>(sW + st * kTcM + h * 64);
+                    uint32_t r[64];
+                    TMEM_LD32(taddr + h * 64, r);
+                    TMEM_LD32(taddr + h * 64 + 32, (r + 32));
+                    tmem_ld_wait();
+                    if (dbg && i == 0) {
+#pragma unroll
+                        for (int j = 0; j < 64; ++j) A.debug_acc[row * kTcM + h * 64 + j] = __uint_as_float(r[j]) * us;
+                    }
+                    float2 t[32];
+#pragma unroll
+                    for (int j = 0; j < 32; ++j)
+                        t[j] = fma2(make_float2(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1])), tk2, w[j]);
+                    if (h == 1) {
+                        // accumulators of buffer b and the w slot are no longer needed: release them early
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) { mbar_arrive(&tempty[b]); mbar_arrive(&empty[st]); }
+                    }
+                    float m8[8];
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        m8[j] = fmax3(fmaxf(t[4 * j].x, t[4 * j].y), fmax3(t[4 * j + 1].x, t[4 * j + 1].y, t[4 * j + 2].x),
+                                      fmax3(t[4 * j + 2].y, t[4 * j + 3].x, t[4 * j + 3].y));
+                    const float cm = fmax3(fmax3(m8[0], m8[1], m8[2]), fmax3(m8[3], m8[4], m8[5]), fmaxf(m8[6], m8[7]));
+                    if (cm > M) { S *= ex2(M - cm); M = cm; }
+                    if (M == -INFINITY) continue;  // only padding seen so far (ragged last tile's upper half)
+                    const float2 sc = tc_sum_chunk<EMU>(t, M);
+                    S += sc.x + sc.y;
+                }
             }
-            const float *w = sW + st * kTcM + h * 64;
-            uint32_t r[64];
-            const uint32_t taddr = tbase + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(b * kTcM + h * 64);
-            TMEM_LD32(taddr, r);
-            TMEM_LD32(taddr + 32, (r + 32));
-            tmem_ld_wait();
-            if (A.debug_acc && i == 0 && blockIdx.x == 0 && blockIdx.y == 0) {
-#pragma unroll
-                for (int j = 0; j < 64; ++j) A.debug_acc[row * kTcM + h * 64 + j] = __uint_as_float(r[j]);
-            }
-            float t[64];
-#pragma unroll
-            for (int j = 0; j < 64; ++j) t[j] = fmaf(__uint_as_float(r[j]), A.tk, w[j]);
-            // accumulator b and the w slot are no longer needed: release them early
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) { mbar_arrive(&tempty[b]); mbar_arrive(&empty[st]); }
-            float cm = t[0];
-#pragma unroll
-            for (int j = 1; j < 64; ++j) cm = fmaxf(cm, t[j]);
-            if (cm > M) { S *= ex2(M - cm); M = cm; }
-            if (M == -INFINITY) continue;  // only padding seen so far (ragged last tile's upper half)
-            float s0 = 0.f, s1 = 0.f;
-#pragma unroll
-            for (int j = 0; j < 64; j += 2) { s0 += ex2(t[j] - M); s1 += ex2(t[j + 1] - M); }
-            S += s0 + s1;
-        }
-        // combine the two column halves of each row (fixed order: half 0 then half 1)
-        float2 *xch = reinterpret_cast<float2 *>(sW + kTcStages * kTcM);  // 128 x float2
-        if (h == 1) xch[row] = make_float2(M, S);
-        asm volatile("bar.sync 1, %0;" ::"r"(32 * kTcEpiWarps));
-        if (h == 0) {
-            const float2 o = xch[row];
-            lse_merge(M, S, o.x, o.y);
-            if (p < A.P) A.part[(long long)s * A.P + p] = make_float2(M, S);
+            if (p < A.P && !A.mma_only) A.part[(long long)s * A.P + p] = make_float2(M, S);
         }
     }
     tc_fence_before();
     __syncthreads();
+    if (A.cyc && blockIdx.x == 0 && threadIdx.x == 0) *A.cyc = clock64() - clk0;
     if (warp == 1) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tbase));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tbase));
     }
 }
 
-// --------------------------------------------------------------------- host side
-size_t tc_image_floats(long long P, int katoms) {
-    return (size_t)((P + kTcM - 1) / kTcM) * 2 * tc_img_bytes(katoms) / 4;
+// ------------------------------------------------------------- K14 MMA probe
+// Raw tcgen05.mma issue rate of one shape (M = 128, N, K = 32 bytes, SS operands on smem
+// garbage), one CTA per SM, groups of 12 MMAs into alternating accumulators, at most two
+// groups in flight.  Writes the SM cycles of CTA 0 (clock64) to cyc.  mode bits (diagnosis of
+// the K3 loop): 1 = operands alternate between two A and two B images (hi/lo pattern);
+// 2 = 24 MMAs per group into two accumulators; 4 = 8 extra warps wait on every group's
+// completion barrier (as K3's epilogue warps do); 8 = they wait with a suspend-time hint.
+template <int N, int TF32>
+__global__ void __launch_bounds__(320, 1) k_mb_mma(int groups, int mode, long long *cyc) {
+    extern __shared__ __align__(1024) unsigned char smraw[];
+    unsigned char *sm = smraw + ((1024 - (smem_u32(smraw) & 1023)) & 1023);
+    __shared__ __align__(8) uint64_t done[2];
+    __shared__ uint32_t tmem_base;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) { mbar_init(&done[0], 1); mbar_init(&done[1], 1); fence_mbar_init(); }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tb = tmem_base;
+    constexpr uint32_t idesc = (1u << 4) | (TF32 ? ((2u << 7) | (2u << 10)) : 0u) | ((uint32_t)(N >> 3) << 17) |
+                               ((uint32_t)(128 >> 4) << 24);
+    const int per = (mode & 2) ? 24 : 12;
+    long long c0 = clock64();
+    if (warp == 0 && lane == 0) {
+        const uint32_t a = smem_u32(sm), b = a + 32768;
+        for (int g = 0; g < groups; ++g) {
+            const int buf = g & 1;
+            if (g >= 2) mbar_wait(&done[buf], ((g >> 1) - 1) & 1);
+            tc_fence_after();
+            for (int k = 0; k < per; ++k) {
+                const uint32_t d = tb + (uint32_t)(buf * 2 * 128 + ((mode & 2) && k >= 12 ? 128 : 0));
+                const uint32_t ko = (uint32_t)(k & 3) * 32;
+                const uint32_t ao = (mode & 1) ? (uint32_t)((k & 1) * 16384) : 0u;
+                const uint32_t bo = (mode & 1) ? (uint32_t)(((k >> 1) & 1) * 16384) : 0u;
+                const uint64_t ad = umma_desc_sw128(a + ao + ko), bd = umma_desc_sw128(b + bo + ko);
+                if constexpr (TF32)
+                    asm volatile(
+                        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+                        "l"(ad), "l"(bd), "r"(idesc), "r"((k % 12) > 0 ? 1 : 0));
+                else
+                    asm volatile(
+                        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+                        "l"(ad), "l"(bd), "r"(idesc), "r"((k % 12) > 0 ? 1 : 0));
+            }
+            umma_commit(&done[buf]);
+        }
+        for (int g = groups - 2 > 0 ? groups - 2 : 0; g < groups; ++g) mbar_wait(&done[g & 1], (g >> 1) & 1);
+    } else if (warp >= 2 && (mode & 4)) {
+        for (int g = 0; g < groups; ++g) {
+            if (mode & 8) mbar_wait_sleep(&done[g & 1], (g >> 1) & 1);
+            else mbar_wait(&done[g & 1], (g >> 1) & 1);
+        }
+    }
+    __syncthreads();
+    long long c1 = clock64();
+    if (blockIdx.x == 0 && threadIdx.x == 0) *cyc = c1 - c0;
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tb));
 }
 
-cudaError_t launch_pack_tc(const float *pts, long long P, int d, int katoms, float *img, cudaStream_t st) {
-    const long long total = ((P + kTcM - 1) / kTcM) * kTcM * 32LL * katoms;
-    long long b = (total + 255) / 256;
-    k_pack_tc<<<(int)(b > 148 * 16 ? 148 * 16 : b), 256, 0, st>>>(pts, P, d, katoms, img);
-    return cudaGetLastError();
-}
-
-template <int KATOMS>
-static cudaError_t launch_tc_k(const TcArgs &A, int ptiles, int nsplit, cudaStream_t st) {
-    const size_t smem = 1024 + 2 * (size_t)tc_img_bytes(KATOMS) + kTcStages * (2 * (size_t)tc_img_bytes(KATOMS) + kTcM * 4)
-                        + kTcM * 8;   // half-combination exchange
-    cudaError_t e = cudaFuncSetAttribute(k_lse_tc<KATOMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+// flops per SM clock of the probe shape (kind & 3 -> 0: f16 N=128, 1: f16 N=256, 2: tf32 N=128,
+// 3: tf32 N=256; kind >> 2 = mode bits)
+cudaError_t microbench_mma(int kind, void *scratch, cudaStream_t st, double *flop_per_clk) {
+    const int groups = 4096;
+    const int mode = kind >> 2;
+    long long *cyc = (long long *)scratch;
+    const size_t smem = 1024 + 65536;
+    int nsm = 148, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    int N = 128, kk = 16;
+#define SK_MMA_PROBE(NN, TF)                                                                              \
+    {                                                                                                     \
+        cudaError_t e = cudaFuncSetAttribute(k_mb_mma<NN, TF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+        if (e != cudaSuccess) return e;                                                                   \
+        k_mb_mma<NN, TF><<<nsm, 320, smem, st>>>(64, mode, cyc);                                          \
+        k_mb_mma<NN, TF><<<nsm, 320, smem, st>>>(groups, mode, cyc);                                      \
+        N = NN; kk = TF ? 8 : 16;                                                                         \
+    }
+    switch (kind & 3) {
+        case 0: SK_MMA_PROBE(128, 0); break;
+        case 1: SK_MMA_PROBE(256, 0); break;
+        case 2: SK_MMA_PROBE(128, 1); break;
+        default: SK_MMA_PROBE(256, 1); break;
+    }
+#undef SK_MMA_PROBE
+    long long c = 0;
+    cudaError_t e = cudaMemcpyAsync(&c, cyc, sizeof c, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return e;
-    dim3 grid(ptiles, nsplit);
-    k_lse_tc<KATOMS><<<grid, kTcThreads, smem, st>>>(A);
+    *flop_per_clk = 2.0 * 128 * N * kk * ((mode & 2) ? 24.0 : 12.0) * groups / (double)(c > 0 ? c : 1);
     return cudaGetLastError();
 }
+
+// --------------------------------------------------------------------- host side
+// images are allocated in pairs of 128-point tiles (a CTA's A operand is 256 points)
+size_t tc_image_bytes(long long P) { return (size_t)((P + 2 * kTcM - 1) / (2 * kTcM)) * 2 * 2 * kTcImg; }
+
+cudaError_t launch_absmax(const float *pts, long long cnt, unsigned *out, cudaStream_t st) {
+    long long b = (cnt + 255) / 256;
+    k_absmax<<<(int)(b > 148 * 8 ? 148 * 8 : (b < 1 ? 1 : b)), 256, 0, st>>>(pts, cnt, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pack_tc(const float *pts, long long P, int d, const unsigned *amax, void *img, cudaStream_t st) {
+    const long long P2 = (P + 2 * kTcM - 1) / (2 * kTcM) * (2 * kTcM);   // zero images up to the pair
+    const long long total = P2 * 8LL;
+    long long b = (total + 255) / 256;
+    k_pack_tc<<<(int)(b > 148 * 16 ? 148 * 16 : b), 256, 0, st>>>(pts, P, P2, d, amax, (unsigned char *)img);
+    return cudaGetLastError();
+}
+
+template <int EMU, int ABUF>
+static cudaError_t launch_tc_v(const TcArgs &A, dim3 grid, cudaStream_t st) {
+    const size_t smem = 1024 + ABUF * 4 * (size_t)kTcImg + tc_stages(ABUF) * (2 * (size_t)kTcImg + kTcM * 4);
+    cudaError_t e = cudaFuncSetAttribute(k_lse_tc<EMU, ABUF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k_lse_tc<EMU, ABUF><<<grid, kTcThreads, smem, st>>>(A);
+    return cudaGetLastError();
+}
+
+template <int EMU>
+static cudaError_t launch_tc_emu(const TcArgs &A, dim3 grid, cudaStream_t st) {
+    // SK_TC_ABUF: 2 = double-buffered A (next item's A loads under the current item), 2-deep B
+    // ring; 1 = single A buffer, 4-deep B ring
+    static const int abuf = [] { const char *e = getenv("SK_TC_ABUF"); return e ? atoi(e) : 2; }();
+    return abuf == 1 ? launch_tc_v<EMU, 1>(A, grid, st) : launch_tc_v<EMU, 2>(A, grid, st);
+}
+
+int tc_points_per_cta() { return 2 * kTcM; }
 
 cudaError_t launch_lse_tc(const TcPass &L, cudaStream_t st) {
     TcArgs A;
-    A.Aimg = L.Aimg; A.Bimg = L.Bimg; A.Bw = L.Bw;
-    A.P = L.P; A.Qtiles = (int)((L.Q + kTcM - 1) / kTcM);
+    A.Aimg = (const unsigned char *)L.Aimg; A.Bimg = (const unsigned char *)L.Bimg; A.Bw = L.Bw;
+    A.amax_p = L.amax_p; A.amax_q = L.amax_q;
+    A.P = L.P; A.Qtiles = (int)((L.Q + kTcM - 1) / kTcM); A.ksteps = L.ksteps;
     A.blk_tiles = L.blk_tiles; A.split_q = L.split_q;
     A.part = L.part; A.tk = 2.f * kLog2e / L.eps; A.stop = L.stop; A.debug_acc = L.debug_acc;
     A.mma_only = L.mma_only;
-    const int ptiles = (L.P + kTcM - 1) / kTcM;
-    const int nsplit = L.nblk * L.split_q;
-    return L.katoms == 1 ? launch_tc_k<1>(A, ptiles, nsplit, st) : launch_tc_k<2>(A, ptiles, nsplit, st);
+    A.cyc = L.cyc;
+    if (A.ksteps < 1 || A.ksteps > 4) return cudaErrorInvalidValue;
+    A.ptiles = (L.P + 2 * kTcM - 1) / (2 * kTcM);
+    A.nblk = L.nblk;
+    const int items = A.ptiles * L.nblk * L.split_q;
+    int nsm = 148, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    dim3 grid(items < nsm ? items : nsm);
+    // fraction of the exponentials evaluated on the FMA pipe (of every 8 pairs); SK_TC_EMU overrides
+    static const int emu = [] { const char *e = getenv("SK_TC_EMU"); return e ? atoi(e) : 2; }();
+    switch (emu) {
+        case 0: return launch_tc_emu<0>(A, grid, st);
+        case 1: return launch_tc_emu<1>(A, grid, st);
+        case 3: return launch_tc_emu<3>(A, grid, st);
+        default: return launch_tc_emu<2>(A, grid, st);
+    }
 }
 
 }  // namespace sk

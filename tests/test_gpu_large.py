@@ -45,7 +45,7 @@ def _row_marginals(x, y, f, g, eps, rows, chunk=64):
 
 
 # ------------------------------------------------------------------ sharding
-@pytest.mark.parametrize("mode,n,m,d", [("online", 6000, 3000, 3), ("stored", 6100, 2048, 16)])
+@pytest.mark.parametrize("mode,n,m,d", [("online", 6000, 3000, 3), ("stored", 6100, 2048, 16), ("online", 6000, 2100, 40)])
 def test_sharded_bit_identical_across_world_sizes(O, ctx, mode, n, m, d):
     import paper_2206_07630_b200 as sk
     rng = np.random.default_rng(n + d)

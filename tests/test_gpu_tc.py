@@ -1,4 +1,4 @@
-"""Tensor-core (tcgen05 3xTF32) cross term, -m gpu: the raw 128x128 tile product against fp64,
+"""Tensor-core (tcgen05 kind::f16, 3-product hi/lo split) cross term, -m gpu: the raw 128x128 tile product against fp64,
 and the d > 16 solve through the tensor-core pass against the oracle and the FFMA kernel."""
 import os
 import subprocess
@@ -20,13 +20,15 @@ def ctx():
     return sk.Context(0)
 
 
-@pytest.mark.parametrize("d", [64, 48, 33, 32, 20, 3])
-def test_tc_tile_product_is_fp32_accurate(ctx, d):
+@pytest.mark.parametrize("d,sx,sy", [(64, 1, 1), (48, 1, 1), (33, 1, 1), (32, 1, 1), (20, 1, 1), (3, 1, 1),
+                                     (64, 1e4, 1e-3), (40, 3e-6, 7e5), (64, 1e30, 1e-30)])
+def test_tc_tile_product_is_fp32_accurate(ctx, d, sx, sy):
+    """Any magnitude: the operands are scaled by exact powers of two before the fp16 split."""
     import ctypes
     import paper_2206_07630_b200 as sk
     rng = np.random.default_rng(d)
-    x = rng.standard_normal((128, d)).astype(np.float32)
-    y = rng.standard_normal((128, d)).astype(np.float32)
+    x = (rng.standard_normal((128, d)) * sx).astype(np.float32)
+    y = (rng.standard_normal((128, d)) * sy).astype(np.float32)
     out = torch.empty((128, 128), dtype=torch.float32, device="cuda")
     xd, yd = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
     ctx.check(ctx.lib.sk_selftest_tc_dot(ctx.h, d, ctypes.c_void_p(xd.data_ptr()), ctypes.c_void_p(yd.data_ptr()),
@@ -34,7 +36,7 @@ def test_tc_tile_product_is_fp32_accurate(ctx, d):
     ref = x.astype(np.float64) @ y.astype(np.float64).T
     scale = np.abs(x).astype(np.float64) @ np.abs(y).astype(np.float64).T
     err = np.abs(out.cpu().numpy() - ref) / scale
-    # 3xTF32: ~2^-22 relative to sum |x_k y_k| (1xTF32 would be ~2^-11)
+    # hi/lo fp16 split, 3 products: ~2^-22 relative to sum |x_k y_k| (one fp16 product: ~2^-11)
     assert err.max() < 4e-6, err.max()
 
 
