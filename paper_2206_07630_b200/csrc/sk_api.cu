@@ -367,8 +367,11 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
     }
     Side Y{(int)m, P.d, D, tq, ypack, yc, ynk, {ypot, ypot + m}};
     // online FFMA path: per-point LSE seeds for the max-free (seeded) passes from sweep 3 on
+    // stored mode with the fused sweep (one persistent CTA per SM): 8 blocks x split_q = one wave
+    static const int fused_env = [] { const char *e = getenv("SK_FUSED"); return e ? atoi(e) : 1; }();
+    const bool fused = stored && fused_env != 0 && stored_fused_supported(m);
     const bool seedable = !stored && !tc;
-    if (seedable) {
+    if (seedable || fused) {   // (the fused stored sweep seeds its row shifts the same way)
         ENSURE(xlse, float, B_XLSE, off[ns]);
         ENSURE(ylse, float, B_YLSE, m);
         for (int i = 0; i < ns; ++i) X[i].lse = xlse + off[i];
@@ -389,9 +392,6 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
     const int Rr = tc ? 1 : (D <= 4 ? 4 : (D <= 16 ? 2 : 1));
     const long long pcta = tc ? tc_points_per_cta() : 128LL * Rr;   // output points per CTA
     const long long ptiles_col = stored ? (m + 511) / 512 : (m + pcta - 1) / pcta;
-    // stored mode with the fused sweep (one persistent CTA per SM): 8 blocks x split_q = one wave
-    static const int fused_env = [] { const char *e = getenv("SK_FUSED"); return e ? atoi(e) : 1; }();
-    const bool fused = stored && fused_env != 0 && stored_fused_supported(m);
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device);
     const int split_q = fused ? std::max(1, nsm / SK_SHARD_BLOCKS)
@@ -445,13 +445,13 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
     // stored mode: one HBM read of C per sweep (fused row + column passes, H4s) when m fits
     bool first = true;
 
-    auto col_stage = [&]() -> sk_status {
+    auto col_stage = [&](const int *only_if) -> sk_status {
         for (int i = 0; i < ns; ++i) {
             const double ent = (double)slices[i].n * m;
             const int t0 = fused ? -1 : tm.start();   // fused: the dominant kernel is the sweep
             if (stored) {
                 StoredPass scol{C[i], slices[i].n, m, P.eps, X[i].pack, col_part(i), bs_rows,
-                                sharded ? blk_per_rank : nblk_glob, split_q, &status->stop};
+                                sharded ? blk_per_rank : nblk_glob, split_q, &status->stop, only_if};
                 CU(launch_stored_cols(scol, st));
             } else if (tc) {
                 TcPass colp{yimg, ximg + offi[i], X[i].pack, amax + 1, amax, (int)m, slices[i].n, ksteps,
@@ -468,12 +468,17 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
         }
         return SK_OK;
     };
-    auto exchange_and_merge_col = [&]() -> sk_status {
+    // the fused stored sweep's column partials are scaled sums (merge mode `scaled`); a column
+    // outside the safe range sets status->colfail and the column pass is redone exactly
+    MergePass mcol_scaled = mcol, mcol_redo = mcol;
+    mcol_scaled.scaled = 1;
+    mcol_redo.only_if = &status->colfail;
+    auto exchange_and_merge_col = [&](const MergePass &mp) -> sk_status {
         if (P.nccl && sharded) {
             int r = g_nccl.allgather(col_part(0), part, (size_t)slot * 2, kNcclFloat32, ctx->comm, st);
             if (r != 0) return fail(ctx, SK_ENCCL, "ncclAllGather failed: %s", g_nccl.errstr ? g_nccl.errstr(r) : "?");
         }
-        CU(launch_merge(mcol, st));
+        CU(launch_merge(mp, st));
         return SK_OK;
     };
 
@@ -485,15 +490,15 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
         for (int c = 0; c < chunk; ++c, ++it) {
             if (fused) {
                 if (first) {  // g^1 from f^0 with a plain column pass
-                    CK(col_stage());
-                    CK(exchange_and_merge_col());
+                    CK(col_stage(nullptr));
+                    CK(exchange_and_merge_col(mcol));
                     launched += ns + 1;
                     first = false;
                 }
                 for (int i = 0; i < ns; ++i) {
                     FusedLaunch fl{C[i], slices[i].n, m, P.eps, Y.pack, X[i].c, {X[i].pot[0], X[i].pot[1]},
-                                   X[i].pack, col_part(i), bs_rows, sharded ? blk_per_rank : nblk_glob, split_q,
-                                   status};
+                                   X[i].pack, X[i].lse, col_part(i), bs_rows, sharded ? blk_per_rank : nblk_glob,
+                                   split_q, status};
                     const int t0 = tm.start();
                     CU(launch_stored_fused(fl, st));
                     tm.stop(t0, sweep, LaunchTimer::FUSED, 2.0 * slices[i].n * m, 4.0 * slices[i].n * m);
@@ -502,13 +507,15 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
                     CU(launch_merge(mrow, st));
                     launched += 2;
                 }
-                CK(exchange_and_merge_col());
-                launched += 1;
+                CK(exchange_and_merge_col(mcol_scaled));
+                CK(col_stage(&status->colfail));           // no-ops unless colfail
+                CK(exchange_and_merge_col(mcol_redo));
+                launched += 2 + ns;
                 ++sweep;
                 continue;
             }
-            CK(col_stage());
-            CK(exchange_and_merge_col());
+            CK(col_stage(nullptr));
+            CK(exchange_and_merge_col(mcol));
             launched += ns + 1;
             for (int i = 0; i < ns; ++i) {
                 const int t0 = tm.start();

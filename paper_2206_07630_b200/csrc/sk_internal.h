@@ -40,6 +40,7 @@ struct DevStatus {
     float tol;
     double E;        // dual objective of the returned iterate
     double fa_local; // sharded: this rank's <f,a> - eps sum(a) partial
+    int colfail;     // stored fused sweep: some column sum left the scaled range -> exact column pass
 };
 
 // Packed tile layout of one side: tiles of tq points; tile t at t*(D+1)*tq floats:
@@ -120,6 +121,8 @@ struct MergePass {
     int no_iter_inc;          // MERGE_ROW of a non-final slice (emulated ranks): keep the counter
     int precomputed = 0;      // MERGE_ROW: potential and w already written (fused stored sweep)
     const Side *Q = nullptr;  // seeded passes: the reduced side, for the exact fallback
+    int scaled = 0;           // MERGE_COL of the fused stored sweep: partials are (-g kappa, A_j)
+    const int *only_if = nullptr;  // run only if *only_if != 0 (the exact column fallback)
 };
 cudaError_t launch_merge(const MergePass &M, cudaStream_t st);
 int merge_blocks(int P);
@@ -176,6 +179,7 @@ struct StoredPass {
     long long blk_rows;   // cols: rows per fixed block (0 = one block of all rows)
     int nblk, split_q;    // cols: blocks and sub-splits per block
     const int *stop;
+    const int *only_if = nullptr;   // cols: run only if *only_if != 0
 };
 cudaError_t launch_stored_rows(const StoredPass &S, cudaStream_t st);
 // Fused single-read sweep (H4s): f^{l+1} rows (written with their w) and the column partials
@@ -186,6 +190,7 @@ struct FusedLaunch {
     const float *gw, *xc;
     float *xpot[2];
     float *xw;
+    float *xlse;      // per-row LSE (log2 units) of the previous sweep: the row shift seed (-inf = none)
     float2 *part;
     long long blk_rows;
     int nblk, split_q;

@@ -266,6 +266,7 @@ __global__ void __launch_bounds__(kMT) k_merge(MergePass Mp, Side S) {
     __shared__ int s_last;
     DevStatus *st = Mp.st;
     if (st && *(volatile int *)&st->stop) return;
+    if (Mp.only_if && !*(volatile const int *)Mp.only_if) return;
     const int l = st ? st->iter : 0;
     const float eps = Mp.eps, kap = kLog2e / eps, epsln2 = eps * kLn2;
     const bool check = Mp.mode == MERGE_COL && l >= 1 &&
@@ -290,6 +291,12 @@ __global__ void __launch_bounds__(kMT) k_merge(MergePass Mp, Side S) {
             // seeded pass: the fixed shift was far from the true maximum -> exact recompute of
             // this point over the whole reduced side (rare; one thread, online max)
             exact_lse_point(S, *Mp.Q, p, eps, M, Ssum);
+        }
+        if (Mp.scaled && !(Ssum >= 0x1p-100f && Ssum <= 0x1p100f)) {
+            // fused stored sweep: the scaled column mass left the safe range -> the whole
+            // column pass is redone exactly (k_cols + this merge, gated on st->colfail)
+            bad |= 2;
+            continue;
         }
         const float lse2 = M + log2f(Ssum);
         if (S.lse) S.lse[p] = lse2;
@@ -336,6 +343,8 @@ __global__ void __launch_bounds__(kMT) k_merge(MergePass Mp, Side S) {
     }
     if (Mp.mode == MERGE_COL) {
         st->ticket_col = 0;
+        if (bt & 2) { st->colfail = 1; __threadfence(); return; }   // decisions left to the exact redo
+        if (Mp.only_if) st->colfail = 0;
         // sharded: f^l may be the non-finite one (rows are not checked locally), so fall back
         // to (f^{l-1}, g^{l-1}), both finite.
         if (bt) { st->nonfinite = 1; st->stop = 1; st->final_iter = Mp.sharded ? max(l - 1, 0) : l; }

@@ -10,6 +10,8 @@
 //                    the rows; partials (max, sum) per column and split.
 // Both feed the same merge kernel (K6) as the online path (the stored side has
 // D = 0 and no |p|^2 folding).  Each pass reads C once: 4nm bytes per launch.
+#include <algorithm>
+
 #include "sk_internal.h"
 #include "sk_common.cuh"
 
@@ -133,6 +135,7 @@ cudaError_t launch_stored_rows(const StoredPass &S, cudaStream_t st) {
 constexpr int kCT = 128;  // threads; 4 columns each -> 512 columns per CTA
 __global__ void __launch_bounds__(kCT) k_cols(StoredPass S) {
     if (S.stop && *(volatile const int *)S.stop) return;
+    if (S.only_if && !*(volatile const int *)S.only_if) return;
     const long long j0 = ((long long)blockIdx.x * kCT + threadIdx.x) * 4;
     const int s = blockIdx.y;
     const int bq = s / S.split_q, u = s % S.split_q;
@@ -203,17 +206,28 @@ cudaError_t launch_stored_cols(const StoredPass &S, cudaStream_t st) {
 namespace sk {
 
 // ------------------------------------------------------------------ K5 fused
-// One HBM read of C per sweep.  CTA s owns the rows of split s (same
-// fixed block structure as k_cols) and, in registers, the (max, sum) state of every column:
-// thread t owns the float4 groups t, t + 512, ... (CPT columns).  Per group of 4 rows:
-//   phase A  warps 4r..4r+3 stream row r (a quarter each) from HBM: exact online
-//            (max, sum) of t = g_j log2(e)/eps - C_ij log2(e)/eps, combined in fixed order
-//            -> f_i = eps log a_i - eps ln2 (M + log2 S) (Alg. 1 l.4), written with its w;
-//   phase B  every thread re-reads its columns of the 4 rows (L2 hits: the group was
-//            bulk-prefetched into L2 one group ahead) and updates the column state with
-//            t = f_i log2(e)/eps - C_ij log2(e)/eps (the partials of g^{l+2}, Alg. 1 l.5).
-// Deterministic: fixed per-row quarter order, per-column sequential row order.
+// One HBM read of C per sweep, one exponential per cost entry.
+// CTA s owns the rows of split s (same fixed block structure as k_cols); thread t owns the
+// columns of float4 groups t, t + 512, ... (CPT columns) in both phases, so every value it
+// needs stays in registers.  Rows stream HBM -> shared memory through a ring of whole-row
+// buffers (1D bulk TMA, mbarrier complete_tx), refilled as soon as a row is in registers.
+// Per row i (log2 units, kappa = log2(e)/eps, t_ij = g_j kappa - C_ij kappa):
+//   row:    e_ij = 2^(t_ij - sigma_i), S_i = sum_j e_ij (fixed reduction tree), with the shift
+//           sigma_i = the row's previous LSE + 4 (validated: S_i in [2^-100, 2^100]; otherwise,
+//           and in the first sweep, the exact row maximum);  lse_i = sigma_i + log2 S_i,
+//           f_i = eps log a_i - eps ln2 lse_i (Alg. 1 l.4), w_i = f_i kappa;
+//   column: the next g-update needs sum_i 2^((f_i - C_ij) kappa)
+//             = 2^(-g_j kappa) sum_i e_ij 2^(sigma_i + w_i)          (the Sinkhorn scaling
+//           identity P = diag(u) K diag(v)), so A_j += e_ij v_i with v_i = 2^(sigma_i + w_i),
+//           the same exponential serving both passes.  sum_j A_j = sum_i a_i, so A_j cannot
+//           overflow; a column whose total mass leaves [2^-100, 2^100] (an unmatched column
+//           early in a solve) is caught by the merge, which redoes the column pass exactly.
+// Output partial (M, S) = (-g_j kappa, A_j) for the standard merge (all M equal).
+// Deterministic: fixed reduction tree per row, sequential row order per column.
 constexpr int kFT = 512;
+constexpr int kFW = kFT / 32;            // warps
+constexpr int kFRingBytes = 3 * 65536;   // row ring (3 rows of m = 16384)
+constexpr float kFusedSeedMargin = 4.f;
 
 struct FusedArgs {
     const float *C; long long n, m;
@@ -222,23 +236,31 @@ struct FusedArgs {
     const float *xc;        // eps log a_i (X side c), n
     float *xpot[2];         // X potential buffers (parity = iteration)
     float *xw;              // X side w pack (f log2(e)/eps), n
+    float *xlse;            // per-row LSE seeds (in/out), n
     float2 *part;           // column partials [nblk * split_q][m]
     long long blk_rows;
-    int split_q;
+    int split_q, stages;
     DevStatus *st;
 };
 
-__device__ __forceinline__ void prefetch_l2(const void *p, uint32_t bytes) {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+__device__ __forceinline__ float warp_sum_tree(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
 }
 
-constexpr int kFR = 2;                  // rows per group
-constexpr int kFWR = (kFT / 32) / kFR;  // warps per row in phase A (8)
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
 
 template <int CPT>
 __global__ void __launch_bounds__(kFT, 1) k_stored_fused(FusedArgs A) {
-    __shared__ float2 red[kFT / 32];
-    __shared__ float wrow[kFR];
+    constexpr int G = CPT / 4;                     // float4 groups per thread
+    extern __shared__ __align__(128) float ring[];   // stages x m floats
+    __shared__ __align__(8) uint64_t full[8];
+    __shared__ float red[2][kFW], redm[kFW];
     if (*(volatile const int *)&A.st->stop) return;
     const int l = A.st->iter;                      // producing f^{l+1}
     float *fnew = ((l + 1) & 1) ? A.xpot[1] : A.xpot[0];   // no dynamic param indexing
@@ -249,132 +271,147 @@ __global__ void __launch_bounds__(kFT, 1) k_stored_fused(FusedArgs A) {
     const long long bs = A.blk_rows > 0 ? A.blk_rows : A.n;
     const long long b0 = bq * bs, nb = max(0LL, min(bs, A.n - b0));
     const long long r0 = b0 + nb * u / A.split_q, r1 = b0 + nb * (u + 1) / A.split_q;
-    const long long m4 = A.m >> 2;
+    const int m = (int)A.m, m4 = m >> 2;
+    const int NS = A.stages;
+    const uint32_t rowb = (uint32_t)m * 4u;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NS; ++i) mbar_init(&full[i], 1);
+        fence_mbar_init();
+        for (int k = 0; k < NS && r0 + k < r1; ++k) {
+            mbar_expect_tx(&full[k], rowb);
+            bulk_g2s(ring + (size_t)k * m, A.C + (r0 + k) * A.m, rowb, &full[k]);
+        }
+    }
+    __syncthreads();
+
+    // this thread's columns: w_j = g_j kappa (-inf padding) and the column accumulators
+    float w[CPT], acc[CPT];
     const float4 *Gw = reinterpret_cast<const float4 *>(A.gw);
-
-    float cM[CPT], cS[CPT];
 #pragma unroll
-    for (int c = 0; c < CPT; ++c) { cM[c] = -INFINITY; cS[c] = 0.f; }
-
-    // L2 prefetch two groups ahead (the TMA engine streams HBM while the warps compute)
-    if (threadIdx.x == 0)
-        for (long long i = r0; i < min(r1, r0 + 2 * kFR); ++i) prefetch_l2(A.C + i * A.m, (uint32_t)(A.m * 4));
-
-    for (long long i0 = r0; i0 < r1; i0 += kFR) {
-        const int rows = (int)min((long long)kFR, r1 - i0);
-        if (threadIdx.x == 0)
-            for (long long i = i0 + 2 * kFR; i < min(r1, i0 + 3 * kFR); ++i)
-                prefetch_l2(A.C + i * A.m, (uint32_t)(A.m * 4));
-        // ---- phase A: row r = warp / kFWR, segment q = warp % kFWR (exact online LSE)
-        {
-            const int r = warp / kFWR, q = warp % kFWR;
-            float M = -INFINITY, S0 = 0.f, S1 = 0.f;
-            if (r < rows) {
-                const float4 *Cr = reinterpret_cast<const float4 *>(A.C + (i0 + r) * A.m);
-                const long long g0 = m4 * q / kFWR, g1 = m4 * (q + 1) / kFWR;
-                long long g = g0 + lane;
-                for (; g + 96 < g1; g += 128) {
-                    float4 c[4], w[4];
-#pragma unroll
-                    for (int v = 0; v < 4; ++v) c[v] = Cr[g + 32 * v];
-#pragma unroll
-                    for (int v = 0; v < 4; ++v) w[v] = __ldg(Gw + g + 32 * v);
-                    float t[16];
-#pragma unroll
-                    for (int v = 0; v < 4; ++v) {
-                        t[4 * v + 0] = fmaf(c[v].x, -kap, w[v].x); t[4 * v + 1] = fmaf(c[v].y, -kap, w[v].y);
-                        t[4 * v + 2] = fmaf(c[v].z, -kap, w[v].z); t[4 * v + 3] = fmaf(c[v].w, -kap, w[v].w);
-                    }
-                    float cm = t[0];
-#pragma unroll
-                    for (int v = 1; v < 16; ++v) cm = fmaxf(cm, t[v]);
-                    if (cm > M) { const float sc = ex2(M - cm); S0 *= sc; S1 *= sc; M = cm; }
-#pragma unroll
-                    for (int v = 0; v < 16; v += 2) { S0 += ex2(t[v] - M); S1 += ex2(t[v + 1] - M); }
-                }
-                for (; g < g1; g += 32) {
-                    const float4 c = Cr[g], w = __ldg(Gw + g);
-                    const float t0 = fmaf(c.x, -kap, w.x), t1 = fmaf(c.y, -kap, w.y),
-                                t2 = fmaf(c.z, -kap, w.z), t3 = fmaf(c.w, -kap, w.w);
-                    const float cm = fmaxf(fmaxf(t0, t1), fmaxf(t2, t3));
-                    if (cm > M) { const float sc = ex2(M - cm); S0 *= sc; S1 *= sc; M = cm; }
-                    S0 += ex2(t0 - M) + ex2(t2 - M);
-                    S1 += ex2(t1 - M) + ex2(t3 - M);
-                }
-            }
-            float Sv = S0 + S1;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                const float M2 = __shfl_xor_sync(0xffffffffu, M, o);
-                const float S2 = __shfl_xor_sync(0xffffffffu, Sv, o);
-                lse_merge(M, Sv, M2, S2);
-            }
-            if (lane == 0) red[warp] = make_float2(M, Sv);
-        }
-        __syncthreads();
-        if (threadIdx.x < rows) {
-            const int r = threadIdx.x;
-            float M = red[kFWR * r].x, Sv = red[kFWR * r].y;
-            for (int q = 1; q < kFWR; ++q) lse_merge(M, Sv, red[kFWR * r + q].x, red[kFWR * r + q].y);
-            const long long i = i0 + r;
-            const float fn = A.xc[i] - epsln2 * (M + log2f(Sv));
-            fnew[i] = fn;
-            const float wv = fn * kap;
-            A.xw[i] = wv;
-            wrow[r] = wv;
-        }
-        __syncthreads();
-        // ---- phase B: column state over the rows of this group (L2 / L1 re-read)
-        float wr[kFR];
-#pragma unroll
-        for (int r = 0; r < kFR; ++r) wr[r] = r < rows ? wrow[r] : -INFINITY;
-#pragma unroll
-        for (int k = 0; k < CPT / 4; ++k) {
-            const long long g = threadIdx.x + (long long)k * kFT;
-            if (g < m4) {
-                float t[4][kFR];
-#pragma unroll
-                for (int r = 0; r < kFR; ++r) {
-                    const long long rr = r < rows ? r : 0;   // duplicate row 0 as padding, masked by wr
-                    const float4 c = *reinterpret_cast<const float4 *>(A.C + (i0 + rr) * A.m + 4 * g);
-                    t[0][r] = fmaf(c.x, -kap, wr[r]); t[1][r] = fmaf(c.y, -kap, wr[r]);
-                    t[2][r] = fmaf(c.z, -kap, wr[r]); t[3][r] = fmaf(c.w, -kap, wr[r]);
-                }
-#pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    const float cm = fmaxf(t[c][0], t[c][1]);
-                    if (cm > cM[4 * k + c]) { cS[4 * k + c] *= ex2(cM[4 * k + c] - cm); cM[4 * k + c] = cm; }
-                    const float mm = cM[4 * k + c];
-                    cS[4 * k + c] += ex2(t[c][0] - mm) + ex2(t[c][1] - mm);
-                }
-            }
-        }
-        __syncthreads();   // red / wrow reuse
+    for (int q = 0; q < G; ++q) {
+        const int g = threadIdx.x + q * kFT;
+        const float4 v = g < m4 ? __ldg(Gw + g) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+        w[4 * q] = v.x; w[4 * q + 1] = v.y; w[4 * q + 2] = v.z; w[4 * q + 3] = v.w;
     }
 #pragma unroll
-    for (int k = 0; k < CPT / 4; ++k) {
-        const long long g = threadIdx.x + (long long)k * kFT;
+    for (int c = 0; c < CPT; ++c) acc[c] = 0.f;
+
+    for (long long i = r0; i < r1; ++i) {
+        const int k = (int)(i - r0);
+        const int st = k % NS;
+        const float4 *row4 = reinterpret_cast<const float4 *>(ring + (size_t)st * m);
+        const float seed = A.xlse[i];
+        mbar_wait(&full[st], (k / NS) & 1);
+        float t[CPT];
+#pragma unroll
+        for (int q = 0; q < G; ++q) {
+            const int g = threadIdx.x + q * kFT;
+            const float4 c = g < m4 ? row4[g] : make_float4(0.f, 0.f, 0.f, 0.f);
+            t[4 * q] = fmaf(c.x, -kap, w[4 * q]); t[4 * q + 1] = fmaf(c.y, -kap, w[4 * q + 1]);
+            t[4 * q + 2] = fmaf(c.z, -kap, w[4 * q + 2]); t[4 * q + 3] = fmaf(c.w, -kap, w[4 * q + 3]);
+        }
+        // ---- row LSE with a seeded shift (uniform decisions: every thread sees the same values)
+        float sig = seed + kFusedSeedMargin, S = 0.f;
+        bool exact = !isfinite(seed);
+        if (!exact) {
+            float p = 0.f;
+#pragma unroll
+            for (int c = 0; c < CPT; ++c) { t[c] = ex2(t[c] - sig); p += t[c]; }   // t now holds e
+            p = warp_sum_tree(p);
+            if (lane == 0) red[k & 1][warp] = p;
+            __syncthreads();
+#pragma unroll
+            for (int x = 0; x < kFW; ++x) S += red[k & 1][x];
+            exact = !(S >= 0x1p-100f && S <= 0x1p100f);
+            if (exact) {   // rare: rebuild t from the row (still in shared memory until refilled)
+#pragma unroll
+                for (int q = 0; q < G; ++q) {
+                    const int g = threadIdx.x + q * kFT;
+                    const float4 c = g < m4 ? row4[g] : make_float4(0.f, 0.f, 0.f, 0.f);
+                    t[4 * q] = fmaf(c.x, -kap, w[4 * q]); t[4 * q + 1] = fmaf(c.y, -kap, w[4 * q + 1]);
+                    t[4 * q + 2] = fmaf(c.z, -kap, w[4 * q + 2]); t[4 * q + 3] = fmaf(c.w, -kap, w[4 * q + 3]);
+                }
+            }
+        }
+        if (exact) {   // exact maximum as the shift (first sweep, or the seed was off)
+            float mx = -INFINITY;
+#pragma unroll
+            for (int c = 0; c < CPT; ++c) mx = fmaxf(mx, t[c]);
+            mx = warp_max(mx);
+            if (lane == 0) redm[warp] = mx;
+            __syncthreads();
+            sig = -INFINITY;
+#pragma unroll
+            for (int x = 0; x < kFW; ++x) sig = fmaxf(sig, redm[x]);
+            float p = 0.f;
+#pragma unroll
+            for (int c = 0; c < CPT; ++c) { t[c] = ex2(t[c] - sig); p += t[c]; }
+            p = warp_sum_tree(p);
+            if (lane == 0) red[k & 1][warp] = p;
+            __syncthreads();
+            S = 0.f;
+#pragma unroll
+            for (int x = 0; x < kFW; ++x) S += red[k & 1][x];
+        }
+        const float lse = sig + log2f(S);
+        const float fn = A.xc[i] - epsln2 * lse;
+        const float wv = fn * kap;
+        if (threadIdx.x == 0) {
+            fnew[i] = fn;
+            A.xw[i] = wv;
+            A.xlse[i] = lse;
+            // every thread has row i in registers (a barrier passed since): refill its slot
+            const long long nx = i + NS;
+            if (nx < r1) {
+                fence_proxy_async();
+                mbar_expect_tx(&full[st], rowb);
+                bulk_g2s(ring + (size_t)st * m, A.C + nx * A.m, rowb, &full[st]);
+            }
+        }
+        // ---- column partials with the same exponentials
+        const float v = ex2(sig + wv);
+#pragma unroll
+        for (int c = 0; c < CPT; ++c) acc[c] = fmaf(t[c], v, acc[c]);
+    }
+#pragma unroll
+    for (int q = 0; q < G; ++q) {
+        const int g = threadIdx.x + q * kFT;
         if (g < m4) {
 #pragma unroll
-            for (int c = 0; c < 4; ++c)
-                A.part[(long long)s * A.m + 4 * g + c] = make_float2(cM[4 * k + c], cS[4 * k + c]);
+            for (int e = 0; e < 4; ++e)
+                A.part[(long long)s * A.m + 4 * g + e] = make_float2(-w[4 * q + e], acc[4 * q + e]);
         }
     }
 }
 
-bool stored_fused_supported(long long m) { return m % 4 == 0 && m <= (long long)kFT * 32; }
+bool stored_fused_supported(long long m) { return m % 4 == 0 && m >= 4 && m <= (long long)kFT * 32; }
 
 cudaError_t launch_stored_fused(const FusedLaunch &L, cudaStream_t st) {
     FusedArgs A;
     A.C = L.C; A.n = L.n; A.m = L.m; A.eps = L.eps; A.gw = L.gw; A.xc = L.xc;
-    A.xpot[0] = L.xpot[0]; A.xpot[1] = L.xpot[1]; A.xw = L.xw; A.part = L.part;
+    A.xpot[0] = L.xpot[0]; A.xpot[1] = L.xpot[1]; A.xw = L.xw; A.xlse = L.xlse; A.part = L.part;
     A.blk_rows = L.blk_rows; A.split_q = L.split_q; A.st = L.st;
+    if (!stored_fused_supported(L.m) || !L.xlse) return cudaErrorInvalidValue;
+    // ring depth: as many whole rows as fit (2 .. 8)
+    const long long rb = L.m * 4;
+    A.stages = (int)std::min<long long>(8, kFRingBytes / rb);
+    const size_t smem = (size_t)A.stages * rb;
     const int grid = L.nblk * L.split_q;
     const long long cpt = (L.m / 4 + kFT - 1) / kFT * 4;
-    if (cpt <= 8) k_stored_fused<8><<<grid, kFT, 0, st>>>(A);
-    else if (cpt <= 16) k_stored_fused<16><<<grid, kFT, 0, st>>>(A);
-    else if (cpt <= 32) k_stored_fused<32><<<grid, kFT, 0, st>>>(A);
+    cudaError_t e = cudaSuccess;
+#define SK_FUSED_LAUNCH(CP)                                                                                   \
+    {                                                                                                         \
+        e = cudaFuncSetAttribute(k_stored_fused<CP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+        if (e != cudaSuccess) return e;                                                                       \
+        k_stored_fused<CP><<<grid, kFT, smem, st>>>(A);                                                       \
+    }
+    if (cpt <= 4) SK_FUSED_LAUNCH(4)
+    else if (cpt <= 8) SK_FUSED_LAUNCH(8)
+    else if (cpt <= 16) SK_FUSED_LAUNCH(16)
+    else if (cpt <= 32) SK_FUSED_LAUNCH(32)
     else return cudaErrorInvalidValue;
+#undef SK_FUSED_LAUNCH
     return cudaGetLastError();
 }
 

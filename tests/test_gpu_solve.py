@@ -172,3 +172,30 @@ def test_stored_parity(O, ctx, n, m, d):
     eps = float(np.float32(0.05 * gen.mean_sq_cost(x, y)))
     a = gen.random_weights(n, rng)
     check_solve(O, sk, ctx, x, y, eps, a=a, mode="stored", what=f"stored {n}x{m}x{d}")
+
+
+@pytest.mark.parametrize("n,m,d,eps_f", [(1003, 16384, 5, 0.1), (257, 12, 3, 0.05), (3000, 4100, 16, 0.02)])
+def test_stored_fused_sweep_parity(O, ctx, n, m, d, eps_f):
+    """The fused single-read stored sweep (one exponential per entry, scaled column sums) at the
+    widest row it supports (m = 16384), a tiny row and a ragged split, against the oracle."""
+    import paper_2206_07630_b200 as sk
+    rng = np.random.default_rng(n + m)
+    x = rng.standard_normal((n, d)).astype(np.float32)
+    y = (rng.standard_normal((m, d)) * 0.8 + 0.3).astype(np.float32)
+    eps = float(np.float32(eps_f * gen.mean_sq_cost(x, y)))
+    check_solve(O, sk, ctx, x, y, eps, mode="stored", what=f"fused {n}x{m}x{d}")
+
+
+def test_stored_fused_column_fallback(O, ctx):
+    """A column of weight 1e-32 drives its scaled column mass below 2^-100 every sweep: the merge
+    must detect it and redo the column pass exactly (status colfail path)."""
+    import paper_2206_07630_b200 as sk
+    rng = np.random.default_rng(5)
+    n, m, d = 900, 1024, 8
+    x = rng.standard_normal((n, d)).astype(np.float32)
+    y = (rng.standard_normal((m, d)) + 0.25).astype(np.float32)
+    b = np.full(m, 1.0, np.float64)
+    b[0] = 1e-32
+    b = (b / b.sum()).astype(np.float32)
+    eps = float(np.float32(0.05 * gen.mean_sq_cost(x, y)))
+    check_solve(O, sk, ctx, x, y, eps, b=b, mode="stored", what="fused colfail")
