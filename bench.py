@@ -240,8 +240,12 @@ class Single(Workload):
         return f0
 
     def _run(self, x, y, init=True):
+        import torch
         sk, p = self.sk, self.p
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        ev[0].record()
         f0 = self._init(x, y) if init else None
+        ev[1].record()
         if self.sharded:
             xl = x[self.row0:self.row0 + self.nl]
             f0l = None if f0 is None else f0[self.row0:self.row0 + self.nl].contiguous()
@@ -250,6 +254,10 @@ class Single(Workload):
         else:
             _, _, rep = sk.sinkhorn_solve(self.ctx, x, y, p.eps, tol=p.tol, max_iter=p.max_iter, mode=self.mode,
                                           f_init=f0)
+        ev[2].record()
+        ev[2].synchronize()
+        self.split_ms = {"init_ms": ev[0].elapsed_time(ev[1]), "solve_call_ms": ev[1].elapsed_time(ev[2]),
+                         "solve_loop_ms": rep["solve_ms"], "build_ms": rep["build_ms"]}
         self.rep = rep
         return float(self.n) * self.m * rep["iterations"] / self.world   # each rank's share
 
@@ -269,7 +277,8 @@ class Single(Workload):
 
     def extra(self):
         out = {"iterations": self.rep["iterations"], "converged": self.rep["converged"],
-               "dual_objective": self.rep["dual_objective"], "build_ms": self.rep["build_ms"]}
+               "dual_objective": self.rep["dual_objective"], "build_ms": self.rep["build_ms"],
+               "last_step_split_ms": getattr(self, "split_ms", None)}
         if hasattr(self, "inner"):
             out["subsample_inner_iterations"] = self.inner["iterations"]
         return out

@@ -473,6 +473,8 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
     MergePass mcol_scaled = mcol, mcol_redo = mcol;
     mcol_scaled.scaled = 1;
     mcol_redo.only_if = &status->colfail;
+    const bool colredo = sharded;   // unsharded: the scaled merge recomputes a failing column itself
+    if (!colredo && fused) { mcol_scaled.Cst = C[0]; mcol_scaled.xw = X[0].pack; mcol_scaled.n_rows = slices[0].n; }
     auto exchange_and_merge_col = [&](const MergePass &mp) -> sk_status {
         if (P.nccl && sharded) {
             int r = g_nccl.allgather(col_part(0), part, (size_t)slot * 2, kNcclFloat32, ctx->comm, st);
@@ -498,19 +500,19 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
                 for (int i = 0; i < ns; ++i) {
                     FusedLaunch fl{C[i], slices[i].n, m, P.eps, Y.pack, X[i].c, {X[i].pot[0], X[i].pot[1]},
                                    X[i].pack, X[i].lse, col_part(i), bs_rows, sharded ? blk_per_rank : nblk_glob,
-                                   split_q, status};
+                                   split_q, status, sharded ? 1 : 0, i + 1 < ns ? 1 : 0};
                     const int t0 = tm.start();
-                    CU(launch_stored_fused(fl, st));
+                    CU(launch_stored_fused(fl, st));   // also advances the sweep counter (row bookkeeping)
                     tm.stop(t0, sweep, LaunchTimer::FUSED, 2.0 * slices[i].n * m, 4.0 * slices[i].n * m);
-                    MergePass mrow{MERGE_ROW, &X[i], part, 1, P.eps, nullptr, status, blke, blkb, nullptr, 0.f,
-                                   sharded ? 1 : 0, i + 1 < ns ? 1 : 0, 1};
-                    CU(launch_merge(mrow, st));
-                    launched += 2;
+                    launched += 1;
                 }
                 CK(exchange_and_merge_col(mcol_scaled));
-                CK(col_stage(&status->colfail));           // no-ops unless colfail
-                CK(exchange_and_merge_col(mcol_redo));
-                launched += 2 + ns;
+                launched += 1;
+                if (colredo) {
+                    CK(col_stage(&status->colfail));       // no-ops unless colfail
+                    CK(exchange_and_merge_col(mcol_redo));
+                    launched += 1 + ns;
+                }
                 ++sweep;
                 continue;
             }

@@ -299,52 +299,88 @@ __global__ void __launch_bounds__(kGT) k_gmm_bures(const float *mux, const float
     }
 }
 
-// K x K entropic OT in fp64 (Alg. 1, g-then-f; R-13), one warp: lane t owns indices t and
-// t + 32.  Each sweep is a g-update then an f-update; err_l is evaluated with the fused
-// identity of the main solver (H5): after an f-update the row marginals are
-// exact, so err_l = sum_j b_j |expm1((g_j^l - g_j^{l+1})/eps)|, known at the next
-// g-update; the returned f~ is f^l of the first l with err_l < tol (or max_iter).
+// K x K entropic OT (Alg. 1, g-then-f; R-13), one warp, in log2 units: F = f kappa,
+// G = g kappa, Kc = -C kappa (kappa = log2(e)/eps, fp64).  Each sweep is a g-update then an
+// f-update; err_l is evaluated with the fused identity of the main solver (H5): after
+// an f-update the row marginals are exact, so err_l = sum_j b_j |expm1((g_j^l - g_j^{l+1})/eps)|,
+// known at the next g-update; the returned f~ is f^l of the first l with err_l < tol (or
+// max_iter).  Layout: lane t owns outputs t and t + 32; a reduction over the K'' inputs runs in
+// registers (8 independent partial maxima / sums).  The state F, G (values ~ cost/eps, hundreds
+// at C3) stays fp64: the iteration converges slowly (thousands of sweeps) and fp32 rounding of
+// the state would accumulate along its slow mode.  The exponentials 2^(v - max) <= 1, their sum
+// and its log2 use fp32 MUFU (relative error ~1e-7 per term, not accumulated in the state).
+// out_k = lw_k - LSE2_r (in_r + Kc[r][k]) (transposed access when cols = 0); returns the fused
+// error sum_k w_k |expm1(ln2 (prev_k - out_k))| when err != 0.
+__device__ __forceinline__ float gmm_update(const double *__restrict__ Kc, int Kx, int Ky, bool cols,
+                                            const double *in, double *out, const double *lw, const float *w,
+                                            bool err) {
+    const int t = threadIdx.x;
+    const int Kout = cols ? Ky : Kx, Kin = cols ? Kx : Ky;
+    const int rs = cols ? Ky : 1, ks = cols ? 1 : Ky;   // Kc index = r * rs + k * ks
+    float e = 0.f;
+    double on[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int k = t + 32 * h;
+        on[h] = 0.0;
+        if (k >= Kout) continue;
+        const double *kc = Kc + k * ks;
+        double v[8], mx = -INFINITY;
+        float s = 0.f;
+        for (int r0 = 0; r0 < Kin; r0 += 8) {   // one chunk when Kin <= 8 (C3: K = 8)
+            double cm = -INFINITY;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                v[u] = r0 + u < Kin ? in[r0 + u] + kc[(r0 + u) * rs] : -INFINITY;
+                cm = fmax(cm, v[u]);
+            }
+            if (cm > mx) { s *= ex2((float)(mx - cm)); mx = cm; }
+            float p[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) p[u] = ex2((float)(v[u] - mx));
+            s += ((p[0] + p[1]) + (p[2] + p[3])) + ((p[4] + p[5]) + (p[6] + p[7]));
+        }
+        on[h] = lw[k] - (mx + (double)__log2f(s));
+        if (err) e += w[k] * fabsf(expm1f((float)(out[k] - on[h]) * kLn2));
+    }
+    __syncwarp();
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+        if (t + 32 * h < Kout) out[t + 32 * h] = on[h];
+    __syncwarp();
+    if (err)
+        for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
+    return e;
+}
+
 __global__ void __launch_bounds__(32) k_gmm_sinkhorn(const double *C, int Kx, int Ky, const float *wx,
                                                       const float *wy, float eps_f, float tol, int max_iter,
                                                       double *ft, int *flags) {
-    __shared__ double f[64], g[64], fprev[64];
-    const double eps = eps_f;
+    __shared__ double Kc[64 * 64], F[64], G[64], la[64], lb[64];
+    const double eps = eps_f, kap = kLog2ed / eps;
     const int t = threadIdx.x;
-    for (int i = t; i < 64; i += 32) { f[i] = 0.0; g[i] = 0.0; fprev[i] = 0.0; }
+    for (int e = t; e < Kx * Ky; e += 32) Kc[e] = -C[e] * kap;
+    for (int i = t; i < 64; i += 32) {
+        F[i] = 0.0;
+        G[i] = 0.0;
+        la[i] = i < Kx ? log2((double)wx[i]) : 0.0;
+        lb[i] = i < Ky ? log2((double)wy[i]) : 0.0;
+    }
     __syncwarp();
     int l = 0;
     for (;;) {
         // g-update g^{l+1} from f^l, with err_l from (g^l, g^{l+1})
-        double e = 0.0;
-        for (int j = t; j < Ky; j += 32) {
-            double mx = -INFINITY;
-            for (int i = 0; i < Kx; ++i) mx = fmax(mx, (f[i] - C[i * Ky + j]) / eps);
-            double s = 0.0;
-            for (int i = 0; i < Kx; ++i) s += exp((f[i] - C[i * Ky + j]) / eps - mx);
-            const double gn = eps * log((double)wy[j]) - eps * (mx + log(s));
-            e += (double)wy[j] * fabs(expm1((g[j] - gn) / eps));
-            g[j] = gn;
-        }
-        for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
-        __syncwarp();
+        const float e = gmm_update(Kc, Kx, Ky, true, F, G, lb, wy, true);
         if (l >= 1 && (e < tol || !isfinite(e))) {
             if (!isfinite(e) && t == 0) atomicOr(flags, 2);
             break;
         }
         if (l >= max_iter) break;
         // f-update f^{l+1} from g^{l+1}
-        for (int i = t; i < Kx; i += 32) {
-            double mx = -INFINITY;
-            for (int j = 0; j < Ky; ++j) mx = fmax(mx, (g[j] - C[i * Ky + j]) / eps);
-            double s = 0.0;
-            for (int j = 0; j < Ky; ++j) s += exp((g[j] - C[i * Ky + j]) / eps - mx);
-            fprev[i] = f[i];
-            f[i] = eps * log((double)wx[i]) - eps * (mx + log(s));
-        }
-        __syncwarp();
+        gmm_update(Kc, Kx, Ky, false, G, F, la, wx, false);
         ++l;
     }
-    for (int i = t; i < Kx; i += 32) ft[i] = f[i];
+    for (int i = t; i < Kx; i += 32) ft[i] = F[i] / kap;
 }
 
 // Cholesky S_k = L L^T (fp64, one CTA, sequential columns), then Linv and log det L.

@@ -122,6 +122,9 @@ struct MergePass {
     int precomputed = 0;      // MERGE_ROW: potential and w already written (fused stored sweep)
     const Side *Q = nullptr;  // seeded passes: the reduced side, for the exact fallback
     int scaled = 0;           // MERGE_COL of the fused stored sweep: partials are (-g kappa, A_j)
+    const float *Cst = nullptr;   // scaled: the full stored C (n_rows x m) for the in-merge exact fallback
+    const float *xw = nullptr;    //         and the X side w = f kappa (n_rows)
+    long long n_rows = 0;
     const int *only_if = nullptr;  // run only if *only_if != 0 (the exact column fallback)
 };
 cudaError_t launch_merge(const MergePass &M, cudaStream_t st);
@@ -195,6 +198,8 @@ struct FusedLaunch {
     long long blk_rows;
     int nblk, split_q;
     DevStatus *st;
+    int sharded = 0;      // row bookkeeping as MERGE_ROW: non-finite rows are caught by the column merge
+    int no_iter_inc = 0;  // non-final slice of the emulated ranks: keep the sweep counter
 };
 bool stored_fused_supported(long long m);
 cudaError_t launch_stored_fused(const FusedLaunch &L, cudaStream_t st);

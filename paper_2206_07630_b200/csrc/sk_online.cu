@@ -260,60 +260,120 @@ __device__ void exact_lse_point(const Side &S, const Side &Q, int p, float eps, 
     }
 }
 
+// Merge of point p given its (M, Ssum) over all splits: new potential (+ packed w), fused
+// error term, non-finite and column-range flags.
+__device__ __forceinline__ void merge_point(const MergePass &Mp, const Side &S, int p, float M, float Ssum,
+                                            bool check, const float *hold, float *hnew, double &e, int &bad) {
+    const float eps = Mp.eps, kap = kLog2e / eps, epsln2 = eps * kLn2;
+    if (Mp.Q && !(Ssum >= 0x1p-100f && Ssum <= 0x1p100f)) {
+        // seeded pass: the fixed shift was far from the true maximum -> exact recompute of
+        // this point over the whole reduced side (rare; one thread, online max)
+        exact_lse_point(S, *Mp.Q, p, eps, M, Ssum);
+    }
+    if (Mp.scaled && !(Ssum >= 0x1p-100f && Ssum <= 0x1p100f)) {
+        // fused stored sweep: the scaled column mass left the safe range (an almost unmatched
+        // column).  Unsharded: exact online LSE of column p over all rows of the stored C here;
+        // sharded (rows on other ranks): the column pass is redone exactly (k_cols + merge,
+        // gated on st->colfail).
+        if (!Mp.Cst) { bad |= 2; return; }
+        const float kap = kLog2e / Mp.eps;
+        M = -INFINITY;
+        Ssum = 0.f;
+        for (long long i = 0; i < Mp.n_rows; ++i) {
+            const float t = fmaf(Mp.Cst[i * S.P + p], -kap, Mp.xw[i]);
+            if (t > M) { Ssum = Ssum * ex2(M - t); M = t; }
+            Ssum += ex2(t - M);
+        }
+    }
+    const float lse2 = M + log2f(Ssum);
+    if (S.lse) S.lse[p] = lse2;
+    if (Mp.mode == MERGE_OUT) {
+        const float v = Mp.out_const + (S.c[p] - epsln2 * lse2);
+        Mp.out[p] = v;
+        bad |= !isfinite(v);
+        return;
+    }
+    const float hn = S.c[p] - epsln2 * lse2;
+    hnew[p] = hn;
+    const long long t = p / S.tq, o = p % S.tq;
+    S.pack[t * (long long)(S.D + 1) * S.tq + (long long)S.D * S.tq + o] = fmaf(hn, kap, -S.nk[p]);
+    bad |= !isfinite(hn);
+    if (check) {
+        const double bj = Mp.wts ? (double)Mp.wts[p] : 1.0 / S.P;
+        e += bj * fabs((double)expm1f((hold[p] - hn) / eps));
+    }
+}
+
+constexpr int kWideMax = 32;      // splits per warp in the WIDE merge (nsplit <= 8 * 32)
+
+// WIDE (many splits): 32 points per block step; warp w reduces splits w, w + 8, ... of the 32
+// points (coalesced rows of the partial array), the 8 warp partials are combined in a fixed
+// order by warp 0 (max first, then the rescaled sums) — deterministic.
+template <bool WIDE>
 __global__ void __launch_bounds__(kMT) k_merge(MergePass Mp, Side S) {
     __shared__ double red[kMT / 32];
     __shared__ int redi[kMT / 32];
     __shared__ int s_last;
+    __shared__ float wM[kMT / 32][32], wS[kMT / 32][32];
     DevStatus *st = Mp.st;
     if (st && *(volatile int *)&st->stop) return;
     if (Mp.only_if && !*(volatile const int *)Mp.only_if) return;
     const int l = st ? st->iter : 0;
-    const float eps = Mp.eps, kap = kLog2e / eps, epsln2 = eps * kLn2;
     const bool check = Mp.mode == MERGE_COL && l >= 1 &&
                        (l % st->check_every == 0 || l == st->max_iter);
     const float *hold = (l & 1) ? S.pot[1] : S.pot[0];      // no dynamic param indexing
     float *hnew = (l & 1) ? S.pot[0] : S.pot[1];
     double e = 0.0;
     int bad = 0;
-    for (int p = blockIdx.x * kMT + threadIdx.x; p < S.P; p += gridDim.x * kMT) {
-        if (Mp.precomputed) {  // fused stored sweep wrote f and w; only check finiteness
-            bad |= !isfinite(hnew[p]);
-            continue;
+    if (WIDE) {
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        constexpr int NW = kMT / 32;
+        for (int pb = blockIdx.x * 32; pb < S.P; pb += gridDim.x * 32) {
+            const int p = pb + lane;
+            // this warp's splits, all loads in flight at once (kWideMax per warp), kept for pass 2
+            float2 v[kWideMax];
+#pragma unroll
+            for (int q = 0; q < kWideMax; ++q) {
+                const int s = warp + q * NW;
+                v[q] = (p < S.P && s < Mp.nsplit) ? Mp.part[(long long)s * S.P + p] : make_float2(-INFINITY, 0.f);
+            }
+            float M = -INFINITY;
+#pragma unroll
+            for (int q = 0; q < kWideMax; ++q) M = fmaxf(M, v[q].x);
+            wM[warp][lane] = M;
+            __syncthreads();
+            M = wM[0][lane];
+#pragma unroll
+            for (int w = 1; w < NW; ++w) M = fmaxf(M, wM[w][lane]);
+            float Ssum = 0.f;
+#pragma unroll
+            for (int q = 0; q < kWideMax; ++q)
+                if (v[q].x != -INFINITY) Ssum += v[q].y * ex2(v[q].x - M);
+            wS[warp][lane] = Ssum;
+            __syncthreads();
+            if (warp == 0 && p < S.P) {
+                Ssum = wS[0][lane];
+#pragma unroll
+                for (int w = 1; w < NW; ++w) Ssum += wS[w][lane];
+                if (Mp.precomputed) bad |= !isfinite(hnew[p]);
+                else merge_point(Mp, S, p, M, Ssum, check, hold, hnew, e, bad);
+            }
+            __syncthreads();
         }
-        float M = -INFINITY;
-        for (int s = 0; s < Mp.nsplit; ++s) M = fmaxf(M, Mp.part[(long long)s * S.P + p].x);
-        float Ssum = 0.f;
-        for (int s = 0; s < Mp.nsplit; ++s) {
-            const float2 v = Mp.part[(long long)s * S.P + p];
-            if (v.x != -INFINITY) Ssum += v.y * ex2(v.x - M);
-        }
-        if (Mp.Q && !(Ssum >= 0x1p-100f && Ssum <= 0x1p100f)) {
-            // seeded pass: the fixed shift was far from the true maximum -> exact recompute of
-            // this point over the whole reduced side (rare; one thread, online max)
-            exact_lse_point(S, *Mp.Q, p, eps, M, Ssum);
-        }
-        if (Mp.scaled && !(Ssum >= 0x1p-100f && Ssum <= 0x1p100f)) {
-            // fused stored sweep: the scaled column mass left the safe range -> the whole
-            // column pass is redone exactly (k_cols + this merge, gated on st->colfail)
-            bad |= 2;
-            continue;
-        }
-        const float lse2 = M + log2f(Ssum);
-        if (S.lse) S.lse[p] = lse2;
-        if (Mp.mode == MERGE_OUT) {
-            const float v = Mp.out_const + (S.c[p] - epsln2 * lse2);
-            Mp.out[p] = v;
-            bad |= !isfinite(v);
-            continue;
-        }
-        const float hn = S.c[p] - epsln2 * lse2;
-        hnew[p] = hn;
-        const long long t = p / S.tq, o = p % S.tq;
-        S.pack[t * (long long)(S.D + 1) * S.tq + (long long)S.D * S.tq + o] = fmaf(hn, kap, -S.nk[p]);
-        bad |= !isfinite(hn);
-        if (check) {
-            const double bj = Mp.wts ? (double)Mp.wts[p] : 1.0 / S.P;
-            e += bj * fabs((double)expm1f((hold[p] - hn) / eps));
+    } else {
+        for (int p = blockIdx.x * kMT + threadIdx.x; p < S.P; p += gridDim.x * kMT) {
+            if (Mp.precomputed) {  // fused stored sweep wrote f and w; only check finiteness
+                bad |= !isfinite(hnew[p]);
+                continue;
+            }
+            float M = -INFINITY;
+            for (int s = 0; s < Mp.nsplit; ++s) M = fmaxf(M, Mp.part[(long long)s * S.P + p].x);
+            float Ssum = 0.f;
+            for (int s = 0; s < Mp.nsplit; ++s) {
+                const float2 v = Mp.part[(long long)s * S.P + p];
+                if (v.x != -INFINITY) Ssum += v.y * ex2(v.x - M);
+            }
+            merge_point(Mp, S, p, M, Ssum, check, hold, hnew, e, bad);
         }
     }
     if (!st) return;
@@ -364,8 +424,16 @@ __global__ void __launch_bounds__(kMT) k_merge(MergePass Mp, Side S) {
     __threadfence();
 }
 
+constexpr int kWideSplits = 12;   // splits from which the merge uses the warp-per-split-group layout
+
 cudaError_t launch_merge(const MergePass &M, cudaStream_t st) {
-    k_merge<<<merge_blocks(M.S->P), kMT, 0, st>>>(M, *M.S);
+    if (M.nsplit >= kWideSplits && M.nsplit <= kWideMax * (kMT / 32)) {
+        int b = (M.S->P + 31) / 32;
+        if (b > 1184) b = 1184;
+        k_merge<true><<<b, kMT, 0, st>>>(M, *M.S);
+    } else {
+        k_merge<false><<<merge_blocks(M.S->P), kMT, 0, st>>>(M, *M.S);
+    }
     return cudaGetLastError();
 }
 

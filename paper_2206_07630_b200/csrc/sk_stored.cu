@@ -18,38 +18,54 @@
 namespace sk {
 
 // ------------------------------------------------------------------- K4
+// Block = 256 columns x 32 rows; x rows staged transposed in shared memory ([k][32 rows]) so a
+// thread reads 4 rows' coordinate k with one broadcast LDS.128; (x_ik - y_jk)^2 accumulated
+// over k in order with packed FFMA2 (each lane is the scalar fmaf chain, bit for bit).
+template <int DP>
 __global__ void __launch_bounds__(256) k_build_cost(const float *__restrict__ x, const float *__restrict__ y,
                                                     long long n, long long m, int d, float *C) {
-    extern __shared__ float sxy[];  // [32][d] rows of x
+    __shared__ __align__(16) float sx[DP][32];
     const long long i0 = (long long)blockIdx.y * 32;
     const long long j = (long long)blockIdx.x * 256 + threadIdx.x;
-    for (int t = threadIdx.x; t < 32 * d; t += 256) {
-        const long long i = i0 + t / d;
-        sxy[t] = i < n ? x[i * d + t % d] : 0.f;
+    for (int t = threadIdx.x; t < 32 * DP; t += 256) {
+        const int r = t / DP, k = t % DP;
+        const long long i = i0 + r;
+        sx[k][r] = (i < n && k < d) ? x[i * d + k] : 0.f;
     }
     __syncthreads();
     if (j >= m) return;
-    float yj[64];
+    float yj[DP];
 #pragma unroll
-    for (int k = 0; k < 64; ++k)
-        if (k < d) yj[k] = y[j * d + k];
-    for (int r = 0; r < 32 && i0 + r < n; ++r) {
-        float s = 0.f;
+    for (int k = 0; k < DP; ++k) yj[k] = k < d ? y[j * d + k] : 0.f;
+    const int rows = (int)min(32LL, n - i0);
 #pragma unroll
-        for (int k = 0; k < 64; ++k)
-            if (k < d) {
-                const float t = sxy[r * d + k] - yj[k];
-                s = fmaf(t, t, s);
-            }
-        C[(i0 + r) * m + j] = s;
+    for (int r = 0; r < 32; r += 4) {
+        float2 a01 = make_float2(0.f, 0.f), a23 = a01;
+#pragma unroll
+        for (int k = 0; k < DP; ++k) {
+            const float4 xv = *reinterpret_cast<const float4 *>(&sx[k][r]);
+            const float2 yy = make_float2(yj[k], yj[k]);
+            const float2 t01 = sub2(make_float2(xv.x, xv.y), yy), t23 = sub2(make_float2(xv.z, xv.w), yy);
+            a01 = fma2(t01, t01, a01);
+            a23 = fma2(t23, t23, a23);
+        }
+        float *out = C + (i0 + r) * m + j;
+        if (r + 0 < rows) out[0] = a01.x;
+        if (r + 1 < rows) out[m] = a01.y;
+        if (r + 2 < rows) out[2 * m] = a23.x;
+        if (r + 3 < rows) out[3 * m] = a23.y;
     }
 }
 
 cudaError_t launch_build_cost(const float *x, const float *y, long long n, long long m, int d, float *C,
                               cudaStream_t st) {
-    if (d > 64) return cudaErrorInvalidValue;
     dim3 grid((unsigned)((m + 255) / 256), (unsigned)((n + 31) / 32));
-    k_build_cost<<<grid, 256, 32 * d * sizeof(float), st>>>(x, y, n, m, d, C);
+    if (d <= 4) k_build_cost<4><<<grid, 256, 0, st>>>(x, y, n, m, d, C);
+    else if (d <= 8) k_build_cost<8><<<grid, 256, 0, st>>>(x, y, n, m, d, C);
+    else if (d <= 16) k_build_cost<16><<<grid, 256, 0, st>>>(x, y, n, m, d, C);
+    else if (d <= 32) k_build_cost<32><<<grid, 256, 0, st>>>(x, y, n, m, d, C);
+    else if (d <= 64) k_build_cost<64><<<grid, 256, 0, st>>>(x, y, n, m, d, C);
+    else return cudaErrorInvalidValue;
     return cudaGetLastError();
 }
 
@@ -241,6 +257,7 @@ struct FusedArgs {
     long long blk_rows;
     int split_q, stages;
     DevStatus *st;
+    int sharded, no_iter_inc;
 };
 
 __device__ __forceinline__ float warp_sum_tree(float v) {
@@ -255,12 +272,74 @@ __device__ __forceinline__ float warp_max(float v) {
     return v;
 }
 
+// Row LSE of one staged row (all threads of the CTA; uniform control flow): t receives
+// e_j = 2^(t_j - sig) for this thread's columns, S = sum_j e_j over the row (fixed tree), with
+// sig = seed + margin when that keeps S in [2^-100, 2^100], else the exact row maximum.
+template <int CPT, int FT = kFT, class W>
+__device__ __forceinline__ void fused_row_lse(const float4 *row4, int m4, float kap, const W &w,
+                                              float seed, float (&t)[CPT], float *red, float *redm, float &sig,
+                                              float &S) {
+    constexpr int G = CPT / 4;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+    for (int q = 0; q < G; ++q) {
+        const int g = threadIdx.x + q * FT;
+        const float4 c = g < m4 ? row4[g] : make_float4(0.f, 0.f, 0.f, 0.f);
+        t[4 * q] = fmaf(c.x, -kap, w(4 * q)); t[4 * q + 1] = fmaf(c.y, -kap, w(4 * q + 1));
+        t[4 * q + 2] = fmaf(c.z, -kap, w(4 * q + 2)); t[4 * q + 3] = fmaf(c.w, -kap, w(4 * q + 3));
+    }
+    sig = seed + kFusedSeedMargin;
+    S = 0.f;
+    bool exact = !isfinite(seed);
+    if (!exact) {
+        float p = 0.f;
+#pragma unroll
+        for (int c = 0; c < CPT; ++c) { t[c] = ex2(t[c] - sig); p += t[c]; }   // t now holds e
+        p = warp_sum_tree(p);
+        if (lane == 0) red[warp] = p;
+        __syncthreads();
+#pragma unroll
+        for (int x = 0; x < FT / 32; ++x) S += red[x];
+        exact = !(S >= 0x1p-100f && S <= 0x1p100f);
+        if (exact) {   // rare: rebuild t from the row (still in shared memory until refilled)
+#pragma unroll
+            for (int q = 0; q < G; ++q) {
+                const int g = threadIdx.x + q * FT;
+                const float4 c = g < m4 ? row4[g] : make_float4(0.f, 0.f, 0.f, 0.f);
+                t[4 * q] = fmaf(c.x, -kap, w(4 * q)); t[4 * q + 1] = fmaf(c.y, -kap, w(4 * q + 1));
+                t[4 * q + 2] = fmaf(c.z, -kap, w(4 * q + 2)); t[4 * q + 3] = fmaf(c.w, -kap, w(4 * q + 3));
+            }
+        }
+    }
+    if (exact) {   // exact maximum as the shift (first sweep, or the seed was off)
+        float mx = -INFINITY;
+#pragma unroll
+        for (int c = 0; c < CPT; ++c) mx = fmaxf(mx, t[c]);
+        mx = warp_max(mx);
+        if (lane == 0) redm[warp] = mx;
+        __syncthreads();
+        sig = -INFINITY;
+#pragma unroll
+        for (int x = 0; x < FT / 32; ++x) sig = fmaxf(sig, redm[x]);
+        float p = 0.f;
+#pragma unroll
+        for (int c = 0; c < CPT; ++c) { t[c] = ex2(t[c] - sig); p += t[c]; }
+        p = warp_sum_tree(p);
+        if (lane == 0) red[warp] = p;
+        __syncthreads();
+        S = 0.f;
+#pragma unroll
+        for (int x = 0; x < FT / 32; ++x) S += red[x];
+    }
+}
+
 template <int CPT>
 __global__ void __launch_bounds__(kFT, 1) k_stored_fused(FusedArgs A) {
     constexpr int G = CPT / 4;                     // float4 groups per thread
     extern __shared__ __align__(128) float ring[];   // stages x m floats
     __shared__ __align__(8) uint64_t full[8];
     __shared__ float red[2][kFW], redm[kFW];
+    __shared__ int s_last;
     if (*(volatile const int *)&A.st->stop) return;
     const int l = A.st->iter;                      // producing f^{l+1}
     float *fnew = ((l + 1) & 1) ? A.xpot[1] : A.xpot[0];   // no dynamic param indexing
@@ -296,6 +375,7 @@ __global__ void __launch_bounds__(kFT, 1) k_stored_fused(FusedArgs A) {
     }
 #pragma unroll
     for (int c = 0; c < CPT; ++c) acc[c] = 0.f;
+    int bad = 0;   // non-finite f in this CTA's rows (thread 0)
 
     for (long long i = r0; i < r1; ++i) {
         const int k = (int)(i - r0);
@@ -303,62 +383,14 @@ __global__ void __launch_bounds__(kFT, 1) k_stored_fused(FusedArgs A) {
         const float4 *row4 = reinterpret_cast<const float4 *>(ring + (size_t)st * m);
         const float seed = A.xlse[i];
         mbar_wait(&full[st], (k / NS) & 1);
-        float t[CPT];
-#pragma unroll
-        for (int q = 0; q < G; ++q) {
-            const int g = threadIdx.x + q * kFT;
-            const float4 c = g < m4 ? row4[g] : make_float4(0.f, 0.f, 0.f, 0.f);
-            t[4 * q] = fmaf(c.x, -kap, w[4 * q]); t[4 * q + 1] = fmaf(c.y, -kap, w[4 * q + 1]);
-            t[4 * q + 2] = fmaf(c.z, -kap, w[4 * q + 2]); t[4 * q + 3] = fmaf(c.w, -kap, w[4 * q + 3]);
-        }
-        // ---- row LSE with a seeded shift (uniform decisions: every thread sees the same values)
-        float sig = seed + kFusedSeedMargin, S = 0.f;
-        bool exact = !isfinite(seed);
-        if (!exact) {
-            float p = 0.f;
-#pragma unroll
-            for (int c = 0; c < CPT; ++c) { t[c] = ex2(t[c] - sig); p += t[c]; }   // t now holds e
-            p = warp_sum_tree(p);
-            if (lane == 0) red[k & 1][warp] = p;
-            __syncthreads();
-#pragma unroll
-            for (int x = 0; x < kFW; ++x) S += red[k & 1][x];
-            exact = !(S >= 0x1p-100f && S <= 0x1p100f);
-            if (exact) {   // rare: rebuild t from the row (still in shared memory until refilled)
-#pragma unroll
-                for (int q = 0; q < G; ++q) {
-                    const int g = threadIdx.x + q * kFT;
-                    const float4 c = g < m4 ? row4[g] : make_float4(0.f, 0.f, 0.f, 0.f);
-                    t[4 * q] = fmaf(c.x, -kap, w[4 * q]); t[4 * q + 1] = fmaf(c.y, -kap, w[4 * q + 1]);
-                    t[4 * q + 2] = fmaf(c.z, -kap, w[4 * q + 2]); t[4 * q + 3] = fmaf(c.w, -kap, w[4 * q + 3]);
-                }
-            }
-        }
-        if (exact) {   // exact maximum as the shift (first sweep, or the seed was off)
-            float mx = -INFINITY;
-#pragma unroll
-            for (int c = 0; c < CPT; ++c) mx = fmaxf(mx, t[c]);
-            mx = warp_max(mx);
-            if (lane == 0) redm[warp] = mx;
-            __syncthreads();
-            sig = -INFINITY;
-#pragma unroll
-            for (int x = 0; x < kFW; ++x) sig = fmaxf(sig, redm[x]);
-            float p = 0.f;
-#pragma unroll
-            for (int c = 0; c < CPT; ++c) { t[c] = ex2(t[c] - sig); p += t[c]; }
-            p = warp_sum_tree(p);
-            if (lane == 0) red[k & 1][warp] = p;
-            __syncthreads();
-            S = 0.f;
-#pragma unroll
-            for (int x = 0; x < kFW; ++x) S += red[k & 1][x];
-        }
+        float t[CPT], sig, S;
+        fused_row_lse<CPT>(row4, m4, kap, [&](int c) { return w[c]; }, seed, t, red[k & 1], redm, sig, S);
         const float lse = sig + log2f(S);
         const float fn = A.xc[i] - epsln2 * lse;
         const float wv = fn * kap;
         if (threadIdx.x == 0) {
             fnew[i] = fn;
+            bad |= !isfinite(fn);
             A.xw[i] = wv;
             A.xlse[i] = lse;
             // every thread has row i in registers (a barrier passed since): refill its slot
@@ -383,6 +415,26 @@ __global__ void __launch_bounds__(kFT, 1) k_stored_fused(FusedArgs A) {
                 A.part[(long long)s * A.m + 4 * g + e] = make_float2(-w[4 * q + e], acc[4 * q + e]);
         }
     }
+    // row bookkeeping (what MERGE_ROW does for the separate passes): the last CTA advances the
+    // sweep counter, or stops on a non-finite f (unsharded; sharded ranks rely on the column merge)
+    if (threadIdx.x == 0) {
+        if (bad) atomicOr(&A.st->nonfinite, 2);   // bit 1: pending, promoted below
+        __threadfence();
+        s_last = atomicAdd(&A.st->ticket_row, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && s_last) {
+        __threadfence();
+        DevStatus *st = A.st;
+        st->ticket_row = 0;
+        const int nf = *(volatile int *)&st->nonfinite;
+        if ((nf & 2) && !A.sharded) { st->nonfinite = 1; st->stop = 1; st->final_iter = l; }
+        else {
+            st->nonfinite = nf & 1;
+            if (!A.no_iter_inc) st->iter = l + 1;
+        }
+        __threadfence();
+    }
 }
 
 bool stored_fused_supported(long long m) { return m % 4 == 0 && m >= 4 && m <= (long long)kFT * 32; }
@@ -392,6 +444,7 @@ cudaError_t launch_stored_fused(const FusedLaunch &L, cudaStream_t st) {
     A.C = L.C; A.n = L.n; A.m = L.m; A.eps = L.eps; A.gw = L.gw; A.xc = L.xc;
     A.xpot[0] = L.xpot[0]; A.xpot[1] = L.xpot[1]; A.xw = L.xw; A.xlse = L.xlse; A.part = L.part;
     A.blk_rows = L.blk_rows; A.split_q = L.split_q; A.st = L.st;
+    A.sharded = L.sharded; A.no_iter_inc = L.no_iter_inc;
     if (!stored_fused_supported(L.m) || !L.xlse) return cudaErrorInvalidValue;
     // ring depth: as many whole rows as fit (2 .. 8)
     const long long rb = L.m * 4;
