@@ -19,12 +19,13 @@
 #include "sk_internal.h"
 #include "sk_lse_tile.cuh"
 
+#include <cstdlib>
+
 namespace sk {
 
 constexpr int kLT = 128;      // LSE kernel threads
 constexpr int kStages = 4;    // bulk-copy ring depth
 constexpr int kLseEmu = 1;    // exp2 pairs (of 4 per chunk) on the FMA pipe when D <= 4
-constexpr int kLseEmuSeeded = 1;
 
 int lse_dpad(int d) {
     if (d <= 4) return d < 1 ? 0 : d;
@@ -96,7 +97,9 @@ struct LseArgs {
 
 constexpr float kSeedMarginMK = 4.f;  // log2 units above the previous LSE
 
-template <int D, int R, bool SEEDED>
+// EMU8: exponential pairs (of every 8 pairs = 2 chunks) evaluated on the FMA pipe in the
+// seeded pass (D <= 4); balances MUFU against the FMA pipe (measured by SK_LSE_EMU8 sweeps)
+template <int D, int R, bool SEEDED, int EMU8 = 2>
 __global__ void __launch_bounds__(kLT) k_lse(LseArgs A) {
     constexpr int TQ = D <= 4 ? 256 : (D <= 16 ? 128 : 64);
     constexpr int TF = (D + 1) * TQ;  // floats per tile
@@ -148,7 +151,10 @@ __global__ void __launch_bounds__(kLT) k_lse(LseArgs A) {
         const float *qt = ring + st * TF;
 #pragma unroll 2
         if (SEEDED) {
-            for (int q = 0; q < TQ; q += kChunk) lse_chunk_seeded<D, R, (D <= 4 ? kLseEmuSeeded : 0)>(qt, TQ, qt + D * TQ, q, pd, M, Sx);
+            for (int q = 0; q < TQ; q += 2 * kChunk) {
+                lse_chunk_seeded<D, R, (D <= 4 ? (EMU8 + 1) / 2 : 0)>(qt, TQ, qt + D * TQ, q, pd, M, Sx);
+                lse_chunk_seeded<D, R, (D <= 4 ? EMU8 / 2 : 0)>(qt, TQ, qt + D * TQ, q + kChunk, pd, M, Sx);
+            }
         } else {
             for (int q = 0; q < TQ; q += kChunk) lse_chunk<D, R, (D <= 4 ? kLseEmu : 0)>(qt, TQ, qt + D * TQ, q, pd, M, Sx);
         }
@@ -175,7 +181,9 @@ static cudaError_t launch_lse_d(const LsePass &L, cudaStream_t st) {
     cudaError_t e = cudaFuncSetAttribute(k_lse<D, R, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k_lse<D, R, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    static const int emu8 = [] { const char *v = getenv("SK_LSE_EMU8"); return v ? atoi(v) : 1; }();
+    auto seeded_fn = emu8 == 0 ? k_lse<D, R, true, 0> : (emu8 == 1 ? k_lse<D, R, true, 1> : k_lse<D, R, true, 2>);
+    e = cudaFuncSetAttribute(seeded_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     LseArgs A;
     A.Ppack = L.Pside->pack; A.P = L.Pside->P; A.Ptq = L.Pside->tq;
@@ -186,7 +194,7 @@ static cudaError_t launch_lse_d(const LsePass &L, cudaStream_t st) {
     A.stop = L.stop;
     A.seed = L.Pside->lse;
     dim3 grid((A.P + kLT * R - 1) / (kLT * R), L.nblk * L.split_q);
-    if (L.seeded && A.seed) k_lse<D, R, true><<<grid, kLT, smem, st>>>(A);
+    if (L.seeded && A.seed) seeded_fn<<<grid, kLT, smem, st>>>(A);
     else k_lse<D, R, false><<<grid, kLT, smem, st>>>(A);
     return cudaGetLastError();
 }
