@@ -317,7 +317,7 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
     const int ksteps = (P.d + 15) / 16;
     const int D = (stored || tc) ? 0 : lse_dpad(P.d);
     if (!stored && !tc && D == 0) return fail(ctx, SK_EUNSUPPORTED, "online path supports d <= 64");
-    const int tq = stored ? 256 : (tc ? 128 : lse_tq(D));
+    const int tq = stored ? 256 : (tc ? tc_points_per_tile() : lse_tq(D));
     const long long yt = lse_tiles(m, tq);
     const int pmode = stored ? PACK_STORED : (tc ? PACK_TC : PACK_ONLINE);
 
@@ -390,7 +390,7 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
     const int blk_per_rank = sharded ? SK_SHARD_BLOCKS / P.world : nblk_glob;
     const int occ = stored ? 8 : (tc ? 1 : lse_occupancy_ctas(D));
     const int Rr = tc ? 1 : (D <= 4 ? 4 : (D <= 16 ? 2 : 1));
-    const long long pcta = tc ? tc_points_per_cta() : 128LL * Rr;   // output points per CTA
+    const long long pcta = tc ? tc_points_per_tile() : 128LL * Rr;   // output points per CTA (pair)
     const long long ptiles_col = stored ? (m + 511) / 512 : (m + pcta - 1) / pcta;
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device);

@@ -87,7 +87,7 @@ size_t tc_image_bytes(long long P);
 cudaError_t launch_absmax(const float *pts, long long cnt, unsigned *out, cudaStream_t st);  // out zeroed first
 cudaError_t launch_pack_tc(const float *pts, long long P, int d, const unsigned *amax, void *img, cudaStream_t st);
 cudaError_t launch_lse_tc(const TcPass &L, cudaStream_t st);
-int tc_points_per_cta();   // output points per K3 CTA (two 128-row A tiles)
+int tc_points_per_tile();  // K3 tile: 256 output points per CTA pair, 256 reduction points per B tile
 
 // One LSE pass: outputs P side points, reduces over Q side.  Splits:
 // nblk blocks of blk_tiles Q tiles each (the last may be shorter; blk_tiles = 0

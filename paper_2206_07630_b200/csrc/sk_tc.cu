@@ -30,6 +30,7 @@
 // The output is the same (max, sum) partial as the FFMA kernel (K2), merged by K6.
 #include <cuda_fp16.h>
 
+#include <algorithm>
 #include <cstdlib>
 
 #include "sk_internal.h"
@@ -41,8 +42,6 @@ namespace sk {
 constexpr int kTcM = 128;       // points per tile (MMA M and N)
 constexpr int kTcEpiWarps = 8;  // two per TMEM lane quadrant (one per A tile)
 constexpr int kTcThreads = 64 + 32 * kTcEpiWarps;
-// smem: ABUF A buffers (64 KB each) + a B ring of tc_stages(ABUF) x (32 KB + 512 B)
-__host__ __device__ constexpr int tc_stages(int abuf) { return abuf == 2 ? 2 : 4; }
 constexpr int kTcImg = kTcM * 128;  // bytes of one fp16 image: 128 rows x 64 halves (16 SW128 atoms)
 
 // ------------------------------------------------------------ operand images
@@ -177,6 +176,8 @@ __device__ __forceinline__ float2 tc_sum_chunk(const float2 (&t)[32], float M) {
     return add2(s0, s1);
 }
 
+// smem: ABUF A buffers (64 KB each) + a B ring of tc_stages(ABUF) x (32 KB + 512 B)
+__host__ __device__ constexpr int tc_stages(int abuf) { return abuf == 2 ? 2 : 4; }
 // Persistent: one CTA per SM walks the work items (A tile pair pt, split s), item =
 // s * ptiles + pt, items blockIdx.x, blockIdx.x + gridDim.x, ...  (concurrent CTAs share the
 // split's B tiles in L2).  The B ring, the two accumulator buffers and the two A buffers are
@@ -358,6 +359,253 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lse_tc(TcArgs A) {
     }
 }
 
+// ------------------------------------------------------- 2-SM (CTA pair) variant
+// cta_group::2: the pair computes a 256 x 256 tile per MMA (M = 256 split over the two SMs'
+// A halves, N = 256 split over their B halves), so each SM reads 8 KB of operands from shared
+// memory per 128-cycle MMA (64 B/clk, half of the 1-SM 128 x 128 shape's demand): the full
+// tensor rate.  Roles per CTA (rank r of the pair):
+//   warp 0   producer: A half (points 256 pt + 128 r) once per item, B halves (points
+//            256 bt + 128 r, images) + all 256 w of the tile into a kT2Stages ring;
+//   warp 1   leader: TMEM allocation (both CTAs allocate, cta_group::2) and the MMA issuer;
+//            peer: relay — waits for its own A/B arrivals and arrives remotely on the leader's
+//            pair barriers (1D bulk copies signal their own CTA's mbarrier);
+//   warps 2-9 epilogue on this CTA's 128 accumulator rows: warp w = lane quadrant w % 4, column
+//            half (w - 2) / 4 (128 of the 256 columns); releases accumulator b remotely on the
+//            leader's tempty.  MMA completion is multicast to both CTAs' barriers.
+constexpr int kT2Stages = 4;
+constexpr int kT2N = 256;                     // MMA N (B points per tile) and A points per item
+constexpr uint32_t kIdescF16M256N256 = (1u << 4) | ((uint32_t)(kT2N >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t saddr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+    return r;
+}
+// Relaxed: the arrivals only signal that a TMEM buffer was drained (tcgen05.wait::ld already
+// retired the loads) or that an async-proxy copy completed; no generic-proxy data is published,
+// and .release.cluster would cost a MEMBAR.ALL.GPU per arrive (measured: 12 % of stall samples).
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void umma2_f16(uint32_t dtmem, uint64_t adesc, uint64_t bdesc, uint32_t accum) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(dtmem),
+        "l"(adesc), "l"(bdesc), "r"(kIdescF16M256N256), "r"(accum));
+}
+__device__ __forceinline__ void umma2_commit_mc(uint64_t *bar) {
+    asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+                 ::"r"(smem_u32(bar)), "h"((uint16_t)3) : "memory");
+}
+
+template <int EMU>
+__global__ void __launch_bounds__(kTcThreads, 1) k_lse_tc2(TcArgs A) {
+    constexpr int ABUF = 2;
+    constexpr int STAGE = 2 * kTcImg;                // own B half: hi + lo (128 points)
+    extern __shared__ __align__(1024) unsigned char smraw[];
+    unsigned char *sm = smraw + ((1024 - (smem_u32(smraw) & 1023)) & 1023);
+    unsigned char *sA = sm;                           // ABUF x [hi | lo] of this CTA's 128 A rows
+    unsigned char *sB = sm + ABUF * 2 * kTcImg;       // kT2Stages x STAGE
+    float *sW = reinterpret_cast<float *>(sB + kT2Stages * STAGE);   // kT2Stages x 256 w
+    float2 *xch = reinterpret_cast<float2 *>(sW + kT2Stages * kT2N); // 128 column-half partials
+    __shared__ __align__(8) uint64_t full[kT2Stages], pfull[kT2Stages], empty[kT2Stages], tfull[2], tempty[2],
+        afull[ABUF], pafull[ABUF], aempty[ABUF];
+    __shared__ uint32_t tmem_base;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_rank();
+    const bool leader = rank == 0;
+    const bool stopped = A.stop && *(volatile const int *)A.stop;   // uniform over the pair (same flag)
+    if (stopped) return;
+    const int nsplit = A.nblk * A.split_q;
+    const int items = A.ptiles * nsplit;
+    const int bt_blk = A.blk_tiles > 0 ? A.blk_tiles : A.Qtiles;
+    auto range = [&](int s, int &t0, int &nt) {
+        const int bq = s / A.split_q, u = s % A.split_q;
+        const int base = bq * bt_blk;
+        const int nt_b = max(0, min(bt_blk, A.Qtiles - base));
+        t0 = base + (int)((long long)nt_b * u / A.split_q);
+        nt = base + (int)((long long)nt_b * (u + 1) / A.split_q) - t0;
+    };
+    const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kT2Stages; ++i) {
+            mbar_init(&full[i], 1); mbar_init(&pfull[i], 1); mbar_init(&empty[i], 1 + kTcEpiWarps);
+        }
+        for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 2 * kTcEpiWarps); }
+        for (int i = 0; i < ABUF; ++i) { mbar_init(&afull[i], 1); mbar_init(&pafull[i], 1); mbar_init(&aempty[i], 1); }
+        fence_mbar_init();
+    }
+    if (warp == 1) {  // both CTAs: 512 TMEM columns = 2 accumulator buffers x 256 columns
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+    tc_fence_before();
+    cluster_sync_all();   // barriers initialised in both CTAs before any remote arrive
+    tc_fence_after();
+    const uint32_t tbase = tmem_base;
+    const long long clk0 = clock64();
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int g = 0, c = 0;
+            for (int it = cid; it < items; it += ncl, ++c) {
+                const int s = it / A.ptiles, pt = it % A.ptiles;
+                int t0, nt;
+                range(s, t0, nt);
+                const int ab = c % ABUF;
+                if (c >= ABUF) mbar_wait_sleep(&aempty[ab], ((c / ABUF) - 1) & 1);
+                mbar_expect_tx(&afull[ab], 2 * kTcImg);
+                bulk_g2s(sA + ab * 2 * kTcImg, A.Aimg + (long long)(2 * pt + rank) * 2 * kTcImg, 2 * kTcImg, &afull[ab]);
+                for (int i = 0; i < nt; ++i, ++g) {
+                    const int st = g % kT2Stages;
+                    if (g >= kT2Stages) mbar_wait_sleep(&empty[st], ((g / kT2Stages) - 1) & 1);
+                    mbar_expect_tx(&full[st], STAGE + kT2N * 4);
+                    bulk_g2s(sB + st * STAGE, A.Bimg + (long long)(2 * (t0 + i) + rank) * 2 * kTcImg, STAGE, &full[st]);
+                    bulk_g2s(sW + st * kT2N, A.Bw + (long long)(t0 + i) * kT2N, kT2N * 4, &full[st]);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0 && !leader) {
+            // relay: own arrivals -> the leader's pair barriers
+            const uint32_t r_pafull = mapa_u32(smem_u32(&pafull[0]), 0), r_pfull = mapa_u32(smem_u32(&pfull[0]), 0);
+            int g = 0, c = 0;
+            for (int it = cid; it < items; it += ncl, ++c) {
+                int t0, nt;
+                range(it / A.ptiles, t0, nt);
+                const int ab = c % ABUF;
+                mbar_wait(&afull[ab], (c / ABUF) & 1);
+                mbar_arrive_cluster(r_pafull + 8 * ab);
+                for (int i = 0; i < nt; ++i, ++g) {
+                    const int st = g % kT2Stages;
+                    mbar_wait(&full[st], (g / kT2Stages) & 1);
+                    mbar_arrive_cluster(r_pfull + 8 * st);
+                }
+            }
+        } else if (lane == 0) {
+            const int ks = A.ksteps;
+            int g = 0, c = 0;
+            for (int it = cid; it < items; it += ncl, ++c) {
+                int t0, nt;
+                range(it / A.ptiles, t0, nt);
+                const int ab = c % ABUF;
+                mbar_wait(&afull[ab], (c / ABUF) & 1);
+                mbar_wait(&pafull[ab], (c / ABUF) & 1);
+                const uint32_t a_hi = smem_u32(sA + ab * 2 * kTcImg), a_lo = a_hi + kTcImg;
+                for (int i = 0; i < nt; ++i, ++g) {
+                    const int st = g % kT2Stages, b = g & 1;
+                    mbar_wait(&full[st], (g / kT2Stages) & 1);
+                    mbar_wait(&pfull[st], (g / kT2Stages) & 1);
+                    if (g >= 2) mbar_wait(&tempty[b], ((g >> 1) - 1) & 1);
+                    tc_fence_after();
+                    const uint32_t b_hi = smem_u32(sB + st * STAGE), b_lo = b_hi + kTcImg;
+                    const uint32_t d = tbase + (uint32_t)(b * kT2N);
+                    for (int k = 0; k < ks; ++k) {   // K = 16 halves = 32 bytes per step
+                        const uint32_t koff = (uint32_t)k * 32;
+                        umma2_f16(d, umma_desc_sw128(a_lo + koff), umma_desc_sw128(b_hi + koff), k > 0);
+                        umma2_f16(d, umma_desc_sw128(a_hi + koff), umma_desc_sw128(b_lo + koff), 1);
+                    }
+                    for (int k = 0; k < ks; ++k) {
+                        const uint32_t koff = (uint32_t)k * 32;
+                        umma2_f16(d, umma_desc_sw128(a_hi + koff), umma_desc_sw128(b_hi + koff), 1);
+                    }
+                    umma2_commit_mc(&empty[st]);   // both CTAs' B slots free once these MMAs retire
+                    umma2_commit_mc(&tfull[b]);    // accumulator b ready in both CTAs
+                }
+                umma2_commit_mc(&aempty[ab]);      // both CTAs' A buffers free
+            }
+        }
+    } else {
+        // epilogue: this CTA's accumulator rows (TMEM lanes) q4*32 + lane, columns h*128 ..+127
+        const int q4 = warp & 3, h = (warp - 2) >> 2;
+        const int row = q4 * 32 + lane;
+        const float tks = ldexpf(A.tk, tc_scale_exp(A.amax_p) + tc_scale_exp(A.amax_q));
+        const float2 tk2 = make_float2(tks, tks);
+        const float us = ldexpf(1.f, tc_scale_exp(A.amax_p) + tc_scale_exp(A.amax_q));  // exact unscale
+        const uint32_t r_tempty = leader ? smem_u32(&tempty[0]) : mapa_u32(smem_u32(&tempty[0]), 0);
+        int g = 0;
+        for (int it = cid; it < items; it += ncl) {
+            const int s = it / A.ptiles, pt = it % A.ptiles;
+            int t0, nt;
+            range(s, t0, nt);
+            const int p = pt * kT2N + (int)rank * kTcM + row;
+            const bool dbg = A.debug_acc && leader && h == 0 && it == 0;
+            float M = -INFINITY, S = 0.f;
+            for (int i = 0; i < nt; ++i, ++g) {
+                const int st = g % kT2Stages, b = g & 1;
+                mbar_wait_sleep(&tfull[b], (g >> 1) & 1);
+                tc_fence_after();
+                if (A.mma_only) {
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) { mbar_arrive_cluster(r_tempty + 8 * b); mbar_arrive(&empty[st]); }
+                    continue;
+                }
+                const uint32_t taddr = tbase + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(b * kT2N + h * 128);
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh) {   // two 64-column chunks
+                    const float2 *w = reinterpret_cast<const float2 *>(sW + st * kT2N + h * 128 + hh * 64);
+                    uint32_t r[64];
+                    TMEM_LD32(taddr + hh * 64, r);
+                    TMEM_LD32(taddr + hh * 64 + 32, (r + 32));
+                    tmem_ld_wait();
+                    if (dbg && i == 0) {
+#pragma unroll
+                        for (int j = 0; j < 64; ++j) A.debug_acc[row * kTcM + hh * 64 + j] = __uint_as_float(r[j]) * us;
+                    }
+                    float2 t[32];
+#pragma unroll
+                    for (int j = 0; j < 32; ++j)
+                        t[j] = fma2(make_float2(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1])), tk2, w[j]);
+                    if (hh == 1) {
+                        // accumulator b (this CTA's half) and the w slot are no longer needed
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) { mbar_arrive_cluster(r_tempty + 8 * b); mbar_arrive(&empty[st]); }
+                    }
+                    float m8[8];
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        m8[j] = fmax3(fmaxf(t[4 * j].x, t[4 * j].y), fmax3(t[4 * j + 1].x, t[4 * j + 1].y, t[4 * j + 2].x),
+                                      fmax3(t[4 * j + 2].y, t[4 * j + 3].x, t[4 * j + 3].y));
+                    const float cm = fmax3(fmax3(m8[0], m8[1], m8[2]), fmax3(m8[3], m8[4], m8[5]), fmaxf(m8[6], m8[7]));
+                    if (cm > M) { S *= ex2(M - cm); M = cm; }
+                    if (M == -INFINITY) continue;  // only padding seen so far
+                    const float2 sc = tc_sum_chunk<EMU>(t, M);
+                    S += sc.x + sc.y;
+                }
+            }
+            // combine the two column halves of each row (fixed order: half 0 then half 1)
+            if (h == 1) xch[row] = make_float2(M, S);
+            asm volatile("bar.sync 1, %0;" ::"r"(32 * kTcEpiWarps));
+            if (h == 0) {
+                const float2 o = xch[row];
+                lse_merge(M, S, o.x, o.y);
+                if (p < A.P && !A.mma_only) A.part[(long long)s * A.P + p] = make_float2(M, S);
+            }
+            asm volatile("bar.sync 1, %0;" ::"r"(32 * kTcEpiWarps));   // xch reuse
+        }
+    }
+    tc_fence_before();
+    cluster_sync_all();
+    if (A.cyc && blockIdx.x == 0 && threadIdx.x == 0) *A.cyc = clock64() - clk0;   // both CTAs done: no remote arrive or MMA still targets this CTA
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tbase));
+    }
+}
+
 // ------------------------------------------------------------- K14 MMA probe
 // Raw tcgen05.mma issue rate of one shape (M = 128, N, K = 32 bytes, SS operands on smem
 // garbage), one CTA per SM, groups of 12 MMAs into alternating accumulators, at most two
@@ -478,6 +726,7 @@ cudaError_t launch_pack_tc(const float *pts, long long P, int d, const unsigned 
     return cudaGetLastError();
 }
 
+
 template <int EMU, int ABUF>
 static cudaError_t launch_tc_v(const TcArgs &A, dim3 grid, cudaStream_t st) {
     const size_t smem = 1024 + ABUF * 4 * (size_t)kTcImg + tc_stages(ABUF) * (2 * (size_t)kTcImg + kTcM * 4);
@@ -495,27 +744,67 @@ static cudaError_t launch_tc_emu(const TcArgs &A, dim3 grid, cudaStream_t st) {
     return abuf == 1 ? launch_tc_v<EMU, 1>(A, grid, st) : launch_tc_v<EMU, 2>(A, grid, st);
 }
 
-int tc_points_per_cta() { return 2 * kTcM; }
+template <int EMU>
+static cudaError_t launch_tc2(const TcArgs &A, int items, cudaStream_t st) {
+    constexpr int ABUF = 2;
+    const size_t smem = 1024 + ABUF * 2 * (size_t)kTcImg + kT2Stages * (2 * (size_t)kTcImg + kT2N * 4) + kTcM * 8;
+    cudaError_t e = cudaFuncSetAttribute(k_lse_tc2<EMU>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int nsm = 148, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const int ncl = std::max(1, std::min(items, nsm / 2));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2 * ncl);
+    cfg.blockDim = dim3(kTcThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k_lse_tc2<EMU>, A);
+}
+
+int tc_points_per_tile() { return kT2N; }
 
 cudaError_t launch_lse_tc(const TcPass &L, cudaStream_t st) {
+    // SK_TC_PAIR: 1 = CTA-pair kernel (cta_group::2, 256 x 256 MMA tiles); 0 = one CTA per SM
+    // (two 128 x 128 accumulators per B tile).  Both read the same images and w arrays (Q side
+    // tiles of 256 points = two 128-point halves) and write the same partials.
+    static const int pair = [] { const char *e = getenv("SK_TC_PAIR"); return e ? atoi(e) : 1; }();
+    // fraction of the exponentials evaluated on the FMA pipe (of every 8 pairs); SK_TC_EMU overrides
+    static const int emu = [] { const char *e = getenv("SK_TC_EMU"); return e ? atoi(e) : (pair ? 1 : 2); }();
     TcArgs A;
     A.Aimg = (const unsigned char *)L.Aimg; A.Bimg = (const unsigned char *)L.Bimg; A.Bw = L.Bw;
     A.amax_p = L.amax_p; A.amax_q = L.amax_q;
-    A.P = L.P; A.Qtiles = (int)((L.Q + kTcM - 1) / kTcM); A.ksteps = L.ksteps;
-    A.blk_tiles = L.blk_tiles; A.split_q = L.split_q;
+    A.P = L.P; A.ksteps = L.ksteps;
+    A.split_q = L.split_q;
     A.part = L.part; A.tk = 2.f * kLog2e / L.eps; A.stop = L.stop; A.debug_acc = L.debug_acc;
     A.mma_only = L.mma_only;
     A.cyc = L.cyc;
     if (A.ksteps < 1 || A.ksteps > 4) return cudaErrorInvalidValue;
-    A.ptiles = (L.P + 2 * kTcM - 1) / (2 * kTcM);
+    A.ptiles = (L.P + kT2N - 1) / kT2N;
     A.nblk = L.nblk;
     const int items = A.ptiles * L.nblk * L.split_q;
+    if (pair) {
+        A.Qtiles = (int)((L.Q + kT2N - 1) / kT2N);
+        A.blk_tiles = L.blk_tiles;
+        switch (emu) {
+            case 0: return launch_tc2<0>(A, items, st);
+            case 2: return launch_tc2<2>(A, items, st);
+            case 3: return launch_tc2<3>(A, items, st);
+            default: return launch_tc2<1>(A, items, st);
+        }
+    }
+    // one-CTA kernel: Q tiles of 128 points (split ranges in the same units)
+    A.Qtiles = (int)((L.Q + kTcM - 1) / kTcM);
+    A.blk_tiles = 2 * L.blk_tiles;
     int nsm = 148, dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     dim3 grid(items < nsm ? items : nsm);
-    // fraction of the exponentials evaluated on the FMA pipe (of every 8 pairs); SK_TC_EMU overrides
-    static const int emu = [] { const char *e = getenv("SK_TC_EMU"); return e ? atoi(e) : 2; }();
     switch (emu) {
         case 0: return launch_tc_emu<0>(A, grid, st);
         case 1: return launch_tc_emu<1>(A, grid, st);
