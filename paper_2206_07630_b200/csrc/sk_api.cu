@@ -370,7 +370,11 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
     // stored mode with the fused sweep (one persistent CTA per SM): 8 blocks x split_q = one wave
     static const int fused_env = [] { const char *e = getenv("SK_FUSED"); return e ? atoi(e) : 1; }();
     const bool fused = stored && fused_env != 0 && stored_fused_supported(m);
-    const bool seedable = !stored && !tc;
+    const bool seedable = !stored;
+    if (tc) {   // the seeded passes' exact fallback reads the caller's coordinates
+        for (int i = 0; i < ns; ++i) X[i].raw = slices[i].x;
+        Y.raw = P.y;
+    }
     if (seedable || fused) {   // (the fused stored sweep seeds its row shifts the same way)
         ENSURE(xlse, float, B_XLSE, off[ns]);
         ENSURE(ylse, float, B_YLSE, m);
@@ -457,6 +461,7 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
                 TcPass colp{yimg, ximg + offi[i], X[i].pack, amax + 1, amax, (int)m, slices[i].n, ksteps,
                             sharded ? blk_per_rank : nblk_glob, (int)(bs_rows / tq), split_q, col_part(i),
                             P.eps, &status->stop, nullptr, 0};
+                if (col_seed && sweep >= 2) colp.seed = Y.lse;
                 CU(launch_lse_tc(colp, st));
             } else {
                 LsePass colp{&Y, &X[i], sharded ? blk_per_rank : nblk_glob, (int)(bs_rows / tq), split_q,
@@ -528,6 +533,7 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
                     TcPass rowp{ximg + offi[i], yimg, Y.pack, amax, amax + 1, (int)slices[i].n, m, ksteps, 1, 0,
                                 split_row, part,
                                 P.eps, &status->stop, nullptr, 0};
+                    if (row_seed && sweep >= 2) rowp.seed = X[i].lse;
                     CU(launch_lse_tc(rowp, st));
                 } else {
                     LsePass rowp{&X[i], &Y, 1, 0, split_row, part, P.eps, &status->stop};
@@ -1187,8 +1193,8 @@ static int nsm_probe(sk_ctx *ctx) {
 }
 
 sk_status sk_microbench(sk_ctx *ctx, int32_t kind, double *value) {
-    if (!ctx || !value || kind < 0 || (kind > 10 && kind < 100) || kind > 163)
-        return fail(ctx, SK_EINVAL, "kind in [0, 10] or [100, 163]");
+    if (!ctx || !value || kind < 0 || (kind > 12 && kind < 100) || kind > 163)
+        return fail(ctx, SK_EINVAL, "kind in [0, 12] or [100, 163]");
     if ((kind >= 5 && kind <= 8) || kind >= 100) {   // raw MMA issue rate of one shape, flop per SM clock
         ENSURE(scr, long long, B_OUT, 16);
         CU(microbench_mma(kind >= 100 ? kind - 100 : kind - 5, scr, ctx->stream, value));
@@ -1226,9 +1232,14 @@ sk_status sk_microbench(sk_ctx *ctx, int32_t kind, double *value) {
         CU(cudaMemsetAsync(amax, 0, 2 * sizeof(unsigned), st));
         CU(launch_fill(w, Q, 0.f, st));
         TcPass tp{img, img, w, amax, amax + 1, (int)P, Q, 4, 1, 0, 37, part, 1.f, nullptr, nullptr,
-                  (kind == 4 || kind == 10) ? 2 : 1};
+                  (kind == 4 || kind == 10) ? 2 : (kind == 11 ? 3 : (kind == 12 ? 4 : 1))};
         ENSURE(cyc, long long, B_FA, 16);
         tp.cyc = cyc;
+        if (kind == 11) {   // the epilogue probe runs the seeded (max-free) variant, as the solver does
+            ENSURE(seed, float, B_YLSE, P);
+            CU(launch_fill(seed, P, 0.f, st));
+            tp.seed = seed;
+        }
         CU(launch_lse_tc(tp, st));  // warm-up
         CU(cudaEventRecord(ctx->ev0, st));
         CU(launch_lse_tc(tp, st));

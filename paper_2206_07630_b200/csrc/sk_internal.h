@@ -56,6 +56,7 @@ struct Side {
     float *nk;        // [P] |p|^2 log2(e)/eps
     float *pot[2];    // double-buffered potential
     float *lse;       // [P] last merged LSE (log2 units): the seed of the next pass (nullable)
+    const float *raw = nullptr;  // PACK_TC: the caller's P x d fp32 coordinates (exact fallback of a seeded pass)
 };
 
 // Pack points (P x d, fp32 row-major), optional weights and initial potential.
@@ -82,6 +83,7 @@ struct TcPass {
     float *debug_acc;
     int mma_only = 0;
     long long *cyc = nullptr;   // K14: SM cycles of CTA 0
+    const float *seed = nullptr;  // seeded pass: fixed shift = seed[p] + margin (no running max); see k_merge
 };
 size_t tc_image_bytes(long long P);
 cudaError_t launch_absmax(const float *pts, long long cnt, unsigned *out, cudaStream_t st);  // out zeroed first

@@ -249,6 +249,22 @@ int merge_blocks(int P) {
 // packed tiles (coordinates + w): the fallback of a seeded pass.
 __device__ void exact_lse_point(const Side &S, const Side &Q, int p, float eps, float &M, float &Ssum) {
     const float tk = 2.f * kLog2e / eps;
+    if (S.D == 0) {
+        // tensor-core pass (PACK_TC): coordinates from the caller's fp32 arrays, w from the plain
+        // [P] array (tiles of tq points, no coordinates)
+        M = -INFINITY;
+        Ssum = 0.f;
+        const float *pp = S.raw + (long long)p * S.d;
+        for (long long q = 0; q < Q.P; ++q) {
+            const float *qq = Q.raw + q * Q.d;
+            float dot = 0.f;
+            for (int k = 0; k < S.d; ++k) dot = fmaf(pp[k], qq[k], dot);
+            const float v = fmaf(dot, tk, Q.pack[q]);
+            if (v > M) { Ssum = Ssum * ex2(M - v); M = v; }
+            Ssum += ex2(v - M);
+        }
+        return;
+    }
     const long long pt = p / S.tq, po = p % S.tq;
     const float *ptile = S.pack + pt * (long long)(S.D + 1) * S.tq;
     float pc[64];
@@ -270,13 +286,13 @@ __device__ void exact_lse_point(const Side &S, const Side &Q, int p, float eps, 
 
 // Merge of point p given its (M, Ssum) over all splits: new potential (+ packed w), fused
 // error term, non-finite and column-range flags.
-__device__ __forceinline__ void merge_point(const MergePass &Mp, const Side &S, int p, float M, float Ssum,
+__device__ __forceinline__ void merge_point(const MergePass &Mp, const Side &S, const Side &Qs, int p, float M, float Ssum,
                                             bool check, const float *hold, float *hnew, double &e, int &bad) {
     const float eps = Mp.eps, kap = kLog2e / eps, epsln2 = eps * kLn2;
     if (Mp.Q && !(Ssum >= 0x1p-100f && Ssum <= 0x1p100f)) {
         // seeded pass: the fixed shift was far from the true maximum -> exact recompute of
         // this point over the whole reduced side (rare; one thread, online max)
-        exact_lse_point(S, *Mp.Q, p, eps, M, Ssum);
+        exact_lse_point(S, Qs, p, eps, M, Ssum);   // (Mp.Q is a host pointer: only a flag here)
     }
     if (Mp.scaled && !(Ssum >= 0x1p-100f && Ssum <= 0x1p100f)) {
         // fused stored sweep: the scaled column mass left the safe range (an almost unmatched
@@ -318,7 +334,7 @@ constexpr int kWideMax = 32;      // splits per warp in the WIDE merge (nsplit <
 // points (coalesced rows of the partial array), the 8 warp partials are combined in a fixed
 // order by warp 0 (max first, then the rescaled sums) — deterministic.
 template <bool WIDE>
-__global__ void __launch_bounds__(kMT) k_merge(MergePass Mp, Side S) {
+__global__ void __launch_bounds__(kMT) k_merge(MergePass Mp, Side S, Side Qs) {
     __shared__ double red[kMT / 32];
     __shared__ int redi[kMT / 32];
     __shared__ int s_last;
@@ -364,7 +380,7 @@ __global__ void __launch_bounds__(kMT) k_merge(MergePass Mp, Side S) {
 #pragma unroll
                 for (int w = 1; w < NW; ++w) Ssum += wS[w][lane];
                 if (Mp.precomputed) bad |= !isfinite(hnew[p]);
-                else merge_point(Mp, S, p, M, Ssum, check, hold, hnew, e, bad);
+                else merge_point(Mp, S, Qs, p, M, Ssum, check, hold, hnew, e, bad);
             }
             __syncthreads();
         }
@@ -381,7 +397,7 @@ __global__ void __launch_bounds__(kMT) k_merge(MergePass Mp, Side S) {
                 const float2 v = Mp.part[(long long)s * S.P + p];
                 if (v.x != -INFINITY) Ssum += v.y * ex2(v.x - M);
             }
-            merge_point(Mp, S, p, M, Ssum, check, hold, hnew, e, bad);
+            merge_point(Mp, S, Qs, p, M, Ssum, check, hold, hnew, e, bad);
         }
     }
     if (!st) return;
@@ -435,12 +451,13 @@ __global__ void __launch_bounds__(kMT) k_merge(MergePass Mp, Side S) {
 constexpr int kWideSplits = 12;   // splits from which the merge uses the warp-per-split-group layout
 
 cudaError_t launch_merge(const MergePass &M, cudaStream_t st) {
+    const Side Qs = M.Q ? *M.Q : Side{};   // the reduced side by value (the fallback runs on the device)
     if (M.nsplit >= kWideSplits && M.nsplit <= kWideMax * (kMT / 32)) {
         int b = (M.S->P + 31) / 32;
         if (b > 1184) b = 1184;
-        k_merge<true><<<b, kMT, 0, st>>>(M, *M.S);
+        k_merge<true><<<b, kMT, 0, st>>>(M, *M.S, Qs);
     } else {
-        k_merge<false><<<merge_blocks(M.S->P), kMT, 0, st>>>(M, *M.S);
+        k_merge<false><<<merge_blocks(M.S->P), kMT, 0, st>>>(M, *M.S, Qs);
     }
     return cudaGetLastError();
 }

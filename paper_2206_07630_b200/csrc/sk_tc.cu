@@ -156,17 +156,22 @@ struct TcArgs {
     float tk;                   // 2 log2(e)/eps
     const int *stop;
     float *debug_acc;           // if non-null: write <p, q> (acc unscaled) of the first Q tile, [128][128]
-    int mma_only;               // K14 microbenchmark: epilogue only releases the buffers (2: and no B reloads)
+    int mma_only;               // K14 microbenchmark: epilogue only releases the buffers (2: and no B reloads;
+                                //   3: the pair kernel issues no MMAs, the epilogue runs in full;
+                                //   4: no MMAs, the epilogue only releases the buffers)
     long long *cyc;             // K14: SM cycles of CTA 0 (clock64 around the work), nullable
+    const float *seed;          // SEEDED (pair kernel): P side last LSE; shift = seed + seed_margin
+    float seed_margin;          // log2 units above the previous LSE (4, as K2; SK_TC_SEED_MARGIN
+                                // overrides it — a test knob that forces the exact fallback)
 };
 
 // exponentials of one 64-column chunk: 32 pairs, EMU of every 8 pairs on the FMA pipe
-template <int EMU>
-__device__ __forceinline__ float2 tc_sum_chunk(const float2 (&t)[32], float M) {
+template <int EMU, int NP = 32>
+__device__ __forceinline__ float2 tc_sum_chunk(const float2 (&t)[NP], float M) {
     const float2 mm = make_float2(M, M);
     float2 s0 = make_float2(0.f, 0.f), s1 = s0;
 #pragma unroll
-    for (int j = 0; j < 32; j += 2) {
+    for (int j = 0; j < NP; j += 2) {
         float2 e0 = sub2(t[j], mm), e1 = sub2(t[j + 1], mm);
         if ((j & 7) >= 8 - EMU) e0 = ex2_emu2(e0); else { e0.x = ex2(e0.x); e0.y = ex2(e0.y); }
         if (((j + 1) & 7) >= 8 - EMU) e1 = ex2_emu2(e1); else { e1.x = ex2(e1.x); e1.y = ex2(e1.y); }
@@ -369,9 +374,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lse_tc(TcArgs A) {
 //   warp 1   leader: TMEM allocation (both CTAs allocate, cta_group::2) and the MMA issuer;
 //            peer: relay — waits for its own A/B arrivals and arrives remotely on the leader's
 //            pair barriers (1D bulk copies signal their own CTA's mbarrier);
-//   warps 2-9 epilogue on this CTA's 128 accumulator rows: warp w = lane quadrant w % 4, column
-//            half (w - 2) / 4 (128 of the 256 columns); releases accumulator b remotely on the
-//            leader's tempty.  MMA completion is multicast to both CTAs' barriers.
+//   warps 2.. epilogue (NE warps) on this CTA's 128 accumulator rows: warp w = lane quadrant
+//            w % 4, column group (w - 2) / 4 (256 / (NE / 4) columns); releases accumulator b
+//            remotely on the leader's tempty.  MMA completion is multicast to both CTAs' barriers.
 constexpr int kT2Stages = 4;
 constexpr int kT2N = 256;                     // MMA N (B points per tile) and A points per item
 constexpr uint32_t kIdescF16M256N256 = (1u << 4) | ((uint32_t)(kT2N >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
@@ -407,8 +412,10 @@ __device__ __forceinline__ void umma2_commit_mc(uint64_t *bar) {
                  ::"r"(smem_u32(bar)), "h"((uint16_t)3) : "memory");
 }
 
-template <int EMU>
-__global__ void __launch_bounds__(kTcThreads, 1) k_lse_tc2(TcArgs A) {
+template <int EMU, int NE, bool SEEDED>
+__global__ void __launch_bounds__(64 + 32 * NE, 1) __maxnreg__(NE == 16 ? 112 : 168) k_lse_tc2(TcArgs A) {
+    constexpr int NQ = NE / 4;                       // epilogue warps per TMEM lane quadrant
+    constexpr int CW = kT2N / NQ;                    // accumulator columns per epilogue warp
     constexpr int ABUF = 2;
     constexpr int STAGE = 2 * kTcImg;                // own B half: hi + lo (128 points)
     extern __shared__ __align__(1024) unsigned char smraw[];
@@ -416,7 +423,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lse_tc2(TcArgs A) {
     unsigned char *sA = sm;                           // ABUF x [hi | lo] of this CTA's 128 A rows
     unsigned char *sB = sm + ABUF * 2 * kTcImg;       // kT2Stages x STAGE
     float *sW = reinterpret_cast<float *>(sB + kT2Stages * STAGE);   // kT2Stages x 256 w
-    float2 *xch = reinterpret_cast<float2 *>(sW + kT2Stages * kT2N); // 128 column-half partials
+    float2 *xch = reinterpret_cast<float2 *>(sW + kT2Stages * kT2N); // (NQ - 1) x 128 column-group partials
     __shared__ __align__(8) uint64_t full[kT2Stages], pfull[kT2Stages], empty[kT2Stages], tfull[2], tempty[2],
         afull[ABUF], pafull[ABUF], aempty[ABUF];
     __shared__ uint32_t tmem_base;
@@ -440,9 +447,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lse_tc2(TcArgs A) {
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < kT2Stages; ++i) {
-            mbar_init(&full[i], 1); mbar_init(&pfull[i], 1); mbar_init(&empty[i], 1 + kTcEpiWarps);
+            mbar_init(&full[i], 1); mbar_init(&pfull[i], 1); mbar_init(&empty[i], 1 + NE);
         }
-        for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 2 * kTcEpiWarps); }
+        for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 2 * NE); }
         for (int i = 0; i < ABUF; ++i) { mbar_init(&afull[i], 1); mbar_init(&pafull[i], 1); mbar_init(&aempty[i], 1); }
         fence_mbar_init();
     }
@@ -511,12 +518,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lse_tc2(TcArgs A) {
                     tc_fence_after();
                     const uint32_t b_hi = smem_u32(sB + st * STAGE), b_lo = b_hi + kTcImg;
                     const uint32_t d = tbase + (uint32_t)(b * kT2N);
-                    for (int k = 0; k < ks; ++k) {   // K = 16 halves = 32 bytes per step
+                    for (int k = 0; k < (A.mma_only >= 3 ? 0 : ks); ++k) {   // K = 16 halves = 32 bytes per step
                         const uint32_t koff = (uint32_t)k * 32;
                         umma2_f16(d, umma_desc_sw128(a_lo + koff), umma_desc_sw128(b_hi + koff), k > 0);
                         umma2_f16(d, umma_desc_sw128(a_hi + koff), umma_desc_sw128(b_lo + koff), 1);
                     }
-                    for (int k = 0; k < ks; ++k) {
+                    for (int k = 0; k < (A.mma_only >= 3 ? 0 : ks); ++k) {
                         const uint32_t koff = (uint32_t)k * 32;
                         umma2_f16(d, umma_desc_sw128(a_hi + koff), umma_desc_sw128(b_hi + koff), 1);
                     }
@@ -527,74 +534,85 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lse_tc2(TcArgs A) {
             }
         }
     } else {
-        // epilogue: this CTA's accumulator rows (TMEM lanes) q4*32 + lane, columns h*128 ..+127
-        const int q4 = warp & 3, h = (warp - 2) >> 2;
+        // epilogue: this CTA's accumulator rows (TMEM lanes) q4*32 + lane, columns hc*CW ..+CW-1
+        // in 64-column chunks.  (A software-pipelined variant — the next chunk's TMEM load in
+        // flight under the current chunk's exponentials — measured slower: the epilogue is bound
+        // by instruction issue next to MUFU, not by TMEM-load latency.)
+        const int q4 = warp & 3, hc = (warp - 2) >> 2;
         const int row = q4 * 32 + lane;
         const float tks = ldexpf(A.tk, tc_scale_exp(A.amax_p) + tc_scale_exp(A.amax_q));
         const float2 tk2 = make_float2(tks, tks);
         const float us = ldexpf(1.f, tc_scale_exp(A.amax_p) + tc_scale_exp(A.amax_q));  // exact unscale
         const uint32_t r_tempty = leader ? smem_u32(&tempty[0]) : mapa_u32(smem_u32(&tempty[0]), 0);
+        const bool full_epi = A.mma_only == 0 || A.mma_only == 3;   // 3: probe without MMAs
         int g = 0;
         for (int it = cid; it < items; it += ncl) {
             const int s = it / A.ptiles, pt = it % A.ptiles;
             int t0, nt;
             range(s, t0, nt);
             const int p = pt * kT2N + (int)rank * kTcM + row;
-            const bool dbg = A.debug_acc && leader && h == 0 && it == 0;
-            float M = -INFINITY, S = 0.f;
+            const bool dbg = A.debug_acc && leader && it == 0 && hc * CW < kTcM;
+            // seeded: fixed shift from the previous pass (no running max; k_merge recomputes a
+            // point exactly if its sum leaves [2^-100, 2^100]); padding rows use 0
+            float M = SEEDED ? (p < A.P ? A.seed[p] + A.seed_margin : 0.f) : -INFINITY, S = 0.f;
             for (int i = 0; i < nt; ++i, ++g) {
                 const int st = g % kT2Stages, b = g & 1;
                 mbar_wait_sleep(&tfull[b], (g >> 1) & 1);
                 tc_fence_after();
-                if (A.mma_only) {
+                if (!full_epi) {   // K14 probes 1, 2, 4: the epilogue only releases the buffers
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) { mbar_arrive_cluster(r_tempty + 8 * b); mbar_arrive(&empty[st]); }
                     continue;
                 }
-                const uint32_t taddr = tbase + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(b * kT2N + h * 128);
+                const uint32_t taddr = tbase + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(b * kT2N + hc * CW);
 #pragma unroll
-                for (int hh = 0; hh < 2; ++hh) {   // two 64-column chunks
-                    const float2 *w = reinterpret_cast<const float2 *>(sW + st * kT2N + h * 128 + hh * 64);
+                for (int hh = 0; hh < CW / 64; ++hh) {   // 64-column chunks
+                    const float2 *w = reinterpret_cast<const float2 *>(sW + st * kT2N + hc * CW + hh * 64);
                     uint32_t r[64];
                     TMEM_LD32(taddr + hh * 64, r);
                     TMEM_LD32(taddr + hh * 64 + 32, (r + 32));
                     tmem_ld_wait();
                     if (dbg && i == 0) {
 #pragma unroll
-                        for (int j = 0; j < 64; ++j) A.debug_acc[row * kTcM + hh * 64 + j] = __uint_as_float(r[j]) * us;
+                        for (int j = 0; j < 64; ++j) A.debug_acc[row * kTcM + hc * CW + hh * 64 + j] = __uint_as_float(r[j]) * us;
                     }
                     float2 t[32];
 #pragma unroll
                     for (int j = 0; j < 32; ++j)
                         t[j] = fma2(make_float2(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1])), tk2, w[j]);
-                    if (hh == 1) {
-                        // accumulator b (this CTA's half) and the w slot are no longer needed
+                    if (hh == CW / 64 - 1) {
+                        // accumulator b (this warp's columns) and the w slot are no longer needed
                         tc_fence_before();
                         __syncwarp();
                         if (lane == 0) { mbar_arrive_cluster(r_tempty + 8 * b); mbar_arrive(&empty[st]); }
                     }
-                    float m8[8];
+                    if constexpr (!SEEDED) {
+                        float m8[8];
 #pragma unroll
-                    for (int j = 0; j < 8; ++j)
-                        m8[j] = fmax3(fmaxf(t[4 * j].x, t[4 * j].y), fmax3(t[4 * j + 1].x, t[4 * j + 1].y, t[4 * j + 2].x),
-                                      fmax3(t[4 * j + 2].y, t[4 * j + 3].x, t[4 * j + 3].y));
-                    const float cm = fmax3(fmax3(m8[0], m8[1], m8[2]), fmax3(m8[3], m8[4], m8[5]), fmaxf(m8[6], m8[7]));
-                    if (cm > M) { S *= ex2(M - cm); M = cm; }
-                    if (M == -INFINITY) continue;  // only padding seen so far
+                        for (int j = 0; j < 8; ++j)
+                            m8[j] = fmax3(fmaxf(t[4 * j].x, t[4 * j].y), fmax3(t[4 * j + 1].x, t[4 * j + 1].y, t[4 * j + 2].x),
+                                          fmax3(t[4 * j + 2].y, t[4 * j + 3].x, t[4 * j + 3].y));
+                        const float cm = fmax3(fmax3(m8[0], m8[1], m8[2]), fmax3(m8[3], m8[4], m8[5]), fmaxf(m8[6], m8[7]));
+                        if (cm > M) { S *= ex2(M - cm); M = cm; }
+                        if (M == -INFINITY) continue;  // only padding seen so far
+                    }
                     const float2 sc = tc_sum_chunk<EMU>(t, M);
                     S += sc.x + sc.y;
                 }
             }
-            // combine the two column halves of each row (fixed order: half 0 then half 1)
-            if (h == 1) xch[row] = make_float2(M, S);
-            asm volatile("bar.sync 1, %0;" ::"r"(32 * kTcEpiWarps));
-            if (h == 0) {
-                const float2 o = xch[row];
-                lse_merge(M, S, o.x, o.y);
+            // combine the column groups of each row in fixed order (group 0, 1, ..)
+            if (hc > 0) xch[(hc - 1) * kTcM + row] = make_float2(M, S);
+            asm volatile("bar.sync 1, %0;" ::"r"(32 * NE));
+            if (hc == 0) {
+#pragma unroll
+                for (int k = 1; k < NQ; ++k) {
+                    const float2 o = xch[(k - 1) * kTcM + row];
+                    lse_merge(M, S, o.x, o.y);
+                }
                 if (p < A.P && !A.mma_only) A.part[(long long)s * A.P + p] = make_float2(M, S);
             }
-            asm volatile("bar.sync 1, %0;" ::"r"(32 * kTcEpiWarps));   // xch reuse
+            asm volatile("bar.sync 1, %0;" ::"r"(32 * NE));   // xch reuse
         }
     }
     tc_fence_before();
@@ -744,11 +762,12 @@ static cudaError_t launch_tc_emu(const TcArgs &A, dim3 grid, cudaStream_t st) {
     return abuf == 1 ? launch_tc_v<EMU, 1>(A, grid, st) : launch_tc_v<EMU, 2>(A, grid, st);
 }
 
-template <int EMU>
+template <int EMU, int NE, bool SEEDED>
 static cudaError_t launch_tc2(const TcArgs &A, int items, cudaStream_t st) {
     constexpr int ABUF = 2;
-    const size_t smem = 1024 + ABUF * 2 * (size_t)kTcImg + kT2Stages * (2 * (size_t)kTcImg + kT2N * 4) + kTcM * 8;
-    cudaError_t e = cudaFuncSetAttribute(k_lse_tc2<EMU>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const size_t smem = 1024 + ABUF * 2 * (size_t)kTcImg + kT2Stages * (2 * (size_t)kTcImg + kT2N * 4) +
+                        (NE / 4 - 1) * kTcM * 8;
+    cudaError_t e = cudaFuncSetAttribute(k_lse_tc2<EMU, NE, SEEDED>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int nsm = 148, dev = 0;
     cudaGetDevice(&dev);
@@ -756,7 +775,7 @@ static cudaError_t launch_tc2(const TcArgs &A, int items, cudaStream_t st) {
     const int ncl = std::max(1, std::min(items, nsm / 2));
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(2 * ncl);
-    cfg.blockDim = dim3(kTcThreads);
+    cfg.blockDim = dim3(64 + 32 * NE);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute at[1];
@@ -764,7 +783,16 @@ static cudaError_t launch_tc2(const TcArgs &A, int items, cudaStream_t st) {
     at[0].val.clusterDim.x = 2; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, k_lse_tc2<EMU>, A);
+    return cudaLaunchKernelEx(&cfg, k_lse_tc2<EMU, NE, SEEDED>, A);
+}
+
+template <int EMU>
+static cudaError_t launch_tc2_ne(const TcArgs &A, int items, cudaStream_t st) {
+    // SK_TC_EPI: epilogue warps of the pair kernel: 16 = four per TMEM lane quadrant (64 columns
+    // each); 8 = two per quadrant (128 columns each)
+    static const int ne = [] { const char *e = getenv("SK_TC_EPI"); return e ? atoi(e) : 16; }();
+    if (A.seed) return ne == 8 ? launch_tc2<EMU, 8, true>(A, items, st) : launch_tc2<EMU, 16, true>(A, items, st);
+    return ne == 8 ? launch_tc2<EMU, 8, false>(A, items, st) : launch_tc2<EMU, 16, false>(A, items, st);
 }
 
 int tc_points_per_tile() { return kT2N; }
@@ -784,6 +812,9 @@ cudaError_t launch_lse_tc(const TcPass &L, cudaStream_t st) {
     A.part = L.part; A.tk = 2.f * kLog2e / L.eps; A.stop = L.stop; A.debug_acc = L.debug_acc;
     A.mma_only = L.mma_only;
     A.cyc = L.cyc;
+    A.seed = pair ? L.seed : nullptr;   // (the one-CTA kernel always tracks the running max)
+    static const float margin = [] { const char *e = getenv("SK_TC_SEED_MARGIN"); return e ? (float)atof(e) : 4.f; }();
+    A.seed_margin = margin;
     if (A.ksteps < 1 || A.ksteps > 4) return cudaErrorInvalidValue;
     A.ptiles = (L.P + kT2N - 1) / kT2N;
     A.nblk = L.nblk;
@@ -792,10 +823,10 @@ cudaError_t launch_lse_tc(const TcPass &L, cudaStream_t st) {
         A.Qtiles = (int)((L.Q + kT2N - 1) / kT2N);
         A.blk_tiles = L.blk_tiles;
         switch (emu) {
-            case 0: return launch_tc2<0>(A, items, st);
-            case 2: return launch_tc2<2>(A, items, st);
-            case 3: return launch_tc2<3>(A, items, st);
-            default: return launch_tc2<1>(A, items, st);
+            case 0: return launch_tc2_ne<0>(A, items, st);
+            case 2: return launch_tc2_ne<2>(A, items, st);
+            case 3: return launch_tc2_ne<3>(A, items, st);
+            default: return launch_tc2_ne<1>(A, items, st);
         }
     }
     // one-CTA kernel: Q tiles of 128 points (split ranges in the same units)

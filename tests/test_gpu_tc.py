@@ -77,3 +77,31 @@ np.savez(sys.argv[1], f=f.cpu().numpy(), g=g.cpu().numpy(), it=r["iterations"])
     assert abs(int(a["it"]) - int(b["it"])) <= 1
     fa, fb = a["f"] - a["f"].mean(), b["f"] - b["f"].mean()
     assert np.abs(fa - fb).max() <= 1e-4 * max(np.abs(fb).max(), 1e-3)
+
+
+def test_tc_seeded_exact_fallback():
+    """The seeded tensor-core passes (fixed shift = previous LSE + margin) with a margin of 300
+    log2 units: every partial sum underflows, so k_merge must recompute every point exactly from
+    the fp32 coordinates; the result must still match the oracle in lockstep."""
+    code = r'''
+import sys, numpy as np, torch
+sys.path.insert(0, %r)
+import paper_2206_07630_b200 as sk
+from workloads import gen
+p = gen.c5(n=1100, d=48, eps_factor=2e-2)
+x, y = p.x[:700].copy(), p.y[:1100].copy()
+ctx = sk.Context(0)
+f, g, r = sk.sinkhorn_solve(ctx, torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda(), p.eps, mode="online")
+np.savez(sys.argv[1], f=f.cpu().numpy(), g=g.cpu().numpy(), it=r["iterations"], E=r["dual_objective"], eps=p.eps)
+''' % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    fn = f"/tmp/tc_fb_{os.getpid()}.npz"
+    subprocess.check_call([sys.executable, "-c", code, fn], env=dict(os.environ, SK_TC_SEED_MARGIN="300"))
+    a = np.load(fn)
+    from oracle import oracle as O
+    p = gen.c5(n=1100, d=48, eps_factor=2e-2)
+    x, y = p.x[:700].copy(), p.y[:1100].copy()
+    it = int(a["it"])
+    assert it > 3   # seeded passes (sweep >= 2) ran
+    lock = O.sinkhorn(x, y, float(a["eps"]), tol=0, max_iter=it)
+    assert_pair_close(a["f"], a["g"], lock.f, lock.g, float(a["eps"]))
+    assert_obj_close(float(a["E"]), lock.E, float(a["eps"]))
