@@ -313,7 +313,30 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
     // tensor-core cross term for d in (16, 64] (BJ.ns "only when d >= 32"; d in (16, 32] pads to
     // K = 32); SK_TC=0 forces the FFMA kernel (tuning / comparison knob)
     static const int tc_env = [] { const char *e = getenv("SK_TC"); return e ? atoi(e) : 1; }();
-    const bool tc = !stored && P.d > 16 && P.d <= 64 && tc_env != 0;
+    bool tc = !stored && P.d > 16 && P.d <= 64 && tc_env != 0;
+    unsigned *amax = nullptr;
+    if (tc) {
+        // per-side max |coordinate| (global over the ranks) -> the fold scales; a problem whose
+        // scaled coordinates would leave the fp16 range runs on the FFMA kernel instead
+        cudaError_t e1;
+        amax = (unsigned *)ensure(ctx, B_TCMAX, 2 * sizeof(unsigned), &e1);
+        if (!amax) return fail(ctx, SK_ENOMEM, "tensor-core scales");
+        CU(cudaMemsetAsync(amax, 0, 2 * sizeof(unsigned), st));
+        for (auto &sl : slices) CU(launch_absmax(sl.x, sl.n * P.d, amax, st));
+        CU(launch_absmax(P.y, m * P.d, amax + 1, st));
+        if (P.nccl && sharded) {
+            int r = g_nccl.allreduce(amax, amax, 1, kNcclFloat32, kNcclMax, ctx->comm, st);
+            if (r != 0) return fail(ctx, SK_ENCCL, "ncclAllReduce(max) failed");
+        }
+        unsigned h[2];
+        CU(cudaMemcpyAsync(h, amax, sizeof h, cudaMemcpyDeviceToHost, st));
+        CU(cudaStreamSynchronize(st));
+        float hx, hy;
+        memcpy(&hx, &h[0], 4);
+        memcpy(&hy, &h[1], 4);
+        tc = tc_fold_ok(hx, hy, P.eps);
+        ctx->cnt.kernel_launches += ns + 1;
+    }
     const int ksteps = (P.d + 15) / 16;
     const int D = (stored || tc) ? 0 : lse_dpad(P.d);
     if (!stored && !tc && D == 0) return fail(ctx, SK_EUNSUPPORTED, "online path supports d <= 64");
@@ -337,7 +360,6 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
     ENSURE(ypot, float, B_YPOT, 2 * m);
     ENSURE(status, DevStatus, B_STATUS, 1);
     char *ximg = nullptr, *yimg = nullptr;
-    unsigned *amax = nullptr;
     std::vector<long long> offi(ns + 1, 0);
     if (tc) {
         for (int i = 0; i < ns; ++i) offi[i + 1] = offi[i] + (long long)tc_image_bytes(slices[i].n);
@@ -345,19 +367,9 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
         ximg = (char *)ensure(ctx, B_XIMG, (size_t)offi[ns], &e1);
         yimg = (char *)ensure(ctx, B_YIMG, tc_image_bytes(m), &e2);
         if (!ximg || !yimg) return fail(ctx, SK_ENOMEM, "tensor-core operand images");
-        amax = (unsigned *)ensure(ctx, B_TCMAX, 2 * sizeof(unsigned), &e1);
-        if (!amax) return fail(ctx, SK_ENOMEM, "tensor-core scales");
-        // per-side max |coordinate| -> exact power-of-two operand scales (global over the ranks)
-        CU(cudaMemsetAsync(amax, 0, 2 * sizeof(unsigned), st));
-        for (int i = 0; i < ns; ++i) CU(launch_absmax(slices[i].x, slices[i].n * P.d, amax, st));
-        CU(launch_absmax(P.y, m * P.d, amax + 1, st));
-        if (P.nccl && sharded) {
-            int r = g_nccl.allreduce(amax, amax, 1, kNcclFloat32, kNcclMax, ctx->comm, st);
-            if (r != 0) return fail(ctx, SK_ENCCL, "ncclAllReduce(max) failed");
-        }
-        for (int i = 0; i < ns; ++i) CU(launch_pack_tc(slices[i].x, slices[i].n, P.d, amax, ximg + offi[i], st));
-        CU(launch_pack_tc(P.y, m, P.d, amax + 1, yimg, st));
-        ctx->cnt.kernel_launches += 2 * ns + 2;
+        for (int i = 0; i < ns; ++i) CU(launch_pack_tc(slices[i].x, slices[i].n, P.d, amax, 0, P.eps, ximg + offi[i], st));
+        CU(launch_pack_tc(P.y, m, P.d, amax, 1, P.eps, yimg, st));
+        ctx->cnt.kernel_launches += ns + 1;
     }
     std::vector<Side> X(ns);
     for (int i = 0; i < ns; ++i) {
@@ -372,8 +384,10 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
     const bool fused = stored && fused_env != 0 && stored_fused_supported(m);
     const bool seedable = !stored;
     if (tc) {   // the seeded passes' exact fallback reads the caller's coordinates
-        for (int i = 0; i < ns; ++i) X[i].raw = slices[i].x;
+        for (int i = 0; i < ns; ++i) { X[i].raw = slices[i].x; X[i].tcimg = (unsigned char *)ximg + offi[i]; X[i].tc_c = tc_fold_c(); }
         Y.raw = P.y;
+        Y.tcimg = (unsigned char *)yimg;
+        Y.tc_c = tc_fold_c();
     }
     if (seedable || fused) {   // (the fused stored sweep seeds its row shifts the same way)
         ENSURE(xlse, float, B_XLSE, off[ns]);
@@ -417,6 +431,12 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
     for (int i = 0; i < ns; ++i)
         CU(pack_side(X[i], slices[i].x, slices[i].a, loga_u, slices[i].f_init, P.eps, st, pmode));
     CU(pack_side(Y, P.y, P.b, logb_u, nullptr, P.eps, st, pmode));
+    if (tc) {   // extra columns: w from the packed sides, zero shifts
+        for (int i = 0; i < ns; ++i) CU(launch_pack_tc_ext(slices[i].n, X[i].pack, X[i].tcimg, st));
+        CU(launch_pack_tc_ext(m, Y.pack, Y.tcimg, st));
+        ctx->cnt.kernel_launches += ns + 1;
+    }
+    static const float tc_margin = [] { const char *e = getenv("SK_TC_SEED_MARGIN"); return e ? (float)atof(e) : 4.f; }();
     CU(launch_status_init(status, P.max_iter, P.check_every, P.tol, st));
     ctx->cnt.kernel_launches += ns + 2;
 
@@ -458,10 +478,10 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
                                 sharded ? blk_per_rank : nblk_glob, split_q, &status->stop, only_if};
                 CU(launch_stored_cols(scol, st));
             } else if (tc) {
-                TcPass colp{yimg, ximg + offi[i], X[i].pack, amax + 1, amax, (int)m, slices[i].n, ksteps,
+                TcPass colp{yimg, ximg + offi[i], (int)m, slices[i].n, ksteps,
                             sharded ? blk_per_rank : nblk_glob, (int)(bs_rows / tq), split_q, col_part(i),
-                            P.eps, &status->stop, nullptr, 0};
-                if (col_seed && sweep >= 2) colp.seed = Y.lse;
+                            P.eps, &status->stop};
+                colp.seeded = col_seed && sweep >= 2;
                 CU(launch_lse_tc(colp, st));
             } else {
                 LsePass colp{&Y, &X[i], sharded ? blk_per_rank : nblk_glob, (int)(bs_rows / tq), split_q,
@@ -480,11 +500,14 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
     mcol_redo.only_if = &status->colfail;
     const bool colredo = sharded;   // unsharded: the scaled merge recomputes a failing column itself
     if (!colredo && fused) { mcol_scaled.Cst = C[0]; mcol_scaled.xw = X[0].pack; mcol_scaled.n_rows = slices[0].n; }
-    auto exchange_and_merge_col = [&](const MergePass &mp) -> sk_status {
+    auto exchange_and_merge_col = [&](const MergePass &mp0) -> sk_status {
         if (P.nccl && sharded) {
             int r = g_nccl.allgather(col_part(0), part, (size_t)slot * 2, kNcclFloat32, ctx->comm, st);
             if (r != 0) return fail(ctx, SK_ENCCL, "ncclAllGather failed: %s", g_nccl.errstr ? g_nccl.errstr(r) : "?");
         }
+        MergePass mp = mp0;
+        mp.tc_fold = tc && col_seed && sweep >= 1;   // the next column pass is seeded
+        mp.tc_margin = tc_margin;
         CU(launch_merge(mp, st));
         return SK_OK;
     };
@@ -530,10 +553,9 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
                     StoredPass srow{C[i], slices[i].n, m, P.eps, Y.pack, part, 0, 1, 1, &status->stop};
                     CU(launch_stored_rows(srow, st));
                 } else if (tc) {
-                    TcPass rowp{ximg + offi[i], yimg, Y.pack, amax, amax + 1, (int)slices[i].n, m, ksteps, 1, 0,
-                                split_row, part,
-                                P.eps, &status->stop, nullptr, 0};
-                    if (row_seed && sweep >= 2) rowp.seed = X[i].lse;
+                    TcPass rowp{ximg + offi[i], yimg, (int)slices[i].n, m, ksteps, 1, 0, split_row, part,
+                                P.eps, &status->stop};
+                    rowp.seeded = row_seed && sweep >= 2;
                     CU(launch_lse_tc(rowp, st));
                 } else {
                     LsePass rowp{&X[i], &Y, 1, 0, split_row, part, P.eps, &status->stop};
@@ -545,6 +567,8 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
                 MergePass mrow{MERGE_ROW, &X[i], part, stored ? 1 : split_row, P.eps, nullptr, status, blke,
                                blkb, nullptr, 0.f, sharded ? 1 : 0, i + 1 < ns ? 1 : 0};
                 if (row_seed) mrow.Q = &Y;
+                mrow.tc_fold = tc && row_seed && sweep >= 1;   // the next row pass is seeded
+                mrow.tc_margin = tc_margin;
                 CU(launch_merge(mrow, st));
                 launched += 2;
             }
@@ -1170,17 +1194,26 @@ sk_status sk_selftest_tc_dot(sk_ctx *ctx, int32_t d, const float *x, const float
     ENSURE(ximg, char, B_XIMG, tc_image_bytes(128));
     ENSURE(yimg, char, B_YIMG, tc_image_bytes(128));
     ENSURE(amax, unsigned, B_TCMAX, 2);
-    ENSURE(w, float, B_SUBG, 128);
     ENSURE(part, float2, B_PART, 128);
     CU(cudaMemsetAsync(amax, 0, 2 * sizeof(unsigned), ctx->stream));
     CU(launch_absmax(dx, 128LL * d, amax, ctx->stream));
     CU(launch_absmax(dy, 128LL * d, amax + 1, ctx->stream));
-    CU(launch_pack_tc(dx, 128, d, amax, ximg, ctx->stream));
-    CU(launch_pack_tc(dy, 128, d, amax + 1, yimg, ctx->stream));
-    CU(launch_fill(w, 128, 0.f, ctx->stream));
-    TcPass tp{ximg, yimg, w, amax, amax + 1, 128, 128, ksteps, 1, 0, 1, part, 1.f, nullptr, dout, 0};
+    unsigned h[2];
+    CU(cudaMemcpyAsync(h, amax, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    float hx, hy;
+    memcpy(&hx, &h[0], 4);
+    memcpy(&hy, &h[1], 4);
+    if (!tc_fold_ok(hx, hy, 1.f)) return fail(ctx, SK_EUNSUPPORTED, "scaled coordinates outside the fp16 range");
+    // eps = 1: the accumulator is 2 log2(e) <x, y> (+ w - sh = 0); the kernel unscales it
+    CU(launch_pack_tc(dx, 128, d, amax, 0, 1.f, ximg, ctx->stream));
+    CU(launch_pack_tc(dy, 128, d, amax, 1, 1.f, yimg, ctx->stream));
+    CU(launch_pack_tc_ext(128, nullptr, ximg, ctx->stream));
+    CU(launch_pack_tc_ext(128, nullptr, yimg, ctx->stream));
+    TcPass tp{ximg, yimg, 128, 128, ksteps, 1, 0, 1, part, 1.f, nullptr};
+    tp.debug_acc = dout;
     CU(launch_lse_tc(tp, ctx->stream));
-    ctx->cnt.kernel_launches += 6;
+    ctx->cnt.kernel_launches += 7;
     CK(sg.flush());
     CU(cudaStreamSynchronize(ctx->stream));
     return SK_OK;
@@ -1224,22 +1257,15 @@ sk_status sk_microbench(sk_ctx *ctx, int32_t kind, double *value) {
         const long long P = 32768, Q = 32768;   // 256 x 256 tiles of 128 x 128 x 64, 3 fp16 MMAs each
         cudaError_t e1;
         char *img = (char *)ensure(ctx, B_XIMG, tc_image_bytes(P), &e1);
-        ENSURE(w, float, B_SUBG, Q);
         ENSURE(part, float2, B_PART, P * 37);
-        ENSURE(amax, unsigned, B_TCMAX, 2);
         if (!img) return fail(ctx, SK_ENOMEM, "tc probe images");
         CU(cudaMemsetAsync(img, 0, tc_image_bytes(P), st));
-        CU(cudaMemsetAsync(amax, 0, 2 * sizeof(unsigned), st));
-        CU(launch_fill(w, Q, 0.f, st));
-        TcPass tp{img, img, w, amax, amax + 1, (int)P, Q, 4, 1, 0, 37, part, 1.f, nullptr, nullptr,
-                  (kind == 4 || kind == 10) ? 2 : (kind == 11 ? 3 : (kind == 12 ? 4 : 1))};
+        CU(launch_pack_tc_ext(P, nullptr, img, st));   // w = 0, shifts 0
+        TcPass tp{img, img, (int)P, Q, 4, 1, 0, 37, part, 1.f, nullptr};
+        tp.mma_only = (kind == 4 || kind == 10) ? 2 : (kind == 11 ? 3 : (kind == 12 ? 4 : 1));
         ENSURE(cyc, long long, B_FA, 16);
         tp.cyc = cyc;
-        if (kind == 11) {   // the epilogue probe runs the seeded (max-free) variant, as the solver does
-            ENSURE(seed, float, B_YLSE, P);
-            CU(launch_fill(seed, P, 0.f, st));
-            tp.seed = seed;
-        }
+        tp.seeded = kind == 11;   // the epilogue probe runs the seeded (max-free) variant, as the solver does
         CU(launch_lse_tc(tp, st));  // warm-up
         CU(cudaEventRecord(ctx->ev0, st));
         CU(launch_lse_tc(tp, st));

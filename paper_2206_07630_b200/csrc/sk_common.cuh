@@ -2,6 +2,7 @@
 // (PTX wrappers: MUFU ex2, packed FP32x2 FFMA2/FADD2, mbarrier + 1D bulk TMA.)
 #pragma once
 
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -140,6 +141,60 @@ __device__ __forceinline__ int block_or(int v, int *scratch /* NT/32 */) {
 #pragma unroll
     for (int i = 0; i < NT / 32; ++i) s |= scratch[i];
     return s;
+}
+
+}  // namespace sk
+
+// ------------------------------------------- K3 tensor-core image layout (shared with K6)
+// One side of P points as images for tcgen05.mma (tiles of 128 points, padded to a multiple of
+// 256 = one CTA-pair tile), in one allocation:
+//   [T x (hi | lo)]   T = tc_tiles(P) tiles of 2 x 16 KB: fp16 hi/lo split of alpha x, K-major
+//                     SWIZZLE_128B (row r of a tile: 128 bytes = 64 halves)
+//   [T x EA]          4 KB per tile, K-major SWIZZLE_32B (16 halves per row): the "A role" extra
+//                     columns [-sh/c, 0, 0, c, c, c, 0 ..]    (sh: the point's folded shift)
+//   [T x EB]          4 KB per tile: the "B role" extra columns [c, 0, 0, w1, w2, w3, 0 ..]
+//                     with w1 + w2 + w3 = w / c (three fp16 pieces, ~33 bits)
+//   [T x 128 floats]  sh, exact (= -c * EA[0])
+// so that one extra K = 16 MMA of EA(p) against EB(q) adds w_q - sh_p to the accumulator.
+namespace sk {
+constexpr int kTcImgBytes = 128 * 128;   // one SW128 image tile (128 rows x 128 bytes)
+constexpr int kTcExtBytes = 128 * 32;    // one SW32 extra tile (128 rows x 32 bytes)
+__host__ __device__ inline long long tc_tiles(long long P) { return (P + 255) / 256 * 2; }
+__host__ __device__ inline long long tc_ea_off(long long P) { return tc_tiles(P) * 2 * kTcImgBytes; }
+__host__ __device__ inline long long tc_eb_off(long long P) { return tc_ea_off(P) + tc_tiles(P) * kTcExtBytes; }
+__host__ __device__ inline long long tc_sh_off(long long P) { return tc_eb_off(P) + tc_tiles(P) * kTcExtBytes; }
+__host__ __device__ inline long long tc_side_bytes(long long P) { return tc_sh_off(P) + tc_tiles(P) * 128 * 4; }
+// byte offset of half `slot` (0..15) of point p inside an extra image (SW32: the 16-byte chunk
+// index is XORed with bit 2 of the row)
+__device__ __forceinline__ long long tc_ext_at(long long p, int slot) {
+    const long long t = p >> 7;
+    const int r = (int)(p & 127), ch = slot >> 3;
+    return t * kTcExtBytes + (r >> 3) * 256 + (r & 7) * 32 + ((ch ^ ((r >> 2) & 1)) << 4) + (slot & 7) * 2;
+}
+// EB slots 3..5 of point p: w / c as three fp16 pieces (w = -inf: [-inf, 0, 0])
+__device__ __forceinline__ void tc_put_w(unsigned char *img, long long P, long long p, float w, float c) {
+    unsigned char *eb = img + tc_eb_off(P);
+    __half h1, h2 = __float2half_rn(0.f), h3 = h2;
+    if (w == -INFINITY) {
+        h1 = __float2half_rn(-INFINITY);
+    } else {
+        const float v = w / c;
+        h1 = __float2half_rn(v);
+        const float r1 = v - __half2float(h1);
+        h2 = __float2half_rn(r1);
+        h3 = __float2half_rn(r1 - __half2float(h2));
+    }
+    *reinterpret_cast<__half *>(eb + tc_ext_at(p, 3)) = h1;
+    *reinterpret_cast<__half *>(eb + tc_ext_at(p, 4)) = h2;
+    *reinterpret_cast<__half *>(eb + tc_ext_at(p, 5)) = h3;
+}
+// EA slot 0 of point p: the shift rounded to c * fp16; returns the exact shift stored in sh[p]
+__device__ __forceinline__ float tc_put_shift(unsigned char *img, long long P, long long p, float sh, float c) {
+    const __half h = __float2half_rn(isfinite(sh) ? sh / c : 0.f);
+    const float exact = __half2float(h) * c;
+    *reinterpret_cast<__half *>(img + tc_ea_off(P) + tc_ext_at(p, 0)) = __hneg(h);
+    reinterpret_cast<float *>(img + tc_sh_off(P))[p] = exact;
+    return exact;
 }
 
 }  // namespace sk

@@ -57,6 +57,8 @@ struct Side {
     float *pot[2];    // double-buffered potential
     float *lse;       // [P] last merged LSE (log2 units): the seed of the next pass (nullable)
     const float *raw = nullptr;  // PACK_TC: the caller's P x d fp32 coordinates (exact fallback of a seeded pass)
+    unsigned char *tcimg = nullptr;  // PACK_TC: the side's K3 images (K6 rewrites w and the shift)
+    float tc_c = 16.f;               //          c of the extra columns
 };
 
 // Pack points (P x d, fp32 row-major), optional weights and initial potential.
@@ -68,26 +70,31 @@ cudaError_t pack_side(const Side &S, const float *pts, const float *wts, float l
                       const float *pot0, float eps, cudaStream_t st, int mode = -1);
 
 // ------------------------------------------------------- K3 tensor-core pass
-// Images: per tile of 128 points [hi | lo] fp16, K-major SW128, K padded to 64 (d <= 64);
-// each side scaled by 2^-e from its max |coordinate| (amax, a device uint: float bits).
+// Per side one image allocation (layout in sk_common.cuh): fp16 hi/lo of alpha x (K-major
+// SW128, K padded to 64, tiles of 128 points padded to 256) plus the extra-column images EA/EB
+// (w and the row shift folded into the MMA) and the exact shifts.  The x side is scaled by 2^s,
+// the y side by (2 log2(e)/eps) 2^-s (s from both sides' max |coordinate|, amax2 = [x, y] as
+// device uint float bits), so the accumulator is the log2-domain exponent minus the row shift.
 struct TcPass {
-    const void *Aimg, *Bimg;    // images of the output side (A) and the reduced side (B)
-    const float *Bw;            // reduced side w (D = 0 pack, tq = 128)
-    const unsigned *amax_p, *amax_q;
+    const void *Aimg, *Bimg;    // images of the output side (A, P points) and the reduced side (B)
     int P;  long long Q;
     int ksteps;                 // ceil(d / 16): K = 16 MMA steps
-    int nblk, blk_tiles, split_q;
+    int nblk, blk_tiles, split_q;   // Q split structure in tiles of 256 points
     float2 *part;
     float eps;
     const int *stop;
-    float *debug_acc;
+    float *debug_acc = nullptr;
     int mma_only = 0;
     long long *cyc = nullptr;   // K14: SM cycles of CTA 0
-    const float *seed = nullptr;  // seeded pass: fixed shift = seed[p] + margin (no running max); see k_merge
+    int seeded = 0;             // the output side's shifts were folded by K6 (max-free pass)
 };
 size_t tc_image_bytes(long long P);
 cudaError_t launch_absmax(const float *pts, long long cnt, unsigned *out, cudaStream_t st);  // out zeroed first
-cudaError_t launch_pack_tc(const float *pts, long long P, int d, const unsigned *amax, void *img, cudaStream_t st);
+cudaError_t launch_pack_tc(const float *pts, long long P, int d, const unsigned *amax2, int role, float eps,
+                           void *img, cudaStream_t st);   // role 0: x side, 1: y side
+cudaError_t launch_pack_tc_ext(long long P, const float *w, void *img, cudaStream_t st);  // w: plain [P] (nullable = 0)
+bool tc_fold_ok(float amax_x, float amax_y, float eps);   // both scaled sides within fp16 range
+float tc_fold_c();                                         // c of the extra columns
 cudaError_t launch_lse_tc(const TcPass &L, cudaStream_t st);
 int tc_points_per_tile();  // K3 tile: 256 output points per CTA pair, 256 reduction points per B tile
 
@@ -128,6 +135,8 @@ struct MergePass {
     const float *xw = nullptr;    //         and the X side w = f kappa (n_rows)
     long long n_rows = 0;
     const int *only_if = nullptr;  // run only if *only_if != 0 (the exact column fallback)
+    int tc_fold = 0;          // K3 side: also fold lse + margin as the next pass's row shift
+    float tc_margin = 4.f;    //          log2 units above the LSE (SK_TC_SEED_MARGIN: test knob)
 };
 cudaError_t launch_merge(const MergePass &M, cudaStream_t st);
 int merge_blocks(int P);

@@ -320,7 +320,12 @@ __device__ __forceinline__ void merge_point(const MergePass &Mp, const Side &S, 
     const float hn = S.c[p] - epsln2 * lse2;
     hnew[p] = hn;
     const long long t = p / S.tq, o = p % S.tq;
-    S.pack[t * (long long)(S.D + 1) * S.tq + (long long)S.D * S.tq + o] = fmaf(hn, kap, -S.nk[p]);
+    const float wn = fmaf(hn, kap, -S.nk[p]);
+    S.pack[t * (long long)(S.D + 1) * S.tq + (long long)S.D * S.tq + o] = wn;
+    if (S.tcimg) {   // K3 side: w into the B-role extra columns, the next row shift into the A role
+        tc_put_w(S.tcimg, S.P, p, wn, S.tc_c);
+        if (Mp.tc_fold) tc_put_shift(S.tcimg, S.P, p, lse2 + Mp.tc_margin, S.tc_c);
+    }
     bad |= !isfinite(hn);
     if (check) {
         const double bj = Mp.wts ? (double)Mp.wts[p] : 1.0 / S.P;

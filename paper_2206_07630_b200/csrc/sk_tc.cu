@@ -1,36 +1,29 @@
 // sk_tc.cu — K3: the online LSE pass with the cross term on the 5th-generation tensor
-// cores (tcgen05, kind::f16 with fp16 operands, fp32 accumulators in TMEM), for d in (16, 64].
+// cores (tcgen05.mma kind::f16, fp16 operands, fp32 accumulators in TMEM), for d in (16, 64].
 //
 // BJ.ns: "computes the -2<x,y> cross term on tensor cores only when d >= 32, using an
 // error-compensated 3xTF32/bf16x3 split".  This kernel uses the same three-product split with
-// IEEE fp16 pieces, which runs at twice the TF32 tensor rate and carries the same 22-bit
-// significand: each side is first scaled by an exact power of two s = 2^-e so that
-// max |s x| lies in [1/2, 1) (K3a absmax), then every coordinate is split once per solve into
-//     hi = fp16(s x),  lo = fp16(s x - hi)      (11 + 11 significand bits)
-// and stored as MMA-ready images (K-major, 128-byte swizzle, tiles of 128 points, K padded to
-// 64).  acc = <s_p p, s_q q> is accumulated as
-//     lo_p . hi_q + hi_p . lo_q + hi_p . hi_q      (3 MMAs per K = 16 step; lo.lo dropped)
-// which is fp32-accurate (error ~2^-22 max|p| max|q| per term); the epilogue folds 1/(s_p s_q)
-// (exact) into the log2-domain scale.  Power-of-two scaling commutes with every fp16/fp32
-// rounding above the subnormal range, so the scale choice does not change the result; the
-// sharded path still takes it from the global maximum (identical on every rank).
+// IEEE fp16 pieces (twice the TF32 tensor rate, the same 22-bit significand).  Per solve, each
+// side is scaled once — x by alpha_x = 2^s, y by alpha_y = tk 2^-s with tk = 2 log2(e)/eps and
+// the integer s balancing the two magnitudes (K3a absmax) — and split into
+//     hi = fp16(alpha x),  lo = fp16(alpha x - hi)        (11 + 11 significand bits)
+// stored as MMA-ready images (K-major, 128-byte swizzle, tiles of 128 points, K padded to 64).
+// The accumulator of a (p, q) entry is
+//     lo_p . hi_q + hi_p . lo_q + hi_p . hi_q  +  EA_p . EB_q
+//   = tk <p, q>  +  w_q - sh_p          (3 x ksteps + 1 MMAs of K = 16; lo.lo dropped)
+// where the extra K = 16 step multiplies the output point's "A role" columns (its shift sh_p)
+// against the reduced point's "B role" columns (w_q = (h_q - |q|^2) log2(e)/eps in three fp16
+// pieces; layout in sk_common.cuh).  So the accumulator IS the log2-domain exponent minus the
+// row shift: the epilogue is one tcgen05.ld and one exponential per entry (seeded passes: no
+// max, no multiply, no w load).  K6 rewrites w and sh of a side after every merge.
 //
-// CTA = 256 output points (two 128-row A tiles, TMEM lanes) x one split of the other side;
-// every B tile of 128 reduction points is multiplied against both A tiles, so the B operand
-// stream from L2 is 1 byte per cost entry (the L2 -> SM bandwidth bound of a 128-row tile):
-//   warp 0   producer: 1D bulk TMA of the A images (once) and of B tile images + w tiles
-//            into a kTcStages-deep ring (mbarrier complete_tx);
-//   warp 1   TMEM allocation (512 columns = 2 buffers x 2 A tiles x 128) and the MMA issuer
-//            (one elected thread): 2 x 3 x ksteps MMAs 128x128x16 per B tile, tcgen05.commit
-//            to the smem-slot and accumulator-ready barriers;
-//   warps 2-9 epilogue: warp w owns TMEM lane quadrant w % 4 of A tile (w - 2) / 4: one output
-//            point per thread, all 128 columns; tcgen05.ld, t = acc * 2 log2(e)/(eps s_p s_q)
-//            + w_q (FFMA2), online (max, sum 2^(t - max)) per 64 columns (FMNMX3 tree,
-//            exponentials on MUFU.EX2 with a fraction on the FMA pipe, FADD2).
+// CTA pair (cta_group::2), persistent: the pair computes 256 x 256 tiles (A: 128 output points
+// per CTA; B: 128 reduction points per CTA), two TMEM accumulator buffers of 256 columns.
 // The output is the same (max, sum) partial as the FFMA kernel (K2), merged by K6.
 #include <cuda_fp16.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 
 #include "sk_internal.h"
@@ -39,10 +32,9 @@
 
 namespace sk {
 
-constexpr int kTcM = 128;       // points per tile (MMA M and N)
-constexpr int kTcEpiWarps = 8;  // two per TMEM lane quadrant (one per A tile)
-constexpr int kTcThreads = 64 + 32 * kTcEpiWarps;
-constexpr int kTcImg = kTcM * 128;  // bytes of one fp16 image: 128 rows x 64 halves (16 SW128 atoms)
+constexpr int kTcM = 128;                 // points per image tile (MMA rows per CTA)
+constexpr int kTcImg = kTcImgBytes;       // bytes of one fp16 image: 128 rows x 64 halves (16 SW128 atoms)
+constexpr float kTcFoldC = 16.f;          // c of the extra columns (sh and w range |.| < 2^20)
 
 // ------------------------------------------------------------ operand images
 // K3a: max |x| over all coordinates (non-negative floats order like their bit patterns).
@@ -55,21 +47,26 @@ __global__ void k_absmax(const float *__restrict__ pts, long long cnt, unsigned 
     if ((threadIdx.x & 31) == 0 && mx > 0.f) atomicMax(out, __float_as_uint(mx));
 }
 
-// exponent e with max = f 2^e, f in [1/2, 1): the side's scale is 2^-e (1 for an all-zero side)
-__device__ __forceinline__ int tc_scale_exp(const unsigned *amax) {
-    const float mx = __uint_as_float(*amax);
+// exponent e with max = f 2^e, f in [1/2, 1) (0 for an all-zero side)
+__host__ __device__ inline int tc_exp_of(float mx) {
     int e = 0;
     if (mx > 0.f) frexpf(mx, &e);
     return e;
 }
+// the balancing exponent s: max |alpha_x x| ~ 2^(ex + s), max |alpha_y y| ~ tk 2^(ey - s)
+__host__ __device__ inline int tc_fold_s(float ax, float ay, float tk) {
+    return (int)rintf(0.5f * (log2f(tk) + (float)tc_exp_of(ay) - (float)tc_exp_of(ax)));
+}
 
-// img: tiles of 128 points, each [hi image | lo image], K-major SWIZZLE_128B canonical
-// layout: 8-row x 128-byte atoms, atom mi at mi * 1024 bytes, the 16-byte chunk c (halves
-// 8c .. 8c+7) of row r stored at chunk c ^ (r % 8).  One thread per (point, chunk).
-__global__ void k_pack_tc(const float *__restrict__ pts, long long P, long long P2, int d, const unsigned *amax,
-                          unsigned char *img) {
+// img: tiles of 128 points, each [hi image | lo image] of alpha * x, K-major SWIZZLE_128B
+// canonical layout: 8-row x 128-byte atoms, atom mi at mi * 1024 bytes, the 16-byte chunk c
+// (halves 8c .. 8c+7) of row r stored at chunk c ^ (r % 8).  One thread per (point, chunk).
+// role 0 (x side): alpha = 2^s; role 1 (y side): alpha = tk 2^-s.
+__global__ void k_pack_tc(const float *__restrict__ pts, long long P, long long P2, int d, const unsigned *amax2,
+                          int role, float tk, unsigned char *img) {
     const long long total = P2 * 8;
-    const float sc = ldexpf(1.f, -tc_scale_exp(amax));
+    const int s = tc_fold_s(__uint_as_float(amax2[0]), __uint_as_float(amax2[1]), tk);
+    const float alpha = role == 0 ? ldexpf(1.f, s) : ldexpf(tk, -s);
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
          e += (long long)gridDim.x * blockDim.x) {
         const long long p = e >> 3;
@@ -80,7 +77,7 @@ __global__ void k_pack_tc(const float *__restrict__ pts, long long P, long long 
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
             const int k = 8 * c + j;
-            const float x = (p < P && k < d) ? pts[p * d + k] * sc : 0.f;
+            const float x = (p < P && k < d) ? pts[p * d + k] * alpha : 0.f;
             hi[j] = __float2half_rn(x);
             lo[j] = __float2half_rn(x - __half2float(hi[j]));
         }
@@ -88,6 +85,22 @@ __global__ void k_pack_tc(const float *__restrict__ pts, long long P, long long 
         unsigned char *base = img + t * 2LL * kTcImg;
         *reinterpret_cast<uint4 *>(base + off) = *reinterpret_cast<const uint4 *>(hi);
         *reinterpret_cast<uint4 *>(base + kTcImg + off) = *reinterpret_cast<const uint4 *>(lo);
+    }
+}
+
+// K3b: the extra columns of every point: EA = [0, 0, 0, c, c, c, 0 ..] (shift 0), EB = [c, 0, 0,
+// w pieces, 0 ..] from the plain w array (w == nullptr: 0; padding points: w = -inf), sh = 0.
+__global__ void k_pack_tc_ext(long long P, long long P2, const float *__restrict__ w, float c, unsigned char *img) {
+    for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < P2; p += (long long)gridDim.x * blockDim.x) {
+        unsigned char *ea = img + tc_ea_off(P), *eb = img + tc_eb_off(P);
+        const __half z = __float2half_rn(0.f), ch = __float2half_rn(c);
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            *reinterpret_cast<__half *>(ea + tc_ext_at(p, k)) = (k >= 3 && k <= 5) ? ch : z;
+            *reinterpret_cast<__half *>(eb + tc_ext_at(p, k)) = (k == 0) ? ch : z;
+        }
+        reinterpret_cast<float *>(img + tc_sh_off(P))[p] = 0.f;
+        tc_put_w(img, P, p, p < P ? (w ? w[p] : 0.f) : -INFINITY, c);
     }
 }
 
@@ -102,7 +115,18 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
     return desc;
 }
 
-// kind::f16, D = F32, A = B = F16, both K-major, M = 128, N = 128
+// SWIZZLE_32B K-major (the 16-half extra images): 8-row groups of 256 bytes
+__device__ __forceinline__ uint64_t umma_desc_sw32(uint32_t saddr) {
+    uint64_t desc = 0;
+    desc |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    desc |= (uint64_t)1 << 16;
+    desc |= (uint64_t)(256 >> 4) << 32;                  // SBO: 8 rows x 32 bytes
+    desc |= (uint64_t)1 << 46;
+    desc |= (uint64_t)6 << 61;                           // SWIZZLE_32B
+    return desc;
+}
+
+// kind::f16, D = F32, A = B = F16, both K-major, M = 128, N = 128 (K14 probe shape)
 constexpr uint32_t kIdescF16 = (1u << 4) | ((uint32_t)(kTcM >> 3) << 17) | ((uint32_t)(kTcM >> 4) << 24);
 
 __device__ __forceinline__ void umma_f16(uint32_t dtmem, uint64_t adesc, uint64_t bdesc, uint32_t accum) {
@@ -146,33 +170,29 @@ __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.
 
 // ------------------------------------------------------------------ the kernel
 struct TcArgs {
-    const unsigned char *Aimg;  // P side images
-    const unsigned char *Bimg;  // Q side images
-    const float *Bw;            // Q side packed w, [Qtiles][128] (D = 0 style plain array, padded -inf)
-    const unsigned *amax_p, *amax_q;  // per-side max |coordinate| (scales)
-    int P, Qtiles, ksteps, ptiles;
-    int nblk, blk_tiles, split_q;   // Q split structure (as K2)
+    const unsigned char *Aimg;  // output side images (P points) incl. EA, sh
+    const unsigned char *Bimg;  // reduced side images (Q points) incl. EB
+    int P, Q, Qtiles, ksteps, ptiles;
+    int nblk, blk_tiles, split_q;   // Q split structure (as K2), in tiles of 256 points
     float2 *part;
-    float tk;                   // 2 log2(e)/eps
+    float tk;                   // 2 log2(e)/eps (only the selftest's unscale uses it)
     const int *stop;
-    float *debug_acc;           // if non-null: write <p, q> (acc unscaled) of the first Q tile, [128][128]
-    int mma_only;               // K14 microbenchmark: epilogue only releases the buffers (2: and no B reloads;
-                                //   3: the pair kernel issues no MMAs, the epilogue runs in full;
-                                //   4: no MMAs, the epilogue only releases the buffers)
+    float *debug_acc;           // if non-null: write <p, q> of the first 128 x 128 block, [128][128]
+    int mma_only;               // K14 probes: 1, 2, 4 = the epilogue only releases the buffers;
+                                //   3 = no MMAs, the epilogue runs in full
     long long *cyc;             // K14: SM cycles of CTA 0 (clock64 around the work), nullable
-    const float *seed;          // SEEDED (pair kernel): P side last LSE; shift = seed + seed_margin
-    float seed_margin;          // log2 units above the previous LSE (4, as K2; SK_TC_SEED_MARGIN
-                                // overrides it — a test knob that forces the exact fallback)
 };
 
-// exponentials of one 64-column chunk: 32 pairs, EMU of every 8 pairs on the FMA pipe
-template <int EMU, int NP = 32>
-__device__ __forceinline__ float2 tc_sum_chunk(const float2 (&t)[NP], float M) {
+// sum of 2^(t - M) over one 64-column chunk (32 pairs), EMU of every 8 pairs on the FMA pipe;
+// SUB = false: M = 0 (seeded passes: the shift is already in the accumulator)
+template <int EMU, bool SUB>
+__device__ __forceinline__ float2 tc_sum_chunk(const float2 (&t)[32], float M) {
     const float2 mm = make_float2(M, M);
     float2 s0 = make_float2(0.f, 0.f), s1 = s0;
 #pragma unroll
-    for (int j = 0; j < NP; j += 2) {
-        float2 e0 = sub2(t[j], mm), e1 = sub2(t[j + 1], mm);
+    for (int j = 0; j < 32; j += 2) {
+        float2 e0 = t[j], e1 = t[j + 1];
+        if constexpr (SUB) { e0 = sub2(e0, mm); e1 = sub2(e1, mm); }
         if ((j & 7) >= 8 - EMU) e0 = ex2_emu2(e0); else { e0.x = ex2(e0.x); e0.y = ex2(e0.y); }
         if (((j + 1) & 7) >= 8 - EMU) e1 = ex2_emu2(e1); else { e1.x = ex2(e1.x); e1.y = ex2(e1.y); }
         s0 = add2(s0, e0);
@@ -181,203 +201,17 @@ __device__ __forceinline__ float2 tc_sum_chunk(const float2 (&t)[NP], float M) {
     return add2(s0, s1);
 }
 
-// smem: ABUF A buffers (64 KB each) + a B ring of tc_stages(ABUF) x (32 KB + 512 B)
-__host__ __device__ constexpr int tc_stages(int abuf) { return abuf == 2 ? 2 : 4; }
-// Persistent: one CTA per SM walks the work items (A tile pair pt, split s), item =
-// s * ptiles + pt, items blockIdx.x, blockIdx.x + gridDim.x, ...  (concurrent CTAs share the
-// split's B tiles in L2).  The B ring, the two accumulator buffers and the two A buffers are
-// carried across items, so the next item's A images load while the current item computes.
-template <int EMU, int ABUF>
-__global__ void __launch_bounds__(kTcThreads, 1) k_lse_tc(TcArgs A) {
-    constexpr int kTcStages = tc_stages(ABUF);
-    constexpr int STAGE = 2 * kTcImg;               // B hi + lo (1024-aligned slots)
-    extern __shared__ __align__(1024) unsigned char smraw[];
-    // 1024-byte alignment of the dynamic smem window for the swizzled operands
-    unsigned char *sm = smraw + ((1024 - (smem_u32(smraw) & 1023)) & 1023);
-    unsigned char *sA = sm;                          // ABUF buffers x 2 A tiles x [hi | lo]
-    unsigned char *sB = sm + ABUF * 4 * kTcImg;      // kTcStages x STAGE
-    float *sW = reinterpret_cast<float *>(sB + kTcStages * STAGE);  // kTcStages x 128 w values
-    __shared__ __align__(8) uint64_t full[kTcStages], empty[kTcStages], tfull[2], tempty[2], afull[2], aempty[2];
-    __shared__ uint32_t tmem_base;
-
-    if (A.stop && *(volatile const int *)A.stop) return;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nsplit = A.nblk * A.split_q;
-    const int items = A.ptiles * nsplit;
-    const int bt = A.blk_tiles > 0 ? A.blk_tiles : A.Qtiles;
-    // B tile range [t0, t0 + nt) of split s (fixed partition: block s / split_q, sub-split s % split_q)
-    auto range = [&](int s, int &t0, int &nt) {
-        const int bq = s / A.split_q, u = s % A.split_q;
-        const int base = bq * bt;
-        const int nt_b = max(0, min(bt, A.Qtiles - base));
-        t0 = base + (int)((long long)nt_b * u / A.split_q);
-        nt = base + (int)((long long)nt_b * (u + 1) / A.split_q) - t0;
-    };
-
-    if (threadIdx.x == 0) {
-        for (int i = 0; i < kTcStages; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1 + kTcEpiWarps); }
-        for (int i = 0; i < 2; ++i) {
-            mbar_init(&tfull[i], 1); mbar_init(&tempty[i], kTcEpiWarps);
-            mbar_init(&afull[i], 1); mbar_init(&aempty[i], 1);
-        }
-        fence_mbar_init();
-    }
-    if (warp == 1) {  // 512 TMEM columns: accumulator (buffer b, A tile a) at column (2b + a) * 128
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base)));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    }
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tbase = tmem_base;
-    const long long clk0 = clock64();
-
-    if (warp == 0) {
-        if (lane == 0) {
-            int g = 0, c = 0;
-            for (int it = blockIdx.x; it < items; it += gridDim.x, ++c) {
-                const int s = it / A.ptiles, pt = it % A.ptiles;
-                int t0, nt;
-                range(s, t0, nt);
-                const int ab = c % ABUF;
-                if (c >= ABUF) mbar_wait_sleep(&aempty[ab], ((c / ABUF) - 1) & 1);
-                mbar_expect_tx(&afull[ab], 4 * kTcImg);
-                bulk_g2s(sA + ab * 4 * kTcImg, A.Aimg + (long long)pt * 4 * kTcImg, 4 * kTcImg, &afull[ab]);
-                for (int i = 0; i < nt; ++i, ++g) {
-                    const int st = g % kTcStages;
-                    if (g >= kTcStages) mbar_wait_sleep(&empty[st], ((g / kTcStages) - 1) & 1);
-                    if (A.mma_only == 2 && g >= kTcStages) {   // K14 probe: MMA rate without the B stream
-                        mbar_arrive(&full[st]);
-                        continue;
-                    }
-                    unsigned char *dst = sB + st * STAGE;
-                    mbar_expect_tx(&full[st], STAGE + kTcM * 4);
-                    bulk_g2s(dst, A.Bimg + (long long)(t0 + i) * 2 * kTcImg, 2 * kTcImg, &full[st]);
-                    bulk_g2s(sW + st * kTcM, A.Bw + (long long)(t0 + i) * kTcM, kTcM * 4, &full[st]);
-                }
-            }
-        }
-    } else if (warp == 1) {
-        if (lane == 0) {
-            const int ks = A.ksteps;
-            int g = 0, c = 0;
-            for (int it = blockIdx.x; it < items; it += gridDim.x, ++c) {
-                int t0, nt;
-                range(it / A.ptiles, t0, nt);
-                const int ab = c % ABUF;
-                mbar_wait(&afull[ab], (c / ABUF) & 1);
-                for (int i = 0; i < nt; ++i, ++g) {
-                    const int st = g % kTcStages, b = g & 1;
-                    mbar_wait(&full[st], (g / kTcStages) & 1);
-                    if (g >= 2) mbar_wait(&tempty[b], ((g >> 1) - 1) & 1);
-                    tc_fence_after();
-                    const uint32_t b_hi = smem_u32(sB + st * STAGE), b_lo = b_hi + kTcImg;
-#pragma unroll
-                    for (int a = 0; a < 2; ++a) {
-                        const uint32_t a_hi = smem_u32(sA + (ab * 2 + a) * 2 * kTcImg), a_lo = a_hi + kTcImg;
-                        const uint32_t d = tbase + (uint32_t)((2 * b + a) * kTcM);
-                        for (int k = 0; k < ks; ++k) {   // K = 16 halves = 32 bytes per step
-                            const uint32_t koff = (uint32_t)k * 32;
-                            umma_f16(d, umma_desc_sw128(a_lo + koff), umma_desc_sw128(b_hi + koff), k > 0);
-                            umma_f16(d, umma_desc_sw128(a_hi + koff), umma_desc_sw128(b_lo + koff), 1);
-                        }
-                        for (int k = 0; k < ks; ++k) {
-                            const uint32_t koff = (uint32_t)k * 32;
-                            umma_f16(d, umma_desc_sw128(a_hi + koff), umma_desc_sw128(b_hi + koff), 1);
-                        }
-                    }
-                    umma_commit(&empty[st]);   // smem slot free once these MMAs retire
-                    umma_commit(&tfull[b]);    // accumulators (b, 0) and (b, 1) ready
-                }
-                umma_commit(&aempty[ab]);      // A buffer free once the item's MMAs retire
-            }
-        }
-    } else {
-        // epilogue: warp w reads TMEM lanes 32*(w%4) .. +31 (its quadrant) of A tile
-        // a = (w-2)/4; thread = one output point, (M, S) over all columns of the item.
-        const int q4 = warp & 3, a = (warp - 2) >> 2;
-        const int row = q4 * 32 + lane;
-        const float tks = ldexpf(A.tk, tc_scale_exp(A.amax_p) + tc_scale_exp(A.amax_q));
-        const float2 tk2 = make_float2(tks, tks);
-        const float us = ldexpf(1.f, tc_scale_exp(A.amax_p) + tc_scale_exp(A.amax_q));  // exact unscale
-        int g = 0;
-        for (int it = blockIdx.x; it < items; it += gridDim.x) {
-            const int s = it / A.ptiles, pt = it % A.ptiles;
-            int t0, nt;
-            range(s, t0, nt);
-            const int p = pt * (2 * kTcM) + a * kTcM + row;
-            const bool dbg = A.debug_acc && a == 0 && it == 0;
-            float M = -INFINITY, S = 0.f;
-            for (int i = 0; i < nt; ++i, ++g) {
-                const int st = g % kTcStages, b = g & 1;
-                mbar_wait_sleep(&tfull[b], (g >> 1) & 1);
-                tc_fence_after();
-                if (A.mma_only) {
-                    tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) { mbar_arrive(&tempty[b]); mbar_arrive(&empty[st]); }
-                    continue;
-                }
-                const uint32_t taddr = tbase + ((uint32_t)(q4 * 32) << 16) + (uint32_t)((2 * b + a) * kTcM);
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {   // two 64-column chunks
-                    const float2 *w = reinterpret_cast<const float2 *>(sW + st * kTcM + h * 64);
-                    uint32_t r[64];
-                    TMEM_LD32(taddr + h * 64, r);
-                    TMEM_LD32(taddr + h * 64 + 32, (r + 32));
-                    tmem_ld_wait();
-                    if (dbg && i == 0) {
-#pragma unroll
-                        for (int j = 0; j < 64; ++j) A.debug_acc[row * kTcM + h * 64 + j] = __uint_as_float(r[j]) * us;
-                    }
-                    float2 t[32];
-#pragma unroll
-                    for (int j = 0; j < 32; ++j)
-                        t[j] = fma2(make_float2(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1])), tk2, w[j]);
-                    if (h == 1) {
-                        // accumulators of buffer b and the w slot are no longer needed: release them early
-                        tc_fence_before();
-                        __syncwarp();
-                        if (lane == 0) { mbar_arrive(&tempty[b]); mbar_arrive(&empty[st]); }
-                    }
-                    float m8[8];
-#pragma unroll
-                    for (int j = 0; j < 8; ++j)
-                        m8[j] = fmax3(fmaxf(t[4 * j].x, t[4 * j].y), fmax3(t[4 * j + 1].x, t[4 * j + 1].y, t[4 * j + 2].x),
-                                      fmax3(t[4 * j + 2].y, t[4 * j + 3].x, t[4 * j + 3].y));
-                    const float cm = fmax3(fmax3(m8[0], m8[1], m8[2]), fmax3(m8[3], m8[4], m8[5]), fmaxf(m8[6], m8[7]));
-                    if (cm > M) { S *= ex2(M - cm); M = cm; }
-                    if (M == -INFINITY) continue;  // only padding seen so far (ragged last tile's upper half)
-                    const float2 sc = tc_sum_chunk<EMU>(t, M);
-                    S += sc.x + sc.y;
-                }
-            }
-            if (p < A.P && !A.mma_only) A.part[(long long)s * A.P + p] = make_float2(M, S);
-        }
-    }
-    tc_fence_before();
-    __syncthreads();
-    if (A.cyc && blockIdx.x == 0 && threadIdx.x == 0) *A.cyc = clock64() - clk0;
-    if (warp == 1) {
-        tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tbase));
-    }
-}
-
-// ------------------------------------------------------- 2-SM (CTA pair) variant
-// cta_group::2: the pair computes a 256 x 256 tile per MMA (M = 256 split over the two SMs'
-// A halves, N = 256 split over their B halves), so each SM reads 8 KB of operands from shared
-// memory per 128-cycle MMA (64 B/clk, half of the 1-SM 128 x 128 shape's demand): the full
-// tensor rate.  Roles per CTA (rank r of the pair):
-//   warp 0   producer: A half (points 256 pt + 128 r) once per item, B halves (points
-//            256 bt + 128 r, images) + all 256 w of the tile into a kT2Stages ring;
+// cta_group::2: the pair computes a 256 x 256 tile per MMA group (M = 256 split over the two
+// SMs' A halves, N = 256 split over their B halves).  Roles per CTA (rank r of the pair):
+//   warp 0   producer: A half (points 256 pt + 128 r: [hi | lo | EA], 36 KB) once per item, B
+//            halves (points 256 bt + 128 r: [hi | lo | EB]) into a kT2Stages ring;
 //   warp 1   leader: TMEM allocation (both CTAs allocate, cta_group::2) and the MMA issuer;
 //            peer: relay — waits for its own A/B arrivals and arrives remotely on the leader's
 //            pair barriers (1D bulk copies signal their own CTA's mbarrier);
 //   warps 2.. epilogue (NE warps) on this CTA's 128 accumulator rows: warp w = lane quadrant
 //            w % 4, column group (w - 2) / 4 (256 / (NE / 4) columns); releases accumulator b
 //            remotely on the leader's tempty.  MMA completion is multicast to both CTAs' barriers.
-constexpr int kT2Stages = 4;
+constexpr int kT2Stages = 4;                  // B ring depth (36 KB stages)
 constexpr int kT2N = 256;                     // MMA N (B points per tile) and A points per item
 constexpr uint32_t kIdescF16M256N256 = (1u << 4) | ((uint32_t)(kT2N >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
 
@@ -412,18 +246,18 @@ __device__ __forceinline__ void umma2_commit_mc(uint64_t *bar) {
                  ::"r"(smem_u32(bar)), "h"((uint16_t)3) : "memory");
 }
 
+
 template <int EMU, int NE, bool SEEDED>
-__global__ void __launch_bounds__(64 + 32 * NE, 1) __maxnreg__(NE == 16 ? 112 : 168) k_lse_tc2(TcArgs A) {
+__global__ void __launch_bounds__(64 + 32 * NE, 1) k_lse_tc2(TcArgs A) {
     constexpr int NQ = NE / 4;                       // epilogue warps per TMEM lane quadrant
     constexpr int CW = kT2N / NQ;                    // accumulator columns per epilogue warp
     constexpr int ABUF = 2;
-    constexpr int STAGE = 2 * kTcImg;                // own B half: hi + lo (128 points)
+    constexpr int STAGE = 2 * kTcImg + kTcExtBytes;  // [hi | lo | extra] of 128 points: 36 KB
     extern __shared__ __align__(1024) unsigned char smraw[];
     unsigned char *sm = smraw + ((1024 - (smem_u32(smraw) & 1023)) & 1023);
-    unsigned char *sA = sm;                           // ABUF x [hi | lo] of this CTA's 128 A rows
-    unsigned char *sB = sm + ABUF * 2 * kTcImg;       // kT2Stages x STAGE
-    float *sW = reinterpret_cast<float *>(sB + kT2Stages * STAGE);   // kT2Stages x 256 w
-    float2 *xch = reinterpret_cast<float2 *>(sW + kT2Stages * kT2N); // (NQ - 1) x 128 column-group partials
+    unsigned char *sA = sm;                           // ABUF x STAGE: this CTA's 128 A rows
+    unsigned char *sB = sm + ABUF * STAGE;            // kT2Stages x STAGE: this CTA's 128 B rows
+    float2 *xch = reinterpret_cast<float2 *>(sB + kT2Stages * STAGE);   // (NQ - 1) x 128 partials
     __shared__ __align__(8) uint64_t full[kT2Stages], pfull[kT2Stages], empty[kT2Stages], tfull[2], tempty[2],
         afull[ABUF], pafull[ABUF], aempty[ABUF];
     __shared__ uint32_t tmem_base;
@@ -447,7 +281,7 @@ __global__ void __launch_bounds__(64 + 32 * NE, 1) __maxnreg__(NE == 16 ? 112 : 
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < kT2Stages; ++i) {
-            mbar_init(&full[i], 1); mbar_init(&pfull[i], 1); mbar_init(&empty[i], 1 + NE);
+            mbar_init(&full[i], 1); mbar_init(&pfull[i], 1); mbar_init(&empty[i], 1);
         }
         for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 2 * NE); }
         for (int i = 0; i < ABUF; ++i) { mbar_init(&afull[i], 1); mbar_init(&pafull[i], 1); mbar_init(&aempty[i], 1); }
@@ -465,21 +299,25 @@ __global__ void __launch_bounds__(64 + 32 * NE, 1) __maxnreg__(NE == 16 ? 112 : 
 
     if (warp == 0) {
         if (lane == 0) {
+            const unsigned char *aext = A.Aimg + tc_ea_off(A.P), *bext = A.Bimg + tc_eb_off(A.Q);
             int g = 0, c = 0;
             for (int it = cid; it < items; it += ncl, ++c) {
                 const int s = it / A.ptiles, pt = it % A.ptiles;
                 int t0, nt;
                 range(s, t0, nt);
                 const int ab = c % ABUF;
+                const long long at = 2LL * pt + rank;   // this CTA's 128-point A tile
                 if (c >= ABUF) mbar_wait_sleep(&aempty[ab], ((c / ABUF) - 1) & 1);
-                mbar_expect_tx(&afull[ab], 2 * kTcImg);
-                bulk_g2s(sA + ab * 2 * kTcImg, A.Aimg + (long long)(2 * pt + rank) * 2 * kTcImg, 2 * kTcImg, &afull[ab]);
+                mbar_expect_tx(&afull[ab], STAGE);
+                bulk_g2s(sA + ab * STAGE, A.Aimg + at * 2 * kTcImg, 2 * kTcImg, &afull[ab]);
+                bulk_g2s(sA + ab * STAGE + 2 * kTcImg, aext + at * kTcExtBytes, kTcExtBytes, &afull[ab]);
                 for (int i = 0; i < nt; ++i, ++g) {
                     const int st = g % kT2Stages;
+                    const long long bt = 2LL * (t0 + i) + rank;
                     if (g >= kT2Stages) mbar_wait_sleep(&empty[st], ((g / kT2Stages) - 1) & 1);
-                    mbar_expect_tx(&full[st], STAGE + kT2N * 4);
-                    bulk_g2s(sB + st * STAGE, A.Bimg + (long long)(2 * (t0 + i) + rank) * 2 * kTcImg, STAGE, &full[st]);
-                    bulk_g2s(sW + st * kT2N, A.Bw + (long long)(t0 + i) * kT2N, kT2N * 4, &full[st]);
+                    mbar_expect_tx(&full[st], STAGE);
+                    bulk_g2s(sB + st * STAGE, A.Bimg + bt * 2 * kTcImg, 2 * kTcImg, &full[st]);
+                    bulk_g2s(sB + st * STAGE + 2 * kTcImg, bext + bt * kTcExtBytes, kTcExtBytes, &full[st]);
                 }
             }
         }
@@ -501,7 +339,7 @@ __global__ void __launch_bounds__(64 + 32 * NE, 1) __maxnreg__(NE == 16 ? 112 : 
                 }
             }
         } else if (lane == 0) {
-            const int ks = A.ksteps;
+            const int ks = A.mma_only == 3 ? 0 : A.ksteps;
             int g = 0, c = 0;
             for (int it = cid; it < items; it += ncl, ++c) {
                 int t0, nt;
@@ -509,24 +347,28 @@ __global__ void __launch_bounds__(64 + 32 * NE, 1) __maxnreg__(NE == 16 ? 112 : 
                 const int ab = c % ABUF;
                 mbar_wait(&afull[ab], (c / ABUF) & 1);
                 mbar_wait(&pafull[ab], (c / ABUF) & 1);
-                const uint32_t a_hi = smem_u32(sA + ab * 2 * kTcImg), a_lo = a_hi + kTcImg;
+                const uint32_t a_hi = smem_u32(sA + ab * STAGE), a_lo = a_hi + kTcImg, a_ex = a_hi + 2 * kTcImg;
                 for (int i = 0; i < nt; ++i, ++g) {
                     const int st = g % kT2Stages, b = g & 1;
                     mbar_wait(&full[st], (g / kT2Stages) & 1);
                     mbar_wait(&pfull[st], (g / kT2Stages) & 1);
                     if (g >= 2) mbar_wait(&tempty[b], ((g >> 1) - 1) & 1);
                     tc_fence_after();
-                    const uint32_t b_hi = smem_u32(sB + st * STAGE), b_lo = b_hi + kTcImg;
+                    const uint32_t b_hi = smem_u32(sB + st * STAGE), b_lo = b_hi + kTcImg, b_ex = b_hi + 2 * kTcImg;
                     const uint32_t d = tbase + (uint32_t)(b * kT2N);
-                    for (int k = 0; k < (A.mma_only >= 3 ? 0 : ks); ++k) {   // K = 16 halves = 32 bytes per step
+                    // smallest magnitudes first (each MMA rounds at the running accumulator's
+                    // scale): the lo cross products, then hi . hi, then the extra columns
+                    // w_q - sh_p, which bring the sum down to t - sh_p in one rounding
+                    for (int k = 0; k < ks; ++k) {   // K = 16 halves = 32 bytes per step
                         const uint32_t koff = (uint32_t)k * 32;
                         umma2_f16(d, umma_desc_sw128(a_lo + koff), umma_desc_sw128(b_hi + koff), k > 0);
                         umma2_f16(d, umma_desc_sw128(a_hi + koff), umma_desc_sw128(b_lo + koff), 1);
                     }
-                    for (int k = 0; k < (A.mma_only >= 3 ? 0 : ks); ++k) {
+                    for (int k = 0; k < ks; ++k) {
                         const uint32_t koff = (uint32_t)k * 32;
                         umma2_f16(d, umma_desc_sw128(a_hi + koff), umma_desc_sw128(b_hi + koff), 1);
                     }
+                    if (A.mma_only != 3) umma2_f16(d, umma_desc_sw32(a_ex), umma_desc_sw32(b_ex), 1);
                     umma2_commit_mc(&empty[st]);   // both CTAs' B slots free once these MMAs retire
                     umma2_commit_mc(&tfull[b]);    // accumulator b ready in both CTAs
                 }
@@ -535,14 +377,12 @@ __global__ void __launch_bounds__(64 + 32 * NE, 1) __maxnreg__(NE == 16 ? 112 : 
         }
     } else {
         // epilogue: this CTA's accumulator rows (TMEM lanes) q4*32 + lane, columns hc*CW ..+CW-1
-        // in 64-column chunks.  (A software-pipelined variant — the next chunk's TMEM load in
-        // flight under the current chunk's exponentials — measured slower: the epilogue is bound
-        // by instruction issue next to MUFU, not by TMEM-load latency.)
+        // in 64-column chunks; the accumulator is t - sh (log2 units).  (A software-pipelined
+        // variant — the next chunk's TMEM load in flight under the current chunk's
+        // exponentials — measured slower: the epilogue is issue-bound next to MUFU.)
         const int q4 = warp & 3, hc = (warp - 2) >> 2;
         const int row = q4 * 32 + lane;
-        const float tks = ldexpf(A.tk, tc_scale_exp(A.amax_p) + tc_scale_exp(A.amax_q));
-        const float2 tk2 = make_float2(tks, tks);
-        const float us = ldexpf(1.f, tc_scale_exp(A.amax_p) + tc_scale_exp(A.amax_q));  // exact unscale
+        const float *sh = reinterpret_cast<const float *>(A.Aimg + tc_sh_off(A.P));
         const uint32_t r_tempty = leader ? smem_u32(&tempty[0]) : mapa_u32(smem_u32(&tempty[0]), 0);
         const bool full_epi = A.mma_only == 0 || A.mma_only == 3;   // 3: probe without MMAs
         int g = 0;
@@ -552,52 +392,52 @@ __global__ void __launch_bounds__(64 + 32 * NE, 1) __maxnreg__(NE == 16 ? 112 : 
             range(s, t0, nt);
             const int p = pt * kT2N + (int)rank * kTcM + row;
             const bool dbg = A.debug_acc && leader && it == 0 && hc * CW < kTcM;
-            // seeded: fixed shift from the previous pass (no running max; k_merge recomputes a
-            // point exactly if its sum leaves [2^-100, 2^100]); padding rows use 0
-            float M = SEEDED ? (p < A.P ? A.seed[p] + A.seed_margin : 0.f) : -INFINITY, S = 0.f;
+            // seeded: the row shift sh_p (previous LSE + margin, folded by K6) is already
+            // subtracted by the MMA: no running max (k_merge recomputes a point exactly if its
+            // sum leaves [2^-100, 2^100]); unseeded: running max of t - sh_p
+            float M = SEEDED ? 0.f : -INFINITY, S = 0.f;
             for (int i = 0; i < nt; ++i, ++g) {
-                const int st = g % kT2Stages, b = g & 1;
+                const int b = g & 1;
                 mbar_wait_sleep(&tfull[b], (g >> 1) & 1);
                 tc_fence_after();
                 if (!full_epi) {   // K14 probes 1, 2, 4: the epilogue only releases the buffers
                     tc_fence_before();
                     __syncwarp();
-                    if (lane == 0) { mbar_arrive_cluster(r_tempty + 8 * b); mbar_arrive(&empty[st]); }
+                    if (lane == 0) mbar_arrive_cluster(r_tempty + 8 * b);
                     continue;
                 }
                 const uint32_t taddr = tbase + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(b * kT2N + hc * CW);
 #pragma unroll
                 for (int hh = 0; hh < CW / 64; ++hh) {   // 64-column chunks
-                    const float2 *w = reinterpret_cast<const float2 *>(sW + st * kT2N + hc * CW + hh * 64);
                     uint32_t r[64];
                     TMEM_LD32(taddr + hh * 64, r);
                     TMEM_LD32(taddr + hh * 64 + 32, (r + 32));
                     tmem_ld_wait();
-                    if (dbg && i == 0) {
-#pragma unroll
-                        for (int j = 0; j < 64; ++j) A.debug_acc[row * kTcM + hc * CW + hh * 64 + j] = __uint_as_float(r[j]) * us;
-                    }
-                    float2 t[32];
-#pragma unroll
-                    for (int j = 0; j < 32; ++j)
-                        t[j] = fma2(make_float2(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1])), tk2, w[j]);
                     if (hh == CW / 64 - 1) {
-                        // accumulator b (this warp's columns) and the w slot are no longer needed
+                        // accumulator b (this warp's columns) is in registers: release it
                         tc_fence_before();
                         __syncwarp();
-                        if (lane == 0) { mbar_arrive_cluster(r_tempty + 8 * b); mbar_arrive(&empty[st]); }
+                        if (lane == 0) mbar_arrive_cluster(r_tempty + 8 * b);
                     }
+                    if (dbg && i == 0) {
+#pragma unroll
+                        for (int j = 0; j < 64; ++j)
+                            A.debug_acc[row * kTcM + hc * CW + hh * 64 + j] = __fdiv_rn(__uint_as_float(r[j]), A.tk);
+                    }
+                    float2 tt[32];
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) tt[j] = make_float2(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
                     if constexpr (!SEEDED) {
                         float m8[8];
 #pragma unroll
                         for (int j = 0; j < 8; ++j)
-                            m8[j] = fmax3(fmaxf(t[4 * j].x, t[4 * j].y), fmax3(t[4 * j + 1].x, t[4 * j + 1].y, t[4 * j + 2].x),
-                                          fmax3(t[4 * j + 2].y, t[4 * j + 3].x, t[4 * j + 3].y));
+                            m8[j] = fmax3(fmaxf(tt[4 * j].x, tt[4 * j].y), fmax3(tt[4 * j + 1].x, tt[4 * j + 1].y, tt[4 * j + 2].x),
+                                          fmax3(tt[4 * j + 2].y, tt[4 * j + 3].x, tt[4 * j + 3].y));
                         const float cm = fmax3(fmax3(m8[0], m8[1], m8[2]), fmax3(m8[3], m8[4], m8[5]), fmaxf(m8[6], m8[7]));
                         if (cm > M) { S *= ex2(M - cm); M = cm; }
                         if (M == -INFINITY) continue;  // only padding seen so far
                     }
-                    const float2 sc = tc_sum_chunk<EMU>(t, M);
+                    const float2 sc = tc_sum_chunk<EMU, !SEEDED>(tt, M);
                     S += sc.x + sc.y;
                 }
             }
@@ -610,7 +450,7 @@ __global__ void __launch_bounds__(64 + 32 * NE, 1) __maxnreg__(NE == 16 ? 112 : 
                     const float2 o = xch[(k - 1) * kTcM + row];
                     lse_merge(M, S, o.x, o.y);
                 }
-                if (p < A.P && !A.mma_only) A.part[(long long)s * A.P + p] = make_float2(M, S);
+                if (p < A.P && !A.mma_only) A.part[(long long)s * A.P + p] = make_float2(M + sh[p], S);
             }
             asm volatile("bar.sync 1, %0;" ::"r"(32 * NE));   // xch reuse
         }
@@ -726,9 +566,9 @@ cudaError_t microbench_mma(int kind, void *scratch, cudaStream_t st, double *flo
     return cudaGetLastError();
 }
 
+
 // --------------------------------------------------------------------- host side
-// images are allocated in pairs of 128-point tiles (a CTA's A operand is 256 points)
-size_t tc_image_bytes(long long P) { return (size_t)((P + 2 * kTcM - 1) / (2 * kTcM)) * 2 * 2 * kTcImg; }
+size_t tc_image_bytes(long long P) { return (size_t)tc_side_bytes(P); }
 
 cudaError_t launch_absmax(const float *pts, long long cnt, unsigned *out, cudaStream_t st) {
     long long b = (cnt + 255) / 256;
@@ -736,37 +576,40 @@ cudaError_t launch_absmax(const float *pts, long long cnt, unsigned *out, cudaSt
     return cudaGetLastError();
 }
 
-cudaError_t launch_pack_tc(const float *pts, long long P, int d, const unsigned *amax, void *img, cudaStream_t st) {
-    const long long P2 = (P + 2 * kTcM - 1) / (2 * kTcM) * (2 * kTcM);   // zero images up to the pair
+cudaError_t launch_pack_tc(const float *pts, long long P, int d, const unsigned *amax2, int role, float eps,
+                           void *img, cudaStream_t st) {
+    const long long P2 = tc_tiles(P) * kTcM;   // zero images up to the pair tile
     const long long total = P2 * 8LL;
     long long b = (total + 255) / 256;
-    k_pack_tc<<<(int)(b > 148 * 16 ? 148 * 16 : b), 256, 0, st>>>(pts, P, P2, d, amax, (unsigned char *)img);
+    k_pack_tc<<<(int)(b > 148 * 16 ? 148 * 16 : b), 256, 0, st>>>(pts, P, P2, d, amax2, role, 2.f * kLog2e / eps,
+                                                                    (unsigned char *)img);
     return cudaGetLastError();
 }
 
-
-template <int EMU, int ABUF>
-static cudaError_t launch_tc_v(const TcArgs &A, dim3 grid, cudaStream_t st) {
-    const size_t smem = 1024 + ABUF * 4 * (size_t)kTcImg + tc_stages(ABUF) * (2 * (size_t)kTcImg + kTcM * 4);
-    cudaError_t e = cudaFuncSetAttribute(k_lse_tc<EMU, ABUF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    k_lse_tc<EMU, ABUF><<<grid, kTcThreads, smem, st>>>(A);
+cudaError_t launch_pack_tc_ext(long long P, const float *w, void *img, cudaStream_t st) {
+    const long long P2 = tc_tiles(P) * kTcM;
+    long long b = (P2 + 255) / 256;
+    k_pack_tc_ext<<<(int)(b > 148 * 8 ? 148 * 8 : b), 256, 0, st>>>(P, P2, w, kTcFoldC, (unsigned char *)img);
     return cudaGetLastError();
 }
 
-template <int EMU>
-static cudaError_t launch_tc_emu(const TcArgs &A, dim3 grid, cudaStream_t st) {
-    // SK_TC_ABUF: 2 = double-buffered A (next item's A loads under the current item), 2-deep B
-    // ring; 1 = single A buffer, 4-deep B ring
-    static const int abuf = [] { const char *e = getenv("SK_TC_ABUF"); return e ? atoi(e) : 2; }();
-    return abuf == 1 ? launch_tc_v<EMU, 1>(A, grid, st) : launch_tc_v<EMU, 2>(A, grid, st);
+float tc_fold_c() { return kTcFoldC; }
+
+bool tc_fold_ok(float amax_x, float amax_y, float eps) {
+    // both scaled sides within fp16 range with headroom: max |alpha x|, max |alpha y| <= 2^13
+    const float tk = 2.f * kLog2e / eps;
+    if (!(tk > 0.f) || !std::isfinite(tk)) return false;
+    const int s = tc_fold_s(amax_x, amax_y, tk);
+    const double mx = amax_x > 0.f ? std::ldexp((double)amax_x, s) : 0.0;
+    const double my = amax_y > 0.f ? (double)amax_y * tk * std::ldexp(1.0, -s) : 0.0;
+    return mx <= 8192.0 && my <= 8192.0;
 }
 
 template <int EMU, int NE, bool SEEDED>
 static cudaError_t launch_tc2(const TcArgs &A, int items, cudaStream_t st) {
     constexpr int ABUF = 2;
-    const size_t smem = 1024 + ABUF * 2 * (size_t)kTcImg + kT2Stages * (2 * (size_t)kTcImg + kT2N * 4) +
-                        (NE / 4 - 1) * kTcM * 8;
+    constexpr size_t STAGE = 2 * (size_t)kTcImg + kTcExtBytes;
+    const size_t smem = 1024 + ABUF * STAGE + kT2Stages * STAGE + (NE / 4 - 1) * kTcM * 8;
     cudaError_t e = cudaFuncSetAttribute(k_lse_tc2<EMU, NE, SEEDED>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int nsm = 148, dev = 0;
@@ -787,60 +630,38 @@ static cudaError_t launch_tc2(const TcArgs &A, int items, cudaStream_t st) {
 }
 
 template <int EMU>
-static cudaError_t launch_tc2_ne(const TcArgs &A, int items, cudaStream_t st) {
-    // SK_TC_EPI: epilogue warps of the pair kernel: 16 = four per TMEM lane quadrant (64 columns
-    // each); 8 = two per quadrant (128 columns each)
+static cudaError_t launch_tc2_ne(const TcArgs &A, int items, bool seeded, cudaStream_t st) {
+    // SK_TC_EPI: epilogue warps (16 = four per TMEM lane quadrant, 64 columns each; 8 = two per
+    // quadrant, 128 columns each)
     static const int ne = [] { const char *e = getenv("SK_TC_EPI"); return e ? atoi(e) : 16; }();
-    if (A.seed) return ne == 8 ? launch_tc2<EMU, 8, true>(A, items, st) : launch_tc2<EMU, 16, true>(A, items, st);
+    if (seeded) return ne == 8 ? launch_tc2<EMU, 8, true>(A, items, st) : launch_tc2<EMU, 16, true>(A, items, st);
     return ne == 8 ? launch_tc2<EMU, 8, false>(A, items, st) : launch_tc2<EMU, 16, false>(A, items, st);
 }
 
 int tc_points_per_tile() { return kT2N; }
 
 cudaError_t launch_lse_tc(const TcPass &L, cudaStream_t st) {
-    // SK_TC_PAIR: 1 = CTA-pair kernel (cta_group::2, 256 x 256 MMA tiles); 0 = one CTA per SM
-    // (two 128 x 128 accumulators per B tile).  Both read the same images and w arrays (Q side
-    // tiles of 256 points = two 128-point halves) and write the same partials.
-    static const int pair = [] { const char *e = getenv("SK_TC_PAIR"); return e ? atoi(e) : 1; }();
     // fraction of the exponentials evaluated on the FMA pipe (of every 8 pairs); SK_TC_EMU overrides
-    static const int emu = [] { const char *e = getenv("SK_TC_EMU"); return e ? atoi(e) : (pair ? 1 : 2); }();
+    static const int emu = [] { const char *e = getenv("SK_TC_EMU"); return e ? atoi(e) : 2; }();
     TcArgs A;
-    A.Aimg = (const unsigned char *)L.Aimg; A.Bimg = (const unsigned char *)L.Bimg; A.Bw = L.Bw;
-    A.amax_p = L.amax_p; A.amax_q = L.amax_q;
-    A.P = L.P; A.ksteps = L.ksteps;
+    A.Aimg = (const unsigned char *)L.Aimg; A.Bimg = (const unsigned char *)L.Bimg;
+    A.P = L.P; A.Q = (int)L.Q; A.ksteps = L.ksteps;
     A.split_q = L.split_q;
     A.part = L.part; A.tk = 2.f * kLog2e / L.eps; A.stop = L.stop; A.debug_acc = L.debug_acc;
     A.mma_only = L.mma_only;
     A.cyc = L.cyc;
-    A.seed = pair ? L.seed : nullptr;   // (the one-CTA kernel always tracks the running max)
-    static const float margin = [] { const char *e = getenv("SK_TC_SEED_MARGIN"); return e ? (float)atof(e) : 4.f; }();
-    A.seed_margin = margin;
     if (A.ksteps < 1 || A.ksteps > 4) return cudaErrorInvalidValue;
     A.ptiles = (L.P + kT2N - 1) / kT2N;
     A.nblk = L.nblk;
+    A.Qtiles = (int)((L.Q + kT2N - 1) / kT2N);
+    A.blk_tiles = L.blk_tiles;
     const int items = A.ptiles * L.nblk * L.split_q;
-    if (pair) {
-        A.Qtiles = (int)((L.Q + kT2N - 1) / kT2N);
-        A.blk_tiles = L.blk_tiles;
-        switch (emu) {
-            case 0: return launch_tc2_ne<0>(A, items, st);
-            case 2: return launch_tc2_ne<2>(A, items, st);
-            case 3: return launch_tc2_ne<3>(A, items, st);
-            default: return launch_tc2_ne<1>(A, items, st);
-        }
-    }
-    // one-CTA kernel: Q tiles of 128 points (split ranges in the same units)
-    A.Qtiles = (int)((L.Q + kTcM - 1) / kTcM);
-    A.blk_tiles = 2 * L.blk_tiles;
-    int nsm = 148, dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    dim3 grid(items < nsm ? items : nsm);
+    const bool seeded = L.seeded != 0;
     switch (emu) {
-        case 0: return launch_tc_emu<0>(A, grid, st);
-        case 1: return launch_tc_emu<1>(A, grid, st);
-        case 3: return launch_tc_emu<3>(A, grid, st);
-        default: return launch_tc_emu<2>(A, grid, st);
+        case 0: return launch_tc2_ne<0>(A, items, seeded, st);
+        case 1: return launch_tc2_ne<1>(A, items, seeded, st);
+        case 3: return launch_tc2_ne<3>(A, items, seeded, st);
+        default: return launch_tc2_ne<2>(A, items, seeded, st);
     }
 }
 
