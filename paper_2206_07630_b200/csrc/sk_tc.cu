@@ -178,8 +178,8 @@ struct TcArgs {
     float tk;                   // 2 log2(e)/eps (only the selftest's unscale uses it)
     const int *stop;
     float *debug_acc;           // if non-null: write <p, q> of the first 128 x 128 block, [128][128]
-    int mma_only;               // K14 probes: 1, 2, 4 = the epilogue only releases the buffers;
-                                //   3 = no MMAs, the epilogue runs in full
+    int mma_only;               // K14 probes: 1, 2, 4 = the epilogue only releases the buffers
+                                //   (2: and the B ring is not reloaded); 3 = no MMAs, full epilogue
     long long *cyc;             // K14: SM cycles of CTA 0 (clock64 around the work), nullable
 };
 
@@ -215,6 +215,11 @@ constexpr int kT2Stages = 4;                  // B ring depth (36 KB stages)
 constexpr int kT2N = 256;                     // MMA N (B points per tile) and A points per item
 constexpr uint32_t kIdescF16M256N256 = (1u << 4) | ((uint32_t)(kT2N >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
 
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred = 0;
+    asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.u32 %0, 1, 0, P;\n\t}" : "=r"(pred));
+    return pred != 0;
+}
 __device__ __forceinline__ uint32_t cluster_rank() {
     uint32_t r;
     asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -247,10 +252,13 @@ __device__ __forceinline__ void umma2_commit_mc(uint64_t *bar) {
 }
 
 
-template <int EMU, int NE, bool SEEDED>
+template <int EMU, int NE, bool SEEDED, int G>
 __global__ void __launch_bounds__(64 + 32 * NE, 1) k_lse_tc2(TcArgs A) {
     constexpr int NQ = NE / 4;                       // epilogue warps per TMEM lane quadrant
-    constexpr int CW = kT2N / NQ;                    // accumulator columns per epilogue warp
+    // G tile groups: group k's warps take the tiles g with g % G == k (accumulator buffer k when
+    // G = 2), so one group's TMEM loads overlap the other group's exponentials
+    constexpr int NQG = NQ / G;                      // warps per lane quadrant and group
+    constexpr int CW = kT2N / NQG;                   // accumulator columns per epilogue warp
     constexpr int ABUF = 2;
     constexpr int STAGE = 2 * kTcImg + kTcExtBytes;  // [hi | lo | extra] of 128 points: 36 KB
     extern __shared__ __align__(1024) unsigned char smraw[];
@@ -283,7 +291,7 @@ __global__ void __launch_bounds__(64 + 32 * NE, 1) k_lse_tc2(TcArgs A) {
         for (int i = 0; i < kT2Stages; ++i) {
             mbar_init(&full[i], 1); mbar_init(&pfull[i], 1); mbar_init(&empty[i], 1);
         }
-        for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 2 * NE); }
+        for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 2 * NE / G); }
         for (int i = 0; i < ABUF; ++i) { mbar_init(&afull[i], 1); mbar_init(&pafull[i], 1); mbar_init(&aempty[i], 1); }
         fence_mbar_init();
     }
@@ -315,6 +323,10 @@ __global__ void __launch_bounds__(64 + 32 * NE, 1) k_lse_tc2(TcArgs A) {
                     const int st = g % kT2Stages;
                     const long long bt = 2LL * (t0 + i) + rank;
                     if (g >= kT2Stages) mbar_wait_sleep(&empty[st], ((g / kT2Stages) - 1) & 1);
+                    if (A.mma_only == 2 && g >= kT2Stages) {   // K14 probe: MMA rate without the B stream
+                        mbar_arrive(&full[st]);
+                        continue;
+                    }
                     mbar_expect_tx(&full[st], STAGE);
                     bulk_g2s(sB + st * STAGE, A.Bimg + bt * 2 * kTcImg, 2 * kTcImg, &full[st]);
                     bulk_g2s(sB + st * STAGE + 2 * kTcImg, bext + bt * kTcExtBytes, kTcExtBytes, &full[st]);
@@ -338,8 +350,10 @@ __global__ void __launch_bounds__(64 + 32 * NE, 1) k_lse_tc2(TcArgs A) {
                     mbar_arrive_cluster(r_pfull + 8 * st);
                 }
             }
-        } else if (lane == 0) {
-            const int ks = A.mma_only == 3 ? 0 : A.ksteps;
+        } else if (leader) {
+            // MMA issuer: the whole warp runs the (warp-uniform) loop, so the descriptors live in
+            // uniform registers; one elected lane issues each tcgen05 instruction
+            const int ks = (A.mma_only == 3 || A.mma_only == 5) ? 0 : A.ksteps;
             int g = 0, c = 0;
             for (int it = cid; it < items; it += ncl, ++c) {
                 int t0, nt;
@@ -347,32 +361,37 @@ __global__ void __launch_bounds__(64 + 32 * NE, 1) k_lse_tc2(TcArgs A) {
                 const int ab = c % ABUF;
                 mbar_wait(&afull[ab], (c / ABUF) & 1);
                 mbar_wait(&pafull[ab], (c / ABUF) & 1);
-                const uint32_t a_hi = smem_u32(sA + ab * STAGE), a_lo = a_hi + kTcImg, a_ex = a_hi + 2 * kTcImg;
+                const uint32_t a_hi = smem_u32(sA + ab * STAGE);
+                const uint64_t da_hi = umma_desc_sw128(a_hi), da_lo = umma_desc_sw128(a_hi + kTcImg),
+                               da_ex = umma_desc_sw32(a_hi + 2 * kTcImg);
                 for (int i = 0; i < nt; ++i, ++g) {
                     const int st = g % kT2Stages, b = g & 1;
                     mbar_wait(&full[st], (g / kT2Stages) & 1);
                     mbar_wait(&pfull[st], (g / kT2Stages) & 1);
-                    if (g >= 2) mbar_wait(&tempty[b], ((g >> 1) - 1) & 1);
+                    if (g >= 2) mbar_wait_sleep(&tempty[b], ((g >> 1) - 1) & 1);
                     tc_fence_after();
-                    const uint32_t b_hi = smem_u32(sB + st * STAGE), b_lo = b_hi + kTcImg, b_ex = b_hi + 2 * kTcImg;
+                    const uint32_t b_hi = smem_u32(sB + st * STAGE);
+                    const uint64_t db_hi = umma_desc_sw128(b_hi), db_lo = umma_desc_sw128(b_hi + kTcImg),
+                                   db_ex = umma_desc_sw32(b_hi + 2 * kTcImg);
                     const uint32_t d = tbase + (uint32_t)(b * kT2N);
-                    // smallest magnitudes first (each MMA rounds at the running accumulator's
-                    // scale): the lo cross products, then hi . hi, then the extra columns
-                    // w_q - sh_p, which bring the sum down to t - sh_p in one rounding
-                    for (int k = 0; k < ks; ++k) {   // K = 16 halves = 32 bytes per step
-                        const uint32_t koff = (uint32_t)k * 32;
-                        umma2_f16(d, umma_desc_sw128(a_lo + koff), umma_desc_sw128(b_hi + koff), k > 0);
-                        umma2_f16(d, umma_desc_sw128(a_hi + koff), umma_desc_sw128(b_lo + koff), 1);
+                    if (elect_one()) {
+                        // smallest magnitudes first (each MMA rounds at the running accumulator's
+                        // scale): the lo cross products, then hi . hi, then the extra columns
+                        // w_q - sh_p, which bring the sum down to t - sh_p in one rounding.
+                        // K = 16 halves = 32 bytes per step = +2 in the descriptor's address field.
+                        for (int k = 0; k < ks; ++k) {
+                            umma2_f16(d, da_lo + 2 * k, db_hi + 2 * k, k > 0);
+                            umma2_f16(d, da_hi + 2 * k, db_lo + 2 * k, 1);
+                        }
+                        for (int k = 0; k < ks; ++k) umma2_f16(d, da_hi + 2 * k, db_hi + 2 * k, 1);
+                        if (A.mma_only != 3 && A.mma_only != 5) umma2_f16(d, da_ex, db_ex, 1);
+                        umma2_commit_mc(&empty[st]);   // both CTAs' B slots free once these MMAs retire
+                        umma2_commit_mc(&tfull[b]);    // accumulator b ready in both CTAs
                     }
-                    for (int k = 0; k < ks; ++k) {
-                        const uint32_t koff = (uint32_t)k * 32;
-                        umma2_f16(d, umma_desc_sw128(a_hi + koff), umma_desc_sw128(b_hi + koff), 1);
-                    }
-                    if (A.mma_only != 3) umma2_f16(d, umma_desc_sw32(a_ex), umma_desc_sw32(b_ex), 1);
-                    umma2_commit_mc(&empty[st]);   // both CTAs' B slots free once these MMAs retire
-                    umma2_commit_mc(&tfull[b]);    // accumulator b ready in both CTAs
+                    __syncwarp();
                 }
-                umma2_commit_mc(&aempty[ab]);      // both CTAs' A buffers free
+                if (elect_one()) umma2_commit_mc(&aempty[ab]);   // both CTAs' A buffers free
+                __syncwarp();
             }
         }
     } else {
@@ -380,23 +399,25 @@ __global__ void __launch_bounds__(64 + 32 * NE, 1) k_lse_tc2(TcArgs A) {
         // in 64-column chunks; the accumulator is t - sh (log2 units).  (A software-pipelined
         // variant — the next chunk's TMEM load in flight under the current chunk's
         // exponentials — measured slower: the epilogue is issue-bound next to MUFU.)
-        const int q4 = warp & 3, hc = (warp - 2) >> 2;
+        const int q4 = warp & 3, h = (warp - 2) >> 2;
+        const int grp = h / NQG, hc = h % NQG;   // tile group, column group
         const int row = q4 * 32 + lane;
         const float *sh = reinterpret_cast<const float *>(A.Aimg + tc_sh_off(A.P));
         const uint32_t r_tempty = leader ? smem_u32(&tempty[0]) : mapa_u32(smem_u32(&tempty[0]), 0);
-        const bool full_epi = A.mma_only == 0 || A.mma_only == 3;   // 3: probe without MMAs
+        const bool full_epi = A.mma_only == 0 || A.mma_only == 3 || A.mma_only == 5;   // 3, 5: probes without MMAs
         int g = 0;
         for (int it = cid; it < items; it += ncl) {
             const int s = it / A.ptiles, pt = it % A.ptiles;
             int t0, nt;
             range(s, t0, nt);
             const int p = pt * kT2N + (int)rank * kTcM + row;
-            const bool dbg = A.debug_acc && leader && it == 0 && hc * CW < kTcM;
+            const bool dbg = A.debug_acc && leader && it == 0 && grp == 0 && hc * CW < kTcM;
             // seeded: the row shift sh_p (previous LSE + margin, folded by K6) is already
             // subtracted by the MMA: no running max (k_merge recomputes a point exactly if its
             // sum leaves [2^-100, 2^100]); unseeded: running max of t - sh_p
             float M = SEEDED ? 0.f : -INFINITY, S = 0.f;
             for (int i = 0; i < nt; ++i, ++g) {
+                if (G > 1 && g % G != grp) continue;
                 const int b = g & 1;
                 mbar_wait_sleep(&tfull[b], (g >> 1) & 1);
                 tc_fence_after();
@@ -410,9 +431,14 @@ __global__ void __launch_bounds__(64 + 32 * NE, 1) k_lse_tc2(TcArgs A) {
 #pragma unroll
                 for (int hh = 0; hh < CW / 64; ++hh) {   // 64-column chunks
                     uint32_t r[64];
-                    TMEM_LD32(taddr + hh * 64, r);
-                    TMEM_LD32(taddr + hh * 64 + 32, (r + 32));
-                    tmem_ld_wait();
+                    if (A.mma_only == 5) {   // K14 probe: the epilogue's arithmetic without TMEM loads
+#pragma unroll
+                        for (int j = 0; j < 64; ++j) r[j] = __float_as_uint(-4.f - 0.01f * (float)((j + lane + i) & 15));
+                    } else {
+                        TMEM_LD32(taddr + hh * 64, r);
+                        TMEM_LD32(taddr + hh * 64 + 32, (r + 32));
+                        tmem_ld_wait();
+                    }
                     if (hh == CW / 64 - 1) {
                         // accumulator b (this warp's columns) is in registers: release it
                         tc_fence_before();
@@ -441,10 +467,10 @@ __global__ void __launch_bounds__(64 + 32 * NE, 1) k_lse_tc2(TcArgs A) {
                     S += sc.x + sc.y;
                 }
             }
-            // combine the column groups of each row in fixed order (group 0, 1, ..)
-            if (hc > 0) xch[(hc - 1) * kTcM + row] = make_float2(M, S);
+            // combine the (tile, column) groups of each row in fixed order (h = 0, 1, ..)
+            if (h > 0) xch[(h - 1) * kTcM + row] = make_float2(M, S);
             asm volatile("bar.sync 1, %0;" ::"r"(32 * NE));
-            if (hc == 0) {
+            if (h == 0) {
 #pragma unroll
                 for (int k = 1; k < NQ; ++k) {
                     const float2 o = xch[(k - 1) * kTcM + row];
@@ -605,12 +631,12 @@ bool tc_fold_ok(float amax_x, float amax_y, float eps) {
     return mx <= 8192.0 && my <= 8192.0;
 }
 
-template <int EMU, int NE, bool SEEDED>
+template <int EMU, int NE, bool SEEDED, int G>
 static cudaError_t launch_tc2(const TcArgs &A, int items, cudaStream_t st) {
     constexpr int ABUF = 2;
     constexpr size_t STAGE = 2 * (size_t)kTcImg + kTcExtBytes;
     const size_t smem = 1024 + ABUF * STAGE + kT2Stages * STAGE + (NE / 4 - 1) * kTcM * 8;
-    cudaError_t e = cudaFuncSetAttribute(k_lse_tc2<EMU, NE, SEEDED>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(k_lse_tc2<EMU, NE, SEEDED, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int nsm = 148, dev = 0;
     cudaGetDevice(&dev);
@@ -626,22 +652,22 @@ static cudaError_t launch_tc2(const TcArgs &A, int items, cudaStream_t st) {
     at[0].val.clusterDim.x = 2; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, k_lse_tc2<EMU, NE, SEEDED>, A);
+    return cudaLaunchKernelEx(&cfg, k_lse_tc2<EMU, NE, SEEDED, G>, A);
 }
 
 template <int EMU>
 static cudaError_t launch_tc2_ne(const TcArgs &A, int items, bool seeded, cudaStream_t st) {
-    // SK_TC_EPI: epilogue warps (16 = four per TMEM lane quadrant, 64 columns each; 8 = two per
-    // quadrant, 128 columns each)
-    static const int ne = [] { const char *e = getenv("SK_TC_EPI"); return e ? atoi(e) : 16; }();
-    if (seeded) return ne == 8 ? launch_tc2<EMU, 8, true>(A, items, st) : launch_tc2<EMU, 16, true>(A, items, st);
-    return ne == 8 ? launch_tc2<EMU, 8, false>(A, items, st) : launch_tc2<EMU, 16, false>(A, items, st);
+    // SK_TC_EPI: epilogue organisation: 162 = 16 warps in two tile groups (even / odd tiles,
+    // 128 columns per warp); 16 = four warps per TMEM lane quadrant on every tile (64 columns)
+    static const int ne = [] { const char *e = getenv("SK_TC_EPI"); return e ? atoi(e) : 162; }();
+    if (seeded) return ne == 16 ? launch_tc2<EMU, 16, true, 1>(A, items, st) : launch_tc2<EMU, 16, true, 2>(A, items, st);
+    return ne == 16 ? launch_tc2<EMU, 16, false, 1>(A, items, st) : launch_tc2<EMU, 16, false, 2>(A, items, st);
 }
 
 int tc_points_per_tile() { return kT2N; }
 
 cudaError_t launch_lse_tc(const TcPass &L, cudaStream_t st) {
-    // fraction of the exponentials evaluated on the FMA pipe (of every 8 pairs); SK_TC_EMU overrides
+    // exponential pairs (of every 8) evaluated on the FMA pipe; SK_TC_EMU overrides
     static const int emu = [] { const char *e = getenv("SK_TC_EMU"); return e ? atoi(e) : 2; }();
     TcArgs A;
     A.Aimg = (const unsigned char *)L.Aimg; A.Bimg = (const unsigned char *)L.Bimg;
@@ -661,6 +687,9 @@ cudaError_t launch_lse_tc(const TcPass &L, cudaStream_t st) {
         case 0: return launch_tc2_ne<0>(A, items, seeded, st);
         case 1: return launch_tc2_ne<1>(A, items, seeded, st);
         case 3: return launch_tc2_ne<3>(A, items, seeded, st);
+        case 4: return launch_tc2_ne<4>(A, items, seeded, st);
+        case 5: return launch_tc2_ne<5>(A, items, seeded, st);
+        case 6: return launch_tc2_ne<6>(A, items, seeded, st);
         default: return launch_tc2_ne<2>(A, items, seeded, st);
     }
 }

@@ -6,7 +6,7 @@ import sys; sys.path.insert(0,'.')
 import paper_2206_07630_b200 as sk
 c=sk.Context(0)
 tile = 3*2*64*256*128   # flops per SM per pair tile
-for k in ['tc_clk', 'tc_epi', 'tc_tmem']:
+for k in ['tc_clk', 'tc_epi', 'tc_math']:
     v = c.microbench(k)
     print('ne $ne emu $e %-8s %.0f cycles per tile' % (k, tile / v))
 "; done; done
