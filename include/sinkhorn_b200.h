@@ -107,6 +107,14 @@ void sk_destroy(sk_ctx *ctx);
 const char *sk_last_error(const sk_ctx *ctx);
 const char *sk_status_string(int status);
 int32_t sk_version(void);
+/* Alg. 1's relaxation omega (read as in DESIGN.md R-1) for the following solves on
+ * this context: every update becomes h <- (1 - omega) h_old + omega h_sinkhorn (omega > 1:
+ * the over-relaxed "momentum" of P:73; omega = 1: plain Sinkhorn, the default).
+ * With omega != 1 the row marginals are not exact after an f-update, so err_l adds the row
+ * term sum_i a_i |expm1((f_i - fsk_i)/eps)| and E uses sum_ij P_ij (both exact, O(n)).
+ * omega must lie in (0, 2) (SK_EINVAL otherwise); the sharded entries return
+ * SK_EUNSUPPORTED for omega != 1. */
+sk_status sk_set_relaxation(sk_ctx *ctx, float omega);
 /* Enable (1) / disable (0) CUDA-event timing of the dominant kernels into sk_counters. */
 sk_status sk_set_timing(sk_ctx *ctx, int32_t enable);
 sk_status sk_get_counters(const sk_ctx *ctx, sk_counters *out /* host */);

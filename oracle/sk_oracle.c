@@ -176,7 +176,19 @@ static double dual_objective(const ora_prob *p, const double *a, const double *b
 }
 
 /* --------------------------------------------------------------- Sinkhorn -- */
-/* Alg. 1 with omega = 1, g-then-f (reading R-2): start f = f0 (0 if NULL), g = 0.
+/* Alg. 1 with relaxation omega, line by line in the R-1 reading:
+ *   g <- g + omega (eps log b + min_eps(C^T - g (+) f)) = (1 - omega) g + omega g_sk(f)
+ *   f <- f + omega (eps log a + min_eps(C - f (+) g))   = (1 - omega) f + omega f_sk(g)
+ * (g_sk, f_sk: the omega = 1 updates above; omega > 1 is the over-relaxed "momentum" of
+ * P:73).  omega == 1 is the plain algorithm. */
+static double omega_g = 1.0;   /* the current call's omega (set by the public entry) */
+
+static void relax(int64_t k, double *v, const double *vsk, double omega) {
+    if (omega == 1.0) { for (int64_t i = 0; i < k; ++i) v[i] = vsk[i]; return; }
+    for (int64_t i = 0; i < k; ++i) v[i] = (1.0 - omega) * v[i] + omega * vsk[i];
+}
+
+/* Alg. 1, g-then-f (reading R-2): start f = f0 (0 if NULL), g = 0.
  * For l = 1..max_iter: g-update, f-update; every check_every sweeps compute the
  * explicit error (threshold appendix) and stop when err < tol.  tol <= 0 runs
  * exactly max_iter sweeps ("lockstep").  On return: f, g = (f^(L), g^(L)),
@@ -187,12 +199,17 @@ static int sinkhorn(const ora_prob *p, const double *a, const double *b, double 
                     double *f, double *g, int *iters, double *err, double *E, double *trace) {
     for (int64_t i = 0; i < p->n; ++i) f[i] = f0 ? f0[i] : 0.0;
     for (int64_t j = 0; j < p->m; ++j) g[j] = 0.0;
+    const double omega = omega_g;
+    double *gs = (double *)malloc(sizeof(double) * (size_t)p->m);
+    double *fs = (double *)malloc(sizeof(double) * (size_t)p->n);
     int l = 0, converged = 0;
     double e = INFINITY;
     while (l < max_iter) {
         ++l;
-        g_update(p, b, f, eps, g, NULL, 0);
-        f_update(p, a, g, eps, f, NULL, 0);
+        g_update(p, b, f, eps, gs, NULL, 0);
+        relax(p->m, g, gs, omega);
+        f_update(p, a, g, eps, fs, NULL, 0);
+        relax(p->n, f, fs, omega);
         if (trace) trace[l - 1] = dual_objective(p, a, b, f, g, eps);
         if (tol > 0.0 && l % check_every == 0) {
             e = marginal_error(p, a, b, f, g, eps);
@@ -200,6 +217,8 @@ static int sinkhorn(const ora_prob *p, const double *a, const double *b, double 
         }
     }
     if (!converged) e = marginal_error(p, a, b, f, g, eps);
+    free(gs);
+    free(fs);
     *iters = l;
     *err = e;
     *E = dual_objective(p, a, b, f, g, eps);
@@ -213,6 +232,18 @@ int ora_sinkhorn_points(int64_t n, int64_t m, int d, const double *x, const doub
                         double *err, double *E, double *trace) {
     ora_prob p = {n, m, d, x, y, NULL};
     return sinkhorn(&p, a, b, eps, tol, max_iter, check_every, f0, f, g, iters, err, E, trace);
+}
+
+/* Relaxed variant (omega > 0; Alg. 1's omega). */
+int ora_sinkhorn_points_omega(int64_t n, int64_t m, int d, const double *x, const double *y,
+                              const double *a, const double *b, double eps, double omega, double tol,
+                              int max_iter, int check_every, const double *f0, double *f, double *g,
+                              int *iters, double *err, double *E, double *trace) {
+    ora_prob p = {n, m, d, x, y, NULL};
+    omega_g = omega;
+    int r = sinkhorn(&p, a, b, eps, tol, max_iter, check_every, f0, f, g, iters, err, E, trace);
+    omega_g = 1.0;
+    return r;
 }
 
 /* ... or an explicit cost matrix (GMM's K x K Bures cost). */

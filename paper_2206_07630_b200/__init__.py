@@ -197,9 +197,18 @@ def sinkhorn_init_subsample(ctx: Context, x, y, idx_x, idx_y, eps: float, inner_
 
 def sinkhorn_solve(ctx: Context, x, y, eps: float, tol: float = 1e-3, max_iter: int = 10000,
                    check_every: int = 1, a=None, b=None, y_shared: bool = False, mode: str = "auto",
-                   f_init=None, g_init=None, f=None, g=None, allow_nonfinite: bool = False):
+                   f_init=None, g_init=None, f=None, g=None, allow_nonfinite: bool = False,
+                   omega: float = 1.0):
     """Solve B >= 1 problems.  x: (n, d) or (B, n, d); y: (m, d) [shared] or (B, m, d).
+    omega: Alg. 1's relaxation (sk_set_relaxation; 1 = plain Sinkhorn).
     Returns (f, g, reports) with f (B, n) / g (B, m) (B dropped for a single problem)."""
+    if omega != 1.0:
+        ctx.check(ctx.lib.sk_set_relaxation(ctx.h, ctypes.c_float(omega)))
+        try:
+            return sinkhorn_solve(ctx, x, y, eps, tol, max_iter, check_every, a, b, y_shared, mode,
+                                  f_init, g_init, f, g, allow_nonfinite)
+        finally:
+            ctx.lib.sk_set_relaxation(ctx.h, ctypes.c_float(1.0))
     single = x.dim() == 2
     xb = x.unsqueeze(0) if single else x
     B, n, d = xb.shape

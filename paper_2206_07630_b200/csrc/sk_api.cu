@@ -73,6 +73,7 @@ struct sk_ctx {
     DevStatus *h_status = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     std::vector<cudaEvent_t> tev;   // per-launch timing events of the dominant kernel (pool)
+    float omega = 1.f;              // Alg. 1's relaxation for the following solves
 };
 
 namespace {
@@ -247,6 +248,7 @@ struct Problem {
     int world;              // ranks of the partition (1 = unsharded)
     bool nccl;              // partials exchanged with ncclAllGather (one local slice)
     bool partitioned = false;  // sharded entries: results must not depend on the world size
+    float omega = 1.f;         // Alg. 1's relaxation (sk_set_relaxation)
 };
 
 // Per-launch CUDA-event timing of the dominant kernel (only while ctx->timing is set).  Each
@@ -302,6 +304,8 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
     cudaStream_t st = ctx->stream;
     LaunchTimer tm(ctx);
     const bool sharded = P.world > 1;
+    if (P.omega != 1.f && (sharded || P.partitioned))
+        return fail(ctx, SK_EUNSUPPORTED, "relaxation (omega != 1) is supported by the unsharded solver only");
     const long long m = P.m, n_glob = P.n_total;
     const int ns = (int)slices.size();
     long long n_max = 0, n_sum = 0;
@@ -381,7 +385,7 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
     // online FFMA path: per-point LSE seeds for the max-free (seeded) passes from sweep 3 on
     // stored mode with the fused sweep (one persistent CTA per SM): 8 blocks x split_q = one wave
     static const int fused_env = [] { const char *e = getenv("SK_FUSED"); return e ? atoi(e) : 1; }();
-    const bool fused = stored && fused_env != 0 && stored_fused_supported(m);
+    const bool fused = stored && fused_env != 0 && stored_fused_supported(m) && P.omega == 1.f;
     const bool seedable = !stored;
     if (tc) {   // the seeded passes' exact fallback reads the caller's coordinates
         for (int i = 0; i < ns; ++i) { X[i].raw = slices[i].x; X[i].tcimg = (unsigned char *)ximg + offi[i]; X[i].tc_c = tc_fold_c(); }
@@ -424,7 +428,7 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
     }
     const long long part_elems = std::max((long long)nsplit_col * m, (long long)split_row * n_max);
     ENSURE(part, float2, B_PART, part_elems);
-    ENSURE(blke, double, B_BLKE, 2048);
+    ENSURE(blke, double, B_BLKE, 2 * kMergeMaxBlocks);
     ENSURE(blkb, int, B_BLKB, 2048);
 
     const float loga_u = (float)(-std::log((double)n_glob)), logb_u = (float)(-std::log((double)m));
@@ -463,6 +467,7 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
     auto col_part = [&](int i) { return part + (sharded ? (long long)slices[i].rank * slot : 0); };
     MergePass mcol{MERGE_COL, &Y, part, nsplit_col, P.eps, P.b, status, blke, blkb, nullptr, 0.f,
                    sharded ? 1 : 0, 0};
+    mcol.omega = P.omega;
     if (col_seed) mcol.Q = &X[0];
     int sweep = 0;   // sweeps enqueued so far (seeded passes from the third on)
 
@@ -567,6 +572,8 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
                 MergePass mrow{MERGE_ROW, &X[i], part, stored ? 1 : split_row, P.eps, nullptr, status, blke,
                                blkb, nullptr, 0.f, sharded ? 1 : 0, i + 1 < ns ? 1 : 0};
                 if (row_seed) mrow.Q = &Y;
+                mrow.omega = P.omega;
+                mrow.wts = slices[i].a;   // (the relaxed row error term weighs rows by a)
                 mrow.tc_fold = tc && row_seed && sweep >= 1;   // the next row pass is seeded
                 mrow.tc_margin = tc_margin;
                 CU(launch_merge(mrow, st));
@@ -609,6 +616,8 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
     double E = 0.0;
     for (int b = 0; b < SK_SHARD_BLOCKS; ++b) E += fa_h[b];
     E += gb_part;
+    // relaxed: after the f-update sum_ij P_ij = sum(a) + mass_dev (kept by the last row merge)
+    if (P.omega != 1.f) E -= (double)P.eps * hs.mass_dev;
     for (int i = 0; i < ns; ++i)
         CU(cudaMemcpyAsync(slices[i].f, X[i].pot[L & 1], sizeof(float) * slices[i].n, cudaMemcpyDeviceToDevice, st));
     CU(cudaMemcpyAsync(P.g, Y.pot[L & 1], sizeof(float) * m, cudaMemcpyDeviceToDevice, st));
@@ -684,6 +693,13 @@ sk_status sk_create(sk_ctx **out, int device, void *stream) {
 sk_status sk_set_stream(sk_ctx *ctx, void *stream) {
     if (!ctx) return SK_EINVAL;
     ctx->stream = (cudaStream_t)stream;
+    return SK_OK;
+}
+
+sk_status sk_set_relaxation(sk_ctx *ctx, float omega) {
+    if (!ctx) return SK_EINVAL;
+    if (!(omega > 0.f && omega < 2.f)) return fail(ctx, SK_EINVAL, "omega must lie in (0, 2), got %g", (double)omega);
+    ctx->omega = omega;
     return SK_OK;
 }
 
@@ -981,7 +997,7 @@ sk_status sinkhorn_init_subsample(sk_ctx *ctx, int64_t n, int64_t m, int32_t d, 
     const int R = D <= 4 ? 4 : (D <= 16 ? 2 : 1);
     const int split = choose_split((n + 128LL * R - 1) / (128LL * R), zt, occ, 64);
     ENSURE(part, float2, B_PART, (long long)split * n);
-    ENSURE(blke, double, B_BLKE, 2048);
+    ENSURE(blke, double, B_BLKE, 2 * kMergeMaxBlocks);
     ENSURE(blkb, int, B_BLKB, 2048);
     CU(launch_status_init(status, 1, 1, 1.f, ctx->stream));
     LsePass lp{&X, &Z, 1, 0, split, part, eps, nullptr};
@@ -1017,6 +1033,7 @@ sk_status solve_impl(sk_ctx *ctx, int64_t B, int64_t n, int64_t m, int32_t d, co
         L.finit = f_init; L.f = f; L.g = g; L.eps = eps; L.tol = tol;
         L.max_iter = max_iter; L.check_every = check_every;
         L.iters = iters; L.conv = conv; L.nonfinite = nonf; L.err = err; L.E = E;
+        L.omega = ctx->omega;
         CU(cudaEventRecord(ctx->ev0, st));
         CU(launch_batched(L, st));
         CU(cudaEventRecord(ctx->ev1, st));
@@ -1052,7 +1069,7 @@ sk_status solve_impl(sk_ctx *ctx, int64_t B, int64_t n, int64_t m, int32_t d, co
         P.y = y + p * ys; P.b = b ? b + p * bs : nullptr;
         P.eps = eps; P.tol = tol; P.max_iter = max_iter; P.check_every = check_every; P.mode = mode;
         P.g = g + p * m;
-        P.world = 1; P.nccl = false;
+        P.world = 1; P.nccl = false; P.omega = ctx->omega;
         std::vector<Slice> sl{Slice{0, n, x + p * xs, a ? a + p * as : nullptr,
                                     f_init ? f_init + p * n : nullptr, f + p * n, 0}};
         CK(solve_core(ctx, P, sl, &rep[p]));
@@ -1130,7 +1147,7 @@ sk_status sinkhorn_solve_sharded(sk_ctx *ctx, int64_t n_total, int64_t row0, int
     P.y = dy; P.b = db;
     P.eps = eps; P.tol = tol; P.max_iter = max_iter; P.check_every = check_every; P.mode = mode;
     P.g = dg;
-    P.world = ctx->world; P.nccl = ctx->world > 1; P.partitioned = true;
+    P.world = ctx->world; P.nccl = ctx->world > 1; P.partitioned = true; P.omega = ctx->omega;
     std::vector<Slice> sl{Slice{row0, n_local, dx, da, dfi, df, ctx->rank}};
     sk_status s = solve_core(ctx, P, sl, rep);
     if (s != SK_OK && s != SK_ENONFINITE) return s;
@@ -1166,7 +1183,7 @@ sk_status sinkhorn_solve_sharded_emulated(sk_ctx *ctx, int32_t world, int64_t n,
     P.y = dy; P.b = db;
     P.eps = eps; P.tol = tol; P.max_iter = max_iter; P.check_every = check_every; P.mode = mode;
     P.g = dg;
-    P.world = world; P.nccl = false; P.partitioned = true;
+    P.world = world; P.nccl = false; P.partitioned = true; P.omega = ctx->omega;
     std::vector<Slice> sl;
     for (int r = 0; r < world; ++r) {
         int64_t r0, nl;

@@ -35,6 +35,7 @@ struct BatchArgs {
     int *iters, *conv, *nonfinite;
     float *err;
     double *E;
+    float omega;                    // Alg. 1's relaxation (1 = plain Sinkhorn)
 };
 
 __host__ __device__ inline int round_up(int v, int a) { return (v + a - 1) / a * a; }
@@ -178,6 +179,9 @@ __device__ __forceinline__ void solve_one(const BatchArgs &A, int prob, float *s
 
     int l = 0, cur = 0, conv = 0, nonfin = 0;
     float err = INFINITY;
+    const float om = A.omega;
+    const bool relaxed = om != 1.f;
+    double row_err = 0.0, mass_dev = 0.0;   // relaxed: row term of err_l and sum P - sum a
     for (;;) {
         // ---- column pass: g^{l+1} (P = y, Q = x)
         const bool check = l >= 1 && (l % A.check_every == 0 || l == A.max_iter);
@@ -185,33 +189,48 @@ __device__ __forceinline__ void solve_one(const BatchArgs &A, int prob, float *s
         int bad = 0;
         float *gold = gb + cur * m, *gnew = gb + (cur ^ 1) * m;
         onchip_pass<D, R, NT, EMU>(yq, Mp, m, xq, wx, Np, tk, mys, l >= 1, [&](int j, float Mv, float Sv) {
-            const float gn = cy[j] - epsln2 * (Mv + log2f(Sv));
+            const float gsk = cy[j] - epsln2 * (Mv + log2f(Sv));
+            // Alg. 1 with relaxation (R-1): g <- (1 - omega) g + omega g_sk
+            const float gn = relaxed ? fmaf(om, gsk - gold[j], gold[j]) : gsk;
             gnew[j] = gn;
             wy[j] = fmaf(gn, kap, -nyk[j]);
             bad |= !isfinite(gn);
             if (check) {
                 const double bj = b ? (double)b[j] : 1.0 / m;
-                e_loc += bj * fabs((double)expm1f((gold[j] - gn) / eps));
+                e_loc += bj * fabs((double)expm1f((gold[j] - gsk) / eps));
             }
         });
         const double e_tot = block_sum_d<NT>(e_loc, red);
         const int any_bad = block_or<NT>(bad, redi);
         if (any_bad) { nonfin = 1; break; }
         if (check) {
-            err = (float)e_tot;
+            err = (float)(e_tot + row_err);   // (row_err = 0 unless relaxed)
             if (err < A.tol) { conv = 1; break; }
             if (l == A.max_iter) break;
         }
         // ---- row pass: f^{l+1} (P = x, Q = y); wy is visible after the block reductions' barriers
         float *fnew = fb + (cur ^ 1) * n;
+        const float *fold = fb + cur * n;
         bad = 0;
+        double r_loc = 0.0, m_loc = 0.0;
         onchip_pass<D, R, NT, EMU>(xq, Np, n, yq, wy, Mp, tk, mxs, l >= 1, [&](int i, float Mv, float Sv) {
-            const float fn = cx[i] - epsln2 * (Mv + log2f(Sv));
+            const float fsk = cx[i] - epsln2 * (Mv + log2f(Sv));
+            const float fn = relaxed ? fmaf(om, fsk - fold[i], fold[i]) : fsk;
             fnew[i] = fn;
             wx[i] = fmaf(fn, kap, -nxk[i]);
             bad |= !isfinite(fn);
+            if (relaxed) {   // sum_j P_ij = a_i exp((f_i - fsk_i)/eps)
+                const double ai = a ? (double)a[i] : 1.0 / n;
+                const double dv = (double)expm1f((fn - fsk) / eps);
+                r_loc += ai * fabs(dv);
+                m_loc += ai * dv;
+            }
         });
         if (block_or<NT>(bad, redi)) { nonfin = 1; break; }
+        if (relaxed) {
+            row_err = block_sum_d<NT>(r_loc, red);
+            mass_dev = block_sum_d<NT>(m_loc, red);
+        }
         cur ^= 1;
         ++l;
     }
@@ -228,7 +247,7 @@ __device__ __forceinline__ void solve_one(const BatchArgs &A, int prob, float *s
         A.g[(size_t)prob * m + j] = go[j];
         s += (double)go[j] * (b ? (double)b[j] : 1.0 / m);
     }
-    const double E = block_sum_d<NT>(s, red);
+    const double E = block_sum_d<NT>(s, red) - (double)eps * mass_dev;   // relaxed: sum P != sum a
     if (threadIdx.x == 0) {
         A.iters[prob] = l;
         A.conv[prob] = conv;
@@ -320,6 +339,7 @@ cudaError_t launch_batched(const BatchLaunch &L, cudaStream_t st) {
     A.n = L.n; A.m = L.m; A.eps = L.eps; A.tol = L.tol;
     A.max_iter = L.max_iter; A.check_every = L.check_every;
     A.iters = L.iters; A.conv = L.conv; A.nonfinite = L.nonfinite; A.err = L.err; A.E = L.E;
+    A.omega = L.omega;
     switch (L.d) {
         case 1: return launch_batched_d<1>(A, L.B, st);
         case 2: return launch_batched_d<2>(A, L.B, st);

@@ -21,6 +21,7 @@ struct BatchLaunch {
     int *iters, *conv, *nonfinite;
     float *err;
     double *E;
+    float omega = 1.f;   // Alg. 1's relaxation
 };
 bool batched_supported(int d, int n, int m);
 size_t batched_smem_bytes(int D, int n, int m);
@@ -41,6 +42,8 @@ struct DevStatus {
     double E;        // dual objective of the returned iterate
     double fa_local; // sharded: this rank's <f,a> - eps sum(a) partial
     int colfail;     // stored fused sweep: some column sum left the scaled range -> exact column pass
+    double row_err;  // relaxed (omega != 1): sum_i a_i |expm1((f_i - fsk_i)/eps)| of the last row merge
+    double mass_dev; //                        sum_ij P_ij - sum_i a_i = sum_i a_i expm1((f_i - fsk_i)/eps)
 };
 
 // Packed tile layout of one side: tiles of tq points; tile t at t*(D+1)*tq floats:
@@ -137,8 +140,10 @@ struct MergePass {
     const int *only_if = nullptr;  // run only if *only_if != 0 (the exact column fallback)
     int tc_fold = 0;          // K3 side: also fold lse + margin as the next pass's row shift
     float tc_margin = 4.f;    //          log2 units above the LSE (SK_TC_SEED_MARGIN: test knob)
+    float omega = 1.f;        // Alg. 1's relaxation: h <- (1 - omega) h_old + omega h_sinkhorn
 };
 cudaError_t launch_merge(const MergePass &M, cudaStream_t st);
+constexpr int kMergeMaxBlocks = 1184;   // blk_err holds 2 x kMergeMaxBlocks doubles
 int merge_blocks(int P);
 
 // E = <f,a> + <g,b> - eps sum(a) of the iterate status->final_iter.

@@ -242,7 +242,7 @@ int lse_occupancy_ctas(int D) {
 constexpr int kMT = 256;
 int merge_blocks(int P) {
     int b = (P + kMT - 1) / kMT;
-    return b < 1 ? 1 : (b > 1184 ? 1184 : b);
+    return b < 1 ? 1 : (b > kMergeMaxBlocks ? kMergeMaxBlocks : b);
 }
 
 // Exact (online max) LSE of output point p of side S over every point of side Q, from the
@@ -287,7 +287,7 @@ __device__ void exact_lse_point(const Side &S, const Side &Q, int p, float eps, 
 // Merge of point p given its (M, Ssum) over all splits: new potential (+ packed w), fused
 // error term, non-finite and column-range flags.
 __device__ __forceinline__ void merge_point(const MergePass &Mp, const Side &S, const Side &Qs, int p, float M, float Ssum,
-                                            bool check, const float *hold, float *hnew, double &e, int &bad) {
+                                            bool check, const float *hold, float *hnew, double &e, double &e2, int &bad) {
     const float eps = Mp.eps, kap = kLog2e / eps, epsln2 = eps * kLn2;
     if (Mp.Q && !(Ssum >= 0x1p-100f && Ssum <= 0x1p100f)) {
         // seeded pass: the fixed shift was far from the true maximum -> exact recompute of
@@ -317,8 +317,17 @@ __device__ __forceinline__ void merge_point(const MergePass &Mp, const Side &S, 
         bad |= !isfinite(v);
         return;
     }
-    const float hn = S.c[p] - epsln2 * lse2;
+    const float hsk = S.c[p] - epsln2 * lse2;   // the Sinkhorn (omega = 1) update
+    // Alg. 1 with relaxation (R-1): h <- (1 - omega) h_old + omega h_sk
+    const float hn = Mp.omega == 1.f ? hsk : fmaf(Mp.omega, hsk - hold[p], hold[p]);
     hnew[p] = hn;
+    if (Mp.omega != 1.f && Mp.mode == MERGE_ROW) {
+        // rows are no longer exact after a relaxed f-update: sum_j P_ij = a_i exp((f_i - fsk_i)/eps)
+        const double ai = Mp.wts ? (double)Mp.wts[p] : 1.0 / S.P;
+        const double dv = (double)expm1f((hn - hsk) / eps);
+        e += ai * fabs(dv);
+        e2 += ai * dv;
+    }
     const long long t = p / S.tq, o = p % S.tq;
     const float wn = fmaf(hn, kap, -S.nk[p]);
     S.pack[t * (long long)(S.D + 1) * S.tq + (long long)S.D * S.tq + o] = wn;
@@ -329,7 +338,7 @@ __device__ __forceinline__ void merge_point(const MergePass &Mp, const Side &S, 
     bad |= !isfinite(hn);
     if (check) {
         const double bj = Mp.wts ? (double)Mp.wts[p] : 1.0 / S.P;
-        e += bj * fabs((double)expm1f((hold[p] - hn) / eps));
+        e += bj * fabs((double)expm1f((hold[p] - hsk) / eps));   // column term of err_l (H5)
     }
 }
 
@@ -343,6 +352,7 @@ __global__ void __launch_bounds__(kMT) k_merge(MergePass Mp, Side S, Side Qs) {
     __shared__ double red[kMT / 32];
     __shared__ int redi[kMT / 32];
     __shared__ int s_last;
+    __shared__ double red2[kMT / 32];
     __shared__ float wM[kMT / 32][32], wS[kMT / 32][32];
     DevStatus *st = Mp.st;
     if (st && *(volatile int *)&st->stop) return;
@@ -352,7 +362,7 @@ __global__ void __launch_bounds__(kMT) k_merge(MergePass Mp, Side S, Side Qs) {
                        (l % st->check_every == 0 || l == st->max_iter);
     const float *hold = (l & 1) ? S.pot[1] : S.pot[0];      // no dynamic param indexing
     float *hnew = (l & 1) ? S.pot[0] : S.pot[1];
-    double e = 0.0;
+    double e = 0.0, e2 = 0.0;
     int bad = 0;
     if (WIDE) {
         const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -385,7 +395,7 @@ __global__ void __launch_bounds__(kMT) k_merge(MergePass Mp, Side S, Side Qs) {
 #pragma unroll
                 for (int w = 1; w < NW; ++w) Ssum += wS[w][lane];
                 if (Mp.precomputed) bad |= !isfinite(hnew[p]);
-                else merge_point(Mp, S, Qs, p, M, Ssum, check, hold, hnew, e, bad);
+                else merge_point(Mp, S, Qs, p, M, Ssum, check, hold, hnew, e, e2, bad);
             }
             __syncthreads();
         }
@@ -402,21 +412,23 @@ __global__ void __launch_bounds__(kMT) k_merge(MergePass Mp, Side S, Side Qs) {
                 const float2 v = Mp.part[(long long)s * S.P + p];
                 if (v.x != -INFINITY) Ssum += v.y * ex2(v.x - M);
             }
-            merge_point(Mp, S, Qs, p, M, Ssum, check, hold, hnew, e, bad);
+            merge_point(Mp, S, Qs, p, M, Ssum, check, hold, hnew, e, e2, bad);
         }
     }
     if (!st) return;
     // block partials -> last block decides (fixed order => deterministic)
     for (int o = 16; o > 0; o >>= 1) {
         e += __shfl_xor_sync(0xffffffffu, e, o);
+        e2 += __shfl_xor_sync(0xffffffffu, e2, o);
         bad |= __shfl_xor_sync(0xffffffffu, bad, o);
     }
-    if ((threadIdx.x & 31) == 0) { red[threadIdx.x >> 5] = e; redi[threadIdx.x >> 5] = bad; }
+    if ((threadIdx.x & 31) == 0) { red[threadIdx.x >> 5] = e; red2[threadIdx.x >> 5] = e2; redi[threadIdx.x >> 5] = bad; }
     __syncthreads();
     if (threadIdx.x == 0) {
-        double be = 0.0; int bb = 0;
-        for (int w = 0; w < kMT / 32; ++w) { be += red[w]; bb |= redi[w]; }
+        double be = 0.0, be2 = 0.0; int bb = 0;
+        for (int w = 0; w < kMT / 32; ++w) { be += red[w]; be2 += red2[w]; bb |= redi[w]; }
         Mp.blk_err[blockIdx.x] = be;
+        Mp.blk_err[kMergeMaxBlocks + blockIdx.x] = be2;
         Mp.blk_bad[blockIdx.x] = bb;
         __threadfence();
         unsigned *tk = Mp.mode == MERGE_COL ? &st->ticket_col : &st->ticket_row;
@@ -425,9 +437,10 @@ __global__ void __launch_bounds__(kMT) k_merge(MergePass Mp, Side S, Side Qs) {
     __syncthreads();
     if (!s_last || threadIdx.x != 0) return;
     __threadfence();
-    double et = 0.0; int bt = 0;
+    double et = 0.0, et2 = 0.0; int bt = 0;
     for (int i = 0; i < (int)gridDim.x; ++i) {
         et += ((volatile double *)Mp.blk_err)[i];
+        et2 += ((volatile double *)Mp.blk_err)[kMergeMaxBlocks + i];
         bt |= ((volatile int *)Mp.blk_bad)[i];
     }
     if (Mp.mode == MERGE_COL) {
@@ -438,12 +451,14 @@ __global__ void __launch_bounds__(kMT) k_merge(MergePass Mp, Side S, Side Qs) {
         // to (f^{l-1}, g^{l-1}), both finite.
         if (bt) { st->nonfinite = 1; st->stop = 1; st->final_iter = Mp.sharded ? max(l - 1, 0) : l; }
         else if (check) {
+            if (Mp.omega != 1.f) et += st->row_err;   // relaxed: the rows of (f^l, g^l) are off too
             st->err = (float)et;
             if ((float)et < st->tol) { st->converged = 1; st->stop = 1; st->final_iter = l; }
             else if (l >= st->max_iter) { st->stop = 1; st->final_iter = l; }
         }
     } else if (Mp.mode == MERGE_ROW) {
         st->ticket_row = 0;
+        if (Mp.omega != 1.f) { st->row_err = et; st->mass_dev = et2; }
         if (bt && !Mp.sharded) { st->nonfinite = 1; st->stop = 1; st->final_iter = l; }
         else if (!Mp.no_iter_inc) st->iter = l + 1;
     } else {
@@ -459,7 +474,7 @@ cudaError_t launch_merge(const MergePass &M, cudaStream_t st) {
     const Side Qs = M.Q ? *M.Q : Side{};   // the reduced side by value (the fallback runs on the device)
     if (M.nsplit >= kWideSplits && M.nsplit <= kWideMax * (kMT / 32)) {
         int b = (M.S->P + 31) / 32;
-        if (b > 1184) b = 1184;
+        if (b > kMergeMaxBlocks) b = kMergeMaxBlocks;
         k_merge<true><<<b, kMT, 0, st>>>(M, *M.S, Qs);
     } else {
         k_merge<false><<<merge_blocks(M.S->P), kMT, 0, st>>>(M, *M.S, Qs);

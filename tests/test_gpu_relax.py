@@ -1,0 +1,101 @@
+"""Alg. 1 with relaxation omega != 1 (reading R-1; P:73 / P:230
+"fixed momentum"), CUDA vs the oracle through the C ABI (-m gpu): the same protocol as
+test_gpu_solve (stop-rule counts, lockstep potentials and E, an fp64 property check of the
+marginal error) on every solver path: on-chip batched (K13), online FFMA (K2), tensor-core
+(K3) and stored (K4/K5, where omega != 1 takes the separate row/column passes)."""
+import numpy as np
+import pytest
+import torch
+
+from parity import assert_obj_close, assert_pair_close, count_tol, plan_marginal_error
+from workloads import gen
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    import paper_2206_07630_b200 as sk
+    return sk.Context(0)
+
+
+def _cuda(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def check_relaxed(O, sk, ctx, x, y, eps, omega, f0=None, a=None, mode="auto", tol=1e-3, what=""):
+    f, g, rep = sk.sinkhorn_solve(ctx, _cuda(x), _cuda(y), eps, tol=tol, mode=mode, omega=omega,
+                                  a=None if a is None else _cuda(a),
+                                  f_init=None if f0 is None else _cuda(np.asarray(f0, np.float32)))
+    f, g = f.cpu().numpy(), g.cpu().numpy()
+    L = rep["iterations"]
+    ref = O.sinkhorn(x, y, eps, a=a, tol=tol, omega=omega, f0=f0)
+    assert abs(L - ref.iterations) <= count_tol(ref.iterations), (what, L, ref.iterations)
+    lock = O.sinkhorn(x, y, eps, a=a, tol=0, max_iter=L, omega=omega, f0=f0)
+    assert_pair_close(f, g, lock.f, lock.g, eps, what=what)
+    assert_obj_close(rep["dual_objective"], lock.E, eps, what=what)
+    assert rep["converged"] and rep["marginal_error"] < tol
+    # the error includes the row term: recomputed in fp64 from the returned pair
+    assert plan_marginal_error(x, y, f, g, eps, a) <= 1.05 * tol + 2e-5, what
+    return rep
+
+
+@pytest.mark.parametrize("omega", [1.05, 1.5, 0.8])
+def test_relaxed_onchip_c1(O, ctx, omega):
+    import paper_2206_07630_b200 as sk
+    p = gen.c1()
+    rep = check_relaxed(O, sk, ctx, p.x, p.y, p.eps, omega, what=f"c1 omega={omega}")
+    if omega == 1.5:   # the over-relaxed iteration is the faster one on C1 (oracle: 50 vs 165)
+        _, _, r1 = sk.sinkhorn_solve(ctx, _cuda(p.x), _cuda(p.y), p.eps)
+        assert rep["iterations"] < r1["iterations"]
+
+
+def test_relaxed_onchip_gaussian_init(O, ctx):
+    import paper_2206_07630_b200 as sk
+    p = gen.c1(seed=1)
+    pot, _ = sk.sinkhorn_init_gaussian(ctx, _cuda(p.x), _cuda(p.y))
+    check_relaxed(O, sk, ctx, p.x, p.y, p.eps, 1.4, f0=pot.cpu().numpy(), what="c1 gaussian omega=1.4")
+
+
+@pytest.mark.parametrize("mode,n,m,d,omega", [("online", 3000, 2600, 3, 1.5), ("online", 1500, 1300, 40, 1.3),
+                                              ("stored", 2000, 1024, 16, 1.6), ("online", 2100, 1800, 8, 0.9)])
+def test_relaxed_multikernel(O, ctx, mode, n, m, d, omega):
+    import paper_2206_07630_b200 as sk
+    rng = np.random.default_rng(n + d)
+    x = rng.random((n, d)).astype(np.float32)
+    y = (rng.random((m, d)) * 0.9 + 0.05).astype(np.float32)
+    a = gen.random_weights(n, rng)
+    eps = float(np.float32(0.03 * gen.mean_sq_cost(x, y)))
+    check_relaxed(O, sk, ctx, x, y, eps, omega, a=a, mode=mode, what=f"{mode} {n}x{m}x{d} omega={omega}")
+
+
+def test_relaxed_batched_sort1d(O, ctx):
+    """A C2-shaped batch (8 problems of 256) with the sorted closed-form init and omega = 1.5."""
+    import paper_2206_07630_b200 as sk
+    c2 = gen.c2(B=8, n=256)
+    xb, yb = _cuda(c2.x), _cuda(c2.y)
+    pot = sk.sinkhorn_init_sort1d(ctx, xb.view(8, 256), yb.view(-1))
+    f, g, reps = sk.sinkhorn_solve(ctx, xb, yb, c2.eps, y_shared=True, f_init=pot, omega=1.5)
+    for k in (0, 5):
+        L = reps[k]["iterations"]
+        f0 = pot[k].cpu().numpy()
+        ref = O.sinkhorn(c2.x[k], c2.y, c2.eps, f0=f0, omega=1.5)
+        assert abs(L - ref.iterations) <= count_tol(ref.iterations)
+        lock = O.sinkhorn(c2.x[k], c2.y, c2.eps, tol=0, max_iter=L, f0=f0, omega=1.5)
+        assert_pair_close(f[k].cpu().numpy(), g[k].cpu().numpy(), lock.f, lock.g, c2.eps)
+        assert_obj_close(reps[k]["dual_objective"], lock.E, c2.eps)
+
+
+def test_relaxation_argument_errors(ctx):
+    import ctypes
+    import paper_2206_07630_b200 as sk
+    for bad in (0.0, -1.0, 2.0, float("nan")):
+        assert ctx.lib.sk_set_relaxation(ctx.h, ctypes.c_float(bad)) == 1   # SK_EINVAL
+    p = gen.c4(n=4096)
+    x, y = _cuda(p.x), _cuda(p.y)
+    with pytest.raises(sk.SinkhornError):   # the sharded entries: unsupported
+        ctx.check(ctx.lib.sk_set_relaxation(ctx.h, ctypes.c_float(1.5)))
+        try:
+            sk.sinkhorn_solve_sharded_emulated(ctx, 2, x, y, p.eps, mode="online")
+        finally:
+            ctx.lib.sk_set_relaxation(ctx.h, ctypes.c_float(1.0))

@@ -11,6 +11,8 @@ import os
 import numpy as np
 import pytest
 
+from workloads import gen
+
 GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "analytic_cases.json")))
 
 
@@ -395,3 +397,56 @@ def test_shard_merge_equals_unsharded_g_update(O):
     b = np.full(40, 1 / 40)
     parts = [O.column_partials(x[s], y, f[s], eps) for s in (slice(0, 16), slice(16, 48), slice(48, 64))]
     assert np.allclose(O.merge_partials(parts, b, eps), O.g_update(x, y, f, eps), atol=1e-12)
+
+
+# ------------------------------------------------- Alg. 1 relaxation (NEXT-1, omega != 1)
+def test_relaxed_one_point_closed_form():
+    """n = m = 1, a = b = 1, C = [[c]]: g_sk(f) = c - f and f_sk(g) = c - g (soft-min of one
+    entry), so the relaxed sweep of Alg. 1 (R-1) is the linear recurrence
+        g <- (1 - w) g + w (c - f),   f <- (1 - w) f + w (c - g)
+    derived by hand; the oracle's generic LSE path must reproduce it sweep for sweep."""
+    from oracle import oracle as O
+    c, f0, eps = 2.5, 0.7, 0.3
+    x = np.array([[0.0]])
+    y = np.array([[np.sqrt(c)]])
+    for w in (0.6, 1.0, 1.5, 1.9):
+        f, g = f0, 0.0
+        for L in range(1, 7):
+            g = (1 - w) * g + w * (c - f)
+            f = (1 - w) * f + w * (c - g)
+            r = O.sinkhorn(x, y, eps, tol=0, max_iter=L, f0=np.array([f0]), omega=w)
+            assert abs(r.f[0] - f) < 1e-12 and abs(r.g[0] - g) < 1e-12, (w, L)
+            # Eq. (2) with one atom: E = f + g - eps exp((f + g - c)/eps)
+            assert abs(r.E - (f + g - eps * np.exp((f + g - c) / eps))) < 1e-12
+
+
+def test_relaxed_iterations_reach_the_same_optimum():
+    """The relaxed map's fixed points are the Sinkhorn fixed points for any omega != 0:
+    omega in {0.7, 1.5} converges to the omega = 1 optimum (centred potentials, E)."""
+    from oracle import oracle as O
+    p = gen.c1(n=40, seed=2, eps_factor=0.1)
+    ref = O.sinkhorn(p.x, p.y, p.eps, tol=1e-11, max_iter=100000)
+    assert ref.converged
+    fr = ref.f - ref.f.mean()
+    for w in (0.7, 1.5):
+        r = O.sinkhorn(p.x, p.y, p.eps, tol=1e-11, max_iter=100000, omega=w)
+        assert r.converged and r.err < 1e-11
+        assert np.abs((r.f - r.f.mean()) - fr).max() < 1e-8 * max(1.0, np.abs(fr).max())
+        assert abs(r.E - ref.E) < 1e-10 * max(1.0, abs(ref.E))
+
+
+def test_relaxed_error_and_objective_are_explicit():
+    """With omega != 1 the rows are not exact after an f-update: the oracle's err and E are
+    the explicit plan sums (threshold appendix, Eq. 2), recomputed here from the returned pair."""
+    from oracle import oracle as O
+    p = gen.c1(n=40, seed=4)
+    r = O.sinkhorn(p.x, p.y, p.eps, tol=0, max_iter=5, omega=1.6)
+    x, y = p.x.astype(np.float64), p.y.astype(np.float64)
+    C = ((x[:, None, :] - y[None, :, :]) ** 2).sum(-1)
+    P = np.exp((r.f[:, None] + r.g[None, :] - C) / p.eps)
+    n, m = C.shape
+    err = np.abs(P.sum(1) - 1 / n).sum() + np.abs(P.sum(0) - 1 / m).sum()
+    assert abs(r.err - err) < 1e-12 * max(1.0, err)
+    E = r.f.mean() + r.g.mean() - p.eps * P.sum()
+    assert abs(r.E - E) < 1e-12 * max(1.0, abs(E))
+    assert np.abs(P.sum(1) - 1 / n).sum() > 1e-6   # the row term is really non-zero here
