@@ -181,7 +181,8 @@ class Single(Workload):
             self.kernel = "k_batched (on-chip solver, one CTA)"
         elif self.name == "c3":
             self.p = gen.c3(eps_factor=args.eps_factor or 0.01); self.init = args.init or "gmm"
-            self.mode = "stored"; self.roof = "hbm"; self.kernel = "k_rows + k_cols (stored-cost sweep, K5)"
+            self.mode = "stored"; self.roof = "hbm"
+            self.kernel = "k_stored_fused (single-read fused stored sweep, K5)"
         elif self.name == "c4":
             self.p = gen.c4(); self.init = args.init or "subsample"; self.mode = "online"; self.roof = "mufu"
             self.kernel = "k_lse<3,4> (online LSE pass, K2)"
@@ -189,7 +190,10 @@ class Single(Workload):
         else:
             self.p = gen.c5(eps_factor=args.eps_factor or 1e-2); self.init = args.init or "gaussian"
             self.mode = "online"; self.roof = "tensor"
-            self.kernel = "k_lse_tc (online LSE pass, tcgen05 kind::f16 3-product hi/lo cross term, K3)"
+            self.kernel = "k_lse_tc2 (online LSE pass, CTA-pair tcgen05 kind::f16 3-product hi/lo cross term " \
+                          "with w and the row shift folded into the MMA, K3)"
+            if os.environ.get("SK_TC", "1") == "0":   # comparison leg: the FFMA kernel at d = 64
+                self.roof = "fp32"; self.kernel = "k_lse<64,1> (online LSE pass, FFMA2 cross term, K2)"
         p = self.p
         self.n, self.m, self.d = p.n, p.m, p.d
         self.sharded = self.name == "c4" and world > 1
@@ -336,6 +340,15 @@ def roofline(w, cnt, steps, pk, src, step_ms):
                 "algorithmic": "3 x 2 x 64 fp16 tensor flops per cost entry per pass (3-product hi/lo split)",
                 "flops_per_launch": flops / nl,
                 "mufu_frac": (cnt["dom_entries"] / dom_s) / ex2_peak if dom_s > 0 else 0.0, **common}
+    if w.roof == "fp32":
+        flops = cnt["dom_entries"] * 2 * w.d            # d FMAs per entry for the cross term
+        achieved = flops / dom_s / 1e12 if dom_s > 0 else 0.0
+        peak = N_SM * 128 * 2 * sm_max * 1e6 / 1e12
+        return {"bound": "alu", "pipe": "FP32 FMA", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak,
+                "peak_source": f"derived: {N_SM} SM x 128 FP32 lanes x 2 flop x {sm_max:.0f} MHz ({src})",
+                "algorithmic": "2 d flops (the cross term's d FMAs) per cost entry per pass",
+                "flops_per_launch": flops / nl, **common}
     achieved = cnt["dom_entries"] / dom_s if dom_s > 0 else 0.0
     peak = N_SM * MUFU_EX2_PER_CLK_SM * sm_max * 1e6
     return {"bound": "alu", "pipe": "MUFU.EX2 (SFU)", "achieved": achieved / 1e9,
