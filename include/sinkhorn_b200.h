@@ -142,6 +142,21 @@ sk_status sk_shard_rows(int64_t n_total, int32_t rank, int32_t world, int64_t *r
 sk_status sinkhorn_sort1d_batched(sk_ctx *ctx, int64_t B, int64_t n, const float *x,
                                   int32_t *perm, int32_t *rank);
 
+/* Soft ranks and soft sort (Sec. 3.1) of B 1D problems with
+ * cost (x - y)^2, from potentials (f, g) (normally the output of sinkhorn_solve): with the
+ * plan P_ij = exp((f_i + g_j - (x_i - y_j)^2)/eps) of Eq. (2),
+ *     rank_i = sum_j P_ij z_j / sum_j P_ij,      sort_j = sum_i P_ij x_i / sum_i P_ij
+ * (R-22: conditional means under the plan, which equal the paper's n P z and
+ * n P^T x whenever P has the uniform marginals).  x: B x n; y: m values (y_shared = 1) or
+ * B x m; f: B x n, g: B x m; z: m (nullable: z_j = j + 1, 1-based ranks); rank: B x n,
+ * sort: B x m (either nullable).  One K15 pass (two sweeps of the other side per output, max
+ * first, so no overflow for any finite (f, g)).  SK_EINVAL on bad sizes, eps <= 0 or
+ * non-finite inputs; SK_EUNSUPPORTED if 2n + 3m floats exceed 200 KiB of shared memory.
+ * Asynchronous except for the input check. */
+sk_status sinkhorn_soft_rank_sort(sk_ctx *ctx, int64_t B, int64_t n, int64_t m, const float *x,
+                                  const float *y, int32_t y_shared, float eps, const float *f,
+                                  const float *g, const float *z, float *rank, float *sort);
+
 /* f^(0) = 0: writes B*n zeros to pot. */
 sk_status sinkhorn_init_zero(sk_ctx *ctx, int64_t B, int64_t n, float *pot);
 

@@ -422,3 +422,17 @@ def merge_partials(parts, b, eps):
     for Mp, Sp in parts:
         S = S + Sp * np.exp(Mp - M)
     return eps * np.log(_d(b)) - eps * (M + np.log(S))
+
+
+def soft_rank_sort(x, y, f, g, eps, z=None):
+    """Soft ranks and soft sort (Sec. 3.1; NEXT-2) from potentials (f, g): the plan
+    P_ij = exp((f_i + g_j - (x_i - y_j)^2)/eps) of Eq. (2), then the conditional means
+        rank = (P z) / (P 1),   sort = (P^T x) / (P^T 1)
+    (reading R-22; the paper's n P z and n P^T x whenever P has the uniform marginals).  z
+    defaults to 1, ..., m (1-based ranks).  Plain fp64 matrix products."""
+    x, y, f, g = _d(x).ravel(), _d(y).ravel(), _d(f).ravel(), _d(g).ravel()
+    m = len(y)
+    z = np.arange(1, m + 1, dtype=np.float64) if z is None else _d(z).ravel()
+    C = (x[:, None] - y[None, :]) ** 2
+    P = np.exp((f[:, None] + g[None, :] - C) / eps)
+    return (P @ z) / P.sum(1), (P.T @ x) / P.sum(0)

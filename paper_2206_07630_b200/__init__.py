@@ -228,6 +228,24 @@ def sinkhorn_solve(ctx: Context, x, y, eps: float, tol: float = 1e-3, max_iter: 
     return f, g, out
 
 
+def sinkhorn_soft_rank_sort(ctx: Context, x, y, eps: float, f, g, z=None,
+                            y_shared: bool = False, ranks: bool = True, sort: bool = True):
+    """Soft ranks E_P[z | i] and soft sort E_P[x | j] of B 1D problems from their potentials
+    (P:138-142, R-22).  x: (B, n) or (n,); y: (m,) [shared] or (B, m);
+    f: like x, g: (B, m) or (m,).  Returns (rank, sort) (None where not requested)."""
+    single = x.dim() == 1
+    xb = x.unsqueeze(0) if single else x
+    B, n = xb.shape
+    m = y.shape[-1]
+    r = _empty((B, n), x) if ranks else None
+    s = _empty((B, m), x) if sort else None
+    ctx.check(ctx.lib.sinkhorn_soft_rank_sort(ctx.h, B, n, m, _ptr(x), _ptr(y), int(y_shared), float(eps),
+                                              _ptr(f), _ptr(g), _ptr(z), _ptr(r), _ptr(s)))
+    if single:
+        return (None if r is None else r.view(n)), (None if s is None else s.view(m))
+    return r, s
+
+
 def sinkhorn_solve_sharded_emulated(ctx: Context, world: int, x, y, eps: float, tol: float = 1e-3,
                                     max_iter: int = 10000, check_every: int = 1, a=None, b=None,
                                     mode: str = "auto", f_init=None):

@@ -796,6 +796,34 @@ sk_status sinkhorn_sort1d_batched(sk_ctx *ctx, int64_t B, int64_t n, const float
     return SK_OK;
 }
 
+sk_status sinkhorn_soft_rank_sort(sk_ctx *ctx, int64_t B, int64_t n, int64_t m, const float *x, const float *y,
+                                  int32_t y_shared, float eps, const float *f, const float *g, const float *z,
+                                  float *rank, float *sort) {
+    if (!ctx) return SK_EINVAL;
+    if (B < 1 || n < 1 || m < 1 || !x || !y || !f || !g) return fail(ctx, SK_EINVAL, "bad arguments");
+    if (!(eps > 0.f) || bad_scalar(eps)) return fail(ctx, SK_EINVAL, "eps must be > 0 and finite");
+    if (!rank && !sort) return SK_OK;
+    if (soft_rank_sort_smem((int)n, (int)m) > 200 * 1024 || n > (1 << 20) || m > (1 << 20))
+        return fail(ctx, SK_EUNSUPPORTED, "soft rank/sort stages 2n + 3m floats in shared memory (<= 200 KiB)");
+    Stager sg(ctx);
+    const long long ycount = y_shared ? m : B * m;
+    const float *dx, *dy, *df, *dg, *dz;
+    float *dr, *ds;
+    CK(sg.in_t(x, (size_t)B * n, &dx));
+    CK(sg.in_t(y, (size_t)ycount, &dy));
+    CK(sg.in_t(f, (size_t)B * n, &df));
+    CK(sg.in_t(g, (size_t)B * m, &dg));
+    CK(sg.in_t(z, z ? (size_t)m : 0, &dz));
+    CK(sg.out_t(rank, rank ? (size_t)B * n : 0, &dr));
+    CK(sg.out_t(sort, sort ? (size_t)B * m : 0, &ds));
+    CK(check_arrays(ctx, {{dx, B * n}, {dy, ycount}, {df, B * n}, {dg, B * m}, {dz, dz ? m : 0}}, {},
+                    "soft rank/sort"));
+    CU(launch_soft_rank_sort(B, (int)n, (int)m, dx, dy, y_shared ? 0 : m, df, dg, dz, eps, dr, ds, ctx->stream));
+    ctx->cnt.kernel_launches++;
+    CK(sg.flush());
+    return SK_OK;
+}
+
 sk_status sinkhorn_init_zero(sk_ctx *ctx, int64_t B, int64_t n, float *pot) {
     if (!ctx) return SK_EINVAL;
     if (B < 1 || n < 1 || !pot) return fail(ctx, SK_EINVAL, "B, n >= 1 and pot required");

@@ -24,6 +24,11 @@ struct BatchLaunch {
     float omega = 1.f;   // Alg. 1's relaxation
 };
 bool batched_supported(int d, int n, int m);
+// K15 soft ranks / soft sort of B 1D problems from their potentials (NEXT-2)
+size_t soft_rank_sort_smem(int n, int m);
+cudaError_t launch_soft_rank_sort(long long B, int n, int m, const float *x, const float *y, long long ys,
+                                  const float *f, const float *g, const float *z, float eps, float *rank,
+                                  float *sort, cudaStream_t st);
 size_t batched_smem_bytes(int D, int n, int m);
 cudaError_t launch_batched(const BatchLaunch &L, cudaStream_t st);
 

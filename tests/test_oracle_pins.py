@@ -450,3 +450,46 @@ def test_relaxed_error_and_objective_are_explicit():
     E = r.f.mean() + r.g.mean() - p.eps * P.sum()
     assert abs(r.E - E) < 1e-12 * max(1.0, abs(E))
     assert np.abs(P.sum(1) - 1 / n).sum() > 1e-6   # the row term is really non-zero here
+
+
+# ------------------------------------------------------ soft ranks / soft sort (NEXT-2)
+def test_soft_rank_sort_eps_to_zero_gives_hard_ranks_and_sort():
+    """as eps -> 0 the entropic plan tends to the sorted matching, so n P z -> the
+    ranks of x (1-based) and n P^T x -> sorted x; checked against numpy's argsort / sort."""
+    from oracle import oracle as O
+    rng = np.random.default_rng(11)
+    n = 6
+    x = rng.random(n)
+    y = np.linspace(0.0, 1.0, n)
+    ranks = np.empty(n)
+    ranks[np.argsort(x, kind="stable")] = np.arange(1, n + 1)
+    errs = []
+    f0 = O.init_sort1d(x, y)   # the sorted eps = 0 dual: the small-eps solves converge fast
+    for eps in (1e-2, 1e-3, 2e-4):
+        r = O.sinkhorn(x[:, None], y[:, None], eps, tol=1e-6, max_iter=2000000, f0=f0)
+        assert r.converged
+        rk, st = O.soft_rank_sort(x, y, r.f, r.g, eps)
+        errs.append(max(np.abs(rk - ranks).max(), np.abs(st - np.sort(x)).max()))
+    assert errs[-1] < 1e-3 and errs[0] > errs[-1]   # converges to the hard operators
+
+
+def test_soft_rank_equals_literal_nPz_when_marginals_are_uniform_and_is_equivariant():
+    """R-22: the conditional means equal the paper's literal n P z and n P^T x when P has
+    the uniform marginals: after the oracle's last f-update the rows are exactly 1/n, so the rank
+    must equal n P z to rounding; at convergence (tol 1e-10) the sort equals n P^T x.  And
+    permuting x permutes the soft ranks and leaves the soft sort unchanged."""
+    from oracle import oracle as O
+    rng = np.random.default_rng(12)
+    n = 9
+    x, y = rng.random(n), np.linspace(0.0, 1.0, n)
+    eps = 0.02
+    r = O.sinkhorn(x[:, None], y[:, None], eps, tol=1e-10, max_iter=100000)
+    rk, st = O.soft_rank_sort(x, y, r.f, r.g, eps)
+    P = np.exp((r.f[:, None] + r.g[None, :] - (x[:, None] - y[None, :]) ** 2) / eps)
+    z = np.arange(1, n + 1)
+    assert np.abs(rk - n * P @ z).max() < 1e-9 * n
+    assert np.abs(st - n * P.T @ x).max() < 1e-8
+    perm = rng.permutation(n)
+    rp = O.sinkhorn(x[perm, None], y[:, None], eps, tol=1e-10, max_iter=100000)
+    rk2, st2 = O.soft_rank_sort(x[perm], y, rp.f, rp.g, eps)
+    assert np.abs(rk2 - rk[perm]).max() < 1e-6 and np.abs(st2 - st).max() < 1e-6
