@@ -226,9 +226,12 @@ class Single(Workload):
         self.xh = torch.from_numpy(p.x).pin_memory()
         self.yh = torch.from_numpy(p.y).pin_memory()
         self.dev = dev
-        if self.init == "gmm":
+        if self.init == "gmm_given":   # the generating mixtures as the GMM parameters (no fitting)
             self.gx = {k: torch.from_numpy(v).to(dev) for k, v in p.extra["gmm_x"].items()}
             self.gy = {k: torch.from_numpy(v).to(dev) for k, v in p.extra["gmm_y"].items()}
+        if self.init == "gmm":          # fit both K = 8 GMMs (on the device, K16) inside the step
+            from workloads import gen as _g
+            self.gmm_idx = (_g.gmm_start_idx(p.n, 8, 3), _g.gmm_start_idx(p.m, 8, 4))
         if self.init == "subsample":
             self.ix = torch.from_numpy(p.extra["idx_x"]).to(dev)
             self.iy = torch.from_numpy(p.extra["idx_y"]).to(dev)
@@ -250,7 +253,10 @@ class Single(Workload):
         if self.init == "gaussian":
             f0, _ = sk.sinkhorn_init_gaussian(self.ctx, x, y)
         elif self.init == "gmm":
-            import torch
+            gx, _ = sk.sinkhorn_fit_gmm(self.ctx, x, 8, self.gmm_idx[0], iters=self.args.gmm_iters)
+            gy, _ = sk.sinkhorn_fit_gmm(self.ctx, y, 8, self.gmm_idx[1], iters=self.args.gmm_iters)
+            f0, _ = sk.sinkhorn_init_gmm(self.ctx, x, y, gx, gy, p.eps)
+        elif self.init == "gmm_given":
             gx, gy = self.gx, self.gy
             if not x.is_cuda:
                 gx = {k: v.cpu() for k, v in gx.items()}
@@ -556,7 +562,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
-    ap.add_argument("--init", default=None, help="c3/c4/c5 initializer: zero|gaussian|gmm|subsample")
+    ap.add_argument("--init", default=None,
+                    help="c3/c4/c5 initializer: zero|gaussian|gmm (fitted on the device)|gmm_given|subsample")
+    ap.add_argument("--gmm-iters", type=int, default=50, help="EM iterations of the device GMM fit (init gmm)")
     ap.add_argument("--eps-factor", type=float, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-k14", action="store_true", help="skip the K14 microbenchmarks")

@@ -436,3 +436,43 @@ def soft_rank_sort(x, y, f, g, eps, z=None):
     C = (x[:, None] - y[None, :]) ** 2
     P = np.exp((f[:, None] + g[None, :] - C) / eps)
     return (P @ z) / P.sum(1), (P.T @ x) / P.sum(0)
+
+
+def gmm_fit(x, K, init_idx, iters, reg_covar=1e-6):
+    """EM for a K-component full-covariance GMM (NEXT-3; "we fit first two K-component
+    GMMs", done with sklearn on the CPU in the paper).  Start (R-23): weights 1/K, means
+    x[init_idx], covariances the biased covariance of x + reg I.  Each iteration, literally:
+        E-step  r_ik = alpha_k N(x_i; m_k, S_k) / sum_l alpha_l N(x_i; m_l, S_l)   (gmm_log_resp)
+        M-step  n_k = sum_i r_ik, alpha_k = n_k / n, m_k = sum_i r_ik x_i / n_k,
+                S_k = sum_i r_ik (x_i - m_k)(x_i - m_k)^T / n_k + reg I.
+    Returns (weights, means, covs, mean log-likelihood of the returned parameters)."""
+    x = _pts(x)
+    n, d = x.shape
+    means = x[np.asarray(init_idx)].copy()
+    m0 = x.mean(0)
+    cov0 = (x - m0).T @ (x - m0) / n + reg_covar * np.eye(d)
+    covs = np.repeat(cov0[None], K, axis=0)
+    weights = np.full(K, 1.0 / K)
+    for _ in range(iters):
+        r = np.exp(gmm_log_resp(x, weights, means, covs))
+        nk = r.sum(0) + 10 * np.finfo(np.float64).eps   # (sklearn's guard for empty components)
+        weights = nk / n
+        means = (r.T @ x) / nk[:, None]
+        for k in range(K):
+            diff = x - means[k]
+            covs[k] = (r[:, k, None] * diff).T @ diff / nk[k] + reg_covar * np.eye(d)
+    return weights, means, covs, gmm_loglik(x, weights, means, covs)
+
+
+def gmm_loglik(x, weights, means, covs):
+    """Mean over points of log sum_k alpha_k N(x_i; m_k, S_k) (Cholesky, a library step)."""
+    x = _pts(x)
+    n, d = x.shape
+    lp = np.empty((n, len(weights)))
+    for k in range(len(weights)):
+        L = np.linalg.cholesky(_d(covs[k]))
+        z = np.linalg.solve(L, (x - _d(means[k])).T)
+        lp[:, k] = np.log(float(weights[k])) - 0.5 * (z * z).sum(0) - np.log(np.diag(L)).sum() \
+            - 0.5 * d * np.log(2 * np.pi)
+    mx = lp.max(1, keepdims=True)
+    return float(np.mean(mx[:, 0] + np.log(np.exp(lp - mx).sum(1))))

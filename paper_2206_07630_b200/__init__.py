@@ -228,6 +228,21 @@ def sinkhorn_solve(ctx: Context, x, y, eps: float, tol: float = 1e-3, max_iter: 
     return f, g, out
 
 
+def sinkhorn_fit_gmm(ctx: Context, x, K: int, init_idx, iters: int = 100, reg_covar: float = 1e-6):
+    """EM fit of a K-component full-covariance GMM of x (n, d) from means x[init_idx] (NEXT-3).
+    Returns ({'weights', 'means', 'covs'} as sinkhorn_init_gmm takes them, mean log-likelihood)."""
+    n, d = x.shape
+    idx = init_idx if isinstance(init_idx, torch.Tensor) else torch.as_tensor(init_idx, dtype=torch.int32)
+    idx = idx.to(torch.int32).contiguous()
+    w = _empty((K,), x)
+    mu = _empty((K, d), x)
+    cov = _empty((K, d, d), x)
+    ll = ctypes.c_double()
+    ctx.check(ctx.lib.sinkhorn_fit_gmm(ctx.h, n, d, _ptr(x), int(K), _ptr(idx, torch.int32), int(iters), float(reg_covar),
+                                       _ptr(w), _ptr(mu), _ptr(cov), ctypes.byref(ll)))
+    return {"weights": w, "means": mu, "covs": cov}, ll.value
+
+
 def sinkhorn_soft_rank_sort(ctx: Context, x, y, eps: float, f, g, z=None,
                             y_shared: bool = False, ranks: bool = True, sort: bool = True):
     """Soft ranks E_P[z | i] and soft sort E_P[x | j] of B 1D problems from their potentials

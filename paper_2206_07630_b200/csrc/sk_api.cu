@@ -81,7 +81,7 @@ enum BufId {
     B_STAGE0 = 0, B_STAGE_END = 16,   // staging of host arrays
     B_FLAG = 16, B_XPACK, B_XC, B_XNK, B_XPOT, B_YPACK, B_YC, B_YNK, B_YPOT, B_PART, B_BLKE, B_BLKB,
     B_STATUS, B_COST, B_REP, B_SORT, B_PERM, B_YSORT, B_GAUSS, B_GAUSS2, B_GMM, B_SUBW, B_SUBZ,
-    B_SUBF, B_SUBG, B_IDX, B_OUT, B_FA, B_QUEUE, B_XIMG, B_YIMG, B_XLSE, B_YLSE, B_TCMAX, B_NBUF
+    B_SUBF, B_SUBG, B_IDX, B_OUT, B_FA, B_QUEUE, B_XIMG, B_YIMG, B_XLSE, B_YLSE, B_TCMAX, B_EMST, B_EMPART, B_EMIDX, B_NBUF
 };
 
 sk_status fail(sk_ctx *c, sk_status s, const char *fmt, ...) {
@@ -793,6 +793,53 @@ sk_status sinkhorn_sort1d_batched(sk_ctx *ctx, int64_t B, int64_t n, const float
     CU(cudaMemcpyAsync(ctx->h_flag, flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));
     if (*ctx->h_flag) return fail(ctx, SK_EINVAL, "NaN key");
+    return SK_OK;
+}
+
+sk_status sinkhorn_fit_gmm(sk_ctx *ctx, int64_t n, int32_t d, const float *x, int32_t K, const int32_t *init_idx,
+                           int32_t iters, float reg_covar, float *weights, float *means, float *covs, double *loglik) {
+    if (!ctx) return SK_EINVAL;
+    if (n < 1 || K < 1 || K > n || !x || !init_idx || !weights || !means || !covs || iters < 0)
+        return fail(ctx, SK_EINVAL, "bad arguments (need 1 <= K <= n, iters >= 0, non-NULL arrays)");
+    if (d < 1 || d > 32 || K > 64) return fail(ctx, SK_EUNSUPPORTED, "GMM fitting supports d <= 32, K <= 64");
+    if (!(reg_covar >= 0.f) || bad_scalar(reg_covar)) return fail(ctx, SK_EINVAL, "reg_covar must be >= 0");
+    // the start indices: in range and distinct (checked on the host: K values)
+    std::vector<int32_t> hidx(K);
+    if (is_device_ptr(init_idx)) CU(cudaMemcpy(hidx.data(), init_idx, sizeof(int32_t) * K, cudaMemcpyDeviceToHost));
+    else memcpy(hidx.data(), init_idx, sizeof(int32_t) * K);
+    {
+        std::vector<int32_t> srt(hidx);
+        std::sort(srt.begin(), srt.end());
+        for (int k = 0; k < K; ++k)
+            if (srt[k] < 0 || srt[k] >= n || (k && srt[k] == srt[k - 1]))
+                return fail(ctx, SK_EINVAL, "init_idx must hold K distinct indices in [0, n)");
+    }
+    Stager sg(ctx);
+    const float *dx;
+    float *dw, *dm, *dc;
+    CK(sg.in_t(x, (size_t)n * d, &dx));
+    CK(sg.out_t(weights, (size_t)K, &dw));
+    CK(sg.out_t(means, (size_t)K * d, &dm));
+    CK(sg.out_t(covs, (size_t)K * d * d, &dc));
+    CK(check_arrays(ctx, {{dx, n * d}}, {}, "GMM fit"));
+    ENSURE(didx, int, B_EMIDX, K);
+    CU(cudaMemcpyAsync(didx, hidx.data(), sizeof(int32_t) * K, cudaMemcpyHostToDevice, ctx->stream));
+    ENSURE(st, double, B_EMST, 2 * em_state_doubles(K, d) + 2 * (size_t)d * d + d + 1);
+    ENSURE(part, double, B_EMPART, std::max(em_work_doubles(K, d), (size_t)296 * d * d));
+    ENSURE(flag, int, B_FLAG, 4);
+    double *mean0 = st + 2 * em_state_doubles(K, d), *cov0 = mean0 + d, *ll = cov0 + (size_t)d * d;
+    CU(cudaMemsetAsync(flag, 0, sizeof(int), ctx->stream));
+    CU(launch_moments(dx, nullptr, n, d, mean0, cov0, part, (long long)std::max(em_work_doubles(K, d), (size_t)296 * d * d),
+                      ctx->stream));
+    CU(launch_gmm_fit(dx, n, d, K, didx, cov0, iters, (double)reg_covar, st, part, flag, dw, dm, dc, ll, ctx->stream));
+    ctx->cnt.kernel_launches += 4 + 4 * (iters + 1) + 3;
+    CK(sg.flush());
+    double hll = 0.0;
+    CU(cudaMemcpyAsync(ctx->h_flag, flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaMemcpyAsync(&hll, ll, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    if (loglik) *loglik = hll;
+    if (*ctx->h_flag) return fail(ctx, SK_ENONFINITE, "a component covariance lost positive definiteness");
     return SK_OK;
 }
 

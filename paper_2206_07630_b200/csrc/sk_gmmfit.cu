@@ -1,0 +1,279 @@
+// sk_gmmfit.cu — K16: fitting the K-component GMMs of the GMM initializer on the device
+// (SURVEY.md NEXT-3).  P:209: "Given two empirical measures mu, nu, we fit first two
+// K-component GMMs"; the paper fits them with sklearn on the CPU, which dominates its GMM
+// initializer's cost.  Here: expectation-maximisation for full-covariance
+// mixtures, fp64 state, from a caller-given start (reading R-23):
+//     weights 1/K, means = x[idx_k], covariances = the biased covariance of x + reg I;
+//   E-step  log p_ik = log w_k - 1/2 |L_k^{-1}(x_i - m_k)|^2 - log det L_k   (S_k = L_k L_k^T),
+//           r_ik = exp(log p_ik - LSE_k log p_ik),  ll = mean_i LSE_k log p_ik - d/2 log 2 pi;
+//   M-step  n_k = sum_i r_ik,  w_k = n_k / n,  m_k = sum_i r_ik x_i / n_k,
+//           S_k = sum_i r_ik x_i x_i^T / n_k - m_k m_k^T + reg I.
+// Kernels per iteration: k_em_chol (one CTA per component: Cholesky, L^-1, log det),
+// k_em_estep (fixed point chunks per CTA: responsibilities, then the sufficient statistics
+// (n_k, sum r x, sum r x x^T upper triangle) accumulated per thread-owned statistic in fp64 and
+// written as per-CTA partials), k_em_mstep (one CTA: fixed-order reduction of the partials and
+// the parameter update).  Deterministic (fixed partition and reduction order).
+#include <cfloat>
+
+#include "sk_internal.h"
+#include "sk_common.cuh"
+
+namespace sk {
+
+constexpr int kEmT = 256;
+constexpr int kEmTile = 64;      // points staged per E-step tile
+constexpr int kEmBlocks = 296;   // fixed point partition (2 CTAs per SM)
+
+__host__ __device__ inline int em_stats(int K, int d) { return K * (1 + d + d * (d + 1) / 2); }
+
+// state (doubles): W[K] | MU[K d] | COV[K d d] | LINV[K d d] | LOGDET[K] | LL[1]
+struct EmState {
+    double *W, *MU, *COV, *LINV, *LOGDET, *LL;
+};
+__host__ __device__ inline EmState em_state(double *base, int K, int d) {
+    EmState s;
+    s.W = base;
+    s.MU = s.W + K;
+    s.COV = s.MU + (long long)K * d;
+    s.LINV = s.COV + (long long)K * d * d;
+    s.LOGDET = s.LINV + (long long)K * d * d;
+    s.LL = s.LOGDET + K;
+    return s;
+}
+size_t em_state_doubles(int K, int d) { return (size_t)K * (1 + d + 2 * d * d + 1) + 1; }
+size_t em_partial_doubles(int K, int d) { return (size_t)kEmBlocks * (em_stats(K, d) + 1); }   // + S + 1 reduced (em_work_doubles)
+size_t em_work_doubles(int K, int d) { return em_partial_doubles(K, d) + em_stats(K, d) + 1; }
+
+// start: w = 1/K, m_k = x[idx_k], S_k = cov0 + reg I (cov0: biased covariance of x)
+__global__ void k_em_init(const float *__restrict__ x, int d, int K, const int *__restrict__ idx,
+                          const double *__restrict__ cov0, double reg, double *base) {
+    const EmState s = em_state(base, K, d);
+    for (int e = threadIdx.x; e < K * d * d; e += blockDim.x) {
+        const int r = (e / d) % d, c = e % d;
+        s.COV[e] = cov0[r * d + c] + (r == c ? reg : 0.0);
+    }
+    for (int e = threadIdx.x; e < K * d; e += blockDim.x)
+        s.MU[e] = (double)x[(long long)idx[e / d] * d + e % d];
+    for (int k = threadIdx.x; k < K; k += blockDim.x) s.W[k] = 1.0 / K;
+}
+
+// Cholesky S_k = L L^T (fp64, textbook Cholesky-Banachiewicz), L^{-1}, log det L.
+__global__ void __launch_bounds__(kEmT) k_em_chol(double *base, int K, int d, int *flags) {
+    extern __shared__ double sm[];
+    const EmState s = em_state(base, K, d);
+    const int dd = d * d, k = blockIdx.x;
+    double *L = sm, *Li = sm + dd;
+    for (int e = threadIdx.x; e < dd; e += blockDim.x) {
+        const int i = e / d, j = e % d;
+        L[e] = 0.5 * (s.COV[(long long)k * dd + i * d + j] + s.COV[(long long)k * dd + j * d + i]);
+        Li[e] = 0.0;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int bad = 0;
+        for (int j = 0; j < d; ++j) {
+            double v = L[j * d + j];
+            for (int t = 0; t < j; ++t) v -= L[j * d + t] * L[j * d + t];
+            if (!(v > 0.0)) { bad = 1; v = 1e-300; }
+            const double ljj = sqrt(v);
+            L[j * d + j] = ljj;
+            for (int i = j + 1; i < d; ++i) {
+                double u = L[i * d + j];
+                for (int t = 0; t < j; ++t) u -= L[i * d + t] * L[j * d + t];
+                L[i * d + j] = u / ljj;
+            }
+            for (int t = j + 1; t < d; ++t) L[j * d + t] = 0.0;
+        }
+        double ld = 0.0;
+        for (int j = 0; j < d; ++j) ld += log(L[j * d + j]);
+        s.LOGDET[k] = ld;
+        if (bad) atomicOr(flags, 1);
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < d; c += blockDim.x) {
+        for (int i = 0; i < d; ++i) {
+            double v = (i == c) ? 1.0 : 0.0;
+            for (int t = 0; t < i; ++t) v -= L[i * d + t] * Li[t * d + c];
+            Li[i * d + c] = v / L[i * d + i];
+        }
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < dd; e += blockDim.x) s.LINV[(long long)k * dd + e] = Li[e];
+}
+
+// E-step + sufficient statistics over this CTA's fixed chunk of points.  Statistic s of
+// component k (base k (1 + d + T)): 0 = n_k, 1..d = sum r x, then sum r x_a x_b for a <= b.
+template <int MAXS>
+__global__ void __launch_bounds__(kEmT) k_em_estep(const float *__restrict__ x, long long n, int d, int K,
+                                                    const double *__restrict__ base, double *part) {
+    extern __shared__ double sm[];
+    double *xs = sm;                          // [kEmTile][d]
+    double *rs = xs + kEmTile * d;            // [kEmTile][K]
+    double *lls = rs + kEmTile * K;           // [kEmTile]
+    const EmState s = em_state(const_cast<double *>(base), K, d);
+    const int T = d * (d + 1) / 2, per = 1 + d + T, S = K * per;
+    const long long chunk = (n + gridDim.x - 1) / gridDim.x;
+    const long long p0 = blockIdx.x * chunk, p1 = min(n, p0 + chunk);
+    // this thread's statistics: (k, kind, a, b) decoded once
+    double acc[MAXS];
+    short sk_[MAXS], sa[MAXS], sb[MAXS];
+#pragma unroll
+    for (int u = 0; u < MAXS; ++u) {
+        acc[u] = 0.0;
+        const int st = threadIdx.x + u * kEmT;
+        sk_[u] = -1;
+        if (st < S) {
+            const int k = st / per, o = st % per;
+            sk_[u] = (short)k;
+            if (o == 0) { sa[u] = -1; sb[u] = -1; }
+            else if (o <= d) { sa[u] = (short)(o - 1); sb[u] = -1; }
+            else {   // packed upper triangle, row-major: (a, b), a <= b
+                int q = o - 1 - d, a = 0;
+                while (q >= d - a) { q -= d - a; ++a; }
+                sa[u] = (short)a; sb[u] = (short)(a + q);
+            }
+        }
+    }
+    double ll = 0.0;
+    for (long long t0 = p0; t0 < p1; t0 += kEmTile) {
+        const int np = (int)min((long long)kEmTile, p1 - t0);
+        for (int e = threadIdx.x; e < np * d; e += kEmT) xs[e] = (double)x[(t0 + e / d) * d + e % d];
+        __syncthreads();
+        for (int e = threadIdx.x; e < np * K; e += kEmT) {   // log p of (point, component) pairs
+            const int pp = e / K, k = e % K;
+            const double *xi = xs + pp * d;
+            const double *Li = s.LINV + (long long)k * d * d;
+            const double *mk = s.MU + (long long)k * d;
+            double q = 0.0;
+            for (int r = 0; r < d; ++r) {
+                double z = 0.0;
+                for (int c = 0; c <= r; ++c) z = fma(Li[r * d + c], xi[c] - mk[c], z);
+                q = fma(z, z, q);
+            }
+            rs[pp * K + k] = log(s.W[k]) - 0.5 * q - s.LOGDET[k];
+        }
+        __syncthreads();
+        if (threadIdx.x < np) {   // normalise point t0 + threadIdx.x (fixed k order)
+            double *ri = rs + threadIdx.x * K;
+            double mx = -INFINITY;
+            for (int k = 0; k < K; ++k) mx = fmax(mx, ri[k]);
+            double den = 0.0;
+            for (int k = 0; k < K; ++k) den += exp(ri[k] - mx);
+            const double lse = mx + log(den);
+            for (int k = 0; k < K; ++k) ri[k] = exp(ri[k] - lse);
+            lls[threadIdx.x] = lse;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < MAXS; ++u) {
+            if (sk_[u] < 0) continue;
+            const int k = sk_[u], a = sa[u], b = sb[u];
+            double v = acc[u];
+            for (int p = 0; p < np; ++p) {
+                const double r = rs[p * K + k];
+                const double f = a < 0 ? 1.0 : (b < 0 ? xs[p * d + a] : xs[p * d + a] * xs[p * d + b]);
+                v = fma(r, f, v);
+            }
+            acc[u] = v;
+        }
+        if (threadIdx.x == 0)
+            for (int p = 0; p < np; ++p) ll += lls[p];
+        __syncthreads();
+    }
+    double *out = part + (long long)blockIdx.x * (S + 1);
+#pragma unroll
+    for (int u = 0; u < MAXS; ++u) {
+        const int st = threadIdx.x + u * kEmT;
+        if (st < S) out[st] = acc[u];
+    }
+    if (threadIdx.x == 0) out[S] = ll;
+}
+
+// Reduction of the per-CTA partials, one warp per statistic: lane l sums CTAs l, l + 32, ... in
+// order, then a fixed shuffle tree (deterministic).  out[S + 1].
+__global__ void __launch_bounds__(kEmT) k_em_reduce(const double *part, int nb, int S1, double *out) {
+    const int st = (blockIdx.x * kEmT + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (st >= S1) return;
+    double v = 0.0;
+    for (int b = lane; b < nb; b += 32) v += part[(long long)b * S1 + st];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) out[st] = v;
+}
+
+// M-step from the reduced statistics: w, m, S (+ reg I) and the mean log-likelihood of the E-step
+// that produced them.
+__global__ void __launch_bounds__(kEmT) k_em_mstep(const double *tot, long long n, int d, int K, double reg,
+                                                    double *base) {
+    const EmState s = em_state(base, K, d);
+    const int T = d * (d + 1) / 2, per = 1 + d + T, S = K * per;
+    const double eps10 = 10.0 * DBL_EPSILON;   // (as sklearn: n_k + 10 eps guards empty components)
+    for (int e = threadIdx.x; e < K * d; e += blockDim.x) {
+        const int k = e / d, a = e % d;
+        s.MU[e] = tot[k * per + 1 + a] / (tot[k * per] + eps10);
+    }
+    for (int k = threadIdx.x; k < K; k += blockDim.x) s.W[k] = (tot[k * per] + eps10) / (double)n;
+    __syncthreads();
+    for (int e = threadIdx.x; e < K * d * d; e += blockDim.x) {
+        const int k = e / (d * d), r = (e / d) % d, c = e % d;
+        const int a = min(r, c), b = max(r, c);
+        const int o = 1 + d + a * d - a * (a - 1) / 2 + (b - a);   // packed (a, b), a <= b
+        const double nk = tot[k * per] + eps10;
+        s.COV[e] = tot[k * per + o] / nk - s.MU[k * d + r] * s.MU[k * d + c] + (r == c ? reg : 0.0);
+    }
+    if (threadIdx.x == 0) *s.LL = tot[S] / (double)n - 0.5 * d * log(2.0 * 3.14159265358979323846);
+}
+
+__global__ void k_em_out(const double *base, int K, int d, float *w, float *mu, float *cov, double *ll_out) {
+    const EmState s = em_state(const_cast<double *>(base), K, d);
+    for (int e = threadIdx.x; e < K * d * d; e += blockDim.x) cov[e] = (float)s.COV[e];
+    for (int e = threadIdx.x; e < K * d; e += blockDim.x) mu[e] = (float)s.MU[e];
+    for (int k = threadIdx.x; k < K; k += blockDim.x) w[k] = (float)s.W[k];
+    if (threadIdx.x == 0 && ll_out) *ll_out = *s.LL;
+}
+
+template <int MAXS>
+static cudaError_t launch_estep(const float *x, long long n, int d, int K, const double *base, double *part,
+                                cudaStream_t st) {
+    const size_t smem = sizeof(double) * ((size_t)kEmTile * (d + K) + kEmTile);
+    k_em_estep<MAXS><<<kEmBlocks, kEmT, smem, st>>>(x, n, d, K, base, part);
+    return cudaGetLastError();
+}
+
+// iters EM steps from the start above; the state (em_state_doubles) and partials
+// (em_partial_doubles) are caller workspace; cov0 = biased covariance of x (d x d).  A final
+// E-step evaluates the mean log-likelihood of the returned parameters.
+cudaError_t launch_gmm_fit(const float *x, long long n, int d, int K, const int *idx, const double *cov0,
+                           int iters, double reg, double *state, double *part, int *flags, float *w, float *mu,
+                           float *cov, double *ll_out, cudaStream_t st) {
+    const int S = em_stats(K, d);
+    const int maxs = (S + kEmT - 1) / kEmT;
+    if (d < 1 || d > 32 || K < 1 || maxs > 40) return cudaErrorInvalidValue;
+    k_em_init<<<1, kEmT, 0, st>>>(x, d, K, idx, cov0, reg, state);
+    const size_t smem_chol = 2 * sizeof(double) * d * d;
+    double *tot = part + em_partial_doubles(K, d);   // [S + 1] after the partials
+    const int rblocks = (32 * (S + 1) + kEmT - 1) / kEmT;
+    cudaError_t e = cudaSuccess;
+    for (int it = 0; it <= iters; ++it) {
+        k_em_chol<<<K, kEmT, smem_chol, st>>>(state, K, d, flags);
+        if (maxs <= 8) e = launch_estep<8>(x, n, d, K, state, part, st);
+        else if (maxs <= 20) e = launch_estep<20>(x, n, d, K, state, part, st);
+        else e = launch_estep<40>(x, n, d, K, state, part, st);
+        if (e != cudaSuccess) return e;
+        k_em_reduce<<<rblocks, kEmT, 0, st>>>(part, kEmBlocks, S + 1, tot);
+        if (it == iters) {   // evaluation only: the log-likelihood of the returned parameters
+            k_em_mstep<<<1, kEmT, 0, st>>>(tot, n, d, K, reg, state + em_state_doubles(K, d));
+            break;
+        }
+        k_em_mstep<<<1, kEmT, 0, st>>>(tot, n, d, K, reg, state);
+    }
+    // the evaluation pass wrote a scratch state; its LL is the returned parameters' likelihood
+    const EmState scratch = em_state(state + em_state_doubles(K, d), K, d);
+    e = cudaMemcpyAsync(em_state(state, K, d).LL, scratch.LL, sizeof(double), cudaMemcpyDeviceToDevice, st);
+    if (e != cudaSuccess) return e;
+    k_em_out<<<1, kEmT, 0, st>>>(state, K, d, w, mu, cov, ll_out);
+    return cudaGetLastError();
+}
+
+int gmm_fit_blocks() { return kEmBlocks; }
+
+}  // namespace sk

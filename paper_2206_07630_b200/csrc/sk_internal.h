@@ -24,6 +24,13 @@ struct BatchLaunch {
     float omega = 1.f;   // Alg. 1's relaxation
 };
 bool batched_supported(int d, int n, int m);
+// K16 GMM fitting by EM (NEXT-3); state and partial workspace sizes in doubles
+size_t em_state_doubles(int K, int d);
+size_t em_partial_doubles(int K, int d);
+size_t em_work_doubles(int K, int d);   // partials + the reduced statistics (launch_gmm_fit's part)
+cudaError_t launch_gmm_fit(const float *x, long long n, int d, int K, const int *idx, const double *cov0,
+                           int iters, double reg, double *state /* 2 x em_state_doubles */, double *part,
+                           int *flags, float *w, float *mu, float *cov, double *ll_out, cudaStream_t st);
 // K15 soft ranks / soft sort of B 1D problems from their potentials (NEXT-2)
 size_t soft_rank_sort_smem(int n, int m);
 cudaError_t launch_soft_rank_sort(long long B, int n, int m, const float *x, const float *y, long long ys,

@@ -493,3 +493,44 @@ def test_soft_rank_equals_literal_nPz_when_marginals_are_uniform_and_is_equivari
     rp = O.sinkhorn(x[perm, None], y[:, None], eps, tol=1e-10, max_iter=100000)
     rk2, st2 = O.soft_rank_sort(x[perm], y, rp.f, rp.g, eps)
     assert np.abs(rk2 - rk[perm]).max() < 1e-6 and np.abs(st2 - st).max() < 1e-6
+
+
+# --------------------------------------------------------------- GMM fitting (NEXT-3)
+def test_gmm_fit_matches_sklearn_em():
+    """The oracle's EM is sklearn's GaussianMixture (full covariance, the paper's fitting tool,
+    P:568) started from the same parameters: equal weights, means and covariances."""
+    from oracle import oracle as O
+    from sklearn.mixture import GaussianMixture
+    rng = np.random.default_rng(21)
+    x = np.concatenate([rng.standard_normal((300, 3)) * 0.5 + c for c in ([0, 0, 0], [3, 1, 0], [-2, 2, 1])])
+    K, iters, reg = 3, 12, 1e-6
+    idx = rng.choice(len(x), K, replace=False)
+    w, m, S, ll = O.gmm_fit(x, K, idx, iters, reg)
+    m0 = x.mean(0)
+    cov0 = (x - m0).T @ (x - m0) / len(x) + reg * np.eye(3)
+    gm = GaussianMixture(K, covariance_type="full", reg_covar=reg, max_iter=iters, tol=0.0, init_params="random",
+                         weights_init=np.full(K, 1.0 / K), means_init=x[idx],
+                         precisions_init=np.repeat(np.linalg.inv(cov0)[None], K, 0), random_state=0)
+    import warnings
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        gm.fit(x)
+    assert np.abs(w - gm.weights_).max() < 1e-10
+    assert np.abs(m - gm.means_).max() < 1e-9
+    assert np.abs(S - gm.covariances_).max() < 1e-9
+    assert abs(ll - gm.score(x)) < 1e-9
+
+
+def test_gmm_fit_em_monotone_and_single_component_closed_form():
+    """EM never decreases the likelihood (textbook property); K = 1 gives the sample mean and
+    biased covariance (+ reg) after one step, whatever the start."""
+    from oracle import oracle as O
+    rng = np.random.default_rng(22)
+    x = rng.standard_normal((400, 4)) @ rng.standard_normal((4, 4)) + 1.5
+    idx = rng.choice(400, 4, replace=False)
+    lls = [O.gmm_fit(x, 4, idx, t)[3] for t in range(0, 8)]
+    assert all(b >= a - 1e-12 for a, b in zip(lls, lls[1:]))
+    w, m, S, _ = O.gmm_fit(x, 1, [7], 1, 1e-6)
+    mu = x.mean(0)
+    assert abs(w[0] - 1) < 1e-12 and np.abs(m[0] - mu).max() < 1e-12
+    assert np.abs(S[0] - ((x - mu).T @ (x - mu) / 400 + 1e-6 * np.eye(4))).max() < 1e-12

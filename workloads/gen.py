@@ -128,6 +128,12 @@ def c3(n: int = 16384, K: int = 8, d: int = 16, eps_factor: float = 0.01) -> Pro
     return Problem("c3", x, y, eps, extra={"gmm_x": f32p(px), "gmm_y": f32p(py)})
 
 
+def gmm_start_idx(n: int, K: int, seed: int) -> np.ndarray:
+    """Start indices of the device GMM fit (NEXT-3, R-23): K distinct points drawn uniformly
+    without replacement (C3: seed 3 for x, seed 4 for y)."""
+    return np.random.default_rng(seed).choice(n, K, replace=False).astype(np.int32)
+
+
 # --------------------------------------------------------------------------- C4
 def _rgb_mixture(n: int, rng, clusters: int = 12) -> np.ndarray:
     centers = rng.uniform(0.1, 0.9, (clusters, 3))
