@@ -142,6 +142,26 @@ sk_status sk_shard_rows(int64_t n_total, int32_t rank, int32_t world, int64_t *r
 sk_status sinkhorn_sort1d_batched(sk_ctx *ctx, int64_t B, int64_t n, const float *x,
                                   int32_t *perm, int32_t *rank);
 
+/* Implicit differentiation: the vector-Jacobian product of the
+ * optimal potentials (f*, g*) = F(x, y, a, b) with a cotangent z = (zf, zg), for the cost
+ * |x - y|^2.  With P_ij = exp((f_i + g_j - C_ij)/eps), r = P 1, c = P^T 1 and
+ * M = [[diag(r), P], [P^T, diag(c)]] (= -eps J_H,(f,g), H = the gradient of Eq. (2))
+ * gives J_F^T z = eps J_H,.^T w with w = M^+ z: w by conjugate gradients preconditioned with
+ * diag(r, c), z first projected on e^perp, e = (1_n, -1_m) (the shift of (f, g): only
+ * shift-invariant losses, sum zf = sum zg, are meaningful; the e component is dropped), until
+ * |residual| <= cg_tol |z| (checked every 8 iterations, at most cg_max_iter); then
+ *   grad_x_i = 2 sum_j P_ij (w_f,i + w_g,j)(x_i - y_j),  grad_y_j = 2 sum_i P_ij (w_f,i + w_g,j)(y_j - x_i),
+ *   grad_a = eps w_f,  grad_b = eps w_g.
+ * (f, g) must be (close to) optimal — normally sinkhorn_solve's output.  x: n x d, y: m x d,
+ * f: n, g: m, zf: n, zg: m; outputs (each nullable): grad_x n x d, grad_y m x d, grad_a n,
+ * grad_b m.  cg_iters / cg_relres (host, nullable): iterations and the final relative
+ * residual.  SK_EINVAL on bad sizes, eps or cg_tol <= 0, non-finite inputs; SK_EUNSUPPORTED
+ * for d > 64.  Blocks. */
+sk_status sinkhorn_vjp(sk_ctx *ctx, int64_t n, int64_t m, int32_t d, const float *x, const float *y,
+                       float eps, const float *f, const float *g, const float *zf, const float *zg,
+                       float cg_tol, int32_t cg_max_iter, float *grad_x, float *grad_y, float *grad_a,
+                       float *grad_b, int32_t *cg_iters, double *cg_relres);
+
 /* GMM fitting for the GMM initializer (Sec. 3.3, "we fit first two K-component GMMs";
  * the paper fits on the CPU with sklearn): `iters` EM steps for a
  * full-covariance K-component mixture of x (n x d, row-major) from the start (R-23)

@@ -476,3 +476,28 @@ def gmm_loglik(x, weights, means, covs):
             - 0.5 * d * np.log(2 * np.pi)
     mx = lp.max(1, keepdims=True)
     return float(np.mean(mx[:, 0] + np.log(np.exp(lp - mx).sum(1))))
+
+
+def sinkhorn_vjp(x, y, f, g, eps, zf, zg):
+    """Implicit differentiation (NEXT-4) of the optimal potentials, dense fp64:
+    H(f, g) = [a - P 1; b - P^T 1] (the gradient of Eq. (2)), J_H,(f,g) = -(1/eps) M with
+    M = [[diag(P 1), P], [P^T, diag(P^T 1)]], so J_F^T z = eps J_H,.^T M^+ z with z
+    projected on e^perp (e = (1, -1), the shift of (f, g)) and the min-norm M^+ z (numpy lstsq,
+    a library step).  For C_ij = |x_i - y_j|^2:
+        grad_x_i = 2 sum_j P_ij (w_f,i + w_g,j)(x_i - y_j), grad_y_j = 2 sum_i P_ij (w_f,i + w_g,j)(y_j - x_i),
+        grad_a = eps w_f, grad_b = eps w_g.   Returns (grad_x, grad_y, grad_a, grad_b)."""
+    x, y, f, g = _pts(x), _pts(y), _d(f).ravel(), _d(g).ravel()
+    n, m = len(f), len(g)
+    C = ((x[:, None, :] - y[None, :, :]) ** 2).sum(-1)
+    P = np.exp((f[:, None] + g[None, :] - C) / eps)
+    M = np.block([[np.diag(P.sum(1)), P], [P.T, np.diag(P.sum(0))]])
+    e = np.concatenate([np.ones(n), -np.ones(m)])
+    z = np.concatenate([_d(zf).ravel(), _d(zg).ravel()])
+    z = z - (z @ e) / (e @ e) * e
+    w = np.linalg.lstsq(M, z, rcond=None)[0]
+    w = w - (w @ e) / (e @ e) * e
+    wf, wg = w[:n], w[n:]
+    S = P * (wf[:, None] + wg[None, :])
+    gx = 2.0 * (S[:, :, None] * (x[:, None, :] - y[None, :, :])).sum(1)
+    gy = 2.0 * (S[:, :, None] * (y[None, :, :] - x[:, None, :])).sum(0)
+    return gx, gy, eps * wf, eps * wg

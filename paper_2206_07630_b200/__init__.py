@@ -243,6 +243,19 @@ def sinkhorn_fit_gmm(ctx: Context, x, K: int, init_idx, iters: int = 100, reg_co
     return {"weights": w, "means": mu, "covs": cov}, ll.value
 
 
+def sinkhorn_vjp(ctx: Context, x, y, eps: float, f, g, zf, zg, cg_tol: float = 1e-6, cg_max_iter: int = 2000):
+    """Implicit-differentiation VJP of the optimal potentials with cotangent (zf, zg):
+    returns ({'x', 'y', 'a', 'b'} gradients, {'cg_iters', 'cg_relres'})."""
+    n, d = x.shape
+    m = y.shape[0]
+    gx, gy, ga, gb = _empty((n, d), x), _empty((m, d), x), _empty((n,), x), _empty((m,), x)
+    it, rr = ctypes.c_int32(), ctypes.c_double()
+    ctx.check(ctx.lib.sinkhorn_vjp(ctx.h, n, m, d, _ptr(x), _ptr(y), float(eps), _ptr(f), _ptr(g), _ptr(zf),
+                                   _ptr(zg), float(cg_tol), int(cg_max_iter), _ptr(gx), _ptr(gy), _ptr(ga), _ptr(gb),
+                                   ctypes.byref(it), ctypes.byref(rr)))
+    return {"x": gx, "y": gy, "a": ga, "b": gb}, {"cg_iters": it.value, "cg_relres": rr.value}
+
+
 def sinkhorn_soft_rank_sort(ctx: Context, x, y, eps: float, f, g, z=None,
                             y_shared: bool = False, ranks: bool = True, sort: bool = True):
     """Soft ranks E_P[z | i] and soft sort E_P[x | j] of B 1D problems from their potentials

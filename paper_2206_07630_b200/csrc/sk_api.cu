@@ -81,7 +81,7 @@ enum BufId {
     B_STAGE0 = 0, B_STAGE_END = 16,   // staging of host arrays
     B_FLAG = 16, B_XPACK, B_XC, B_XNK, B_XPOT, B_YPACK, B_YC, B_YNK, B_YPOT, B_PART, B_BLKE, B_BLKB,
     B_STATUS, B_COST, B_REP, B_SORT, B_PERM, B_YSORT, B_GAUSS, B_GAUSS2, B_GMM, B_SUBW, B_SUBZ,
-    B_SUBF, B_SUBG, B_IDX, B_OUT, B_FA, B_QUEUE, B_XIMG, B_YIMG, B_XLSE, B_YLSE, B_TCMAX, B_EMST, B_EMPART, B_EMIDX, B_NBUF
+    B_SUBF, B_SUBG, B_IDX, B_OUT, B_FA, B_QUEUE, B_XIMG, B_YIMG, B_XLSE, B_YLSE, B_TCMAX, B_EMST, B_EMPART, B_EMIDX, B_VJP, B_NBUF
 };
 
 sk_status fail(sk_ctx *c, sk_status s, const char *fmt, ...) {
@@ -840,6 +840,43 @@ sk_status sinkhorn_fit_gmm(sk_ctx *ctx, int64_t n, int32_t d, const float *x, in
     CU(cudaStreamSynchronize(ctx->stream));
     if (loglik) *loglik = hll;
     if (*ctx->h_flag) return fail(ctx, SK_ENONFINITE, "a component covariance lost positive definiteness");
+    return SK_OK;
+}
+
+sk_status sinkhorn_vjp(sk_ctx *ctx, int64_t n, int64_t m, int32_t d, const float *x, const float *y, float eps,
+                       const float *f, const float *g, const float *zf, const float *zg, float cg_tol,
+                       int32_t cg_max_iter, float *grad_x, float *grad_y, float *grad_a, float *grad_b,
+                       int32_t *cg_iters, double *cg_relres) {
+    if (!ctx) return SK_EINVAL;
+    if (n < 1 || m < 1 || d < 1 || !x || !y || !f || !g || !zf || !zg || cg_max_iter < 1)
+        return fail(ctx, SK_EINVAL, "bad arguments");
+    if (d > 64) return fail(ctx, SK_EUNSUPPORTED, "d <= 64");
+    if (!(eps > 0.f) || bad_scalar(eps) || !(cg_tol > 0.f) || bad_scalar(cg_tol))
+        return fail(ctx, SK_EINVAL, "eps and cg_tol must be > 0 and finite");
+    Stager sg(ctx);
+    const float *dx, *dy, *df, *dg, *dzf, *dzg;
+    float *gx, *gy, *ga, *gb;
+    CK(sg.in_t(x, (size_t)n * d, &dx));
+    CK(sg.in_t(y, (size_t)m * d, &dy));
+    CK(sg.in_t(f, (size_t)n, &df));
+    CK(sg.in_t(g, (size_t)m, &dg));
+    CK(sg.in_t(zf, (size_t)n, &dzf));
+    CK(sg.in_t(zg, (size_t)m, &dzg));
+    CK(sg.out_t(grad_x, grad_x ? (size_t)n * d : 0, &gx));
+    CK(sg.out_t(grad_y, grad_y ? (size_t)m * d : 0, &gy));
+    CK(sg.out_t(grad_a, grad_a ? (size_t)n : 0, &ga));
+    CK(sg.out_t(grad_b, grad_b ? (size_t)m : 0, &gb));
+    CK(check_arrays(ctx, {{dx, n * d}, {dy, m * d}, {df, n}, {dg, m}, {dzf, n}, {dzg, m}}, {}, "vjp"));
+    ENSURE(work, double, B_VJP, vjp_work_doubles(n, m, d) + (size_t)std::max(n, m) * d);
+    int it = 0;
+    double rr = 0.0;
+    CU(launch_vjp(n, m, d, dx, dy, eps, df, dg, dzf, dzg, (double)cg_tol, cg_max_iter, work, gx, gy, ga, gb, &it,
+                  &rr, ctx->stream));
+    ctx->cnt.kernel_launches += 3 + 3 * it + 1 + (gx ? 2 : 0) + (gy ? 2 : 0);
+    CK(sg.flush());
+    CU(cudaStreamSynchronize(ctx->stream));
+    if (cg_iters) *cg_iters = it;
+    if (cg_relres) *cg_relres = rr;
     return SK_OK;
 }
 

@@ -31,6 +31,11 @@ size_t em_work_doubles(int K, int d);   // partials + the reduced statistics (la
 cudaError_t launch_gmm_fit(const float *x, long long n, int d, int K, const int *idx, const double *cov0,
                            int iters, double reg, double *state /* 2 x em_state_doubles */, double *part,
                            int *flags, float *w, float *mu, float *cov, double *ll_out, cudaStream_t st);
+// K17 implicit differentiation (NEXT-4)
+size_t vjp_work_doubles(long long n, long long m, int d);
+cudaError_t launch_vjp(long long n, long long m, int d, const float *x, const float *y, float eps, const float *f,
+                       const float *g, const float *zf, const float *zg, double tol, int max_iter, double *work,
+                       float *gx, float *gy, float *ga, float *gb, int *iters, double *relres, cudaStream_t st);
 // K15 soft ranks / soft sort of B 1D problems from their potentials (NEXT-2)
 size_t soft_rank_sort_smem(int n, int m);
 cudaError_t launch_soft_rank_sort(long long B, int n, int m, const float *x, const float *y, long long ys,

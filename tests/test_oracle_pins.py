@@ -534,3 +534,58 @@ def test_gmm_fit_em_monotone_and_single_component_closed_form():
     mu = x.mean(0)
     assert abs(w[0] - 1) < 1e-12 and np.abs(m[0] - mu).max() < 1e-12
     assert np.abs(S[0] - ((x - mu).T @ (x - mu) / 400 + 1e-6 * np.eye(4))).max() < 1e-12
+
+
+# --------------------------------------------------- implicit differentiation (NEXT-4)
+def _solve_tight(O, x, y, eps, a=None, b=None, f0=None):
+    r = O.sinkhorn(x, y, eps, a=a, b=b, tol=1e-13, max_iter=200000, f0=f0)
+    assert r.converged
+    return r
+
+
+def test_vjp_matches_finite_differences_of_the_solve():
+    """the implicit VJP equals central differences of the (tightly converged) oracle
+    solve for a shift-invariant loss l = <zf, f*> + <zg, g*> (sum zf = sum zg), w.r.t. x, y and
+    simplex-tangent perturbations of a."""
+    from oracle import oracle as O
+    rng = np.random.default_rng(31)
+    n, m, d = 6, 5, 2
+    x, y = rng.standard_normal((n, d)), rng.standard_normal((m, d)) + 0.3
+    a = gen.random_weights(n, rng).astype(np.float64)
+    eps = 0.4
+    zf, zg = rng.standard_normal(n), rng.standard_normal(m)
+    zg += (zf.sum() - zg.sum()) / m
+    base = _solve_tight(O, x, y, eps, a=a)
+    gx, gy, ga, _ = O.sinkhorn_vjp(x, y, base.f, base.g, eps, zf, zg)  # (the VJP itself takes a only via f, g)
+
+    def loss(xx, yy, aa):
+        r = _solve_tight(O, xx, yy, eps, a=aa, f0=base.f)
+        return zf @ r.f + zg @ r.g
+    h = 1e-5
+    for i, k in [(0, 0), (3, 1), (5, 0)]:
+        dx = np.zeros_like(x); dx[i, k] = h
+        fd = (loss(x + dx, y, a) - loss(x - dx, y, a)) / (2 * h)
+        assert abs(fd - gx[i, k]) < 1e-6 * max(1.0, abs(fd)), (i, k, fd, gx[i, k])
+    for j, k in [(1, 0), (4, 1)]:
+        dy = np.zeros_like(y); dy[j, k] = h
+        fd = (loss(x, y + dy, a) - loss(x, y - dy, a)) / (2 * h)
+        assert abs(fd - gy[j, k]) < 1e-6 * max(1.0, abs(fd)), (j, k, fd, gy[j, k])
+    da = np.zeros(n); da[1], da[4] = h, -h    # tangent to the simplex
+    fd = (loss(x, y, a + da) - loss(x, y, a - da)) / (2 * h)
+    assert abs(fd - (ga[1] - ga[4])) < 1e-6 * max(1.0, abs(fd))
+
+
+def test_vjp_envelope_closed_form():
+    """z = (a, b): l = <a, f*> + <b, g*> = E* + eps, and by the envelope theorem
+    dE*/dx_i = sum_j P_ij dC_ij/dx_i = 2 sum_j P_ij (x_i - y_j) (closed form, no linear solve)."""
+    from oracle import oracle as O
+    p = gen.c1(n=48, seed=5, eps_factor=0.05)
+    r = _solve_tight(O, p.x, p.y, p.eps)
+    n = len(r.f)
+    gx, gy, _, _ = O.sinkhorn_vjp(p.x, p.y, r.f, r.g, p.eps, np.full(n, 1 / n), np.full(len(r.g), 1 / len(r.g)))
+    x, y = p.x.astype(np.float64), p.y.astype(np.float64)
+    C = ((x[:, None] - y[None]) ** 2).sum(-1)
+    P = np.exp((r.f[:, None] + r.g[None] - C) / p.eps)
+    env_x = 2 * (P.sum(1)[:, None] * x - P @ y)
+    env_y = 2 * (P.sum(0)[:, None] * y - P.T @ x)
+    assert np.abs(gx - env_x).max() < 1e-8 and np.abs(gy - env_y).max() < 1e-8
