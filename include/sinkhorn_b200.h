@@ -115,6 +115,14 @@ int32_t sk_version(void);
  * omega must lie in (0, 2) (SK_EINVAL otherwise); the sharded entries return
  * SK_EUNSUPPORTED for omega != 1. */
 sk_status sk_set_relaxation(sk_ctx *ctx, float omega);
+/* eps-decay ("gradually reducing the regularization term from 5 eps to eps by a factor
+ * of 0.8"; R-25) for the following solves on this context: sweep l = 1, 2, ... uses
+ * eps_l = max(eps, eps * init * rate^(l-1)) for both of its updates; the T sweeps with
+ * eps_l > eps are not checked (the stop rule runs on sweeps l > T with (l - T) % check_every
+ * == 0) and count in rep.iterations.  init <= 1 turns it off (the default); otherwise rate
+ * must lie in (0, 1) (SK_EINVAL).  On the multi-kernel paths it needs omega = 1
+ * (SK_EUNSUPPORTED otherwise) and max_iter > T; the sharded entries return SK_EUNSUPPORTED. */
+sk_status sk_set_eps_decay(sk_ctx *ctx, float init, float rate);
 /* Enable (1) / disable (0) CUDA-event timing of the dominant kernels into sk_counters. */
 sk_status sk_set_timing(sk_ctx *ctx, int32_t enable);
 sk_status sk_get_counters(const sk_ctx *ctx, sk_counters *out /* host */);

@@ -56,6 +56,8 @@ def _L():
         lib.ora_sinkhorn_points.argtypes = [I64, I64, I, P, P, P, P, D, D, I, I, P, P, P, P, P, P, P]
         lib.ora_sinkhorn_points_omega.restype = I
         lib.ora_sinkhorn_points_omega.argtypes = [I64, I64, I, P, P, P, P, D, D, D, I, I, P, P, P, P, P, P, P]
+        lib.ora_sinkhorn_points_decay.restype = I
+        lib.ora_sinkhorn_points_decay.argtypes = [I64, I64, I, P, P, P, P, D, D, D, D, D, I, I, P, P, P, P, P, P, P]
         lib.ora_sinkhorn_matrix.restype = I
         lib.ora_sinkhorn_matrix.argtypes = [I64, I64, P, P, P, D, D, I, I, P, P, P, P, P, P, P]
         lib.ora_f_update_points.argtypes = [I64, I64, I, P, P, P, P, D, P, P, I64]
@@ -125,9 +127,10 @@ class Result(dict):
 
 
 def sinkhorn(x, y, eps, a=None, b=None, tol=1e-3, max_iter=10000, check_every=1,
-             f0=None, trace=False, omega=1.0) -> Result:
+             f0=None, trace=False, omega=1.0, eps_decay=None) -> Result:
     """Alg. 1, g-then-f, explicit stopping rule; tol<=0 = exactly max_iter sweeps.
-    omega: Alg. 1's relaxation (R-1 reading): v <- (1 - omega) v + omega v_sinkhorn."""
+    omega: Alg. 1's relaxation (R-1 reading): v <- (1 - omega) v + omega v_sinkhorn.
+    eps_decay: (init, rate) for sweep l's eps_l = max(eps, eps init rate^(l-1)) (R-25)."""
     x, y = _pts(x), _pts(y)
     n, m, d = x.shape[0], y.shape[0], x.shape[1]
     a, b = _weights(a, n), _weights(b, m)
@@ -135,7 +138,8 @@ def sinkhorn(x, y, eps, a=None, b=None, tol=1e-3, max_iter=10000, check_every=1,
     it, err, E = ctypes.c_int(), ctypes.c_double(), ctypes.c_double()
     f0a = None if f0 is None else _d(f0)
     tr = np.empty(max_iter) if trace else None
-    conv = _L().ora_sinkhorn_points_omega(n, m, d, _p(x), _p(y), _p(a), _p(b), float(eps), float(omega),
+    di, dr = (0.0, 1.0) if eps_decay is None else (float(eps_decay[0]), float(eps_decay[1]))
+    conv = _L().ora_sinkhorn_points_decay(n, m, d, _p(x), _p(y), _p(a), _p(b), float(eps), float(omega), di, dr,
                                           float(tol), int(max_iter), int(check_every), _p(f0a), _p(f),
                                           _p(g), ctypes.byref(it), ctypes.byref(err), ctypes.byref(E), _p(tr))
     r = Result(f=f, g=g, iterations=it.value, converged=bool(conv), err=err.value, E=E.value)

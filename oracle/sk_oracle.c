@@ -182,6 +182,11 @@ static double dual_objective(const ora_prob *p, const double *a, const double *b
  * (g_sk, f_sk: the omega = 1 updates above; omega > 1 is the over-relaxed "momentum" of
  * P:73).  omega == 1 is the plain algorithm. */
 static double omega_g = 1.0;   /* the current call's omega (set by the public entry) */
+/* eps-decay ("gradually reducing the regularization term from 5 eps to eps by a factor of
+ * 0.8"; reading R-25): sweep l = 1, 2, ... uses eps_l = max(eps, eps * decay_init * decay_rate^(l-1))
+ * for both of its updates; the T sweeps with eps_l > eps are not checked, the stop rule runs on
+ * the sweeps l > T with (l - T) % check_every == 0.  decay_init = 0: off. */
+static double decay_init_g = 0.0, decay_rate_g = 1.0;
 
 static void relax(int64_t k, double *v, const double *vsk, double omega) {
     if (omega == 1.0) { for (int64_t i = 0; i < k; ++i) v[i] = vsk[i]; return; }
@@ -202,16 +207,21 @@ static int sinkhorn(const ora_prob *p, const double *a, const double *b, double 
     const double omega = omega_g;
     double *gs = (double *)malloc(sizeof(double) * (size_t)p->m);
     double *fs = (double *)malloc(sizeof(double) * (size_t)p->n);
-    int l = 0, converged = 0;
+    int l = 0, converged = 0, T = 0;
     double e = INFINITY;
     while (l < max_iter) {
         ++l;
-        g_update(p, b, f, eps, gs, NULL, 0);
+        double el = eps;
+        if (decay_init_g > 0.0) {
+            const double v = eps * decay_init_g * pow(decay_rate_g, (double)(l - 1));
+            if (v > eps) { el = v; T = l; }
+        }
+        g_update(p, b, f, el, gs, NULL, 0);
         relax(p->m, g, gs, omega);
-        f_update(p, a, g, eps, fs, NULL, 0);
+        f_update(p, a, g, el, fs, NULL, 0);
         relax(p->n, f, fs, omega);
         if (trace) trace[l - 1] = dual_objective(p, a, b, f, g, eps);
-        if (tol > 0.0 && l % check_every == 0) {
+        if (tol > 0.0 && l > T && (l - T) % check_every == 0) {
             e = marginal_error(p, a, b, f, g, eps);
             if (e < tol) { converged = 1; break; }
         }
@@ -243,6 +253,22 @@ int ora_sinkhorn_points_omega(int64_t n, int64_t m, int d, const double *x, cons
     omega_g = omega;
     int r = sinkhorn(&p, a, b, eps, tol, max_iter, check_every, f0, f, g, iters, err, E, trace);
     omega_g = 1.0;
+    return r;
+}
+
+/* ... with eps-decay (R-25). */
+int ora_sinkhorn_points_decay(int64_t n, int64_t m, int d, const double *x, const double *y,
+                              const double *a, const double *b, double eps, double omega, double decay_init,
+                              double decay_rate, double tol, int max_iter, int check_every, const double *f0,
+                              double *f, double *g, int *iters, double *err, double *E, double *trace) {
+    ora_prob p = {n, m, d, x, y, NULL};
+    omega_g = omega;
+    decay_init_g = decay_init;
+    decay_rate_g = decay_rate;
+    int r = sinkhorn(&p, a, b, eps, tol, max_iter, check_every, f0, f, g, iters, err, E, trace);
+    omega_g = 1.0;
+    decay_init_g = 0.0;
+    decay_rate_g = 1.0;
     return r;
 }
 

@@ -74,6 +74,7 @@ struct sk_ctx {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     std::vector<cudaEvent_t> tev;   // per-launch timing events of the dominant kernel (pool)
     float omega = 1.f;              // Alg. 1's relaxation for the following solves
+    float decay_init = 0.f, decay_rate = 1.f;   // eps-decay for the following solves (R-25)
 };
 
 namespace {
@@ -306,6 +307,8 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
     const bool sharded = P.world > 1;
     if (P.omega != 1.f && (sharded || P.partitioned))
         return fail(ctx, SK_EUNSUPPORTED, "relaxation (omega != 1) is supported by the unsharded solver only");
+    if (ctx->decay_init > 0.f && (sharded || P.partitioned))
+        return fail(ctx, SK_EUNSUPPORTED, "eps-decay is supported by the unsharded solver only");
     const long long m = P.m, n_glob = P.n_total;
     const int ns = (int)slices.size();
     long long n_max = 0, n_sum = 0;
@@ -693,6 +696,16 @@ sk_status sk_create(sk_ctx **out, int device, void *stream) {
 sk_status sk_set_stream(sk_ctx *ctx, void *stream) {
     if (!ctx) return SK_EINVAL;
     ctx->stream = (cudaStream_t)stream;
+    return SK_OK;
+}
+
+sk_status sk_set_eps_decay(sk_ctx *ctx, float init, float rate) {
+    if (!ctx) return SK_EINVAL;
+    if (init <= 1.f) { ctx->decay_init = 0.f; ctx->decay_rate = 1.f; return SK_OK; }   // off
+    if (!(rate > 0.f && rate < 1.f) || bad_scalar(init))
+        return fail(ctx, SK_EINVAL, "eps-decay needs init > 1 (finite) and rate in (0, 1)");
+    ctx->decay_init = init;
+    ctx->decay_rate = rate;
     return SK_OK;
 }
 
@@ -1146,6 +1159,7 @@ sk_status solve_impl(sk_ctx *ctx, int64_t B, int64_t n, int64_t m, int32_t d, co
         L.max_iter = max_iter; L.check_every = check_every;
         L.iters = iters; L.conv = conv; L.nonfinite = nonf; L.err = err; L.E = E;
         L.omega = ctx->omega;
+        L.decay_init = ctx->decay_init; L.decay_rate = ctx->decay_rate;
         CU(cudaEventRecord(ctx->ev0, st));
         CU(launch_batched(L, st));
         CU(cudaEventRecord(ctx->ev1, st));
@@ -1175,6 +1189,15 @@ sk_status solve_impl(sk_ctx *ctx, int64_t B, int64_t n, int64_t m, int32_t d, co
         if (any_nf) return fail(ctx, SK_ENONFINITE, "potentials became non-finite");
         return SK_OK;
     }
+    // eps-decay (R-25) on the multi-kernel path: with omega = 1 a sweep is a map f -> f (its
+    // g-update reads only f), so the T decay sweeps run as one-sweep solves at eps_l, each
+    // starting from the previous f; the solve at the target eps then starts from f^T
+    int T = 0;
+    if (ctx->decay_init > 0.f) {
+        if (ctx->omega != 1.f)
+            return fail(ctx, SK_EUNSUPPORTED, "eps-decay with omega != 1 runs on the on-chip solver only");
+        while (T < max_iter && (double)eps * ctx->decay_init * std::pow((double)ctx->decay_rate, T) > (double)eps) ++T;
+    }
     for (long long p = 0; p < B; ++p) {
         Problem P;
         P.n_total = n; P.m = m; P.d = d;
@@ -1182,9 +1205,24 @@ sk_status solve_impl(sk_ctx *ctx, int64_t B, int64_t n, int64_t m, int32_t d, co
         P.eps = eps; P.tol = tol; P.max_iter = max_iter; P.check_every = check_every; P.mode = mode;
         P.g = g + p * m;
         P.world = 1; P.nccl = false; P.omega = ctx->omega;
-        std::vector<Slice> sl{Slice{0, n, x + p * xs, a ? a + p * as : nullptr,
-                                    f_init ? f_init + p * n : nullptr, f + p * n, 0}};
+        const float *fi = f_init ? f_init + p * n : nullptr;
+        double extra_ms = 0.0;
+        for (int t = 0; t < T; ++t) {
+            Problem Pt = P;
+            Pt.eps = (float)((double)eps * ctx->decay_init * std::pow((double)ctx->decay_rate, t));
+            Pt.max_iter = 1;   // (its stop check measures err_1 at eps_l: one column pass more)
+            std::vector<Slice> st{Slice{0, n, x + p * xs, a ? a + p * as : nullptr, fi, f + p * n, 0}};
+            sk_report r1{};
+            CK(solve_core(ctx, Pt, st, &r1));
+            extra_ms += r1.solve_ms;
+            fi = f + p * n;
+        }
+        P.max_iter = max_iter - T;
+        std::vector<Slice> sl{Slice{0, n, x + p * xs, a ? a + p * as : nullptr, fi, f + p * n, 0}};
+        if (P.max_iter < 1) return fail(ctx, SK_EINVAL, "max_iter must exceed the %d eps-decay sweeps", T);
         CK(solve_core(ctx, P, sl, &rep[p]));
+        rep[p].iterations += T;
+        rep[p].solve_ms += extra_ms;
     }
     return SK_OK;
 }

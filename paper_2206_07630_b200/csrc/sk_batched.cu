@@ -36,6 +36,7 @@ struct BatchArgs {
     float *err;
     double *E;
     float omega;                    // Alg. 1's relaxation (1 = plain Sinkhorn)
+    float decay_init, decay_rate;   // eps-decay (decay_init <= 0: off)
 };
 
 __host__ __device__ inline int round_up(int v, int a) { return (v + a - 1) / a * a; }
@@ -106,10 +107,11 @@ template <int D, int R, int NT, int EMU>
 __device__ __forceinline__ void solve_one(const BatchArgs &A, int prob, float *sm) {
     const int n = A.n, m = A.m;
     const int Np = round_up(n, kChunk), Mp = round_up(m, kChunk);
-    const float eps = A.eps;
-    const float kap = kLog2e / eps;     // log2(e)/eps
-    const float tk = 2.f * kap;         // scale of the cross term
-    const float epsln2 = eps * kLn2;
+    const float eps_t = A.eps;          // the target eps
+    float eps = eps_t;                  // this sweep's eps (eps-decay, R-25)
+    float kap = kLog2e / eps;           // log2(e)/eps
+    float tk = 2.f * kap;               // scale of the cross term
+    float epsln2 = eps * kLn2;
 
     float *xq = sm;                     // [D][Np]
     float *wx = xq + D * Np;            // [Np]   (f_i - |x_i|^2) kappa
@@ -182,13 +184,49 @@ __device__ __forceinline__ void solve_one(const BatchArgs &A, int prob, float *s
     const float om = A.omega;
     const bool relaxed = om != 1.f;
     double row_err = 0.0, mass_dev = 0.0;   // relaxed: row term of err_l and sum P - sum a
+    // eps-decay (R-25): sweep l + 1 uses max(eps, eps init rate^l); the T decay sweeps
+    // are not checked; the constants that carry eps are refreshed when it changes
+    auto eps_of = [&](int s) {
+        if (A.decay_init <= 0.f) return eps_t;
+        const float v = eps_t * A.decay_init * powf(A.decay_rate, (float)s);
+        return v > eps_t ? v : eps_t;
+    };
+    int T = 0;
+    while (T < A.max_iter && eps_of(T) > eps_t) ++T;
+    auto refresh = [&](float e) {
+        eps = e; kap = kLog2e / e; tk = 2.f * kap; epsln2 = e * kLn2;
+        const float *fc = fb + cur * n;
+        for (int i = threadIdx.x; i < n; i += NT) {
+            float s2 = 0.f;
+#pragma unroll
+            for (int k = 0; k < D; ++k) s2 = fmaf(xq[k * Np + i], xq[k * Np + i], s2);
+            cx[i] = fmaf(e, a ? logf(a[i]) : loga_u, s2);
+            nxk[i] = s2 * kap;
+            wx[i] = fmaf(fc[i], kap, -nxk[i]);
+        }
+        for (int j = threadIdx.x; j < m; j += NT) {
+            float s2 = 0.f;
+#pragma unroll
+            for (int k = 0; k < D; ++k) s2 = fmaf(yq[k * Mp + j], yq[k * Mp + j], s2);
+            cy[j] = fmaf(e, b ? logf(b[j]) : logb_u, s2);
+            nyk[j] = s2 * kap;
+        }
+        __syncthreads();
+    };
+    bool fresh = true;   // the LSE seeds (previous sweep's LSE) belong to this sweep's eps
     for (;;) {
+        {
+            const float el = eps_of(l);
+            fresh = el == eps;
+            if (!fresh) refresh(el);
+        }
+        const bool seeded = l >= 1 && fresh;
         // ---- column pass: g^{l+1} (P = y, Q = x)
-        const bool check = l >= 1 && (l % A.check_every == 0 || l == A.max_iter);
+        const bool check = l > T && ((l - T) % A.check_every == 0 || l == A.max_iter);
         double e_loc = 0.0;
         int bad = 0;
         float *gold = gb + cur * m, *gnew = gb + (cur ^ 1) * m;
-        onchip_pass<D, R, NT, EMU>(yq, Mp, m, xq, wx, Np, tk, mys, l >= 1, [&](int j, float Mv, float Sv) {
+        onchip_pass<D, R, NT, EMU>(yq, Mp, m, xq, wx, Np, tk, mys, seeded, [&](int j, float Mv, float Sv) {
             const float gsk = cy[j] - epsln2 * (Mv + log2f(Sv));
             // Alg. 1 with relaxation (R-1): g <- (1 - omega) g + omega g_sk
             const float gn = relaxed ? fmaf(om, gsk - gold[j], gold[j]) : gsk;
@@ -206,14 +244,14 @@ __device__ __forceinline__ void solve_one(const BatchArgs &A, int prob, float *s
         if (check) {
             err = (float)(e_tot + row_err);   // (row_err = 0 unless relaxed)
             if (err < A.tol) { conv = 1; break; }
-            if (l == A.max_iter) break;
         }
+        if (l >= A.max_iter) break;   // (also when max_iter <= T: no sweep is checked)
         // ---- row pass: f^{l+1} (P = x, Q = y); wy is visible after the block reductions' barriers
         float *fnew = fb + (cur ^ 1) * n;
         const float *fold = fb + cur * n;
         bad = 0;
         double r_loc = 0.0, m_loc = 0.0;
-        onchip_pass<D, R, NT, EMU>(xq, Np, n, yq, wy, Mp, tk, mxs, l >= 1, [&](int i, float Mv, float Sv) {
+        onchip_pass<D, R, NT, EMU>(xq, Np, n, yq, wy, Mp, tk, mxs, seeded, [&](int i, float Mv, float Sv) {
             const float fsk = cx[i] - epsln2 * (Mv + log2f(Sv));
             const float fn = relaxed ? fmaf(om, fsk - fold[i], fold[i]) : fsk;
             fnew[i] = fn;
@@ -340,6 +378,7 @@ cudaError_t launch_batched(const BatchLaunch &L, cudaStream_t st) {
     A.max_iter = L.max_iter; A.check_every = L.check_every;
     A.iters = L.iters; A.conv = L.conv; A.nonfinite = L.nonfinite; A.err = L.err; A.E = L.E;
     A.omega = L.omega;
+    A.decay_init = L.decay_init; A.decay_rate = L.decay_rate;
     switch (L.d) {
         case 1: return launch_batched_d<1>(A, L.B, st);
         case 2: return launch_batched_d<2>(A, L.B, st);

@@ -22,6 +22,7 @@ struct BatchLaunch {
     float *err;
     double *E;
     float omega = 1.f;   // Alg. 1's relaxation
+    float decay_init = 0.f, decay_rate = 1.f;   // eps-decay (R-25; decay_init <= 0: off)
 };
 bool batched_supported(int d, int n, int m);
 // K16 GMM fitting by EM (NEXT-3); state and partial workspace sizes in doubles

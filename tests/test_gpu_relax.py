@@ -23,15 +23,15 @@ def _cuda(a):
     return torch.from_numpy(np.ascontiguousarray(a)).cuda()
 
 
-def check_relaxed(O, sk, ctx, x, y, eps, omega, f0=None, a=None, mode="auto", tol=1e-3, what=""):
+def check_relaxed(O, sk, ctx, x, y, eps, omega, f0=None, a=None, mode="auto", tol=1e-3, what="", decay=None):
     f, g, rep = sk.sinkhorn_solve(ctx, _cuda(x), _cuda(y), eps, tol=tol, mode=mode, omega=omega,
-                                  a=None if a is None else _cuda(a),
+                                  a=None if a is None else _cuda(a), eps_decay=decay,
                                   f_init=None if f0 is None else _cuda(np.asarray(f0, np.float32)))
     f, g = f.cpu().numpy(), g.cpu().numpy()
     L = rep["iterations"]
-    ref = O.sinkhorn(x, y, eps, a=a, tol=tol, omega=omega, f0=f0)
+    ref = O.sinkhorn(x, y, eps, a=a, tol=tol, omega=omega, f0=f0, eps_decay=decay)
     assert abs(L - ref.iterations) <= count_tol(ref.iterations), (what, L, ref.iterations)
-    lock = O.sinkhorn(x, y, eps, a=a, tol=0, max_iter=L, omega=omega, f0=f0)
+    lock = O.sinkhorn(x, y, eps, a=a, tol=0, max_iter=L, omega=omega, f0=f0, eps_decay=decay)
     assert_pair_close(f, g, lock.f, lock.g, eps, what=what)
     assert_obj_close(rep["dual_objective"], lock.E, eps, what=what)
     assert rep["converged"] and rep["marginal_error"] < tol
@@ -99,3 +99,48 @@ def test_relaxation_argument_errors(ctx):
             sk.sinkhorn_solve_sharded_emulated(ctx, 2, x, y, p.eps, mode="online")
         finally:
             ctx.lib.sk_set_relaxation(ctx.h, ctypes.c_float(1.0))
+
+
+# ------------------------------------------------------------- eps-decay (NEXT-1, R-25)
+@pytest.mark.parametrize("omega", [1.0, 1.5])
+def test_eps_decay_onchip_c1(O, ctx, omega):
+    import paper_2206_07630_b200 as sk
+    p = gen.c1()
+    check_relaxed(O, sk, ctx, p.x, p.y, p.eps, omega, decay=(5.0, 0.8), what=f"c1 decay omega={omega}")
+
+
+@pytest.mark.parametrize("mode,n,m,d", [("online", 3000, 2600, 3), ("online", 1500, 1300, 40), ("stored", 2000, 1024, 16)])
+def test_eps_decay_multikernel(O, ctx, mode, n, m, d):
+    import paper_2206_07630_b200 as sk
+    rng = np.random.default_rng(n + 2 * d)
+    x = rng.random((n, d)).astype(np.float32)
+    y = (rng.random((m, d)) * 0.9 + 0.05).astype(np.float32)
+    eps = float(np.float32(0.03 * gen.mean_sq_cost(x, y)))
+    check_relaxed(O, sk, ctx, x, y, eps, 1.0, mode=mode, decay=(5.0, 0.8), what=f"{mode} decay {n}x{m}x{d}")
+
+
+def test_eps_decay_batched_and_errors(O, ctx):
+    import ctypes
+    import paper_2206_07630_b200 as sk
+    c2 = gen.c2(B=4, n=1024)   # (the C2 shape: ~30 sweeps; long trajectories of this 1D problem at
+    xb, yb = _cuda(c2.x), _cuda(c2.y)   # eps = 1e-3 drift past 1e-4 in fp32 with or without decay)
+    pot = sk.sinkhorn_init_sort1d(ctx, xb.view(4, 1024), yb.view(-1))
+    f, g, reps = sk.sinkhorn_solve(ctx, xb, yb, c2.eps, y_shared=True, f_init=pot, eps_decay=(5.0, 0.8))
+    k = 2
+    f0 = pot[k].cpu().numpy()
+    ref = O.sinkhorn(c2.x[k], c2.y, c2.eps, f0=f0, eps_decay=(5.0, 0.8))
+    assert abs(reps[k]["iterations"] - ref.iterations) <= count_tol(ref.iterations)
+    lock = O.sinkhorn(c2.x[k], c2.y, c2.eps, tol=0, max_iter=reps[k]["iterations"], f0=f0, eps_decay=(5.0, 0.8))
+    assert_pair_close(f[k].cpu().numpy(), g[k].cpu().numpy(), lock.f, lock.g, c2.eps)
+    assert ctx.lib.sk_set_eps_decay(ctx.h, ctypes.c_float(5.0), ctypes.c_float(1.5)) == 1   # SK_EINVAL
+    x = _cuda(np.random.default_rng(1).random((3000, 3)).astype(np.float32))
+    with pytest.raises(sk.SinkhornError):   # multi-kernel: decay with omega != 1 is unsupported
+        sk.sinkhorn_solve(ctx, x, x, 0.01, mode="online", omega=1.3, eps_decay=(5.0, 0.8))
+
+
+def test_eps_decay_max_iter_inside_the_decay(ctx):
+    """max_iter <= T: the on-chip solver stops at max_iter (no sweep is checked) instead of looping."""
+    import paper_2206_07630_b200 as sk
+    p = gen.c1()
+    f, g, rep = sk.sinkhorn_solve(ctx, _cuda(p.x), _cuda(p.y), p.eps, max_iter=3, eps_decay=(5.0, 0.8))
+    assert rep["iterations"] == 3 and not rep["converged"]

@@ -589,3 +589,34 @@ def test_vjp_envelope_closed_form():
     env_x = 2 * (P.sum(1)[:, None] * x - P @ y)
     env_y = 2 * (P.sum(0)[:, None] * y - P.T @ x)
     assert np.abs(gx - env_x).max() < 1e-8 and np.abs(gy - env_y).max() < 1e-8
+
+
+# ------------------------------------------------------------------ eps-decay (NEXT-1)
+def test_eps_decay_is_a_chain_of_plain_sweeps():
+    """R-25: with omega = 1 a sweep maps f to f (its g-update reads only f), so L sweeps with
+    eps-decay equal T single plain sweeps at eps_l = eps 5 0.8^(l-1) chained through f0,
+    followed by L - T plain sweeps at eps (the plain solver is pinned above)."""
+    from oracle import oracle as O
+    p = gen.c1(n=50, seed=6)
+    L = 14
+    r = O.sinkhorn(p.x, p.y, p.eps, tol=0, max_iter=L, eps_decay=(5.0, 0.8))
+    f = None
+    T = 0
+    while p.eps * 5.0 * 0.8 ** T > p.eps:
+        f = O.sinkhorn(p.x, p.y, p.eps * 5.0 * 0.8 ** T, tol=0, max_iter=1, f0=f).f
+        T += 1
+    assert T == 8
+    q = O.sinkhorn(p.x, p.y, p.eps, tol=0, max_iter=L - T, f0=f)
+    assert np.abs(r.f - q.f).max() < 1e-12 and np.abs(r.g - q.g).max() < 1e-12 and abs(r.E - q.E) < 1e-12
+
+
+def test_eps_decay_same_optimum_and_off_switch():
+    from oracle import oracle as O
+    p = gen.c1(n=40, seed=7, eps_factor=0.1)
+    ref = O.sinkhorn(p.x, p.y, p.eps, tol=1e-11, max_iter=100000)
+    r = O.sinkhorn(p.x, p.y, p.eps, tol=1e-11, max_iter=100000, eps_decay=(5.0, 0.8))
+    assert r.converged
+    assert np.abs((r.f - r.f.mean()) - (ref.f - ref.f.mean())).max() < 1e-8
+    off = O.sinkhorn(p.x, p.y, p.eps, tol=1e-3, eps_decay=(1.0, 0.8))   # init <= 1: no decay sweep
+    plain = O.sinkhorn(p.x, p.y, p.eps, tol=1e-3)
+    assert off.iterations == plain.iterations and np.array_equal(off.f, plain.f)
