@@ -58,10 +58,11 @@ constexpr float kSeedMargin = 4.f;   // log2 units added to the previous sweep's
 // rescale); if the sum leaves [2^-100, 2^100] the point is recomputed exactly.
 // out(p, M, S) is called for every valid p by the thread that owns it.
 template <int D, int R, int NT, int EMU, typename Out>
-__device__ __forceinline__ void onchip_pass(const float *__restrict__ pc, int pstride, int P,
+__device__ __forceinline__ void onchip_pass(const float *__restrict__ pc, int pstride, int p0, int P,
                                             const float *__restrict__ qc, const float *__restrict__ qw,
                                             int Qp, float tk, float *pm, bool seeded, Out out) {
-    for (int pb = 0; pb < P; pb += R * NT) {
+    // outputs p in [p0, P)
+    for (int pb = p0; pb < P; pb += R * NT) {
         float2 pd[R][D];
         float M[R];
         float2 S[R];
@@ -102,9 +103,33 @@ __device__ __forceinline__ void onchip_pass(const float *__restrict__ pc, int ps
     }
 }
 
-// Solve problem `prob` with the whole CTA.
-template <int D, int R, int NT, int EMU>
-__device__ __forceinline__ void solve_one(const BatchArgs &A, int prob, float *sm) {
+// ---------------------------------------------------------- CTA-pair (cluster) helpers
+__device__ __forceinline__ uint32_t cl_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t cl_map(const void *p, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void cl_st(uint32_t addr, float v) {
+    asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
+}
+__device__ __forceinline__ void cl_st(uint32_t addr, double v) {
+    asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(addr), "d"(v) : "memory");
+}
+__device__ __forceinline__ void cl_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// Solve problem `prob` with the whole CTA (CL = 1) or a CTA pair (CL = 2: each CTA computes the
+// outputs of one half of every pass and stores them into both CTAs' shared memory (DSMEM);
+// reductions combine the two halves' block partials in a fixed order, so both CTAs take the
+// same decisions).  The per-point arithmetic is the same for CL = 1 and 2 (same potentials).
+template <int D, int R, int NT, int EMU, int CL>
+__device__ __forceinline__ void solve_one(const BatchArgs &A, int prob, float *sm, uint32_t rank) {
     const int n = A.n, m = A.m;
     const int Np = round_up(n, kChunk), Mp = round_up(m, kChunk);
     const float eps_t = A.eps;          // the target eps
@@ -127,6 +152,28 @@ __device__ __forceinline__ void solve_one(const BatchArgs &A, int prob, float *s
     float *mys = mxs + n;               // [m]    (y side, column pass)
     double *red = reinterpret_cast<double *>(mys + m + ((n + m) & 1));  // scratch
     int *redi = reinterpret_cast<int *>(red + 32);
+    double *xr = red + 48;              // [2 ranks][8] exchanged block partials (CL = 2)
+    // this CTA's output ranges (CL = 2: halves, aligned to R * NT rounds)
+    const int hn = CL > 1 ? (n + 1) / 2 : n, hm = CL > 1 ? (m + 1) / 2 : m;
+    const int i0 = CL > 1 ? (int)rank * hn : 0, i1 = CL > 1 ? min(n, i0 + hn) : n;
+    const int j0 = CL > 1 ? (int)rank * hm : 0, j1 = CL > 1 ? min(m, j0 + hm) : m;
+    const uint32_t peer_base = CL > 1 ? cl_map(sm, rank ^ 1u) : 0u;
+    auto rput = [&](float *loc, float v) {   // the same slot in the peer CTA
+        if constexpr (CL > 1) cl_st(peer_base + (smem_u32(loc) - smem_u32(sm)), v);
+    };
+    // sum of this CTA's block partial v[k] with the peer's (fixed order: rank 0 + rank 1)
+    auto xsum = [&](double (&v)[4], int cnt) {
+        if constexpr (CL > 1) {
+            if (threadIdx.x == 0)
+                for (int k = 0; k < cnt; ++k) {
+                    xr[rank * 8 + k] = v[k];
+                    cl_st(peer_base + (smem_u32(&xr[rank * 8 + k]) - smem_u32(sm)), v[k]);
+                }
+            cl_sync();
+            for (int k = 0; k < cnt; ++k) v[k] = xr[k] + xr[8 + k];
+            cl_sync();   // (xr reusable)
+        }
+    };
 
     const float *x = A.x + prob * A.xs;
     const float *y = A.y + prob * A.ys;
@@ -226,36 +273,42 @@ __device__ __forceinline__ void solve_one(const BatchArgs &A, int prob, float *s
         double e_loc = 0.0;
         int bad = 0;
         float *gold = gb + cur * m, *gnew = gb + (cur ^ 1) * m;
-        onchip_pass<D, R, NT, EMU>(yq, Mp, m, xq, wx, Np, tk, mys, seeded, [&](int j, float Mv, float Sv) {
+        onchip_pass<D, R, NT, EMU>(yq, Mp, j0, j1, xq, wx, Np, tk, mys, seeded, [&](int j, float Mv, float Sv) {
             const float gsk = cy[j] - epsln2 * (Mv + log2f(Sv));
             // Alg. 1 with relaxation (R-1): g <- (1 - omega) g + omega g_sk
             const float gn = relaxed ? fmaf(om, gsk - gold[j], gold[j]) : gsk;
+            const float wv = fmaf(gn, kap, -nyk[j]);
             gnew[j] = gn;
-            wy[j] = fmaf(gn, kap, -nyk[j]);
+            wy[j] = wv;
+            rput(&gnew[j], gn);
+            rput(&wy[j], wv);
             bad |= !isfinite(gn);
             if (check) {
                 const double bj = b ? (double)b[j] : 1.0 / m;
                 e_loc += bj * fabs((double)expm1f((gold[j] - gsk) / eps));
             }
         });
-        const double e_tot = block_sum_d<NT>(e_loc, red);
-        const int any_bad = block_or<NT>(bad, redi);
-        if (any_bad) { nonfin = 1; break; }
+        double cv[4] = {block_sum_d<NT>(e_loc, red), (double)block_or<NT>(bad, redi), 0.0, 0.0};
+        xsum(cv, 2);   // (CL = 2: also publishes the peer's half of g and w)
+        if (cv[1] != 0.0) { nonfin = 1; break; }
         if (check) {
-            err = (float)(e_tot + row_err);   // (row_err = 0 unless relaxed)
+            err = (float)(cv[0] + row_err);   // (row_err = 0 unless relaxed)
             if (err < A.tol) { conv = 1; break; }
         }
         if (l >= A.max_iter) break;   // (also when max_iter <= T: no sweep is checked)
-        // ---- row pass: f^{l+1} (P = x, Q = y); wy is visible after the block reductions' barriers
+        // ---- row pass: f^{l+1} (P = x, Q = y); wy is visible after the reductions' barriers
         float *fnew = fb + (cur ^ 1) * n;
         const float *fold = fb + cur * n;
         bad = 0;
         double r_loc = 0.0, m_loc = 0.0;
-        onchip_pass<D, R, NT, EMU>(xq, Np, n, yq, wy, Mp, tk, mxs, seeded, [&](int i, float Mv, float Sv) {
+        onchip_pass<D, R, NT, EMU>(xq, Np, i0, i1, yq, wy, Mp, tk, mxs, seeded, [&](int i, float Mv, float Sv) {
             const float fsk = cx[i] - epsln2 * (Mv + log2f(Sv));
             const float fn = relaxed ? fmaf(om, fsk - fold[i], fold[i]) : fsk;
+            const float wv = fmaf(fn, kap, -nxk[i]);
             fnew[i] = fn;
-            wx[i] = fmaf(fn, kap, -nxk[i]);
+            wx[i] = wv;
+            rput(&fnew[i], fn);
+            rput(&wx[i], wv);
             bad |= !isfinite(fn);
             if (relaxed) {   // sum_j P_ij = a_i exp((f_i - fsk_i)/eps)
                 const double ai = a ? (double)a[i] : 1.0 / n;
@@ -264,11 +317,14 @@ __device__ __forceinline__ void solve_one(const BatchArgs &A, int prob, float *s
                 m_loc += ai * dv;
             }
         });
-        if (block_or<NT>(bad, redi)) { nonfin = 1; break; }
+        double rv[4] = {(double)block_or<NT>(bad, redi), 0.0, 0.0, 0.0};
         if (relaxed) {
-            row_err = block_sum_d<NT>(r_loc, red);
-            mass_dev = block_sum_d<NT>(m_loc, red);
+            rv[1] = block_sum_d<NT>(r_loc, red);
+            rv[2] = block_sum_d<NT>(m_loc, red);
         }
+        xsum(rv, 3);
+        if (rv[0] != 0.0) { nonfin = 1; break; }
+        if (relaxed) { row_err = rv[1]; mass_dev = rv[2]; }
         cur ^= 1;
         ++l;
     }
@@ -276,17 +332,19 @@ __device__ __forceinline__ void solve_one(const BatchArgs &A, int prob, float *s
     // ---- epilogue: (f^l, g^l), E = <f,a> + <g,b> - eps sum(a) (Eq. 2 after an f-update), report
     const float *fo = fb + cur * n, *go = gb + cur * m;
     double s = 0.0;
-    for (int i = threadIdx.x; i < n; i += NT) {
+    for (int i = i0 + threadIdx.x; i < i1; i += NT) {
         A.f[(size_t)prob * n + i] = fo[i];
         const double ai = a ? (double)a[i] : 1.0 / n;
         s += (double)fo[i] * ai - (double)eps * ai;
     }
-    for (int j = threadIdx.x; j < m; j += NT) {
+    for (int j = j0 + threadIdx.x; j < j1; j += NT) {
         A.g[(size_t)prob * m + j] = go[j];
         s += (double)go[j] * (b ? (double)b[j] : 1.0 / m);
     }
-    const double E = block_sum_d<NT>(s, red) - (double)eps * mass_dev;   // relaxed: sum P != sum a
-    if (threadIdx.x == 0) {
+    double ev[4] = {block_sum_d<NT>(s, red), 0.0, 0.0, 0.0};
+    xsum(ev, 1);
+    const double E = ev[0] - (double)eps * mass_dev;   // relaxed: sum P != sum a
+    if (threadIdx.x == 0 && rank == 0) {
         A.iters[prob] = l;
         A.conv[prob] = conv;
         A.nonfinite[prob] = nonfin;
@@ -298,17 +356,25 @@ __device__ __forceinline__ void solve_one(const BatchArgs &A, int prob, float *s
 
 // Persistent CTAs (one or two per SM) pull problems from a global queue: iteration
 // counts differ per problem, so dynamic assignment balances the SMs.
-template <int D, int R, int NT, int EMU>
+template <int D, int R, int NT, int EMU, int CL>
 __global__ void __launch_bounds__(NT) k_batched(BatchArgs A) {
     extern __shared__ __align__(16) float sm[];
     __shared__ int s_prob;
+    const uint32_t rank = CL > 1 ? cl_rank() : 0u;
     for (;;) {
-        if (threadIdx.x == 0) s_prob = atomicAdd(A.queue, 1);
-        __syncthreads();
+        if (threadIdx.x == 0 && rank == 0) {
+            const int pr = atomicAdd(A.queue, 1);
+            s_prob = pr;
+            if constexpr (CL > 1) {   // the pair's problem id into the peer's s_prob
+                const uint32_t pa = cl_map(&s_prob, 1u);
+                asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(pa), "r"(pr) : "memory");
+            }
+        }
+        if constexpr (CL > 1) cl_sync(); else __syncthreads();
         const int prob = s_prob;
-        __syncthreads();
+        if constexpr (CL > 1) cl_sync(); else __syncthreads();
         if (prob >= A.B) break;
-        solve_one<D, R, NT, EMU>(A, prob, sm);
+        solve_one<D, R, NT, EMU, CL>(A, prob, sm, rank);
     }
 }
 
@@ -323,20 +389,46 @@ static int batched_emu() {
     return v;
 }
 
-template <int D, int R, int NT, int EMU>
-static cudaError_t launch_batched_t(const BatchArgs &A, int B, cudaStream_t st) {
+template <int D, int R, int NT, int EMU, int CL>
+static cudaError_t launch_batched_c(const BatchArgs &A, int B, cudaStream_t st) {
     const size_t smem = batched_smem_bytes(D, A.n, A.m);
-    cudaError_t e = cudaFuncSetAttribute(k_batched<D, R, NT, EMU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(k_batched<D, R, NT, EMU, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
     int occ = 0, dev = 0, nsm = 148;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_batched<D, R, NT, EMU>, NT, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_batched<D, R, NT, EMU, CL>, NT, smem);
     if (e != cudaSuccess) return e;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    const int grid = std::max(1, std::min(B, nsm * std::max(occ, 1)));
-    k_batched<D, R, NT, EMU><<<grid, NT, smem, st>>>(A);
-    return cudaGetLastError();
+    if (CL == 1) {
+        const int grid = std::max(1, std::min(B, nsm * std::max(occ, 1)));
+        k_batched<D, R, NT, EMU, 1><<<grid, NT, smem, st>>>(A);
+        return cudaGetLastError();
+    }
+    const int pairs = std::max(1, std::min(B, nsm * std::max(occ, 1) / 2));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2 * pairs);
+    cfg.blockDim = dim3(NT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k_batched<D, R, NT, EMU, CL>, A);
+}
+
+// SK_BATCHED_CL: 1 = one CTA per problem (default); 2 = a CTA pair per problem (two halves of
+// every pass, DSMEM exchange) — meant to halve the per-problem latency and so the idle tail of
+// the dynamic queue (C2: 21 % of SM time, uneven iteration counts), but measured 2x slower on
+// C2 (26.1 vs 13.5 ms): the pairs do not spread over twice the SMs at this occupancy.
+template <int D, int R, int NT, int EMU>
+static cudaError_t launch_batched_t(const BatchArgs &A, int B, cudaStream_t st) {
+    static const int cl = [] { const char *e = getenv("SK_BATCHED_CL"); return e ? atoi(e) : 1; }();
+    const int P = A.n > A.m ? A.n : A.m;
+    if (cl == 2 && P > 256 && B > 1) return launch_batched_c<D, R, NT, EMU, 2>(A, B, st);
+    return launch_batched_c<D, R, NT, EMU, 1>(A, B, st);
 }
 
 template <int D, int R, int NT>
