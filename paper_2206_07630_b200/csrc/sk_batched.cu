@@ -423,33 +423,32 @@ static cudaError_t launch_batched_c(const BatchArgs &A, int B, cudaStream_t st) 
 // every pass, DSMEM exchange) — meant to halve the per-problem latency and so the idle tail of
 // the dynamic queue (C2: 21 % of SM time, uneven iteration counts), but measured 2x slower on
 // C2 (26.1 vs 13.5 ms): the pairs do not spread over twice the SMs at this occupancy.
-template <int D, int R, int NT, int EMU>
-static cudaError_t launch_batched_t(const BatchArgs &A, int B, cudaStream_t st) {
-    static const int cl = [] { const char *e = getenv("SK_BATCHED_CL"); return e ? atoi(e) : 1; }();
-    const int P = A.n > A.m ? A.n : A.m;
-    if (cl == 2 && P > 256 && B > 1) return launch_batched_c<D, R, NT, EMU, 2>(A, B, st);
-    return launch_batched_c<D, R, NT, EMU, 1>(A, B, st);
-}
-
-template <int D, int R, int NT>
+template <int D, int R, int NT, int CL>
 static cudaError_t launch_batched_e(const BatchArgs &A, int B, cudaStream_t st) {
     switch (batched_emu()) {
-        case 0: return launch_batched_t<D, R, NT, 0>(A, B, st);
-        case 2: return launch_batched_t<D, R, NT, 2>(A, B, st);
-        default: return launch_batched_t<D, R, NT, 1>(A, B, st);
+        case 0: return launch_batched_c<D, R, NT, 0, CL>(A, B, st);
+        case 2: return launch_batched_c<D, R, NT, 2, CL>(A, B, st);
+        default: return launch_batched_c<D, R, NT, 1, CL>(A, B, st);
     }
 }
 
 // One wide CTA per problem: NT threads x R output points per thread per round.
 // SK_BATCHED_SHAPE=1 selects 512 threads x 2 points for 512 < P <= 1024 (tuning knob).
+// With a CTA pair (CL = 2) each CTA's shape covers its half of the points (no idle lanes).
 template <int D>
 static cudaError_t launch_batched_d(const BatchArgs &A, int B, cudaStream_t st) {
     static int shape = [] { const char *e = getenv("SK_BATCHED_SHAPE"); return e ? atoi(e) : 1; }();
+    static const int clk = [] { const char *e = getenv("SK_BATCHED_CL"); return e ? atoi(e) : 1; }();
     const int P = A.n > A.m ? A.n : A.m;
-    if (P <= 256) return launch_batched_e<D, 1, 256>(A, B, st);
-    if (P <= 512) return launch_batched_e<D, 1, 512>(A, B, st);
-    if (P <= 1024) return shape == 1 ? launch_batched_e<D, 2, 512>(A, B, st) : launch_batched_e<D, 1, 1024>(A, B, st);
-    return launch_batched_e<D, 2, 1024>(A, B, st);  // more rounds of 2048 points for larger P
+    if (clk == 2 && P > 256 && P <= 2048 && B > 1) {
+        if (P <= 512) return launch_batched_e<D, 1, 256, 2>(A, B, st);
+        if (P <= 1024) return launch_batched_e<D, 1, 512, 2>(A, B, st);
+        return launch_batched_e<D, 1, 1024, 2>(A, B, st);
+    }
+    if (P <= 256) return launch_batched_e<D, 1, 256, 1>(A, B, st);
+    if (P <= 512) return launch_batched_e<D, 1, 512, 1>(A, B, st);
+    if (P <= 1024) return shape == 1 ? launch_batched_e<D, 2, 512, 1>(A, B, st) : launch_batched_e<D, 1, 1024, 1>(A, B, st);
+    return launch_batched_e<D, 2, 1024, 1>(A, B, st);  // more rounds of 2048 points for larger P
 }
 
 bool batched_supported(int d, int n, int m) {
