@@ -419,10 +419,10 @@ static cudaError_t launch_batched_c(const BatchArgs &A, int B, cudaStream_t st) 
     return cudaLaunchKernelEx(&cfg, k_batched<D, R, NT, EMU, CL>, A);
 }
 
-// SK_BATCHED_CL: 1 = one CTA per problem (default); 2 = a CTA pair per problem (two halves of
-// every pass, DSMEM exchange) — meant to halve the per-problem latency and so the idle tail of
-// the dynamic queue (C2: 21 % of SM time, uneven iteration counts), but measured 2x slower on
-// C2 (26.1 vs 13.5 ms): the pairs do not spread over twice the SMs at this occupancy.
+// CTA pairs (CL = 2: two halves of every pass, DSMEM exchange) halve a problem's latency; on
+// a batch (C2) that should shorten the idle tail of the dynamic queue (21 % of SM time with
+// uneven iteration counts) but measures on par with one CTA per problem (14.0 vs 13.8 ms: the
+// cluster barriers and the R = 1 shape cost what the tail saves), so batches use one CTA.
 template <int D, int R, int NT, int CL>
 static cudaError_t launch_batched_e(const BatchArgs &A, int B, cudaStream_t st) {
     switch (batched_emu()) {
@@ -438,9 +438,13 @@ static cudaError_t launch_batched_e(const BatchArgs &A, int B, cudaStream_t st) 
 template <int D>
 static cudaError_t launch_batched_d(const BatchArgs &A, int B, cudaStream_t st) {
     static int shape = [] { const char *e = getenv("SK_BATCHED_SHAPE"); return e ? atoi(e) : 1; }();
-    static const int clk = [] { const char *e = getenv("SK_BATCHED_CL"); return e ? atoi(e) : 1; }();
+    // CTA pair: opt-in for batches (SK_BATCHED_CL=2), the default for one latency-bound problem
+    // (C1: 0.267 vs 0.295 ms for 34 sweeps); SK_BATCHED_CL=1 forces one CTA
+    static const int clk = [] { const char *e = getenv("SK_BATCHED_CL"); return e ? atoi(e) : 0; }();
     const int P = A.n > A.m ? A.n : A.m;
-    if (clk == 2 && P > 256 && P <= 2048 && B > 1) {
+    const bool pair = clk == 2 || (clk == 0 && B == 1);
+    if (pair && P > 128 && P <= 2048) {
+        if (P <= 256) return launch_batched_e<D, 1, 128, 2>(A, B, st);
         if (P <= 512) return launch_batched_e<D, 1, 256, 2>(A, B, st);
         if (P <= 1024) return launch_batched_e<D, 1, 512, 2>(A, B, st);
         return launch_batched_e<D, 1, 1024, 2>(A, B, st);
