@@ -217,6 +217,21 @@ sk_status sinkhorn_init_sort1d(sk_ctx *ctx, int64_t B, int64_t n, int64_t m, con
                                const float *y, int32_t y_shared, int32_t dualsort_iters,
                                float *pot, int32_t *perm, int32_t *rank);
 
+/* General 1D initializer (Sec. 3.1 for any n, m and weights; Alg. 3/4,
+ * P:429-455) for d = 1 and cost (x - y)^2: sort x (sigma) and y (rho); the
+ * north-west corner plan of (a_sigma, b_rho) — a staircase whose cumulative-mass ties split it
+ * into trees (exact ties: integers for uniform weights, fp64 cumulative sums of the fp32
+ * weights otherwise); its eps = 0 dual by Alg. 3 in reading R-26 (every tree's root bounded by
+ * the feasibility of all its sources, all trees from f = 0, Jacobi rounds, UpdateTree after
+ * each) until f is unchanged or max_rounds rounds (0 = n + m + 2); f^(0)_{sigma(k)} = f~_k.
+ * With n = m and uniform weights this is DualSort's fixed point (sinkhorn_init_sort1d is the
+ * O(n) route for that case).  x: B x n; y: m (y_shared) or B x m; a: B x n, b like y
+ * (nullable = uniform, positive); pot: B x n (x side); rounds: B (nullable).  n, m <= 4096.
+ * SK_EINVAL: bad sizes, NaN, non-positive weights; SK_EUNSUPPORTED: too large.  Blocks. */
+sk_status sinkhorn_init_nw1d(sk_ctx *ctx, int64_t B, int64_t n, int64_t m, const float *x,
+                             const float *y, int32_t y_shared, const float *a, const float *b,
+                             int32_t max_rounds, float *pot, int32_t *rounds);
+
 /* Gaussian initializer (Sec. 3.2): weighted means and biased
  * covariances (+ ridge_rel * tr/d * I, R-11) computed on device with fp64
  * accumulation; matrix square roots by fp64 coupled Newton-Schulz (R-12);

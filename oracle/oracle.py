@@ -505,3 +505,114 @@ def sinkhorn_vjp(x, y, f, g, eps, zf, zg):
     gx = 2.0 * (S[:, :, None] * (x[:, None, :] - y[None, :, :])).sum(1)
     gy = 2.0 * (S[:, :, None] * (y[None, :, :] - x[:, None, :])).sum(0)
     return gx, gy, eps * wf, eps * wg
+
+
+# ------------------------------------------------ general 1D: NW corner + Alg. 3/4 (NEXT-2)
+def nw_corner_support(a_sorted, b_sorted, uniform=False):
+    """North-west corner solution on sorted supports: its support edges (k, l) in walk
+    order and the tree id of each edge.  A tie of the cumulative masses A_k = B_l before the
+    end starts a new tree (the support graph is a forest).  Reading R-26: ties are exact
+    — integer k m == l n for uniform weights, else fp64 cumulative sums of the (fp32) weights."""
+    n, m = len(a_sorted), len(b_sorted)
+    if uniform:
+        Acum = lambda k: (k + 1) * m          # (k + 1)/n scaled by n m
+        Bcum = lambda l: (l + 1) * n
+    else:
+        A = np.cumsum(np.asarray(a_sorted, np.float64))
+        B = np.cumsum(np.asarray(b_sorted, np.float64))
+        Acum, Bcum = (lambda k: A[k]), (lambda l: B[l])
+    edges, tree = [], []
+    k = l = t = 0
+    while True:
+        edges.append((k, l))
+        tree.append(t)
+        if k == n - 1 and l == m - 1:
+            break
+        ak, bl = Acum(k), Bcum(l)
+        if ak < bl:
+            k += 1
+        elif bl < ak:
+            l += 1
+        else:
+            k += 1
+            l += 1
+            t += 1
+    return edges, tree
+
+
+def dual_from_primal(C, edges, tree, max_rounds=100000):
+    """Alg. 3 (Recover dual from primal) with Alg. 4 (UpdateTree), in reading R-26:
+    f = 0; repeat {
+      for every tree k (the first included, from f = 0 as DualSort, R-7):
+          f_{s(k)} <- min_{i in T_k, j} c_ij - c_{iota(j),j} + f_{iota(j)} - (f_i - f_{s(k)})
+      (the printed line 5 is the term i = s(k); a tree's sources move together — f_i - f_{s(k)}
+      is fixed by its tight edges — so every source's feasibility bounds the root);
+      for every tree: UpdateTree — walk its edges in pre-order from s(k):
+          a new sink t:   g_t <- c_{s,t} - f_s;    a new source s:   f_s <- c_{s,t} - g_t
+    } until no root moves (a root moves only if its bound is below it by more than
+    1e-12 max(1, max|C|): its own tight edges give f_{s(k)} itself up to fp64 rounding).  The walk order of the NW staircase is a pre-order traversal from
+    the tree's smallest source.  With n = m uniform (n one-edge trees) this is DualSort's Jacobi
+    fixed point (Alg. 2, R-5/R-7).  Returns (f, g, rounds)."""
+    C = _d(C)
+    n, m = C.shape
+    K = tree[-1] + 1
+    trees = [[e for e, t in zip(edges, tree) if t == k] for k in range(K)]
+    roots = [tr[0][0] for tr in trees]
+    srcs = [sorted({i for (i, _) in tr}) for tr in trees]
+    iota = np.full(m, -1)
+    for (i, j) in edges:
+        if iota[j] < 0 or i < iota[j]:
+            iota[j] = i
+    f, g = np.zeros(n), np.zeros(m)
+
+    def update_tree(tr):
+        seen_s, seen_t = {tr[0][0]}, set()
+        for (i, j) in tr:
+            if i in seen_s and j not in seen_t:
+                g[j] = C[i, j] - f[i]
+                seen_t.add(j)
+            elif j in seen_t and i not in seen_s:
+                f[i] = C[i, j] - g[j]
+                seen_s.add(i)
+    for tr in trees:
+        update_tree(tr)
+    tol = 1e-12 * max(1.0, float(np.abs(C).max()))
+    for rounds in range(1, max_rounds + 1):
+        fold = f.copy()
+        base = -C[iota, np.arange(m)] + fold[iota]          # -g_j of the tight edge (iota(j), j)
+        moved = False
+        for k in range(K):
+            s = roots[k]
+            v = min(np.min(C[i, :] + base - (fold[i] - fold[s])) for i in srcs[k])
+            if v < fold[s] - tol:   # R-26: the tree's own tight edges give f_s to rounding
+                f[s] = v
+                moved = True
+        if not moved:
+            return f, g, rounds
+        for tr in trees:
+            update_tree(tr)
+    return f, g, max_rounds
+
+
+def init_nw1d(x, y, a=None, b=None):
+    """General 1D initializer (Sec. 3.1 with any n, m and weights; NEXT-2): sort x
+    (sigma) and y (rho), the NW corner plan of (a_sigma, b_rho), its eps = 0 dual by
+    Alg. 3 on the sorted cost (x_sigma_k - y_rho_l)^2, f0_{sigma(k)} = f~_k."""
+    x = np.asarray(x, np.float32).ravel()
+    y = np.asarray(y, np.float32).ravel()
+    px, _ = sort_rank(x)
+    py, _ = sort_rank(y)
+    uniform = a is None and b is None
+    a_s = None if a is None else np.asarray(a, np.float32).ravel()[px]
+    b_s = None if b is None else np.asarray(b, np.float32).ravel()[py]
+    if not uniform:
+        a_s = np.full(x.size, 1.0 / x.size) if a_s is None else a_s
+        b_s = np.full(y.size, 1.0 / y.size) if b_s is None else b_s
+    edges, tree = nw_corner_support(np.ones(x.size) if uniform else a_s, np.ones(y.size) if uniform else b_s,
+                                    uniform=uniform)
+    xs, ys = x[px].astype(np.float64), y[py].astype(np.float64)
+    C = (xs[:, None] - ys[None, :]) ** 2
+    fs, _, _ = dual_from_primal(C, edges, tree)
+    f0 = np.empty(x.size)
+    f0[px] = fs
+    return f0

@@ -236,6 +236,20 @@ def sinkhorn_solve(ctx: Context, x, y, eps: float, tol: float = 1e-3, max_iter: 
     return f, g, out
 
 
+def sinkhorn_init_nw1d(ctx: Context, x, y, a=None, b=None, y_shared: bool = True, max_rounds: int = 0):
+    """General 1D initializer (NW corner + Alg. 3/4, R-26): x (B, n) or (n,); y (m,) [shared] or
+    (B, m); weights like x / y (None = uniform).  Returns (f0 like x, rounds per problem)."""
+    single = x.dim() == 1
+    xb = x.unsqueeze(0) if single else x
+    B, n = xb.shape
+    m = y.shape[-1]
+    pot = _empty((B, n), x)
+    rounds = torch.zeros(B, dtype=torch.int32, device=x.device) if x.is_cuda else torch.zeros(B, dtype=torch.int32)
+    ctx.check(ctx.lib.sinkhorn_init_nw1d(ctx.h, B, n, m, _ptr(x), _ptr(y), int(y_shared), _ptr(a), _ptr(b),
+                                         int(max_rounds), _ptr(pot), _ptr(rounds, torch.int32)))
+    return (pot.view(n) if single else pot), rounds
+
+
 def sinkhorn_fit_gmm(ctx: Context, x, K: int, init_idx, iters: int = 100, reg_covar: float = 1e-6):
     """EM fit of a K-component full-covariance GMM of x (n, d) from means x[init_idx] (NEXT-3).
     Returns ({'weights', 'means', 'covs'} as sinkhorn_init_gmm takes them, mean log-likelihood)."""

@@ -40,7 +40,7 @@ class SkCounters(ctypes.Structure):
 EXPORTS = [
     "sk_create", "sk_set_stream", "sk_destroy", "sk_last_error", "sk_status_string", "sk_version",
     "sk_set_timing", "sk_set_relaxation", "sk_set_eps_decay", "sk_get_counters", "sk_reset_counters", "sk_nccl_unique_id", "sk_comm_init",
-    "sk_shard_rows", "sinkhorn_sort1d_batched", "sinkhorn_soft_rank_sort", "sinkhorn_fit_gmm", "sinkhorn_vjp", "sinkhorn_init_zero", "sinkhorn_init_sort1d",
+    "sk_shard_rows", "sinkhorn_sort1d_batched", "sinkhorn_soft_rank_sort", "sinkhorn_fit_gmm", "sinkhorn_vjp", "sinkhorn_init_nw1d", "sinkhorn_init_zero", "sinkhorn_init_sort1d",
     "sinkhorn_init_gaussian", "sinkhorn_init_gmm", "sinkhorn_init_subsample", "sinkhorn_solve",
     "sinkhorn_solve_sharded", "sinkhorn_solve_sharded_emulated", "sk_selftest_tc_dot",
     "sk_microbench",
@@ -78,6 +78,7 @@ def load() -> ctypes.CDLL:
         "sinkhorn_init_zero": (S, [P, I64, I64, P]),
         "sinkhorn_soft_rank_sort": (S, [P, I64, I64, I64, P, P, I32, F, P, P, P, P, P]),
         "sinkhorn_fit_gmm": (S, [P, I64, I32, P, I32, P, I32, F, P, P, P, ctypes.POINTER(D)]),
+        "sinkhorn_init_nw1d": (S, [P, I64, I64, I64, P, P, I32, P, P, I32, P, P]),
         "sinkhorn_vjp": (S, [P, I64, I64, I32, P, P, F, P, P, P, P, F, I32, P, P, P, P, ctypes.POINTER(I32),
                              ctypes.POINTER(D)]),
         "sinkhorn_init_sort1d": (S, [P, I64, I64, I64, P, P, I32, I32, P, P, P]),

@@ -938,7 +938,7 @@ sk_status sinkhorn_init_sort1d(sk_ctx *ctx, int64_t B, int64_t n, int64_t m, con
                                int32_t *perm, int32_t *rank) {
     if (!ctx) return SK_EINVAL;
     if (B < 1 || n < 1 || m < 1 || !x || !y || !pot) return fail(ctx, SK_EINVAL, "bad arguments");
-    if (n != m) return fail(ctx, SK_EUNSUPPORTED, "sort1d initializer needs n == m (general NW is a later row)");
+    if (n != m) return fail(ctx, SK_EUNSUPPORTED, "sort1d initializer needs n == m (sinkhorn_init_nw1d: any n, m)");
     if (n > 4096) return fail(ctx, SK_EUNSUPPORTED, "sort1d initializer supports n <= 4096");
     if (dualsort_iters < 0) return fail(ctx, SK_EINVAL, "dualsort_iters >= 0");
     Stager sg(ctx);
@@ -959,6 +959,43 @@ sk_status sinkhorn_init_sort1d(sk_ctx *ctx, int64_t B, int64_t n, int64_t m, con
     CU(launch_sort_rows(dy, (int)(y_shared ? 1 : B), (int)m, m, pscr, nullptr, ys, flag, ctx->stream));
     CU(launch_sort_rows(dx, (int)B, (int)n, n, dperm, drank, xs, flag, ctx->stream));
     CU(launch_sort1d_dual(xs, dperm, ys, y_shared, (int)B, (int)n, dualsort_iters, dpot, ctx->stream));
+    ctx->cnt.kernel_launches += 3;
+    CK(sg.flush());
+    CU(cudaMemcpyAsync(ctx->h_flag, flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    if (*ctx->h_flag) return fail(ctx, SK_EINVAL, "NaN in x or y");
+    return SK_OK;
+}
+
+sk_status sinkhorn_init_nw1d(sk_ctx *ctx, int64_t B, int64_t n, int64_t m, const float *x, const float *y,
+                             int32_t y_shared, const float *a, const float *b, int32_t max_rounds, float *pot,
+                             int32_t *rounds) {
+    if (!ctx) return SK_EINVAL;
+    if (B < 1 || n < 1 || m < 1 || !x || !y || !pot) return fail(ctx, SK_EINVAL, "bad arguments");
+    if (max_rounds < 0) return fail(ctx, SK_EINVAL, "max_rounds >= 0 (0 = until converged)");
+    if (n > 4096 || m > 4096 || nw1d_smem_bytes((int)n, (int)m) > 220 * 1024)
+        return fail(ctx, SK_EUNSUPPORTED, "general 1D initializer: n, m <= 4096 and the problem in shared memory");
+    Stager sg(ctx);
+    const long long ycount = (y_shared ? 1 : B) * m;
+    const float *dx, *dy, *da, *db;
+    float *dpot;
+    int *drounds;
+    CK(sg.in_t(x, (size_t)B * n, &dx));
+    CK(sg.in_t(y, (size_t)ycount, &dy));
+    CK(sg.in_t(a, a ? (size_t)B * n : 0, &da));
+    CK(sg.in_t(b, b ? (size_t)ycount : 0, &db));
+    CK(sg.out_t(pot, (size_t)B * n, &dpot));
+    CK(sg.out_t(rounds, rounds ? (size_t)B : 0, &drounds));
+    CK(check_arrays(ctx, {{dx, B * n}, {dy, ycount}}, {{da, da ? B * n : 0}, {db, db ? ycount : 0}}, "sinkhorn_init_nw1d"));
+    ENSURE(flag, int, B_FLAG, 4);
+    ENSURE(xs, float, B_SORT, B * n);
+    ENSURE(ys, float, B_YSORT, ycount);
+    ENSURE(pscr, int, B_PERM, ycount + B * n);
+    CU(cudaMemsetAsync(flag, 0, sizeof(int), ctx->stream));
+    CU(launch_sort_rows(dy, (int)(y_shared ? 1 : B), (int)m, m, pscr, nullptr, ys, flag, ctx->stream));
+    CU(launch_sort_rows(dx, (int)B, (int)n, n, pscr + ycount, nullptr, xs, flag, ctx->stream));
+    CU(launch_nw1d(xs, pscr + ycount, ys, pscr, y_shared ? 1 : 0, da, db, (int)B, (int)n, (int)m,
+                   max_rounds ? max_rounds : (int)(n + m + 2), dpot, drounds, ctx->stream));
     ctx->cnt.kernel_launches += 3;
     CK(sg.flush());
     CU(cudaMemcpyAsync(ctx->h_flag, flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));

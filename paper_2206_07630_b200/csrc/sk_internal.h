@@ -25,6 +25,11 @@ struct BatchLaunch {
     float decay_init = 0.f, decay_rate = 1.f;   // eps-decay (R-25; decay_init <= 0: off)
 };
 bool batched_supported(int d, int n, int m);
+// K18 general 1D initializer (NW corner + Alg. 3/4, R-26) on sorted supports
+size_t nw1d_smem_bytes(int n, int m);
+cudaError_t launch_nw1d(const float *xs, const int *xperm, const float *ys, const int *yperm, int y_shared,
+                        const float *a, const float *b, int B, int n, int m, int max_rounds, float *pot, int *rounds,
+                        cudaStream_t st);
 // K16 GMM fitting by EM (NEXT-3); state and partial workspace sizes in doubles
 size_t em_state_doubles(int K, int d);
 size_t em_partial_doubles(int K, int d);

@@ -193,3 +193,147 @@ cudaError_t launch_sort1d_dual(const float *xs_sorted, const int *perm, const fl
 }
 
 }  // namespace sk
+
+namespace sk {
+
+// ------------------------------------------------------------------- K18
+// General 1D initializer (Sec. 3.1 for any n, m and weights; reading R-26):
+// on the sorted supports, the north-west corner plan — a staircase of edges whose
+// cumulative-mass ties split it into trees — and its eps = 0 dual by Alg. 3/4
+// (P:429-455): f = 0, UpdateTree for every tree, then rounds of
+//     f_{s(k)} <- min_{i in T_k, j} c_ij - c_{iota(j),j} + f_{iota(j)} - (f_i - f_{s(k)})   (Jacobi, all trees)
+//     UpdateTree(k) for every tree
+// until f is unchanged.  One CTA per problem; the NW walk by one thread (exact ties: integers
+// for uniform weights, fp64 cumulative sums otherwise), the tree walks one thread per tree, the
+// root minimum over all (i, j) pairs by all threads (fp64, order-free min: deterministic).
+constexpr int kNW = 512;
+
+__device__ __forceinline__ unsigned long long ord_dbl(double v) {   // order-preserving key
+    const unsigned long long u = __double_as_longlong(v);
+    return (u & 0x8000000000000000ull) ? ~u : (u | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double dbl_ord(unsigned long long k) {
+    return __longlong_as_double((k & 0x8000000000000000ull) ? (k & 0x7fffffffffffffffull) : ~k);
+}
+
+__global__ void __launch_bounds__(kNW) k_nw1d(const float *__restrict__ xs_all, const int *__restrict__ xperm_all,
+                                              const float *__restrict__ ys_all, const int *__restrict__ yperm_all,
+                                              int y_shared, const float *__restrict__ a, const float *__restrict__ b,
+                                              int n, int m, int max_rounds, float *pot, int *rounds_out) {
+    extern __shared__ double smd[];
+    const long long pr = blockIdx.x;
+    double *X = smd, *Y = X + n, *f = Y + m, *g = f + n, *fold = g + m, *base = fold + n;
+    int *ei = reinterpret_cast<int *>(base + m);   // edges (n + m - 1 at most)
+    int *ej = ei + (n + m);
+    int *tel = ej + (n + m);                        // tree t: edges [tel[t], tel[t + 1])
+    int *iota = tel + (n + m + 1);                  // smallest source of sink j
+    int *tof = iota + m;                            // tree of source i
+    unsigned long long *slot = reinterpret_cast<unsigned long long *>(tof + n + 1);  // [K] (4(n+m)+1 ints + 1 pad)
+    __shared__ int sK, sE, schanged;
+    const float *xs = xs_all + pr * n;
+    const int *xperm = xperm_all + pr * n;
+    const float *ys = ys_all + (y_shared ? 0 : pr * m);
+    const int *yperm = yperm_all + (y_shared ? 0 : pr * m);
+    for (int i = threadIdx.x; i < n; i += kNW) X[i] = (double)xs[i];
+    for (int j = threadIdx.x; j < m; j += kNW) { Y[j] = (double)ys[j]; iota[j] = -1; }
+    __syncthreads();
+    if (threadIdx.x == 0) {   // the NW walk: edges in staircase order, trees at the ties
+        const bool uni = !a && !b;
+        const float *ar = a ? a + pr * n : nullptr, *br = b ? b + (y_shared ? 0 : pr * m) : nullptr;
+        double A = 0.0, Bc = 0.0;
+        int k = 0, l = 0, t = 0, e = 0;
+        if (!uni) {
+            A = ar ? (double)ar[xperm[0]] : 1.0 / n;
+            Bc = br ? (double)br[yperm[0]] : 1.0 / m;
+        }
+        tel[0] = 0;
+        for (;;) {
+            ei[e] = k; ej[e] = l; ++e;
+            if (iota[l] < 0) iota[l] = k;
+            tof[k] = t;
+            if (k == n - 1 && l == m - 1) break;
+            int step;   // 1: source, 2: sink, 3: both (a tie: a new tree)
+            if (uni) {
+                const long long ak = (long long)(k + 1) * m, bl = (long long)(l + 1) * n;
+                step = ak < bl ? 1 : (bl < ak ? 2 : 3);
+            } else {
+                step = A < Bc ? 1 : (Bc < A ? 2 : 3);
+            }
+            if (step & 1) { ++k; if (!uni) A += ar ? (double)ar[xperm[k]] : 1.0 / n; }
+            if (step & 2) { ++l; if (!uni) Bc += br ? (double)br[yperm[l]] : 1.0 / m; }
+            if (step == 3) tel[++t] = e;
+        }
+        tel[t + 1] = e;
+        sK = t + 1;
+        sE = e;
+    }
+    __syncthreads();
+    const int K = sK;
+    for (int i = threadIdx.x; i < n; i += kNW) f[i] = 0.0;
+    __syncthreads();
+    auto cost = [&](int i, int j) { const double d = X[i] - Y[j]; return d * d; };
+    auto update_trees = [&]() {   // Alg. 4 for every tree (one thread per tree)
+        for (int t = threadIdx.x; t < K; t += kNW) {
+            int pi = -1, pj = -1;
+            for (int e = tel[t]; e < tel[t + 1]; ++e) {
+                const int i = ei[e], j = ej[e];
+                if (i != pi && j != pj) g[j] = cost(i, j) - f[i];        // the root's first edge
+                else if (i == pi) g[j] = cost(i, j) - f[i];              // a new sink
+                else f[i] = cost(i, j) - g[j];                            // a new source
+                pi = i; pj = j;
+            }
+        }
+        __syncthreads();
+    };
+    update_trees();
+    // R-26: a root moves only if its bound is below it by more than tol (its own tight edges
+    // give the root value itself up to fp64 rounding); max |C| is at a corner of the sorted cost
+    const double cmax = fmax(fmax(cost(0, 0), cost(0, m - 1)), fmax(cost(n - 1, 0), cost(n - 1, m - 1)));
+    const double tol = 1e-12 * fmax(1.0, cmax);
+    int rounds = 0;
+    for (; rounds < max_rounds;) {
+        ++rounds;
+        for (int i = threadIdx.x; i < n; i += kNW) fold[i] = f[i];
+        for (int t = threadIdx.x; t < K; t += kNW) slot[t] = ~0ull;
+        if (threadIdx.x == 0) schanged = 0;
+        __syncthreads();
+        for (int j = threadIdx.x; j < m; j += kNW) base[j] = -cost(iota[j], j) + fold[iota[j]];
+        __syncthreads();
+        // per source i: min_j c_ij + base_j - (f_i - f_root) -> its tree's slot (order-free min)
+        for (int i = threadIdx.x; i < n; i += kNW) {
+            const int t = tof[i];
+            const int root = ei[tel[t]];
+            double v = INFINITY;
+            for (int j = 0; j < m; ++j) v = fmin(v, cost(i, j) + base[j] - (fold[i] - fold[root]));
+            atomicMin(&slot[t], ord_dbl(v));
+        }
+        __syncthreads();
+        for (int t = threadIdx.x; t < K; t += kNW) {
+            const int root = ei[tel[t]];
+            const double v = dbl_ord(slot[t]);
+            if (v < fold[root] - tol) { f[root] = v; schanged = 1; }
+        }
+        __syncthreads();
+        if (!schanged) break;
+        update_trees();
+    }
+    for (int i = threadIdx.x; i < n; i += kNW) pot[pr * n + xperm[i]] = (float)f[i];
+    if (threadIdx.x == 0 && rounds_out) rounds_out[pr] = rounds;
+}
+
+size_t nw1d_smem_bytes(int n, int m) {
+    return sizeof(double) * (3 * (size_t)n + 3 * (size_t)m) + sizeof(int) * (4 * (size_t)(n + m) + 2) +
+           sizeof(unsigned long long) * (size_t)(n < m ? n : m);
+}
+
+cudaError_t launch_nw1d(const float *xs, const int *xperm, const float *ys, const int *yperm, int y_shared,
+                        const float *a, const float *b, int B, int n, int m, int max_rounds, float *pot, int *rounds,
+                        cudaStream_t st) {
+    const size_t smem = nw1d_smem_bytes(n, m);
+    cudaError_t e = cudaFuncSetAttribute(k_nw1d, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k_nw1d<<<B, kNW, smem, st>>>(xs, xperm, ys, yperm, y_shared, a, b, n, m, max_rounds, pot, rounds);
+    return cudaGetLastError();
+}
+
+}  // namespace sk

@@ -620,3 +620,48 @@ def test_eps_decay_same_optimum_and_off_switch():
     off = O.sinkhorn(p.x, p.y, p.eps, tol=1e-3, eps_decay=(1.0, 0.8))   # init <= 1: no decay sweep
     plain = O.sinkhorn(p.x, p.y, p.eps, tol=1e-3)
     assert off.iterations == plain.iterations and np.array_equal(off.f, plain.f)
+
+
+# -------------------------------------------- general 1D NW + Alg. 3/4 (NEXT-2, R-26)
+def test_nw1d_reduces_to_dualsort_when_n_equals_m():
+    """Uniform n = m: the NW plan is the sorted identity (n one-edge trees) and Alg. 3 in reading
+    R-26 is DualSort's Jacobi iteration from f = 0 (Alg. 2, R-5/R-7, pinned above): the same
+    fixed point."""
+    from oracle import oracle as O
+    rng = np.random.default_rng(41)
+    for n in (1, 2, 7, 40):
+        x, y = rng.random(n).astype(np.float32), rng.random(n).astype(np.float32)
+        assert np.abs(O.init_nw1d(x, y) - O.init_sort1d(x, y)).max() < 1e-12
+
+
+@pytest.mark.parametrize("n,m,weights", [(3, 5, False), (6, 4, True), (5, 5, True), (4, 6, False), (2, 6, True),
+                                          (6, 6, False), (4, 2, False)])
+def test_nw1d_dual_is_lp_optimal(n, m, weights):
+    """The eps = 0 dual of the general 1D problem: feasible (f_i + g_j <= c_ij), tight on the NW
+    support, and <f, a> + <g, b> equals the optimal value of the transport LP solved by brute
+    force (scipy linprog) — strong duality."""
+    from oracle import oracle as O
+    from scipy.optimize import linprog
+    rng = np.random.default_rng(n * 10 + m)
+    x, y = rng.random(n).astype(np.float32), rng.random(m).astype(np.float32)
+    a = gen.random_weights(n, rng) if weights else np.full(n, 1.0 / n, np.float32)
+    b = gen.random_weights(m, rng) if weights else np.full(m, 1.0 / m, np.float32)
+    px, py = np.argsort(x, kind="stable"), np.argsort(y, kind="stable")
+    xs, ys = x[px].astype(np.float64), y[py].astype(np.float64)
+    C = (xs[:, None] - ys[None, :]) ** 2
+    edges, tree = O.nw_corner_support(a[px] if weights else np.ones(n), b[py] if weights else np.ones(m),
+                                      uniform=not weights)
+    f, g, _ = O.dual_from_primal(C, edges, tree)
+    assert (f[:, None] + g[None, :] - C).max() <= 1e-12
+    for (i, j) in edges:
+        assert abs(f[i] + g[j] - C[i, j]) <= 1e-12
+    A_eq = np.zeros((n + m, n * m))
+    for i in range(n):
+        A_eq[i, i * m:(i + 1) * m] = 1
+    for j in range(m):
+        A_eq[n + j, j::m] = 1
+    aa, bb = a[px].astype(np.float64), b[py].astype(np.float64)
+    bb = bb * aa.sum() / bb.sum()
+    lp = linprog(C.ravel(), A_eq=A_eq, b_eq=np.concatenate([aa, bb]), bounds=(0, None), method="highs")
+    # g on every sink (the c-transform also covers sinks a tree never reached: none for NW)
+    assert abs(f @ aa + g @ bb - lp.fun) < 1e-9
