@@ -77,7 +77,7 @@ __global__ void k_reduce_cols(const double *in, int nb, int E, double *out) {
 cudaError_t launch_moments(const float *x, const float *w, long long n, int d, double *mean,
                            double *cov, double *scratch, long long scratch_doubles, cudaStream_t st) {
     if (d > 64) return cudaErrorInvalidValue;
-    long long nb = (n + 4095) / 4096;
+    long long nb = (n + 63) / 64;   // one 64-point chunk per CTA up to 296 CTAs (a fixed partition of n)
     if (nb > 296) nb = 296;
     if (nb * d * d > scratch_doubles) nb = scratch_doubles / (d * d);
     if (nb < 1) return cudaErrorInvalidValue;
