@@ -103,14 +103,26 @@ __global__ void __launch_bounds__(kEmT) k_em_chol(double *base, int K, int d, in
 
 // E-step + sufficient statistics over this CTA's fixed chunk of points.  Statistic s of
 // component k (base k (1 + d + T)): 0 = n_k, 1..d = sum r x, then sum r x_a x_b for a <= b.
-template <int MAXS>
+template <int MAXS, int DM>
 __global__ void __launch_bounds__(kEmT) k_em_estep(const float *__restrict__ x, long long n, int d, int K,
                                                     const double *__restrict__ base, double *part) {
     extern __shared__ double sm[];
     double *xs = sm;                          // [kEmTile][d]
     double *rs = xs + kEmTile * d;            // [kEmTile][K]
     double *lls = rs + kEmTile * K;           // [kEmTile]
+    double *sL = lls + kEmTile;               // [K][DM][DM] L^{-1} (lower triangle used)
+    double *sM = sL + K * DM * DM;            // [K][DM] means
+    double *sC = sM + K * DM;                 // [K] log w_k - log det L_k
     const EmState s = em_state(const_cast<double *>(base), K, d);
+    for (int e = threadIdx.x; e < K * DM * DM; e += kEmT) {
+        const int k = e / (DM * DM), r = (e / DM) % DM, c = e % DM;
+        sL[e] = (r < d && c < d) ? s.LINV[(long long)k * d * d + r * d + c] : 0.0;
+    }
+    for (int e = threadIdx.x; e < K * DM; e += kEmT) {
+        const int k = e / DM, c = e % DM;
+        sM[e] = c < d ? s.MU[(long long)k * d + c] : 0.0;
+    }
+    for (int k = threadIdx.x; k < K; k += kEmT) sC[k] = log(s.W[k]) - s.LOGDET[k];
     const int T = d * (d + 1) / 2, per = 1 + d + T, S = K * per;
     const long long chunk = (n + gridDim.x - 1) / gridDim.x;
     const long long p0 = blockIdx.x * chunk, p1 = min(n, p0 + chunk);
@@ -142,15 +154,20 @@ __global__ void __launch_bounds__(kEmT) k_em_estep(const float *__restrict__ x, 
         for (int e = threadIdx.x; e < np * K; e += kEmT) {   // log p of (point, component) pairs
             const int pp = e / K, k = e % K;
             const double *xi = xs + pp * d;
-            const double *Li = s.LINV + (long long)k * d * d;
-            const double *mk = s.MU + (long long)k * d;
+            const double *Li = sL + k * DM * DM;
+            const double *mk = sM + k * DM;
+            double dx[DM];
+#pragma unroll
+            for (int c = 0; c < DM; ++c) dx[c] = c < d ? xi[c] - mk[c] : 0.0;
             double q = 0.0;
-            for (int r = 0; r < d; ++r) {
+#pragma unroll
+            for (int r = 0; r < DM; ++r) {
                 double z = 0.0;
-                for (int c = 0; c <= r; ++c) z = fma(Li[r * d + c], xi[c] - mk[c], z);
-                q = fma(z, z, q);
+#pragma unroll
+                for (int c = 0; c <= r; ++c) z = fma(Li[r * DM + c], dx[c], z);
+                q = fma(z, z, q);   // (rows r >= d are zero)
             }
-            rs[pp * K + k] = log(s.W[k]) - 0.5 * q - s.LOGDET[k];
+            rs[pp * K + k] = sC[k] - 0.5 * q;
         }
         __syncthreads();
         if (threadIdx.x < np) {   // normalise point t0 + threadIdx.x (fixed k order)
@@ -231,12 +248,21 @@ __global__ void k_em_out(const double *base, int K, int d, float *w, float *mu, 
     if (threadIdx.x == 0 && ll_out) *ll_out = *s.LL;
 }
 
+template <int MAXS, int DM>
+static cudaError_t launch_estep_d(const float *x, long long n, int d, int K, const double *base, double *part,
+                                  cudaStream_t st) {
+    const size_t smem = sizeof(double) * ((size_t)kEmTile * (d + K) + kEmTile + (size_t)K * (DM * DM + DM + 1));
+    cudaError_t e = cudaFuncSetAttribute(k_em_estep<MAXS, DM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k_em_estep<MAXS, DM><<<kEmBlocks, kEmT, smem, st>>>(x, n, d, K, base, part);
+    return cudaGetLastError();
+}
 template <int MAXS>
 static cudaError_t launch_estep(const float *x, long long n, int d, int K, const double *base, double *part,
                                 cudaStream_t st) {
-    const size_t smem = sizeof(double) * ((size_t)kEmTile * (d + K) + kEmTile);
-    k_em_estep<MAXS><<<kEmBlocks, kEmT, smem, st>>>(x, n, d, K, base, part);
-    return cudaGetLastError();
+    if (d <= 8) return launch_estep_d<MAXS, 8>(x, n, d, K, base, part, st);
+    if (d <= 16) return launch_estep_d<MAXS, 16>(x, n, d, K, base, part, st);
+    return launch_estep_d<MAXS, 32>(x, n, d, K, base, part, st);
 }
 
 // iters EM steps from the start above; the state (em_state_doubles) and partials
