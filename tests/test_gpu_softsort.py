@@ -100,3 +100,23 @@ def test_host_buffers_and_errors(O, ctx):
     with pytest.raises(sk.SinkhornError):
         bad = f.clone(); bad[3] = float("nan")
         sk.sinkhorn_soft_rank_sort(ctx, x.cuda(), y.cuda(), 0.01, bad.cuda(), g.cuda(), y_shared=True)
+
+
+def test_full_c2_batch_sampled(O, ctx):
+    """The bench's launch configuration (BJ.cfg2: 1024 problems of 1024, the default step's solve
+    then K15 on the whole batch): sampled problems against the oracle's soft rank/sort of the
+    oracle's lockstep potentials, with the derived amplification bound of the e2e test."""
+    import paper_2206_07630_b200 as sk
+    c2 = gen.c2()
+    xb, yb = torch.from_numpy(c2.x).cuda(), torch.from_numpy(c2.y).cuda()
+    pot = sk.sinkhorn_init_sort1d(ctx, xb.view(1024, 1024), yb.view(-1))
+    f, g, reps = sk.sinkhorn_solve(ctx, xb, yb, c2.eps, y_shared=True, f_init=pot)
+    rk, st = sk.sinkhorn_soft_rank_sort(ctx, xb.view(1024, 1024), yb.view(-1), c2.eps, f, g, y_shared=True)
+    for k in (0, 511, 1023):
+        lock = O.sinkhorn(c2.x[k], c2.y, c2.eps, tol=0, max_iter=reps[k]["iterations"], f0=pot[k].cpu().numpy())
+        rko, sto = O.soft_rank_sort(c2.x[k].ravel(), c2.y.ravel(), lock.f, lock.g, c2.eps)
+        fc, gc = centred(f[k].cpu().numpy(), g[k].cpu().numpy())
+        foc, goc = centred(lock.f, lock.g)
+        amp = np.expm1(2 * (np.abs(fc - foc).max() + np.abs(gc - goc).max()) / c2.eps)
+        assert np.abs(rk[k].cpu().numpy() - rko).max() <= amp * 1023 + 1e-3, k
+        assert np.abs(st[k].cpu().numpy() - sto).max() <= amp + 1e-5, k
