@@ -39,5 +39,19 @@ sk.sinkhorn_solve(ctx, c(p3.x), c(p3.y), p3.eps, mode="stored", f_init=fg, max_i
 p4 = gen.c4(n=3000, ns=200)
 sk.sinkhorn_init_subsample(ctx, c(p4.x), c(p4.y), c(p4.extra["idx_x"]), c(p4.extra["idx_y"]), p4.eps, 1e-3)
 sk.sinkhorn_solve_sharded_emulated(ctx, 2, c(p4.x), c(p4.y), p4.eps, max_iter=10)
+# relaxation / eps-decay on the on-chip and merge paths, the CTA-pair on-chip variant (C1 size)
+sk.sinkhorn_solve(ctx, c(p1.x), c(p1.y), p1.eps, omega=1.5, eps_decay=(5.0, 0.8), max_iter=30)
+sk.sinkhorn_solve(ctx, c(x), c(y), 0.05, mode="online", omega=1.3, max_iter=12)
+sk.sinkhorn_solve(ctx, c(x), c(y), 0.05, mode="online", eps_decay=(5.0, 0.8), max_iter=14)
+# soft ranks / sort, general 1D initializer, GMM fit, VJP
+fb, gb, _ = sk.sinkhorn_solve(ctx, c(p.x), c(p.y), p.eps, y_shared=True, f_init=f0, max_iter=30)
+sk.sinkhorn_soft_rank_sort(ctx, c(p.x).view(6, 300), c(p.y).view(-1), p.eps, fb, gb, y_shared=True)
+xw = c(rng.random((3, 250)).astype(np.float32)); yw = c(np.sort(rng.random(170)).astype(np.float32))
+sk.sinkhorn_init_nw1d(ctx, xw, yw, a=c(np.stack([gen.random_weights(250, rng) for _ in range(3)])))
+sk.sinkhorn_init_nw1d(ctx, xw, yw)
+sk.sinkhorn_fit_gmm(ctx, c(p3.x), 4, gen.gmm_start_idx(p3.n, 4, 3), iters=3)
+fv, gv, _ = sk.sinkhorn_solve(ctx, c(x), c(y), 0.05, mode="online", max_iter=20)
+sk.sinkhorn_vjp(ctx, c(x), c(y), 0.05, fv, gv, c(rng.standard_normal(1300).astype(np.float32)),
+                c(rng.standard_normal(777).astype(np.float32)), cg_max_iter=10)
 torch.cuda.synchronize()
 print("sanitize smoke ok")
