@@ -58,6 +58,8 @@ def _L():
         lib.ora_sinkhorn_points_omega.argtypes = [I64, I64, I, P, P, P, P, D, D, D, I, I, P, P, P, P, P, P, P]
         lib.ora_sinkhorn_points_decay.restype = I
         lib.ora_sinkhorn_points_decay.argtypes = [I64, I64, I, P, P, P, P, D, D, D, D, D, I, I, P, P, P, P, P, P, P]
+        lib.ora_sinkhorn_points_anderson.restype = I
+        lib.ora_sinkhorn_points_anderson.argtypes = [I64, I64, I, P, P, P, P, D, I, D, I, I, P, P, P, P, P, P]
         lib.ora_sinkhorn_matrix.restype = I
         lib.ora_sinkhorn_matrix.argtypes = [I64, I64, P, P, P, D, D, I, I, P, P, P, P, P, P, P]
         lib.ora_f_update_points.argtypes = [I64, I64, I, P, P, P, P, D, P, P, I64]
@@ -146,6 +148,21 @@ def sinkhorn(x, y, eps, a=None, b=None, tol=1e-3, max_iter=10000, check_every=1,
     if trace:
         r["trace"] = tr[: it.value]
     return r
+
+
+def sinkhorn_anderson(x, y, eps, mem=5, a=None, b=None, tol=1e-3, max_iter=10000, check_every=1, f0=None) -> Result:
+    """Alg. 1 with Anderson acceleration of memory `mem` on the sweep map (R-27):
+    returns the last iterate's pair (f, g_sk(f)) with its explicit error and Eq. (2)."""
+    x, y = _pts(x), _pts(y)
+    n, m, d = x.shape[0], y.shape[0], x.shape[1]
+    a, b = _weights(a, n), _weights(b, m)
+    f, g = np.empty(n), np.empty(m)
+    it, err, E = ctypes.c_int(), ctypes.c_double(), ctypes.c_double()
+    f0a = None if f0 is None else _d(f0)
+    conv = _L().ora_sinkhorn_points_anderson(n, m, d, _p(x), _p(y), _p(a), _p(b), float(eps), int(mem), float(tol),
+                                             int(max_iter), int(check_every), _p(f0a), _p(f), _p(g),
+                                             ctypes.byref(it), ctypes.byref(err), ctypes.byref(E))
+    return Result(f=f, g=g, iterations=it.value, converged=bool(conv), err=err.value, E=E.value)
 
 
 def sinkhorn_matrix(C, eps, a=None, b=None, tol=1e-3, max_iter=10000, check_every=1,

@@ -235,6 +235,84 @@ static int sinkhorn(const ora_prob *p, const double *a, const double *b, double 
     return converged;
 }
 
+/* Anderson acceleration (NEXT-1; "Anderson acceleration (And = 5)"; reading
+ * R-27): type-II Anderson with memory mem on the sweep map T(f) = f_sk(g_sk(f)).  Sweep l:
+ *   g~ = g_sk(f), f~ = T(f) = f_sk(g~);  the iterate's pair (f, g~) has exact columns, so
+ *   err_l = the explicit L1 error of (f, g~) (its row term); stop if err_l < tol (checked when
+ *   l % k == 0 and at l = max_iter);
+ *   r = f~ - f; keep the last mem (f~, r); with >= 2 kept:
+ *   alpha = argmin |R alpha|^2 + lam |alpha|^2 s.t. sum alpha = 1 (lam = 1e-8 tr(R^T R)/cnt, 1 if 0),
+ *   i.e. alpha = x / sum x with (R^T R + lam I) x = 1;  f <- sum_i alpha_i f~_i (else f <- f~).
+ * Returns (f, g~) of the last evaluated sweep. */
+static int sinkhorn_anderson(const ora_prob *p, const double *a, const double *b, double eps, double tol,
+                             int max_iter, int check_every, const double *f0, int mem, double *f, double *g,
+                             int *iters, double *err, double *E) {
+    const int64_t n = p->n, m = p->m;
+    for (int64_t i = 0; i < n; ++i) f[i] = f0 ? f0[i] : 0.0;
+    double *ft = (double *)malloc(sizeof(double) * (size_t)n);
+    double *F = (double *)malloc(sizeof(double) * (size_t)n * mem);
+    double *R = (double *)malloc(sizeof(double) * (size_t)n * mem);
+    double G[16 * 16], x[16];
+    int l = 0, converged = 0, cnt = 0, head = 0;
+    double e = INFINITY;
+    while (l < max_iter) {
+        ++l;
+        g_update(p, b, f, eps, g, NULL, 0);
+        f_update(p, a, g, eps, ft, NULL, 0);
+        if (tol > 0.0 && (l % check_every == 0 || l == max_iter)) {
+            e = marginal_error(p, a, b, f, g, eps);
+            if (e < tol) { converged = 1; break; }
+        }
+        if (l == max_iter) break;
+        for (int64_t i = 0; i < n; ++i) { F[(int64_t)head * n + i] = ft[i]; R[(int64_t)head * n + i] = ft[i] - f[i]; }
+        head = (head + 1) % mem;
+        if (cnt < mem) ++cnt;
+        if (cnt < 2) { for (int64_t i = 0; i < n; ++i) f[i] = ft[i]; continue; }
+        double tr = 0.0;
+        for (int u = 0; u < cnt; ++u)
+            for (int v = 0; v < cnt; ++v) {
+                double s = 0.0;
+                for (int64_t i = 0; i < n; ++i) s += R[(int64_t)u * n + i] * R[(int64_t)v * n + i];
+                G[u * cnt + v] = s;
+                if (u == v) tr += s;
+            }
+        const double lam = tr > 0.0 ? 1e-8 * tr / cnt : 1.0;   /* (all residuals 0: equal weights) */
+        for (int u = 0; u < cnt; ++u) { G[u * cnt + u] += lam; x[u] = 1.0; }
+        for (int c = 0; c < cnt; ++c)        /* Gaussian elimination (SPD: no pivoting) */
+            for (int r = c + 1; r < cnt; ++r) {
+                const double q = G[r * cnt + c] / G[c * cnt + c];
+                for (int k = c; k < cnt; ++k) G[r * cnt + k] -= q * G[c * cnt + k];
+                x[r] -= q * x[c];
+            }
+        for (int r = cnt - 1; r >= 0; --r) {
+            double s = x[r];
+            for (int k = r + 1; k < cnt; ++k) s -= G[r * cnt + k] * x[k];
+            x[r] = s / G[r * cnt + r];
+        }
+        double sx = 0.0;
+        for (int u = 0; u < cnt; ++u) sx += x[u];
+        for (int64_t i = 0; i < n; ++i) {
+            double v = 0.0;
+            for (int u = 0; u < cnt; ++u) v += (x[u] / sx) * F[(int64_t)u * n + i];
+            f[i] = v;
+        }
+    }
+    if (!converged) e = marginal_error(p, a, b, f, g, eps);
+    free(ft); free(F); free(R);
+    *iters = l;
+    *err = e;
+    *E = dual_objective(p, a, b, f, g, eps);
+    return converged;
+}
+
+int ora_sinkhorn_points_anderson(int64_t n, int64_t m, int d, const double *x, const double *y, const double *a,
+                                 const double *b, double eps, int mem, double tol, int max_iter, int check_every,
+                                 const double *f0, double *f, double *g, int *iters, double *err, double *E) {
+    ora_prob p = {n, m, d, x, y, NULL};
+    if (mem < 1 || mem > 16) return -1;
+    return sinkhorn_anderson(&p, a, b, eps, tol, max_iter, check_every, f0, mem, f, g, iters, err, E);
+}
+
 /* Public entry points: point clouds (cost by direct differences) ... */
 int ora_sinkhorn_points(int64_t n, int64_t m, int d, const double *x, const double *y,
                         const double *a, const double *b, double eps, double tol, int max_iter,

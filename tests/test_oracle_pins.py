@@ -665,3 +665,72 @@ def test_nw1d_dual_is_lp_optimal(n, m, weights):
     lp = linprog(C.ravel(), A_eq=A_eq, b_eq=np.concatenate([aa, bb]), bounds=(0, None), method="highs")
     # g on every sink (the c-transform also covers sinks a tree never reached: none for NW)
     assert abs(f @ aa + g @ bb - lp.fun) < 1e-9
+
+
+# ------------------------------------------------- Anderson acceleration (NEXT-1, R-27)
+def test_anderson_memory_one_is_plain_sinkhorn():
+    """mem = 1 keeps no second residual, so f^{l+1} = T(f^l): sweep L returns (f^{L-1},
+    g_sk(f^{L-1})), i.e. the plain solver's f after L - 1 sweeps and its g after L."""
+    from oracle import oracle as O
+    p = gen.c1(n=60, seed=8)
+    f0 = np.linspace(-0.1, 0.1, 60)
+    for L in (1, 2, 7):
+        r = O.sinkhorn_anderson(p.x, p.y, p.eps, mem=1, tol=0, max_iter=L, f0=f0)
+        q = O.sinkhorn(p.x, p.y, p.eps, tol=0, max_iter=L, f0=f0)
+        fq = f0 if L == 1 else O.sinkhorn(p.x, p.y, p.eps, tol=0, max_iter=L - 1, f0=f0).f
+        assert np.abs(r.g - q.g).max() < 1e-12 and np.abs(r.f - fq).max() < 1e-12 and r.iterations == L
+
+
+def test_anderson_mixing_step_is_the_constrained_least_squares_combination():
+    """One mixing step checked against an independent solution of min |sum_u alpha_u r_u|^2 +
+    lam |alpha|^2 s.t. sum alpha = 1 (alpha_0 = 1 - sum gamma, unconstrained lstsq in gamma on
+    the stacked system [R; sqrt(lam) I]; the oracle solves the normal equations), with the map
+    T(f) = f_sk(g_sk(f)) taken from single plain sweeps (R-27)."""
+    from oracle import oracle as O
+    p = gen.c1(n=50, seed=9)
+    T = lambda f: O.sinkhorn(p.x, p.y, p.eps, tol=0, max_iter=1, f0=f)
+    f0 = np.zeros(50)
+    for mem, L in ((3, 4), (5, 4), (2, 5)):
+        fs, Fs = [f0], []
+        for l in range(L - 1):            # sweeps 1..L-1 each mix; sweep L returns (f^{L-1}, g~)
+            Fs.append(T(fs[-1]).f)
+            Rk = [Fs[u] - fs[u] for u in range(len(Fs))][-mem:]
+            Fk = Fs[-mem:]
+            if len(Rk) < 2:
+                fs.append(Fk[-1])
+                continue
+            # the Tikhonov term lam |alpha|^2 (lam = 1e-8 tr(R^T R)/cnt) as extra rows sqrt(lam) I
+            k = len(Rk)
+            lam = 1e-8 * sum(float(r @ r) for r in Rk) / k
+            Ra = np.concatenate([np.stack(Rk, 1), np.sqrt(lam) * np.eye(k)], 0)
+            R0, D = Ra[:, 0], Ra[:, 1:] - Ra[:, :1]
+            gam = np.linalg.lstsq(D, -R0, rcond=None)[0]
+            alpha = np.concatenate([[1 - gam.sum()], gam])
+            fs.append(sum(al * F for al, F in zip(alpha, Fk)))
+        r = O.sinkhorn_anderson(p.x, p.y, p.eps, mem=mem, tol=0, max_iter=L, f0=f0)
+        scale = np.abs(fs[-1]).max()
+        assert np.abs(r.f - fs[-1]).max() < 1e-9 * scale, (mem, L)
+        assert np.abs(r.g - T(fs[-1]).g).max() < 1e-9 * scale
+
+
+def test_anderson_reaches_the_sinkhorn_optimum_with_explicit_error():
+    """Anderson's fixed points are T's: the converged pair is the plain optimum (centred), its
+    err is the explicit plan error (columns exact), and on C1 it needs fewer sweeps."""
+    from oracle import oracle as O
+    p = gen.c1(n=40, seed=10, eps_factor=0.1)
+    ref = O.sinkhorn(p.x, p.y, p.eps, tol=1e-11, max_iter=100000)
+    r = O.sinkhorn_anderson(p.x, p.y, p.eps, mem=5, tol=1e-11, max_iter=100000)
+    assert r.converged and r.err < 1e-11
+    fr = ref.f - ref.f.mean()
+    assert np.abs((r.f - r.f.mean()) - fr).max() < 1e-8 * max(1.0, np.abs(fr).max())
+    assert abs(r.E - ref.E) < 1e-10 * max(1.0, abs(ref.E))
+    s = O.sinkhorn_anderson(p.x, p.y, p.eps, mem=4, tol=0, max_iter=6)
+    x, y = p.x.astype(np.float64), p.y.astype(np.float64)
+    C = ((x[:, None, :] - y[None, :, :]) ** 2).sum(-1)
+    P = np.exp((s.f[:, None] + s.g[None, :] - C) / p.eps)
+    n, m = C.shape
+    assert np.abs(P.sum(0) - 1 / m).max() < 1e-13   # g = g_sk(f): exact columns
+    err = np.abs(P.sum(1) - 1 / n).sum()
+    assert abs(s.err - err) < 1e-12 * max(1.0, err) and err > 1e-6
+    q = gen.c1()
+    assert O.sinkhorn_anderson(q.x, q.y, q.eps, mem=5).iterations < O.sinkhorn(q.x, q.y, q.eps).iterations / 3
