@@ -123,6 +123,19 @@ sk_status sk_set_relaxation(sk_ctx *ctx, float omega);
  * must lie in (0, 1) (SK_EINVAL).  On the multi-kernel paths it needs omega = 1
  * (SK_EUNSUPPORTED otherwise) and max_iter > T; the sharded entries return SK_EUNSUPPORTED. */
 sk_status sk_set_eps_decay(sk_ctx *ctx, float init, float rate);
+/* Anderson acceleration ("Anderson acceleration (And = 5)"; R-27) for
+ * the following solves on this context: type-II Anderson with memory mem on the sweep map
+ * T(f) = f_sk(g_sk(f)).  Sweep l evaluates g~ = g_sk(f^l) and T(f^l); err_l is the L1 error of
+ * the pair (f^l, g~) (its columns are exact: err_l = sum_i a_i |expm1((f^l_i - T(f^l)_i)/eps)|),
+ * checked when l % check_every == 0 and at l = max_iter; then f^{l+1} = sum_u alpha_u T(f_u)
+ * over the last mem sweeps, alpha = argmin |R alpha|^2 + lam |alpha|^2 subject to
+ * sum alpha = 1 (R = residuals T(f_u) - f_u, lam = 1e-8 tr(R^T R) / count, or 1 when all
+ * residuals are 0).  The result is
+ * (f^l, g~) of the last sweep and rep.iterations the sweeps evaluated.  mem in {0, 1}: off (the
+ * default); mem in [2, 8]: on; otherwise SK_EINVAL.  Runs on the on-chip solver (problems
+ * sinkhorn_solve routes to it: B > 1 or n m <= 2^18, with room in shared memory); other paths,
+ * omega != 1 and eps-decay return SK_EUNSUPPORTED. */
+sk_status sk_set_anderson(sk_ctx *ctx, int32_t mem);
 /* Enable (1) / disable (0) CUDA-event timing of the dominant kernels into sk_counters. */
 sk_status sk_set_timing(sk_ctx *ctx, int32_t enable);
 sk_status sk_get_counters(const sk_ctx *ctx, sk_counters *out /* host */);

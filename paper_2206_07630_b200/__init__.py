@@ -198,11 +198,19 @@ def sinkhorn_init_subsample(ctx: Context, x, y, idx_x, idx_y, eps: float, inner_
 def sinkhorn_solve(ctx: Context, x, y, eps: float, tol: float = 1e-3, max_iter: int = 10000,
                    check_every: int = 1, a=None, b=None, y_shared: bool = False, mode: str = "auto",
                    f_init=None, g_init=None, f=None, g=None, allow_nonfinite: bool = False,
-                   omega: float = 1.0, eps_decay=None):
+                   omega: float = 1.0, eps_decay=None, anderson: int = 0):
     """Solve B >= 1 problems.  x: (n, d) or (B, n, d); y: (m, d) [shared] or (B, m, d).
     omega: Alg. 1's relaxation (sk_set_relaxation; 1 = plain Sinkhorn).
     eps_decay: (init, rate) for sk_set_eps_decay (e.g. (5, 0.8), P:491), None = off.
+    anderson: Anderson memory for sk_set_anderson (e.g. 5), 0 = off.
     Returns (f, g, reports) with f (B, n) / g (B, m) (B dropped for a single problem)."""
+    if anderson:
+        ctx.check(ctx.lib.sk_set_anderson(ctx.h, int(anderson)))
+        try:
+            return sinkhorn_solve(ctx, x, y, eps, tol, max_iter, check_every, a, b, y_shared, mode,
+                                  f_init, g_init, f, g, allow_nonfinite, omega, eps_decay)
+        finally:
+            ctx.lib.sk_set_anderson(ctx.h, 0)
     if eps_decay is not None:
         ctx.check(ctx.lib.sk_set_eps_decay(ctx.h, ctypes.c_float(eps_decay[0]), ctypes.c_float(eps_decay[1])))
         try:

@@ -75,6 +75,7 @@ struct sk_ctx {
     std::vector<cudaEvent_t> tev;   // per-launch timing events of the dominant kernel (pool)
     float omega = 1.f;              // Alg. 1's relaxation for the following solves
     float decay_init = 0.f, decay_rate = 1.f;   // eps-decay for the following solves (R-25)
+    int anderson = 0;               // Anderson memory for the following solves (R-27; 0: off)
 };
 
 namespace {
@@ -302,6 +303,8 @@ struct LaunchTimer {
 };
 
 sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, sk_report *rep) {
+    if (ctx->anderson >= 2)
+        return fail(ctx, SK_EUNSUPPORTED, "Anderson acceleration runs on the on-chip solver only (small problems)");
     cudaStream_t st = ctx->stream;
     LaunchTimer tm(ctx);
     const bool sharded = P.world > 1;
@@ -706,6 +709,13 @@ sk_status sk_set_eps_decay(sk_ctx *ctx, float init, float rate) {
         return fail(ctx, SK_EINVAL, "eps-decay needs init > 1 (finite) and rate in (0, 1)");
     ctx->decay_init = init;
     ctx->decay_rate = rate;
+    return SK_OK;
+}
+
+sk_status sk_set_anderson(sk_ctx *ctx, int32_t mem) {
+    if (!ctx) return SK_EINVAL;
+    if (mem < 0 || mem > 8) return fail(ctx, SK_EINVAL, "Anderson memory must lie in [0, 8], got %d", (int)mem);
+    ctx->anderson = mem >= 2 ? mem : 0;
     return SK_OK;
 }
 
@@ -1181,7 +1191,10 @@ sk_status solve_impl(sk_ctx *ctx, int64_t B, int64_t n, int64_t m, int32_t d, co
                      float eps, float tol, int32_t max_iter, int32_t check_every, sk_cost_mode mode,
                      const float *f_init, float *f, float *g, sk_report *rep) {
     cudaStream_t st = ctx->stream;
-    const bool small = batched_supported(d, (int)n, (int)m) && (B > 1 || (double)n * m <= (double)(1 << 18));
+    const bool small = batched_supported(d, (int)n, (int)m, ctx->anderson) &&
+                       (B > 1 || (double)n * m <= (double)(1 << 18));
+    if (ctx->anderson >= 2 && (ctx->omega != 1.f || ctx->decay_init > 0.f))
+        return fail(ctx, SK_EUNSUPPORTED, "Anderson acceleration combines with neither omega != 1 nor eps-decay");
     if (small && mode != SK_COST_STORED) {
         ENSURE(rp, char, B_REP, (size_t)B * (3 * sizeof(int) + sizeof(float) + sizeof(double)) + 64);
         ENSURE(queue, int, B_QUEUE, 4);
@@ -1197,6 +1210,7 @@ sk_status solve_impl(sk_ctx *ctx, int64_t B, int64_t n, int64_t m, int32_t d, co
         L.iters = iters; L.conv = conv; L.nonfinite = nonf; L.err = err; L.E = E;
         L.omega = ctx->omega;
         L.decay_init = ctx->decay_init; L.decay_rate = ctx->decay_rate;
+        L.anderson = ctx->anderson;
         CU(cudaEventRecord(ctx->ev0, st));
         CU(launch_batched(L, st));
         CU(cudaEventRecord(ctx->ev1, st));
@@ -1220,8 +1234,9 @@ sk_status solve_impl(sk_ctx *ctx, int64_t B, int64_t n, int64_t m, int32_t d, co
             rep[p].build_ms = 0.0;
             rep[p].solve_ms = ms;
             any_nf |= hn[p];
-            ctx->cnt.lse_ex2 += (double)n * m * (2.0 * hi[p] + 1.0);
-            if (ctx->timing) ctx->cnt.dom_entries += (double)n * m * (2.0 * hi[p] + 1.0);
+            const double passes = 2.0 * hi[p] + (ctx->anderson >= 2 ? 0.0 : 1.0);   // (Anderson: 2 per sweep)
+            ctx->cnt.lse_ex2 += (double)n * m * passes;
+            if (ctx->timing) ctx->cnt.dom_entries += (double)n * m * passes;
         }
         if (any_nf) return fail(ctx, SK_ENONFINITE, "potentials became non-finite");
         return SK_OK;

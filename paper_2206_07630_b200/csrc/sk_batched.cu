@@ -37,17 +37,43 @@ struct BatchArgs {
     double *E;
     float omega;                    // Alg. 1's relaxation (1 = plain Sinkhorn)
     float decay_init, decay_rate;   // eps-decay (decay_init <= 0: off)
+    int anderson;                   // Anderson memory (R-27; < 2: off)
 };
 
 __host__ __device__ inline int round_up(int v, int a) { return (v + a - 1) / a * a; }
 
-size_t batched_smem_bytes(int D, int n, int m) {
+constexpr int kRedDoubles = 96;       // reduction scratch (block sums, flags, pair exchange)
+constexpr int kAndMax = 8;            // largest Anderson memory
+constexpr int kAndDoubles = 2 * kAndMax * kAndMax + kAndMax + 32 * (kAndMax + 2);   // G, solve, alpha, partials
+
+size_t batched_smem_bytes(int D, int n, int m, int mem) {
     const int Np = round_up(n, kChunk), Mp = round_up(m, kChunk);
     size_t floats = (size_t)(D + 1) * (Np + Mp)   // packed coords + w, both sides
                     + 2 * (size_t)(n + m)         // finalize constant c and ||.||^2 kappa
                     + 2 * (size_t)(n + m)         // double-buffered f and g
-                    + (size_t)(n + m);            // last running max per point (seed)
-    return floats * sizeof(float) + 64 * sizeof(double);
+                    + (size_t)(n + m) + 2;        // last running max per point (seed), alignment
+    size_t bytes = floats * sizeof(float) + kRedDoubles * sizeof(double);
+    if (mem >= 2) bytes += kAndDoubles * sizeof(double) + 2 * (size_t)mem * n * sizeof(float);   // + T(f), residuals
+    return bytes;
+}
+
+// Fixed-order block sums of v[0..k) (k <= kAndMax + 2); all threads get the results in v.
+template <int NT>
+__device__ __forceinline__ void block_sum_vec(double *v, int k, double *scratch /* 32 x (kAndMax+2) */) {
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    for (int u = 0; u < k; ++u) {
+        double t = v[u];
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        if (l == 0) scratch[w * (kAndMax + 2) + u] = t;
+    }
+    __syncthreads();
+    for (int u = 0; u < k; ++u) {
+        double t = 0.0;
+#pragma unroll
+        for (int i = 0; i < NT / 32; ++i) t += scratch[i * (kAndMax + 2) + u];
+        v[u] = t;
+    }
 }
 
 constexpr float kSeedMargin = 4.f;   // log2 units added to the previous sweep's max
@@ -152,7 +178,15 @@ __device__ __forceinline__ void solve_one(const BatchArgs &A, int prob, float *s
     float *mys = mxs + n;               // [m]    (y side, column pass)
     double *red = reinterpret_cast<double *>(mys + m + ((n + m) & 1));  // scratch
     int *redi = reinterpret_cast<int *>(red + 32);
-    double *xr = red + 48;              // [2 ranks][8] exchanged block partials (CL = 2)
+    double *xr = red + 48;              // [2 ranks][16] exchanged block partials (CL = 2)
+    // Anderson (R-27): Gram matrix of the residuals, mixing weights, partials; T(f) and residuals
+    const int am = A.anderson >= 2 ? A.anderson : 0;
+    double *Gm = red + kRedDoubles;     // [kAndMax][kAndMax]
+    double *Gs = Gm + kAndMax * kAndMax;   // [kAndMax][kAndMax] the regularized system (eliminated)
+    double *al = Gs + kAndMax * kAndMax;
+    double *vred = al + kAndMax;        // [32][kAndMax + 2]
+    float *Fh = reinterpret_cast<float *>(vred + 32 * (kAndMax + 2));   // [am][n]
+    float *Rh = Fh + (size_t)am * n;                                    // [am][n]
     // this CTA's output ranges (CL = 2: halves, aligned to R * NT rounds)
     const int hn = CL > 1 ? (n + 1) / 2 : n, hm = CL > 1 ? (m + 1) / 2 : m;
     const int i0 = CL > 1 ? (int)rank * hn : 0, i1 = CL > 1 ? min(n, i0 + hn) : n;
@@ -162,15 +196,15 @@ __device__ __forceinline__ void solve_one(const BatchArgs &A, int prob, float *s
         if constexpr (CL > 1) cl_st(peer_base + (smem_u32(loc) - smem_u32(sm)), v);
     };
     // sum of this CTA's block partial v[k] with the peer's (fixed order: rank 0 + rank 1)
-    auto xsum = [&](double (&v)[4], int cnt) {
+    auto xsum = [&](double *v, int cnt) {
         if constexpr (CL > 1) {
             if (threadIdx.x == 0)
                 for (int k = 0; k < cnt; ++k) {
-                    xr[rank * 8 + k] = v[k];
-                    cl_st(peer_base + (smem_u32(&xr[rank * 8 + k]) - smem_u32(sm)), v[k]);
+                    xr[rank * 16 + k] = v[k];
+                    cl_st(peer_base + (smem_u32(&xr[rank * 16 + k]) - smem_u32(sm)), v[k]);
                 }
             cl_sync();
-            for (int k = 0; k < cnt; ++k) v[k] = xr[k] + xr[8 + k];
+            for (int k = 0; k < cnt; ++k) v[k] = xr[k] + xr[16 + k];
             cl_sync();   // (xr reusable)
         }
     };
@@ -227,6 +261,8 @@ __device__ __forceinline__ void solve_one(const BatchArgs &A, int prob, float *s
     __syncthreads();
 
     int l = 0, cur = 0, conv = 0, nonfin = 0;
+    int a_cnt = 0, a_head = 0;   // Anderson history: filled slots, next slot
+    bool out_gtilde = false;     // Anderson: the result is (f^l, g_sk(f^l)) (the g buffer not flipped)
     float err = INFINITY;
     const float om = A.omega;
     const bool relaxed = om != 1.f;
@@ -269,7 +305,7 @@ __device__ __forceinline__ void solve_one(const BatchArgs &A, int prob, float *s
         }
         const bool seeded = l >= 1 && fresh;
         // ---- column pass: g^{l+1} (P = y, Q = x)
-        const bool check = l > T && ((l - T) % A.check_every == 0 || l == A.max_iter);
+        const bool check = !am && l > T && ((l - T) % A.check_every == 0 || l == A.max_iter);
         double e_loc = 0.0;
         int bad = 0;
         float *gold = gb + cur * m, *gnew = gb + (cur ^ 1) * m;
@@ -295,11 +331,87 @@ __device__ __forceinline__ void solve_one(const BatchArgs &A, int prob, float *s
             err = (float)(cv[0] + row_err);   // (row_err = 0 unless relaxed)
             if (err < A.tol) { conv = 1; break; }
         }
-        if (l >= A.max_iter) break;   // (also when max_iter <= T: no sweep is checked)
+        if (!am && l >= A.max_iter) break;   // (also when max_iter <= T: no sweep is checked)
         // ---- row pass: f^{l+1} (P = x, Q = y); wy is visible after the reductions' barriers
         float *fnew = fb + (cur ^ 1) * n;
         const float *fold = fb + cur * n;
         bad = 0;
+        if (am) {
+            // Anderson (R-27): sweep l + 1 of the map T(f) = f_sk(g_sk(f)).  The
+            // pair (f^l, g~) has exact columns: err = sum_i a_i |expm1((f_i - T(f)_i)/eps)|.
+            const bool check_a = (l + 1) % A.check_every == 0 || l + 1 == A.max_iter;
+            const int cn = a_cnt < am ? a_cnt + 1 : am;   // slots after this push
+            double dv[kAndMax], e_row = 0.0;
+#pragma unroll
+            for (int u = 0; u < kAndMax; ++u) dv[u] = 0.0;
+            onchip_pass<D, R, NT, EMU>(xq, Np, i0, i1, yq, wy, Mp, tk, mxs, seeded, [&](int i, float Mv, float Sv) {
+                const float fsk = cx[i] - epsln2 * (Mv + log2f(Sv));
+                const float r = fsk - fold[i];
+                bad |= !isfinite(fsk);
+                if (check_a) e_row += (a ? (double)a[i] : 1.0 / n) * fabs((double)expm1f(-r / eps));
+                Fh[(size_t)a_head * n + i] = fsk;
+#pragma unroll
+                for (int u = 0; u < kAndMax; ++u)
+                    if (u < cn) dv[u] += (double)r * (double)(u == a_head ? r : Rh[(size_t)u * n + i]);
+                Rh[(size_t)a_head * n + i] = r;
+            });
+            double vv[kAndMax + 2];   // cn dots, the error, the non-finite flag
+#pragma unroll
+            for (int u = 0; u < kAndMax; ++u) vv[u] = dv[u];
+            vv[cn] = e_row;
+            vv[cn + 1] = (double)bad;
+            block_sum_vec<NT>(vv, cn + 2, vred);
+            xsum(vv, cn + 2);
+            const double *dv_s = vv;
+            if (dv_s[cn + 1] != 0.0) { nonfin = 1; break; }
+            if (check_a) {
+                err = (float)dv_s[cn];
+                if (err < A.tol) { conv = 1; out_gtilde = true; break; }
+            }
+            if (l + 1 >= A.max_iter) { out_gtilde = true; break; }
+            if (threadIdx.x == 0) {   // Gram row/column of the new slot; alpha from (G + lam I) x = 1
+                for (int u = 0; u < cn; ++u) Gm[a_head * kAndMax + u] = Gm[u * kAndMax + a_head] = dv_s[u];
+                double *xs = al, tr = 0.0;
+                for (int u = 0; u < cn; ++u) tr += Gm[u * kAndMax + u];
+                const double lam = tr > 0.0 ? 1e-8 * tr / cn : 1.0;   // (all residuals 0: equal weights)
+                for (int u = 0; u < cn; ++u) {
+                    for (int v = 0; v < cn; ++v) Gs[u * cn + v] = Gm[u * kAndMax + v];
+                    Gs[u * cn + u] += lam;
+                    xs[u] = 1.0;
+                }
+                for (int c = 0; c < cn; ++c)
+                    for (int rr = c + 1; rr < cn; ++rr) {
+                        const double q = Gs[rr * cn + c] / Gs[c * cn + c];
+                        for (int k = c; k < cn; ++k) Gs[rr * cn + k] -= q * Gs[c * cn + k];
+                        xs[rr] -= q * xs[c];
+                    }
+                for (int rr = cn - 1; rr >= 0; --rr) {
+                    double t = xs[rr];
+                    for (int k = rr + 1; k < cn; ++k) t -= Gs[rr * cn + k] * xs[k];
+                    xs[rr] = t / Gs[rr * cn + rr];
+                }
+                double sx = 0.0;
+                for (int u = 0; u < cn; ++u) sx += xs[u];
+                for (int u = 0; u < cn; ++u) al[u] = xs[u] / sx;   // (in place)
+            }
+            a_head = (a_head + 1) % am;
+            a_cnt = cn;
+            __syncthreads();
+            for (int i = i0 + threadIdx.x; i < i1; i += NT) {   // f^{l+1} = sum_u alpha_u T(f_u)
+                double v = 0.0;
+                for (int u = 0; u < cn; ++u) v += al[u] * (double)Fh[(size_t)u * n + i];
+                const float fn = (float)v;
+                const float wv = fmaf(fn, kap, -nxk[i]);
+                fnew[i] = fn;
+                wx[i] = wv;
+                rput(&fnew[i], fn);
+                rput(&wx[i], wv);
+            }
+            if constexpr (CL > 1) cl_sync(); else __syncthreads();
+            cur ^= 1;
+            ++l;
+            continue;
+        }
         double r_loc = 0.0, m_loc = 0.0;
         onchip_pass<D, R, NT, EMU>(xq, Np, i0, i1, yq, wy, Mp, tk, mxs, seeded, [&](int i, float Mv, float Sv) {
             const float fsk = cx[i] - epsln2 * (Mv + log2f(Sv));
@@ -330,7 +442,7 @@ __device__ __forceinline__ void solve_one(const BatchArgs &A, int prob, float *s
     }
 
     // ---- epilogue: (f^l, g^l), E = <f,a> + <g,b> - eps sum(a) (Eq. 2 after an f-update), report
-    const float *fo = fb + cur * n, *go = gb + cur * m;
+    const float *fo = fb + cur * n, *go = gb + (out_gtilde ? cur ^ 1 : cur) * m;
     double s = 0.0;
     for (int i = i0 + threadIdx.x; i < i1; i += NT) {
         A.f[(size_t)prob * n + i] = fo[i];
@@ -345,7 +457,7 @@ __device__ __forceinline__ void solve_one(const BatchArgs &A, int prob, float *s
     xsum(ev, 1);
     const double E = ev[0] - (double)eps * mass_dev;   // relaxed: sum P != sum a
     if (threadIdx.x == 0 && rank == 0) {
-        A.iters[prob] = l;
+        A.iters[prob] = am ? l + 1 : l;   // (Anderson: sweeps evaluated, as the oracle counts)
         A.conv[prob] = conv;
         A.nonfinite[prob] = nonfin;
         A.err[prob] = err;
@@ -391,7 +503,7 @@ static int batched_emu() {
 
 template <int D, int R, int NT, int EMU, int CL>
 static cudaError_t launch_batched_c(const BatchArgs &A, int B, cudaStream_t st) {
-    const size_t smem = batched_smem_bytes(D, A.n, A.m);
+    const size_t smem = batched_smem_bytes(D, A.n, A.m, A.anderson);
     cudaError_t e = cudaFuncSetAttribute(k_batched<D, R, NT, EMU, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
@@ -455,8 +567,8 @@ static cudaError_t launch_batched_d(const BatchArgs &A, int B, cudaStream_t st) 
     return launch_batched_e<D, 2, 1024, 1>(A, B, st);  // more rounds of 2048 points for larger P
 }
 
-bool batched_supported(int d, int n, int m) {
-    return d >= 1 && d <= 4 && batched_smem_bytes(d, n, m) <= 200 * 1024;
+bool batched_supported(int d, int n, int m, int mem) {
+    return d >= 1 && d <= 4 && mem <= kAndMax && batched_smem_bytes(d, n, m, mem) <= 200 * 1024;
 }
 
 cudaError_t launch_batched(const BatchLaunch &L, cudaStream_t st) {
@@ -474,6 +586,7 @@ cudaError_t launch_batched(const BatchLaunch &L, cudaStream_t st) {
     A.iters = L.iters; A.conv = L.conv; A.nonfinite = L.nonfinite; A.err = L.err; A.E = L.E;
     A.omega = L.omega;
     A.decay_init = L.decay_init; A.decay_rate = L.decay_rate;
+    A.anderson = L.anderson;
     switch (L.d) {
         case 1: return launch_batched_d<1>(A, L.B, st);
         case 2: return launch_batched_d<2>(A, L.B, st);

@@ -23,8 +23,9 @@ struct BatchLaunch {
     double *E;
     float omega = 1.f;   // Alg. 1's relaxation
     float decay_init = 0.f, decay_rate = 1.f;   // eps-decay (R-25; decay_init <= 0: off)
+    int anderson = 0;    // Anderson memory (R-27; < 2: off)
 };
-bool batched_supported(int d, int n, int m);
+bool batched_supported(int d, int n, int m, int mem = 0);
 // K18 general 1D initializer (NW corner + Alg. 3/4, R-26) on sorted supports
 size_t nw1d_smem_bytes(int n, int m);
 cudaError_t launch_nw1d(const float *xs, const int *xperm, const float *ys, const int *yperm, int y_shared,
@@ -47,7 +48,7 @@ size_t soft_rank_sort_smem(int n, int m);
 cudaError_t launch_soft_rank_sort(long long B, int n, int m, const float *x, const float *y, long long ys,
                                   const float *f, const float *g, const float *z, float eps, float *rank,
                                   float *sort, cudaStream_t st);
-size_t batched_smem_bytes(int D, int n, int m);
+size_t batched_smem_bytes(int D, int n, int m, int mem = 0);
 cudaError_t launch_batched(const BatchLaunch &L, cudaStream_t st);
 
 // ------------------------------------------------- multi-kernel online path
