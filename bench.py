@@ -119,11 +119,11 @@ class C2(Workload):
                 "parallelism": f"dp{self.world} (independent problems per rank)",
                 "l2": "flushed (256 MiB write) before every timed step"}
 
-    def _run(self, x, y, init=True):
+    def _run(self, x, y, init=True, anderson=0):
         sk, p = self.sk, self.p
         f0 = sk.sinkhorn_init_sort1d(self.ctx, x.view(self.B, self.n), y.view(self.m), y_shared=True) if init else None
         self.f, self.g, reps = sk.sinkhorn_solve(self.ctx, x, y, p.eps, tol=p.tol, max_iter=p.max_iter,
-                                                 y_shared=True, f_init=f0)
+                                                 y_shared=True, f_init=f0, anderson=anderson)
         self.its = np.array([r["iterations"] for r in reps])
         return float(self.n) * self.m * float(self.its.sum())
 
@@ -162,6 +162,17 @@ class C2(Workload):
         out["soft_rank_sort"] = {"ms": ms, "ex2_per_s": ex2 / (ms / 1e3),
                                  "mufu_frac": ex2 / (ms / 1e3) / (N_SM * MUFU_EX2_PER_CLK_SM * 1965e6),
                                  "note": "K15: ranks E_P[z|i] and sort E_P[x|j] of the 1024-problem batch (R-22)"}
+        # NEXT-1: the same step (sort1d init + solve to tol) with Anderson acceleration (m = 5, R-27)
+        self._run(self.x, self.y, anderson=5)
+        e0.record(st)
+        for _ in range(3):
+            ent = self._run(self.x, self.y, anderson=5)
+        e1.record(st)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / 3
+        out["anderson5"] = {"time_to_tol_ms": ms, "iterations_mean": float(self.its.mean()),
+                            "iterations_max": int(self.its.max()), "cost_entries_per_s": ent / (ms / 1e3),
+                            "note": "sort1d init + Anderson (memory 5) to the same tol; entries = n m sweeps"}
         return out
 
     kernel = "k_batched<1,2,512> (on-chip persistent solver, K13)"
@@ -269,7 +280,7 @@ class Single(Workload):
             f0 = None
         return f0
 
-    def _run(self, x, y, init=True):
+    def _run(self, x, y, init=True, anderson=0):
         import torch
         sk, p = self.sk, self.p
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
@@ -283,7 +294,7 @@ class Single(Workload):
                                                   max_iter=p.max_iter, mode=self.mode, f_init_local=f0l)
         else:
             _, _, rep = sk.sinkhorn_solve(self.ctx, x, y, p.eps, tol=p.tol, max_iter=p.max_iter, mode=self.mode,
-                                          f_init=f0)
+                                          f_init=f0, anderson=anderson)
         ev[2].record()
         ev[2].synchronize()
         self.split_ms = {"init_ms": ev[0].elapsed_time(ev[1]), "solve_call_ms": ev[1].elapsed_time(ev[2]),
@@ -311,6 +322,17 @@ class Single(Workload):
                "last_step_split_ms": getattr(self, "split_ms", None)}
         if hasattr(self, "inner"):
             out["subsample_inner_iterations"] = self.inner["iterations"]
+        if self.name == "c1" and not self.sharded:   # NEXT-1: Anderson (memory 5, R-27) on the same step
+            import torch
+            self._run(self.x, self.y, anderson=5)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(5):
+                self._run(self.x, self.y, anderson=5)
+            e1.record()
+            torch.cuda.synchronize()
+            out["anderson5"] = {"time_to_tol_ms": e0.elapsed_time(e1) / 5, "iterations": self.rep["iterations"],
+                                "note": "same init + Anderson (memory 5) to the same tol"}
         return out
 
     def cpu_sample(self, target_s=10.0):

@@ -42,9 +42,10 @@ struct BatchArgs {
 
 __host__ __device__ inline int round_up(int v, int a) { return (v + a - 1) / a * a; }
 
-constexpr int kRedDoubles = 96;       // reduction scratch (block sums, flags, pair exchange)
+constexpr int kRedW = 4;              // values per pass reduction (error, flag, relaxed row terms)
+constexpr int kRedDoubles = 2 * 32 * kRedW + 2 * 2 * 16;   // double-buffered partials, pair exchange
 constexpr int kAndMax = 8;            // largest Anderson memory
-constexpr int kAndDoubles = 2 * kAndMax * kAndMax + kAndMax + 32 * (kAndMax + 2);   // G, solve, alpha, partials
+constexpr int kAndDoubles = kAndMax * kAndMax + 2 * 32 * (kAndMax + 2);   // Gram matrix, partials
 
 size_t batched_smem_bytes(int D, int n, int m, int mem) {
     const int Np = round_up(n, kChunk), Mp = round_up(m, kChunk);
@@ -57,22 +58,37 @@ size_t batched_smem_bytes(int D, int n, int m, int mem) {
     return bytes;
 }
 
-// Fixed-order block sums of v[0..k) (k <= kAndMax + 2); all threads get the results in v.
-template <int NT>
-__device__ __forceinline__ void block_sum_vec(double *v, int k, double *scratch /* 32 x (kAndMax+2) */) {
+// Fixed-order block sums of v[0..k) (k <= ST); all threads get the results in v.  The
+// partials alternate between two scratch halves (par), so one barrier per reduction suffices:
+// reduction r + 2 rewrites a half only after every thread has passed reduction r + 1's
+// barrier, i.e. finished reading reduction r.  The barrier also orders the pass's shared-memory
+// writes before the next pass's reads.
+template <int NT, int ST>
+__device__ __forceinline__ void block_red(double *v, int k, double *scratch /* 2 x 32 x ST */, int &par) {
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-    __syncthreads();
-    for (int u = 0; u < k; ++u) {
-        double t = v[u];
-        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-        if (l == 0) scratch[w * (kAndMax + 2) + u] = t;
+    double *sc = scratch + par * 32 * ST;
+    par ^= 1;
+    double t[ST];
+#pragma unroll
+    for (int u = 0; u < ST; ++u) t[u] = u < k ? v[u] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)   // (level by level: the k shuffles of a level overlap)
+#pragma unroll
+        for (int u = 0; u < ST; ++u)
+            if (u < k) t[u] += __shfl_xor_sync(0xffffffffu, t[u], o);
+    if (l == 0) {
+#pragma unroll
+        for (int u = 0; u < ST; ++u)
+            if (u < k) sc[w * ST + u] = t[u];
     }
     __syncthreads();
-    for (int u = 0; u < k; ++u) {
-        double t = 0.0;
 #pragma unroll
-        for (int i = 0; i < NT / 32; ++i) t += scratch[i * (kAndMax + 2) + u];
-        v[u] = t;
+    for (int u = 0; u < ST; ++u) {
+        if (u >= k) continue;
+        double a = 0.0;
+#pragma unroll
+        for (int i = 0; i < NT / 32; ++i) a += sc[i * ST + u];
+        v[u] = a;
     }
 }
 
@@ -177,15 +193,13 @@ __device__ __forceinline__ void solve_one(const BatchArgs &A, int prob, float *s
     float *mxs = gb + 2 * m;            // [n]    last running max (x side, row pass)
     float *mys = mxs + n;               // [m]    (y side, column pass)
     double *red = reinterpret_cast<double *>(mys + m + ((n + m) & 1));  // scratch
-    int *redi = reinterpret_cast<int *>(red + 32);
-    double *xr = red + 48;              // [2 ranks][16] exchanged block partials (CL = 2)
+    double *xr = red + 2 * 32 * kRedW;  // [2 halves][2 ranks][16] exchanged block partials (CL = 2)
+    int rpar = 0, xpar = 0;             // the halves the next reductions use
     // Anderson (R-27): Gram matrix of the residuals, mixing weights, partials; T(f) and residuals
     const int am = A.anderson >= 2 ? A.anderson : 0;
     double *Gm = red + kRedDoubles;     // [kAndMax][kAndMax]
-    double *Gs = Gm + kAndMax * kAndMax;   // [kAndMax][kAndMax] the regularized system (eliminated)
-    double *al = Gs + kAndMax * kAndMax;
-    double *vred = al + kAndMax;        // [32][kAndMax + 2]
-    float *Fh = reinterpret_cast<float *>(vred + 32 * (kAndMax + 2));   // [am][n]
+    double *vred = Gm + kAndMax * kAndMax;   // [2][32][kAndMax + 2]
+    float *Fh = reinterpret_cast<float *>(vred + 2 * 32 * (kAndMax + 2));   // [am][n]
     float *Rh = Fh + (size_t)am * n;                                    // [am][n]
     // this CTA's output ranges (CL = 2: halves, aligned to R * NT rounds)
     const int hn = CL > 1 ? (n + 1) / 2 : n, hm = CL > 1 ? (m + 1) / 2 : m;
@@ -195,17 +209,20 @@ __device__ __forceinline__ void solve_one(const BatchArgs &A, int prob, float *s
     auto rput = [&](float *loc, float v) {   // the same slot in the peer CTA
         if constexpr (CL > 1) cl_st(peer_base + (smem_u32(loc) - smem_u32(sm)), v);
     };
-    // sum of this CTA's block partial v[k] with the peer's (fixed order: rank 0 + rank 1)
+    // sum of this CTA's block partial v[k] with the peer's (fixed order: rank 0 + rank 1).  One
+    // cluster barrier: it also publishes the pass's DSMEM stores, and the two halves of xr
+    // alternate (as in block_red), so a half is rewritten only after both CTAs have read it.
     auto xsum = [&](double *v, int cnt) {
         if constexpr (CL > 1) {
+            double *xh = xr + xpar * 32;
+            xpar ^= 1;
             if (threadIdx.x == 0)
                 for (int k = 0; k < cnt; ++k) {
-                    xr[rank * 16 + k] = v[k];
-                    cl_st(peer_base + (smem_u32(&xr[rank * 16 + k]) - smem_u32(sm)), v[k]);
+                    xh[rank * 16 + k] = v[k];
+                    cl_st(peer_base + (smem_u32(&xh[rank * 16 + k]) - smem_u32(sm)), v[k]);
                 }
             cl_sync();
-            for (int k = 0; k < cnt; ++k) v[k] = xr[k] + xr[16 + k];
-            cl_sync();   // (xr reusable)
+            for (int k = 0; k < cnt; ++k) v[k] = xh[k] + xh[16 + k];
         }
     };
 
@@ -324,7 +341,8 @@ __device__ __forceinline__ void solve_one(const BatchArgs &A, int prob, float *s
                 e_loc += bj * fabs((double)expm1f((gold[j] - gsk) / eps));
             }
         });
-        double cv[4] = {block_sum_d<NT>(e_loc, red), (double)block_or<NT>(bad, redi), 0.0, 0.0};
+        double cv[2] = {e_loc, (double)bad};
+        block_red<NT, kRedW>(cv, 2, red, rpar);
         xsum(cv, 2);   // (CL = 2: also publishes the peer's half of g and w)
         if (cv[1] != 0.0) { nonfin = 1; break; }
         if (check) {
@@ -355,51 +373,86 @@ __device__ __forceinline__ void solve_one(const BatchArgs &A, int prob, float *s
                     if (u < cn) dv[u] += (double)r * (double)(u == a_head ? r : Rh[(size_t)u * n + i]);
                 Rh[(size_t)a_head * n + i] = r;
             });
-            double vv[kAndMax + 2];   // cn dots, the error, the non-finite flag
+            double vv[kAndMax + 2];   // slots 0..7: the dots (0 beyond cn), 8: the error, 9: the flag
 #pragma unroll
             for (int u = 0; u < kAndMax; ++u) vv[u] = dv[u];
-            vv[cn] = e_row;
-            vv[cn + 1] = (double)bad;
-            block_sum_vec<NT>(vv, cn + 2, vred);
-            xsum(vv, cn + 2);
-            const double *dv_s = vv;
-            if (dv_s[cn + 1] != 0.0) { nonfin = 1; break; }
+            vv[kAndMax] = e_row;
+            vv[kAndMax + 1] = (double)bad;
+            block_red<NT, kAndMax + 2>(vv, kAndMax + 2, vred, rpar);
+            xsum(vv, kAndMax + 2);
+            if (vv[kAndMax + 1] != 0.0) { nonfin = 1; break; }
             if (check_a) {
-                err = (float)dv_s[cn];
+                err = (float)vv[kAndMax];
                 if (err < A.tol) { conv = 1; out_gtilde = true; break; }
             }
             if (l + 1 >= A.max_iter) { out_gtilde = true; break; }
-            if (threadIdx.x == 0) {   // Gram row/column of the new slot; alpha from (G + lam I) x = 1
-                for (int u = 0; u < cn; ++u) Gm[a_head * kAndMax + u] = Gm[u * kAndMax + a_head] = dv_s[u];
-                double *xs = al, tr = 0.0;
-                for (int u = 0; u < cn; ++u) tr += Gm[u * kAndMax + u];
-                const double lam = tr > 0.0 ? 1e-8 * tr / cn : 1.0;   // (all residuals 0: equal weights)
-                for (int u = 0; u < cn; ++u) {
-                    for (int v = 0; v < cn; ++v) Gs[u * cn + v] = Gm[u * kAndMax + v];
-                    Gs[u * cn + u] += lam;
-                    xs[u] = 1.0;
+            // alpha from (G + lam I) x = 1, alpha = x / sum x: every warp solves the cn x cn
+            // system redundantly in registers (lane r holds row r; Gauss-Jordan, pivots in
+            // order, the same bits in every warp), so no barrier publishes alpha
+            const int lane = threadIdx.x & 31;
+            double dl = 0.0;          // this lane's new Gram entry <r_new, r_lane>
+#pragma unroll
+            for (int u = 0; u < kAndMax; ++u)
+                if (u == lane) dl = vv[u];
+            double row[kAndMax];
+#pragma unroll
+            for (int u = 0; u < kAndMax; ++u) {
+                double gv;
+                if (lane == a_head) gv = vv[u];
+                else if (u == a_head) gv = dl;
+                else gv = lane < kAndMax ? Gm[lane * kAndMax + u] : 0.0;
+                row[u] = (lane < cn && u < cn) ? gv : (u == lane ? 1.0 : 0.0);
+            }
+            double diag = 0.0;
+#pragma unroll
+            for (int u = 0; u < kAndMax; ++u)
+                if (u == lane) diag = row[u];
+            double tr = lane < cn ? diag : 0.0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) tr += __shfl_xor_sync(0xffffffffu, tr, o);
+            const double lam = tr > 0.0 ? 1e-8 * tr / cn : 1.0;   // (all residuals 0: equal weights)
+#pragma unroll
+            for (int u = 0; u < kAndMax; ++u)
+                if (u == lane && lane < cn) row[u] += lam;
+            double rhs = lane < cn ? 1.0 : 0.0;
+            for (int c = 0; c < cn; ++c) {
+                double piv[kAndMax], myc = 0.0;
+#pragma unroll
+                for (int u = 0; u < kAndMax; ++u) {
+                    piv[u] = __shfl_sync(0xffffffffu, row[u], c);
+                    if (u == c) myc = row[u];
                 }
-                for (int c = 0; c < cn; ++c)
-                    for (int rr = c + 1; rr < cn; ++rr) {
-                        const double q = Gs[rr * cn + c] / Gs[c * cn + c];
-                        for (int k = c; k < cn; ++k) Gs[rr * cn + k] -= q * Gs[c * cn + k];
-                        xs[rr] -= q * xs[c];
-                    }
-                for (int rr = cn - 1; rr >= 0; --rr) {
-                    double t = xs[rr];
-                    for (int k = rr + 1; k < cn; ++k) t -= Gs[rr * cn + k] * xs[k];
-                    xs[rr] = t / Gs[rr * cn + rr];
+                const double prhs = __shfl_sync(0xffffffffu, rhs, c);
+                const double pcc = __shfl_sync(0xffffffffu, myc, c);
+                if (lane != c) {
+                    const double q = myc / pcc;
+#pragma unroll
+                    for (int u = 0; u < kAndMax; ++u) row[u] = fma(-q, piv[u], row[u]);
+                    rhs = fma(-q, prhs, rhs);
                 }
-                double sx = 0.0;
-                for (int u = 0; u < cn; ++u) sx += xs[u];
-                for (int u = 0; u < cn; ++u) al[u] = xs[u] / sx;   // (in place)
+            }
+#pragma unroll
+            for (int u = 0; u < kAndMax; ++u)
+                if (u == lane) diag = row[u];
+            const double xl = lane < cn ? rhs / diag : 0.0;
+            double sx = xl;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) sx += __shfl_xor_sync(0xffffffffu, sx, o);
+            const double al_l = xl / sx;
+            double au[kAndMax];
+#pragma unroll
+            for (int u = 0; u < kAndMax; ++u) au[u] = __shfl_sync(0xffffffffu, al_l, u);
+            if (threadIdx.x < 32 && lane < cn) {   // the Gram row/column of the new slot, for later sweeps
+                Gm[a_head * kAndMax + lane] = dl;
+                Gm[lane * kAndMax + a_head] = dl;
             }
             a_head = (a_head + 1) % am;
             a_cnt = cn;
-            __syncthreads();
             for (int i = i0 + threadIdx.x; i < i1; i += NT) {   // f^{l+1} = sum_u alpha_u T(f_u)
-                double v = 0.0;
-                for (int u = 0; u < cn; ++u) v += al[u] * (double)Fh[(size_t)u * n + i];
+                double v = 0.0;                                  // (Fh[.][i] written by this thread)
+#pragma unroll
+                for (int u = 0; u < kAndMax; ++u)
+                    if (u < cn) v = fma(au[u], (double)Fh[(size_t)u * n + i], v);
                 const float fn = (float)v;
                 const float wv = fmaf(fn, kap, -nxk[i]);
                 fnew[i] = fn;
@@ -429,12 +482,9 @@ __device__ __forceinline__ void solve_one(const BatchArgs &A, int prob, float *s
                 m_loc += ai * dv;
             }
         });
-        double rv[4] = {(double)block_or<NT>(bad, redi), 0.0, 0.0, 0.0};
-        if (relaxed) {
-            rv[1] = block_sum_d<NT>(r_loc, red);
-            rv[2] = block_sum_d<NT>(m_loc, red);
-        }
-        xsum(rv, 3);
+        double rv[3] = {(double)bad, r_loc, m_loc};
+        block_red<NT, kRedW>(rv, relaxed ? 3 : 1, red, rpar);
+        xsum(rv, relaxed ? 3 : 1);
         if (rv[0] != 0.0) { nonfin = 1; break; }
         if (relaxed) { row_err = rv[1]; mass_dev = rv[2]; }
         cur ^= 1;
@@ -453,7 +503,8 @@ __device__ __forceinline__ void solve_one(const BatchArgs &A, int prob, float *s
         A.g[(size_t)prob * m + j] = go[j];
         s += (double)go[j] * (b ? (double)b[j] : 1.0 / m);
     }
-    double ev[4] = {block_sum_d<NT>(s, red), 0.0, 0.0, 0.0};
+    double ev[1] = {s};
+    block_red<NT, kRedW>(ev, 1, red, rpar);
     xsum(ev, 1);
     const double E = ev[0] - (double)eps * mass_dev;   // relaxed: sum P != sum a
     if (threadIdx.x == 0 && rank == 0) {
@@ -467,9 +518,10 @@ __device__ __forceinline__ void solve_one(const BatchArgs &A, int prob, float *s
 }
 
 // Persistent CTAs (one or two per SM) pull problems from a global queue: iteration
-// counts differ per problem, so dynamic assignment balances the SMs.
+// counts differ per problem, so dynamic assignment balances the SMs.  NT <= 512: two
+// CTAs per SM (64 registers; C2 13.4 ms vs 14.0 ms at one CTA per SM with 124 registers).
 template <int D, int R, int NT, int EMU, int CL>
-__global__ void __launch_bounds__(NT) k_batched(BatchArgs A) {
+__global__ void __launch_bounds__(NT, NT <= 512 ? 2 : 1) k_batched(BatchArgs A) {
     extern __shared__ __align__(16) float sm[];
     __shared__ int s_prob;
     const uint32_t rank = CL > 1 ? cl_rank() : 0u;
@@ -490,17 +542,8 @@ __global__ void __launch_bounds__(NT) k_batched(BatchArgs A) {
     }
 }
 
-// EMU: exponential pairs (of 4 per chunk) evaluated on the FMA pipe instead of MUFU.
-// Default 1 (25%); SK_BATCHED_EMU=0..2 overrides it (tuning knob).
-static int batched_emu() {
-    static int v = [] {
-        const char *e = getenv("SK_BATCHED_EMU");
-        int x = e ? atoi(e) : 1;
-        return x < 0 ? 0 : (x > 2 ? 2 : x);
-    }();
-    return v;
-}
-
+// EMU: exponential pairs (of 4 per chunk) evaluated on the FMA pipe instead of MUFU: 1 (25 %)
+// measured best on C2 (0 and 2 were tuning variants, dropped to bound compile time).
 template <int D, int R, int NT, int EMU, int CL>
 static cudaError_t launch_batched_c(const BatchArgs &A, int B, cudaStream_t st) {
     const size_t smem = batched_smem_bytes(D, A.n, A.m, A.anderson);
@@ -537,11 +580,7 @@ static cudaError_t launch_batched_c(const BatchArgs &A, int B, cudaStream_t st) 
 // cluster barriers and the R = 1 shape cost what the tail saves), so batches use one CTA.
 template <int D, int R, int NT, int CL>
 static cudaError_t launch_batched_e(const BatchArgs &A, int B, cudaStream_t st) {
-    switch (batched_emu()) {
-        case 0: return launch_batched_c<D, R, NT, 0, CL>(A, B, st);
-        case 2: return launch_batched_c<D, R, NT, 2, CL>(A, B, st);
-        default: return launch_batched_c<D, R, NT, 1, CL>(A, B, st);
-    }
+    return launch_batched_c<D, R, NT, 1, CL>(A, B, st);
 }
 
 // One wide CTA per problem: NT threads x R output points per thread per round.
