@@ -459,29 +459,64 @@ def soft_rank_sort(x, y, f, g, eps, z=None):
     return (P @ z) / P.sum(1), (P.T @ x) / P.sum(0)
 
 
-def gmm_fit(x, K, init_idx, iters, reg_covar=1e-6):
+def kmeans(x, init_idx, iters):
+    """Lloyd's k-means (the k-means start of the GMM fit, "sklearn"; reading R-28)
+    from centers x[init_idx]: `iters` times (assign every point to its nearest center in squared
+    Euclidean distance, ties to the lowest k; move each non-empty cluster's center to its mean,
+    an empty cluster keeps its center), then a final assignment to the returned centers.
+    Returns (centers K x d, labels n)."""
+    x = _pts(x)
+    c = x[np.asarray(init_idx)].copy()
+
+    def assign(c):
+        d2 = ((x[:, None, :] - c[None, :, :]) ** 2).sum(-1)
+        return np.argmin(d2, axis=1)   # (first minimum: the lowest k)
+
+    for _ in range(iters):
+        lab = assign(c)
+        for k in range(len(c)):
+            if np.any(lab == k):
+                c[k] = x[lab == k].mean(0)
+    return c, assign(c)
+
+
+def _gmm_mstep(x, r, reg_covar):
+    """M-step: n_k = sum_i r_ik (+ 10 eps, sklearn's guard), alpha_k = n_k / n,
+    m_k = sum_i r_ik x_i / n_k, S_k = sum_i r_ik (x_i - m_k)(x_i - m_k)^T / n_k + reg I."""
+    n, d = x.shape
+    nk = r.sum(0) + 10 * np.finfo(np.float64).eps
+    weights = nk / n
+    means = (r.T @ x) / nk[:, None]
+    covs = np.empty((r.shape[1], d, d))
+    for k in range(r.shape[1]):
+        diff = x - means[k]
+        covs[k] = (r[:, k, None] * diff).T @ diff / nk[k] + reg_covar * np.eye(d)
+    return weights, means, covs
+
+
+def gmm_fit(x, K, init_idx, iters, reg_covar=1e-6, kmeans_iters=0):
     """EM for a K-component full-covariance GMM (NEXT-3; "we fit first two K-component
-    GMMs", done with sklearn on the CPU in the paper).  Start (R-23): weights 1/K, means
-    x[init_idx], covariances the biased covariance of x + reg I.  Each iteration, literally:
+    GMMs", done with sklearn on the CPU in the paper).  Start (R-23): kmeans_iters = 0:
+    weights 1/K, means x[init_idx], covariances the biased covariance of x + reg I;
+    kmeans_iters > 0 (R-28, sklearn's init_params="kmeans"): the M-step of the one-hot
+    responsibilities of kmeans(x, init_idx, kmeans_iters).  Each iteration, literally:
         E-step  r_ik = alpha_k N(x_i; m_k, S_k) / sum_l alpha_l N(x_i; m_l, S_l)   (gmm_log_resp)
-        M-step  n_k = sum_i r_ik, alpha_k = n_k / n, m_k = sum_i r_ik x_i / n_k,
-                S_k = sum_i r_ik (x_i - m_k)(x_i - m_k)^T / n_k + reg I.
+        M-step  (_gmm_mstep).
     Returns (weights, means, covs, mean log-likelihood of the returned parameters)."""
     x = _pts(x)
     n, d = x.shape
-    means = x[np.asarray(init_idx)].copy()
-    m0 = x.mean(0)
-    cov0 = (x - m0).T @ (x - m0) / n + reg_covar * np.eye(d)
-    covs = np.repeat(cov0[None], K, axis=0)
-    weights = np.full(K, 1.0 / K)
+    if kmeans_iters > 0:
+        _, lab = kmeans(x, init_idx, kmeans_iters)
+        weights, means, covs = _gmm_mstep(x, np.eye(K)[lab], reg_covar)
+    else:
+        means = x[np.asarray(init_idx)].copy()
+        m0 = x.mean(0)
+        cov0 = (x - m0).T @ (x - m0) / n + reg_covar * np.eye(d)
+        covs = np.repeat(cov0[None], K, axis=0)
+        weights = np.full(K, 1.0 / K)
     for _ in range(iters):
         r = np.exp(gmm_log_resp(x, weights, means, covs))
-        nk = r.sum(0) + 10 * np.finfo(np.float64).eps   # (sklearn's guard for empty components)
-        weights = nk / n
-        means = (r.T @ x) / nk[:, None]
-        for k in range(K):
-            diff = x - means[k]
-            covs[k] = (r[:, k, None] * diff).T @ diff / nk[k] + reg_covar * np.eye(d)
+        weights, means, covs = _gmm_mstep(x, r, reg_covar)
     return weights, means, covs, gmm_loglik(x, weights, means, covs)
 
 

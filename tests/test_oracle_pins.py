@@ -536,6 +536,50 @@ def test_gmm_fit_em_monotone_and_single_component_closed_form():
     assert np.abs(S[0] - ((x - mu).T @ (x - mu) / 400 + 1e-6 * np.eye(4))).max() < 1e-12
 
 
+def test_kmeans_matches_sklearn_lloyd():
+    """R-28: the oracle's Lloyd iterations are sklearn's KMeans (algorithm="lloyd", the same
+    initial centers, n_init=1, tol=0) for several iteration counts: equal centers and labels."""
+    from oracle import oracle as O
+    from sklearn.cluster import KMeans
+    rng = np.random.default_rng(23)
+    x = np.concatenate([rng.standard_normal((250, 4)) * 0.7 + c for c in rng.standard_normal((4, 4)) * 3])
+    idx = rng.choice(len(x), 4, replace=False)
+    for T in (1, 3, 20):
+        c, lab = O.kmeans(x, idx, T)
+        km = KMeans(4, init=x[idx], n_init=1, max_iter=T, tol=0.0, algorithm="lloyd").fit(x)
+        assert np.abs(c - km.cluster_centers_).max() < 1e-12, T
+        assert np.array_equal(lab, km.labels_), T
+
+
+def test_gmm_fit_kmeans_start_matches_sklearn_em():
+    """R-28: with kmeans_iters > 0 the fit starts from the one-hot M-step of the k-means labels
+    (sklearn's init_params="kmeans"), written here independently (counts, cluster means, np.cov
+    with bias), and the EM steps then equal sklearn's GaussianMixture from that start."""
+    from oracle import oracle as O
+    from sklearn.mixture import GaussianMixture
+    rng = np.random.default_rng(24)
+    x = np.concatenate([rng.standard_normal((300, 3)) * 0.6 + c for c in ([0, 0, 0], [3, 1, 0], [-2, 2, 1])])
+    K, reg = 3, 1e-6
+    idx = rng.choice(len(x), K, replace=False)
+    _, lab = O.kmeans(x, idx, 5)
+    w0 = np.array([(lab == k).sum() for k in range(K)]) / len(x)
+    m0 = np.stack([x[lab == k].mean(0) for k in range(K)])
+    S0 = np.stack([np.cov(x[lab == k].T, bias=True) + reg * np.eye(3) for k in range(K)])
+    w, m, S, _ = O.gmm_fit(x, K, idx, 0, reg, kmeans_iters=5)
+    assert np.abs(w - w0).max() < 1e-12 and np.abs(m - m0).max() < 1e-12 and np.abs(S - S0).max() < 1e-12
+    w, m, S, ll = O.gmm_fit(x, K, idx, 7, reg, kmeans_iters=5)
+    gm = GaussianMixture(K, covariance_type="full", reg_covar=reg, max_iter=7, tol=0.0, init_params="random",
+                         weights_init=w0, means_init=m0, precisions_init=np.linalg.inv(S0), random_state=0)
+    import warnings
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        gm.fit(x)
+    assert np.abs(w - gm.weights_).max() < 1e-10
+    assert np.abs(m - gm.means_).max() < 1e-9
+    assert np.abs(S - gm.covariances_).max() < 1e-9
+    assert abs(ll - gm.score(x)) < 1e-9
+
+
 # --------------------------------------------------- implicit differentiation (NEXT-4)
 def _solve_tight(O, x, y, eps, a=None, b=None, f0=None):
     r = O.sinkhorn(x, y, eps, a=a, b=b, tol=1e-13, max_iter=200000, f0=f0)
