@@ -257,6 +257,9 @@ class Single(Workload):
              "parallelism": f"row-sharded x{self.world}" if self.sharded else "1 GPU",
              "l2": "flushed (256 MiB write) before every timed step" if self.name in ("c1",) else
                    "inputs + cost larger than L2 / flushed before each step"}
+        if self.init == "gmm":
+            c["gmm_fit"] = {"K": 8, "kmeans_iters": self.args.gmm_kmeans_iters, "em_iters": self.args.gmm_iters,
+                            "start": "gen.gmm_start_idx seeds 3/4 (R-23/R-28)"}
         return c
 
     def _init(self, x, y):
@@ -264,8 +267,10 @@ class Single(Workload):
         if self.init == "gaussian":
             f0, _ = sk.sinkhorn_init_gaussian(self.ctx, x, y)
         elif self.init == "gmm":
-            gx, _ = sk.sinkhorn_fit_gmm(self.ctx, x, 8, self.gmm_idx[0], iters=self.args.gmm_iters)
-            gy, _ = sk.sinkhorn_fit_gmm(self.ctx, y, 8, self.gmm_idx[1], iters=self.args.gmm_iters)
+            gx, _ = sk.sinkhorn_fit_gmm(self.ctx, x, 8, self.gmm_idx[0], iters=self.args.gmm_iters,
+                                        kmeans_iters=self.args.gmm_kmeans_iters)
+            gy, _ = sk.sinkhorn_fit_gmm(self.ctx, y, 8, self.gmm_idx[1], iters=self.args.gmm_iters,
+                                        kmeans_iters=self.args.gmm_kmeans_iters)
             f0, _ = sk.sinkhorn_init_gmm(self.ctx, x, y, gx, gy, p.eps)
         elif self.init == "gmm_given":
             gx, gy = self.gx, self.gy
@@ -587,6 +592,8 @@ def main():
     ap.add_argument("--init", default=None,
                     help="c3/c4/c5 initializer: zero|gaussian|gmm (fitted on the device)|gmm_given|subsample")
     ap.add_argument("--gmm-iters", type=int, default=50, help="EM iterations of the device GMM fit (init gmm)")
+    ap.add_argument("--gmm-kmeans-iters", type=int, default=10,
+                    help="Lloyd steps of the fit's k-means start (R-28; sklearn's default start), 0 = start at x[idx]")
     ap.add_argument("--eps-factor", type=float, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-k14", action="store_true", help="skip the K14 microbenchmarks")

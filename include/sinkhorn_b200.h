@@ -185,17 +185,20 @@ sk_status sinkhorn_vjp(sk_ctx *ctx, int64_t n, int64_t m, int32_t d, const float
 
 /* GMM fitting for the GMM initializer (Sec. 3.3, "we fit first two K-component GMMs";
  * the paper fits on the CPU with sklearn): `iters` EM steps for a
- * full-covariance K-component mixture of x (n x d, row-major) from the start (R-23)
- * weights 1/K, means x[init_idx[k]], covariances = biased covariance of x + reg_covar I; each
+ * full-covariance K-component mixture of x (n x d, row-major).  Start (R-23/R-28):
+ * kmeans_iters = 0: weights 1/K, means x[init_idx[k]], covariances = biased covariance of x +
+ * reg_covar I; kmeans_iters > 0 (sklearn's init_params="kmeans"): kmeans_iters Lloyd steps
+ * from centers x[init_idx[k]] (nearest center in fp64, ties to the lowest k, an empty cluster
+ * keeps its center), a final assignment, and the M-step of those one-hot responsibilities.  Each
  * M-step adds reg_covar I (as sklearn's reg_covar).  fp64 state and sufficient statistics,
  * deterministic.  Outputs (caller-owned, device or host): weights K, means K x d, covs
  * K x d x d (fp32, the layout sinkhorn_init_gmm takes); loglik (host, nullable) = mean
- * log-likelihood of the returned parameters.  SK_EINVAL: bad sizes, K > n, iters < 0,
+ * log-likelihood of the returned parameters.  SK_EINVAL: bad sizes, K > n, iters < 0, kmeans_iters < 0,
  * reg_covar < 0, non-finite x, init_idx not K distinct indices in [0, n); SK_EUNSUPPORTED:
  * d > 32 or K > 64; SK_ENONFINITE: a covariance lost positive definiteness.  Blocks. */
 sk_status sinkhorn_fit_gmm(sk_ctx *ctx, int64_t n, int32_t d, const float *x, int32_t K,
-                           const int32_t *init_idx, int32_t iters, float reg_covar, float *weights,
-                           float *means, float *covs, double *loglik);
+                           const int32_t *init_idx, int32_t kmeans_iters, int32_t iters, float reg_covar,
+                           float *weights, float *means, float *covs, double *loglik);
 
 /* Soft ranks and soft sort (Sec. 3.1) of B 1D problems with
  * cost (x - y)^2, from potentials (f, g) (normally the output of sinkhorn_solve): with the

@@ -258,8 +258,10 @@ def sinkhorn_init_nw1d(ctx: Context, x, y, a=None, b=None, y_shared: bool = True
     return (pot.view(n) if single else pot), rounds
 
 
-def sinkhorn_fit_gmm(ctx: Context, x, K: int, init_idx, iters: int = 100, reg_covar: float = 1e-6):
-    """EM fit of a K-component full-covariance GMM of x (n, d) from means x[init_idx] (NEXT-3).
+def sinkhorn_fit_gmm(ctx: Context, x, K: int, init_idx, iters: int = 100, reg_covar: float = 1e-6,
+                     kmeans_iters: int = 0):
+    """EM fit of a K-component full-covariance GMM of x (n, d) (NEXT-3), started from means
+    x[init_idx] (kmeans_iters = 0) or from kmeans_iters Lloyd steps from those centers (R-28).
     Returns ({'weights', 'means', 'covs'} as sinkhorn_init_gmm takes them, mean log-likelihood)."""
     n, d = x.shape
     idx = init_idx if isinstance(init_idx, torch.Tensor) else torch.as_tensor(init_idx, dtype=torch.int32)
@@ -268,7 +270,7 @@ def sinkhorn_fit_gmm(ctx: Context, x, K: int, init_idx, iters: int = 100, reg_co
     mu = _empty((K, d), x)
     cov = _empty((K, d, d), x)
     ll = ctypes.c_double()
-    ctx.check(ctx.lib.sinkhorn_fit_gmm(ctx.h, n, d, _ptr(x), int(K), _ptr(idx, torch.int32), int(iters), float(reg_covar),
+    ctx.check(ctx.lib.sinkhorn_fit_gmm(ctx.h, n, d, _ptr(x), int(K), _ptr(idx, torch.int32), int(kmeans_iters), int(iters), float(reg_covar),
                                        _ptr(w), _ptr(mu), _ptr(cov), ctypes.byref(ll)))
     return {"weights": w, "means": mu, "covs": cov}, ll.value
 

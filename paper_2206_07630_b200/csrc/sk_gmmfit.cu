@@ -8,6 +8,10 @@
 //           r_ik = exp(log p_ik - LSE_k log p_ik),  ll = mean_i LSE_k log p_ik - d/2 log 2 pi;
 //   M-step  n_k = sum_i r_ik,  w_k = n_k / n,  m_k = sum_i r_ik x_i / n_k,
 //           S_k = sum_i r_ik x_i x_i^T / n_k - m_k m_k^T + reg I.
+// k-means start (kmeans_iters > 0, reading R-28 = sklearn's init_params="kmeans"): Lloyd from
+// centers x[idx] (assign to the nearest center, ties to the lowest k; non-empty clusters move
+// to their mean), a final assignment, and the M-step of those one-hot responsibilities.  The
+// hard assignment reuses the E-step kernel (HARD: r_ik one-hot) and its statistics.
 // Kernels per iteration: k_em_chol (one CTA per component: Cholesky, L^-1, log det),
 // k_em_estep (fixed point chunks per CTA: responsibilities, then the sufficient statistics
 // (n_k, sum r x, sum r x x^T upper triangle) accumulated per thread-owned statistic in fp64 and
@@ -103,7 +107,7 @@ __global__ void __launch_bounds__(kEmT) k_em_chol(double *base, int K, int d, in
 
 // E-step + sufficient statistics over this CTA's fixed chunk of points.  Statistic s of
 // component k (base k (1 + d + T)): 0 = n_k, 1..d = sum r x, then sum r x_a x_b for a <= b.
-template <int MAXS, int DM>
+template <int MAXS, int DM, bool HARD>
 __global__ void __launch_bounds__(kEmT) k_em_estep(const float *__restrict__ x, long long n, int d, int K,
                                                     const double *__restrict__ base, double *part) {
     extern __shared__ double sm[];
@@ -114,15 +118,17 @@ __global__ void __launch_bounds__(kEmT) k_em_estep(const float *__restrict__ x, 
     double *sM = sL + K * DM * DM;            // [K][DM] means
     double *sC = sM + K * DM;                 // [K] log w_k - log det L_k
     const EmState s = em_state(const_cast<double *>(base), K, d);
-    for (int e = threadIdx.x; e < K * DM * DM; e += kEmT) {
-        const int k = e / (DM * DM), r = (e / DM) % DM, c = e % DM;
-        sL[e] = (r < d && c < d) ? s.LINV[(long long)k * d * d + r * d + c] : 0.0;
-    }
+    if (!HARD)
+        for (int e = threadIdx.x; e < K * DM * DM; e += kEmT) {
+            const int k = e / (DM * DM), r = (e / DM) % DM, c = e % DM;
+            sL[e] = (r < d && c < d) ? s.LINV[(long long)k * d * d + r * d + c] : 0.0;
+        }
     for (int e = threadIdx.x; e < K * DM; e += kEmT) {
         const int k = e / DM, c = e % DM;
         sM[e] = c < d ? s.MU[(long long)k * d + c] : 0.0;
     }
-    for (int k = threadIdx.x; k < K; k += kEmT) sC[k] = log(s.W[k]) - s.LOGDET[k];
+    if (!HARD)
+        for (int k = threadIdx.x; k < K; k += kEmT) sC[k] = log(s.W[k]) - s.LOGDET[k];
     const int T = d * (d + 1) / 2, per = 1 + d + T, S = K * per;
     const long long chunk = (n + gridDim.x - 1) / gridDim.x;
     const long long p0 = blockIdx.x * chunk, p1 = min(n, p0 + chunk);
@@ -160,6 +166,12 @@ __global__ void __launch_bounds__(kEmT) k_em_estep(const float *__restrict__ x, 
 #pragma unroll
             for (int c = 0; c < DM; ++c) dx[c] = c < d ? xi[c] - mk[c] : 0.0;
             double q = 0.0;
+            if (HARD) {   // k-means: minus the squared distance (summed in coordinate order)
+#pragma unroll
+                for (int c = 0; c < DM; ++c) q += dx[c] * dx[c];
+                rs[pp * K + k] = -q;
+                continue;
+            }
 #pragma unroll
             for (int r = 0; r < DM; ++r) {
                 double z = 0.0;
@@ -170,7 +182,14 @@ __global__ void __launch_bounds__(kEmT) k_em_estep(const float *__restrict__ x, 
             rs[pp * K + k] = sC[k] - 0.5 * q;
         }
         __syncthreads();
-        if (threadIdx.x < np) {   // normalise point t0 + threadIdx.x (fixed k order)
+        if (HARD && threadIdx.x < np) {   // nearest center, ties to the lowest k: one-hot
+            double *ri = rs + threadIdx.x * K;
+            int kb = 0;
+            for (int k = 1; k < K; ++k)
+                if (ri[k] > ri[kb]) kb = k;
+            lls[threadIdx.x] = -ri[kb];   // (inertia)
+            for (int k = 0; k < K; ++k) ri[k] = k == kb ? 1.0 : 0.0;
+        } else if (threadIdx.x < np) {   // normalise point t0 + threadIdx.x (fixed k order)
             double *ri = rs + threadIdx.x * K;
             double mx = -INFINITY;
             for (int k = 0; k < K; ++k) mx = fmax(mx, ri[k]);
@@ -240,6 +259,17 @@ __global__ void __launch_bounds__(kEmT) k_em_mstep(const double *tot, long long 
     if (threadIdx.x == 0) *s.LL = tot[S] / (double)n - 0.5 * d * log(2.0 * 3.14159265358979323846);
 }
 
+// Lloyd's center update from the hard statistics: a non-empty cluster moves to its mean.
+__global__ void k_km_update(const double *tot, int d, int K, double *base) {
+    const EmState s = em_state(base, K, d);
+    const int per = 1 + d + d * (d + 1) / 2;
+    for (int e = threadIdx.x; e < K * d; e += blockDim.x) {
+        const int k = e / d, a = e % d;
+        const double nk = tot[k * per];
+        if (nk > 0.0) s.MU[e] = tot[k * per + 1 + a] / nk;
+    }
+}
+
 __global__ void k_em_out(const double *base, int K, int d, float *w, float *mu, float *cov, double *ll_out) {
     const EmState s = em_state(const_cast<double *>(base), K, d);
     for (int e = threadIdx.x; e < K * d * d; e += blockDim.x) cov[e] = (float)s.COV[e];
@@ -248,29 +278,37 @@ __global__ void k_em_out(const double *base, int K, int d, float *w, float *mu, 
     if (threadIdx.x == 0 && ll_out) *ll_out = *s.LL;
 }
 
-template <int MAXS, int DM>
+template <int MAXS, int DM, bool HARD>
 static cudaError_t launch_estep_d(const float *x, long long n, int d, int K, const double *base, double *part,
                                   cudaStream_t st) {
     const size_t smem = sizeof(double) * ((size_t)kEmTile * (d + K) + kEmTile + (size_t)K * (DM * DM + DM + 1));
-    cudaError_t e = cudaFuncSetAttribute(k_em_estep<MAXS, DM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(k_em_estep<MAXS, DM, HARD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
     if (e != cudaSuccess) return e;
-    k_em_estep<MAXS, DM><<<kEmBlocks, kEmT, smem, st>>>(x, n, d, K, base, part);
+    k_em_estep<MAXS, DM, HARD><<<kEmBlocks, kEmT, smem, st>>>(x, n, d, K, base, part);
     return cudaGetLastError();
 }
-template <int MAXS>
-static cudaError_t launch_estep(const float *x, long long n, int d, int K, const double *base, double *part,
-                                cudaStream_t st) {
-    if (d <= 8) return launch_estep_d<MAXS, 8>(x, n, d, K, base, part, st);
-    if (d <= 16) return launch_estep_d<MAXS, 16>(x, n, d, K, base, part, st);
-    return launch_estep_d<MAXS, 32>(x, n, d, K, base, part, st);
+template <int MAXS, bool HARD>
+static cudaError_t launch_estep_m(const float *x, long long n, int d, int K, const double *base, double *part,
+                                  cudaStream_t st) {
+    if (d <= 8) return launch_estep_d<MAXS, 8, HARD>(x, n, d, K, base, part, st);
+    if (d <= 16) return launch_estep_d<MAXS, 16, HARD>(x, n, d, K, base, part, st);
+    return launch_estep_d<MAXS, 32, HARD>(x, n, d, K, base, part, st);
+}
+template <bool HARD>
+static cudaError_t launch_estep(int maxs, const float *x, long long n, int d, int K, const double *base,
+                                double *part, cudaStream_t st) {
+    if (maxs <= 8) return launch_estep_m<8, HARD>(x, n, d, K, base, part, st);
+    if (maxs <= 20) return launch_estep_m<20, HARD>(x, n, d, K, base, part, st);
+    return launch_estep_m<40, HARD>(x, n, d, K, base, part, st);
 }
 
 // iters EM steps from the start above; the state (em_state_doubles) and partials
 // (em_partial_doubles) are caller workspace; cov0 = biased covariance of x (d x d).  A final
 // E-step evaluates the mean log-likelihood of the returned parameters.
 cudaError_t launch_gmm_fit(const float *x, long long n, int d, int K, const int *idx, const double *cov0,
-                           int iters, double reg, double *state, double *part, int *flags, float *w, float *mu,
-                           float *cov, double *ll_out, cudaStream_t st) {
+                           int kmeans_iters, int iters, double reg, double *state, double *part, int *flags,
+                           float *w, float *mu, float *cov, double *ll_out, cudaStream_t st) {
     const int S = em_stats(K, d);
     const int maxs = (S + kEmT - 1) / kEmT;
     if (d < 1 || d > 32 || K < 1 || maxs > 40) return cudaErrorInvalidValue;
@@ -279,11 +317,16 @@ cudaError_t launch_gmm_fit(const float *x, long long n, int d, int K, const int 
     double *tot = part + em_partial_doubles(K, d);   // [S + 1] after the partials
     const int rblocks = (32 * (S + 1) + kEmT - 1) / kEmT;
     cudaError_t e = cudaSuccess;
+    for (int t = 0; t <= kmeans_iters && kmeans_iters > 0; ++t) {   // Lloyd, then the one-hot M-step
+        e = launch_estep<true>(maxs, x, n, d, K, state, part, st);
+        if (e != cudaSuccess) return e;
+        k_em_reduce<<<rblocks, kEmT, 0, st>>>(part, kEmBlocks, S + 1, tot);
+        if (t < kmeans_iters) k_km_update<<<1, kEmT, 0, st>>>(tot, d, K, state);
+        else k_em_mstep<<<1, kEmT, 0, st>>>(tot, n, d, K, reg, state);
+    }
     for (int it = 0; it <= iters; ++it) {
         k_em_chol<<<K, kEmT, smem_chol, st>>>(state, K, d, flags);
-        if (maxs <= 8) e = launch_estep<8>(x, n, d, K, state, part, st);
-        else if (maxs <= 20) e = launch_estep<20>(x, n, d, K, state, part, st);
-        else e = launch_estep<40>(x, n, d, K, state, part, st);
+        e = launch_estep<false>(maxs, x, n, d, K, state, part, st);
         if (e != cudaSuccess) return e;
         k_em_reduce<<<rblocks, kEmT, 0, st>>>(part, kEmBlocks, S + 1, tot);
         if (it == iters) {   // evaluation only: the log-likelihood of the returned parameters

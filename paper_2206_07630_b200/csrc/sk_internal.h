@@ -36,7 +36,7 @@ size_t em_state_doubles(int K, int d);
 size_t em_partial_doubles(int K, int d);
 size_t em_work_doubles(int K, int d);   // partials + the reduced statistics (launch_gmm_fit's part)
 cudaError_t launch_gmm_fit(const float *x, long long n, int d, int K, const int *idx, const double *cov0,
-                           int iters, double reg, double *state /* 2 x em_state_doubles */, double *part,
+                           int kmeans_iters, int iters, double reg, double *state /* 2 x em_state_doubles */, double *part,
                            int *flags, float *w, float *mu, float *cov, double *ll_out, cudaStream_t st);
 // K17 implicit differentiation (NEXT-4)
 size_t vjp_work_doubles(long long n, long long m, int d);

@@ -39,6 +39,25 @@ def test_fit_parity(O, ctx, n, d, K, iters):
     assert abs(ll - llo) <= 1e-9 * max(1.0, abs(llo))
 
 
+@pytest.mark.parametrize("n,d,K,km,iters", [(900, 3, 3, 4, 0), (2500, 7, 5, 10, 8), (16384, 16, 8, 10, 20),
+                                             (1000, 2, 6, 30, 3)])
+def test_fit_kmeans_start_parity(O, ctx, n, d, K, km, iters):
+    """R-28: Lloyd steps (hard assignments decided in fp64 on both sides) then the one-hot
+    M-step and EM; iters = 0 checks the k-means start itself."""
+    import paper_2206_07630_b200 as sk
+    if n == 16384:
+        x = gen.c3().x
+    else:
+        rng = np.random.default_rng(n + d + km)
+        cents = rng.standard_normal((K, d)) * 3
+        x = (cents[rng.integers(0, K, n)] + rng.standard_normal((n, d)) * 0.9).astype(np.float32)
+    idx = gen.gmm_start_idx(len(x), K, seed=n + 1)
+    g, ll = sk.sinkhorn_fit_gmm(ctx, torch.from_numpy(x).cuda(), K, idx, iters=iters, kmeans_iters=km)
+    w, m, S, llo = O.gmm_fit(x, K, idx, iters, 1e-6, kmeans_iters=km)
+    assert _close(g["weights"], w, 1e-6) and _close(g["means"], m, 1e-6) and _close(g["covs"], S, 1e-6)
+    assert abs(ll - llo) <= 1e-9 * max(1.0, abs(llo))
+
+
 def test_fitted_gmm_initializer_c3(O, ctx):
     """The paper's GMM initializer with GMMs fitted on the device: f0 vs the oracle's
     initializer evaluated with the oracle's own fitted mixtures."""
@@ -67,6 +86,8 @@ def test_fit_errors(ctx):
         sk.sinkhorn_fit_gmm(ctx, x, 3, [1, 2, 100])        # out of range
     with pytest.raises(sk.SinkhornError):
         sk.sinkhorn_fit_gmm(ctx, torch.rand(100, 33, device="cuda"), 2, [0, 1])   # d > 32
+    with pytest.raises(sk.SinkhornError):
+        sk.sinkhorn_fit_gmm(ctx, x, 2, [0, 1], kmeans_iters=-1)
     bad = x.clone(); bad[5, 1] = float("inf")
     with pytest.raises(sk.SinkhornError):
         sk.sinkhorn_fit_gmm(ctx, bad, 2, [0, 1])
