@@ -29,6 +29,7 @@ constexpr int kEmTile = 64;      // points staged per E-step tile
 constexpr int kEmBlocks = 296;   // fixed point partition (2 CTAs per SM)
 
 __host__ __device__ inline int em_stats(int K, int d) { return K * (1 + d + d * (d + 1) / 2); }
+__host__ __device__ inline int em_xs(int d) { return d + 2 - (d & 1); }   // padded row stride of x tiles
 
 // state (doubles): W[K] | MU[K d] | COV[K d d] | LINV[K d d] | LOGDET[K] | LL[1]
 struct EmState {
@@ -61,71 +62,98 @@ __global__ void k_em_init(const float *__restrict__ x, int d, int K, const int *
     for (int k = threadIdx.x; k < K; k += blockDim.x) s.W[k] = 1.0 / K;
 }
 
-// Cholesky S_k = L L^T (fp64, textbook Cholesky-Banachiewicz), L^{-1}, log det L.
-__global__ void __launch_bounds__(kEmT) k_em_chol(double *base, int K, int d, int *flags) {
-    extern __shared__ double sm[];
+// Cholesky S_k = L L^T (fp64), L^{-1}, log det L: one warp per component, lane i holding row i
+// in registers.  Right-looking: step j takes the pivot from lane j, scales column j, and updates
+// the trailing lower triangle with column j broadcast by shuffles.  Then lane c forward-solves
+// column c of L^{-1} (L broadcast from shared memory).  DM >= d (compile-time register rows).
+template <int DM>
+__global__ void __launch_bounds__(32) k_em_chol(double *base, int K, int d, int *flags) {
+    __shared__ double sL[DM * DM];
     const EmState s = em_state(base, K, d);
-    const int dd = d * d, k = blockIdx.x;
-    double *L = sm, *Li = sm + dd;
-    for (int e = threadIdx.x; e < dd; e += blockDim.x) {
-        const int i = e / d, j = e % d;
-        L[e] = 0.5 * (s.COV[(long long)k * dd + i * d + j] + s.COV[(long long)k * dd + j * d + i]);
-        Li[e] = 0.0;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        int bad = 0;
-        for (int j = 0; j < d; ++j) {
-            double v = L[j * d + j];
-            for (int t = 0; t < j; ++t) v -= L[j * d + t] * L[j * d + t];
-            if (!(v > 0.0)) { bad = 1; v = 1e-300; }
-            const double ljj = sqrt(v);
-            L[j * d + j] = ljj;
-            for (int i = j + 1; i < d; ++i) {
-                double u = L[i * d + j];
-                for (int t = 0; t < j; ++t) u -= L[i * d + t] * L[j * d + t];
-                L[i * d + j] = u / ljj;
-            }
-            for (int t = j + 1; t < d; ++t) L[j * d + t] = 0.0;
+    const int dd = d * d, k = blockIdx.x, lane = threadIdx.x;
+    double a[DM];
+#pragma unroll
+    for (int c = 0; c < DM; ++c)
+        a[c] = (lane < d && c < d) ? 0.5 * (s.COV[(long long)k * dd + lane * d + c] + s.COV[(long long)k * dd + c * d + lane])
+                                    : 0.0;
+    int bad = 0;
+#pragma unroll
+    for (int j = 0; j < DM; ++j) {
+        if (j >= d) break;
+        double v = __shfl_sync(0xffffffffu, a[j], j);   // the pivot a_jj (lane j's current value)
+        if (!(v > 0.0)) { bad = 1; v = 1e-300; }
+        const double ljj = sqrt(v), rj = 1.0 / ljj;
+        const double lij = lane == j ? ljj : (lane > j ? a[j] * rj : 0.0);
+        a[j] = lij;
+#pragma unroll
+        for (int c = j + 1; c < DM; ++c) {   // a_ic -= l_ij l_cj for j < c <= i
+            const double lcj = __shfl_sync(0xffffffffu, lij, c);
+            if (c <= lane) a[c] = fma(-lij, lcj, a[c]);
         }
-        double ld = 0.0;
-        for (int j = 0; j < d; ++j) ld += log(L[j * d + j]);
+    }
+#pragma unroll
+    for (int c = 0; c < DM; ++c)
+        if (c > lane) a[c] = 0.0;
+    double ld = 0.0;
+#pragma unroll
+    for (int c = 0; c < DM; ++c)
+        if (c == lane && lane < d) ld = log(a[c]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ld += __shfl_xor_sync(0xffffffffu, ld, o);
+    if (lane < d) {
+#pragma unroll
+        for (int c = 0; c < DM; ++c) sL[lane * DM + c] = a[c];
+    }
+    __syncwarp();
+    if (lane == 0) {
         s.LOGDET[k] = ld;
         if (bad) atomicOr(flags, 1);
     }
-    __syncthreads();
-    for (int c = threadIdx.x; c < d; c += blockDim.x) {
-        for (int i = 0; i < d; ++i) {
-            double v = (i == c) ? 1.0 : 0.0;
-            for (int t = 0; t < i; ++t) v -= L[i * d + t] * Li[t * d + c];
-            Li[i * d + c] = v / L[i * d + i];
+    if (lane < d) {   // column `lane` of L^{-1}: Li[i] = (delta_ic - sum_{t<i} L_it Li[t]) / L_ii
+        double col[DM], rd[DM];
+#pragma unroll
+        for (int i = 0; i < DM; ++i) rd[i] = i < d ? 1.0 / sL[i * DM + i] : 0.0;   // (independent)
+#pragma unroll
+        for (int i = 0; i < DM; ++i) {
+            double v = i == lane ? 1.0 : 0.0;
+#pragma unroll
+            for (int t = 0; t < i; ++t) v = fma(-sL[i * DM + t], col[t], v);
+            col[i] = v * rd[i];
         }
+#pragma unroll
+        for (int i = 0; i < DM; ++i)
+            if (i < d) s.LINV[(long long)k * dd + i * d + lane] = col[i];
     }
-    __syncthreads();
-    for (int e = threadIdx.x; e < dd; e += blockDim.x) s.LINV[(long long)k * dd + e] = Li[e];
 }
 
 // E-step + sufficient statistics over this CTA's fixed chunk of points.  Statistic s of
 // component k (base k (1 + d + T)): 0 = n_k, 1..d = sum r x, then sum r x_a x_b for a <= b.
-template <int MAXS, int DM, bool HARD>
+// OWN (K d <= kEmT): thread t = (k, a) owns n_k (a = 0), sum r x_a and the row sum r x_a x_b
+// (all b in registers, the b >= a half stored): one broadcast row of x per point instead of
+// three loads per statistic.  Otherwise each thread owns up to MAXS statistics.
+template <int MAXS, int DM, bool HARD, bool OWN>
 __global__ void __launch_bounds__(kEmT) k_em_estep(const float *__restrict__ x, long long n, int d, int K,
                                                     const double *__restrict__ base, double *part) {
     extern __shared__ double sm[];
-    double *xs = sm;                          // [kEmTile][d]
-    double *rs = xs + kEmTile * d;            // [kEmTile][K]
+    // row strides padded by 16 bytes: the lanes of a warp read the rows of different points /
+    // components at once, and unpadded 128-byte multiples would put them all in the same banks
+    const int XS = em_xs(d);
+    constexpr int LS = DM * DM + 2, MS = DM + 2;
+    double *xs = sm;                          // [kEmTile][XS]
+    double *rs = xs + kEmTile * XS;           // [kEmTile][K]
     double *lls = rs + kEmTile * K;           // [kEmTile]
-    double *sL = lls + kEmTile;               // [K][DM][DM] L^{-1} (lower triangle used)
-    double *sM = sL + K * DM * DM;            // [K][DM] means
-    double *sC = sM + K * DM;                 // [K] log w_k - log det L_k
+    double *sL = lls + kEmTile;               // [K][LS] L^{-1} rows (lower triangle used)
+    double *sM = sL + K * LS;                 // [K][MS] means
+    double *sC = sM + K * MS;                 // [K] log w_k - log det L_k
     const EmState s = em_state(const_cast<double *>(base), K, d);
     if (!HARD)
         for (int e = threadIdx.x; e < K * DM * DM; e += kEmT) {
             const int k = e / (DM * DM), r = (e / DM) % DM, c = e % DM;
-            sL[e] = (r < d && c < d) ? s.LINV[(long long)k * d * d + r * d + c] : 0.0;
+            sL[k * LS + r * DM + c] = (r < d && c < d) ? s.LINV[(long long)k * d * d + r * d + c] : 0.0;
         }
     for (int e = threadIdx.x; e < K * DM; e += kEmT) {
         const int k = e / DM, c = e % DM;
-        sM[e] = c < d ? s.MU[(long long)k * d + c] : 0.0;
+        sM[k * MS + c] = c < d ? s.MU[(long long)k * d + c] : 0.0;
     }
     if (!HARD)
         for (int k = threadIdx.x; k < K; k += kEmT) sC[k] = log(s.W[k]) - s.LOGDET[k];
@@ -153,15 +181,22 @@ __global__ void __launch_bounds__(kEmT) k_em_estep(const float *__restrict__ x, 
         }
     }
     double ll = 0.0;
+    const int ok = threadIdx.x / d, oa = threadIdx.x % d;   // OWN: this thread's (k, a)
+    const bool owner = OWN && (int)threadIdx.x < K * d;
+    double on = 0.0, osum = 0.0, oxx[OWN ? DM : 1];
+#pragma unroll
+    for (int b = 0; b < (OWN ? DM : 1); ++b) oxx[b] = 0.0;
     for (long long t0 = p0; t0 < p1; t0 += kEmTile) {
         const int np = (int)min((long long)kEmTile, p1 - t0);
-        for (int e = threadIdx.x; e < np * d; e += kEmT) xs[e] = (double)x[(t0 + e / d) * d + e % d];
+        for (int e = threadIdx.x; e < np * d; e += kEmT) xs[(e / d) * XS + e % d] = (double)x[(t0 + e / d) * d + e % d];
         __syncthreads();
-        for (int e = threadIdx.x; e < np * K; e += kEmT) {   // log p of (point, component) pairs
-            const int pp = e / K, k = e % K;
-            const double *xi = xs + pp * d;
-            const double *Li = sL + k * DM * DM;
-            const double *mk = sM + k * DM;
+        // log p of (point, component) pairs.  K <= 32: groups of G = pow2 >= K consecutive lanes
+        // per point, so the normalisation (max, sum of exps / the nearest center) is a group
+        // shuffle reduction with one exponential per lane; otherwise one thread per point.
+        auto logp = [&](int pp, int k) {
+            const double *xi = xs + pp * XS;
+            const double *Li = sL + k * LS;
+            const double *mk = sM + k * MS;
             double dx[DM];
 #pragma unroll
             for (int c = 0; c < DM; ++c) dx[c] = c < d ? xi[c] - mk[c] : 0.0;
@@ -169,8 +204,7 @@ __global__ void __launch_bounds__(kEmT) k_em_estep(const float *__restrict__ x, 
             if (HARD) {   // k-means: minus the squared distance (summed in coordinate order)
 #pragma unroll
                 for (int c = 0; c < DM; ++c) q += dx[c] * dx[c];
-                rs[pp * K + k] = -q;
-                continue;
+                return -q;
             }
 #pragma unroll
             for (int r = 0; r < DM; ++r) {
@@ -179,35 +213,76 @@ __global__ void __launch_bounds__(kEmT) k_em_estep(const float *__restrict__ x, 
                 for (int c = 0; c <= r; ++c) z = fma(Li[r * DM + c], dx[c], z);
                 q = fma(z, z, q);   // (rows r >= d are zero)
             }
-            rs[pp * K + k] = sC[k] - 0.5 * q;
+            return sC[k] - 0.5 * q;
+        };
+        if (K <= 32) {
+            const int G = K <= 1 ? 1 : 1 << (32 - __clz(K - 1));
+            for (int b0 = 0; b0 < np; b0 += kEmT / G) {
+                const int pp = b0 + (int)threadIdx.x / G, k = (int)threadIdx.x % G;
+                const bool live = pp < np && k < K;
+                const double lp = live ? logp(pp, k) : -INFINITY;
+                double mx = lp;
+                int kb = live ? k : 1 << 30;
+                for (int o = G / 2; o > 0; o >>= 1) {   // max; HARD: the first maximum's k
+                    const double om = __shfl_xor_sync(0xffffffffu, mx, o);
+                    const int okb = __shfl_xor_sync(0xffffffffu, kb, o);
+                    if (om > mx || (om == mx && okb < kb)) { mx = om; kb = okb; }
+                }
+                if (HARD) {
+                    if (live) rs[pp * K + k] = k == kb ? 1.0 : 0.0;
+                    if (live && k == 0) lls[pp] = -mx;   // (inertia)
+                } else {
+                    double den = live ? exp(lp - mx) : 0.0;
+                    for (int o = G / 2; o > 0; o >>= 1) den += __shfl_xor_sync(0xffffffffu, den, o);
+                    const double lse = mx + log(den);
+                    if (live) rs[pp * K + k] = exp(lp - lse);
+                    if (live && k == 0) lls[pp] = lse;
+                }
+            }
+        } else {
+            for (int e = threadIdx.x; e < np * K; e += kEmT) rs[e] = logp(e / K, e % K);
+            __syncthreads();
+            if (HARD && threadIdx.x < np) {   // nearest center, ties to the lowest k: one-hot
+                double *ri = rs + threadIdx.x * K;
+                int kb = 0;
+                for (int k = 1; k < K; ++k)
+                    if (ri[k] > ri[kb]) kb = k;
+                lls[threadIdx.x] = -ri[kb];   // (inertia)
+                for (int k = 0; k < K; ++k) ri[k] = k == kb ? 1.0 : 0.0;
+            } else if (threadIdx.x < np) {   // normalise point t0 + threadIdx.x (fixed k order)
+                double *ri = rs + threadIdx.x * K;
+                double mx = -INFINITY;
+                for (int k = 0; k < K; ++k) mx = fmax(mx, ri[k]);
+                double den = 0.0;
+                for (int k = 0; k < K; ++k) den += exp(ri[k] - mx);
+                const double lse = mx + log(den);
+                for (int k = 0; k < K; ++k) ri[k] = exp(ri[k] - lse);
+                lls[threadIdx.x] = lse;
+            }
         }
         __syncthreads();
-        if (HARD && threadIdx.x < np) {   // nearest center, ties to the lowest k: one-hot
-            double *ri = rs + threadIdx.x * K;
-            int kb = 0;
-            for (int k = 1; k < K; ++k)
-                if (ri[k] > ri[kb]) kb = k;
-            lls[threadIdx.x] = -ri[kb];   // (inertia)
-            for (int k = 0; k < K; ++k) ri[k] = k == kb ? 1.0 : 0.0;
-        } else if (threadIdx.x < np) {   // normalise point t0 + threadIdx.x (fixed k order)
-            double *ri = rs + threadIdx.x * K;
-            double mx = -INFINITY;
-            for (int k = 0; k < K; ++k) mx = fmax(mx, ri[k]);
-            double den = 0.0;
-            for (int k = 0; k < K; ++k) den += exp(ri[k] - mx);
-            const double lse = mx + log(den);
-            for (int k = 0; k < K; ++k) ri[k] = exp(ri[k] - lse);
-            lls[threadIdx.x] = lse;
-        }
-        __syncthreads();
+        if constexpr (OWN) {
+            if (owner) {
+                for (int p = 0; p < np; ++p) {
+                    const double r = rs[p * K + ok];
+                    const double *xp = xs + p * XS;
+                    const double ra = r * xp[oa];
+                    on += r;
+                    osum += ra;
 #pragma unroll
-        for (int u = 0; u < MAXS; ++u) {
+                    for (int b = 0; b < DM; ++b)
+                        if (b < d) oxx[b] = fma(ra, xp[b], oxx[b]);
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < (OWN ? 0 : MAXS); ++u) {
             if (sk_[u] < 0) continue;
             const int k = sk_[u], a = sa[u], b = sb[u];
             double v = acc[u];
             for (int p = 0; p < np; ++p) {
                 const double r = rs[p * K + k];
-                const double f = a < 0 ? 1.0 : (b < 0 ? xs[p * d + a] : xs[p * d + a] * xs[p * d + b]);
+                const double f = a < 0 ? 1.0 : (b < 0 ? xs[p * XS + a] : xs[p * XS + a] * xs[p * XS + b]);
                 v = fma(r, f, v);
             }
             acc[u] = v;
@@ -217,8 +292,19 @@ __global__ void __launch_bounds__(kEmT) k_em_estep(const float *__restrict__ x, 
         __syncthreads();
     }
     double *out = part + (long long)blockIdx.x * (S + 1);
+    if constexpr (OWN) {
+        if (owner) {
+            double *ok_out = out + ok * per;
+            if (oa == 0) ok_out[0] = on;
+            ok_out[1 + oa] = osum;
+            const int o0 = 1 + d + oa * d - oa * (oa - 1) / 2;   // packed (a, a)
 #pragma unroll
-    for (int u = 0; u < MAXS; ++u) {
+            for (int b = 0; b < DM; ++b)
+                if (b >= oa && b < d) ok_out[o0 + (b - oa)] = oxx[b];
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < (OWN ? 0 : MAXS); ++u) {
         const int st = threadIdx.x + u * kEmT;
         if (st < S) out[st] = acc[u];
     }
@@ -278,29 +364,30 @@ __global__ void k_em_out(const double *base, int K, int d, float *w, float *mu, 
     if (threadIdx.x == 0 && ll_out) *ll_out = *s.LL;
 }
 
-template <int MAXS, int DM, bool HARD>
+template <int MAXS, int DM, bool HARD, bool OWN>
 static cudaError_t launch_estep_d(const float *x, long long n, int d, int K, const double *base, double *part,
                                   cudaStream_t st) {
-    const size_t smem = sizeof(double) * ((size_t)kEmTile * (d + K) + kEmTile + (size_t)K * (DM * DM + DM + 1));
-    cudaError_t e = cudaFuncSetAttribute(k_em_estep<MAXS, DM, HARD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    const size_t smem = sizeof(double) * ((size_t)kEmTile * (em_xs(d) + K) + kEmTile + (size_t)K * (DM * DM + DM + 5));
+    cudaError_t e = cudaFuncSetAttribute(k_em_estep<MAXS, DM, HARD, OWN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
-    k_em_estep<MAXS, DM, HARD><<<kEmBlocks, kEmT, smem, st>>>(x, n, d, K, base, part);
+    k_em_estep<MAXS, DM, HARD, OWN><<<kEmBlocks, kEmT, smem, st>>>(x, n, d, K, base, part);
     return cudaGetLastError();
 }
-template <int MAXS, bool HARD>
+template <int MAXS, bool HARD, bool OWN>
 static cudaError_t launch_estep_m(const float *x, long long n, int d, int K, const double *base, double *part,
                                   cudaStream_t st) {
-    if (d <= 8) return launch_estep_d<MAXS, 8, HARD>(x, n, d, K, base, part, st);
-    if (d <= 16) return launch_estep_d<MAXS, 16, HARD>(x, n, d, K, base, part, st);
-    return launch_estep_d<MAXS, 32, HARD>(x, n, d, K, base, part, st);
+    if (d <= 8) return launch_estep_d<MAXS, 8, HARD, OWN>(x, n, d, K, base, part, st);
+    if (d <= 16) return launch_estep_d<MAXS, 16, HARD, OWN>(x, n, d, K, base, part, st);
+    return launch_estep_d<MAXS, 32, HARD, OWN>(x, n, d, K, base, part, st);
 }
 template <bool HARD>
 static cudaError_t launch_estep(int maxs, const float *x, long long n, int d, int K, const double *base,
                                 double *part, cudaStream_t st) {
-    if (maxs <= 8) return launch_estep_m<8, HARD>(x, n, d, K, base, part, st);
-    if (maxs <= 20) return launch_estep_m<20, HARD>(x, n, d, K, base, part, st);
-    return launch_estep_m<40, HARD>(x, n, d, K, base, part, st);
+    if (K * d <= kEmT) return launch_estep_m<1, HARD, true>(x, n, d, K, base, part, st);
+    if (maxs <= 8) return launch_estep_m<8, HARD, false>(x, n, d, K, base, part, st);
+    if (maxs <= 20) return launch_estep_m<20, HARD, false>(x, n, d, K, base, part, st);
+    return launch_estep_m<40, HARD, false>(x, n, d, K, base, part, st);
 }
 
 // iters EM steps from the start above; the state (em_state_doubles) and partials
@@ -313,7 +400,6 @@ cudaError_t launch_gmm_fit(const float *x, long long n, int d, int K, const int 
     const int maxs = (S + kEmT - 1) / kEmT;
     if (d < 1 || d > 32 || K < 1 || maxs > 40) return cudaErrorInvalidValue;
     k_em_init<<<1, kEmT, 0, st>>>(x, d, K, idx, cov0, reg, state);
-    const size_t smem_chol = 2 * sizeof(double) * d * d;
     double *tot = part + em_partial_doubles(K, d);   // [S + 1] after the partials
     const int rblocks = (32 * (S + 1) + kEmT - 1) / kEmT;
     cudaError_t e = cudaSuccess;
@@ -325,7 +411,9 @@ cudaError_t launch_gmm_fit(const float *x, long long n, int d, int K, const int 
         else k_em_mstep<<<1, kEmT, 0, st>>>(tot, n, d, K, reg, state);
     }
     for (int it = 0; it <= iters; ++it) {
-        k_em_chol<<<K, kEmT, smem_chol, st>>>(state, K, d, flags);
+        if (d <= 8) k_em_chol<8><<<K, 32, 0, st>>>(state, K, d, flags);
+        else if (d <= 16) k_em_chol<16><<<K, 32, 0, st>>>(state, K, d, flags);
+        else k_em_chol<32><<<K, 32, 0, st>>>(state, K, d, flags);
         e = launch_estep<false>(maxs, x, n, d, K, state, part, st);
         if (e != cudaSuccess) return e;
         k_em_reduce<<<rblocks, kEmT, 0, st>>>(part, kEmBlocks, S + 1, tot);
