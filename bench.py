@@ -327,17 +327,21 @@ class Single(Workload):
                "last_step_split_ms": getattr(self, "split_ms", None)}
         if hasattr(self, "inner"):
             out["subsample_inner_iterations"] = self.inner["iterations"]
-        if self.name == "c1" and not self.sharded:   # NEXT-1: Anderson (memory 5, R-27) on the same step
+        if not self.sharded and not self.args.no_anderson:   # NEXT-1: Anderson (memory 5, R-27), same step
             import torch
+            reps = 5 if self.name == "c1" else (1 if self.name == "c4" else 3)
             self._run(self.x, self.y, anderson=5)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            for _ in range(5):
-                self._run(self.x, self.y, anderson=5)
+            for _ in range(reps):
+                ent = self._run(self.x, self.y, anderson=5)
             e1.record()
             torch.cuda.synchronize()
-            out["anderson5"] = {"time_to_tol_ms": e0.elapsed_time(e1) / 5, "iterations": self.rep["iterations"],
-                                "note": "same init + Anderson (memory 5) to the same tol"}
+            ms = e0.elapsed_time(e1) / reps
+            out["anderson5"] = {"time_to_tol_ms": ms, "iterations": self.rep["iterations"],
+                                "converged": self.rep["converged"], "cost_entries_per_s": ent * self.world / (ms / 1e3),
+                                "solve_ms": self.rep["solve_ms"],
+                                "note": "same init + Anderson (memory 5) to the same tol (K13 / K19)"}
         return out
 
     def cpu_sample(self, target_s=10.0):
@@ -592,6 +596,7 @@ def main():
     ap.add_argument("--init", default=None,
                     help="c3/c4/c5 initializer: zero|gaussian|gmm (fitted on the device)|gmm_given|subsample")
     ap.add_argument("--gmm-iters", type=int, default=50, help="EM iterations of the device GMM fit (init gmm)")
+    ap.add_argument("--no-anderson", action="store_true", help="skip the Anderson time-to-tol extra")
     ap.add_argument("--gmm-kmeans-iters", type=int, default=10,
                     help="Lloyd steps of the fit's k-means start (R-28; sklearn's default start), 0 = start at x[idx]")
     ap.add_argument("--eps-factor", type=float, default=None)

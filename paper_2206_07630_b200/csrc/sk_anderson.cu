@@ -1,0 +1,166 @@
+// sk_anderson.cu — K19: Anderson acceleration ("Anderson
+// acceleration (And = 5)"; R-27) on the multi-kernel solver (K2 / K3 / K4 passes).
+// Sweep l evaluates g~ = g_sk(f^l) (column pass + merge) and T(f^l) = f_sk(g~) (row pass +
+// merge, which also sums err_l = sum_i a_i |expm1((f^l_i - T(f^l)_i)/eps)| and takes the stop
+// decision); then, unless stopped:
+//   k_and_dots  : r = T(f^l) - f^l into the ring slot `head` with T(f^l), and per-block fp64
+//                 partials of <r, R_u> for the filled slots (fixed grid: deterministic);
+//   k_and_solve : one warp: fixed-order sums of the partials -> the Gram row/column of the
+//                 slot, alpha from (G + lam I) x = 1 (lam = 1e-8 tr G / count, 1 if tr G = 0),
+//                 alpha = x / sum x (Gauss-Jordan, lane r holds row r), the ring advances;
+//   k_and_mix   : f^{l+1} = sum_u alpha_u T(f_u) over the filled slots, written over T(f^l) in
+//                 the potential buffer with its packed w (and the K3 image's w columns).
+// All three return at once when the stop flag is set.  State lives on the device (no host
+// round trip per sweep).
+#include "sk_internal.h"
+#include "sk_common.cuh"
+
+namespace sk {
+
+constexpr int kAT = 256;
+constexpr int kAndBlocks = 296;
+constexpr int kAndM = 8;   // largest memory
+
+struct AndState {
+    int head, cnt;
+    double G[kAndM * kAndM];
+    double alpha[kAndM];
+};
+
+size_t anderson_state_bytes() { return sizeof(AndState); }
+size_t anderson_blk_doubles() { return (size_t)kAndBlocks * kAndM; }
+
+// F, R: [mem][n] fp32 ring; blk: [kAndBlocks][kAndM]
+__global__ void __launch_bounds__(kAT) k_and_dots(Side X, const DevStatus *st, const AndState *as, int mem,
+                                                   float *F, float *R, double *blk) {
+    __shared__ double red[kAT / 32][kAndM];
+    if (*(volatile const int *)&st->stop) return;
+    const int l1 = st->iter;   // = l + 1 after the row merge of sweep l
+    const float *f = (l1 & 1) ? X.pot[0] : X.pot[1];   // f^l   = pot[l & 1]
+    const float *T = (l1 & 1) ? X.pot[1] : X.pot[0];   // T(f^l) = pot[(l + 1) & 1]
+    const int head = as->head, cn = as->cnt < mem ? as->cnt + 1 : mem;
+    const long long n = X.P;
+    double acc[kAndM];
+#pragma unroll
+    for (int u = 0; u < kAndM; ++u) acc[u] = 0.0;
+    for (long long i = blockIdx.x * (long long)kAT + threadIdx.x; i < n; i += (long long)gridDim.x * kAT) {
+        const float t = T[i], r = t - f[i];
+        F[(long long)head * n + i] = t;
+#pragma unroll
+        for (int u = 0; u < kAndM; ++u)
+            if (u < cn) acc[u] = fma((double)r, (double)(u == head ? r : R[(long long)u * n + i]), acc[u]);
+        R[(long long)head * n + i] = r;
+    }
+    const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
+#pragma unroll
+    for (int u = 0; u < kAndM; ++u) {
+        double v = acc[u];
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (ln == 0) red[w][u] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < kAndM) {
+        double v = 0.0;
+        for (int k = 0; k < kAT / 32; ++k) v += red[k][threadIdx.x];
+        blk[(long long)blockIdx.x * kAndM + threadIdx.x] = v;
+    }
+}
+
+__global__ void __launch_bounds__(32) k_and_solve(const DevStatus *st, AndState *as, int mem, const double *blk,
+                                                   int nblk) {
+    if (*(volatile const int *)&st->stop) return;
+    const int lane = threadIdx.x, head = as->head, cn = as->cnt < mem ? as->cnt + 1 : mem;
+    double dl = 0.0;   // <r_new, r_lane>, summed over the blocks in order
+    if (lane < cn)
+        for (int b = 0; b < nblk; ++b) dl += blk[(long long)b * kAndM + lane];
+    double row[kAndM];
+#pragma unroll
+    for (int u = 0; u < kAndM; ++u) {
+        const double du = __shfl_sync(0xffffffffu, dl, u);   // <r_new, r_u>
+        double gv;
+        if (lane == head) gv = du;
+        else if (u == head) gv = dl;
+        else gv = lane < kAndM ? as->G[lane * kAndM + u] : 0.0;
+        row[u] = (lane < cn && u < cn) ? gv : (u == lane ? 1.0 : 0.0);
+    }
+    __syncwarp();
+    if (lane < cn) {   // the Gram row/column of the new slot, for later sweeps
+        as->G[head * kAndM + lane] = dl;
+        as->G[lane * kAndM + head] = dl;
+    }
+    double diag = 0.0;
+#pragma unroll
+    for (int u = 0; u < kAndM; ++u)
+        if (u == lane) diag = row[u];
+    double tr = lane < cn ? diag : 0.0;
+    for (int o = 16; o > 0; o >>= 1) tr += __shfl_xor_sync(0xffffffffu, tr, o);
+    const double lam = tr > 0.0 ? 1e-8 * tr / cn : 1.0;
+#pragma unroll
+    for (int u = 0; u < kAndM; ++u)
+        if (u == lane && lane < cn) row[u] += lam;
+    double rhs = lane < cn ? 1.0 : 0.0;
+    for (int c = 0; c < cn; ++c) {   // Gauss-Jordan, pivots in order
+        double piv[kAndM], myc = 0.0;
+#pragma unroll
+        for (int u = 0; u < kAndM; ++u) {
+            piv[u] = __shfl_sync(0xffffffffu, row[u], c);
+            if (u == c) myc = row[u];
+        }
+        const double prhs = __shfl_sync(0xffffffffu, rhs, c);
+        const double pcc = __shfl_sync(0xffffffffu, myc, c);
+        if (lane != c) {
+            const double q = myc / pcc;
+#pragma unroll
+            for (int u = 0; u < kAndM; ++u) row[u] = fma(-q, piv[u], row[u]);
+            rhs = fma(-q, prhs, rhs);
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < kAndM; ++u)
+        if (u == lane) diag = row[u];
+    const double xl = lane < cn ? rhs / diag : 0.0;
+    double sx = xl;
+    for (int o = 16; o > 0; o >>= 1) sx += __shfl_xor_sync(0xffffffffu, sx, o);
+    if (lane < kAndM) as->alpha[lane] = lane < cn ? xl / sx : 0.0;
+    if (lane == 0) {
+        as->head = (head + 1) % mem;
+        as->cnt = cn;
+    }
+}
+
+__global__ void __launch_bounds__(kAT) k_and_mix(Side X, const DevStatus *st, const AndState *as, const float *F,
+                                                  float eps) {
+    if (*(volatile const int *)&st->stop) return;
+    const int l1 = st->iter;
+    float *fn = (l1 & 1) ? X.pot[1] : X.pot[0];   // the slot holding T(f^l) -> f^{l+1}
+    const int cn = as->cnt;   // (advanced by k_and_solve)
+    double al[kAndM];
+#pragma unroll
+    for (int u = 0; u < kAndM; ++u) al[u] = as->alpha[u];
+    const float kap = kLog2e / eps;
+    const long long n = X.P;
+    for (long long i = blockIdx.x * (long long)kAT + threadIdx.x; i < n; i += (long long)gridDim.x * kAT) {
+        double v = 0.0;
+#pragma unroll
+        for (int u = 0; u < kAndM; ++u)
+            if (u < cn) v = fma(al[u], (double)F[(long long)u * n + i], v);
+        const float h = (float)v;
+        fn[i] = h;
+        const float wn = fmaf(h, kap, -X.nk[i]);
+        const long long t = i / X.tq, o = i % X.tq;
+        X.pack[t * (long long)(X.D + 1) * X.tq + (long long)X.D * X.tq + o] = wn;
+        if (X.tcimg) tc_put_w(X.tcimg, X.P, i, wn, X.tc_c);
+    }
+}
+
+cudaError_t launch_anderson_step(const Side &X, const DevStatus *st, void *state, int mem, float *F, float *R,
+                                 double *blk, float eps, cudaStream_t s) {
+    if (mem < 2 || mem > kAndM) return cudaErrorInvalidValue;
+    AndState *as = (AndState *)state;
+    k_and_dots<<<kAndBlocks, kAT, 0, s>>>(X, st, as, mem, F, R, blk);
+    k_and_solve<<<1, 32, 0, s>>>(st, as, mem, blk, kAndBlocks);
+    k_and_mix<<<kAndBlocks, kAT, 0, s>>>(X, st, as, F, eps);
+    return cudaGetLastError();
+}
+
+}  // namespace sk

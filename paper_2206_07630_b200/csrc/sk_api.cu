@@ -83,7 +83,7 @@ enum BufId {
     B_STAGE0 = 0, B_STAGE_END = 16,   // staging of host arrays
     B_FLAG = 16, B_XPACK, B_XC, B_XNK, B_XPOT, B_YPACK, B_YC, B_YNK, B_YPOT, B_PART, B_BLKE, B_BLKB,
     B_STATUS, B_COST, B_REP, B_SORT, B_PERM, B_YSORT, B_GAUSS, B_GAUSS2, B_GMM, B_SUBW, B_SUBZ,
-    B_SUBF, B_SUBG, B_IDX, B_OUT, B_FA, B_QUEUE, B_XIMG, B_YIMG, B_XLSE, B_YLSE, B_TCMAX, B_EMST, B_EMPART, B_EMIDX, B_VJP, B_NBUF
+    B_SUBF, B_SUBG, B_IDX, B_OUT, B_FA, B_QUEUE, B_XIMG, B_YIMG, B_XLSE, B_YLSE, B_TCMAX, B_EMST, B_EMPART, B_EMIDX, B_VJP, B_ANDFR, B_ANDBLK, B_ANDST, B_NBUF
 };
 
 sk_status fail(sk_ctx *c, sk_status s, const char *fmt, ...) {
@@ -303,11 +303,14 @@ struct LaunchTimer {
 };
 
 sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, sk_report *rep) {
-    if (ctx->anderson >= 2)
-        return fail(ctx, SK_EUNSUPPORTED, "Anderson acceleration runs on the on-chip solver only (small problems)");
     cudaStream_t st = ctx->stream;
     LaunchTimer tm(ctx);
     const bool sharded = P.world > 1;
+    // Anderson (R-27, K19): unsharded, one slice, omega = 1 (the rows of every iterate must be
+    // exact for the fused error); the stored path runs the separate row/column passes
+    const int amem = ctx->anderson >= 2 ? ctx->anderson : 0;
+    if (amem && (sharded || P.partitioned || slices.size() != 1 || P.omega != 1.f))
+        return fail(ctx, SK_EUNSUPPORTED, "Anderson acceleration runs on the unsharded solvers only");
     if (P.omega != 1.f && (sharded || P.partitioned))
         return fail(ctx, SK_EUNSUPPORTED, "relaxation (omega != 1) is supported by the unsharded solver only");
     if (ctx->decay_init > 0.f && (sharded || P.partitioned))
@@ -391,7 +394,7 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
     // online FFMA path: per-point LSE seeds for the max-free (seeded) passes from sweep 3 on
     // stored mode with the fused sweep (one persistent CTA per SM): 8 blocks x split_q = one wave
     static const int fused_env = [] { const char *e = getenv("SK_FUSED"); return e ? atoi(e) : 1; }();
-    const bool fused = stored && fused_env != 0 && stored_fused_supported(m) && P.omega == 1.f;
+    const bool fused = stored && fused_env != 0 && stored_fused_supported(m) && P.omega == 1.f && !amem;
     const bool seedable = !stored;
     if (tc) {   // the seeded passes' exact fallback reads the caller's coordinates
         for (int i = 0; i < ns; ++i) { X[i].raw = slices[i].x; X[i].tcimg = (unsigned char *)ximg + offi[i]; X[i].tc_c = tc_fold_c(); }
@@ -447,8 +450,21 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
         ctx->cnt.kernel_launches += ns + 1;
     }
     static const float tc_margin = [] { const char *e = getenv("SK_TC_SEED_MARGIN"); return e ? (float)atof(e) : 4.f; }();
-    CU(launch_status_init(status, P.max_iter, P.check_every, P.tol, st));
+    CU(launch_status_init(status, P.max_iter, P.check_every, P.tol, st, amem ? 1 : 0));
     ctx->cnt.kernel_launches += ns + 2;
+    float *andF = nullptr, *andR = nullptr;
+    double *andblk = nullptr;
+    void *andst = nullptr;
+    if (amem) {
+        ENSURE(afr, float, B_ANDFR, 2 * (size_t)amem * slices[0].n);
+        ENSURE(ablk, double, B_ANDBLK, anderson_blk_doubles());
+        ENSURE(ast, char, B_ANDST, anderson_state_bytes());
+        andF = afr;
+        andR = afr + (size_t)amem * slices[0].n;
+        andblk = ablk;
+        andst = ast;
+        CU(cudaMemsetAsync(andst, 0, anderson_state_bytes(), st));
+    }
 
     std::vector<float *> C(ns, nullptr);
     double build_ms = 0.0;
@@ -474,6 +490,7 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
     MergePass mcol{MERGE_COL, &Y, part, nsplit_col, P.eps, P.b, status, blke, blkb, nullptr, 0.f,
                    sharded ? 1 : 0, 0};
     mcol.omega = P.omega;
+    mcol.anderson = amem ? 1 : 0;
     if (col_seed) mcol.Q = &X[0];
     int sweep = 0;   // sweeps enqueued so far (seeded passes from the third on)
 
@@ -582,8 +599,13 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
                 mrow.wts = slices[i].a;   // (the relaxed row error term weighs rows by a)
                 mrow.tc_fold = tc && row_seed && sweep >= 1;   // the next row pass is seeded
                 mrow.tc_margin = tc_margin;
+                mrow.anderson = amem ? 1 : 0;
                 CU(launch_merge(mrow, st));
                 launched += 2;
+                if (amem) {   // f^{l+1} = sum_u alpha_u T(f_u) over the pot/pack/image of X
+                    CU(launch_anderson_step(X[0], status, andst, amem, andF, andR, andblk, P.eps, st));
+                    launched += 3;
+                }
             }
             ++sweep;
         }
@@ -626,14 +648,15 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
     if (P.omega != 1.f) E -= (double)P.eps * hs.mass_dev;
     for (int i = 0; i < ns; ++i)
         CU(cudaMemcpyAsync(slices[i].f, X[i].pot[L & 1], sizeof(float) * slices[i].n, cudaMemcpyDeviceToDevice, st));
-    CU(cudaMemcpyAsync(P.g, Y.pot[L & 1], sizeof(float) * m, cudaMemcpyDeviceToDevice, st));
+    // (Anderson: the pair is (f^L, g_sk(f^L)), g one buffer ahead; L + 1 sweeps were evaluated)
+    CU(cudaMemcpyAsync(P.g, Y.pot[(L + (amem ? 1 : 0)) & 1], sizeof(float) * m, cudaMemcpyDeviceToDevice, st));
     ctx->cnt.kernel_launches += launched;
     ctx->cnt.lse_launches += (long long)(ns + 1) * (hs.iter + 1);
     if (ctx->timing) ctx->cnt.lse_ms += ms;
-    const double entries = (double)n_sum * m * (2.0 * L + 1.0);
+    const double entries = (double)n_sum * m * (amem ? 2.0 * (L + 1) : 2.0 * L + 1.0);
     ctx->cnt.lse_ex2 += entries;
     if (stored) ctx->cnt.lse_bytes += 4.0 * (double)n_sum * m * (fused ? (1.0 + hs.iter) : (2.0 * L + 1.0));
-    rep->iterations = L;
+    rep->iterations = amem ? L + 1 : L;
     rep->converged = hs.converged;
     rep->marginal_error = hs.err;
     rep->dual_objective = E;

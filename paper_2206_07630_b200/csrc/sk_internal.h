@@ -68,6 +68,7 @@ struct DevStatus {
     int colfail;     // stored fused sweep: some column sum left the scaled range -> exact column pass
     double row_err;  // relaxed (omega != 1): sum_i a_i |expm1((f_i - fsk_i)/eps)| of the last row merge
     double mass_dev; //                        sum_ij P_ij - sum_i a_i = sum_i a_i expm1((f_i - fsk_i)/eps)
+    int g_off;       // Anderson (R-27): the returned g is g_sk(f^L), in buffer [(L + 1) & 1]
 };
 
 // Packed tile layout of one side: tiles of tq points; tile t at t*(D+1)*tq floats:
@@ -165,8 +166,16 @@ struct MergePass {
     int tc_fold = 0;          // K3 side: also fold lse + margin as the next pass's row shift
     float tc_margin = 4.f;    //          log2 units above the LSE (SK_TC_SEED_MARGIN: test knob)
     float omega = 1.f;        // Alg. 1's relaxation: h <- (1 - omega) h_old + omega h_sinkhorn
+    int anderson = 0;         // Anderson (R-27): COL takes no decision; ROW sums err_l of (f^l, g~)
+                              // and decides (checked at (l + 1) % k == 0 and l + 1 = max_iter)
 };
 cudaError_t launch_merge(const MergePass &M, cudaStream_t st);
+// K19 Anderson step after the row merge of a sweep (sk_anderson.cu): state = anderson_state_bytes()
+// (zeroed before the solve), F/R = 2 x mem x n floats, blk = anderson_blk_doubles().
+size_t anderson_state_bytes();
+size_t anderson_blk_doubles();
+cudaError_t launch_anderson_step(const Side &X, const DevStatus *st, void *state, int mem, float *F, float *R,
+                                 double *blk, float eps, cudaStream_t s);
 constexpr int kMergeMaxBlocks = 1184;   // blk_err holds 2 x kMergeMaxBlocks doubles
 int merge_blocks(int P);
 
@@ -175,7 +184,7 @@ cudaError_t launch_report(const Side &X, const Side &Y, const float *a, const fl
                           DevStatus *st, int local_only, long long n_uniform, cudaStream_t s);
 
 cudaError_t launch_status_init(DevStatus *st, int max_iter, int check_every, float tol,
-                               cudaStream_t s);
+                               cudaStream_t s, int g_off = 0);
 cudaError_t launch_report_blocks(const Side &X, const float *a, float eps, DevStatus *st, long long n_uniform,
                                  long long row0, long long bs, double *out, cudaStream_t s);
 

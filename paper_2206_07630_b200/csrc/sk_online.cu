@@ -336,6 +336,10 @@ __device__ __forceinline__ void merge_point(const MergePass &Mp, const Side &S, 
         if (Mp.tc_fold) tc_put_shift(S.tcimg, S.P, p, lse2 + Mp.tc_margin, S.tc_c);
     }
     bad |= !isfinite(hn);
+    if (Mp.anderson && Mp.mode == MERGE_ROW) {   // row term of err_l for (f^l, g~): columns are exact
+        const double ai = Mp.wts ? (double)Mp.wts[p] : 1.0 / S.P;
+        e += ai * fabs((double)expm1f((hold[p] - hsk) / eps));
+    }
     if (check) {
         const double bj = Mp.wts ? (double)Mp.wts[p] : 1.0 / S.P;
         e += bj * fabs((double)expm1f((hold[p] - hsk) / eps));   // column term of err_l (H5)
@@ -358,7 +362,7 @@ __global__ void __launch_bounds__(kMT) k_merge(MergePass Mp, Side S, Side Qs) {
     if (st && *(volatile int *)&st->stop) return;
     if (Mp.only_if && !*(volatile const int *)Mp.only_if) return;
     const int l = st ? st->iter : 0;
-    const bool check = Mp.mode == MERGE_COL && l >= 1 &&
+    const bool check = Mp.mode == MERGE_COL && !Mp.anderson && l >= 1 &&
                        (l % st->check_every == 0 || l == st->max_iter);
     const float *hold = (l & 1) ? S.pot[1] : S.pot[0];      // no dynamic param indexing
     float *hnew = (l & 1) ? S.pot[0] : S.pot[1];
@@ -456,6 +460,19 @@ __global__ void __launch_bounds__(kMT) k_merge(MergePass Mp, Side S, Side Qs) {
             if ((float)et < st->tol) { st->converged = 1; st->stop = 1; st->final_iter = l; }
             else if (l >= st->max_iter) { st->stop = 1; st->final_iter = l; }
         }
+    } else if (Mp.mode == MERGE_ROW && Mp.anderson) {
+        // Anderson: sweep l + 1 evaluated; the result would be (f^l, g~) (g in buffer (l + 1) & 1)
+        st->ticket_row = 0;
+        const int l1 = l + 1;
+        if (bt) { st->nonfinite = 1; st->stop = 1; st->final_iter = l; }
+        else {
+            if (l1 % st->check_every == 0 || l1 >= st->max_iter) {
+                st->err = (float)et;
+                if ((float)et < st->tol) { st->converged = 1; st->stop = 1; st->final_iter = l; }
+            }
+            if (!st->stop && l1 >= st->max_iter) { st->stop = 1; st->final_iter = l; }
+            if (!st->stop) st->iter = l1;
+        }
     } else if (Mp.mode == MERGE_ROW) {
         st->ticket_row = 0;
         if (Mp.omega != 1.f) { st->row_err = et; st->mass_dev = et2; }
@@ -487,8 +504,8 @@ __global__ void __launch_bounds__(1024) k_report(Side X, Side Y, const float *a,
                                                   float eps, DevStatus *st, int local_only,
                                                   long long n_uniform) {
     __shared__ double red[32];
-    const int l = st->final_iter;
-    const float *f = (l & 1) ? X.pot[1] : X.pot[0], *g = (l & 1) ? Y.pot[1] : Y.pot[0];
+    const int l = st->final_iter, lg = l + st->g_off;
+    const float *f = (l & 1) ? X.pot[1] : X.pot[0], *g = (lg & 1) ? Y.pot[1] : Y.pot[0];
     double s = 0.0;
     for (int i = threadIdx.x; i < X.P; i += 1024) {
         const double ai = a ? (double)a[i] : 1.0 / n_uniform;
@@ -510,8 +527,9 @@ cudaError_t launch_report(const Side &X, const Side &Y, const float *a, const fl
     return cudaGetLastError();
 }
 
-__global__ void k_status_init(DevStatus *st, int max_iter, int check_every, float tol) {
+__global__ void k_status_init(DevStatus *st, int max_iter, int check_every, float tol, int g_off) {
     DevStatus z = {};
+    z.g_off = g_off;
     z.max_iter = max_iter;
     z.check_every = check_every;
     z.tol = tol;
@@ -547,8 +565,8 @@ cudaError_t launch_report_blocks(const Side &X, const float *a, float eps, DevSt
 }
 
 cudaError_t launch_status_init(DevStatus *st, int max_iter, int check_every, float tol,
-                               cudaStream_t s) {
-    k_status_init<<<1, 1, 0, s>>>(st, max_iter, check_every, tol);
+                               cudaStream_t s, int g_off) {
+    k_status_init<<<1, 1, 0, s>>>(st, max_iter, check_every, tol, g_off);
     return cudaGetLastError();
 }
 

@@ -25,8 +25,8 @@ def _cuda(a):
     return torch.from_numpy(np.ascontiguousarray(a)).cuda()
 
 
-def check_anderson(O, sk, ctx, x, y, eps, mem, f0=None, a=None, tol=1e-3, what=""):
-    f, g, rep = sk.sinkhorn_solve(ctx, _cuda(x), _cuda(y), eps, tol=tol, anderson=mem,
+def check_anderson(O, sk, ctx, x, y, eps, mem, f0=None, a=None, tol=1e-3, what="", mode="auto"):
+    f, g, rep = sk.sinkhorn_solve(ctx, _cuda(x), _cuda(y), eps, tol=tol, anderson=mem, mode=mode,
                                   a=None if a is None else _cuda(a),
                                   f_init=None if f0 is None else _cuda(np.asarray(f0, np.float32)))
     f, g = f.cpu().numpy(), g.cpu().numpy()
@@ -99,6 +99,21 @@ def test_anderson_batched_sort1d(O, ctx):
         assert abs(reps[k]["dual_objective"] - ref.E) <= 3e-5 * abs(ref.E), (k, reps[k]["dual_objective"], ref.E)
 
 
+@pytest.mark.parametrize("mode,n,m,d,mem", [("online", 3000, 2600, 3, 5), ("online", 1500, 1300, 40, 5),
+                                            ("stored", 2000, 1024, 16, 4), ("online", 2100, 1800, 8, 3)])
+def test_anderson_multikernel(O, ctx, mode, n, m, d, mem):
+    """K19 on the online FFMA (K2), tensor-core (K3, d = 40) and stored (K4) solvers."""
+    import paper_2206_07630_b200 as sk
+    rng = np.random.default_rng(n + d + 7)
+    x = rng.random((n, d)).astype(np.float32)
+    y = (rng.random((m, d)) * 0.9 + 0.05).astype(np.float32)
+    a = gen.random_weights(n, rng)
+    eps = float(np.float32(0.03 * gen.mean_sq_cost(x, y)))
+    rep = check_anderson(O, sk, ctx, x, y, eps, mem, a=a, mode=mode, what=f"{mode} {n}x{m}x{d} mem={mem}")
+    _, _, r0 = sk.sinkhorn_solve(ctx, _cuda(x), _cuda(y), eps, a=_cuda(a), mode=mode)
+    assert rep["iterations"] < r0["iterations"]
+
+
 def test_anderson_max_iter_and_check_every(O, ctx):
     """An unreachable tol runs exactly max_iter sweeps and returns (f^{L-1}, g_sk(f^{L-1})); check_every
     > 1 stops on a multiple of it."""
@@ -123,8 +138,12 @@ def test_anderson_argument_and_path_errors(ctx):
     with pytest.raises(sk.SinkhornError):   # combined with eps-decay
         sk.sinkhorn_solve(ctx, x, y, p.eps, eps_decay=(5.0, 0.8), anderson=5)
     big = _cuda(np.random.default_rng(1).random((3000, 3)).astype(np.float32))
-    with pytest.raises(sk.SinkhornError):   # multi-kernel paths: unsupported
-        sk.sinkhorn_solve(ctx, big, big, 0.01, mode="online", anderson=5)
+    with pytest.raises(sk.SinkhornError):   # the sharded entries: unsupported
+        ctx.check(ctx.lib.sk_set_anderson(ctx.h, 5))
+        try:
+            sk.sinkhorn_solve_sharded_emulated(ctx, 2, big, big, 0.01, mode="online")
+        finally:
+            ctx.lib.sk_set_anderson(ctx.h, 0)
     # the context is back to plain Sinkhorn afterwards
     _, _, r = sk.sinkhorn_solve(ctx, x, y, p.eps)
     assert r["iterations"] > 100
