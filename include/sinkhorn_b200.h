@@ -132,10 +132,11 @@ sk_status sk_set_eps_decay(sk_ctx *ctx, float init, float rate);
  * sum alpha = 1 (R = residuals T(f_u) - f_u, lam = 1e-8 tr(R^T R) / count, or 1 when all
  * residuals are 0).  The result is
  * (f^l, g~) of the last sweep and rep.iterations the sweeps evaluated.  mem in {0, 1}: off (the
- * default); mem in [2, 8]: on; otherwise SK_EINVAL.  Runs in sinkhorn_solve on every path (the
- * on-chip solver K13; the online FFMA / tensor-core / stored multi-kernel solvers via K19, the
- * stored one with separate row and column passes); the sharded entries, omega != 1 and
- * eps-decay return SK_EUNSUPPORTED. */
+ * default); mem in [2, 8]: on; otherwise SK_EINVAL.  Runs on every path (the on-chip solver
+ * K13; the online FFMA / tensor-core / stored multi-kernel solvers via K19, the stored one
+ * with separate row and column passes; the sharded entries sum the Gram dots and the error
+ * over the ranks: one ncclAllReduce of 9 doubles per sweep); omega != 1 and eps-decay return
+ * SK_EUNSUPPORTED. */
 sk_status sk_set_anderson(sk_ctx *ctx, int32_t mem);
 /* Enable (1) / disable (0) CUDA-event timing of the dominant kernels into sk_counters. */
 sk_status sk_set_timing(sk_ctx *ctx, int32_t enable);

@@ -1,16 +1,21 @@
 // sk_anderson.cu — K19: Anderson acceleration ("Anderson
 // acceleration (And = 5)"; R-27) on the multi-kernel solver (K2 / K3 / K4 passes).
 // Sweep l evaluates g~ = g_sk(f^l) (column pass + merge) and T(f^l) = f_sk(g~) (row pass +
-// merge, which also sums err_l = sum_i a_i |expm1((f^l_i - T(f^l)_i)/eps)| and takes the stop
-// decision); then, unless stopped:
+// merge, which also sums this slice's err_l term sum_i a_i |expm1((f^l_i - T(f^l)_i)/eps)|
+// into vec[8]); then per slice (row shard):
 //   k_and_dots  : r = T(f^l) - f^l into the ring slot `head` with T(f^l), and per-block fp64
 //                 partials of <r, R_u> for the filled slots (fixed grid: deterministic);
-//   k_and_solve : one warp: fixed-order sums of the partials -> the Gram row/column of the
-//                 slot, alpha from (G + lam I) x = 1 (lam = 1e-8 tr G / count, 1 if tr G = 0),
-//                 alpha = x / sum x (Gauss-Jordan, lane r holds row r), the ring advances;
+//   k_and_rowsum: one warp: the slice's dots summed over the blocks in order -> vec[0..8);
+// (sharded: ncclAllReduce(sum) of vec over the ranks), then once:
+//   k_and_decide: one warp: vec summed over the slices in order -> err_l and the stop decision
+//                 (checked at (l + 1) % k == 0 and l + 1 = max_iter); unless stopped, the Gram
+//                 row/column of the slot, alpha from (G + lam I) x = 1 (lam = 1e-8 tr G / count,
+//                 1 if tr G = 0), alpha = x / sum x (Gauss-Jordan, lane r holds row r), the ring
+//                 advances and the sweep counter moves to l + 1;
+// and per slice:
 //   k_and_mix   : f^{l+1} = sum_u alpha_u T(f_u) over the filled slots, written over T(f^l) in
 //                 the potential buffer with its packed w (and the K3 image's w columns).
-// All three return at once when the stop flag is set.  State lives on the device (no host
+// Every kernel returns at once when the stop flag is set.  State lives on the device (no host
 // round trip per sweep).
 #include "sk_internal.h"
 #include "sk_common.cuh"
@@ -29,15 +34,16 @@ struct AndState {
 
 size_t anderson_state_bytes() { return sizeof(AndState); }
 size_t anderson_blk_doubles() { return (size_t)kAndBlocks * kAndM; }
+size_t anderson_vec_doubles() { return 16; }
 
 // F, R: [mem][n] fp32 ring; blk: [kAndBlocks][kAndM]
 __global__ void __launch_bounds__(kAT) k_and_dots(Side X, const DevStatus *st, const AndState *as, int mem,
                                                    float *F, float *R, double *blk) {
     __shared__ double red[kAT / 32][kAndM];
     if (*(volatile const int *)&st->stop) return;
-    const int l1 = st->iter;   // = l + 1 after the row merge of sweep l
-    const float *f = (l1 & 1) ? X.pot[0] : X.pot[1];   // f^l   = pot[l & 1]
-    const float *T = (l1 & 1) ? X.pot[1] : X.pot[0];   // T(f^l) = pot[(l + 1) & 1]
+    const int l = st->iter;   // (the decision has not advanced it yet)
+    const float *f = (l & 1) ? X.pot[1] : X.pot[0];   // f^l    = pot[l & 1]
+    const float *T = (l & 1) ? X.pot[0] : X.pot[1];   // T(f^l) = pot[(l + 1) & 1]
     const int head = as->head, cn = as->cnt < mem ? as->cnt + 1 : mem;
     const long long n = X.P;
     double acc[kAndM];
@@ -66,13 +72,40 @@ __global__ void __launch_bounds__(kAT) k_and_dots(Side X, const DevStatus *st, c
     }
 }
 
-__global__ void __launch_bounds__(32) k_and_solve(const DevStatus *st, AndState *as, int mem, const double *blk,
-                                                   int nblk) {
+__global__ void __launch_bounds__(32) k_and_rowsum(const DevStatus *st, const double *blk, int nblk, double *vec) {
+    if (*(volatile const int *)&st->stop) return;
+    const int lane = threadIdx.x;
+    if (lane < kAndM) {
+        double v = 0.0;
+        for (int b = 0; b < nblk; ++b) v += blk[(long long)b * kAndM + lane];
+        vec[lane] = v;
+    }
+}
+
+__global__ void __launch_bounds__(32) k_and_decide(DevStatus *st, AndState *as, int mem, const double *vec, int ns) {
     if (*(volatile const int *)&st->stop) return;
     const int lane = threadIdx.x, head = as->head, cn = as->cnt < mem ? as->cnt + 1 : mem;
-    double dl = 0.0;   // <r_new, r_lane>, summed over the blocks in order
-    if (lane < cn)
-        for (int b = 0; b < nblk; ++b) dl += blk[(long long)b * kAndM + lane];
+    double dl = 0.0, et = 0.0;   // <r_new, r_lane> and err_l, summed over the slices in order
+    for (int i = 0; i < ns; ++i) {
+        if (lane < kAndM) dl += vec[i * 16 + lane];
+        et += vec[i * 16 + kAndM];
+    }
+    if (lane >= cn) dl = 0.0;
+    // the stop decision (every lane computes it; lane 0 writes)
+    const int l = st->iter, l1 = l + 1;
+    bool stop = false;
+    if (l1 % st->check_every == 0 || l1 >= st->max_iter) {
+        if (lane == 0) st->err = (float)et;
+        if ((float)et < st->tol) {
+            stop = true;
+            if (lane == 0) st->converged = 1;
+        }
+    }
+    if (l1 >= st->max_iter) stop = true;
+    if (stop) {
+        if (lane == 0) { st->final_iter = l; __threadfence(); st->stop = 1; }
+        return;
+    }
     double row[kAndM];
 #pragma unroll
     for (int u = 0; u < kAndM; ++u) {
@@ -125,6 +158,7 @@ __global__ void __launch_bounds__(32) k_and_solve(const DevStatus *st, AndState 
     if (lane == 0) {
         as->head = (head + 1) % mem;
         as->cnt = cn;
+        st->iter = l1;
     }
 }
 
@@ -133,7 +167,7 @@ __global__ void __launch_bounds__(kAT) k_and_mix(Side X, const DevStatus *st, co
     if (*(volatile const int *)&st->stop) return;
     const int l1 = st->iter;
     float *fn = (l1 & 1) ? X.pot[1] : X.pot[0];   // the slot holding T(f^l) -> f^{l+1}
-    const int cn = as->cnt;   // (advanced by k_and_solve)
+    const int cn = as->cnt;   // (advanced by k_and_decide)
     double al[kAndM];
 #pragma unroll
     for (int u = 0; u < kAndM; ++u) al[u] = as->alpha[u];
@@ -153,13 +187,22 @@ __global__ void __launch_bounds__(kAT) k_and_mix(Side X, const DevStatus *st, co
     }
 }
 
-cudaError_t launch_anderson_step(const Side &X, const DevStatus *st, void *state, int mem, float *F, float *R,
-                                 double *blk, float eps, cudaStream_t s) {
+cudaError_t launch_anderson_dots(const Side &X, const DevStatus *st, const void *state, int mem, float *F,
+                                 float *R, double *blk, double *vec, cudaStream_t s) {
     if (mem < 2 || mem > kAndM) return cudaErrorInvalidValue;
-    AndState *as = (AndState *)state;
-    k_and_dots<<<kAndBlocks, kAT, 0, s>>>(X, st, as, mem, F, R, blk);
-    k_and_solve<<<1, 32, 0, s>>>(st, as, mem, blk, kAndBlocks);
-    k_and_mix<<<kAndBlocks, kAT, 0, s>>>(X, st, as, F, eps);
+    k_and_dots<<<kAndBlocks, kAT, 0, s>>>(X, st, (const AndState *)state, mem, F, R, blk);
+    k_and_rowsum<<<1, 32, 0, s>>>(st, blk, kAndBlocks, vec);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_anderson_decide(DevStatus *st, void *state, int mem, const double *vec, int ns, cudaStream_t s) {
+    k_and_decide<<<1, 32, 0, s>>>(st, (AndState *)state, mem, vec, ns);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_anderson_mix(const Side &X, const DevStatus *st, const void *state, const float *F, float eps,
+                                cudaStream_t s) {
+    k_and_mix<<<kAndBlocks, kAT, 0, s>>>(X, st, (const AndState *)state, F, eps);
     return cudaGetLastError();
 }
 

@@ -25,7 +25,7 @@ typedef int (*fn_allgather)(const void *, void *, size_t, int, nccl_comm_t, cuda
 typedef int (*fn_allreduce)(const void *, void *, size_t, int, int, nccl_comm_t, cudaStream_t);
 typedef int (*fn_destroy)(nccl_comm_t);
 typedef const char *(*fn_errstr)(int);
-constexpr int kNcclFloat32 = 7, kNcclFloat64 = 8, kNcclMax = 2;
+constexpr int kNcclFloat32 = 7, kNcclFloat64 = 8, kNcclSum = 0, kNcclMax = 2;
 
 struct Nccl {
     void *h = nullptr;
@@ -83,7 +83,7 @@ enum BufId {
     B_STAGE0 = 0, B_STAGE_END = 16,   // staging of host arrays
     B_FLAG = 16, B_XPACK, B_XC, B_XNK, B_XPOT, B_YPACK, B_YC, B_YNK, B_YPOT, B_PART, B_BLKE, B_BLKB,
     B_STATUS, B_COST, B_REP, B_SORT, B_PERM, B_YSORT, B_GAUSS, B_GAUSS2, B_GMM, B_SUBW, B_SUBZ,
-    B_SUBF, B_SUBG, B_IDX, B_OUT, B_FA, B_QUEUE, B_XIMG, B_YIMG, B_XLSE, B_YLSE, B_TCMAX, B_EMST, B_EMPART, B_EMIDX, B_VJP, B_ANDFR, B_ANDBLK, B_ANDST, B_NBUF
+    B_SUBF, B_SUBG, B_IDX, B_OUT, B_FA, B_QUEUE, B_XIMG, B_YIMG, B_XLSE, B_YLSE, B_TCMAX, B_EMST, B_EMPART, B_EMIDX, B_VJP, B_ANDFR, B_ANDBLK, B_ANDVEC, B_ANDST, B_NBUF
 };
 
 sk_status fail(sk_ctx *c, sk_status s, const char *fmt, ...) {
@@ -306,11 +306,11 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
     cudaStream_t st = ctx->stream;
     LaunchTimer tm(ctx);
     const bool sharded = P.world > 1;
-    // Anderson (R-27, K19): unsharded, one slice, omega = 1 (the rows of every iterate must be
-    // exact for the fused error); the stored path runs the separate row/column passes
+    // Anderson (R-27, K19): omega = 1; the stored path runs the separate row/column passes; rows
+    // may be sharded (the Gram dots and the error are summed over the slices / ranks)
     const int amem = ctx->anderson >= 2 ? ctx->anderson : 0;
-    if (amem && (sharded || P.partitioned || slices.size() != 1 || P.omega != 1.f))
-        return fail(ctx, SK_EUNSUPPORTED, "Anderson acceleration runs on the unsharded solvers only");
+    if (amem && P.omega != 1.f)
+        return fail(ctx, SK_EUNSUPPORTED, "Anderson acceleration needs omega = 1");
     if (P.omega != 1.f && (sharded || P.partitioned))
         return fail(ctx, SK_EUNSUPPORTED, "relaxation (omega != 1) is supported by the unsharded solver only");
     if (ctx->decay_init > 0.f && (sharded || P.partitioned))
@@ -452,19 +452,23 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
     static const float tc_margin = [] { const char *e = getenv("SK_TC_SEED_MARGIN"); return e ? (float)atof(e) : 4.f; }();
     CU(launch_status_init(status, P.max_iter, P.check_every, P.tol, st, amem ? 1 : 0));
     ctx->cnt.kernel_launches += ns + 2;
-    float *andF = nullptr, *andR = nullptr;
-    double *andblk = nullptr;
+    float *andfr = nullptr;     // per slice i: F at 2 mem off[i], R at F + mem n_i
+    double *andblk = nullptr, *andvec = nullptr;
     void *andst = nullptr;
     if (amem) {
-        ENSURE(afr, float, B_ANDFR, 2 * (size_t)amem * slices[0].n);
+        ENSURE(afr, float, B_ANDFR, 2 * (size_t)amem * off[ns]);
         ENSURE(ablk, double, B_ANDBLK, anderson_blk_doubles());
+        ENSURE(avec, double, B_ANDVEC, anderson_vec_doubles() * ns);
         ENSURE(ast, char, B_ANDST, anderson_state_bytes());
-        andF = afr;
-        andR = afr + (size_t)amem * slices[0].n;
+        andfr = afr;
         andblk = ablk;
+        andvec = avec;
         andst = ast;
         CU(cudaMemsetAsync(andst, 0, anderson_state_bytes(), st));
+        CU(cudaMemsetAsync(andvec, 0, sizeof(double) * anderson_vec_doubles() * ns, st));
     }
+    auto andF = [&](int i) { return andfr + 2 * (size_t)amem * off[i]; };
+    auto andR = [&](int i) { return andfr + 2 * (size_t)amem * off[i] + (size_t)amem * slices[i].n; };
 
     std::vector<float *> C(ns, nullptr);
     double build_ms = 0.0;
@@ -600,12 +604,23 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
                 mrow.tc_fold = tc && row_seed && sweep >= 1;   // the next row pass is seeded
                 mrow.tc_margin = tc_margin;
                 mrow.anderson = amem ? 1 : 0;
+                mrow.and_err = amem ? andvec + anderson_vec_doubles() * i + 8 : nullptr;
                 CU(launch_merge(mrow, st));
                 launched += 2;
-                if (amem) {   // f^{l+1} = sum_u alpha_u T(f_u) over the pot/pack/image of X
-                    CU(launch_anderson_step(X[0], status, andst, amem, andF, andR, andblk, P.eps, st));
-                    launched += 3;
+                if (amem) {   // this slice's residual into the ring and its Gram dots
+                    CU(launch_anderson_dots(X[i], status, andst, amem, andF(i), andR(i), andblk,
+                                            andvec + anderson_vec_doubles() * i, st));
+                    launched += 2;
                 }
+            }
+            if (amem) {   // the sums over the ranks, the decision, f^{l+1} = sum_u alpha_u T(f_u)
+                if (P.nccl && sharded) {
+                    int r = g_nccl.allreduce(andvec, andvec, 9, kNcclFloat64, kNcclSum, ctx->comm, st);
+                    if (r != 0) return fail(ctx, SK_ENCCL, "ncclAllReduce(Anderson) failed");
+                }
+                CU(launch_anderson_decide(status, andst, amem, andvec, ns, st));
+                for (int i = 0; i < ns; ++i) CU(launch_anderson_mix(X[i], status, andst, andF(i), P.eps, st));
+                launched += 1 + ns;
             }
             ++sweep;
         }

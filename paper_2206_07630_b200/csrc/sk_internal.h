@@ -166,16 +166,21 @@ struct MergePass {
     int tc_fold = 0;          // K3 side: also fold lse + margin as the next pass's row shift
     float tc_margin = 4.f;    //          log2 units above the LSE (SK_TC_SEED_MARGIN: test knob)
     float omega = 1.f;        // Alg. 1's relaxation: h <- (1 - omega) h_old + omega h_sinkhorn
-    int anderson = 0;         // Anderson (R-27): COL takes no decision; ROW sums err_l of (f^l, g~)
-                              // and decides (checked at (l + 1) % k == 0 and l + 1 = max_iter)
+    int anderson = 0;         // Anderson (R-27): COL takes no decision; ROW writes its slice's
+    double *and_err = nullptr;//   row term of err_l for (f^l, g~) to *and_err (K19 decides)
 };
 cudaError_t launch_merge(const MergePass &M, cudaStream_t st);
-// K19 Anderson step after the row merge of a sweep (sk_anderson.cu): state = anderson_state_bytes()
-// (zeroed before the solve), F/R = 2 x mem x n floats, blk = anderson_blk_doubles().
+// K19 Anderson (sk_anderson.cu): state = anderson_state_bytes() (zeroed before the solve); per
+// slice F/R = 2 x mem x n floats, blk = anderson_blk_doubles(), vec = anderson_vec_doubles()
+// (vec[0..8): Gram dots, vec[8]: the row term of err_l written by the row merge).
 size_t anderson_state_bytes();
 size_t anderson_blk_doubles();
-cudaError_t launch_anderson_step(const Side &X, const DevStatus *st, void *state, int mem, float *F, float *R,
-                                 double *blk, float eps, cudaStream_t s);
+size_t anderson_vec_doubles();
+cudaError_t launch_anderson_dots(const Side &X, const DevStatus *st, const void *state, int mem, float *F,
+                                 float *R, double *blk, double *vec, cudaStream_t s);
+cudaError_t launch_anderson_decide(DevStatus *st, void *state, int mem, const double *vec, int ns, cudaStream_t s);
+cudaError_t launch_anderson_mix(const Side &X, const DevStatus *st, const void *state, const float *F, float eps,
+                                cudaStream_t s);
 constexpr int kMergeMaxBlocks = 1184;   // blk_err holds 2 x kMergeMaxBlocks doubles
 int merge_blocks(int P);
 

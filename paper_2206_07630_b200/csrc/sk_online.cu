@@ -461,18 +461,11 @@ __global__ void __launch_bounds__(kMT) k_merge(MergePass Mp, Side S, Side Qs) {
             else if (l >= st->max_iter) { st->stop = 1; st->final_iter = l; }
         }
     } else if (Mp.mode == MERGE_ROW && Mp.anderson) {
-        // Anderson: sweep l + 1 evaluated; the result would be (f^l, g~) (g in buffer (l + 1) & 1)
+        // Anderson: this slice's row term of err_l; K19's k_and_decide sums the slices (ranks),
+        // decides and advances the sweep counter
         st->ticket_row = 0;
-        const int l1 = l + 1;
-        if (bt) { st->nonfinite = 1; st->stop = 1; st->final_iter = l; }
-        else {
-            if (l1 % st->check_every == 0 || l1 >= st->max_iter) {
-                st->err = (float)et;
-                if ((float)et < st->tol) { st->converged = 1; st->stop = 1; st->final_iter = l; }
-            }
-            if (!st->stop && l1 >= st->max_iter) { st->stop = 1; st->final_iter = l; }
-            if (!st->stop) st->iter = l1;
-        }
+        *Mp.and_err = et;
+        if (bt && !Mp.sharded) { st->nonfinite = 1; st->stop = 1; st->final_iter = l; }
     } else if (Mp.mode == MERGE_ROW) {
         st->ticket_row = 0;
         if (Mp.omega != 1.f) { st->row_err = et; st->mass_dev = et2; }

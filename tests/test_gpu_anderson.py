@@ -114,6 +114,51 @@ def test_anderson_multikernel(O, ctx, mode, n, m, d, mem):
     assert rep["iterations"] < r0["iterations"]
 
 
+@pytest.mark.parametrize("mode,d", [("online", 3), ("online", 40), ("stored", 16)])
+def test_anderson_multikernel_max_iter_and_check_every(O, ctx, mode, d):
+    """K19: an unreachable tol stops at max_iter with (f^{L-1}, g_sk(f^{L-1})) (lockstep), and
+    check_every = 3 stops on a multiple of 3 sweeps."""
+    import paper_2206_07630_b200 as sk
+    rng = np.random.default_rng(40 + d)
+    n, m = 1800, 1536
+    x = rng.random((n, d)).astype(np.float32)
+    y = rng.random((m, d)).astype(np.float32)
+    eps = float(np.float32(0.05 * gen.mean_sq_cost(x, y)))
+    f, g, rep = sk.sinkhorn_solve(ctx, _cuda(x), _cuda(y), eps, tol=1e-30, max_iter=7, mode=mode, anderson=4)
+    assert rep["iterations"] == 7 and not rep["converged"]
+    lock = O.sinkhorn_anderson(x, y, eps, mem=4, tol=0, max_iter=7)
+    assert_pair_close(f.cpu().numpy(), g.cpu().numpy(), lock.f, lock.g, eps, what=f"{mode} d={d} max_iter")
+    assert_obj_close(rep["dual_objective"], lock.E, eps)
+    _, _, rep = sk.sinkhorn_solve(ctx, _cuda(x), _cuda(y), eps, check_every=3, mode=mode, anderson=4)
+    assert rep["converged"] and rep["iterations"] % 3 == 0
+
+
+@pytest.mark.parametrize("world,mode,d", [(2, "online", 3), (4, "online", 40), (8, "stored", 16)])
+def test_anderson_sharded_emulated(O, ctx, world, mode, d):
+    """Rows sharded over `world` emulated ranks (slices): the Gram dots and the error are summed
+    over the slices in rank order (the NCCL path allreduces the same 9 numbers): lockstep with
+    the oracle, and the same stop count as the unsharded solve."""
+    import ctypes
+    import paper_2206_07630_b200 as sk
+    rng = np.random.default_rng(50 + world + d)
+    n, m = 6000, 1600
+    x = rng.random((n, d)).astype(np.float32)
+    y = rng.random((m, d)).astype(np.float32)
+    eps = float(np.float32(0.05 * gen.mean_sq_cost(x, y)))
+    ctx.check(ctx.lib.sk_set_anderson(ctx.h, 5))
+    try:
+        f, g, rep = sk.sinkhorn_solve_sharded_emulated(ctx, world, _cuda(x), _cuda(y), eps, mode=mode)
+    finally:
+        ctx.lib.sk_set_anderson(ctx.h, 0)
+    L = rep["iterations"]
+    ref = O.sinkhorn_anderson(x, y, eps, mem=5)
+    assert abs(L - ref.iterations) <= count_tol(ref.iterations), (L, ref.iterations)
+    lock = O.sinkhorn_anderson(x, y, eps, mem=5, tol=0, max_iter=L)
+    assert_pair_close(f.cpu().numpy(), g.cpu().numpy(), lock.f, lock.g, eps, what=f"sharded x{world} {mode}")
+    assert_obj_close(rep["dual_objective"], lock.E, eps)
+    assert rep["converged"]
+
+
 def test_anderson_max_iter_and_check_every(O, ctx):
     """An unreachable tol runs exactly max_iter sweeps and returns (f^{L-1}, g_sk(f^{L-1})); check_every
     > 1 stops on a multiple of it."""
@@ -137,13 +182,6 @@ def test_anderson_argument_and_path_errors(ctx):
         sk.sinkhorn_solve(ctx, x, y, p.eps, omega=1.5, anderson=5)
     with pytest.raises(sk.SinkhornError):   # combined with eps-decay
         sk.sinkhorn_solve(ctx, x, y, p.eps, eps_decay=(5.0, 0.8), anderson=5)
-    big = _cuda(np.random.default_rng(1).random((3000, 3)).astype(np.float32))
-    with pytest.raises(sk.SinkhornError):   # the sharded entries: unsupported
-        ctx.check(ctx.lib.sk_set_anderson(ctx.h, 5))
-        try:
-            sk.sinkhorn_solve_sharded_emulated(ctx, 2, big, big, 0.01, mode="online")
-        finally:
-            ctx.lib.sk_set_anderson(ctx.h, 0)
     # the context is back to plain Sinkhorn afterwards
     _, _, r = sk.sinkhorn_solve(ctx, x, y, p.eps)
     assert r["iterations"] > 100
