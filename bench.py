@@ -93,6 +93,7 @@ class Workload:
     the C ABI with pinned host buffers."""
     scaling = "weak"
     roof = "mufu"           # mufu | hbm | ffma
+    fma_exp_share = 0.25    # mufu roof: share of the exponentials evaluated on the FMA pipe (K13: 1 of 4 pairs)
 
     def cpu_sample(self):  # -> (entries, seconds, threads, description)
         raise NotImplementedError
@@ -216,6 +217,7 @@ class Single(Workload):
             self.kernel = "k_stored_fused (single-read fused stored sweep, K5)"
         elif self.name == "c4":
             self.p = gen.c4(); self.init = args.init or "subsample"; self.mode = "online"; self.roof = "mufu"
+            self.fma_exp_share = 0.125   # K2 seeded passes: 1 of 8 exponential pairs on the FMA pipe
             self.kernel = "k_lse<3,4> (online LSE pass, K2)"
             self.scaling = "strong"
         else:
@@ -408,8 +410,13 @@ def roofline(w, cnt, steps, pk, src, step_ms):
                 "flops_per_launch": flops / nl, **common}
     achieved = cnt["dom_entries"] / dom_s if dom_s > 0 else 0.0
     peak = N_SM * MUFU_EX2_PER_CLK_SM * sm_max * 1e6
+    share = float(getattr(w, "fma_exp_share", 0.0))
     return {"bound": "alu", "pipe": "MUFU.EX2 (SFU)", "achieved": achieved / 1e9,
             "peak": peak / 1e9, "unit": "Gex2/s", "frac": achieved / peak,
+            "exp_on_fma_share": share, "xu_frac": (1.0 - share) * achieved / peak,
+            "frac_note": "achieved counts every cost entry's exponential; a share of them runs on the FMA pipe "
+                         "(Cody-Waite + polynomial), so frac is exponentials per MUFU slot and xu_frac the XU "
+                         "pipe's own utilisation",
             "peak_source": f"derived: {N_SM} SM x {MUFU_EX2_PER_CLK_SM} ex2/clk x {sm_max:.0f} MHz "
                            f"(sm_max_mhz from MEASURED_PEAKS.json, {src})",
             "algorithmic": "one exp2 per cost entry per pass; 2 passes per sweep (+1 column pass for err_L)",
