@@ -216,3 +216,45 @@ def test_c5_reduced_full_convergence(O, ctx, eps_factor):
     lock = O.sinkhorn(p.x, p.y, p.eps, tol=0, max_iter=rep["iterations"])
     assert_pair_close(f.cpu().numpy(), g.cpu().numpy(), lock.f, lock.g, p.eps)
     assert_obj_close(rep["dual_objective"], lock.E, p.eps)
+
+
+# ------------------------------------------ Anderson (K19) at full size: properties
+def _col_marginals(x, y, f, g, eps, cols):
+    """fp64 column sums of the plan of (f, g) on sampled columns (property check of CUDA outputs)."""
+    x64 = np.asarray(x, np.float64)
+    f64 = np.asarray(f, np.float64)
+    out = []
+    for j in cols:
+        C = ((x64 - np.asarray(y[j], np.float64)[None, :]) ** 2).sum(-1)
+        out.append(np.exp((f64 + float(g[j]) - C) / eps).sum())
+    return np.array(out)
+
+
+@pytest.mark.parametrize("cfg", ["c4", "c5"])
+def test_anderson_full_size_properties(ctx, cfg):
+    """C4 / C5 at the bench's full size with Anderson (m = 5, K19): converged in fewer sweeps than
+    the plain solve; the returned pair (f^L, g_sk(f^L)) has exact column marginals (sampled,
+    fp64), its rows deviate by the reported error on average, and E agrees with the plain
+    solve's (both at err < tol)."""
+    import paper_2206_07630_b200 as sk
+    if cfg == "c4":
+        p = gen.c4()
+        f0, _, _ = sk.sinkhorn_init_subsample(ctx, _cuda(p.x), _cuda(p.y), _cuda(p.extra["idx_x"]),
+                                              _cuda(p.extra["idx_y"]), p.eps, p.tol / 10)
+    else:
+        p = gen.c5()
+        f0, _ = sk.sinkhorn_init_gaussian(ctx, _cuda(p.x), _cuda(p.y))
+    xd, yd = _cuda(p.x), _cuda(p.y)
+    f, g, rep = sk.sinkhorn_solve(ctx, xd, yd, p.eps, tol=p.tol, mode="online", f_init=f0, anderson=5)
+    _, _, r0 = sk.sinkhorn_solve(ctx, xd, yd, p.eps, tol=p.tol, mode="online", f_init=f0)
+    assert rep["converged"] and rep["marginal_error"] < p.tol
+    assert rep["iterations"] < r0["iterations"], (rep["iterations"], r0["iterations"])
+    f, g = f.cpu().numpy(), g.cpu().numpy()
+    rng = np.random.default_rng(5)
+    cols = np.sort(rng.choice(p.m, 24, replace=False))
+    cm = _col_marginals(p.x, p.y, f, g, p.eps, cols)
+    assert np.abs(cm * p.m - 1.0).max() < 1e-3
+    rows = np.sort(rng.choice(p.n, 256, replace=False))
+    rm = _row_marginals(p.x, p.y, f, g, p.eps, rows)
+    assert np.abs(rm * p.n - 1.0).mean() < 10 * p.tol
+    assert_obj_close(rep["dual_objective"], r0["dual_objective"], p.eps, rtol=1e-4)
