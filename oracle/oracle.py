@@ -494,7 +494,7 @@ def _gmm_mstep(x, r, reg_covar):
     return weights, means, covs
 
 
-def gmm_fit(x, K, init_idx, iters, reg_covar=1e-6, kmeans_iters=0):
+def gmm_fit(x, K, init_idx, iters, reg_covar=1e-6, kmeans_iters=0, tol=0.0, return_iters=False):
     """EM for a K-component full-covariance GMM (NEXT-3; "we fit first two K-component
     GMMs", done with sklearn on the CPU in the paper).  Start (R-23): kmeans_iters = 0:
     weights 1/K, means x[init_idx], covariances the biased covariance of x + reg I;
@@ -502,7 +502,10 @@ def gmm_fit(x, K, init_idx, iters, reg_covar=1e-6, kmeans_iters=0):
     responsibilities of kmeans(x, init_idx, kmeans_iters).  Each iteration, literally:
         E-step  r_ik = alpha_k N(x_i; m_k, S_k) / sum_l alpha_l N(x_i; m_l, S_l)   (gmm_log_resp)
         M-step  (_gmm_mstep).
-    Returns (weights, means, covs, mean log-likelihood of the returned parameters)."""
+    tol > 0 (sklearn's convergence rule, R-28): iteration k's E-step gives the mean
+    log-likelihood ll_k of the current parameters; after its M-step, stop if |ll_k - ll_{k-1}| <
+    tol (ll_0 = -inf).  Returns (weights, means, covs, mean log-likelihood of the returned
+    parameters[, EM iterations run])."""
     x = _pts(x)
     n, d = x.shape
     if kmeans_iters > 0:
@@ -514,10 +517,17 @@ def gmm_fit(x, K, init_idx, iters, reg_covar=1e-6, kmeans_iters=0):
         cov0 = (x - m0).T @ (x - m0) / n + reg_covar * np.eye(d)
         covs = np.repeat(cov0[None], K, axis=0)
         weights = np.full(K, 1.0 / K)
+    ll_prev, done = -np.inf, 0
     for _ in range(iters):
+        ll = gmm_loglik(x, weights, means, covs)
         r = np.exp(gmm_log_resp(x, weights, means, covs))
         weights, means, covs = _gmm_mstep(x, r, reg_covar)
-    return weights, means, covs, gmm_loglik(x, weights, means, covs)
+        done += 1
+        if tol > 0 and abs(ll - ll_prev) < tol:
+            break
+        ll_prev = ll
+    out = (weights, means, covs, gmm_loglik(x, weights, means, covs))
+    return out + (done,) if return_iters else out
 
 
 def gmm_loglik(x, weights, means, covs):

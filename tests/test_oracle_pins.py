@@ -580,6 +580,32 @@ def test_gmm_fit_kmeans_start_matches_sklearn_em():
     assert abs(ll - gm.score(x)) < 1e-9
 
 
+def test_gmm_fit_tol_stops_like_sklearn():
+    """R-28: with tol > 0 the EM loop stops as sklearn's GaussianMixture(tol) does: the same
+    iteration count and parameters from the same start."""
+    from oracle import oracle as O
+    from sklearn.mixture import GaussianMixture
+    rng = np.random.default_rng(25)
+    x = np.concatenate([rng.standard_normal((400, 3)) * 0.8 + c for c in ([0, 0, 0], [2.5, 1, 0], [-2, 2, 1])])
+    K, reg = 3, 1e-6
+    idx = rng.choice(len(x), K, replace=False)
+    _, lab = O.kmeans(x, idx, 6)
+    w0 = np.array([(lab == k).sum() for k in range(K)]) / len(x)
+    m0 = np.stack([x[lab == k].mean(0) for k in range(K)])
+    S0 = np.stack([np.cov(x[lab == k].T, bias=True) + reg * np.eye(3) for k in range(K)])
+    import warnings
+    for tol in (1e-2, 1e-3, 1e-5):
+        w, m, S, ll, it = O.gmm_fit(x, K, idx, 100, reg, kmeans_iters=6, tol=tol, return_iters=True)
+        gm = GaussianMixture(K, covariance_type="full", reg_covar=reg, max_iter=100, tol=tol,
+                             weights_init=w0, means_init=m0, precisions_init=np.linalg.inv(S0))
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            gm.fit(x)
+        assert it == gm.n_iter_, (tol, it, gm.n_iter_)
+        assert np.abs(m - gm.means_).max() < 1e-9 and np.abs(S - gm.covariances_).max() < 1e-9
+        assert np.abs(w - gm.weights_).max() < 1e-10
+
+
 # --------------------------------------------------- implicit differentiation (NEXT-4)
 def _solve_tight(O, x, y, eps, a=None, b=None, f0=None):
     r = O.sinkhorn(x, y, eps, a=a, b=b, tol=1e-13, max_iter=200000, f0=f0)
