@@ -260,7 +260,8 @@ class Single(Workload):
              "l2": "flushed (256 MiB write) before every timed step" if self.name in ("c1",) else
                    "inputs + cost larger than L2 / flushed before each step"}
         if self.init == "gmm":
-            c["gmm_fit"] = {"K": 8, "kmeans_iters": self.args.gmm_kmeans_iters, "em_iters": self.args.gmm_iters,
+            c["gmm_fit"] = {"K": 8, "kmeans_iters": self.args.gmm_kmeans_iters, "em_max_iters": self.args.gmm_iters,
+                            "em_tol": self.args.gmm_tol,
                             "start": "gen.gmm_start_idx seeds 3/4 (R-23/R-28)"}
         return c
 
@@ -270,9 +271,9 @@ class Single(Workload):
             f0, _ = sk.sinkhorn_init_gaussian(self.ctx, x, y)
         elif self.init == "gmm":
             gx, _ = sk.sinkhorn_fit_gmm(self.ctx, x, 8, self.gmm_idx[0], iters=self.args.gmm_iters,
-                                        kmeans_iters=self.args.gmm_kmeans_iters)
+                                        kmeans_iters=self.args.gmm_kmeans_iters, tol=self.args.gmm_tol)
             gy, _ = sk.sinkhorn_fit_gmm(self.ctx, y, 8, self.gmm_idx[1], iters=self.args.gmm_iters,
-                                        kmeans_iters=self.args.gmm_kmeans_iters)
+                                        kmeans_iters=self.args.gmm_kmeans_iters, tol=self.args.gmm_tol)
             f0, _ = sk.sinkhorn_init_gmm(self.ctx, x, y, gx, gy, p.eps)
         elif self.init == "gmm_given":
             gx, gy = self.gx, self.gy
@@ -602,7 +603,10 @@ def main():
     ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--init", default=None,
                     help="c3/c4/c5 initializer: zero|gaussian|gmm (fitted on the device)|gmm_given|subsample")
-    ap.add_argument("--gmm-iters", type=int, default=50, help="EM iterations of the device GMM fit (init gmm)")
+    ap.add_argument("--gmm-iters", type=int, default=100, help="max EM iterations of the device GMM fit (init gmm; "
+                    "sklearn's default max_iter)")
+    ap.add_argument("--gmm-tol", type=float, default=1e-3, help="EM convergence tol (sklearn's default; 0 = run "
+                    "all --gmm-iters)")
     ap.add_argument("--no-anderson", action="store_true", help="skip the Anderson time-to-tol extra")
     ap.add_argument("--gmm-kmeans-iters", type=int, default=10,
                     help="Lloyd steps of the fit's k-means start (R-28; sklearn's default start), 0 = start at x[idx]")

@@ -192,15 +192,19 @@ sk_status sinkhorn_vjp(sk_ctx *ctx, int64_t n, int64_t m, int32_t d, const float
  * reg_covar I; kmeans_iters > 0 (sklearn's init_params="kmeans"): kmeans_iters Lloyd steps
  * from centers x[init_idx[k]] (nearest center in fp64, ties to the lowest k, an empty cluster
  * keeps its center), a final assignment, and the M-step of those one-hot responsibilities.  Each
- * M-step adds reg_covar I (as sklearn's reg_covar).  fp64 state and sufficient statistics,
+ * M-step adds reg_covar I (as sklearn's reg_covar).  tol > 0 stops EM as sklearn's
+ * GaussianMixture(tol) does: after the M-step of an iteration whose E-step log-likelihood moved by
+ * less than tol (tol = 0: exactly `iters` steps).  fp64 state and sufficient statistics,
  * deterministic.  Outputs (caller-owned, device or host): weights K, means K x d, covs
  * K x d x d (fp32, the layout sinkhorn_init_gmm takes); loglik (host, nullable) = mean
- * log-likelihood of the returned parameters.  SK_EINVAL: bad sizes, K > n, iters < 0, kmeans_iters < 0,
+ * log-likelihood of the returned parameters; n_iter (host, nullable) = EM steps run.
+ * SK_EINVAL: bad sizes, K > n, iters < 0, kmeans_iters < 0, tol < 0,
  * reg_covar < 0, non-finite x, init_idx not K distinct indices in [0, n); SK_EUNSUPPORTED:
  * d > 32 or K > 64; SK_ENONFINITE: a covariance lost positive definiteness.  Blocks. */
 sk_status sinkhorn_fit_gmm(sk_ctx *ctx, int64_t n, int32_t d, const float *x, int32_t K,
-                           const int32_t *init_idx, int32_t kmeans_iters, int32_t iters, float reg_covar,
-                           float *weights, float *means, float *covs, double *loglik);
+                           const int32_t *init_idx, int32_t kmeans_iters, int32_t iters, float tol,
+                           float reg_covar, float *weights, float *means, float *covs, double *loglik,
+                           int32_t *n_iter);
 
 /* Soft ranks and soft sort (Sec. 3.1) of B 1D problems with
  * cost (x - y)^2, from potentials (f, g) (normally the output of sinkhorn_solve): with the
@@ -266,10 +270,11 @@ sk_status sinkhorn_init_gaussian(sk_ctx *ctx, int64_t n, int64_t m, int32_t d, c
  * weights wx[Kx], means mux[Kx][d], covariances covx[Kx][d][d]) fitted to mu and
  * tau (Ky, wy, muy, covy) fitted to nu: C~_kl = ||m_k - m'_l||^2 + B^2(S_k, S'_l)
  * (Eq. 6) with fp64 Newton-Schulz square roots; the Kx x Ky entropic
- * problem at the same eps (R-13) is solved in fp64 to inner_tol (max
- * inner_max_iter sweeps) -> f~; f^(0)(x) = sum_k f~_k p_k(x), p_k the posterior
- * responsibilities (Eq. 7), on the smaller side (*side as above).
- * Mixture parameters are inputs (fitting is a later row).  d <= 64, K <= 64. */
+ * problem at the same eps (R-13) is solved in fp64 with Anderson acceleration (memory 5,
+ * DESIGN.md R-30; err = the row term of (f^l, g_sk(f^l))) to inner_tol (max inner_max_iter
+ * sweeps; the binding's default 1e-9: ~100 sweeps at C3) -> f~; f^(0)(x) = sum_k f~_k p_k(x),
+ * p_k the posterior responsibilities (Eq. 7), on the smaller side (*side as above).
+ * Mixture parameters are inputs (sinkhorn_fit_gmm fits them).  d <= 64, K <= 64. */
 sk_status sinkhorn_init_gmm(sk_ctx *ctx, int64_t n, int64_t m, int32_t d, const float *x,
                             const float *y, int32_t Kx, const float *wx, const float *mux,
                             const float *covx, int32_t Ky, const float *wy, const float *muy,

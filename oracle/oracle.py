@@ -58,6 +58,8 @@ def _L():
         lib.ora_sinkhorn_points_omega.argtypes = [I64, I64, I, P, P, P, P, D, D, D, I, I, P, P, P, P, P, P, P]
         lib.ora_sinkhorn_points_decay.restype = I
         lib.ora_sinkhorn_points_decay.argtypes = [I64, I64, I, P, P, P, P, D, D, D, D, D, I, I, P, P, P, P, P, P, P]
+        lib.ora_sinkhorn_matrix_anderson.restype = I
+        lib.ora_sinkhorn_matrix_anderson.argtypes = [I64, I64, P, P, P, D, I, D, I, I, P, P, P, P, P, P]
         lib.ora_sinkhorn_points_anderson.restype = I
         lib.ora_sinkhorn_points_anderson.argtypes = [I64, I64, I, P, P, P, P, D, I, D, I, I, P, P, P, P, P, P]
         lib.ora_sinkhorn_matrix.restype = I
@@ -166,13 +168,18 @@ def sinkhorn_anderson(x, y, eps, mem=5, a=None, b=None, tol=1e-3, max_iter=10000
 
 
 def sinkhorn_matrix(C, eps, a=None, b=None, tol=1e-3, max_iter=10000, check_every=1,
-                    f0=None, trace=False) -> Result:
+                    f0=None, trace=False, anderson=0) -> Result:
     C = _d(C)
     n, m = C.shape
     a, b = _weights(a, n), _weights(b, m)
     f, g = np.empty(n), np.empty(m)
     it, err, E = ctypes.c_int(), ctypes.c_double(), ctypes.c_double()
     f0a = None if f0 is None else _d(f0)
+    if anderson:   # Anderson on the sweep map (R-27), as sinkhorn_anderson for a given cost matrix
+        conv = _L().ora_sinkhorn_matrix_anderson(n, m, _p(C), _p(a), _p(b), float(eps), int(anderson), float(tol),
+                                                 int(max_iter), int(check_every), _p(f0a), _p(f), _p(g),
+                                                 ctypes.byref(it), ctypes.byref(err), ctypes.byref(E))
+        return Result(f=f, g=g, iterations=it.value, converged=bool(conv), err=err.value, E=E.value)
     tr = np.empty(max_iter) if trace else None
     conv = _L().ora_sinkhorn_matrix(n, m, _p(C), _p(a), _p(b), float(eps), float(tol),
                                     int(max_iter), int(check_every), _p(f0a), _p(f), _p(g),
@@ -387,18 +394,22 @@ def gmm_cost(mx, cx, my, cy):
     return C
 
 
-def init_gmm(x, y, gx: dict, gy: dict, eps, inner_tol=1e-4, inner_max_iter=100000):
+def init_gmm(x, y, gx: dict, gy: dict, eps, inner_tol=1e-9, inner_max_iter=100000):
     """GMM initializer (Sec. 3.3): K x K Bures-cost Sinkhorn at the same eps
-    (reading R-13) -> f~; f0_i = sum_k f~_k p_k(x_i) on the smaller side."""
+    (reading R-13), solved with Anderson acceleration (memory 5, reading R-30) -> f~;
+    f0_i = sum_k f~_k p_k(x_i) on the smaller side."""
     x, y = _pts(x), _pts(y)
     if x.shape[0] > y.shape[0]:
         f, _ = init_gmm(y, x, gy, gx, eps, inner_tol, inner_max_iter)
         return f, 1
     C = gmm_cost(gx["means"], gx["covs"], gy["means"], gy["covs"])
-    r = sinkhorn_matrix(C, eps, a=_d(gx["weights"]), b=_d(gy["weights"]), tol=inner_tol,
-                        max_iter=inner_max_iter)
+    a = _d(gx["weights"])
+    r = sinkhorn_matrix(C, eps, a=a, b=_d(gy["weights"]), tol=inner_tol, max_iter=inner_max_iter, anderson=5)
+    # (f~ is defined up to a constant and Anderson's mixing moves it along that line: the
+    # returned f~ is the representative with sum_k a_k f~_k = 0, R-30)
+    ft = r.f - (a * r.f).sum() / a.sum()
     P = np.exp(gmm_log_resp(x, gx["weights"], gx["means"], gx["covs"]))
-    return P @ r.f, 0
+    return P @ ft, 0
 
 
 # ------------------------------------------------------------- Subsample ---

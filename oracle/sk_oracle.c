@@ -358,6 +358,14 @@ int ora_sinkhorn_matrix(int64_t n, int64_t m, const double *C, const double *a, 
     return sinkhorn(&p, a, b, eps, tol, max_iter, check_every, f0, f, g, iters, err, E, trace);
 }
 
+int ora_sinkhorn_matrix_anderson(int64_t n, int64_t m, const double *C, const double *a, const double *b,
+                                 double eps, int mem, double tol, int max_iter, int check_every, const double *f0,
+                                 double *f, double *g, int *iters, double *err, double *E) {
+    ora_prob p = {n, m, 0, NULL, NULL, C};
+    if (mem < 1 || mem > 16) return -1;
+    return sinkhorn_anderson(&p, a, b, eps, tol, max_iter, check_every, f0, mem, f, g, iters, err, E);
+}
+
 void ora_f_update_points(int64_t n, int64_t m, int d, const double *x, const double *y,
                          const double *a, const double *g, double eps, double *f,
                          const int64_t *rows, int64_t cnt) {

@@ -166,7 +166,7 @@ def sinkhorn_init_gaussian(ctx: Context, x, y, a=None, b=None, ridge_rel: float 
     return pot, side.value
 
 
-def sinkhorn_init_gmm(ctx: Context, x, y, gx: dict, gy: dict, eps: float, inner_tol: float = 1e-4,
+def sinkhorn_init_gmm(ctx: Context, x, y, gx: dict, gy: dict, eps: float, inner_tol: float = 1e-9,
                       inner_max_iter: int = 100000):
     """gx/gy: {'weights': (K,), 'means': (K, d), 'covs': (K, d, d)} fp32 tensors."""
     n, d = x.shape
@@ -259,10 +259,12 @@ def sinkhorn_init_nw1d(ctx: Context, x, y, a=None, b=None, y_shared: bool = True
 
 
 def sinkhorn_fit_gmm(ctx: Context, x, K: int, init_idx, iters: int = 100, reg_covar: float = 1e-6,
-                     kmeans_iters: int = 0):
+                     kmeans_iters: int = 0, tol: float = 0.0, return_iters: bool = False):
     """EM fit of a K-component full-covariance GMM of x (n, d) (NEXT-3), started from means
-    x[init_idx] (kmeans_iters = 0) or from kmeans_iters Lloyd steps from those centers (R-28).
-    Returns ({'weights', 'means', 'covs'} as sinkhorn_init_gmm takes them, mean log-likelihood)."""
+    x[init_idx] (kmeans_iters = 0) or from kmeans_iters Lloyd steps from those centers (R-28);
+    tol > 0 stops EM as sklearn's GaussianMixture(tol) does.
+    Returns ({'weights', 'means', 'covs'} as sinkhorn_init_gmm takes them, mean log-likelihood
+    [, EM steps run])."""
     n, d = x.shape
     idx = init_idx if isinstance(init_idx, torch.Tensor) else torch.as_tensor(init_idx, dtype=torch.int32)
     idx = idx.to(torch.int32).contiguous()
@@ -270,9 +272,12 @@ def sinkhorn_fit_gmm(ctx: Context, x, K: int, init_idx, iters: int = 100, reg_co
     mu = _empty((K, d), x)
     cov = _empty((K, d, d), x)
     ll = ctypes.c_double()
-    ctx.check(ctx.lib.sinkhorn_fit_gmm(ctx.h, n, d, _ptr(x), int(K), _ptr(idx, torch.int32), int(kmeans_iters), int(iters), float(reg_covar),
-                                       _ptr(w), _ptr(mu), _ptr(cov), ctypes.byref(ll)))
-    return {"weights": w, "means": mu, "covs": cov}, ll.value
+    it = ctypes.c_int32()
+    ctx.check(ctx.lib.sinkhorn_fit_gmm(ctx.h, n, d, _ptr(x), int(K), _ptr(idx, torch.int32), int(kmeans_iters),
+                                       int(iters), float(tol), float(reg_covar), _ptr(w), _ptr(mu), _ptr(cov),
+                                       ctypes.byref(ll), ctypes.byref(it)))
+    g = {"weights": w, "means": mu, "covs": cov}
+    return (g, ll.value, it.value) if return_iters else (g, ll.value)
 
 
 def sinkhorn_vjp(ctx: Context, x, y, eps: float, f, g, zf, zg, cg_tol: float = 1e-6, cg_max_iter: int = 2000):

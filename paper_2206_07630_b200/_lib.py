@@ -78,7 +78,8 @@ def load() -> ctypes.CDLL:
         "sinkhorn_sort1d_batched": (S, [P, I64, I64, P, P, P]),
         "sinkhorn_init_zero": (S, [P, I64, I64, P]),
         "sinkhorn_soft_rank_sort": (S, [P, I64, I64, I64, P, P, I32, F, P, P, P, P, P]),
-        "sinkhorn_fit_gmm": (S, [P, I64, I32, P, I32, P, I32, I32, F, P, P, P, ctypes.POINTER(D)]),
+        "sinkhorn_fit_gmm": (S, [P, I64, I32, P, I32, P, I32, I32, F, F, P, P, P, ctypes.POINTER(D),
+                                 ctypes.POINTER(I32)]),
         "sinkhorn_init_nw1d": (S, [P, I64, I64, I64, P, P, I32, P, P, I32, P, P]),
         "sinkhorn_vjp": (S, [P, I64, I64, I32, P, P, F, P, P, P, P, F, I32, P, P, P, P, ctypes.POINTER(I32),
                              ctypes.POINTER(D)]),

@@ -858,13 +858,14 @@ sk_status sinkhorn_sort1d_batched(sk_ctx *ctx, int64_t B, int64_t n, const float
 }
 
 sk_status sinkhorn_fit_gmm(sk_ctx *ctx, int64_t n, int32_t d, const float *x, int32_t K, const int32_t *init_idx,
-                           int32_t kmeans_iters, int32_t iters, float reg_covar, float *weights, float *means,
-                           float *covs, double *loglik) {
+                           int32_t kmeans_iters, int32_t iters, float tol, float reg_covar, float *weights,
+                           float *means, float *covs, double *loglik, int32_t *n_iter) {
     if (!ctx) return SK_EINVAL;
     if (n < 1 || K < 1 || K > n || !x || !init_idx || !weights || !means || !covs || iters < 0 || kmeans_iters < 0)
         return fail(ctx, SK_EINVAL, "bad arguments (need 1 <= K <= n, iters >= 0, kmeans_iters >= 0, non-NULL arrays)");
     if (d < 1 || d > 32 || K > 64) return fail(ctx, SK_EUNSUPPORTED, "GMM fitting supports d <= 32, K <= 64");
     if (!(reg_covar >= 0.f) || bad_scalar(reg_covar)) return fail(ctx, SK_EINVAL, "reg_covar must be >= 0");
+    if (!(tol >= 0.f) || bad_scalar(tol)) return fail(ctx, SK_EINVAL, "tol must be finite and >= 0");
     // the start indices: in range and distinct (checked on the host: K values)
     std::vector<int32_t> hidx(K);
     if (is_device_ptr(init_idx)) CU(cudaMemcpy(hidx.data(), init_idx, sizeof(int32_t) * K, cudaMemcpyDeviceToHost));
@@ -890,18 +891,21 @@ sk_status sinkhorn_fit_gmm(sk_ctx *ctx, int64_t n, int32_t d, const float *x, in
     ENSURE(part, double, B_EMPART, std::max(em_work_doubles(K, d), (size_t)296 * d * d));
     ENSURE(flag, int, B_FLAG, 4);
     double *mean0 = st + 2 * em_state_doubles(K, d), *cov0 = mean0 + d, *ll = cov0 + (size_t)d * d;
-    CU(cudaMemsetAsync(flag, 0, sizeof(int), ctx->stream));
+    CU(cudaMemsetAsync(flag, 0, 3 * sizeof(int), ctx->stream));
     CU(launch_moments(dx, nullptr, n, d, mean0, cov0, part, (long long)std::max(em_work_doubles(K, d), (size_t)296 * d * d),
                       ctx->stream));
-    CU(launch_gmm_fit(dx, n, d, K, didx, cov0, kmeans_iters, iters, (double)reg_covar, st, part, flag, dw, dm, dc, ll,
-                      ctx->stream));
+    CU(launch_gmm_fit(dx, n, d, K, didx, cov0, kmeans_iters, iters, (double)tol, (double)reg_covar, st, part, flag, dw,
+                      dm, dc, ll, ctx->h_flag, ctx->stream));
     ctx->cnt.kernel_launches += 4 + 3 * (kmeans_iters > 0 ? kmeans_iters + 1 : 0) + 4 * (iters + 1) + 3;
     CK(sg.flush());
     double hll = 0.0;
-    CU(cudaMemcpyAsync(ctx->h_flag, flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    int hf[3] = {0, 0, 0};
+    CU(cudaMemcpyAsync(hf, flag, sizeof hf, cudaMemcpyDeviceToHost, ctx->stream));
     CU(cudaMemcpyAsync(&hll, ll, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));
+    *ctx->h_flag = hf[0];
     if (loglik) *loglik = hll;
+    if (n_iter) *n_iter = hf[2];
     if (*ctx->h_flag) return fail(ctx, SK_ENONFINITE, "a component covariance lost positive definiteness");
     return SK_OK;
 }

@@ -300,24 +300,19 @@ __global__ void __launch_bounds__(kGT) k_gmm_bures(const float *mux, const float
 }
 
 // K x K entropic OT (Alg. 1, g-then-f; R-13), one warp, in log2 units: F = f kappa,
-// G = g kappa, Kc = -C kappa (kappa = log2(e)/eps, fp64).  Each sweep is a g-update then an
-// f-update; err_l is evaluated with the fused identity of the main solver (H5): after
-// an f-update the row marginals are exact, so err_l = sum_j b_j |expm1((g_j^l - g_j^{l+1})/eps)|,
-// known at the next g-update; the returned f~ is f^l of the first l with err_l < tol (or
-// max_iter).  Layout: lane t owns outputs t and t + 32; a reduction over the K'' inputs runs in
-// registers (8 independent partial maxima / sums).  The state F, G (values ~ cost/eps, hundreds
-// at C3) stays fp64: the iteration converges slowly (thousands of sweeps) and fp32 rounding of
-// the state would accumulate along its slow mode.  The exponentials 2^(v - max) <= 1, their sum
-// and its log2 use fp32 MUFU (relative error ~1e-7 per term, not accumulated in the state).
-// out_k = lw_k - LSE2_r (in_r + Kc[r][k]) (transposed access when cols = 0); returns the fused
-// error sum_k w_k |expm1(ln2 (prev_k - out_k))| when err != 0.
-__device__ __forceinline__ float gmm_update(const double *__restrict__ Kc, int Kx, int Ky, bool cols,
-                                            const double *in, double *out, const double *lw, const float *w,
-                                            bool err) {
+// G = g kappa, Kc = -C kappa (kappa = log2(e)/eps, fp64).
+// The K x K solve with Anderson acceleration (memory 5, reading R-30: the inner problem of the
+// GMM initializer converges in thousands of plain sweeps at C3's eps; the paper only asks for
+// its solution).  fp64 throughout (the mixing is sensitive to rounding near the solution).  Sweep
+// l: G = g_sk(F), T = f_sk(G); err_l = sum_k a_k |expm1(ln2 (F_k - T_k))| (the row term of
+// (f^l, g~), whose columns are exact); stop if err_l < tol (-> f~ = f^l) or at max_iter; else
+// the ring slot gets (T, T - F) and F = sum_u alpha_u T_u with alpha from the regularised Gram
+// system (lam = 1e-8 tr G / count) as in K13/K19.  Lane t owns outputs t and t + 32.
+__device__ __forceinline__ void gmm_update_d(const double *__restrict__ Kc, int Kx, int Ky, bool cols,
+                                             const double *in, double *out, const double *lw) {
     const int t = threadIdx.x;
     const int Kout = cols ? Ky : Kx, Kin = cols ? Kx : Ky;
-    const int rs = cols ? Ky : 1, ks = cols ? 1 : Ky;   // Kc index = r * rs + k * ks
-    float e = 0.f;
+    const int rs = cols ? Ky : 1, ks = cols ? 1 : Ky;
     double on[2];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -325,38 +320,26 @@ __device__ __forceinline__ float gmm_update(const double *__restrict__ Kc, int K
         on[h] = 0.0;
         if (k >= Kout) continue;
         const double *kc = Kc + k * ks;
-        double v[8], mx = -INFINITY;
-        float s = 0.f;
-        for (int r0 = 0; r0 < Kin; r0 += 8) {   // one chunk when Kin <= 8 (C3: K = 8)
-            double cm = -INFINITY;
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                v[u] = r0 + u < Kin ? in[r0 + u] + kc[(r0 + u) * rs] : -INFINITY;
-                cm = fmax(cm, v[u]);
-            }
-            if (cm > mx) { s *= ex2((float)(mx - cm)); mx = cm; }
-            float p[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) p[u] = ex2((float)(v[u] - mx));
-            s += ((p[0] + p[1]) + (p[2] + p[3])) + ((p[4] + p[5]) + (p[6] + p[7]));
-        }
-        on[h] = lw[k] - (mx + (double)__log2f(s));
-        if (err) e += w[k] * fabsf(expm1f((float)(out[k] - on[h]) * kLn2));
+        double mx = -INFINITY;
+        for (int r = 0; r < Kin; ++r) mx = fmax(mx, in[r] + kc[r * rs]);
+        double sm = 0.0;
+        for (int r = 0; r < Kin; ++r) sm += exp2(in[r] + kc[r * rs] - mx);
+        on[h] = lw[k] - (mx + log2(sm));
     }
     __syncwarp();
 #pragma unroll
     for (int h = 0; h < 2; ++h)
         if (t + 32 * h < Kout) out[t + 32 * h] = on[h];
     __syncwarp();
-    if (err)
-        for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
-    return e;
 }
 
-__global__ void __launch_bounds__(32) k_gmm_sinkhorn(const double *C, int Kx, int Ky, const float *wx,
-                                                      const float *wy, float eps_f, float tol, int max_iter,
-                                                      double *ft, int *flags) {
-    __shared__ double Kc[64 * 64], F[64], G[64], la[64], lb[64];
+constexpr int kGmmAnd = 5;
+
+__global__ void __launch_bounds__(32) k_gmm_sinkhorn_and(const double *C, int Kx, int Ky, const float *wx,
+                                                          const float *wy, float eps_f, float tol, int max_iter,
+                                                          double *ft, int *flags) {
+    __shared__ double Kc[64 * 64], F[64], G[64], T[64], la[64], lb[64];
+    __shared__ double Fh[kGmmAnd][64], Rh[kGmmAnd][64], Gm[kGmmAnd * kGmmAnd];
     const double eps = eps_f, kap = kLog2ed / eps;
     const int t = threadIdx.x;
     for (int e = t; e < Kx * Ky; e += 32) Kc[e] = -C[e] * kap;
@@ -367,20 +350,104 @@ __global__ void __launch_bounds__(32) k_gmm_sinkhorn(const double *C, int Kx, in
         lb[i] = i < Ky ? log2((double)wy[i]) : 0.0;
     }
     __syncwarp();
-    int l = 0;
-    for (;;) {
-        // g-update g^{l+1} from f^l, with err_l from (g^l, g^{l+1})
-        const float e = gmm_update(Kc, Kx, Ky, true, F, G, lb, wy, true);
-        if (l >= 1 && (e < tol || !isfinite(e))) {
-            if (!isfinite(e) && t == 0) atomicOr(flags, 2);
-            break;
+    int head = 0, cnt = 0;
+    for (int l = 0;; ++l) {
+        gmm_update_d(Kc, Kx, Ky, true, F, G, lb);
+        gmm_update_d(Kc, Kx, Ky, false, G, T, la);
+        double e = 0.0;
+        for (int k = t; k < Kx; k += 32) e += (double)wx[k] * fabs(expm1(kLn2d * (F[k] - T[k])));
+        for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
+        if (!isfinite(e)) { if (t == 0) atomicOr(flags, 2); break; }
+        if ((float)e < tol || l + 1 >= max_iter) break;
+        const int cn = cnt < kGmmAnd ? cnt + 1 : kGmmAnd;
+        double dv[kGmmAnd];
+#pragma unroll
+        for (int u = 0; u < kGmmAnd; ++u) dv[u] = 0.0;
+        for (int k = t; k < Kx; k += 32) {
+            const double r = T[k] - F[k];
+#pragma unroll
+            for (int u = 0; u < kGmmAnd; ++u)
+                if (u < cn) dv[u] += r * (u == head ? r : Rh[u][k]);
+            Fh[head][k] = T[k];
+            Rh[head][k] = r;
         }
-        if (l >= max_iter) break;
-        // f-update f^{l+1} from g^{l+1}
-        gmm_update(Kc, Kx, Ky, false, G, F, la, wx, false);
-        ++l;
+        double dl = 0.0;   // lane u: <r_new, r_u>
+#pragma unroll
+        for (int u = 0; u < kGmmAnd; ++u) {
+            double v = dv[u];
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (t == u) dl = v;
+        }
+        __syncwarp();
+        double row[kGmmAnd];
+#pragma unroll
+        for (int u = 0; u < kGmmAnd; ++u) {
+            const double du = __shfl_sync(0xffffffffu, dl, u);
+            double gv;
+            if (t == head) gv = du;
+            else if (u == head) gv = dl;
+            else gv = t < kGmmAnd ? Gm[t * kGmmAnd + u] : 0.0;
+            row[u] = (t < cn && u < cn) ? gv : (u == t ? 1.0 : 0.0);
+        }
+        __syncwarp();
+        if (t < cn) { Gm[head * kGmmAnd + t] = dl; Gm[t * kGmmAnd + head] = dl; }
+        double diag = 0.0;
+#pragma unroll
+        for (int u = 0; u < kGmmAnd; ++u)
+            if (u == t) diag = row[u];
+        double tr = t < cn ? diag : 0.0;
+        for (int o = 16; o > 0; o >>= 1) tr += __shfl_xor_sync(0xffffffffu, tr, o);
+        const double lam = tr > 0.0 ? 1e-8 * tr / cn : 1.0;
+#pragma unroll
+        for (int u = 0; u < kGmmAnd; ++u)
+            if (u == t && t < cn) row[u] += lam;
+        double rhs = t < cn ? 1.0 : 0.0;
+        for (int c = 0; c < cn; ++c) {
+            double piv[kGmmAnd], myc = 0.0;
+#pragma unroll
+            for (int u = 0; u < kGmmAnd; ++u) {
+                piv[u] = __shfl_sync(0xffffffffu, row[u], c);
+                if (u == c) myc = row[u];
+            }
+            const double prhs = __shfl_sync(0xffffffffu, rhs, c);
+            const double pcc = __shfl_sync(0xffffffffu, myc, c);
+            if (t != c) {
+                const double q = myc / pcc;
+#pragma unroll
+                for (int u = 0; u < kGmmAnd; ++u) row[u] = fma(-q, piv[u], row[u]);
+                rhs = fma(-q, prhs, rhs);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kGmmAnd; ++u)
+            if (u == t) diag = row[u];
+        const double xl = t < cn ? rhs / diag : 0.0;
+        double sx = xl;
+        for (int o = 16; o > 0; o >>= 1) sx += __shfl_xor_sync(0xffffffffu, sx, o);
+        double al[kGmmAnd];
+#pragma unroll
+        for (int u = 0; u < kGmmAnd; ++u) al[u] = __shfl_sync(0xffffffffu, xl / sx, u);
+        __syncwarp();
+        for (int k = t; k < Kx; k += 32) {
+            double v = 0.0;
+#pragma unroll
+            for (int u = 0; u < kGmmAnd; ++u)
+                if (u < cn) v = fma(al[u], Fh[u][k], v);
+            F[k] = v;
+        }
+        head = (head + 1) % kGmmAnd;
+        cnt = cn;
+        __syncwarp();
     }
-    for (int i = t; i < Kx; i += 32) ft[i] = F[i] / kap;
+    // f~ is defined up to a constant and the mixing moves it along that line: return the
+    // representative with sum_k a_k f~_k = 0 (R-30)
+    double ma = 0.0, sa = 0.0;
+    for (int k = t; k < Kx; k += 32) { ma += (double)wx[k] * F[k]; sa += (double)wx[k]; }
+    for (int o = 16; o > 0; o >>= 1) {
+        ma += __shfl_xor_sync(0xffffffffu, ma, o);
+        sa += __shfl_xor_sync(0xffffffffu, sa, o);
+    }
+    for (int i = t; i < Kx; i += 32) ft[i] = (F[i] - ma / sa) / kap;
 }
 
 // Cholesky S_k = L L^T (fp64, one CTA, sequential columns), then Linv and log det L.
@@ -479,7 +546,7 @@ cudaError_t launch_gmm_init(const float *x, long long n, int d, int Kx, const fl
     if ((e = cudaFuncSetAttribute(k_gmm_chol, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2))) return e;
     k_gmm_sqrt<<<Kx, kGT, s5, st>>>(covx, d, R, flags);
     k_gmm_bures<<<Kx * Ky, kGT, s5, st>>>(mux, covx, Kx, muy, covy, Ky, d, R, C, flags);
-    k_gmm_sinkhorn<<<1, 32, 0, st>>>(C, Kx, Ky, wx, wy, eps, inner_tol, inner_max_iter, ft, flags);
+    k_gmm_sinkhorn_and<<<1, 32, 0, st>>>(C, Kx, Ky, wx, wy, eps, inner_tol, inner_max_iter, ft, flags);
     k_gmm_chol<<<Kx, kGT, s2, st>>>(covx, d, Linv, logdet, flags);
     long long b = (n + kGT - 1) / kGT;
     k_gmm_pot<<<(int)(b > 148 * 8 ? 148 * 8 : b), kGT, 0, st>>>(x, n, d, Kx, wx, mux, Linv, logdet, ft, pot);

@@ -60,6 +60,7 @@ __global__ void k_em_init(const float *__restrict__ x, int d, int K, const int *
     for (int e = threadIdx.x; e < K * d; e += blockDim.x)
         s.MU[e] = (double)x[(long long)idx[e / d] * d + e % d];
     for (int k = threadIdx.x; k < K; k += blockDim.x) s.W[k] = 1.0 / K;
+    if (threadIdx.x == 0) *s.LL = -INFINITY;   // (no previous log-likelihood)
 }
 
 // Cholesky S_k = L L^T (fp64), L^{-1}, log det L: one warp per component, lane i holding row i
@@ -67,8 +68,9 @@ __global__ void k_em_init(const float *__restrict__ x, int d, int K, const int *
 // the trailing lower triangle with column j broadcast by shuffles.  Then lane c forward-solves
 // column c of L^{-1} (L broadcast from shared memory).  DM >= d (compile-time register rows).
 template <int DM>
-__global__ void __launch_bounds__(32) k_em_chol(double *base, int K, int d, int *flags) {
+__global__ void __launch_bounds__(32) k_em_chol(double *base, int K, int d, int *flags, const int *skip) {
     __shared__ double sL[DM * DM];
+    if (skip && *(volatile const int *)skip) return;
     const EmState s = em_state(base, K, d);
     const int dd = d * d, k = blockIdx.x, lane = threadIdx.x;
     double a[DM];
@@ -133,8 +135,10 @@ __global__ void __launch_bounds__(32) k_em_chol(double *base, int K, int d, int 
 // three loads per statistic.  Otherwise each thread owns up to MAXS statistics.
 template <int MAXS, int DM, bool HARD, bool OWN>
 __global__ void __launch_bounds__(kEmT) k_em_estep(const float *__restrict__ x, long long n, int d, int K,
-                                                    const double *__restrict__ base, double *part) {
+                                                    const double *__restrict__ base, double *part,
+                                                    const int *skip) {
     extern __shared__ double sm[];
+    if (skip && *(volatile const int *)skip) return;
     // row strides padded by 16 bytes: the lanes of a warp read the rows of different points /
     // components at once, and unpadded 128-byte multiples would put them all in the same banks
     const int XS = em_xs(d);
@@ -313,7 +317,8 @@ __global__ void __launch_bounds__(kEmT) k_em_estep(const float *__restrict__ x, 
 
 // Reduction of the per-CTA partials, one warp per statistic: lane l sums CTAs l, l + 32, ... in
 // order, then a fixed shuffle tree (deterministic).  out[S + 1].
-__global__ void __launch_bounds__(kEmT) k_em_reduce(const double *part, int nb, int S1, double *out) {
+__global__ void __launch_bounds__(kEmT) k_em_reduce(const double *part, int nb, int S1, double *out, const int *skip) {
+    if (skip && *(volatile const int *)skip) return;
     const int st = (blockIdx.x * kEmT + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (st >= S1) return;
     double v = 0.0;
@@ -324,9 +329,16 @@ __global__ void __launch_bounds__(kEmT) k_em_reduce(const double *part, int nb, 
 
 // M-step from the reduced statistics: w, m, S (+ reg I) and the mean log-likelihood of the E-step
 // that produced them.
+// mode 0: EM step (tracks convergence: *LL holds the previous E-step's log-likelihood; flags[1]
+// = converged (|ll - ll_prev| < tol, the later EM kernels then return at once), flags[2] = EM
+// steps done); mode 1: the k-means start's one-hot M-step (LL reset to -inf); mode 2: the
+// evaluation pass into the scratch state (LL only matters).
 __global__ void __launch_bounds__(kEmT) k_em_mstep(const double *tot, long long n, int d, int K, double reg,
-                                                    double *base) {
+                                                    double *base, int mode, double tol, int *flags) {
+    if (mode == 0 && *(volatile const int *)&flags[1]) return;
     const EmState s = em_state(base, K, d);
+    const double ll_prev = *s.LL;
+    __syncthreads();
     const int T = d * (d + 1) / 2, per = 1 + d + T, S = K * per;
     const double eps10 = 10.0 * DBL_EPSILON;   // (as sklearn: n_k + 10 eps guards empty components)
     for (int e = threadIdx.x; e < K * d; e += blockDim.x) {
@@ -342,7 +354,14 @@ __global__ void __launch_bounds__(kEmT) k_em_mstep(const double *tot, long long 
         const double nk = tot[k * per] + eps10;
         s.COV[e] = tot[k * per + o] / nk - s.MU[k * d + r] * s.MU[k * d + c] + (r == c ? reg : 0.0);
     }
-    if (threadIdx.x == 0) *s.LL = tot[S] / (double)n - 0.5 * d * log(2.0 * 3.14159265358979323846);
+    if (threadIdx.x == 0) {
+        const double ll = tot[S] / (double)n - 0.5 * d * log(2.0 * 3.14159265358979323846);
+        *s.LL = mode == 1 ? -INFINITY : ll;
+        if (mode == 0) {
+            flags[2] += 1;
+            if (tol > 0.0 && fabs(ll - ll_prev) < tol) flags[1] = 1;
+        }
+    }
 }
 
 // Lloyd's center update from the hard statistics: a non-empty cluster moves to its mean.
@@ -366,36 +385,37 @@ __global__ void k_em_out(const double *base, int K, int d, float *w, float *mu, 
 
 template <int MAXS, int DM, bool HARD, bool OWN>
 static cudaError_t launch_estep_d(const float *x, long long n, int d, int K, const double *base, double *part,
-                                  cudaStream_t st) {
+                                  const int *skip, cudaStream_t st) {
     const size_t smem = sizeof(double) * ((size_t)kEmTile * (em_xs(d) + K) + kEmTile + (size_t)K * (DM * DM + DM + 5));
     cudaError_t e = cudaFuncSetAttribute(k_em_estep<MAXS, DM, HARD, OWN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
-    k_em_estep<MAXS, DM, HARD, OWN><<<kEmBlocks, kEmT, smem, st>>>(x, n, d, K, base, part);
+    k_em_estep<MAXS, DM, HARD, OWN><<<kEmBlocks, kEmT, smem, st>>>(x, n, d, K, base, part, skip);
     return cudaGetLastError();
 }
 template <int MAXS, bool HARD, bool OWN>
 static cudaError_t launch_estep_m(const float *x, long long n, int d, int K, const double *base, double *part,
-                                  cudaStream_t st) {
-    if (d <= 8) return launch_estep_d<MAXS, 8, HARD, OWN>(x, n, d, K, base, part, st);
-    if (d <= 16) return launch_estep_d<MAXS, 16, HARD, OWN>(x, n, d, K, base, part, st);
-    return launch_estep_d<MAXS, 32, HARD, OWN>(x, n, d, K, base, part, st);
+                                  const int *skip, cudaStream_t st) {
+    if (d <= 8) return launch_estep_d<MAXS, 8, HARD, OWN>(x, n, d, K, base, part, skip, st);
+    if (d <= 16) return launch_estep_d<MAXS, 16, HARD, OWN>(x, n, d, K, base, part, skip, st);
+    return launch_estep_d<MAXS, 32, HARD, OWN>(x, n, d, K, base, part, skip, st);
 }
 template <bool HARD>
 static cudaError_t launch_estep(int maxs, const float *x, long long n, int d, int K, const double *base,
-                                double *part, cudaStream_t st) {
-    if (K * d <= kEmT) return launch_estep_m<1, HARD, true>(x, n, d, K, base, part, st);
-    if (maxs <= 8) return launch_estep_m<8, HARD, false>(x, n, d, K, base, part, st);
-    if (maxs <= 20) return launch_estep_m<20, HARD, false>(x, n, d, K, base, part, st);
-    return launch_estep_m<40, HARD, false>(x, n, d, K, base, part, st);
+                                double *part, const int *skip, cudaStream_t st) {
+    if (K * d <= kEmT) return launch_estep_m<1, HARD, true>(x, n, d, K, base, part, skip, st);
+    if (maxs <= 8) return launch_estep_m<8, HARD, false>(x, n, d, K, base, part, skip, st);
+    if (maxs <= 20) return launch_estep_m<20, HARD, false>(x, n, d, K, base, part, skip, st);
+    return launch_estep_m<40, HARD, false>(x, n, d, K, base, part, skip, st);
 }
 
 // iters EM steps from the start above; the state (em_state_doubles) and partials
 // (em_partial_doubles) are caller workspace; cov0 = biased covariance of x (d x d).  A final
 // E-step evaluates the mean log-likelihood of the returned parameters.
 cudaError_t launch_gmm_fit(const float *x, long long n, int d, int K, const int *idx, const double *cov0,
-                           int kmeans_iters, int iters, double reg, double *state, double *part, int *flags,
-                           float *w, float *mu, float *cov, double *ll_out, cudaStream_t st) {
+                           int kmeans_iters, int iters, double tol, double reg, double *state, double *part,
+                           int *flags, float *w, float *mu, float *cov, double *ll_out, int *h_conv,
+                           cudaStream_t st) {
     const int S = em_stats(K, d);
     const int maxs = (S + kEmT - 1) / kEmT;
     if (d < 1 || d > 32 || K < 1 || maxs > 40) return cudaErrorInvalidValue;
@@ -404,24 +424,36 @@ cudaError_t launch_gmm_fit(const float *x, long long n, int d, int K, const int 
     const int rblocks = (32 * (S + 1) + kEmT - 1) / kEmT;
     cudaError_t e = cudaSuccess;
     for (int t = 0; t <= kmeans_iters && kmeans_iters > 0; ++t) {   // Lloyd, then the one-hot M-step
-        e = launch_estep<true>(maxs, x, n, d, K, state, part, st);
+        e = launch_estep<true>(maxs, x, n, d, K, state, part, nullptr, st);
         if (e != cudaSuccess) return e;
-        k_em_reduce<<<rblocks, kEmT, 0, st>>>(part, kEmBlocks, S + 1, tot);
+        k_em_reduce<<<rblocks, kEmT, 0, st>>>(part, kEmBlocks, S + 1, tot, nullptr);
         if (t < kmeans_iters) k_km_update<<<1, kEmT, 0, st>>>(tot, d, K, state);
-        else k_em_mstep<<<1, kEmT, 0, st>>>(tot, n, d, K, reg, state);
+        else k_em_mstep<<<1, kEmT, 0, st>>>(tot, n, d, K, reg, state, 1, 0.0, flags);
     }
+    const int *skip = flags + 1;   // set once EM has converged (tol > 0): the rest are no-ops
+    int poll = 2, next_poll = 2;   // tol > 0: the host reads the flag after 2, 4, 8, ... steps
     for (int it = 0; it <= iters; ++it) {
-        if (d <= 8) k_em_chol<8><<<K, 32, 0, st>>>(state, K, d, flags);
-        else if (d <= 16) k_em_chol<16><<<K, 32, 0, st>>>(state, K, d, flags);
-        else k_em_chol<32><<<K, 32, 0, st>>>(state, K, d, flags);
-        e = launch_estep<false>(maxs, x, n, d, K, state, part, st);
+        if (tol > 0.0 && h_conv && it == next_poll && it < iters) {
+            e = cudaMemcpyAsync(h_conv, flags + 1, sizeof(int), cudaMemcpyDeviceToHost, st);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+            if (e != cudaSuccess) return e;
+            if (*h_conv) it = iters;   // straight to the evaluation pass
+            poll *= 2;
+            next_poll = it + poll;
+        }
+        const bool eval = it == iters;   // evaluation only: the log-likelihood of the returned parameters
+        const int *sk = eval ? nullptr : skip;
+        if (d <= 8) k_em_chol<8><<<K, 32, 0, st>>>(state, K, d, flags, sk);
+        else if (d <= 16) k_em_chol<16><<<K, 32, 0, st>>>(state, K, d, flags, sk);
+        else k_em_chol<32><<<K, 32, 0, st>>>(state, K, d, flags, sk);
+        e = launch_estep<false>(maxs, x, n, d, K, state, part, sk, st);
         if (e != cudaSuccess) return e;
-        k_em_reduce<<<rblocks, kEmT, 0, st>>>(part, kEmBlocks, S + 1, tot);
-        if (it == iters) {   // evaluation only: the log-likelihood of the returned parameters
-            k_em_mstep<<<1, kEmT, 0, st>>>(tot, n, d, K, reg, state + em_state_doubles(K, d));
+        k_em_reduce<<<rblocks, kEmT, 0, st>>>(part, kEmBlocks, S + 1, tot, sk);
+        if (eval) {
+            k_em_mstep<<<1, kEmT, 0, st>>>(tot, n, d, K, reg, state + em_state_doubles(K, d), 2, 0.0, flags);
             break;
         }
-        k_em_mstep<<<1, kEmT, 0, st>>>(tot, n, d, K, reg, state);
+        k_em_mstep<<<1, kEmT, 0, st>>>(tot, n, d, K, reg, state, 0, tol, flags);
     }
     // the evaluation pass wrote a scratch state; its LL is the returned parameters' likelihood
     const EmState scratch = em_state(state + em_state_doubles(K, d), K, d);

@@ -58,6 +58,27 @@ def test_fit_kmeans_start_parity(O, ctx, n, d, K, km, iters):
     assert abs(ll - llo) <= 1e-9 * max(1.0, abs(llo))
 
 
+@pytest.mark.parametrize("n,d,K,tol", [(2500, 7, 5, 1e-3), (16384, 16, 8, 1e-3), (3000, 4, 6, 1e-5)])
+def test_fit_tol_stops_like_the_oracle(O, ctx, n, d, K, tol):
+    """sklearn's convergence rule on the device (flags set by the M-step, later EM kernels
+    return at once): the same EM step count and parameters as the oracle (itself pinned to
+    sklearn's n_iter_)."""
+    import paper_2206_07630_b200 as sk
+    if n == 16384:
+        x = gen.c3().x
+    else:
+        rng = np.random.default_rng(n + K)
+        cents = rng.standard_normal((K, d)) * 3
+        x = (cents[rng.integers(0, K, n)] + rng.standard_normal((n, d)) * 0.9).astype(np.float32)
+    idx = gen.gmm_start_idx(len(x), K, seed=n + 2)
+    g, ll, it = sk.sinkhorn_fit_gmm(ctx, torch.from_numpy(x).cuda(), K, idx, iters=100, kmeans_iters=10, tol=tol,
+                                    return_iters=True)
+    w, m, S, llo, ito = O.gmm_fit(x, K, idx, 100, 1e-6, kmeans_iters=10, tol=tol, return_iters=True)
+    assert it == ito, (it, ito)
+    assert _close(g["weights"], w, 1e-6) and _close(g["means"], m, 1e-6) and _close(g["covs"], S, 1e-6)
+    assert abs(ll - llo) <= 1e-9 * max(1.0, abs(llo))
+
+
 def test_fitted_gmm_initializer_c3(O, ctx):
     """The paper's GMM initializer with GMMs fitted on the device: f0 vs the oracle's
     initializer evaluated with the oracle's own fitted mixtures."""
@@ -88,6 +109,8 @@ def test_fit_errors(ctx):
         sk.sinkhorn_fit_gmm(ctx, torch.rand(100, 33, device="cuda"), 2, [0, 1])   # d > 32
     with pytest.raises(sk.SinkhornError):
         sk.sinkhorn_fit_gmm(ctx, x, 2, [0, 1], kmeans_iters=-1)
+    with pytest.raises(sk.SinkhornError):
+        sk.sinkhorn_fit_gmm(ctx, x, 2, [0, 1], tol=-1.0)
     bad = x.clone(); bad[5, 1] = float("inf")
     with pytest.raises(sk.SinkhornError):
         sk.sinkhorn_fit_gmm(ctx, bad, 2, [0, 1])

@@ -12,9 +12,9 @@ ix, iy = gen.gmm_start_idx(p.n, 8, 3), gen.gmm_start_idx(p.m, 8, 4)
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
 for rep in range(3):
     ev[0].record()
-    gx, _ = sk.sinkhorn_fit_gmm(ctx, x, 8, ix, iters=50, kmeans_iters=10)
+    gx, _ = sk.sinkhorn_fit_gmm(ctx, x, 8, ix, iters=100, kmeans_iters=10, tol=1e-3)
     ev[1].record()
-    gy, _ = sk.sinkhorn_fit_gmm(ctx, y, 8, iy, iters=50, kmeans_iters=10)
+    gy, _ = sk.sinkhorn_fit_gmm(ctx, y, 8, iy, iters=100, kmeans_iters=10, tol=1e-3)
     ev[2].record()
     f0, side = sk.sinkhorn_init_gmm(ctx, x, y, gx, gy, p.eps)
     ev[3].record()
