@@ -145,11 +145,7 @@ def test_anderson_sharded_emulated(O, ctx, world, mode, d):
     x = rng.random((n, d)).astype(np.float32)
     y = rng.random((m, d)).astype(np.float32)
     eps = float(np.float32(0.05 * gen.mean_sq_cost(x, y)))
-    ctx.check(ctx.lib.sk_set_anderson(ctx.h, 5))
-    try:
-        f, g, rep = sk.sinkhorn_solve_sharded_emulated(ctx, world, _cuda(x), _cuda(y), eps, mode=mode)
-    finally:
-        ctx.lib.sk_set_anderson(ctx.h, 0)
+    f, g, rep = sk.sinkhorn_solve_sharded_emulated(ctx, world, _cuda(x), _cuda(y), eps, mode=mode, anderson=5)
     L = rep["iterations"]
     ref = O.sinkhorn_anderson(x, y, eps, mem=5)
     assert abs(L - ref.iterations) <= count_tol(ref.iterations), (L, ref.iterations)
