@@ -112,8 +112,8 @@ int32_t sk_version(void);
  * the over-relaxed "momentum" of P:73; omega = 1: plain Sinkhorn, the default).
  * With omega != 1 the row marginals are not exact after an f-update, so err_l adds the row
  * term sum_i a_i |expm1((f_i - fsk_i)/eps)| and E uses sum_ij P_ij (both exact, O(n)).
- * omega must lie in (0, 2) (SK_EINVAL otherwise); the sharded entries return
- * SK_EUNSUPPORTED for omega != 1. */
+ * omega must lie in (0, 2) (SK_EINVAL otherwise); the sharded entries sum the row terms over
+ * the ranks (one ncclAllReduce of 2 doubles per sweep). */
 sk_status sk_set_relaxation(sk_ctx *ctx, float omega);
 /* eps-decay ("gradually reducing the regularization term from 5 eps to eps by a factor
  * of 0.8"; R-25) for the following solves on this context: sweep l = 1, 2, ... uses

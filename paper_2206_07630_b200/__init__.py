@@ -313,9 +313,16 @@ def sinkhorn_soft_rank_sort(ctx: Context, x, y, eps: float, f, g, z=None,
 
 def sinkhorn_solve_sharded_emulated(ctx: Context, world: int, x, y, eps: float, tol: float = 1e-3,
                                     max_iter: int = 10000, check_every: int = 1, a=None, b=None,
-                                    mode: str = "auto", f_init=None, anderson: int = 0):
+                                    mode: str = "auto", f_init=None, anderson: int = 0, omega: float = 1.0):
     """The row-sharded algorithm for `world` virtual ranks on one GPU (test entry).
-    anderson: Anderson memory (sk_set_anderson), 0 = off."""
+    anderson: Anderson memory (sk_set_anderson), 0 = off; omega: relaxation (sk_set_relaxation)."""
+    if omega != 1.0:
+        ctx.check(ctx.lib.sk_set_relaxation(ctx.h, ctypes.c_float(omega)))
+        try:
+            return sinkhorn_solve_sharded_emulated(ctx, world, x, y, eps, tol, max_iter, check_every, a, b, mode,
+                                                   f_init, anderson)
+        finally:
+            ctx.lib.sk_set_relaxation(ctx.h, ctypes.c_float(1.0))
     if anderson:
         ctx.check(ctx.lib.sk_set_anderson(ctx.h, int(anderson)))
         try:
@@ -336,9 +343,18 @@ def sinkhorn_solve_sharded_emulated(ctx: Context, world: int, x, y, eps: float, 
 
 def sinkhorn_solve_sharded(ctx: Context, n_total: int, row0: int, x_local, y, eps: float,
                            tol: float = 1e-3, max_iter: int = 10000, check_every: int = 1,
-                           a_local=None, b=None, mode: str = "auto", f_init_local=None, anderson: int = 0):
+                           a_local=None, b=None, mode: str = "auto", f_init_local=None, anderson: int = 0,
+                           omega: float = 1.0):
     """Rows [row0, row0 + n_local) of an n_total-row problem on this rank (sk_comm_init first);
-    anderson: Anderson memory (sk_set_anderson; one 9-double allreduce per sweep), 0 = off."""
+    anderson: Anderson memory (sk_set_anderson; one 9-double allreduce per sweep), 0 = off;
+    omega: relaxation (sk_set_relaxation; one 2-double allreduce of the row terms per sweep)."""
+    if omega != 1.0:
+        ctx.check(ctx.lib.sk_set_relaxation(ctx.h, ctypes.c_float(omega)))
+        try:
+            return sinkhorn_solve_sharded(ctx, n_total, row0, x_local, y, eps, tol, max_iter, check_every,
+                                          a_local, b, mode, f_init_local, anderson)
+        finally:
+            ctx.lib.sk_set_relaxation(ctx.h, ctypes.c_float(1.0))
     if anderson:
         ctx.check(ctx.lib.sk_set_anderson(ctx.h, int(anderson)))
         try:

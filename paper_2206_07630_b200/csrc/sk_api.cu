@@ -311,8 +311,6 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
     const int amem = ctx->anderson >= 2 ? ctx->anderson : 0;
     if (amem && P.omega != 1.f)
         return fail(ctx, SK_EUNSUPPORTED, "Anderson acceleration needs omega = 1");
-    if (P.omega != 1.f && (sharded || P.partitioned))
-        return fail(ctx, SK_EUNSUPPORTED, "relaxation (omega != 1) is supported by the unsharded solver only");
     if (ctx->decay_init > 0.f && (sharded || P.partitioned))
         return fail(ctx, SK_EUNSUPPORTED, "eps-decay is supported by the unsharded solver only");
     const long long m = P.m, n_glob = P.n_total;
@@ -600,6 +598,7 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
                                blkb, nullptr, 0.f, sharded ? 1 : 0, i + 1 < ns ? 1 : 0};
                 if (row_seed) mrow.Q = &Y;
                 mrow.omega = P.omega;
+                mrow.accum = i > 0 ? 1 : 0;
                 mrow.wts = slices[i].a;   // (the relaxed row error term weighs rows by a)
                 mrow.tc_fold = tc && row_seed && sweep >= 1;   // the next row pass is seeded
                 mrow.tc_margin = tc_margin;
@@ -612,6 +611,10 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
                                             andvec + anderson_vec_doubles() * i, st));
                     launched += 2;
                 }
+            }
+            if (P.omega != 1.f && P.nccl && sharded) {   // relaxed: the row terms of err and E over the ranks
+                int r = g_nccl.allreduce(&status->row_err, &status->row_err, 2, kNcclFloat64, kNcclSum, ctx->comm, st);
+                if (r != 0) return fail(ctx, SK_ENCCL, "ncclAllReduce(row terms) failed");
             }
             if (amem) {   // the sums over the ranks, the decision, f^{l+1} = sum_u alpha_u T(f_u)
                 if (P.nccl && sharded) {

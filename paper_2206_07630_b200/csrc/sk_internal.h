@@ -169,6 +169,7 @@ struct MergePass {
     int tc_fold = 0;          // K3 side: also fold lse + margin as the next pass's row shift
     float tc_margin = 4.f;    //          log2 units above the LSE (SK_TC_SEED_MARGIN: test knob)
     float omega = 1.f;        // Alg. 1's relaxation: h <- (1 - omega) h_old + omega h_sinkhorn
+    int accum = 0;            // relaxed ROW of a later slice: add its row terms (row_err, mass_dev)
     int anderson = 0;         // Anderson (R-27): COL takes no decision; ROW writes its slice's
     double *and_err = nullptr;//   row term of err_l for (f^l, g~) to *and_err (K19 decides)
 };

@@ -468,7 +468,10 @@ __global__ void __launch_bounds__(kMT) k_merge(MergePass Mp, Side S, Side Qs) {
         if (bt && !Mp.sharded) { st->nonfinite = 1; st->stop = 1; st->final_iter = l; }
     } else if (Mp.mode == MERGE_ROW) {
         st->ticket_row = 0;
-        if (Mp.omega != 1.f) { st->row_err = et; st->mass_dev = et2; }
+        if (Mp.omega != 1.f) {   // (row shards: summed over the slices here, over ranks by an allreduce)
+            if (Mp.accum) { st->row_err += et; st->mass_dev += et2; }
+            else { st->row_err = et; st->mass_dev = et2; }
+        }
         if (bt && !Mp.sharded) { st->nonfinite = 1; st->stop = 1; st->final_iter = l; }
         else if (!Mp.no_iter_inc) st->iter = l + 1;
     } else {

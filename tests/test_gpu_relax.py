@@ -91,14 +91,29 @@ def test_relaxation_argument_errors(ctx):
     import paper_2206_07630_b200 as sk
     for bad in (0.0, -1.0, 2.0, float("nan")):
         assert ctx.lib.sk_set_relaxation(ctx.h, ctypes.c_float(bad)) == 1   # SK_EINVAL
-    p = gen.c4(n=4096)
-    x, y = _cuda(p.x), _cuda(p.y)
-    with pytest.raises(sk.SinkhornError):   # the sharded entries: unsupported
-        ctx.check(ctx.lib.sk_set_relaxation(ctx.h, ctypes.c_float(1.5)))
-        try:
-            sk.sinkhorn_solve_sharded_emulated(ctx, 2, x, y, p.eps, mode="online")
-        finally:
-            ctx.lib.sk_set_relaxation(ctx.h, ctypes.c_float(1.0))
+
+
+@pytest.mark.parametrize("world,mode,d,omega", [(2, "online", 3, 1.5), (4, "online", 40, 1.3), (8, "stored", 16, 1.4),
+                                              (2, "online", 8, 0.8)])
+def test_relaxed_sharded_emulated(O, ctx, world, mode, d, omega):
+    """omega != 1 with rows sharded over `world` emulated ranks: the row terms of err_l and of
+    sum P (E) are summed over the shards (over ranks: one 2-double allreduce per sweep)."""
+    import paper_2206_07630_b200 as sk
+    rng = np.random.default_rng(60 + world + d)
+    n, m = 6000, 1600
+    x = rng.random((n, d)).astype(np.float32)
+    y = rng.random((m, d)).astype(np.float32)
+    a = gen.random_weights(n, rng)
+    eps = float(np.float32(0.04 * gen.mean_sq_cost(x, y)))
+    f, g, rep = sk.sinkhorn_solve_sharded_emulated(ctx, world, _cuda(x), _cuda(y), eps, a=_cuda(a), mode=mode,
+                                                   omega=omega)
+    L = rep["iterations"]
+    ref = O.sinkhorn(x, y, eps, a=a, omega=omega)
+    assert abs(L - ref.iterations) <= count_tol(ref.iterations), (L, ref.iterations)
+    lock = O.sinkhorn(x, y, eps, a=a, tol=0, max_iter=L, omega=omega)
+    assert_pair_close(f.cpu().numpy(), g.cpu().numpy(), lock.f, lock.g, eps, what=f"relaxed x{world} {mode}")
+    assert_obj_close(rep["dual_objective"], lock.E, eps)
+    assert rep["converged"] and plan_marginal_error(x, y, f.cpu().numpy(), g.cpu().numpy(), eps, a) <= 1.05e-3 + 2e-5
 
 
 # ------------------------------------------------------------- eps-decay (NEXT-1, R-25)
