@@ -121,7 +121,8 @@ sk_status sk_set_relaxation(sk_ctx *ctx, float omega);
  * eps_l > eps are not checked (the stop rule runs on sweeps l > T with (l - T) % check_every
  * == 0) and count in rep.iterations.  init <= 1 turns it off (the default); otherwise rate
  * must lie in (0, 1) (SK_EINVAL).  On the multi-kernel paths it needs omega = 1
- * (SK_EUNSUPPORTED otherwise) and max_iter > T; the sharded entries return SK_EUNSUPPORTED. */
+ * (SK_EUNSUPPORTED otherwise) and max_iter > T; the sharded entries chain the T decay sweeps
+ * the same way (each rank's rows through its own f). */
 sk_status sk_set_eps_decay(sk_ctx *ctx, float init, float rate);
 /* Anderson acceleration ("Anderson acceleration (And = 5)"; R-27) for
  * the following solves on this context: type-II Anderson with memory mem on the sweep map

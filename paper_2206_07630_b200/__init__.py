@@ -313,9 +313,18 @@ def sinkhorn_soft_rank_sort(ctx: Context, x, y, eps: float, f, g, z=None,
 
 def sinkhorn_solve_sharded_emulated(ctx: Context, world: int, x, y, eps: float, tol: float = 1e-3,
                                     max_iter: int = 10000, check_every: int = 1, a=None, b=None,
-                                    mode: str = "auto", f_init=None, anderson: int = 0, omega: float = 1.0):
+                                    mode: str = "auto", f_init=None, anderson: int = 0, omega: float = 1.0,
+                                    eps_decay=None):
     """The row-sharded algorithm for `world` virtual ranks on one GPU (test entry).
-    anderson: Anderson memory (sk_set_anderson), 0 = off; omega: relaxation (sk_set_relaxation)."""
+    anderson: Anderson memory (sk_set_anderson), 0 = off; omega: relaxation (sk_set_relaxation);
+    eps_decay: (init, rate) for sk_set_eps_decay, None = off."""
+    if eps_decay is not None:
+        ctx.check(ctx.lib.sk_set_eps_decay(ctx.h, ctypes.c_float(eps_decay[0]), ctypes.c_float(eps_decay[1])))
+        try:
+            return sinkhorn_solve_sharded_emulated(ctx, world, x, y, eps, tol, max_iter, check_every, a, b, mode,
+                                                   f_init, anderson, omega)
+        finally:
+            ctx.lib.sk_set_eps_decay(ctx.h, ctypes.c_float(0.0), ctypes.c_float(1.0))
     if omega != 1.0:
         ctx.check(ctx.lib.sk_set_relaxation(ctx.h, ctypes.c_float(omega)))
         try:

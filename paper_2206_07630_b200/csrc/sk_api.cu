@@ -311,8 +311,6 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
     const int amem = ctx->anderson >= 2 ? ctx->anderson : 0;
     if (amem && P.omega != 1.f)
         return fail(ctx, SK_EUNSUPPORTED, "Anderson acceleration needs omega = 1");
-    if (ctx->decay_init > 0.f && (sharded || P.partitioned))
-        return fail(ctx, SK_EUNSUPPORTED, "eps-decay is supported by the unsharded solver only");
     const long long m = P.m, n_glob = P.n_total;
     const int ns = (int)slices.size();
     long long n_max = 0, n_sum = 0;
@@ -681,6 +679,34 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
     rep->build_ms = build_ms;
     rep->solve_ms = ms;
     if (hs.nonfinite) return fail(ctx, SK_ENONFINITE, "potentials became non-finite after sweep %d", L);
+    return SK_OK;
+}
+
+// eps-decay (R-25) around solve_core for the sharded entries: with omega = 1 a sweep is a map
+// f -> f, so the T decay sweeps are one-sweep solves at eps_l chained through each slice's f
+// (as the unsharded multi-kernel path does in solve_impl), then the solve at the target eps.
+sk_status solve_core_decay(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, sk_report *rep) {
+    if (ctx->decay_init <= 0.f) return solve_core(ctx, P, slices, rep);
+    if (P.omega != 1.f) return fail(ctx, SK_EUNSUPPORTED, "eps-decay with omega != 1 runs on the on-chip solver only");
+    if (ctx->anderson >= 2) return fail(ctx, SK_EUNSUPPORTED, "Anderson acceleration does not combine with eps-decay");
+    int T = 0;
+    while (T < P.max_iter && (double)P.eps * ctx->decay_init * std::pow((double)ctx->decay_rate, T) > (double)P.eps) ++T;
+    if (P.max_iter - T < 1) return fail(ctx, SK_EINVAL, "max_iter must exceed the %d eps-decay sweeps", T);
+    double extra_ms = 0.0;
+    for (int t = 0; t < T; ++t) {
+        Problem Pt = P;
+        Pt.eps = (float)((double)P.eps * ctx->decay_init * std::pow((double)ctx->decay_rate, t));
+        Pt.max_iter = 1;
+        sk_report r1{};
+        CK(solve_core(ctx, Pt, slices, &r1));
+        extra_ms += r1.solve_ms;
+        for (auto &sl : slices) sl.f_init = sl.f;   // chained through f
+    }
+    Problem Pf = P;
+    Pf.max_iter = P.max_iter - T;
+    CK(solve_core(ctx, Pf, slices, rep));
+    rep->iterations += T;
+    rep->solve_ms += extra_ms;
     return SK_OK;
 }
 
@@ -1398,7 +1424,7 @@ sk_status sinkhorn_solve_sharded(sk_ctx *ctx, int64_t n_total, int64_t row0, int
     P.g = dg;
     P.world = ctx->world; P.nccl = ctx->world > 1; P.partitioned = true; P.omega = ctx->omega;
     std::vector<Slice> sl{Slice{row0, n_local, dx, da, dfi, df, ctx->rank}};
-    sk_status s = solve_core(ctx, P, sl, rep);
+    sk_status s = solve_core_decay(ctx, P, sl, rep);
     if (s != SK_OK && s != SK_ENONFINITE) return s;
     sk_status s2 = sg.flush();
     CU(cudaStreamSynchronize(ctx->stream));
@@ -1440,7 +1466,7 @@ sk_status sinkhorn_solve_sharded_emulated(sk_ctx *ctx, int32_t world, int64_t n,
         if (nl < 1) return fail(ctx, SK_EUNSUPPORTED, "rank %d would own no rows (n too small for %d ranks)", r, world);
         sl.push_back(Slice{r0, nl, dx + r0 * d, da ? da + r0 : nullptr, dfi ? dfi + r0 : nullptr, df + r0, r});
     }
-    sk_status s = solve_core(ctx, P, sl, rep);
+    sk_status s = solve_core_decay(ctx, P, sl, rep);
     if (s != SK_OK && s != SK_ENONFINITE) return s;
     sk_status s2 = sg.flush();
     CU(cudaStreamSynchronize(ctx->stream));

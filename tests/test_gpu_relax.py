@@ -159,3 +159,23 @@ def test_eps_decay_max_iter_inside_the_decay(ctx):
     p = gen.c1()
     f, g, rep = sk.sinkhorn_solve(ctx, _cuda(p.x), _cuda(p.y), p.eps, max_iter=3, eps_decay=(5.0, 0.8))
     assert rep["iterations"] == 3 and not rep["converged"]
+
+
+@pytest.mark.parametrize("world,mode,d", [(2, "online", 3), (4, "stored", 16)])
+def test_eps_decay_sharded_emulated(O, ctx, world, mode, d):
+    """eps-decay (R-25) with rows sharded over emulated ranks: the decay sweeps are chained
+    one-sweep solves through each shard's f, as on the unsharded multi-kernel path."""
+    import paper_2206_07630_b200 as sk
+    rng = np.random.default_rng(70 + world + d)
+    n, m = 6000, 1600
+    x = rng.random((n, d)).astype(np.float32)
+    y = rng.random((m, d)).astype(np.float32)
+    eps = float(np.float32(0.03 * gen.mean_sq_cost(x, y)))
+    f, g, rep = sk.sinkhorn_solve_sharded_emulated(ctx, world, _cuda(x), _cuda(y), eps, mode=mode,
+                                                   eps_decay=(5.0, 0.8))
+    L = rep["iterations"]
+    ref = O.sinkhorn(x, y, eps, eps_decay=(5.0, 0.8))
+    assert abs(L - ref.iterations) <= count_tol(ref.iterations), (L, ref.iterations)
+    lock = O.sinkhorn(x, y, eps, tol=0, max_iter=L, eps_decay=(5.0, 0.8))
+    assert_pair_close(f.cpu().numpy(), g.cpu().numpy(), lock.f, lock.g, eps, what=f"decay x{world} {mode}")
+    assert_obj_close(rep["dual_objective"], lock.E, eps)
