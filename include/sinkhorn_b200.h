@@ -272,7 +272,7 @@ sk_status sinkhorn_init_gaussian(sk_ctx *ctx, int64_t n, int64_t m, int32_t d, c
  * tau (Ky, wy, muy, covy) fitted to nu: C~_kl = ||m_k - m'_l||^2 + B^2(S_k, S'_l)
  * (Eq. 6) with fp64 Newton-Schulz square roots; the Kx x Ky entropic
  * problem at the same eps (R-13) is solved in fp64 with Anderson acceleration (memory 5,
- * DESIGN.md R-30; err = the row term of (f^l, g_sk(f^l))) to inner_tol (max inner_max_iter
+ * DESIGN.md R-29; err = the row term of (f^l, g_sk(f^l))) to inner_tol (max inner_max_iter
  * sweeps; the binding's default 1e-9: ~100 sweeps at C3) -> f~; f^(0)(x) = sum_k f~_k p_k(x),
  * p_k the posterior responsibilities (Eq. 7), on the smaller side (*side as above).
  * Mixture parameters are inputs (sinkhorn_fit_gmm fits them).  d <= 64, K <= 64. */

@@ -396,7 +396,7 @@ def gmm_cost(mx, cx, my, cy):
 
 def init_gmm(x, y, gx: dict, gy: dict, eps, inner_tol=1e-9, inner_max_iter=100000):
     """GMM initializer (Sec. 3.3): K x K Bures-cost Sinkhorn at the same eps
-    (reading R-13), solved with Anderson acceleration (memory 5, reading R-30) -> f~;
+    (reading R-13), solved with Anderson acceleration (memory 5, reading R-29) -> f~;
     f0_i = sum_k f~_k p_k(x_i) on the smaller side."""
     x, y = _pts(x), _pts(y)
     if x.shape[0] > y.shape[0]:
@@ -406,7 +406,7 @@ def init_gmm(x, y, gx: dict, gy: dict, eps, inner_tol=1e-9, inner_max_iter=10000
     a = _d(gx["weights"])
     r = sinkhorn_matrix(C, eps, a=a, b=_d(gy["weights"]), tol=inner_tol, max_iter=inner_max_iter, anderson=5)
     # (f~ is defined up to a constant and Anderson's mixing moves it along that line: the
-    # returned f~ is the representative with sum_k a_k f~_k = 0, R-30)
+    # returned f~ is the representative with sum_k a_k f~_k = 0, R-29)
     ft = r.f - (a * r.f).sum() / a.sum()
     P = np.exp(gmm_log_resp(x, gx["weights"], gx["means"], gx["covs"]))
     return P @ ft, 0

@@ -301,7 +301,7 @@ __global__ void __launch_bounds__(kGT) k_gmm_bures(const float *mux, const float
 
 // K x K entropic OT (Alg. 1, g-then-f; R-13), one warp, in log2 units: F = f kappa,
 // G = g kappa, Kc = -C kappa (kappa = log2(e)/eps, fp64).
-// The K x K solve with Anderson acceleration (memory 5, reading R-30: the inner problem of the
+// The K x K solve with Anderson acceleration (memory 5, reading R-29: the inner problem of the
 // GMM initializer converges in thousands of plain sweeps at C3's eps; the paper only asks for
 // its solution).  fp64 throughout (the mixing is sensitive to rounding near the solution).  Sweep
 // l: G = g_sk(F), T = f_sk(G); err_l = sum_k a_k |expm1(ln2 (F_k - T_k))| (the row term of
@@ -440,7 +440,7 @@ __global__ void __launch_bounds__(32) k_gmm_sinkhorn_and(const double *C, int Kx
         __syncwarp();
     }
     // f~ is defined up to a constant and the mixing moves it along that line: return the
-    // representative with sum_k a_k f~_k = 0 (R-30)
+    // representative with sum_k a_k f~_k = 0 (R-29)
     double ma = 0.0, sa = 0.0;
     for (int k = t; k < Kx; k += 32) { ma += (double)wx[k] * F[k]; sa += (double)wx[k]; }
     for (int o = 16; o > 0; o >>= 1) {
