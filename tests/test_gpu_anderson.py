@@ -181,3 +181,24 @@ def test_anderson_argument_and_path_errors(ctx):
     # the context is back to plain Sinkhorn afterwards
     _, _, r = sk.sinkhorn_solve(ctx, x, y, p.eps)
     assert r["iterations"] > 100
+
+
+def test_anderson_host_buffers_match_device(ctx):
+    """The e2e path: host (pinned) inputs staged by the library give the same Anderson solve as
+    device inputs (on-chip batch and multi-kernel)."""
+    import paper_2206_07630_b200 as sk
+    c2 = gen.c2(B=16, n=1024)
+    xh, yh = torch.from_numpy(c2.x).pin_memory(), torch.from_numpy(c2.y).pin_memory()
+    fd, gd, rd = sk.sinkhorn_solve(ctx, xh.cuda(), yh.cuda(), c2.eps, y_shared=True, anderson=5)
+    fh, gh, rh = sk.sinkhorn_solve(ctx, xh, yh, c2.eps, y_shared=True, anderson=5)
+    assert [r["iterations"] for r in rd] == [r["iterations"] for r in rh]
+    assert torch.equal(fd.cpu(), fh) and torch.equal(gd.cpu(), gh)
+    rng = np.random.default_rng(9)
+    x = rng.random((3000, 3)).astype(np.float32)
+    y = rng.random((2500, 3)).astype(np.float32)
+    eps = float(np.float32(0.05 * gen.mean_sq_cost(x, y)))
+    xh, yh = torch.from_numpy(x).pin_memory(), torch.from_numpy(y).pin_memory()
+    fd, gd, rd = sk.sinkhorn_solve(ctx, xh.cuda(), yh.cuda(), eps, mode="online", anderson=5)
+    fh, gh, rh = sk.sinkhorn_solve(ctx, xh, yh, eps, mode="online", anderson=5)
+    assert rd["iterations"] == rh["iterations"]
+    assert torch.equal(fd.cpu(), fh) and torch.equal(gd.cpu(), gh)
