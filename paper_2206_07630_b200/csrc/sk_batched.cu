@@ -359,20 +359,23 @@ __device__ __forceinline__ void solve_one(const BatchArgs &A, int prob, float *s
             // pair (f^l, g~) has exact columns: err = sum_i a_i |expm1((f_i - T(f)_i)/eps)|.
             const bool check_a = (l + 1) % A.check_every == 0 || l + 1 == A.max_iter;
             const int cn = a_cnt < am ? a_cnt + 1 : am;   // slots after this push
+            onchip_pass<D, R, NT, EMU>(xq, Np, i0, i1, yq, wy, Mp, tk, mxs, seeded, [&](int i, float Mv, float Sv) {
+                const float fsk = cx[i] - epsln2 * (Mv + log2f(Sv));
+                bad |= !isfinite(fsk);
+                Fh[(size_t)a_head * n + i] = fsk;   // (the residual and the dots after the pass:
+            });                                     //  no extra registers live in it)
             double dv[kAndMax], e_row = 0.0;
 #pragma unroll
             for (int u = 0; u < kAndMax; ++u) dv[u] = 0.0;
-            onchip_pass<D, R, NT, EMU>(xq, Np, i0, i1, yq, wy, Mp, tk, mxs, seeded, [&](int i, float Mv, float Sv) {
-                const float fsk = cx[i] - epsln2 * (Mv + log2f(Sv));
+            for (int i = i0 + threadIdx.x; i < i1; i += NT) {   // (the points this thread wrote)
+                const float fsk = Fh[(size_t)a_head * n + i];
                 const float r = fsk - fold[i];
-                bad |= !isfinite(fsk);
                 if (check_a) e_row += (a ? (double)a[i] : 1.0 / n) * fabs((double)expm1f(-r / eps));
-                Fh[(size_t)a_head * n + i] = fsk;
 #pragma unroll
                 for (int u = 0; u < kAndMax; ++u)
                     if (u < cn) dv[u] += (double)r * (double)(u == a_head ? r : Rh[(size_t)u * n + i]);
                 Rh[(size_t)a_head * n + i] = r;
-            });
+            }
             double vv[kAndMax + 2];   // slots 0..7: the dots (0 beyond cn), 8: the error, 9: the flag
 #pragma unroll
             for (int u = 0; u < kAndMax; ++u) vv[u] = dv[u];
