@@ -2,15 +2,17 @@
 """Benchmark of the hot path (BASELINE.json metric: Sinkhorn cost-entries/s — n*m per
 iteration — and time-to-tol per init, with the roofline fraction of the dominant kernel).
 
-Default workload (N=1): BASELINE.json configs[1] (C2) — B=1024 independent 1D problems,
-n=m=1024, eps=1e-3, tol=1e-3.  One step = the paper's method on the whole batch: the
-sorted closed-form dual initializer (Sec. 3.1) followed by the on-chip batched Sinkhorn
-solve to tolerance.  value = sum_b n*m*L_b / step time.  With N>1 (torchrun) every rank
-solves its own batch of 1024 problems (weak scaling, no data-path collective).
+Default workload: BASELINE.json configs[3] (C4), the largest configuration and the one its
+">= 6x at 8 GPUs" target names — n = m = 262144 RGB-pixel-shaped points in [0,1]^3, eps = 1e-2,
+tol = 1e-3, online cost.  One step = the paper's method on the whole problem: the subsample
+initializer (Sec. 3.4: 4096 points per side, inner solve to tol/10, Eq. (8) extrapolation)
+followed by the Sinkhorn solve to tolerance.  value = n*m*L / step time.  With N > 1
+(torchrun) the rows of x are sharded over the ranks (sinkhorn_solve_sharded: per-rank block
+partials of the column pass exchanged with ncclAllGather every sweep; strong scaling, the total
+problem is fixed; the initializer is replicated).
 
-Other workloads (parity configs, also measurable): --workload c1 | c3 | c4 | c5.
-  c4 is row-sharded over N GPUs (NCCL allgather of column partials every sweep; strong
-  scaling: the total problem is fixed).
+Other workloads (also measurable): --workload c1 | c2 | c3 | c5.  C2 (1024 independent 1D
+problems per rank) scales weakly with no data-path collective.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload ...]
 """
@@ -99,6 +101,14 @@ class Workload:
         raise NotImplementedError
 
 
+def c2_config(world):
+    return {"workload": "BJ.cfg2 (C2): batched 1D sorting/ranking, B=1024 per GPU x n=m=1024, d=1, "
+                        "x~U[0,1), y_j=j/(m-1), eps=1e-3, tol=1e-3 (L1 marginal), max_iter=10000",
+            "init": "sort1d (closed-form eps=0 dual, Sec. 3.1)", "global_batch": 1024 * world,
+            "parallelism": f"dp{world} (independent problems per rank)",
+            "l2": "flushed (256 MiB write) before every timed step"}
+
+
 class C2(Workload):
     name = "c2"
 
@@ -114,11 +124,7 @@ class C2(Workload):
         self.yh = torch.from_numpy(p.y).pin_memory()
 
     def config(self):
-        return {"workload": "BJ.cfg2 (C2): batched 1D sorting/ranking, B=1024 per GPU x n=m=1024, d=1, "
-                            "x~U[0,1), y_j=j/(m-1), eps=1e-3, tol=1e-3 (L1 marginal), max_iter=10000",
-                "init": "sort1d (closed-form eps=0 dual, Sec. 3.1)", "global_batch": 1024 * self.world,
-                "parallelism": f"dp{self.world} (independent problems per rank)",
-                "l2": "flushed (256 MiB write) before every timed step"}
+        return c2_config(self.world)
 
     def _run(self, x, y, init=True, anderson=0):
         sk, p = self.sk, self.p
@@ -200,33 +206,63 @@ class C2(Workload):
         return e, t, O.num_threads(), f"{nprob} of the 1024 C2 problems (sort1d init + fp64 solve to tol)"
 
 
+def single_spec(args):
+    """The problem, initializer, cost mode and dominant kernel of one single-problem workload
+    (C1, C3, C4, C5) — shared by both arms so that their config dicts are identical."""
+    from workloads import gen
+    name = args.workload
+    sp = {"name": name, "scaling": "weak", "fma_exp_share": 0.25}
+    if name == "c1":
+        sp.update(p=gen.c1(), init="gaussian", mode="auto", roof="mufu", kernel="k_batched (on-chip solver, one CTA)")
+    elif name == "c3":
+        sp.update(p=gen.c3(eps_factor=args.eps_factor or 0.01), init=args.init or "gmm", mode="stored", roof="hbm",
+                  kernel="k_stored_fused (single-read fused stored sweep, K5)")
+    elif name == "c4":
+        sp.update(p=gen.c4(), init=args.init or "subsample", mode="online", roof="mufu", scaling="strong",
+                  fma_exp_share=0.125,   # K2 seeded passes: 1 of 8 exponential pairs on the FMA pipe
+                  kernel="k_lse<3,4> (online LSE pass, K2)")
+    else:
+        sp.update(p=gen.c5(eps_factor=args.eps_factor or 1e-2), init=args.init or "gaussian", mode="online",
+                  roof="tensor", kernel="k_lse_tc2 (online LSE pass, CTA-pair tcgen05 kind::f16 3-product hi/lo "
+                                        "cross term with w and the row shift folded into the MMA, K3)")
+        if args.ffma:   # comparison leg: the FFMA kernel at d = 64
+            sp.update(roof="fp32", kernel="k_lse<64,1> (online LSE pass, FFMA2 cross term, K2)")
+    return sp
+
+
+def single_config(sp, args, world):
+    p, name = sp["p"], sp["name"]
+    sharded = name == "c4" and world > 1
+    c = {"workload": {"c1": "BJ.cfg1 (C1): n=m=256, d=2, Gaussian clouds, eps=0.01*mean(C)",
+                      "c3": f"BJ.cfg3 (C3): n=m=16384, d=16 GMM clouds, stored-cost mode (1 GiB C), eps={p.eps:.4g}",
+                      "c4": "BJ.cfg4 (C4): n=m=262144, d=3 RGB-pixel mixtures, eps=1e-2, online cost",
+                      "c5": f"BJ.cfg5 (C5): n=m=65536, d=64 embeddings, eps={p.eps:.4g}, online cost"}[name],
+         "n": p.n, "m": p.m, "d": p.d, "init": sp["init"], "tol": p.tol, "mode": sp["mode"],
+         "parallelism": f"row-sharded x{world} (NCCL allgather of block partials per sweep)" if sharded else
+                        ("1 GPU" if world == 1 else f"{world} independent replicas"),
+         "l2": "flushed (256 MiB write) before every timed step" if name in ("c1",) else
+               "inputs + cost larger than L2 / flushed before each step"}
+    if sp["init"] == "subsample":
+        c["subsample"] = {"ns": int(p.extra["idx_x"].size), "inner_tol": p.tol / 10}
+    if sp["init"] == "gmm":
+        c["gmm_fit"] = {"K": 8, "kmeans_iters": args.gmm_kmeans_iters, "em_max_iters": args.gmm_iters,
+                        "em_tol": args.gmm_tol, "start": "gen.gmm_start_idx seeds 3/4 (R-23/R-28)"}
+    if name == "c5" and args.ffma:
+        c["kernel_variant"] = "FFMA cross term (sk_set_tuning tc=0)"
+    return c
+
+
 class Single(Workload):
     """One problem (C1, C3, C4, C5); C4 is row-sharded over the ranks."""
 
     def __init__(self, sk, ctx, dev, rank, world, args):
-        from workloads import gen
         import torch
         self.sk, self.ctx, self.world, self.rank, self.args = sk, ctx, world, rank, args
-        self.name = args.workload
-        if self.name == "c1":
-            self.p = gen.c1(); self.init = "gaussian"; self.mode = "auto"; self.roof = "mufu"
-            self.kernel = "k_batched (on-chip solver, one CTA)"
-        elif self.name == "c3":
-            self.p = gen.c3(eps_factor=args.eps_factor or 0.01); self.init = args.init or "gmm"
-            self.mode = "stored"; self.roof = "hbm"
-            self.kernel = "k_stored_fused (single-read fused stored sweep, K5)"
-        elif self.name == "c4":
-            self.p = gen.c4(); self.init = args.init or "subsample"; self.mode = "online"; self.roof = "mufu"
-            self.fma_exp_share = 0.125   # K2 seeded passes: 1 of 8 exponential pairs on the FMA pipe
-            self.kernel = "k_lse<3,4> (online LSE pass, K2)"
-            self.scaling = "strong"
-        else:
-            self.p = gen.c5(eps_factor=args.eps_factor or 1e-2); self.init = args.init or "gaussian"
-            self.mode = "online"; self.roof = "tensor"
-            self.kernel = "k_lse_tc2 (online LSE pass, CTA-pair tcgen05 kind::f16 3-product hi/lo cross term " \
-                          "with w and the row shift folded into the MMA, K3)"
-            if os.environ.get("SK_TC", "1") == "0":   # comparison leg: the FFMA kernel at d = 64
-                self.roof = "fp32"; self.kernel = "k_lse<64,1> (online LSE pass, FFMA2 cross term, K2)"
+        self.spec = sp = single_spec(args)
+        self.name, self.p, self.init, self.mode, self.roof = sp["name"], sp["p"], sp["init"], sp["mode"], sp["roof"]
+        self.kernel, self.scaling, self.fma_exp_share = sp["kernel"], sp["scaling"], sp["fma_exp_share"]
+        if self.name == "c5" and args.ffma:
+            ctx.set_tuning("tc", 0)
         p = self.p
         self.n, self.m, self.d = p.n, p.m, p.d
         self.sharded = self.name == "c4" and world > 1
@@ -250,20 +286,7 @@ class Single(Workload):
             self.iy = torch.from_numpy(p.extra["idx_y"]).to(dev)
 
     def config(self):
-        p = self.p
-        c = {"workload": {"c1": "BJ.cfg1 (C1): n=m=256, d=2, Gaussian clouds, eps=0.01*mean(C)",
-                          "c3": f"BJ.cfg3 (C3): n=m=16384, d=16 GMM clouds, stored-cost mode (1 GiB C), eps={p.eps:.4g}",
-                          "c4": "BJ.cfg4 (C4): n=m=262144, d=3 RGB-pixel mixtures, eps=1e-2, online cost",
-                          "c5": f"BJ.cfg5 (C5): n=m=65536, d=64 embeddings, eps={p.eps:.4g}, online cost"}[self.name],
-             "init": self.init, "tol": p.tol, "mode": self.mode,
-             "parallelism": f"row-sharded x{self.world}" if self.sharded else "1 GPU",
-             "l2": "flushed (256 MiB write) before every timed step" if self.name in ("c1",) else
-                   "inputs + cost larger than L2 / flushed before each step"}
-        if self.init == "gmm":
-            c["gmm_fit"] = {"K": 8, "kmeans_iters": self.args.gmm_kmeans_iters, "em_max_iters": self.args.gmm_iters,
-                            "em_tol": self.args.gmm_tol,
-                            "start": "gen.gmm_start_idx seeds 3/4 (R-23/R-28)"}
-        return c
+        return single_config(self.spec, self.args, self.world)
 
     def _init(self, x, y):
         sk, p = self.sk, self.p
@@ -348,23 +371,56 @@ class Single(Workload):
         return out
 
     def cpu_sample(self, target_s=10.0):
-        """The fp64 oracle timed on a bounded sample: one f-update (row LSE pass) on sampled
-        rows, sized to take about target_s seconds."""
-        from oracle import oracle as O
-        p = self.p
-        g = np.zeros(p.m)
+        return single_cpu_sample(self.p, target_s)
 
-        def run(k):
-            rows = np.linspace(0, p.n - 1, k).astype(np.int64)
+    def cpu_extra(self, target_s=10.0):
+        """Beside the sampled sweep: the oracle's time-to-tol extrapolated from it (L of our solve
+        x the measured fp64 sweep time; the initializer likewise), and a full fp64 run (init +
+        solve to tol) of the same recipe at reduced n (full runs take hours)."""
+        from oracle import oracle as O
+        from workloads import gen
+        e, t, thr, _ = single_cpu_sample(self.p, target_s / 2)
+        rate = e / t                      # cost entries (one per sweep = 2 passes) per second
+        p, L = self.p, self.rep["iterations"]
+        out = {"kind": "oracle", "cores": thr, "sweep_entries_per_s": rate,
+               "time_to_tol_s_extrapolated": (p.n * p.m * L) / rate,
+               "extrapolation": f"L = {L} sweeps (this run's) x n m / measured fp64 sweep rate"}
+        if self.init == "subsample" and hasattr(self, "inner"):
+            ns = int(p.extra["idx_x"].size)
+            out["init_s_extrapolated"] = (ns * ns * self.inner["iterations"] + p.n * ns / 2) / rate
+        if self.name == "c4":   # full fp64 run at reduced n: subsample init + solve to tol
+            q = gen.c4(n=2048, ns=256)
             t0 = time.perf_counter()
-            O.f_update(p.x, p.y, g, p.eps, rows=rows)
-            return time.perf_counter() - t0
-        k = min(p.n, 32)
-        t = run(k)
-        k = int(min(p.n, max(k, k * target_s / max(t, 1e-4))))
-        t = run(k)
-        return float(k) * p.m / 2, t, O.num_threads(), \
-            f"oracle row pass (f-update) over {k} sampled rows x {p.m} columns; one cost entry = 2 passes"
+            f0 = O.init_subsample(q.x, q.y, q.extra["idx_x"], q.extra["idx_y"], q.eps, q.tol / 10)
+            f0 = f0[0] if isinstance(f0, tuple) else f0
+            r = O.sinkhorn(q.x, q.y, q.eps, tol=q.tol, f0=f0)
+            tt = time.perf_counter() - t0
+            out["reduced_n_full_run"] = {"n": q.n, "ns": 256, "iterations": r.iterations, "time_to_tol_s": tt,
+                                         "value": q.n * q.m * r.iterations / tt, "unit": "cost-entries/s"}
+        return out
+
+
+def single_cpu_sample(p, target_s=10.0):
+    """The fp64 oracle timed on a bounded sample of one sweep: the g-update (column pass) on
+    sampled columns and the f-update (row pass) on sampled rows, sized to take about target_s
+    seconds.  Returns (cost entries, seconds, threads, description); one cost entry = 2 passes."""
+    from oracle import oracle as O
+    g, f = np.zeros(p.m), np.zeros(p.n)
+
+    def run(k):
+        rows = np.linspace(0, p.n - 1, k).astype(np.int64)
+        cols = np.linspace(0, p.m - 1, k).astype(np.int64)
+        t0 = time.perf_counter()
+        O.g_update(p.x, p.y, f, p.eps, cols=cols)
+        O.f_update(p.x, p.y, g, p.eps, rows=rows)
+        return time.perf_counter() - t0
+    k = min(p.n, p.m, 16)
+    t = run(k)
+    k = int(min(p.n, p.m, max(k, k * target_s / max(t, 1e-4))))
+    t = run(k)
+    return float(k) * (p.m + p.n) / 2, t, O.num_threads(), \
+        f"oracle sweep sample: g-update on {k} sampled columns + f-update on {k} sampled rows " \
+        f"(of {p.n} x {p.m}); one cost entry = 2 passes"
 
 
 def make_workload(args, sk, ctx, dev, rank, world):
@@ -443,27 +499,27 @@ def run_reference(args):
     from oracle import oracle as O
     O.build()
 
-    class _Stub:
-        pass
-    w = C2.__new__(C2) if args.workload == "c2" else Single.__new__(Single)
-    if args.workload != "c2":
-        from workloads import gen
-        w.name = args.workload
-        w.p = {"c1": gen.c1, "c3": lambda: gen.c3(eps_factor=args.eps_factor or 0.01), "c4": gen.c4,
-               "c5": lambda: gen.c5(eps_factor=args.eps_factor or 1e-2)}[w.name]()
-    w.world = world
+    if args.workload == "c2":
+        w = C2.__new__(C2)
+        cfg = c2_config(world)
+        sample = lambda warm: w.cpu_sample(1 if warm else 2)   # noqa: E731
+        scaling = "weak"
+    else:
+        sp = single_spec(args)
+        cfg = single_config(sp, args, world)   # the same dict as our arm's
+        sample = lambda warm: single_cpu_sample(sp["p"], 1.0 if warm else 3.0)   # noqa: E731
+        scaling = sp["scaling"]
     for _ in range(args.warmup):
-        (w.cpu_sample(1) if args.workload == "c2" else w.cpu_sample(target_s=1.0))
+        sample(True)
     tot_e, tot_t, thr, desc = 0.0, 0.0, 1, ""
     for _ in range(args.steps):
-        e, t, thr, desc = w.cpu_sample(2) if args.workload == "c2" else w.cpu_sample(target_s=5.0)
+        e, t, thr, desc = sample(False)
         tot_e += e
         tot_t += t
     v = tot_e / tot_t
-    cfg = w.config() if args.workload == "c2" else {"workload": args.workload}
     line = {"impl": "reference", "metric": "sinkhorn_cost_entries_per_s", "value": v, "unit": "cost-entries/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": cfg,
             "cpu_baseline": {"value": v, "unit": "cost-entries/s", "cores": thr, "kind": "oracle", "sample": desc},
             "e2e": {"value": v, "unit": "cost-entries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -584,6 +640,8 @@ def run_ours(args):
                 e, t, thr, desc = w.cpu_sample()
                 line["cpu_baseline"] = {"value": e / t, "unit": "cost-entries/s", "cores": thr, "kind": "oracle",
                                         "sample": f"{desc}, {t:.1f} s"}
+                if hasattr(w, "cpu_extra"):
+                    line["cpu_baseline"].update(w.cpu_extra())
             except Exception as ex:  # pragma: no cover
                 line["cpu_baseline"] = {"value": None, "error": repr(ex)}
         print(json.dumps(line), flush=True)
@@ -600,7 +658,8 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--workload", default="c4", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--ffma", action="store_true", help="c5: the FFMA cross-term kernel (sk_set_tuning tc=0)")
     ap.add_argument("--init", default=None,
                     help="c3/c4/c5 initializer: zero|gaussian|gmm (fitted on the device)|gmm_given|subsample")
     ap.add_argument("--gmm-iters", type=int, default=100, help="max EM iterations of the device GMM fit (init gmm; "

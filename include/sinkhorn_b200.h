@@ -139,6 +139,27 @@ sk_status sk_set_eps_decay(sk_ctx *ctx, float init, float rate);
  * over the ranks: one ncclAllReduce of 9 doubles per sweep); omega != 1 and eps-decay return
  * SK_EUNSUPPORTED. */
 sk_status sk_set_anderson(sk_ctx *ctx, int32_t mem);
+/* The solver options currently set on this context (each output nullable, host): omega
+ * (sk_set_relaxation), the eps-decay (init, rate) (init 0 = off) and the Anderson memory (0 =
+ * off).  Lets a caller change an option for one solve and restore the previous setting. */
+sk_status sk_get_solver_options(const sk_ctx *ctx, float *omega, float *decay_init, float *decay_rate,
+                                int32_t *anderson);
+/* Diagnostics / tuning of kernel variants (DESIGN.md section 6 measures each): key = value for the
+ * following calls on this context.  None changes what is computed beyond fp32 rounding; each
+ * selects a kernel variant or a balance of the exponential between MUFU and the FMA pipe:
+ *   "tc" 0|1 (1): tcgen05 cross term (K3) for d in (16, 64]; 0 = FFMA kernel K2;
+ *   "fused" 0|1 (1): stored mode's fused single-read sweep K5; 0 = separate row/column passes;
+ *   "seeded" 0|1 (1): max-free (seeded) LSE passes from the third sweep;
+ *   "tc_margin" [0, 1000] (4): K3 seeded shift above the previous LSE, log2 units;
+ *   "lse_margin" [0, 1000] (4): K2 seeded shift above the previous LSE, log2 units (a margin
+ *       beyond ~100 forces every seeded point through its exact fallback / the column redo);
+ *   "lse_emu8" 0..2 (1): K2 seeded (d <= 4) exponential pairs of 8 on the FMA pipe;
+ *   "tc_emu" 0..6 (2): K3 exponential pairs of 8 on the FMA pipe;
+ *   "tc_epi" 16|162 (162): K3 epilogue organisation;
+ *   "batched_shape" 0|1 (1): K13 512 threads x 2 points (1) or 1024 x 1 (0) for 512 < P <= 1024;
+ *   "batched_cl" 0..2 (0): K13 one CTA (1) or a CTA pair (2) per problem (0: pair only for B = 1).
+ * SK_EINVAL for an unknown key or a value out of range. */
+sk_status sk_set_tuning(sk_ctx *ctx, const char *key, double value);
 /* Enable (1) / disable (0) CUDA-event timing of the dominant kernels into sk_counters. */
 sk_status sk_set_timing(sk_ctx *ctx, int32_t enable);
 sk_status sk_get_counters(const sk_ctx *ctx, sk_counters *out /* host */);
@@ -151,6 +172,11 @@ sk_status sk_reset_counters(sk_ctx *ctx);
  * run time (libnccl.so.2); SK_ENCCL if unavailable. */
 sk_status sk_nccl_unique_id(sk_ctx *ctx, void *out_128B /* host */);
 sk_status sk_comm_init(sk_ctx *ctx, const void *id_128B /* host */, int32_t rank, int32_t world);
+/* Test hook: with enable = 1 a communicator of world size 1 (sk_comm_init(ctx, id, 0, 1)) takes
+ * the NCCL branch of sinkhorn_solve_sharded (ncclAllGather of the block partials, the
+ * ncclAllReduce sites of omega != 1 and Anderson) instead of the local shortcut, so the NCCL
+ * data plane runs on a one-GPU box; results are bit-identical to world 1 without it. */
+sk_status sk_set_force_nccl(sk_ctx *ctx, int32_t enable);
 /* Row block owned by `rank` in the fixed global partition used by
  * sinkhorn_solve_sharded: rows [*row0, *row0 + *n_local) of n_total.  The
  * partition is a function of n_total only (SK_SHARD_BLOCKS blocks), which is what
@@ -262,7 +288,8 @@ sk_status sinkhorn_init_nw1d(sk_ctx *ctx, int64_t B, int64_t n, int64_t m, const
  * potential f*(x) = ||x||^2 - (x - m_mu)^T A (x - m_mu) - 2 m_nu^T x
  * (Gaussian-Potential appendix, R-4), evaluated on the smaller side
  * (n <= m: x, *side = 0; else y with roles swapped, *side = 1, R-15).
- * a, b nullable (uniform).  pot: n (side 0) or m (side 1).  d <= 64. */
+ * a, b nullable (uniform).  pot: n (side 0) or m (side 1).  d <= 64 (SK_EUNSUPPORTED for d in
+ * (64, 256], SK_EINVAL beyond). */
 sk_status sinkhorn_init_gaussian(sk_ctx *ctx, int64_t n, int64_t m, int32_t d, const float *x,
                                  const float *a, const float *y, const float *b, float ridge_rel,
                                  float *pot, int32_t *side /* host */);
@@ -275,7 +302,8 @@ sk_status sinkhorn_init_gaussian(sk_ctx *ctx, int64_t n, int64_t m, int32_t d, c
  * DESIGN.md R-29; err = the row term of (f^l, g_sk(f^l))) to inner_tol (max inner_max_iter
  * sweeps; the binding's default 1e-9: ~100 sweeps at C3) -> f~; f^(0)(x) = sum_k f~_k p_k(x),
  * p_k the posterior responsibilities (Eq. 7), on the smaller side (*side as above).
- * Mixture parameters are inputs (sinkhorn_fit_gmm fits them).  d <= 64, K <= 64. */
+ * Mixture parameters are inputs (sinkhorn_fit_gmm fits them).  K <= 64; d <= 64
+ * (SK_EUNSUPPORTED for d in (64, 256], SK_EINVAL beyond). */
 sk_status sinkhorn_init_gmm(sk_ctx *ctx, int64_t n, int64_t m, int32_t d, const float *x,
                             const float *y, int32_t Kx, const float *wx, const float *mux,
                             const float *covx, int32_t Ky, const float *wy, const float *muy,
@@ -304,11 +332,15 @@ sk_status sinkhorn_init_subsample(sk_ctx *ctx, int64_t n, int64_t m, int32_t d, 
  *     With f_init (or neither) each sweep is g-update then f-update (R-2).  With
  *     g_init the transposed problem is solved (x<->y, a<->b, f<->g).
  *   f: B x n, g: B x m outputs;  rep: B host reports.
- * Kernels: problems with n, m <= 4096 and d <= 4 run the on-chip solver (one CTA
- * per problem, whole iteration loop on chip, per-problem convergence); larger
- * problems run the multi-kernel online LSE path (cost recomputed per pass; FFMA
- * cross term) or, with SK_COST_STORED, the stored-cost sweep.  Blocks until the
- * reports are filled.  d <= 256. */
+ * Kernels: problems with d <= 4 that fit one CTA's shared memory (n, m up to ~4096) run the
+ * on-chip solver K13 (one CTA or CTA pair per problem, the whole iteration loop on chip,
+ * per-problem convergence); larger problems run the multi-kernel path: online LSE passes with
+ * the cost recomputed per pass (FFMA cross term K2 for d <= 16; the tcgen05 cross term K3 for
+ * d in (16, 64], K2 when the scaled coordinates leave the fp16 range) or, with SK_COST_STORED
+ * (or AUTO for 8 <= d < 32 when 4nm bytes fit), the stored-cost sweep (K4 build, K5 fused
+ * single-read sweep).  Blocks until the reports are filled.
+ * SK_EINVAL for d < 1 or d > 256 (and the conventions above); SK_EUNSUPPORTED for d in
+ * (64, 256] (no kernel of this build) and for n, m >= 2^31. */
 sk_status sinkhorn_solve(sk_ctx *ctx, int64_t B, int64_t n, int64_t m, int32_t d, const float *x,
                          const float *y, int32_t y_shared, const float *a, const float *b, float eps,
                          float tol, int32_t max_iter, int32_t check_every, sk_cost_mode mode,
@@ -319,9 +351,14 @@ sk_status sinkhorn_solve(sk_ctx *ctx, int64_t B, int64_t n, int64_t m, int32_t d
  * design): this rank owns rows [row0, row0 + n_local) as given by sk_shard_rows.
  * x_local, a_local (nullable), f_init_local (nullable), f_local: this rank's
  * rows; y, b (nullable), g: replicated (m).  Every sweep: local row pass (f),
- * local column partials (max, sum-exp) per fixed row block, ncclAllGather of the
- * partials, identical rank-order merge on every rank (g, error, stop flag).
- * Requires sk_comm_init (world 1 works without it).  Blocks. */
+ * local column partials (max, sum-exp), merged per fixed row block on the rank (8 B per column
+ * per block), ncclAllGather of the block partials (SK_SHARD_BLOCKS / world blocks per rank),
+ * identical block-order merge on every rank (g, error, stop flag).  From the third sweep the
+ * column pass is seeded (max-free); if any column's seeded sum leaves [2^-100, 2^100] the
+ * merge flags it and the column pass is redone exactly (one more allgather, enqueued every
+ * sweep, a no-op otherwise).  The unsharded solver runs the same merge tree, so the results are
+ * bit-identical to sinkhorn_solve's for plain Sinkhorn (omega = 1, no Anderson, online cost).
+ * Requires sk_comm_init (world 1 works without it).  d as sinkhorn_solve.  Blocks. */
 sk_status sinkhorn_solve_sharded(sk_ctx *ctx, int64_t n_total, int64_t row0, int64_t n_local,
                                  int64_t m, int32_t d, const float *x_local, const float *y,
                                  const float *a_local, const float *b, float eps, float tol,

@@ -10,6 +10,7 @@ any step of the method.
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes
 from typing import List, Optional, Tuple
 
@@ -80,6 +81,20 @@ class Context:
         self.check(self.lib.sk_microbench(self.h, k, ctypes.byref(v)))
         return v.value
 
+    def set_tuning(self, key: str, value: float) -> None:
+        """Diagnostic kernel-variant knobs (sk_set_tuning; keys in include/sinkhorn_b200.h)."""
+        self.check(self.lib.sk_set_tuning(self.h, key.encode(), float(value)))
+
+    def set_force_nccl(self, on: bool) -> None:
+        """Test hook: a 1-rank communicator takes the NCCL branch of the sharded solver."""
+        self.check(self.lib.sk_set_force_nccl(self.h, int(on)))
+
+    def solver_options(self) -> dict:
+        om, di, dr, am = ctypes.c_float(), ctypes.c_float(), ctypes.c_float(), ctypes.c_int32()
+        self.check(self.lib.sk_get_solver_options(self.h, ctypes.byref(om), ctypes.byref(di), ctypes.byref(dr),
+                                                  ctypes.byref(am)))
+        return {"omega": om.value, "eps_decay": (di.value, dr.value), "anderson": am.value}
+
     def nccl_unique_id(self) -> bytes:
         buf = ctypes.create_string_buffer(128)
         self.check(self.lib.sk_nccl_unique_id(self.h, buf))
@@ -102,6 +117,27 @@ class Context:
 
 
 # ------------------------------------------------------------------ marshalling
+@contextlib.contextmanager
+def _solver_options(ctx: Context, omega=None, eps_decay=None, anderson=None):
+    """Set the given solver options on the context for one call, then restore the previous
+    settings (None leaves an option as the context has it)."""
+    if omega is None and eps_decay is None and anderson is None:
+        yield
+        return
+    prev = ctx.solver_options()
+    try:
+        if omega is not None:
+            ctx.check(ctx.lib.sk_set_relaxation(ctx.h, ctypes.c_float(omega)))
+        if eps_decay is not None:
+            ctx.check(ctx.lib.sk_set_eps_decay(ctx.h, ctypes.c_float(eps_decay[0]), ctypes.c_float(eps_decay[1])))
+        if anderson is not None:
+            ctx.check(ctx.lib.sk_set_anderson(ctx.h, int(anderson)))
+        yield
+    finally:
+        ctx.lib.sk_set_relaxation(ctx.h, ctypes.c_float(prev["omega"]))
+        ctx.lib.sk_set_eps_decay(ctx.h, ctypes.c_float(prev["eps_decay"][0]), ctypes.c_float(prev["eps_decay"][1]))
+        ctx.lib.sk_set_anderson(ctx.h, int(prev["anderson"]))
+
 def _ptr(t: Optional[torch.Tensor], dtype=torch.float32):
     if t is None:
         return None
@@ -198,33 +234,21 @@ def sinkhorn_init_subsample(ctx: Context, x, y, idx_x, idx_y, eps: float, inner_
 def sinkhorn_solve(ctx: Context, x, y, eps: float, tol: float = 1e-3, max_iter: int = 10000,
                    check_every: int = 1, a=None, b=None, y_shared: bool = False, mode: str = "auto",
                    f_init=None, g_init=None, f=None, g=None, allow_nonfinite: bool = False,
-                   omega: float = 1.0, eps_decay=None, anderson: int = 0):
+                   omega: Optional[float] = None, eps_decay=None, anderson: Optional[int] = None):
     """Solve B >= 1 problems.  x: (n, d) or (B, n, d); y: (m, d) [shared] or (B, m, d).
     omega: Alg. 1's relaxation (sk_set_relaxation; 1 = plain Sinkhorn).
-    eps_decay: (init, rate) for sk_set_eps_decay (e.g. (5, 0.8), P:491), None = off.
+    eps_decay: (init, rate) for sk_set_eps_decay (e.g. (5, 0.8), P:491; (0, 1) = off).
     anderson: Anderson memory for sk_set_anderson (e.g. 5), 0 = off.
+    Each option given applies to this call only (the context's previous setting is restored);
+    None uses the context's setting (default: plain Sinkhorn).
     Returns (f, g, reports) with f (B, n) / g (B, m) (B dropped for a single problem)."""
-    if anderson:
-        ctx.check(ctx.lib.sk_set_anderson(ctx.h, int(anderson)))
-        try:
-            return sinkhorn_solve(ctx, x, y, eps, tol, max_iter, check_every, a, b, y_shared, mode,
-                                  f_init, g_init, f, g, allow_nonfinite, omega, eps_decay)
-        finally:
-            ctx.lib.sk_set_anderson(ctx.h, 0)
-    if eps_decay is not None:
-        ctx.check(ctx.lib.sk_set_eps_decay(ctx.h, ctypes.c_float(eps_decay[0]), ctypes.c_float(eps_decay[1])))
-        try:
-            return sinkhorn_solve(ctx, x, y, eps, tol, max_iter, check_every, a, b, y_shared, mode,
-                                  f_init, g_init, f, g, allow_nonfinite, omega)
-        finally:
-            ctx.lib.sk_set_eps_decay(ctx.h, ctypes.c_float(0.0), ctypes.c_float(1.0))
-    if omega != 1.0:
-        ctx.check(ctx.lib.sk_set_relaxation(ctx.h, ctypes.c_float(omega)))
-        try:
-            return sinkhorn_solve(ctx, x, y, eps, tol, max_iter, check_every, a, b, y_shared, mode,
-                                  f_init, g_init, f, g, allow_nonfinite)
-        finally:
-            ctx.lib.sk_set_relaxation(ctx.h, ctypes.c_float(1.0))
+    with _solver_options(ctx, omega, eps_decay, anderson):
+        return _solve(ctx, x, y, eps, tol, max_iter, check_every, a, b, y_shared, mode, f_init, g_init, f, g,
+                      allow_nonfinite)
+
+
+def _solve(ctx, x, y, eps, tol, max_iter, check_every, a, b, y_shared, mode, f_init, g_init, f, g,
+           allow_nonfinite):
     single = x.dim() == 2
     xb = x.unsqueeze(0) if single else x
     B, n, d = xb.shape
@@ -313,32 +337,15 @@ def sinkhorn_soft_rank_sort(ctx: Context, x, y, eps: float, f, g, z=None,
 
 def sinkhorn_solve_sharded_emulated(ctx: Context, world: int, x, y, eps: float, tol: float = 1e-3,
                                     max_iter: int = 10000, check_every: int = 1, a=None, b=None,
-                                    mode: str = "auto", f_init=None, anderson: int = 0, omega: float = 1.0,
-                                    eps_decay=None):
+                                    mode: str = "auto", f_init=None, anderson: Optional[int] = None,
+                                    omega: Optional[float] = None, eps_decay=None):
     """The row-sharded algorithm for `world` virtual ranks on one GPU (test entry).
-    anderson: Anderson memory (sk_set_anderson), 0 = off; omega: relaxation (sk_set_relaxation);
-    eps_decay: (init, rate) for sk_set_eps_decay, None = off."""
-    if eps_decay is not None:
-        ctx.check(ctx.lib.sk_set_eps_decay(ctx.h, ctypes.c_float(eps_decay[0]), ctypes.c_float(eps_decay[1])))
-        try:
-            return sinkhorn_solve_sharded_emulated(ctx, world, x, y, eps, tol, max_iter, check_every, a, b, mode,
-                                                   f_init, anderson, omega)
-        finally:
-            ctx.lib.sk_set_eps_decay(ctx.h, ctypes.c_float(0.0), ctypes.c_float(1.0))
-    if omega != 1.0:
-        ctx.check(ctx.lib.sk_set_relaxation(ctx.h, ctypes.c_float(omega)))
-        try:
-            return sinkhorn_solve_sharded_emulated(ctx, world, x, y, eps, tol, max_iter, check_every, a, b, mode,
-                                                   f_init, anderson)
-        finally:
-            ctx.lib.sk_set_relaxation(ctx.h, ctypes.c_float(1.0))
-    if anderson:
-        ctx.check(ctx.lib.sk_set_anderson(ctx.h, int(anderson)))
-        try:
-            return sinkhorn_solve_sharded_emulated(ctx, world, x, y, eps, tol, max_iter, check_every, a, b, mode,
-                                                   f_init)
-        finally:
-            ctx.lib.sk_set_anderson(ctx.h, 0)
+    anderson / omega / eps_decay: as sinkhorn_solve (this call only; None = the context's)."""
+    with _solver_options(ctx, omega, eps_decay, anderson):
+        return _solve_sharded_emulated(ctx, world, x, y, eps, tol, max_iter, check_every, a, b, mode, f_init)
+
+
+def _solve_sharded_emulated(ctx, world, x, y, eps, tol, max_iter, check_every, a, b, mode, f_init):
     n, d = x.shape
     m = y.shape[0]
     f = _empty((n,), x)
@@ -352,25 +359,18 @@ def sinkhorn_solve_sharded_emulated(ctx: Context, world: int, x, y, eps: float, 
 
 def sinkhorn_solve_sharded(ctx: Context, n_total: int, row0: int, x_local, y, eps: float,
                            tol: float = 1e-3, max_iter: int = 10000, check_every: int = 1,
-                           a_local=None, b=None, mode: str = "auto", f_init_local=None, anderson: int = 0,
-                           omega: float = 1.0):
+                           a_local=None, b=None, mode: str = "auto", f_init_local=None,
+                           anderson: Optional[int] = None, omega: Optional[float] = None, eps_decay=None):
     """Rows [row0, row0 + n_local) of an n_total-row problem on this rank (sk_comm_init first);
     anderson: Anderson memory (sk_set_anderson; one 9-double allreduce per sweep), 0 = off;
-    omega: relaxation (sk_set_relaxation; one 2-double allreduce of the row terms per sweep)."""
-    if omega != 1.0:
-        ctx.check(ctx.lib.sk_set_relaxation(ctx.h, ctypes.c_float(omega)))
-        try:
-            return sinkhorn_solve_sharded(ctx, n_total, row0, x_local, y, eps, tol, max_iter, check_every,
-                                          a_local, b, mode, f_init_local, anderson)
-        finally:
-            ctx.lib.sk_set_relaxation(ctx.h, ctypes.c_float(1.0))
-    if anderson:
-        ctx.check(ctx.lib.sk_set_anderson(ctx.h, int(anderson)))
-        try:
-            return sinkhorn_solve_sharded(ctx, n_total, row0, x_local, y, eps, tol, max_iter, check_every,
-                                          a_local, b, mode, f_init_local)
-        finally:
-            ctx.lib.sk_set_anderson(ctx.h, 0)
+    omega: relaxation (sk_set_relaxation; one 2-double allreduce of the row terms per sweep);
+    eps_decay: (init, rate).  Each applies to this call only (None = the context's setting)."""
+    with _solver_options(ctx, omega, eps_decay, anderson):
+        return _solve_sharded(ctx, n_total, row0, x_local, y, eps, tol, max_iter, check_every, a_local, b, mode,
+                              f_init_local)
+
+
+def _solve_sharded(ctx, n_total, row0, x_local, y, eps, tol, max_iter, check_every, a_local, b, mode, f_init_local):
     n_local, d = x_local.shape
     m = y.shape[0]
     f = _empty((n_local,), x_local)

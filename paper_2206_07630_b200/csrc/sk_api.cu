@@ -76,6 +76,20 @@ struct sk_ctx {
     float omega = 1.f;              // Alg. 1's relaxation for the following solves
     float decay_init = 0.f, decay_rate = 1.f;   // eps-decay for the following solves (R-25)
     int anderson = 0;               // Anderson memory for the following solves (R-27; 0: off)
+    int force_nccl = 0;             // sk_set_force_nccl: a 1-rank communicator takes the NCCL path
+    // diagnostics / tuning (sk_set_tuning): kernel variants and balances measured in DESIGN.md
+    struct Tuning {
+        int tc = 1;             // tensor-core cross term for d in (16, 64] (0: FFMA kernel K2)
+        int fused = 1;          // stored mode: the fused single-read sweep K5
+        int seeded = 1;         // max-free (seeded) passes from the third sweep
+        float tc_margin = 4.f;  // K3 seeded shift above the previous LSE (log2 units)
+        float lse_margin = 4.f; // K2 seeded shift above the previous LSE (log2 units)
+        int lse_emu8 = 1;       // K2 seeded D <= 4: exponential pairs of 8 on the FMA pipe
+        int tc_emu = 2;         // K3: exponential pairs of 8 on the FMA pipe
+        int tc_epi = 162;       // K3 epilogue organisation (162 or 16)
+        int batched_shape = 1;  // K13: 512 x 2 points for 512 < P <= 1024 (0: 1024 x 1)
+        int batched_cl = 0;     // K13: 0 auto, 1 one CTA, 2 a CTA pair per problem
+    } tune;
 };
 
 namespace {
@@ -83,7 +97,7 @@ enum BufId {
     B_STAGE0 = 0, B_STAGE_END = 16,   // staging of host arrays
     B_FLAG = 16, B_XPACK, B_XC, B_XNK, B_XPOT, B_YPACK, B_YC, B_YNK, B_YPOT, B_PART, B_BLKE, B_BLKB,
     B_STATUS, B_COST, B_REP, B_SORT, B_PERM, B_YSORT, B_GAUSS, B_GAUSS2, B_GMM, B_SUBW, B_SUBZ,
-    B_SUBF, B_SUBG, B_IDX, B_OUT, B_FA, B_QUEUE, B_XIMG, B_YIMG, B_XLSE, B_YLSE, B_TCMAX, B_EMST, B_EMPART, B_EMIDX, B_VJP, B_ANDFR, B_ANDBLK, B_ANDVEC, B_ANDST, B_NBUF
+    B_SUBF, B_SUBG, B_IDX, B_OUT, B_FA, B_QUEUE, B_XIMG, B_YIMG, B_XLSE, B_YLSE, B_TCMAX, B_EMST, B_EMPART, B_EMIDX, B_VJP, B_ANDFR, B_ANDBLK, B_ANDVEC, B_ANDST, B_XCHG, B_NBUF
 };
 
 sk_status fail(sk_ctx *c, sk_status s, const char *fmt, ...) {
@@ -248,7 +262,7 @@ struct Problem {
     sk_cost_mode mode;
     float *g;               // device output (m)
     int world;              // ranks of the partition (1 = unsharded)
-    bool nccl;              // partials exchanged with ncclAllGather (one local slice)
+    bool nccl;              // partials exchanged with ncclAllGather (one local slice; world >= 1)
     bool partitioned = false;  // sharded entries: results must not depend on the world size
     float omega = 1.f;         // Alg. 1's relaxation (sk_set_relaxation)
 };
@@ -305,7 +319,10 @@ struct LaunchTimer {
 sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, sk_report *rep) {
     cudaStream_t st = ctx->stream;
     LaunchTimer tm(ctx);
-    const bool sharded = P.world > 1;
+    // sharded: the rank partition of the rows (SK_SHARD_BLOCKS / world blocks per rank); a 1-rank
+    // communicator (sk_set_force_nccl) takes the same path with its 8 blocks
+    const bool sharded = P.world > 1 || P.nccl;
+    const auto &T = ctx->tune;
     // Anderson (R-27, K19): omega = 1; the stored path runs the separate row/column passes; rows
     // may be sharded (the Gram dots and the error are summed over the slices / ranks)
     const int amem = ctx->anderson >= 2 ? ctx->anderson : 0;
@@ -320,9 +337,8 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
     if (P.mode == SK_COST_AUTO) stored = stored_ok && P.d >= 8 && P.d < 32 && 4.0 * n_sum * m <= 8.0e9;
     if (stored && !stored_ok) return fail(ctx, SK_EUNSUPPORTED, "stored-cost mode needs m %% 4 == 0");
     // tensor-core cross term for d in (16, 64] (BJ.ns "only when d >= 32"; d in (16, 32] pads to
-    // K = 32); SK_TC=0 forces the FFMA kernel (tuning / comparison knob)
-    static const int tc_env = [] { const char *e = getenv("SK_TC"); return e ? atoi(e) : 1; }();
-    bool tc = !stored && P.d > 16 && P.d <= 64 && tc_env != 0;
+    // K = 32); sk_set_tuning("tc", 0) forces the FFMA kernel (comparison knob)
+    bool tc = !stored && P.d > 16 && P.d <= 64 && T.tc != 0;
     unsigned *amax = nullptr;
     if (tc) {
         // per-side max |coordinate| (global over the ranks) -> the fold scales; a problem whose
@@ -389,8 +405,7 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
     Side Y{(int)m, P.d, D, tq, ypack, yc, ynk, {ypot, ypot + m}};
     // online FFMA path: per-point LSE seeds for the max-free (seeded) passes from sweep 3 on
     // stored mode with the fused sweep (one persistent CTA per SM): 8 blocks x split_q = one wave
-    static const int fused_env = [] { const char *e = getenv("SK_FUSED"); return e ? atoi(e) : 1; }();
-    const bool fused = stored && fused_env != 0 && stored_fused_supported(m) && P.omega == 1.f && !amem;
+    const bool fused = stored && T.fused != 0 && stored_fused_supported(m) && P.omega == 1.f && !amem;
     const bool seedable = !stored;
     if (tc) {   // the seeded passes' exact fallback reads the caller's coordinates
         for (int i = 0; i < ns; ++i) { X[i].raw = slices[i].x; X[i].tcimg = (unsigned char *)ximg + offi[i]; X[i].tc_c = tc_fold_c(); }
@@ -404,10 +419,13 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
         for (int i = 0; i < ns; ++i) X[i].lse = xlse + off[i];
         Y.lse = ylse;
     }
-    static const int seed_env = [] { const char *e = getenv("SK_SEEDED"); return e ? atoi(e) : 1; }();
-    // the column pass's exact fallback needs all rows: seeded only in the unsharded entry
-    const bool col_seed = seedable && seed_env && !P.partitioned && !sharded && ns == 1;
-    const bool row_seed = seedable && seed_env;
+    // seeded passes from the third sweep.  Rows: a point whose seeded sum leaves the safe range is
+    // recomputed exactly in the merge (the reduced side, all columns, is on every rank).  Columns:
+    // the exact fallback would need every rank's rows, so a failing column makes the merge set
+    // st->colfail and the whole column pass is redone exactly (gated on the flag) - the same path
+    // for every entry, so the unsharded, emulated and sharded solves are bit-identical.
+    const bool col_seed = seedable && T.seeded;
+    const bool row_seed = seedable && T.seeded;
 
     // column-pass partition (a function of n_total, m, d only): SK_SHARD_BLOCKS fixed row
     // blocks, each cut into split_q sub-splits sized for the 8-rank launch; empty blocks
@@ -427,12 +445,23 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
     int split_row = 1;
     if (!stored) {
         // from n_total, not the local slice: the row-pass split (and so the summation order of
-        // every row's LSE) is the same for every partition of the rows
-        const long long ptiles_row = (n_glob + pcta - 1) / pcta;
+        // every row's LSE) is the same for every partition of the rows; sized for the 8-rank
+        // launch (one block of rows per GPU), so that every rank's launch fills the GPU - fewer
+        // ranks run the same split structure in more waves
+        const long long ptiles_row = (bs_rows + pcta - 1) / pcta;
         split_row = choose_split(ptiles_row, yt, occ, 64);
     }
     const long long part_elems = std::max((long long)nsplit_col * m, (long long)split_row * n_max);
     ENSURE(part, float2, B_PART, part_elems);
+    // online passes: the column partials are pre-merged per fixed row block (K6a) into the
+    // exchange buffer [nblk_x][m] - the allgather payload (8 B per column per block) - and the
+    // blocks merged in block order: the same merge tree for every partition of the rows
+    const int nblk_x = sharded ? SK_SHARD_BLOCKS : nblk_glob;
+    float2 *xchg = nullptr;
+    if (!stored) {
+        ENSURE(xc2, float2, B_XCHG, (long long)nblk_x * m);
+        xchg = xc2;
+    }
     ENSURE(blke, double, B_BLKE, 2 * kMergeMaxBlocks);
     ENSURE(blkb, int, B_BLKB, 2048);
 
@@ -445,7 +474,7 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
         CU(launch_pack_tc_ext(m, Y.pack, Y.tcimg, st));
         ctx->cnt.kernel_launches += ns + 1;
     }
-    static const float tc_margin = [] { const char *e = getenv("SK_TC_SEED_MARGIN"); return e ? (float)atof(e) : 4.f; }();
+    const float tc_margin = T.tc_margin;
     CU(launch_status_init(status, P.max_iter, P.check_every, P.tol, st, amem ? 1 : 0));
     ctx->cnt.kernel_launches += ns + 2;
     float *andfr = nullptr;     // per slice i: F at 2 mem off[i], R at F + mem n_i
@@ -487,37 +516,47 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
 
     const long long slot = (long long)blk_per_rank * split_q * m;   // one rank's partial slots
     auto col_part = [&](int i) { return part + (sharded ? (long long)slices[i].rank * slot : 0); };
-    MergePass mcol{MERGE_COL, &Y, part, nsplit_col, P.eps, P.b, status, blke, blkb, nullptr, 0.f,
-                   sharded ? 1 : 0, 0};
+    MergePass mcol{MERGE_COL, &Y, stored ? part : xchg, stored ? nsplit_col : nblk_x, P.eps, P.b, status, blke,
+                   blkb, nullptr, 0.f, sharded ? 1 : 0, 0};
     mcol.omega = P.omega;
     mcol.anderson = amem ? 1 : 0;
-    if (col_seed) mcol.Q = &X[0];
     int sweep = 0;   // sweeps enqueued so far (seeded passes from the third on)
 
     // stored mode: one HBM read of C per sweep (fused row + column passes, H4s) when m fits
     bool first = true;
 
-    auto col_stage = [&](const int *only_if) -> sk_status {
+    // column pass of every slice (+ its per-block premerge into the exchange buffer); seeded:
+    // max-free (shift = previous LSE + margin); only_if: the gated exact redo (not timed)
+    auto col_stage = [&](const int *only_if, bool seeded) -> sk_status {
+        const int nb = sharded ? blk_per_rank : nblk_glob;
         for (int i = 0; i < ns; ++i) {
             const double ent = (double)slices[i].n * m;
-            const int t0 = fused ? -1 : tm.start();   // fused: the dominant kernel is the sweep
+            const int t0 = (fused || only_if) ? -1 : tm.start();   // fused: the dominant kernel is the sweep
             if (stored) {
-                StoredPass scol{C[i], slices[i].n, m, P.eps, X[i].pack, col_part(i), bs_rows,
-                                sharded ? blk_per_rank : nblk_glob, split_q, &status->stop, only_if};
+                StoredPass scol{C[i], slices[i].n, m, P.eps, X[i].pack, col_part(i), bs_rows, nb, split_q,
+                                &status->stop, only_if};
                 CU(launch_stored_cols(scol, st));
             } else if (tc) {
-                TcPass colp{yimg, ximg + offi[i], (int)m, slices[i].n, ksteps,
-                            sharded ? blk_per_rank : nblk_glob, (int)(bs_rows / tq), split_q, col_part(i),
-                            P.eps, &status->stop};
-                colp.seeded = col_seed && sweep >= 2;
+                TcPass colp{yimg, ximg + offi[i], (int)m, slices[i].n, ksteps, nb, (int)(bs_rows / tq), split_q,
+                            col_part(i), P.eps, &status->stop};
+                colp.seeded = seeded;
+                colp.only_if = only_if;
+                colp.emu = T.tc_emu;
+                colp.epi = T.tc_epi;
                 CU(launch_lse_tc(colp, st));
             } else {
-                LsePass colp{&Y, &X[i], sharded ? blk_per_rank : nblk_glob, (int)(bs_rows / tq), split_q,
-                             col_part(i), P.eps, &status->stop};
-                colp.seeded = col_seed && sweep >= 2;
+                LsePass colp{&Y, &X[i], nb, (int)(bs_rows / tq), split_q, col_part(i), P.eps, &status->stop};
+                colp.seeded = seeded;
+                colp.only_if = only_if;
+                colp.emu8 = T.lse_emu8;
+                colp.margin = T.lse_margin;
                 CU(launch_lse(colp, st));
             }
-            tm.stop(t0, sweep, LaunchTimer::COL, ent, stored ? 4.0 * ent : 0.0);
+            if (t0 >= 0) tm.stop(t0, sweep, LaunchTimer::COL, ent, stored ? 4.0 * ent : 0.0);
+            if (!stored) {
+                const long long xoff = sharded ? (long long)slices[i].rank * blk_per_rank * m : 0;
+                CU(launch_premerge(col_part(i), nb, split_q, m, xchg + xoff, &status->stop, only_if, st));
+            }
         }
         return SK_OK;
     };
@@ -526,11 +565,18 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
     MergePass mcol_scaled = mcol, mcol_redo = mcol;
     mcol_scaled.scaled = 1;
     mcol_redo.only_if = &status->colfail;
+    MergePass mcol_seeded = mcol;   // after a seeded online column pass: out-of-range sums -> redo
+    mcol_seeded.range_redo = 1;
     const bool colredo = sharded;   // unsharded: the scaled merge recomputes a failing column itself
     if (!colredo && fused) { mcol_scaled.Cst = C[0]; mcol_scaled.xw = X[0].pack; mcol_scaled.n_rows = slices[0].n; }
     auto exchange_and_merge_col = [&](const MergePass &mp0) -> sk_status {
         if (P.nccl && sharded) {
-            int r = g_nccl.allgather(col_part(0), part, (size_t)slot * 2, kNcclFloat32, ctx->comm, st);
+            // stored: the split partials; online: this rank's pre-merged block partials
+            const size_t cnt = stored ? (size_t)slot * 2 : (size_t)blk_per_rank * m * 2;
+            const void *src = stored ? (const void *)col_part(0)
+                                     : (const void *)(xchg + (long long)slices[0].rank * blk_per_rank * m);
+            void *dst = stored ? (void *)part : (void *)xchg;
+            int r = g_nccl.allgather(src, dst, cnt, kNcclFloat32, ctx->comm, st);
             if (r != 0) return fail(ctx, SK_ENCCL, "ncclAllGather failed: %s", g_nccl.errstr ? g_nccl.errstr(r) : "?");
         }
         MergePass mp = mp0;
@@ -548,7 +594,7 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
         for (int c = 0; c < chunk; ++c, ++it) {
             if (fused) {
                 if (first) {  // g^1 from f^0 with a plain column pass
-                    CK(col_stage(nullptr));
+                    CK(col_stage(nullptr, false));
                     CK(exchange_and_merge_col(mcol));
                     launched += ns + 1;
                     first = false;
@@ -565,16 +611,22 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
                 CK(exchange_and_merge_col(mcol_scaled));
                 launched += 1;
                 if (colredo) {
-                    CK(col_stage(&status->colfail));       // no-ops unless colfail
+                    CK(col_stage(&status->colfail, false));   // no-ops unless colfail
                     CK(exchange_and_merge_col(mcol_redo));
                     launched += 1 + ns;
                 }
                 ++sweep;
                 continue;
             }
-            CK(col_stage(nullptr));
-            CK(exchange_and_merge_col(mcol));
-            launched += ns + 1;
+            const bool cseed = col_seed && sweep >= 2;
+            CK(col_stage(nullptr, cseed));
+            CK(exchange_and_merge_col(cseed ? mcol_seeded : mcol));
+            launched += (stored ? 1 : 2) * ns + 1;
+            if (cseed) {   // the exact redo when a seeded column sum left the safe range (no-ops otherwise)
+                CK(col_stage(&status->colfail, false));
+                CK(exchange_and_merge_col(mcol_redo));
+                launched += 2 * ns + 1;
+            }
             for (int i = 0; i < ns; ++i) {
                 const int t0 = tm.start();
                 if (stored) {
@@ -584,10 +636,14 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
                     TcPass rowp{ximg + offi[i], yimg, (int)slices[i].n, m, ksteps, 1, 0, split_row, part,
                                 P.eps, &status->stop};
                     rowp.seeded = row_seed && sweep >= 2;
+                    rowp.emu = T.tc_emu;
+                    rowp.epi = T.tc_epi;
                     CU(launch_lse_tc(rowp, st));
                 } else {
                     LsePass rowp{&X[i], &Y, 1, 0, split_row, part, P.eps, &status->stop};
                     rowp.seeded = row_seed && sweep >= 2;
+                    rowp.emu8 = T.lse_emu8;
+                    rowp.margin = T.lse_margin;
                     CU(launch_lse(rowp, st));
                 }
                 tm.stop(t0, sweep, LaunchTimer::ROW, (double)slices[i].n * m, stored ? 4.0 * slices[i].n * m : 0.0);
@@ -598,6 +654,7 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
                 mrow.omega = P.omega;
                 mrow.accum = i > 0 ? 1 : 0;
                 mrow.wts = slices[i].a;   // (the relaxed row error term weighs rows by a)
+                mrow.n_uniform = n_glob;  //  uniform: 1 / n_total (a slice holds part of the rows)
                 mrow.tc_fold = tc && row_seed && sweep >= 1;   // the next row pass is seeded
                 mrow.tc_margin = tc_margin;
                 mrow.anderson = amem ? 1 : 0;
@@ -715,7 +772,8 @@ sk_status validate_common(sk_ctx *ctx, long long n, long long m, int d, float ep
     if (!ctx) return SK_EINVAL;
     if (n < 1 || m < 1) return fail(ctx, SK_EINVAL, "n and m must be >= 1 (n=%lld m=%lld)", n, m);
     if (n > (1LL << 31) - 1 || m > (1LL << 31) - 1) return fail(ctx, SK_EUNSUPPORTED, "n, m < 2^31");
-    if (d < 1 || d > 64) return fail(ctx, SK_EINVAL, "d must be in [1, 64] (d=%d)", d);
+    if (d < 1 || d > 256) return fail(ctx, SK_EINVAL, "d must be in [1, 256] (d=%d)", d);
+    if (d > 64) return fail(ctx, SK_EUNSUPPORTED, "this build's kernels support d <= 64 (d=%d)", d);
     if (!(eps > 0.f) || bad_scalar(eps)) return fail(ctx, SK_EINVAL, "eps must be finite and > 0");
     if (!(tol > 0.f) || bad_scalar(tol)) return fail(ctx, SK_EINVAL, "tol must be finite and > 0");
     if (max_iter < 1) return fail(ctx, SK_EINVAL, "max_iter must be >= 1");
@@ -783,6 +841,45 @@ sk_status sk_set_anderson(sk_ctx *ctx, int32_t mem) {
     if (!ctx) return SK_EINVAL;
     if (mem < 0 || mem > 8) return fail(ctx, SK_EINVAL, "Anderson memory must lie in [0, 8], got %d", (int)mem);
     ctx->anderson = mem >= 2 ? mem : 0;
+    return SK_OK;
+}
+
+sk_status sk_set_force_nccl(sk_ctx *ctx, int32_t enable) {
+    if (!ctx) return SK_EINVAL;
+    ctx->force_nccl = enable ? 1 : 0;
+    return SK_OK;
+}
+
+sk_status sk_get_solver_options(const sk_ctx *ctx, float *omega, float *decay_init, float *decay_rate,
+                                int32_t *anderson) {
+    if (!ctx) return SK_EINVAL;
+    if (omega) *omega = ctx->omega;
+    if (decay_init) *decay_init = ctx->decay_init;
+    if (decay_rate) *decay_rate = ctx->decay_rate;
+    if (anderson) *anderson = ctx->anderson;
+    return SK_OK;
+}
+
+sk_status sk_set_tuning(sk_ctx *ctx, const char *key, double value) {
+    if (!ctx) return SK_EINVAL;
+    if (!key) return fail(ctx, SK_EINVAL, "key is NULL");
+    auto &T = ctx->tune;
+    const std::string k(key);
+    const int iv = (int)value;
+    auto need = [&](bool ok) -> sk_status {
+        return ok ? SK_OK : fail(ctx, SK_EINVAL, "sk_set_tuning(%s, %g): value out of range", key, value);
+    };
+    if (k == "tc") { CK(need(iv == 0 || iv == 1)); T.tc = iv; }
+    else if (k == "fused") { CK(need(iv == 0 || iv == 1)); T.fused = iv; }
+    else if (k == "seeded") { CK(need(iv == 0 || iv == 1)); T.seeded = iv; }
+    else if (k == "tc_margin") { CK(need(value >= 0.0 && value <= 1000.0)); T.tc_margin = (float)value; }
+    else if (k == "lse_margin") { CK(need(value >= 0.0 && value <= 1000.0)); T.lse_margin = (float)value; }
+    else if (k == "lse_emu8") { CK(need(iv >= 0 && iv <= 2)); T.lse_emu8 = iv; }
+    else if (k == "tc_emu") { CK(need(iv >= 0 && iv <= 6)); T.tc_emu = iv; }
+    else if (k == "tc_epi") { CK(need(iv == 16 || iv == 162)); T.tc_epi = iv; }
+    else if (k == "batched_shape") { CK(need(iv == 0 || iv == 1)); T.batched_shape = iv; }
+    else if (k == "batched_cl") { CK(need(iv >= 0 && iv <= 2)); T.batched_cl = iv; }
+    else return fail(ctx, SK_EINVAL, "sk_set_tuning: unknown key '%s'", key);
     return SK_OK;
 }
 
@@ -1091,8 +1188,9 @@ sk_status sinkhorn_init_gaussian(sk_ctx *ctx, int64_t n, int64_t m, int32_t d, c
                                  const float *a, const float *y, const float *b, float ridge_rel,
                                  float *pot, int32_t *side) {
     if (!ctx) return SK_EINVAL;
-    if (n < 1 || m < 1 || d < 1 || d > 64 || !x || !y || !pot || !side)
-        return fail(ctx, SK_EINVAL, "bad arguments (d in [1,64])");
+    if (n < 1 || m < 1 || d < 1 || d > 256 || !x || !y || !pot || !side)
+        return fail(ctx, SK_EINVAL, "bad arguments (d in [1,256])");
+    if (d > 64) return fail(ctx, SK_EUNSUPPORTED, "the Gaussian initializer supports d <= 64");
     if (!(ridge_rel >= 0.f) || bad_scalar(ridge_rel)) return fail(ctx, SK_EINVAL, "ridge_rel >= 0");
     const bool swap = n > m;  // potential on the smaller side
     Stager sg(ctx);
@@ -1129,8 +1227,9 @@ sk_status sinkhorn_init_gmm(sk_ctx *ctx, int64_t n, int64_t m, int32_t d, const 
                             const float *wy, const float *muy, const float *covy, float eps,
                             float inner_tol, int32_t inner_max_iter, float *pot, int32_t *side) {
     if (!ctx) return SK_EINVAL;
-    if (n < 1 || m < 1 || d < 1 || d > 64 || !x || !y || !pot || !side)
-        return fail(ctx, SK_EINVAL, "bad arguments (d in [1,64])");
+    if (n < 1 || m < 1 || d < 1 || d > 256 || !x || !y || !pot || !side)
+        return fail(ctx, SK_EINVAL, "bad arguments (d in [1,256])");
+    if (d > 64) return fail(ctx, SK_EUNSUPPORTED, "the GMM initializer supports d <= 64");
     if (Kx < 1 || Ky < 1 || Kx > 64 || Ky > 64) return fail(ctx, SK_EINVAL, "1 <= K <= 64");
     if (!wx || !mux || !covx || !wy || !muy || !covy) return fail(ctx, SK_EINVAL, "mixture parameters required");
     if (!(eps > 0.f) || bad_scalar(eps) || !(inner_tol > 0.f) || inner_max_iter < 1)
@@ -1284,6 +1383,8 @@ sk_status solve_impl(sk_ctx *ctx, int64_t B, int64_t n, int64_t m, int32_t d, co
         L.omega = ctx->omega;
         L.decay_init = ctx->decay_init; L.decay_rate = ctx->decay_rate;
         L.anderson = ctx->anderson;
+        L.shape = ctx->tune.batched_shape;
+        L.cl = ctx->tune.batched_cl;
         CU(cudaEventRecord(ctx->ev0, st));
         CU(launch_batched(L, st));
         CU(cudaEventRecord(ctx->ev1, st));
@@ -1422,7 +1523,8 @@ sk_status sinkhorn_solve_sharded(sk_ctx *ctx, int64_t n_total, int64_t row0, int
     P.y = dy; P.b = db;
     P.eps = eps; P.tol = tol; P.max_iter = max_iter; P.check_every = check_every; P.mode = mode;
     P.g = dg;
-    P.world = ctx->world; P.nccl = ctx->world > 1; P.partitioned = true; P.omega = ctx->omega;
+    P.world = ctx->world; P.nccl = ctx->world > 1 || (ctx->force_nccl && ctx->comm); P.partitioned = true;
+    P.omega = ctx->omega;
     std::vector<Slice> sl{Slice{row0, n_local, dx, da, dfi, df, ctx->rank}};
     sk_status s = solve_core_decay(ctx, P, sl, rep);
     if (s != SK_OK && s != SK_ENONFINITE) return s;

@@ -587,14 +587,13 @@ static cudaError_t launch_batched_e(const BatchArgs &A, int B, cudaStream_t st) 
 }
 
 // One wide CTA per problem: NT threads x R output points per thread per round.
-// SK_BATCHED_SHAPE=1 selects 512 threads x 2 points for 512 < P <= 1024 (tuning knob).
-// With a CTA pair (CL = 2) each CTA's shape covers its half of the points (no idle lanes).
+// shape 1 (sk_set_tuning "batched_shape", default) selects 512 threads x 2 points for
+// 512 < P <= 1024, shape 0 1024 x 1.  With a CTA pair (CL = 2) each CTA's shape covers its half
+// of the points (no idle lanes).
 template <int D>
-static cudaError_t launch_batched_d(const BatchArgs &A, int B, cudaStream_t st) {
-    static int shape = [] { const char *e = getenv("SK_BATCHED_SHAPE"); return e ? atoi(e) : 1; }();
-    // CTA pair: opt-in for batches (SK_BATCHED_CL=2), the default for one latency-bound problem
-    // (C1: 0.267 vs 0.295 ms for 34 sweeps); SK_BATCHED_CL=1 forces one CTA
-    static const int clk = [] { const char *e = getenv("SK_BATCHED_CL"); return e ? atoi(e) : 0; }();
+static cudaError_t launch_batched_d(const BatchArgs &A, int B, int shape, int clk, cudaStream_t st) {
+    // CTA pair: opt-in for batches (sk_set_tuning "batched_cl" = 2), the default for one
+    // latency-bound problem (C1: 0.267 vs 0.295 ms for 34 sweeps); 1 forces one CTA
     const int P = A.n > A.m ? A.n : A.m;
     const bool pair = clk == 2 || (clk == 0 && B == 1);
     if (pair && P > 128 && P <= 2048) {
@@ -630,10 +629,10 @@ cudaError_t launch_batched(const BatchLaunch &L, cudaStream_t st) {
     A.decay_init = L.decay_init; A.decay_rate = L.decay_rate;
     A.anderson = L.anderson;
     switch (L.d) {
-        case 1: return launch_batched_d<1>(A, L.B, st);
-        case 2: return launch_batched_d<2>(A, L.B, st);
-        case 3: return launch_batched_d<3>(A, L.B, st);
-        case 4: return launch_batched_d<4>(A, L.B, st);
+        case 1: return launch_batched_d<1>(A, L.B, L.shape, L.cl, st);
+        case 2: return launch_batched_d<2>(A, L.B, L.shape, L.cl, st);
+        case 3: return launch_batched_d<3>(A, L.B, L.shape, L.cl, st);
+        case 4: return launch_batched_d<4>(A, L.B, L.shape, L.cl, st);
         default: return cudaErrorInvalidValue;
     }
 }

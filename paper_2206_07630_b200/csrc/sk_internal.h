@@ -24,6 +24,8 @@ struct BatchLaunch {
     float omega = 1.f;   // Alg. 1's relaxation
     float decay_init = 0.f, decay_rate = 1.f;   // eps-decay (R-25; decay_init <= 0: off)
     int anderson = 0;    // Anderson memory (R-27; < 2: off)
+    int shape = 1;       // sk_set_tuning "batched_shape" (512 x 2 points for 512 < P <= 1024)
+    int cl = 0;          // sk_set_tuning "batched_cl": 0 auto, 1 one CTA, 2 CTA pair per problem
 };
 bool batched_supported(int d, int n, int m, int mem = 0);
 // K18 general 1D initializer (NW corner + Alg. 3/4, R-26) on sorted supports
@@ -118,6 +120,9 @@ struct TcPass {
     int mma_only = 0;
     long long *cyc = nullptr;   // K14: SM cycles of CTA 0
     int seeded = 0;             // the output side's shifts were folded by K6 (max-free pass)
+    const int *only_if = nullptr;   // run only if *only_if != 0 (the exact redo of a seeded column pass)
+    int emu = 2;                // exponential pairs (of every 8) on the FMA pipe (sk_set_tuning "tc_emu")
+    int epi = 162;              // epilogue organisation (sk_set_tuning "tc_epi": 162 or 16)
 };
 size_t tc_image_bytes(long long P);
 cudaError_t launch_absmax(const float *pts, long long cnt, unsigned *out, cudaStream_t st);  // out zeroed first
@@ -140,7 +145,15 @@ struct LsePass {
     float eps;
     const int *stop;  // device flag (nullable)
     int seeded = 0;   // fixed shift = Pside->lse[p] + margin (no running max); see k_merge
+    const int *only_if = nullptr;   // run only if *only_if != 0 (the exact redo of a seeded column pass)
+    int emu8 = 1;     // seeded D <= 4: exponential pairs (of 8) on the FMA pipe (sk_set_tuning "lse_emu8")
+    float margin = 4.f;   // seeded: log2 units above the previous LSE (sk_set_tuning "lse_margin")
 };
+// K6a: per fixed row block, the stable merge of its split_q sub-split partials in fixed order:
+// part [nblk * split_q][P] -> out [nblk][P], one (M, S) per point per block (the exchange payload
+// of the column pass; the same merge tree for every partition of the rows).
+cudaError_t launch_premerge(const float2 *part, int nblk, int split_q, long long P, float2 *out, const int *stop,
+                            const int *only_if, cudaStream_t st);
 cudaError_t launch_lse(const LsePass &L, cudaStream_t st);
 int lse_occupancy_ctas(int D);  // resident CTAs per SM of the LSE kernel for D
 
@@ -172,6 +185,10 @@ struct MergePass {
     int accum = 0;            // relaxed ROW of a later slice: add its row terms (row_err, mass_dev)
     int anderson = 0;         // Anderson (R-27): COL takes no decision; ROW writes its slice's
     double *and_err = nullptr;//   row term of err_l for (f^l, g~) to *and_err (K19 decides)
+    long long n_uniform = 0;  // uniform weights (wts == nullptr): 1 / n_uniform (0: the side's own P);
+                              //   a row slice of a sharded solve weighs its rows by 1 / n_total
+    int range_redo = 0;       // COL after a seeded pass: a sum outside [2^-100, 2^100] sets
+                              //   st->colfail (no decision) and the column pass is redone exactly
 };
 cudaError_t launch_merge(const MergePass &M, cudaStream_t st);
 // K19 Anderson (sk_anderson.cu): state = anderson_state_bytes() (zeroed before the solve); per

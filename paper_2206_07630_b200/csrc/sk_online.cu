@@ -92,10 +92,11 @@ struct LseArgs {
     float2 *part;
     float tk;
     const int *stop;
+    const int *only_if;     // run only if *only_if != 0 (nullable)
     const float *seed;      // SEEDED: P side last LSE
+    float margin;           // SEEDED: shift = seed + margin (log2 units)
 };
 
-constexpr float kSeedMarginMK = 4.f;  // log2 units above the previous LSE
 
 // EMU8: exponential pairs (of every 8 pairs = 2 chunks) evaluated on the FMA pipe in the
 // seeded pass (D <= 4); balances MUFU against the FMA pipe (measured by SK_LSE_EMU8 sweeps)
@@ -106,6 +107,7 @@ __global__ void __launch_bounds__(kLT) k_lse(LseArgs A) {
     extern __shared__ __align__(128) float ring[];  // [kStages][TF]
     __shared__ __align__(8) uint64_t full[kStages];
     if (A.stop && *(volatile const int *)A.stop) return;
+    if (A.only_if && !*(volatile const int *)A.only_if) return;
 
     // ---- this CTA's Q range: split s = blockIdx.y -> block b, sub-split u
     const int s = blockIdx.y;
@@ -131,7 +133,7 @@ __global__ void __launch_bounds__(kLT) k_lse(LseArgs A) {
             const float v = p < A.P ? tile[k * A.Ptq + po] * A.tk : 0.f;
             pd[r][k] = make_float2(v, v);
         }
-        M[r] = (SEEDED && p < A.P) ? A.seed[p] + kSeedMarginMK : -INFINITY;
+        M[r] = (SEEDED && p < A.P) ? A.seed[p] + A.margin : -INFINITY;
         Sx[r] = make_float2(0.f, 0.f);
     }
 
@@ -181,7 +183,7 @@ static cudaError_t launch_lse_d(const LsePass &L, cudaStream_t st) {
     cudaError_t e = cudaFuncSetAttribute(k_lse<D, R, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
-    static const int emu8 = [] { const char *v = getenv("SK_LSE_EMU8"); return v ? atoi(v) : 1; }();
+    const int emu8 = L.emu8;
     auto seeded_fn = emu8 == 0 ? k_lse<D, R, true, 0> : (emu8 == 1 ? k_lse<D, R, true, 1> : k_lse<D, R, true, 2>);
     e = cudaFuncSetAttribute(seeded_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -192,7 +194,9 @@ static cudaError_t launch_lse_d(const LsePass &L, cudaStream_t st) {
     A.part = L.part;
     A.tk = 2.f * kLog2e / L.eps;
     A.stop = L.stop;
+    A.only_if = L.only_if;
     A.seed = L.Pside->lse;
+    A.margin = L.margin;
     dim3 grid((A.P + kLT * R - 1) / (kLT * R), L.nblk * L.split_q);
     if (L.seeded && A.seed) seeded_fn<<<grid, kLT, smem, st>>>(A);
     else k_lse<D, R, false><<<grid, kLT, smem, st>>>(A);
@@ -289,6 +293,14 @@ __device__ void exact_lse_point(const Side &S, const Side &Q, int p, float eps, 
 __device__ __forceinline__ void merge_point(const MergePass &Mp, const Side &S, const Side &Qs, int p, float M, float Ssum,
                                             bool check, const float *hold, float *hnew, double &e, double &e2, int &bad) {
     const float eps = Mp.eps, kap = kLog2e / eps, epsln2 = eps * kLn2;
+    const double wu = 1.0 / (double)(Mp.n_uniform > 0 ? Mp.n_uniform : S.P);   // uniform weight
+    if (Mp.range_redo && !(Ssum >= 0x1p-100f && Ssum <= 0x1p100f)) {
+        // seeded column pass: the fixed shift was far from this column's true maximum.  The exact
+        // pass is redone for every column (k_lse / k_lse_tc2 + premerge + merge, gated on
+        // st->colfail) so that every partition of the rows takes the same path.
+        bad |= 2;
+        return;
+    }
     if (Mp.Q && !(Ssum >= 0x1p-100f && Ssum <= 0x1p100f)) {
         // seeded pass: the fixed shift was far from the true maximum -> exact recompute of
         // this point over the whole reduced side (rare; one thread, online max)
@@ -323,7 +335,7 @@ __device__ __forceinline__ void merge_point(const MergePass &Mp, const Side &S, 
     hnew[p] = hn;
     if (Mp.omega != 1.f && Mp.mode == MERGE_ROW) {
         // rows are no longer exact after a relaxed f-update: sum_j P_ij = a_i exp((f_i - fsk_i)/eps)
-        const double ai = Mp.wts ? (double)Mp.wts[p] : 1.0 / S.P;
+        const double ai = Mp.wts ? (double)Mp.wts[p] : wu;
         const double dv = (double)expm1f((hn - hsk) / eps);
         e += ai * fabs(dv);
         e2 += ai * dv;
@@ -337,11 +349,11 @@ __device__ __forceinline__ void merge_point(const MergePass &Mp, const Side &S, 
     }
     bad |= !isfinite(hn);
     if (Mp.anderson && Mp.mode == MERGE_ROW) {   // row term of err_l for (f^l, g~): columns are exact
-        const double ai = Mp.wts ? (double)Mp.wts[p] : 1.0 / S.P;
+        const double ai = Mp.wts ? (double)Mp.wts[p] : wu;
         e += ai * fabs((double)expm1f((hold[p] - hsk) / eps));
     }
     if (check) {
-        const double bj = Mp.wts ? (double)Mp.wts[p] : 1.0 / S.P;
+        const double bj = Mp.wts ? (double)Mp.wts[p] : wu;
         e += bj * fabs((double)expm1f((hold[p] - hsk) / eps));   // column term of err_l (H5)
     }
 }
@@ -492,6 +504,40 @@ cudaError_t launch_merge(const MergePass &M, cudaStream_t st) {
     } else {
         k_merge<false><<<merge_blocks(M.S->P), kMT, 0, st>>>(M, *M.S, Qs);
     }
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------- K6a
+// One (M, S) per point per fixed row block from its split_q sub-split partials, merged in split
+// order (the first step of the column pass's fixed merge tree; k_merge then merges the blocks in
+// block order).  Sharded solves exchange exactly these block partials: 8 B per column per block.
+__global__ void __launch_bounds__(256) k_premerge(const float2 *__restrict__ part, int nblk, int split_q,
+                                                  long long P, float2 *__restrict__ out, const int *stop,
+                                                  const int *only_if) {
+    if (stop && *(volatile const int *)stop) return;
+    if (only_if && !*(volatile const int *)only_if) return;
+    const long long total = (long long)nblk * P;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+         t += (long long)gridDim.x * blockDim.x) {
+        const long long b = t / P, p = t - b * P;
+        const float2 *src = part + b * split_q * P + p;
+        float M = -INFINITY;
+        for (int u = 0; u < split_q; ++u) M = fmaxf(M, src[u * P].x);
+        float S = 0.f;
+        for (int u = 0; u < split_q; ++u) {
+            const float2 v = src[u * P];
+            if (v.x != -INFINITY) S = fmaf(v.y, ex2(v.x - M), S);
+        }
+        out[t] = make_float2(M, S);
+    }
+}
+
+cudaError_t launch_premerge(const float2 *part, int nblk, int split_q, long long P, float2 *out, const int *stop,
+                            const int *only_if, cudaStream_t st) {
+    const long long total = (long long)nblk * P;
+    long long b = (total + 255) / 256;
+    if (b > 148 * 8) b = 148 * 8;
+    k_premerge<<<(int)(b < 1 ? 1 : b), 256, 0, st>>>(part, nblk, split_q, P, out, stop, only_if);
     return cudaGetLastError();
 }
 

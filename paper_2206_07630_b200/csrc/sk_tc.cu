@@ -177,6 +177,7 @@ struct TcArgs {
     float2 *part;
     float tk;                   // 2 log2(e)/eps (only the selftest's unscale uses it)
     const int *stop;
+    const int *only_if;         // run only if *only_if != 0 (nullable; the exact column redo)
     float *debug_acc;           // if non-null: write <p, q> of the first 128 x 128 block, [128][128]
     int mma_only;               // K14 probes: 1, 2, 4 = the epilogue only releases the buffers
                                 //   (2: and the B ring is not reloaded); 3 = no MMAs, full epilogue
@@ -273,7 +274,8 @@ __global__ void __launch_bounds__(64 + 32 * NE, 1) k_lse_tc2(TcArgs A) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_rank();
     const bool leader = rank == 0;
-    const bool stopped = A.stop && *(volatile const int *)A.stop;   // uniform over the pair (same flag)
+    // uniform over the pair (same flags)
+    const bool stopped = (A.stop && *(volatile const int *)A.stop) || (A.only_if && !*(volatile const int *)A.only_if);
     if (stopped) return;
     const int nsplit = A.nblk * A.split_q;
     const int items = A.ptiles * nsplit;
@@ -656,10 +658,9 @@ static cudaError_t launch_tc2(const TcArgs &A, int items, cudaStream_t st) {
 }
 
 template <int EMU>
-static cudaError_t launch_tc2_ne(const TcArgs &A, int items, bool seeded, cudaStream_t st) {
-    // SK_TC_EPI: epilogue organisation: 162 = 16 warps in two tile groups (even / odd tiles,
-    // 128 columns per warp); 16 = four warps per TMEM lane quadrant on every tile (64 columns)
-    static const int ne = [] { const char *e = getenv("SK_TC_EPI"); return e ? atoi(e) : 162; }();
+static cudaError_t launch_tc2_ne(const TcArgs &A, int items, bool seeded, int ne, cudaStream_t st) {
+    // epilogue organisation (sk_set_tuning "tc_epi"): 162 = 16 warps in two tile groups (even /
+    // odd tiles, 128 columns per warp); 16 = four warps per TMEM lane quadrant on every tile
     if (seeded) return ne == 16 ? launch_tc2<EMU, 16, true, 1>(A, items, st) : launch_tc2<EMU, 16, true, 2>(A, items, st);
     return ne == 16 ? launch_tc2<EMU, 16, false, 1>(A, items, st) : launch_tc2<EMU, 16, false, 2>(A, items, st);
 }
@@ -667,13 +668,13 @@ static cudaError_t launch_tc2_ne(const TcArgs &A, int items, bool seeded, cudaSt
 int tc_points_per_tile() { return kT2N; }
 
 cudaError_t launch_lse_tc(const TcPass &L, cudaStream_t st) {
-    // exponential pairs (of every 8) evaluated on the FMA pipe; SK_TC_EMU overrides
-    static const int emu = [] { const char *e = getenv("SK_TC_EMU"); return e ? atoi(e) : 2; }();
+    // exponential pairs (of every 8) evaluated on the FMA pipe (sk_set_tuning "tc_emu")
+    const int emu = L.emu, ne = L.epi;
     TcArgs A;
     A.Aimg = (const unsigned char *)L.Aimg; A.Bimg = (const unsigned char *)L.Bimg;
     A.P = L.P; A.Q = (int)L.Q; A.ksteps = L.ksteps;
     A.split_q = L.split_q;
-    A.part = L.part; A.tk = 2.f * kLog2e / L.eps; A.stop = L.stop; A.debug_acc = L.debug_acc;
+    A.part = L.part; A.tk = 2.f * kLog2e / L.eps; A.stop = L.stop; A.only_if = L.only_if; A.debug_acc = L.debug_acc;
     A.mma_only = L.mma_only;
     A.cyc = L.cyc;
     if (A.ksteps < 1 || A.ksteps > 4) return cudaErrorInvalidValue;
@@ -684,13 +685,13 @@ cudaError_t launch_lse_tc(const TcPass &L, cudaStream_t st) {
     const int items = A.ptiles * L.nblk * L.split_q;
     const bool seeded = L.seeded != 0;
     switch (emu) {
-        case 0: return launch_tc2_ne<0>(A, items, seeded, st);
-        case 1: return launch_tc2_ne<1>(A, items, seeded, st);
-        case 3: return launch_tc2_ne<3>(A, items, seeded, st);
-        case 4: return launch_tc2_ne<4>(A, items, seeded, st);
-        case 5: return launch_tc2_ne<5>(A, items, seeded, st);
-        case 6: return launch_tc2_ne<6>(A, items, seeded, st);
-        default: return launch_tc2_ne<2>(A, items, seeded, st);
+        case 0: return launch_tc2_ne<0>(A, items, seeded, ne, st);
+        case 1: return launch_tc2_ne<1>(A, items, seeded, ne, st);
+        case 3: return launch_tc2_ne<3>(A, items, seeded, ne, st);
+        case 4: return launch_tc2_ne<4>(A, items, seeded, ne, st);
+        case 5: return launch_tc2_ne<5>(A, items, seeded, ne, st);
+        case 6: return launch_tc2_ne<6>(A, items, seeded, ne, st);
+        default: return launch_tc2_ne<2>(A, items, seeded, ne, st);
     }
 }
 

@@ -16,7 +16,8 @@ import numpy as np
 import pytest
 import torch
 
-from parity import (INIT_RTOL, assert_obj_close, assert_pair_close, centred, count_tol, rel_inf)
+from parity import (INIT_RTOL, assert_obj_close, assert_pair_close, centred, count_tol, plan_marginal_error,
+                    rel_inf)
 from workloads import gen
 
 pytestmark = pytest.mark.gpu
@@ -65,12 +66,20 @@ def test_sharded_bit_identical_across_world_sizes(O, ctx, mode, n, m, d):
     # the real sharded entry at world = 1 runs the same partition: bit-identical
     fs, gs, rs = sk.sinkhorn_solve_sharded(ctx, n, 0, xd, yd, eps, a_local=ad, mode=mode)
     assert torch.equal(fs, f1) and torch.equal(gs, g1) and rs["dual_objective"] == r1["dual_objective"]
-    # the unsharded entry may also seed its column pass (needs all rows for the exact fallback):
-    # same iterate up to fp32 rounding
+    # the unsharded entry runs the same merge tree (per-block premerge, block-order merge, the
+    # seeded column pass with the gated exact redo): bit-identical on the online paths.  Stored:
+    # its fused single-read sweep recomputes a failing column inside the merge instead - the same
+    # iterate up to fp32 rounding
     fu, gu, ru = sk.sinkhorn_solve(ctx, xd, yd, eps, a=ad, mode=mode)
-    assert abs(ru["iterations"] - r1["iterations"]) <= 1
-    if ru["iterations"] == r1["iterations"]:
-        assert_pair_close(fu.cpu().numpy(), gu.cpu().numpy(), f1.cpu().numpy(), g1.cpu().numpy(), eps, rtol=1e-5)
+    if mode == "online":
+        assert ru["iterations"] == r1["iterations"]
+        assert torch.equal(fu, f1) and torch.equal(gu, g1)
+        assert ru["dual_objective"] == r1["dual_objective"] and ru["marginal_error"] == r1["marginal_error"]
+    else:
+        assert abs(ru["iterations"] - r1["iterations"]) <= 1
+        if ru["iterations"] == r1["iterations"]:
+            assert_pair_close(fu.cpu().numpy(), gu.cpu().numpy(), f1.cpu().numpy(), g1.cpu().numpy(), eps,
+                              rtol=1e-5)
     # and the oracle (unsharded, fp64)
     L = r1["iterations"]
     ref = O.sinkhorn(x, y, eps, a=a)
@@ -78,6 +87,72 @@ def test_sharded_bit_identical_across_world_sizes(O, ctx, mode, n, m, d):
     lock = O.sinkhorn(x, y, eps, a=a, tol=0, max_iter=L)
     assert_pair_close(f1.cpu().numpy(), g1.cpu().numpy(), lock.f, lock.g, eps)
     assert_obj_close(r1["dual_objective"], lock.E, eps)
+
+
+@pytest.mark.parametrize("accel", ["plain", "omega", "anderson"])
+def test_sharded_uniform_weights_error_and_objective(O, ctx, accel):
+    """Uniform row weights (a = NULL) in the sharded entries: every row slice weighs its rows by
+    1 / n_total (not 1 / n_local), so the reported marginal error, E and the stop sweep equal the
+    unsharded solve's for W = 2, 4, 8 (the relaxed / Anderson row terms were W times
+    too large); the explicit fp64 error of the returned pair (recomputed by the test) agrees."""
+    import paper_2206_07630_b200 as sk
+    rng = np.random.default_rng(11)
+    n, m, d = 6000, 2500, 3
+    x = rng.random((n, d)).astype(np.float32)
+    y = rng.random((m, d)).astype(np.float32)
+    eps = float(np.float32(0.05 * gen.mean_sq_cost(x, y)))
+    xd, yd = _cuda(x), _cuda(y)
+    kw = {"plain": {}, "omega": {"omega": 1.3}, "anderson": {"anderson": 5}}[accel]
+    fu, gu, ru = sk.sinkhorn_solve(ctx, xd, yd, eps, mode="online", **kw)
+    for W in (2, 4, 8):
+        f, g, r = sk.sinkhorn_solve_sharded_emulated(ctx, W, xd, yd, eps, mode="online", **kw)
+        if accel == "plain":   # the same merge tree: bit-identical
+            assert r["iterations"] == ru["iterations"] and torch.equal(f, fu) and torch.equal(g, gu)
+        # accelerated: the row terms are summed per slice (rank) - equal up to rounding
+        assert abs(r["iterations"] - ru["iterations"]) <= 1, (W, r, ru)
+        if r["iterations"] == ru["iterations"]:
+            assert abs(r["marginal_error"] - ru["marginal_error"]) <= 1e-3 * ru["marginal_error"] + 1e-7, (W, r, ru)
+            assert_obj_close(r["dual_objective"], ru["dual_objective"], eps, rtol=1e-6)
+        err = plan_marginal_error(x, y, f.cpu().numpy(), g.cpu().numpy(), eps)
+        assert abs(err - r["marginal_error"]) <= 0.02 * err + 1e-6, (W, err, r["marginal_error"])
+
+
+@pytest.fixture(scope="module")
+def nccl_ctx():
+    """A context with a 1-rank NCCL communicator and the force-NCCL hook: sinkhorn_solve_sharded
+    then runs its NCCL data plane (allgather of the block partials, the allreduce sites)."""
+    import paper_2206_07630_b200 as sk
+    c = sk.Context(0)
+    try:
+        uid = c.nccl_unique_id()
+        c.comm_init(uid, 0, 1)
+    except sk.SinkhornError as ex:   # NCCL must load on a GPU box: fail loudly, never skip
+        raise AssertionError(f"NCCL unavailable: {ex}")
+    c.set_force_nccl(True)
+    yield c
+    c.close()
+
+
+@pytest.mark.parametrize("accel", ["plain", "omega", "anderson", "stored"])
+def test_nccl_branch_one_rank_bit_identical(ctx, nccl_ctx, accel):
+    """the NCCL branch of the sharded solver (ncclAllGather of the block partials,
+    ncclAllReduce of the relaxed row terms / the Anderson Gram dots, ncclAllGather of E's block
+    sums) on a 1-rank communicator is bit-identical to the emulated world-1 solve."""
+    import paper_2206_07630_b200 as sk
+    rng = np.random.default_rng(12)
+    n, m, d = 5000, 3000, (16 if accel == "stored" else 3)
+    x = rng.random((n, d)).astype(np.float32)
+    y = rng.random((m, d)).astype(np.float32)
+    a = gen.random_weights(n, rng)
+    eps = float(np.float32(0.04 * gen.mean_sq_cost(x, y)))
+    xd, yd, ad = _cuda(x), _cuda(y), _cuda(a)
+    mode = "stored" if accel == "stored" else "online"
+    kw = {"plain": {}, "stored": {}, "omega": {"omega": 1.2}, "anderson": {"anderson": 5}}[accel]
+    fe, ge, re_ = sk.sinkhorn_solve_sharded_emulated(ctx, 1, xd, yd, eps, a=ad, mode=mode, **kw)
+    fn, gn, rn = sk.sinkhorn_solve_sharded(nccl_ctx, n, 0, xd, yd, eps, a_local=ad, mode=mode, **kw)
+    assert rn["iterations"] == re_["iterations"] and rn["converged"] == re_["converged"] == 1
+    assert torch.equal(fn, fe) and torch.equal(gn, ge)
+    assert rn["dual_objective"] == re_["dual_objective"] and rn["marginal_error"] == re_["marginal_error"]
 
 
 def test_shard_partition_small_n_rejected_for_empty_ranks(ctx):

@@ -202,25 +202,18 @@ def test_stored_fused_column_fallback(O, ctx):
 
 
 def test_onchip_cta_pair_variant_is_bit_identical(O, ctx):
-    """SK_BATCHED_CL=2 (a CTA pair per problem, DSMEM exchange) computes every point's LSE with
-    the same arithmetic: the same potentials and counts as one CTA per problem."""
-    import os, subprocess, sys
-    code = r'''
-import sys, numpy as np, torch
-sys.path.insert(0, %r)
-import paper_2206_07630_b200 as sk
-from workloads import gen
-c2 = gen.c2(B=16, n=1024)
-ctx = sk.Context(0)
-xb, yb = torch.from_numpy(c2.x).cuda(), torch.from_numpy(c2.y).cuda()
-pot = sk.sinkhorn_init_sort1d(ctx, xb.view(16, 1024), yb.view(-1))
-f, g, r = sk.sinkhorn_solve(ctx, xb, yb, c2.eps, y_shared=True, f_init=pot)
-np.savez(sys.argv[1], f=f.cpu().numpy(), g=g.cpu().numpy(), it=[q["iterations"] for q in r])
-''' % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    """sk_set_tuning("batched_cl", 2) (a CTA pair per problem, DSMEM exchange) computes every
+    point's LSE with the same arithmetic: the same potentials and counts as one CTA per problem."""
+    import paper_2206_07630_b200 as sk
+    c2 = gen.c2(B=16, n=1024)
     outs = []
-    for cl in ("1", "2"):
-        fn = f"/tmp/cl_{cl}_{os.getpid()}.npz"
-        subprocess.check_call([sys.executable, "-c", code, fn], env=dict(os.environ, SK_BATCHED_CL=cl))
-        outs.append(np.load(fn))
-    assert np.array_equal(outs[0]["it"], outs[1]["it"])
-    assert np.array_equal(outs[0]["f"], outs[1]["f"]) and np.array_equal(outs[0]["g"], outs[1]["g"])
+    for cl in (1, 2):
+        c = sk.Context(0)
+        c.set_tuning("batched_cl", cl)
+        xb, yb = torch.from_numpy(c2.x).cuda(), torch.from_numpy(c2.y).cuda()
+        pot = sk.sinkhorn_init_sort1d(c, xb.view(16, 1024), yb.view(-1))
+        f, g, r = sk.sinkhorn_solve(c, xb, yb, c2.eps, y_shared=True, f_init=pot)
+        outs.append((f.cpu().numpy(), g.cpu().numpy(), [q["iterations"] for q in r]))
+        c.close()
+    assert outs[0][2] == outs[1][2]
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])

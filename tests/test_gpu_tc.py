@@ -55,53 +55,45 @@ def test_tc_solve_parity(O, ctx, n, m, d, eps_factor):
 
 
 def test_tc_matches_ffma_kernel():
-    """Same problem through the tcgen05 pass and (SK_TC=0) the FFMA pass: same iteration count,
-    potentials within fp32 noise of each other."""
-    code = r'''
-import sys, numpy as np, torch
-sys.path.insert(0, %r)
-import paper_2206_07630_b200 as sk
-from workloads import gen
-p = gen.c5(n=1536, eps_factor=1e-2)
-ctx = sk.Context(0)
-f, g, r = sk.sinkhorn_solve(ctx, torch.from_numpy(p.x).cuda(), torch.from_numpy(p.y).cuda(), p.eps, mode="online")
-np.savez(sys.argv[1], f=f.cpu().numpy(), g=g.cpu().numpy(), it=r["iterations"])
-''' % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    """Same problem through the tcgen05 pass and (sk_set_tuning("tc", 0)) the FFMA pass: same
+    iteration count, potentials within fp32 noise of each other."""
+    import paper_2206_07630_b200 as sk
+    p = gen.c5(n=1536, eps_factor=1e-2)
     outs = []
-    for tc in ("1", "0"):
-        fn = f"/tmp/tc_cmp_{tc}_{os.getpid()}.npz"
-        env = dict(os.environ, SK_TC=tc)
-        subprocess.check_call([sys.executable, "-c", code, fn], env=env)
-        outs.append(np.load(fn))
-    a, b = outs
-    assert abs(int(a["it"]) - int(b["it"])) <= 1
-    fa, fb = a["f"] - a["f"].mean(), b["f"] - b["f"].mean()
+    for tc in (1, 0):
+        ctx = sk.Context(0)
+        ctx.set_tuning("tc", tc)
+        f, g, r = sk.sinkhorn_solve(ctx, torch.from_numpy(p.x).cuda(), torch.from_numpy(p.y).cuda(), p.eps,
+                                    mode="online")
+        outs.append((f.cpu().numpy(), r["iterations"]))
+        ctx.close()
+    (fa, ia), (fb, ib) = outs
+    assert abs(ia - ib) <= 1
+    fa, fb = fa - fa.mean(), fb - fb.mean()
     assert np.abs(fa - fb).max() <= 1e-4 * max(np.abs(fb).max(), 1e-3)
 
 
-def test_tc_seeded_exact_fallback():
-    """The seeded tensor-core passes (fixed shift = previous LSE + margin) with a margin of 300
-    log2 units: every partial sum underflows, so k_merge must recompute every point exactly from
-    the fp32 coordinates; the result must still match the oracle in lockstep."""
-    code = r'''
-import sys, numpy as np, torch
-sys.path.insert(0, %r)
-import paper_2206_07630_b200 as sk
-from workloads import gen
-p = gen.c5(n=1100, d=48, eps_factor=2e-2)
-x, y = p.x[:700].copy(), p.y[:1100].copy()
-ctx = sk.Context(0)
-f, g, r = sk.sinkhorn_solve(ctx, torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda(), p.eps, mode="online")
-np.savez(sys.argv[1], f=f.cpu().numpy(), g=g.cpu().numpy(), it=r["iterations"], E=r["dual_objective"], eps=p.eps)
-''' % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    fn = f"/tmp/tc_fb_{os.getpid()}.npz"
-    subprocess.check_call([sys.executable, "-c", code, fn], env=dict(os.environ, SK_TC_SEED_MARGIN="300"))
-    a = np.load(fn)
-    from oracle import oracle as O
-    p = gen.c5(n=1100, d=48, eps_factor=2e-2)
-    x, y = p.x[:700].copy(), p.y[:1100].copy()
-    it = int(a["it"])
+@pytest.mark.parametrize("d", [48, 3])
+def test_seeded_exact_fallback_and_column_redo(O, d):
+    """The seeded passes (fixed shift = previous LSE + margin) with a margin of 300 log2 units:
+    every partial sum underflows, so k_merge must recompute every row exactly and every seeded
+    column pass must be redone exactly (the colfail redo, K3 at d = 48 / K2 at d = 3); the
+    result must still match the oracle in lockstep."""
+    import paper_2206_07630_b200 as sk
+    if d == 48:
+        p = gen.c5(n=1100, d=48, eps_factor=2e-2)
+        x, y, eps = p.x[:700].copy(), p.y[:1100].copy(), p.eps
+    else:
+        rng = np.random.default_rng(3)
+        x = rng.random((5000, 3)).astype(np.float32)
+        y = rng.random((4100, 3)).astype(np.float32)
+        eps = float(np.float32(0.03 * gen.mean_sq_cost(x, y)))
+    ctx = sk.Context(0)
+    ctx.set_tuning("tc_margin" if d == 48 else "lse_margin", 300)
+    f, g, r = sk.sinkhorn_solve(ctx, torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda(), eps, mode="online")
+    ctx.close()
+    it = r["iterations"]
     assert it > 3   # seeded passes (sweep >= 2) ran
-    lock = O.sinkhorn(x, y, float(a["eps"]), tol=0, max_iter=it)
-    assert_pair_close(a["f"], a["g"], lock.f, lock.g, float(a["eps"]))
-    assert_obj_close(float(a["E"]), lock.E, float(a["eps"]))
+    lock = O.sinkhorn(x, y, eps, tol=0, max_iter=it)
+    assert_pair_close(f.cpu().numpy(), g.cpu().numpy(), lock.f, lock.g, eps)
+    assert_obj_close(r["dual_objective"], lock.E, eps)
