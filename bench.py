@@ -334,7 +334,9 @@ class Single(Workload):
         return float(self.n) * self.m * rep["iterations"] / self.world   # each rank's share
 
     def step(self):
-        return self._run(self.x, self.y)
+        e = self._run(self.x, self.y)
+        self.step_L = self.rep["iterations"]
+        return e
 
     def e2e_step(self):
         e = self._run(self.xh, self.yh)
@@ -381,7 +383,7 @@ class Single(Workload):
         from workloads import gen
         e, t, thr, _ = single_cpu_sample(self.p, target_s / 2)
         rate = e / t                      # cost entries (one per sweep = 2 passes) per second
-        p, L = self.p, self.rep["iterations"]
+        p, L = self.p, self.step_L
         out = {"kind": "oracle", "cores": thr, "sweep_entries_per_s": rate,
                "time_to_tol_s_extrapolated": (p.n * p.m * L) / rate,
                "extrapolation": f"L = {L} sweeps (this run's) x n m / measured fp64 sweep rate"}

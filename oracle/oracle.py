@@ -155,6 +155,8 @@ def sinkhorn(x, y, eps, a=None, b=None, tol=1e-3, max_iter=10000, check_every=1,
 def sinkhorn_anderson(x, y, eps, mem=5, a=None, b=None, tol=1e-3, max_iter=10000, check_every=1, f0=None) -> Result:
     """Alg. 1 with Anderson acceleration of memory `mem` on the sweep map (R-27):
     returns the last iterate's pair (f, g_sk(f)) with its explicit error and Eq. (2)."""
+    if not 1 <= int(mem) <= 16:
+        raise ValueError(f"Anderson memory must lie in [1, 16], got {mem}")
     x, y = _pts(x), _pts(y)
     n, m, d = x.shape[0], y.shape[0], x.shape[1]
     a, b = _weights(a, n), _weights(b, m)
@@ -176,6 +178,8 @@ def sinkhorn_matrix(C, eps, a=None, b=None, tol=1e-3, max_iter=10000, check_ever
     it, err, E = ctypes.c_int(), ctypes.c_double(), ctypes.c_double()
     f0a = None if f0 is None else _d(f0)
     if anderson:   # Anderson on the sweep map (R-27), as sinkhorn_anderson for a given cost matrix
+        if not 1 <= int(anderson) <= 16:
+            raise ValueError(f"Anderson memory must lie in [1, 16], got {anderson}")
         conv = _L().ora_sinkhorn_matrix_anderson(n, m, _p(C), _p(a), _p(b), float(eps), int(anderson), float(tol),
                                                  int(max_iter), int(check_every), _p(f0a), _p(f), _p(g),
                                                  ctypes.byref(it), ctypes.byref(err), ctypes.byref(E))
@@ -394,20 +398,26 @@ def gmm_cost(mx, cx, my, cy):
     return C
 
 
-def init_gmm(x, y, gx: dict, gy: dict, eps, inner_tol=1e-9, inner_max_iter=100000):
-    """GMM initializer (Sec. 3.3): K x K Bures-cost Sinkhorn at the same eps
-    (reading R-13), solved with Anderson acceleration (memory 5, reading R-29) -> f~;
-    f0_i = sum_k f~_k p_k(x_i) on the smaller side."""
+def gmm_dual(gx: dict, gy: dict, eps, inner_tol=1e-12, inner_max_iter=2000000):
+    """The K x K problem of the GMM initializer (Sec. 3.3, "regularized K x K OT problem",
+    Eq. 6 costs): plain log-domain Sinkhorn (O2, Alg. 1 with omega = 1) between the mixture
+    weights at the same eps (reading R-13), to inner_tol in fp64 -> f~, returned as the
+    representative with sum_k a_k f~_k = 0 (f~ is defined up to a constant, R-29)."""
+    C = gmm_cost(gx["means"], gx["covs"], gy["means"], gy["covs"])
+    a = _d(gx["weights"])
+    r = sinkhorn_matrix(C, eps, a=a, b=_d(gy["weights"]), tol=inner_tol, max_iter=inner_max_iter)
+    return r.f - (a * r.f).sum() / a.sum(), r
+
+
+def init_gmm(x, y, gx: dict, gy: dict, eps, inner_tol=1e-12, inner_max_iter=2000000):
+    """GMM initializer (Sec. 3.3): f~ of the K x K Bures-cost problem (gmm_dual:
+    plain Sinkhorn to inner_tol 1e-12, reading R-13); f0_i = sum_k f~_k p_k(x_i) on the
+    smaller side."""
     x, y = _pts(x), _pts(y)
     if x.shape[0] > y.shape[0]:
         f, _ = init_gmm(y, x, gy, gx, eps, inner_tol, inner_max_iter)
         return f, 1
-    C = gmm_cost(gx["means"], gx["covs"], gy["means"], gy["covs"])
-    a = _d(gx["weights"])
-    r = sinkhorn_matrix(C, eps, a=a, b=_d(gy["weights"]), tol=inner_tol, max_iter=inner_max_iter, anderson=5)
-    # (f~ is defined up to a constant and Anderson's mixing moves it along that line: the
-    # returned f~ is the representative with sum_k a_k f~_k = 0, R-29)
-    ft = r.f - (a * r.f).sum() / a.sum()
+    ft, _ = gmm_dual(gx, gy, eps, inner_tol, inner_max_iter)
     P = np.exp(gmm_log_resp(x, gx["weights"], gx["means"], gx["covs"]))
     return P @ ft, 0
 

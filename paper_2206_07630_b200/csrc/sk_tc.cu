@@ -419,7 +419,10 @@ __global__ void __launch_bounds__(64 + 32 * NE, 1) k_lse_tc2(TcArgs A) {
             // sum leaves [2^-100, 2^100]); unseeded: running max of t - sh_p
             float M = SEEDED ? 0.f : -INFINITY, S = 0.f;
             for (int i = 0; i < nt; ++i, ++g) {
-                if (G > 1 && g % G != grp) continue;
+                // tile group by the tile's index within the item (not the CTA's stream position):
+                // which group sums which tiles - and so the item's result - is a function of the
+                // item alone, whatever the launch's item schedule (bit-identity across world sizes)
+                if (G > 1 && i % G != grp) continue;
                 const int b = g & 1;
                 mbar_wait_sleep(&tfull[b], (g >> 1) & 1);
                 tc_fence_after();

@@ -362,6 +362,77 @@ def test_gmm_cost_and_init_properties(O):
     assert np.allclose(f, fp, atol=1e-9)
 
 
+def _tiny_cov_mixture(points, weights, var=1e-8):
+    d = points.shape[1]
+    return {"weights": np.asarray(weights, np.float64), "means": np.asarray(points, np.float64),
+            "covs": np.array([var * np.eye(d)] * len(points))}
+
+
+@pytest.mark.parametrize("n,m", [(6, 9), (9, 6)])
+def test_gmm_init_point_limit_is_the_point_cloud_potential(O, n, m):
+    """P:214: "in the limit where K -> n, n components with means (x_i)_i and zero covariance"
+    the GMM initializer recovers the original potential f*.  Components at the points with
+    covariance 1e-8 I (Bures cost 0, responsibilities one-hot) and the points' own weights: the
+    centred f^(0) equals the converged point-cloud potential of the oracle's Sinkhorn (on the
+    smaller side: f* for n <= m, g* otherwise).  Non-uniform weights and n != m, so a
+    transposed or side-swapped K x K problem, a sign error or a wrong eps fails."""
+    rng = np.random.default_rng(40 + n)
+    x = rng.uniform(-1, 1, (n, 2)).astype(np.float32)
+    y = (rng.uniform(-1, 1, (m, 2)) + 0.3).astype(np.float32)
+    a = rng.uniform(0.5, 1.5, n); a /= a.sum()
+    b = rng.uniform(0.5, 1.5, m); b /= b.sum()
+    eps = 0.3
+    f0, side = O.init_gmm(x, y, _tiny_cov_mixture(x, a), _tiny_cov_mixture(y, b), eps)
+    ref = O.sinkhorn(x, y, eps, a=a, b=b, tol=1e-13, max_iter=200000)
+    assert ref.converged
+    want = ref.f if n <= m else ref.g
+    assert side == (0 if n <= m else 1)
+    c = (f0 - f0.mean()) - (want - want.mean())
+    assert np.abs(c).max() <= 1e-6 * max(np.abs(want).max(), eps), np.abs(c).max()
+    # the same with a wrong eps, or the transposed problem, is far off (the pin discriminates)
+    f_bad, _ = O.init_gmm(x, y, _tiny_cov_mixture(x, a), _tiny_cov_mixture(y, b), 2 * eps)
+    assert np.abs((f_bad - f_bad.mean()) - (want - want.mean())).max() > 1e-3
+
+
+def test_gmm_init_separated_components_take_their_dual_value(O):
+    """Well-separated components with tiny covariances: every point's
+    responsibilities are one-hot at its own component, so f^(0)_i = f~_k(i), and f~ is the dual of
+    the discrete problem between the component means with weights (alpha, beta) (Bures cost 0 for
+    equal covariances, Eq. 6) - solved here as a point-cloud problem of the means."""
+    rng = np.random.default_rng(44)
+    mx = np.array([[0.0, 0.0], [6.0, 0.0], [0.0, 7.0]])
+    my = np.array([[1.0, 1.0], [5.0, 2.0], [2.0, 6.0], [7.0, 7.0]])
+    al = np.array([0.5, 0.3, 0.2]); be = np.array([0.1, 0.4, 0.3, 0.2])
+    lab = rng.integers(0, 3, 40)
+    x = (mx[lab] + 1e-4 * rng.standard_normal((40, 2))).astype(np.float32)
+    y = rng.standard_normal((60, 2)).astype(np.float32)
+    eps = 1.5
+    gx, gy = _tiny_cov_mixture(mx, al, 1e-6), _tiny_cov_mixture(my, be, 1e-6)
+    f0, side = O.init_gmm(x, y, gx, gy, eps)
+    ref = O.sinkhorn(mx.astype(np.float32), my.astype(np.float32), eps, a=al, b=be, tol=1e-13, max_iter=200000)
+    # the means are exact in fp32 here, so the point problem is the K x K problem
+    diff = f0 - ref.f[lab]
+    assert side == 0 and np.ptp(diff) <= 1e-7 * max(np.abs(ref.f).max(), eps), np.ptp(diff)
+
+
+def test_gmm_dual_plain_and_anderson_land_on_the_same_solution(O):
+    """The K x K problem's solution does not depend on the solver (R-29: the GPU's K11 solves it
+    with Anderson): plain Sinkhorn (the oracle, O2) and Anderson (memory 5) to 1e-12 give the same
+    gauge-fixed f~."""
+    rng = np.random.default_rng(45)
+    gx, gy = _mix(rng, 6, 3), _mix(rng, 5, 3)
+    ft, r = O.gmm_dual(gx, gy, 0.4)
+    assert r.converged and r.err < 1e-12
+    C = O.gmm_cost(gx["means"], gx["covs"], gy["means"], gy["covs"])
+    ra = O.sinkhorn_matrix(C, 0.4, a=gx["weights"], b=gy["weights"], tol=1e-12, max_iter=100000, anderson=5)
+    a = np.asarray(gx["weights"], np.float64)
+    fa = ra.f - (a * ra.f).sum() / a.sum()
+    assert ra.converged and ra.iterations < r.iterations
+    assert np.abs(fa - ft).max() <= 1e-7 * np.abs(ft).max()
+    with pytest.raises(ValueError):
+        O.sinkhorn_matrix(C, 0.4, a=gx["weights"], b=gy["weights"], anderson=17)
+
+
 # ------------------------------------------------------------------ Subsample
 def test_subsample_full_equals_solution(O):
     rng = np.random.default_rng(19)
