@@ -291,6 +291,11 @@ static int sinkhorn_anderson(const ora_prob *p, const double *a, const double *b
         }
         double sx = 0.0;
         for (int u = 0; u < cnt; ++u) sx += x[u];
+        /* degenerate least squares (R-30; SPEC "fall back to the plain update for that
+         * step"): a non-finite or zero sum, or a non-finite weight -> f <- f~ this sweep */
+        int degen = !isfinite(sx) || sx == 0.0;
+        for (int u = 0; u < cnt; ++u) degen |= !isfinite(x[u] / sx);
+        if (degen) { for (int64_t i = 0; i < n; ++i) f[i] = ft[i]; continue; }
         for (int64_t i = 0; i < n; ++i) {
             double v = 0.0;
             for (int u = 0; u < cnt; ++u) v += (x[u] / sx) * F[(int64_t)u * n + i];

@@ -93,6 +93,12 @@ __global__ void __launch_bounds__(32) k_and_decide(DevStatus *st, AndState *as, 
     if (lane >= cn) dl = 0.0;
     // the stop decision (every lane computes it; lane 0 writes)
     const int l = st->iter, l1 = l + 1;
+    if (!isfinite(et)) {
+        // T(f^l) became non-finite on some slice (rank): (f^l, g~ = g_sk(f^l)) is the last finite
+        // pair (a sharded row merge does not stop on its own slice's non-finite rows)
+        if (lane == 0) { st->err = (float)et; st->nonfinite = 1; st->final_iter = l; __threadfence(); st->stop = 1; }
+        return;
+    }
     bool stop = false;
     if (l1 % st->check_every == 0 || l1 >= st->max_iter) {
         if (lane == 0) st->err = (float)et;
@@ -154,7 +160,12 @@ __global__ void __launch_bounds__(32) k_and_decide(DevStatus *st, AndState *as, 
     const double xl = lane < cn ? rhs / diag : 0.0;
     double sx = xl;
     for (int o = 16; o > 0; o >>= 1) sx += __shfl_xor_sync(0xffffffffu, sx, o);
-    if (lane < kAndM) as->alpha[lane] = lane < cn ? xl / sx : 0.0;
+    // degenerate least squares (R-30): a non-finite or zero sum x, or a non-finite alpha, falls
+    // back to the plain update f^{l+1} = T(f^l) for this sweep (the history is kept)
+    double al = xl / sx;
+    const bool degen = !isfinite(sx) || sx == 0.0 || __any_sync(0xffffffffu, lane < cn && !isfinite(al));
+    if (degen) al = lane == head ? 1.0 : 0.0;
+    if (lane < kAndM) as->alpha[lane] = lane < cn ? al : 0.0;
     if (lane == 0) {
         as->head = (head + 1) % mem;
         as->cnt = cn;

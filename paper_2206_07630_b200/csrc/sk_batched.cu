@@ -441,7 +441,10 @@ __device__ __forceinline__ void solve_one(const BatchArgs &A, int prob, float *s
             double sx = xl;
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) sx += __shfl_xor_sync(0xffffffffu, sx, o);
-            const double al_l = xl / sx;
+            // degenerate least squares (R-30): fall back to the plain update T(f^l) for this sweep
+            double al_l = xl / sx;
+            if (!isfinite(sx) || sx == 0.0 || __any_sync(0xffffffffu, lane < cn && !isfinite(al_l)))
+                al_l = lane == a_head ? 1.0 : 0.0;
             double au[kAndMax];
 #pragma unroll
             for (int u = 0; u < kAndMax; ++u) au[u] = __shfl_sync(0xffffffffu, al_l, u);

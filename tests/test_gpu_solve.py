@@ -217,3 +217,31 @@ def test_onchip_cta_pair_variant_is_bit_identical(O, ctx):
         c.close()
     assert outs[0][2] == outs[1][2]
     assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+
+
+@pytest.mark.parametrize("entry", ["solve", "anderson", "onchip", "sharded2", "sharded2_anderson"])
+def test_nonfinite_potentials_are_reported(ctx, entry):
+    """Error contract (include/sinkhorn_b200.h): finite inputs whose squared norms
+    overflow fp32 make the potentials non-finite in the first sweep -> SK_ENONFINITE (never SK_OK
+    with a NaN error), and f, g hold the last finite iterate (here f^(0) = 0, g^(0) = 0)."""
+    import paper_2206_07630_b200 as sk
+    from paper_2206_07630_b200 import _lib
+    rng = np.random.default_rng(21)
+    n, m = (256, 256) if entry == "onchip" else (3000, 2500)
+    x = torch.from_numpy(rng.uniform(1e19, 2e19, (n, 1)).astype(np.float32)).cuda()
+    y = torch.from_numpy(rng.uniform(-2e19, -1e19, (m, 1)).astype(np.float32)).cuda()
+    kw = {"anderson": 5} if "anderson" in entry else {}
+    with pytest.raises(sk.SinkhornError) as ei:
+        if entry.startswith("sharded2"):
+            sk.sinkhorn_solve_sharded_emulated(ctx, 2, x, y, 1.0, mode="online", **kw)
+        elif entry == "onchip":
+            f = torch.full((2, n), 7.0, device="cuda")
+            g = torch.full((2, m), 7.0, device="cuda")
+            sk.sinkhorn_solve(ctx, torch.stack([x, x]), torch.stack([y, y]), 1.0, f=f, g=g)
+        else:
+            f = torch.full((1, n), 7.0, device="cuda")
+            g = torch.full((1, m), 7.0, device="cuda")
+            sk.sinkhorn_solve(ctx, x, y, 1.0, mode="online", f=f, g=g, **kw)
+    assert ei.value.status == _lib.SK_ENONFINITE, str(ei.value)
+    if not entry.startswith("sharded2"):
+        assert bool(torch.isfinite(f).all()) and bool(torch.isfinite(g).all())
