@@ -126,11 +126,11 @@ class C2(Workload):
     def config(self):
         return c2_config(self.world)
 
-    def _run(self, x, y, init=True, anderson=0):
+    def _run(self, x, y, init=True, anderson=None, adaptive=None):
         sk, p = self.sk, self.p
         f0 = sk.sinkhorn_init_sort1d(self.ctx, x.view(self.B, self.n), y.view(self.m), y_shared=True) if init else None
         self.f, self.g, reps = sk.sinkhorn_solve(self.ctx, x, y, p.eps, tol=p.tol, max_iter=p.max_iter,
-                                                 y_shared=True, f_init=f0, anderson=anderson)
+                                                 y_shared=True, f_init=f0, anderson=anderson, adaptive=adaptive)
         self.its = np.array([r["iterations"] for r in reps])
         return float(self.n) * self.m * float(self.its.sum())
 
@@ -180,6 +180,17 @@ class C2(Workload):
         out["anderson5"] = {"time_to_tol_ms": ms, "iterations_mean": float(self.its.mean()),
                             "iterations_max": int(self.its.max()), "cost_entries_per_s": ent / (ms / 1e3),
                             "note": "sort1d init + Anderson (memory 5) to the same tol; entries = n m sweeps"}
+        # NEXT-1: adaptive momentum (window 10; R-31)
+        self._run(self.x, self.y, adaptive=10)
+        e0.record(st)
+        for _ in range(3):
+            ent = self._run(self.x, self.y, adaptive=10)
+        e1.record(st)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / 3
+        out["adaptive10"] = {"time_to_tol_ms": ms, "iterations_mean": float(self.its.mean()),
+                             "iterations_max": int(self.its.max()), "cost_entries_per_s": ent / (ms / 1e3),
+                             "note": "sort1d init + adaptive momentum (window 10) to the same tol"}
         return out
 
     kernel = "k_batched<1,2,512> (on-chip persistent solver, K13)"
@@ -311,7 +322,7 @@ class Single(Workload):
             f0 = None
         return f0
 
-    def _run(self, x, y, init=True, anderson=0):
+    def _run(self, x, y, init=True, anderson=None, adaptive=None):
         import torch
         sk, p = self.sk, self.p
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
@@ -325,7 +336,7 @@ class Single(Workload):
                                                   max_iter=p.max_iter, mode=self.mode, f_init_local=f0l)
         else:
             _, _, rep = sk.sinkhorn_solve(self.ctx, x, y, p.eps, tol=p.tol, max_iter=p.max_iter, mode=self.mode,
-                                          f_init=f0, anderson=anderson)
+                                          f_init=f0, anderson=anderson, adaptive=adaptive)
         ev[2].record()
         ev[2].synchronize()
         self.split_ms = {"init_ms": ev[0].elapsed_time(ev[1]), "solve_call_ms": ev[1].elapsed_time(ev[2]),
@@ -370,6 +381,18 @@ class Single(Workload):
                                 "converged": self.rep["converged"], "cost_entries_per_s": ent * self.world / (ms / 1e3),
                                 "solve_ms": self.rep["solve_ms"],
                                 "note": "same init + Anderson (memory 5) to the same tol (K13 / K19)"}
+            # adaptive momentum (window 10; R-31), same step
+            self._run(self.x, self.y, adaptive=10)
+            e0.record()
+            for _ in range(reps):
+                ent = self._run(self.x, self.y, adaptive=10)
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / reps
+            out["adaptive10"] = {"time_to_tol_ms": ms, "iterations": self.rep["iterations"],
+                                 "converged": self.rep["converged"],
+                                 "cost_entries_per_s": ent * self.world / (ms / 1e3),
+                                 "note": "same init + adaptive momentum (window 10) to the same tol"}
         return out
 
     def cpu_sample(self, target_s=10.0):

@@ -139,11 +139,25 @@ sk_status sk_set_eps_decay(sk_ctx *ctx, float init, float rate);
  * over the ranks: one ncclAllReduce of 9 doubles per sweep); omega != 1 and eps-decay return
  * SK_EUNSUPPORTED. */
 sk_status sk_set_anderson(sk_ctx *ctx, int32_t mem);
+/* Adaptive momentum ("adaptive momentum", "adapt=10, meaning adaptation is
+ * recomputed after 10 iterations"; R-31 after SPEC S:178) for the following
+ * solves on this context, window T = adapt_iters: the solve starts plain (omega = 1); whenever a
+ * window ends at sweep l = kT with k >= 2, the per-sweep contraction of the L1 marginal error
+ * over the window, rho = (err_l / err_{l-T})^(1/T), sets omega = 2 / (1 + sqrt(max(0, 1 - rho)))
+ * clipped to [1, 1.95], which Alg. 1's relaxed updates (as sk_set_relaxation) use from sweep
+ * l + 2 on (the fused error of sweep l is known during sweep l + 1); a non-finite ratio keeps
+ * omega.  err_l is evaluated at every window end whatever check_every is.  adapt_iters = 0: off
+ * (the default); < 0: SK_EINVAL.  Runs on the on-chip solver (per problem) and the multi-kernel
+ * solvers (omega lives on the device: no host round trip), sharded included (the row terms summed
+ * over the ranks as for a fixed omega; the stored path runs its separate row / column passes);
+ * a fixed omega != 1, Anderson and eps-decay return SK_EUNSUPPORTED with it. */
+sk_status sk_set_adaptive_momentum(sk_ctx *ctx, int32_t adapt_iters);
 /* The solver options currently set on this context (each output nullable, host): omega
- * (sk_set_relaxation), the eps-decay (init, rate) (init 0 = off) and the Anderson memory (0 =
- * off).  Lets a caller change an option for one solve and restore the previous setting. */
+ * (sk_set_relaxation), the eps-decay (init, rate) (init 0 = off), the Anderson memory (0 = off)
+ * and the adaptive-momentum window (0 = off).  Lets a caller change an option for one solve and
+ * restore the previous setting. */
 sk_status sk_get_solver_options(const sk_ctx *ctx, float *omega, float *decay_init, float *decay_rate,
-                                int32_t *anderson);
+                                int32_t *anderson, int32_t *adapt_iters);
 /* Diagnostics / tuning of kernel variants (DESIGN.md section 6 measures each): key = value for the
  * following calls on this context.  None changes what is computed beyond fp32 rounding; each
  * selects a kernel variant or a balance of the exponential between MUFU and the FMA pipe:

@@ -58,6 +58,9 @@ def _L():
         lib.ora_sinkhorn_points_omega.argtypes = [I64, I64, I, P, P, P, P, D, D, D, I, I, P, P, P, P, P, P, P]
         lib.ora_sinkhorn_points_decay.restype = I
         lib.ora_sinkhorn_points_decay.argtypes = [I64, I64, I, P, P, P, P, D, D, D, D, D, I, I, P, P, P, P, P, P, P]
+        lib.ora_sinkhorn_points_adaptive.restype = I
+        lib.ora_sinkhorn_points_adaptive.argtypes = [I64, I64, I, P, P, P, P, D, D, I, D, I, I, P, P, P, P, P, P,
+                                                     P, P]
         lib.ora_sinkhorn_matrix_anderson.restype = I
         lib.ora_sinkhorn_matrix_anderson.argtypes = [I64, I64, P, P, P, D, I, D, I, I, P, P, P, P, P, P]
         lib.ora_sinkhorn_points_anderson.restype = I
@@ -150,6 +153,31 @@ def sinkhorn(x, y, eps, a=None, b=None, tol=1e-3, max_iter=10000, check_every=1,
     if trace:
         r["trace"] = tr[: it.value]
     return r
+
+
+def sinkhorn_adaptive(x, y, eps, adapt_iters=10, a=None, b=None, tol=1e-3, max_iter=10000, check_every=1,
+                      f0=None, g0=None, omega=1.0) -> Result:
+    """Alg. 1 with adaptive momentum ("adapt=10"; reading R-31): plain sweeps, then
+    after every window of adapt_iters sweeps (from the second on) omega = 2/(1 + sqrt(1 - rho))
+    (clipped to [1, 1.95]) from the window's per-sweep error contraction rho, applied from two
+    sweeps later.  adapt_iters = 0: the fixed-omega solver with an optional starting g0.
+    Returns the Result of sinkhorn() plus r.omega: the omega of every sweep."""
+    x, y = _pts(x), _pts(y)
+    n, m, d = x.shape[0], y.shape[0], x.shape[1]
+    a, b = _weights(a, n), _weights(b, m)
+    f, g = np.empty(n), np.empty(m)
+    it, err, E = ctypes.c_int(), ctypes.c_double(), ctypes.c_double()
+    f0a = None if f0 is None else _d(f0)
+    g0a = None if g0 is None else _d(g0)
+    om = np.empty(max_iter)
+    conv = _L().ora_sinkhorn_points_adaptive(n, m, d, _p(x), _p(y), _p(a), _p(b), float(eps), float(omega),
+                                             int(adapt_iters), float(tol), int(max_iter), int(check_every), _p(f0a),
+                                             _p(g0a), _p(f), _p(g), ctypes.byref(it), ctypes.byref(err),
+                                             ctypes.byref(E), _p(om))
+    if conv < 0:
+        raise ValueError("adapt_iters must be >= 0")
+    return Result(f=f, g=g, iterations=it.value, converged=bool(conv), err=err.value, E=E.value,
+                  omega=om[: it.value])
 
 
 def sinkhorn_anderson(x, y, eps, mem=5, a=None, b=None, tol=1e-3, max_iter=10000, check_every=1, f0=None) -> Result:

@@ -187,6 +187,26 @@ static double omega_g = 1.0;   /* the current call's omega (set by the public en
  * for both of its updates; the T sweeps with eps_l > eps are not checked, the stop rule runs on
  * the sweeps l > T with (l - T) % check_every == 0.  decay_init = 0: off. */
 static double decay_init_g = 0.0, decay_rate_g = 1.0;
+/* Adaptive momentum ("adaptive momentum (adapt=10, meaning adaptation is recomputed after 10
+ * iterations)"; reading R-31 after SPEC S:178): with window T = adapt_g > 0 the
+ * solve starts plain (omega = 1); after sweep l = kT (k >= 2) the per-sweep contraction of the
+ * explicit L1 error over the last window, rho = (err_l / err_{l-T})^(1/T), gives
+ * omega = 2 / (1 + sqrt(max(0, 1 - rho))) clipped to [1, 1.95], used from sweep l + 2 on (the
+ * fused error of sweep l is known during sweep l + 1).  A non-finite ratio keeps omega.
+ * g0 (nullable) starts g (the relaxed g-update reads it); omega_out (nullable, max_iter entries)
+ * receives the omega of every sweep. */
+static int adapt_g = 0;
+static const double *g0_g = NULL;
+static double *omega_out_g = NULL;
+
+static double adaptive_omega(double ratio, int T, double cur) {
+    if (!isfinite(ratio) || ratio < 0.0) return cur;
+    const double rho = pow(ratio, 1.0 / (double)T);
+    double w = 2.0 / (1.0 + sqrt(fmax(0.0, 1.0 - rho)));
+    if (!(w >= 1.0)) w = 1.0;
+    if (w > 1.95) w = 1.95;
+    return w;
+}
 
 static void relax(int64_t k, double *v, const double *vsk, double omega) {
     if (omega == 1.0) { for (int64_t i = 0; i < k; ++i) v[i] = vsk[i]; return; }
@@ -203,14 +223,18 @@ static int sinkhorn(const ora_prob *p, const double *a, const double *b, double 
                     double tol, int max_iter, int check_every, const double *f0,
                     double *f, double *g, int *iters, double *err, double *E, double *trace) {
     for (int64_t i = 0; i < p->n; ++i) f[i] = f0 ? f0[i] : 0.0;
-    for (int64_t j = 0; j < p->m; ++j) g[j] = 0.0;
-    const double omega = omega_g;
+    for (int64_t j = 0; j < p->m; ++j) g[j] = g0_g ? g0_g[j] : 0.0;
+    const int adapt = adapt_g;
+    double omega = adapt ? 1.0 : omega_g, omega_sched = omega, err_win = 0.0;
+    int sched_at = -1;
     double *gs = (double *)malloc(sizeof(double) * (size_t)p->m);
     double *fs = (double *)malloc(sizeof(double) * (size_t)p->n);
     int l = 0, converged = 0, T = 0;
     double e = INFINITY;
     while (l < max_iter) {
         ++l;
+        if (l == sched_at) omega = omega_sched;
+        if (omega_out_g) omega_out_g[l - 1] = omega;
         double el = eps;
         if (decay_init_g > 0.0) {
             const double v = eps * decay_init_g * pow(decay_rate_g, (double)(l - 1));
@@ -221,9 +245,16 @@ static int sinkhorn(const ora_prob *p, const double *a, const double *b, double 
         f_update(p, a, g, el, fs, NULL, 0);
         relax(p->n, f, fs, omega);
         if (trace) trace[l - 1] = dual_objective(p, a, b, f, g, eps);
+        int have_e = 0;
         if (tol > 0.0 && l > T && (l - T) % check_every == 0) {
             e = marginal_error(p, a, b, f, g, eps);
+            have_e = 1;
             if (e < tol) { converged = 1; break; }
+        }
+        if (adapt && l % adapt == 0) {   /* the end of a window: err_l against err_{l-T} */
+            const double en = have_e ? e : marginal_error(p, a, b, f, g, eps);
+            if (l >= 2 * adapt) { omega_sched = adaptive_omega(en / err_win, adapt, omega); sched_at = l + 2; }
+            err_win = en;
         }
     }
     if (!converged) e = marginal_error(p, a, b, f, g, eps);
@@ -336,6 +367,25 @@ int ora_sinkhorn_points_omega(int64_t n, int64_t m, int d, const double *x, cons
     omega_g = omega;
     int r = sinkhorn(&p, a, b, eps, tol, max_iter, check_every, f0, f, g, iters, err, E, trace);
     omega_g = 1.0;
+    return r;
+}
+
+/* ... with adaptive momentum (R-31) and an optional starting g. */
+int ora_sinkhorn_points_adaptive(int64_t n, int64_t m, int d, const double *x, const double *y,
+                                 const double *a, const double *b, double eps, double omega, int adapt_iters,
+                                 double tol, int max_iter, int check_every, const double *f0, const double *g0,
+                                 double *f, double *g, int *iters, double *err, double *E, double *omega_out) {
+    if (adapt_iters < 0) return -1;
+    ora_prob p = {n, m, d, x, y, NULL};
+    omega_g = omega;
+    adapt_g = adapt_iters;
+    g0_g = g0;
+    omega_out_g = omega_out;
+    int r = sinkhorn(&p, a, b, eps, tol, max_iter, check_every, f0, f, g, iters, err, E, NULL);
+    omega_g = 1.0;
+    adapt_g = 0;
+    g0_g = NULL;
+    omega_out_g = NULL;
     return r;
 }
 

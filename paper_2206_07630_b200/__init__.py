@@ -90,10 +90,11 @@ class Context:
         self.check(self.lib.sk_set_force_nccl(self.h, int(on)))
 
     def solver_options(self) -> dict:
-        om, di, dr, am = ctypes.c_float(), ctypes.c_float(), ctypes.c_float(), ctypes.c_int32()
+        om, di, dr = ctypes.c_float(), ctypes.c_float(), ctypes.c_float()
+        am, ad = ctypes.c_int32(), ctypes.c_int32()
         self.check(self.lib.sk_get_solver_options(self.h, ctypes.byref(om), ctypes.byref(di), ctypes.byref(dr),
-                                                  ctypes.byref(am)))
-        return {"omega": om.value, "eps_decay": (di.value, dr.value), "anderson": am.value}
+                                                  ctypes.byref(am), ctypes.byref(ad)))
+        return {"omega": om.value, "eps_decay": (di.value, dr.value), "anderson": am.value, "adaptive": ad.value}
 
     def nccl_unique_id(self) -> bytes:
         buf = ctypes.create_string_buffer(128)
@@ -118,10 +119,10 @@ class Context:
 
 # ------------------------------------------------------------------ marshalling
 @contextlib.contextmanager
-def _solver_options(ctx: Context, omega=None, eps_decay=None, anderson=None):
+def _solver_options(ctx: Context, omega=None, eps_decay=None, anderson=None, adaptive=None):
     """Set the given solver options on the context for one call, then restore the previous
     settings (None leaves an option as the context has it)."""
-    if omega is None and eps_decay is None and anderson is None:
+    if omega is None and eps_decay is None and anderson is None and adaptive is None:
         yield
         return
     prev = ctx.solver_options()
@@ -132,11 +133,14 @@ def _solver_options(ctx: Context, omega=None, eps_decay=None, anderson=None):
             ctx.check(ctx.lib.sk_set_eps_decay(ctx.h, ctypes.c_float(eps_decay[0]), ctypes.c_float(eps_decay[1])))
         if anderson is not None:
             ctx.check(ctx.lib.sk_set_anderson(ctx.h, int(anderson)))
+        if adaptive is not None:
+            ctx.check(ctx.lib.sk_set_adaptive_momentum(ctx.h, int(adaptive)))
         yield
     finally:
         ctx.lib.sk_set_relaxation(ctx.h, ctypes.c_float(prev["omega"]))
         ctx.lib.sk_set_eps_decay(ctx.h, ctypes.c_float(prev["eps_decay"][0]), ctypes.c_float(prev["eps_decay"][1]))
         ctx.lib.sk_set_anderson(ctx.h, int(prev["anderson"]))
+        ctx.lib.sk_set_adaptive_momentum(ctx.h, int(prev["adaptive"]))
 
 def _ptr(t: Optional[torch.Tensor], dtype=torch.float32):
     if t is None:
@@ -234,15 +238,17 @@ def sinkhorn_init_subsample(ctx: Context, x, y, idx_x, idx_y, eps: float, inner_
 def sinkhorn_solve(ctx: Context, x, y, eps: float, tol: float = 1e-3, max_iter: int = 10000,
                    check_every: int = 1, a=None, b=None, y_shared: bool = False, mode: str = "auto",
                    f_init=None, g_init=None, f=None, g=None, allow_nonfinite: bool = False,
-                   omega: Optional[float] = None, eps_decay=None, anderson: Optional[int] = None):
+                   omega: Optional[float] = None, eps_decay=None, anderson: Optional[int] = None,
+                   adaptive: Optional[int] = None):
     """Solve B >= 1 problems.  x: (n, d) or (B, n, d); y: (m, d) [shared] or (B, m, d).
     omega: Alg. 1's relaxation (sk_set_relaxation; 1 = plain Sinkhorn).
     eps_decay: (init, rate) for sk_set_eps_decay (e.g. (5, 0.8), P:491; (0, 1) = off).
     anderson: Anderson memory for sk_set_anderson (e.g. 5), 0 = off.
+    adaptive: adaptive-momentum window for sk_set_adaptive_momentum (e.g. 10), 0 = off.
     Each option given applies to this call only (the context's previous setting is restored);
     None uses the context's setting (default: plain Sinkhorn).
     Returns (f, g, reports) with f (B, n) / g (B, m) (B dropped for a single problem)."""
-    with _solver_options(ctx, omega, eps_decay, anderson):
+    with _solver_options(ctx, omega, eps_decay, anderson, adaptive):
         return _solve(ctx, x, y, eps, tol, max_iter, check_every, a, b, y_shared, mode, f_init, g_init, f, g,
                       allow_nonfinite)
 
@@ -338,10 +344,10 @@ def sinkhorn_soft_rank_sort(ctx: Context, x, y, eps: float, f, g, z=None,
 def sinkhorn_solve_sharded_emulated(ctx: Context, world: int, x, y, eps: float, tol: float = 1e-3,
                                     max_iter: int = 10000, check_every: int = 1, a=None, b=None,
                                     mode: str = "auto", f_init=None, anderson: Optional[int] = None,
-                                    omega: Optional[float] = None, eps_decay=None):
+                                    omega: Optional[float] = None, eps_decay=None, adaptive: Optional[int] = None):
     """The row-sharded algorithm for `world` virtual ranks on one GPU (test entry).
-    anderson / omega / eps_decay: as sinkhorn_solve (this call only; None = the context's)."""
-    with _solver_options(ctx, omega, eps_decay, anderson):
+    anderson / omega / eps_decay / adaptive: as sinkhorn_solve (this call only; None = the context's)."""
+    with _solver_options(ctx, omega, eps_decay, anderson, adaptive):
         return _solve_sharded_emulated(ctx, world, x, y, eps, tol, max_iter, check_every, a, b, mode, f_init)
 
 
@@ -360,12 +366,14 @@ def _solve_sharded_emulated(ctx, world, x, y, eps, tol, max_iter, check_every, a
 def sinkhorn_solve_sharded(ctx: Context, n_total: int, row0: int, x_local, y, eps: float,
                            tol: float = 1e-3, max_iter: int = 10000, check_every: int = 1,
                            a_local=None, b=None, mode: str = "auto", f_init_local=None,
-                           anderson: Optional[int] = None, omega: Optional[float] = None, eps_decay=None):
+                           anderson: Optional[int] = None, omega: Optional[float] = None, eps_decay=None,
+                           adaptive: Optional[int] = None):
     """Rows [row0, row0 + n_local) of an n_total-row problem on this rank (sk_comm_init first);
     anderson: Anderson memory (sk_set_anderson; one 9-double allreduce per sweep), 0 = off;
     omega: relaxation (sk_set_relaxation; one 2-double allreduce of the row terms per sweep);
-    eps_decay: (init, rate).  Each applies to this call only (None = the context's setting)."""
-    with _solver_options(ctx, omega, eps_decay, anderson):
+    eps_decay: (init, rate); adaptive: the adaptive-momentum window.  Each applies to this call only
+    (None = the context's setting)."""
+    with _solver_options(ctx, omega, eps_decay, anderson, adaptive):
         return _solve_sharded(ctx, n_total, row0, x_local, y, eps, tol, max_iter, check_every, a_local, b, mode,
                               f_init_local)
 

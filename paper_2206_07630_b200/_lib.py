@@ -40,6 +40,7 @@ class SkCounters(ctypes.Structure):
 EXPORTS = [
     "sk_create", "sk_set_stream", "sk_destroy", "sk_last_error", "sk_status_string", "sk_version",
     "sk_set_timing", "sk_set_relaxation", "sk_set_eps_decay", "sk_set_anderson", "sk_get_solver_options",
+    "sk_set_adaptive_momentum",
     "sk_set_tuning", "sk_set_force_nccl", "sk_get_counters", "sk_reset_counters", "sk_nccl_unique_id", "sk_comm_init",
     "sk_shard_rows", "sinkhorn_sort1d_batched", "sinkhorn_soft_rank_sort", "sinkhorn_fit_gmm", "sinkhorn_vjp", "sinkhorn_init_nw1d", "sinkhorn_init_zero", "sinkhorn_init_sort1d",
     "sinkhorn_init_gaussian", "sinkhorn_init_gmm", "sinkhorn_init_subsample", "sinkhorn_solve",
@@ -72,7 +73,8 @@ def load() -> ctypes.CDLL:
         "sk_set_eps_decay": (S, [P, F, F]),
         "sk_set_anderson": (S, [P, I32]),
         "sk_get_solver_options": (S, [P, ctypes.POINTER(F), ctypes.POINTER(F), ctypes.POINTER(F),
-                                      ctypes.POINTER(I32)]),
+                                      ctypes.POINTER(I32), ctypes.POINTER(I32)]),
+        "sk_set_adaptive_momentum": (S, [P, I32]),
         "sk_set_tuning": (S, [P, ctypes.c_char_p, D]),
         "sk_set_force_nccl": (S, [P, I32]),
         "sk_get_counters": (S, [P, ctypes.POINTER(SkCounters)]),

@@ -76,6 +76,7 @@ struct sk_ctx {
     float omega = 1.f;              // Alg. 1's relaxation for the following solves
     float decay_init = 0.f, decay_rate = 1.f;   // eps-decay for the following solves (R-25)
     int anderson = 0;               // Anderson memory for the following solves (R-27; 0: off)
+    int adapt = 0;                  // adaptive momentum window (R-31; 0: off)
     int force_nccl = 0;             // sk_set_force_nccl: a 1-rank communicator takes the NCCL path
     // diagnostics / tuning (sk_set_tuning): kernel variants and balances measured in DESIGN.md
     struct Tuning {
@@ -328,6 +329,11 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
     const int amem = ctx->anderson >= 2 ? ctx->anderson : 0;
     if (amem && P.omega != 1.f)
         return fail(ctx, SK_EUNSUPPORTED, "Anderson acceleration needs omega = 1");
+    // adaptive momentum (R-31): starts plain, the merges read omega from the device status
+    const int adapt = ctx->adapt;
+    if (adapt && (amem || P.omega != 1.f))
+        return fail(ctx, SK_EUNSUPPORTED, "adaptive momentum combines with neither Anderson nor a fixed omega");
+    const bool rterms = adapt || P.omega != 1.f;   // relaxed row terms of err and E
     const long long m = P.m, n_glob = P.n_total;
     const int ns = (int)slices.size();
     long long n_max = 0, n_sum = 0;
@@ -405,7 +411,7 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
     Side Y{(int)m, P.d, D, tq, ypack, yc, ynk, {ypot, ypot + m}};
     // online FFMA path: per-point LSE seeds for the max-free (seeded) passes from sweep 3 on
     // stored mode with the fused sweep (one persistent CTA per SM): 8 blocks x split_q = one wave
-    const bool fused = stored && T.fused != 0 && stored_fused_supported(m) && P.omega == 1.f && !amem;
+    const bool fused = stored && T.fused != 0 && stored_fused_supported(m) && P.omega == 1.f && !amem && !adapt;
     const bool seedable = !stored;
     if (tc) {   // the seeded passes' exact fallback reads the caller's coordinates
         for (int i = 0; i < ns; ++i) { X[i].raw = slices[i].x; X[i].tcimg = (unsigned char *)ximg + offi[i]; X[i].tc_c = tc_fold_c(); }
@@ -475,7 +481,7 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
         ctx->cnt.kernel_launches += ns + 1;
     }
     const float tc_margin = T.tc_margin;
-    CU(launch_status_init(status, P.max_iter, P.check_every, P.tol, st, amem ? 1 : 0));
+    CU(launch_status_init(status, P.max_iter, P.check_every, P.tol, st, amem ? 1 : 0, adapt ? 1.f : P.omega));
     ctx->cnt.kernel_launches += ns + 2;
     float *andfr = nullptr;     // per slice i: F at 2 mem off[i], R at F + mem n_i
     double *andblk = nullptr, *andvec = nullptr;
@@ -519,6 +525,7 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
     MergePass mcol{MERGE_COL, &Y, stored ? part : xchg, stored ? nsplit_col : nblk_x, P.eps, P.b, status, blke,
                    blkb, nullptr, 0.f, sharded ? 1 : 0, 0};
     mcol.omega = P.omega;
+    mcol.adapt = adapt;
     mcol.anderson = amem ? 1 : 0;
     int sweep = 0;   // sweeps enqueued so far (seeded passes from the third on)
 
@@ -652,6 +659,7 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
                                blkb, nullptr, 0.f, sharded ? 1 : 0, i + 1 < ns ? 1 : 0};
                 if (row_seed) mrow.Q = &Y;
                 mrow.omega = P.omega;
+                mrow.adapt = adapt;
                 mrow.accum = i > 0 ? 1 : 0;
                 mrow.wts = slices[i].a;   // (the relaxed row error term weighs rows by a)
                 mrow.n_uniform = n_glob;  //  uniform: 1 / n_total (a slice holds part of the rows)
@@ -667,7 +675,7 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
                     launched += 2;
                 }
             }
-            if (P.omega != 1.f && P.nccl && sharded) {   // relaxed: the row terms of err and E over the ranks
+            if (rterms && P.nccl && sharded) {   // relaxed: the row terms of err and E over the ranks
                 int r = g_nccl.allreduce(&status->row_err, &status->row_err, 2, kNcclFloat64, kNcclSum, ctx->comm, st);
                 if (r != 0) return fail(ctx, SK_ENCCL, "ncclAllReduce(row terms) failed");
             }
@@ -718,18 +726,18 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
     for (int b = 0; b < SK_SHARD_BLOCKS; ++b) E += fa_h[b];
     E += gb_part;
     // relaxed: after the f-update sum_ij P_ij = sum(a) + mass_dev (kept by the last row merge)
-    if (P.omega != 1.f) E -= (double)P.eps * hs.mass_dev;
+    if (rterms) E -= (double)P.eps * hs.mass_dev;
     for (int i = 0; i < ns; ++i)
         CU(cudaMemcpyAsync(slices[i].f, X[i].pot[L & 1], sizeof(float) * slices[i].n, cudaMemcpyDeviceToDevice, st));
     // (Anderson: the pair is (f^L, g_sk(f^L)), g one buffer ahead; L + 1 sweeps were evaluated)
-    CU(cudaMemcpyAsync(P.g, Y.pot[(L + (amem ? 1 : 0)) & 1], sizeof(float) * m, cudaMemcpyDeviceToDevice, st));
+    CU(cudaMemcpyAsync(P.g, Y.pot[(L + hs.g_off) & 1], sizeof(float) * m, cudaMemcpyDeviceToDevice, st));
     ctx->cnt.kernel_launches += launched;
     ctx->cnt.lse_launches += (long long)(ns + 1) * (hs.iter + 1);
     if (ctx->timing) ctx->cnt.lse_ms += ms;
     const double entries = (double)n_sum * m * (amem ? 2.0 * (L + 1) : 2.0 * L + 1.0);
     ctx->cnt.lse_ex2 += entries;
     if (stored) ctx->cnt.lse_bytes += 4.0 * (double)n_sum * m * (fused ? (1.0 + hs.iter) : (2.0 * L + 1.0));
-    rep->iterations = amem ? L + 1 : L;
+    rep->iterations = L + hs.g_off;   // (Anderson: the sweeps evaluated)
     rep->converged = hs.converged;
     rep->marginal_error = hs.err;
     rep->dual_objective = E;
@@ -746,6 +754,7 @@ sk_status solve_core_decay(sk_ctx *ctx, const Problem &P, std::vector<Slice> &sl
     if (ctx->decay_init <= 0.f) return solve_core(ctx, P, slices, rep);
     if (P.omega != 1.f) return fail(ctx, SK_EUNSUPPORTED, "eps-decay with omega != 1 runs on the on-chip solver only");
     if (ctx->anderson >= 2) return fail(ctx, SK_EUNSUPPORTED, "Anderson acceleration does not combine with eps-decay");
+    if (ctx->adapt) return fail(ctx, SK_EUNSUPPORTED, "adaptive momentum does not combine with eps-decay");
     int T = 0;
     while (T < P.max_iter && (double)P.eps * ctx->decay_init * std::pow((double)ctx->decay_rate, T) > (double)P.eps) ++T;
     if (P.max_iter - T < 1) return fail(ctx, SK_EINVAL, "max_iter must exceed the %d eps-decay sweeps", T);
@@ -851,12 +860,21 @@ sk_status sk_set_force_nccl(sk_ctx *ctx, int32_t enable) {
 }
 
 sk_status sk_get_solver_options(const sk_ctx *ctx, float *omega, float *decay_init, float *decay_rate,
-                                int32_t *anderson) {
+                                int32_t *anderson, int32_t *adapt_iters) {
     if (!ctx) return SK_EINVAL;
     if (omega) *omega = ctx->omega;
     if (decay_init) *decay_init = ctx->decay_init;
     if (decay_rate) *decay_rate = ctx->decay_rate;
     if (anderson) *anderson = ctx->anderson;
+    if (adapt_iters) *adapt_iters = ctx->adapt;
+    return SK_OK;
+}
+
+sk_status sk_set_adaptive_momentum(sk_ctx *ctx, int32_t adapt_iters) {
+    if (!ctx) return SK_EINVAL;
+    if (adapt_iters < 0 || adapt_iters > 100000)
+        return fail(ctx, SK_EINVAL, "adapt_iters must lie in [0, 100000], got %d", (int)adapt_iters);
+    ctx->adapt = adapt_iters;
     return SK_OK;
 }
 
@@ -1367,6 +1385,8 @@ sk_status solve_impl(sk_ctx *ctx, int64_t B, int64_t n, int64_t m, int32_t d, co
                        (B > 1 || (double)n * m <= (double)(1 << 18));
     if (ctx->anderson >= 2 && (ctx->omega != 1.f || ctx->decay_init > 0.f))
         return fail(ctx, SK_EUNSUPPORTED, "Anderson acceleration combines with neither omega != 1 nor eps-decay");
+    if (ctx->adapt && (ctx->anderson >= 2 || ctx->omega != 1.f || ctx->decay_init > 0.f))
+        return fail(ctx, SK_EUNSUPPORTED, "adaptive momentum combines with neither Anderson, a fixed omega nor eps-decay");
     if (small && mode != SK_COST_STORED) {
         ENSURE(rp, char, B_REP, (size_t)B * (3 * sizeof(int) + sizeof(float) + sizeof(double)) + 64);
         ENSURE(queue, int, B_QUEUE, 4);
@@ -1383,6 +1403,7 @@ sk_status solve_impl(sk_ctx *ctx, int64_t B, int64_t n, int64_t m, int32_t d, co
         L.omega = ctx->omega;
         L.decay_init = ctx->decay_init; L.decay_rate = ctx->decay_rate;
         L.anderson = ctx->anderson;
+        L.adapt = ctx->adapt;
         L.shape = ctx->tune.batched_shape;
         L.cl = ctx->tune.batched_cl;
         CU(cudaEventRecord(ctx->ev0, st));

@@ -38,6 +38,7 @@ struct BatchArgs {
     float omega;                    // Alg. 1's relaxation (1 = plain Sinkhorn)
     float decay_init, decay_rate;   // eps-decay (decay_init <= 0: off)
     int anderson;                   // Anderson memory (R-27; < 2: off)
+    int adapt;                      // adaptive momentum window T (R-31; 0: off)
 };
 
 __host__ __device__ inline int round_up(int v, int a) { return (v + a - 1) / a * a; }
@@ -281,8 +282,10 @@ __device__ __forceinline__ void solve_one(const BatchArgs &A, int prob, float *s
     int a_cnt = 0, a_head = 0;   // Anderson history: filled slots, next slot
     bool out_gtilde = false;     // Anderson: the result is (f^l, g_sk(f^l)) (the g buffer not flipped)
     float err = INFINITY;
-    const float om = A.omega;
-    const bool relaxed = om != 1.f;
+    // adaptive momentum (R-31): plain until the second window's error, then omega from each
+    // window's contraction, applied two sweeps after the window's last sweep
+    float om = A.adapt > 0 ? 1.f : A.omega, om_next = om, err_win = 0.f;
+    const bool relaxed = A.adapt > 0 || om != 1.f;
     double row_err = 0.0, mass_dev = 0.0;   // relaxed: row term of err_l and sum P - sum a
     // eps-decay (R-25): sweep l + 1 uses max(eps, eps init rate^l); the T decay sweeps
     // are not checked; the constants that carry eps are refreshed when it changes
@@ -323,6 +326,7 @@ __device__ __forceinline__ void solve_one(const BatchArgs &A, int prob, float *s
         const bool seeded = l >= 1 && fresh;
         // ---- column pass: g^{l+1} (P = y, Q = x)
         const bool check = !am && l > T && ((l - T) % A.check_every == 0 || l == A.max_iter);
+        const bool chk_ad = A.adapt > 0 && l >= 1 && l % A.adapt == 0;   // err_l ends a window
         double e_loc = 0.0;
         int bad = 0;
         float *gold = gb + cur * m, *gnew = gb + (cur ^ 1) * m;
@@ -336,7 +340,7 @@ __device__ __forceinline__ void solve_one(const BatchArgs &A, int prob, float *s
             rput(&gnew[j], gn);
             rput(&wy[j], wv);
             bad |= !isfinite(gn);
-            if (check) {
+            if (check || chk_ad) {
                 const double bj = b ? (double)b[j] : 1.0 / m;
                 e_loc += bj * fabs((double)expm1f((gold[j] - gsk) / eps));
             }
@@ -345,9 +349,16 @@ __device__ __forceinline__ void solve_one(const BatchArgs &A, int prob, float *s
         block_red<NT, kRedW>(cv, 2, red, rpar);
         xsum(cv, 2);   // (CL = 2: also publishes the peer's half of g and w)
         if (cv[1] != 0.0) { nonfin = 1; break; }
-        if (check) {
-            err = (float)(cv[0] + row_err);   // (row_err = 0 unless relaxed)
-            if (err < A.tol) { conv = 1; break; }
+        if (check || chk_ad) {
+            const float en = (float)(cv[0] + row_err);   // (row_err = 0 unless relaxed)
+            if (check) {
+                err = en;
+                if (err < A.tol) { conv = 1; break; }
+            }
+            if (chk_ad) {
+                if (l >= 2 * A.adapt) om_next = adaptive_omega((double)en / (double)err_win, A.adapt, om);
+                err_win = en;
+            }
         }
         if (!am && l >= A.max_iter) break;   // (also when max_iter <= T: no sweep is checked)
         // ---- row pass: f^{l+1} (P = x, Q = y); wy is visible after the reductions' barriers
@@ -493,6 +504,7 @@ __device__ __forceinline__ void solve_one(const BatchArgs &A, int prob, float *s
         xsum(rv, relaxed ? 3 : 1);
         if (rv[0] != 0.0) { nonfin = 1; break; }
         if (relaxed) { row_err = rv[1]; mass_dev = rv[2]; }
+        om = om_next;   // (adaptive: the estimate from err_{l-1}'s window, from sweep l + 2 on)
         cur ^= 1;
         ++l;
     }
@@ -631,6 +643,7 @@ cudaError_t launch_batched(const BatchLaunch &L, cudaStream_t st) {
     A.omega = L.omega;
     A.decay_init = L.decay_init; A.decay_rate = L.decay_rate;
     A.anderson = L.anderson;
+    A.adapt = L.adapt;
     switch (L.d) {
         case 1: return launch_batched_d<1>(A, L.B, L.shape, L.cl, st);
         case 2: return launch_batched_d<2>(A, L.B, L.shape, L.cl, st);

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <math.h>
 #include <stdint.h>
 
 namespace sk {
@@ -26,7 +27,19 @@ struct BatchLaunch {
     int anderson = 0;    // Anderson memory (R-27; < 2: off)
     int shape = 1;       // sk_set_tuning "batched_shape" (512 x 2 points for 512 < P <= 1024)
     int cl = 0;          // sk_set_tuning "batched_cl": 0 auto, 1 one CTA, 2 CTA pair per problem
+    int adapt = 0;       // adaptive momentum window T (R-31; 0: off)
 };
+// Adaptive momentum (R-31): from the error ratio err_l / err_{l-T} of one window,
+// rho = ratio^(1/T) and omega = 2 / (1 + sqrt(max(0, 1 - rho))) clipped to [1, 1.95]; a
+// non-finite or negative ratio keeps the current omega.
+__host__ __device__ inline float adaptive_omega(double ratio, int T, float cur) {
+    if (!(ratio >= 0.0) || ratio > 1e300) return cur;
+    const double rho = pow(ratio, 1.0 / (double)T);
+    double w = 2.0 / (1.0 + sqrt(fmax(0.0, 1.0 - rho)));
+    if (!(w >= 1.0)) w = 1.0;
+    if (w > 1.95) w = 1.95;
+    return (float)w;
+}
 bool batched_supported(int d, int n, int m, int mem = 0);
 // K18 general 1D initializer (NW corner + Alg. 3/4, R-26) on sorted supports
 size_t nw1d_smem_bytes(int n, int m);
@@ -74,6 +87,9 @@ struct DevStatus {
     double row_err;  // relaxed (omega != 1): sum_i a_i |expm1((f_i - fsk_i)/eps)| of the last row merge
     double mass_dev; //                        sum_ij P_ij - sum_i a_i = sum_i a_i expm1((f_i - fsk_i)/eps)
     int g_off;       // Anderson (R-27): the returned g is g_sk(f^L), in buffer [(L + 1) & 1]
+    float omega;     // the relaxation of the current sweep (adaptive momentum, R-31, changes it)
+    float omega_next;//   set by the column merge at the end of a window, applied by the row merge
+    float err_win;   //   err at the end of the previous window
 };
 
 // Packed tile layout of one side: tiles of tq points; tile t at t*(D+1)*tq floats:
@@ -185,6 +201,8 @@ struct MergePass {
     int accum = 0;            // relaxed ROW of a later slice: add its row terms (row_err, mass_dev)
     int anderson = 0;         // Anderson (R-27): COL takes no decision; ROW writes its slice's
     double *and_err = nullptr;//   row term of err_l for (f^l, g~) to *and_err (K19 decides)
+    int adapt = 0;            // adaptive momentum window T (R-31): omega from st->omega, and the
+                              //   column merge estimates the next omega at the end of a window
     long long n_uniform = 0;  // uniform weights (wts == nullptr): 1 / n_uniform (0: the side's own P);
                               //   a row slice of a sharded solve weighs its rows by 1 / n_total
     int range_redo = 0;       // COL after a seeded pass: a sum outside [2^-100, 2^100] sets
@@ -210,7 +228,7 @@ cudaError_t launch_report(const Side &X, const Side &Y, const float *a, const fl
                           DevStatus *st, int local_only, long long n_uniform, cudaStream_t s);
 
 cudaError_t launch_status_init(DevStatus *st, int max_iter, int check_every, float tol,
-                               cudaStream_t s, int g_off = 0);
+                               cudaStream_t s, int g_off = 0, float omega0 = 1.f);
 cudaError_t launch_report_blocks(const Side &X, const float *a, float eps, DevStatus *st, long long n_uniform,
                                  long long row0, long long bs, double *out, cudaStream_t s);
 

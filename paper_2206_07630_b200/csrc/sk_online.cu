@@ -291,7 +291,8 @@ __device__ void exact_lse_point(const Side &S, const Side &Q, int p, float eps, 
 // Merge of point p given its (M, Ssum) over all splits: new potential (+ packed w), fused
 // error term, non-finite and column-range flags.
 __device__ __forceinline__ void merge_point(const MergePass &Mp, const Side &S, const Side &Qs, int p, float M, float Ssum,
-                                            bool check, const float *hold, float *hnew, double &e, double &e2, int &bad) {
+                                            bool check, float om, bool rterms, const float *hold, float *hnew,
+                                            double &e, double &e2, int &bad) {
     const float eps = Mp.eps, kap = kLog2e / eps, epsln2 = eps * kLn2;
     const double wu = 1.0 / (double)(Mp.n_uniform > 0 ? Mp.n_uniform : S.P);   // uniform weight
     if (Mp.range_redo && !(Ssum >= 0x1p-100f && Ssum <= 0x1p100f)) {
@@ -331,9 +332,9 @@ __device__ __forceinline__ void merge_point(const MergePass &Mp, const Side &S, 
     }
     const float hsk = S.c[p] - epsln2 * lse2;   // the Sinkhorn (omega = 1) update
     // Alg. 1 with relaxation (R-1): h <- (1 - omega) h_old + omega h_sk
-    const float hn = Mp.omega == 1.f ? hsk : fmaf(Mp.omega, hsk - hold[p], hold[p]);
+    const float hn = om == 1.f ? hsk : fmaf(om, hsk - hold[p], hold[p]);
     hnew[p] = hn;
-    if (Mp.omega != 1.f && Mp.mode == MERGE_ROW) {
+    if (rterms && Mp.mode == MERGE_ROW) {
         // rows are no longer exact after a relaxed f-update: sum_j P_ij = a_i exp((f_i - fsk_i)/eps)
         const double ai = Mp.wts ? (double)Mp.wts[p] : wu;
         const double dv = (double)expm1f((hn - hsk) / eps);
@@ -376,6 +377,11 @@ __global__ void __launch_bounds__(kMT) k_merge(MergePass Mp, Side S, Side Qs) {
     const int l = st ? st->iter : 0;
     const bool check = Mp.mode == MERGE_COL && !Mp.anderson && l >= 1 &&
                        (l % st->check_every == 0 || l == st->max_iter);
+    // adaptive momentum (R-31): err_l also at the end of every window; omega of this sweep from
+    // the status (rewritten only by the last block of a row merge, after every block has read it)
+    const bool chk_ad = Mp.mode == MERGE_COL && Mp.adapt > 0 && l >= 1 && l % Mp.adapt == 0;
+    const float om = (st && Mp.adapt > 0) ? st->omega : Mp.omega;
+    const bool rterms = Mp.adapt > 0 || Mp.omega != 1.f;
     const float *hold = (l & 1) ? S.pot[1] : S.pot[0];      // no dynamic param indexing
     float *hnew = (l & 1) ? S.pot[0] : S.pot[1];
     double e = 0.0, e2 = 0.0;
@@ -411,7 +417,7 @@ __global__ void __launch_bounds__(kMT) k_merge(MergePass Mp, Side S, Side Qs) {
 #pragma unroll
                 for (int w = 1; w < NW; ++w) Ssum += wS[w][lane];
                 if (Mp.precomputed) bad |= !isfinite(hnew[p]);
-                else merge_point(Mp, S, Qs, p, M, Ssum, check, hold, hnew, e, e2, bad);
+                else merge_point(Mp, S, Qs, p, M, Ssum, check || chk_ad, om, rterms, hold, hnew, e, e2, bad);
             }
             __syncthreads();
         }
@@ -428,7 +434,7 @@ __global__ void __launch_bounds__(kMT) k_merge(MergePass Mp, Side S, Side Qs) {
                 const float2 v = Mp.part[(long long)s * S.P + p];
                 if (v.x != -INFINITY) Ssum += v.y * ex2(v.x - M);
             }
-            merge_point(Mp, S, Qs, p, M, Ssum, check, hold, hnew, e, e2, bad);
+            merge_point(Mp, S, Qs, p, M, Ssum, check || chk_ad, om, rterms, hold, hnew, e, e2, bad);
         }
     }
     if (!st) return;
@@ -463,14 +469,32 @@ __global__ void __launch_bounds__(kMT) k_merge(MergePass Mp, Side S, Side Qs) {
         st->ticket_col = 0;
         if (bt & 2) { st->colfail = 1; __threadfence(); return; }   // decisions left to the exact redo
         if (Mp.only_if) st->colfail = 0;
-        // sharded: f^l may be the non-finite one (rows are not checked locally), so fall back
-        // to (f^{l-1}, g^{l-1}), both finite.
-        if (bt) { st->nonfinite = 1; st->stop = 1; st->final_iter = Mp.sharded ? max(l - 1, 0) : l; }
-        else if (check) {
-            if (Mp.omega != 1.f) et += st->row_err;   // relaxed: the rows of (f^l, g^l) are off too
-            st->err = (float)et;
-            if ((float)et < st->tol) { st->converged = 1; st->stop = 1; st->final_iter = l; }
-            else if (l >= st->max_iter) { st->stop = 1; st->final_iter = l; }
+        if (bt) {
+            st->nonfinite = 1;
+            st->stop = 1;
+            if (Mp.anderson) {
+                // g~ = g_sk(f^l) is the non-finite one: (f^{l-1}, g~_{l-1}) are still in their
+                // buffers (sweep l wrote the other ones); at l = 0, (f^0, g^0 = 0)
+                if (l >= 1) st->final_iter = l - 1;
+                else { st->final_iter = 0; st->g_off = 0; }
+            } else {
+                // sharded: f^l may be the non-finite one (rows are not checked locally), so fall
+                // back to (f^{l-1}, g^{l-1}), both finite
+                st->final_iter = Mp.sharded ? max(l - 1, 0) : l;
+            }
+        } else if (check || chk_ad) {
+            if (rterms) et += st->row_err;   // relaxed: the rows of (f^l, g^l) are off too
+            const float en = (float)et;
+            if (check) {
+                st->err = en;
+                if (en < st->tol) { st->converged = 1; st->stop = 1; st->final_iter = l; }
+                else if (l >= st->max_iter) { st->stop = 1; st->final_iter = l; }
+            }
+            if (chk_ad) {   // a window ends at sweep l: omega from sweep l + 2 on (R-31)
+                if (l >= 2 * Mp.adapt)
+                    st->omega_next = adaptive_omega((double)en / (double)st->err_win, Mp.adapt, st->omega);
+                st->err_win = en;
+            }
         }
     } else if (Mp.mode == MERGE_ROW && Mp.anderson) {
         // Anderson: this slice's row term of err_l; K19's k_and_decide sums the slices (ranks),
@@ -480,12 +504,15 @@ __global__ void __launch_bounds__(kMT) k_merge(MergePass Mp, Side S, Side Qs) {
         if (bt && !Mp.sharded) { st->nonfinite = 1; st->stop = 1; st->final_iter = l; }
     } else if (Mp.mode == MERGE_ROW) {
         st->ticket_row = 0;
-        if (Mp.omega != 1.f) {   // (row shards: summed over the slices here, over ranks by an allreduce)
+        if (rterms) {   // (row shards: summed over the slices here, over ranks by an allreduce)
             if (Mp.accum) { st->row_err += et; st->mass_dev += et2; }
             else { st->row_err = et; st->mass_dev = et2; }
         }
         if (bt && !Mp.sharded) { st->nonfinite = 1; st->stop = 1; st->final_iter = l; }
-        else if (!Mp.no_iter_inc) st->iter = l + 1;
+        else if (!Mp.no_iter_inc) {
+            st->iter = l + 1;
+            if (Mp.adapt > 0) st->omega = st->omega_next;   // the next sweep's relaxation
+        }
     } else {
         st->ticket_row = 0;
         if (bt) st->nonfinite = 1;
@@ -569,9 +596,11 @@ cudaError_t launch_report(const Side &X, const Side &Y, const float *a, const fl
     return cudaGetLastError();
 }
 
-__global__ void k_status_init(DevStatus *st, int max_iter, int check_every, float tol, int g_off) {
+__global__ void k_status_init(DevStatus *st, int max_iter, int check_every, float tol, int g_off, float omega0) {
     DevStatus z = {};
     z.g_off = g_off;
+    z.omega = omega0;
+    z.omega_next = omega0;
     z.max_iter = max_iter;
     z.check_every = check_every;
     z.tol = tol;
@@ -607,8 +636,8 @@ cudaError_t launch_report_blocks(const Side &X, const float *a, float eps, DevSt
 }
 
 cudaError_t launch_status_init(DevStatus *st, int max_iter, int check_every, float tol,
-                               cudaStream_t s, int g_off) {
-    k_status_init<<<1, 1, 0, s>>>(st, max_iter, check_every, tol, g_off);
+                               cudaStream_t s, int g_off, float omega0) {
+    k_status_init<<<1, 1, 0, s>>>(st, max_iter, check_every, tol, g_off, omega0);
     return cudaGetLastError();
 }
 

@@ -133,7 +133,7 @@ def nccl_ctx():
     c.close()
 
 
-@pytest.mark.parametrize("accel", ["plain", "omega", "anderson", "stored"])
+@pytest.mark.parametrize("accel", ["plain", "omega", "anderson", "adaptive", "stored"])
 def test_nccl_branch_one_rank_bit_identical(ctx, nccl_ctx, accel):
     """the NCCL branch of the sharded solver (ncclAllGather of the block partials,
     ncclAllReduce of the relaxed row terms / the Anderson Gram dots, ncclAllGather of E's block
@@ -147,7 +147,8 @@ def test_nccl_branch_one_rank_bit_identical(ctx, nccl_ctx, accel):
     eps = float(np.float32(0.04 * gen.mean_sq_cost(x, y)))
     xd, yd, ad = _cuda(x), _cuda(y), _cuda(a)
     mode = "stored" if accel == "stored" else "online"
-    kw = {"plain": {}, "stored": {}, "omega": {"omega": 1.2}, "anderson": {"anderson": 5}}[accel]
+    kw = {"plain": {}, "stored": {}, "omega": {"omega": 1.2}, "anderson": {"anderson": 5},
+          "adaptive": {"adaptive": 10}}[accel]
     fe, ge, re_ = sk.sinkhorn_solve_sharded_emulated(ctx, 1, xd, yd, eps, a=ad, mode=mode, **kw)
     fn, gn, rn = sk.sinkhorn_solve_sharded(nccl_ctx, n, 0, xd, yd, eps, a_local=ad, mode=mode, **kw)
     assert rn["iterations"] == re_["iterations"] and rn["converged"] == re_["converged"] == 1

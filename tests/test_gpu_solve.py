@@ -219,7 +219,7 @@ def test_onchip_cta_pair_variant_is_bit_identical(O, ctx):
     assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
 
 
-@pytest.mark.parametrize("entry", ["solve", "anderson", "onchip", "sharded2", "sharded2_anderson"])
+@pytest.mark.parametrize("entry", ["solve", "anderson", "onchip", "onchip_anderson", "sharded2", "sharded2_anderson"])
 def test_nonfinite_potentials_are_reported(ctx, entry):
     """Error contract (include/sinkhorn_b200.h): finite inputs whose squared norms
     overflow fp32 make the potentials non-finite in the first sweep -> SK_ENONFINITE (never SK_OK
@@ -227,17 +227,17 @@ def test_nonfinite_potentials_are_reported(ctx, entry):
     import paper_2206_07630_b200 as sk
     from paper_2206_07630_b200 import _lib
     rng = np.random.default_rng(21)
-    n, m = (256, 256) if entry == "onchip" else (3000, 2500)
+    n, m = (256, 256) if entry.startswith("onchip") else (3000, 2500)
     x = torch.from_numpy(rng.uniform(1e19, 2e19, (n, 1)).astype(np.float32)).cuda()
     y = torch.from_numpy(rng.uniform(-2e19, -1e19, (m, 1)).astype(np.float32)).cuda()
     kw = {"anderson": 5} if "anderson" in entry else {}
     with pytest.raises(sk.SinkhornError) as ei:
         if entry.startswith("sharded2"):
             sk.sinkhorn_solve_sharded_emulated(ctx, 2, x, y, 1.0, mode="online", **kw)
-        elif entry == "onchip":
+        elif entry.startswith("onchip"):
             f = torch.full((2, n), 7.0, device="cuda")
             g = torch.full((2, m), 7.0, device="cuda")
-            sk.sinkhorn_solve(ctx, torch.stack([x, x]), torch.stack([y, y]), 1.0, f=f, g=g)
+            sk.sinkhorn_solve(ctx, torch.stack([x, x]), torch.stack([y, y]), 1.0, f=f, g=g, **kw)
         else:
             f = torch.full((1, n), 7.0, device="cuda")
             g = torch.full((1, m), 7.0, device="cuda")

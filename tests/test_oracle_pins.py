@@ -433,6 +433,48 @@ def test_gmm_dual_plain_and_anderson_land_on_the_same_solution(O):
         O.sinkhorn_matrix(C, 0.4, a=gx["weights"], b=gy["weights"], anderson=17)
 
 
+# ------------------------------------------------------------------ adaptive momentum (R-31)
+def test_adaptive_momentum_reduces_to_the_pinned_solvers(O):
+    """Adaptive momentum ("adapt=10"; reading R-31) is the plain solver
+    until its first adaptation and the (pinned) relaxed solver between adaptations:
+    (a) the first 2T + 1 sweeps equal plain Sinkhorn exactly;
+    (b) the omega it switches to at sweep 2T + 2 is 2/(1 + sqrt(1 - rho)) with rho the per-sweep
+        contraction of the explicit L1 errors of an independent plain run at sweeps T and 2T;
+    (c) the next T sweeps equal the relaxed solver at that omega started from (f, g) of sweep
+        2T + 1;  (d) it reaches the plain optimum, in fewer sweeps than plain Sinkhorn on C1."""
+    p = gen.c1()
+    T = 10
+    plain = O.sinkhorn(p.x, p.y, p.eps, tol=0, max_iter=2 * T + 1)
+    ad = O.sinkhorn_adaptive(p.x, p.y, p.eps, T, tol=0, max_iter=2 * T + 1)
+    assert np.array_equal(ad.f, plain.f) and np.array_equal(ad.g, plain.g)
+    assert np.all(ad.omega == 1.0)
+    eT = O.marginal_error(p.x, p.y, *[O.sinkhorn(p.x, p.y, p.eps, tol=0, max_iter=T)[k] for k in ("f", "g")], p.eps)
+    e2T = O.marginal_error(p.x, p.y, *[O.sinkhorn(p.x, p.y, p.eps, tol=0, max_iter=2 * T)[k] for k in ("f", "g")],
+                           p.eps)
+    rho = (e2T / eT) ** (1.0 / T)
+    w_star = min(max(2.0 / (1.0 + math.sqrt(max(0.0, 1.0 - rho))), 1.0), 1.95)
+    s = T - 1
+    long = O.sinkhorn_adaptive(p.x, p.y, p.eps, T, tol=0, max_iter=2 * T + 1 + s)
+    assert abs(long.omega[2 * T + 1] - w_star) < 1e-12 and 1.0 < w_star < 1.95
+    assert np.all(long.omega[2 * T + 1:] == long.omega[2 * T + 1])
+    rel = O.sinkhorn_adaptive(p.x, p.y, p.eps, 0, tol=0, max_iter=s, f0=ad.f, g0=ad.g, omega=long.omega[2 * T + 1])
+    assert np.abs(rel.f - long.f).max() < 1e-12 and np.abs(rel.g - long.g).max() < 1e-12
+    # g0 is read by the relaxed g-update only: at omega = 1 it changes nothing
+    r1 = O.sinkhorn_adaptive(p.x, p.y, p.eps, 0, tol=0, max_iter=3, g0=np.full(p.m, 5.0))
+    r2 = O.sinkhorn(p.x, p.y, p.eps, tol=0, max_iter=3)
+    assert np.array_equal(r1.f, r2.f) and np.array_equal(r1.g, r2.g)
+    # (d) the same optimum, fewer sweeps
+    ref = O.sinkhorn(p.x, p.y, p.eps, tol=1e-10, max_iter=100000)
+    adc = O.sinkhorn_adaptive(p.x, p.y, p.eps, T, tol=1e-10, max_iter=100000)
+    assert adc.converged and adc.iterations < ref.iterations
+    fa, ga = adc.f - adc.f.mean(), adc.g + adc.f.mean()
+    fr, gr = ref.f - ref.f.mean(), ref.g + ref.f.mean()
+    assert np.abs(fa - fr).max() < 1e-7 * max(np.abs(fr).max(), 1) and np.abs(ga - gr).max() < 1e-7 * max(np.abs(gr).max(), 1)
+    at = O.sinkhorn_adaptive(p.x, p.y, p.eps, T)
+    assert at.converged and at.iterations < O.sinkhorn(p.x, p.y, p.eps).iterations / 2
+    assert abs(O.marginal_error(p.x, p.y, at.f, at.g, p.eps) - at.err) < 1e-12
+
+
 # ------------------------------------------------------------------ Subsample
 def test_subsample_full_equals_solution(O):
     rng = np.random.default_rng(19)

@@ -31,5 +31,5 @@ FULL="timeout 900 ncu --set full --clock-control none --import-source on"
 $FULL -k regex:k_lse -s 4 -c 1 -o "$O/full_c4" python tools/prof_c4.py c4 > "$O/full_c4.log" 2>&1; echo "full c4 rc=$?"
 $FULL -k regex:k_batched -c 1 -o "$O/full_c2" python bench.py --workload c2 --steps 1 --warmup 0 --no-k14 --no-cpu-baseline > "$O/full_c2.log" 2>&1; echo "full c2 rc=$?"
 $FULL -k regex:k_stored_fused -s 2 -c 1 -o "$O/full_c3" python tools/prof_c4.py c3 > "$O/full_c3.log" 2>&1; echo "full c3 rc=$?"
-$FULL -k regex:k_lse_tc -s 5 -c 1 -o "$O/full_c5" python tools/prof_c4.py c5 > "$O/full_c5.log" 2>&1; echo "full c5 rc=$?"
+$FULL -k regex:k_lse_tc -s 4 -c 1 -o "$O/full_c5" python tools/prof_c4.py c5 > "$O/full_c5.log" 2>&1; echo "full c5 rc=$?"
 for f in "$O"/bench_*.json; do echo "== $f"; tail -c 600 "$f"; echo; done
