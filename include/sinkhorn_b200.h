@@ -171,7 +171,10 @@ sk_status sk_get_solver_options(const sk_ctx *ctx, float *omega, float *decay_in
  *   "tc_emu" 0..6 (2): K3 exponential pairs of 8 on the FMA pipe;
  *   "tc_epi" 16|162 (162): K3 epilogue organisation;
  *   "batched_shape" 0|1 (1): K13 512 threads x 2 points (1) or 1024 x 1 (0) for 512 < P <= 1024;
- *   "batched_cl" 0..2 (0): K13 one CTA (1) or a CTA pair (2) per problem (0: pair only for B = 1).
+ *   "batched_cl" 0..2 (0): K13 one CTA (1) or a CTA pair (2) per problem (0: pair only for B = 1);
+ *   "batched_park" >= 0 (12): K13 batches with more problems than resident CTAs run at most this
+ *       many sweeps per turn, then park (state to the workspace) and re-queue with their predicted
+ *       remaining sweeps as priority (bit-identical results; 0: one turn per problem, FIFO).
  * SK_EINVAL for an unknown key or a value out of range. */
 sk_status sk_set_tuning(sk_ctx *ctx, const char *key, double value);
 /* Enable (1) / disable (0) CUDA-event timing of the dominant kernels into sk_counters. */

@@ -90,6 +90,7 @@ struct sk_ctx {
         int tc_epi = 162;       // K3 epilogue organisation (162 or 16)
         int batched_shape = 1;  // K13: 512 x 2 points for 512 < P <= 1024 (0: 1024 x 1)
         int batched_cl = 0;     // K13: 0 auto, 1 one CTA, 2 a CTA pair per problem
+        int batched_park = 12;  // K13 batches: sweeps per turn of the park / resume scheduler (0: off)
     } tune;
 };
 
@@ -98,7 +99,7 @@ enum BufId {
     B_STAGE0 = 0, B_STAGE_END = 16,   // staging of host arrays
     B_FLAG = 16, B_XPACK, B_XC, B_XNK, B_XPOT, B_YPACK, B_YC, B_YNK, B_YPOT, B_PART, B_BLKE, B_BLKB,
     B_STATUS, B_COST, B_REP, B_SORT, B_PERM, B_YSORT, B_GAUSS, B_GAUSS2, B_GMM, B_SUBW, B_SUBZ,
-    B_SUBF, B_SUBG, B_IDX, B_OUT, B_FA, B_QUEUE, B_XIMG, B_YIMG, B_XLSE, B_YLSE, B_TCMAX, B_EMST, B_EMPART, B_EMIDX, B_VJP, B_ANDFR, B_ANDBLK, B_ANDVEC, B_ANDST, B_XCHG, B_NBUF
+    B_SUBF, B_SUBG, B_IDX, B_OUT, B_FA, B_QUEUE, B_XIMG, B_YIMG, B_XLSE, B_YLSE, B_TCMAX, B_EMST, B_EMPART, B_EMIDX, B_VJP, B_ANDFR, B_ANDBLK, B_ANDVEC, B_ANDST, B_XCHG, B_PARK, B_NBUF
 };
 
 sk_status fail(sk_ctx *c, sk_status s, const char *fmt, ...) {
@@ -897,6 +898,7 @@ sk_status sk_set_tuning(sk_ctx *ctx, const char *key, double value) {
     else if (k == "tc_epi") { CK(need(iv == 16 || iv == 162)); T.tc_epi = iv; }
     else if (k == "batched_shape") { CK(need(iv == 0 || iv == 1)); T.batched_shape = iv; }
     else if (k == "batched_cl") { CK(need(iv >= 0 && iv <= 2)); T.batched_cl = iv; }
+    else if (k == "batched_park") { CK(need(iv >= 0 && iv <= 100000)); T.batched_park = iv; }
     else return fail(ctx, SK_EINVAL, "sk_set_tuning: unknown key '%s'", key);
     return SK_OK;
 }
@@ -1404,6 +1406,18 @@ sk_status solve_impl(sk_ctx *ctx, int64_t B, int64_t n, int64_t m, int32_t d, co
         L.decay_init = ctx->decay_init; L.decay_rate = ctx->decay_rate;
         L.anderson = ctx->anderson;
         L.adapt = ctx->adapt;
+        if (B > 1 && ctx->tune.batched_park > 0) {
+            // park / resume workspace: state, keys, finished count, headers, LSE seeds
+            const size_t bytes = (size_t)B * (8 * sizeof(double) + sizeof(float) * (n + m)) + 16 +
+                                 sizeof(int) * park_queue_ints((int)B);
+            ENSURE(pk, char, B_PARK, bytes);
+            char *q = pk;
+            L.phdr = (double *)q; q += (size_t)B * 8 * sizeof(double);
+            L.done = (int *)q; q += 16;
+            L.pq = (int *)q; q += sizeof(int) * park_queue_ints((int)B);
+            L.pseed = (float *)q;
+            L.park = ctx->tune.batched_park;
+        }
         L.shape = ctx->tune.batched_shape;
         L.cl = ctx->tune.batched_cl;
         CU(cudaEventRecord(ctx->ev0, st));

@@ -39,7 +39,18 @@ struct BatchArgs {
     float decay_init, decay_rate;   // eps-decay (decay_init <= 0: off)
     int anderson;                   // Anderson memory (R-27; < 2: off)
     int adapt;                      // adaptive momentum window T (R-31; 0: off)
+    // park / resume scheduling (CL = 1 batches larger than the resident CTAs; park = 0: off): a
+    // problem runs at most `park` sweeps per turn, then its state is saved and it is re-queued
+    // with the predicted number of remaining sweeps as its priority
+    int park;
+    unsigned long long *pq;         // [kParkBuckets] bucket stacks: (ABA tag << 32) | (top problem + 1),
+                                    // then int next[B]: the problem below each parked one (+ 1; 0 = none)
+    float *pseed;                   // [B][n + m] the per-point LSE seeds (mxs, mys)
+    double *phdr;                   // [B][8] sweep count, relaxed / adaptive state
+    int *done;                      // problems finished
 };
+// priority buckets of parked problems: predicted remaining sweeps, clamped to [0, 63]
+constexpr int kParkBuckets = 64;
 
 __host__ __device__ inline int round_up(int v, int a) { return (v + a - 1) / a * a; }
 
@@ -172,7 +183,7 @@ __device__ __forceinline__ void cl_sync() {
 // reductions combine the two halves' block partials in a fixed order, so both CTAs take the
 // same decisions).  The per-point arithmetic is the same for CL = 1 and 2 (same potentials).
 template <int D, int R, int NT, int EMU, int CL>
-__device__ __forceinline__ void solve_one(const BatchArgs &A, int prob, float *sm, uint32_t rank) {
+__device__ __forceinline__ int solve_one(const BatchArgs &A, int prob, bool resume, float *sm, uint32_t rank) {
     const int n = A.n, m = A.m;
     const int Np = round_up(n, kChunk), Mp = round_up(m, kChunk);
     const float eps_t = A.eps;          // the target eps
@@ -246,10 +257,12 @@ __device__ __forceinline__ void solve_one(const BatchArgs &A, int prob, float *s
             const float la = a ? logf(a[i]) : loga_u;
             cx[i] = fmaf(eps, la, s);
             nxk[i] = s * kap;
-            const float f0 = A.finit ? A.finit[(size_t)prob * A.fs + i] : 0.f;
+            // (resume: the parked f^l and seeds, written by another CTA: L2 loads)
+            const float f0 = resume ? __ldcg(A.f + (size_t)prob * n + i)
+                                    : (A.finit ? A.finit[(size_t)prob * A.fs + i] : 0.f);
             fb[i] = f0;
             wx[i] = fmaf(f0, kap, -nxk[i]);
-            mxs[i] = -INFINITY;
+            mxs[i] = resume ? __ldcg(A.pseed + (size_t)prob * (n + m) + i) : -INFINITY;
         } else {
 #pragma unroll
             for (int k = 0; k < D; ++k) xq[k * Np + i] = 0.f;
@@ -268,8 +281,8 @@ __device__ __forceinline__ void solve_one(const BatchArgs &A, int prob, float *s
             const float lb = b ? logf(b[j]) : logb_u;
             cy[j] = fmaf(eps, lb, s);
             nyk[j] = s * kap;
-            gb[j] = 0.f;  // g^(0) = 0 (only f^(0) is needed)
-            mys[j] = -INFINITY;
+            gb[j] = resume ? __ldcg(A.g + (size_t)prob * m + j) : 0.f;  // g^(0) = 0 (only f^(0) is needed)
+            mys[j] = resume ? __ldcg(A.pseed + (size_t)prob * (n + m) + n + j) : -INFINITY;
         } else {
 #pragma unroll
             for (int k = 0; k < D; ++k) yq[k * Mp + j] = 0.f;
@@ -279,6 +292,8 @@ __device__ __forceinline__ void solve_one(const BatchArgs &A, int prob, float *s
     __syncthreads();
 
     int l = 0, cur = 0, conv = 0, nonfin = 0;
+    const double *hdr = A.phdr + (size_t)prob * 8;
+    if (resume) l = (int)__ldcg(hdr);
     int a_cnt = 0, a_head = 0;   // Anderson history: filled slots, next slot
     bool out_gtilde = false;     // Anderson: the result is (f^l, g_sk(f^l)) (the g buffer not flipped)
     float err = INFINITY;
@@ -287,6 +302,13 @@ __device__ __forceinline__ void solve_one(const BatchArgs &A, int prob, float *s
     float om = A.adapt > 0 ? 1.f : A.omega, om_next = om, err_win = 0.f;
     const bool relaxed = A.adapt > 0 || om != 1.f;
     double row_err = 0.0, mass_dev = 0.0;   // relaxed: row term of err_l and sum P - sum a
+    if (resume) {
+        row_err = __ldcg(hdr + 1); mass_dev = __ldcg(hdr + 2); err = (float)__ldcg(hdr + 3);
+        om = (float)__ldcg(hdr + 4); om_next = (float)__ldcg(hdr + 5); err_win = (float)__ldcg(hdr + 6);
+    }
+    // park after `park` sweeps of this turn; the errors of its last two sweeps predict the rest
+    const int l_park = A.park > 0 ? l + A.park : 0x7fffffff;
+    float pe1 = INFINITY, pe2 = INFINITY;
     // eps-decay (R-25): sweep l + 1 uses max(eps, eps init rate^l); the T decay sweeps
     // are not checked; the constants that carry eps are refreshed when it changes
     auto eps_of = [&](int s) {
@@ -318,6 +340,46 @@ __device__ __forceinline__ void solve_one(const BatchArgs &A, int prob, float *s
     };
     bool fresh = true;   // the LSE seeds (previous sweep's LSE) belong to this sweep's eps
     for (;;) {
+        if (l >= l_park) {
+            // park: (f^l, g^l), the seeds and the sweep state -> global; the priority is the
+            // predicted remaining sweep count log(err_{l-1} / tol) / log(1 / rho),
+            // rho = err_{l-1} / err_{l-2} (a problem without both errors goes first)
+            const float *fo = fb + cur * n, *go = gb + cur * m;
+            for (int i = threadIdx.x; i < n; i += NT) {
+                A.f[(size_t)prob * n + i] = fo[i];
+                A.pseed[(size_t)prob * (n + m) + i] = mxs[i];
+            }
+            for (int j = threadIdx.x; j < m; j += NT) {
+                A.g[(size_t)prob * m + j] = go[j];
+                A.pseed[(size_t)prob * (n + m) + n + j] = mys[j];
+            }
+            float key = 1e30f;
+            if (threadIdx.x == 0) {
+                double *h = A.phdr + (size_t)prob * 8;
+                h[0] = (double)l; h[1] = row_err; h[2] = mass_dev; h[3] = (double)err;
+                h[4] = (double)om; h[5] = (double)om_next; h[6] = (double)err_win;
+                if (pe1 < INFINITY && pe2 < INFINITY && pe2 > 0.f) {
+                    const float rho = fminf(fmaxf(pe2 / pe1, 1e-6f), 0.999999f);
+                    key = fmaxf(logf(fmaxf(pe2, 1e-30f) / A.tol), 0.f) / -logf(rho);
+                    if (!(key >= 0.f)) key = 1e30f;
+                }
+            }
+            __threadfence();
+            __syncthreads();
+            if (threadIdx.x == 0) {   // push onto its priority bucket (lock-free stack, ABA-tagged)
+                const int bk = key >= (float)(kParkBuckets - 1) ? kParkBuckets - 1 : (int)key;
+                volatile int *nxt = reinterpret_cast<volatile int *>(A.pq + kParkBuckets);
+                for (;;) {
+                    const unsigned long long old = *(volatile unsigned long long *)(A.pq + bk);
+                    nxt[prob] = (int)(old & 0xffffffffull);
+                    __threadfence();
+                    const unsigned long long nw = (((old >> 32) + 1ull) << 32) | (unsigned long long)(prob + 1);
+                    if (atomicCAS(A.pq + bk, old, nw) == old) break;
+                }
+            }
+            __syncthreads();   // smem is reused by the next problem
+            return 1;
+        }
         {
             const float el = eps_of(l);
             fresh = el == eps;
@@ -327,6 +389,7 @@ __device__ __forceinline__ void solve_one(const BatchArgs &A, int prob, float *s
         // ---- column pass: g^{l+1} (P = y, Q = x)
         const bool check = !am && l > T && ((l - T) % A.check_every == 0 || l == A.max_iter);
         const bool chk_ad = A.adapt > 0 && l >= 1 && l % A.adapt == 0;   // err_l ends a window
+        const bool chk_pk = l >= 1 && (l == l_park - 2 || l == l_park - 1);   // the park's predictor
         double e_loc = 0.0;
         int bad = 0;
         float *gold = gb + cur * m, *gnew = gb + (cur ^ 1) * m;
@@ -340,7 +403,7 @@ __device__ __forceinline__ void solve_one(const BatchArgs &A, int prob, float *s
             rput(&gnew[j], gn);
             rput(&wy[j], wv);
             bad |= !isfinite(gn);
-            if (check || chk_ad) {
+            if (check || chk_ad || chk_pk) {
                 const double bj = b ? (double)b[j] : 1.0 / m;
                 e_loc += bj * fabs((double)expm1f((gold[j] - gsk) / eps));
             }
@@ -349,8 +412,9 @@ __device__ __forceinline__ void solve_one(const BatchArgs &A, int prob, float *s
         block_red<NT, kRedW>(cv, 2, red, rpar);
         xsum(cv, 2);   // (CL = 2: also publishes the peer's half of g and w)
         if (cv[1] != 0.0) { nonfin = 1; break; }
-        if (check || chk_ad) {
+        if (check || chk_ad || chk_pk) {
             const float en = (float)(cv[0] + row_err);   // (row_err = 0 unless relaxed)
+            if (chk_pk) { if (l == l_park - 2) pe1 = en; else pe2 = en; }
             if (check) {
                 err = en;
                 if (err < A.tol) { conv = 1; break; }
@@ -531,8 +595,10 @@ __device__ __forceinline__ void solve_one(const BatchArgs &A, int prob, float *s
         A.nonfinite[prob] = nonfin;
         A.err[prob] = err;
         A.E[prob] = E;
+        if (A.done) atomicAdd(A.done, 1);
     }
     __syncthreads();  // smem is reused by the next problem
+    return 0;
 }
 
 // Persistent CTAs (one or two per SM) pull problems from a global queue: iteration
@@ -541,12 +607,52 @@ __device__ __forceinline__ void solve_one(const BatchArgs &A, int prob, float *s
 template <int D, int R, int NT, int EMU, int CL>
 __global__ void __launch_bounds__(NT, NT <= 512 ? 2 : 1) k_batched(BatchArgs A) {
     extern __shared__ __align__(16) float sm[];
-    __shared__ int s_prob;
+    __shared__ int s_prob, s_res;
     const uint32_t rank = CL > 1 ? cl_rank() : 0u;
     for (;;) {
-        if (threadIdx.x == 0 && rank == 0) {
+        if constexpr (CL == 1) {
+            if (threadIdx.x < 32) {   // warp 0: the next problem - fresh ones first, then parked ones
+                const int lane = threadIdx.x;
+                int pr = 0, res = 0;
+                if (lane == 0) pr = atomicAdd(A.queue, 1);
+                pr = __shfl_sync(0xffffffffu, pr, 0);
+                if (pr >= A.B) {
+                    pr = A.B;
+                    while (A.park > 0) {
+                        // the highest non-empty priority bucket (most remaining sweeps): pop its
+                        // top by compare-and-swap - O(1) per claim, no scan of the problems
+                        volatile unsigned long long *hd = A.pq;
+                        const unsigned long long a0 = hd[lane], a1 = hd[lane + 32];
+                        const unsigned lo = __ballot_sync(0xffffffffu, (a0 & 0xffffffffull) != 0ull);
+                        const unsigned hi = __ballot_sync(0xffffffffu, (a1 & 0xffffffffull) != 0ull);
+                        if (lo | hi) {
+                            const int bk = hi ? 32 + 31 - __clz(hi) : 31 - __clz(lo);
+                            int got = 0;
+                            if (lane == 0) {
+                                const unsigned long long old = hd[bk];
+                                const int top = (int)(old & 0xffffffffull);
+                                if (top != 0) {
+                                    const int below = reinterpret_cast<volatile int *>(A.pq + kParkBuckets)[top - 1];
+                                    const unsigned long long nw = (((old >> 32) + 1ull) << 32) | (unsigned)below;
+                                    if (atomicCAS(A.pq + bk, old, nw) == old) got = top;
+                                }
+                            }
+                            got = __shfl_sync(0xffffffffu, got, 0);
+                            if (got) { pr = got - 1; res = 1; break; }
+                            continue;   // lost the race: look again
+                        }
+                        // nothing parked: done when every problem has finished, else wait for a park
+                        if (*(volatile const int *)A.done >= A.B) break;
+                        __nanosleep(1000);
+                    }
+                }
+                if (lane == 0) { s_prob = pr; s_res = res; }
+                __threadfence();   // (the claimed problem's parked state is read after this)
+            }
+        } else if (threadIdx.x == 0 && rank == 0) {
             const int pr = atomicAdd(A.queue, 1);
             s_prob = pr;
+            s_res = 0;
             if constexpr (CL > 1) {   // the pair's problem id into the peer's s_prob
                 const uint32_t pa = cl_map(&s_prob, 1u);
                 asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(pa), "r"(pr) : "memory");
@@ -554,9 +660,10 @@ __global__ void __launch_bounds__(NT, NT <= 512 ? 2 : 1) k_batched(BatchArgs A) 
         }
         if constexpr (CL > 1) cl_sync(); else __syncthreads();
         const int prob = s_prob;
+        const bool resume = CL == 1 && s_res != 0;
         if constexpr (CL > 1) cl_sync(); else __syncthreads();
         if (prob >= A.B) break;
-        solve_one<D, R, NT, EMU, CL>(A, prob, sm, rank);
+        solve_one<D, R, NT, EMU, CL>(A, prob, resume, sm, rank);
     }
 }
 
@@ -573,11 +680,14 @@ static cudaError_t launch_batched_c(const BatchArgs &A, int B, cudaStream_t st) 
     if (e != cudaSuccess) return e;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    BatchArgs Ap = A;
     if (CL == 1) {
         const int grid = std::max(1, std::min(B, nsm * std::max(occ, 1)));
-        k_batched<D, R, NT, EMU, 1><<<grid, NT, smem, st>>>(A);
+        if (!(A.park > 0 && B > grid && A.pq)) Ap.park = 0;   // park only when problems queue up
+        k_batched<D, R, NT, EMU, 1><<<grid, NT, smem, st>>>(Ap);
         return cudaGetLastError();
     }
+    Ap.park = 0;   // (CTA pairs: one turn per problem)
     const int pairs = std::max(1, std::min(B, nsm * std::max(occ, 1) / 2));
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(2 * pairs);
@@ -589,7 +699,7 @@ static cudaError_t launch_batched_c(const BatchArgs &A, int B, cudaStream_t st) 
     at[0].val.clusterDim.x = 2; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, k_batched<D, R, NT, EMU, CL>, A);
+    return cudaLaunchKernelEx(&cfg, k_batched<D, R, NT, EMU, CL>, Ap);
 }
 
 // CTA pairs (CL = 2: two halves of every pass, DSMEM exchange) halve a problem's latency; on
@@ -623,6 +733,8 @@ static cudaError_t launch_batched_d(const BatchArgs &A, int B, int shape, int cl
     return launch_batched_e<D, 2, 1024, 1>(A, B, st);  // more rounds of 2048 points for larger P
 }
 
+size_t park_queue_ints(int B) { return 2 * (size_t)kParkBuckets + (size_t)B; }
+
 bool batched_supported(int d, int n, int m, int mem) {
     return d >= 1 && d <= 4 && mem <= kAndMax && batched_smem_bytes(d, n, m, mem) <= 200 * 1024;
 }
@@ -644,6 +756,17 @@ cudaError_t launch_batched(const BatchLaunch &L, cudaStream_t st) {
     A.decay_init = L.decay_init; A.decay_rate = L.decay_rate;
     A.anderson = L.anderson;
     A.adapt = L.adapt;
+    A.park = (L.anderson >= 2 || L.decay_init > 0.f) ? 0 : L.park;
+    A.pq = reinterpret_cast<unsigned long long *>(L.pq); A.pseed = L.pseed; A.phdr = L.phdr; A.done = L.done;
+    if (A.park > 0) {
+        if (!A.pq || !A.done || !A.pseed || !A.phdr) return cudaErrorInvalidValue;
+        e = cudaMemsetAsync(A.pq, 0, sizeof(int) * 2 * kParkBuckets, st);   // empty stacks
+        if (e == cudaSuccess) e = cudaMemsetAsync(A.done, 0, sizeof(int), st);
+        if (e != cudaSuccess) return e;
+    } else if (A.done) {
+        e = cudaMemsetAsync(A.done, 0, sizeof(int), st);
+        if (e != cudaSuccess) return e;
+    }
     switch (L.d) {
         case 1: return launch_batched_d<1>(A, L.B, L.shape, L.cl, st);
         case 2: return launch_batched_d<2>(A, L.B, L.shape, L.cl, st);

@@ -28,6 +28,13 @@ struct BatchLaunch {
     int shape = 1;       // sk_set_tuning "batched_shape" (512 x 2 points for 512 < P <= 1024)
     int cl = 0;          // sk_set_tuning "batched_cl": 0 auto, 1 one CTA, 2 CTA pair per problem
     int adapt = 0;       // adaptive momentum window T (R-31; 0: off)
+    // park / resume scheduling of batches (sweeps per turn; 0: off) and its workspace:
+    // pq park_queue_ints(B) ints, pseed [B][n + m] float, phdr [B][8] double, done [1] int
+    int park = 0;
+    int *pq = nullptr;
+    float *pseed = nullptr;
+    double *phdr = nullptr;
+    int *done = nullptr;
 };
 // Adaptive momentum (R-31): from the error ratio err_l / err_{l-T} of one window,
 // rho = ratio^(1/T) and omega = 2 / (1 + sqrt(max(0, 1 - rho))) clipped to [1, 1.95]; a
@@ -41,6 +48,7 @@ __host__ __device__ inline float adaptive_omega(double ratio, int T, float cur) 
     return (float)w;
 }
 bool batched_supported(int d, int n, int m, int mem = 0);
+size_t park_queue_ints(int B);
 // K18 general 1D initializer (NW corner + Alg. 3/4, R-26) on sorted supports
 size_t nw1d_smem_bytes(int n, int m);
 cudaError_t launch_nw1d(const float *xs, const int *xperm, const float *ys, const int *yperm, int y_shared,

@@ -109,3 +109,25 @@ def test_c2_batched_solve_full_launch(O, ctx, c2, init):
     if init == "sort1d":
         its = np.array([r["iterations"] for r in reps])
         assert its.max() < 200, its.max()   # the eps=0 dual start is close (Sec. 3.1)
+
+
+@pytest.mark.parametrize("kw", [{}, {"omega": 1.3}, {"adaptive": 10}])
+def test_c2_park_resume_scheduler_is_bit_identical(kw):
+    """K13's park / resume scheduler (sk_set_tuning batched_park: a problem runs at most k sweeps
+    per turn, parks its state and re-queues by predicted remaining sweeps) changes only which CTA
+    runs which sweeps: the full C2 batch's potentials, counts, errors and objectives are
+    bit-identical to one turn per problem (batched_park = 0), for plain, relaxed and adaptive."""
+    import paper_2206_07630_b200 as sk
+    p = gen.c2()
+    outs = []
+    for park in (8, 3, 0):
+        c = sk.Context(0)
+        c.set_tuning("batched_park", park)
+        x, y = torch.from_numpy(p.x).cuda(), torch.from_numpy(p.y).cuda()
+        f0 = sk.sinkhorn_init_sort1d(c, x.view(1024, 1024), y.view(1024), y_shared=True)
+        f, g, reps = sk.sinkhorn_solve(c, x, y, p.eps, y_shared=True, f_init=f0, **kw)
+        outs.append((f.cpu(), g.cpu(), [(r["iterations"], r["marginal_error"], r["dual_objective"]) for r in reps]))
+        c.close()
+    for f, g, r in outs[:2]:
+        assert torch.equal(f, outs[2][0]) and torch.equal(g, outs[2][1]) and r == outs[2][2]
+    assert max(it for it, _, _ in outs[2][2]) > 8   # problems did park
