@@ -415,6 +415,14 @@ class Single(Workload):
         if self.init == "subsample" and hasattr(self, "inner"):
             ns = int(p.extra["idx_x"].size)
             out["init_s_extrapolated"] = (ns * ns * self.inner["iterations"] + p.n * ns / 2) / rate
+        if self.name == "c5":   # full fp64 run at reduced n: Gaussian init + solve to tol (same eps factor)
+            q = gen.c5(n=1024, eps_factor=self.args.eps_factor or 1e-2)
+            t0 = time.perf_counter()
+            f0, _ = O.init_gaussian(q.x, q.y)
+            r = O.sinkhorn(q.x, q.y, q.eps, tol=q.tol, f0=f0)
+            tt = time.perf_counter() - t0
+            out["reduced_n_full_run"] = {"n": q.n, "iterations": r.iterations, "time_to_tol_s": tt,
+                                         "value": q.n * q.m * r.iterations / tt, "unit": "cost-entries/s"}
         if self.name == "c4":   # full fp64 run at reduced n: subsample init + solve to tol
             q = gen.c4(n=2048, ns=256)
             t0 = time.perf_counter()
