@@ -131,7 +131,7 @@ class C2(Workload):
         f0 = sk.sinkhorn_init_sort1d(self.ctx, x.view(self.B, self.n), y.view(self.m), y_shared=True) if init else None
         self.f, self.g, reps = sk.sinkhorn_solve(self.ctx, x, y, p.eps, tol=p.tol, max_iter=p.max_iter,
                                                  y_shared=True, f_init=f0, anderson=anderson, adaptive=adaptive)
-        self.its = np.array([r["iterations"] for r in reps])
+        self.its = reps.column("iterations")
         return float(self.n) * self.m * float(self.its.sum())
 
     def step(self):

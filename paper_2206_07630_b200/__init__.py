@@ -12,8 +12,9 @@ from __future__ import annotations
 
 import contextlib
 import ctypes
-from typing import List, Optional, Tuple
+from typing import List, Optional, Sequence, Tuple
 
+import numpy as np
 import torch
 
 from . import _lib
@@ -118,6 +119,33 @@ class Context:
 
 
 # ------------------------------------------------------------------ marshalling
+_REPORT_DTYPE = np.dtype({"names": [k for k, _ in SkReport._fields_],
+                          "formats": ["<i4", "<i4", "<f4", "<f8", "<f8", "<f8", "<f8"],
+                          "offsets": [getattr(SkReport, k).offset for k, _ in SkReport._fields_],
+                          "itemsize": ctypes.sizeof(SkReport)})
+
+
+class Reports(Sequence):
+    """The B host reports of a batched solve: a sequence of per-problem dicts (built on access)
+    over one structured array; column(name) gives a field for every problem as a numpy array
+    (no per-problem Python work - a 1024-problem batch would spend ~1 ms building dicts)."""
+
+    def __init__(self, raw):
+        self.arr = np.frombuffer(raw, dtype=_REPORT_DTYPE).copy()
+
+    def __len__(self) -> int:
+        return len(self.arr)
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            return [self[k] for k in range(*i.indices(len(self)))]
+        r = self.arr[i]
+        return {k: r[k].item() for k in self.arr.dtype.names}
+
+    def column(self, name: str) -> np.ndarray:
+        return self.arr[name]
+
+
 @contextlib.contextmanager
 def _solver_options(ctx: Context, omega=None, eps_decay=None, anderson=None, adaptive=None):
     """Set the given solver options on the context for one call, then restore the previous
@@ -268,10 +296,9 @@ def _solve(ctx, x, y, eps, tol, max_iter, check_every, a, b, y_shared, mode, f_i
                                 float(eps), float(tol), int(max_iter), int(check_every), _MODES[mode],
                                 _ptr(f_init), _ptr(g_init), _ptr(f), _ptr(g), reps)
     ctx.check(st, allow_nonfinite)
-    out = [r.as_dict() for r in reps]
     if single:
-        return f.view(n), g.view(m), out[0]
-    return f, g, out
+        return f.view(n), g.view(m), reps[0].as_dict()
+    return f, g, Reports(reps)
 
 
 def sinkhorn_init_nw1d(ctx: Context, x, y, a=None, b=None, y_shared: bool = True, max_rounds: int = 0):

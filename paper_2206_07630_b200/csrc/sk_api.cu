@@ -99,7 +99,7 @@ enum BufId {
     B_STAGE0 = 0, B_STAGE_END = 16,   // staging of host arrays
     B_FLAG = 16, B_XPACK, B_XC, B_XNK, B_XPOT, B_YPACK, B_YC, B_YNK, B_YPOT, B_PART, B_BLKE, B_BLKB,
     B_STATUS, B_COST, B_REP, B_SORT, B_PERM, B_YSORT, B_GAUSS, B_GAUSS2, B_GMM, B_SUBW, B_SUBZ,
-    B_SUBF, B_SUBG, B_IDX, B_OUT, B_FA, B_QUEUE, B_XIMG, B_YIMG, B_XLSE, B_YLSE, B_TCMAX, B_EMST, B_EMPART, B_EMIDX, B_VJP, B_ANDFR, B_ANDBLK, B_ANDVEC, B_ANDST, B_XCHG, B_PARK, B_NBUF
+    B_SUBF, B_SUBG, B_IDX, B_OUT, B_FA, B_QUEUE, B_XIMG, B_YIMG, B_XLSE, B_YLSE, B_TCMAX, B_EMST, B_EMPART, B_EMIDX, B_VJP, B_ANDFR, B_ANDBLK, B_ANDVEC, B_ANDST, B_XCHG, B_PARK, B_XCNT, B_NBUF
 };
 
 sk_status fail(sk_ctx *c, sk_status s, const char *fmt, ...) {
@@ -465,9 +465,15 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
     // blocks merged in block order: the same merge tree for every partition of the rows
     const int nblk_x = sharded ? SK_SHARD_BLOCKS : nblk_glob;
     float2 *xchg = nullptr;
+    int *xcnt = nullptr;   // K2: arrival counters of the fused premerge [8 blocks][P tiles]
     if (!stored) {
         ENSURE(xc2, float2, B_XCHG, (long long)nblk_x * m);
         xchg = xc2;
+        if (!tc) {
+            ENSURE(xc3, int, B_XCNT, (long long)SK_SHARD_BLOCKS * ptiles_col);
+            xcnt = xc3;
+            CU(cudaMemsetAsync(xcnt, 0, sizeof(int) * (size_t)SK_SHARD_BLOCKS * ptiles_col, st));
+        }
     }
     ENSURE(blke, double, B_BLKE, 2 * kMergeMaxBlocks);
     ENSURE(blkb, int, B_BLKB, 2048);
@@ -558,10 +564,14 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
                 colp.only_if = only_if;
                 colp.emu8 = T.lse_emu8;
                 colp.margin = T.lse_margin;
+                // the block partials straight into the exchange buffer (fused K6a)
+                const long long b0 = sharded ? (long long)slices[i].rank * blk_per_rank : 0;
+                colp.xchg = xchg + b0 * m;
+                colp.cnt = xcnt + b0 * ptiles_col;
                 CU(launch_lse(colp, st));
             }
             if (t0 >= 0) tm.stop(t0, sweep, LaunchTimer::COL, ent, stored ? 4.0 * ent : 0.0);
-            if (!stored) {
+            if (tc) {   // (K2 merges its blocks itself)
                 const long long xoff = sharded ? (long long)slices[i].rank * blk_per_rank * m : 0;
                 CU(launch_premerge(col_part(i), nb, split_q, m, xchg + xoff, &status->stop, only_if, st));
             }
@@ -629,11 +639,11 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
             const bool cseed = col_seed && sweep >= 2;
             CK(col_stage(nullptr, cseed));
             CK(exchange_and_merge_col(cseed ? mcol_seeded : mcol));
-            launched += (stored ? 1 : 2) * ns + 1;
+            launched += (tc ? 2 : 1) * ns + 1;   // (+ the premerge on the tensor-core path)
             if (cseed) {   // the exact redo when a seeded column sum left the safe range (no-ops otherwise)
                 CK(col_stage(&status->colfail, false));
                 CK(exchange_and_merge_col(mcol_redo));
-                launched += 2 * ns + 1;
+                launched += (tc ? 2 : 1) * ns + 1;
             }
             for (int i = 0; i < ns; ++i) {
                 const int t0 = tm.start();

@@ -172,6 +172,8 @@ struct LsePass {
     const int *only_if = nullptr;   // run only if *only_if != 0 (the exact redo of a seeded column pass)
     int emu8 = 1;     // seeded D <= 4: exponential pairs (of 8) on the FMA pipe (sk_set_tuning "lse_emu8")
     float margin = 4.f;   // seeded: log2 units above the previous LSE (sk_set_tuning "lse_margin")
+    float2 *xchg = nullptr;   // non-null: fused K6a - the block partials [nblk][P] (this slice's
+    int *cnt = nullptr;       //   slots) and the arrival counters [nblk][P tiles] (zero between launches)
 };
 // K6a: per fixed row block, the stable merge of its split_q sub-split partials in fixed order:
 // part [nblk * split_q][P] -> out [nblk][P], one (M, S) per point per block (the exchange payload

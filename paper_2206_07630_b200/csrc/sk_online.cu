@@ -95,8 +95,23 @@ struct LseArgs {
     const int *only_if;     // run only if *only_if != 0 (nullable)
     const float *seed;      // SEEDED: P side last LSE
     float margin;           // SEEDED: shift = seed + margin (log2 units)
+    float2 *xchg;           // non-null: the last CTA of each (P tile, block) merges the block's
+    int *cnt;               //   split_q partials into xchg [nblk][P] (K6a fused); cnt [nblk][P tiles]
 };
 
+
+// K6a: one point's block partial from its split_q sub-split partials src[u * P], merged in split
+// order (L2 loads: other CTAs wrote them)
+__device__ __forceinline__ float2 premerge_point(const float2 *src, int split_q, long long P) {
+    float M = -INFINITY;
+    for (int u = 0; u < split_q; ++u) M = fmaxf(M, __ldcg(src + u * P).x);
+    float S = 0.f;
+    for (int u = 0; u < split_q; ++u) {
+        const float2 v = __ldcg(src + u * P);
+        if (v.x != -INFINITY) S = fmaf(v.y, ex2(v.x - M), S);
+    }
+    return make_float2(M, S);
+}
 
 // EMU8: exponential pairs (of every 8 pairs = 2 chunks) evaluated on the FMA pipe in the
 // seeded pass (D <= 4); balances MUFU against the FMA pipe (measured by SK_LSE_EMU8 sweeps)
@@ -173,6 +188,26 @@ __global__ void __launch_bounds__(kLT) k_lse(LseArgs A) {
         const int p = blockIdx.x * (kLT * R) + r * kLT + threadIdx.x;
         if (p < A.P) A.part[(long long)s * A.P + p] = make_float2(M[r], Sx[r].x + Sx[r].y);
     }
+    if (A.xchg) {
+        // K6a fused: the last of the block's split_q CTAs for this P tile merges their partials in
+        // split order (the premerge arithmetic) while they are still in L2, and writes the block
+        // partial - the exchange payload - directly
+        __shared__ int s_last;
+        __threadfence();
+        __syncthreads();
+        int *c = A.cnt + (long long)b * gridDim.x + blockIdx.x;
+        if (threadIdx.x == 0) s_last = atomicAdd(c, 1) == A.split_q - 1;
+        __syncthreads();
+        if (!s_last) return;
+        __threadfence();
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int p = blockIdx.x * (kLT * R) + r * kLT + threadIdx.x;
+            if (p < A.P) A.xchg[(long long)b * A.P + p] = premerge_point(A.part + (long long)b * A.split_q * A.P + p,
+                                                                        A.split_q, A.P);
+        }
+        if (threadIdx.x == 0) *c = 0;   // (ready for the next launch)
+    }
 }
 
 template <int D>
@@ -197,6 +232,8 @@ static cudaError_t launch_lse_d(const LsePass &L, cudaStream_t st) {
     A.only_if = L.only_if;
     A.seed = L.Pside->lse;
     A.margin = L.margin;
+    A.xchg = L.xchg;
+    A.cnt = L.cnt;
     dim3 grid((A.P + kLT * R - 1) / (kLT * R), L.nblk * L.split_q);
     if (L.seeded && A.seed) seeded_fn<<<grid, kLT, smem, st>>>(A);
     else k_lse<D, R, false><<<grid, kLT, smem, st>>>(A);
@@ -547,15 +584,7 @@ __global__ void __launch_bounds__(256) k_premerge(const float2 *__restrict__ par
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
          t += (long long)gridDim.x * blockDim.x) {
         const long long b = t / P, p = t - b * P;
-        const float2 *src = part + b * split_q * P + p;
-        float M = -INFINITY;
-        for (int u = 0; u < split_q; ++u) M = fmaxf(M, src[u * P].x);
-        float S = 0.f;
-        for (int u = 0; u < split_q; ++u) {
-            const float2 v = src[u * P];
-            if (v.x != -INFINITY) S = fmaf(v.y, ex2(v.x - M), S);
-        }
-        out[t] = make_float2(M, S);
+        out[t] = premerge_point(part + b * split_q * P + p, split_q, P);
     }
 }
 
