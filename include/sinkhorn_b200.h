@@ -413,7 +413,8 @@ sk_status sk_selftest_tc_dot(sk_ctx *ctx, int32_t d, const float *x, const float
  * 3, 4 in flop per SM clock (cycles of the first CTA); 11 = the K3 kernel with its MMAs
  * skipped (epilogue-only rate); 12 = MMAs skipped and the epilogue only releasing the
  * buffers (operand stream and synchronisation rate); 13 = the epilogue's arithmetic without
- * MMAs or TMEM loads; 9..13 in equivalent flop per SM clock; 100 + (shape | mode << 2) = the raw
+ * MMAs or TMEM loads; 14 = the whole seeded K3 kernel (MMAs + TMEM loads + epilogue); 9..14 in
+ * equivalent flop per SM clock; 100 + (shape | mode << 2) = the raw
  * probe with diagnostic mode bits (sk_tc.cu k_mb_mma).  *value (host)
  * receives the rate.  Blocks. */
 sk_status sk_microbench(sk_ctx *ctx, int32_t kind, double *value);

@@ -76,7 +76,7 @@ class Context:
     def microbench(self, kind: str) -> float:
         """K14 roofline denominators: 'ex2' (ex2/s), 'ffma' (FMA/s), 'hbm' (read B/s), 'tc' (fp16 MMA flop/s)."""
         k = {"ex2": 0, "ffma": 1, "hbm": 2, "tc": 3, "tc_noload": 4, "mma_f16_n128": 5, "mma_f16_n256": 6,
-             "mma_tf32_n128": 7, "mma_tf32_n256": 8, "tc_clk": 9, "tc_noload_clk": 10, "tc_epi": 11, "tc_tmem": 12, "tc_math": 13}[kind] \
+             "mma_tf32_n128": 7, "mma_tf32_n256": 8, "tc_clk": 9, "tc_noload_clk": 10, "tc_epi": 11, "tc_tmem": 12, "tc_math": 13, "tc_full": 14}[kind] \
             if isinstance(kind, str) else int(kind)
         v = ctypes.c_double()
         self.check(self.lib.sk_microbench(self.h, k, ctypes.byref(v)))

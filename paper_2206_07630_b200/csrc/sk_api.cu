@@ -1665,8 +1665,8 @@ static int nsm_probe(sk_ctx *ctx) {
 }
 
 sk_status sk_microbench(sk_ctx *ctx, int32_t kind, double *value) {
-    if (!ctx || !value || kind < 0 || (kind > 13 && kind < 100) || kind > 163)
-        return fail(ctx, SK_EINVAL, "kind in [0, 13] or [100, 163]");
+    if (!ctx || !value || kind < 0 || (kind > 14 && kind < 100) || kind > 163)
+        return fail(ctx, SK_EINVAL, "kind in [0, 14] or [100, 163]");
     if ((kind >= 5 && kind <= 8) || kind >= 100) {   // raw MMA issue rate of one shape, flop per SM clock
         ENSURE(scr, long long, B_OUT, 16);
         CU(microbench_mma(kind >= 100 ? kind - 100 : kind - 5, scr, ctx->stream, value));
@@ -1701,10 +1701,12 @@ sk_status sk_microbench(sk_ctx *ctx, int32_t kind, double *value) {
         CU(cudaMemsetAsync(img, 0, tc_image_bytes(P), st));
         CU(launch_pack_tc_ext(P, nullptr, img, st));   // w = 0, shifts 0
         TcPass tp{img, img, (int)P, Q, 4, 1, 0, 37, part, 1.f, nullptr};
-        tp.mma_only = (kind == 4 || kind == 10) ? 2 : (kind == 11 ? 3 : (kind == 12 ? 4 : (kind == 13 ? 5 : 1)));
+        tp.mma_only = (kind == 4 || kind == 10) ? 2 : (kind == 11 ? 3 : (kind == 12 ? 4 : (kind == 13 ? 5 : (kind == 14 ? 0 : 1))));
+        tp.emu = ctx->tune.tc_emu;
+        tp.epi = ctx->tune.tc_epi;
         ENSURE(cyc, long long, B_FA, 16);
         tp.cyc = cyc;
-        tp.seeded = kind == 11 || kind == 13;   // the epilogue probe runs the seeded (max-free) variant, as the solver does
+        tp.seeded = kind == 11 || kind == 13 || kind == 14;   // the seeded (max-free) epilogue, as the solver runs
         CU(launch_lse_tc(tp, st));  // warm-up
         CU(cudaEventRecord(ctx->ev0, st));
         CU(launch_lse_tc(tp, st));
