@@ -234,7 +234,7 @@ def single_spec(args):
                   kernel="k_lse<3,4> (online LSE pass, K2)")
     else:
         sp.update(p=gen.c5(eps_factor=args.eps_factor or 1e-2), init=args.init or "gaussian", mode="online",
-                  roof="tensor", kernel="k_lse_tc2 (online LSE pass, CTA-pair tcgen05 kind::f16 3-product hi/lo "
+                  roof="tensor", scaling="strong", kernel="k_lse_tc2 (online LSE pass, CTA-pair tcgen05 kind::f16 3-product hi/lo "
                                         "cross term with w and the row shift folded into the MMA, K3)")
         if args.ffma:   # comparison leg: the FFMA kernel at d = 64
             sp.update(roof="fp32", kernel="k_lse<64,1> (online LSE pass, FFMA2 cross term, K2)")
@@ -243,7 +243,7 @@ def single_spec(args):
 
 def single_config(sp, args, world):
     p, name = sp["p"], sp["name"]
-    sharded = name == "c4" and (world > 1 or args.force_sharded)
+    sharded = name in ("c4", "c5") and (world > 1 or args.force_sharded)
     c = {"workload": {"c1": "BJ.cfg1 (C1): n=m=256, d=2, Gaussian clouds, eps=0.01*mean(C)",
                       "c3": f"BJ.cfg3 (C3): n=m=16384, d=16 GMM clouds, stored-cost mode (1 GiB C), eps={p.eps:.4g}",
                       "c4": "BJ.cfg4 (C4): n=m=262144, d=3 RGB-pixel mixtures, eps=1e-2, online cost",
@@ -276,13 +276,14 @@ class Single(Workload):
             ctx.set_tuning("tc", 0)
         p = self.p
         self.n, self.m, self.d = p.n, p.m, p.d
-        self.sharded = self.name == "c4" and (world > 1 or args.force_sharded)
+        # C4 and C5 (BJ.cfg4/5: "1/2/4/8 GPUs") shard their rows; C1/C3 run replicas
+        self.sharded = self.name in ("c4", "c5") and (world > 1 or args.force_sharded)
         if self.sharded:
             from paper_2206_07630_b200 import dist as skd
             skd.init_comm(ctx)
             if world == 1:   # (--force-sharded: the 1-rank communicator takes the NCCL data plane)
                 ctx.set_force_nccl(True)
-        self.row0, self.nl = sk.shard_rows(p.n, rank, world) if self.name == "c4" else (0, p.n)
+        self.row0, self.nl = sk.shard_rows(p.n, rank, world) if self.sharded else (0, p.n)
         self.x = torch.from_numpy(p.x).to(dev)
         self.y = torch.from_numpy(p.y).to(dev)
         self.xh = torch.from_numpy(p.x).pin_memory()

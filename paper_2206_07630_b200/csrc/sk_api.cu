@@ -440,8 +440,11 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
     const long long bs_rows = shard_block_rows(n_glob);
     const int nblk_glob = (int)((n_glob + bs_rows - 1) / bs_rows);
     const int blk_per_rank = sharded ? SK_SHARD_BLOCKS / P.world : nblk_glob;
-    const int occ = stored ? 8 : (tc ? 1 : lse_occupancy_ctas(D));
-    const int Rr = tc ? 1 : (D <= 4 ? 4 : (D <= 16 ? 2 : 1));
+    // small online problems (d <= 4): one output point per thread, so their few P tiles still fill
+    // the SMs (a function of the global sizes: the split structure stays partition-invariant)
+    const bool r1 = !stored && !tc && D <= 4 && std::max(n_glob, m) <= 16384;
+    const int occ = stored ? 8 : (tc ? 1 : lse_occupancy_ctas(D, r1 ? 1 : 0));
+    const int Rr = tc ? 1 : (r1 ? 1 : (D <= 4 ? 4 : (D <= 16 ? 2 : 1)));
     const long long pcta = tc ? tc_points_per_tile() : 128LL * Rr;   // output points per CTA (pair)
     const long long ptiles_col = stored ? (m + 511) / 512 : (m + pcta - 1) / pcta;
     int nsm = 148;
@@ -564,6 +567,7 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
                 colp.only_if = only_if;
                 colp.emu8 = T.lse_emu8;
                 colp.margin = T.lse_margin;
+                colp.R = r1 ? 1 : 0;
                 // the block partials straight into the exchange buffer (fused K6a)
                 const long long b0 = sharded ? (long long)slices[i].rank * blk_per_rank : 0;
                 colp.xchg = xchg + b0 * m;
@@ -662,6 +666,7 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
                     rowp.seeded = row_seed && sweep >= 2;
                     rowp.emu8 = T.lse_emu8;
                     rowp.margin = T.lse_margin;
+                    rowp.R = r1 ? 1 : 0;
                     CU(launch_lse(rowp, st));
                 }
                 tm.stop(t0, sweep, LaunchTimer::ROW, (double)slices[i].n * m, stored ? 4.0 * slices[i].n * m : 0.0);

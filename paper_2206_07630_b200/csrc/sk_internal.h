@@ -172,6 +172,7 @@ struct LsePass {
     const int *only_if = nullptr;   // run only if *only_if != 0 (the exact redo of a seeded column pass)
     int emu8 = 1;     // seeded D <= 4: exponential pairs (of 8) on the FMA pipe (sk_set_tuning "lse_emu8")
     float margin = 4.f;   // seeded: log2 units above the previous LSE (sk_set_tuning "lse_margin")
+    int R = 0;            // output points per thread: 0 = the default for D, 1 = one (D <= 4: small problems)
     float2 *xchg = nullptr;   // non-null: fused K6a - the block partials [nblk][P] (this slice's
     int *cnt = nullptr;       //   slots) and the arrival counters [nblk][P tiles] (zero between launches)
 };
@@ -181,7 +182,7 @@ struct LsePass {
 cudaError_t launch_premerge(const float2 *part, int nblk, int split_q, long long P, float2 *out, const int *stop,
                             const int *only_if, cudaStream_t st);
 cudaError_t launch_lse(const LsePass &L, cudaStream_t st);
-int lse_occupancy_ctas(int D);  // resident CTAs per SM of the LSE kernel for D
+int lse_occupancy_ctas(int D, int R = 0);  // resident CTAs per SM of the LSE kernel for D (R = 0: default)
 
 enum MergeMode { MERGE_COL = 0, MERGE_ROW = 1, MERGE_OUT = 2 };
 struct MergePass {

@@ -210,9 +210,8 @@ __global__ void __launch_bounds__(kLT) k_lse(LseArgs A) {
     }
 }
 
-template <int D>
-static cudaError_t launch_lse_d(const LsePass &L, cudaStream_t st) {
-    constexpr int R = kR<D>;
+template <int D, int R>
+static cudaError_t launch_lse_dr(const LsePass &L, cudaStream_t st) {
     constexpr int TQ = D <= 4 ? 256 : (D <= 16 ? 128 : 64);
     const size_t smem = (size_t)kStages * (D + 1) * TQ * sizeof(float);
     cudaError_t e = cudaFuncSetAttribute(k_lse<D, R, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -240,6 +239,15 @@ static cudaError_t launch_lse_d(const LsePass &L, cudaStream_t st) {
     return cudaGetLastError();
 }
 
+// R: output points per thread (small problems: one, so that their few P tiles still fill the
+// SMs; a point's sum does not depend on R - only the split structure fixes the order)
+template <int D>
+static cudaError_t launch_lse_d(const LsePass &L, cudaStream_t st) {
+    if constexpr (kR<D> > 1)
+        if (L.R == 1) return launch_lse_dr<D, 1>(L, st);
+    return launch_lse_dr<D, kR<D>>(L, st);
+}
+
 cudaError_t launch_lse(const LsePass &L, cudaStream_t st) {
     switch (L.Pside->D) {
         case 1: return launch_lse_d<1>(L, st);
@@ -254,9 +262,8 @@ cudaError_t launch_lse(const LsePass &L, cudaStream_t st) {
     }
 }
 
-template <int D>
+template <int D, int R = kR<D>>
 static int occ_d() {
-    constexpr int R = kR<D>;
     constexpr int TQ = D <= 4 ? 256 : (D <= 16 ? 128 : 64);
     const size_t smem = (size_t)kStages * (D + 1) * TQ * sizeof(float);
     cudaFuncSetAttribute(k_lse<D, R, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -265,7 +272,15 @@ static int occ_d() {
     return n > 0 ? n : 1;
 }
 
-int lse_occupancy_ctas(int D) {
+int lse_occupancy_ctas(int D, int R) {
+    if (R == 1 && D <= 4) {
+        switch (D) {
+            case 1: return occ_d<1, 1>();
+            case 2: return occ_d<2, 1>();
+            case 3: return occ_d<3, 1>();
+            default: return occ_d<4, 1>();
+        }
+    }
     switch (D) {
         case 1: return occ_d<1>();
         case 2: return occ_d<2>();
