@@ -345,7 +345,7 @@ class Single(Workload):
         self.split_ms = {"init_ms": ev[0].elapsed_time(ev[1]), "solve_call_ms": ev[1].elapsed_time(ev[2]),
                          "solve_loop_ms": rep["solve_ms"], "build_ms": rep["build_ms"]}
         self.rep = rep
-        return float(self.n) * self.m * rep["iterations"] / self.world   # each rank's share
+        return float(self.n) * self.m * rep["iterations"] / (self.world if self.sharded else 1)   # this rank's share
 
     def step(self):
         e = self._run(self.x, self.y)
@@ -381,7 +381,7 @@ class Single(Workload):
             torch.cuda.synchronize()
             ms = e0.elapsed_time(e1) / reps
             out["anderson5"] = {"time_to_tol_ms": ms, "iterations": self.rep["iterations"],
-                                "converged": self.rep["converged"], "cost_entries_per_s": ent * self.world / (ms / 1e3),
+                                "converged": self.rep["converged"], "cost_entries_per_s": ent / (ms / 1e3),
                                 "solve_ms": self.rep["solve_ms"],
                                 "note": "same init + Anderson (memory 5) to the same tol (K13 / K19)"}
             # adaptive momentum (window 10; R-31), same step
@@ -394,7 +394,7 @@ class Single(Workload):
             ms = e0.elapsed_time(e1) / reps
             out["adaptive10"] = {"time_to_tol_ms": ms, "iterations": self.rep["iterations"],
                                  "converged": self.rep["converged"],
-                                 "cost_entries_per_s": ent * self.world / (ms / 1e3),
+                                 "cost_entries_per_s": ent / (ms / 1e3),
                                  "note": "same init + adaptive momentum (window 10) to the same tol"}
         return out
 
