@@ -169,7 +169,8 @@ sk_status sk_get_solver_options(const sk_ctx *ctx, float *omega, float *decay_in
  *       beyond ~100 forces every seeded point through its exact fallback / the column redo);
  *   "lse_emu8" 0..2 (1): K2 seeded (d <= 4) exponential pairs of 8 on the FMA pipe;
  *   "tc_emu" 0..6 (2): K3 exponential pairs of 8 on the FMA pipe;
- *   "tc_epi" 16|162 (162): K3 epilogue organisation;
+ *   "tc_epi" 16|162 (16): K3 epilogue organisation (16 warps on every tile, or two tile groups of 8);
+ *   "tc_pipe" 0|1 (0): K3 seeded epilogue with software-pipelined TMEM loads (tile groups only);
  *   "batched_shape" 0|1 (1): K13 512 threads x 2 points (1) or 1024 x 1 (0) for 512 < P <= 1024;
  *   "batched_cl" 0..2 (0): K13 one CTA (1) or a CTA pair (2) per problem (0: pair only for B = 1);
  *   "batched_park" >= 0 (12): K13 batches with more problems than resident CTAs run at most this

@@ -87,7 +87,8 @@ struct sk_ctx {
         float lse_margin = 4.f; // K2 seeded shift above the previous LSE (log2 units)
         int lse_emu8 = 1;       // K2 seeded D <= 4: exponential pairs of 8 on the FMA pipe
         int tc_emu = 2;         // K3: exponential pairs of 8 on the FMA pipe
-        int tc_epi = 162;       // K3 epilogue organisation (162 or 16)
+        int tc_epi = 16;        // K3 epilogue organisation (16 or 162)
+        int tc_pipe = 0;        // K3 seeded epilogue with software-pipelined TMEM loads
         int batched_shape = 1;  // K13: 512 x 2 points for 512 < P <= 1024 (0: 1024 x 1)
         int batched_cl = 0;     // K13: 0 auto, 1 one CTA, 2 a CTA pair per problem
         int batched_park = 12;  // K13 batches: sweeps per turn of the park / resume scheduler (0: off)
@@ -560,6 +561,7 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
                 colp.only_if = only_if;
                 colp.emu = T.tc_emu;
                 colp.epi = T.tc_epi;
+                colp.pipe = T.tc_pipe;
                 CU(launch_lse_tc(colp, st));
             } else {
                 LsePass colp{&Y, &X[i], nb, (int)(bs_rows / tq), split_q, col_part(i), P.eps, &status->stop};
@@ -660,6 +662,7 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
                     rowp.seeded = row_seed && sweep >= 2;
                     rowp.emu = T.tc_emu;
                     rowp.epi = T.tc_epi;
+                    rowp.pipe = T.tc_pipe;
                     CU(launch_lse_tc(rowp, st));
                 } else {
                     LsePass rowp{&X[i], &Y, 1, 0, split_row, part, P.eps, &status->stop};
@@ -911,6 +914,7 @@ sk_status sk_set_tuning(sk_ctx *ctx, const char *key, double value) {
     else if (k == "lse_emu8") { CK(need(iv >= 0 && iv <= 2)); T.lse_emu8 = iv; }
     else if (k == "tc_emu") { CK(need(iv >= 0 && iv <= 6)); T.tc_emu = iv; }
     else if (k == "tc_epi") { CK(need(iv == 16 || iv == 162)); T.tc_epi = iv; }
+    else if (k == "tc_pipe") { CK(need(iv == 0 || iv == 1)); T.tc_pipe = iv; }
     else if (k == "batched_shape") { CK(need(iv == 0 || iv == 1)); T.batched_shape = iv; }
     else if (k == "batched_cl") { CK(need(iv >= 0 && iv <= 2)); T.batched_cl = iv; }
     else if (k == "batched_park") { CK(need(iv >= 0 && iv <= 100000)); T.batched_park = iv; }
@@ -1709,6 +1713,7 @@ sk_status sk_microbench(sk_ctx *ctx, int32_t kind, double *value) {
         tp.mma_only = (kind == 4 || kind == 10) ? 2 : (kind == 11 ? 3 : (kind == 12 ? 4 : (kind == 13 ? 5 : (kind == 14 ? 0 : 1))));
         tp.emu = ctx->tune.tc_emu;
         tp.epi = ctx->tune.tc_epi;
+        tp.pipe = ctx->tune.tc_pipe;
         ENSURE(cyc, long long, B_FA, 16);
         tp.cyc = cyc;
         tp.seeded = kind == 11 || kind == 13 || kind == 14;   // the seeded (max-free) epilogue, as the solver runs

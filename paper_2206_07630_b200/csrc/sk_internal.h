@@ -146,7 +146,8 @@ struct TcPass {
     int seeded = 0;             // the output side's shifts were folded by K6 (max-free pass)
     const int *only_if = nullptr;   // run only if *only_if != 0 (the exact redo of a seeded column pass)
     int emu = 2;                // exponential pairs (of every 8) on the FMA pipe (sk_set_tuning "tc_emu")
-    int epi = 162;              // epilogue organisation (sk_set_tuning "tc_epi": 162 or 16)
+    int epi = 16;               // epilogue organisation (sk_set_tuning "tc_epi": 16 or 162)
+    int pipe = 0;               // seeded epilogue with software-pipelined TMEM loads (sk_set_tuning "tc_pipe")
 };
 size_t tc_image_bytes(long long P);
 cudaError_t launch_absmax(const float *pts, long long cnt, unsigned *out, cudaStream_t st);  // out zeroed first

@@ -202,6 +202,22 @@ __device__ __forceinline__ float2 tc_sum_chunk(const float2 (&t)[32], float M) {
     return add2(s0, s1);
 }
 
+// the same over one 32-column chunk (16 pairs; seeded: M = 0), the FMA-pipe pairs as above
+template <int EMU>
+__device__ __forceinline__ float2 tc_sum_half(const uint32_t (&r)[32]) {
+    float2 s0 = make_float2(0.f, 0.f), s1 = s0;
+#pragma unroll
+    for (int j = 0; j < 16; j += 2) {
+        float2 e0 = make_float2(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
+        float2 e1 = make_float2(__uint_as_float(r[2 * j + 2]), __uint_as_float(r[2 * j + 3]));
+        if ((j & 7) >= 8 - EMU) e0 = ex2_emu2(e0); else { e0.x = ex2(e0.x); e0.y = ex2(e0.y); }
+        if (((j + 1) & 7) >= 8 - EMU) e1 = ex2_emu2(e1); else { e1.x = ex2(e1.x); e1.y = ex2(e1.y); }
+        s0 = add2(s0, e0);
+        s1 = add2(s1, e1);
+    }
+    return add2(s0, s1);
+}
+
 // cta_group::2: the pair computes a 256 x 256 tile per MMA group (M = 256 split over the two
 // SMs' A halves, N = 256 split over their B halves).  Roles per CTA (rank r of the pair):
 //   warp 0   producer: A half (points 256 pt + 128 r: [hi | lo | EA], 36 KB) once per item, B
@@ -253,7 +269,7 @@ __device__ __forceinline__ void umma2_commit_mc(uint64_t *bar) {
 }
 
 
-template <int EMU, int NE, bool SEEDED, int G>
+template <int EMU, int NE, bool SEEDED, int G, int PL = 0, bool DBG = false>
 __global__ void __launch_bounds__(64 + 32 * NE, 1) k_lse_tc2(TcArgs A) {
     constexpr int NQ = NE / 4;                       // epilogue warps per TMEM lane quadrant
     // G tile groups: group k's warps take the tiles g with g % G == k (accumulator buffer k when
@@ -413,7 +429,9 @@ __global__ void __launch_bounds__(64 + 32 * NE, 1) k_lse_tc2(TcArgs A) {
             int t0, nt;
             range(s, t0, nt);
             const int p = pt * kT2N + (int)rank * kTcM + row;
-            const bool dbg = A.debug_acc && leader && it == 0 && grp == 0 && hc * CW < kTcM;
+            // (DBG: the selftest's raw accumulator dump - its own instantiation, so that the
+            // division code stays out of the solver's epilogue loop and instruction cache)
+            const bool dbg = DBG && A.debug_acc && leader && it == 0 && grp == 0 && hc * CW < kTcM;
             // seeded: the row shift sh_p (previous LSE + margin, folded by K6) is already
             // subtracted by the MMA: no running max (k_merge recomputes a point exactly if its
             // sum leaves [2^-100, 2^100]); unseeded: running max of t - sh_p
@@ -433,6 +451,35 @@ __global__ void __launch_bounds__(64 + 32 * NE, 1) k_lse_tc2(TcArgs A) {
                     continue;
                 }
                 const uint32_t taddr = tbase + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(b * kT2N + hc * CW);
+                if constexpr (SEEDED && PL) {
+                    // software-pipelined: 32-column chunks double-buffered in registers - the next
+                    // chunk's tcgen05.ld is in flight while this chunk's exponentials run (the
+                    // wait::ld at the end of an iteration only covers that one load)
+                    uint32_t ra[32], rb[32];
+                    TMEM_LD32(taddr, ra);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int c = 0; c < CW / 32; c += 2) {
+                        TMEM_LD32(taddr + (c + 1) * 32, rb);
+                        {
+                            const float2 sc = tc_sum_half<EMU>(ra);
+                            S += sc.x + sc.y;
+                        }
+                        tmem_ld_wait();
+                        if (c + 2 < CW / 32) TMEM_LD32(taddr + (c + 2) * 32, ra);
+                        else {   // every load of accumulator b has retired: release it
+                            tc_fence_before();
+                            __syncwarp();
+                            if (lane == 0) mbar_arrive_cluster(r_tempty + 8 * b);
+                        }
+                        {
+                            const float2 sc = tc_sum_half<EMU>(rb);
+                            S += sc.x + sc.y;
+                        }
+                        if (c + 2 < CW / 32) tmem_ld_wait();
+                    }
+                    continue;
+                }
 #pragma unroll
                 for (int hh = 0; hh < CW / 64; ++hh) {   // 64-column chunks
                     uint32_t r[64];
@@ -450,7 +497,7 @@ __global__ void __launch_bounds__(64 + 32 * NE, 1) k_lse_tc2(TcArgs A) {
                         __syncwarp();
                         if (lane == 0) mbar_arrive_cluster(r_tempty + 8 * b);
                     }
-                    if (dbg && i == 0) {
+                    if (DBG && dbg && i == 0) {
 #pragma unroll
                         for (int j = 0; j < 64; ++j)
                             A.debug_acc[row * kTcM + hc * CW + hh * 64 + j] = __fdiv_rn(__uint_as_float(r[j]), A.tk);
@@ -636,12 +683,12 @@ bool tc_fold_ok(float amax_x, float amax_y, float eps) {
     return mx <= 8192.0 && my <= 8192.0;
 }
 
-template <int EMU, int NE, bool SEEDED, int G>
+template <int EMU, int NE, bool SEEDED, int G, int PL = 0, bool DBG = false>
 static cudaError_t launch_tc2(const TcArgs &A, int items, cudaStream_t st) {
     constexpr int ABUF = 2;
     constexpr size_t STAGE = 2 * (size_t)kTcImg + kTcExtBytes;
     const size_t smem = 1024 + ABUF * STAGE + kT2Stages * STAGE + (NE / 4 - 1) * kTcM * 8;
-    cudaError_t e = cudaFuncSetAttribute(k_lse_tc2<EMU, NE, SEEDED, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(k_lse_tc2<EMU, NE, SEEDED, G, PL, DBG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int nsm = 148, dev = 0;
     cudaGetDevice(&dev);
@@ -657,14 +704,17 @@ static cudaError_t launch_tc2(const TcArgs &A, int items, cudaStream_t st) {
     at[0].val.clusterDim.x = 2; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, k_lse_tc2<EMU, NE, SEEDED, G>, A);
+    return cudaLaunchKernelEx(&cfg, k_lse_tc2<EMU, NE, SEEDED, G, PL, DBG>, A);
 }
 
 template <int EMU>
-static cudaError_t launch_tc2_ne(const TcArgs &A, int items, bool seeded, int ne, cudaStream_t st) {
+static cudaError_t launch_tc2_ne(const TcArgs &A, int items, bool seeded, int ne, int pipe, cudaStream_t st) {
     // epilogue organisation (sk_set_tuning "tc_epi"): 162 = 16 warps in two tile groups (even /
     // odd tiles, 128 columns per warp); 16 = four warps per TMEM lane quadrant on every tile
-    if (seeded) return ne == 16 ? launch_tc2<EMU, 16, true, 1>(A, items, st) : launch_tc2<EMU, 16, true, 2>(A, items, st);
+    if (seeded) {
+        if (pipe && ne != 16) return launch_tc2<EMU, 16, true, 2, 1>(A, items, st);
+        return ne == 16 ? launch_tc2<EMU, 16, true, 1>(A, items, st) : launch_tc2<EMU, 16, true, 2>(A, items, st);
+    }
     return ne == 16 ? launch_tc2<EMU, 16, false, 1>(A, items, st) : launch_tc2<EMU, 16, false, 2>(A, items, st);
 }
 
@@ -687,14 +737,15 @@ cudaError_t launch_lse_tc(const TcPass &L, cudaStream_t st) {
     A.blk_tiles = L.blk_tiles;
     const int items = A.ptiles * L.nblk * L.split_q;
     const bool seeded = L.seeded != 0;
+    if (L.debug_acc) return launch_tc2<2, 16, false, 2, 0, true>(A, items, st);   // (selftest)
     switch (emu) {
-        case 0: return launch_tc2_ne<0>(A, items, seeded, ne, st);
-        case 1: return launch_tc2_ne<1>(A, items, seeded, ne, st);
-        case 3: return launch_tc2_ne<3>(A, items, seeded, ne, st);
-        case 4: return launch_tc2_ne<4>(A, items, seeded, ne, st);
-        case 5: return launch_tc2_ne<5>(A, items, seeded, ne, st);
-        case 6: return launch_tc2_ne<6>(A, items, seeded, ne, st);
-        default: return launch_tc2_ne<2>(A, items, seeded, ne, st);
+        case 0: return launch_tc2_ne<0>(A, items, seeded, ne, L.pipe, st);
+        case 1: return launch_tc2_ne<1>(A, items, seeded, ne, L.pipe, st);
+        case 3: return launch_tc2_ne<3>(A, items, seeded, ne, L.pipe, st);
+        case 4: return launch_tc2_ne<4>(A, items, seeded, ne, L.pipe, st);
+        case 5: return launch_tc2_ne<5>(A, items, seeded, ne, L.pipe, st);
+        case 6: return launch_tc2_ne<6>(A, items, seeded, ne, L.pipe, st);
+        default: return launch_tc2_ne<2>(A, items, seeded, ne, L.pipe, st);
     }
 }
 
