@@ -3,10 +3,11 @@
 * the fixed row partition agrees across ranks and covers [0, n);
 * the NCCL unique id moves from rank 0 to every rank over the process group;
 * max/sum reductions used by bench.py's max-over-ranks timing;
-* the decomposition the sharded solver implements — per-rank column partials of the
-  g-pass over its row block, gathered and merged in rank order — reproduces the
-  unsharded fp64 oracle, for one g-update and for a whole sharded Sinkhorn run
-  (oracle arithmetic; the gloo all_gather stands in for ncclAllGather).
+* the decomposition the sharded solver implements — column partials of the g-pass per
+  sub-split of each fixed row block, merged per block on the rank, the block partials gathered
+  and merged in block order — reproduces the unsharded fp64 oracle, for one g-update and for a
+  whole sharded Sinkhorn run (oracle arithmetic; the gloo all_gather stands in for
+  ncclAllGather).
 """
 import os
 import socket
@@ -62,12 +63,33 @@ def _worker(rank, world, port, q):
         r0, nl = skd.shard_plan(len(x), world)[rank]
         rows = slice(r0, r0 + nl)
 
-        def sharded_g(f):
-            M, S = O.column_partials(x[rows], y, f[rows], eps)
-            allM, allS = [None] * world, [None] * world
-            dist.all_gather_object(allM, M)
-            dist.all_gather_object(allS, S)
-            return O.merge_partials(list(zip(allM, allS)), np.full(len(y), 1 / len(y)), eps)
+        # the solver's two-level merge tree: each fixed row block (SK_SHARD_BLOCKS of them) is cut
+        # into sub-splits; a rank merges its blocks' sub-split partials per block (K6a), the block
+        # partials are all-gathered (ncclAllGather in the library) and merged in block order
+        B8 = 8
+        bs = -(-len(x) // B8)
+        bs = -(-bs // 256) * 256
+
+        def lse_merge(parts):
+            M = np.max([p_[0] for p_ in parts], axis=0)
+            S = np.zeros_like(M)
+            for Mp, Sp in parts:
+                S = S + Sp * np.exp(Mp - M)
+            return M, S
+
+        def sharded_g(f, split_q=3):
+            mine = []
+            for b in range(B8):
+                lo, hi = max(b * bs, r0), min((b + 1) * bs, r0 + nl)
+                if lo >= hi:
+                    continue
+                cuts = [lo + (hi - lo) * u // split_q for u in range(split_q + 1)]
+                subs = [O.column_partials(x[c0:c1], y, f[c0:c1], eps) for c0, c1 in zip(cuts, cuts[1:]) if c1 > c0]
+                mine.append((b, lse_merge(subs)))
+            gathered = [None] * world
+            dist.all_gather_object(gathered, mine)
+            blocks = sorted((b, ms) for part in gathered for b, ms in part)
+            return O.merge_partials([ms for _, ms in blocks], np.full(len(y), 1 / len(y)), eps)
 
         f = np.random.default_rng(7).standard_normal(len(x)) * 0.01
         g_sh = sharded_g(f)
