@@ -97,6 +97,7 @@ struct LseArgs {
     float margin;           // SEEDED: shift = seed + margin (log2 units)
     float2 *xchg;           // non-null: the last CTA of each (P tile, block) merges the block's
     int *cnt;               //   split_q partials into xchg [nblk][P] (K6a fused); cnt [nblk][P tiles]
+    int ptiles;             // P tiles (the 1D grid of the fused premerge)
 };
 
 
@@ -124,8 +125,18 @@ __global__ void __launch_bounds__(kLT) k_lse(LseArgs A) {
     if (A.stop && *(volatile const int *)A.stop) return;
     if (A.only_if && !*(volatile const int *)A.only_if) return;
 
-    // ---- this CTA's Q range: split s = blockIdx.y -> block b, sub-split u
-    const int s = blockIdx.y;
+    // ---- this CTA's P tile px and Q range: split s -> block b, sub-split u.  2D grid (P tiles,
+    // splits); with the fused premerge a 1D grid with the sub-split fastest, so that a (P tile,
+    // block)'s split_q CTAs run back to back and their partials are merged (and discarded) from L2
+    int s, px;
+    if (A.xchg) {
+        const int id = blockIdx.x, uu = id % A.split_q, rr = id / A.split_q;
+        px = rr % A.ptiles;
+        s = (rr / A.ptiles) * A.split_q + uu;
+    } else {
+        s = blockIdx.y;
+        px = blockIdx.x;
+    }
     const int b = s / A.split_q, u = s % A.split_q;
     const int bt = A.blk_tiles > 0 ? A.blk_tiles : A.Qtiles;
     const int base = b * bt;
@@ -140,7 +151,7 @@ __global__ void __launch_bounds__(kLT) k_lse(LseArgs A) {
     float2 Sx[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-        const int p = blockIdx.x * (kLT * R) + r * kLT + threadIdx.x;
+        const int p = px * (kLT * R) + r * kLT + threadIdx.x;
         const int pt = p / A.Ptq, po = p % A.Ptq;
         const float *tile = A.Ppack + (long long)pt * (D + 1) * A.Ptq;
 #pragma unroll
@@ -185,7 +196,7 @@ __global__ void __launch_bounds__(kLT) k_lse(LseArgs A) {
 
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-        const int p = blockIdx.x * (kLT * R) + r * kLT + threadIdx.x;
+        const int p = px * (kLT * R) + r * kLT + threadIdx.x;
         if (p < A.P) A.part[(long long)s * A.P + p] = make_float2(M[r], Sx[r].x + Sx[r].y);
     }
     if (A.xchg) {
@@ -195,18 +206,30 @@ __global__ void __launch_bounds__(kLT) k_lse(LseArgs A) {
         __shared__ int s_last;
         __threadfence();
         __syncthreads();
-        int *c = A.cnt + (long long)b * gridDim.x + blockIdx.x;
+        int *c = A.cnt + (long long)b * A.ptiles + px;
         if (threadIdx.x == 0) s_last = atomicAdd(c, 1) == A.split_q - 1;
         __syncthreads();
         if (!s_last) return;
         __threadfence();
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-            const int p = blockIdx.x * (kLT * R) + r * kLT + threadIdx.x;
+            const int p = px * (kLT * R) + r * kLT + threadIdx.x;
             if (p < A.P) A.xchg[(long long)b * A.P + p] = premerge_point(A.part + (long long)b * A.split_q * A.P + p,
                                                                         A.split_q, A.P);
         }
         if (threadIdx.x == 0) *c = 0;   // (ready for the next launch)
+        // the group's sub-split partials are dead: drop their L2 lines without writing them back
+        // (only whole 128-byte lines inside the group's partial rows)
+        // (per sub-split row: the whole 128-byte lines inside [p0, p1) - rows start anywhere)
+        __syncthreads();
+        const int p0 = px * kLT * R, p1 = min(A.P, p0 + kLT * R);
+        for (int uu = 0; uu < A.split_q; ++uu) {
+            const float2 *rowp = A.part + ((long long)b * A.split_q + uu) * A.P;
+            const unsigned long long a0 = (reinterpret_cast<unsigned long long>(rowp + p0) + 127ull) & ~127ull;
+            const unsigned long long a1 = reinterpret_cast<unsigned long long>(rowp + p1) & ~127ull;
+            for (unsigned long long a = a0 + 128ull * threadIdx.x; a < a1; a += 128ull * kLT)
+                asm volatile("discard.global.L2 [%0], 128;" ::"l"(a) : "memory");
+        }
     }
 }
 
@@ -233,7 +256,9 @@ static cudaError_t launch_lse_dr(const LsePass &L, cudaStream_t st) {
     A.margin = L.margin;
     A.xchg = L.xchg;
     A.cnt = L.cnt;
-    dim3 grid((A.P + kLT * R - 1) / (kLT * R), L.nblk * L.split_q);
+    A.ptiles = (A.P + kLT * R - 1) / (kLT * R);
+    dim3 grid(A.ptiles, L.nblk * L.split_q);
+    if (A.xchg) grid = dim3((unsigned)A.ptiles * L.nblk * L.split_q, 1);
     if (L.seeded && A.seed) seeded_fn<<<grid, kLT, smem, st>>>(A);
     else k_lse<D, R, false><<<grid, kLT, smem, st>>>(A);
     return cudaGetLastError();
