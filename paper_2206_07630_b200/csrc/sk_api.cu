@@ -100,7 +100,7 @@ enum BufId {
     B_STAGE0 = 0, B_STAGE_END = 16,   // staging of host arrays
     B_FLAG = 16, B_XPACK, B_XC, B_XNK, B_XPOT, B_YPACK, B_YC, B_YNK, B_YPOT, B_PART, B_BLKE, B_BLKB,
     B_STATUS, B_COST, B_REP, B_SORT, B_PERM, B_YSORT, B_GAUSS, B_GAUSS2, B_GMM, B_SUBW, B_SUBZ,
-    B_SUBF, B_SUBG, B_IDX, B_OUT, B_FA, B_QUEUE, B_XIMG, B_YIMG, B_XLSE, B_YLSE, B_TCMAX, B_EMST, B_EMPART, B_EMIDX, B_VJP, B_ANDFR, B_ANDBLK, B_ANDVEC, B_ANDST, B_XCHG, B_PARK, B_XCNT, B_NBUF
+    B_SUBF, B_SUBG, B_IDX, B_OUT, B_FA, B_QUEUE, B_XIMG, B_YIMG, B_XLSE, B_YLSE, B_TCMAX, B_EMST, B_EMPART, B_EMIDX, B_VJP, B_ANDFR, B_ANDBLK, B_ANDVEC, B_ANDST, B_XCHG, B_PARK, B_XCNT, B_XROW, B_XCNT2, B_NBUF
 };
 
 sk_status fail(sk_ctx *c, sk_status s, const char *fmt, ...) {
@@ -479,6 +479,18 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
             CU(cudaMemsetAsync(xcnt, 0, sizeof(int) * (size_t)SK_SHARD_BLOCKS * ptiles_col, st));
         }
     }
+    // K2 row pass: its split_row partials merged per P tile the same way into one (M, S) per row
+    // (xrow), which the row merge then reads as a single split
+    float2 *xrow = nullptr;
+    int *xcnt2 = nullptr;
+    if (!stored && !tc) {
+        const long long ptiles_rmax = (n_max + pcta - 1) / pcta;
+        ENSURE(xr2, float2, B_XROW, n_max);
+        ENSURE(xr3, int, B_XCNT2, ptiles_rmax);
+        xrow = xr2;
+        xcnt2 = xr3;
+        CU(cudaMemsetAsync(xcnt2, 0, sizeof(int) * (size_t)ptiles_rmax, st));
+    }
     ENSURE(blke, double, B_BLKE, 2 * kMergeMaxBlocks);
     ENSURE(blkb, int, B_BLKB, 2048);
 
@@ -670,12 +682,14 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
                     rowp.emu8 = T.lse_emu8;
                     rowp.margin = T.lse_margin;
                     rowp.R = r1 ? 1 : 0;
+                    rowp.xchg = xrow;
+                    rowp.cnt = xcnt2;
                     CU(launch_lse(rowp, st));
                 }
                 tm.stop(t0, sweep, LaunchTimer::ROW, (double)slices[i].n * m, stored ? 4.0 * slices[i].n * m : 0.0);
                 // only the last slice's merge advances the sweep counter
-                MergePass mrow{MERGE_ROW, &X[i], part, stored ? 1 : split_row, P.eps, nullptr, status, blke,
-                               blkb, nullptr, 0.f, sharded ? 1 : 0, i + 1 < ns ? 1 : 0};
+                MergePass mrow{MERGE_ROW, &X[i], xrow ? xrow : part, (stored || xrow) ? 1 : split_row, P.eps, nullptr,
+                               status, blke, blkb, nullptr, 0.f, sharded ? 1 : 0, i + 1 < ns ? 1 : 0};
                 if (row_seed) mrow.Q = &Y;
                 mrow.omega = P.omega;
                 mrow.adapt = adapt;
