@@ -260,6 +260,8 @@ def single_config(sp, args, world):
                         "em_tol": args.gmm_tol, "start": "gen.gmm_start_idx seeds 3/4 (R-23/R-28)"}
     if name == "c5" and args.ffma:
         c["kernel_variant"] = "FFMA cross term (sk_set_tuning tc=0)"
+    if args.tune:
+        c["tuning"] = dict(t.split("=", 1) for t in args.tune)
     return c
 
 
@@ -590,6 +592,9 @@ def run_ours(args):
     torch.cuda.set_device(dev)
     stream = torch.cuda.Stream(dev)
     ctx = sk.Context(dev.index, stream)
+    for t in args.tune:
+        key, val = t.split("=", 1)
+        ctx.set_tuning(key, float(val))
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
     def barrier():
@@ -708,6 +713,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c4", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--ffma", action="store_true", help="c5: the FFMA cross-term kernel (sk_set_tuning tc=0)")
+    ap.add_argument("--tune", action="append", default=[], metavar="KEY=VALUE",
+                    help="sk_set_tuning diagnostic knob (repeatable; recorded in config)")
     ap.add_argument("--force-sharded", action="store_true",
                     help="c4 at N=1 through the sharded entry with a 1-rank NCCL communicator (test of the N>1 path)")
     ap.add_argument("--init", default=None,
