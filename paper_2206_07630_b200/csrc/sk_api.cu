@@ -464,16 +464,17 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
     }
     const long long part_elems = std::max((long long)nsplit_col * m, (long long)split_row * n_max);
     ENSURE(part, float2, B_PART, part_elems);
-    // online passes: the column partials are pre-merged per fixed row block (K6a) into the
-    // exchange buffer [nblk_x][m] - the allgather payload (8 B per column per block) - and the
-    // blocks merged in block order: the same merge tree for every partition of the rows
+    // the column partials are pre-merged per fixed row block (K6a) into the exchange buffer
+    // [nblk_x][m] - the allgather payload (8 B per column per block) - and the blocks merged in
+    // block order: the same merge tree for every partition of the rows (and a 8-way merge instead
+    // of a nblk x split_q one: the stored path's 144-split merge took 31 us per sweep)
     const int nblk_x = sharded ? SK_SHARD_BLOCKS : nblk_glob;
     float2 *xchg = nullptr;
     int *xcnt = nullptr;   // K2: arrival counters of the fused premerge [8 blocks][P tiles]
-    if (!stored) {
+    {
         ENSURE(xc2, float2, B_XCHG, (long long)nblk_x * m);
         xchg = xc2;
-        if (!tc) {
+        if (!tc && !stored) {
             ENSURE(xc3, int, B_XCNT, (long long)SK_SHARD_BLOCKS * ptiles_col);
             xcnt = xc3;
             CU(cudaMemsetAsync(xcnt, 0, sizeof(int) * (size_t)SK_SHARD_BLOCKS * ptiles_col, st));
@@ -545,7 +546,7 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
 
     const long long slot = (long long)blk_per_rank * split_q * m;   // one rank's partial slots
     auto col_part = [&](int i) { return part + (sharded ? (long long)slices[i].rank * slot : 0); };
-    MergePass mcol{MERGE_COL, &Y, stored ? part : xchg, stored ? nsplit_col : nblk_x, P.eps, P.b, status, blke,
+    MergePass mcol{MERGE_COL, &Y, xchg, nblk_x, P.eps, P.b, status, blke,
                    blkb, nullptr, 0.f, sharded ? 1 : 0, 0};
     mcol.omega = P.omega;
     mcol.adapt = adapt;
@@ -589,7 +590,7 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
                 CU(launch_lse(colp, st));
             }
             if (t0 >= 0) tm.stop(t0, sweep, LaunchTimer::COL, ent, stored ? 4.0 * ent : 0.0);
-            if (tc) {   // (K2 merges its blocks itself)
+            if (tc || stored) {   // (K2 merges its blocks itself)
                 const long long xoff = sharded ? (long long)slices[i].rank * blk_per_rank * m : 0;
                 CU(launch_premerge(col_part(i), nb, split_q, m, xchg + xoff, &status->stop, only_if, st));
             }
@@ -606,13 +607,10 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
     const bool colredo = sharded;   // unsharded: the scaled merge recomputes a failing column itself
     if (!colredo && fused) { mcol_scaled.Cst = C[0]; mcol_scaled.xw = X[0].pack; mcol_scaled.n_rows = slices[0].n; }
     auto exchange_and_merge_col = [&](const MergePass &mp0) -> sk_status {
-        if (P.nccl && sharded) {
-            // stored: the split partials; online: this rank's pre-merged block partials
-            const size_t cnt = stored ? (size_t)slot * 2 : (size_t)blk_per_rank * m * 2;
-            const void *src = stored ? (const void *)col_part(0)
-                                     : (const void *)(xchg + (long long)slices[0].rank * blk_per_rank * m);
-            void *dst = stored ? (void *)part : (void *)xchg;
-            int r = g_nccl.allgather(src, dst, cnt, kNcclFloat32, ctx->comm, st);
+        if (P.nccl && sharded) {   // this rank's pre-merged block partials
+            const size_t cnt = (size_t)blk_per_rank * m * 2;
+            const void *src = (const void *)(xchg + (long long)slices[0].rank * blk_per_rank * m);
+            int r = g_nccl.allgather(src, (void *)xchg, cnt, kNcclFloat32, ctx->comm, st);
             if (r != 0) return fail(ctx, SK_ENCCL, "ncclAllGather failed: %s", g_nccl.errstr ? g_nccl.errstr(r) : "?");
         }
         MergePass mp = mp0;
@@ -642,14 +640,17 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
                     const int t0 = tm.start();
                     CU(launch_stored_fused(fl, st));   // also advances the sweep counter (row bookkeeping)
                     tm.stop(t0, sweep, LaunchTimer::FUSED, 2.0 * slices[i].n * m, 4.0 * slices[i].n * m);
-                    launched += 1;
+                    const long long xoff = sharded ? (long long)slices[i].rank * blk_per_rank * m : 0;
+                    CU(launch_premerge(col_part(i), sharded ? blk_per_rank : nblk_glob, split_q, m, xchg + xoff,
+                                       &status->stop, nullptr, st));
+                    launched += 2;
                 }
                 CK(exchange_and_merge_col(mcol_scaled));
                 launched += 1;
                 if (colredo) {
                     CK(col_stage(&status->colfail, false));   // no-ops unless colfail
                     CK(exchange_and_merge_col(mcol_redo));
-                    launched += 1 + ns;
+                    launched += 1 + 2 * ns;
                 }
                 ++sweep;
                 continue;
@@ -657,11 +658,11 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
             const bool cseed = col_seed && sweep >= 2;
             CK(col_stage(nullptr, cseed));
             CK(exchange_and_merge_col(cseed ? mcol_seeded : mcol));
-            launched += (tc ? 2 : 1) * ns + 1;   // (+ the premerge on the tensor-core path)
+            launched += (tc || stored ? 2 : 1) * ns + 1;   // (+ the premerge on the tensor-core / stored paths)
             if (cseed) {   // the exact redo when a seeded column sum left the safe range (no-ops otherwise)
                 CK(col_stage(&status->colfail, false));
                 CK(exchange_and_merge_col(mcol_redo));
-                launched += (tc ? 2 : 1) * ns + 1;
+                launched += (tc || stored ? 2 : 1) * ns + 1;
             }
             for (int i = 0; i < ns; ++i) {
                 const int t0 = tm.start();
