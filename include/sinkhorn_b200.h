@@ -163,7 +163,8 @@ sk_status sk_get_solver_options(const sk_ctx *ctx, float *omega, float *decay_in
  * selects a kernel variant or a balance of the exponential between MUFU and the FMA pipe:
  *   "tc" 0|1 (1): tcgen05 cross term (K3) for d in (16, 64]; 0 = FFMA kernel K2;
  *   "fused" 0|1 (1): stored mode's fused single-read sweep K5; 0 = separate row/column passes;
- *   "seeded" 0|1 (1): max-free (seeded) LSE passes from the third sweep;
+ *   "seeded" 0|1 (1): max-free (seeded) LSE passes from the second sweep on ("seed_from" >= 1 (1):
+ *       the first seeded sweep, 0-based);
  *   "tc_margin" [0, 1000] (4): K3 seeded shift above the previous LSE, log2 units;
  *   "lse_margin" [0, 1000] (4): K2 seeded shift above the previous LSE, log2 units (a margin
  *       beyond ~100 forces every seeded point through its exact fallback / the column redo);
@@ -371,7 +372,7 @@ sk_status sinkhorn_solve(sk_ctx *ctx, int64_t B, int64_t n, int64_t m, int32_t d
  * rows; y, b (nullable), g: replicated (m).  Every sweep: local row pass (f),
  * local column partials (max, sum-exp), merged per fixed row block on the rank (8 B per column
  * per block), ncclAllGather of the block partials (SK_SHARD_BLOCKS / world blocks per rank),
- * identical block-order merge on every rank (g, error, stop flag).  From the third sweep the
+ * identical block-order merge on every rank (g, error, stop flag).  From the second sweep the
  * column pass is seeded (max-free); if any column's seeded sum leaves [2^-100, 2^100] the
  * merge flags it and the column pass is redone exactly (one more allgather, enqueued every
  * sweep, a no-op otherwise).  The unsharded solver runs the same merge tree, so the results are

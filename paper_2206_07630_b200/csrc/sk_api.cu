@@ -82,7 +82,8 @@ struct sk_ctx {
     struct Tuning {
         int tc = 1;             // tensor-core cross term for d in (16, 64] (0: FFMA kernel K2)
         int fused = 1;          // stored mode: the fused single-read sweep K5
-        int seeded = 1;         // max-free (seeded) passes from the third sweep
+        int seeded = 1;         // max-free (seeded) passes (from sweep seed_from on)
+        int seed_from = 1;      // the first seeded sweep (0-based, >= 1: sweep 0 has no previous LSEs)
         float tc_margin = 4.f;  // K3 seeded shift above the previous LSE (log2 units)
         float lse_margin = 4.f; // K2 seeded shift above the previous LSE (log2 units)
         int lse_emu8 = 1;       // K2 seeded D <= 4: exponential pairs of 8 on the FMA pipe
@@ -411,7 +412,7 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
                     {xpot + 2 * off[i], xpot + 2 * off[i] + n}};
     }
     Side Y{(int)m, P.d, D, tq, ypack, yc, ynk, {ypot, ypot + m}};
-    // online FFMA path: per-point LSE seeds for the max-free (seeded) passes from sweep 3 on
+    // online paths: per-point LSE seeds for the max-free (seeded) passes from sweep seed_from on
     // stored mode with the fused sweep (one persistent CTA per SM): 8 blocks x split_q = one wave
     const bool fused = stored && T.fused != 0 && stored_fused_supported(m) && P.omega == 1.f && !amem && !adapt;
     const bool seedable = !stored;
@@ -427,13 +428,14 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
         for (int i = 0; i < ns; ++i) X[i].lse = xlse + off[i];
         Y.lse = ylse;
     }
-    // seeded passes from the third sweep.  Rows: a point whose seeded sum leaves the safe range is
+    // seeded passes from sweep seed_from (the second).  Rows: a point whose seeded sum leaves the safe range is
     // recomputed exactly in the merge (the reduced side, all columns, is on every rank).  Columns:
     // the exact fallback would need every rank's rows, so a failing column makes the merge set
     // st->colfail and the whole column pass is redone exactly (gated on the flag) - the same path
     // for every entry, so the unsharded, emulated and sharded solves are bit-identical.
     const bool col_seed = seedable && T.seeded;
     const bool row_seed = seedable && T.seeded;
+    const int seed_from = T.seed_from;   // the first seeded sweep (0-based; its seeds are the previous sweep's LSEs)
 
     // column-pass partition (a function of n_total, m, d only): SK_SHARD_BLOCKS fixed row
     // blocks, each cut into split_q sub-splits sized for the 8-rank launch; empty blocks
@@ -551,7 +553,7 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
     mcol.omega = P.omega;
     mcol.adapt = adapt;
     mcol.anderson = amem ? 1 : 0;
-    int sweep = 0;   // sweeps enqueued so far (seeded passes from the third on)
+    int sweep = 0;   // sweeps enqueued so far (seeded passes from seed_from on)
 
     // stored mode: one HBM read of C per sweep (fused row + column passes, H4s) when m fits
     bool first = true;
@@ -614,7 +616,7 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
             if (r != 0) return fail(ctx, SK_ENCCL, "ncclAllGather failed: %s", g_nccl.errstr ? g_nccl.errstr(r) : "?");
         }
         MergePass mp = mp0;
-        mp.tc_fold = tc && col_seed && sweep >= 1;   // the next column pass is seeded
+        mp.tc_fold = tc && col_seed && sweep + 1 >= seed_from;   // the next column pass is seeded
         mp.tc_margin = tc_margin;
         CU(launch_merge(mp, st));
         return SK_OK;
@@ -655,7 +657,7 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
                 ++sweep;
                 continue;
             }
-            const bool cseed = col_seed && sweep >= 2;
+            const bool cseed = col_seed && sweep >= seed_from;
             CK(col_stage(nullptr, cseed));
             CK(exchange_and_merge_col(cseed ? mcol_seeded : mcol));
             launched += (tc || stored ? 2 : 1) * ns + 1;   // (+ the premerge on the tensor-core / stored paths)
@@ -672,14 +674,14 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
                 } else if (tc) {
                     TcPass rowp{ximg + offi[i], yimg, (int)slices[i].n, m, ksteps, 1, 0, split_row, part,
                                 P.eps, &status->stop};
-                    rowp.seeded = row_seed && sweep >= 2;
+                    rowp.seeded = row_seed && sweep >= seed_from;
                     rowp.emu = T.tc_emu;
                     rowp.epi = T.tc_epi;
                     rowp.pipe = T.tc_pipe;
                     CU(launch_lse_tc(rowp, st));
                 } else {
                     LsePass rowp{&X[i], &Y, 1, 0, split_row, part, P.eps, &status->stop};
-                    rowp.seeded = row_seed && sweep >= 2;
+                    rowp.seeded = row_seed && sweep >= seed_from;
                     rowp.emu8 = T.lse_emu8;
                     rowp.margin = T.lse_margin;
                     rowp.R = r1 ? 1 : 0;
@@ -697,7 +699,7 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
                 mrow.accum = i > 0 ? 1 : 0;
                 mrow.wts = slices[i].a;   // (the relaxed row error term weighs rows by a)
                 mrow.n_uniform = n_glob;  //  uniform: 1 / n_total (a slice holds part of the rows)
-                mrow.tc_fold = tc && row_seed && sweep >= 1;   // the next row pass is seeded
+                mrow.tc_fold = tc && row_seed && sweep + 1 >= seed_from;   // the next row pass is seeded
                 mrow.tc_margin = tc_margin;
                 mrow.anderson = amem ? 1 : 0;
                 mrow.and_err = amem ? andvec + anderson_vec_doubles() * i + 8 : nullptr;
@@ -924,6 +926,7 @@ sk_status sk_set_tuning(sk_ctx *ctx, const char *key, double value) {
     if (k == "tc") { CK(need(iv == 0 || iv == 1)); T.tc = iv; }
     else if (k == "fused") { CK(need(iv == 0 || iv == 1)); T.fused = iv; }
     else if (k == "seeded") { CK(need(iv == 0 || iv == 1)); T.seeded = iv; }
+    else if (k == "seed_from") { CK(need(iv >= 1 && iv <= 1000)); T.seed_from = iv; }
     else if (k == "tc_margin") { CK(need(value >= 0.0 && value <= 1000.0)); T.tc_margin = (float)value; }
     else if (k == "lse_margin") { CK(need(value >= 0.0 && value <= 1000.0)); T.lse_margin = (float)value; }
     else if (k == "lse_emu8") { CK(need(iv >= 0 && iv <= 2)); T.lse_emu8 = iv; }
