@@ -63,3 +63,18 @@ def test_no_product_import_of_oracle():
                 txt = open(os.path.join(dp, fn), errors="ignore").read()
                 for bad in ("import oracle", "from oracle", "sk_oracle", "libsk_oracle"):
                     assert bad not in txt, (fn, bad)
+
+
+def test_reports_view_of_the_batched_host_reports():
+    """sinkhorn_solve's batched reports: the structured-array view (Reports) gives the same
+    per-problem dicts as the ctypes structs and whole columns as numpy arrays."""
+    from paper_2206_07630_b200 import Reports, SkReport
+    raw = (SkReport * 4)()
+    for k in range(4):
+        raw[k].iterations, raw[k].converged, raw[k].marginal_error = 10 + k, k % 2, 0.25 * k
+        raw[k].dual_objective, raw[k].solve_ms = -1.5 * k, 2.0
+    rep = Reports(raw)
+    assert len(rep) == 4 and [r["iterations"] for r in rep] == [10, 11, 12, 13]
+    assert rep[2] == raw[2].as_dict()
+    assert rep.column("converged").tolist() == [0, 1, 0, 1]
+    assert rep[1:3] == [raw[1].as_dict(), raw[2].as_dict()]
