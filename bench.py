@@ -465,7 +465,7 @@ def make_workload(args, sk, ctx, dev, rank, world):
     return C2(sk, ctx, dev, rank, world, args) if args.workload == "c2" else Single(sk, ctx, dev, rank, world, args)
 
 
-def roofline(w, cnt, steps, pk, src, step_ms):
+def roofline(w, cnt, steps, pk, src, step_ms, clocks=None):
     """Roofline of the dominant kernel: ALGORITHMIC units per launch / its average launch
     duration, both from the library's per-launch CUDA events on the launching stream
     (sk_counters.dom_*: launches that returned at entry after the stop flag are excluded)."""
@@ -499,9 +499,10 @@ def roofline(w, cnt, steps, pk, src, step_ms):
                 "algorithmic": "3 x 2 x 64 fp16 tensor flops per cost entry per pass (3-product hi/lo split)",
                 "flops_per_launch": flops / nl,
                 "mufu_frac": ent_s / ex2_peak,
-                "tmem_read_frac": ent_s * 4 / (N_SM * 64 * sm_max * 1e6),
-                "tmem_note": "every fp32 accumulator is read back once: 4 B per entry against 64 B/clk/SM of "
-                             "tcgen05.ld bandwidth (the same 16 entries/clk/SM as MUFU.EX2) - the epilogue's floor",
+                # under the 1000 W cap the SM clock drops: the fraction of the burst rate at the
+                # clock the run actually had (the tensor pipe's own utilisation, ncu's view)
+                "frac_of_burst_at_observed_clock": (achieved / float(pk["bf16_tflops"])) * sm_max /
+                                                   float((clocks or {}).get("sm_mhz") or sm_max),
                 **common}
     if w.roof == "fp32":
         flops = cnt["dom_entries"] * 2 * w.d            # d FMAs per entry for the cross term
@@ -681,7 +682,7 @@ def run_ours(args):
             "config": w.config(),
             "time_to_tol_ms": {"init": ms / args.steps, "zero_init": zero["time_to_tol_ms"]},
             "solve": extra, "zero_init": zero,
-            "roofline": roofline(w, cnt, args.steps, pk, src, ms_all / args.steps),
+            "roofline": roofline(w, cnt, args.steps, pk, src, ms_all / args.steps, clk.summary()),
             "gpu_launches": int(cnt["kernel_launches"]),
             "clocks": clk.summary(),
             "k14_measured_peaks": k14,
