@@ -229,9 +229,13 @@ def single_spec(args):
         sp.update(p=gen.c3(eps_factor=args.eps_factor or 0.01), init=args.init or "gmm", mode="stored", roof="hbm",
                   kernel="k_stored_fused (single-read fused stored sweep, K5)")
     elif name == "c4":
+        ffma = any(t.replace(" ", "") in ("tc=0", "tc_small_d=0") for t in args.tune)
         sp.update(p=gen.c4(), init=args.init or "subsample", mode="online", roof="mufu", scaling="strong",
-                  fma_exp_share=0.125,   # K2 seeded passes: 1 of 8 exponential pairs on the FMA pipe
-                  kernel="k_lse<3,4> (online LSE pass, K2)")
+                  # K3 passes: 2 of 8 exponential pairs on the FMA pipe (K2: 1 of 8)
+                  fma_exp_share=0.125 if ffma else 0.25,
+                  kernel="k_lse<3,4> (online LSE pass, FFMA cross term, K2)" if ffma else
+                         "k_lse_tc2 (online LSE pass, tcgen05 cross term (d = 3 in one K = 16 step, 3-product "
+                         "fp16 split) with w and the row shift folded into the MMA, K3)")
     else:
         sp.update(p=gen.c5(eps_factor=args.eps_factor or 1e-2), init=args.init or "gaussian", mode="online",
                   roof="tensor", scaling="strong", kernel="k_lse_tc2 (online LSE pass, CTA-pair tcgen05 kind::f16 3-product hi/lo "

@@ -161,7 +161,9 @@ sk_status sk_get_solver_options(const sk_ctx *ctx, float *omega, float *decay_in
 /* Diagnostics / tuning of kernel variants (DESIGN.md section 6 measures each): key = value for the
  * following calls on this context.  None changes what is computed beyond fp32 rounding; each
  * selects a kernel variant or a balance of the exponential between MUFU and the FMA pipe:
- *   "tc" 0|1 (1): tcgen05 cross term (K3) for d in (16, 64]; 0 = FFMA kernel K2;
+ *   "tc" 0|1 (1): tcgen05 cross term (K3) for d in [tc_min_d, 64], and for every d <= 64 on large
+ *       problems (max(n, m) > 16384) while "tc_small_d" is 1; 0 = FFMA kernel K2 everywhere;
+ *   "tc_min_d" 1..65 (17), "tc_small_d" 0|1 (1): see "tc";
  *   "fused" 0|1 (1): stored mode's fused single-read sweep K5; 0 = separate row/column passes;
  *   "seeded" 0|1 (1): max-free (seeded) LSE passes from the second sweep on ("seed_from" >= 1 (1):
  *       the first seeded sweep, 0-based);
@@ -354,8 +356,9 @@ sk_status sinkhorn_init_subsample(sk_ctx *ctx, int64_t n, int64_t m, int32_t d, 
  * Kernels: problems with d <= 4 that fit one CTA's shared memory (n, m up to ~4096) run the
  * on-chip solver K13 (one CTA or CTA pair per problem, the whole iteration loop on chip,
  * per-problem convergence); larger problems run the multi-kernel path: online LSE passes with
- * the cost recomputed per pass (FFMA cross term K2 for d <= 16; the tcgen05 cross term K3 for
- * d in (16, 64], K2 when the scaled coordinates leave the fp16 range) or, with SK_COST_STORED
+ * the cost recomputed per pass (the tcgen05 cross term K3 for d in (16, 64] and, on problems
+ * with max(n, m) > 16384, for every d; the FFMA cross term K2 otherwise and when the scaled
+ * coordinates leave the fp16 range) or, with SK_COST_STORED
  * (or AUTO for 8 <= d < 32 when 4nm bytes fit), the stored-cost sweep (K4 build, K5 fused
  * single-read sweep).  Blocks until the reports are filled.
  * SK_EINVAL for d < 1 or d > 256 (and the conventions above); SK_EUNSUPPORTED for d in

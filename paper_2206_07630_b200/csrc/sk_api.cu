@@ -80,7 +80,9 @@ struct sk_ctx {
     int force_nccl = 0;             // sk_set_force_nccl: a 1-rank communicator takes the NCCL path
     // diagnostics / tuning (sk_set_tuning): kernel variants and balances measured in DESIGN.md
     struct Tuning {
-        int tc = 1;             // tensor-core cross term for d in (16, 64] (0: FFMA kernel K2)
+        int tc = 1;             // tensor-core cross term for d in [tc_min_d, 64] (0: FFMA kernel K2)
+        int tc_min_d = 17;      // the smallest d on the tensor-core kernel K3 (BJ.ns: FFMA below) ...
+        int tc_small_d = 1;     // ... except for large problems (max(n, m) > 16384): K3 at every d
         int fused = 1;          // stored mode: the fused single-read sweep K5
         int seeded = 1;         // max-free (seeded) passes (from sweep seed_from on)
         int seed_from = 1;      // the first seeded sweep (0-based, >= 1: sweep 0 has no previous LSEs)
@@ -347,7 +349,11 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
     if (stored && !stored_ok) return fail(ctx, SK_EUNSUPPORTED, "stored-cost mode needs m %% 4 == 0");
     // tensor-core cross term for d in (16, 64] (BJ.ns "only when d >= 32"; d in (16, 32] pads to
     // K = 32); sk_set_tuning("tc", 0) forces the FFMA kernel (comparison knob)
-    bool tc = !stored && P.d > 16 && P.d <= 64 && T.tc != 0;
+    // large problems run the tensor-core cross term at every d (T.tc_small_d): at small d it is not
+    // the cross term's flops that matter but the FMA pipe it occupies next to the FMA-pipe
+    // exponentials (C4, d = 3: 1162 -> 1104 ms); small problems keep K2 below tc_min_d
+    const bool large_p = std::max(n_glob, m) > 16384;
+    bool tc = !stored && P.d <= 64 && T.tc != 0 && (P.d >= T.tc_min_d || (large_p && T.tc_small_d));
     unsigned *amax = nullptr;
     if (tc) {
         // per-side max |coordinate| (global over the ranks) -> the fold scales; a problem whose
@@ -924,6 +930,8 @@ sk_status sk_set_tuning(sk_ctx *ctx, const char *key, double value) {
         return ok ? SK_OK : fail(ctx, SK_EINVAL, "sk_set_tuning(%s, %g): value out of range", key, value);
     };
     if (k == "tc") { CK(need(iv == 0 || iv == 1)); T.tc = iv; }
+    else if (k == "tc_min_d") { CK(need(iv >= 1 && iv <= 65)); T.tc_min_d = iv; }
+    else if (k == "tc_small_d") { CK(need(iv == 0 || iv == 1)); T.tc_small_d = iv; }
     else if (k == "fused") { CK(need(iv == 0 || iv == 1)); T.fused = iv; }
     else if (k == "seeded") { CK(need(iv == 0 || iv == 1)); T.seeded = iv; }
     else if (k == "seed_from") { CK(need(iv >= 1 && iv <= 1000)); T.seed_from = iv; }
