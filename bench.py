@@ -236,6 +236,11 @@ def single_spec(args):
                   kernel="k_lse<3,4> (online LSE pass, FFMA cross term, K2)" if ffma else
                          "k_lse_tc2 (online LSE pass, tcgen05 cross term (d = 3 in one K = 16 step, 3-product "
                          "fp16 split) with w and the row shift folded into the MMA, K3)")
+        if not ffma:
+            sp["traffic_note"] = ("DRAM bytes of one seeded K3 column pass (ncu): mostly re-reads of the reduced side's "
+                                  "operand images (K padded to 64 halves: 320 B per point, 84 MB per side, larger than "
+                                  "what stays in L2 next to the other side's); the kernel is MUFU/FMA-bound at 0.5 % of "
+                                  "HBM bandwidth")
     else:
         sp.update(p=gen.c5(eps_factor=args.eps_factor or 1e-2), init=args.init or "gaussian", mode="online",
                   roof="tensor", scaling="strong", kernel="k_lse_tc2 (online LSE pass, CTA-pair tcgen05 kind::f16 3-product hi/lo "
@@ -278,6 +283,7 @@ class Single(Workload):
         self.spec = sp = single_spec(args)
         self.name, self.p, self.init, self.mode, self.roof = sp["name"], sp["p"], sp["init"], sp["mode"], sp["roof"]
         self.kernel, self.scaling, self.fma_exp_share = sp["kernel"], sp["scaling"], sp["fma_exp_share"]
+        self.traffic_note = sp.get("traffic_note")
         if self.name == "c5" and args.ffma:
             ctx.set_tuning("tc", 0)
         p = self.p
@@ -480,6 +486,8 @@ def roofline(w, cnt, steps, pk, src, step_ms, clocks=None):
               "avg_launch_ms": cnt["dom_ms"] / nl,
               "share_of_step": (cnt["dom_ms"] / max(steps, 1)) / step_ms if step_ms > 0 else None,
               "traffic": traffic_from_profile(w)}
+    if getattr(w, "traffic_note", None):
+        common["traffic_note"] = w.traffic_note
     if w.roof == "hbm":
         achieved = cnt["dom_bytes"] / dom_s / 1e9 if dom_s > 0 else 0.0
         peak = float(pk["hbm_gbs"])
