@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(kAT) k_and_mix(Side X, const DevStatus *st, co
         const float wn = fmaf(h, kap, -X.nk[i]);
         const long long t = i / X.tq, o = i % X.tq;
         X.pack[t * (long long)(X.D + 1) * X.tq + (long long)X.D * X.tq + o] = wn;
-        if (X.tcimg) tc_put_w(X.tcimg, X.P, i, wn, X.tc_c);
+        if (X.tcimg) tc_put_w(X.tcimg, X.P, i, wn, X.tc_c, X.tc_rb);
     }
 }
 

@@ -401,14 +401,17 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
     ENSURE(status, DevStatus, B_STATUS, 1);
     char *ximg = nullptr, *yimg = nullptr;
     std::vector<long long> offi(ns + 1, 0);
+    // d <= 16 (one K = 16 step): compact SW32 operand images, a quarter of the K = 64 bytes
+    const int tc_rb = (P.d + 15) / 16 == 1 ? 32 : 128;
     if (tc) {
-        for (int i = 0; i < ns; ++i) offi[i + 1] = offi[i] + (long long)tc_image_bytes(slices[i].n);
+        for (int i = 0; i < ns; ++i) offi[i + 1] = offi[i] + (long long)tc_image_bytes(slices[i].n, tc_rb);
         cudaError_t e1, e2;
         ximg = (char *)ensure(ctx, B_XIMG, (size_t)offi[ns], &e1);
-        yimg = (char *)ensure(ctx, B_YIMG, tc_image_bytes(m), &e2);
+        yimg = (char *)ensure(ctx, B_YIMG, tc_image_bytes(m, tc_rb), &e2);
         if (!ximg || !yimg) return fail(ctx, SK_ENOMEM, "tensor-core operand images");
-        for (int i = 0; i < ns; ++i) CU(launch_pack_tc(slices[i].x, slices[i].n, P.d, amax, 0, P.eps, ximg + offi[i], st));
-        CU(launch_pack_tc(P.y, m, P.d, amax, 1, P.eps, yimg, st));
+        for (int i = 0; i < ns; ++i)
+            CU(launch_pack_tc(slices[i].x, slices[i].n, P.d, amax, 0, P.eps, ximg + offi[i], st, tc_rb));
+        CU(launch_pack_tc(P.y, m, P.d, amax, 1, P.eps, yimg, st, tc_rb));
         ctx->cnt.kernel_launches += ns + 1;
     }
     std::vector<Side> X(ns);
@@ -423,7 +426,10 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
     const bool fused = stored && T.fused != 0 && stored_fused_supported(m) && P.omega == 1.f && !amem && !adapt;
     const bool seedable = !stored;
     if (tc) {   // the seeded passes' exact fallback reads the caller's coordinates
-        for (int i = 0; i < ns; ++i) { X[i].raw = slices[i].x; X[i].tcimg = (unsigned char *)ximg + offi[i]; X[i].tc_c = tc_fold_c(); }
+        for (int i = 0; i < ns; ++i) {
+            X[i].raw = slices[i].x; X[i].tcimg = (unsigned char *)ximg + offi[i]; X[i].tc_c = tc_fold_c(); X[i].tc_rb = tc_rb;
+        }
+        Y.tc_rb = tc_rb;
         Y.raw = P.y;
         Y.tcimg = (unsigned char *)yimg;
         Y.tc_c = tc_fold_c();
@@ -508,8 +514,8 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
         CU(pack_side(X[i], slices[i].x, slices[i].a, loga_u, slices[i].f_init, P.eps, st, pmode));
     CU(pack_side(Y, P.y, P.b, logb_u, nullptr, P.eps, st, pmode));
     if (tc) {   // extra columns: w from the packed sides, zero shifts
-        for (int i = 0; i < ns; ++i) CU(launch_pack_tc_ext(slices[i].n, X[i].pack, X[i].tcimg, st));
-        CU(launch_pack_tc_ext(m, Y.pack, Y.tcimg, st));
+        for (int i = 0; i < ns; ++i) CU(launch_pack_tc_ext(slices[i].n, X[i].pack, X[i].tcimg, st, tc_rb));
+        CU(launch_pack_tc_ext(m, Y.pack, Y.tcimg, st, tc_rb));
         ctx->cnt.kernel_launches += ns + 1;
     }
     const float tc_margin = T.tc_margin;
@@ -583,6 +589,7 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
                 colp.emu = T.tc_emu;
                 colp.epi = T.tc_epi;
                 colp.pipe = T.tc_pipe;
+                colp.rb = tc_rb;
                 CU(launch_lse_tc(colp, st));
             } else {
                 LsePass colp{&Y, &X[i], nb, (int)(bs_rows / tq), split_q, col_part(i), P.eps, &status->stop};
@@ -684,6 +691,7 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
                     rowp.emu = T.tc_emu;
                     rowp.epi = T.tc_epi;
                     rowp.pipe = T.tc_pipe;
+                    rowp.rb = tc_rb;
                     CU(launch_lse_tc(rowp, st));
                 } else {
                     LsePass rowp{&X[i], &Y, 1, 0, split_row, part, P.eps, &status->stop};
@@ -1665,8 +1673,9 @@ sk_status sk_selftest_tc_dot(sk_ctx *ctx, int32_t d, const float *x, const float
     CK(sg.in_t(x, (size_t)128 * d, &dx));
     CK(sg.in_t(y, (size_t)128 * d, &dy));
     CK(sg.out_t(out, (size_t)128 * 128, &dout));
-    ENSURE(ximg, char, B_XIMG, tc_image_bytes(128));
-    ENSURE(yimg, char, B_YIMG, tc_image_bytes(128));
+    const int rb = ksteps == 1 ? 32 : 128;   // (the solver's layout for this d)
+    ENSURE(ximg, char, B_XIMG, tc_image_bytes(128, rb));
+    ENSURE(yimg, char, B_YIMG, tc_image_bytes(128, rb));
     ENSURE(amax, unsigned, B_TCMAX, 2);
     ENSURE(part, float2, B_PART, 128);
     CU(cudaMemsetAsync(amax, 0, 2 * sizeof(unsigned), ctx->stream));
@@ -1680,11 +1689,12 @@ sk_status sk_selftest_tc_dot(sk_ctx *ctx, int32_t d, const float *x, const float
     memcpy(&hy, &h[1], 4);
     if (!tc_fold_ok(hx, hy, 1.f)) return fail(ctx, SK_EUNSUPPORTED, "scaled coordinates outside the fp16 range");
     // eps = 1: the accumulator is 2 log2(e) <x, y> (+ w - sh = 0); the kernel unscales it
-    CU(launch_pack_tc(dx, 128, d, amax, 0, 1.f, ximg, ctx->stream));
-    CU(launch_pack_tc(dy, 128, d, amax, 1, 1.f, yimg, ctx->stream));
-    CU(launch_pack_tc_ext(128, nullptr, ximg, ctx->stream));
-    CU(launch_pack_tc_ext(128, nullptr, yimg, ctx->stream));
+    CU(launch_pack_tc(dx, 128, d, amax, 0, 1.f, ximg, ctx->stream, rb));
+    CU(launch_pack_tc(dy, 128, d, amax, 1, 1.f, yimg, ctx->stream, rb));
+    CU(launch_pack_tc_ext(128, nullptr, ximg, ctx->stream, rb));
+    CU(launch_pack_tc_ext(128, nullptr, yimg, ctx->stream, rb));
     TcPass tp{ximg, yimg, 128, 128, ksteps, 1, 0, 1, part, 1.f, nullptr};
+    tp.rb = rb;
     tp.debug_acc = dout;
     CU(launch_lse_tc(tp, ctx->stream));
     ctx->cnt.kernel_launches += 7;

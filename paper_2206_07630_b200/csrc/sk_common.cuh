@@ -148,8 +148,9 @@ __device__ __forceinline__ int block_or(int v, int *scratch /* NT/32 */) {
 // ------------------------------------------- K3 tensor-core image layout (shared with K6)
 // One side of P points as images for tcgen05.mma (tiles of 128 points, padded to a multiple of
 // 256 = one CTA-pair tile), in one allocation:
-//   [T x (hi | lo)]   T = tc_tiles(P) tiles of 2 x 16 KB: fp16 hi/lo split of alpha x, K-major
-//                     SWIZZLE_128B (row r of a tile: 128 bytes = 64 halves)
+//   [T x (hi | lo)]   T = tc_tiles(P) tiles of 2 x 128 rb bytes: fp16 hi/lo split of alpha x,
+//                     K-major; rb = 128: SWIZZLE_128B (row r of a tile: 64 halves, d <= 64);
+//                     rb = 32: SWIZZLE_32B (16 halves, d <= 16 - a quarter of the bytes)
 //   [T x EA]          4 KB per tile, K-major SWIZZLE_32B (16 halves per row): the "A role" extra
 //                     columns [-sh/c, 0, 0, c, c, c, 0 ..]    (sh: the point's folded shift)
 //   [T x EB]          4 KB per tile: the "B role" extra columns [c, 0, 0, w1, w2, w3, 0 ..]
@@ -160,10 +161,10 @@ namespace sk {
 constexpr int kTcImgBytes = 128 * 128;   // one SW128 image tile (128 rows x 128 bytes)
 constexpr int kTcExtBytes = 128 * 32;    // one SW32 extra tile (128 rows x 32 bytes)
 __host__ __device__ inline long long tc_tiles(long long P) { return (P + 255) / 256 * 2; }
-__host__ __device__ inline long long tc_ea_off(long long P) { return tc_tiles(P) * 2 * kTcImgBytes; }
-__host__ __device__ inline long long tc_eb_off(long long P) { return tc_ea_off(P) + tc_tiles(P) * kTcExtBytes; }
-__host__ __device__ inline long long tc_sh_off(long long P) { return tc_eb_off(P) + tc_tiles(P) * kTcExtBytes; }
-__host__ __device__ inline long long tc_side_bytes(long long P) { return tc_sh_off(P) + tc_tiles(P) * 128 * 4; }
+__host__ __device__ inline long long tc_ea_off(long long P, int rb = 128) { return tc_tiles(P) * 2 * 128LL * rb; }
+__host__ __device__ inline long long tc_eb_off(long long P, int rb = 128) { return tc_ea_off(P, rb) + tc_tiles(P) * kTcExtBytes; }
+__host__ __device__ inline long long tc_sh_off(long long P, int rb = 128) { return tc_eb_off(P, rb) + tc_tiles(P) * kTcExtBytes; }
+__host__ __device__ inline long long tc_side_bytes(long long P, int rb = 128) { return tc_sh_off(P, rb) + tc_tiles(P) * 128 * 4; }
 // byte offset of half `slot` (0..15) of point p inside an extra image (SW32: the 16-byte chunk
 // index is XORed with bit 2 of the row)
 __device__ __forceinline__ long long tc_ext_at(long long p, int slot) {
@@ -172,8 +173,9 @@ __device__ __forceinline__ long long tc_ext_at(long long p, int slot) {
     return t * kTcExtBytes + (r >> 3) * 256 + (r & 7) * 32 + ((ch ^ ((r >> 2) & 1)) << 4) + (slot & 7) * 2;
 }
 // EB slots 3..5 of point p: w / c as three fp16 pieces (w = -inf: [-inf, 0, 0])
-__device__ __forceinline__ void tc_put_w(unsigned char *img, long long P, long long p, float w, float c) {
-    unsigned char *eb = img + tc_eb_off(P);
+__device__ __forceinline__ void tc_put_w(unsigned char *img, long long P, long long p, float w, float c,
+                                         int rb = 128) {
+    unsigned char *eb = img + tc_eb_off(P, rb);
     __half h1, h2 = __float2half_rn(0.f), h3 = h2;
     if (w == -INFINITY) {
         h1 = __float2half_rn(-INFINITY);
@@ -189,11 +191,12 @@ __device__ __forceinline__ void tc_put_w(unsigned char *img, long long P, long l
     *reinterpret_cast<__half *>(eb + tc_ext_at(p, 5)) = h3;
 }
 // EA slot 0 of point p: the shift rounded to c * fp16; returns the exact shift stored in sh[p]
-__device__ __forceinline__ float tc_put_shift(unsigned char *img, long long P, long long p, float sh, float c) {
+__device__ __forceinline__ float tc_put_shift(unsigned char *img, long long P, long long p, float sh, float c,
+                                             int rb = 128) {
     const __half h = __float2half_rn(isfinite(sh) ? sh / c : 0.f);
     const float exact = __half2float(h) * c;
-    *reinterpret_cast<__half *>(img + tc_ea_off(P) + tc_ext_at(p, 0)) = __hneg(h);
-    reinterpret_cast<float *>(img + tc_sh_off(P))[p] = exact;
+    *reinterpret_cast<__half *>(img + tc_ea_off(P, rb) + tc_ext_at(p, 0)) = __hneg(h);
+    reinterpret_cast<float *>(img + tc_sh_off(P, rb))[p] = exact;
     return exact;
 }
 

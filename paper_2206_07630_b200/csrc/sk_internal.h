@@ -116,6 +116,7 @@ struct Side {
     const float *raw = nullptr;  // PACK_TC: the caller's P x d fp32 coordinates (exact fallback of a seeded pass)
     unsigned char *tcimg = nullptr;  // PACK_TC: the side's K3 images (K6 rewrites w and the shift)
     float tc_c = 16.f;               //          c of the extra columns
+    int tc_rb = 128;                 //          image row bytes (32: the compact d <= 16 layout)
 };
 
 // Pack points (P x d, fp32 row-major), optional weights and initial potential.
@@ -148,12 +149,14 @@ struct TcPass {
     int emu = 2;                // exponential pairs (of every 8) on the FMA pipe (sk_set_tuning "tc_emu")
     int epi = 16;               // epilogue organisation (sk_set_tuning "tc_epi": 16 or 162)
     int pipe = 0;               // seeded epilogue with software-pipelined TMEM loads (sk_set_tuning "tc_pipe")
+    int rb = 128;               // image row bytes of both sides (32: compact K = 16 images, ksteps == 1)
 };
-size_t tc_image_bytes(long long P);
+size_t tc_image_bytes(long long P, int rb = 128);
 cudaError_t launch_absmax(const float *pts, long long cnt, unsigned *out, cudaStream_t st);  // out zeroed first
 cudaError_t launch_pack_tc(const float *pts, long long P, int d, const unsigned *amax2, int role, float eps,
-                           void *img, cudaStream_t st);   // role 0: x side, 1: y side
-cudaError_t launch_pack_tc_ext(long long P, const float *w, void *img, cudaStream_t st);  // w: plain [P] (nullable = 0)
+                           void *img, cudaStream_t st, int rb = 128);   // role 0: x side, 1: y side
+cudaError_t launch_pack_tc_ext(long long P, const float *w, void *img, cudaStream_t st,
+                               int rb = 128);  // w: plain [P] (nullable = 0)
 bool tc_fold_ok(float amax_x, float amax_y, float eps);   // both scaled sides within fp16 range
 float tc_fold_c();                                         // c of the extra columns
 cudaError_t launch_lse_tc(const TcPass &L, cudaStream_t st);

@@ -422,8 +422,8 @@ __device__ __forceinline__ void merge_point(const MergePass &Mp, const Side &S, 
     const float wn = fmaf(hn, kap, -S.nk[p]);
     S.pack[t * (long long)(S.D + 1) * S.tq + (long long)S.D * S.tq + o] = wn;
     if (S.tcimg) {   // K3 side: w into the B-role extra columns, the next row shift into the A role
-        tc_put_w(S.tcimg, S.P, p, wn, S.tc_c);
-        if (Mp.tc_fold) tc_put_shift(S.tcimg, S.P, p, lse2 + Mp.tc_margin, S.tc_c);
+        tc_put_w(S.tcimg, S.P, p, wn, S.tc_c, S.tc_rb);
+        if (Mp.tc_fold) tc_put_shift(S.tcimg, S.P, p, lse2 + Mp.tc_margin, S.tc_c, S.tc_rb);
     }
     bad |= !isfinite(hn);
     if (Mp.anderson && Mp.mode == MERGE_ROW) {   // row term of err_l for (f^l, g~): columns are exact

@@ -63,14 +63,17 @@ __host__ __device__ inline int tc_fold_s(float ax, float ay, float tk) {
 // (halves 8c .. 8c+7) of row r stored at chunk c ^ (r % 8).  One thread per (point, chunk).
 // role 0 (x side): alpha = 2^s; role 1 (y side): alpha = tk 2^-s.
 __global__ void k_pack_tc(const float *__restrict__ pts, long long P, long long P2, int d, const unsigned *amax2,
-                          int role, float tk, unsigned char *img) {
-    const long long total = P2 * 8;
+                          int role, float tk, unsigned char *img, int rb) {
+    // rb = 128: SW128 (8 chunks of 8 halves per row); rb = 32: SW32 (2 chunks, d <= 16), the
+    // 16-byte chunk index XORed with bit 2 of the row, 8-row groups of 256 bytes
+    const int cpr = rb / 16;
+    const long long total = P2 * cpr;
     const int s = tc_fold_s(__uint_as_float(amax2[0]), __uint_as_float(amax2[1]), tk);
     const float alpha = role == 0 ? ldexpf(1.f, s) : ldexpf(tk, -s);
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
          e += (long long)gridDim.x * blockDim.x) {
-        const long long p = e >> 3;
-        const int c = (int)(e & 7);
+        const long long p = e / cpr;
+        const int c = (int)(e % cpr);
         const long long t = p / kTcM;
         const int r = (int)(p % kTcM);
         __align__(16) __half hi[8], lo[8];
@@ -81,26 +84,29 @@ __global__ void k_pack_tc(const float *__restrict__ pts, long long P, long long 
             hi[j] = __float2half_rn(x);
             lo[j] = __float2half_rn(x - __half2float(hi[j]));
         }
-        const long long off = (long long)(r >> 3) * 1024 + (r & 7) * 128 + ((c ^ (r & 7)) << 4);
-        unsigned char *base = img + t * 2LL * kTcImg;
+        const long long off = rb == 128 ? (long long)(r >> 3) * 1024 + (r & 7) * 128 + ((c ^ (r & 7)) << 4)
+                                        : (long long)(r >> 3) * 256 + (r & 7) * 32 + ((c ^ ((r >> 2) & 1)) << 4);
+        const long long ib = 128LL * rb;   // bytes of one image tile
+        unsigned char *base = img + t * 2LL * ib;
         *reinterpret_cast<uint4 *>(base + off) = *reinterpret_cast<const uint4 *>(hi);
-        *reinterpret_cast<uint4 *>(base + kTcImg + off) = *reinterpret_cast<const uint4 *>(lo);
+        *reinterpret_cast<uint4 *>(base + ib + off) = *reinterpret_cast<const uint4 *>(lo);
     }
 }
 
 // K3b: the extra columns of every point: EA = [0, 0, 0, c, c, c, 0 ..] (shift 0), EB = [c, 0, 0,
 // w pieces, 0 ..] from the plain w array (w == nullptr: 0; padding points: w = -inf), sh = 0.
-__global__ void k_pack_tc_ext(long long P, long long P2, const float *__restrict__ w, float c, unsigned char *img) {
+__global__ void k_pack_tc_ext(long long P, long long P2, const float *__restrict__ w, float c, unsigned char *img,
+                              int rb) {
     for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < P2; p += (long long)gridDim.x * blockDim.x) {
-        unsigned char *ea = img + tc_ea_off(P), *eb = img + tc_eb_off(P);
+        unsigned char *ea = img + tc_ea_off(P, rb), *eb = img + tc_eb_off(P, rb);
         const __half z = __float2half_rn(0.f), ch = __float2half_rn(c);
 #pragma unroll
         for (int k = 0; k < 16; ++k) {
             *reinterpret_cast<__half *>(ea + tc_ext_at(p, k)) = (k >= 3 && k <= 5) ? ch : z;
             *reinterpret_cast<__half *>(eb + tc_ext_at(p, k)) = (k == 0) ? ch : z;
         }
-        reinterpret_cast<float *>(img + tc_sh_off(P))[p] = 0.f;
-        tc_put_w(img, P, p, p < P ? (w ? w[p] : 0.f) : -INFINITY, c);
+        reinterpret_cast<float *>(img + tc_sh_off(P, rb))[p] = 0.f;
+        tc_put_w(img, P, p, p < P ? (w ? w[p] : 0.f) : -INFINITY, c, rb);
     }
 }
 
@@ -269,7 +275,7 @@ __device__ __forceinline__ void umma2_commit_mc(uint64_t *bar) {
 }
 
 
-template <int EMU, int NE, bool SEEDED, int G, int PL = 0, bool DBG = false>
+template <int EMU, int NE, bool SEEDED, int G, int PL = 0, bool DBG = false, int RB = 128>
 __global__ void __launch_bounds__(64 + 32 * NE, 1) k_lse_tc2(TcArgs A) {
     constexpr int NQ = NE / 4;                       // epilogue warps per TMEM lane quadrant
     // G tile groups: group k's warps take the tiles g with g % G == k (accumulator buffer k when
@@ -277,7 +283,9 @@ __global__ void __launch_bounds__(64 + 32 * NE, 1) k_lse_tc2(TcArgs A) {
     constexpr int NQG = NQ / G;                      // warps per lane quadrant and group
     constexpr int CW = kT2N / NQG;                   // accumulator columns per epilogue warp
     constexpr int ABUF = 2;
-    constexpr int STAGE = 2 * kTcImg + kTcExtBytes;  // [hi | lo | extra] of 128 points: 36 KB
+    // [hi | lo | extra] of 128 points: 36 KB (RB = 128), 12 KB (RB = 32: the compact d <= 16 images)
+    constexpr int IMG = 128 * RB;
+    constexpr int STAGE = 2 * IMG + kTcExtBytes;
     extern __shared__ __align__(1024) unsigned char smraw[];
     unsigned char *sm = smraw + ((1024 - (smem_u32(smraw) & 1023)) & 1023);
     unsigned char *sA = sm;                           // ABUF x STAGE: this CTA's 128 A rows
@@ -325,7 +333,7 @@ __global__ void __launch_bounds__(64 + 32 * NE, 1) k_lse_tc2(TcArgs A) {
 
     if (warp == 0) {
         if (lane == 0) {
-            const unsigned char *aext = A.Aimg + tc_ea_off(A.P), *bext = A.Bimg + tc_eb_off(A.Q);
+            const unsigned char *aext = A.Aimg + tc_ea_off(A.P, RB), *bext = A.Bimg + tc_eb_off(A.Q, RB);
             int g = 0, c = 0;
             for (int it = cid; it < items; it += ncl, ++c) {
                 const int s = it / A.ptiles, pt = it % A.ptiles;
@@ -335,8 +343,8 @@ __global__ void __launch_bounds__(64 + 32 * NE, 1) k_lse_tc2(TcArgs A) {
                 const long long at = 2LL * pt + rank;   // this CTA's 128-point A tile
                 if (c >= ABUF) mbar_wait_sleep(&aempty[ab], ((c / ABUF) - 1) & 1);
                 mbar_expect_tx(&afull[ab], STAGE);
-                bulk_g2s(sA + ab * STAGE, A.Aimg + at * 2 * kTcImg, 2 * kTcImg, &afull[ab]);
-                bulk_g2s(sA + ab * STAGE + 2 * kTcImg, aext + at * kTcExtBytes, kTcExtBytes, &afull[ab]);
+                bulk_g2s(sA + ab * STAGE, A.Aimg + at * 2 * IMG, 2 * IMG, &afull[ab]);
+                bulk_g2s(sA + ab * STAGE + 2 * IMG, aext + at * kTcExtBytes, kTcExtBytes, &afull[ab]);
                 for (int i = 0; i < nt; ++i, ++g) {
                     const int st = g % kT2Stages;
                     const long long bt = 2LL * (t0 + i) + rank;
@@ -346,8 +354,8 @@ __global__ void __launch_bounds__(64 + 32 * NE, 1) k_lse_tc2(TcArgs A) {
                         continue;
                     }
                     mbar_expect_tx(&full[st], STAGE);
-                    bulk_g2s(sB + st * STAGE, A.Bimg + bt * 2 * kTcImg, 2 * kTcImg, &full[st]);
-                    bulk_g2s(sB + st * STAGE + 2 * kTcImg, bext + bt * kTcExtBytes, kTcExtBytes, &full[st]);
+                    bulk_g2s(sB + st * STAGE, A.Bimg + bt * 2 * IMG, 2 * IMG, &full[st]);
+                    bulk_g2s(sB + st * STAGE + 2 * IMG, bext + bt * kTcExtBytes, kTcExtBytes, &full[st]);
                 }
             }
         }
@@ -380,8 +388,9 @@ __global__ void __launch_bounds__(64 + 32 * NE, 1) k_lse_tc2(TcArgs A) {
                 mbar_wait(&afull[ab], (c / ABUF) & 1);
                 mbar_wait(&pafull[ab], (c / ABUF) & 1);
                 const uint32_t a_hi = smem_u32(sA + ab * STAGE);
-                const uint64_t da_hi = umma_desc_sw128(a_hi), da_lo = umma_desc_sw128(a_hi + kTcImg),
-                               da_ex = umma_desc_sw32(a_hi + 2 * kTcImg);
+                const uint64_t da_hi = RB == 128 ? umma_desc_sw128(a_hi) : umma_desc_sw32(a_hi),
+                               da_lo = RB == 128 ? umma_desc_sw128(a_hi + IMG) : umma_desc_sw32(a_hi + IMG),
+                               da_ex = umma_desc_sw32(a_hi + 2 * IMG);
                 for (int i = 0; i < nt; ++i, ++g) {
                     const int st = g % kT2Stages, b = g & 1;
                     mbar_wait(&full[st], (g / kT2Stages) & 1);
@@ -389,8 +398,9 @@ __global__ void __launch_bounds__(64 + 32 * NE, 1) k_lse_tc2(TcArgs A) {
                     if (g >= 2) mbar_wait_sleep(&tempty[b], ((g >> 1) - 1) & 1);
                     tc_fence_after();
                     const uint32_t b_hi = smem_u32(sB + st * STAGE);
-                    const uint64_t db_hi = umma_desc_sw128(b_hi), db_lo = umma_desc_sw128(b_hi + kTcImg),
-                                   db_ex = umma_desc_sw32(b_hi + 2 * kTcImg);
+                    const uint64_t db_hi = RB == 128 ? umma_desc_sw128(b_hi) : umma_desc_sw32(b_hi),
+                                   db_lo = RB == 128 ? umma_desc_sw128(b_hi + IMG) : umma_desc_sw32(b_hi + IMG),
+                                   db_ex = umma_desc_sw32(b_hi + 2 * IMG);
                     const uint32_t d = tbase + (uint32_t)(b * kT2N);
                     if (elect_one()) {
                         // smallest magnitudes first (each MMA rounds at the running accumulator's
@@ -420,7 +430,7 @@ __global__ void __launch_bounds__(64 + 32 * NE, 1) k_lse_tc2(TcArgs A) {
         const int q4 = warp & 3, h = (warp - 2) >> 2;
         const int grp = h / NQG, hc = h % NQG;   // tile group, column group
         const int row = q4 * 32 + lane;
-        const float *sh = reinterpret_cast<const float *>(A.Aimg + tc_sh_off(A.P));
+        const float *sh = reinterpret_cast<const float *>(A.Aimg + tc_sh_off(A.P, RB));
         const uint32_t r_tempty = leader ? smem_u32(&tempty[0]) : mapa_u32(smem_u32(&tempty[0]), 0);
         const bool full_epi = A.mma_only == 0 || A.mma_only == 3 || A.mma_only == 5;   // 3, 5: probes without MMAs
         int g = 0;
@@ -646,7 +656,7 @@ cudaError_t microbench_mma(int kind, void *scratch, cudaStream_t st, double *flo
 
 
 // --------------------------------------------------------------------- host side
-size_t tc_image_bytes(long long P) { return (size_t)tc_side_bytes(P); }
+size_t tc_image_bytes(long long P, int rb) { return (size_t)tc_side_bytes(P, rb); }
 
 cudaError_t launch_absmax(const float *pts, long long cnt, unsigned *out, cudaStream_t st) {
     long long b = (cnt + 255) / 256;
@@ -655,19 +665,20 @@ cudaError_t launch_absmax(const float *pts, long long cnt, unsigned *out, cudaSt
 }
 
 cudaError_t launch_pack_tc(const float *pts, long long P, int d, const unsigned *amax2, int role, float eps,
-                           void *img, cudaStream_t st) {
+                           void *img, cudaStream_t st, int rb) {
+    if (!(rb == 128 || (rb == 32 && d <= 16))) return cudaErrorInvalidValue;
     const long long P2 = tc_tiles(P) * kTcM;   // zero images up to the pair tile
-    const long long total = P2 * 8LL;
+    const long long total = P2 * (rb / 16);
     long long b = (total + 255) / 256;
     k_pack_tc<<<(int)(b > 148 * 16 ? 148 * 16 : b), 256, 0, st>>>(pts, P, P2, d, amax2, role, 2.f * kLog2e / eps,
-                                                                    (unsigned char *)img);
+                                                                    (unsigned char *)img, rb);
     return cudaGetLastError();
 }
 
-cudaError_t launch_pack_tc_ext(long long P, const float *w, void *img, cudaStream_t st) {
+cudaError_t launch_pack_tc_ext(long long P, const float *w, void *img, cudaStream_t st, int rb) {
     const long long P2 = tc_tiles(P) * kTcM;
     long long b = (P2 + 255) / 256;
-    k_pack_tc_ext<<<(int)(b > 148 * 8 ? 148 * 8 : b), 256, 0, st>>>(P, P2, w, kTcFoldC, (unsigned char *)img);
+    k_pack_tc_ext<<<(int)(b > 148 * 8 ? 148 * 8 : b), 256, 0, st>>>(P, P2, w, kTcFoldC, (unsigned char *)img, rb);
     return cudaGetLastError();
 }
 
@@ -683,12 +694,12 @@ bool tc_fold_ok(float amax_x, float amax_y, float eps) {
     return mx <= 8192.0 && my <= 8192.0;
 }
 
-template <int EMU, int NE, bool SEEDED, int G, int PL = 0, bool DBG = false>
+template <int EMU, int NE, bool SEEDED, int G, int PL = 0, bool DBG = false, int RB = 128>
 static cudaError_t launch_tc2(const TcArgs &A, int items, cudaStream_t st) {
     constexpr int ABUF = 2;
-    constexpr size_t STAGE = 2 * (size_t)kTcImg + kTcExtBytes;
+    constexpr size_t STAGE = 2 * (size_t)(128 * RB) + kTcExtBytes;
     const size_t smem = 1024 + ABUF * STAGE + kT2Stages * STAGE + (NE / 4 - 1) * kTcM * 8;
-    cudaError_t e = cudaFuncSetAttribute(k_lse_tc2<EMU, NE, SEEDED, G, PL, DBG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(k_lse_tc2<EMU, NE, SEEDED, G, PL, DBG, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int nsm = 148, dev = 0;
     cudaGetDevice(&dev);
@@ -704,7 +715,7 @@ static cudaError_t launch_tc2(const TcArgs &A, int items, cudaStream_t st) {
     at[0].val.clusterDim.x = 2; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, k_lse_tc2<EMU, NE, SEEDED, G, PL, DBG>, A);
+    return cudaLaunchKernelEx(&cfg, k_lse_tc2<EMU, NE, SEEDED, G, PL, DBG, RB>, A);
 }
 
 template <int EMU>
@@ -737,6 +748,19 @@ cudaError_t launch_lse_tc(const TcPass &L, cudaStream_t st) {
     A.blk_tiles = L.blk_tiles;
     const int items = A.ptiles * L.nblk * L.split_q;
     const bool seeded = L.seeded != 0;
+    if (L.rb == 32) {
+        // compact K = 16 images (d <= 16): the solver's variants (tc_emu 1..3, both epilogues)
+        if (A.ksteps != 1) return cudaErrorInvalidValue;
+        if (L.debug_acc) return launch_tc2<2, 16, false, 2, 0, true, 32>(A, items, st);   // (selftest)
+        const bool g1 = ne == 16;
+#define SK_TC32(E) \
+        return seeded ? (g1 ? launch_tc2<E, 16, true, 1, 0, false, 32>(A, items, st) : launch_tc2<E, 16, true, 2, 0, false, 32>(A, items, st)) \
+                      : (g1 ? launch_tc2<E, 16, false, 1, 0, false, 32>(A, items, st) : launch_tc2<E, 16, false, 2, 0, false, 32>(A, items, st));
+        if (emu <= 1) { SK_TC32(1) }
+        if (emu >= 3) { SK_TC32(3) }
+        SK_TC32(2)
+#undef SK_TC32
+    }
     if (L.debug_acc) return launch_tc2<2, 16, false, 2, 0, true>(A, items, st);   // (selftest)
     switch (emu) {
         case 0: return launch_tc2_ne<0>(A, items, seeded, ne, L.pipe, st);

@@ -20,7 +20,7 @@ def ctx():
     return sk.Context(0)
 
 
-@pytest.mark.parametrize("d,sx,sy", [(64, 1, 1), (48, 1, 1), (33, 1, 1), (32, 1, 1), (20, 1, 1), (3, 1, 1),
+@pytest.mark.parametrize("d,sx,sy", [(64, 1, 1), (48, 1, 1), (33, 1, 1), (32, 1, 1), (20, 1, 1), (16, 1, 1), (3, 1, 1),
                                      (64, 1e4, 1e-3), (40, 3e-6, 7e5), (64, 1e30, 1e-30)])
 def test_tc_tile_product_is_fp32_accurate(ctx, d, sx, sy):
     """Any magnitude: the operands are scaled by exact powers of two before the fp16 split."""
