@@ -237,10 +237,9 @@ def single_spec(args):
                          "k_lse_tc2 (online LSE pass, tcgen05 cross term (d = 3 in one K = 16 step, 3-product "
                          "fp16 split) with w and the row shift folded into the MMA, K3)")
         if not ffma:
-            sp["traffic_note"] = ("DRAM bytes of one seeded K3 column pass (ncu): mostly re-reads of the reduced side's "
-                                  "operand images (K padded to 64 halves: 320 B per point, 84 MB per side, larger than "
-                                  "what stays in L2 next to the other side's); the kernel is MUFU/FMA-bound at 0.5 % of "
-                                  "HBM bandwidth")
+            sp["traffic_note"] = ("DRAM bytes of one seeded K3 column pass (ncu): both sides' operand images (compact "
+                                  "K = 16 layout, 132 B per point, 35 MB per side) and the partials; the kernel is "
+                                  "MUFU/FMA-bound, far from HBM bandwidth")
     else:
         sp.update(p=gen.c5(eps_factor=args.eps_factor or 1e-2), init=args.init or "gaussian", mode="online",
                   roof="tensor", scaling="strong", kernel="k_lse_tc2 (online LSE pass, CTA-pair tcgen05 kind::f16 3-product hi/lo "
