@@ -190,6 +190,13 @@ struct TcArgs {
     long long *cyc;             // K14: SM cycles of CTA 0 (clock64 around the work), nullable
 };
 
+// which exponential pairs of a chunk go to the FMA pipe: EMU < 100: the last EMU of every 8;
+// EMU >= 100: the last EMU - 100 of every 16 (finer balances)
+template <int EMU>
+__device__ __forceinline__ constexpr bool tc_emu_pair(int j) {
+    return EMU >= 100 ? (j & 15) >= 16 - (EMU - 100) : (j & 7) >= 8 - EMU;
+}
+
 // sum of 2^(t - M) over one 64-column chunk (32 pairs), EMU of every 8 pairs on the FMA pipe;
 // SUB = false: M = 0 (seeded passes: the shift is already in the accumulator)
 template <int EMU, bool SUB>
@@ -200,8 +207,8 @@ __device__ __forceinline__ float2 tc_sum_chunk(const float2 (&t)[32], float M) {
     for (int j = 0; j < 32; j += 2) {
         float2 e0 = t[j], e1 = t[j + 1];
         if constexpr (SUB) { e0 = sub2(e0, mm); e1 = sub2(e1, mm); }
-        if ((j & 7) >= 8 - EMU) e0 = ex2_emu2(e0); else { e0.x = ex2(e0.x); e0.y = ex2(e0.y); }
-        if (((j + 1) & 7) >= 8 - EMU) e1 = ex2_emu2(e1); else { e1.x = ex2(e1.x); e1.y = ex2(e1.y); }
+        if (tc_emu_pair<EMU>(j)) e0 = ex2_emu2(e0); else { e0.x = ex2(e0.x); e0.y = ex2(e0.y); }
+        if (tc_emu_pair<EMU>(j + 1)) e1 = ex2_emu2(e1); else { e1.x = ex2(e1.x); e1.y = ex2(e1.y); }
         s0 = add2(s0, e0);
         s1 = add2(s1, e1);
     }
@@ -216,8 +223,8 @@ __device__ __forceinline__ float2 tc_sum_half(const uint32_t (&r)[32]) {
     for (int j = 0; j < 16; j += 2) {
         float2 e0 = make_float2(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
         float2 e1 = make_float2(__uint_as_float(r[2 * j + 2]), __uint_as_float(r[2 * j + 3]));
-        if ((j & 7) >= 8 - EMU) e0 = ex2_emu2(e0); else { e0.x = ex2(e0.x); e0.y = ex2(e0.y); }
-        if (((j + 1) & 7) >= 8 - EMU) e1 = ex2_emu2(e1); else { e1.x = ex2(e1.x); e1.y = ex2(e1.y); }
+        if (tc_emu_pair<EMU>(j)) e0 = ex2_emu2(e0); else { e0.x = ex2(e0.x); e0.y = ex2(e0.y); }
+        if (tc_emu_pair<EMU>(j + 1)) e1 = ex2_emu2(e1); else { e1.x = ex2(e1.x); e1.y = ex2(e1.y); }
         s0 = add2(s0, e0);
         s1 = add2(s1, e1);
     }
@@ -757,7 +764,7 @@ cudaError_t launch_lse_tc(const TcPass &L, cudaStream_t st) {
         return seeded ? (g1 ? launch_tc2<E, 16, true, 1, 0, false, 32>(A, items, st) : launch_tc2<E, 16, true, 2, 0, false, 32>(A, items, st)) \
                       : (g1 ? launch_tc2<E, 16, false, 1, 0, false, 32>(A, items, st) : launch_tc2<E, 16, false, 2, 0, false, 32>(A, items, st));
         if (emu <= 1) { SK_TC32(1) }
-        if (emu >= 3) { SK_TC32(3) }
+        if (emu == 3) { SK_TC32(3) }
         SK_TC32(2)
 #undef SK_TC32
     }
