@@ -178,7 +178,10 @@ sk_status sk_get_solver_options(const sk_ctx *ctx, float *omega, float *decay_in
  *   "batched_cl" 0..2 (0): K13 one CTA (1) or a CTA pair (2) per problem (0: pair only for B = 1);
  *   "batched_park" >= 0 (12): K13 batches with more problems than resident CTAs run at most this
  *       many sweeps per turn, then park (state to the workspace) and re-queue with their predicted
- *       remaining sweeps as priority (bit-identical results; 0: one turn per problem, FIFO).
+ *       remaining sweeps as priority (bit-identical results; 0: one turn per problem, FIFO);
+ *   "grid_solver" 0|1 (1): the subsample initializer's inner solve (plain Sinkhorn, d <= 4, both
+ *       subsamples in every SM's shared memory, ns * ms > 2^18) in one grid-persistent launch
+ *       (K20); 0 = the general solver (K13 / multi-kernel).
  * SK_EINVAL for an unknown key or a value out of range. */
 sk_status sk_set_tuning(sk_ctx *ctx, const char *key, double value);
 /* Enable (1) / disable (0) CUDA-event timing of the dominant kernels into sk_counters. */
@@ -333,7 +336,8 @@ sk_status sinkhorn_init_gmm(sk_ctx *ctx, int64_t n, int64_t m, int32_t d, const 
 
 /* Subsample initializer (Sec. 3.4): w = x[idx_x] (ns points),
  * z = y[idx_y] (ms points), uniform weights; inner Sinkhorn at the same eps to
- * inner_tol (max inner_max_iter) -> g~; then Eq. (8)
+ * inner_tol (max inner_max_iter) -> g~ (one grid-persistent launch, K20, when it applies: see
+ * sk_set_tuning "grid_solver"); then Eq. (8)
  *   f^(0)_i = -eps log (1/ms) sum_j exp((g~_j - c(x_i, z_j))/eps)
  * in one online LSE pass over all of x.  Indices must be distinct and in range.
  * *side as above (n > m: roles swapped).  inner (nullable, host): report of the

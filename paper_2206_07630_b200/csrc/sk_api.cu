@@ -95,6 +95,7 @@ struct sk_ctx {
         int batched_shape = 1;  // K13: 512 x 2 points for 512 < P <= 1024 (0: 1024 x 1)
         int batched_cl = 0;     // K13: 0 auto, 1 one CTA, 2 a CTA pair per problem
         int batched_park = 12;  // K13 batches: sweeps per turn of the park / resume scheduler (0: off)
+        int grid_solver = 1;    // the subsample initializer's inner solve on K20 (0: solve_impl)
     } tune;
 };
 
@@ -103,7 +104,7 @@ enum BufId {
     B_STAGE0 = 0, B_STAGE_END = 16,   // staging of host arrays
     B_FLAG = 16, B_XPACK, B_XC, B_XNK, B_XPOT, B_YPACK, B_YC, B_YNK, B_YPOT, B_PART, B_BLKE, B_BLKB,
     B_STATUS, B_COST, B_REP, B_SORT, B_PERM, B_YSORT, B_GAUSS, B_GAUSS2, B_GMM, B_SUBW, B_SUBZ,
-    B_SUBF, B_SUBG, B_IDX, B_OUT, B_FA, B_QUEUE, B_XIMG, B_YIMG, B_XLSE, B_YLSE, B_TCMAX, B_EMST, B_EMPART, B_EMIDX, B_VJP, B_ANDFR, B_ANDBLK, B_ANDVEC, B_ANDST, B_XCHG, B_PARK, B_XCNT, B_XROW, B_XCNT2, B_NBUF
+    B_SUBF, B_SUBG, B_IDX, B_OUT, B_FA, B_QUEUE, B_XIMG, B_YIMG, B_XLSE, B_YLSE, B_TCMAX, B_EMST, B_EMPART, B_EMIDX, B_VJP, B_ANDFR, B_ANDBLK, B_ANDVEC, B_ANDST, B_XCHG, B_PARK, B_XCNT, B_XROW, B_XCNT2, B_GRID, B_NBUF
 };
 
 sk_status fail(sk_ctx *c, sk_status s, const char *fmt, ...) {
@@ -952,6 +953,7 @@ sk_status sk_set_tuning(sk_ctx *ctx, const char *key, double value) {
     else if (k == "batched_shape") { CK(need(iv == 0 || iv == 1)); T.batched_shape = iv; }
     else if (k == "batched_cl") { CK(need(iv >= 0 && iv <= 2)); T.batched_cl = iv; }
     else if (k == "batched_park") { CK(need(iv >= 0 && iv <= 100000)); T.batched_park = iv; }
+    else if (k == "grid_solver") { CK(need(iv == 0 || iv == 1)); T.grid_solver = iv; }
     else return fail(ctx, SK_EINVAL, "sk_set_tuning: unknown key '%s'", key);
     return SK_OK;
 }
@@ -1388,8 +1390,38 @@ sk_status sinkhorn_init_subsample(sk_ctx *ctx, int64_t n, int64_t m, int32_t d, 
     ctx->cnt.kernel_launches += 2;
     // inner solve (uniform weights, same eps, inner_tol) -> g~ (Sec. 3.4)
     sk_report rin{};
-    sk_status s = solve_impl(ctx, 1, ns, ms, d, w, 0, z, 0, nullptr, 0, nullptr, 0, eps, inner_tol,
-                             inner_max_iter, 1, SK_COST_ONLINE, nullptr, fb, gbv, &rin);
+    sk_status s;
+    // plain Sinkhorn on a problem whose clouds fit every SM's shared memory: one grid-persistent
+    // launch (K20) instead of the multi-kernel loop (C4's 4096^2 inner solve: 9.2 -> ~2 ms)
+    const bool plain = ctx->anderson < 2 && ctx->omega == 1.f && ctx->decay_init <= 0.f && !ctx->adapt;
+    if (plain && ctx->tune.grid_solver && grid_solver_supported(d, (int)ns, (int)ms) &&
+        (double)ns * ms > (double)(1 << 18)) {
+        int nsm = 148;
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device);
+        ENSURE(gw, char, B_GRID, grid_solver_workspace_bytes((int)ns, (int)ms, nsm));
+        GridLaunch GL{(int)ns, (int)ms, d, w, z, nullptr, nullptr, nullptr, eps, inner_tol, inner_max_iter, 1,
+                      fb, gbv, gw, nullptr};
+        GridResult hr{};
+        GL.res_host = &hr;
+        CU(cudaEventRecord(ctx->ev0, ctx->stream));
+        CU(launch_grid_solver(GL, ctx->stream));
+        CU(cudaEventRecord(ctx->ev1, ctx->stream));
+        CU(cudaStreamSynchronize(ctx->stream));
+        float gms = 0.f;
+        CU(cudaEventElapsedTime(&gms, ctx->ev0, ctx->ev1));
+        ctx->cnt.kernel_launches += 1;
+        ctx->cnt.lse_launches += 1;
+        ctx->cnt.lse_ex2 += (double)ns * ms * (2.0 * hr.iterations + 1.0);
+        rin.iterations = hr.iterations;
+        rin.converged = hr.converged;
+        rin.marginal_error = hr.err;
+        rin.dual_objective = hr.E;
+        rin.solve_ms = gms;
+        s = hr.nonfinite ? SK_ENONFINITE : SK_OK;
+    } else {
+        s = solve_impl(ctx, 1, ns, ms, d, w, 0, z, 0, nullptr, 0, nullptr, 0, eps, inner_tol,
+                       inner_max_iter, 1, SK_COST_ONLINE, nullptr, fb, gbv, &rin);
+    }
     if (s != SK_OK && s != SK_ENONFINITE) return s;
     if (inner) *inner = rin;
     if (s == SK_ENONFINITE) return fail(ctx, SK_ENONFINITE, "inner subsample solve became non-finite");

@@ -77,6 +77,29 @@ cudaError_t launch_soft_rank_sort(long long B, int n, int m, const float *x, con
 size_t batched_smem_bytes(int D, int n, int m, int mem = 0);
 cudaError_t launch_batched(const BatchLaunch &L, cudaStream_t st);
 
+// ------------------------------------------------ K20: grid-persistent medium solver
+// One problem (online cost, d <= 4, both clouds in every CTA's shared memory), plain Sinkhorn
+// (omega = 1), solved in one cooperative launch (sk_grid.cu).  Used for the subsample
+// initializer's inner solve.
+struct GridResult {
+    double E;
+    int iterations, converged, nonfinite;
+    float err;
+};
+struct GridLaunch {
+    int n, m, d;
+    const float *x, *y, *a, *b, *finit;   // device; a, b, finit nullable
+    float eps, tol;
+    int max_iter, check_every;
+    float *f, *g;                         // device outputs
+    void *work;                           // grid_solver_workspace_bytes(n, m, #SMs)
+    GridResult *res_host;                 // pinned host result (copied on the stream), nullable
+};
+bool grid_solver_supported(int d, int n, int m);
+size_t grid_solver_smem(int d, int n, int m);
+size_t grid_solver_workspace_bytes(int n, int m, int nsm);
+cudaError_t launch_grid_solver(const GridLaunch &L, cudaStream_t st);
+
 // ------------------------------------------------- multi-kernel online path
 // Device status of one solve (all fields written only by kernels' last blocks).
 struct DevStatus {

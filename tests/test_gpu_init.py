@@ -82,6 +82,59 @@ def test_subsample_init(O, ctx, n, ns):
     assert rel_inf(centred(pot.cpu().numpy()), centred(ref), p.eps) <= INIT_RTOL
 
 
+@pytest.mark.parametrize("n,m,d,ns,ms,eps_f,cap,shift", [(7000, 9000, 3, 1500, 1100, 0.01, 0, 0.0),
+                                                          (6000, 6000, 2, 700, 800, 0.003, 60, 1.0),
+                                                          (8000, 9000, 4, 1200, 3100, 0.05, 0, 0.0),
+                                                          (5000, 5000, 1, 600, 4737, 0.05, 0, 0.0)])
+def test_subsample_inner_grid_solver(O, ctx, n, m, d, ns, ms, eps_f, cap, shift):
+    """K20 (the grid-persistent inner solve), side 0 (n <= m): ragged ns != ms, d = 1..4, point
+    counts past the one-round-per-CTA limit (4737 > 32 x 148), and a small eps whose first seeded
+    sweeps move the LSEs by more than the seeded range (the exact redo of a point group) - run for
+    `cap` sweeps on clouds shifted apart (on overlapping clouds the centred potentials span only
+    ~0.01 of max |q|^2, so fp32's ulp(|q|^2) / eps rounding alone is 1.3e-4 of them after 60
+    sweeps on both paths, tools/k20_check.py).  The inner report (L, err, E) against the oracle's inner solve, the potential in
+    lockstep, and the same through the multi-kernel path (sk_set_tuning grid_solver 0)."""
+    import paper_2206_07630_b200 as sk
+    from parity import assert_obj_close, count_tol
+    rng = np.random.default_rng(n + d)
+    x = rng.random((n, d)).astype(np.float32)
+    y = (rng.random((m, d)) * 0.9 + 0.05 + shift).astype(np.float32)
+    ix = np.sort(rng.choice(n, ns, replace=False)).astype(np.int32)
+    iy = np.sort(rng.choice(m, ms, replace=False)).astype(np.int32)
+    eps = float(np.float32(eps_f * gen.mean_sq_cost(x, y)))
+    tol, max_iter = (1e-12, cap) if cap else (1e-4, 10000)
+    w, z = x[ix], y[iy]
+    ref = None if cap else O.sinkhorn(w, z, eps, tol=tol)
+    for gs in (1, 0):
+        ctx.set_tuning("grid_solver", gs)
+        try:
+            pot, side, inner = sk.sinkhorn_init_subsample(ctx, _cuda(x), _cuda(y), _cuda(ix), _cuda(iy), eps, tol,
+                                                         inner_max_iter=max_iter)
+        finally:
+            ctx.set_tuning("grid_solver", 1)
+        assert side == 0, (gs, side)
+        if cap:
+            assert inner["iterations"] == cap and not inner["converged"], (gs, inner)
+        else:
+            assert inner["converged"], (gs, inner)
+            assert abs(inner["iterations"] - ref.iterations) <= count_tol(ref.iterations), (gs, inner, ref.iterations)
+        lock = O.sinkhorn(w, z, eps, tol=0, max_iter=inner["iterations"])
+        assert_obj_close(inner["dual_objective"], lock.E, eps, what=f"grid_solver={gs}")
+        # the reported err_L is formed from fp32 potentials at the scale of |q|^2: ~4 ulp(max |q|^2) /
+        # eps of noise per term (as test_gpu_adaptive)
+        scale = max(float((w.astype(np.float64) ** 2).sum(-1).max()), float((z.astype(np.float64) ** 2).sum(-1).max()))
+        slack = 4 * 2.0 ** -24 * scale / eps
+        assert abs(inner["marginal_error"] - lock.err) <= 0.02 * lock.err + slack + 1e-7, (gs, inner, lock.err, slack)
+        ex = O.subsample_extrapolate(x, z, lock.g, eps)
+        assert rel_inf(centred(pot.cpu().numpy()), centred(ex), eps) <= INIT_RTOL, gs
+    # a capped inner solve: max_iter sweeps, not converged
+    _, _, capped = sk.sinkhorn_init_subsample(ctx, _cuda(x), _cuda(y), _cuda(ix), _cuda(iy), eps, 1e-12,
+                                             inner_max_iter=5)
+    assert capped["iterations"] == 5 and not capped["converged"]
+    lock5 = O.sinkhorn(w, z, eps, tol=0, max_iter=5)
+    assert_obj_close(capped["dual_objective"], lock5.E, eps, what="capped")
+
+
 def test_initializer_argument_errors(ctx):
     import paper_2206_07630_b200 as sk
     x = _cuda(np.random.default_rng(0).random((10, 2)).astype(np.float32))
