@@ -1404,7 +1404,15 @@ sk_status sinkhorn_init_subsample(sk_ctx *ctx, int64_t n, int64_t m, int32_t d, 
         GridResult hr{};
         GL.res_host = &hr;
         CU(cudaEventRecord(ctx->ev0, ctx->stream));
-        CU(launch_grid_solver(GL, ctx->stream));
+        const cudaError_t ge = launch_grid_solver(GL, ctx->stream);
+        if (ge == cudaErrorCooperativeLaunchTooLarge || ge == cudaErrorInvalidConfiguration) {
+            // (fewer SMs available than the grid needs co-resident: the general solver)
+            cudaGetLastError();
+            s = solve_impl(ctx, 1, ns, ms, d, w, 0, z, 0, nullptr, 0, nullptr, 0, eps, inner_tol,
+                           inner_max_iter, 1, SK_COST_ONLINE, nullptr, fb, gbv, &rin);
+            goto inner_done;
+        }
+        CU(ge);
         CU(cudaEventRecord(ctx->ev1, ctx->stream));
         CU(cudaStreamSynchronize(ctx->stream));
         float gms = 0.f;
@@ -1422,6 +1430,7 @@ sk_status sinkhorn_init_subsample(sk_ctx *ctx, int64_t n, int64_t m, int32_t d, 
         s = solve_impl(ctx, 1, ns, ms, d, w, 0, z, 0, nullptr, 0, nullptr, 0, eps, inner_tol,
                        inner_max_iter, 1, SK_COST_ONLINE, nullptr, fb, gbv, &rin);
     }
+inner_done:
     if (s != SK_OK && s != SK_ENONFINITE) return s;
     if (inner) *inner = rin;
     if (s == SK_ENONFINITE) return fail(ctx, SK_ENONFINITE, "inner subsample solve became non-finite");
