@@ -21,7 +21,9 @@ namespace sk {
 constexpr int kGT = 256;
 
 // ------------------------------------------------------------- moments
-// out[blk][E]: E = d (pass 1, mean == nullptr) or d*d (pass 2, centred by mean).
+// out[blk][E]: E = d (pass 1, mean == nullptr) or d*d (pass 2, centred by mean).  Pass 2: the
+// 16 x 16 threads each own a 4 x 4 block of entries (rows br + 16 i, columns bc + 16 j: per chunk
+// row, 2 broadcast + 4 conflict-free shared loads feed 16 FMAs).
 __global__ void __launch_bounds__(kGT) k_moment_partials(const float *__restrict__ x,
                                                          const float *__restrict__ w, long long n,
                                                          int d, const double *__restrict__ mean,
@@ -29,9 +31,9 @@ __global__ void __launch_bounds__(kGT) k_moment_partials(const float *__restrict
     constexpr int CH = 64;
     extern __shared__ double xs[];  // [CH][d] weighted/centred chunk, then [CH] weights
     double *ws = xs + CH * d;
-    const int E = mean ? d * d : d;
     const long long per = (n + gridDim.x - 1) / gridDim.x;
     const long long lo = blockIdx.x * per, hi = min(n, lo + per);
+    const int br = threadIdx.x >> 4, bc = threadIdx.x & 15;
     double acc[16];
 #pragma unroll
     for (int t = 0; t < 16; ++t) acc[t] = 0.0;
@@ -45,32 +47,55 @@ __global__ void __launch_bounds__(kGT) k_moment_partials(const float *__restrict
         }
         for (int r = threadIdx.x; r < cnt; r += kGT) ws[r] = w ? (double)w[c0 + r] : 1.0 / n;
         __syncthreads();
+        if (mean) {
+            for (int r = 0; r < cnt; ++r) {
+                const double *xr = xs + r * d;
+                const double wr = ws[r];
+                double a[4], b[4];
 #pragma unroll
-        for (int t = 0; t < 16; ++t) {
-            const int e = threadIdx.x + t * kGT;
-            if (e >= E) break;
-            double s = 0.0;
-            if (mean) {
-                const int k = e / d, l = e % d;
-                for (int r = 0; r < cnt; ++r) s += ws[r] * xs[r * d + k] * xs[r * d + l];
-            } else {
-                for (int r = 0; r < cnt; ++r) s += ws[r] * xs[r * d + e];
+                for (int i = 0; i < 4; ++i) a[i] = br + 16 * i < d ? wr * xr[br + 16 * i] : 0.0;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) b[j] = bc + 16 * j < d ? xr[bc + 16 * j] : 0.0;
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) acc[4 * i + j] = fma(a[i], b[j], acc[4 * i + j]);
             }
-            acc[t] += s;
+        } else if (threadIdx.x < d) {
+            double sm = 0.0;
+            for (int r = 0; r < cnt; ++r) sm += ws[r] * xs[r * d + threadIdx.x];
+            acc[0] += sm;
         }
     }
+    if (mean) {
 #pragma unroll
-    for (int t = 0; t < 16; ++t) {
-        const int e = threadIdx.x + t * kGT;
-        if (e < E) out[(long long)blockIdx.x * E + e] = acc[t];
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int k = br + 16 * i, l = bc + 16 * j;
+                if (k < d && l < d) out[(long long)blockIdx.x * d * d + k * d + l] = acc[4 * i + j];
+            }
+    } else if (threadIdx.x < d) {
+        out[(long long)blockIdx.x * d + threadIdx.x] = acc[0];
     }
 }
 
-__global__ void k_reduce_cols(const double *in, int nb, int E, double *out) {
-    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) {
-        double s = 0.0;
-        for (int b = 0; b < nb; ++b) s += in[(long long)b * E + e];
-        out[e] = s;
+// Fixed-order sum over the nb block partials: 8 warps split the blocks (block b to warp b % 8, in
+// order), then the 8 warp sums in warp order; 32 entries per CTA (lane = entry).
+__global__ void __launch_bounds__(256) k_reduce_cols(const double *in, int nb, int E, double *out) {
+    __shared__ double ps[8][32];
+    const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+    const int e = blockIdx.x * 32 + lane;
+    double s = 0.0;
+    if (e < E)
+        for (int b = wp; b < nb; b += 8) s += in[(long long)b * E + e];
+    ps[wp][lane] = s;
+    __syncthreads();
+    if (wp == 0 && e < E) {
+        double t = 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) t += ps[u][lane];
+        out[e] = t;
     }
 }
 
@@ -83,20 +108,40 @@ cudaError_t launch_moments(const float *x, const float *w, long long n, int d, d
     if (nb < 1) return cudaErrorInvalidValue;
     const size_t smem = (64 * (size_t)d + 64) * sizeof(double);
     k_moment_partials<<<(int)nb, kGT, smem, st>>>(x, w, n, d, nullptr, scratch);
-    k_reduce_cols<<<1, 256, 0, st>>>(scratch, (int)nb, d, mean);
+    k_reduce_cols<<<(d + 31) / 32, 256, 0, st>>>(scratch, (int)nb, d, mean);
     k_moment_partials<<<(int)nb, kGT, smem, st>>>(x, w, n, d, mean, scratch);
-    k_reduce_cols<<<(d * d + 255) / 256, 256, 0, st>>>(scratch, (int)nb, d * d, cov);
+    k_reduce_cols<<<(d * d + 31) / 32, 256, 0, st>>>(scratch, (int)nb, d * d, cov);
     return cudaGetLastError();
 }
 
 // ----------------------------------------------------- fp64 dense helpers
-// C = A * B (d x d, smem), all threads of the block; C must not alias A or B.
+// C = A * B (d x d, smem, d <= 64), blockDim.x == 256; C must not alias A or B.  Thread (br, bc)
+// of 16 x 16 owns C[br + 16 i][bc + 16 j], i, j < 4: per k, 4 broadcast loads of A and 4
+// conflict-free loads of B feed 16 FMAs; each entry sums over k in order.
 __device__ void mm(const double *A, const double *B, double *C, int d) {
-    for (int e = threadIdx.x; e < d * d; e += blockDim.x) {
-        const int i = e / d, j = e % d;
-        double s = 0.0;
-        for (int k = 0; k < d; ++k) s += A[i * d + k] * B[k * d + j];
-        C[e] = s;
+    const int br = threadIdx.x >> 4, bc = threadIdx.x & 15;
+    double acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+    if (br < d && bc < d) {
+        for (int k = 0; k < d; ++k) {
+            double a[4], b[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) a[i] = br + 16 * i < d ? A[(br + 16 * i) * d + k] : 0.0;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) b[j] = bc + 16 * j < d ? B[k * d + bc + 16 * j] : 0.0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (br + 16 * i < d && bc + 16 * j < d) C[(br + 16 * i) * d + bc + 16 * j] = acc[i][j];
     }
     __syncthreads();
 }
@@ -212,40 +257,97 @@ cudaError_t launch_gauss_A(const double *mean_mu, double *cov_mu, const double *
     return cudaGetLastError();
 }
 
-// f*(x_i) in fp64, thread per point (d <= 64; A, means cached in smem).
+// f*(x_i) in fp64 (d <= 64; A, means cached in shared memory), tiles of 64 points: the tile's
+// centred coordinates staged by coalesced loads; thread (kq, p) forms rows k in [16 kq, 16 kq + 16)
+// of A c_p (c_p 8 at a time in registers, A read as broadcast double2) and its part of
+// c_p^T A c_p; the 4 parts summed in kq order.
+constexpr int kPotTile = 64;
+
+size_t gauss_pot_smem(int d) {
+    const int dp = (d + 1) & ~1;
+    return sizeof(double) * ((size_t)d * dp + 2 * d + (size_t)kPotTile * (d + 1) + 4 * kPotTile) +
+           sizeof(float) * (size_t)kPotTile * d;
+}
+
 __global__ void __launch_bounds__(kGT) k_gauss_pot(const float *__restrict__ x, long long n, int d,
                                                     const double *__restrict__ mmu,
                                                     const double *__restrict__ mnu,
                                                     const double *__restrict__ A, float *pot) {
     extern __shared__ double s[];
-    double *sA = s, *smu = s + d * d, *snu = smu + d;
-    for (int e = threadIdx.x; e < d * d; e += blockDim.x) sA[e] = A[e];
+    const int dp = (d + 1) & ~1, d1 = d + 1;
+    double *sA = s;                       // [d][dp]
+    double *smu = sA + d * dp, *snu = smu + d;
+    double *cs = snu + d;                 // [64][d + 1] centred coordinates
+    double *red = cs + kPotTile * d1;     // [4][64]
+    float *xr = reinterpret_cast<float *>(red + 4 * kPotTile);   // [64][d] raw coordinates
+    for (int e = threadIdx.x; e < d * dp; e += blockDim.x) {
+        const int k = e / dp, l = e % dp;
+        sA[e] = l < d ? A[k * d + l] : 0.0;
+    }
     for (int k = threadIdx.x; k < d; k += blockDim.x) { smu[k] = mmu[k]; snu[k] = mnu[k]; }
-    __syncthreads();
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-         i += (long long)gridDim.x * blockDim.x) {
-        const float *xi = x + i * d;
-        double nx = 0.0, lin = 0.0, quad = 0.0;
-        for (int k = 0; k < d; ++k) {
-            const double xk = xi[k];
-            nx += xk * xk;
-            lin += snu[k] * xk;
-            const double ck = xk - smu[k];
-            double row = 0.0;
-            for (int l = 0; l < d; ++l) row += sA[k * d + l] * ((double)xi[l] - smu[l]);
-            quad += ck * row;
+    const int p = threadIdx.x & (kPotTile - 1), kq = threadIdx.x >> 6;
+    const long long tiles = (n + kPotTile - 1) / kPotTile;
+    for (long long tb = blockIdx.x; tb < tiles; tb += gridDim.x) {
+        const long long i0 = tb * kPotTile;
+        const int cnt = (int)min((long long)kPotTile, n - i0);
+        __syncthreads();   // (the previous tile's readers are done; sA / means visible)
+        for (int e = threadIdx.x; e < kPotTile * d; e += blockDim.x) {
+            const int r = e / d, k = e % d;
+            const float v = r < cnt ? x[(i0 + r) * d + k] : 0.f;
+            xr[e] = v;
+            cs[r * d1 + k] = (double)v - smu[k];
         }
-        pot[i] = (float)(nx - quad - 2.0 * lin);
+        __syncthreads();
+        const double *cp = cs + p * d1;
+        double row[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) row[u] = 0.0;
+        for (int l0 = 0; l0 < d; l0 += 8) {
+            double c[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) c[u] = l0 + u < d ? cp[l0 + u] : 0.0;
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+                const int k = 16 * kq + u;
+                if (k >= d) break;
+                const double2 *ar = reinterpret_cast<const double2 *>(sA + k * dp + l0);
+                double r = row[u];
+#pragma unroll
+                for (int v = 0; v < 4; ++v) {
+                    if (l0 + 2 * v >= dp) break;
+                    const double2 a2 = ar[v];
+                    r = fma(a2.x, c[2 * v], r);
+                    r = fma(a2.y, c[2 * v + 1], r);
+                }
+                row[u] = r;
+            }
+        }
+        double q = 0.0;
+#pragma unroll
+        for (int u = 0; u < 16; ++u)
+            if (16 * kq + u < d) q = fma(cp[16 * kq + u], row[u], q);
+        red[kq * kPotTile + p] = q;
+        __syncthreads();
+        if (kq == 0 && p < cnt) {
+            const double quad = ((red[p] + red[kPotTile + p]) + red[2 * kPotTile + p]) + red[3 * kPotTile + p];
+            double nx = 0.0, lin = 0.0;
+            for (int k = 0; k < d; ++k) {
+                const double xk = xr[p * d + k];
+                nx += xk * xk;
+                lin += snu[k] * xk;
+            }
+            pot[i0 + p] = (float)(nx - quad - 2.0 * lin);
+        }
     }
 }
 
 cudaError_t launch_gauss_potential(const float *x, long long n, int d, const double *m_mu,
                                    const double *m_nu, const double *A, float *pot, cudaStream_t st) {
-    const size_t smem = ((size_t)d * d + 2 * d) * sizeof(double);
+    const size_t smem = gauss_pot_smem(d);
     cudaError_t e = cudaFuncSetAttribute(k_gauss_pot, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    long long b = (n + kGT - 1) / kGT;
-    k_gauss_pot<<<(int)(b > 148 * 8 ? 148 * 8 : b), kGT, smem, st>>>(x, n, d, m_mu, m_nu, A, pot);
+    const long long tiles = (n + kPotTile - 1) / kPotTile;
+    k_gauss_pot<<<(int)(tiles > 148 * 2 ? 148 * 2 : tiles), kGT, smem, st>>>(x, n, d, m_mu, m_nu, A, pot);
     return cudaGetLastError();
 }
 
