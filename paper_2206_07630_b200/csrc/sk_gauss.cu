@@ -126,6 +126,7 @@ __device__ void mm(const double *A, const double *B, double *C, int d) {
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
     if (br < d && bc < d) {
+#pragma unroll 4
         for (int k = 0; k < d; ++k) {
             double a[4], b[4];
 #pragma unroll
