@@ -22,8 +22,9 @@ constexpr int kGT = 256;
 
 // ------------------------------------------------------------- moments
 // out[blk][E]: E = d (pass 1, mean == nullptr) or d*d (pass 2, centred by mean).  Pass 2: the
-// 16 x 16 threads each own a 4 x 4 block of entries (rows br + 16 i, columns bc + 16 j: per chunk
-// row, 2 broadcast + 4 conflict-free shared loads feed 16 FMAs).
+// 16 x 16 threads each own a TI x TI block of entries (rows br + 16 i, columns bc + 16 j, TI =
+// ceil(d / 16): per chunk row, TI broadcast + TI conflict-free shared loads feed TI^2 FMAs).
+template <int TI>
 __global__ void __launch_bounds__(kGT) k_moment_partials(const float *__restrict__ x,
                                                          const float *__restrict__ w, long long n,
                                                          int d, const double *__restrict__ mean,
@@ -34,9 +35,9 @@ __global__ void __launch_bounds__(kGT) k_moment_partials(const float *__restrict
     const long long per = (n + gridDim.x - 1) / gridDim.x;
     const long long lo = blockIdx.x * per, hi = min(n, lo + per);
     const int br = threadIdx.x >> 4, bc = threadIdx.x & 15;
-    double acc[16];
+    double acc[TI * TI];
 #pragma unroll
-    for (int t = 0; t < 16; ++t) acc[t] = 0.0;
+    for (int t = 0; t < TI * TI; ++t) acc[t] = 0.0;
     for (long long c0 = lo; c0 < hi; c0 += CH) {
         const int cnt = (int)min((long long)CH, hi - c0);
         __syncthreads();
@@ -51,15 +52,15 @@ __global__ void __launch_bounds__(kGT) k_moment_partials(const float *__restrict
             for (int r = 0; r < cnt; ++r) {
                 const double *xr = xs + r * d;
                 const double wr = ws[r];
-                double a[4], b[4];
+                double a[TI], b[TI];
 #pragma unroll
-                for (int i = 0; i < 4; ++i) a[i] = br + 16 * i < d ? wr * xr[br + 16 * i] : 0.0;
+                for (int i = 0; i < TI; ++i) a[i] = br + 16 * i < d ? wr * xr[br + 16 * i] : 0.0;
 #pragma unroll
-                for (int j = 0; j < 4; ++j) b[j] = bc + 16 * j < d ? xr[bc + 16 * j] : 0.0;
+                for (int j = 0; j < TI; ++j) b[j] = bc + 16 * j < d ? xr[bc + 16 * j] : 0.0;
 #pragma unroll
-                for (int i = 0; i < 4; ++i)
+                for (int i = 0; i < TI; ++i)
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) acc[4 * i + j] = fma(a[i], b[j], acc[4 * i + j]);
+                    for (int j = 0; j < TI; ++j) acc[TI * i + j] = fma(a[i], b[j], acc[TI * i + j]);
             }
         } else if (threadIdx.x < d) {
             double sm = 0.0;
@@ -69,11 +70,11 @@ __global__ void __launch_bounds__(kGT) k_moment_partials(const float *__restrict
     }
     if (mean) {
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < TI; ++i)
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
+            for (int j = 0; j < TI; ++j) {
                 const int k = br + 16 * i, l = bc + 16 * j;
-                if (k < d && l < d) out[(long long)blockIdx.x * d * d + k * d + l] = acc[4 * i + j];
+                if (k < d && l < d) out[(long long)blockIdx.x * d * d + k * d + l] = acc[TI * i + j];
             }
     } else if (threadIdx.x < d) {
         out[(long long)blockIdx.x * d + threadIdx.x] = acc[0];
@@ -107,43 +108,53 @@ cudaError_t launch_moments(const float *x, const float *w, long long n, int d, d
     if (nb * d * d > scratch_doubles) nb = scratch_doubles / (d * d);
     if (nb < 1) return cudaErrorInvalidValue;
     const size_t smem = (64 * (size_t)d + 64) * sizeof(double);
-    k_moment_partials<<<(int)nb, kGT, smem, st>>>(x, w, n, d, nullptr, scratch);
+    auto kern = d <= 16 ? k_moment_partials<1> : d <= 32 ? k_moment_partials<2>
+              : d <= 48 ? k_moment_partials<3> : k_moment_partials<4>;
+    kern<<<(int)nb, kGT, smem, st>>>(x, w, n, d, nullptr, scratch);
     k_reduce_cols<<<(d + 31) / 32, 256, 0, st>>>(scratch, (int)nb, d, mean);
-    k_moment_partials<<<(int)nb, kGT, smem, st>>>(x, w, n, d, mean, scratch);
+    kern<<<(int)nb, kGT, smem, st>>>(x, w, n, d, mean, scratch);
     k_reduce_cols<<<(d * d + 31) / 32, 256, 0, st>>>(scratch, (int)nb, d * d, cov);
     return cudaGetLastError();
 }
 
 // ----------------------------------------------------- fp64 dense helpers
 // C = A * B (d x d, smem, d <= 64), blockDim.x == 256; C must not alias A or B.  Thread (br, bc)
-// of 16 x 16 owns C[br + 16 i][bc + 16 j], i, j < 4: per k, 4 broadcast loads of A and 4
-// conflict-free loads of B feed 16 FMAs; each entry sums over k in order.
-__device__ void mm(const double *A, const double *B, double *C, int d) {
+// of 16 x 16 owns C[br + 16 i][bc + 16 j], i, j < TI = ceil(d / 16): per k, TI broadcast loads
+// of A and TI conflict-free loads of B feed TI^2 FMAs; each entry sums over k in order.
+template <int TI>
+__device__ __forceinline__ void mm_t(const double *A, const double *B, double *C, int d) {
     const int br = threadIdx.x >> 4, bc = threadIdx.x & 15;
-    double acc[4][4];
+    double acc[TI][TI];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < TI; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+        for (int j = 0; j < TI; ++j) acc[i][j] = 0.0;
     if (br < d && bc < d) {
 #pragma unroll 4
         for (int k = 0; k < d; ++k) {
-            double a[4], b[4];
+            double a[TI], b[TI];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) a[i] = br + 16 * i < d ? A[(br + 16 * i) * d + k] : 0.0;
+            for (int i = 0; i < TI; ++i) a[i] = br + 16 * i < d ? A[(br + 16 * i) * d + k] : 0.0;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) b[j] = bc + 16 * j < d ? B[k * d + bc + 16 * j] : 0.0;
+            for (int j = 0; j < TI; ++j) b[j] = bc + 16 * j < d ? B[k * d + bc + 16 * j] : 0.0;
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
+            for (int i = 0; i < TI; ++i)
 #pragma unroll
-                for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+                for (int j = 0; j < TI; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
         }
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < TI; ++i)
 #pragma unroll
-            for (int j = 0; j < 4; ++j)
+            for (int j = 0; j < TI; ++j)
                 if (br + 16 * i < d && bc + 16 * j < d) C[(br + 16 * i) * d + bc + 16 * j] = acc[i][j];
     }
+}
+
+__device__ void mm(const double *A, const double *B, double *C, int d) {
+    if (d <= 16) mm_t<1>(A, B, C, d);
+    else if (d <= 32) mm_t<2>(A, B, C, d);
+    else if (d <= 48) mm_t<3>(A, B, C, d);
+    else mm_t<4>(A, B, C, d);
     __syncthreads();
 }
 
