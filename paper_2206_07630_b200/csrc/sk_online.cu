@@ -534,14 +534,28 @@ __global__ void __launch_bounds__(kMT) k_merge(MergePass Mp, Side S, Side Qs) {
         s_last = atomicAdd(tk, 1u) == gridDim.x - 1;
     }
     __syncthreads();
-    if (!s_last || threadIdx.x != 0) return;
+    if (!s_last) return;
     __threadfence();
+    // the last block sums the block partials: thread t takes blocks t, t + 256, ... in order,
+    // then a fixed tree (lanes by xor, the 8 warps in order) - deterministic, and parallel (a
+    // serial sum over ~1000 blocks by one thread took tens of microseconds)
     double et = 0.0, et2 = 0.0; int bt = 0;
-    for (int i = 0; i < (int)gridDim.x; ++i) {
-        et += ((volatile double *)Mp.blk_err)[i];
-        et2 += ((volatile double *)Mp.blk_err)[kMergeMaxBlocks + i];
-        bt |= ((volatile int *)Mp.blk_bad)[i];
+    for (int i = threadIdx.x; i < (int)gridDim.x; i += kMT) {
+        et += __ldcg(Mp.blk_err + i);
+        et2 += __ldcg(Mp.blk_err + kMergeMaxBlocks + i);
+        bt |= __ldcg(Mp.blk_bad + i);
     }
+    for (int o = 16; o > 0; o >>= 1) {
+        et += __shfl_xor_sync(0xffffffffu, et, o);
+        et2 += __shfl_xor_sync(0xffffffffu, et2, o);
+        bt |= __shfl_xor_sync(0xffffffffu, bt, o);
+    }
+    __syncthreads();   // (red / red2 / redi reused)
+    if ((threadIdx.x & 31) == 0) { red[threadIdx.x >> 5] = et; red2[threadIdx.x >> 5] = et2; redi[threadIdx.x >> 5] = bt; }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    et = 0.0; et2 = 0.0; bt = 0;
+    for (int w = 0; w < kMT / 32; ++w) { et += red[w]; et2 += red2[w]; bt |= redi[w]; }
     if (Mp.mode == MERGE_COL) {
         st->ticket_col = 0;
         if (bt & 2) { st->colfail = 1; __threadfence(); return; }   // decisions left to the exact redo
@@ -645,10 +659,11 @@ __global__ void __launch_bounds__(1024) k_report(Side X, Side Y, const float *a,
     const int l = st->final_iter, lg = l + st->g_off;
     const float *f = (l & 1) ? X.pot[1] : X.pot[0], *g = (lg & 1) ? Y.pot[1] : Y.pot[0];
     double s = 0.0;
-    for (int i = threadIdx.x; i < X.P; i += 1024) {
-        const double ai = a ? (double)a[i] : 1.0 / n_uniform;
-        s += (double)f[i] * ai - (double)eps * ai;
-    }
+    if (!local_only)   // (local_only: <f,a> comes from k_report_blocks)
+        for (int i = threadIdx.x; i < X.P; i += 1024) {
+            const double ai = a ? (double)a[i] : 1.0 / n_uniform;
+            s += (double)f[i] * ai - (double)eps * ai;
+        }
     double s2 = 0.0;
     for (int j = threadIdx.x; j < Y.P; j += 1024) s2 += (double)g[j] * (b ? (double)b[j] : 1.0 / Y.P);
     const double fa = block_sum_d<1024>(s, red);
