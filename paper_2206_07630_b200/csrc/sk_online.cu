@@ -114,6 +114,24 @@ __device__ __forceinline__ float2 premerge_point(const float2 *src, int split_q,
     return make_float2(M, S);
 }
 
+// The same merge (the same max, the same fmaf order) with all partials in flight at once: one L2
+// round trip instead of 2 x split_q dependent ones.  For the standalone premerge kernel only (its
+// 64 extra registers would cut K2's occupancy if inlined into the fused premerge).
+__device__ __forceinline__ float2 premerge_point_r(const float2 *src, int split_q, long long P) {
+    if (split_q > 32) return premerge_point(src, split_q, P);
+    float2 v[32];
+#pragma unroll
+    for (int u = 0; u < 32; ++u) v[u] = u < split_q ? __ldcg(src + u * P) : make_float2(-INFINITY, 0.f);
+    float M = -INFINITY;
+#pragma unroll
+    for (int u = 0; u < 32; ++u) M = fmaxf(M, v[u].x);
+    float S = 0.f;
+#pragma unroll
+    for (int u = 0; u < 32; ++u)
+        if (u < split_q && v[u].x != -INFINITY) S = fmaf(v[u].y, ex2(v[u].x - M), S);
+    return make_float2(M, S);
+}
+
 // EMU8: exponential pairs (of every 8 pairs = 2 chunks) evaluated on the FMA pipe in the
 // seeded pass (D <= 4); balances MUFU against the FMA pipe (measured by SK_LSE_EMU8 sweeps)
 template <int D, int R, bool SEEDED, int EMU8 = 2>
@@ -505,11 +523,23 @@ __global__ void __launch_bounds__(kMT) k_merge(MergePass Mp, Side S, Side Qs) {
                 continue;
             }
             float M = -INFINITY;
-            for (int s = 0; s < Mp.nsplit; ++s) M = fmaxf(M, Mp.part[(long long)s * S.P + p].x);
             float Ssum = 0.f;
-            for (int s = 0; s < Mp.nsplit; ++s) {
-                const float2 v = Mp.part[(long long)s * S.P + p];
-                if (v.x != -INFINITY) Ssum += v.y * ex2(v.x - M);
+            if (Mp.nsplit <= 16) {   // (all partials in flight at once; the same arithmetic)
+                float2 v[16];
+#pragma unroll
+                for (int s = 0; s < 16; ++s)
+                    v[s] = s < Mp.nsplit ? Mp.part[(long long)s * S.P + p] : make_float2(-INFINITY, 0.f);
+#pragma unroll
+                for (int s = 0; s < 16; ++s) M = fmaxf(M, v[s].x);
+#pragma unroll
+                for (int s = 0; s < 16; ++s)
+                    if (s < Mp.nsplit && v[s].x != -INFINITY) Ssum += v[s].y * ex2(v[s].x - M);
+            } else {
+                for (int s = 0; s < Mp.nsplit; ++s) M = fmaxf(M, Mp.part[(long long)s * S.P + p].x);
+                for (int s = 0; s < Mp.nsplit; ++s) {
+                    const float2 v = Mp.part[(long long)s * S.P + p];
+                    if (v.x != -INFINITY) Ssum += v.y * ex2(v.x - M);
+                }
             }
             merge_point(Mp, S, Qs, p, M, Ssum, check || chk_ad, om, rterms, hold, hnew, e, e2, bad);
         }
@@ -638,7 +668,7 @@ __global__ void __launch_bounds__(256) k_premerge(const float2 *__restrict__ par
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
          t += (long long)gridDim.x * blockDim.x) {
         const long long b = t / P, p = t - b * P;
-        out[t] = premerge_point(part + b * split_q * P + p, split_q, P);
+        out[t] = premerge_point_r(part + b * split_q * P + p, split_q, P);
     }
 }
 
