@@ -161,7 +161,7 @@ sk_status sk_get_solver_options(const sk_ctx *ctx, float *omega, float *decay_in
 /* Diagnostics / tuning of kernel variants (DESIGN.md section 6 measures each): key = value for the
  * following calls on this context.  None changes what is computed beyond fp32 rounding; each
  * selects a kernel variant or a balance of the exponential between MUFU and the FMA pipe:
- *   "tc" 0|1 (1): tcgen05 cross term (K3) for d in [tc_min_d, 64], and for every d <= 64 on large
+ *   "tc" 0|1 (1): tcgen05 cross term (K3) for d in [tc_min_d, 256], and for every d on large
  *       problems (max(n, m) > 16384) while "tc_small_d" is 1; 0 = FFMA kernel K2 everywhere;
  *   "tc_min_d" 1..65 (17), "tc_small_d" 0|1 (1): see "tc";
  *   "fused" 0|1 (1): stored mode's fused single-read sweep K5; 0 = separate row/column passes;
@@ -341,7 +341,7 @@ sk_status sinkhorn_init_gmm(sk_ctx *ctx, int64_t n, int64_t m, int32_t d, const 
  *   f^(0)_i = -eps log (1/ms) sum_j exp((g~_j - c(x_i, z_j))/eps)
  * in one online LSE pass over all of x.  Indices must be distinct and in range.
  * *side as above (n > m: roles swapped).  inner (nullable, host): report of the
- * inner solve.  pot: n (side 0) or m (side 1). */
+ * inner solve.  pot: n (side 0) or m (side 1).  d in [1, 256] (SK_EINVAL beyond). */
 sk_status sinkhorn_init_subsample(sk_ctx *ctx, int64_t n, int64_t m, int32_t d, const float *x,
                                   const float *y, int64_t ns, const int32_t *idx_x, int64_t ms,
                                   const int32_t *idx_y, float eps, float inner_tol,
@@ -360,13 +360,14 @@ sk_status sinkhorn_init_subsample(sk_ctx *ctx, int64_t n, int64_t m, int32_t d, 
  * Kernels: problems with d <= 4 that fit one CTA's shared memory (n, m up to ~4096) run the
  * on-chip solver K13 (one CTA or CTA pair per problem, the whole iteration loop on chip,
  * per-problem convergence); larger problems run the multi-kernel path: online LSE passes with
- * the cost recomputed per pass (the tcgen05 cross term K3 for d in (16, 64] and, on problems
- * with max(n, m) > 16384, for every d; the FFMA cross term K2 otherwise and when the scaled
- * coordinates leave the fp16 range) or, with SK_COST_STORED
+ * the cost recomputed per pass (the tcgen05 cross term K3 for d in (16, 256] — d > 64 in K
+ * chunks of 64 — and, on problems with max(n, m) > 16384, for every d; the FFMA cross term K2
+ * otherwise and when the scaled coordinates leave the fp16 range; for d > 64 K2 keeps the output
+ * point's coordinates in shared memory) or, with SK_COST_STORED
  * (or AUTO for 8 <= d < 32 when 4nm bytes fit), the stored-cost sweep (K4 build, K5 fused
  * single-read sweep).  Blocks until the reports are filled.
- * SK_EINVAL for d < 1 or d > 256 (and the conventions above); SK_EUNSUPPORTED for d in
- * (64, 256] (no kernel of this build) and for n, m >= 2^31. */
+ * SK_EINVAL for d < 1 or d > 256 (and the conventions above); SK_EUNSUPPORTED for
+ * n, m >= 2^31. */
 sk_status sinkhorn_solve(sk_ctx *ctx, int64_t B, int64_t n, int64_t m, int32_t d, const float *x,
                          const float *y, int32_t y_shared, const float *a, const float *b, float eps,
                          float tol, int32_t max_iter, int32_t check_every, sk_cost_mode mode,
@@ -408,7 +409,7 @@ sk_status sinkhorn_solve_sharded_emulated(sk_ctx *ctx, int32_t world, int64_t n,
 /* Diagnostic: out[i][j] = <x_i, y_j> for 128 x d and 128 x d fp32 inputs (row-major;
  * out 128 x 128), computed by the tensor-core path of the LSE pass (K3: 3-product fp16
  * hi/lo split of power-of-two scaled operands, tcgen05.mma kind::f16, fp32 accumulators read
- * back from TMEM and unscaled exactly).  d in [1, 64].  For
+ * back from TMEM and unscaled exactly).  d in [1, 256].  For
  * testing the operand layout and the error compensation.  Blocks. */
 sk_status sk_selftest_tc_dot(sk_ctx *ctx, int32_t d, const float *x, const float *y, float *out);
 

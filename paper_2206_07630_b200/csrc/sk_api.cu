@@ -354,7 +354,7 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
     // the cross term's flops that matter but the FMA pipe it occupies next to the FMA-pipe
     // exponentials (C4, d = 3: 1162 -> 1104 ms); small problems keep K2 below tc_min_d
     const bool large_p = std::max(n_glob, m) > 16384;
-    bool tc = !stored && P.d <= 64 && T.tc != 0 && (P.d >= T.tc_min_d || (large_p && T.tc_small_d));
+    bool tc = !stored && P.d <= 256 && T.tc != 0 && (P.d >= T.tc_min_d || (large_p && T.tc_small_d));
     unsigned *amax = nullptr;
     if (tc) {
         // per-side max |coordinate| (global over the ranks) -> the fold scales; a problem whose
@@ -380,7 +380,7 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
     }
     const int ksteps = (P.d + 15) / 16;
     const int D = (stored || tc) ? 0 : lse_dpad(P.d);
-    if (!stored && !tc && D == 0) return fail(ctx, SK_EUNSUPPORTED, "online path supports d <= 64");
+    if (!stored && !tc && D == 0) return fail(ctx, SK_EUNSUPPORTED, "online path supports d <= 256");
     const int tq = stored ? 256 : (tc ? tc_points_per_tile() : lse_tq(D));
     const long long yt = lse_tiles(m, tq);
     const int pmode = stored ? PACK_STORED : (tc ? PACK_TC : PACK_ONLINE);
@@ -402,8 +402,9 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
     ENSURE(status, DevStatus, B_STATUS, 1);
     char *ximg = nullptr, *yimg = nullptr;
     std::vector<long long> offi(ns + 1, 0);
-    // d <= 16 (one K = 16 step): compact SW32 operand images, a quarter of the K = 64 bytes
-    const int tc_rb = (P.d + 15) / 16 == 1 ? 32 : 128;
+    // d <= 16 (one K = 16 step): compact SW32 operand images, a quarter of the K = 64 bytes;
+    // d > 64: K chunks of 64
+    const int tc_rb = tc_row_bytes(P.d);
     if (tc) {
         for (int i = 0; i < ns; ++i) offi[i + 1] = offi[i] + (long long)tc_image_bytes(slices[i].n, tc_rb);
         cudaError_t e1, e2;
@@ -833,7 +834,6 @@ sk_status validate_common(sk_ctx *ctx, long long n, long long m, int d, float ep
     if (n < 1 || m < 1) return fail(ctx, SK_EINVAL, "n and m must be >= 1 (n=%lld m=%lld)", n, m);
     if (n > (1LL << 31) - 1 || m > (1LL << 31) - 1) return fail(ctx, SK_EUNSUPPORTED, "n, m < 2^31");
     if (d < 1 || d > 256) return fail(ctx, SK_EINVAL, "d must be in [1, 256] (d=%d)", d);
-    if (d > 64) return fail(ctx, SK_EUNSUPPORTED, "this build's kernels support d <= 64 (d=%d)", d);
     if (!(eps > 0.f) || bad_scalar(eps)) return fail(ctx, SK_EINVAL, "eps must be finite and > 0");
     if (!(tol > 0.f) || bad_scalar(tol)) return fail(ctx, SK_EINVAL, "tol must be finite and > 0");
     if (max_iter < 1) return fail(ctx, SK_EINVAL, "max_iter must be >= 1");
@@ -1706,7 +1706,7 @@ sk_status sinkhorn_solve_sharded_emulated(sk_ctx *ctx, int32_t world, int64_t n,
 
 sk_status sk_selftest_tc_dot(sk_ctx *ctx, int32_t d, const float *x, const float *y, float *out) {
     if (!ctx) return SK_EINVAL;
-    if (d < 1 || d > 64 || !x || !y || !out) return fail(ctx, SK_EINVAL, "d in [1, 64], non-NULL arrays");
+    if (d < 1 || d > 256 || !x || !y || !out) return fail(ctx, SK_EINVAL, "d in [1, 256], non-NULL arrays");
     const int ksteps = (d + 15) / 16;
     Stager sg(ctx);
     const float *dx, *dy;
@@ -1714,7 +1714,7 @@ sk_status sk_selftest_tc_dot(sk_ctx *ctx, int32_t d, const float *x, const float
     CK(sg.in_t(x, (size_t)128 * d, &dx));
     CK(sg.in_t(y, (size_t)128 * d, &dy));
     CK(sg.out_t(out, (size_t)128 * 128, &dout));
-    const int rb = ksteps == 1 ? 32 : 128;   // (the solver's layout for this d)
+    const int rb = tc_row_bytes(d);   // (the solver's layout for this d)
     ENSURE(ximg, char, B_XIMG, tc_image_bytes(128, rb));
     ENSURE(yimg, char, B_YIMG, tc_image_bytes(128, rb));
     ENSURE(amax, unsigned, B_TCMAX, 2);

@@ -175,6 +175,12 @@ struct TcPass {
     int rb = 128;               // image row bytes of both sides (32: compact K = 16 images, ksteps == 1)
 };
 size_t tc_image_bytes(long long P, int rb = 128);
+// image row bytes for d: 32 (compact K = 16, d <= 16), 128 (K = 64), 128 KC (KC chunks of K = 64,
+// d in (64, 256])
+inline int tc_row_bytes(int d) {
+    const int ks = (d + 15) / 16;
+    return ks == 1 ? 32 : 128 * ((ks + 3) / 4);
+}
 cudaError_t launch_absmax(const float *pts, long long cnt, unsigned *out, cudaStream_t st);  // out zeroed first
 cudaError_t launch_pack_tc(const float *pts, long long P, int d, const unsigned *amax2, int role, float eps,
                            void *img, cudaStream_t st, int rb = 128);   // role 0: x side, 1: y side

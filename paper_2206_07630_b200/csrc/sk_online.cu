@@ -25,7 +25,9 @@ namespace sk {
 
 constexpr int kLT = 128;      // LSE kernel threads
 constexpr int kStages = 4;    // bulk-copy ring depth
-constexpr int kLseEmu = 1;    // exp2 pairs (of 4 per chunk) on the FMA pipe when D <= 4
+constexpr int kLseEmu = 1;
+constexpr int kWideTQ = 32;   // D > 64: reduction points per tile
+constexpr int kWideStages = 2;    // exp2 pairs (of 4 per chunk) on the FMA pipe when D <= 4
 
 int lse_dpad(int d) {
     if (d <= 4) return d < 1 ? 0 : d;
@@ -33,10 +35,12 @@ int lse_dpad(int d) {
     if (d <= 16) return 16;
     if (d <= 32) return 32;
     if (d <= 64) return 64;
+    if (d <= 128) return 128;
+    if (d <= 256) return 256;
     return 0;
 }
 
-int lse_tq(int D) { return D <= 4 ? 256 : (D <= 16 ? 128 : 64); }
+int lse_tq(int D) { return D <= 4 ? 256 : (D <= 16 ? 128 : (D <= 64 ? 64 : kWideTQ)); }
 
 template <int D> constexpr int kR = D <= 4 ? 4 : (D <= 16 ? 2 : 1);
 
@@ -132,6 +136,72 @@ __device__ __forceinline__ float2 premerge_point_r(const float2 *src, int split_
     return make_float2(M, S);
 }
 
+// K2 item of this CTA: P tile px and Q range [t0, t0 + nt) of split s -> block b, sub-split u.
+// 2D grid (P tiles, splits); with the fused premerge a 1D grid with the sub-split fastest, so
+// that a (P tile, block)'s split_q CTAs run back to back and their partials are merged (and
+// discarded) from L2
+__device__ __forceinline__ void lse_item(const LseArgs &A, int &s, int &px, int &b, int &t0, int &nt) {
+    if (A.xchg) {
+        const int id = blockIdx.x, uu = id % A.split_q, rr = id / A.split_q;
+        px = rr % A.ptiles;
+        s = (rr / A.ptiles) * A.split_q + uu;
+    } else {
+        s = blockIdx.y;
+        px = blockIdx.x;
+    }
+    b = s / A.split_q;
+    const int u = s % A.split_q;
+    const int bt = A.blk_tiles > 0 ? A.blk_tiles : A.Qtiles;
+    const int base = b * bt;
+    const int nt_b = max(0, min(bt, A.Qtiles - base));
+    t0 = base + (int)((long long)nt_b * u / A.split_q);
+    nt = base + (int)((long long)nt_b * (u + 1) / A.split_q) - t0;
+}
+
+// K2 tail: the CTA's split partials, then (fused K6a) the block premerge by the last CTA of
+// each (P tile, block)
+template <int R>
+__device__ __forceinline__ void lse_store(const LseArgs &A, int s, int b, int px, const float (&M)[R],
+                                          const float2 (&Sx)[R]) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int p = px * (kLT * R) + r * kLT + threadIdx.x;
+        if (p < A.P) A.part[(long long)s * A.P + p] = make_float2(M[r], Sx[r].x + Sx[r].y);
+    }
+    if (A.xchg) {
+        // K6a fused: the last of the block's split_q CTAs for this P tile merges their partials in
+        // split order (the premerge arithmetic) while they are still in L2, and writes the block
+        // partial - the exchange payload - directly
+        __shared__ int s_last;
+        __threadfence();
+        __syncthreads();
+        int *c = A.cnt + (long long)b * A.ptiles + px;
+        if (threadIdx.x == 0) s_last = atomicAdd(c, 1) == A.split_q - 1;
+        __syncthreads();
+        if (!s_last) return;
+        __threadfence();
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int p = px * (kLT * R) + r * kLT + threadIdx.x;
+            if (p < A.P) A.xchg[(long long)b * A.P + p] = premerge_point(A.part + (long long)b * A.split_q * A.P + p,
+                                                                        A.split_q, A.P);
+        }
+        if (threadIdx.x == 0) *c = 0;   // (ready for the next launch)
+        // the group's sub-split partials are dead: drop their L2 lines without writing them back
+        // (only whole 128-byte lines inside the group's partial rows)
+        // (per sub-split row: the whole 128-byte lines inside [p0, p1) - rows start anywhere)
+        __syncthreads();
+        const int p0 = px * kLT * R, p1 = min(A.P, p0 + kLT * R);
+        for (int uu = 0; uu < A.split_q; ++uu) {
+            const float2 *rowp = A.part + ((long long)b * A.split_q + uu) * A.P;
+            const unsigned long long a0 = (reinterpret_cast<unsigned long long>(rowp + p0) + 127ull) & ~127ull;
+            const unsigned long long a1 = reinterpret_cast<unsigned long long>(rowp + p1) & ~127ull;
+            for (unsigned long long a = a0 + 128ull * threadIdx.x; a < a1; a += 128ull * kLT)
+                asm volatile("discard.global.L2 [%0], 128;" ::"l"(a) : "memory");
+        }
+    }
+}
+
 // EMU8: exponential pairs (of every 8 pairs = 2 chunks) evaluated on the FMA pipe in the
 // seeded pass (D <= 4); balances MUFU against the FMA pipe (measured by SK_LSE_EMU8 sweeps)
 template <int D, int R, bool SEEDED, int EMU8 = 2>
@@ -143,25 +213,8 @@ __global__ void __launch_bounds__(kLT) k_lse(LseArgs A) {
     if (A.stop && *(volatile const int *)A.stop) return;
     if (A.only_if && !*(volatile const int *)A.only_if) return;
 
-    // ---- this CTA's P tile px and Q range: split s -> block b, sub-split u.  2D grid (P tiles,
-    // splits); with the fused premerge a 1D grid with the sub-split fastest, so that a (P tile,
-    // block)'s split_q CTAs run back to back and their partials are merged (and discarded) from L2
-    int s, px;
-    if (A.xchg) {
-        const int id = blockIdx.x, uu = id % A.split_q, rr = id / A.split_q;
-        px = rr % A.ptiles;
-        s = (rr / A.ptiles) * A.split_q + uu;
-    } else {
-        s = blockIdx.y;
-        px = blockIdx.x;
-    }
-    const int b = s / A.split_q, u = s % A.split_q;
-    const int bt = A.blk_tiles > 0 ? A.blk_tiles : A.Qtiles;
-    const int base = b * bt;
-    const int nt_b = max(0, min(bt, A.Qtiles - base));
-    const int t0 = base + (int)((long long)nt_b * u / A.split_q);
-    const int t1 = base + (int)((long long)nt_b * (u + 1) / A.split_q);
-    const int nt = t1 - t0;
+    int s, px, b, t0, nt;
+    lse_item(A, s, px, b, t0, nt);
 
     // ---- output points: R per thread
     float2 pd[R][D];
@@ -212,43 +265,108 @@ __global__ void __launch_bounds__(kLT) k_lse(LseArgs A) {
         }
     }
 
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-        const int p = px * (kLT * R) + r * kLT + threadIdx.x;
-        if (p < A.P) A.part[(long long)s * A.P + p] = make_float2(M[r], Sx[r].x + Sx[r].y);
+    lse_store<R>(A, s, b, px, M, Sx);
+}
+
+// D in {128, 256} (d in (64, 256]): the output point's scaled coordinates do not fit registers;
+// they are staged once in shared memory, one column per thread ([D][kLT]: conflict-free), and each
+// 32-point reduction tile is reduced with 32 running t's per thread (broadcast float4 loads of the
+// tile's coordinates).  Always unseeded (exact running max per tile); the partials and the fused
+// premerge are K2's.  Large problems with d > 64 run on the tensor cores (K3); this kernel serves
+// small problems and the subsample initializer's extension pass.
+template <int D>
+__global__ void __launch_bounds__(kLT) k_lse_wide(LseArgs A) {
+    constexpr int TQ = kWideTQ, TF = (D + 1) * TQ;
+    extern __shared__ __align__(128) float ring[];   // [kWideStages][TF], then sP [D][kLT]
+    float *sP = ring + kWideStages * TF;
+    __shared__ __align__(8) uint64_t full[kWideStages];
+    if (A.stop && *(volatile const int *)A.stop) return;
+    if (A.only_if && !*(volatile const int *)A.only_if) return;
+    int s, px, b, t0, nt;
+    lse_item(A, s, px, b, t0, nt);
+    {
+        const int p = px * kLT + threadIdx.x;
+        const int pt = p / A.Ptq, po = p % A.Ptq;
+        const float *tile = A.Ppack + (long long)pt * (D + 1) * A.Ptq;
+        for (int k = 0; k < D; ++k) sP[k * kLT + threadIdx.x] = p < A.P ? tile[k * A.Ptq + po] * A.tk : 0.f;
     }
-    if (A.xchg) {
-        // K6a fused: the last of the block's split_q CTAs for this P tile merges their partials in
-        // split order (the premerge arithmetic) while they are still in L2, and writes the block
-        // partial - the exchange payload - directly
-        __shared__ int s_last;
-        __threadfence();
-        __syncthreads();
-        int *c = A.cnt + (long long)b * A.ptiles + px;
-        if (threadIdx.x == 0) s_last = atomicAdd(c, 1) == A.split_q - 1;
-        __syncthreads();
-        if (!s_last) return;
-        __threadfence();
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-            const int p = px * (kLT * R) + r * kLT + threadIdx.x;
-            if (p < A.P) A.xchg[(long long)b * A.P + p] = premerge_point(A.part + (long long)b * A.split_q * A.P + p,
-                                                                        A.split_q, A.P);
-        }
-        if (threadIdx.x == 0) *c = 0;   // (ready for the next launch)
-        // the group's sub-split partials are dead: drop their L2 lines without writing them back
-        // (only whole 128-byte lines inside the group's partial rows)
-        // (per sub-split row: the whole 128-byte lines inside [p0, p1) - rows start anywhere)
-        __syncthreads();
-        const int p0 = px * kLT * R, p1 = min(A.P, p0 + kLT * R);
-        for (int uu = 0; uu < A.split_q; ++uu) {
-            const float2 *rowp = A.part + ((long long)b * A.split_q + uu) * A.P;
-            const unsigned long long a0 = (reinterpret_cast<unsigned long long>(rowp + p0) + 127ull) & ~127ull;
-            const unsigned long long a1 = reinterpret_cast<unsigned long long>(rowp + p1) & ~127ull;
-            for (unsigned long long a = a0 + 128ull * threadIdx.x; a < a1; a += 128ull * kLT)
-                asm volatile("discard.global.L2 [%0], 128;" ::"l"(a) : "memory");
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kWideStages; ++i) mbar_init(&full[i], 1);
+        fence_mbar_init();
+        for (int i = 0; i < kWideStages && i < nt; ++i) {
+            mbar_expect_tx(&full[i], TF * 4);
+            bulk_g2s(ring + i * TF, A.Qpack + (long long)(t0 + i) * TF, TF * 4, &full[i]);
         }
     }
+    __syncthreads();
+    float M[1] = {-INFINITY};
+    float2 Sx[1] = {make_float2(0.f, 0.f)};
+    for (int i = 0; i < nt; ++i) {
+        const int st = i % kWideStages;
+        mbar_wait(&full[st], (i / kWideStages) & 1);
+        const float *qt = ring + st * TF;
+        float t[TQ];
+#pragma unroll
+        for (int j = 0; j < TQ; j += 4) {
+            const float4 w = *reinterpret_cast<const float4 *>(qt + D * TQ + j);
+            t[j] = w.x; t[j + 1] = w.y; t[j + 2] = w.z; t[j + 3] = w.w;
+        }
+#pragma unroll 4
+        for (int k = 0; k < D; ++k) {
+            const float pv = sP[k * kLT + threadIdx.x];
+#pragma unroll
+            for (int j = 0; j < TQ; j += 4) {
+                const float4 c = *reinterpret_cast<const float4 *>(qt + k * TQ + j);
+                t[j] = fmaf(pv, c.x, t[j]); t[j + 1] = fmaf(pv, c.y, t[j + 1]);
+                t[j + 2] = fmaf(pv, c.z, t[j + 2]); t[j + 3] = fmaf(pv, c.w, t[j + 3]);
+            }
+        }
+        float cm = t[0];
+#pragma unroll
+        for (int j = 1; j < TQ; ++j) cm = fmaxf(cm, t[j]);
+        if (cm > M[0]) { Sx[0].x *= ex2(M[0] - cm); M[0] = cm; }
+        if (M[0] != -INFINITY) {   // (a tile's first point is always real: M is finite here)
+#pragma unroll
+            for (int j = 0; j < TQ; j += 2) {
+                Sx[0].x += ex2(t[j] - M[0]);
+                Sx[0].y += ex2(t[j + 1] - M[0]);
+            }
+        }
+        __syncthreads();  // everyone is done with stage st
+        if (threadIdx.x == 0 && i + kWideStages < nt) {
+            fence_proxy_async();
+            mbar_expect_tx(&full[st], TF * 4);
+            bulk_g2s(ring + st * TF, A.Qpack + (long long)(t0 + i + kWideStages) * TF, TF * 4, &full[st]);
+        }
+    }
+    lse_store<1>(A, s, b, px, M, Sx);
+}
+
+template <int D>
+constexpr size_t wide_smem() { return (size_t)(kWideStages * (D + 1) * kWideTQ + D * kLT) * sizeof(float); }
+
+template <int D>
+static cudaError_t launch_lse_wide(const LsePass &L, cudaStream_t st) {
+    const size_t smem = wide_smem<D>();
+    cudaError_t e = cudaFuncSetAttribute(k_lse_wide<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    LseArgs A;
+    A.Ppack = L.Pside->pack; A.P = L.Pside->P; A.Ptq = L.Pside->tq;
+    A.Qpack = L.Qside->pack; A.Qtiles = (int)lse_tiles(L.Qside->P, L.Qside->tq);
+    A.blk_tiles = L.blk_tiles; A.split_q = L.split_q;
+    A.part = L.part;
+    A.tk = 2.f * kLog2e / L.eps;
+    A.stop = L.stop;
+    A.only_if = L.only_if;
+    A.seed = nullptr;
+    A.margin = 0.f;
+    A.xchg = L.xchg;
+    A.cnt = L.cnt;
+    A.ptiles = (A.P + kLT - 1) / kLT;
+    dim3 grid(A.ptiles, L.nblk * L.split_q);
+    if (A.xchg) grid = dim3((unsigned)A.ptiles * L.nblk * L.split_q, 1);
+    k_lse_wide<D><<<grid, kLT, smem, st>>>(A);
+    return cudaGetLastError();
 }
 
 template <int D, int R>
@@ -301,6 +419,8 @@ cudaError_t launch_lse(const LsePass &L, cudaStream_t st) {
         case 16: return launch_lse_d<16>(L, st);
         case 32: return launch_lse_d<32>(L, st);
         case 64: return launch_lse_d<64>(L, st);
+        case 128: return launch_lse_wide<128>(L, st);
+        case 256: return launch_lse_wide<256>(L, st);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -312,6 +432,15 @@ static int occ_d() {
     cudaFuncSetAttribute(k_lse<D, R, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int n = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_lse<D, R, false>, kLT, smem) != cudaSuccess) n = 1;
+    return n > 0 ? n : 1;
+}
+
+template <int D>
+static int occ_wide() {
+    const size_t smem = wide_smem<D>();
+    cudaFuncSetAttribute(k_lse_wide<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_lse_wide<D>, kLT, smem) != cudaSuccess) n = 1;
     return n > 0 ? n : 1;
 }
 
@@ -333,6 +462,8 @@ int lse_occupancy_ctas(int D, int R) {
         case 16: return occ_d<16>();
         case 32: return occ_d<32>();
         case 64: return occ_d<64>();
+        case 128: return occ_wide<128>();
+        case 256: return occ_wide<256>();
         default: return 1;
     }
 }
@@ -366,8 +497,6 @@ __device__ void exact_lse_point(const Side &S, const Side &Q, int p, float eps, 
     }
     const long long pt = p / S.tq, po = p % S.tq;
     const float *ptile = S.pack + pt * (long long)(S.D + 1) * S.tq;
-    float pc[64];
-    for (int k = 0; k < S.D; ++k) pc[k] = ptile[k * S.tq + po] * tk;
     M = -INFINITY;
     Ssum = 0.f;
     const long long qt = lse_tiles(Q.P, Q.tq);
@@ -376,7 +505,7 @@ __device__ void exact_lse_point(const Side &S, const Side &Q, int p, float eps, 
         for (int o = 0; o < Q.tq; ++o) {
             float v = tile[Q.D * Q.tq + o];
             if (v == -INFINITY) continue;
-            for (int k = 0; k < Q.D; ++k) v = fmaf(pc[k], tile[k * Q.tq + o], v);
+            for (int k = 0; k < Q.D; ++k) v = fmaf(ptile[k * S.tq + po] * tk, tile[k * Q.tq + o], v);
             if (v > M) { Ssum = Ssum * ex2(M - v); M = v; }
             Ssum += ex2(v - M);
         }

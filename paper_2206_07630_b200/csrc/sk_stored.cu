@@ -57,6 +57,49 @@ __global__ void __launch_bounds__(256) k_build_cost(const float *__restrict__ x,
     }
 }
 
+// d in (64, 256]: the same per-lane fmaf chains (k in order), y taken 32 coordinates at a time
+// into registers and the 32 rows' sums kept across the chunks
+template <int DP>
+__global__ void __launch_bounds__(256) k_build_cost_wide(const float *__restrict__ x, const float *__restrict__ y,
+                                                         long long n, long long m, int d, float *C) {
+    __shared__ __align__(16) float sx[DP][32];
+    const long long i0 = (long long)blockIdx.y * 32;
+    const long long j = (long long)blockIdx.x * 256 + threadIdx.x;
+    for (int t = threadIdx.x; t < 32 * DP; t += 256) {
+        const int r = t / DP, k = t % DP;
+        const long long i = i0 + r;
+        sx[k][r] = (i < n && k < d) ? x[i * d + k] : 0.f;
+    }
+    __syncthreads();
+    if (j >= m) return;
+    float2 acc[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) acc[r] = make_float2(0.f, 0.f);
+    for (int kc = 0; kc < DP; kc += 32) {
+        float yj[32];
+#pragma unroll
+        for (int kk = 0; kk < 32; ++kk) yj[kk] = kc + kk < d ? y[j * d + kc + kk] : 0.f;
+#pragma unroll
+        for (int r = 0; r < 32; r += 4) {
+#pragma unroll
+            for (int kk = 0; kk < 32; ++kk) {
+                const float4 xv = *reinterpret_cast<const float4 *>(&sx[kc + kk][r]);
+                const float2 yy = make_float2(yj[kk], yj[kk]);
+                const float2 t01 = sub2(make_float2(xv.x, xv.y), yy), t23 = sub2(make_float2(xv.z, xv.w), yy);
+                acc[r / 2] = fma2(t01, t01, acc[r / 2]);
+                acc[r / 2 + 1] = fma2(t23, t23, acc[r / 2 + 1]);
+            }
+        }
+    }
+    const int rows = (int)min(32LL, n - i0);
+#pragma unroll
+    for (int r = 0; r < 32; r += 2) {
+        float *out = C + (i0 + r) * m + j;
+        if (r < rows) out[0] = acc[r / 2].x;
+        if (r + 1 < rows) out[m] = acc[r / 2].y;
+    }
+}
+
 cudaError_t launch_build_cost(const float *x, const float *y, long long n, long long m, int d, float *C,
                               cudaStream_t st) {
     dim3 grid((unsigned)((m + 255) / 256), (unsigned)((n + 31) / 32));
@@ -65,6 +108,8 @@ cudaError_t launch_build_cost(const float *x, const float *y, long long n, long 
     else if (d <= 16) k_build_cost<16><<<grid, 256, 0, st>>>(x, y, n, m, d, C);
     else if (d <= 32) k_build_cost<32><<<grid, 256, 0, st>>>(x, y, n, m, d, C);
     else if (d <= 64) k_build_cost<64><<<grid, 256, 0, st>>>(x, y, n, m, d, C);
+    else if (d <= 128) k_build_cost_wide<128><<<grid, 256, 0, st>>>(x, y, n, m, d, C);
+    else if (d <= 256) k_build_cost_wide<256><<<grid, 256, 0, st>>>(x, y, n, m, d, C);
     else return cudaErrorInvalidValue;
     return cudaGetLastError();
 }

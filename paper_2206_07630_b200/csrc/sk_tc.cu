@@ -64,8 +64,9 @@ __host__ __device__ inline int tc_fold_s(float ax, float ay, float tk) {
 // role 0 (x side): alpha = 2^s; role 1 (y side): alpha = tk 2^-s.
 __global__ void k_pack_tc(const float *__restrict__ pts, long long P, long long P2, int d, const unsigned *amax2,
                           int role, float tk, unsigned char *img, int rb) {
-    // rb = 128: SW128 (8 chunks of 8 halves per row); rb = 32: SW32 (2 chunks, d <= 16), the
-    // 16-byte chunk index XORed with bit 2 of the row, 8-row groups of 256 bytes
+    // rb = 128: SW128 (8 chunks of 8 halves per row); rb = 128 KC (d in (64, 256]): KC such SW128
+    // K chunks per tile, each chunk's hi and lo images adjacent; rb = 32: SW32 (2 chunks,
+    // d <= 16), the 16-byte chunk index XORed with bit 2 of the row, 8-row groups of 256 bytes
     const int cpr = rb / 16;
     const long long total = P2 * cpr;
     const int s = tc_fold_s(__uint_as_float(amax2[0]), __uint_as_float(amax2[1]), tk);
@@ -84,12 +85,19 @@ __global__ void k_pack_tc(const float *__restrict__ pts, long long P, long long 
             hi[j] = __float2half_rn(x);
             lo[j] = __float2half_rn(x - __half2float(hi[j]));
         }
-        const long long off = rb == 128 ? (long long)(r >> 3) * 1024 + (r & 7) * 128 + ((c ^ (r & 7)) << 4)
-                                        : (long long)(r >> 3) * 256 + (r & 7) * 32 + ((c ^ ((r >> 2) & 1)) << 4);
-        const long long ib = 128LL * rb;   // bytes of one image tile
+        const long long ib = 128LL * rb;   // bytes of one image tile (all K chunks)
         unsigned char *base = img + t * 2LL * ib;
-        *reinterpret_cast<uint4 *>(base + off) = *reinterpret_cast<const uint4 *>(hi);
-        *reinterpret_cast<uint4 *>(base + ib + off) = *reinterpret_cast<const uint4 *>(lo);
+        if (rb >= 128) {
+            // K chunk kc = c / 8 (64 halves) at kc * 32 KB: [hi 16 KB | lo 16 KB] (rb = 128: one chunk)
+            const int kc = c >> 3, cc = c & 7;
+            const long long off = (long long)kc * 2 * kTcImgBytes + (r >> 3) * 1024 + (r & 7) * 128 + ((cc ^ (r & 7)) << 4);
+            *reinterpret_cast<uint4 *>(base + off) = *reinterpret_cast<const uint4 *>(hi);
+            *reinterpret_cast<uint4 *>(base + kTcImgBytes + off) = *reinterpret_cast<const uint4 *>(lo);
+        } else {
+            const long long off = (long long)(r >> 3) * 256 + (r & 7) * 32 + ((c ^ ((r >> 2) & 1)) << 4);
+            *reinterpret_cast<uint4 *>(base + off) = *reinterpret_cast<const uint4 *>(hi);
+            *reinterpret_cast<uint4 *>(base + ib + off) = *reinterpret_cast<const uint4 *>(lo);
+        }
     }
 }
 
@@ -282,23 +290,31 @@ __device__ __forceinline__ void umma2_commit_mc(uint64_t *bar) {
 }
 
 
-template <int EMU, int NE, bool SEEDED, int G, int PL = 0, bool DBG = false, int RB = 128>
+// KC > 1 (d in (64, 256], RB = 128): the images hold KC K chunks of 64 halves; the A half of an
+// item is staged whole (KC chunks, one buffer when KC > 2), the B half of a tile arrives chunk by
+// chunk through a two-stage ring of K3's 36 KB stages (the extra columns with the last chunk), and
+// the tile's accumulator takes 3 x 4 MMAs per chunk plus the extra-column MMA after the last.
+template <int EMU, int NE, bool SEEDED, int G, int PL = 0, bool DBG = false, int RB = 128, int KC = 1>
 __global__ void __launch_bounds__(64 + 32 * NE, 1) k_lse_tc2(TcArgs A) {
     constexpr int NQ = NE / 4;                       // epilogue warps per TMEM lane quadrant
     // G tile groups: group k's warps take the tiles g with g % G == k (accumulator buffer k when
     // G = 2), so one group's TMEM loads overlap the other group's exponentials
     constexpr int NQG = NQ / G;                      // warps per lane quadrant and group
     constexpr int CW = kT2N / NQG;                   // accumulator columns per epilogue warp
-    constexpr int ABUF = 2;
+    static_assert(KC == 1 || RB == 128, "K chunks use the SW128 images");
+    constexpr int ABUF = KC > 2 ? 1 : 2;
+    constexpr int NBS = KC > 1 ? 2 : kT2Stages;       // B ring depth
+    constexpr int RBX = RB * KC;                      // image row bytes (the side's offsets)
     // [hi | lo | extra] of 128 points: 36 KB (RB = 128), 12 KB (RB = 32: the compact d <= 16 images)
     constexpr int IMG = 128 * RB;
-    constexpr int STAGE = 2 * IMG + kTcExtBytes;
+    constexpr int STAGE = 2 * IMG + kTcExtBytes;      // B stage: one K chunk (+ the extra columns)
+    constexpr int ASTAGE = 2 * KC * IMG + kTcExtBytes;
     extern __shared__ __align__(1024) unsigned char smraw[];
     unsigned char *sm = smraw + ((1024 - (smem_u32(smraw) & 1023)) & 1023);
-    unsigned char *sA = sm;                           // ABUF x STAGE: this CTA's 128 A rows
-    unsigned char *sB = sm + ABUF * STAGE;            // kT2Stages x STAGE: this CTA's 128 B rows
-    float2 *xch = reinterpret_cast<float2 *>(sB + kT2Stages * STAGE);   // (NQ - 1) x 128 partials
-    __shared__ __align__(8) uint64_t full[kT2Stages], pfull[kT2Stages], empty[kT2Stages], tfull[2], tempty[2],
+    unsigned char *sA = sm;                           // ABUF x ASTAGE: this CTA's 128 A rows
+    unsigned char *sB = sm + ABUF * ASTAGE;           // NBS x STAGE: this CTA's 128 B rows
+    float2 *xch = reinterpret_cast<float2 *>(sB + NBS * STAGE);   // (NQ - 1) x 128 partials
+    __shared__ __align__(8) uint64_t full[NBS], pfull[NBS], empty[NBS], tfull[2], tempty[2],
         afull[ABUF], pafull[ABUF], aempty[ABUF];
     __shared__ uint32_t tmem_base;
 
@@ -321,7 +337,7 @@ __global__ void __launch_bounds__(64 + 32 * NE, 1) k_lse_tc2(TcArgs A) {
     const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
 
     if (threadIdx.x == 0) {
-        for (int i = 0; i < kT2Stages; ++i) {
+        for (int i = 0; i < NBS; ++i) {
             mbar_init(&full[i], 1); mbar_init(&pfull[i], 1); mbar_init(&empty[i], 1);
         }
         for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 2 * NE / G); }
@@ -340,7 +356,7 @@ __global__ void __launch_bounds__(64 + 32 * NE, 1) k_lse_tc2(TcArgs A) {
 
     if (warp == 0) {
         if (lane == 0) {
-            const unsigned char *aext = A.Aimg + tc_ea_off(A.P, RB), *bext = A.Bimg + tc_eb_off(A.Q, RB);
+            const unsigned char *aext = A.Aimg + tc_ea_off(A.P, RBX), *bext = A.Bimg + tc_eb_off(A.Q, RBX);
             int g = 0, c = 0;
             for (int it = cid; it < items; it += ncl, ++c) {
                 const int s = it / A.ptiles, pt = it % A.ptiles;
@@ -349,20 +365,23 @@ __global__ void __launch_bounds__(64 + 32 * NE, 1) k_lse_tc2(TcArgs A) {
                 const int ab = c % ABUF;
                 const long long at = 2LL * pt + rank;   // this CTA's 128-point A tile
                 if (c >= ABUF) mbar_wait_sleep(&aempty[ab], ((c / ABUF) - 1) & 1);
-                mbar_expect_tx(&afull[ab], STAGE);
-                bulk_g2s(sA + ab * STAGE, A.Aimg + at * 2 * IMG, 2 * IMG, &afull[ab]);
-                bulk_g2s(sA + ab * STAGE + 2 * IMG, aext + at * kTcExtBytes, kTcExtBytes, &afull[ab]);
-                for (int i = 0; i < nt; ++i, ++g) {
-                    const int st = g % kT2Stages;
+                mbar_expect_tx(&afull[ab], ASTAGE);
+                bulk_g2s(sA + ab * ASTAGE, A.Aimg + at * 2 * KC * IMG, 2 * KC * IMG, &afull[ab]);
+                bulk_g2s(sA + ab * ASTAGE + 2 * KC * IMG, aext + at * kTcExtBytes, kTcExtBytes, &afull[ab]);
+                for (int i = 0; i < nt; ++i) {
                     const long long bt = 2LL * (t0 + i) + rank;
-                    if (g >= kT2Stages) mbar_wait_sleep(&empty[st], ((g / kT2Stages) - 1) & 1);
-                    if (A.mma_only == 2 && g >= kT2Stages) {   // K14 probe: MMA rate without the B stream
-                        mbar_arrive(&full[st]);
-                        continue;
+                    for (int kc = 0; kc < KC; ++kc, ++g) {
+                        const int st = g % NBS;
+                        const bool last = kc == KC - 1;
+                        if (g >= NBS) mbar_wait_sleep(&empty[st], ((g / NBS) - 1) & 1);
+                        if (A.mma_only == 2 && g >= NBS) {   // K14 probe: MMA rate without the B stream
+                            mbar_arrive(&full[st]);
+                            continue;
+                        }
+                        mbar_expect_tx(&full[st], 2 * IMG + (last ? kTcExtBytes : 0));
+                        bulk_g2s(sB + st * STAGE, A.Bimg + (bt * KC + kc) * 2 * IMG, 2 * IMG, &full[st]);
+                        if (last) bulk_g2s(sB + st * STAGE + 2 * IMG, bext + bt * kTcExtBytes, kTcExtBytes, &full[st]);
                     }
-                    mbar_expect_tx(&full[st], STAGE);
-                    bulk_g2s(sB + st * STAGE, A.Bimg + bt * 2 * IMG, 2 * IMG, &full[st]);
-                    bulk_g2s(sB + st * STAGE + 2 * IMG, bext + bt * kTcExtBytes, kTcExtBytes, &full[st]);
                 }
             }
         }
@@ -377,9 +396,9 @@ __global__ void __launch_bounds__(64 + 32 * NE, 1) k_lse_tc2(TcArgs A) {
                 const int ab = c % ABUF;
                 mbar_wait(&afull[ab], (c / ABUF) & 1);
                 mbar_arrive_cluster(r_pafull + 8 * ab);
-                for (int i = 0; i < nt; ++i, ++g) {
-                    const int st = g % kT2Stages;
-                    mbar_wait(&full[st], (g / kT2Stages) & 1);
+                for (int i = 0; i < nt * KC; ++i, ++g) {
+                    const int st = g % NBS;
+                    mbar_wait(&full[st], (g / NBS) & 1);
                     mbar_arrive_cluster(r_pfull + 8 * st);
                 }
             }
@@ -387,43 +406,77 @@ __global__ void __launch_bounds__(64 + 32 * NE, 1) k_lse_tc2(TcArgs A) {
             // MMA issuer: the whole warp runs the (warp-uniform) loop, so the descriptors live in
             // uniform registers; one elected lane issues each tcgen05 instruction
             const int ks = (A.mma_only == 3 || A.mma_only == 5) ? 0 : A.ksteps;
-            int g = 0, c = 0;
+            int g = 0, c = 0, gc = 0;   // tiles, items, B chunks
             for (int it = cid; it < items; it += ncl, ++c) {
                 int t0, nt;
                 range(it / A.ptiles, t0, nt);
                 const int ab = c % ABUF;
                 mbar_wait(&afull[ab], (c / ABUF) & 1);
                 mbar_wait(&pafull[ab], (c / ABUF) & 1);
-                const uint32_t a_hi = smem_u32(sA + ab * STAGE);
-                const uint64_t da_hi = RB == 128 ? umma_desc_sw128(a_hi) : umma_desc_sw32(a_hi),
-                               da_lo = RB == 128 ? umma_desc_sw128(a_hi + IMG) : umma_desc_sw32(a_hi + IMG),
-                               da_ex = umma_desc_sw32(a_hi + 2 * IMG);
-                for (int i = 0; i < nt; ++i, ++g) {
-                    const int st = g % kT2Stages, b = g & 1;
-                    mbar_wait(&full[st], (g / kT2Stages) & 1);
-                    mbar_wait(&pfull[st], (g / kT2Stages) & 1);
-                    if (g >= 2) mbar_wait_sleep(&tempty[b], ((g >> 1) - 1) & 1);
-                    tc_fence_after();
-                    const uint32_t b_hi = smem_u32(sB + st * STAGE);
-                    const uint64_t db_hi = RB == 128 ? umma_desc_sw128(b_hi) : umma_desc_sw32(b_hi),
-                                   db_lo = RB == 128 ? umma_desc_sw128(b_hi + IMG) : umma_desc_sw32(b_hi + IMG),
-                                   db_ex = umma_desc_sw32(b_hi + 2 * IMG);
-                    const uint32_t d = tbase + (uint32_t)(b * kT2N);
-                    if (elect_one()) {
-                        // smallest magnitudes first (each MMA rounds at the running accumulator's
-                        // scale): the lo cross products, then hi . hi, then the extra columns
-                        // w_q - sh_p, which bring the sum down to t - sh_p in one rounding.
-                        // K = 16 halves = 32 bytes per step = +2 in the descriptor's address field.
-                        for (int k = 0; k < ks; ++k) {
-                            umma2_f16(d, da_lo + 2 * k, db_hi + 2 * k, k > 0);
-                            umma2_f16(d, da_hi + 2 * k, db_lo + 2 * k, 1);
+                if constexpr (KC == 1) {
+                    const uint32_t a_hi = smem_u32(sA + ab * STAGE);
+                    const uint64_t da_hi = RB == 128 ? umma_desc_sw128(a_hi) : umma_desc_sw32(a_hi),
+                                   da_lo = RB == 128 ? umma_desc_sw128(a_hi + IMG) : umma_desc_sw32(a_hi + IMG),
+                                   da_ex = umma_desc_sw32(a_hi + 2 * IMG);
+                    for (int i = 0; i < nt; ++i, ++g) {
+                        const int st = g % kT2Stages, b = g & 1;
+                        mbar_wait(&full[st], (g / kT2Stages) & 1);
+                        mbar_wait(&pfull[st], (g / kT2Stages) & 1);
+                        if (g >= 2) mbar_wait_sleep(&tempty[b], ((g >> 1) - 1) & 1);
+                        tc_fence_after();
+                        const uint32_t b_hi = smem_u32(sB + st * STAGE);
+                        const uint64_t db_hi = RB == 128 ? umma_desc_sw128(b_hi) : umma_desc_sw32(b_hi),
+                                       db_lo = RB == 128 ? umma_desc_sw128(b_hi + IMG) : umma_desc_sw32(b_hi + IMG),
+                                       db_ex = umma_desc_sw32(b_hi + 2 * IMG);
+                        const uint32_t d = tbase + (uint32_t)(b * kT2N);
+                        if (elect_one()) {
+                            // smallest magnitudes first (each MMA rounds at the running accumulator's
+                            // scale): the lo cross products, then hi . hi, then the extra columns
+                            // w_q - sh_p, which bring the sum down to t - sh_p in one rounding.
+                            // K = 16 halves = 32 bytes per step = +2 in the descriptor's address field.
+                            for (int k = 0; k < ks; ++k) {
+                                umma2_f16(d, da_lo + 2 * k, db_hi + 2 * k, k > 0);
+                                umma2_f16(d, da_hi + 2 * k, db_lo + 2 * k, 1);
+                            }
+                            for (int k = 0; k < ks; ++k) umma2_f16(d, da_hi + 2 * k, db_hi + 2 * k, 1);
+                            if (A.mma_only != 3 && A.mma_only != 5) umma2_f16(d, da_ex, db_ex, 1);
+                            umma2_commit_mc(&empty[st]);   // both CTAs' B slots free once these MMAs retire
+                            umma2_commit_mc(&tfull[b]);    // accumulator b ready in both CTAs
                         }
-                        for (int k = 0; k < ks; ++k) umma2_f16(d, da_hi + 2 * k, db_hi + 2 * k, 1);
-                        if (A.mma_only != 3 && A.mma_only != 5) umma2_f16(d, da_ex, db_ex, 1);
-                        umma2_commit_mc(&empty[st]);   // both CTAs' B slots free once these MMAs retire
-                        umma2_commit_mc(&tfull[b]);    // accumulator b ready in both CTAs
+                        __syncwarp();
                     }
-                    __syncwarp();
+                } else {
+                    // K chunks: per tile, KC ring stages; the lo cross products then hi . hi of
+                    // each chunk (the chunk's 4 K steps), the extra columns after the last chunk
+                    const uint32_t a0 = smem_u32(sA + ab * ASTAGE);
+                    const uint64_t da_ex = umma_desc_sw32(a0 + 2 * KC * IMG);
+                    for (int i = 0; i < nt; ++i, ++g) {
+                        const int b = g & 1;
+                        const uint32_t d = tbase + (uint32_t)(b * kT2N);
+                        for (int kc = 0; kc < KC; ++kc, ++gc) {
+                            const int st = gc % NBS;
+                            mbar_wait(&full[st], (gc / NBS) & 1);
+                            mbar_wait(&pfull[st], (gc / NBS) & 1);
+                            if (kc == 0 && g >= 2) mbar_wait_sleep(&tempty[b], ((g >> 1) - 1) & 1);
+                            tc_fence_after();
+                            const uint32_t a_hi = a0 + kc * 2 * IMG, b_hi = smem_u32(sB + st * STAGE);
+                            const uint64_t da_hi = umma_desc_sw128(a_hi), da_lo = umma_desc_sw128(a_hi + IMG),
+                                           db_hi = umma_desc_sw128(b_hi), db_lo = umma_desc_sw128(b_hi + IMG),
+                                           db_ex = umma_desc_sw32(b_hi + 2 * IMG);
+                            const int kn = min(4, ks - 4 * kc);
+                            if (elect_one()) {
+                                for (int k = 0; k < kn; ++k) {
+                                    umma2_f16(d, da_lo + 2 * k, db_hi + 2 * k, kc > 0 || k > 0);
+                                    umma2_f16(d, da_hi + 2 * k, db_lo + 2 * k, 1);
+                                }
+                                for (int k = 0; k < kn; ++k) umma2_f16(d, da_hi + 2 * k, db_hi + 2 * k, 1);
+                                if (kc == KC - 1 && A.mma_only != 3 && A.mma_only != 5) umma2_f16(d, da_ex, db_ex, 1);
+                                umma2_commit_mc(&empty[st]);
+                                if (kc == KC - 1) umma2_commit_mc(&tfull[b]);
+                            }
+                            __syncwarp();
+                        }
+                    }
                 }
                 if (elect_one()) umma2_commit_mc(&aempty[ab]);   // both CTAs' A buffers free
                 __syncwarp();
@@ -437,7 +490,7 @@ __global__ void __launch_bounds__(64 + 32 * NE, 1) k_lse_tc2(TcArgs A) {
         const int q4 = warp & 3, h = (warp - 2) >> 2;
         const int grp = h / NQG, hc = h % NQG;   // tile group, column group
         const int row = q4 * 32 + lane;
-        const float *sh = reinterpret_cast<const float *>(A.Aimg + tc_sh_off(A.P, RB));
+        const float *sh = reinterpret_cast<const float *>(A.Aimg + tc_sh_off(A.P, RBX));
         const uint32_t r_tempty = leader ? smem_u32(&tempty[0]) : mapa_u32(smem_u32(&tempty[0]), 0);
         const bool full_epi = A.mma_only == 0 || A.mma_only == 3 || A.mma_only == 5;   // 3, 5: probes without MMAs
         int g = 0;
@@ -673,7 +726,7 @@ cudaError_t launch_absmax(const float *pts, long long cnt, unsigned *out, cudaSt
 
 cudaError_t launch_pack_tc(const float *pts, long long P, int d, const unsigned *amax2, int role, float eps,
                            void *img, cudaStream_t st, int rb) {
-    if (!(rb == 128 || (rb == 32 && d <= 16))) return cudaErrorInvalidValue;
+    if (!((rb % 128 == 0 && rb >= 128 && rb <= 512 && d <= rb / 2) || (rb == 32 && d <= 16))) return cudaErrorInvalidValue;
     const long long P2 = tc_tiles(P) * kTcM;   // zero images up to the pair tile
     const long long total = P2 * (rb / 16);
     long long b = (total + 255) / 256;
@@ -701,12 +754,15 @@ bool tc_fold_ok(float amax_x, float amax_y, float eps) {
     return mx <= 8192.0 && my <= 8192.0;
 }
 
-template <int EMU, int NE, bool SEEDED, int G, int PL = 0, bool DBG = false, int RB = 128>
+template <int EMU, int NE, bool SEEDED, int G, int PL = 0, bool DBG = false, int RB = 128, int KC = 1>
 static cudaError_t launch_tc2(const TcArgs &A, int items, cudaStream_t st) {
-    constexpr int ABUF = 2;
+    constexpr int ABUF = KC > 2 ? 1 : 2;
+    constexpr int NBS = KC > 1 ? 2 : kT2Stages;
     constexpr size_t STAGE = 2 * (size_t)(128 * RB) + kTcExtBytes;
-    const size_t smem = 1024 + ABUF * STAGE + kT2Stages * STAGE + (NE / 4 - 1) * kTcM * 8;
-    cudaError_t e = cudaFuncSetAttribute(k_lse_tc2<EMU, NE, SEEDED, G, PL, DBG, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    constexpr size_t ASTAGE = 2 * (size_t)KC * (128 * RB) + kTcExtBytes;
+    const size_t smem = 1024 + ABUF * ASTAGE + NBS * STAGE + (NE / 4 - 1) * kTcM * 8;
+    static_assert(1024 + ABUF * ASTAGE + NBS * STAGE + (NE / 4 - 1) * kTcM * 8 <= 227 * 1024, "K3 shared memory");
+    cudaError_t e = cudaFuncSetAttribute(k_lse_tc2<EMU, NE, SEEDED, G, PL, DBG, RB, KC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int nsm = 148, dev = 0;
     cudaGetDevice(&dev);
@@ -722,7 +778,7 @@ static cudaError_t launch_tc2(const TcArgs &A, int items, cudaStream_t st) {
     at[0].val.clusterDim.x = 2; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, k_lse_tc2<EMU, NE, SEEDED, G, PL, DBG, RB>, A);
+    return cudaLaunchKernelEx(&cfg, k_lse_tc2<EMU, NE, SEEDED, G, PL, DBG, RB, KC>, A);
 }
 
 template <int EMU>
@@ -748,7 +804,7 @@ cudaError_t launch_lse_tc(const TcPass &L, cudaStream_t st) {
     A.part = L.part; A.tk = 2.f * kLog2e / L.eps; A.stop = L.stop; A.only_if = L.only_if; A.debug_acc = L.debug_acc;
     A.mma_only = L.mma_only;
     A.cyc = L.cyc;
-    if (A.ksteps < 1 || A.ksteps > 4) return cudaErrorInvalidValue;
+    if (A.ksteps < 1 || A.ksteps > 16) return cudaErrorInvalidValue;
     A.ptiles = (L.P + kT2N - 1) / kT2N;
     A.nblk = L.nblk;
     A.Qtiles = (int)((L.Q + kT2N - 1) / kT2N);
@@ -768,6 +824,21 @@ cudaError_t launch_lse_tc(const TcPass &L, cudaStream_t st) {
         SK_TC32(2)
 #undef SK_TC32
     }
+    if (L.rb > 128) {
+        // d in (64, 256]: KC = rb / 128 K chunks; the MMAs grow with d while the epilogue does not,
+        // so every exponential stays on MUFU (EMU 0) and the tile groups alternate (G = 2)
+        const int kc = L.rb / 128;
+        if (L.rb % 128 || kc > 4 || (A.ksteps + 3) / 4 != kc) return cudaErrorInvalidValue;
+#define SK_TCK(KC) \
+        return L.debug_acc ? launch_tc2<0, 16, false, 2, 0, true, 128, KC>(A, items, st) \
+                           : (seeded ? launch_tc2<0, 16, true, 2, 0, false, 128, KC>(A, items, st) \
+                                     : launch_tc2<0, 16, false, 2, 0, false, 128, KC>(A, items, st));
+        if (kc == 2) { SK_TCK(2) }
+        if (kc == 3) { SK_TCK(3) }
+        SK_TCK(4)
+#undef SK_TCK
+    }
+    if (A.ksteps > 4) return cudaErrorInvalidValue;
     if (L.debug_acc) return launch_tc2<2, 16, false, 2, 0, true>(A, items, st);   // (selftest)
     switch (emu) {
         case 0: return launch_tc2_ne<0>(A, items, seeded, ne, L.pipe, st);
