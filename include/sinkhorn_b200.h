@@ -312,8 +312,8 @@ sk_status sinkhorn_init_nw1d(sk_ctx *ctx, int64_t B, int64_t n, int64_t m, const
  * potential f*(x) = ||x||^2 - (x - m_mu)^T A (x - m_mu) - 2 m_nu^T x
  * (Gaussian-Potential appendix, R-4), evaluated on the smaller side
  * (n <= m: x, *side = 0; else y with roles swapped, *side = 1, R-15).
- * a, b nullable (uniform).  pot: n (side 0) or m (side 1).  d <= 64 (SK_EUNSUPPORTED for d in
- * (64, 256], SK_EINVAL beyond). */
+ * a, b nullable (uniform).  pot: n (side 0) or m (side 1).  d in [1, 256] (SK_EINVAL beyond);
+ * d > 64 runs the square roots over the whole grid (one cooperative launch, matrices in L2). */
 sk_status sinkhorn_init_gaussian(sk_ctx *ctx, int64_t n, int64_t m, int32_t d, const float *x,
                                  const float *a, const float *y, const float *b, float ridge_rel,
                                  float *pot, int32_t *side /* host */);

@@ -1265,7 +1265,6 @@ sk_status sinkhorn_init_gaussian(sk_ctx *ctx, int64_t n, int64_t m, int32_t d, c
     if (!ctx) return SK_EINVAL;
     if (n < 1 || m < 1 || d < 1 || d > 256 || !x || !y || !pot || !side)
         return fail(ctx, SK_EINVAL, "bad arguments (d in [1,256])");
-    if (d > 64) return fail(ctx, SK_EUNSUPPORTED, "the Gaussian initializer supports d <= 64");
     if (!(ridge_rel >= 0.f) || bad_scalar(ridge_rel)) return fail(ctx, SK_EINVAL, "ridge_rel >= 0");
     const bool swap = n > m;  // potential on the smaller side
     Stager sg(ctx);
@@ -1278,15 +1277,17 @@ sk_status sinkhorn_init_gaussian(sk_ctx *ctx, int64_t n, int64_t m, int32_t d, c
     CK(sg.out_t(pot, (size_t)(swap ? m : n), &dpot));
     CK(check_arrays(ctx, {{dx, n * d}, {dy, m * d}}, {{da, n}, {db, m}}, "sinkhorn_init_gaussian"));
     if (swap) { std::swap(dx, dy); std::swap(da, db); std::swap(n, m); }
-    const long long nbmax = 296;
-    ENSURE(gw, double, B_GAUSS, 2 * 64 + 3 * 64 * 64);
+    const long long nbmax = moments_blocks(d);
+    const long long D = std::max(d, 64), wide = d > 64 ? (long long)gauss_wide_work_doubles(d) : 0;
+    ENSURE(gw, double, B_GAUSS, 2 * D + 3 * D * D + wide);
     ENSURE(scr, double, B_GAUSS2, nbmax * d * d + 64);
-    double *mmu = gw, *mnu = gw + 64, *Smu = gw + 128, *Snu = Smu + 64 * 64, *A = Snu + 64 * 64;
+    double *mmu = gw, *mnu = gw + D, *Smu = gw + 2 * D, *Snu = Smu + D * D, *A = Snu + D * D;
+    double *wk = d > 64 ? A + D * D : nullptr;
     ENSURE(flag, int, B_FLAG, 4);
     CU(cudaMemsetAsync(flag, 0, sizeof(int), ctx->stream));
     CU(launch_moments(dx, da, n, d, mmu, Smu, scr, nbmax * d * d, ctx->stream));
     CU(launch_moments(dy, db, m, d, mnu, Snu, scr, nbmax * d * d, ctx->stream));
-    CU(launch_gauss_A(mmu, Smu, mnu, Snu, d, ridge_rel, A, flag, ctx->stream));
+    CU(launch_gauss_A(mmu, Smu, mnu, Snu, d, ridge_rel, A, flag, ctx->stream, wk));
     CU(launch_gauss_potential(dx, n, d, mmu, mnu, A, dpot, ctx->stream));
     ctx->cnt.kernel_launches += 10;
     CK(sg.flush());

@@ -13,6 +13,10 @@
 //   f~ from the K x K entropic problem at the same eps (R-13), fp64, one CTA;
 //   f^(0)(x) = sum_k f~_k p_k(x),  p_k = alpha_k N(x; m_k, S_k) / sum_l (...)  (Eq. 7),
 //            log-domain with Cholesky factors, fp64.
+#include <cooperative_groups.h>
+
+#include <algorithm>
+
 #include "sk_internal.h"
 #include "sk_common.cuh"
 
@@ -100,9 +104,78 @@ __global__ void __launch_bounds__(256) k_reduce_cols(const double *in, int nb, i
     }
 }
 
+// d in (64, 256]: the covariance partials per (64 x 64 output tile, row block): the tile's 64
+// weighted centred columns and 64 centred columns of a 32-row chunk staged in shared memory;
+// thread (br, bc) of 16 x 16 owns entries (i0 + br + 16 i, j0 + bc + 16 j), i, j < 4, each summed
+// over the block's rows in order (as the d <= 64 kernel).
+__global__ void __launch_bounds__(kGT) k_cov_partials_wide(const float *__restrict__ x, const float *__restrict__ w,
+                                                           long long n, int d, const double *__restrict__ mean,
+                                                           double *out) {
+    constexpr int CH = 32;   // rows per chunk (64 columns per side: 33 KB of static shared memory)
+    __shared__ double xa[CH][65], xb[CH][65], ws[CH];
+    const int nt = (d + 63) / 64;
+    const int i0 = (blockIdx.x / nt) * 64, j0 = (blockIdx.x % nt) * 64;
+    const long long per = (n + gridDim.y - 1) / gridDim.y;
+    const long long lo = blockIdx.y * per, hi = min(n, lo + per);
+    const int br = threadIdx.x >> 4, bc = threadIdx.x & 15;
+    double acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+    for (long long c0 = lo; c0 < hi; c0 += CH) {
+        const int cnt = (int)min((long long)CH, hi - c0);
+        __syncthreads();
+        for (int t = threadIdx.x; t < cnt * 64; t += kGT) {
+            const int r = t / 64, k = t % 64;
+            const long long row = (c0 + r) * d;
+            xa[r][k] = i0 + k < d ? (double)x[row + i0 + k] - mean[i0 + k] : 0.0;
+            xb[r][k] = j0 + k < d ? (double)x[row + j0 + k] - mean[j0 + k] : 0.0;
+        }
+        for (int r = threadIdx.x; r < cnt; r += kGT) ws[r] = w ? (double)w[c0 + r] : 1.0 / n;
+        __syncthreads();
+        for (int r = 0; r < cnt; ++r) {
+            const double wr = ws[r];
+            double a[4], b[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) a[i] = wr * xa[r][br + 16 * i];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) b[j] = xb[r][bc + 16 * j];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+        }
+    }
+    double *o = out + (long long)blockIdx.y * d * d;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int k = i0 + br + 16 * i, l = j0 + bc + 16 * j;
+            if (k < d && l < d) o[k * d + l] = acc[i][j];
+        }
+}
+
+long long moments_blocks(int d) { return d <= 64 ? 296 : std::max(1, 592 / (((d + 63) / 64) * ((d + 63) / 64))); }
+
 cudaError_t launch_moments(const float *x, const float *w, long long n, int d, double *mean,
                            double *cov, double *scratch, long long scratch_doubles, cudaStream_t st) {
-    if (d > 64) return cudaErrorInvalidValue;
+    if (d > 256) return cudaErrorInvalidValue;
+    if (d > 64) {
+        long long nb = std::min((n + 63) / 64, moments_blocks(d));
+        if (nb * d * d > scratch_doubles) nb = scratch_doubles / ((long long)d * d);
+        if (nb < 1) return cudaErrorInvalidValue;
+        const size_t smem = (64 * (size_t)d + 64) * sizeof(double);
+        cudaError_t e = cudaFuncSetAttribute(k_moment_partials<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        k_moment_partials<1><<<(int)nb, kGT, smem, st>>>(x, w, n, d, nullptr, scratch);   // (pass 1: d <= 256 threads)
+        k_reduce_cols<<<(d + 31) / 32, 256, 0, st>>>(scratch, (int)nb, d, mean);
+        const int nt = (d + 63) / 64;
+        k_cov_partials_wide<<<dim3((unsigned)(nt * nt), (unsigned)nb), kGT, 0, st>>>(x, w, n, d, mean, scratch);
+        k_reduce_cols<<<(d * d + 31) / 32, 256, 0, st>>>(scratch, (int)nb, d * d, cov);
+        return cudaGetLastError();
+    }
     long long nb = (n + 63) / 64;   // one 64-point chunk per CTA up to 296 CTAs (a fixed partition of n)
     if (nb > 296) nb = 296;
     if (nb * d * d > scratch_doubles) nb = scratch_doubles / (d * d);
@@ -258,10 +331,174 @@ __global__ void __launch_bounds__(kGT) k_gauss_A(double *cov_mu, double *cov_nu,
     if (threadIdx.x == 0) *ns_fail = (r1 > 1e-6 || r2 > 1e-6 || !isfinite(r1) || !isfinite(r2));
 }
 
+// ---- d in (64, 256]: the same algorithm over the whole grid (one cooperative launch); the d x d
+// fp64 matrices live in global memory (L2-resident: 6 x 512 KB at d = 256), read with ld.global.cg
+// (written by other CTAs between grid barriers); products in 32 x 32 output tiles, one per CTA
+// in turn, each entry summed over k in order; norms as fixed-order sums of the CTAs' partials.
+namespace cgw {
+namespace cg = cooperative_groups;
+constexpr int kT = 32;
+
+__device__ double grid_sum(double v, double *red, double *gpart, cg::grid_group &grid) {
+    const double b = block_sum_any(v, red);
+    if (threadIdx.x == 0) gpart[blockIdx.x] = b;
+    grid.sync();
+    double t = 0.0;
+    for (unsigned k = 0; k < gridDim.x; ++k) t += __ldcg(gpart + k);
+    grid.sync();   // (gpart is reused by the next sum)
+    return t;
+}
+
+// C = A B (d x d); C must not alias A or B
+__device__ void mm(const double *A, const double *B, double *C, int d, cg::grid_group &grid) {
+    __shared__ double sa[kT][kT + 1], sb[kT][kT + 1];
+    const int nt = (d + kT - 1) / kT;
+    const int ty = threadIdx.x >> 4, tx = threadIdx.x & 15;
+    for (int t = blockIdx.x; t < nt * nt; t += gridDim.x) {
+        const int i0 = (t / nt) * kT, j0 = (t % nt) * kT;
+        double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+        for (int k0 = 0; k0 < d; k0 += kT) {
+            __syncthreads();
+            for (int e = threadIdx.x; e < kT * kT; e += blockDim.x) {
+                const int r = e / kT, c = e % kT;
+                sa[r][c] = (i0 + r < d && k0 + c < d) ? __ldcg(A + (long long)(i0 + r) * d + k0 + c) : 0.0;
+                sb[r][c] = (k0 + r < d && j0 + c < d) ? __ldcg(B + (long long)(k0 + r) * d + j0 + c) : 0.0;
+            }
+            __syncthreads();
+#pragma unroll 8
+            for (int kk = 0; kk < kT; ++kk) {
+                const double a0 = sa[ty][kk], a1 = sa[ty + 16][kk], b0 = sb[kk][tx], b1 = sb[kk][tx + 16];
+                acc[0][0] = fma(a0, b0, acc[0][0]);
+                acc[0][1] = fma(a0, b1, acc[0][1]);
+                acc[1][0] = fma(a1, b0, acc[1][0]);
+                acc[1][1] = fma(a1, b1, acc[1][1]);
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const int r = i0 + ty + 16 * i, c = j0 + tx + 16 * j;
+                if (r < d && c < d) C[(long long)r * d + c] = acc[i][j];
+            }
+    }
+    grid.sync();
+}
+
+__device__ void copy(const double *S, double *D, int d, cg::grid_group &grid) {
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < (long long)d * d;
+         e += (long long)gridDim.x * blockDim.x)
+        D[e] = __ldcg(S + e);
+    grid.sync();
+}
+
+__device__ void symmetrize(double *A, int d, cg::grid_group &grid) {
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < (long long)d * d;
+         e += (long long)gridDim.x * blockDim.x) {
+        const int i = (int)(e / d), j = (int)(e % d);
+        if (i < j) {
+            const double v = 0.5 * (__ldcg(A + (long long)i * d + j) + __ldcg(A + (long long)j * d + i));
+            A[(long long)i * d + j] = v;
+            A[(long long)j * d + i] = v;
+        }
+    }
+    grid.sync();
+}
+
+// coupled Newton-Schulz as ns_sqrt above (same iteration, stop rule and budget)
+__device__ double ns_sqrt(const double *M, double *Y, double *Z, double *T, double *U, int d, double *red,
+                          double *gpart, cg::grid_group &grid) {
+    const long long dd = (long long)d * d, g0 = blockIdx.x * (long long)blockDim.x + threadIdx.x,
+                    gs = (long long)gridDim.x * blockDim.x;
+    double fr = 0.0;
+    for (long long e = g0; e < dd; e += gs) { const double v = __ldcg(M + e); fr += v * v; }
+    const double nrm = sqrt(grid_sum(fr, red, gpart, grid));
+    for (long long e = g0; e < dd; e += gs) {
+        Y[e] = __ldcg(M + e) / nrm;
+        Z[e] = (e / d == e % d) ? 1.0 : 0.0;
+    }
+    grid.sync();
+    double res = INFINITY, prev = INFINITY;
+    for (int it = 0; it < 100; ++it) {
+        mm(Z, Y, T, d, grid);  // T = Z Y
+        double r = 0.0;
+        for (long long e = g0; e < dd; e += gs) {
+            const double t = __ldcg(T + e);
+            const double v = t - ((e / d == e % d) ? 1.0 : 0.0);
+            r += v * v;
+            T[e] = ((e / d == e % d) ? 1.5 : 0.0) - 0.5 * t;
+        }
+        res = sqrt(grid_sum(r, red, gpart, grid));   // (its barriers publish T)
+        if (res < 1e-13 * d || (res < 1e-7 && res > 0.5 * prev)) break;
+        prev = res;
+        mm(Y, T, U, d, grid);  // U = Y T
+        copy(U, Y, d, grid);
+        mm(T, Z, U, d, grid);  // U = T Z
+        copy(U, Z, d, grid);
+    }
+    const double sq = sqrt(nrm);
+    for (long long e = g0; e < dd; e += gs) {
+        Y[e] = __ldcg(Y + e) * sq;
+        Z[e] = __ldcg(Z + e) / sq;
+    }
+    grid.sync();
+    return res;
+}
+}  // namespace cgw
+
+// work: 4 d^2 + gridDim.x doubles
+__global__ void __launch_bounds__(kGT) k_gauss_A_wide(double *cov_mu, double *cov_nu, int d, float ridge_rel,
+                                                       double *Aout, int *ns_fail, double *work) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    __shared__ double red[kGT / 32];
+    const long long dd = (long long)d * d, g0 = blockIdx.x * (long long)blockDim.x + threadIdx.x,
+                    gs = (long long)gridDim.x * blockDim.x;
+    double *Smu = cov_mu, *Snu = cov_nu, *R = work, *Ri = work + dd, *T = work + 2 * dd, *U = work + 3 * dd,
+           *gpart = work + 4 * dd;
+    double tr_mu = 0.0, tr_nu = 0.0;
+    for (int k = 0; k < d; ++k) { tr_mu += cov_mu[(long long)k * d + k]; tr_nu += cov_nu[(long long)k * d + k]; }
+    grid.sync();   // (every thread has read the diagonals before they change)
+    for (long long e = g0; e < dd; e += gs)
+        if (e / d == e % d) {
+            Smu[e] += ridge_rel * tr_mu / d;
+            Snu[e] += ridge_rel * tr_nu / d;
+        }
+    grid.sync();
+    cgw::symmetrize(Smu, d, grid);
+    cgw::symmetrize(Snu, d, grid);
+    const double r1 = cgw::ns_sqrt(Smu, R, Ri, T, U, d, red, gpart, grid);   // R = S_mu^{1/2}, Ri = S_mu^{-1/2}
+    cgw::mm(R, Snu, T, d, grid);                                               // T = R S_nu
+    double *Mm = Smu;
+    cgw::mm(T, R, Mm, d, grid);                                                // Mm = R S_nu R
+    cgw::symmetrize(Mm, d, grid);
+    double *Q = Snu, *Qi = R;
+    const double r2 = cgw::ns_sqrt(Mm, Q, Qi, T, U, d, red, gpart, grid);    // Q = Mm^{1/2}
+    cgw::mm(Ri, Q, T, d, grid);
+    cgw::mm(T, Ri, U, d, grid);                                                // A = Ri Q Ri
+    cgw::symmetrize(U, d, grid);
+    for (long long e = g0; e < dd; e += gs) Aout[e] = __ldcg(U + e);
+    if (blockIdx.x == 0 && threadIdx.x == 0) *ns_fail = (r1 > 1e-6 || r2 > 1e-6 || !isfinite(r1) || !isfinite(r2));
+}
+
+size_t gauss_wide_work_doubles(int d) { return 4 * (size_t)d * d + 256; }
+
 cudaError_t launch_gauss_A(const double *mean_mu, double *cov_mu, const double *mean_nu,
                            double *cov_nu, int d, float ridge_rel, double *A, int *ns_fail,
-                           cudaStream_t st) {
+                           cudaStream_t st, double *work) {
     (void)mean_mu; (void)mean_nu;
+    if (d > 64) {
+        if (!work || d > 256) return cudaErrorInvalidValue;
+        const int nt = (d + cgw::kT - 1) / cgw::kT;
+        int dev = 0, nsm = 148, occ = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gauss_A_wide, kGT, 0);
+        if (e != cudaSuccess) return e;
+        const int G = std::max(1, std::min({nt * nt, nsm * std::max(occ, 1), 256}));
+        void *args[] = {&cov_mu, &cov_nu, &d, &ridge_rel, &A, &ns_fail, &work};
+        return cudaLaunchCooperativeKernel((const void *)k_gauss_A_wide, dim3(G), dim3(kGT), args, 0, st);
+    }
     const size_t smem = 6 * (size_t)d * d * sizeof(double);
     cudaError_t e = cudaFuncSetAttribute(k_gauss_A, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -353,8 +590,67 @@ __global__ void __launch_bounds__(kGT) k_gauss_pot(const float *__restrict__ x, 
     }
 }
 
+// d in (64, 256]: A (d x d fp64, 512 KB at d = 256) stays in global memory / L2; the tile's centred
+// coordinates in shared memory ([64][d + 1]); thread (kq, p) forms the rows k = kq, kq + 4, .. of
+// A c_p (a warp shares kq: A rows are broadcast loads) and its part of c_p^T A c_p; the 4 parts
+// summed in kq order.
+__global__ void __launch_bounds__(kGT) k_gauss_pot_wide(const float *__restrict__ x, long long n, int d,
+                                                         const double *__restrict__ mmu,
+                                                         const double *__restrict__ mnu,
+                                                         const double *__restrict__ A, float *pot) {
+    extern __shared__ double s[];
+    const int d1 = d + 1;
+    double *cs = s;                       // [64][d + 1]
+    double *red = cs + kPotTile * d1;     // [4][64]
+    const int p = threadIdx.x & (kPotTile - 1), kq = threadIdx.x >> 6;
+    const long long tiles = (n + kPotTile - 1) / kPotTile;
+    for (long long tb = blockIdx.x; tb < tiles; tb += gridDim.x) {
+        const long long i0 = tb * kPotTile;
+        const int cnt = (int)min((long long)kPotTile, n - i0);
+        __syncthreads();
+        for (int e = threadIdx.x; e < kPotTile * d; e += blockDim.x) {
+            const int r = e / d, k = e % d;
+            cs[r * d1 + k] = r < cnt ? (double)x[(i0 + r) * d + k] - mmu[k] : 0.0;
+        }
+        __syncthreads();
+        const double *cp = cs + p * d1;
+        double q = 0.0;
+        for (int k = kq; k < d; k += 4) {
+            const double *ar = A + (long long)k * d;
+            double r0 = 0.0, r1 = 0.0;
+            int l = 0;
+            for (; l + 1 < d; l += 2) {
+                r0 = fma(__ldg(ar + l), cp[l], r0);
+                r1 = fma(__ldg(ar + l + 1), cp[l + 1], r1);
+            }
+            if (l < d) r0 = fma(__ldg(ar + l), cp[l], r0);
+            q = fma(cp[k], r0 + r1, q);
+        }
+        red[kq * kPotTile + p] = q;
+        __syncthreads();
+        if (kq == 0 && p < cnt) {
+            const double quad = ((red[p] + red[kPotTile + p]) + red[2 * kPotTile + p]) + red[3 * kPotTile + p];
+            double nx = 0.0, lin = 0.0;
+            for (int k = 0; k < d; ++k) {
+                const double xk = x[(i0 + p) * d + k];
+                nx += xk * xk;
+                lin += mnu[k] * xk;
+            }
+            pot[i0 + p] = (float)(nx - quad - 2.0 * lin);
+        }
+    }
+}
+
 cudaError_t launch_gauss_potential(const float *x, long long n, int d, const double *m_mu,
                                    const double *m_nu, const double *A, float *pot, cudaStream_t st) {
+    if (d > 64) {
+        const size_t smem = sizeof(double) * ((size_t)kPotTile * (d + 1) + 4 * kPotTile);
+        cudaError_t e = cudaFuncSetAttribute(k_gauss_pot_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        const long long tiles = (n + kPotTile - 1) / kPotTile;
+        k_gauss_pot_wide<<<(int)(tiles > 148 ? 148 : tiles), kGT, smem, st>>>(x, n, d, m_mu, m_nu, A, pot);
+        return cudaGetLastError();
+    }
     const size_t smem = gauss_pot_smem(d);
     cudaError_t e = cudaFuncSetAttribute(k_gauss_pot, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

@@ -296,7 +296,9 @@ cudaError_t launch_moments(const float *x, const float *w, long long n, int d, d
                            double *cov, double *scratch, long long scratch_doubles, cudaStream_t st);
 cudaError_t launch_gauss_A(const double *mean_mu, double *cov_mu, const double *mean_nu,
                            double *cov_nu, int d, float ridge_rel, double *A, int *ns_fail,
-                           cudaStream_t st);
+                           cudaStream_t st, double *work = nullptr);   // work: d > 64 (gauss_wide_work_doubles)
+size_t gauss_wide_work_doubles(int d);
+long long moments_blocks(int d);   // row blocks of the moment partials (scratch: moments_blocks(d) * d^2)
 cudaError_t launch_gauss_potential(const float *x, long long n, int d, const double *m_mu,
                                    const double *m_nu, const double *A, float *pot, cudaStream_t st);
 
