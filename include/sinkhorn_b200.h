@@ -326,8 +326,8 @@ sk_status sinkhorn_init_gaussian(sk_ctx *ctx, int64_t n, int64_t m, int32_t d, c
  * DESIGN.md R-29; err = the row term of (f^l, g_sk(f^l))) to inner_tol (max inner_max_iter
  * sweeps; the binding's default 1e-9: ~100 sweeps at C3) -> f~; f^(0)(x) = sum_k f~_k p_k(x),
  * p_k the posterior responsibilities (Eq. 7), on the smaller side (*side as above).
- * Mixture parameters are inputs (sinkhorn_fit_gmm fits them).  K <= 64; d <= 64
- * (SK_EUNSUPPORTED for d in (64, 256], SK_EINVAL beyond). */
+ * Mixture parameters are inputs (sinkhorn_fit_gmm fits them).  K <= 64; d in [1, 256]
+ * (SK_EINVAL beyond); d > 64 keeps each CTA's d x d matrices in global memory (L2). */
 sk_status sinkhorn_init_gmm(sk_ctx *ctx, int64_t n, int64_t m, int32_t d, const float *x,
                             const float *y, int32_t Kx, const float *wx, const float *mux,
                             const float *covx, int32_t Ky, const float *wy, const float *muy,

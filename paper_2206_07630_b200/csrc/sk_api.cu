@@ -1305,7 +1305,6 @@ sk_status sinkhorn_init_gmm(sk_ctx *ctx, int64_t n, int64_t m, int32_t d, const 
     if (!ctx) return SK_EINVAL;
     if (n < 1 || m < 1 || d < 1 || d > 256 || !x || !y || !pot || !side)
         return fail(ctx, SK_EINVAL, "bad arguments (d in [1,256])");
-    if (d > 64) return fail(ctx, SK_EUNSUPPORTED, "the GMM initializer supports d <= 64");
     if (Kx < 1 || Ky < 1 || Kx > 64 || Ky > 64) return fail(ctx, SK_EINVAL, "1 <= K <= 64");
     if (!wx || !mux || !covx || !wy || !muy || !covy) return fail(ctx, SK_EINVAL, "mixture parameters required");
     if (!(eps > 0.f) || bad_scalar(eps) || !(inner_tol > 0.f) || inner_max_iter < 1)

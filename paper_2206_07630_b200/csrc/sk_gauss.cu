@@ -661,8 +661,11 @@ cudaError_t launch_gauss_potential(const float *x, long long n, int d, const dou
 
 // ------------------------------------------------------------------ GMM
 // work layout (doubles): R [Kx][d*d] (S_k^{1/2}), Linv [Kx][d*d], logdet [Kx], C [Kx*Ky], ft [Kx]
+constexpr int kGmmWideSlots = 32;   // d > 64: CTAs (each with 5 d x d scratch matrices) of the NS kernels
+
 size_t gmm_work_doubles(int d, int Kx, int Ky) {
-    return (size_t)2 * Kx * d * d + Kx + (size_t)Kx * Ky + Kx;
+    const size_t base = (size_t)2 * Kx * d * d + Kx + (size_t)Kx * Ky + Kx;
+    return d > 64 ? base + (size_t)kGmmWideSlots * 5 * d * d : base;
 }
 
 __global__ void __launch_bounds__(kGT) k_gmm_sqrt(const float *covx, int d, double *R, int *flags) {
@@ -940,16 +943,226 @@ __global__ void __launch_bounds__(kGT) k_gmm_pot(const float *__restrict__ x, lo
     }
 }
 
+// ---- d in (64, 256]: the same per-component / per-pair steps with each CTA's d x d matrices in
+// global memory (its slot of 5 d^2 doubles, L2-resident) instead of shared memory: block-level
+// products in 32 x 32 tiles (each entry summed over k in order), the same coupled Newton-Schulz
+// iteration and stop rule as ns_sqrt, the Cholesky factorisation with the rows below the pivot
+// updated in parallel.  Scratch written and read by the same CTA between __syncthreads.
+namespace gwide {
+constexpr int kT = 32;
+
+__device__ void mm(const double *A, const double *B, double *C, int d) {
+    __shared__ double sa[kT][kT + 1], sb[kT][kT + 1];
+    const int nt = (d + kT - 1) / kT;
+    const int ty = threadIdx.x >> 4, tx = threadIdx.x & 15;
+    for (int t = 0; t < nt * nt; ++t) {
+        const int i0 = (t / nt) * kT, j0 = (t % nt) * kT;
+        double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+        for (int k0 = 0; k0 < d; k0 += kT) {
+            __syncthreads();
+            for (int e = threadIdx.x; e < kT * kT; e += blockDim.x) {
+                const int r = e / kT, c = e % kT;
+                sa[r][c] = (i0 + r < d && k0 + c < d) ? __ldcg(A + (long long)(i0 + r) * d + k0 + c) : 0.0;
+                sb[r][c] = (k0 + r < d && j0 + c < d) ? __ldcg(B + (long long)(k0 + r) * d + j0 + c) : 0.0;
+            }
+            __syncthreads();
+#pragma unroll 8
+            for (int kk = 0; kk < kT; ++kk) {
+                const double a0 = sa[ty][kk], a1 = sa[ty + 16][kk], b0 = sb[kk][tx], b1 = sb[kk][tx + 16];
+                acc[0][0] = fma(a0, b0, acc[0][0]);
+                acc[0][1] = fma(a0, b1, acc[0][1]);
+                acc[1][0] = fma(a1, b0, acc[1][0]);
+                acc[1][1] = fma(a1, b1, acc[1][1]);
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const int r = i0 + ty + 16 * i, c = j0 + tx + 16 * j;
+                if (r < d && c < d) C[(long long)r * d + c] = acc[i][j];
+            }
+    }
+    __syncthreads();
+}
+
+__device__ void symmetrize(double *A, int d) {
+    for (int e = threadIdx.x; e < d * d; e += blockDim.x) {
+        const int i = e / d, j = e % d;
+        if (i < j) {
+            const double v = 0.5 * (__ldcg(A + i * d + j) + __ldcg(A + j * d + i));
+            A[i * d + j] = v;
+            A[j * d + i] = v;
+        }
+    }
+    __syncthreads();
+}
+
+__device__ double ns_sqrt(const double *M, double *Y, double *Z, double *T, double *U, int d, double *red) {
+    const int dd = d * d;
+    double fr = 0.0;
+    for (int e = threadIdx.x; e < dd; e += blockDim.x) { const double v = __ldcg(M + e); fr += v * v; }
+    const double nrm = sqrt(block_sum_any(fr, red));
+    for (int e = threadIdx.x; e < dd; e += blockDim.x) {
+        Y[e] = __ldcg(M + e) / nrm;
+        Z[e] = (e / d == e % d) ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    double res = INFINITY, prev = INFINITY;
+    for (int it = 0; it < 100; ++it) {
+        mm(Z, Y, T, d);
+        double r = 0.0;
+        for (int e = threadIdx.x; e < dd; e += blockDim.x) {
+            const double t = __ldcg(T + e);
+            const double v = t - ((e / d == e % d) ? 1.0 : 0.0);
+            r += v * v;
+            T[e] = ((e / d == e % d) ? 1.5 : 0.0) - 0.5 * t;
+        }
+        res = sqrt(block_sum_any(r, red));
+        if (res < 1e-13 * d || (res < 1e-7 && res > 0.5 * prev)) break;
+        prev = res;
+        mm(Y, T, U, d);
+        for (int e = threadIdx.x; e < dd; e += blockDim.x) Y[e] = __ldcg(U + e);
+        __syncthreads();
+        mm(T, Z, U, d);
+        for (int e = threadIdx.x; e < dd; e += blockDim.x) Z[e] = __ldcg(U + e);
+        __syncthreads();
+    }
+    const double sq = sqrt(nrm);
+    for (int e = threadIdx.x; e < dd; e += blockDim.x) {
+        Y[e] = __ldcg(Y + e) * sq;
+        Z[e] = __ldcg(Z + e) / sq;
+    }
+    __syncthreads();
+    return res;
+}
+}  // namespace gwide
+
+// R_k = S_k^{1/2} for every x component (CTA slot b takes components b, b + G, ..)
+__global__ void __launch_bounds__(kGT) k_gmm_sqrt_wide(const float *covx, int d, int Kx, double *R, double *slots,
+                                                        int *flags) {
+    __shared__ double red[kGT / 32];
+    const long long dd = (long long)d * d;
+    double *M = slots + blockIdx.x * 5 * dd, *Y = M + dd, *Z = M + 2 * dd, *T = M + 3 * dd, *U = M + 4 * dd;
+    for (int k = blockIdx.x; k < Kx; k += gridDim.x) {
+        for (int e = threadIdx.x; e < dd; e += blockDim.x) M[e] = covx[k * dd + e];
+        __syncthreads();
+        gwide::symmetrize(M, d);
+        const double r = gwide::ns_sqrt(M, Y, Z, T, U, d, red);
+        for (int e = threadIdx.x; e < dd; e += blockDim.x) R[k * dd + e] = __ldcg(Y + e);
+        if (threadIdx.x == 0 && (r > 1e-6 || !isfinite(r))) atomicOr(flags, 1);
+        __syncthreads();
+    }
+}
+
+// C_kl = |m_k - m'_l|^2 + tr(S_k + S'_l - 2 (R_k S'_l R_k)^{1/2}) for every pair (Eq. 6)
+__global__ void __launch_bounds__(kGT) k_gmm_bures_wide(const float *mux, const float *covx, int Kx,
+                                                         const float *muy, const float *covy, int Ky, int d,
+                                                         const double *R, double *C, double *slots, int *flags) {
+    __shared__ double red[kGT / 32];
+    const long long dd = (long long)d * d;
+    double *Sy = slots + blockIdx.x * 5 * dd, *Rk = Sy + dd, *M = Sy + 2 * dd, *T = Sy + 3 * dd, *U = Sy + 4 * dd;
+    for (int pr = blockIdx.x; pr < Kx * Ky; pr += gridDim.x) {
+        const int k = pr / Ky, l = pr % Ky;
+        for (int e = threadIdx.x; e < dd; e += blockDim.x) {
+            Sy[e] = covy[l * dd + e];
+            Rk[e] = __ldcg(R + k * dd + e);
+        }
+        __syncthreads();
+        gwide::symmetrize(Sy, d);
+        gwide::mm(Rk, Sy, T, d);
+        gwide::mm(T, Rk, M, d);
+        gwide::symmetrize(M, d);
+        double *Y = Sy, *Z = Rk;
+        const double r = gwide::ns_sqrt(M, Y, Z, T, U, d, red);
+        if (threadIdx.x == 0) {
+            double tr = 0.0, dm = 0.0;
+            for (int i = 0; i < d; ++i) {
+                tr += (double)covx[k * dd + (long long)i * d + i] + (double)covy[l * dd + (long long)i * d + i]
+                      - 2.0 * __ldcg(Y + (long long)i * d + i);
+                const double t = (double)mux[k * d + i] - (double)muy[l * d + i];
+                dm += t * t;
+            }
+            C[k * Ky + l] = dm + tr;
+            if (r > 1e-6 || !isfinite(r)) atomicOr(flags, 1);
+        }
+        __syncthreads();
+    }
+}
+
+// Cholesky-Banachiewicz per component (one CTA each, L in the slot): row j's pivot by thread 0,
+// the rows below by the whole CTA; then L^{-1} a column per thread and log det L
+__global__ void __launch_bounds__(kGT) k_gmm_chol_wide(const float *covx, int d, int Kx, double *Linv,
+                                                        double *logdet, double *slots, int *flags) {
+    __shared__ double s_ljj;
+    const long long dd = (long long)d * d;
+    double *L = slots + blockIdx.x * 5 * dd;
+    for (int k = blockIdx.x; k < Kx; k += gridDim.x) {
+        double *Li = Linv + k * dd;
+        for (int e = threadIdx.x; e < dd; e += blockDim.x) {
+            const int i = e / d, j = e % d;
+            L[e] = 0.5 * ((double)covx[k * dd + (long long)i * d + j] + (double)covx[k * dd + (long long)j * d + i]);
+        }
+        __syncthreads();
+        int bad = 0;
+        for (int j = 0; j < d; ++j) {
+            if (threadIdx.x == 0) {
+                double s = __ldcg(L + (long long)j * d + j);
+                for (int t = 0; t < j; ++t) { const double v = __ldcg(L + (long long)j * d + t); s -= v * v; }
+                if (!(s > 0.0)) { bad = 1; s = 1e-300; }
+                s_ljj = sqrt(s);
+                L[(long long)j * d + j] = s_ljj;
+            }
+            __syncthreads();
+            const double ljj = s_ljj;
+            for (int i = j + 1 + threadIdx.x; i < d; i += blockDim.x) {
+                double v = __ldcg(L + (long long)i * d + j);
+                for (int t = 0; t < j; ++t) v -= __ldcg(L + (long long)i * d + t) * __ldcg(L + (long long)j * d + t);
+                L[(long long)i * d + j] = v / ljj;
+            }
+            __syncthreads();
+        }
+        for (int e = threadIdx.x; e < dd; e += blockDim.x)
+            if (e % d > e / d) L[e] = 0.0;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double ld = 0.0;
+            for (int j = 0; j < d; ++j) ld += log(__ldcg(L + (long long)j * d + j));
+            logdet[k] = ld;
+            if (bad) atomicOr(flags, 4);
+        }
+        for (int c = threadIdx.x; c < d; c += blockDim.x) {
+            for (int i = 0; i < d; ++i) {
+                double v = (i == c) ? 1.0 : 0.0;
+                for (int t = 0; t < i; ++t) v -= __ldcg(L + (long long)i * d + t) * __ldcg(Li + (long long)t * d + c);
+                Li[(long long)i * d + c] = v / __ldcg(L + (long long)i * d + i);
+            }
+        }
+        __syncthreads();
+    }
+}
+
 cudaError_t launch_gmm_init(const float *x, long long n, int d, int Kx, const float *wx,
                             const float *mux, const float *covx, int Ky, const float *wy,
                             const float *muy, const float *covy, float eps, float inner_tol,
                             int inner_max_iter, float *pot, double *work, int *flags,
                             cudaStream_t st) {
-    if (d > 64 || Kx > 64 || Ky > 64) return cudaErrorInvalidValue;
+    if (d > 256 || Kx > 64 || Ky > 64) return cudaErrorInvalidValue;
     const int dd = d * d;
     double *R = work, *Linv = R + (size_t)Kx * dd, *logdet = Linv + (size_t)Kx * dd,
            *C = logdet + Kx, *ft = C + (size_t)Kx * Ky;
     cudaError_t e;
+    if (d > 64) {
+        double *slots = ft + Kx;
+        const int gs = std::min(Kx, kGmmWideSlots), gp = std::min(Kx * Ky, kGmmWideSlots);
+        k_gmm_sqrt_wide<<<gs, kGT, 0, st>>>(covx, d, Kx, R, slots, flags);
+        k_gmm_bures_wide<<<gp, kGT, 0, st>>>(mux, covx, Kx, muy, covy, Ky, d, R, C, slots, flags);
+        k_gmm_sinkhorn_and<<<1, 32, 0, st>>>(C, Kx, Ky, wx, wy, eps, inner_tol, inner_max_iter, ft, flags);
+        k_gmm_chol_wide<<<gs, kGT, 0, st>>>(covx, d, Kx, Linv, logdet, slots, flags);
+        long long b = (n + kGT - 1) / kGT;
+        k_gmm_pot<<<(int)(b > 148 * 8 ? 148 * 8 : b), kGT, 0, st>>>(x, n, d, Kx, wx, mux, Linv, logdet, ft, pot);
+        return cudaGetLastError();
+    }
     size_t s5 = 5 * (size_t)dd * sizeof(double), s2 = 2 * (size_t)dd * sizeof(double);
     if ((e = cudaFuncSetAttribute(k_gmm_sqrt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s5))) return e;
     if ((e = cudaFuncSetAttribute(k_gmm_bures, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s5))) return e;

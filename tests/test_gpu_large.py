@@ -133,21 +133,21 @@ def nccl_ctx():
     c.close()
 
 
-@pytest.mark.parametrize("accel", ["plain", "omega", "anderson", "adaptive", "stored", "tc"])
+@pytest.mark.parametrize("accel", ["plain", "omega", "anderson", "adaptive", "stored", "tc", "wide"])
 def test_nccl_branch_one_rank_bit_identical(ctx, nccl_ctx, accel):
     """the NCCL branch of the sharded solver (ncclAllGather of the block partials,
     ncclAllReduce of the relaxed row terms / the Anderson Gram dots, ncclAllGather of E's block
     sums) on a 1-rank communicator is bit-identical to the emulated world-1 solve."""
     import paper_2206_07630_b200 as sk
     rng = np.random.default_rng(12)
-    n, m, d = (20000 if accel == "tc" else 5000), 3000, (16 if accel == "stored" else 3)   # tc: large, K3
+    n, m, d = (20000 if accel == "tc" else 5000), 3000, {"stored": 16, "wide": 128}.get(accel, 3)   # tc: large, K3
     x = rng.random((n, d)).astype(np.float32)
     y = rng.random((m, d)).astype(np.float32)
     a = gen.random_weights(n, rng)
     eps = float(np.float32(0.04 * gen.mean_sq_cost(x, y)))
     xd, yd, ad = _cuda(x), _cuda(y), _cuda(a)
     mode = "stored" if accel == "stored" else "online"
-    kw = {"plain": {}, "stored": {}, "tc": {}, "omega": {"omega": 1.2}, "anderson": {"anderson": 5},
+    kw = {"plain": {}, "stored": {}, "tc": {}, "wide": {}, "omega": {"omega": 1.2}, "anderson": {"anderson": 5},
           "adaptive": {"adaptive": 10}}[accel]
     fe, ge, re_ = sk.sinkhorn_solve_sharded_emulated(ctx, 1, xd, yd, eps, a=ad, mode=mode, **kw)
     fn, gn, rn = sk.sinkhorn_solve_sharded(nccl_ctx, n, 0, xd, yd, eps, a_local=ad, mode=mode, **kw)

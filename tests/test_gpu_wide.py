@@ -47,7 +47,7 @@ def _problem(n, m, d, eps_factor, seed=0):
     return x, y, float(np.float32(eps_factor * gen.mean_sq_cost(x, y)))
 
 
-@pytest.mark.parametrize("n,m,d,tc", [(1100, 1300, 128, 1), (700, 515, 96, 1), (900, 1000, 256, 1),
+@pytest.mark.parametrize("n,m,d,tc", [(1100, 1300, 128, 1), (700, 515, 96, 1), (900, 1000, 256, 1), (1000, 777, 65, 1),
                                       (1100, 1300, 128, 0), (600, 700, 200, 0), (513, 515, 256, 0)])
 def test_wide_solve_parity(O, ctx, n, m, d, tc):
     """Solve to tol (count within 2 %, P1) and lockstep potentials / objective (P2): tc = 1 the
@@ -181,8 +181,43 @@ def test_wide_gaussian_init_then_solve(O, ctx):
     assert_pair_close(f.cpu().numpy(), g.cpu().numpy(), lock.f, lock.g, eps)
 
 
+def _mixture(rng, K, d, shift):
+    """K components: weights, means N(shift, 4 I), covariances A A^T / d + 0.2 I (fp32)."""
+    w = rng.uniform(0.5, 1.5, K)
+    mu = shift + 2.0 * rng.standard_normal((K, d))
+    A = rng.standard_normal((K, d, d))
+    cov = np.einsum("kij,klj->kil", A, A) / d + 0.2 * np.eye(d)
+    return {"weights": (w / w.sum()).astype(np.float32), "means": mu.astype(np.float32),
+            "covs": cov.astype(np.float32)}
+
+
+def _sample(rng, g, n):
+    K, d = g["means"].shape
+    w = g["weights"].astype(np.float64)
+    comp = rng.choice(K, n, p=w / w.sum())
+    L = np.linalg.cholesky(g["covs"].astype(np.float64))
+    z = rng.standard_normal((n, d))
+    return (g["means"][comp] + np.einsum("nij,nj->ni", L[comp], z)).astype(np.float32)
+
+
+@pytest.mark.parametrize("d,Kx,Ky,n,m", [(96, 4, 3, 1500, 1700), (256, 3, 4, 1200, 1100)])
+def test_wide_gmm_init(O, ctx, d, Kx, Ky, n, m):
+    """GMM initializer at d > 64 with given mixtures (Eq. 6 Bures costs from per-pair Newton-Schulz
+    square roots, the K x K problem, Cholesky responsibilities) against the oracle; n > m swaps."""
+    import paper_2206_07630_b200 as sk
+    rng = np.random.default_rng(d)
+    gx, gy = _mixture(rng, Kx, d, 0.0), _mixture(rng, Ky, d, 0.5)
+    x, y = _sample(rng, gx, n), _sample(rng, gy, m)
+    eps = float(np.float32(0.05 * gen.mean_sq_cost(x, y)))
+    pot, side = sk.sinkhorn_init_gmm(ctx, _cuda(x), _cuda(y), {k: _cuda(v) for k, v in gx.items()},
+                                     {k: _cuda(v) for k, v in gy.items()}, eps)
+    ref, so = O.init_gmm(x, y, gx, gy, eps)
+    assert side == so
+    assert rel_inf(centred(pot.cpu().numpy()), centred(ref), eps) <= INIT_RTOL
+
+
 def test_wide_error_contract(ctx):
-    """d = 257 is SK_EINVAL; the GMM initializer keeps d <= 64 (SK_EUNSUPPORTED)."""
+    """d = 257 is SK_EINVAL."""
     import paper_2206_07630_b200 as sk
     x = torch.rand(64, 257, device="cuda")
     with pytest.raises(sk.SinkhornError, match="SK_EINVAL"):
