@@ -249,9 +249,11 @@ sk_status sinkhorn_vjp(sk_ctx *ctx, int64_t n, int64_t m, int32_t d, const float
  * deterministic.  Outputs (caller-owned, device or host): weights K, means K x d, covs
  * K x d x d (fp32, the layout sinkhorn_init_gmm takes); loglik (host, nullable) = mean
  * log-likelihood of the returned parameters; n_iter (host, nullable) = EM steps run.
- * SK_EINVAL: bad sizes, K > n, iters < 0, kmeans_iters < 0, tol < 0,
+ * d in [1, 256]: d <= 32 runs the fused E-step (statistics in registers), d > 32 the tiled one
+ * (responsibilities in workspace, the x x^T statistics by 64 x 64 tiles).
+ * SK_EINVAL: bad sizes, d > 256, K > n, iters < 0, kmeans_iters < 0, tol < 0,
  * reg_covar < 0, non-finite x, init_idx not K distinct indices in [0, n); SK_EUNSUPPORTED:
- * d > 32 or K > 64; SK_ENONFINITE: a covariance lost positive definiteness.  Blocks. */
+ * K > 64; SK_ENONFINITE: a covariance lost positive definiteness.  Blocks. */
 sk_status sinkhorn_fit_gmm(sk_ctx *ctx, int64_t n, int32_t d, const float *x, int32_t K,
                            const int32_t *init_idx, int32_t kmeans_iters, int32_t iters, float tol,
                            float reg_covar, float *weights, float *means, float *covs, double *loglik,

@@ -103,7 +103,7 @@ namespace {
 enum BufId {
     B_STAGE0 = 0, B_STAGE_END = 16,   // staging of host arrays
     B_FLAG = 16, B_XPACK, B_XC, B_XNK, B_XPOT, B_YPACK, B_YC, B_YNK, B_YPOT, B_PART, B_BLKE, B_BLKB,
-    B_STATUS, B_COST, B_REP, B_SORT, B_PERM, B_YSORT, B_GAUSS, B_GAUSS2, B_GMM, B_SUBW, B_SUBZ,
+    B_STATUS, B_COST, B_REP, B_SORT, B_PERM, B_YSORT, B_GAUSS, B_GAUSS2, B_GMM, B_EMWIDE, B_SUBW, B_SUBZ,
     B_SUBF, B_SUBG, B_IDX, B_OUT, B_FA, B_QUEUE, B_XIMG, B_YIMG, B_XLSE, B_YLSE, B_TCMAX, B_EMST, B_EMPART, B_EMIDX, B_VJP, B_ANDFR, B_ANDBLK, B_ANDVEC, B_ANDST, B_XCHG, B_PARK, B_XCNT, B_XROW, B_XCNT2, B_GRID, B_NBUF
 };
 
@@ -1064,7 +1064,8 @@ sk_status sinkhorn_fit_gmm(sk_ctx *ctx, int64_t n, int32_t d, const float *x, in
     if (!ctx) return SK_EINVAL;
     if (n < 1 || K < 1 || K > n || !x || !init_idx || !weights || !means || !covs || iters < 0 || kmeans_iters < 0)
         return fail(ctx, SK_EINVAL, "bad arguments (need 1 <= K <= n, iters >= 0, kmeans_iters >= 0, non-NULL arrays)");
-    if (d < 1 || d > 32 || K > 64) return fail(ctx, SK_EUNSUPPORTED, "GMM fitting supports d <= 32, K <= 64");
+    if (d < 1 || d > 256) return fail(ctx, SK_EINVAL, "d must be in [1, 256]");
+    if (K > 64) return fail(ctx, SK_EUNSUPPORTED, "GMM fitting supports K <= 64");
     if (!(reg_covar >= 0.f) || bad_scalar(reg_covar)) return fail(ctx, SK_EINVAL, "reg_covar must be >= 0");
     if (!(tol >= 0.f) || bad_scalar(tol)) return fail(ctx, SK_EINVAL, "tol must be finite and >= 0");
     // the start indices: in range and distinct (checked on the host: K values)
@@ -1089,14 +1090,19 @@ sk_status sinkhorn_fit_gmm(sk_ctx *ctx, int64_t n, int32_t d, const float *x, in
     ENSURE(didx, int, B_EMIDX, K);
     CU(cudaMemcpyAsync(didx, hidx.data(), sizeof(int32_t) * K, cudaMemcpyHostToDevice, ctx->stream));
     ENSURE(st, double, B_EMST, 2 * em_state_doubles(K, d) + 2 * (size_t)d * d + d + 1);
-    ENSURE(part, double, B_EMPART, std::max(em_work_doubles(K, d), (size_t)296 * d * d));
+    const size_t partn = std::max(em_work_doubles(K, d), (size_t)moments_blocks(d) * d * d);
+    ENSURE(part, double, B_EMPART, partn);
+    double *wide = nullptr;
+    if (d > 32) {
+        ENSURE(wd, double, B_EMWIDE, em_wide_doubles(n, K, d));
+        wide = wd;
+    }
     ENSURE(flag, int, B_FLAG, 4);
     double *mean0 = st + 2 * em_state_doubles(K, d), *cov0 = mean0 + d, *ll = cov0 + (size_t)d * d;
     CU(cudaMemsetAsync(flag, 0, 3 * sizeof(int), ctx->stream));
-    CU(launch_moments(dx, nullptr, n, d, mean0, cov0, part, (long long)std::max(em_work_doubles(K, d), (size_t)296 * d * d),
-                      ctx->stream));
+    CU(launch_moments(dx, nullptr, n, d, mean0, cov0, part, (long long)partn, ctx->stream));
     CU(launch_gmm_fit(dx, n, d, K, didx, cov0, kmeans_iters, iters, (double)tol, (double)reg_covar, st, part, flag, dw,
-                      dm, dc, ll, ctx->h_flag, ctx->stream));
+                      dm, dc, ll, ctx->h_flag, ctx->stream, wide));
     ctx->cnt.kernel_launches += 4 + 3 * (kmeans_iters > 0 ? kmeans_iters + 1 : 0) + 4 * (iters + 1) + 3;
     CK(sg.flush());
     double hll = 0.0;

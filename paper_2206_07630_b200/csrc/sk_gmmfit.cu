@@ -17,6 +17,7 @@
 // (n_k, sum r x, sum r x x^T upper triangle) accumulated per thread-owned statistic in fp64 and
 // written as per-CTA partials), k_em_mstep (one CTA: fixed-order reduction of the partials and
 // the parameter update).  Deterministic (fixed partition and reduction order).
+#include <algorithm>
 #include <cfloat>
 
 #include "sk_internal.h"
@@ -45,8 +46,16 @@ __host__ __device__ inline EmState em_state(double *base, int K, int d) {
     s.LL = s.LOGDET + K;
     return s;
 }
+// d > 32 (the wide path): a row partition of at most 48 blocks, fewer when the statistics are many
+// (the partials stay <= 2^24 doubles)
+inline int em_nb(int K, int d) {
+    if (d <= 32) return kEmBlocks;
+    const long long S1 = em_stats(K, d) + 1;
+    return (int)std::max(1LL, std::min(48LL, (1LL << 24) / S1));
+}
 size_t em_state_doubles(int K, int d) { return (size_t)K * (1 + d + 2 * d * d + 1) + 1; }
-size_t em_partial_doubles(int K, int d) { return (size_t)kEmBlocks * (em_stats(K, d) + 1); }   // + S + 1 reduced (em_work_doubles)
+size_t em_partial_doubles(int K, int d) { return (size_t)em_nb(K, d) * (em_stats(K, d) + 1); }   // + S + 1 reduced (em_work_doubles)
+size_t em_wide_doubles(long long n, int K, int d) { return d > 32 ? (size_t)n * K + (size_t)K * d * d : 0; }
 size_t em_work_doubles(int K, int d) { return em_partial_doubles(K, d) + em_stats(K, d) + 1; }
 
 // start: w = 1/K, m_k = x[idx_k], S_k = cov0 + reg I (cov0: biased covariance of x)
@@ -383,6 +392,192 @@ __global__ void k_em_out(const double *base, int K, int d, float *w, float *mu, 
     if (threadIdx.x == 0 && ll_out) *ll_out = *s.LL;
 }
 
+// ---------------------------------------------------------------- d in (32, 256]
+// The same EM with the per-component work split differently: Cholesky one CTA per component (L in
+// a scratch slot, rows below each pivot in parallel); responsibilities one thread per point
+// (log p_ik for all k from L^-1 rows read as broadcasts, normalised in k order, written to
+// resp [n][K]); the statistics of each (row block, component, 64 x 64 tile of x x^T) by one CTA
+// (rows in order, as the fused E-step), n_k and sum r x by the tile-(0, 0) CTA.  Same partials
+// layout, reduction, M-step and stopping rule as d <= 32.
+__global__ void __launch_bounds__(kEmT) k_em_chol_wide(double *base, int K, int d, int *flags, const int *skip,
+                                                        double *Lscr) {
+    __shared__ double s_ljj;
+    if (skip && *(volatile const int *)skip) return;
+    const EmState s = em_state(base, K, d);
+    const long long dd = (long long)d * d;
+    const int k = blockIdx.x;
+    double *L = Lscr + k * dd, *Li = s.LINV + k * dd;
+    for (long long e = threadIdx.x; e < dd; e += blockDim.x) {
+        const int i = (int)(e / d), j = (int)(e % d);
+        L[e] = 0.5 * (s.COV[k * dd + (long long)i * d + j] + s.COV[k * dd + (long long)j * d + i]);
+    }
+    __syncthreads();
+    int bad = 0;
+    for (int j = 0; j < d; ++j) {
+        if (threadIdx.x == 0) {
+            double v = __ldcg(L + (long long)j * d + j);
+            for (int t = 0; t < j; ++t) { const double a = __ldcg(L + (long long)j * d + t); v -= a * a; }
+            if (!(v > 0.0)) { bad = 1; v = 1e-300; }
+            s_ljj = sqrt(v);
+            L[(long long)j * d + j] = s_ljj;
+        }
+        __syncthreads();
+        const double ljj = s_ljj;
+        for (int i = j + 1 + threadIdx.x; i < d; i += blockDim.x) {
+            double v = __ldcg(L + (long long)i * d + j);
+            for (int t = 0; t < j; ++t) v -= __ldcg(L + (long long)i * d + t) * __ldcg(L + (long long)j * d + t);
+            L[(long long)i * d + j] = v / ljj;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        double ld = 0.0;
+        for (int j = 0; j < d; ++j) ld += log(__ldcg(L + (long long)j * d + j));
+        s.LOGDET[k] = ld;
+        if (bad) atomicOr(flags, 1);
+    }
+    for (int c = threadIdx.x; c < d; c += blockDim.x)
+        for (int i = 0; i < d; ++i) {
+            double v = (i == c) ? 1.0 : 0.0;
+            for (int t = c; t < i; ++t) v -= __ldcg(L + (long long)i * d + t) * __ldcg(Li + (long long)t * d + c);
+            Li[(long long)i * d + c] = i < c ? 0.0 : v / __ldcg(L + (long long)i * d + i);
+        }
+}
+
+template <bool HARD>
+__global__ void __launch_bounds__(kEmT) k_em_resp_wide(const float *__restrict__ x, long long n, int d, int K,
+                                                        const double *__restrict__ base, double *resp, double *part,
+                                                        const int *skip) {
+    __shared__ double lls[kEmT];
+    if (skip && *(volatile const int *)skip) return;
+    const EmState s = em_state(const_cast<double *>(base), K, d);
+    const int S = em_stats(K, d);
+    const long long chunk = (n + gridDim.x - 1) / gridDim.x;
+    const long long p0 = blockIdx.x * chunk, p1 = min(n, p0 + chunk);
+    double ll = 0.0;
+    for (long long t0 = p0; t0 < p1; t0 += kEmT) {
+        const long long i = t0 + threadIdx.x;
+        if (i < p1) {
+            const float *xi = x + i * d;
+            double *ri = resp + i * K;
+            double mx = -INFINITY;
+            int kb = 0;
+            for (int k = 0; k < K; ++k) {
+                const double *mk = s.MU + (long long)k * d;
+                double q = 0.0;
+                if (HARD) {
+                    for (int c = 0; c < d; ++c) { const double t = (double)xi[c] - mk[c]; q += t * t; }
+                    q = -q;
+                    if (q > mx) { mx = q; kb = k; }
+                } else {
+                    const double *Lk = s.LINV + (long long)k * d * d;
+                    double qq = 0.0;
+                    for (int r = 0; r < d; ++r) {
+                        double z = 0.0;
+                        for (int c = 0; c <= r; ++c) z = fma(Lk[(long long)r * d + c], (double)xi[c] - mk[c], z);
+                        qq = fma(z, z, qq);
+                    }
+                    q = log(s.W[k]) - s.LOGDET[k] - 0.5 * qq;
+                    mx = fmax(mx, q);
+                }
+                ri[k] = q;
+            }
+            if (HARD) {
+                for (int k = 0; k < K; ++k) ri[k] = k == kb ? 1.0 : 0.0;
+                lls[threadIdx.x] = -mx;   // (inertia)
+            } else {
+                double den = 0.0;
+                for (int k = 0; k < K; ++k) den += exp(ri[k] - mx);
+                const double lse = mx + log(den);
+                for (int k = 0; k < K; ++k) ri[k] = exp(ri[k] - lse);
+                lls[threadIdx.x] = lse;
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const int np = (int)min((long long)kEmT, p1 - t0);
+            for (int p = 0; p < np; ++p) ll += lls[p];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) part[(long long)blockIdx.x * (S + 1) + S] = ll;
+}
+
+__global__ void __launch_bounds__(kEmT) k_em_stats_wide(const float *__restrict__ x, long long n, int d, int K,
+                                                         const double *__restrict__ resp, double *part,
+                                                         const int *skip) {
+    constexpr int CH = 32;
+    __shared__ double xa[CH][65], xb[CH][65], rr[CH];
+    if (skip && *(volatile const int *)skip) return;
+    const int nt = (d + 63) / 64, ti = blockIdx.x / nt, tj = blockIdx.x % nt;
+    if (ti > tj) return;   // (the packed upper triangle only)
+    const int k = blockIdx.y, b = blockIdx.z;
+    const int i0 = ti * 64, j0 = tj * 64;
+    const int T = d * (d + 1) / 2, per = 1 + d + T, S = K * per;
+    const long long chunk = (n + gridDim.z - 1) / gridDim.z;
+    const long long p0 = b * chunk, p1 = min(n, p0 + chunk);
+    const int br = threadIdx.x >> 4, bc = threadIdx.x & 15;
+    double acc[4][4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
+    double nk = 0.0, sx = 0.0;   // tile (0, 0): n_k (thread 0) and sum r x_a (thread a < d)
+    const bool first = blockIdx.x == 0;
+    for (long long c0 = p0; c0 < p1; c0 += CH) {
+        const int cnt = (int)min((long long)CH, p1 - c0);
+        __syncthreads();
+        for (int t = threadIdx.x; t < cnt * 64; t += kEmT) {
+            const int r = t / 64, c = t % 64;
+            const long long row = (c0 + r) * d;
+            xa[r][c] = i0 + c < d ? (double)x[row + i0 + c] : 0.0;
+            xb[r][c] = j0 + c < d ? (double)x[row + j0 + c] : 0.0;
+        }
+        for (int r = threadIdx.x; r < cnt; r += kEmT) rr[r] = resp[(c0 + r) * K + k];
+        __syncthreads();
+        for (int r = 0; r < cnt; ++r) {
+            const double w = rr[r];
+            double a[4], bb[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) a[u] = w * xa[r][br + 16 * u];
+#pragma unroll
+            for (int v = 0; v < 4; ++v) bb[v] = xb[r][bc + 16 * v];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int v = 0; v < 4; ++v) acc[u][v] = fma(a[u], bb[v], acc[u][v]);
+        }
+        if (first) {
+            for (int r = 0; r < cnt; ++r) {
+                const double w = rr[r];
+                if (threadIdx.x == 0) nk += w;
+                if ((int)threadIdx.x < d) sx = fma(w, (double)x[(c0 + r) * d + threadIdx.x], sx);
+            }
+        }
+    }
+    double *out = part + (long long)b * (S + 1) + (long long)k * per;
+    if (first) {
+        if (threadIdx.x == 0) out[0] = nk;
+        if ((int)threadIdx.x < d) out[1 + threadIdx.x] = sx;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            const int a = i0 + br + 16 * u, c = j0 + bc + 16 * v;
+            if (a < d && c < d && c >= a) out[1 + d + a * d - a * (a - 1) / 2 + (c - a)] = acc[u][v];
+        }
+}
+
+template <bool HARD>
+static cudaError_t launch_estep_wide(const float *x, long long n, int d, int K, const double *base, double *part,
+                                     double *resp, const int *skip, cudaStream_t st) {
+    const int nb = em_nb(K, d), nt = (d + 63) / 64;
+    k_em_resp_wide<HARD><<<nb, kEmT, 0, st>>>(x, n, d, K, base, resp, part, skip);
+    k_em_stats_wide<<<dim3((unsigned)(nt * nt), (unsigned)K, (unsigned)nb), kEmT, 0, st>>>(x, n, d, K, resp, part, skip);
+    return cudaGetLastError();
+}
+
 template <int MAXS, int DM, bool HARD, bool OWN>
 static cudaError_t launch_estep_d(const float *x, long long n, int d, int K, const double *base, double *part,
                                   const int *skip, cudaStream_t st) {
@@ -415,18 +610,27 @@ static cudaError_t launch_estep(int maxs, const float *x, long long n, int d, in
 cudaError_t launch_gmm_fit(const float *x, long long n, int d, int K, const int *idx, const double *cov0,
                            int kmeans_iters, int iters, double tol, double reg, double *state, double *part,
                            int *flags, float *w, float *mu, float *cov, double *ll_out, int *h_conv,
-                           cudaStream_t st) {
+                           cudaStream_t st, double *wide) {
     const int S = em_stats(K, d);
     const int maxs = (S + kEmT - 1) / kEmT;
-    if (d < 1 || d > 32 || K < 1 || maxs > 40) return cudaErrorInvalidValue;
+    const bool wd = d > 32;
+    if (d < 1 || d > 256 || K < 1 || K > 64 || (!wd && maxs > 40) || (wd && !wide)) return cudaErrorInvalidValue;
+    const int nb = em_nb(K, d);
+    double *resp = wide, *Lscr = wide ? wide + n * K : nullptr;
+    auto estep = [&](bool hard, const int *sk) {
+        if (wd) return hard ? launch_estep_wide<true>(x, n, d, K, state, part, resp, sk, st)
+                            : launch_estep_wide<false>(x, n, d, K, state, part, resp, sk, st);
+        return hard ? launch_estep<true>(maxs, x, n, d, K, state, part, sk, st)
+                    : launch_estep<false>(maxs, x, n, d, K, state, part, sk, st);
+    };
     k_em_init<<<1, kEmT, 0, st>>>(x, d, K, idx, cov0, reg, state);
     double *tot = part + em_partial_doubles(K, d);   // [S + 1] after the partials
     const int rblocks = (32 * (S + 1) + kEmT - 1) / kEmT;
     cudaError_t e = cudaSuccess;
     for (int t = 0; t <= kmeans_iters && kmeans_iters > 0; ++t) {   // Lloyd, then the one-hot M-step
-        e = launch_estep<true>(maxs, x, n, d, K, state, part, nullptr, st);
+        e = estep(true, nullptr);
         if (e != cudaSuccess) return e;
-        k_em_reduce<<<rblocks, kEmT, 0, st>>>(part, kEmBlocks, S + 1, tot, nullptr);
+        k_em_reduce<<<rblocks, kEmT, 0, st>>>(part, nb, S + 1, tot, nullptr);
         if (t < kmeans_iters) k_km_update<<<1, kEmT, 0, st>>>(tot, d, K, state);
         else k_em_mstep<<<1, kEmT, 0, st>>>(tot, n, d, K, reg, state, 1, 0.0, flags);
     }
@@ -443,12 +647,13 @@ cudaError_t launch_gmm_fit(const float *x, long long n, int d, int K, const int 
         }
         const bool eval = it == iters;   // evaluation only: the log-likelihood of the returned parameters
         const int *sk = eval ? nullptr : skip;
-        if (d <= 8) k_em_chol<8><<<K, 32, 0, st>>>(state, K, d, flags, sk);
+        if (wd) k_em_chol_wide<<<K, kEmT, 0, st>>>(state, K, d, flags, sk, Lscr);
+        else if (d <= 8) k_em_chol<8><<<K, 32, 0, st>>>(state, K, d, flags, sk);
         else if (d <= 16) k_em_chol<16><<<K, 32, 0, st>>>(state, K, d, flags, sk);
         else k_em_chol<32><<<K, 32, 0, st>>>(state, K, d, flags, sk);
-        e = launch_estep<false>(maxs, x, n, d, K, state, part, sk, st);
+        e = estep(false, sk);
         if (e != cudaSuccess) return e;
-        k_em_reduce<<<rblocks, kEmT, 0, st>>>(part, kEmBlocks, S + 1, tot, sk);
+        k_em_reduce<<<rblocks, kEmT, 0, st>>>(part, nb, S + 1, tot, sk);
         if (eval) {
             k_em_mstep<<<1, kEmT, 0, st>>>(tot, n, d, K, reg, state + em_state_doubles(K, d), 2, 0.0, flags);
             break;

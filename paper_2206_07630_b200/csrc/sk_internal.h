@@ -58,12 +58,13 @@ cudaError_t launch_nw1d(const float *xs, const int *xperm, const float *ys, cons
 size_t em_state_doubles(int K, int d);
 size_t em_partial_doubles(int K, int d);
 size_t em_work_doubles(int K, int d);   // partials + the reduced statistics (launch_gmm_fit's part)
+size_t em_wide_doubles(long long n, int K, int d);   // d > 32: responsibilities [n][K] + Cholesky scratch
 cudaError_t launch_gmm_fit(const float *x, long long n, int d, int K, const int *idx, const double *cov0,
                            int kmeans_iters, int iters, double tol, double reg,
                            double *state /* 2 x em_state_doubles */, double *part,
                            int *flags /* [3]: non-PD, converged, EM steps */, float *w, float *mu, float *cov,
                            double *ll_out, int *h_conv /* pinned host int, nullable: convergence polls */,
-                           cudaStream_t st);
+                           cudaStream_t st, double *wide = nullptr /* d > 32: em_wide_doubles */);
 // K17 implicit differentiation (NEXT-4)
 size_t vjp_work_doubles(long long n, long long m, int d);
 cudaError_t launch_vjp(long long n, long long m, int d, const float *x, const float *y, float eps, const float *f,

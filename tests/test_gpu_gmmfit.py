@@ -106,7 +106,7 @@ def test_fit_errors(ctx):
     with pytest.raises(sk.SinkhornError):
         sk.sinkhorn_fit_gmm(ctx, x, 3, [1, 2, 100])        # out of range
     with pytest.raises(sk.SinkhornError):
-        sk.sinkhorn_fit_gmm(ctx, torch.rand(100, 33, device="cuda"), 2, [0, 1])   # d > 32
+        sk.sinkhorn_fit_gmm(ctx, torch.rand(100, 257, device="cuda"), 2, [0, 1])   # d > 256
     with pytest.raises(sk.SinkhornError):
         sk.sinkhorn_fit_gmm(ctx, x, 2, [0, 1], kmeans_iters=-1)
     with pytest.raises(sk.SinkhornError):
@@ -114,3 +114,22 @@ def test_fit_errors(ctx):
     bad = x.clone(); bad[5, 1] = float("inf")
     with pytest.raises(sk.SinkhornError):
         sk.sinkhorn_fit_gmm(ctx, bad, 2, [0, 1])
+
+
+@pytest.mark.parametrize("n,d,K,km,iters,tol", [(3000, 50, 10, 10, 6, 0.0), (2000, 40, 5, 0, 8, 0.0),
+                                                (4000, 64, 8, 10, 100, 1e-3), (1200, 130, 3, 5, 4, 0.0)])
+def test_fit_wide_parity(O, ctx, n, d, K, km, iters, tol):
+    """d > 32 (the wide path: per-component Cholesky CTAs, responsibilities per point, the
+    x x^T statistics by 64 x 64 tiles; P:388's word-embedding mixtures are d = 50, K up to 50)
+    against the oracle's EM, k-means start and stopping rule included."""
+    import paper_2206_07630_b200 as sk
+    rng = np.random.default_rng(n + d)
+    cents = rng.standard_normal((K, d)) * 2
+    x = (cents[rng.integers(0, K, n)] + rng.standard_normal((n, d)) * 0.9).astype(np.float32)
+    idx = gen.gmm_start_idx(n, K, seed=n + 3)
+    g, ll, it = sk.sinkhorn_fit_gmm(ctx, torch.from_numpy(x).cuda(), K, idx, iters=iters, kmeans_iters=km, tol=tol,
+                                    return_iters=True)
+    w, m, S, llo, ito = O.gmm_fit(x, K, idx, iters, 1e-6, kmeans_iters=km, tol=tol, return_iters=True)
+    assert it == ito, (it, ito)
+    assert _close(g["weights"], w, 1e-6) and _close(g["means"], m, 1e-6) and _close(g["covs"], S, 1e-6)
+    assert abs(ll - llo) <= 1e-9 * max(1.0, abs(llo))
