@@ -229,8 +229,8 @@ sk_status sinkhorn_sort1d_batched(sk_ctx *ctx, int64_t B, int64_t n, const float
  * (f, g) must be (close to) optimal — normally sinkhorn_solve's output.  x: n x d, y: m x d,
  * f: n, g: m, zf: n, zg: m; outputs (each nullable): grad_x n x d, grad_y m x d, grad_a n,
  * grad_b m.  cg_iters / cg_relres (host, nullable): iterations and the final relative
- * residual.  SK_EINVAL on bad sizes, eps or cg_tol <= 0, non-finite inputs; SK_EUNSUPPORTED
- * for d > 64.  Blocks. */
+ * residual.  d in [1, 256] (d > 64: 32-point CTAs with the coordinates in shared memory).
+ * SK_EINVAL on bad sizes (d > 256), eps or cg_tol <= 0, non-finite inputs.  Blocks. */
 sk_status sinkhorn_vjp(sk_ctx *ctx, int64_t n, int64_t m, int32_t d, const float *x, const float *y,
                        float eps, const float *f, const float *g, const float *zf, const float *zg,
                        float cg_tol, int32_t cg_max_iter, float *grad_x, float *grad_y, float *grad_a,

@@ -1122,9 +1122,8 @@ sk_status sinkhorn_vjp(sk_ctx *ctx, int64_t n, int64_t m, int32_t d, const float
                        int32_t cg_max_iter, float *grad_x, float *grad_y, float *grad_a, float *grad_b,
                        int32_t *cg_iters, double *cg_relres) {
     if (!ctx) return SK_EINVAL;
-    if (n < 1 || m < 1 || d < 1 || !x || !y || !f || !g || !zf || !zg || cg_max_iter < 1)
-        return fail(ctx, SK_EINVAL, "bad arguments");
-    if (d > 64) return fail(ctx, SK_EUNSUPPORTED, "d <= 64");
+    if (n < 1 || m < 1 || d < 1 || d > 256 || !x || !y || !f || !g || !zf || !zg || cg_max_iter < 1)
+        return fail(ctx, SK_EINVAL, "bad arguments (d in [1, 256])");
     if (!(eps > 0.f) || bad_scalar(eps) || !(cg_tol > 0.f) || bad_scalar(cg_tol))
         return fail(ctx, SK_EINVAL, "eps and cg_tol must be > 0 and finite");
     Stager sg(ctx);

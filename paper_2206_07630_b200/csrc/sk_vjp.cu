@@ -79,7 +79,84 @@ __global__ void __launch_bounds__(kVT) k_plan_pass(const float *__restrict__ ps,
             if (k < d) G[(long long)p * d + k] = gk[k];
 }
 
-static int dm_of(int d) { return d <= 4 ? 4 : (d <= 16 ? 16 : (d <= 32 ? 32 : (d <= 64 ? 64 : 0))); }
+static int dm_of(int d) { return d <= 4 ? 4 : (d <= 16 ? 16 : (d <= 32 ? 32 : (d <= 64 ? 64 : (d <= 256 ? 256 : 0)))); }
+
+// K17a for d in (64, 256]: 32 output points per CTA, 256 threads.  Per 32-point reduced tile:
+// phase 1, thread (p, u) forms P_pq for q = u, u + 8, .. (the cost in k order with direct fp32
+// differences, as above) into shared memory; phase 2, thread p sums A[p] over the tile in q order
+// and threads (p, u) accumulate G[p][k] for k = u, u + 8, .. (32 doubles each) in q order.
+constexpr int kVWP = 32, kVWQ = 32, kVWT = 256;
+__global__ void __launch_bounds__(kVWT) k_plan_pass_wide(const float *__restrict__ ps, const float *__restrict__ hp,
+                                                         int P, const float *__restrict__ qs,
+                                                         const float *__restrict__ hq, int Q, int d, float eps,
+                                                         const double *__restrict__ s, const double *__restrict__ v,
+                                                         double *A, double *G) {
+    extern __shared__ float wsm[];
+    const int d1 = d + 1;
+    float *sp = wsm;                        // [kVWP][d + 1]
+    float *sq = sp + kVWP * d1;             // [kVWQ][d + 1]
+    double *pw = reinterpret_cast<double *>(sq + kVWQ * d1 + ((kVWP + kVWQ) * d1 & 1));   // [kVWP][kVWQ]
+    double *qv = pw + kVWP * kVWQ;          // [kVWQ]
+    float *qh = reinterpret_cast<float *>(qv + kVWQ);   // [kVWQ]
+    const int p0 = blockIdx.x * kVWP;
+    const int pl = threadIdx.x >> 3, u = threadIdx.x & 7;
+    const int p = p0 + pl;
+    const float kap = kLog2e / eps;
+    for (int e = threadIdx.x; e < kVWP * d; e += kVWT) {
+        const int r = e / d, k = e % d;
+        sp[r * d1 + k] = p0 + r < P ? ps[(long long)(p0 + r) * d + k] : 0.f;
+    }
+    const float hpp = p < P ? hp[p] : 0.f;
+    const double spp = (s && p < P) ? s[p] : 0.0;
+    double a = 0.0, gk[32];
+#pragma unroll
+    for (int t = 0; t < 32; ++t) gk[t] = 0.0;
+    for (int q0 = 0; q0 < Q; q0 += kVWQ) {
+        const int nq = min(kVWQ, Q - q0);
+        __syncthreads();
+        for (int e = threadIdx.x; e < kVWQ * d; e += kVWT) {
+            const int r = e / d, k = e % d;
+            sq[r * d1 + k] = r < nq ? qs[(long long)(q0 + r) * d + k] : 0.f;
+        }
+        for (int e = threadIdx.x; e < kVWQ; e += kVWT) {
+            qh[e] = e < nq ? hq[q0 + e] : 0.f;
+            qv[e] = e < nq ? (v ? v[q0 + e] : 1.0) : 0.0;
+        }
+        __syncthreads();
+        for (int j = u; j < nq; j += 8) {
+            const float *pp = sp + pl * d1, *qq = sq + j * d1;
+            float c = 0.f;
+            for (int k = 0; k < d; ++k) {
+                const float df = pp[k] - qq[k];
+                c = fmaf(df, df, c);
+            }
+            pw[pl * kVWQ + j] = (double)ex2((hpp + qh[j] - c) * kap);
+        }
+        __syncthreads();
+        if (u == 0)
+            for (int j = 0; j < nq; ++j) a = fma(pw[pl * kVWQ + j], qv[j], a);
+        if (G) {
+            const float *pp = sp + pl * d1;
+            for (int j = 0; j < nq; ++j) {
+                const double wt = pw[pl * kVWQ + j] * (spp + qv[j]);
+                const float *qq = sq + j * d1;
+#pragma unroll
+                for (int t = 0; t < 32; ++t) {
+                    const int k = u + 8 * t;
+                    if (k < d) gk[t] = fma(wt, (double)(pp[k] - qq[k]), gk[t]);
+                }
+            }
+        }
+    }
+    if (p >= P) return;
+    if (A && u == 0) A[p] = a;
+    if (G)
+#pragma unroll
+        for (int t = 0; t < 32; ++t) {
+            const int k = u + 8 * t;
+            if (k < d) G[(long long)p * d + k] = gk[t];
+        }
+}
 
 cudaError_t launch_plan_pass(const float *ps, const float *hp, int P, const float *qs, const float *hq, int Q, int d,
                              float eps, const double *s, const double *v, double *A, double *G, cudaStream_t st) {
@@ -89,6 +166,14 @@ cudaError_t launch_plan_pass(const float *ps, const float *hp, int P, const floa
         case 16: k_plan_pass<16><<<grid, kVT, 0, st>>>(ps, hp, P, qs, hq, Q, d, eps, s, v, A, G); break;
         case 32: k_plan_pass<32><<<grid, kVT, 0, st>>>(ps, hp, P, qs, hq, Q, d, eps, s, v, A, G); break;
         case 64: k_plan_pass<64><<<grid, kVT, 0, st>>>(ps, hp, P, qs, hq, Q, d, eps, s, v, A, G); break;
+        case 256: {
+            const size_t smem = sizeof(float) * ((size_t)(kVWP + kVWQ) * (d + 1) + 1) +
+                                sizeof(double) * ((size_t)kVWP * kVWQ + kVWQ) + sizeof(float) * kVWQ + 16;
+            cudaError_t e = cudaFuncSetAttribute(k_plan_pass_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess) return e;
+            k_plan_pass_wide<<<(P + kVWP - 1) / kVWP, kVWT, smem, st>>>(ps, hp, P, qs, hq, Q, d, eps, s, v, A, G);
+            break;
+        }
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();

@@ -26,7 +26,7 @@ def _rel(u, v):
 
 
 @pytest.mark.parametrize("n,m,d,epsf", [(40, 33, 2, 0.05), (256, 256, 2, 0.01), (200, 150, 16, 0.05),
-                                        (64, 70, 64, 0.1), (1, 5, 3, 0.1)])
+                                        (64, 70, 64, 0.1), (1, 5, 3, 0.1), (90, 77, 100, 0.1), (70, 65, 256, 0.1)])
 def test_vjp_parity_on_oracle_potentials(O, ctx, n, m, d, epsf):
     import paper_2206_07630_b200 as sk
     rng = np.random.default_rng(n * 3 + d)
@@ -66,6 +66,24 @@ def test_vjp_envelope_at_scale(ctx):
     assert _rel(grads["x"].cpu().numpy(), env) <= 1e-3, _rel(grads["x"].cpu().numpy(), env)
 
 
+def test_vjp_envelope_wide(ctx):
+    """The envelope check at d = 128 (the wide plan pass, n = m = 2048, BJ.cfg5-shaped points) on
+    the GPU's own K-chunked tensor-core solve."""
+    import paper_2206_07630_b200 as sk
+    p = gen.c5(n=2048, d=128, eps_factor=5e-2)
+    x, y = _c(p.x), _c(p.y)
+    f, g, rep = sk.sinkhorn_solve(ctx, x, y, p.eps, tol=1e-6, mode="online")
+    n = p.x.shape[0]
+    grads, info = sk.sinkhorn_vjp(ctx, x, y, p.eps, f, g, torch.full((n,), 1 / n, device="cuda"),
+                                  torch.full((n,), 1 / n, device="cuda"), cg_tol=1e-8)
+    X, Y = p.x.astype(np.float64), p.y.astype(np.float64)
+    F, G = f.cpu().numpy().astype(np.float64), g.cpu().numpy().astype(np.float64)
+    C = ((X[:, None] - Y[None]) ** 2).sum(-1)
+    P = np.exp((F[:, None] + G[None] - C) / p.eps)
+    env = 2 * (P.sum(1)[:, None] * X - P @ Y)
+    assert _rel(grads["x"].cpu().numpy(), env) <= 1e-3, _rel(grads["x"].cpu().numpy(), env)
+
+
 def test_vjp_errors(ctx):
     import paper_2206_07630_b200 as sk
     x, y = torch.rand(10, 2, device="cuda"), torch.rand(9, 2, device="cuda")
@@ -73,4 +91,4 @@ def test_vjp_errors(ctx):
     with pytest.raises(sk.SinkhornError):
         sk.sinkhorn_vjp(ctx, x, y, 0.0, f, g, f, g)
     with pytest.raises(sk.SinkhornError):
-        sk.sinkhorn_vjp(ctx, torch.rand(10, 65, device="cuda"), torch.rand(9, 65, device="cuda"), 0.1, f, g, f, g)
+        sk.sinkhorn_vjp(ctx, torch.rand(10, 257, device="cuda"), torch.rand(9, 257, device="cuda"), 0.1, f, g, f, g)
