@@ -212,7 +212,9 @@ sk_status sk_shard_rows(int64_t n_total, int32_t rank, int32_t world, int64_t *r
 /* Batched stable sort / rank of B rows of n fp32 keys (the sorting permutations
  * sigma of P:110): perm[b][k] = index of the k-th smallest key of row b, ties by
  * index (stable), -0.0 == +0.0 (R-16); rank[b][perm[b][k]] = k.  perm or rank may
- * be NULL.  Bit-exact.  SK_EINVAL on NaN keys.  n <= 8192 per row. */
+ * be NULL.  Bit-exact.  SK_EINVAL on NaN keys.  n <= 2^24 per row (n <= 8192: one CTA per row
+ * in shared memory; longer rows: the bitonic network over a global key array, 8192-key segments
+ * in shared memory). */
 sk_status sinkhorn_sort1d_batched(sk_ctx *ctx, int64_t B, int64_t n, const float *x,
                                   int32_t *perm, int32_t *rank);
 
@@ -286,8 +288,9 @@ sk_status sinkhorn_init_zero(sk_ctx *ctx, int64_t B, int64_t n, float *pot);
  *   dualsort_iters == L > 0: exactly L vectorised (Jacobi) sweeps of Alg. 2,
  *     O(L n^2) (the paper's "3 iterations").
  * x: B x n; y: m values (y_shared = 1) or B x m.  pot: B x n (x side).  perm /
- * rank (nullable): the sort of x as in sinkhorn_sort1d_batched.
- * SK_EUNSUPPORTED if n != m (general NW + Alg. 3 is a later row). */
+ * rank (nullable): the sort of x as in sinkhorn_sort1d_batched.  n <= 2^24 (the closed form;
+ * n > 4096 keeps its scans in workspace), paper mode n <= 4096.
+ * SK_EUNSUPPORTED if n != m (sinkhorn_init_nw1d takes any n, m) or beyond those sizes. */
 sk_status sinkhorn_init_sort1d(sk_ctx *ctx, int64_t B, int64_t n, int64_t m, const float *x,
                                const float *y, int32_t y_shared, int32_t dualsort_iters,
                                float *pot, int32_t *perm, int32_t *rank);

@@ -103,7 +103,7 @@ namespace {
 enum BufId {
     B_STAGE0 = 0, B_STAGE_END = 16,   // staging of host arrays
     B_FLAG = 16, B_XPACK, B_XC, B_XNK, B_XPOT, B_YPACK, B_YC, B_YNK, B_YPOT, B_PART, B_BLKE, B_BLKB,
-    B_STATUS, B_COST, B_REP, B_SORT, B_PERM, B_YSORT, B_GAUSS, B_GAUSS2, B_GMM, B_EMWIDE, B_SUBW, B_SUBZ,
+    B_STATUS, B_COST, B_REP, B_SORT, B_PERM, B_YSORT, B_GAUSS, B_GAUSS2, B_GMM, B_EMWIDE, B_SORTKEYS, B_DUALSCR, B_SUBW, B_SUBZ,
     B_SUBF, B_SUBG, B_IDX, B_OUT, B_FA, B_QUEUE, B_XIMG, B_YIMG, B_XLSE, B_YLSE, B_TCMAX, B_EMST, B_EMPART, B_EMIDX, B_VJP, B_ANDFR, B_ANDBLK, B_ANDVEC, B_ANDST, B_XCHG, B_PARK, B_XCNT, B_XROW, B_XCNT2, B_GRID, B_NBUF
 };
 
@@ -1039,7 +1039,7 @@ sk_status sinkhorn_sort1d_batched(sk_ctx *ctx, int64_t B, int64_t n, const float
                                   int32_t *rank) {
     if (!ctx) return SK_EINVAL;
     if (B < 1 || n < 1) return fail(ctx, SK_EINVAL, "B, n must be >= 1");
-    if (n > 8192) return fail(ctx, SK_EUNSUPPORTED, "sort rows of at most 8192 keys");
+    if (n > (1LL << 24)) return fail(ctx, SK_EUNSUPPORTED, "sort rows of at most 2^24 keys");
     if (!x) return fail(ctx, SK_EINVAL, "x is NULL");
     Stager sg(ctx);
     const float *dx;
@@ -1049,7 +1049,12 @@ sk_status sinkhorn_sort1d_batched(sk_ctx *ctx, int64_t B, int64_t n, const float
     CK(sg.out_t(rank, (size_t)B * n, &dr));
     ENSURE(flag, int, B_FLAG, 4);
     CU(cudaMemsetAsync(flag, 0, sizeof(int), ctx->stream));
-    CU(launch_sort_rows(dx, (int)B, (int)n, n, dp, dr, nullptr, flag, ctx->stream));
+    unsigned long long *gk = nullptr;
+    if (sort_rows_scratch_keys((int)B, (int)n)) {
+        ENSURE(kk, unsigned long long, B_SORTKEYS, sort_rows_scratch_keys((int)B, (int)n));
+        gk = kk;
+    }
+    CU(launch_sort_rows(dx, (int)B, (int)n, n, dp, dr, nullptr, flag, ctx->stream, gk));
     ctx->cnt.kernel_launches++;
     CK(sg.flush());
     CU(cudaMemcpyAsync(ctx->h_flag, flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
@@ -1199,7 +1204,9 @@ sk_status sinkhorn_init_sort1d(sk_ctx *ctx, int64_t B, int64_t n, int64_t m, con
     if (!ctx) return SK_EINVAL;
     if (B < 1 || n < 1 || m < 1 || !x || !y || !pot) return fail(ctx, SK_EINVAL, "bad arguments");
     if (n != m) return fail(ctx, SK_EUNSUPPORTED, "sort1d initializer needs n == m (sinkhorn_init_nw1d: any n, m)");
-    if (n > 4096) return fail(ctx, SK_EUNSUPPORTED, "sort1d initializer supports n <= 4096");
+    if (n > (1LL << 24)) return fail(ctx, SK_EUNSUPPORTED, "sort1d initializer supports n <= 2^24");
+    if (dualsort_iters > 0 && n > 4096)
+        return fail(ctx, SK_EUNSUPPORTED, "paper-mode DualSort (L Jacobi sweeps, O(L n^2)) supports n <= 4096");
     if (dualsort_iters < 0) return fail(ctx, SK_EINVAL, "dualsort_iters >= 0");
     Stager sg(ctx);
     const float *dx, *dy;
@@ -1216,9 +1223,19 @@ sk_status sinkhorn_init_sort1d(sk_ctx *ctx, int64_t B, int64_t n, int64_t m, con
     ENSURE(pscr, int, B_PERM, (y_shared ? 1 : B) * m + B * n);
     int *dperm = dperm_user ? dperm_user : pscr + (y_shared ? 1 : B) * m;
     CU(cudaMemsetAsync(flag, 0, sizeof(int), ctx->stream));
-    CU(launch_sort_rows(dy, (int)(y_shared ? 1 : B), (int)m, m, pscr, nullptr, ys, flag, ctx->stream));
-    CU(launch_sort_rows(dx, (int)B, (int)n, n, dperm, drank, xs, flag, ctx->stream));
-    CU(launch_sort1d_dual(xs, dperm, ys, y_shared, (int)B, (int)n, dualsort_iters, dpot, ctx->stream));
+    unsigned long long *gk = nullptr;
+    double *gd = nullptr;
+    if (sort_rows_scratch_keys((int)B, (int)n)) {
+        ENSURE(kk, unsigned long long, B_SORTKEYS, sort_rows_scratch_keys((int)B, (int)n));
+        gk = kk;
+    }
+    if (n > 4096) {
+        ENSURE(dd, double, B_DUALSCR, 4 * B * n);
+        gd = dd;
+    }
+    CU(launch_sort_rows(dy, (int)(y_shared ? 1 : B), (int)m, m, pscr, nullptr, ys, flag, ctx->stream, gk));
+    CU(launch_sort_rows(dx, (int)B, (int)n, n, dperm, drank, xs, flag, ctx->stream, gk));
+    CU(launch_sort1d_dual(xs, dperm, ys, y_shared, (int)B, (int)n, dualsort_iters, dpot, ctx->stream, gd));
     ctx->cnt.kernel_launches += 3;
     CK(sg.flush());
     CU(cudaMemcpyAsync(ctx->h_flag, flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));

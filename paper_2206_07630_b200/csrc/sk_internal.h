@@ -287,10 +287,14 @@ cudaError_t launch_check_indices(const int *idx, long long cnt, long long n, int
                                  cudaStream_t st);
 
 // ----------------------------------------------------------------- sort1d
+// rows of n > 8192 keys need gkeys (sort_rows_scratch_keys(B, n) u64); the closed-form dual for
+// n > 4096 needs gscr (4 B n doubles)
+size_t sort_rows_scratch_keys(int B, int n);
 cudaError_t launch_sort_rows(const float *x, int B, int n, long long stride, int *perm, int *rank,
-                             float *sorted, int *nanflag, cudaStream_t st);
+                             float *sorted, int *nanflag, cudaStream_t st, unsigned long long *gkeys = nullptr);
 cudaError_t launch_sort1d_dual(const float *xs_sorted, const int *perm, const float *ys_sorted,
-                               int y_shared, int B, int n, int iters, float *pot, cudaStream_t st);
+                               int y_shared, int B, int n, int iters, float *pot, cudaStream_t st,
+                               double *gscr = nullptr);
 
 // --------------------------------------------------------------- Gaussian
 cudaError_t launch_moments(const float *x, const float *w, long long n, int d, double *mean,

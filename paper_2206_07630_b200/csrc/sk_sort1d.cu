@@ -17,6 +17,8 @@
 //     The oracle runs Alg. 2 itself to its fixed point; parity checks the two agree.
 //     Paper mode (iters = L > 0): exactly L Jacobi sweeps of Alg. 2, O(L n^2).
 //     Then f^(0)_{sigma(k)} = f~_k.
+#include <algorithm>
+
 #include "sk_internal.h"
 #include "sk_common.cuh"
 
@@ -70,10 +72,113 @@ __global__ void __launch_bounds__(kST) k_sort_rows(const float *__restrict__ x, 
     }
 }
 
+// ---- rows longer than 8192 keys: the same bitonic network over a global key array per row
+// (B x N2 keys), compare distances j >= kSeg by one launch per (k, j) stage over all rows, and
+// the stages j < kSeg of every k on 8192-key segments in shared memory.  The direction of a
+// comparison is that of the global key index (i & k), so the result is the whole-row bitonic
+// sort: keys (orderable value, index) are distinct, hence a stable sort by value.
+constexpr int kSeg = 8192;
+
+__global__ void k_keys_init(const float *__restrict__ x, int B, int n, long long stride, int N2,
+                            unsigned long long *keys, int *nanflag) {
+    const long long tot = (long long)B * N2;
+    int bad = 0;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot; e += (long long)gridDim.x * blockDim.x) {
+        const long long row = e / N2;
+        const int i = (int)(e % N2);
+        if (i < n) {
+            const float v = x[row * stride + i];
+            bad |= isnan(v);
+            keys[e] = ((unsigned long long)orderable(v) << 32) | (unsigned)i;
+        } else {
+            keys[e] = ~0ull;
+        }
+    }
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(nanflag, 1);
+}
+
+// one global stage (k, j >= kSeg): every pair (i, i ^ j) with i < i ^ j once
+__global__ void k_bitonic_global(unsigned long long *keys, int B, int N2, int k, int j) {
+    const long long half = (long long)B * (N2 / 2);
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < half; t += (long long)gridDim.x * blockDim.x) {
+        const long long row = t / (N2 / 2);
+        const int q = (int)(t % (N2 / 2));
+        const int i = ((q / j) * 2 * j) + (q % j);   // the lower index of the pair
+        unsigned long long *kr = keys + row * N2;
+        const unsigned long long A = kr[i], Bk = kr[i + j];
+        const bool up = (i & k) == 0;
+        if ((A > Bk) == up) { kr[i] = Bk; kr[i + j] = A; }
+    }
+}
+
+// the stages (k, j) for j = jmax, .., 1 (jmax < kSeg; kmin..kmax: every k in [kmin, kmax] with all
+// its j) on one kSeg segment in shared memory
+__global__ void __launch_bounds__(kST) k_bitonic_seg(unsigned long long *keys, int N2, int kmin, int kmax) {
+    extern __shared__ unsigned long long sk_[];
+    const int segs = N2 / kSeg;
+    const long long row = blockIdx.x / segs;
+    const int base = (blockIdx.x % segs) * kSeg;
+    unsigned long long *kr = keys + row * N2 + base;
+    for (int i = threadIdx.x; i < kSeg; i += kST) sk_[i] = kr[i];
+    __syncthreads();
+    for (int k = kmin; k <= kmax; k <<= 1) {
+        for (int j = min(k >> 1, kSeg >> 1); j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < kSeg; i += kST) {
+                const int ixj = i ^ j;
+                if (ixj > i) {
+                    const unsigned long long A = sk_[i], Bk = sk_[ixj];
+                    const bool up = ((base + i) & k) == 0;
+                    if ((A > Bk) == up) { sk_[i] = Bk; sk_[ixj] = A; }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (int i = threadIdx.x; i < kSeg; i += kST) kr[i] = sk_[i];
+}
+
+__global__ void k_keys_out(const unsigned long long *keys, const float *__restrict__ x, int B, int n, long long stride,
+                           int N2, int *perm, int *rank, float *sorted) {
+    const long long tot = (long long)B * n;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot; e += (long long)gridDim.x * blockDim.x) {
+        const long long row = e / n;
+        const int k = (int)(e % n);
+        const int idx = (int)(keys[row * N2 + k] & 0xffffffffu);
+        if (perm) perm[row * n + k] = idx;
+        if (rank) rank[row * n + idx] = k;
+        if (sorted) sorted[row * n + k] = x[row * stride + idx];
+    }
+}
+
+size_t sort_rows_scratch_keys(int B, int n) {
+    if (n <= kSeg) return 0;
+    long long N2 = 1;
+    while (N2 < n) N2 <<= 1;
+    return (size_t)B * N2;
+}
+
 cudaError_t launch_sort_rows(const float *x, int B, int n, long long stride, int *perm, int *rank,
-                             float *sorted, int *nanflag, cudaStream_t st) {
+                             float *sorted, int *nanflag, cudaStream_t st, unsigned long long *gkeys) {
     int N2 = 1;
     while (N2 < n) N2 <<= 1;
+    if (n > kSeg) {
+        if (!gkeys) return cudaErrorInvalidValue;
+        const size_t smem = (size_t)kSeg * sizeof(unsigned long long);
+        cudaError_t e = cudaFuncSetAttribute(k_bitonic_seg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        const long long tot = (long long)B * N2;
+        const int g = (int)std::min<long long>((tot + 255) / 256, 148 * 16);
+        k_keys_init<<<g, 256, 0, st>>>(x, B, n, stride, N2, gkeys, nanflag);
+        const int nseg = B * (N2 / kSeg);
+        k_bitonic_seg<<<nseg, kST, smem, st>>>(gkeys, N2, 2, kSeg);   // every segment sorted (alternating)
+        for (int k = 2 * kSeg; k <= N2; k <<= 1) {
+            for (int j = k >> 1; j >= kSeg; j >>= 1) k_bitonic_global<<<g, 256, 0, st>>>(gkeys, B, N2, k, j);
+            k_bitonic_seg<<<nseg, kST, smem, st>>>(gkeys, N2, k, k);   // j = kSeg / 2 .. 1 of this k
+        }
+        const int go = (int)std::min<long long>(((long long)B * n + 255) / 256, 148 * 16);
+        k_keys_out<<<go, 256, 0, st>>>(gkeys, x, B, n, stride, N2, perm, rank, sorted);
+        return cudaGetLastError();
+    }
     const size_t smem = (size_t)N2 * sizeof(unsigned long long);
     cudaError_t e = cudaFuncSetAttribute(k_sort_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -105,12 +210,16 @@ __device__ void block_scan(double *v, int n, int op, bool reverse, double *tmp /
     __syncthreads();
 }
 
+// (gscr != nullptr: n > 4096, the four n-vectors of problem b in gscr + 4 n b instead of shared
+// memory; the same scans in the same order)
 __global__ void __launch_bounds__(kST) k_dual_closed(const float *__restrict__ xs_all,
                                                      const int *__restrict__ perm,
                                                      const float *__restrict__ ys_all, int y_shared,
-                                                     int n, float *pot) {
+                                                     int n, float *pot, double *gscr) {
     extern __shared__ double sd[];
-    double *F = sd, *Bv = sd + n, *Fm = sd + 2 * n, *Bm = sd + 3 * n, *tmp = sd + 4 * n;
+    __shared__ double tmp_g[kST];
+    double *base = gscr ? gscr + 4LL * n * blockIdx.x : sd;
+    double *F = base, *Bv = base + n, *Fm = base + 2 * n, *Bm = base + 3 * n, *tmp = gscr ? tmp_g : sd + 4 * n;
     const int prob = blockIdx.x;
     const float *xs = xs_all + (long long)prob * n;
     const float *ys = ys_all + (y_shared ? 0 : (long long)prob * n);
@@ -175,13 +284,15 @@ __global__ void __launch_bounds__(kST) k_dual_jacobi(const float *__restrict__ x
 }
 
 cudaError_t launch_sort1d_dual(const float *xs_sorted, const int *perm, const float *ys_sorted,
-                               int y_shared, int B, int n, int iters, float *pot, cudaStream_t st) {
+                               int y_shared, int B, int n, int iters, float *pot, cudaStream_t st, double *gscr) {
     if (iters <= 0) {
-        const size_t smem = (4 * (size_t)n + kST) * sizeof(double);
+        const bool glob = n > 4096;
+        if (glob && !gscr) return cudaErrorInvalidValue;
+        const size_t smem = glob ? 0 : (4 * (size_t)n + kST) * sizeof(double);
         cudaError_t e = cudaFuncSetAttribute(k_dual_closed, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem);
         if (e != cudaSuccess) return e;
-        k_dual_closed<<<B, kST, smem, st>>>(xs_sorted, perm, ys_sorted, y_shared, n, pot);
+        k_dual_closed<<<B, kST, smem, st>>>(xs_sorted, perm, ys_sorted, y_shared, n, pot, glob ? gscr : nullptr);
     } else {
         const size_t smem = 5 * (size_t)n * sizeof(double);
         cudaError_t e = cudaFuncSetAttribute(k_dual_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize,

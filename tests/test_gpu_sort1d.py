@@ -20,7 +20,8 @@ def _cuda(a):
     return torch.from_numpy(np.ascontiguousarray(a)).cuda()
 
 
-@pytest.mark.parametrize("B,n", [(1024, 1024), (3, 1), (5, 1000), (2, 4097), (1, 8192)])
+@pytest.mark.parametrize("B,n", [(1024, 1024), (3, 1), (5, 1000), (2, 4097), (1, 8192), (2, 8193), (3, 20000),
+                                 (1, 100000)])
 def test_sort_rank_bit_exact(O, ctx, B, n):
     import paper_2206_07630_b200 as sk
     rng = np.random.default_rng(B + n)
@@ -73,6 +74,43 @@ def test_sort1d_paper_mode(O, ctx, L):
     for b in range(4):
         f0 = O.init_sort1d(x[b], y, sweeps=L)
         assert np.abs(pot[b] - f0).max() <= 1e-6
+
+
+@pytest.mark.parametrize("B,n,shared", [(1, 6000, True), (1, 8300, False)])
+def test_sort1d_large_n_vs_oracle(O, ctx, B, n, shared):
+    """n > 4096: the closed-form scans in workspace (and, n > 8192, the global bitonic sort)
+    against the oracle's Alg. 2 Jacobi fixed point."""
+    import paper_2206_07630_b200 as sk
+    rng = np.random.default_rng(n)
+    x = rng.random((B, n), dtype=np.float32)
+    y = (np.arange(n) / (n - 1)).astype(np.float32) if shared else rng.random((B, n), dtype=np.float32)
+    pot = sk.sinkhorn_init_sort1d(ctx, _cuda(x), _cuda(y), y_shared=shared).cpu().numpy()
+    for b in range(B):
+        f0 = O.init_sort1d(x[b], y if shared else y[b])
+        assert np.abs(pot[b] - f0).max() <= 1e-6, b
+
+
+def test_sort1d_fixed_point_at_scale(O, ctx):
+    """n = 200000 (one problem): the returned dual is the fixed point of Alg. 2 on the sorted
+    supports — f_i = min_j (c_ij - c_jj + f_j) — checked on 512 sampled rows over all j in fp64,
+    with f <= 0 and max f = 0 (the fixed point from f = 0)."""
+    import paper_2206_07630_b200 as sk
+    n = 200000
+    rng = np.random.default_rng(5)
+    x = rng.random((1, n), dtype=np.float32)
+    y = rng.standard_normal(n).astype(np.float32)
+    pot, perm, _ = sk.sinkhorn_init_sort1d(ctx, _cuda(x), _cuda(y), y_shared=True, want_perm=True)
+    pot, perm = pot.cpu().numpy()[0].astype(np.float64), perm.cpu().numpy()[0]
+    assert np.array_equal(perm, O.sort_rank(x)[0][0])
+    xs = x[0][perm].astype(np.float64)
+    ys = np.sort(y).astype(np.float64)
+    fs = pot[perm]
+    cjj = (xs - ys) ** 2
+    scale = max(1.0, np.abs(fs).max())
+    assert fs.max() <= 1e-6 * scale and abs(fs.max()) <= 1e-6 * scale
+    for i in np.sort(rng.choice(n, 512, replace=False)):
+        best = np.min((xs[i] - ys) ** 2 - cjj + fs)
+        assert abs(best - fs[i]) <= 1e-5 * scale, (i, best, fs[i])
 
 
 def test_sort1d_unshared_targets(O, ctx):
