@@ -269,8 +269,9 @@ sk_status sinkhorn_fit_gmm(sk_ctx *ctx, int64_t n, int32_t d, const float *x, in
  * n P^T x whenever P has the uniform marginals).  x: B x n; y: m values (y_shared = 1) or
  * B x m; f: B x n, g: B x m; z: m (nullable: z_j = j + 1, 1-based ranks); rank: B x n,
  * sort: B x m (either nullable).  One K15 pass (two sweeps of the other side per output, max
- * first, so no overflow for any finite (f, g)).  SK_EINVAL on bad sizes, eps <= 0 or
- * non-finite inputs; SK_EUNSUPPORTED if 2n + 3m floats exceed 200 KiB of shared memory.
+ * first, so no overflow for any finite (f, g); problems whose 2n + 3m floats exceed 200 KiB read
+ * the other side from global memory).  SK_EINVAL on bad sizes, eps <= 0 or non-finite inputs;
+ * SK_EUNSUPPORTED for n or m > 2^24 or B > 65535.
  * Asynchronous except for the input check. */
 sk_status sinkhorn_soft_rank_sort(sk_ctx *ctx, int64_t B, int64_t n, int64_t m, const float *x,
                                   const float *y, int32_t y_shared, float eps, const float *f,

@@ -1165,8 +1165,8 @@ sk_status sinkhorn_soft_rank_sort(sk_ctx *ctx, int64_t B, int64_t n, int64_t m, 
     if (B < 1 || n < 1 || m < 1 || !x || !y || !f || !g) return fail(ctx, SK_EINVAL, "bad arguments");
     if (!(eps > 0.f) || bad_scalar(eps)) return fail(ctx, SK_EINVAL, "eps must be > 0 and finite");
     if (!rank && !sort) return SK_OK;
-    if (soft_rank_sort_smem((int)n, (int)m) > 200 * 1024 || n > (1 << 20) || m > (1 << 20))
-        return fail(ctx, SK_EUNSUPPORTED, "soft rank/sort stages 2n + 3m floats in shared memory (<= 200 KiB)");
+    if (n > (1 << 24) || m > (1 << 24) || B > 65535)
+        return fail(ctx, SK_EUNSUPPORTED, "soft rank/sort: n, m <= 2^24, B <= 65535");
     Stager sg(ctx);
     const long long ycount = y_shared ? m : B * m;
     const float *dx, *dy, *df, *dg, *dz;

@@ -54,6 +54,24 @@ def test_kernel_parity_on_oracle_potentials(O, ctx, n, m, weights, zgiven):
         assert rel_inf(st_g[k].cpu().numpy(), S[k], 1e-3) <= RTOL_KERNEL, k
 
 
+@pytest.mark.parametrize("B,n,m", [(2, 8000, 12000), (1, 30000, 2000)])
+def test_large_problems_global_kernel(O, ctx, B, n, m):
+    """2n + 3m floats beyond shared memory: the global-memory K15 variant against the oracle's
+    fp64 conditional means, on arbitrary finite potentials."""
+    import paper_2206_07630_b200 as sk
+    rng = np.random.default_rng(n + m)
+    eps = 1e-2
+    x = rng.random((B, n)).astype(np.float32)
+    y = np.sort(rng.random(m)).astype(np.float32)
+    f = (rng.standard_normal((B, n)) * eps).astype(np.float32)
+    g = (rng.standard_normal((B, m)) * eps).astype(np.float32)
+    rk_g, st_g = sk.sinkhorn_soft_rank_sort(ctx, _c(x), _c(y), eps, _c(f), _c(g), y_shared=True)
+    for k in range(B):
+        rk, st = O.soft_rank_sort(x[k], y, f[k], g[k], eps)
+        assert rel_inf(rk_g[k].cpu().numpy(), rk, 1.0) <= RTOL_KERNEL, k
+        assert rel_inf(st_g[k].cpu().numpy(), st, 1e-3) <= RTOL_KERNEL, k
+
+
 def test_end_to_end_c2_batch(O, ctx):
     """A C2-shaped batch (BJ.cfg2 recipe, 16 problems of 1024): sort1d init -> solve -> K15,
     against the oracle replaying L_gpu sweeps from the same f0 (sampled problems)."""
