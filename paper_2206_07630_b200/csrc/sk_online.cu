@@ -324,7 +324,12 @@ __global__ void __launch_bounds__(kLT) k_lse_wide(LseArgs A) {
         float cm = t[0];
 #pragma unroll
         for (int j = 1; j < TQ; ++j) cm = fmaxf(cm, t[j]);
-        if (cm > M[0]) { Sx[0].x *= ex2(M[0] - cm); M[0] = cm; }
+        if (cm > M[0]) {   // (both partial sums)
+            const float sc = ex2(M[0] - cm);
+            Sx[0].x *= sc;
+            Sx[0].y *= sc;
+            M[0] = cm;
+        }
         if (M[0] != -INFINITY) {   // (a tile's first point is always real: M is finite here)
 #pragma unroll
             for (int j = 0; j < TQ; j += 2) {

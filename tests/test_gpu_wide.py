@@ -48,7 +48,8 @@ def _problem(n, m, d, eps_factor, seed=0):
 
 
 @pytest.mark.parametrize("n,m,d,tc", [(1100, 1300, 128, 1), (700, 515, 96, 1), (900, 1000, 256, 1), (1000, 777, 65, 1),
-                                      (1100, 1300, 128, 0), (600, 700, 200, 0), (513, 515, 256, 0)])
+                                      (1100, 1300, 128, 0), (600, 700, 200, 0), (513, 515, 256, 0), (1100, 2100, 128, 0),
+                                      (3000, 5000, 100, 0)])
 def test_wide_solve_parity(O, ctx, n, m, d, tc):
     """Solve to tol (count within 2 %, P1) and lockstep potentials / objective (P2): tc = 1 the
     K-chunked tensor-core pass, tc = 0 the wide FFMA pass."""
@@ -111,19 +112,23 @@ def test_wide_stored_parity(O, ctx, d):
     assert_obj_close(rep["dual_objective"], lock.E, eps)
 
 
-@pytest.mark.parametrize("mode,d", [("online", 128), ("online", 256)])
-def test_wide_sharded_bit_identical(O, ctx, mode, d):
-    """Row-sharded (emulated W = 1, 2, 4) at d > 64 on the tensor-core pass: bit-identical
-    across world sizes and with the unsharded entry; lockstep vs the oracle."""
+@pytest.mark.parametrize("mode,d,tc", [("online", 128, 1), ("online", 256, 1), ("online", 200, 0)])
+def test_wide_sharded_bit_identical(O, ctx, mode, d, tc):
+    """Row-sharded (emulated W = 1, 2, 4) at d > 64 on the tensor-core pass (tc = 1) and on the
+    wide FFMA pass with its fused premerge (tc = 0): bit-identical across world sizes and with the
+    unsharded entry; lockstep vs the oracle."""
     import paper_2206_07630_b200 as sk
     x, y, eps = _problem(6000, 2100, d, 3e-2)
     xd, yd = _cuda(x), _cuda(y)
-    outs = {W: sk.sinkhorn_solve_sharded_emulated(ctx, W, xd, yd, eps, mode=mode) for W in (1, 2, 4)}
+    c = sk.Context(0)
+    c.set_tuning("tc", tc)
+    outs = {W: sk.sinkhorn_solve_sharded_emulated(c, W, xd, yd, eps, mode=mode) for W in (1, 2, 4)}
     f1, g1, r1 = outs[1]
     for W in (2, 4):
         f, g, r = outs[W]
         assert torch.equal(f, f1) and torch.equal(g, g1) and r["iterations"] == r1["iterations"], W
-    fu, gu, ru = sk.sinkhorn_solve(ctx, xd, yd, eps, mode=mode)
+    fu, gu, ru = sk.sinkhorn_solve(c, xd, yd, eps, mode=mode)
+    c.close()
     assert ru["iterations"] == r1["iterations"] and torch.equal(fu, f1) and torch.equal(gu, g1)
     lock = O.sinkhorn(x, y, eps, tol=0, max_iter=r1["iterations"])
     assert_pair_close(f1.cpu().numpy(), g1.cpu().numpy(), lock.f, lock.g, eps)
