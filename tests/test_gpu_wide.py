@@ -229,3 +229,31 @@ def test_wide_error_contract(ctx):
         sk.sinkhorn_solve(ctx, x, x, 0.1)
     with pytest.raises(sk.SinkhornError, match="SK_EINVAL"):
         sk.sinkhorn_init_gaussian(ctx, x, x)
+
+
+def _lse_rows(Z):
+    mx = Z.max(1, keepdims=True)
+    return (mx + np.log(np.exp(Z - mx).sum(1, keepdims=True))).ravel()
+
+
+@pytest.mark.parametrize("d", [256, 160])
+def test_wide_tc_full_launch_first_sweep_sampled(O, ctx, d):
+    """K3 with K chunks at a launch size with many tiles per item (n = m = 16384, BJ.cfg5 recipe
+    at d): the first sweep from f0 = 0 — g1 on 256 sampled columns and f1 (from the returned g1)
+    on 256 sampled rows — against fp64 log-sum-exps of the exact costs."""
+    import paper_2206_07630_b200 as sk
+    p = gen.c5(n=16384, d=d, eps_factor=1e-2)
+    n = p.x.shape[0]
+    f, g, rep = sk.sinkhorn_solve(ctx, _cuda(p.x), _cuda(p.y), p.eps, tol=1e-12, max_iter=1, mode="online")
+    f, g = f.cpu().numpy().astype(np.float64), g.cpu().numpy().astype(np.float64)
+    X, Y, eps = p.x.astype(np.float64), p.y.astype(np.float64), float(p.eps)
+    rng = np.random.default_rng(d)
+    cols = rng.choice(n, 256, replace=False)
+    rows = rng.choice(n, 256, replace=False)
+    x2, y2 = (X ** 2).sum(1), (Y ** 2).sum(1)
+    g_ref = O.g_update(p.x, p.y, np.zeros(n), eps, cols=cols)
+    C2 = x2[rows, None] + y2[None, :] - 2 * X[rows] @ Y.T         # sampled rows x all columns
+    f_ref = eps * np.log(1.0 / n) - eps * _lse_rows((g[None, :] - C2) / eps)
+    scale = max(np.abs(g_ref).max(), eps)
+    assert np.abs(g[cols] - g_ref).max() <= 1e-4 * scale, np.abs(g[cols] - g_ref).max() / scale
+    assert np.abs(f[rows] - f_ref).max() <= 1e-4 * max(np.abs(f_ref).max(), eps)
