@@ -214,10 +214,22 @@ sk_status check_arrays(sk_ctx *ctx, std::initializer_list<std::pair<const float 
                        const char *what) {
     ENSURE(flag, int, B_FLAG, 4);
     CU(cudaMemsetAsync(flag, 0, sizeof(int), ctx->stream));
-    for (auto &p : finite)
-        if (p.first) { CU(launch_check_finite(p.first, p.second, flag, ctx->stream)); ctx->cnt.kernel_launches++; }
-    for (auto &p : positive)
-        if (p.first) { CU(launch_check_positive(p.first, p.second, flag, ctx->stream)); ctx->cnt.kernel_launches++; }
+    CheckList L{};
+    auto flush = [&]() -> sk_status {
+        if (L.cnt) { CU(launch_check_multi(L, flag, ctx->stream)); ctx->cnt.kernel_launches++; }
+        L = CheckList{};
+        return SK_OK;
+    };
+    auto add = [&](const float *p, long long n, int pos) -> sk_status {
+        if (!p || n <= 0) return SK_OK;
+        if (L.cnt == 8) CK(flush());
+        L.p[L.cnt] = p; L.n[L.cnt] = n; L.positive[L.cnt] = pos; ++L.cnt;
+        L.total += n;
+        return SK_OK;
+    };
+    for (auto &p : finite) CK(add(p.first, p.second, 0));
+    for (auto &p : positive) CK(add(p.first, p.second, 1));
+    CK(flush());
     CU(cudaMemcpyAsync(ctx->h_flag, flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));
     if (*ctx->h_flag) return fail(ctx, SK_EINVAL, "%s: non-finite input or non-positive weight", what);

@@ -279,6 +279,14 @@ cudaError_t launch_report_blocks(const Side &X, const float *a, float eps, DevSt
 
 // ------------------------------------------------------------ misc kernels
 cudaError_t launch_fill(float *p, long long n, float v, cudaStream_t st);
+struct CheckList {   // up to 8 arrays checked by one launch (n > 0 entries only)
+    const float *p[8];
+    long long n[8];
+    int positive[8];
+    int cnt;
+    long long total;
+};
+cudaError_t launch_check_multi(const CheckList &L, int *flag, cudaStream_t st);
 cudaError_t launch_check_finite(const float *p, long long n, int *flag, cudaStream_t st);
 cudaError_t launch_check_positive(const float *p, long long n, int *flag, cudaStream_t st);
 cudaError_t launch_gather_rows(const float *src, const int *idx, long long cnt, int d, float *dst,

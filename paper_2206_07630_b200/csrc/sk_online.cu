@@ -913,6 +913,28 @@ __global__ void k_check(const float *p, long long n, int *flag, int positive) {
     if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
 }
 
+// All of a call's input checks in one launch: entry e covers [off_e, off_e + n_e) of the
+// concatenated index range (finite, or finite and > 0).
+__global__ void k_check_multi(CheckList L, int *flag) {
+    int bad = 0;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < L.total;
+         t += (long long)gridDim.x * blockDim.x) {
+        int e = 0;
+        long long o = t;
+        while (o >= L.n[e]) { o -= L.n[e]; ++e; }
+        const float v = L.p[e][o];
+        bad |= !isfinite(v) || (L.positive[e] && !(v > 0.f));
+    }
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
+cudaError_t launch_check_multi(const CheckList &L, int *flag, cudaStream_t st) {
+    if (L.total <= 0) return cudaSuccess;
+    long long b = (L.total + 255) / 256;
+    k_check_multi<<<(int)(b > 2048 ? 2048 : b), 256, 0, st>>>(L, flag);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_check_finite(const float *p, long long n, int *flag, cudaStream_t st) {
     if (n <= 0) return cudaSuccess;
     long long b = (n + 255) / 256;
