@@ -160,13 +160,14 @@ __device__ __forceinline__ void lse_item(const LseArgs &A, int &s, int &px, int 
 
 // K2 tail: the CTA's split partials, then (fused K6a) the block premerge by the last CTA of
 // each (P tile, block)
+// (act: this thread owns output points - threadIdx.x < kLT; the others only join the barriers)
 template <int R>
 __device__ __forceinline__ void lse_store(const LseArgs &A, int s, int b, int px, const float (&M)[R],
-                                          const float2 (&Sx)[R]) {
+                                          const float2 (&Sx)[R], bool act = true) {
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         const int p = px * (kLT * R) + r * kLT + threadIdx.x;
-        if (p < A.P) A.part[(long long)s * A.P + p] = make_float2(M[r], Sx[r].x + Sx[r].y);
+        if (act && p < A.P) A.part[(long long)s * A.P + p] = make_float2(M[r], Sx[r].x + Sx[r].y);
     }
     if (A.xchg) {
         // K6a fused: the last of the block's split_q CTAs for this P tile merges their partials in
@@ -183,8 +184,8 @@ __device__ __forceinline__ void lse_store(const LseArgs &A, int s, int b, int px
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             const int p = px * (kLT * R) + r * kLT + threadIdx.x;
-            if (p < A.P) A.xchg[(long long)b * A.P + p] = premerge_point(A.part + (long long)b * A.split_q * A.P + p,
-                                                                        A.split_q, A.P);
+            if (act && p < A.P) A.xchg[(long long)b * A.P + p] = premerge_point(A.part + (long long)b * A.split_q * A.P + p,
+                                                                               A.split_q, A.P);
         }
         if (threadIdx.x == 0) *c = 0;   // (ready for the next launch)
         // the group's sub-split partials are dead: drop their L2 lines without writing them back
@@ -196,8 +197,9 @@ __device__ __forceinline__ void lse_store(const LseArgs &A, int s, int b, int px
             const float2 *rowp = A.part + ((long long)b * A.split_q + uu) * A.P;
             const unsigned long long a0 = (reinterpret_cast<unsigned long long>(rowp + p0) + 127ull) & ~127ull;
             const unsigned long long a1 = reinterpret_cast<unsigned long long>(rowp + p1) & ~127ull;
-            for (unsigned long long a = a0 + 128ull * threadIdx.x; a < a1; a += 128ull * kLT)
-                asm volatile("discard.global.L2 [%0], 128;" ::"l"(a) : "memory");
+            if (act)
+                for (unsigned long long a = a0 + 128ull * threadIdx.x; a < a1; a += 128ull * kLT)
+                    asm volatile("discard.global.L2 [%0], 128;" ::"l"(a) : "memory");
         }
     }
 }
@@ -269,26 +271,31 @@ __global__ void __launch_bounds__(kLT) k_lse(LseArgs A) {
 }
 
 // D in {128, 256} (d in (64, 256]): the output point's scaled coordinates do not fit registers;
-// they are staged once in shared memory, one column per thread ([D][kLT]: conflict-free), and each
-// 32-point reduction tile is reduced with 32 running t's per thread (broadcast float4 loads of the
-// tile's coordinates).  Always unseeded (exact running max per tile); the partials and the fused
-// premerge are K2's.  Large problems with d > 64 run on the tensor cores (K3); this kernel serves
-// small problems and the subsample initializer's extension pass.
+// they are staged once in shared memory, one column per point ([D][kLT]: conflict-free), and two
+// threads per output point (threads t and t + kLT) each reduce half of every 32-point reduction
+// tile with 16 running t's (broadcast float4 loads of the tile's coordinates); the two halves'
+// (max, sum) are merged through shared memory at the end.  Always unseeded (exact running max
+// per tile); the partials and the fused premerge are K2's.  Large problems with d > 64 run on the
+// tensor cores (K3); this kernel serves small problems with the tensor cores off, coordinates
+// outside the fp16 fold, and the subsample initializer's extension pass.
+constexpr int kWideT = 2 * kLT;
 template <int D>
-__global__ void __launch_bounds__(kLT) k_lse_wide(LseArgs A) {
-    constexpr int TQ = kWideTQ, TF = (D + 1) * TQ;
+__global__ void __launch_bounds__(kWideT) k_lse_wide(LseArgs A) {
+    constexpr int TQ = kWideTQ, TF = (D + 1) * TQ, HQ = TQ / 2;
     extern __shared__ __align__(128) float ring[];   // [kWideStages][TF], then sP [D][kLT]
     float *sP = ring + kWideStages * TF;
     __shared__ __align__(8) uint64_t full[kWideStages];
+    __shared__ float2 half_ms[kLT];
     if (A.stop && *(volatile const int *)A.stop) return;
     if (A.only_if && !*(volatile const int *)A.only_if) return;
     int s, px, b, t0, nt;
     lse_item(A, s, px, b, t0, nt);
-    {
-        const int p = px * kLT + threadIdx.x;
+    const int pl = threadIdx.x % kLT, hq = threadIdx.x / kLT;   // output point, tile half
+    for (int e = threadIdx.x; e < D * kLT; e += kWideT) {
+        const int k = e / kLT, q = e % kLT;
+        const int p = px * kLT + q;
         const int pt = p / A.Ptq, po = p % A.Ptq;
-        const float *tile = A.Ppack + (long long)pt * (D + 1) * A.Ptq;
-        for (int k = 0; k < D; ++k) sP[k * kLT + threadIdx.x] = p < A.P ? tile[k * A.Ptq + po] * A.tk : 0.f;
+        sP[e] = p < A.P ? A.Ppack[(long long)pt * (D + 1) * A.Ptq + k * A.Ptq + po] * A.tk : 0.f;
     }
     if (threadIdx.x == 0) {
         for (int i = 0; i < kWideStages; ++i) mbar_init(&full[i], 1);
@@ -299,23 +306,23 @@ __global__ void __launch_bounds__(kLT) k_lse_wide(LseArgs A) {
         }
     }
     __syncthreads();
-    float M[1] = {-INFINITY};
-    float2 Sx[1] = {make_float2(0.f, 0.f)};
+    float M = -INFINITY;
+    float2 Sx = make_float2(0.f, 0.f);
     for (int i = 0; i < nt; ++i) {
         const int st = i % kWideStages;
         mbar_wait(&full[st], (i / kWideStages) & 1);
-        const float *qt = ring + st * TF;
-        float t[TQ];
+        const float *qt = ring + st * TF + hq * HQ;
+        float t[HQ];
 #pragma unroll
-        for (int j = 0; j < TQ; j += 4) {
+        for (int j = 0; j < HQ; j += 4) {
             const float4 w = *reinterpret_cast<const float4 *>(qt + D * TQ + j);
             t[j] = w.x; t[j + 1] = w.y; t[j + 2] = w.z; t[j + 3] = w.w;
         }
 #pragma unroll 4
         for (int k = 0; k < D; ++k) {
-            const float pv = sP[k * kLT + threadIdx.x];
+            const float pv = sP[k * kLT + pl];
 #pragma unroll
-            for (int j = 0; j < TQ; j += 4) {
+            for (int j = 0; j < HQ; j += 4) {
                 const float4 c = *reinterpret_cast<const float4 *>(qt + k * TQ + j);
                 t[j] = fmaf(pv, c.x, t[j]); t[j + 1] = fmaf(pv, c.y, t[j + 1]);
                 t[j + 2] = fmaf(pv, c.z, t[j + 2]); t[j + 3] = fmaf(pv, c.w, t[j + 3]);
@@ -323,18 +330,18 @@ __global__ void __launch_bounds__(kLT) k_lse_wide(LseArgs A) {
         }
         float cm = t[0];
 #pragma unroll
-        for (int j = 1; j < TQ; ++j) cm = fmaxf(cm, t[j]);
-        if (cm > M[0]) {   // (both partial sums)
-            const float sc = ex2(M[0] - cm);
-            Sx[0].x *= sc;
-            Sx[0].y *= sc;
-            M[0] = cm;
+        for (int j = 1; j < HQ; ++j) cm = fmaxf(cm, t[j]);
+        if (cm > M) {   // (both partial sums)
+            const float sc = ex2(M - cm);
+            Sx.x *= sc;
+            Sx.y *= sc;
+            M = cm;
         }
-        if (M[0] != -INFINITY) {   // (a tile's first point is always real: M is finite here)
+        if (M != -INFINITY) {   // (a half whose points are all padding keeps M = -inf)
 #pragma unroll
-            for (int j = 0; j < TQ; j += 2) {
-                Sx[0].x += ex2(t[j] - M[0]);
-                Sx[0].y += ex2(t[j + 1] - M[0]);
+            for (int j = 0; j < HQ; j += 2) {
+                Sx.x += ex2(t[j] - M);
+                Sx.y += ex2(t[j + 1] - M);
             }
         }
         __syncthreads();  // everyone is done with stage st
@@ -344,7 +351,19 @@ __global__ void __launch_bounds__(kLT) k_lse_wide(LseArgs A) {
             bulk_g2s(ring + st * TF, A.Qpack + (long long)(t0 + i + kWideStages) * TF, TF * 4, &full[st]);
         }
     }
-    lse_store<1>(A, s, b, px, M, Sx);
+    // the point's two halves: (M, S) of the second half merged into the first
+    if (hq == 1) half_ms[pl] = make_float2(M, Sx.x + Sx.y);
+    __syncthreads();
+    float Mo[1] = {M};
+    float2 So[1] = {Sx};
+    if (hq == 0) {
+        const float2 o = half_ms[pl];
+        float S = Sx.x + Sx.y;
+        if (o.x > M) { S = (M == -INFINITY ? 0.f : S * ex2(M - o.x)) + o.y; Mo[0] = o.x; }
+        else if (o.x != -INFINITY) S += o.y * ex2(o.x - M);
+        So[0] = make_float2(S, 0.f);
+    }
+    lse_store<1>(A, s, b, px, Mo, So, hq == 0);
 }
 
 template <int D>
@@ -370,7 +389,7 @@ static cudaError_t launch_lse_wide(const LsePass &L, cudaStream_t st) {
     A.ptiles = (A.P + kLT - 1) / kLT;
     dim3 grid(A.ptiles, L.nblk * L.split_q);
     if (A.xchg) grid = dim3((unsigned)A.ptiles * L.nblk * L.split_q, 1);
-    k_lse_wide<D><<<grid, kLT, smem, st>>>(A);
+    k_lse_wide<D><<<grid, kWideT, smem, st>>>(A);
     return cudaGetLastError();
 }
 
@@ -445,7 +464,7 @@ static int occ_wide() {
     const size_t smem = wide_smem<D>();
     cudaFuncSetAttribute(k_lse_wide<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int n = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_lse_wide<D>, kLT, smem) != cudaSuccess) n = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_lse_wide<D>, kWideT, smem) != cudaSuccess) n = 1;
     return n > 0 ? n : 1;
 }
 
