@@ -270,32 +270,36 @@ __global__ void __launch_bounds__(kLT) k_lse(LseArgs A) {
     lse_store<R>(A, s, b, px, M, Sx);
 }
 
-// D in {128, 256} (d in (64, 256]): the output point's scaled coordinates do not fit registers;
-// they are staged once in shared memory, one column per point ([D][kLT]: conflict-free), and two
-// threads per output point (threads t and t + kLT) each reduce half of every 32-point reduction
-// tile with 16 running t's (broadcast float4 loads of the tile's coordinates); the two halves'
-// (max, sum) are merged through shared memory at the end.  Always unseeded (exact running max
-// per tile); the partials and the fused premerge are K2's.  Large problems with d > 64 run on the
-// tensor cores (K3); this kernel serves small problems with the tensor cores off, coordinates
-// outside the fp16 fold, and the subsample initializer's extension pass.
+// D in {128, 256} (d in (64, 256]): the output points' scaled coordinates do not fit registers;
+// they are staged once in shared memory as [D/4][kLT][4] (four consecutive coordinates of a point
+// in one 16-byte word).  Register tiles: thread (pg, qg) of 32 x 8 takes the points pg + 32 r
+// (r < 4) and the reduction points 4 qg .. 4 qg + 3 of every 32-point tile, so four coordinates
+// of four points and of four reduction points (eight 128-bit shared loads, the latter broadcast
+// across the warp) feed 64 FFMAs.  Each thread keeps a running (max, sum) per point over its
+// share of the reduction points; the eight shares of a point are merged in qg order at the end.
+// Always unseeded (exact running max per tile); the partials and the fused premerge are K2's.
+// Large problems with d > 64 run on the tensor cores (K3); this kernel serves small problems with
+// the tensor cores off, coordinates outside the fp16 fold, and the subsample initializer's
+// extension pass.
 constexpr int kWideT = 2 * kLT;
 template <int D>
 __global__ void __launch_bounds__(kWideT) k_lse_wide(LseArgs A) {
-    constexpr int TQ = kWideTQ, TF = (D + 1) * TQ, HQ = TQ / 2;
-    extern __shared__ __align__(128) float ring[];   // [kWideStages][TF], then sP [D][kLT]
+    constexpr int TQ = kWideTQ, TF = (D + 1) * TQ;
+    extern __shared__ __align__(128) float ring[];   // [kWideStages][TF], then sP [D/4][kLT][4]
     float *sP = ring + kWideStages * TF;
     __shared__ __align__(8) uint64_t full[kWideStages];
-    __shared__ float2 half_ms[kLT];
+    __shared__ float2 share[8][kLT];
     if (A.stop && *(volatile const int *)A.stop) return;
     if (A.only_if && !*(volatile const int *)A.only_if) return;
     int s, px, b, t0, nt;
     lse_item(A, s, px, b, t0, nt);
-    const int pl = threadIdx.x % kLT, hq = threadIdx.x / kLT;   // output point, tile half
+    const int pg = threadIdx.x & 31, qg = threadIdx.x >> 5;
     for (int e = threadIdx.x; e < D * kLT; e += kWideT) {
         const int k = e / kLT, q = e % kLT;
         const int p = px * kLT + q;
         const int pt = p / A.Ptq, po = p % A.Ptq;
-        sP[e] = p < A.P ? A.Ppack[(long long)pt * (D + 1) * A.Ptq + k * A.Ptq + po] * A.tk : 0.f;
+        sP[((k >> 2) * kLT + q) * 4 + (k & 3)] =
+            p < A.P ? A.Ppack[(long long)pt * (D + 1) * A.Ptq + k * A.Ptq + po] * A.tk : 0.f;
     }
     if (threadIdx.x == 0) {
         for (int i = 0; i < kWideStages; ++i) mbar_init(&full[i], 1);
@@ -306,43 +310,46 @@ __global__ void __launch_bounds__(kWideT) k_lse_wide(LseArgs A) {
         }
     }
     __syncthreads();
-    float M = -INFINITY;
-    float2 Sx = make_float2(0.f, 0.f);
+    float M[4], S[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) { M[r] = -INFINITY; S[r] = 0.f; }
+    const float4 *sP4 = reinterpret_cast<const float4 *>(sP);
     for (int i = 0; i < nt; ++i) {
         const int st = i % kWideStages;
         mbar_wait(&full[st], (i / kWideStages) & 1);
-        const float *qt = ring + st * TF + hq * HQ;
-        float t[HQ];
+        const float *qt = ring + st * TF + 4 * qg;
+        float t[4][4];
+        {
+            const float4 w = *reinterpret_cast<const float4 *>(qt + D * TQ);
 #pragma unroll
-        for (int j = 0; j < HQ; j += 4) {
-            const float4 w = *reinterpret_cast<const float4 *>(qt + D * TQ + j);
-            t[j] = w.x; t[j + 1] = w.y; t[j + 2] = w.z; t[j + 3] = w.w;
+            for (int r = 0; r < 4; ++r) { t[r][0] = w.x; t[r][1] = w.y; t[r][2] = w.z; t[r][3] = w.w; }
         }
-#pragma unroll 4
-        for (int k = 0; k < D; ++k) {
-            const float pv = sP[k * kLT + pl];
+#pragma unroll 2
+        for (int k4 = 0; k4 < D / 4; ++k4) {
+            float4 pv[4], c[4];
 #pragma unroll
-            for (int j = 0; j < HQ; j += 4) {
-                const float4 c = *reinterpret_cast<const float4 *>(qt + k * TQ + j);
-                t[j] = fmaf(pv, c.x, t[j]); t[j + 1] = fmaf(pv, c.y, t[j + 1]);
-                t[j + 2] = fmaf(pv, c.z, t[j + 2]); t[j + 3] = fmaf(pv, c.w, t[j + 3]);
+            for (int r = 0; r < 4; ++r) pv[r] = sP4[k4 * kLT + pg + 32 * r];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) c[u] = *reinterpret_cast<const float4 *>(qt + (4 * k4 + u) * TQ);
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const float pk[4] = {pv[r].x, pv[r].y, pv[r].z, pv[r].w};
+                float2 a = make_float2(t[r][0], t[r][1]), bq = make_float2(t[r][2], t[r][3]);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {   // coordinate 4 k4 + u, in k order per entry (FFMA2)
+                    const float2 pp = make_float2(pk[u], pk[u]);
+                    a = fma2(pp, make_float2(c[u].x, c[u].y), a);
+                    bq = fma2(pp, make_float2(c[u].z, c[u].w), bq);
+                }
+                t[r][0] = a.x; t[r][1] = a.y; t[r][2] = bq.x; t[r][3] = bq.y;
             }
         }
-        float cm = t[0];
 #pragma unroll
-        for (int j = 1; j < HQ; ++j) cm = fmaxf(cm, t[j]);
-        if (cm > M) {   // (both partial sums)
-            const float sc = ex2(M - cm);
-            Sx.x *= sc;
-            Sx.y *= sc;
-            M = cm;
-        }
-        if (M != -INFINITY) {   // (a half whose points are all padding keeps M = -inf)
-#pragma unroll
-            for (int j = 0; j < HQ; j += 2) {
-                Sx.x += ex2(t[j] - M);
-                Sx.y += ex2(t[j + 1] - M);
-            }
+        for (int r = 0; r < 4; ++r) {
+            const float cm = fmaxf(fmaxf(t[r][0], t[r][1]), fmaxf(t[r][2], t[r][3]));
+            if (cm > M[r]) { S[r] *= ex2(M[r] - cm); M[r] = cm; }
+            if (M[r] != -INFINITY)   // (four padding points keep M = -inf)
+                S[r] += (ex2(t[r][0] - M[r]) + ex2(t[r][1] - M[r])) + (ex2(t[r][2] - M[r]) + ex2(t[r][3] - M[r]));
         }
         __syncthreads();  // everyone is done with stage st
         if (threadIdx.x == 0 && i + kWideStages < nt) {
@@ -351,19 +358,28 @@ __global__ void __launch_bounds__(kWideT) k_lse_wide(LseArgs A) {
             bulk_g2s(ring + st * TF, A.Qpack + (long long)(t0 + i + kWideStages) * TF, TF * 4, &full[st]);
         }
     }
-    // the point's two halves: (M, S) of the second half merged into the first
-    if (hq == 1) half_ms[pl] = make_float2(M, Sx.x + Sx.y);
+    // point q's eight shares (qg = 0 .. 7) merged in qg order by thread q
+#pragma unroll
+    for (int r = 0; r < 4; ++r) share[qg][pg + 32 * r] = make_float2(M[r], S[r]);
     __syncthreads();
-    float Mo[1] = {M};
-    float2 So[1] = {Sx};
-    if (hq == 0) {
-        const float2 o = half_ms[pl];
-        float S = Sx.x + Sx.y;
-        if (o.x > M) { S = (M == -INFINITY ? 0.f : S * ex2(M - o.x)) + o.y; Mo[0] = o.x; }
-        else if (o.x != -INFINITY) S += o.y * ex2(o.x - M);
-        So[0] = make_float2(S, 0.f);
+    float Mo[1] = {-INFINITY};
+    float2 So[1] = {make_float2(0.f, 0.f)};
+    const bool act = threadIdx.x < kLT;
+    if (act) {
+        float m = -INFINITY;
+#pragma unroll
+        for (int g = 0; g < 8; ++g) m = fmaxf(m, share[g][threadIdx.x].x);
+        float sum = 0.f;
+        if (m != -INFINITY)
+#pragma unroll
+            for (int g = 0; g < 8; ++g) {
+                const float2 v = share[g][threadIdx.x];
+                if (v.x != -INFINITY) sum = fmaf(v.y, ex2(v.x - m), sum);
+            }
+        Mo[0] = m;
+        So[0] = make_float2(sum, 0.f);
     }
-    lse_store<1>(A, s, b, px, Mo, So, hq == 0);
+    lse_store<1>(A, s, b, px, Mo, So, act);
 }
 
 template <int D>
