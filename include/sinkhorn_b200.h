@@ -305,8 +305,11 @@ sk_status sinkhorn_init_sort1d(sk_ctx *ctx, int64_t B, int64_t n, int64_t m, con
  * each) until f is unchanged or max_rounds rounds (0 = n + m + 2); f^(0)_{sigma(k)} = f~_k.
  * With n = m and uniform weights this is DualSort's fixed point (sinkhorn_init_sort1d is the
  * O(n) route for that case).  x: B x n; y: m (y_shared) or B x m; a: B x n, b like y
- * (nullable = uniform, positive); pot: B x n (x side); rounds: B (nullable).  n, m <= 4096.
- * SK_EINVAL: bad sizes, NaN, non-positive weights; SK_EUNSUPPORTED: too large.  Blocks. */
+ * (nullable = uniform, positive); pot: B x n (x side); rounds: B (nullable).  n, m <= 2^20:
+ * one CTA per problem, O(n m) per round (many-tree problems — uniform weights with n, m sharing
+ * a large divisor — take many rounds); the arrays in shared memory up to ~4096 points, in a
+ * global slot beyond.  SK_EINVAL: bad sizes, NaN, non-positive weights; SK_EUNSUPPORTED: too
+ * large.  Blocks. */
 sk_status sinkhorn_init_nw1d(sk_ctx *ctx, int64_t B, int64_t n, int64_t m, const float *x,
                              const float *y, int32_t y_shared, const float *a, const float *b,
                              int32_t max_rounds, float *pot, int32_t *rounds);

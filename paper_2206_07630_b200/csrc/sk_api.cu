@@ -1262,8 +1262,8 @@ sk_status sinkhorn_init_nw1d(sk_ctx *ctx, int64_t B, int64_t n, int64_t m, const
     if (!ctx) return SK_EINVAL;
     if (B < 1 || n < 1 || m < 1 || !x || !y || !pot) return fail(ctx, SK_EINVAL, "bad arguments");
     if (max_rounds < 0) return fail(ctx, SK_EINVAL, "max_rounds >= 0 (0 = until converged)");
-    if (n > 4096 || m > 4096 || nw1d_smem_bytes((int)n, (int)m) > 220 * 1024)
-        return fail(ctx, SK_EUNSUPPORTED, "general 1D initializer: n, m <= 4096 and the problem in shared memory");
+    if (n > (1 << 20) || m > (1 << 20))
+        return fail(ctx, SK_EUNSUPPORTED, "general 1D initializer: n, m <= 2^20 (O(n m) per round on one CTA)");
     Stager sg(ctx);
     const long long ycount = (y_shared ? 1 : B) * m;
     const float *dx, *dy, *da, *db;
@@ -1281,10 +1281,21 @@ sk_status sinkhorn_init_nw1d(sk_ctx *ctx, int64_t B, int64_t n, int64_t m, const
     ENSURE(ys, float, B_YSORT, ycount);
     ENSURE(pscr, int, B_PERM, ycount + B * n);
     CU(cudaMemsetAsync(flag, 0, sizeof(int), ctx->stream));
-    CU(launch_sort_rows(dy, (int)(y_shared ? 1 : B), (int)m, m, pscr, nullptr, ys, flag, ctx->stream));
-    CU(launch_sort_rows(dx, (int)B, (int)n, n, pscr + ycount, nullptr, xs, flag, ctx->stream));
+    unsigned long long *gk = nullptr;
+    const size_t nk = std::max(sort_rows_scratch_keys((int)(y_shared ? 1 : B), (int)m), sort_rows_scratch_keys((int)B, (int)n));
+    if (nk) {
+        ENSURE(kk, unsigned long long, B_SORTKEYS, nk);
+        gk = kk;
+    }
+    char *gslot = nullptr;
+    if (nw1d_smem_bytes((int)n, (int)m) > 220 * 1024) {
+        ENSURE(gs, char, B_DUALSCR, (size_t)B * nw1d_slot_bytes((int)n, (int)m));
+        gslot = gs;
+    }
+    CU(launch_sort_rows(dy, (int)(y_shared ? 1 : B), (int)m, m, pscr, nullptr, ys, flag, ctx->stream, gk));
+    CU(launch_sort_rows(dx, (int)B, (int)n, n, pscr + ycount, nullptr, xs, flag, ctx->stream, gk));
     CU(launch_nw1d(xs, pscr + ycount, ys, pscr, y_shared ? 1 : 0, da, db, (int)B, (int)n, (int)m,
-                   max_rounds ? max_rounds : (int)(n + m + 2), dpot, drounds, ctx->stream));
+                   max_rounds ? max_rounds : (int)(n + m + 2), dpot, drounds, ctx->stream, gslot));
     ctx->cnt.kernel_launches += 3;
     CK(sg.flush());
     CU(cudaMemcpyAsync(ctx->h_flag, flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));

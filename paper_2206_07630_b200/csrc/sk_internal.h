@@ -53,7 +53,8 @@ size_t park_queue_ints(int B);
 size_t nw1d_smem_bytes(int n, int m);
 cudaError_t launch_nw1d(const float *xs, const int *xperm, const float *ys, const int *yperm, int y_shared,
                         const float *a, const float *b, int B, int n, int m, int max_rounds, float *pot, int *rounds,
-                        cudaStream_t st);
+                        cudaStream_t st, char *gscr = nullptr);
+size_t nw1d_slot_bytes(int n, int m);   // per-problem global slot beyond shared memory
 // K16 GMM fitting by EM (NEXT-3); state and partial workspace sizes in doubles
 size_t em_state_doubles(int K, int d);
 size_t em_partial_doubles(int K, int d);

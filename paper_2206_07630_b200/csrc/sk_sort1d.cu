@@ -330,9 +330,12 @@ __device__ __forceinline__ double dbl_ord(unsigned long long k) {
 __global__ void __launch_bounds__(kNW) k_nw1d(const float *__restrict__ xs_all, const int *__restrict__ xperm_all,
                                               const float *__restrict__ ys_all, const int *__restrict__ yperm_all,
                                               int y_shared, const float *__restrict__ a, const float *__restrict__ b,
-                                              int n, int m, int max_rounds, float *pot, int *rounds_out) {
-    extern __shared__ double smd[];
+                                              int n, int m, int max_rounds, float *pot, int *rounds_out,
+                                              char *gscr, long long gstride) {
+    extern __shared__ double smd_[];
     const long long pr = blockIdx.x;
+    // (gscr: problems beyond shared memory keep the same arrays in a global slot per problem)
+    double *smd = gscr ? reinterpret_cast<double *>(gscr + pr * gstride) : smd_;
     double *X = smd, *Y = X + n, *f = Y + m, *g = f + n, *fold = g + m, *base = fold + n;
     int *ei = reinterpret_cast<int *>(base + m);   // edges (n + m - 1 at most)
     int *ej = ei + (n + m);
@@ -437,13 +440,21 @@ size_t nw1d_smem_bytes(int n, int m) {
            sizeof(unsigned long long) * (size_t)(n < m ? n : m);
 }
 
+size_t nw1d_slot_bytes(int n, int m) { return (nw1d_smem_bytes(n, m) + 255) / 256 * 256; }
+
 cudaError_t launch_nw1d(const float *xs, const int *xperm, const float *ys, const int *yperm, int y_shared,
                         const float *a, const float *b, int B, int n, int m, int max_rounds, float *pot, int *rounds,
-                        cudaStream_t st) {
-    const size_t smem = nw1d_smem_bytes(n, m);
-    cudaError_t e = cudaFuncSetAttribute(k_nw1d, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                        cudaStream_t st, char *gscr) {
+    const size_t bytes = nw1d_smem_bytes(n, m);
+    if (bytes > 220 * 1024) {
+        if (!gscr) return cudaErrorInvalidValue;
+        k_nw1d<<<B, kNW, 0, st>>>(xs, xperm, ys, yperm, y_shared, a, b, n, m, max_rounds, pot, rounds, gscr,
+                                  (long long)nw1d_slot_bytes(n, m));
+        return cudaGetLastError();
+    }
+    cudaError_t e = cudaFuncSetAttribute(k_nw1d, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     if (e != cudaSuccess) return e;
-    k_nw1d<<<B, kNW, smem, st>>>(xs, xperm, ys, yperm, y_shared, a, b, n, m, max_rounds, pot, rounds);
+    k_nw1d<<<B, kNW, bytes, st>>>(xs, xperm, ys, yperm, y_shared, a, b, n, m, max_rounds, pot, rounds, nullptr, 0);
     return cudaGetLastError();
 }
 

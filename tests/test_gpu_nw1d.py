@@ -40,6 +40,24 @@ def test_nw1d_parity(O, ctx, n, m, weights):
         assert np.abs(f0[k].cpu().numpy() - fo).max() <= 1e-6 * max(1.0, np.abs(fo).max()), k
 
 
+@pytest.mark.parametrize("n,m,weights", [(5000, 7000, True), (9000, 3000, True)])
+def test_nw1d_beyond_shared_memory(O, ctx, n, m, weights):
+    """Problems whose arrays exceed shared memory keep them in a global slot (one CTA each; the
+    n = 9000 side also takes the global-memory sort)."""
+    import paper_2206_07630_b200 as sk
+    rng = np.random.default_rng(n + m)
+    B = 2
+    x = rng.random((B, n)).astype(np.float32)
+    y = np.sort(rng.random(m)).astype(np.float32)
+    a = np.stack([gen.random_weights(n, rng) for _ in range(B)]) if weights else None
+    b = gen.random_weights(m, rng) if weights else None
+    f0, rounds = sk.sinkhorn_init_nw1d(ctx, _c(x), _c(y), a=None if a is None else _c(a),
+                                       b=None if b is None else _c(b), y_shared=True)
+    for k in range(B):
+        fo = O.init_nw1d(x[k], y, None if a is None else a[k], b)
+        assert np.abs(f0[k].cpu().numpy() - fo).max() <= 1e-6 * max(1.0, np.abs(fo).max()), k
+
+
 def test_nw1d_batched_targets_and_solve(O, ctx):
     """Non-shared targets (B x m), then a solve from f0 with n != m: oracle parity, and fewer sweeps
     than the zero start (the point of the initializer)."""
