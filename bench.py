@@ -241,7 +241,7 @@ def single_spec(args):
                                   "K = 16 layout, 132 B per point, 35 MB per side) and the partials; the kernel is "
                                   "MUFU/FMA-bound, far from HBM bandwidth")
     else:
-        sp.update(p=gen.c5(eps_factor=args.eps_factor or 1e-2), init=args.init or "gaussian", mode="online",
+        sp.update(p=gen.c5(d=args.d or 64, eps_factor=args.eps_factor or 1e-2), init=args.init or "gaussian", mode="online",
                   roof="tensor", scaling="strong", kernel="k_lse_tc2 (online LSE pass, CTA-pair tcgen05 kind::f16 3-product hi/lo "
                                         "cross term with w and the row shift folded into the MMA, K3)")
         if args.ffma:   # comparison leg: the FFMA kernel at d = 64
@@ -255,7 +255,8 @@ def single_config(sp, args, world):
     c = {"workload": {"c1": "BJ.cfg1 (C1): n=m=256, d=2, Gaussian clouds, eps=0.01*mean(C)",
                       "c3": f"BJ.cfg3 (C3): n=m=16384, d=16 GMM clouds, stored-cost mode (1 GiB C), eps={p.eps:.4g}",
                       "c4": "BJ.cfg4 (C4): n=m=262144, d=3 RGB-pixel mixtures, eps=1e-2, online cost",
-                      "c5": f"BJ.cfg5 (C5): n=m=65536, d=64 embeddings, eps={p.eps:.4g}, online cost"}[name],
+                      "c5": f"BJ.cfg5 (C5): n=m=65536, d={p.d} embeddings, eps={p.eps:.4g}, online cost"
+                            + ("" if p.d == 64 else " (the BJ.cfg5 recipe at another d: not a BASELINE configuration)")}[name],
          "n": p.n, "m": p.m, "d": p.d, "init": sp["init"], "tol": p.tol, "mode": sp["mode"],
          "parallelism": f"row-sharded x{world} (NCCL allgather of block partials per sweep)" if sharded else
                         ("1 GPU" if world == 1 else f"{world} independent replicas"),
@@ -496,7 +497,8 @@ def roofline(w, cnt, steps, pk, src, step_ms, clocks=None):
                                "once for a row pass and the next column pass",
                 "bytes_per_launch": cnt["dom_bytes"] / nl, **common}
     if w.roof == "tensor":
-        flops = cnt["dom_entries"] * 3 * 2 * 64          # 3 fp16 MMAs (hi.hi, hi.lo, lo.hi), K = 64
+        kpad = 16 * ((int(w.d) + 15) // 16)   # the MMA K steps K3 issues (d = 64: 64)
+        flops = cnt["dom_entries"] * 3 * 2 * kpad        # 3 fp16 MMAs (hi.hi, hi.lo, lo.hi), K = d padded to 16
         achieved = flops / dom_s / 1e12 if dom_s > 0 else 0.0
         # K3 runs inside a long step (many back-to-back launches): the sustained figure
         # (fp16 dense = bf16 dense rate); the burst one beside it
@@ -507,7 +509,8 @@ def roofline(w, cnt, steps, pk, src, step_ms, clocks=None):
                 "peak_source": f"MEASURED_PEAKS.json bf16_tflops_sustained (kernel timed inside a long step; fp16 "
                                f"runs at the bf16 rate), {src}",
                 "frac_of_burst": achieved / float(pk["bf16_tflops"]),
-                "algorithmic": "3 x 2 x 64 fp16 tensor flops per cost entry per pass (3-product hi/lo split)",
+                "algorithmic": f"3 x 2 x {kpad} fp16 tensor flops per cost entry per pass (3-product hi/lo split, "
+                               f"K = d padded to 16)",
                 "flops_per_launch": flops / nl,
                 "mufu_frac": ent_s / ex2_peak,
                 # under the 1000 W cap the SM clock drops: the fraction of the burst rate at the
@@ -543,6 +546,8 @@ def traffic_from_profile(w):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant kernel from the
     committed `ncu --set full` capture (profiles/traffic.json, written by tools/ncu_summary.py)."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
+    if w.name == "c5" and getattr(w, "d", 64) != 64:   # (the capture is of the d = 64 launch)
+        return None
     try:
         t = json.load(open(p)).get(w.name)
         return t
@@ -741,6 +746,8 @@ def main():
     ap.add_argument("--gmm-kmeans-iters", type=int, default=10,
                     help="Lloyd steps of the fit's k-means start (R-28; sklearn's default start), 0 = start at x[idx]")
     ap.add_argument("--eps-factor", type=float, default=None)
+    ap.add_argument("--d", type=int, default=None,
+                    help="c5 only: the BJ.cfg5 recipe at another dimension (17..256; K3 in K chunks above 64)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-k14", action="store_true", help="skip the K14 microbenchmarks")
     args = ap.parse_args()
