@@ -18,6 +18,9 @@ $B --no-k14 --workload c3 --init gaussian --eps-factor 0.05 --no-cpu-baseline --
 $B --no-k14 --workload c5 --steps 5 --warmup 3 > "$O/bench_c5.json" 2> "$O/bench_c5.err"; echo "c5 rc=$?"
 $B --no-k14 --workload c5 --eps-factor 0.1 --no-cpu-baseline --steps 5 --warmup 3 > "$O/bench_c5_e1.json" 2> "$O/bench_c5_e1.err"; echo "c5e1 rc=$?"
 $B --no-k14 --workload c5 --eps-factor 0.001 --no-cpu-baseline --steps 3 --warmup 3 > "$O/bench_c5_e3.json" 2> "$O/bench_c5_e3.err"; echo "c5e3 rc=$?"
+for dd in 128 256; do
+  $B --no-k14 --workload c5 --d $dd --no-cpu-baseline --steps 3 --warmup 3 > "$O/bench_c5_d$dd.json" 2> "$O/bench_c5_d$dd.err"; echo "c5 d=$dd rc=$?"
+done
 timeout 300 python tools/shard_cost.py c4 12 > "$O/shard_cost_c4.json" 2>&1; echo "shard c4 rc=$?"
 timeout 300 python tools/shard_cost.py c5 8 > "$O/shard_cost_c5.json" 2>&1; echo "shard c5 rc=$?"
 # launch lists (cold-cache, serialised: shares only) of the default bench command and the others
