@@ -5,7 +5,7 @@
 //            two passes, fp64 per-block partials, fixed-order final sums;
 //   A = S_mu^{-1/2} (S_mu^{1/2} S_nu S_mu^{1/2})^{1/2} S_mu^{-1/2}
 //            with fp64 coupled Newton-Schulz square roots (budget R-12)
-//            in one CTA;
+//            in one CTA (d > 64: over the whole grid, one cooperative launch);
 //   f*(x) = ||x||^2 - (x - m_mu)^T A (x - m_mu) - 2 m_nu^T x   (R-4).
 // GMM (Sec. 3.3):
 //   C~_kl = ||m_k - m'_l||^2 + tr(S_k + S'_l - 2 (S_k^{1/2} S'_l S_k^{1/2})^{1/2})  (Eq. 6)
@@ -13,6 +13,8 @@
 //   f~ from the K x K entropic problem at the same eps (R-13), fp64, one CTA;
 //   f^(0)(x) = sum_k f~_k p_k(x),  p_k = alpha_k N(x; m_k, S_k) / sum_l (...)  (Eq. 7),
 //            log-domain with Cholesky factors, fp64.
+//   d > 64: the per-component / per-pair matrices in global-memory slots (L2) instead of
+//   shared memory.
 #include <cooperative_groups.h>
 
 #include <algorithm>

@@ -16,7 +16,8 @@
 // k_em_estep (fixed point chunks per CTA: responsibilities, then the sufficient statistics
 // (n_k, sum r x, sum r x x^T upper triangle) accumulated per thread-owned statistic in fp64 and
 // written as per-CTA partials), k_em_mstep (one CTA: fixed-order reduction of the partials and
-// the parameter update).  Deterministic (fixed partition and reduction order).
+// the parameter update).  Deterministic (fixed partition and reduction order).  d > 32: the
+// E-step split into per-point responsibilities and tiled x x^T statistics (the *_wide kernels).
 #include <algorithm>
 #include <cfloat>
 

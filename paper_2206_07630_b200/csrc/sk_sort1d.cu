@@ -3,7 +3,9 @@
 // K8: one CTA per row; keys packed as (order-preserving uint32 of the float,
 //     original index) in one uint64 and bitonic-sorted in shared memory — unique
 //     keys, so the result equals a stable sort with ties broken by index (R-16;
-//     -0.0 is normalised to +0.0, NaN raises a flag).  Bit-exact.
+//     -0.0 is normalised to +0.0, NaN raises a flag).  Bit-exact.  Rows longer than 8192
+//     keys: the same network over a global key array (long-distance stages one launch
+//     each, the rest on 8192-key segments in shared memory).
 // K9: for n = m, uniform weights and c(x, y) = (x - y)^2, the sorted identity
 //     matching is optimal.  DualSort (Alg. 2, read as
 //     f_i <- min_j (c_ij - c_jj + f_j), R-5) is a Bellman-Ford relaxation on the
@@ -15,6 +17,7 @@
 //        f~_k = min(0, F_k - max_{j<=k} F_j, B_k - max_{j>=k} B_j),
 //     i.e. four fp64 block scans (prefix sum, suffix sum, prefix max, suffix max).
 //     The oracle runs Alg. 2 itself to its fixed point; parity checks the two agree.
+//     (n > 4096: the four n-vectors live in workspace instead of shared memory.)
 //     Paper mode (iters = L > 0): exactly L Jacobi sweeps of Alg. 2, O(L n^2).
 //     Then f^(0)_{sigma(k)} = f~_k.
 #include <algorithm>

@@ -1,5 +1,6 @@
 // sk_tc.cu — K3: the online LSE pass with the cross term on the 5th-generation tensor
-// cores (tcgen05.mma kind::f16, fp16 operands, fp32 accumulators in TMEM), for d in (16, 64].
+// cores (tcgen05.mma kind::f16, fp16 operands, fp32 accumulators in TMEM), for d in (16, 256]
+// (d > 64 in K chunks of 64, template KC) and for every d on large problems.
 //
 // BJ.ns: "computes the -2<x,y> cross term on tensor cores only when d >= 32, using an
 // error-compensated 3xTF32/bf16x3 split".  This kernel uses the same three-product split with
