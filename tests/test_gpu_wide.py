@@ -257,3 +257,20 @@ def test_wide_tc_full_launch_first_sweep_sampled(O, ctx, d):
     scale = max(np.abs(g_ref).max(), eps)
     assert np.abs(g[cols] - g_ref).max() <= 1e-4 * scale, np.abs(g[cols] - g_ref).max() / scale
     assert np.abs(f[rows] - f_ref).max() <= 1e-4 * max(np.abs(f_ref).max(), eps)
+
+
+def test_wide_relaxation_and_adaptive(O, ctx):
+    """The accelerations on the K-chunked tensor-core path (d = 128): relaxation omega = 1.2 and
+    adaptive momentum (window 10) against the oracle's counts and lockstep pairs."""
+    import paper_2206_07630_b200 as sk
+    x, y, eps = _problem(1100, 1300, 128, 2e-2)
+    f, g, rep = sk.sinkhorn_solve(ctx, _cuda(x), _cuda(y), eps, mode="online", omega=1.2)
+    ref = O.sinkhorn(x, y, eps, omega=1.2)
+    assert rep["converged"] and abs(rep["iterations"] - ref.iterations) <= count_tol(ref.iterations)
+    lock = O.sinkhorn(x, y, eps, tol=0, max_iter=rep["iterations"], omega=1.2)
+    assert_pair_close(f.cpu().numpy(), g.cpu().numpy(), lock.f, lock.g, eps)
+    f, g, rep = sk.sinkhorn_solve(ctx, _cuda(x), _cuda(y), eps, mode="online", adaptive=10)
+    ref = O.sinkhorn_adaptive(x, y, eps, adapt_iters=10)
+    assert rep["converged"] and abs(rep["iterations"] - ref.iterations) <= count_tol(ref.iterations)
+    lock = O.sinkhorn_adaptive(x, y, eps, adapt_iters=10, tol=0, max_iter=rep["iterations"])
+    assert_pair_close(f.cpu().numpy(), g.cpu().numpy(), lock.f, lock.g, eps)
