@@ -373,7 +373,8 @@ sk_status sinkhorn_init_subsample(sk_ctx *ctx, int64_t n, int64_t m, int32_t d, 
  * chunks of 64 — and, on problems with max(n, m) > 16384, for every d; the FFMA cross term K2
  * otherwise and when the scaled coordinates leave the fp16 range; for d > 64 K2 keeps the output
  * point's coordinates in shared memory) or, with SK_COST_STORED
- * (or AUTO for 8 <= d < 32 when 4nm bytes fit), the stored-cost sweep (K4 build, K5 fused
+ * (or AUTO for 8 <= d < 32 when the 4nm bytes fit the device's free memory; AUTO falls back
+ * to the online cost otherwise), the stored-cost sweep (K4 build, K5 fused
  * single-read sweep).  Blocks until the reports are filled.
  * SK_EINVAL for d < 1 or d > 256 (and the conventions above); SK_EUNSUPPORTED for
  * n, m >= 2^31. */

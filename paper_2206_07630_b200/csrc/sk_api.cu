@@ -358,7 +358,16 @@ sk_status solve_core(sk_ctx *ctx, const Problem &P, std::vector<Slice> &slices, 
     for (auto &sl : slices) { n_max = std::max(n_max, sl.n); n_sum += sl.n; }
     const bool stored_ok = P.d >= 1 && (m % 4 == 0);
     bool stored = P.mode == SK_COST_STORED;
-    if (P.mode == SK_COST_AUTO) stored = stored_ok && P.d >= 8 && P.d < 32 && 4.0 * n_sum * m <= 8.0e9;
+    if (P.mode == SK_COST_AUTO) {
+        stored = stored_ok && P.d >= 8 && P.d < 32 && 4.0 * n_sum * m <= 8.0e9;
+        if (stored) {   // AUTO falls back to the online cost when C does not fit
+            const size_t need = sizeof(float) * (size_t)n_sum * m;
+            size_t fr = 0, tot = 0;
+            if (ctx->bufs[B_COST].cap < need &&
+                (cudaMemGetInfo(&fr, &tot) != cudaSuccess || fr + ctx->bufs[B_COST].cap < need + ((size_t)512 << 20)))
+                stored = false;
+        }
+    }
     if (stored && !stored_ok) return fail(ctx, SK_EUNSUPPORTED, "stored-cost mode needs m %% 4 == 0");
     // tensor-core cross term for d in (16, 64] (BJ.ns "only when d >= 32"; d in (16, 32] pads to
     // K = 32); sk_set_tuning("tc", 0) forces the FFMA kernel (comparison knob)
